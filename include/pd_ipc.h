@@ -1,0 +1,156 @@
+/*
+ * pd_ipc.h -- C ABI of the B200 (sm_100a) PD+IPC iteration library.
+ *
+ * What it computes: Algorithm 1 of arXiv 2312.02999 ("Efficient Incremental Potential Contact
+ * for Actuated Face Simulation"): per iteration the projective-dynamics local
+ * step (Eq. 1), the elastic gradient (Eq. 2/4, :82-98), the IPC barrier
+ * terms on the embedded surface s = W x (Eq. 3, :88-93 and :143), the contact global step
+ * (Eq. 4, :95-98) solved exactly through the contact-reduced Schur complement onto the
+ * contact vertex set S (section 3, :129-247, generalised as SURVEY.md 8(a) a7-a9), CCD
+ * (:99, :115), the backtracking line search (:116) and the update x <- x + alpha dx (:117,
+ * read with the current iterate).  Readings of silent points are SURVEY.md
+ * section 8(c) Z1-Z28 and are listed in DESIGN.md.
+ *
+ * Conventions.  All reals are float64 (meters); all indices int32, zero-based; host-side
+ * arrays are row-major AoS ("[n][3]" means n consecutive xyz triples).  Every entry point
+ * returns 0 on success or a negative PD_IPC_E_* code; no C++ exception crosses the ABI.
+ * The caller owns all inputs; the library deep-copies what it needs at create time, so the
+ * caller may free its arrays as soon as a call returns.  The handle owns every device buffer
+ * and the factorisation.  A handle is single-threaded: use one handle per process and GPU.
+ * There is no CPU fallback: every iteration runs in the library's CUDA kernels, and create
+ * fails with PD_IPC_E_CUDA when no CUDA device is present.
+ */
+#ifndef PD_IPC_H
+#define PD_IPC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* error codes; SPEC.md:48,57,101-102,115,166,285,294 name the cases */
+#define PD_IPC_OK              0
+#define PD_IPC_E_ARG          -1  /* NULL pointer, d_hat <= 0, kappa <= 0, bad sequence index */
+#define PD_IPC_E_MESH         -2  /* index out of range, det(D_m) <= 0, W row not convex /
+                                     not summing to 1 within 1e-12, degenerate surface tri */
+#define PD_IPC_E_ACTUATION    -3  /* |A - A^T|max > 1e-9 |A|max, det A <= 0, or non-finite  */
+#define PD_IPC_E_NOT_SPD      -4  /* no fixed vertices, or the Cholesky factorisation failed */
+#define PD_IPC_E_INTERSECTING -5  /* a surface distance <= 0 at create / set_positions       */
+#define PD_IPC_E_NONFINITE    -6  /* a NaN/Inf appeared during step (state = last iterate)   */
+#define PD_IPC_E_CUDA         -7  /* CUDA runtime error or no device                         */
+#define PD_IPC_E_OOM          -8  /* device or host allocation failed                        */
+#define PD_IPC_E_CAPACITY     -9  /* a contact buffer capacity was exceeded                  */
+
+/* stats flags */
+#define PD_IPC_FLAG_STALL      1  /* line search found no decrease in 31 trials: alpha = 0   */
+
+typedef struct pd_ipc pd_ipc;     /* opaque handle */
+
+/* Mesh + collision proxy ("mesh" of the north_star create call).
+ *   tets      [n_tets][4]  vertex ids; each tet must have det(D_m) > 0
+ *   fixed     [n_fixed]    Dirichlet vertex ids, n_fixed >= 1
+ *   surf_tris [n_surf_tris][3] surface-vertex ids of the embedded surface
+ *   embed_tet [n_surf_verts]   host tet of each surface vertex
+ *   embed_w   [n_surf_verts][4] barycentric weights in [0,1] summing to 1: row j of W
+ *   n_surf_tris == 0 means pure PD (no contact). */
+typedef struct {
+    int32_t n_verts, n_tets;
+    const int32_t *tets;
+    int32_t n_fixed;
+    const int32_t *fixed;
+    int32_t n_surf_verts, n_surf_tris;
+    const int32_t *surf_tris;
+    const int32_t *embed_tet;
+    const double *embed_w;
+} pd_ipc_mesh;
+
+typedef struct {
+    int32_t n_seq;            /* independent actuation sequences sharing the mesh (>= 1)      */
+    int32_t device;           /* CUDA device ordinal                                          */
+    int32_t ls_max_halvings;  /* line search halvings (default 30)                 */
+    int32_t accd_max_iters;   /* ACCD iteration cap (default 10000)                */
+    int32_t A_on_device;      /* 0: A_next is host memory; 1: device pointer [n_seq][T][9]    */
+    int32_t max_pairs;        /* capacity of candidate / active pair buffers (0 = auto)       */
+    double accd_s;            /* ACCD gap fraction s_gap (default 0.1)                        */
+} pd_ipc_options;
+
+/* Per sequence, describing the LAST iteration of the last pd_ipc_step call. */
+typedef struct {
+    int32_t iters;            /* iterations run in the last step call                         */
+    int32_t n_cand;           /* broad-phase candidates (static, d_hat-inflated)              */
+    int32_t n_active;         /* |C| = PT + EE active pairs                                   */
+    int32_t n_S;              /* n_c = |S|                                                     */
+    int32_t ls_trials;        /* line-search energy evaluations                               */
+    int32_t flags;            /* PD_IPC_FLAG_*                                                 */
+    double alpha_max;         /* alpha_m from CCD                                              */
+    double alpha;             /* accepted step                                                 */
+    double dE;                /* surrogate energy change at the accepted step                  */
+    double min_dist;          /* min active-pair distance before the step (0 if C empty)      */
+    double ms[6];             /* device time per stage over the call: IPC, G-Step, CCD, LS,
+                                 Misc, total (Table 1 categories)               */
+} pd_ipc_stats;
+
+/* Create a solver: validates the mesh, computes B_i = D_m^{-1} and w_i = det/6, assembles the
+ * scalar PD matrix L (H = L (x) I3, Eq. 2), eliminates the Dirichlet vertices, orders and
+ * factorises L_FF = L L^T on the host (supernodal Cholesky, the paper's one-time
+ * prefactorisation), uploads everything to HBM.  rest_pos [n_verts][3] is both
+ * the rest shape and the start state x_0 of every sequence.  A [n_seq][n_tets][9] row-major
+ * symmetric actuation of the first frame.  d_hat > 0 activation distance (d_0,
+ * PAPER.md:88), kappa > 0 barrier stiffness.  opt may be NULL (defaults).
+ * On failure *out is NULL and the return code says why (pd_ipc_last_error(NULL) has text). */
+int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double *A,
+                  double d_hat, double kappa, const pd_ipc_options *opt, pd_ipc **out);
+
+/* Run n_iters iterations of Algorithm 1 (a fixed count) on every sequence.
+ * A_next: NULL keeps the current actuation; otherwise [n_seq][n_tets][9] on the host, or on
+ * the device when opt.A_on_device = 1.  stats: NULL or [n_seq].  Blocks until done. */
+int pd_ipc_step(pd_ipc *h, const double *A_next, int32_t n_iters, pd_ipc_stats *stats);
+
+/* Copy positions of sequence seq (all vertices, fixed ones at rest) into out [n_verts][3]. */
+int pd_ipc_positions(const pd_ipc *h, int32_t seq, double *out);
+
+/* Free everything.  NULL is a no-op. */
+void pd_ipc_destroy(pd_ipc *h);
+
+/* Last error text: owned by h, or by a thread-local buffer when h == NULL. */
+const char *pd_ipc_last_error(const pd_ipc *h);
+
+/* ---- parity / test hooks (not on the timed path) ------------------------------------- */
+
+/* Overwrite the state of sequence seq with x [n_verts][3] (fixed vertices must be at rest).
+ * Checks that the surface is intersection-free (all active distances > 0). */
+int pd_ipc_set_positions(pd_ipc *h, int32_t seq, const double *x);
+
+/* p_i = vec_rowmajor(R_i A_i) of the last local step of sequence seq: [n_tets][9]. */
+int pd_ipc_get_projections(const pd_ipc *h, int32_t seq, double *p);
+
+/* Active set C and contact vertex set S of the last iteration of sequence seq.
+ * pt [n_pt][2] = (surface vertex j, triangle f) sorted; ee [n_ee][2] = (edge e, edge e'),
+ * e < e', sorted, edges = unique sorted surface-vertex pairs in lexicographic order;
+ * S [n_S] sorted simulation vertex ids.  Pass NULL arrays to query the sizes only. */
+int pd_ipc_get_contacts(const pd_ipc *h, int32_t seq, int32_t *pt, int32_t *n_pt,
+                        int32_t *ee, int32_t *n_ee, int32_t *S, int32_t *n_S);
+
+/* Vectors of the last iteration of sequence seq, each [n_verts][3] with zeros on fixed
+ * vertices: which = 0 g-hat (elastic + barrier gradient), 1 dx, 2 elastic gradient only. */
+int pd_ipc_get_vector(const pd_ipc *h, int32_t seq, int32_t which, double *out);
+
+/* Debug level: 1 makes step keep p, C, S, g-hat, dx of the last iteration for the hooks
+ * above (extra device->host copies; off by default and on the timed path never used). */
+int pd_ipc_set_debug(pd_ipc *h, int32_t level);
+
+/* Host-only check of the one-time setup (no GPU used): builds L_FF, orders and factorises it,
+ * and solves L_FF x = b on the host with the supernodal factor.  b, x: [n_verts] (entries on
+ * fixed vertices ignored / returned as 0).  stats (may be NULL): [supernodes, nnz(L), max
+ * supernode width, supernodal etree depth]. */
+int pd_ipc_debug_factor_solve(const pd_ipc_mesh *mesh, const double *rest_pos, const double *b,
+                              double *x, int64_t *stats);
+
+/* Library build identification (for the bench record). */
+const char *pd_ipc_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PD_IPC_H */

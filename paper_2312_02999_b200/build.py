@@ -1,0 +1,51 @@
+"""Builds libpd_ipc.so in-tree for sm_100a with nvcc (no JIT cache, no torch extension)."""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+OUT = os.path.join(HERE, "libpd_ipc.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ["-O3", "-lineinfo", "-Wno-deprecated-gpu-targets", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
+# translation units; the contact unit must not contract a*b+c into FMA (bit-exact distances)
+UNITS = [("k_elastic.cu", []), ("k_trisolve.cu", []), ("k_dense.cu", []), ("prims.cu", []),
+         ("k_contact.cu", ["-fmad=false"]), ("engine.cu", []), ("setup.cpp", [])]
+
+
+def _stale(objs):
+    if not os.path.exists(OUT):
+        return True
+    t = os.path.getmtime(OUT)
+    srcs = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
+    srcs.append(os.path.join(os.path.dirname(HERE), "include", "pd_ipc.h"))
+    srcs.append(os.path.abspath(__file__))
+    return any(os.path.getmtime(s) > t for s in srcs)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    objs = []
+    if not force and not _stale(objs):
+        return OUT
+    for src, extra in UNITS:
+        obj = os.path.join(objdir, src + ".o")
+        cmd = [NVCC] + ARCH + COMMON + extra + ["-c", os.path.join(CSRC, src), "-o", obj]
+        if src.endswith(".cpp"):
+            cmd = [NVCC] + COMMON + ["-x", "c++", "-c", os.path.join(CSRC, src), "-o", obj]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+        objs.append(obj)
+    cmd = [NVCC] + ARCH + ["-shared", "-o", OUT] + objs + ["-lcudart"]
+    subprocess.run(cmd, check=True)
+    return OUT
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose=True)
+    print(OUT)

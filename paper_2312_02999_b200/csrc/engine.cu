@@ -1,0 +1,911 @@
+// C ABI (include/pd_ipc.h) and the per-iteration orchestration of the PD+IPC hot path.
+//
+// One iteration of Algorithm 1 on the device, stream-ordered:
+//   Misc   : a1 local step (fused polar + per-corner elastic forces), a2 gather -> g_el
+//   IPC    : a3 s = W x, a4 hash broad phase, a5 narrow phase + per-pair derivatives + PSD,
+//            a6 S, g-hat = g_el + W^T grad_s B, B-check
+//   G-Step : a7/a8 one forward solve (3 gradient columns + the contact panel), a9 dense
+//            K_s = V^T V, Sigma_s = K_s^{-1}, Sigma-hat Cholesky, u, t = B u, one backward
+//            solve of w + V t  -> dx = -(H + B)^{-1} g-hat exactly
+//   CCD    : ds = W dx, swept broad phase, ACCD -> alpha_m
+//   LS     : surrogate energy differences at alpha_m 2^-h, first decrease -> alpha; x += alpha dx
+// The host reads back four counts per iteration (candidates, active pairs, |S|, swept
+// candidates) to size the launches; everything else stays on the device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/pd_ipc.h"
+#include "kernels.h"
+#include "prims.h"
+#include "setup.h"
+
+namespace pdipc {
+
+struct CudaError : std::runtime_error {
+    int code;
+    CudaError(const std::string &m, int c) : std::runtime_error(m), code(c) {}
+};
+
+#define CK(x)                                                                              \
+    do {                                                                                   \
+        cudaError_t e_ = (x);                                                              \
+        if (e_ != cudaSuccess)                                                             \
+            throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_),               \
+                            e_ == cudaErrorMemoryAllocation ? PD_IPC_E_OOM : PD_IPC_E_CUDA); \
+    } while (0)
+
+template <class T>
+struct DBuf {
+    T *p = nullptr;
+    size_t n = 0;
+    void ensure(size_t m) {
+        if (m <= n && p) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        size_t cap = std::max<size_t>(m, 1);
+        if (n) cap = std::max(cap, n + n / 2);
+        CK(cudaMalloc(&p, cap * sizeof(T)));
+        n = cap;
+    }
+    void exact(size_t m) {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        ensure(m);
+    }
+    void upload(const T *h, size_t m) {   // m may be 0 (a 1-element buffer is still allocated)
+        exact(std::max<size_t>(m, 1));
+        if (m && h) CK(cudaMemcpy(p, h, m * sizeof(T), cudaMemcpyHostToDevice));
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+static int bits_for(unsigned long long v) {   // bits to represent values < v (v >= 1)
+    int b = 0;
+    while (b < 64 && (1ull << b) < v) ++b;
+    return std::max(b, 1);
+}
+
+struct Seq {
+    DBuf<double4> x;
+    DBuf<double> A6;
+    DBuf<double> p;
+    pd_ipc_stats stats;
+    // debug copies of the last iteration
+    std::vector<int32_t> pt, ee, S;
+    std::vector<double> ghat, gel, dx, proj;
+};
+
+struct StageTimer {
+    cudaEvent_t ev[6];
+    void init() { for (auto &e : ev) CK(cudaEventCreate(&e)); }
+    void destroy() { for (auto &e : ev) cudaEventDestroy(e); }
+};
+
+}  // namespace pdipc
+
+using namespace pdipc;
+
+struct pd_ipc {
+    std::string err;
+    int device = 0, nsm = 148;
+    cudaStream_t st = nullptr;
+    pd_ipc_options opt{};
+    double dh = 0, kappa = 0, dh2 = 0;
+    HostMesh hm;
+    HostFactor hf;
+    int n = 0, T = 0, nf = 0, Ns = 0, Nt = 0, Ne = 0;
+    int capS = 0, ldv = 0;
+    int debug = 0;
+    double cell0 = 0;
+    // mesh (shared by sequences)
+    DBuf<int4> tets;
+    DBuf<double> B, w;
+    DBuf<int> inc_ptr, inc, q2v, v2q;
+    DBuf<int> Wp, Wc, WTp, WTr, tris, edges;
+    DBuf<double> Wv, WTv;
+    // factor
+    DevFactor F;
+    DBuf<int> f_c0, f_rowptr, f_rows, f_parent, f_seg_ptr, f_seg_d, f_seg_klo, f_seg_khi, f_fd, f_col2sn;
+    DBuf<long long> f_valptr;
+    DBuf<double> f_L;
+    // sequences
+    std::vector<std::unique_ptr<Seq>> seqs;
+    // work buffers
+    DBuf<double> fc, G, Z, A9stage;
+    DBuf<double4> g_el, s, ds, dx, gs;
+    DBuf<double4> blo, bhi;
+    DBuf<int> hcnt, hstart, hent;
+    unsigned hmask = 0;
+    DBuf<unsigned long long> cand, cand_tmp, akeys;
+    DBuf<int> flag, pos, ctype, atype, ids, iscr;
+    DBuf<double> cd2, ad2, grad, Hp, dist;
+    DBuf<int> mark, spos, qS;
+    DBuf<unsigned long long> rec, rec_tmp;
+    DBuf<int> bccnt, bcoff;
+    DBuf<int> ts_lo, ts_hi, ts_cnt, ts_ptr, ts_rem, ts_done, ticket;
+    DBuf<double> V, K, Bc, Sh, U, Tt, yS, rhs, u, tv, part, b0;
+    DBuf<double> dscal;     // [0]=ext cell, [1]=amin, [2..4]=ls, [5..8]=ls_out, [9..10]=scal
+    DBuf<int> dint;         // [0..3] counts, [4] info
+    StageTimer tm;
+};
+
+static thread_local std::string g_last_error;
+
+static int fail(pd_ipc *h, int code, const std::string &msg) {
+    if (h) h->err = msg;
+    g_last_error = msg;
+    return code;
+}
+
+// ------------------------------------------------------------------ helpers --------------
+static void sync_read_ints(pd_ipc *h, int *dst, const int *src, int k) {
+    CK(cudaMemcpyAsync(dst, src, sizeof(int) * k, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+}
+
+static void set_d(pd_ipc *h, double *dptr, double v) {
+    CK(cudaMemcpyAsync(dptr, &v, sizeof(double), cudaMemcpyHostToDevice, h->st));
+}
+
+// Broad phase: static (ds == nullptr, boxes inflated by infl) or swept.  Produces sorted unique
+// PT keys in cand[0..npt) and EE keys in cand[npt..npt+nee).
+static void broad_phase(pd_ipc *h, const double4 *ds, double infl, int *npt_out, int *nee_out) {
+    cudaStream_t st = h->st;
+    const int Ns = h->Ns, Nt = h->Nt, Ne = h->Ne;
+    const int nbox = Ns + Nt + Ne;
+    h->blo.ensure(nbox);
+    h->bhi.ensure(nbox);
+    double *ext = h->dscal.p + 0;
+    set_d(h, ext, h->cell0);
+    launch_boxes(h->s.p, ds, h->tris.p, h->edges.p, Ns, Nt, Ne, infl, h->blo.p, h->bhi.p, ext, st);
+    const unsigned M = h->hmask + 1;
+    int *cnt_pt = h->dint.p + 0, *cnt_ee = h->dint.p + 1;
+    for (int pass = 0; pass < 2; ++pass) {
+        int counts[2];
+        for (int kind = 0; kind < 2; ++kind) {   // 0 = PT (B = tris), 1 = EE (B = edges)
+            const int b0 = kind == 0 ? Ns : Ns + Nt, nb = kind == 0 ? Nt : Ne;
+            const int a0 = kind == 0 ? 0 : Ns + Nt, na = kind == 0 ? Ns : Ne;
+            int *hc = h->hcnt.p + (size_t)kind * (M + 1);
+            int *hs = h->hstart.p + (size_t)kind * (M + 1);
+            int *he = h->hent.p + (size_t)kind * (h->hent.n / 2);
+            CK(cudaMemsetAsync(hc, 0, sizeof(int) * (M + 1), st));
+            launch_hash_insert(h->blo.p, h->bhi.p, b0, nb, ext, h->hmask, hc, nullptr, nullptr, st);
+            scan_exclusive(hc, hs, (int)M, h->iscr.p, st);
+            CK(cudaMemsetAsync(hc, 0, sizeof(int) * (M + 1), st));
+            launch_hash_insert(h->blo.p, h->bhi.p, b0, nb, ext, h->hmask, hc, hs, he, st);
+            int *cnt = kind == 0 ? cnt_pt : cnt_ee;
+            CK(cudaMemsetAsync(cnt, 0, sizeof(int), st));
+            const int cap = (int)(h->cand.n / 2);
+            unsigned long long *out = h->cand.p + (size_t)kind * cap;
+            launch_hash_query(h->blo.p, h->bhi.p, a0, na, b0, kind == 0 ? Nt : Ne, ext, h->hmask, hs,
+                              he, kind == 0, h->tris.p, h->edges.p, out, cnt, cap, st);
+        }
+        sync_read_ints(h, counts, h->dint.p, 2);
+        const int cap = (int)(h->cand.n / 2);
+        if (counts[0] <= cap && counts[1] <= cap) {
+            // sort + unique each list, then pack PT | EE contiguously in cand_tmp -> cand
+            int res[2];
+            for (int kind = 0; kind < 2; ++kind) {
+                unsigned long long *keys = h->cand.p + (size_t)kind * cap;
+                int nk = counts[kind];
+                unsigned long long range = kind == 0 ? (unsigned long long)Ns * Nt : (unsigned long long)Ne * Ne;
+                h->cand_tmp.ensure(2 * (size_t)cap);
+                // sort scratch = this kind's half of cand_tmp (the PT result lives in the other)
+                radix_sort_u64(reinterpret_cast<uint64_t *>(keys),
+                               reinterpret_cast<uint64_t *>(h->cand_tmp.p + (size_t)kind * cap), nk,
+                               bits_for(range), h->iscr.p, st);
+                unique_sorted_u64(reinterpret_cast<uint64_t *>(keys), nk,
+                                  reinterpret_cast<uint64_t *>(h->cand_tmp.p + (size_t)kind * cap), h->flag.p,
+                                  h->pos.p, h->iscr.p, st);
+                CK(cudaMemcpyAsync(h->dint.p + 2 + kind, h->pos.p + nk, sizeof(int), cudaMemcpyDeviceToDevice, st));
+            }
+            sync_read_ints(h, res, h->dint.p + 2, 2);
+            CK(cudaMemcpyAsync(h->cand.p, h->cand_tmp.p, sizeof(unsigned long long) * res[0],
+                               cudaMemcpyDeviceToDevice, st));
+            CK(cudaMemcpyAsync(h->cand.p + res[0], h->cand_tmp.p + cap, sizeof(unsigned long long) * res[1],
+                               cudaMemcpyDeviceToDevice, st));
+            *npt_out = res[0];
+            *nee_out = res[1];
+            return;
+        }
+        // grow and redo
+        size_t need = 2 * (size_t)std::max(counts[0], counts[1]) + 1024;
+        h->cand.exact(2 * need);
+        h->cand_tmp.exact(2 * need);
+        h->flag.exact(2 * need + 1);
+        h->pos.exact(2 * need + 1);
+        h->iscr.exact(std::max(radix_scratch_ints((int)(2 * need)), scan_scratch_ints((int)(2 * need))) + 1024);
+    }
+    throw CudaError("broad phase capacity", PD_IPC_E_CAPACITY);
+}
+
+static void ensure_pair_buffers(pd_ipc *h, size_t ncand) {
+    h->flag.ensure(ncand + 1);
+    h->pos.ensure(ncand + 1);
+    h->ctype.ensure(ncand + 1);
+    h->cd2.ensure(ncand + 1);
+    h->iscr.ensure(std::max(radix_scratch_ints((int)ncand + 1), scan_scratch_ints((int)ncand + 1)) + 1024);
+}
+
+// One PD+IPC iteration of sequence q.  Returns 0 or an error code.
+static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
+    cudaStream_t st = h->st;
+    const int T = h->T, nf = h->nf, Ns = h->Ns, Nt = h->Nt, Ne = h->Ne;
+    auto &ev = h->tm.ev;
+    CK(cudaEventRecord(ev[0], st));
+    // ---------------- Misc: a1 local step + a2 gather
+    launch_local_step(h->tets.p, q.x.p, h->B.p, q.A6.p, h->w.p, T, h->fc.p,
+                      h->debug ? q.p.p : nullptr, st);
+    launch_gather_elastic(h->inc_ptr.p, h->inc.p, h->fc.p, nf, h->g_el.p, st);
+    CK(cudaEventRecord(ev[1], st));
+    // ---------------- IPC
+    int n_pt = 0, n_ee = 0, nS = 0, n_cand = 0;
+    double min_dist = 0.0;
+    int *nS_dev = h->spos.p + nf;     // exclusive scan total of the S marks
+    if (Nt > 0) {
+        launch_surface(h->Wp.p, h->Wc.p, h->Wv.p, q.x.p, Ns, h->s.p, st);
+        int cpt, cee;
+        broad_phase(h, nullptr, 0.5 * h->dh * 1.01, &cpt, &cee);
+        n_cand = cpt + cee;
+        ensure_pair_buffers(h, n_cand);
+        launch_narrow(h->cand.p, cpt, 1, Nt, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->dh2, h->flag.p,
+                      h->ctype.p, h->cd2.p, st);
+        launch_narrow(h->cand.p + cpt, cee, 0, Ne, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->dh2,
+                      h->flag.p + cpt, h->ctype.p + cpt, h->cd2.p + cpt, st);
+        // scan flags of PT and EE separately so that actives are [PT | EE], each sorted
+        scan_exclusive(h->flag.p, h->pos.p, cpt, h->iscr.p, st);
+        CK(cudaMemcpyAsync(h->dint.p + 0, h->pos.p + cpt, sizeof(int), cudaMemcpyDeviceToDevice, st));
+        int npt_h;
+        sync_read_ints(h, &npt_h, h->dint.p, 1);
+        n_pt = npt_h;
+        h->akeys.ensure(n_cand + 1);
+        h->atype.ensure(n_cand + 1);
+        h->ad2.ensure(n_cand + 1);
+        launch_compact_active(h->cand.p, cpt, h->flag.p, h->pos.p, h->ctype.p, h->cd2.p, 0, h->akeys.p,
+                              h->atype.p, h->ad2.p, st);
+        scan_exclusive(h->flag.p + cpt, h->pos.p, cee, h->iscr.p, st);
+        CK(cudaMemcpyAsync(h->dint.p + 1, h->pos.p + cee, sizeof(int), cudaMemcpyDeviceToDevice, st));
+        launch_compact_active(h->cand.p + cpt, cee, h->flag.p + cpt, h->pos.p, h->ctype.p + cpt,
+                              h->cd2.p + cpt, n_pt, h->akeys.p, h->atype.p, h->ad2.p, st);
+        int nee_h;
+        sync_read_ints(h, &nee_h, h->dint.p + 1, 1);
+        n_ee = nee_h;
+        const int na = n_pt + n_ee;
+        h->grad.ensure(12 * (size_t)na + 12);
+        h->Hp.ensure(78 * (size_t)na + 78);
+        h->dist.ensure(na + 1);
+        h->ids.ensure(4 * (size_t)na + 4);
+        launch_pair_derivs(h->akeys.p, h->atype.p, h->ad2.p, n_pt, na, h->s.p, h->tris.p, h->edges.p, Nt,
+                           Ne, h->dh, h->kappa, h->grad.p, h->Hp.p, h->dist.p, h->ids.p, st);
+        // S
+        CK(cudaMemsetAsync(h->mark.p, 0, sizeof(int) * nf, st));
+        launch_mark_S(h->ids.p, na, h->Wp.p, h->Wc.p, h->v2q.p, h->mark.p, st);
+        scan_exclusive(h->mark.p, h->spos.p, nf, h->iscr.p, st);
+        launch_compact_S(h->mark.p, h->spos.p, nf, h->qS.p, st);
+        sync_read_ints(h, &nS, nS_dev, 1);
+        if (nS > h->capS) throw CudaError("contact vertex set exceeds capacity", PD_IPC_E_CAPACITY);
+        if (na > 0) {
+            std::vector<double> dd(na);
+            CK(cudaMemcpy(dd.data(), h->dist.p, sizeof(double) * na, cudaMemcpyDeviceToHost));
+            min_dist = *std::min_element(dd.begin(), dd.end());
+            if (!(min_dist > 0)) throw CudaError("non-positive distance", PD_IPC_E_NONFINITE);
+        }
+        // gradient pull-back (deterministic: sort records by surface vertex)
+        CK(cudaMemsetAsync(h->gs.p, 0, sizeof(double4) * Ns, st));
+        if (na > 0) {
+            const int sh = bits_for(4ull * na);
+            h->rec.ensure(4 * (size_t)na + 1);
+            h->rec_tmp.ensure(4 * (size_t)na + 1);
+            h->iscr.ensure(radix_scratch_ints(4 * na) + 1024);
+            launch_grad_records(h->ids.p, na, sh, h->rec.p, st);
+            radix_sort_u64(reinterpret_cast<uint64_t *>(h->rec.p), reinterpret_cast<uint64_t *>(h->rec_tmp.p),
+                           4 * na, sh + bits_for(Ns), h->iscr.p, st);
+            launch_grad_reduce(h->rec.p, 4 * na, sh, h->grad.p, h->gs.p, st);
+        }
+        launch_grad_pullback(h->g_el.p, h->WTp.p, h->WTr.p, h->WTv.p, h->gs.p, nf, h->G.p, st);
+        // B-check records
+        if (nS > 0) {
+            h->bccnt.ensure(na + 1);
+            h->bcoff.ensure(na + 1);
+            launch_bc_count(h->ids.p, na, h->Wp.p, h->Wc.p, h->v2q.p, h->bccnt.p, st);
+            scan_exclusive(h->bccnt.p, h->bcoff.p, na, h->iscr.p, st);
+            int nrec;
+            sync_read_ints(h, &nrec, h->bcoff.p + na, 1);
+            const int sh = bits_for(256ull * na);
+            h->rec.ensure(nrec + 1);
+            h->rec_tmp.ensure(nrec + 1);
+            h->iscr.ensure(radix_scratch_ints(nrec) + 1024);
+            launch_bc_records(h->ids.p, na, h->Wp.p, h->Wc.p, h->v2q.p, h->spos.p, nS, sh, h->bcoff.p,
+                              h->rec.p, st);
+            radix_sort_u64(reinterpret_cast<uint64_t *>(h->rec.p), reinterpret_cast<uint64_t *>(h->rec_tmp.p),
+                           nrec, sh + bits_for((unsigned long long)nS * nS), h->iscr.p, st);
+            const int ldb = 3 * h->capS;
+            launch_zero_square(h->Bc.p, ldb, 3 * nS, st);
+            launch_bc_reduce(h->rec.p, nrec, sh, nS, h->ids.p, h->Wp.p, h->Wv.p, h->Hp.p, h->Bc.p, ldb, st);
+        }
+    } else {
+        CK(cudaMemsetAsync(nS_dev, 0, sizeof(int), st));
+        launch_grad_pullback(h->g_el.p, h->WTp.p, h->WTr.p, h->WTv.p, nullptr, nf, h->G.p, st);
+    }
+    if (h->debug) {
+        std::vector<double> G4(4 * (size_t)nf), g4(4 * (size_t)nf);
+        CK(cudaMemcpyAsync(G4.data(), h->G.p, sizeof(double) * 4 * nf, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(g4.data(), h->g_el.p, sizeof(double) * 4 * nf, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        q.ghat.assign(3 * (size_t)h->n, 0.0);
+        q.gel.assign(3 * (size_t)h->n, 0.0);
+        for (int k = 0; k < nf; ++k)
+            for (int a = 0; a < 3; ++a) {
+                q.ghat[3 * (size_t)h->hm.q2v[k] + a] = G4[4 * (size_t)k + a];
+                q.gel[3 * (size_t)h->hm.q2v[k] + a] = g4[4 * (size_t)k + a];
+            }
+        int na = n_pt + n_ee;
+        std::vector<unsigned long long> ak(na);
+        if (na) CK(cudaMemcpy(ak.data(), h->akeys.p, sizeof(unsigned long long) * na, cudaMemcpyDeviceToHost));
+        q.pt.clear();
+        q.ee.clear();
+        for (int k = 0; k < na; ++k) {
+            unsigned long long nb = k < n_pt ? (unsigned long long)Nt : (unsigned long long)Ne;
+            auto &v = k < n_pt ? q.pt : q.ee;
+            v.push_back((int32_t)(ak[k] / nb));
+            v.push_back((int32_t)(ak[k] % nb));
+        }
+        std::vector<int> qs(nS);
+        if (nS) CK(cudaMemcpy(qs.data(), h->qS.p, sizeof(int) * nS, cudaMemcpyDeviceToHost));
+        q.S.clear();
+        for (int v : qs) q.S.push_back(h->hm.q2v[v]);
+        std::sort(q.S.begin(), q.S.end());
+    }
+    CK(cudaEventRecord(ev[2], st));
+    // ---------------- G-Step
+    const DevFactor &F = h->F;
+    CK(cudaMemsetAsync(h->ticket.p, 0, 2 * sizeof(int), st));
+    launch_ts_items(F.sn_c0, F.sn_fd, F.sn_parent, F.nsn, h->qS.p, nS_dev, h->ts_lo.p, h->ts_hi.p,
+                    h->ts_cnt.p, h->ts_rem.p, st);
+    scan_exclusive(h->ts_cnt.p, h->ts_ptr.p, F.nsn, h->iscr.p, st);
+    launch_forward_solve(F, h->ts_lo.p, h->ts_hi.p, h->ts_ptr.p, h->qS.p, h->ts_rem.p, h->ticket.p, h->G.p,
+                         h->V.p, h->ldv, h->nsm, st);
+    if (nS > 0) {
+        const int ldk = h->capS, m3 = 3 * nS, ldb = 3 * h->capS;
+        launch_panel_yS(h->qS.p, nS_dev, nS, F, h->V.p, h->ldv, h->G.p, h->yS.p, st);
+        launch_panel_syrk(F, h->ts_lo.p, h->ts_hi.p, h->V.p, h->ldv, nS_dev, nS, h->K.p, ldk, st);
+        int *info = h->dint.p + 4;
+        CK(cudaMemsetAsync(info, 0, sizeof(int), st));
+        dense_spd_inverse(h->K.p, ldk, nS, h->U.p, h->Tt.p, info, st);
+        dense_negate(h->K.p, ldk, nS, st);                    // K <- Sigma_s = K_s^{-1}
+        launch_assemble_sigma_hat(h->K.p, ldk, h->Bc.p, ldb, h->Sh.p, ldb, nS, st);
+        dense_potrf(h->Sh.p, ldb, m3, h->Tt.p, info, st);
+        launch_kron_matvec(h->K.p, ldk, nS, h->yS.p, h->rhs.p, st);
+        launch_chol_solve(h->Sh.p, ldb, m3, h->rhs.p, h->u.p, st);
+        launch_matvec(h->Bc.p, ldb, m3, h->u.p, h->tv.p, st);
+        launch_panel_correct(F, h->ts_lo.p, h->ts_hi.p, h->V.p, h->ldv, h->G.p, h->tv.p, h->Z.p, st);
+    } else {
+        CK(cudaMemcpyAsync(h->Z.p, h->G.p, sizeof(double) * 4 * nf, cudaMemcpyDeviceToDevice, st));
+    }
+    launch_backward_solve(F, h->ts_done.p, h->ticket.p, h->Z.p, h->nsm, st);
+    CK(cudaMemsetAsync(h->dx.p, 0, sizeof(double4) * h->n, st));
+    launch_scatter_dx(h->Z.p, h->q2v.p, nf, h->dx.p, st);
+    CK(cudaEventRecord(ev[3], st));
+    // ---------------- CCD
+    double *amin = h->dscal.p + 1;
+    double *ls = h->dscal.p + 2, *ls_out = h->dscal.p + 5, *scal = h->dscal.p + 9;
+    set_d(h, amin, 1.0);
+    int spt = 0, see = 0;
+    if (Nt > 0) {
+        launch_surface(h->Wp.p, h->Wc.p, h->Wv.p, h->dx.p, Ns, h->ds.p, st);
+        broad_phase(h, h->ds.p, h->dh, &spt, &see);
+        launch_accd(h->cand.p, spt, 1, Nt, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->ds.p, h->opt.accd_s,
+                    h->opt.accd_max_iters, amin, st);
+        launch_accd(h->cand.p + spt, see, 0, Ne, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->ds.p,
+                    h->opt.accd_s, h->opt.accd_max_iters, amin, st);
+    }
+    CK(cudaEventRecord(ev[4], st));
+    // ---------------- LS
+    {
+        int nb1 = gdx_partials(h->g_el.p, h->dx.p, h->q2v.p, nf, h->part.p, st);
+        sum_partials(h->part.p, nb1, scal + 0, st);
+        int nb2 = quad_partials(h->tets.p, h->dx.p, h->B.p, h->w.p, T, h->part.p + nb1, st);
+        sum_partials(h->part.p + nb1, nb2, scal + 1, st);
+        CK(cudaMemcpyAsync(ls, amin, sizeof(double), cudaMemcpyDeviceToDevice, st));
+        double zeros[2] = {0.0, 0.0};
+        CK(cudaMemcpyAsync(ls + 1, zeros, 2 * sizeof(double), cudaMemcpyHostToDevice, st));
+        const int nsw = spt + see;
+        h->b0.ensure(nsw + 1);
+        const int nbp = (spt + 255) / 256, nbe = (see + 255) / 256;
+        const int pld = nbp + nbe + 1;
+        h->part.ensure(std::max<size_t>(8 * (size_t)pld, 2 * (size_t)std::max(nb1, nb2) + 16));
+        if (nsw > 0) {
+            launch_ls_b0(h->cand.p, spt, 1, Nt, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->dh, h->b0.p, st);
+            launch_ls_b0(h->cand.p + spt, see, 0, Ne, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->dh,
+                         h->b0.p + spt, st);
+        }
+        const int hmax = h->opt.ls_max_halvings;
+        for (int h0 = 0; h0 <= hmax; h0 += 8) {
+            launch_ls_trials(h->cand.p, spt, 1, Nt, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->ds.p, h->dh,
+                             h->b0.p, ls, h0, h->part.p, pld, st);
+            launch_ls_trials(h->cand.p + spt, see, 0, Ne, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->ds.p,
+                             h->dh, h->b0.p + spt, ls, h0, h->part.p + nbp, pld, st);
+            launch_ls_decide(h->part.p, pld, nbp + nbe, scal, h->kappa, h0, hmax, ls, ls_out, st);
+        }
+        launch_update(q.x.p, h->dx.p, h->q2v.p, nf, ls_out, st);
+    }
+    CK(cudaEventRecord(ev[5], st));
+    // ---------------- stats
+    double sc[11];
+    CK(cudaMemcpyAsync(sc, h->dscal.p, sizeof(sc), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    int info_h = 0, fault_h = 0;
+    CK(cudaMemcpy(&info_h, h->dint.p + 4, sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&fault_h, h->ticket.p + 1, sizeof(int), cudaMemcpyDeviceToHost));
+    if (fault_h) throw CudaError("triangular solve dependency wait timed out", PD_IPC_E_CUDA);
+    if (info_h) throw CudaError("dense Cholesky: matrix not SPD", PD_IPC_E_NOT_SPD);
+    for (int k = 0; k < 5; ++k) {
+        float f;
+        CK(cudaEventElapsedTime(&f, ev[k], ev[k + 1]));
+        ms[k == 0 ? 4 : k - 1] += f;       // Misc, IPC, G, CCD, LS
+    }
+    float tot;
+    CK(cudaEventElapsedTime(&tot, ev[0], ev[5]));
+    ms[5] += tot;
+    pd_ipc_stats &S = q.stats;
+    S.n_cand = n_cand;
+    S.n_active = n_pt + n_ee;
+    S.n_S = nS;
+    S.alpha_max = sc[2];
+    S.alpha = sc[5];
+    S.ls_trials = (int)sc[6];
+    S.dE = sc[7];
+    S.flags = (int)sc[8];
+    S.min_dist = min_dist;
+    if (!std::isfinite(sc[5]) || !std::isfinite(sc[9]) || !std::isfinite(sc[10]))
+        throw CudaError("non-finite value in step", PD_IPC_E_NONFINITE);
+    if (h->debug) {
+        std::vector<double4> d4(h->n);
+        CK(cudaMemcpy(d4.data(), h->dx.p, sizeof(double4) * h->n, cudaMemcpyDeviceToHost));
+        q.dx.resize(3 * (size_t)h->n);
+        for (int v = 0; v < h->n; ++v) {
+            q.dx[3 * v] = d4[v].x;
+            q.dx[3 * v + 1] = d4[v].y;
+            q.dx[3 * v + 2] = d4[v].z;
+        }
+    }
+    (void)last;
+}
+
+// ------------------------------------------------------------------ ABI -------------------
+static int validate_actuation(const double *A, size_t nmat, std::string &err) {
+    for (size_t t = 0; t < nmat; ++t) {
+        const double *a = A + 9 * t;
+        double mx = 0, asym = 0;
+        for (int k = 0; k < 9; ++k) {
+            if (!std::isfinite(a[k])) { err = "non-finite actuation"; return PD_IPC_E_ACTUATION; }
+            mx = std::max(mx, std::fabs(a[k]));
+        }
+        asym = std::max({std::fabs(a[1] - a[3]), std::fabs(a[2] - a[6]), std::fabs(a[5] - a[7])});
+        if (asym > 1e-9 * mx) { err = "actuation not symmetric"; return PD_IPC_E_ACTUATION; }
+        double det = a[0] * (a[4] * a[8] - a[5] * a[7]) - a[1] * (a[3] * a[8] - a[5] * a[6]) +
+                     a[2] * (a[3] * a[7] - a[4] * a[6]);
+        if (!(det > 0)) { err = "actuation det <= 0"; return PD_IPC_E_ACTUATION; }
+    }
+    return 0;
+}
+
+static void upload_actuation(pd_ipc *h, const double *A, bool on_device) {
+    const int T = h->T;
+    for (size_t sq = 0; sq < h->seqs.size(); ++sq) {
+        const double *src = A + 9 * (size_t)T * sq;
+        const double *dsrc = src;
+        if (!on_device) {
+            h->A9stage.ensure(9 * (size_t)T);
+            CK(cudaMemcpyAsync(h->A9stage.p, src, sizeof(double) * 9 * T, cudaMemcpyHostToDevice, h->st));
+            dsrc = h->A9stage.p;
+        }
+        launch_ingest_actuation(dsrc, h->seqs[sq]->A6.p, T, h->st);
+    }
+}
+
+extern "C" {
+
+int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double *A, double d_hat,
+                  double kappa, const pd_ipc_options *opt, pd_ipc **out) {
+    if (out) *out = nullptr;
+    if (!mesh || !rest_pos || !A || !out) return fail(nullptr, PD_IPC_E_ARG, "NULL argument");
+    if (!(d_hat > 0) || !(kappa > 0)) return fail(nullptr, PD_IPC_E_ARG, "d_hat and kappa must be > 0");
+    std::unique_ptr<pd_ipc> h(new pd_ipc());
+    pd_ipc_options o{};
+    o.n_seq = 1;
+    o.device = 0;
+    o.ls_max_halvings = 30;
+    o.accd_max_iters = 10000;
+    o.A_on_device = 0;
+    o.max_pairs = 0;
+    o.accd_s = 0.1;
+    if (opt) {
+        o = *opt;
+        if (o.n_seq <= 0) o.n_seq = 1;
+        if (o.ls_max_halvings <= 0) o.ls_max_halvings = 30;
+        if (o.accd_max_iters <= 0) o.accd_max_iters = 10000;
+        if (!(o.accd_s > 0 && o.accd_s < 1)) o.accd_s = 0.1;
+    }
+    h->opt = o;
+    h->dh = d_hat;
+    h->kappa = kappa;
+    h->dh2 = d_hat * d_hat;
+    std::string err;
+    int rc = build_host_mesh(mesh->n_verts, mesh->n_tets, mesh->tets, mesh->n_fixed, mesh->fixed,
+                             rest_pos, mesh->n_surf_verts, mesh->n_surf_tris, mesh->surf_tris,
+                             mesh->embed_tet, mesh->embed_w, h->hm, err);
+    if (rc) return fail(nullptr, rc, err);
+    rc = validate_actuation(A, (size_t)o.n_seq * mesh->n_tets, err);
+    if (rc) return fail(nullptr, rc, err);
+    rc = factorize(h->hm, h->hf, err);
+    if (rc) return fail(nullptr, rc, err);
+    try {
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0)
+            return fail(nullptr, PD_IPC_E_CUDA, "no CUDA device");
+        if (o.device < 0 || o.device >= ndev) return fail(nullptr, PD_IPC_E_ARG, "bad device ordinal");
+        CK(cudaSetDevice(o.device));
+        h->device = o.device;
+        CK(cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, o.device));
+        CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+        h->tm.init();
+        dense_init();
+        contact_init();
+        HostMesh &m = h->hm;
+        HostFactor &f = h->hf;
+        h->n = m.n;
+        h->T = m.T;
+        h->nf = m.nf;
+        h->Ns = m.Ns;
+        h->Nt = m.Nt;
+        h->Ne = m.Ne;
+        // mesh SoA
+        {
+            std::vector<double> Bs(9 * (size_t)m.T);
+            for (int t = 0; t < m.T; ++t)
+                for (int k = 0; k < 9; ++k) Bs[(size_t)k * m.T + t] = m.B[9 * (size_t)t + k];
+            h->B.upload(Bs.data(), Bs.size());
+            h->w.upload(m.w.data(), m.w.size());
+            h->tets.upload(reinterpret_cast<const int4 *>(m.tets.data()), m.T);
+        }
+        h->inc_ptr.upload(m.inc_ptr.data(), m.inc_ptr.size());
+        h->inc.upload(m.inc.data(), std::max<size_t>(m.inc.size(), 1));
+        h->q2v.upload(m.q2v.data(), m.q2v.size());
+        h->v2q.upload(m.v2q.data(), m.v2q.size());
+        h->Wp.upload(m.W_ptr.data(), m.W_ptr.size());
+        h->Wc.upload(m.W_col.data(), std::max<size_t>(m.W_col.size(), 1));
+        h->Wv.upload(m.W_val.data(), std::max<size_t>(m.W_val.size(), 1));
+        h->WTp.upload(m.WT_ptr.data(), m.WT_ptr.size());
+        h->WTr.upload(m.WT_row.data(), std::max<size_t>(m.WT_row.size(), 1));
+        h->WTv.upload(m.WT_val.data(), std::max<size_t>(m.WT_val.size(), 1));
+        h->tris.upload(m.tris.data(), std::max<size_t>(m.tris.size(), 1));
+        h->edges.upload(m.edges.data(), std::max<size_t>(m.edges.size(), 1));
+        // factor
+        h->f_c0.upload(f.sn_c0.data(), f.sn_c0.size());
+        h->f_rowptr.upload(f.sn_rowptr.data(), f.sn_rowptr.size());
+        h->f_rows.upload(f.sn_rows.data(), f.sn_rows.size());
+        h->f_parent.upload(f.sn_parent.data(), f.sn_parent.size());
+        h->f_seg_ptr.upload(f.seg_ptr.data(), f.seg_ptr.size());
+        h->f_seg_d.upload(f.seg_d.data(), std::max<size_t>(f.seg_d.size(), 1));
+        h->f_seg_klo.upload(f.seg_klo.data(), std::max<size_t>(f.seg_klo.size(), 1));
+        h->f_seg_khi.upload(f.seg_khi.data(), std::max<size_t>(f.seg_khi.size(), 1));
+        h->f_fd.upload(f.sn_fd.data(), f.sn_fd.size());
+        h->f_col2sn.upload(f.col2sn.data(), f.col2sn.size());
+        {
+            std::vector<long long> vp(f.sn_valptr.begin(), f.sn_valptr.end());
+            h->f_valptr.upload(vp.data(), vp.size());
+        }
+        h->f_L.upload(f.vals.data(), f.vals.size());
+        DevFactor &F = h->F;
+        F.nf = f.nf; F.nsn = f.nsn;
+        F.sn_c0 = h->f_c0.p; F.sn_rowptr = h->f_rowptr.p; F.sn_rows = h->f_rows.p; F.sn_parent = h->f_parent.p;
+        F.sn_valptr = h->f_valptr.p; F.L = h->f_L.p;
+        F.seg_ptr = h->f_seg_ptr.p; F.seg_d = h->f_seg_d.p; F.seg_klo = h->f_seg_klo.p; F.seg_khi = h->f_seg_khi.p;
+        F.sn_fd = h->f_fd.p; F.col2sn = h->f_col2sn.p;
+        // contact capacity: S is a subset of the free vertices in the W support (n2)
+        {
+            std::vector<char> sup(m.nf, 0);
+            int n2 = 0;
+            for (size_t k = 0; k < m.W_col.size(); ++k) {
+                int qv = m.v2q[m.W_col[k]];
+                if (qv >= 0 && !sup[qv]) { sup[qv] = 1; ++n2; }
+            }
+            h->capS = std::max(1, std::min(n2, 6144));
+        }
+        h->ldv = ((h->capS + 31) / 32) * 32;
+        const int nf = m.nf;
+        // sequences
+        for (int sq = 0; sq < o.n_seq; ++sq) {
+            std::unique_ptr<Seq> s(new Seq());
+            std::vector<double4> x4(m.n);
+            for (int v = 0; v < m.n; ++v) x4[v] = make_double4(rest_pos[3 * v], rest_pos[3 * v + 1], rest_pos[3 * v + 2], 0.0);
+            s->x.upload(x4.data(), x4.size());
+            s->A6.exact(6 * (size_t)m.T);
+            s->p.exact(9 * (size_t)m.T);
+            std::memset(&s->stats, 0, sizeof(s->stats));
+            h->seqs.push_back(std::move(s));
+        }
+        // work buffers
+        h->fc.exact(12 * (size_t)m.T);
+        h->g_el.exact(nf);
+        h->G.exact(4 * (size_t)nf);
+        h->Z.exact(4 * (size_t)nf);
+        h->dx.exact(m.n);
+        h->s.exact(std::max(1, m.Ns));
+        h->ds.exact(std::max(1, m.Ns));
+        h->gs.exact(std::max(1, m.Ns));
+        h->mark.exact(nf + 1);
+        h->spos.exact(nf + 1);
+        h->qS.exact(nf + 1);
+        h->ts_lo.exact(f.nsn);
+        h->ts_hi.exact(f.nsn);
+        h->ts_cnt.exact(f.nsn + 1);
+        h->ts_ptr.exact(f.nsn + 1);
+        h->ts_rem.exact(f.nsn);
+        h->ts_done.exact(f.nsn);
+        h->ticket.exact(4);
+        h->dscal.exact(16);
+        h->dint.exact(16);
+        const size_t cap_cand = o.max_pairs > 0 ? (size_t)o.max_pairs
+                                                : std::max<size_t>(1 << 16, 16 * (size_t)(m.Ns + m.Ne));
+        h->cand.exact(2 * cap_cand);
+        h->cand_tmp.exact(2 * cap_cand);
+        ensure_pair_buffers(h.get(), 2 * cap_cand);
+        h->iscr.ensure(std::max({radix_scratch_ints((int)(2 * cap_cand)), scan_scratch_ints(nf + 1),
+                                 scan_scratch_ints(f.nsn + 1)}) + 1024);
+        {
+            unsigned M = 1024;
+            while (M < 16u * (unsigned)std::max(m.Nt, m.Ne)) M <<= 1;
+            h->hmask = M - 1;
+            h->hcnt.exact(2 * (size_t)(M + 1));
+            h->hstart.exact(2 * (size_t)(M + 1));
+            h->hent.exact(2 * 8 * (size_t)std::max(1, std::max(m.Nt, m.Ne)));
+            h->iscr.ensure(scan_scratch_ints(M) + 1024);
+        }
+        h->cell0 = std::max(m.mean_edge, 2.0 * d_hat);
+        if (m.Nt > 0) {
+            const int cS = h->capS;
+            h->V.exact((size_t)nf * h->ldv);
+            h->K.exact((size_t)cS * cS);
+            h->Bc.exact((size_t)9 * cS * cS);
+            h->Sh.exact((size_t)9 * cS * cS);
+            h->U.exact((size_t)(cS + 64) * 64);
+            h->yS.exact(3 * (size_t)cS);
+            h->rhs.exact(3 * (size_t)cS);
+            h->u.exact(3 * (size_t)cS);
+            h->tv.exact(3 * (size_t)cS);
+        } else {
+            h->V.exact(32);
+        }
+        h->Tt.exact(64 * 64);
+        h->part.exact(std::max<size_t>(4096, (size_t)(m.T + 255) / 256 + (nf + 255) / 256 + 64));
+        upload_actuation(h.get(), A, false);
+        CK(cudaStreamSynchronize(h->st));
+    } catch (const CudaError &e) {
+        int code = e.code;
+        std::string msg = e.what();
+        if (h->st) cudaStreamDestroy(h->st);
+        return fail(nullptr, code, msg);
+    }
+    *out = h.release();
+    return PD_IPC_OK;
+}
+
+int pd_ipc_step(pd_ipc *h, const double *A_next, int32_t n_iters, pd_ipc_stats *stats) {
+    if (!h) return fail(nullptr, PD_IPC_E_ARG, "NULL handle");
+    if (n_iters < 0) return fail(h, PD_IPC_E_ARG, "n_iters < 0");
+    try {
+        CK(cudaSetDevice(h->device));
+        if (A_next) {
+            if (!h->opt.A_on_device) {
+                std::string err;
+                int rc = validate_actuation(A_next, h->seqs.size() * (size_t)h->T, err);
+                if (rc) return fail(h, rc, err);
+            }
+            upload_actuation(h, A_next, h->opt.A_on_device != 0);
+        }
+        for (auto &sq : h->seqs) {
+            double ms[6] = {0, 0, 0, 0, 0, 0};
+            for (int it = 0; it < n_iters; ++it) iterate(h, *sq, it == n_iters - 1, ms);
+            sq->stats.iters = n_iters;
+            for (int k = 0; k < 6; ++k) sq->stats.ms[k] = ms[k];
+        }
+        if (stats)
+            for (size_t sq = 0; sq < h->seqs.size(); ++sq) stats[sq] = h->seqs[sq]->stats;
+    } catch (const CudaError &e) {
+        return fail(h, e.code, e.what());
+    }
+    return PD_IPC_OK;
+}
+
+int pd_ipc_positions(const pd_ipc *h, int32_t seq, double *out) {
+    if (!h || !out) return fail(nullptr, PD_IPC_E_ARG, "NULL argument");
+    if (seq < 0 || seq >= (int)h->seqs.size()) return fail(const_cast<pd_ipc *>(h), PD_IPC_E_ARG, "bad sequence");
+    try {
+        std::vector<double4> x4(h->n);
+        CK(cudaMemcpy(x4.data(), h->seqs[seq]->x.p, sizeof(double4) * h->n, cudaMemcpyDeviceToHost));
+        for (int v = 0; v < h->n; ++v) {
+            out[3 * v] = x4[v].x;
+            out[3 * v + 1] = x4[v].y;
+            out[3 * v + 2] = x4[v].z;
+        }
+    } catch (const CudaError &e) {
+        return fail(const_cast<pd_ipc *>(h), e.code, e.what());
+    }
+    return PD_IPC_OK;
+}
+
+void pd_ipc_destroy(pd_ipc *h) {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    cudaDeviceSynchronize();
+    // DBuf members free in their own scope via release; explicit for clarity
+    h->tm.destroy();
+    if (h->st) cudaStreamDestroy(h->st);
+    auto rel = [](auto &b) { b.release(); };
+    rel(h->tets); rel(h->B); rel(h->w); rel(h->inc_ptr); rel(h->inc); rel(h->q2v); rel(h->v2q);
+    rel(h->Wp); rel(h->Wc); rel(h->WTp); rel(h->WTr); rel(h->tris); rel(h->edges); rel(h->Wv); rel(h->WTv);
+    rel(h->f_c0); rel(h->f_rowptr); rel(h->f_rows); rel(h->f_parent); rel(h->f_seg_ptr); rel(h->f_seg_d);
+    rel(h->f_seg_klo); rel(h->f_seg_khi); rel(h->f_fd); rel(h->f_col2sn); rel(h->f_valptr); rel(h->f_L);
+    for (auto &s : h->seqs) { rel(s->x); rel(s->A6); rel(s->p); }
+    rel(h->fc); rel(h->G); rel(h->Z); rel(h->A9stage); rel(h->g_el); rel(h->s); rel(h->ds); rel(h->dx);
+    rel(h->gs); rel(h->blo); rel(h->bhi); rel(h->hcnt); rel(h->hstart); rel(h->hent); rel(h->cand);
+    rel(h->cand_tmp); rel(h->akeys); rel(h->flag); rel(h->pos); rel(h->ctype); rel(h->atype); rel(h->ids);
+    rel(h->iscr); rel(h->cd2); rel(h->ad2); rel(h->grad); rel(h->Hp); rel(h->dist); rel(h->mark);
+    rel(h->spos); rel(h->qS); rel(h->rec); rel(h->rec_tmp); rel(h->bccnt); rel(h->bcoff); rel(h->ts_lo);
+    rel(h->ts_hi); rel(h->ts_cnt); rel(h->ts_ptr); rel(h->ts_rem); rel(h->ts_done); rel(h->ticket);
+    rel(h->V); rel(h->K); rel(h->Bc); rel(h->Sh); rel(h->U); rel(h->Tt); rel(h->yS); rel(h->rhs);
+    rel(h->u); rel(h->tv); rel(h->part); rel(h->b0); rel(h->dscal); rel(h->dint);
+    delete h;
+}
+
+const char *pd_ipc_last_error(const pd_ipc *h) {
+    return h ? h->err.c_str() : g_last_error.c_str();
+}
+
+int pd_ipc_set_positions(pd_ipc *h, int32_t seq, const double *x) {
+    if (!h || !x) return fail(nullptr, PD_IPC_E_ARG, "NULL argument");
+    if (seq < 0 || seq >= (int)h->seqs.size()) return fail(h, PD_IPC_E_ARG, "bad sequence");
+    for (int v = 0; v < h->n; ++v)
+        if (h->hm.is_fixed[v])
+            for (int a = 0; a < 3; ++a)
+                if (x[3 * v + a] != h->hm.rest[3 * v + a])
+                    return fail(h, PD_IPC_E_ARG, "fixed vertex moved");
+    try {
+        std::vector<double4> x4(h->n);
+        for (int v = 0; v < h->n; ++v) x4[v] = make_double4(x[3 * v], x[3 * v + 1], x[3 * v + 2], 0.0);
+        CK(cudaMemcpy(h->seqs[seq]->x.p, x4.data(), sizeof(double4) * h->n, cudaMemcpyHostToDevice));
+        if (h->Nt > 0) {
+            // intersection check: every pair within d_hat must have a positive distance
+            launch_surface(h->Wp.p, h->Wc.p, h->Wv.p, h->seqs[seq]->x.p, h->Ns, h->s.p, h->st);
+            int cpt, cee;
+            broad_phase(h, nullptr, 0.5 * h->dh * 1.01, &cpt, &cee);
+            ensure_pair_buffers(h, cpt + cee);
+            launch_narrow(h->cand.p, cpt, 1, h->Nt, h->s.p, h->tris.p, h->edges.p, h->Nt, h->Ne, h->dh2,
+                          h->flag.p, h->ctype.p, h->cd2.p, h->st);
+            launch_narrow(h->cand.p + cpt, cee, 0, h->Ne, h->s.p, h->tris.p, h->edges.p, h->Nt, h->Ne, h->dh2,
+                          h->flag.p + cpt, h->ctype.p + cpt, h->cd2.p + cpt, h->st);
+            std::vector<double> d2(cpt + cee);
+            CK(cudaStreamSynchronize(h->st));
+            if (cpt + cee)
+                CK(cudaMemcpy(d2.data(), h->cd2.p, sizeof(double) * (cpt + cee), cudaMemcpyDeviceToHost));
+            for (double v : d2)
+                if (!(v > 0)) return fail(h, PD_IPC_E_INTERSECTING, "intersecting state");
+        }
+    } catch (const CudaError &e) {
+        return fail(h, e.code, e.what());
+    }
+    return PD_IPC_OK;
+}
+
+int pd_ipc_set_debug(pd_ipc *h, int32_t level) {
+    if (!h) return fail(nullptr, PD_IPC_E_ARG, "NULL handle");
+    h->debug = level;
+    return PD_IPC_OK;
+}
+
+int pd_ipc_get_projections(const pd_ipc *h, int32_t seq, double *p) {
+    if (!h || !p) return fail(nullptr, PD_IPC_E_ARG, "NULL argument");
+    if (seq < 0 || seq >= (int)h->seqs.size()) return fail(const_cast<pd_ipc *>(h), PD_IPC_E_ARG, "bad sequence");
+    if (!h->debug) return fail(const_cast<pd_ipc *>(h), PD_IPC_E_ARG, "enable pd_ipc_set_debug first");
+    try {
+        std::vector<double> soa(9 * (size_t)h->T);
+        CK(cudaMemcpy(soa.data(), h->seqs[seq]->p.p, sizeof(double) * soa.size(), cudaMemcpyDeviceToHost));
+        for (int t = 0; t < h->T; ++t)
+            for (int k = 0; k < 9; ++k) p[9 * (size_t)t + k] = soa[(size_t)k * h->T + t];
+    } catch (const CudaError &e) {
+        return fail(const_cast<pd_ipc *>(h), e.code, e.what());
+    }
+    return PD_IPC_OK;
+}
+
+int pd_ipc_get_contacts(const pd_ipc *h, int32_t seq, int32_t *pt, int32_t *n_pt, int32_t *ee,
+                        int32_t *n_ee, int32_t *S, int32_t *n_S) {
+    if (!h || !n_pt || !n_ee || !n_S) return fail(nullptr, PD_IPC_E_ARG, "NULL argument");
+    if (seq < 0 || seq >= (int)h->seqs.size()) return fail(const_cast<pd_ipc *>(h), PD_IPC_E_ARG, "bad sequence");
+    const Seq &q = *h->seqs[seq];
+    *n_pt = (int32_t)(q.pt.size() / 2);
+    *n_ee = (int32_t)(q.ee.size() / 2);
+    *n_S = (int32_t)q.S.size();
+    if (pt) std::copy(q.pt.begin(), q.pt.end(), pt);
+    if (ee) std::copy(q.ee.begin(), q.ee.end(), ee);
+    if (S) std::copy(q.S.begin(), q.S.end(), S);
+    return PD_IPC_OK;
+}
+
+int pd_ipc_get_vector(const pd_ipc *h, int32_t seq, int32_t which, double *out) {
+    if (!h || !out) return fail(nullptr, PD_IPC_E_ARG, "NULL argument");
+    if (seq < 0 || seq >= (int)h->seqs.size()) return fail(const_cast<pd_ipc *>(h), PD_IPC_E_ARG, "bad sequence");
+    const Seq &q = *h->seqs[seq];
+    const std::vector<double> &v = which == 0 ? q.ghat : which == 1 ? q.dx : q.gel;
+    if (v.size() != 3 * (size_t)h->n) return fail(const_cast<pd_ipc *>(h), PD_IPC_E_ARG, "not available (debug off?)");
+    std::copy(v.begin(), v.end(), out);
+    return PD_IPC_OK;
+}
+
+const char *pd_ipc_build_info(void) {
+    return "pd_ipc sm_100a build " __DATE__ " " __TIME__;
+}
+
+// Host-only debug entry (no GPU needed): runs setup + factorisation and solves L_FF x = b on
+// the host with the supernodal factor; reports factor statistics.  Used by CPU tests of the
+// setup logic.  b, x: [n_verts] (values on fixed vertices ignored / set to 0).
+int pd_ipc_debug_factor_solve(const pd_ipc_mesh *mesh, const double *rest_pos, const double *b,
+                              double *x, int64_t *stats /* [nsn, nnzL, max_width, depth] */) {
+    if (!mesh || !rest_pos) return fail(nullptr, PD_IPC_E_ARG, "NULL argument");
+    HostMesh m;
+    HostFactor f;
+    std::string err;
+    int rc = build_host_mesh(mesh->n_verts, mesh->n_tets, mesh->tets, mesh->n_fixed, mesh->fixed, rest_pos,
+                             mesh->n_surf_verts, mesh->n_surf_tris, mesh->surf_tris, mesh->embed_tet,
+                             mesh->embed_w, m, err);
+    if (rc) return fail(nullptr, rc, err);
+    rc = factorize(m, f, err);
+    if (rc) return fail(nullptr, rc, err);
+    if (stats) {
+        stats[0] = f.nsn;
+        stats[1] = f.nnzL;
+        stats[2] = f.max_width;
+        stats[3] = f.depth;
+    }
+    if (b && x) {
+        std::vector<double> y(f.nf);
+        for (int q = 0; q < f.nf; ++q) y[q] = b[m.q2v[q]];
+        for (int s = 0; s < f.nsn; ++s) {        // forward
+            int c0 = f.sn_c0[s], w = f.sn_c0[s + 1] - c0, r0 = f.sn_rowptr[s], nr = f.sn_rowptr[s + 1] - r0;
+            const double *L = &f.vals[f.sn_valptr[s]];
+            for (int k = 0; k < w; ++k) {
+                y[c0 + k] /= L[k + (size_t)k * nr];
+                for (int i = k + 1; i < nr; ++i) y[f.sn_rows[r0 + i]] -= L[i + (size_t)k * nr] * y[c0 + k];
+            }
+        }
+        for (int s = f.nsn - 1; s >= 0; --s) {  // backward
+            int c0 = f.sn_c0[s], w = f.sn_c0[s + 1] - c0, r0 = f.sn_rowptr[s], nr = f.sn_rowptr[s + 1] - r0;
+            const double *L = &f.vals[f.sn_valptr[s]];
+            for (int k = w - 1; k >= 0; --k) {
+                double acc = y[c0 + k];
+                for (int i = k + 1; i < nr; ++i) acc -= L[i + (size_t)k * nr] * y[f.sn_rows[r0 + i]];
+                y[c0 + k] = acc / L[k + (size_t)k * nr];
+            }
+        }
+        for (int v = 0; v < m.n; ++v) x[v] = 0.0;
+        for (int q = 0; q < f.nf; ++q) x[m.q2v[q]] = y[q];
+    }
+    return PD_IPC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,906 @@
+// Contact part of the PD+IPC iteration on the embedded surface s = W x:
+// spatial-hash broad phase (a4), narrow phase with the canonical distance types and the
+// warp-per-pair barrier gradient / Hessian / PSD projection (a5), contact vertex set S and the
+// deterministic pull-back of gradient and B-check (a6), ACCD (a10) and the line-search barrier
+// energy differences (a11).
+//
+// PAPER.md:88-93 (section 2.2, Eq. 3): B(x) = kappa sum_{k in C} b(d_k), active when d < d_0.
+// PositiveDefinite(script-B) -- per pair, 12x12, eigenvalues clamped at 0
+// (SURVEY Z17).  PAPER.md:99,115-116: CCD then backtracking line search.
+// Readings: SURVEY.md 8(c) "Canonical distance routine" (types by Ericson RTCD 5.1.5 / 5.1.9,
+// den from the cross product, d^2 by the type's closed form, dots summed x+y then +z, division
+// last) and Z3/Z4 (b(d) = -(d-dh)^2 ln(d/dh) in the unsquared distance).
+//
+// THIS TRANSLATION UNIT IS COMPILED WITH -fmad=false: every product and sum is rounded
+// separately, exactly like the oracle's numpy ufuncs, so that the active set C and S are
+// bit-exact on identical positions.
+#include "kernels.h"
+
+#include "dev_common.cuh"
+
+namespace pdipc {
+
+// ------------------------------------------------------------------ vector helpers --------
+struct V3 { double x, y, z; };
+__device__ __forceinline__ V3 mk(double4 a) { return {a.x, a.y, a.z}; }
+__device__ __forceinline__ V3 sub(V3 a, V3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ double dot(V3 a, V3 b) { return (a.x * b.x + a.y * b.y) + a.z * b.z; }
+__device__ __forceinline__ V3 cross(V3 u, V3 v) {
+    return {u.y * v.z - u.z * v.y, u.z * v.x - u.x * v.z, u.x * v.y - u.y * v.x};
+}
+__device__ __forceinline__ V3 axpy(V3 s, double t, V3 d) { return {s.x + t * d.x, s.y + t * d.y, s.z + t * d.z}; }
+
+// type labels (this file's own enumeration)
+enum { T_PT_A = 0, T_PT_B, T_PT_C, T_PT_AB, T_PT_AC, T_PT_BC, T_PT_F,
+       T_EE = 7, T_EE_PA, T_EE_PB, T_EE_PC, T_EE_PD, T_EE_AC, T_EE_AD, T_EE_BC, T_EE_BD };
+
+__device__ __forceinline__ double d2_pp(V3 p, V3 q) { V3 r = sub(p, q); return dot(r, r); }
+__device__ __forceinline__ double d2_pe(V3 p, V3 a, V3 b) {
+    V3 c = cross(sub(a, p), sub(b, p));
+    V3 e = sub(b, a);
+    return dot(c, c) / dot(e, e);
+}
+__device__ __forceinline__ double d2_plane(V3 p, V3 a, V3 b, V3 c) {
+    V3 n = cross(sub(b, a), sub(c, a));
+    double t = dot(sub(p, a), n);
+    return (t * t) / dot(n, n);
+}
+__device__ __forceinline__ double d2_ll(V3 a, V3 b, V3 c, V3 d) {
+    V3 n = cross(sub(b, a), sub(d, c));
+    double t = dot(sub(c, a), n);
+    return (t * t) / dot(n, n);
+}
+
+__device__ int pt_type(V3 p, V3 a, V3 b, V3 c) {
+    V3 ab = sub(b, a), ac = sub(c, a), ap = sub(p, a);
+    double d1 = dot(ab, ap), d2 = dot(ac, ap);
+    if (d1 <= 0 && d2 <= 0) return T_PT_A;
+    V3 bp = sub(p, b);
+    double d3 = dot(ab, bp), d4 = dot(ac, bp);
+    if (d3 >= 0 && d4 <= d3) return T_PT_B;
+    double vc = d1 * d4 - d3 * d2;
+    if (vc <= 0 && d1 >= 0 && d3 <= 0) return T_PT_AB;
+    V3 cp = sub(p, c);
+    double d5 = dot(ab, cp), d6 = dot(ac, cp);
+    if (d6 >= 0 && d5 <= d6) return T_PT_C;
+    double vb = d5 * d2 - d1 * d6;
+    if (vb <= 0 && d2 >= 0 && d6 <= 0) return T_PT_AC;
+    double va = d3 * d6 - d5 * d4;
+    if (va <= 0 && (d4 - d3) >= 0 && (d5 - d6) >= 0) return T_PT_BC;
+    return T_PT_F;
+}
+
+__device__ __forceinline__ double clamp01(double v) { return fmin(fmax(v, 0.0), 1.0); }
+
+__device__ int ee_type(V3 a, V3 b, V3 c, V3 d) {
+    V3 d1 = sub(b, a), d2 = sub(d, c), r = sub(a, c);
+    double A = dot(d1, d1), E = dot(d2, d2), F = dot(d2, r), C = dot(d1, r), Bv = dot(d1, d2);
+    V3 cr = cross(d1, d2);
+    double den = dot(cr, cr);
+    double s = 0.0;
+    if (den > 1e-20 * A * E) s = clamp01((Bv * F - C * E) / den);
+    double t = (Bv * s + F) / E;
+    if (t < 0.0) { t = 0.0; s = clamp01(-C / A); }
+    else if (t > 1.0) { t = 1.0; s = clamp01((Bv - C) / A); }
+    bool s_in = s > 0.0 && s < 1.0, t_in = t > 0.0 && t < 1.0;
+    bool s1 = s >= 1.0, t1 = t >= 1.0;
+    if (s_in && t_in) return T_EE;
+    if (t_in) return s1 ? T_EE_PB : T_EE_PA;
+    if (s_in) return t1 ? T_EE_PD : T_EE_PC;
+    return s1 ? (t1 ? T_EE_BD : T_EE_BC) : (t1 ? T_EE_AD : T_EE_AC);
+}
+
+__device__ double type_d2(int ty, V3 P0, V3 P1, V3 P2, V3 P3) {
+    switch (ty) {
+        case T_PT_A: return d2_pp(P0, P1);
+        case T_PT_B: return d2_pp(P0, P2);
+        case T_PT_C: return d2_pp(P0, P3);
+        case T_PT_AB: return d2_pe(P0, P1, P2);
+        case T_PT_AC: return d2_pe(P0, P1, P3);
+        case T_PT_BC: return d2_pe(P0, P2, P3);
+        case T_PT_F: return d2_plane(P0, P1, P2, P3);
+        case T_EE: return d2_ll(P0, P1, P2, P3);
+        case T_EE_PA: return d2_pe(P0, P2, P3);
+        case T_EE_PB: return d2_pe(P1, P2, P3);
+        case T_EE_PC: return d2_pe(P2, P0, P1);
+        case T_EE_PD: return d2_pe(P3, P0, P1);
+        case T_EE_AC: return d2_pp(P0, P2);
+        case T_EE_AD: return d2_pp(P0, P3);
+        case T_EE_BC: return d2_pp(P1, P2);
+        default: return d2_pp(P1, P3);
+    }
+}
+
+// (type, d^2) of a pair; is_pt: (p, a, b, c) else (a, b, c, d)
+__device__ __forceinline__ double pair_d2(bool is_pt, V3 P0, V3 P1, V3 P2, V3 P3, int *ty) {
+    int t = is_pt ? pt_type(P0, P1, P2, P3) : ee_type(P0, P1, P2, P3);
+    *ty = t;
+    return type_d2(t, P0, P1, P2, P3);
+}
+
+// ------------------------------------------------------------------ barrier ---------------
+__device__ __forceinline__ double bar(double d, double dh) {
+    if (!(d > 0.0) || !(d < dh)) return 0.0;
+    double t = d - dh;
+    return -(t * t) * log(d / dh);
+}
+
+// ------------------------------------------------------------------ pair fetch ------------
+struct PairCtx {
+    const double4 *s;
+    const int *tris, *edges;
+    int Nt, Ne;
+};
+
+__device__ __forceinline__ void pair_ids(const PairCtx &c, bool is_pt, int i0, int i1, int id[4]) {
+    if (is_pt) {
+        id[0] = i0;
+        id[1] = c.tris[3 * i1];
+        id[2] = c.tris[3 * i1 + 1];
+        id[3] = c.tris[3 * i1 + 2];
+    } else {
+        id[0] = c.edges[2 * i0];
+        id[1] = c.edges[2 * i0 + 1];
+        id[2] = c.edges[2 * i1];
+        id[3] = c.edges[2 * i1 + 1];
+    }
+}
+
+// ------------------------------------------------------------------ a4 broad phase --------
+// Boxes: mode 0 (static): [s - r, s + r] per point, r = infl; mode 1 (swept): over
+// [s, s + ds] inflated by infl (the oracle's definition, exact).
+__global__ void k_boxes(const double4 *__restrict__ s, const double4 *__restrict__ ds,
+                        const int *__restrict__ tris, const int *__restrict__ edges, int Ns,
+                        int Nt, int Ne, double infl, double4 *__restrict__ lo,
+                        double4 *__restrict__ hi, double *__restrict__ ext) {
+    // layout: points [0, Ns), tris [Ns, Ns+Nt), edges [Ns+Nt, Ns+Nt+Ne)
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    double e = 0.0;
+    if (i < Ns + Nt + Ne) {
+        int id[3], cnt;
+        if (i < Ns) { id[0] = i; cnt = 1; }
+        else if (i < Ns + Nt) { int f = i - Ns; id[0] = tris[3 * f]; id[1] = tris[3 * f + 1]; id[2] = tris[3 * f + 2]; cnt = 3; }
+        else { int k = i - Ns - Nt; id[0] = edges[2 * k]; id[1] = edges[2 * k + 1]; cnt = 2; }
+        double l[3] = {1e300, 1e300, 1e300}, h[3] = {-1e300, -1e300, -1e300};
+        for (int q = 0; q < cnt; ++q) {
+            double4 p = s[id[q]];
+            double a[3] = {p.x, p.y, p.z};
+            double b[3] = {p.x, p.y, p.z};
+            if (ds) {
+                double4 d = ds[id[q]];
+                double b2[3] = {p.x + d.x, p.y + d.y, p.z + d.z};
+                for (int k = 0; k < 3; ++k) { a[k] = fmin(a[k], b2[k]); b[k] = fmax(b[k], b2[k]); }
+            }
+            for (int k = 0; k < 3; ++k) { l[k] = fmin(l[k], a[k]); h[k] = fmax(h[k], b[k]); }
+        }
+        double4 L = make_double4(l[0] - infl, l[1] - infl, l[2] - infl, 0.0);
+        double4 H = make_double4(h[0] + infl, h[1] + infl, h[2] + infl, 0.0);
+        lo[i] = L;
+        hi[i] = H;
+        e = fmax(fmax(H.x - L.x, H.y - L.y), H.z - L.z);
+    }
+    e = warp_max(e);
+    if ((threadIdx.x & 31) == 0 && e > 0.0) atomicMax(reinterpret_cast<unsigned long long *>(ext),
+                                                       (unsigned long long)__double_as_longlong(e));
+}
+
+__device__ __forceinline__ unsigned cell_hash(int x, int y, int z, unsigned mask) {
+    return ((unsigned)x * 73856093u ^ (unsigned)y * 19349663u ^ (unsigned)z * 83492791u) & mask;
+}
+
+__device__ __forceinline__ void cell_range(double4 lo, double4 hi, double inv, int c0[3], int c1[3]) {
+    c0[0] = (int)floor(lo.x * inv); c1[0] = (int)floor(hi.x * inv);
+    c0[1] = (int)floor(lo.y * inv); c1[1] = (int)floor(hi.y * inv);
+    c0[2] = (int)floor(lo.z * inv); c1[2] = (int)floor(hi.z * inv);
+}
+
+// count / fill the hash table with the B-side boxes [b0, b0+nb)
+__global__ void k_hash_insert(const double4 *__restrict__ lo, const double4 *__restrict__ hi,
+                              int b0, int nb, const double *__restrict__ cell, unsigned mask,
+                              int *__restrict__ cnt, const int *__restrict__ start,
+                              int *__restrict__ entries) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nb) return;
+    const double inv = 1.0 / *cell;
+    int c0[3], c1[3];
+    cell_range(lo[b0 + i], hi[b0 + i], inv, c0, c1);
+    for (int x = c0[0]; x <= c1[0]; ++x)
+        for (int y = c0[1]; y <= c1[1]; ++y)
+            for (int z = c0[2]; z <= c1[2]; ++z) {
+                unsigned h = cell_hash(x, y, z, mask);
+                int slot = atomicAdd(cnt + h, 1);
+                if (entries) entries[start[h] + slot] = i;
+            }
+}
+
+__device__ __forceinline__ bool overlap(double4 la, double4 ha, double4 lb, double4 hb) {
+    return la.x <= hb.x && lb.x <= ha.x && la.y <= hb.y && lb.y <= ha.y && la.z <= hb.z && lb.z <= ha.z;
+}
+
+// Query A-side boxes against the table; emit keys a*nB + b (dedup by the lowest shared cell,
+// residual duplicates removed by sort + unique).  ee: A and B are the same edge set, a < b,
+// pairs sharing a vertex excluded; pt: A = points, B = tris, incident pairs excluded.
+__global__ void k_hash_query(const double4 *__restrict__ lo, const double4 *__restrict__ hi,
+                             int a0, int na, int b0, int nB, const double *__restrict__ cell,
+                             unsigned mask, const int *__restrict__ start,
+                             const int *__restrict__ entries, int is_pt,
+                             const int *__restrict__ tris, const int *__restrict__ edges,
+                             unsigned long long *__restrict__ out, int *__restrict__ count,
+                             int cap) {
+    int a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= na) return;
+    const double inv = 1.0 / *cell;
+    const double4 la = lo[a0 + a], ha = hi[a0 + a];
+    int c0[3], c1[3];
+    cell_range(la, ha, inv, c0, c1);
+    int av[2];
+    if (!is_pt) { av[0] = edges[2 * a]; av[1] = edges[2 * a + 1]; }
+    for (int x = c0[0]; x <= c1[0]; ++x)
+        for (int y = c0[1]; y <= c1[1]; ++y)
+            for (int z = c0[2]; z <= c1[2]; ++z) {
+                unsigned h = cell_hash(x, y, z, mask);
+                for (int k = start[h]; k < start[h + 1]; ++k) {
+                    int b = entries[k];
+                    if (!is_pt && b <= a) continue;
+                    const double4 lb = lo[b0 + b], hb = hi[b0 + b];
+                    if (!overlap(la, ha, lb, hb)) continue;
+                    // lowest shared cell
+                    int m0 = max(c0[0], (int)floor(lb.x * inv)), m1 = max(c0[1], (int)floor(lb.y * inv)),
+                        m2 = max(c0[2], (int)floor(lb.z * inv));
+                    if (m0 != x || m1 != y || m2 != z) continue;
+                    if (is_pt) {
+                        if (tris[3 * b] == a || tris[3 * b + 1] == a || tris[3 * b + 2] == a) continue;
+                    } else {
+                        int b0v = edges[2 * b], b1v = edges[2 * b + 1];
+                        if (b0v == av[0] || b0v == av[1] || b1v == av[0] || b1v == av[1]) continue;
+                    }
+                    int pos = atomicAdd(count, 1);
+                    if (pos < cap) out[pos] = (unsigned long long)a * (unsigned long long)nB + b;
+                }
+            }
+}
+
+// ------------------------------------------------------------------ a5 narrow filter ------
+// flag[i] = d^2 < dh2 for candidate keys; stores type and d^2
+__global__ void k_narrow(const unsigned long long *__restrict__ keys, int n, int is_pt, int nB,
+                         PairCtx c, double dh2, int *__restrict__ flag, int *__restrict__ type,
+                         double *__restrict__ d2out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    unsigned long long k = keys[i];
+    int i0 = (int)(k / nB), i1 = (int)(k % nB);
+    int id[4];
+    pair_ids(c, is_pt, i0, i1, id);
+    int ty;
+    double d2 = pair_d2(is_pt, mk(c.s[id[0]]), mk(c.s[id[1]]), mk(c.s[id[2]]), mk(c.s[id[3]]), &ty);
+    flag[i] = d2 < dh2 ? 1 : 0;
+    type[i] = ty;
+    d2out[i] = d2;
+}
+
+__global__ void k_compact_active(const unsigned long long *__restrict__ keys, int n,
+                                 const int *__restrict__ flag, const int *__restrict__ pos,
+                                 const int *__restrict__ type, const double *__restrict__ d2,
+                                 int base, unsigned long long *__restrict__ akeys,
+                                 int *__restrict__ atype, double *__restrict__ ad2) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || !flag[i]) return;
+    int p = base + pos[i];
+    akeys[p] = keys[i];
+    atype[p] = type[i];
+    ad2[p] = d2[i];
+}
+
+// ------------------------------------------------------------------ a5 derivatives --------
+// Hyper-dual number: value, d/dx_i, d/dx_j, d2/dx_i dx_j.
+struct HD { double v, a, b, ab; };
+__device__ __forceinline__ HD hsub(HD x, HD y) { return {x.v - y.v, x.a - y.a, x.b - y.b, x.ab - y.ab}; }
+__device__ __forceinline__ HD hadd(HD x, HD y) { return {x.v + y.v, x.a + y.a, x.b + y.b, x.ab + y.ab}; }
+__device__ __forceinline__ HD hmul(HD x, HD y) {
+    return {x.v * y.v, x.a * y.v + x.v * y.a, x.b * y.v + x.v * y.b,
+            x.ab * y.v + x.a * y.b + x.b * y.a + x.v * y.ab};
+}
+__device__ __forceinline__ HD hdiv(HD x, HD y) {
+    double g = 1.0 / y.v, g1 = -g * g, g2 = 2.0 * g * g * g;
+    HD r = {g, g1 * y.a, g1 * y.b, g1 * y.ab + g2 * y.a * y.b};
+    return hmul(x, r);
+}
+struct HV { HD x, y, z; };
+__device__ __forceinline__ HV vsub(HV a, HV b) { return {hsub(a.x, b.x), hsub(a.y, b.y), hsub(a.z, b.z)}; }
+__device__ __forceinline__ HD vdot(HV a, HV b) { return hadd(hadd(hmul(a.x, b.x), hmul(a.y, b.y)), hmul(a.z, b.z)); }
+__device__ __forceinline__ HV vcross(HV u, HV v) {
+    return {hsub(hmul(u.y, v.z), hmul(u.z, v.y)), hsub(hmul(u.z, v.x), hmul(u.x, v.z)),
+            hsub(hmul(u.x, v.y), hmul(u.y, v.x))};
+}
+__device__ HD h_pp(HV p, HV q) { HV r = vsub(p, q); return vdot(r, r); }
+__device__ HD h_pe(HV p, HV a, HV b) {
+    HV c = vcross(vsub(a, p), vsub(b, p));
+    HV e = vsub(b, a);
+    return hdiv(vdot(c, c), vdot(e, e));
+}
+__device__ HD h_plane(HV p, HV a, HV b, HV c) {
+    HV n = vcross(vsub(b, a), vsub(c, a));
+    HD t = vdot(vsub(p, a), n);
+    return hdiv(hmul(t, t), vdot(n, n));
+}
+__device__ HD h_ll(HV a, HV b, HV c, HV d) {
+    HV n = vcross(vsub(b, a), vsub(d, c));
+    HD t = vdot(vsub(c, a), n);
+    return hdiv(hmul(t, t), vdot(n, n));
+}
+__device__ HD h_type_d2(int ty, const HV P[4]) {
+    switch (ty) {
+        case T_PT_A: return h_pp(P[0], P[1]);
+        case T_PT_B: return h_pp(P[0], P[2]);
+        case T_PT_C: return h_pp(P[0], P[3]);
+        case T_PT_AB: return h_pe(P[0], P[1], P[2]);
+        case T_PT_AC: return h_pe(P[0], P[1], P[3]);
+        case T_PT_BC: return h_pe(P[0], P[2], P[3]);
+        case T_PT_F: return h_plane(P[0], P[1], P[2], P[3]);
+        case T_EE: return h_ll(P[0], P[1], P[2], P[3]);
+        case T_EE_PA: return h_pe(P[0], P[2], P[3]);
+        case T_EE_PB: return h_pe(P[1], P[2], P[3]);
+        case T_EE_PC: return h_pe(P[2], P[0], P[1]);
+        case T_EE_PD: return h_pe(P[3], P[0], P[1]);
+        case T_EE_AC: return h_pp(P[0], P[2]);
+        case T_EE_AD: return h_pp(P[0], P[3]);
+        case T_EE_BC: return h_pp(P[1], P[2]);
+        default: return h_pp(P[1], P[3]);
+    }
+}
+
+__constant__ unsigned char c_ui[78], c_uj[78];
+
+constexpr int kPD_WARPS = 4;
+
+// Warp per active pair: grad/hess of d^2 (hyper-dual, one Hessian entry per lane-evaluation),
+// chain rule to d, barrier derivatives, 12x12 H_k, parallel-ordered cyclic Jacobi, clamp,
+// H_k^+ (packed upper, 78) and h_k = kappa b' grad d (12).
+__global__ void __launch_bounds__(kPD_WARPS * 32) k_pair_derivs(
+    const unsigned long long *__restrict__ akeys, const int *__restrict__ atype,
+    const double *__restrict__ ad2, int n_pt, int n_all, PairCtx c, double dh, double kappa,
+    double *__restrict__ grad, double *__restrict__ Hp, double *__restrict__ dist,
+    int *__restrict__ ids_out) {
+    __shared__ double Hs[kPD_WARPS][12][13];
+    __shared__ double Vs[kPD_WARPS][12][13];
+    __shared__ double gs[kPD_WARPS][12];
+    __shared__ double rot[kPD_WARPS][6][2];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const int k = blockIdx.x * kPD_WARPS + wl;
+    if (k >= n_all) return;
+    const bool is_pt = k < n_pt;
+    const int nB = is_pt ? c.Nt : c.Ne;
+    const unsigned long long key = akeys[k];
+    int id[4];
+    pair_ids(c, is_pt, (int)(key / nB), (int)(key % nB), id);
+    if (lane < 4) ids_out[4 * k + lane] = id[lane];
+    double y[12];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        double4 p = c.s[id[q]];
+        y[3 * q] = p.x; y[3 * q + 1] = p.y; y[3 * q + 2] = p.z;
+    }
+    const int ty = atype[k];
+    const double d2 = ad2[k];
+    double (*H)[13] = Hs[wl];
+    double (*V)[13] = Vs[wl];
+    // hyper-dual evaluations: entries e = lane, lane+32, lane+64 (< 78)
+    for (int e = lane; e < 78; e += 32) {
+        const int ei = c_ui[e], ej = c_uj[e];
+        HV P[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            HD cx = {y[3 * q], 0, 0, 0}, cy = {y[3 * q + 1], 0, 0, 0}, cz = {y[3 * q + 2], 0, 0, 0};
+            HD *comp[3] = {&cx, &cy, &cz};
+            for (int a = 0; a < 3; ++a) {
+                if (3 * q + a == ei) comp[a]->a = 1.0;
+                if (3 * q + a == ej) comp[a]->b = 1.0;
+            }
+            P[q] = {cx, cy, cz};
+        }
+        HD f = h_type_d2(ty, P);
+        H[ei][ej] = f.ab;
+        H[ej][ei] = f.ab;
+        if (ei == ej) gs[wl][ei] = f.a;
+    }
+    __syncwarp();
+    // chain rule: gd = g/(2d); Hd = (H2 - 2 gd gd^T)/(2d); Hk = kappa (b'' gd gd^T + b' Hd)
+    const double d = sqrt(d2);
+    const double t = d - dh, lg = log(d / dh);
+    const double b1 = -2.0 * t * lg - (t * t) / d;
+    const double b2 = -2.0 * lg - 4.0 * t / d + (t * t) / (d * d);
+    for (int e = lane; e < 144; e += 32) {
+        int i = e / 12, j = e % 12;
+        double gi = gs[wl][i] / (2.0 * d), gj = gs[wl][j] / (2.0 * d);
+        double Hd = (H[i][j] - 2.0 * gi * gj) / (2.0 * d);
+        double v = kappa * (b2 * gi * gj + b1 * Hd);
+        V[i][j] = v;          // stage in V, copy back after all lanes read H
+    }
+    __syncwarp();
+    for (int e = lane; e < 144; e += 32) {
+        int i = e / 12, j = e % 12;
+        H[i][j] = V[i][j];
+        V[i][j] = (i == j) ? 1.0 : 0.0;
+    }
+    if (lane < 12) grad[12 * (size_t)k + lane] = kappa * b1 * (gs[wl][lane] / (2.0 * d));
+    if (lane == 0) dist[k] = d;
+    __syncwarp();
+    // symmetrize
+    for (int e = lane; e < 144; e += 32) {
+        int i = e / 12, j = e % 12;
+        if (i < j) {
+            double m = 0.5 * (H[i][j] + H[j][i]);
+            H[i][j] = m;
+            H[j][i] = m;
+        }
+    }
+    __syncwarp();
+    // parallel-ordered cyclic Jacobi (round-robin tournament, 11 rounds x 6 disjoint pairs)
+    double fro = 0.0;
+    for (int e = lane; e < 144; e += 32) fro += H[e / 12][e % 12] * H[e / 12][e % 12];
+    fro = warp_sum(fro);
+    for (int sweep = 0; sweep < 20; ++sweep) {
+        double off = 0.0;
+        for (int e = lane; e < 144; e += 32) {
+            int i = e / 12, j = e % 12;
+            if (i != j) off += H[i][j] * H[i][j];
+        }
+        off = warp_sum(off);
+        if (off <= 1e-30 * fro) break;
+        for (int round = 0; round < 11; ++round) {
+            // pairs of the round: players 0..11, player 11 fixed, others rotate
+            if (lane < 6) {
+                int pa, pb;
+                if (lane == 0) { pa = 11; pb = round; }
+                else { pa = (round + lane) % 11; pb = (round + 11 - lane) % 11; }
+                int p = min(pa, pb), q = max(pa, pb);
+                double apq = H[p][q], cth = 1.0, sth = 0.0;
+                if (fabs(apq) > 1e-300) {
+                    double tau = (H[q][q] - H[p][p]) / (2.0 * apq);
+                    double tt = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                    cth = 1.0 / sqrt(1.0 + tt * tt);
+                    sth = tt * cth;
+                }
+                rot[wl][lane][0] = cth;
+                rot[wl][lane][1] = sth;
+            }
+            __syncwarp();
+            // rows: H <- J^T H
+            for (int e = lane; e < 72; e += 32) {
+                int pr = e / 12, m = e % 12;
+                int pa, pb;
+                if (pr == 0) { pa = 11; pb = round; }
+                else { pa = (round + pr) % 11; pb = (round + 11 - pr) % 11; }
+                int p = min(pa, pb), q = max(pa, pb);
+                double cth = rot[wl][pr][0], sth = rot[wl][pr][1];
+                double hp = H[p][m], hq = H[q][m];
+                H[p][m] = cth * hp - sth * hq;
+                H[q][m] = sth * hp + cth * hq;
+            }
+            __syncwarp();
+            // columns: H <- H J, V <- V J
+            for (int e = lane; e < 72; e += 32) {
+                int pr = e / 12, m = e % 12;
+                int pa, pb;
+                if (pr == 0) { pa = 11; pb = round; }
+                else { pa = (round + pr) % 11; pb = (round + 11 - pr) % 11; }
+                int p = min(pa, pb), q = max(pa, pb);
+                double cth = rot[wl][pr][0], sth = rot[wl][pr][1];
+                double hp = H[m][p], hq = H[m][q];
+                H[m][p] = cth * hp - sth * hq;
+                H[m][q] = sth * hp + cth * hq;
+                double vp = V[m][p], vq = V[m][q];
+                V[m][p] = cth * vp - sth * vq;
+                V[m][q] = sth * vp + cth * vq;
+            }
+            __syncwarp();
+        }
+    }
+    // H^+ = sum_m max(lambda_m, 0) v_m v_m^T, packed upper
+    for (int e = lane; e < 78; e += 32) {
+        int i = c_ui[e], j = c_uj[e];
+        double acc = 0.0;
+        for (int m = 0; m < 12; ++m) {
+            double l = H[m][m];
+            if (l > 0.0) acc += l * V[i][m] * V[j][m];
+        }
+        Hp[78 * (size_t)k + e] = acc;
+    }
+}
+
+// ------------------------------------------------------------------ a6 contact set S ------
+__global__ void k_mark_S(const int *__restrict__ ids, int n_all, const int *__restrict__ Wp,
+                         const int *__restrict__ Wc, const int *__restrict__ v2q,
+                         int *__restrict__ mark) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 4 * n_all) return;
+    int j = ids[i];
+    for (int k = Wp[j]; k < Wp[j + 1]; ++k) {
+        int q = v2q[Wc[k]];
+        if (q >= 0) mark[q] = 1;
+    }
+}
+
+__global__ void k_compact_S(const int *__restrict__ mark, const int *__restrict__ pos, int nf,
+                            int *__restrict__ qS) {
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < nf && mark[q]) qS[pos[q]] = q;
+}
+
+// gradient records: key = (surface vertex << sh) | (4k + slot)
+__global__ void k_grad_records(const int *__restrict__ ids, int n_all, int sh,
+                               unsigned long long *__restrict__ rec) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 4 * n_all) return;
+    rec[i] = ((unsigned long long)ids[i] << sh) | (unsigned long long)i;
+}
+
+// per run of equal surface vertex: gs[j] = sum of h_k[slot] in (k, slot) order
+__global__ void k_grad_reduce(const unsigned long long *__restrict__ rec, int n, int sh,
+                              const double *__restrict__ grad, double4 *__restrict__ gs) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    unsigned long long j = rec[i] >> sh;
+    if (i > 0 && (rec[i - 1] >> sh) == j) return;
+    double gx = 0, gy = 0, gz = 0;
+    const unsigned long long m = (1ull << sh) - 1;
+    for (int r = i; r < n && (rec[r] >> sh) == j; ++r) {
+        unsigned long long ks = rec[r] & m;
+        const double *g = grad + 12 * (ks >> 2) + 3 * (ks & 3);
+        gx += g[0];
+        gy += g[1];
+        gz += g[2];
+    }
+    gs[j] = make_double4(gx, gy, gz, 0.0);
+}
+
+// G[q] (solve RHS, factor order, [nf][4]) = g_el[q] + sum_{(j,w) in W^T row q} w gs[j]
+__global__ void k_grad_pullback(const double4 *__restrict__ g_el, const int *__restrict__ WTp,
+                                const int *__restrict__ WTr, const double *__restrict__ WTv,
+                                const double4 *__restrict__ gs, int nf, double *__restrict__ G) {
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nf) return;
+    double4 g = g_el[q];
+    double bx = 0, by = 0, bz = 0;
+    if (gs) {
+        for (int k = WTp[q]; k < WTp[q + 1]; ++k) {
+            double w = WTv[k];
+            double4 v = gs[WTr[k]];
+            bx += w * v.x;
+            by += w * v.y;
+            bz += w * v.z;
+        }
+    }
+    G[4 * (size_t)q + 0] = g.x + bx;
+    G[4 * (size_t)q + 1] = g.y + by;
+    G[4 * (size_t)q + 2] = g.z + bz;
+    G[4 * (size_t)q + 3] = 0.0;
+}
+
+// B-check records.  Count per pair, then write at scanned offsets.
+__device__ __forceinline__ int bc_count_pair(const int *id, const int *Wp, const int *Wc,
+                                             const int *v2q) {
+    int nfree[4];
+    for (int a = 0; a < 4; ++a) {
+        nfree[a] = 0;
+        for (int k = Wp[id[a]]; k < Wp[id[a] + 1]; ++k) nfree[a] += v2q[Wc[k]] >= 0;
+    }
+    int s = 0;
+    for (int a = 0; a < 4; ++a) s += nfree[a];
+    return s * s;
+}
+
+__global__ void k_bc_count(const int *__restrict__ ids, int n_all, const int *__restrict__ Wp,
+                           const int *__restrict__ Wc, const int *__restrict__ v2q,
+                           int *__restrict__ cnt) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n_all) return;
+    cnt[k] = bc_count_pair(ids + 4 * k, Wp, Wc, v2q);
+}
+
+// key = ((ia * nS + ib) << sh) | (k * 256 + sa * 64 + sb * 16 + na * 4 + nb)
+__global__ void k_bc_records(const int *__restrict__ ids, int n_all, const int *__restrict__ Wp,
+                             const int *__restrict__ Wc, const int *__restrict__ v2q,
+                             const int *__restrict__ sidx, int nS, int sh,
+                             const int *__restrict__ off, unsigned long long *__restrict__ rec) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n_all) return;
+    const int *id = ids + 4 * k;
+    int p = off[k];
+    for (int sa = 0; sa < 4; ++sa)
+        for (int na = 0; na < Wp[id[sa] + 1] - Wp[id[sa]]; ++na) {
+            int qa = v2q[Wc[Wp[id[sa]] + na]];
+            if (qa < 0) continue;
+            for (int sb = 0; sb < 4; ++sb)
+                for (int nb = 0; nb < Wp[id[sb] + 1] - Wp[id[sb]]; ++nb) {
+                    int qb = v2q[Wc[Wp[id[sb]] + nb]];
+                    if (qb < 0) continue;
+                    unsigned long long tgt = (unsigned long long)sidx[qa] * nS + sidx[qb];
+                    unsigned long long lo = (unsigned long long)k * 256 + sa * 64 + sb * 16 + na * 4 + nb;
+                    rec[p++] = (tgt << sh) | lo;
+                }
+        }
+}
+
+__device__ __forceinline__ int upk(int i, int j) {   // packed upper index, i <= j
+    return i * 12 - (i * (i - 1)) / 2 + (j - i);
+}
+
+__global__ void k_bc_reduce(const unsigned long long *__restrict__ rec, int n, int sh, int nS,
+                            const int *__restrict__ ids, const int *__restrict__ Wp,
+                            const double *__restrict__ Wv, const double *__restrict__ Hp,
+                            double *__restrict__ Bc, int ldb) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    unsigned long long tgt = rec[i] >> sh;
+    if (i > 0 && (rec[i - 1] >> sh) == tgt) return;
+    double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    const unsigned long long m = (1ull << sh) - 1;
+    for (int r = i; r < n && (rec[r] >> sh) == tgt; ++r) {
+        unsigned long long lo = rec[r] & m;
+        int k = (int)(lo >> 8), sa = (int)(lo >> 6) & 3, sb = (int)(lo >> 4) & 3, na = (int)(lo >> 2) & 3,
+            nb = (int)lo & 3;
+        const int *id = ids + 4 * k;
+        double w = Wv[Wp[id[sa]] + na] * Wv[Wp[id[sb]] + nb];
+        const double *H = Hp + 78 * (size_t)k;
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) {
+                int ii = 3 * sa + a, jj = 3 * sb + b;
+                double h = ii <= jj ? H[upk(ii, jj)] : H[upk(jj, ii)];
+                acc[3 * a + b] += w * h;
+            }
+    }
+    int ia = (int)(tgt / nS), ib = (int)(tgt % nS);
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) Bc[(size_t)(3 * ia + a) * ldb + 3 * ib + b] = acc[3 * a + b];
+}
+
+__global__ void k_zero_square(double *M, int ld, int n) {
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < (size_t)n * n;
+         e += (size_t)gridDim.x * blockDim.x)
+        M[(e / n) * ld + e % n] = 0.0;
+}
+
+// ------------------------------------------------------------------ a10 ACCD --------------
+// SURVEY 8(c) O7 as written.  Swept candidate keys -> TOI; atomic min into *amin.
+__global__ void k_accd(const unsigned long long *__restrict__ keys, int n, int is_pt, int nB,
+                       PairCtx c, const double4 *__restrict__ ds, double s_gap, int max_iters,
+                       double *__restrict__ amin) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    double toi = 1.0;
+    if (i < n) {
+        unsigned long long k = keys[i];
+        int id[4];
+        pair_ids(c, is_pt, (int)(k / nB), (int)(k % nB), id);
+        V3 P[4], D[4];
+        for (int q = 0; q < 4; ++q) { P[q] = mk(c.s[id[q]]); D[q] = mk(ds[id[q]]); }
+        V3 mean = {(((D[0].x + D[1].x) + D[2].x) + D[3].x) / 4.0, (((D[0].y + D[1].y) + D[2].y) + D[3].y) / 4.0,
+                   (((D[0].z + D[1].z) + D[2].z) + D[3].z) / 4.0};
+        double nr[4];
+        for (int q = 0; q < 4; ++q) { V3 p = sub(D[q], mean); nr[q] = sqrt(dot(p, p)); }
+        double lp = is_pt ? nr[0] + fmax(fmax(nr[1], nr[2]), nr[3]) : fmax(nr[0], nr[1]) + fmax(nr[2], nr[3]);
+        if (lp > 0.0) {
+            int ty;
+            double d_init = sqrt(pair_d2(is_pt, P[0], P[1], P[2], P[3], &ty));
+            double g = s_gap * d_init;
+            double t = 0.0, tl = (1.0 - s_gap) * d_init / lp;
+            int it = 0;
+            bool done = false;
+            while (it < max_iters) {
+                double tt = t + tl;
+                double d = sqrt(pair_d2(is_pt, axpy(P[0], tt, D[0]), axpy(P[1], tt, D[1]),
+                                        axpy(P[2], tt, D[2]), axpy(P[3], tt, D[3]), &ty));
+                ++it;
+                bool gap_exit = t > 0 && d < g;
+                if (gap_exit) { toi = t; done = true; break; }
+                if (tt > 1.0) { toi = 1.0; done = true; break; }
+                t = tt;
+                tl = 0.9 * d / lp;
+            }
+            if (!done) toi = t;
+        }
+    }
+    toi = warp_min(toi);
+    if ((threadIdx.x & 31) == 0) atomic_min_nonneg(amin, toi);
+}
+
+// ------------------------------------------------------------------ a11 line search -------
+// b0[i] = b(d(s)) per swept candidate
+__global__ void k_ls_b0(const unsigned long long *__restrict__ keys, int n, int is_pt, int nB,
+                        PairCtx c, double dh, double *__restrict__ b0) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    unsigned long long k = keys[i];
+    int id[4], ty;
+    pair_ids(c, is_pt, (int)(k / nB), (int)(k % nB), id);
+    double d2 = pair_d2(is_pt, mk(c.s[id[0]]), mk(c.s[id[1]]), mk(c.s[id[2]]), mk(c.s[id[3]]), &ty);
+    b0[i] = bar(sqrt(d2), dh);
+}
+
+// per block partial sums of b(d(alpha_h)) - b0 for trials h = h0 .. h0+7
+__global__ void __launch_bounds__(256) k_ls_trials(const unsigned long long *__restrict__ keys,
+                                                   int n, int is_pt, int nB, PairCtx c,
+                                                   const double4 *__restrict__ ds, double dh,
+                                                   const double *__restrict__ b0,
+                                                   const double *__restrict__ ls,  // [alpha_m, accepted flag, h0]
+                                                   int h0, double *__restrict__ part, int part_ld) {
+    if (ls[1] != 0.0) return;   // already accepted
+    __shared__ double sh[8];
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const double am = ls[0];
+    int id[4];
+    V3 P[4], D[4];
+    double bb0 = 0.0;
+    if (i < n) {
+        unsigned long long k = keys[i];
+        pair_ids(c, is_pt, (int)(k / nB), (int)(k % nB), id);
+        for (int q = 0; q < 4; ++q) { P[q] = mk(c.s[id[q]]); D[q] = mk(ds[id[q]]); }
+        bb0 = b0[i];
+    }
+    for (int h = 0; h < 8; ++h) {
+        double v = 0.0;
+        if (i < n) {
+            double al = ldexp(am, -(h0 + h));
+            int ty;
+            double d2 = pair_d2(is_pt, axpy(P[0], al, D[0]), axpy(P[1], al, D[1]), axpy(P[2], al, D[2]),
+                                axpy(P[3], al, D[3]), &ty);
+            v = bar(sqrt(d2), dh) - bb0;
+        }
+        v = block_sum<256>(v, sh);
+        if (threadIdx.x == 0) part[(size_t)h * part_ld + blockIdx.x] = v;
+    }
+}
+
+// decide: dE(alpha_h) = alpha gTdx + 0.5 alpha alpha quad + kappa dB
+__global__ void k_ls_decide(const double *__restrict__ part, int part_ld, int npart,
+                            const double *__restrict__ scal,   // [gTdx, quad]
+                            double kappa, int h0, int hmax, double *__restrict__ ls,
+                            double *__restrict__ out /* alpha, trials, dE, flags */) {
+    if (ls[1] != 0.0) return;
+    __shared__ double sh[32];
+    const double am = ls[0];
+    for (int h = 0; h < 8; ++h) {
+        double s = 0.0;
+        for (int b = threadIdx.x; b < npart; b += blockDim.x) s += part[(size_t)h * part_ld + b];
+        s = block_sum<1024>(s, sh);
+        if (threadIdx.x == 0) {
+            int hh = h0 + h;
+            if (hh <= hmax && ls[1] == 0.0) {
+                double al = ldexp(am, -hh);
+                double dE = al * scal[0] + 0.5 * al * al * scal[1] + kappa * s;
+                if (dE < 0.0) {
+                    ls[1] = 1.0;
+                    out[0] = al;
+                    out[1] = hh + 1;
+                    out[2] = dE;
+                    out[3] = 0;
+                } else if (hh == hmax) {
+                    ls[1] = 2.0;
+                    out[0] = 0.0;
+                    out[1] = hh + 1;
+                    out[2] = 0.0;
+                    out[3] = 1;   // stall
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ host wrappers ---------
+void contact_init() {
+    unsigned char ui[78], uj[78];
+    int e = 0;
+    for (int i = 0; i < 12; ++i)
+        for (int j = i; j < 12; ++j) { ui[e] = (unsigned char)i; uj[e] = (unsigned char)j; ++e; }
+    cudaMemcpyToSymbol(c_ui, ui, 78);
+    cudaMemcpyToSymbol(c_uj, uj, 78);
+}
+
+void launch_boxes(const double4 *s, const double4 *ds, const int *tris, const int *edges, int Ns,
+                  int Nt, int Ne, double infl, double4 *lo, double4 *hi, double *ext,
+                  cudaStream_t st) {
+    int n = Ns + Nt + Ne;
+    k_boxes<<<(n + 255) / 256, 256, 0, st>>>(s, ds, tris, edges, Ns, Nt, Ne, infl, lo, hi, ext);
+}
+void launch_hash_insert(const double4 *lo, const double4 *hi, int b0, int nb, const double *cell,
+                        unsigned mask, int *cnt, const int *start, int *entries, cudaStream_t st) {
+    if (nb > 0) k_hash_insert<<<(nb + 255) / 256, 256, 0, st>>>(lo, hi, b0, nb, cell, mask, cnt, start, entries);
+}
+void launch_hash_query(const double4 *lo, const double4 *hi, int a0, int na, int b0, int nB,
+                       const double *cell, unsigned mask, const int *start, const int *entries,
+                       int is_pt, const int *tris, const int *edges, unsigned long long *out,
+                       int *count, int cap, cudaStream_t st) {
+    if (na > 0)
+        k_hash_query<<<(na + 127) / 128, 128, 0, st>>>(lo, hi, a0, na, b0, nB, cell, mask, start,
+                                                       entries, is_pt, tris, edges, out, count, cap);
+}
+void launch_narrow(const unsigned long long *keys, int n, int is_pt, int nB, const double4 *s,
+                   const int *tris, const int *edges, int Nt, int Ne, double dh2, int *flag,
+                   int *type, double *d2, cudaStream_t st) {
+    if (n <= 0) return;
+    PairCtx c{s, tris, edges, Nt, Ne};
+    k_narrow<<<(n + 255) / 256, 256, 0, st>>>(keys, n, is_pt, nB, c, dh2, flag, type, d2);
+}
+void launch_compact_active(const unsigned long long *keys, int n, const int *flag, const int *pos,
+                           const int *type, const double *d2, int base, unsigned long long *akeys,
+                           int *atype, double *ad2, cudaStream_t st) {
+    if (n > 0)
+        k_compact_active<<<(n + 255) / 256, 256, 0, st>>>(keys, n, flag, pos, type, d2, base, akeys, atype, ad2);
+}
+void launch_pair_derivs(const unsigned long long *akeys, const int *atype, const double *ad2,
+                        int n_pt, int n_all, const double4 *s, const int *tris, const int *edges,
+                        int Nt, int Ne, double dh, double kappa, double *grad, double *Hp,
+                        double *dist, int *ids, cudaStream_t st) {
+    if (n_all <= 0) return;
+    PairCtx c{s, tris, edges, Nt, Ne};
+    k_pair_derivs<<<(n_all + kPD_WARPS - 1) / kPD_WARPS, kPD_WARPS * 32, 0, st>>>(
+        akeys, atype, ad2, n_pt, n_all, c, dh, kappa, grad, Hp, dist, ids);
+}
+void launch_mark_S(const int *ids, int n_all, const int *Wp, const int *Wc, const int *v2q,
+                   int *mark, cudaStream_t st) {
+    if (n_all > 0) k_mark_S<<<(4 * n_all + 255) / 256, 256, 0, st>>>(ids, n_all, Wp, Wc, v2q, mark);
+}
+void launch_compact_S(const int *mark, const int *pos, int nf, int *qS, cudaStream_t st) {
+    k_compact_S<<<(nf + 255) / 256, 256, 0, st>>>(mark, pos, nf, qS);
+}
+void launch_grad_records(const int *ids, int n_all, int sh, unsigned long long *rec,
+                         cudaStream_t st) {
+    if (n_all > 0) k_grad_records<<<(4 * n_all + 255) / 256, 256, 0, st>>>(ids, n_all, sh, rec);
+}
+void launch_grad_reduce(const unsigned long long *rec, int n, int sh, const double *grad,
+                        double4 *gs, cudaStream_t st) {
+    if (n > 0) k_grad_reduce<<<(n + 255) / 256, 256, 0, st>>>(rec, n, sh, grad, gs);
+}
+void launch_grad_pullback(const double4 *g_el, const int *WTp, const int *WTr, const double *WTv,
+                          const double4 *gs, int nf, double *G, cudaStream_t st) {
+    k_grad_pullback<<<(nf + 255) / 256, 256, 0, st>>>(g_el, WTp, WTr, WTv, gs, nf, G);
+}
+void launch_bc_count(const int *ids, int n_all, const int *Wp, const int *Wc, const int *v2q,
+                     int *cnt, cudaStream_t st) {
+    if (n_all > 0) k_bc_count<<<(n_all + 255) / 256, 256, 0, st>>>(ids, n_all, Wp, Wc, v2q, cnt);
+}
+void launch_bc_records(const int *ids, int n_all, const int *Wp, const int *Wc, const int *v2q,
+                       const int *sidx, int nS, int sh, const int *off, unsigned long long *rec,
+                       cudaStream_t st) {
+    if (n_all > 0)
+        k_bc_records<<<(n_all + 127) / 128, 128, 0, st>>>(ids, n_all, Wp, Wc, v2q, sidx, nS, sh, off, rec);
+}
+void launch_bc_reduce(const unsigned long long *rec, int n, int sh, int nS, const int *ids,
+                      const int *Wp, const double *Wv, const double *Hp, double *Bc, int ldb,
+                      cudaStream_t st) {
+    if (n > 0) k_bc_reduce<<<(n + 255) / 256, 256, 0, st>>>(rec, n, sh, nS, ids, Wp, Wv, Hp, Bc, ldb);
+}
+void launch_zero_square(double *M, int ld, int n, cudaStream_t st) {
+    if (n > 0) k_zero_square<<<256, 256, 0, st>>>(M, ld, n);
+}
+void launch_accd(const unsigned long long *keys, int n, int is_pt, int nB, const double4 *s,
+                 const int *tris, const int *edges, int Nt, int Ne, const double4 *ds, double s_gap,
+                 int max_iters, double *amin, cudaStream_t st) {
+    if (n <= 0) return;
+    PairCtx c{s, tris, edges, Nt, Ne};
+    k_accd<<<(n + 127) / 128, 128, 0, st>>>(keys, n, is_pt, nB, c, ds, s_gap, max_iters, amin);
+}
+void launch_ls_b0(const unsigned long long *keys, int n, int is_pt, int nB, const double4 *s,
+                  const int *tris, const int *edges, int Nt, int Ne, double dh, double *b0,
+                  cudaStream_t st) {
+    if (n <= 0) return;
+    PairCtx c{s, tris, edges, Nt, Ne};
+    k_ls_b0<<<(n + 255) / 256, 256, 0, st>>>(keys, n, is_pt, nB, c, dh, b0);
+}
+int launch_ls_trials(const unsigned long long *keys, int n, int is_pt, int nB, const double4 *s,
+                     const int *tris, const int *edges, int Nt, int Ne, const double4 *ds,
+                     double dh, const double *b0, const double *ls, int h0, double *part,
+                     int part_ld, cudaStream_t st) {
+    if (n <= 0) return 0;
+    PairCtx c{s, tris, edges, Nt, Ne};
+    int nb = (n + 255) / 256;
+    k_ls_trials<<<nb, 256, 0, st>>>(keys, n, is_pt, nB, c, ds, dh, b0, ls, h0, part, part_ld);
+    return nb;
+}
+void launch_ls_decide(const double *part, int part_ld, int npart, const double *scal, double kappa,
+                      int h0, int hmax, double *ls, double *out, cudaStream_t st) {
+    k_ls_decide<<<1, 1024, 0, st>>>(part, part_ld, npart, scal, kappa, h0, hmax, ls, out);
+}
+
+}  // namespace pdipc

@@ -1,0 +1,336 @@
+// Elastic part of the PD+IPC iteration: actuation ingestion, the fused local step (a1),
+// the atomics-free elastic gradient gather (a2), surface interpolation s = W x (a3), and the
+// per-tet / per-vertex reductions of the line search (a11) and the update x += alpha dx.
+//
+// PAPER.md:73-79 (Eq. 1): E_i(x) = min_R ||F_i(x) - R A_i||_F^2; "we find the best rotation
+// R_i using the polar decomposition of F_i A_i" in parallel over elements.
+// PAPER.md:97,113 (Eq. 4): elastic gradient sum_i w_i G_i^T (G_i x - p_i).
+// s = W x.
+#include "kernels.h"
+
+#include "dev_common.cuh"
+
+namespace pdipc {
+
+// ------------------------------------------------------------------ actuation ingestion ----
+// A9 [T][9] row-major (ABI layout) -> SoA A6 [6][T] = (a00, a01, a02, a11, a12, a22).
+__global__ void k_ingest_actuation(const double *__restrict__ A9, double *__restrict__ A6, int T) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= T) return;
+    const double *a = A9 + 9 * (size_t)t;
+    A6[0 * (size_t)T + t] = a[0];
+    A6[1 * (size_t)T + t] = a[1];
+    A6[2 * (size_t)T + t] = a[2];
+    A6[3 * (size_t)T + t] = a[4];
+    A6[4 * (size_t)T + t] = a[5];
+    A6[5 * (size_t)T + t] = a[8];
+}
+
+// ------------------------------------------------------------------ 3x3 polar -------------
+// Symmetric 3x3 eigen-decomposition by cyclic Jacobi (FP64).  S = V diag(l) V^T.
+__device__ __forceinline__ void jacobi_rot(double S[3][3], double V[3][3], int p, int q) {
+    double apq = S[p][q];
+    if (fabs(apq) < 1e-300) return;
+    double tau = (S[q][q] - S[p][p]) / (2.0 * apq);
+    double t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+    double c = rsqrt(1.0 + t * t);
+    double s = t * c;
+    // S <- J^T S J
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        double skp = S[k][p], skq = S[k][q];
+        S[k][p] = c * skp - s * skq;
+        S[k][q] = s * skp + c * skq;
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        double spk = S[p][k], sqk = S[q][k];
+        S[p][k] = c * spk - s * sqk;
+        S[q][k] = s * spk + c * sqk;
+    }
+    S[p][q] = S[q][p] = 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        double vkp = V[k][p], vkq = V[k][q];
+        V[k][p] = c * vkp - s * vkq;
+        V[k][q] = s * vkp + c * vkq;
+    }
+}
+
+// Rotation factor R of M with the reflection fix: SVD M = U S V^T, flip the
+// smallest singular axis when det < 0, R = U V^T.  Computed from the eigenvectors V of M^T M
+// (Jacobi), u1 = M v1/|M v1|, u2 = Gram-Schmidt(M v2), u3 = u1 x u2, v3 = v1 x v2.
+__device__ void polar_rotation(const double M[3][3], double R[3][3]) {
+    double S[3][3], V[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            S[i][j] = M[0][i] * M[0][j] + M[1][i] * M[1][j] + M[2][i] * M[2][j];
+            V[i][j] = i == j ? 1.0 : 0.0;
+        }
+    const double tr2 = S[0][0] * S[0][0] + S[1][1] * S[1][1] + S[2][2] * S[2][2];
+    for (int sweep = 0; sweep < 12; ++sweep) {
+        double off = S[0][1] * S[0][1] + S[0][2] * S[0][2] + S[1][2] * S[1][2];
+        if (off <= 1e-34 * tr2) break;
+        jacobi_rot(S, V, 0, 1);
+        jacobi_rot(S, V, 0, 2);
+        jacobi_rot(S, V, 1, 2);
+    }
+    // order eigenvalues descending
+    int i1 = 0, i2 = 1, i3 = 2;
+    double l[3] = {S[0][0], S[1][1], S[2][2]};
+    if (l[i1] < l[i2]) { int t = i1; i1 = i2; i2 = t; }
+    if (l[i2] < l[i3]) { int t = i2; i2 = i3; i3 = t; }
+    if (l[i1] < l[i2]) { int t = i1; i1 = i2; i2 = t; }
+    double v1[3] = {V[0][i1], V[1][i1], V[2][i1]};
+    double v2[3] = {V[0][i2], V[1][i2], V[2][i2]};
+    double u1[3], u2[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        u1[a] = M[a][0] * v1[0] + M[a][1] * v1[1] + M[a][2] * v1[2];
+        u2[a] = M[a][0] * v2[0] + M[a][1] * v2[1] + M[a][2] * v2[2];
+    }
+    double n1 = sqrt(u1[0] * u1[0] + u1[1] * u1[1] + u1[2] * u1[2]);
+    if (n1 > 0) {
+        for (int a = 0; a < 3; ++a) u1[a] /= n1;
+    } else {
+        u1[0] = 1; u1[1] = 0; u1[2] = 0;
+    }
+    double dp = u1[0] * u2[0] + u1[1] * u2[1] + u1[2] * u2[2];
+    for (int a = 0; a < 3; ++a) u2[a] -= dp * u1[a];
+    double n2 = sqrt(u2[0] * u2[0] + u2[1] * u2[1] + u2[2] * u2[2]);
+    if (n2 > 1e-150 && n2 > 1e-14 * n1) {
+        for (int a = 0; a < 3; ++a) u2[a] /= n2;
+    } else {                                   // rank <= 1: any unit vector orthogonal to u1
+        double e[3] = {0, 0, 0};
+        int k = fabs(u1[0]) < 0.6 ? 0 : (fabs(u1[1]) < 0.6 ? 1 : 2);
+        e[k] = 1.0;
+        double d = u1[k];
+        for (int a = 0; a < 3; ++a) u2[a] = e[a] - d * u1[a];
+        double nn = sqrt(u2[0] * u2[0] + u2[1] * u2[1] + u2[2] * u2[2]);
+        for (int a = 0; a < 3; ++a) u2[a] /= nn;
+    }
+    double u3[3] = {u1[1] * u2[2] - u1[2] * u2[1], u1[2] * u2[0] - u1[0] * u2[2],
+                    u1[0] * u2[1] - u1[1] * u2[0]};
+    double v3[3] = {v1[1] * v2[2] - v1[2] * v2[1], v1[2] * v2[0] - v1[0] * v2[2],
+                    v1[0] * v2[1] - v1[1] * v2[0]};
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) R[a][b] = u1[a] * v1[b] + u2[a] * v2[b] + u3[a] * v3[b];
+}
+
+// ------------------------------------------------------------------ a1 local step ---------
+// One thread per tet.  Reads tet (int4), x (double4 per vertex, L2-resident gather),
+// B (SoA [9][T]), A (SoA [6][T]), w; writes the per-corner elastic forces
+// f_{i,c} = w_i (F_i - P_i) g_{i,c} as fc[T][4][3] (coalesced 96 B per tet) and, when
+// p != nullptr, p_i = vec(R_i A_i) (SoA [9][T]) for the parity hook.
+__global__ void __launch_bounds__(128) k_local_step(
+    const int4 *__restrict__ tets, const double4 *__restrict__ x, const double *__restrict__ B,
+    const double *__restrict__ A6, const double *__restrict__ w, int T, double *__restrict__ fc,
+    double *__restrict__ p) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= T) return;
+    const int4 tv = tets[t];
+    const double4 x0 = x[tv.x], x1 = x[tv.y], x2 = x[tv.z], x3 = x[tv.w];
+    double Bm[3][3];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) Bm[k / 3][k % 3] = __ldg(B + (size_t)k * T + t);
+    const double a00 = __ldg(A6 + t), a01 = __ldg(A6 + (size_t)T + t), a02 = __ldg(A6 + 2 * (size_t)T + t),
+                 a11 = __ldg(A6 + 3 * (size_t)T + t), a12 = __ldg(A6 + 4 * (size_t)T + t),
+                 a22 = __ldg(A6 + 5 * (size_t)T + t);
+    const double A[3][3] = {{a00, a01, a02}, {a01, a11, a12}, {a02, a12, a22}};
+    const double wt = __ldg(w + t);
+    // D_s = [x1-x0, x2-x0, x3-x0] (columns); F = D_s B
+    const double Ds[3][3] = {{x1.x - x0.x, x2.x - x0.x, x3.x - x0.x},
+                             {x1.y - x0.y, x2.y - x0.y, x3.y - x0.y},
+                             {x1.z - x0.z, x2.z - x0.z, x3.z - x0.z}};
+    double F[3][3], M[3][3], R[3][3], P[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) F[a][b] = Ds[a][0] * Bm[0][b] + Ds[a][1] * Bm[1][b] + Ds[a][2] * Bm[2][b];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) M[a][b] = F[a][0] * A[0][b] + F[a][1] * A[1][b] + F[a][2] * A[2][b];
+    polar_rotation(M, R);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) P[a][b] = R[a][0] * A[0][b] + R[a][1] * A[1][b] + R[a][2] * A[2][b];
+    if (p) {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) p[(size_t)k * T + t] = P[k / 3][k % 3];
+    }
+    // r = w (F - P);  f_c = r g_c, g_c = row c-1 of B (c = 1..3), f_0 = -(f_1 + f_2 + f_3)
+    double r[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) r[a][b] = wt * (F[a][b] - P[a][b]);
+    double f[4][3];
+#pragma unroll
+    for (int c = 1; c < 4; ++c)
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+            f[c][a] = r[a][0] * Bm[c - 1][0] + r[a][1] * Bm[c - 1][1] + r[a][2] * Bm[c - 1][2];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) f[0][a] = -(f[1][a] + f[2][a] + f[3][a]);
+    double2 *o = reinterpret_cast<double2 *>(fc + 12 * (size_t)t);
+    o[0] = make_double2(f[0][0], f[0][1]);
+    o[1] = make_double2(f[0][2], f[1][0]);
+    o[2] = make_double2(f[1][1], f[1][2]);
+    o[3] = make_double2(f[2][0], f[2][1]);
+    o[4] = make_double2(f[2][2], f[3][0]);
+    o[5] = make_double2(f[3][1], f[3][2]);
+}
+
+// ------------------------------------------------------------------ a2 gather -------------
+// g_el[q] = sum over incidences (t, c) of vertex q2v[q] of f_{t,c}: transpose-CSR gather in
+// factor order, deterministic, no atomics.  Output double4 [nf] (w = 0).
+__global__ void k_gather_elastic(const int *__restrict__ inc_ptr, const int *__restrict__ inc,
+                                 const double *__restrict__ fc, int nf, double4 *__restrict__ g) {
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nf) return;
+    double gx = 0, gy = 0, gz = 0;
+    for (int k = __ldg(inc_ptr + q); k < __ldg(inc_ptr + q + 1); ++k) {
+        int tc = __ldg(inc + k);
+        const double *f = fc + 12 * (size_t)(tc >> 2) + 3 * (tc & 3);
+        gx += f[0];
+        gy += f[1];
+        gz += f[2];
+    }
+    g[q] = make_double4(gx, gy, gz, 0.0);
+}
+
+// ------------------------------------------------------------------ a3 s = W x ------------
+__global__ void k_surface(const int *__restrict__ Wp, const int *__restrict__ Wc,
+                          const double *__restrict__ Wv, const double4 *__restrict__ x, int Ns,
+                          double4 *__restrict__ s) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= Ns) return;
+    double sx = 0, sy = 0, sz = 0;
+    for (int k = Wp[j]; k < Wp[j + 1]; ++k) {
+        double wv = Wv[k];
+        double4 xv = x[Wc[k]];
+        sx += wv * xv.x;
+        sy += wv * xv.y;
+        sz += wv * xv.z;
+    }
+    s[j] = make_double4(sx, sy, sz, 0.0);
+}
+
+// ds = W dx (dx given per vertex, zero on fixed)
+// (same kernel as k_surface applied to dx)
+
+// ------------------------------------------------------------------ a11 reductions ---------
+// partial[b] = sum over tets of block b of w ||D_s(dx) B||^2   (= dx^T H dx over all DOFs)
+__global__ void __launch_bounds__(256) k_quad_partials(const int4 *__restrict__ tets,
+                                                       const double4 *__restrict__ dx,
+                                                       const double *__restrict__ B,
+                                                       const double *__restrict__ w, int T,
+                                                       double *__restrict__ part) {
+    __shared__ double sh[8];
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    double v = 0.0;
+    if (t < T) {
+        const int4 tv = tets[t];
+        const double4 x0 = dx[tv.x], x1 = dx[tv.y], x2 = dx[tv.z], x3 = dx[tv.w];
+        const double Ds[3][3] = {{x1.x - x0.x, x2.x - x0.x, x3.x - x0.x},
+                                 {x1.y - x0.y, x2.y - x0.y, x3.y - x0.y},
+                                 {x1.z - x0.z, x2.z - x0.z, x3.z - x0.z}};
+        double Bm[3][3];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) Bm[k / 3][k % 3] = B[(size_t)k * T + t];
+        double acc = 0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+                double F = Ds[a][0] * Bm[0][b] + Ds[a][1] * Bm[1][b] + Ds[a][2] * Bm[2][b];
+                acc += F * F;
+            }
+        v = w[t] * acc;
+    }
+    v = block_sum<256>(v, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = v;
+}
+
+// partial[b] = sum over q of block b of g_el[q] . dx[q2v[q]]
+__global__ void __launch_bounds__(256) k_gdx_partials(const double4 *__restrict__ g,
+                                                      const double4 *__restrict__ dx,
+                                                      const int *__restrict__ q2v, int nf,
+                                                      double *__restrict__ part) {
+    __shared__ double sh[8];
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    double v = 0.0;
+    if (q < nf) {
+        double4 a = g[q], b = dx[q2v[q]];
+        v = a.x * b.x + a.y * b.y + a.z * b.z;
+    }
+    v = block_sum<256>(v, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = v;
+}
+
+// x[v] += alpha dx[v] for free v
+__global__ void k_update(double4 *__restrict__ x, const double4 *__restrict__ dx,
+                         const int *__restrict__ q2v, int nf, const double *__restrict__ alpha) {
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nf) return;
+    int v = q2v[q];
+    double a = *alpha;
+    double4 xv = x[v], d = dx[v];
+    xv.x += a * d.x;
+    xv.y += a * d.y;
+    xv.z += a * d.z;
+    x[v] = xv;
+}
+
+// scatter dx from factor order (solution of the backward solve, [nf][4], negated) to vertices
+__global__ void k_scatter_dx(const double *__restrict__ z, const int *__restrict__ q2v, int nf,
+                             double4 *__restrict__ dx) {
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nf) return;
+    const double *r = z + 4 * (size_t)q;
+    dx[q2v[q]] = make_double4(-r[0], -r[1], -r[2], 0.0);
+}
+
+// ------------------------------------------------------------------ host wrappers ---------
+void launch_ingest_actuation(const double *A9, double *A6, int T, cudaStream_t st) {
+    k_ingest_actuation<<<(T + 255) / 256, 256, 0, st>>>(A9, A6, T);
+}
+void launch_local_step(const int4 *tets, const double4 *x, const double *B, const double *A6,
+                       const double *w, int T, double *fc, double *p, cudaStream_t st) {
+    k_local_step<<<(T + 127) / 128, 128, 0, st>>>(tets, x, B, A6, w, T, fc, p);
+}
+void launch_gather_elastic(const int *inc_ptr, const int *inc, const double *fc, int nf,
+                           double4 *g, cudaStream_t st) {
+    k_gather_elastic<<<(nf + 127) / 128, 128, 0, st>>>(inc_ptr, inc, fc, nf, g);
+}
+void launch_surface(const int *Wp, const int *Wc, const double *Wv, const double4 *x, int Ns,
+                    double4 *s, cudaStream_t st) {
+    if (Ns > 0) k_surface<<<(Ns + 127) / 128, 128, 0, st>>>(Wp, Wc, Wv, x, Ns, s);
+}
+int quad_partials(const int4 *tets, const double4 *dx, const double *B, const double *w, int T,
+                  double *part, cudaStream_t st) {
+    int nb = (T + 255) / 256;
+    k_quad_partials<<<nb, 256, 0, st>>>(tets, dx, B, w, T, part);
+    return nb;
+}
+int gdx_partials(const double4 *g, const double4 *dx, const int *q2v, int nf, double *part,
+                 cudaStream_t st) {
+    int nb = (nf + 255) / 256;
+    k_gdx_partials<<<nb, 256, 0, st>>>(g, dx, q2v, nf, part);
+    return nb;
+}
+void launch_update(double4 *x, const double4 *dx, const int *q2v, int nf, const double *alpha,
+                   cudaStream_t st) {
+    k_update<<<(nf + 255) / 256, 256, 0, st>>>(x, dx, q2v, nf, alpha);
+}
+void launch_scatter_dx(const double *z, const int *q2v, int nf, double4 *dx, cudaStream_t st) {
+    k_scatter_dx<<<(nf + 255) / 256, 256, 0, st>>>(z, q2v, nf, dx);
+}
+
+}  // namespace pdipc

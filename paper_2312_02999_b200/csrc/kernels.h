@@ -1,0 +1,113 @@
+// Host-callable launchers of the CUDA kernels (internal to the library).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace pdipc {
+
+struct DevFactor {
+    int nf = 0, nsn = 0;
+    int *sn_c0 = nullptr, *sn_rowptr = nullptr, *sn_rows = nullptr, *sn_parent = nullptr;
+    long long *sn_valptr = nullptr;
+    double *L = nullptr;
+    int *seg_ptr = nullptr, *seg_d = nullptr, *seg_klo = nullptr, *seg_khi = nullptr;
+    int *sn_fd = nullptr, *col2sn = nullptr;
+};
+
+// ---- k_elastic.cu
+void launch_ingest_actuation(const double *A9, double *A6, int T, cudaStream_t st);
+void launch_local_step(const int4 *tets, const double4 *x, const double *B, const double *A6,
+                       const double *w, int T, double *fc, double *p, cudaStream_t st);
+void launch_gather_elastic(const int *inc_ptr, const int *inc, const double *fc, int nf,
+                           double4 *g, cudaStream_t st);
+void launch_surface(const int *Wp, const int *Wc, const double *Wv, const double4 *x, int Ns,
+                    double4 *s, cudaStream_t st);
+int quad_partials(const int4 *tets, const double4 *dx, const double *B, const double *w, int T,
+                  double *part, cudaStream_t st);
+int gdx_partials(const double4 *g, const double4 *dx, const int *q2v, int nf, double *part,
+                 cudaStream_t st);
+void launch_update(double4 *x, const double4 *dx, const int *q2v, int nf, const double *alpha,
+                   cudaStream_t st);
+void launch_scatter_dx(const double *z, const int *q2v, int nf, double4 *dx, cudaStream_t st);
+
+// ---- k_trisolve.cu
+void launch_ts_items(const int *sn_c0, const int *sn_fd, const int *sn_parent, int nsn,
+                     const int *qS, const int *nS_ptr, int *lo, int *hi, int *cnt, int *rem,
+                     cudaStream_t st);
+void launch_forward_solve(const DevFactor &F, const int *lo, const int *hi, const int *item_ptr,
+                          const int *qS, int *rem, int *ticket, double *G, double *V, int ldv,
+                          int nsm, cudaStream_t st);
+void launch_backward_solve(const DevFactor &F, int *done, int *ticket, double *Z, int nsm,
+                           cudaStream_t st);
+void launch_panel_yS(const int *qS, const int *nS_ptr, int nS_host, const DevFactor &F,
+                     const double *V, int ldv, const double *G, double *yS, cudaStream_t st);
+void launch_panel_correct(const DevFactor &F, const int *lo, const int *hi, const double *V,
+                          int ldv, const double *G, const double *t, double *Z, cudaStream_t st);
+void launch_panel_syrk(const DevFactor &F, const int *lo, const int *hi, const double *V, int ldv,
+                       const int *nS_ptr, int nS_host, double *K, int ldk, cudaStream_t st);
+
+// ---- k_dense.cu
+void dense_init();
+void dense_potrf(double *A, int ld, int m, double *T, int *info, cudaStream_t st);
+void dense_spd_inverse(double *A, int ld, int m, double *U, double *T, int *info, cudaStream_t st);
+void dense_negate(double *A, int ld, int m, cudaStream_t st);
+void launch_assemble_sigma_hat(const double *Sig, int lds, const double *Bc, int ldb, double *Sh,
+                               int ldh, int nS, cudaStream_t st);
+void launch_kron_matvec(const double *Sig, int lds, int nS, const double *x, double *y,
+                        cudaStream_t st);
+void launch_matvec(const double *M, int ldm, int n, const double *x, double *y, cudaStream_t st);
+void launch_chol_solve(const double *L, int ld, int n, const double *b, double *u, cudaStream_t st);
+
+// ---- k_contact.cu
+void contact_init();
+void launch_boxes(const double4 *s, const double4 *ds, const int *tris, const int *edges, int Ns,
+                  int Nt, int Ne, double infl, double4 *lo, double4 *hi, double *ext,
+                  cudaStream_t st);
+void launch_hash_insert(const double4 *lo, const double4 *hi, int b0, int nb, const double *cell,
+                        unsigned mask, int *cnt, const int *start, int *entries, cudaStream_t st);
+void launch_hash_query(const double4 *lo, const double4 *hi, int a0, int na, int b0, int nB,
+                       const double *cell, unsigned mask, const int *start, const int *entries,
+                       int is_pt, const int *tris, const int *edges, unsigned long long *out,
+                       int *count, int cap, cudaStream_t st);
+void launch_narrow(const unsigned long long *keys, int n, int is_pt, int nB, const double4 *s,
+                   const int *tris, const int *edges, int Nt, int Ne, double dh2, int *flag,
+                   int *type, double *d2, cudaStream_t st);
+void launch_compact_active(const unsigned long long *keys, int n, const int *flag, const int *pos,
+                           const int *type, const double *d2, int base, unsigned long long *akeys,
+                           int *atype, double *ad2, cudaStream_t st);
+void launch_pair_derivs(const unsigned long long *akeys, const int *atype, const double *ad2,
+                        int n_pt, int n_all, const double4 *s, const int *tris, const int *edges,
+                        int Nt, int Ne, double dh, double kappa, double *grad, double *Hp,
+                        double *dist, int *ids, cudaStream_t st);
+void launch_mark_S(const int *ids, int n_all, const int *Wp, const int *Wc, const int *v2q,
+                   int *mark, cudaStream_t st);
+void launch_compact_S(const int *mark, const int *pos, int nf, int *qS, cudaStream_t st);
+void launch_grad_records(const int *ids, int n_all, int sh, unsigned long long *rec,
+                         cudaStream_t st);
+void launch_grad_reduce(const unsigned long long *rec, int n, int sh, const double *grad,
+                        double4 *gs, cudaStream_t st);
+void launch_grad_pullback(const double4 *g_el, const int *WTp, const int *WTr, const double *WTv,
+                          const double4 *gs, int nf, double *G, cudaStream_t st);
+void launch_bc_count(const int *ids, int n_all, const int *Wp, const int *Wc, const int *v2q,
+                     int *cnt, cudaStream_t st);
+void launch_bc_records(const int *ids, int n_all, const int *Wp, const int *Wc, const int *v2q,
+                       const int *sidx, int nS, int sh, const int *off, unsigned long long *rec,
+                       cudaStream_t st);
+void launch_bc_reduce(const unsigned long long *rec, int n, int sh, int nS, const int *ids,
+                      const int *Wp, const double *Wv, const double *Hp, double *Bc, int ldb,
+                      cudaStream_t st);
+void launch_zero_square(double *M, int ld, int n, cudaStream_t st);
+void launch_accd(const unsigned long long *keys, int n, int is_pt, int nB, const double4 *s,
+                 const int *tris, const int *edges, int Nt, int Ne, const double4 *ds, double s_gap,
+                 int max_iters, double *amin, cudaStream_t st);
+void launch_ls_b0(const unsigned long long *keys, int n, int is_pt, int nB, const double4 *s,
+                  const int *tris, const int *edges, int Nt, int Ne, double dh, double *b0,
+                  cudaStream_t st);
+int launch_ls_trials(const unsigned long long *keys, int n, int is_pt, int nB, const double4 *s,
+                     const int *tris, const int *edges, int Nt, int Ne, const double4 *ds,
+                     double dh, const double *b0, const double *ls, int h0, double *part,
+                     int part_ld, cudaStream_t st);
+void launch_ls_decide(const double *part, int part_ld, int npart, const double *scal, double kappa,
+                      int h0, int hmax, double *ls, double *out, cudaStream_t st);
+
+}  // namespace pdipc

@@ -1,0 +1,212 @@
+// Device-wide primitives used by the contact pipeline: exclusive scan, LSD radix sort of
+// 64-bit keys, unique.  Hand-written (no CUB); deterministic for a given input.
+#include "prims.h"
+
+#include "dev_common.cuh"
+
+namespace pdipc {
+
+// ----------------------------------------------------------------------- exclusive scan ----
+constexpr int kScanNT = 1024, kScanIPT = 4, kScanTile = kScanNT * kScanIPT;
+
+template <int NT>
+__device__ int block_exclusive_scan(int v, int *sh, int *total) {
+    // warp inclusive scan
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) sh[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        int s = lane < NT / 32 ? sh[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        if (lane < NT / 32) sh[lane] = s;
+    }
+    __syncthreads();
+    int base = wid > 0 ? sh[wid - 1] : 0;
+    if (total) *total = sh[NT / 32 - 1];
+    __syncthreads();
+    return base + x - v;
+}
+
+__global__ void __launch_bounds__(kScanNT) k_scan_partials(const int *in, int n, int *part) {
+    __shared__ int sh[32];
+    int base = blockIdx.x * kScanTile + threadIdx.x * kScanIPT;
+    int s = 0;
+#pragma unroll
+    for (int i = 0; i < kScanIPT; ++i) s += (base + i < n) ? in[base + i] : 0;
+    int tot;
+    block_exclusive_scan<kScanNT>(s, sh, &tot);
+    if (threadIdx.x == 0) part[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kScanNT) k_scan_tiles(const int *in, int n, int *out,
+                                                        const int *part, int nparts) {
+    __shared__ int sh[32];
+    __shared__ int off;
+    if (threadIdx.x == 0) {
+        int o = 0;
+        for (int b = 0; b < (int)blockIdx.x; ++b) o += part[b];   // nparts is small
+        off = o;
+    }
+    __syncthreads();
+    int base = blockIdx.x * kScanTile + threadIdx.x * kScanIPT;
+    int v[kScanIPT];
+    int s = 0;
+#pragma unroll
+    for (int i = 0; i < kScanIPT; ++i) {
+        v[i] = (base + i < n) ? in[base + i] : 0;
+        s += v[i];
+    }
+    int tot;
+    int ex = block_exclusive_scan<kScanNT>(s, sh, &tot) + off;
+#pragma unroll
+    for (int i = 0; i < kScanIPT; ++i) {
+        if (base + i < n) out[base + i] = ex;
+        ex += v[i];
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == kScanNT - 1) out[n] = ex;
+    (void)nparts;
+}
+
+void scan_exclusive(const int *in, int *out, int n, int *scratch, cudaStream_t st) {
+    if (n <= 0) {
+        cudaMemsetAsync(out, 0, sizeof(int), st);
+        return;
+    }
+    int nb = (n + kScanTile - 1) / kScanTile;
+    k_scan_partials<<<nb, kScanNT, 0, st>>>(in, n, scratch);
+    k_scan_tiles<<<nb, kScanNT, 0, st>>>(in, n, out, scratch, nb);
+}
+
+int scan_scratch_ints(int n) { return (n + kScanTile - 1) / kScanTile + 1; }
+
+// ----------------------------------------------------------------------- radix sort -------
+constexpr int kRsNT = 256, kRsIPT = 16, kRsTile = kRsNT * kRsIPT, kRsWarps = kRsNT / 32;
+
+__global__ void __launch_bounds__(kRsNT) k_rs_hist(const uint64_t *keys, int n, int shift,
+                                                   int *hist, int nblocks) {
+    __shared__ int h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const int base = blockIdx.x * kRsTile;
+#pragma unroll 4
+    for (int i = 0; i < kRsIPT; ++i) {
+        int idx = base + i * kRsNT + threadIdx.x;
+        if (idx < n) atomicAdd(&h[(int)((keys[idx] >> shift) & 255u)], 1);
+    }
+    __syncthreads();
+    hist[threadIdx.x * nblocks + blockIdx.x] = h[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(kRsNT) k_rs_scatter(const uint64_t *in, uint64_t *out, int n,
+                                                      int shift, const int *offs, int nblocks) {
+    __shared__ int base[256];
+    __shared__ int wcnt[kRsWarps][256];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    base[tid] = offs[tid * nblocks + blockIdx.x];
+    const unsigned lt = (1u << lane) - 1u;
+    const int tb = blockIdx.x * kRsTile;
+    for (int i = 0; i < kRsIPT; ++i) {
+        int idx = tb + i * kRsNT + tid;
+        bool valid = idx < n;
+        uint64_t k = valid ? in[idx] : 0;
+        int d = valid ? (int)((k >> shift) & 255u) : 256 + lane;
+#pragma unroll
+        for (int w = 0; w < kRsWarps; ++w) wcnt[w][tid] = 0;
+        __syncthreads();
+        unsigned peers = __match_any_sync(0xffffffffu, d);
+        int rank = __popc(peers & lt);
+        if (valid && rank == 0) wcnt[wid][d] = __popc(peers);
+        __syncthreads();
+        {
+            int run = base[tid];
+#pragma unroll
+            for (int w = 0; w < kRsWarps; ++w) {
+                int c = wcnt[w][tid];
+                wcnt[w][tid] = run;
+                run += c;
+            }
+            base[tid] = run;
+        }
+        __syncthreads();
+        if (valid) out[wcnt[wid][d] + rank] = k;
+        __syncthreads();
+    }
+}
+
+int radix_scratch_ints(int nmax) {
+    int nb = (nmax + kRsTile - 1) / kRsTile;
+    if (nb < 1) nb = 1;
+    return 2 * 256 * nb + 1 + scan_scratch_ints(256 * nb);
+}
+
+// Sorts keys[0..n) ascending by their low `bits` bits (higher bits must be zero or are
+// ignored); result in keys.  tmp: n uint64; scratch: radix_scratch_ints(n) ints.
+void radix_sort_u64(uint64_t *keys, uint64_t *tmp, int n, int bits, int *scratch,
+                    cudaStream_t st) {
+    if (n <= 1 || bits <= 0) return;
+    int nb = (n + kRsTile - 1) / kRsTile;
+    int *hist = scratch;
+    int *offs = scratch + 256 * nb;
+    int *sscr = offs + 256 * nb + 1;
+    uint64_t *src = keys, *dst = tmp;
+    int passes = (bits + 7) / 8;
+    for (int p = 0; p < passes; ++p) {
+        int shift = 8 * p;
+        k_rs_hist<<<nb, kRsNT, 0, st>>>(src, n, shift, hist, nb);
+        scan_exclusive(hist, offs, 256 * nb, sscr, st);
+        k_rs_scatter<<<nb, kRsNT, 0, st>>>(src, dst, n, shift, offs, nb);
+        uint64_t *t = src;
+        src = dst;
+        dst = t;
+    }
+    if (src != keys) cudaMemcpyAsync(keys, src, sizeof(uint64_t) * n, cudaMemcpyDeviceToDevice, st);
+}
+
+// ----------------------------------------------------------------------- unique -----------
+__global__ void k_unique_flags(const uint64_t *k, int n, int *flag) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) flag[i] = (i == 0 || k[i] != k[i - 1]) ? 1 : 0;
+}
+
+__global__ void k_unique_write(const uint64_t *k, int n, const int *pos, uint64_t *out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && (i == 0 || k[i] != k[i - 1])) out[pos[i]] = k[i];
+}
+
+void unique_sorted_u64(const uint64_t *keys, int n, uint64_t *out, int *flags, int *pos,
+                       int *scratch, cudaStream_t st) {
+    if (n <= 0) {
+        cudaMemsetAsync(pos, 0, sizeof(int), st);
+        return;
+    }
+    int nb = (n + 255) / 256;
+    k_unique_flags<<<nb, 256, 0, st>>>(keys, n, flags);
+    scan_exclusive(flags, pos, n, scratch, st);
+    k_unique_write<<<nb, 256, 0, st>>>(keys, n, pos, out);
+}
+
+// ----------------------------------------------------------------------- reductions -------
+__global__ void k_sum_partials(const double *part, int n, double *out) {
+    // one block, fixed order: deterministic
+    __shared__ double sh[32];
+    double s = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
+    s = block_sum<1024>(s, sh);
+    if (threadIdx.x == 0) *out = s;
+}
+
+void sum_partials(const double *part, int n, double *out, cudaStream_t st) {
+    k_sum_partials<<<1, 1024, 0, st>>>(part, n, out);
+}
+
+}  // namespace pdipc

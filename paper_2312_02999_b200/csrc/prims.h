@@ -1,0 +1,18 @@
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace pdipc {
+// out[0..n] : exclusive scan of in[0..n), out[n] = total.  scratch: scan_scratch_ints(n).
+void scan_exclusive(const int *in, int *out, int n, int *scratch, cudaStream_t st);
+int scan_scratch_ints(int n);
+// ascending LSD radix sort of the low `bits` bits; tmp: n keys; scratch: radix_scratch_ints(n)
+void radix_sort_u64(uint64_t *keys, uint64_t *tmp, int n, int bits, int *scratch,
+                    cudaStream_t st);
+int radix_scratch_ints(int nmax);
+// out = unique(keys) for sorted keys; count at pos[n]; flags, pos: n+1 ints
+void unique_sorted_u64(const uint64_t *keys, int n, uint64_t *out, int *flags, int *pos,
+                       int *scratch, cudaStream_t st);
+// *out = sum(part[0..n)) in a fixed order (one block)
+void sum_partials(const double *part, int n, double *out, cudaStream_t st);
+}  // namespace pdipc

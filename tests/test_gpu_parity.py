@@ -1,0 +1,142 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same inputs.
+
+Tolerances (north_star): C and S bit-exact as sorted int lists on identical x;
+p_i within 1e-5 relative; g-hat 1e-10; dx (lockstep) 1e-8 relative; alpha_m 1e-10 or a logged
+discrete flip; positions after N free-running iterations within 1e-5 x bbox diagonal.
+"""
+import numpy as np
+import pytest
+
+import scenes
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2312_02999_b200 import pd_ipc
+    return pd_ipc
+
+
+@pytest.fixture(scope="module")
+def c1_oracle():
+    from oracle import OracleSolver
+    sc = scenes.slabs_c1()
+    o = OracleSolver(sc)
+    log = []
+    o.run_frame(sc.rest.copy(), sc.actuation(0), sc.n_iters, log)
+    return sc, o, log
+
+
+def _rel(a, b):
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+def test_local_step_projections_c1(P):
+    from oracle import build_mesh
+    from oracle.local import local_step
+    sc = scenes.slabs_c1()
+    s = P.Solver(sc)
+    P.set_debug(s.h, 1)
+    rng = np.random.default_rng(3)
+    x = sc.rest.copy()
+    free = np.setdiff1d(np.arange(sc.n_verts), sc.fixed)
+    x[free] += 0.05 * sc.h * rng.standard_normal((free.size, 3))
+    P.set_positions(s.h, x)
+    s.step(n_iters=1)
+    p_gpu = P.get_projections(s.h, sc.n_tets)
+    p_ref = local_step(build_mesh(sc), x, sc.actuation(0))
+    rel = np.abs(p_gpu - p_ref).max(axis=1) / np.abs(p_ref).max(axis=1)
+    assert rel.max() < 1e-5, rel.max()
+    assert rel.max() < 1e-11           # expected FP64 agreement
+    s.close()
+
+
+def test_pure_pd_box(P):
+    from oracle import OracleSolver
+    sc = scenes.box_c5("10k")
+    o = OracleSolver(sc)
+    s = P.Solver(sc)
+    P.set_debug(s.h, 1)
+    x = sc.rest.copy()
+    for it in range(3):
+        ref = o.iterate(x, sc.actuation(0))
+        P.set_positions(s.h, x)
+        st = s.step(n_iters=1)[0]
+        dx = P.get_vector(s.h, sc.n_verts, 1)
+        assert _rel(dx, ref["dx"]) < 1e-8
+        assert st["alpha"] == 1.0 and st["alpha_max"] == 1.0
+        x = ref["x"]
+    s.close()
+
+
+def test_c1_lockstep(P, c1_oracle):
+    sc, o, log = c1_oracle
+    s = P.Solver(sc)
+    P.set_debug(s.h, 1)
+    x = sc.rest.copy()
+    flips = []
+    for k, ref in enumerate(log):
+        P.set_positions(s.h, x)
+        st = s.step(n_iters=1)[0]
+        pt, ee, S = P.get_contacts(s.h)
+        rpt = np.stack([ref["C"]["pt"][0], ref["C"]["pt"][1]], 1) if ref["n_pt"] else np.zeros((0, 2))
+        ree = np.stack([ref["C"]["ee"][0], ref["C"]["ee"][1]], 1) if ref["n_ee"] else np.zeros((0, 2))
+        assert np.array_equal(pt, rpt), f"iteration {k}: PT set differs"
+        assert np.array_equal(ee, ree), f"iteration {k}: EE set differs"
+        assert np.array_equal(S, ref["S"]), f"iteration {k}: S differs"
+        g = P.get_vector(s.h, sc.n_verts, 0)
+        gref = np.zeros((sc.n_verts, 3))
+        gref[o.mesh.free] = ref["ghat"].reshape(-1, 3)
+        assert _rel(g, gref) < 1e-10, (k, _rel(g, gref))
+        dx = P.get_vector(s.h, sc.n_verts, 1)
+        assert _rel(dx, ref["dx"]) < 1e-8, (k, _rel(dx, ref["dx"]))
+        if abs(st["alpha_max"] - ref["alpha_m"]) > 1e-10 * ref["alpha_m"]:
+            flips.append((k, "alpha_m", st["alpha_max"], ref["alpha_m"]))
+        if st["alpha"] != ref["alpha"]:
+            flips.append((k, "alpha", st["alpha"], ref["alpha"]))
+        xg = s.positions()
+        if not flips:
+            assert np.abs(xg - ref["x"]).max() < 1e-9 * sc.bbox_diag()
+        x = ref["x"]
+    assert len(flips) <= 2, flips
+    s.close()
+
+
+def test_c1_free_running(P, c1_oracle):
+    sc, o, log = c1_oracle
+    s = P.Solver(sc)
+    stats = s.step(n_iters=sc.n_iters)[0]
+    xg = s.positions()
+    err = np.abs(xg - log[-1]["x"]).max()
+    assert err <= 1e-5 * sc.bbox_diag(), err
+    assert stats["flags"] == 0
+    s.close()
+
+
+def test_face_small_lockstep(P):
+    from oracle import OracleSolver
+    sc = scenes.face_small(n_frames=2)
+    o = OracleSolver(sc)
+    A = sc.actuation(1) * 0 + np.tile(np.eye(3).reshape(1, 9), (sc.n_tets, 1))
+    A[:, 4] += 0.5 * sc.meta["lip_mask"]          # full lip actuation at once (App. A.13)
+    s = P.Solver(sc, A=A[None])
+    P.set_debug(s.h, 1)
+    x = sc.rest.copy()
+    seen_contact = False
+    for k in range(8):
+        ref = o.iterate(x, A)
+        P.set_positions(s.h, x)
+        st = s.step(n_iters=1)[0]
+        pt, ee, S = P.get_contacts(s.h)
+        assert pt.shape[0] == ref["n_pt"] and ee.shape[0] == ref["n_ee"]
+        assert np.array_equal(S, ref["S"])
+        seen_contact |= ref["n_pt"] + ref["n_ee"] > 0
+        dx = P.get_vector(s.h, sc.n_verts, 1)
+        assert _rel(dx, ref["dx"]) < 1e-8, (k, _rel(dx, ref["dx"]))
+        x = ref["x"]
+    assert seen_contact
+    s.close()
