@@ -147,6 +147,17 @@ int pd_ipc_set_debug(pd_ipc *h, int32_t level);
 int pd_ipc_debug_factor_solve(const pd_ipc_mesh *mesh, const double *rest_pos, const double *b,
                               double *x, int64_t *stats);
 
+/* Device timing of kernel groups (CUDA events on the library stream around each group, every
+ * iteration; on = 1 enables).  pd_ipc_kernel_times copies the accumulated milliseconds and
+ * launch counts of the K groups (returns K) into ms[K], counts[K] (either may be NULL) and
+ * resets them if reset != 0; pd_ipc_kernel_name(i) names group i (0 = "local_step"). */
+int pd_ipc_set_timing(pd_ipc *h, int32_t on);
+int pd_ipc_kernel_times(pd_ipc *h, double *ms, int64_t *counts, int32_t reset);
+const char *pd_ipc_kernel_name(int32_t id);
+
+/* Number of CUDA kernels this library has launched in the process so far. */
+int64_t pd_ipc_launch_count(void);
+
 /* Library build identification (for the bench record). */
 const char *pd_ipc_build_info(void);
 

@@ -5,6 +5,12 @@
 
 namespace pdipc {
 
+// Every kernel launch of the library goes through PDI_LAUNCH so that the number of our
+// kernels launched inside a timed region can be reported (bench.py "gpu_launches").
+void note_launch();
+long long launch_count();
+#define PDI_LAUNCH(kern, ...) ::pdipc::note_launch(), kern<<<__VA_ARGS__>>>
+
 constexpr int kWarp = 32;
 
 __device__ __forceinline__ double warp_sum(double v) {

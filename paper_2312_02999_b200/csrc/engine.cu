@@ -94,6 +94,40 @@ struct StageTimer {
     void destroy() { for (auto &e : ev) cudaEventDestroy(e); }
 };
 
+// Per-kernel-group device timing (CUDA events on the library stream), for the roofline report.
+enum KId { K_LOCAL = 0, K_GATHER, K_BROAD, K_NARROW, K_DERIV, K_ASSEMBLY, K_FWD, K_DENSE, K_BWD,
+           K_CCD, K_LS, K_NUM };
+static const char *kKernelNames[K_NUM] = {"local_step", "gather", "broad_phase", "narrow_phase",
+                                          "pair_derivatives", "contact_assembly", "forward_solve",
+                                          "dense_schur", "backward_solve", "ccd", "line_search"};
+struct KTimer {
+    bool on = false;
+    cudaEvent_t ev[K_NUM][2];
+    bool used[K_NUM] = {};
+    double ms[K_NUM] = {};
+    long long cnt[K_NUM] = {};
+    void init() {
+        for (int k = 0; k < K_NUM; ++k) { CK(cudaEventCreate(&ev[k][0])); CK(cudaEventCreate(&ev[k][1])); }
+    }
+    void destroy() {
+        for (int k = 0; k < K_NUM; ++k) { cudaEventDestroy(ev[k][0]); cudaEventDestroy(ev[k][1]); }
+    }
+    void start(int k, cudaStream_t st) { if (on) CK(cudaEventRecord(ev[k][0], st)); }
+    void stop(int k, cudaStream_t st) {
+        if (on) { CK(cudaEventRecord(ev[k][1], st)); used[k] = true; }
+    }
+    void collect() {     // after a stream synchronize
+        for (int k = 0; k < K_NUM; ++k)
+            if (used[k]) {
+                float f;
+                CK(cudaEventElapsedTime(&f, ev[k][0], ev[k][1]));
+                ms[k] += f;
+                cnt[k] += 1;
+                used[k] = false;
+            }
+    }
+};
+
 }  // namespace pdipc
 
 using namespace pdipc;
@@ -119,8 +153,9 @@ struct pd_ipc {
     // factor
     DevFactor F;
     DBuf<int> f_c0, f_rowptr, f_rows, f_parent, f_seg_ptr, f_seg_d, f_seg_klo, f_seg_khi, f_fd, f_col2sn;
-    DBuf<long long> f_valptr;
-    DBuf<double> f_L;
+    DBuf<long long> f_valptr, f_dinv_ptr;
+    DBuf<double> f_L, f_dinv, Ug, Up;
+    DBuf<int> f_uoff, f_urow_sn, f_rc_ptr, f_rc_idx, f_urel, f_ch_ptr, f_ch;
     // sequences
     std::vector<std::unique_ptr<Seq>> seqs;
     // work buffers
@@ -140,6 +175,10 @@ struct pd_ipc {
     DBuf<double> dscal;     // [0]=ext cell, [1]=amin, [2..4]=ls, [5..8]=ls_out, [9..10]=scal
     DBuf<int> dint;         // [0..3] counts, [4] info
     StageTimer tm;
+    KTimer kt;
+    // debugging aid: PDIPC_TRACE=<file> appends per-item forward-solve timestamps
+    FILE *trace_file = nullptr;
+    DBuf<unsigned long long> trace;
 };
 
 static thread_local std::string g_last_error;
@@ -247,20 +286,28 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
     auto &ev = h->tm.ev;
     CK(cudaEventRecord(ev[0], st));
     // ---------------- Misc: a1 local step + a2 gather
+    KTimer &kt = h->kt;
+    kt.start(K_LOCAL, st);
     launch_local_step(h->tets.p, q.x.p, h->B.p, q.A6.p, h->w.p, T, h->fc.p,
                       h->debug ? q.p.p : nullptr, st);
+    kt.stop(K_LOCAL, st);
+    kt.start(K_GATHER, st);
     launch_gather_elastic(h->inc_ptr.p, h->inc.p, h->fc.p, nf, h->g_el.p, st);
+    kt.stop(K_GATHER, st);
     CK(cudaEventRecord(ev[1], st));
     // ---------------- IPC
     int n_pt = 0, n_ee = 0, nS = 0, n_cand = 0;
     double min_dist = 0.0;
     int *nS_dev = h->spos.p + nf;     // exclusive scan total of the S marks
     if (Nt > 0) {
+        kt.start(K_BROAD, st);
         launch_surface(h->Wp.p, h->Wc.p, h->Wv.p, q.x.p, Ns, h->s.p, st);
         int cpt, cee;
         broad_phase(h, nullptr, 0.5 * h->dh * 1.01, &cpt, &cee);
+        kt.stop(K_BROAD, st);
         n_cand = cpt + cee;
         ensure_pair_buffers(h, n_cand);
+        kt.start(K_NARROW, st);
         launch_narrow(h->cand.p, cpt, 1, Nt, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->dh2, h->flag.p,
                       h->ctype.p, h->cd2.p, st);
         launch_narrow(h->cand.p + cpt, cee, 0, Ne, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->dh2,
@@ -288,8 +335,12 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
         h->Hp.ensure(78 * (size_t)na + 78);
         h->dist.ensure(na + 1);
         h->ids.ensure(4 * (size_t)na + 4);
+        kt.stop(K_NARROW, st);
+        kt.start(K_DERIV, st);
         launch_pair_derivs(h->akeys.p, h->atype.p, h->ad2.p, n_pt, na, h->s.p, h->tris.p, h->edges.p, Nt,
                            Ne, h->dh, h->kappa, h->grad.p, h->Hp.p, h->dist.p, h->ids.p, st);
+        kt.stop(K_DERIV, st);
+        kt.start(K_ASSEMBLY, st);
         // S
         CK(cudaMemsetAsync(h->mark.p, 0, sizeof(int) * nf, st));
         launch_mark_S(h->ids.p, na, h->Wp.p, h->Wc.p, h->v2q.p, h->mark.p, st);
@@ -336,6 +387,7 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
             launch_zero_square(h->Bc.p, ldb, 3 * nS, st);
             launch_bc_reduce(h->rec.p, nrec, sh, nS, h->ids.p, h->Wp.p, h->Wv.p, h->Hp.p, h->Bc.p, ldb, st);
         }
+        kt.stop(K_ASSEMBLY, st);
     } else {
         CK(cudaMemsetAsync(nS_dev, 0, sizeof(int), st));
         launch_grad_pullback(h->g_el.p, h->WTp.p, h->WTr.p, h->WTv.p, nullptr, nf, h->G.p, st);
@@ -373,11 +425,27 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
     // ---------------- G-Step
     const DevFactor &F = h->F;
     CK(cudaMemsetAsync(h->ticket.p, 0, 2 * sizeof(int), st));
+    kt.start(K_FWD, st);
     launch_ts_items(F.sn_c0, F.sn_fd, F.sn_parent, F.nsn, h->qS.p, nS_dev, h->ts_lo.p, h->ts_hi.p,
                     h->ts_cnt.p, h->ts_rem.p, st);
     scan_exclusive(h->ts_cnt.p, h->ts_ptr.p, F.nsn, h->iscr.p, st);
+    const int ldu = std::max(32, ((nS + 31) / 32) * 32);
+    if (nS > 0) h->Up.ensure((size_t)std::max(1, F.nU) * ldu);
+    if (h->trace_file) h->trace.ensure(4 * (size_t)F.nsn * (2 + (h->capS + 31) / 32));
     launch_forward_solve(F, h->ts_lo.p, h->ts_hi.p, h->ts_ptr.p, h->qS.p, h->ts_rem.p, h->ticket.p, h->G.p,
-                         h->V.p, h->ldv, h->nsm, st);
+                         h->V.p, h->ldv, h->Ug.p, nS > 0 ? h->Up.p : nullptr, ldu, h->nsm,
+                         h->trace_file ? h->trace.p : nullptr, st);
+    if (h->trace_file && nS > 0 && std::ftell(h->trace_file) < (30l << 20)) {
+        int nitems;
+        sync_read_ints(h, &nitems, h->ts_ptr.p + F.nsn, 1);
+        std::vector<unsigned long long> tr(4 * (size_t)nitems);
+        CK(cudaMemcpy(tr.data(), h->trace.p, tr.size() * 8, cudaMemcpyDeviceToHost));
+        fwrite(&nitems, sizeof(int), 1, h->trace_file);
+        fwrite(tr.data(), 8, tr.size(), h->trace_file);
+        fflush(h->trace_file);
+    }
+    kt.stop(K_FWD, st);
+    kt.start(K_DENSE, st);
     if (nS > 0) {
         const int ldk = h->capS, m3 = 3 * nS, ldb = 3 * h->capS;
         launch_panel_yS(h->qS.p, nS_dev, nS, F, h->V.p, h->ldv, h->G.p, h->yS.p, st);
@@ -395,7 +463,10 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
     } else {
         CK(cudaMemcpyAsync(h->Z.p, h->G.p, sizeof(double) * 4 * nf, cudaMemcpyDeviceToDevice, st));
     }
+    kt.stop(K_DENSE, st);
+    kt.start(K_BWD, st);
     launch_backward_solve(F, h->ts_done.p, h->ticket.p, h->Z.p, h->nsm, st);
+    kt.stop(K_BWD, st);
     CK(cudaMemsetAsync(h->dx.p, 0, sizeof(double4) * h->n, st));
     launch_scatter_dx(h->Z.p, h->q2v.p, nf, h->dx.p, st);
     CK(cudaEventRecord(ev[3], st));
@@ -404,6 +475,7 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
     double *ls = h->dscal.p + 2, *ls_out = h->dscal.p + 5, *scal = h->dscal.p + 9;
     set_d(h, amin, 1.0);
     int spt = 0, see = 0;
+    kt.start(K_CCD, st);
     if (Nt > 0) {
         launch_surface(h->Wp.p, h->Wc.p, h->Wv.p, h->dx.p, Ns, h->ds.p, st);
         broad_phase(h, h->ds.p, h->dh, &spt, &see);
@@ -412,8 +484,10 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
         launch_accd(h->cand.p + spt, see, 0, Ne, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->ds.p,
                     h->opt.accd_s, h->opt.accd_max_iters, amin, st);
     }
+    kt.stop(K_CCD, st);
     CK(cudaEventRecord(ev[4], st));
     // ---------------- LS
+    kt.start(K_LS, st);
     {
         int nb1 = gdx_partials(h->g_el.p, h->dx.p, h->q2v.p, nf, h->part.p, st);
         sum_partials(h->part.p, nb1, scal + 0, st);
@@ -442,6 +516,7 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
         }
         launch_update(q.x.p, h->dx.p, h->q2v.p, nf, ls_out, st);
     }
+    kt.stop(K_LS, st);
     CK(cudaEventRecord(ev[5], st));
     // ---------------- stats
     double sc[11];
@@ -460,6 +535,7 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
     float tot;
     CK(cudaEventElapsedTime(&tot, ev[0], ev[5]));
     ms[5] += tot;
+    kt.collect();
     pd_ipc_stats &S = q.stats;
     S.n_cand = n_cand;
     S.n_active = n_pt + n_ee;
@@ -563,8 +639,11 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         CK(cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, o.device));
         CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
         h->tm.init();
+        h->kt.init();
+        if (const char *tp = std::getenv("PDIPC_TRACE")) h->trace_file = std::fopen(tp, "wb");
         dense_init();
         contact_init();
+        trisolve_init();
         HostMesh &m = h->hm;
         HostFactor &f = h->hf;
         h->n = m.n;
@@ -610,7 +689,23 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             h->f_valptr.upload(vp.data(), vp.size());
         }
         h->f_L.upload(f.vals.data(), f.vals.size());
+        h->f_uoff.upload(f.uoff.data(), f.uoff.size());
+        h->f_urow_sn.upload(f.urow_sn.data(), f.urow_sn.size());
+        h->f_rc_ptr.upload(f.rc_ptr.data(), f.rc_ptr.size());
+        h->f_rc_idx.upload(f.rc_idx.data(), f.rc_idx.size());
+        h->f_urel.upload(f.urel.data(), f.urel.size());
+        h->f_ch_ptr.upload(f.ch_ptr.data(), f.ch_ptr.size());
+        h->f_ch.upload(f.ch.data(), f.ch.size());
+        {
+            std::vector<long long> dp(f.dinv_ptr.begin(), f.dinv_ptr.end());
+            h->f_dinv_ptr.upload(dp.data(), dp.size());
+        }
+        h->f_dinv.upload(f.dinv.data(), f.dinv.size());
+        h->Ug.exact(4 * (size_t)std::max(1, f.uoff[f.nsn]));
         DevFactor &F = h->F;
+        F.uoff = h->f_uoff.p; F.urow_sn = h->f_urow_sn.p; F.rc_ptr = h->f_rc_ptr.p; F.rc_idx = h->f_rc_idx.p;
+        F.dinv_ptr = h->f_dinv_ptr.p; F.dinv = h->f_dinv.p; F.nU = f.uoff[f.nsn];
+        F.urel = h->f_urel.p; F.ch_ptr = h->f_ch_ptr.p; F.ch = h->f_ch.p;
         F.nf = f.nf; F.nsn = f.nsn;
         F.sn_c0 = h->f_c0.p; F.sn_rowptr = h->f_rowptr.p; F.sn_rows = h->f_rows.p; F.sn_parent = h->f_parent.p;
         F.sn_valptr = h->f_valptr.p; F.L = h->f_L.p;
@@ -755,12 +850,17 @@ void pd_ipc_destroy(pd_ipc *h) {
     cudaDeviceSynchronize();
     // DBuf members free in their own scope via release; explicit for clarity
     h->tm.destroy();
+    h->kt.destroy();
+    if (h->trace_file) std::fclose(h->trace_file);
+    h->trace.release();
     if (h->st) cudaStreamDestroy(h->st);
     auto rel = [](auto &b) { b.release(); };
     rel(h->tets); rel(h->B); rel(h->w); rel(h->inc_ptr); rel(h->inc); rel(h->q2v); rel(h->v2q);
     rel(h->Wp); rel(h->Wc); rel(h->WTp); rel(h->WTr); rel(h->tris); rel(h->edges); rel(h->Wv); rel(h->WTv);
     rel(h->f_c0); rel(h->f_rowptr); rel(h->f_rows); rel(h->f_parent); rel(h->f_seg_ptr); rel(h->f_seg_d);
     rel(h->f_seg_klo); rel(h->f_seg_khi); rel(h->f_fd); rel(h->f_col2sn); rel(h->f_valptr); rel(h->f_L);
+    rel(h->f_dinv_ptr); rel(h->f_dinv); rel(h->Ug); rel(h->Up); rel(h->f_uoff); rel(h->f_urow_sn);
+    rel(h->f_rc_ptr); rel(h->f_rc_idx); rel(h->f_urel); rel(h->f_ch_ptr); rel(h->f_ch);
     for (auto &s : h->seqs) { rel(s->x); rel(s->A6); rel(s->p); }
     rel(h->fc); rel(h->G); rel(h->Z); rel(h->A9stage); rel(h->g_el); rel(h->s); rel(h->ds); rel(h->dx);
     rel(h->gs); rel(h->blo); rel(h->bhi); rel(h->hcnt); rel(h->hstart); rel(h->hent); rel(h->cand);
@@ -861,6 +961,28 @@ const char *pd_ipc_build_info(void) {
     return "pd_ipc sm_100a build " __DATE__ " " __TIME__;
 }
 
+int pd_ipc_set_timing(pd_ipc *h, int32_t on) {
+    if (!h) return fail(nullptr, PD_IPC_E_ARG, "NULL handle");
+    h->kt.on = on != 0;
+    return PD_IPC_OK;
+}
+
+int pd_ipc_kernel_times(pd_ipc *h, double *ms, int64_t *counts, int32_t reset) {
+    if (!h) return fail(nullptr, PD_IPC_E_ARG, "NULL handle");
+    for (int k = 0; k < K_NUM; ++k) {
+        if (ms) ms[k] = h->kt.ms[k];
+        if (counts) counts[k] = h->kt.cnt[k];
+        if (reset) { h->kt.ms[k] = 0; h->kt.cnt[k] = 0; }
+    }
+    return K_NUM;
+}
+
+const char *pd_ipc_kernel_name(int32_t id) {
+    return (id >= 0 && id < K_NUM) ? kKernelNames[id] : "";
+}
+
+int64_t pd_ipc_launch_count(void) { return pdipc::launch_count(); }
+
 // Host-only debug entry (no GPU needed): runs setup + factorisation and solves L_FF x = b on
 // the host with the supernodal factor; reports factor statistics.  Used by CPU tests of the
 // setup logic.  b, x: [n_verts] (values on fixed vertices ignored / set to 0).
@@ -881,6 +1003,26 @@ int pd_ipc_debug_factor_solve(const pd_ipc_mesh *mesh, const double *rest_pos, c
         stats[1] = f.nnzL;
         stats[2] = f.max_width;
         stats[3] = f.depth;
+        int64_t maxseg = 0, segrows = 0;
+        for (int s = 0; s < f.nsn; ++s) {
+            maxseg = std::max<int64_t>(maxseg, f.seg_ptr[s + 1] - f.seg_ptr[s]);
+            for (int g = f.seg_ptr[s]; g < f.seg_ptr[s + 1]; ++g) segrows += f.seg_khi[g] - f.seg_klo[g];
+        }
+        stats[4] = (int64_t)f.seg_d.size();
+        stats[5] = maxseg;
+        stats[6] = segrows;
+        int64_t offrows = 0;
+        for (int s = 0; s < f.nsn; ++s)
+            offrows += (f.sn_rowptr[s + 1] - f.sn_rowptr[s]) - (f.sn_c0[s + 1] - f.sn_c0[s]);
+        stats[7] = offrows;
+    }
+    if (const char *dump = std::getenv("PDIPC_DUMP_SUPERNODES")) {   // debugging aid
+        if (FILE *fp = std::fopen(dump, "w")) {
+            for (int s = 0; s < f.nsn; ++s)
+                std::fprintf(fp, "%d %d %d %d %d\n", s, f.sn_c0[s], f.sn_c0[s + 1] - f.sn_c0[s],
+                             f.sn_rowptr[s + 1] - f.sn_rowptr[s], f.sn_parent[s]);
+            std::fclose(fp);
+        }
     }
     if (b && x) {
         std::vector<double> y(f.nf);

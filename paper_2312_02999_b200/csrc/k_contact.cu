@@ -801,18 +801,18 @@ void launch_boxes(const double4 *s, const double4 *ds, const int *tris, const in
                   int Nt, int Ne, double infl, double4 *lo, double4 *hi, double *ext,
                   cudaStream_t st) {
     int n = Ns + Nt + Ne;
-    k_boxes<<<(n + 255) / 256, 256, 0, st>>>(s, ds, tris, edges, Ns, Nt, Ne, infl, lo, hi, ext);
+    PDI_LAUNCH(k_boxes, (n + 255) / 256, 256, 0, st)(s, ds, tris, edges, Ns, Nt, Ne, infl, lo, hi, ext);
 }
 void launch_hash_insert(const double4 *lo, const double4 *hi, int b0, int nb, const double *cell,
                         unsigned mask, int *cnt, const int *start, int *entries, cudaStream_t st) {
-    if (nb > 0) k_hash_insert<<<(nb + 255) / 256, 256, 0, st>>>(lo, hi, b0, nb, cell, mask, cnt, start, entries);
+    if (nb > 0) PDI_LAUNCH(k_hash_insert, (nb + 255) / 256, 256, 0, st)(lo, hi, b0, nb, cell, mask, cnt, start, entries);
 }
 void launch_hash_query(const double4 *lo, const double4 *hi, int a0, int na, int b0, int nB,
                        const double *cell, unsigned mask, const int *start, const int *entries,
                        int is_pt, const int *tris, const int *edges, unsigned long long *out,
                        int *count, int cap, cudaStream_t st) {
     if (na > 0)
-        k_hash_query<<<(na + 127) / 128, 128, 0, st>>>(lo, hi, a0, na, b0, nB, cell, mask, start,
+        PDI_LAUNCH(k_hash_query, (na + 127) / 128, 128, 0, st)(lo, hi, a0, na, b0, nB, cell, mask, start,
                                                        entries, is_pt, tris, edges, out, count, cap);
 }
 void launch_narrow(const unsigned long long *keys, int n, int is_pt, int nB, const double4 *s,
@@ -820,13 +820,13 @@ void launch_narrow(const unsigned long long *keys, int n, int is_pt, int nB, con
                    int *type, double *d2, cudaStream_t st) {
     if (n <= 0) return;
     PairCtx c{s, tris, edges, Nt, Ne};
-    k_narrow<<<(n + 255) / 256, 256, 0, st>>>(keys, n, is_pt, nB, c, dh2, flag, type, d2);
+    PDI_LAUNCH(k_narrow, (n + 255) / 256, 256, 0, st)(keys, n, is_pt, nB, c, dh2, flag, type, d2);
 }
 void launch_compact_active(const unsigned long long *keys, int n, const int *flag, const int *pos,
                            const int *type, const double *d2, int base, unsigned long long *akeys,
                            int *atype, double *ad2, cudaStream_t st) {
     if (n > 0)
-        k_compact_active<<<(n + 255) / 256, 256, 0, st>>>(keys, n, flag, pos, type, d2, base, akeys, atype, ad2);
+        PDI_LAUNCH(k_compact_active, (n + 255) / 256, 256, 0, st)(keys, n, flag, pos, type, d2, base, akeys, atype, ad2);
 }
 void launch_pair_derivs(const unsigned long long *akeys, const int *atype, const double *ad2,
                         int n_pt, int n_all, const double4 *s, const int *tris, const int *edges,
@@ -834,59 +834,59 @@ void launch_pair_derivs(const unsigned long long *akeys, const int *atype, const
                         double *dist, int *ids, cudaStream_t st) {
     if (n_all <= 0) return;
     PairCtx c{s, tris, edges, Nt, Ne};
-    k_pair_derivs<<<(n_all + kPD_WARPS - 1) / kPD_WARPS, kPD_WARPS * 32, 0, st>>>(
+    PDI_LAUNCH(k_pair_derivs, (n_all + kPD_WARPS - 1) / kPD_WARPS, kPD_WARPS * 32, 0, st)(
         akeys, atype, ad2, n_pt, n_all, c, dh, kappa, grad, Hp, dist, ids);
 }
 void launch_mark_S(const int *ids, int n_all, const int *Wp, const int *Wc, const int *v2q,
                    int *mark, cudaStream_t st) {
-    if (n_all > 0) k_mark_S<<<(4 * n_all + 255) / 256, 256, 0, st>>>(ids, n_all, Wp, Wc, v2q, mark);
+    if (n_all > 0) PDI_LAUNCH(k_mark_S, (4 * n_all + 255) / 256, 256, 0, st)(ids, n_all, Wp, Wc, v2q, mark);
 }
 void launch_compact_S(const int *mark, const int *pos, int nf, int *qS, cudaStream_t st) {
-    k_compact_S<<<(nf + 255) / 256, 256, 0, st>>>(mark, pos, nf, qS);
+    PDI_LAUNCH(k_compact_S, (nf + 255) / 256, 256, 0, st)(mark, pos, nf, qS);
 }
 void launch_grad_records(const int *ids, int n_all, int sh, unsigned long long *rec,
                          cudaStream_t st) {
-    if (n_all > 0) k_grad_records<<<(4 * n_all + 255) / 256, 256, 0, st>>>(ids, n_all, sh, rec);
+    if (n_all > 0) PDI_LAUNCH(k_grad_records, (4 * n_all + 255) / 256, 256, 0, st)(ids, n_all, sh, rec);
 }
 void launch_grad_reduce(const unsigned long long *rec, int n, int sh, const double *grad,
                         double4 *gs, cudaStream_t st) {
-    if (n > 0) k_grad_reduce<<<(n + 255) / 256, 256, 0, st>>>(rec, n, sh, grad, gs);
+    if (n > 0) PDI_LAUNCH(k_grad_reduce, (n + 255) / 256, 256, 0, st)(rec, n, sh, grad, gs);
 }
 void launch_grad_pullback(const double4 *g_el, const int *WTp, const int *WTr, const double *WTv,
                           const double4 *gs, int nf, double *G, cudaStream_t st) {
-    k_grad_pullback<<<(nf + 255) / 256, 256, 0, st>>>(g_el, WTp, WTr, WTv, gs, nf, G);
+    PDI_LAUNCH(k_grad_pullback, (nf + 255) / 256, 256, 0, st)(g_el, WTp, WTr, WTv, gs, nf, G);
 }
 void launch_bc_count(const int *ids, int n_all, const int *Wp, const int *Wc, const int *v2q,
                      int *cnt, cudaStream_t st) {
-    if (n_all > 0) k_bc_count<<<(n_all + 255) / 256, 256, 0, st>>>(ids, n_all, Wp, Wc, v2q, cnt);
+    if (n_all > 0) PDI_LAUNCH(k_bc_count, (n_all + 255) / 256, 256, 0, st)(ids, n_all, Wp, Wc, v2q, cnt);
 }
 void launch_bc_records(const int *ids, int n_all, const int *Wp, const int *Wc, const int *v2q,
                        const int *sidx, int nS, int sh, const int *off, unsigned long long *rec,
                        cudaStream_t st) {
     if (n_all > 0)
-        k_bc_records<<<(n_all + 127) / 128, 128, 0, st>>>(ids, n_all, Wp, Wc, v2q, sidx, nS, sh, off, rec);
+        PDI_LAUNCH(k_bc_records, (n_all + 127) / 128, 128, 0, st)(ids, n_all, Wp, Wc, v2q, sidx, nS, sh, off, rec);
 }
 void launch_bc_reduce(const unsigned long long *rec, int n, int sh, int nS, const int *ids,
                       const int *Wp, const double *Wv, const double *Hp, double *Bc, int ldb,
                       cudaStream_t st) {
-    if (n > 0) k_bc_reduce<<<(n + 255) / 256, 256, 0, st>>>(rec, n, sh, nS, ids, Wp, Wv, Hp, Bc, ldb);
+    if (n > 0) PDI_LAUNCH(k_bc_reduce, (n + 255) / 256, 256, 0, st)(rec, n, sh, nS, ids, Wp, Wv, Hp, Bc, ldb);
 }
 void launch_zero_square(double *M, int ld, int n, cudaStream_t st) {
-    if (n > 0) k_zero_square<<<256, 256, 0, st>>>(M, ld, n);
+    if (n > 0) PDI_LAUNCH(k_zero_square, 256, 256, 0, st)(M, ld, n);
 }
 void launch_accd(const unsigned long long *keys, int n, int is_pt, int nB, const double4 *s,
                  const int *tris, const int *edges, int Nt, int Ne, const double4 *ds, double s_gap,
                  int max_iters, double *amin, cudaStream_t st) {
     if (n <= 0) return;
     PairCtx c{s, tris, edges, Nt, Ne};
-    k_accd<<<(n + 127) / 128, 128, 0, st>>>(keys, n, is_pt, nB, c, ds, s_gap, max_iters, amin);
+    PDI_LAUNCH(k_accd, (n + 127) / 128, 128, 0, st)(keys, n, is_pt, nB, c, ds, s_gap, max_iters, amin);
 }
 void launch_ls_b0(const unsigned long long *keys, int n, int is_pt, int nB, const double4 *s,
                   const int *tris, const int *edges, int Nt, int Ne, double dh, double *b0,
                   cudaStream_t st) {
     if (n <= 0) return;
     PairCtx c{s, tris, edges, Nt, Ne};
-    k_ls_b0<<<(n + 255) / 256, 256, 0, st>>>(keys, n, is_pt, nB, c, dh, b0);
+    PDI_LAUNCH(k_ls_b0, (n + 255) / 256, 256, 0, st)(keys, n, is_pt, nB, c, dh, b0);
 }
 int launch_ls_trials(const unsigned long long *keys, int n, int is_pt, int nB, const double4 *s,
                      const int *tris, const int *edges, int Nt, int Ne, const double4 *ds,
@@ -895,12 +895,12 @@ int launch_ls_trials(const unsigned long long *keys, int n, int is_pt, int nB, c
     if (n <= 0) return 0;
     PairCtx c{s, tris, edges, Nt, Ne};
     int nb = (n + 255) / 256;
-    k_ls_trials<<<nb, 256, 0, st>>>(keys, n, is_pt, nB, c, ds, dh, b0, ls, h0, part, part_ld);
+    PDI_LAUNCH(k_ls_trials, nb, 256, 0, st)(keys, n, is_pt, nB, c, ds, dh, b0, ls, h0, part, part_ld);
     return nb;
 }
 void launch_ls_decide(const double *part, int part_ld, int npart, const double *scal, double kappa,
                       int h0, int hmax, double *ls, double *out, cudaStream_t st) {
-    k_ls_decide<<<1, 1024, 0, st>>>(part, part_ld, npart, scal, kappa, h0, hmax, ls, out);
+    PDI_LAUNCH(k_ls_decide, 1, 1024, 0, st)(part, part_ld, npart, scal, kappa, h0, hmax, ls, out);
 }
 
 }  // namespace pdipc

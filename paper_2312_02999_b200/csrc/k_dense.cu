@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(1024) k_chol_solve(const double *L, int ld, in
 // ------------------------------------------------------------------ host drivers ----------
 static void tile_gemm(const TileArgs &a, int nblocks, cudaStream_t st) {
     if (nblocks <= 0) return;
-    k_tile_gemm<<<nblocks, 256, 2 * NB * SST * sizeof(double), st>>>(a);
+    PDI_LAUNCH(k_tile_gemm, nblocks, 256, 2 * NB * SST * sizeof(double), st)(a);
 }
 
 constexpr int kPotrfSmem = 2 * NB * (NB + 1) * (int)sizeof(double);
@@ -314,7 +314,7 @@ void dense_init() {
 void dense_potrf(double *A, int ld, int m, double *T, int *info, cudaStream_t st) {
     const int nt = (m + NB - 1) / NB;
     for (int k = 0; k < nt; ++k) {
-        k_tile_potrf<<<1, 256, kPotrfSmem, st>>>(A, ld, m, k, T, 0, info);
+        PDI_LAUNCH(k_tile_potrf, 1, 256, kPotrfSmem, st)(A, ld, m, k, T, 0, info);
         TileArgs a{TM_TRSM, nt, k, m, A, ld, T, nullptr};
         tile_gemm(a, nt - k - 1, st);
         a.mode = TM_POTRF_UPD;
@@ -328,12 +328,12 @@ void dense_potrf(double *A, int ld, int m, double *T, int *info, cudaStream_t st
 void dense_spd_inverse(double *A, int ld, int m, double *U, double *T, int *info, cudaStream_t st) {
     const int nt = (m + NB - 1) / NB;
     for (int k = 0; k < nt; ++k) {
-        k_tile_potrf<<<1, 256, kPotrfSmem, st>>>(A, ld, m, k, T, 1, info);
+        PDI_LAUNCH(k_tile_potrf, 1, 256, kPotrfSmem, st)(A, ld, m, k, T, 1, info);
         TileArgs a{TM_SWEEP_PANEL, nt, k, m, A, ld, T, U};
         tile_gemm(a, nt - 1, st);
         a.mode = TM_SWEEP_UPD;
         tile_gemm(a, (nt - 1) * (nt - 1), st);
-        k_sweep_finish<<<64, 256, 0, st>>>(A, ld, m, k, U, T);
+        PDI_LAUNCH(k_sweep_finish, 64, 256, 0, st)(A, ld, m, k, U, T);
     }
 }
 
@@ -345,24 +345,24 @@ __global__ void k_negate(double *A, int ld, int m) {
         A[(e / m) * ld + e % m] = -A[(e / m) * ld + e % m];
 }
 void dense_negate(double *A, int ld, int m, cudaStream_t st) {
-    k_negate<<<256, 256, 0, st>>>(A, ld, m);
+    PDI_LAUNCH(k_negate, 256, 256, 0, st)(A, ld, m);
 }
 
 void launch_assemble_sigma_hat(const double *Sig, int lds, const double *Bc, int ldb, double *Sh,
                                int ldh, int nS, cudaStream_t st) {
-    k_assemble_sigma_hat<<<512, 256, 0, st>>>(Sig, lds, Bc, ldb, Sh, ldh, nS);
+    PDI_LAUNCH(k_assemble_sigma_hat, 512, 256, 0, st)(Sig, lds, Bc, ldb, Sh, ldh, nS);
 }
 void launch_kron_matvec(const double *Sig, int lds, int nS, const double *x, double *y,
                         cudaStream_t st) {
     int rows = 3 * nS;
-    k_kron_matvec<<<(rows * 32 + 255) / 256, 256, 0, st>>>(Sig, lds, nS, x, y);
+    PDI_LAUNCH(k_kron_matvec, (rows * 32 + 255) / 256, 256, 0, st)(Sig, lds, nS, x, y);
 }
 void launch_matvec(const double *M, int ldm, int n, const double *x, double *y, cudaStream_t st) {
-    k_matvec<<<(n * 32 + 255) / 256, 256, 0, st>>>(M, ldm, n, x, y);
+    PDI_LAUNCH(k_matvec, (n * 32 + 255) / 256, 256, 0, st)(M, ldm, n, x, y);
 }
 void launch_chol_solve(const double *L, int ld, int n, const double *b, double *u,
                        cudaStream_t st) {
-    k_chol_solve<<<1, 1024, 0, st>>>(L, ld, n, b, u);
+    PDI_LAUNCH(k_chol_solve, 1, 1024, 0, st)(L, ld, n, b, u);
 }
 
 }  // namespace pdipc

@@ -299,38 +299,38 @@ __global__ void k_scatter_dx(const double *__restrict__ z, const int *__restrict
 
 // ------------------------------------------------------------------ host wrappers ---------
 void launch_ingest_actuation(const double *A9, double *A6, int T, cudaStream_t st) {
-    k_ingest_actuation<<<(T + 255) / 256, 256, 0, st>>>(A9, A6, T);
+    PDI_LAUNCH(k_ingest_actuation, (T + 255) / 256, 256, 0, st)(A9, A6, T);
 }
 void launch_local_step(const int4 *tets, const double4 *x, const double *B, const double *A6,
                        const double *w, int T, double *fc, double *p, cudaStream_t st) {
-    k_local_step<<<(T + 127) / 128, 128, 0, st>>>(tets, x, B, A6, w, T, fc, p);
+    PDI_LAUNCH(k_local_step, (T + 127) / 128, 128, 0, st)(tets, x, B, A6, w, T, fc, p);
 }
 void launch_gather_elastic(const int *inc_ptr, const int *inc, const double *fc, int nf,
                            double4 *g, cudaStream_t st) {
-    k_gather_elastic<<<(nf + 127) / 128, 128, 0, st>>>(inc_ptr, inc, fc, nf, g);
+    PDI_LAUNCH(k_gather_elastic, (nf + 127) / 128, 128, 0, st)(inc_ptr, inc, fc, nf, g);
 }
 void launch_surface(const int *Wp, const int *Wc, const double *Wv, const double4 *x, int Ns,
                     double4 *s, cudaStream_t st) {
-    if (Ns > 0) k_surface<<<(Ns + 127) / 128, 128, 0, st>>>(Wp, Wc, Wv, x, Ns, s);
+    if (Ns > 0) PDI_LAUNCH(k_surface, (Ns + 127) / 128, 128, 0, st)(Wp, Wc, Wv, x, Ns, s);
 }
 int quad_partials(const int4 *tets, const double4 *dx, const double *B, const double *w, int T,
                   double *part, cudaStream_t st) {
     int nb = (T + 255) / 256;
-    k_quad_partials<<<nb, 256, 0, st>>>(tets, dx, B, w, T, part);
+    PDI_LAUNCH(k_quad_partials, nb, 256, 0, st)(tets, dx, B, w, T, part);
     return nb;
 }
 int gdx_partials(const double4 *g, const double4 *dx, const int *q2v, int nf, double *part,
                  cudaStream_t st) {
     int nb = (nf + 255) / 256;
-    k_gdx_partials<<<nb, 256, 0, st>>>(g, dx, q2v, nf, part);
+    PDI_LAUNCH(k_gdx_partials, nb, 256, 0, st)(g, dx, q2v, nf, part);
     return nb;
 }
 void launch_update(double4 *x, const double4 *dx, const int *q2v, int nf, const double *alpha,
                    cudaStream_t st) {
-    k_update<<<(nf + 255) / 256, 256, 0, st>>>(x, dx, q2v, nf, alpha);
+    PDI_LAUNCH(k_update, (nf + 255) / 256, 256, 0, st)(x, dx, q2v, nf, alpha);
 }
 void launch_scatter_dx(const double *z, const int *q2v, int nf, double4 *dx, cudaStream_t st) {
-    k_scatter_dx<<<(nf + 255) / 256, 256, 0, st>>>(z, q2v, nf, dx);
+    PDI_LAUNCH(k_scatter_dx, (nf + 255) / 256, 256, 0, st)(z, q2v, nf, dx);
 }
 
 }  // namespace pdipc

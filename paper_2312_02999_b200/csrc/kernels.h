@@ -12,7 +12,14 @@ struct DevFactor {
     double *L = nullptr;
     int *seg_ptr = nullptr, *seg_d = nullptr, *seg_klo = nullptr, *seg_khi = nullptr;
     int *sn_fd = nullptr, *col2sn = nullptr;
+    int *uoff = nullptr, *urow_sn = nullptr, *rc_ptr = nullptr, *rc_idx = nullptr;
+    int *urel = nullptr, *ch_ptr = nullptr, *ch = nullptr;
+    long long *dinv_ptr = nullptr;
+    double *dinv = nullptr;
+    int nU = 0;
 };
+
+long long launch_count();   // prims.cu: kernels launched so far (PDI_LAUNCH)
 
 // ---- k_elastic.cu
 void launch_ingest_actuation(const double *A9, double *A6, int T, cudaStream_t st);
@@ -34,9 +41,11 @@ void launch_scatter_dx(const double *z, const int *q2v, int nf, double4 *dx, cud
 void launch_ts_items(const int *sn_c0, const int *sn_fd, const int *sn_parent, int nsn,
                      const int *qS, const int *nS_ptr, int *lo, int *hi, int *cnt, int *rem,
                      cudaStream_t st);
+void trisolve_init();
 void launch_forward_solve(const DevFactor &F, const int *lo, const int *hi, const int *item_ptr,
                           const int *qS, int *rem, int *ticket, double *G, double *V, int ldv,
-                          int nsm, cudaStream_t st);
+                          double *Ug, double *Up, int ldu, int nsm, unsigned long long *trace,
+                          cudaStream_t st);
 void launch_backward_solve(const DevFactor &F, int *done, int *ticket, double *Z, int nsm,
                            cudaStream_t st);
 void launch_panel_yS(const int *qS, const int *nS_ptr, int nS_host, const DevFactor &F,

@@ -6,6 +6,10 @@
 
 namespace pdipc {
 
+static long long g_launches = 0;     // handles are single-threaded (pd_ipc.h)
+void note_launch() { ++g_launches; }
+long long launch_count() { return g_launches; }
+
 // ----------------------------------------------------------------------- exclusive scan ----
 constexpr int kScanNT = 1024, kScanIPT = 4, kScanTile = kScanNT * kScanIPT;
 
@@ -83,8 +87,8 @@ void scan_exclusive(const int *in, int *out, int n, int *scratch, cudaStream_t s
         return;
     }
     int nb = (n + kScanTile - 1) / kScanTile;
-    k_scan_partials<<<nb, kScanNT, 0, st>>>(in, n, scratch);
-    k_scan_tiles<<<nb, kScanNT, 0, st>>>(in, n, out, scratch, nb);
+    PDI_LAUNCH(k_scan_partials, nb, kScanNT, 0, st)(in, n, scratch);
+    PDI_LAUNCH(k_scan_tiles, nb, kScanNT, 0, st)(in, n, out, scratch, nb);
 }
 
 int scan_scratch_ints(int n) { return (n + kScanTile - 1) / kScanTile + 1; }
@@ -162,9 +166,9 @@ void radix_sort_u64(uint64_t *keys, uint64_t *tmp, int n, int bits, int *scratch
     int passes = (bits + 7) / 8;
     for (int p = 0; p < passes; ++p) {
         int shift = 8 * p;
-        k_rs_hist<<<nb, kRsNT, 0, st>>>(src, n, shift, hist, nb);
+        PDI_LAUNCH(k_rs_hist, nb, kRsNT, 0, st)(src, n, shift, hist, nb);
         scan_exclusive(hist, offs, 256 * nb, sscr, st);
-        k_rs_scatter<<<nb, kRsNT, 0, st>>>(src, dst, n, shift, offs, nb);
+        PDI_LAUNCH(k_rs_scatter, nb, kRsNT, 0, st)(src, dst, n, shift, offs, nb);
         uint64_t *t = src;
         src = dst;
         dst = t;
@@ -190,9 +194,9 @@ void unique_sorted_u64(const uint64_t *keys, int n, uint64_t *out, int *flags, i
         return;
     }
     int nb = (n + 255) / 256;
-    k_unique_flags<<<nb, 256, 0, st>>>(keys, n, flags);
+    PDI_LAUNCH(k_unique_flags, nb, 256, 0, st)(keys, n, flags);
     scan_exclusive(flags, pos, n, scratch, st);
-    k_unique_write<<<nb, 256, 0, st>>>(keys, n, pos, out);
+    PDI_LAUNCH(k_unique_write, nb, 256, 0, st)(keys, n, pos, out);
 }
 
 // ----------------------------------------------------------------------- reductions -------
@@ -206,7 +210,7 @@ __global__ void k_sum_partials(const double *part, int n, double *out) {
 }
 
 void sum_partials(const double *part, int n, double *out, cudaStream_t st) {
-    k_sum_partials<<<1, 1024, 0, st>>>(part, n, out);
+    PDI_LAUNCH(k_sum_partials, 1, 1024, 0, st)(part, n, out);
 }
 
 }  // namespace pdipc

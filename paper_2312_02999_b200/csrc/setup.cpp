@@ -346,14 +346,18 @@ int factorize(HostMesh &m, HostFactor &f, std::string &err) {
         // the last column of each supernode; keep all (memory ~ nnz(L) ints)
     }
     // ---- supernodes: fundamental + small relaxed chains, capped width
-    const int CAP = 128;
+    // Relaxed amalgamation: every etree chain (column j-1's parent is j) is merged up to CAP
+    // columns, accepting explicit zeros.  The triangular solves are latency-bound (one work
+    // item per supernode on the critical path), so fewer, wider supernodes win over the extra
+    // flops; fundamental supernodes are merged regardless.
+    const int CAP = 128, RELAX = 128;
     std::vector<int> sn_start;
     int width = 0;
     for (int j = 0; j < nf; ++j) {
         bool merge = false;
         if (j > 0 && parent[j - 1] == j && width < CAP) {
             bool fund = nchild[j] == 1 && cs[j - 1].size() == cs[j].size() + 1;
-            merge = fund || width < 4;
+            merge = fund || width < RELAX;
         }
         if (!merge) { sn_start.push_back(j); width = 1; }
         else ++width;
@@ -473,6 +477,85 @@ int factorize(HostMesh &m, HostFactor &f, std::string &err) {
         }
         for (int k = 0; k < w; ++k)                      // keep the diagonal block lower
             for (int i = 0; i < k; ++i) Ls[i + (size_t)k * nr] = 0.0;
+    }
+    // ---- right-looking update rows (U) and their per-row gather lists, diagonal inverses
+    {
+        f.uoff.assign(nsn + 1, 0);
+        for (int d = 0; d < nsn; ++d) {
+            int w = sn_start[d + 1] - sn_start[d];
+            int nr = f.sn_rowptr[d + 1] - f.sn_rowptr[d];
+            f.uoff[d + 1] = f.uoff[d] + (nr - w);
+        }
+        f.urow_sn.resize(f.uoff[nsn]);
+        std::vector<int> cnt(nf + 1, 0);
+        for (int d = 0; d < nsn; ++d) {
+            int w = sn_start[d + 1] - sn_start[d];
+            for (int k = w; k < f.sn_rowptr[d + 1] - f.sn_rowptr[d]; ++k) {
+                cnt[f.sn_rows[f.sn_rowptr[d] + k] + 1]++;
+                f.urow_sn[f.uoff[d] + k - w] = d;
+            }
+        }
+        // Multifrontal extend-add lists: the update block of supernode c (one U row per
+        // off-diagonal row of c, already including c's own children) is consumed by its
+        // parent s: rows that are columns of s are subtracted from s's right-hand side, the
+        // others are added into s's own update block.  rc lists are indexed by the supernode
+        // row slot sn_rowptr[s] + p (p = position of the row in R_s); sources are the child
+        // U rows landing on that row, in increasing child order (deterministic).
+        (void)cnt;
+        const int nslots = f.sn_rowptr[nsn];
+        std::vector<int> scount(nslots + 1, 0);
+        std::vector<std::vector<std::pair<int, int>>> src(nsn);   // per parent: (slot, u)
+        for (int c = 0; c < nsn; ++c) {
+            const int s = f.sn_parent[c];
+            if (s < 0) continue;
+            const int wc = sn_start[c + 1] - sn_start[c];
+            const int *Rs = &f.sn_rows[f.sn_rowptr[s]];
+            const int nrs = f.sn_rowptr[s + 1] - f.sn_rowptr[s];
+            for (int k = wc; k < f.sn_rowptr[c + 1] - f.sn_rowptr[c]; ++k) {
+                const int r = f.sn_rows[f.sn_rowptr[c] + k];
+                const int p = (int)(std::lower_bound(Rs, Rs + nrs, r) - Rs);
+                if (p >= nrs || Rs[p] != r) { err = "supernode row containment violated"; return PD_IPC_E_NOT_SPD; }
+                src[s].push_back({f.sn_rowptr[s] + p, f.uoff[c] + k - wc});
+            }
+        }
+        f.urel.assign(f.uoff[nsn], -1);
+        for (int s = 0; s < nsn; ++s)
+            for (auto &pr : src[s]) f.urel[pr.second] = pr.first - f.sn_rowptr[s];
+        f.ch_ptr.assign(nsn + 1, 0);
+        for (int c = 0; c < nsn; ++c)
+            if (f.sn_parent[c] >= 0) f.ch_ptr[f.sn_parent[c] + 1]++;
+        for (int s = 0; s < nsn; ++s) f.ch_ptr[s + 1] += f.ch_ptr[s];
+        f.ch.assign(f.ch_ptr[nsn], 0);
+        {
+            std::vector<int> cf(f.ch_ptr.begin(), f.ch_ptr.end() - 1);
+            for (int c = 0; c < nsn; ++c)
+                if (f.sn_parent[c] >= 0) f.ch[cf[f.sn_parent[c]]++] = c;
+        }
+        for (int s = 0; s < nsn; ++s)
+            for (auto &pr : src[s]) scount[pr.first + 1]++;
+        f.rc_ptr.assign(nslots + 1, 0);
+        for (int i = 0; i < nslots; ++i) f.rc_ptr[i + 1] = f.rc_ptr[i] + scount[i + 1];
+        f.rc_idx.assign(f.rc_ptr[nslots], 0);
+        std::vector<int> fill(f.rc_ptr.begin(), f.rc_ptr.end() - 1);
+        for (int s = 0; s < nsn; ++s)          // children in increasing order
+            for (auto &pr : src[s]) f.rc_idx[fill[pr.first]++] = pr.second;
+        f.dinv_ptr.assign(nsn + 1, 0);
+        for (int s = 0; s < nsn; ++s) {
+            int w = sn_start[s + 1] - sn_start[s];
+            f.dinv_ptr[s + 1] = f.dinv_ptr[s] + (int64_t)w * w;
+        }
+        f.dinv.assign((size_t)f.dinv_ptr[nsn], 0.0);
+        for (int s = 0; s < nsn; ++s) {
+            const int w = sn_start[s + 1] - sn_start[s], nr = f.sn_rowptr[s + 1] - f.sn_rowptr[s];
+            const double *Ls = &f.vals[(size_t)f.sn_valptr[s]];
+            double *D = &f.dinv[(size_t)f.dinv_ptr[s]];
+            for (int c = 0; c < w; ++c)            // column c of L_ss^{-1} by forward substitution
+                for (int i = c; i < w; ++i) {
+                    double acc = (i == c) ? 1.0 : 0.0;
+                    for (int k = c; k < i; ++k) acc -= Ls[i + (size_t)k * nr] * D[(size_t)k * w + c];
+                    D[(size_t)i * w + c] = acc / Ls[i + (size_t)i * nr];
+                }
+        }
     }
     // ---- transpose incidence in factor order and W^T over factor positions
     {

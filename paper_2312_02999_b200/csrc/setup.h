@@ -47,6 +47,16 @@ struct HostFactor {
     // lie in s's columns
     std::vector<int32_t> seg_ptr, seg_d, seg_klo, seg_khi;
     std::vector<int32_t> sn_nchild;    // [nsn]
+    // right-looking update rows: supernode d writes U rows uoff[d] .. uoff[d+1)-1, one per
+    // off-diagonal row of d; factor row r gathers the U rows listed in rc_idx[rc_ptr[r]..]
+    std::vector<int32_t> uoff;         // [nsn+1]
+    std::vector<int32_t> urow_sn;      // [uoff[nsn]] owner supernode of each U row
+    std::vector<int32_t> rc_ptr, rc_idx;
+    std::vector<int32_t> urel;         // [nU] position of a U row's matrix row in the parent's R
+    std::vector<int32_t> ch_ptr, ch;   // children of each supernode (increasing order)
+    // inverse of each diagonal block (lower triangular, row-major w x w)
+    std::vector<int64_t> dinv_ptr;     // [nsn+1]
+    std::vector<double> dinv;
     int max_width = 0, max_rows = 0, depth = 0;
     int64_t nnzL = 0;
 };

@@ -79,10 +79,36 @@ lib.pd_ipc_debug_factor_solve.argtypes = [C.POINTER(pd_ipc_mesh), C.POINTER(C.c_
                                           C.POINTER(C.c_int64)]
 lib.pd_ipc_debug_factor_solve.restype = C.c_int
 
+lib.pd_ipc_set_timing.argtypes = [_P, C.c_int32]
+lib.pd_ipc_set_timing.restype = C.c_int
+lib.pd_ipc_kernel_times.argtypes = [_P, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int32]
+lib.pd_ipc_kernel_times.restype = C.c_int
+lib.pd_ipc_kernel_name.argtypes = [C.c_int32]
+lib.pd_ipc_kernel_name.restype = C.c_char_p
+lib.pd_ipc_launch_count.argtypes = []
+lib.pd_ipc_launch_count.restype = C.c_int64
+
 EXPORTED = ["pd_ipc_create", "pd_ipc_step", "pd_ipc_positions", "pd_ipc_destroy",
             "pd_ipc_last_error", "pd_ipc_set_positions", "pd_ipc_set_debug",
             "pd_ipc_get_projections", "pd_ipc_get_contacts", "pd_ipc_get_vector",
-            "pd_ipc_build_info", "pd_ipc_debug_factor_solve"]
+            "pd_ipc_build_info", "pd_ipc_debug_factor_solve", "pd_ipc_set_timing",
+            "pd_ipc_kernel_times", "pd_ipc_kernel_name", "pd_ipc_launch_count"]
+
+
+def set_timing(h, on=True):
+    _check(lib.pd_ipc_set_timing(h, int(on)), h)
+
+
+def kernel_times(h, reset=False):
+    """{group name: (ms accumulated, count)} of the timed kernel groups."""
+    ms = (C.c_double * 32)()
+    cnt = (C.c_int64 * 32)()
+    k = lib.pd_ipc_kernel_times(h, ms, cnt, int(reset))
+    return {lib.pd_ipc_kernel_name(i).decode(): (ms[i], cnt[i]) for i in range(k)}
+
+
+def launch_count() -> int:
+    return int(lib.pd_ipc_launch_count())
 
 
 class PdIpcError(RuntimeError):
@@ -215,7 +241,7 @@ def build_info() -> str:
 def debug_factor_solve(scene, b=None):
     """Host-only setup check: factorise L_FF and solve L_FF x = b.  Returns (x, stats)."""
     m = _MeshArgs(scene)
-    stats = np.zeros(4, np.int64)
+    stats = np.zeros(8, np.int64)
     n = m.rest.shape[0]
     if b is None:
         rc = lib.pd_ipc_debug_factor_solve(C.byref(m.mesh), _dp(m.rest), None, None,
