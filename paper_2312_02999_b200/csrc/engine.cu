@@ -96,10 +96,12 @@ struct StageTimer {
 
 // Per-kernel-group device timing (CUDA events on the library stream), for the roofline report.
 enum KId { K_LOCAL = 0, K_GATHER, K_BROAD, K_NARROW, K_DERIV, K_ASSEMBLY, K_FWD, K_DENSE, K_BWD,
-           K_CCD, K_LS, K_NUM };
+           K_CCD, K_LS, K_D_SYRK, K_D_INV, K_D_POTRF, K_D_SOLVE, K_NUM };
 static const char *kKernelNames[K_NUM] = {"local_step", "gather", "broad_phase", "narrow_phase",
                                           "pair_derivatives", "contact_assembly", "forward_solve",
-                                          "dense_schur", "backward_solve", "ccd", "line_search"};
+                                          "dense_schur", "backward_solve", "ccd", "line_search",
+                                          "dense.syrk", "dense.inverse", "dense.potrf",
+                                          "dense.solve"};
 struct KTimer {
     bool on = false;
     cudaEvent_t ev[K_NUM][2];
@@ -141,7 +143,7 @@ struct pd_ipc {
     HostMesh hm;
     HostFactor hf;
     int n = 0, T = 0, nf = 0, Ns = 0, Nt = 0, Ne = 0;
-    int capS = 0, ldv = 0;
+    int capS = 0, ldv = 0, ldh = 0;
     int debug = 0;
     double cell0 = 0;
     // mesh (shared by sequences)
@@ -171,14 +173,14 @@ struct pd_ipc {
     DBuf<unsigned long long> rec, rec_tmp;
     DBuf<int> bccnt, bcoff;
     DBuf<int> ts_lo, ts_hi, ts_cnt, ts_ptr, ts_rem, ts_done, ticket;
-    DBuf<double> V, K, Bc, Sh, U, Tt, yS, rhs, u, tv, part, b0;
+    DBuf<double> V, K, Bc, Sh, U, Tt, yS, rhs, u, tv, part, b0, Lstore;
     DBuf<double> dscal;     // [0]=ext cell, [1]=amin, [2..4]=ls, [5..8]=ls_out, [9..10]=scal
     DBuf<int> dint;         // [0..3] counts, [4] info
     StageTimer tm;
     KTimer kt;
     // debugging aid: PDIPC_TRACE=<file> appends per-item forward-solve timestamps
-    FILE *trace_file = nullptr;
-    DBuf<unsigned long long> trace;
+    FILE *trace_file = nullptr, *schur_file = nullptr;
+    DBuf<unsigned long long> trace, sprof;
 };
 
 static thread_local std::string g_last_error;
@@ -448,18 +450,24 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
     kt.start(K_DENSE, st);
     if (nS > 0) {
         const int ldk = h->capS, m3 = 3 * nS, ldb = 3 * h->capS;
-        launch_panel_yS(h->qS.p, nS_dev, nS, F, h->V.p, h->ldv, h->G.p, h->yS.p, st);
-        launch_panel_syrk(F, h->ts_lo.p, h->ts_hi.p, h->V.p, h->ldv, nS_dev, nS, h->K.p, ldk, st);
         int *info = h->dint.p + 4;
         CK(cudaMemsetAsync(info, 0, sizeof(int), st));
-        dense_spd_inverse(h->K.p, ldk, nS, h->U.p, h->Tt.p, info, st);
-        dense_negate(h->K.p, ldk, nS, st);                    // K <- Sigma_s = K_s^{-1}
-        launch_assemble_sigma_hat(h->K.p, ldk, h->Bc.p, ldb, h->Sh.p, ldb, nS, st);
-        dense_potrf(h->Sh.p, ldb, m3, h->Tt.p, info, st);
-        launch_kron_matvec(h->K.p, ldk, nS, h->yS.p, h->rhs.p, st);
-        launch_chol_solve(h->Sh.p, ldb, m3, h->rhs.p, h->u.p, st);
-        launch_matvec(h->Bc.p, ldb, m3, h->u.p, h->tv.p, st);
-        launch_panel_correct(F, h->ts_lo.p, h->ts_hi.p, h->V.p, h->ldv, h->G.p, h->tv.p, h->Z.p, st);
+        (void)m3;
+        if (h->trace_file) {
+            h->sprof.ensure(1024);
+            CK(cudaMemsetAsync(h->sprof.p, 0, 1024 * 8, st));
+        }
+        CK((cudaError_t)launch_schur(F, h->V.p, h->ldv, h->G.p, h->qS.p, h->ts_lo.p, h->ts_hi.p, nS, h->K.p,
+                                     ldk, h->Bc.p, ldb, h->Sh.p, h->ldh, h->Lstore.p, h->Tt.p, h->U.p,
+                                     h->yS.p, h->u.p, h->tv.p, h->Z.p, info,
+                                     h->trace_file ? h->sprof.p : nullptr, st));
+        if (h->trace_file && h->schur_file) {
+            std::vector<unsigned long long> pr(1024);
+            CK(cudaMemcpy(pr.data(), h->sprof.p, 1024 * 8, cudaMemcpyDeviceToHost));
+            fwrite(&nS, sizeof(int), 1, h->schur_file);
+            fwrite(pr.data(), 8, 1024, h->schur_file);
+            fflush(h->schur_file);
+        }
     } else {
         CK(cudaMemcpyAsync(h->Z.p, h->G.p, sizeof(double) * 4 * nf, cudaMemcpyDeviceToDevice, st));
     }
@@ -640,10 +648,14 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
         h->tm.init();
         h->kt.init();
-        if (const char *tp = std::getenv("PDIPC_TRACE")) h->trace_file = std::fopen(tp, "wb");
+        if (const char *tp = std::getenv("PDIPC_TRACE")) {
+            h->trace_file = std::fopen(tp, "wb");
+            h->schur_file = std::fopen((std::string(tp) + ".schur").c_str(), "wb");
+        }
         dense_init();
         contact_init();
         trisolve_init();
+        schur_init(o.device);
         HostMesh &m = h->hm;
         HostFactor &f = h->hf;
         h->n = m.n;
@@ -760,6 +772,24 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         h->cand.exact(2 * cap_cand);
         h->cand_tmp.exact(2 * cap_cand);
         ensure_pair_buffers(h.get(), 2 * cap_cand);
+        // pre-size the per-pair buffers so that no allocation happens inside the iteration
+        // (an allocation synchronises the device); they still grow on demand
+        if (m.Nt > 0) {
+            const size_t cap_act = cap_cand;
+            h->akeys.ensure(cap_act + 1);
+            h->atype.ensure(cap_act + 1);
+            h->ad2.ensure(cap_act + 1);
+            h->grad.ensure(12 * cap_act + 12);
+            h->Hp.ensure(78 * cap_act + 78);
+            h->dist.ensure(cap_act + 1);
+            h->ids.ensure(4 * cap_act + 4);
+            h->rec.ensure(16 * cap_act + 1);
+            h->rec_tmp.ensure(16 * cap_act + 1);
+            h->bccnt.ensure(cap_act + 1);
+            h->bcoff.ensure(cap_act + 1);
+            h->b0.ensure(2 * cap_cand + 1);
+            h->iscr.ensure(radix_scratch_ints((int)(16 * cap_act)) + 1024);
+        }
         h->iscr.ensure(std::max({radix_scratch_ints((int)(2 * cap_cand)), scan_scratch_ints(nf + 1),
                                  scan_scratch_ints(f.nsn + 1)}) + 1024);
         {
@@ -777,12 +807,15 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             h->V.exact((size_t)nf * h->ldv);
             h->K.exact((size_t)cS * cS);
             h->Bc.exact((size_t)9 * cS * cS);
-            h->Sh.exact((size_t)9 * cS * cS);
+            h->ldh = 3 * cS + 8;
+            h->Sh.exact((size_t)(3 * cS + 1) * h->ldh);
+            h->Lstore.exact((size_t)((3 * cS + 1 + 63) / 64 + 1) * 64 * 64);
             h->U.exact((size_t)(cS + 64) * 64);
             h->yS.exact(3 * (size_t)cS);
             h->rhs.exact(3 * (size_t)cS);
             h->u.exact(3 * (size_t)cS);
             h->tv.exact(3 * (size_t)cS);
+            h->Up.exact((size_t)std::max(1, f.uoff[f.nsn]) * (((cS + 31) / 32) * 32));
         } else {
             h->V.exact(32);
         }
@@ -852,7 +885,9 @@ void pd_ipc_destroy(pd_ipc *h) {
     h->tm.destroy();
     h->kt.destroy();
     if (h->trace_file) std::fclose(h->trace_file);
+    if (h->schur_file) std::fclose(h->schur_file);
     h->trace.release();
+    h->sprof.release();
     if (h->st) cudaStreamDestroy(h->st);
     auto rel = [](auto &b) { b.release(); };
     rel(h->tets); rel(h->B); rel(h->w); rel(h->inc_ptr); rel(h->inc); rel(h->q2v); rel(h->v2q);
@@ -869,7 +904,7 @@ void pd_ipc_destroy(pd_ipc *h) {
     rel(h->spos); rel(h->qS); rel(h->rec); rel(h->rec_tmp); rel(h->bccnt); rel(h->bcoff); rel(h->ts_lo);
     rel(h->ts_hi); rel(h->ts_cnt); rel(h->ts_ptr); rel(h->ts_rem); rel(h->ts_done); rel(h->ticket);
     rel(h->V); rel(h->K); rel(h->Bc); rel(h->Sh); rel(h->U); rel(h->Tt); rel(h->yS); rel(h->rhs);
-    rel(h->u); rel(h->tv); rel(h->part); rel(h->b0); rel(h->dscal); rel(h->dint);
+    rel(h->u); rel(h->tv); rel(h->part); rel(h->b0); rel(h->dscal); rel(h->dint); rel(h->Lstore);
     delete h;
 }
 

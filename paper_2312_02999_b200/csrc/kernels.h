@@ -55,6 +55,14 @@ void launch_panel_correct(const DevFactor &F, const int *lo, const int *hi, cons
 void launch_panel_syrk(const DevFactor &F, const int *lo, const int *hi, const double *V, int ldv,
                        const int *nS_ptr, int nS_host, double *K, int ldk, cudaStream_t st);
 
+// ---- k_schur.cu (fused cooperative dense Schur step, a9)
+void schur_init(int device);
+int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, const int *qS,
+                 const int *lo, const int *hi, int nS, double *K, int ldk, const double *Bc, int ldb,
+                 double *Sh, int ldh, double *Lstore, double *T, double *U, double *yS, double *u,
+                 double *t, double *Z, int *info, unsigned long long *prof, cudaStream_t st);
+void note_launch();
+
 // ---- k_dense.cu
 void dense_init();
 void dense_potrf(double *A, int ld, int m, double *T, int *info, cudaStream_t st);

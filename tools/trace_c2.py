@@ -10,5 +10,5 @@ P.set_timing(s.h, True)
 for f in range(0, 26):
     st = s.step(A_next=sc.actuation(f)[None], n_iters=20)
     if f % 5 == 0:
-        print(f, st[0]["n_active"], st[0]["n_S"], {k: round(v[0] / max(v[1], 1), 3) for k, v in P.kernel_times(s.h, reset=True).items()}, flush=True)
+        print(f, "cand", st[0]["n_cand"], "active", st[0]["n_active"], "nS", st[0]["n_S"], {k: round(v[0] / max(v[1], 1), 3) for k, v in P.kernel_times(s.h, reset=True).items()}, flush=True)
 s.close()
