@@ -164,7 +164,7 @@ struct pd_ipc {
     DBuf<double> fc, G, Z, A9stage;
     DBuf<double4> g_el, s, ds, dx, gs;
     DBuf<double4> blo, bhi;
-    DBuf<int> hcnt, hstart, hent;
+    DBuf<int> hcnt, hstart, hent, qcnt, qoff;
     unsigned hmask = 0;
     DBuf<unsigned long long> cand, cand_tmp, akeys;
     DBuf<int> flag, pos, ctype, atype, ids, iscr;
@@ -174,7 +174,9 @@ struct pd_ipc {
     DBuf<int> bccnt, bcoff;
     DBuf<int> ts_lo, ts_hi, ts_cnt, ts_ptr, ts_rem, ts_done, ticket;
     DBuf<double> V, K, Bc, Sh, U, Tt, yS, rhs, u, tv, part, b0, Lstore;
-    DBuf<double> dscal;     // [0]=ext cell, [1]=amin, [2..4]=ls, [5..8]=ls_out, [9..10]=scal
+    DBuf<double> dscal;     // [0]=ext cell, [1]=amin, [2..4]=ls, [5..8]=ls_out, [9..10]=scal,
+                            // [11]=max |pair term| (fixed-point scale), [12]=min active distance
+    DBuf<long long> gsq;    // surface gradient, fixed point [Ns][3]
     DBuf<int> dint;         // [0..3] counts, [4] info
     StageTimer tm;
     KTimer kt;
@@ -197,13 +199,72 @@ static void sync_read_ints(pd_ipc *h, int *dst, const int *src, int k) {
     CK(cudaStreamSynchronize(h->st));
 }
 
-static void set_d(pd_ipc *h, double *dptr, double v) {
-    CK(cudaMemcpyAsync(dptr, &v, sizeof(double), cudaMemcpyHostToDevice, h->st));
-}
+// device scalar <- v, stream-ordered, no host staging (a pageable H2D copy would block)
+static void set_d(pd_ipc *h, double *dptr, double v) { launch_set_double(dptr, v, h->st); }
+
+static void broad_phase_sort(pd_ipc *h, const double4 *ds, double infl, int *npt_out, int *nee_out);
 
 // Broad phase: static (ds == nullptr, boxes inflated by infl) or swept.  Produces sorted unique
-// PT keys in cand[0..npt) and EE keys in cand[npt..npt+nee).
+// PT keys in cand[0..npt) and EE keys in cand[npt..npt+nee).  Sort-free: every query sorts its
+// own (short) partner list, so the lists come out globally sorted; one host read of the sizes.
 static void broad_phase(pd_ipc *h, const double4 *ds, double infl, int *npt_out, int *nee_out) {
+    cudaStream_t st = h->st;
+    const int Ns = h->Ns, Nt = h->Nt, Ne = h->Ne;
+    const int nbox = Ns + Nt + Ne;
+    h->blo.ensure(nbox);
+    h->bhi.ensure(nbox);
+    double *ext = h->dscal.p + 0;
+    set_d(h, ext, h->cell0);
+    launch_boxes(h->s.p, ds, h->tris.p, h->edges.p, Ns, Nt, Ne, infl, h->blo.p, h->bhi.p, ext, st);
+    const unsigned M = h->hmask + 1;
+    const int qn = std::max(Ns, Ne) + 1;
+    h->qcnt.ensure(2 * (size_t)qn);
+    h->qoff.ensure(2 * (size_t)qn);
+    int *ovf = h->dint.p + 6;
+    CK(cudaMemsetAsync(ovf, 0, sizeof(int), st));
+    for (int kind = 0; kind < 2; ++kind) {   // 0 = PT (B = tris), 1 = EE (B = edges)
+        const int b0 = kind == 0 ? Ns : Ns + Nt, nb = kind == 0 ? Nt : Ne;
+        const int a0 = kind == 0 ? 0 : Ns + Nt, na = kind == 0 ? Ns : Ne;
+        int *hc = h->hcnt.p + (size_t)kind * (M + 1);
+        int *hs = h->hstart.p + (size_t)kind * (M + 1);
+        int *he = h->hent.p + (size_t)kind * (h->hent.n / 2);
+        CK(cudaMemsetAsync(hc, 0, sizeof(int) * (M + 1), st));
+        launch_hash_insert(h->blo.p, h->bhi.p, b0, nb, ext, h->hmask, hc, nullptr, nullptr, st);
+        scan_exclusive(hc, hs, (int)M, h->iscr.p, st);
+        CK(cudaMemsetAsync(hc, 0, sizeof(int) * (M + 1), st));
+        launch_hash_insert(h->blo.p, h->bhi.p, b0, nb, ext, h->hmask, hc, hs, he, st);
+        int *qc = h->qcnt.p + (size_t)kind * qn, *qo = h->qoff.p + (size_t)kind * qn;
+        launch_hash_query_local(h->blo.p, h->bhi.p, a0, na, b0, kind == 0 ? Nt : Ne, ext, h->hmask, hs, he,
+                                kind == 0, h->tris.p, h->edges.p, qc, nullptr, nullptr, ovf, st);
+        scan_exclusive(qc, qo, na, h->iscr.p, st);
+        CK(cudaMemcpyAsync(h->dint.p + 2 + kind, qo + na, sizeof(int), cudaMemcpyDeviceToDevice, st));
+    }
+    int res[5];
+    sync_read_ints(h, res, h->dint.p + 2, 5);   // [2] npt, [3] nee, [6] overflow
+    if (res[4]) {                               // a query exceeded its local list: sort path
+        broad_phase_sort(h, ds, infl, npt_out, nee_out);
+        return;
+    }
+    const size_t need = (size_t)res[0] + res[1] + 1;
+    if (h->cand.n < need) {
+        h->cand.exact(2 * need);
+        h->cand_tmp.exact(2 * need);
+    }
+    for (int kind = 0; kind < 2; ++kind) {
+        const int b0 = kind == 0 ? Ns : Ns + Nt;
+        const int a0 = kind == 0 ? 0 : Ns + Nt, na = kind == 0 ? Ns : Ne;
+        int *hs = h->hstart.p + (size_t)kind * (M + 1);
+        int *he = h->hent.p + (size_t)kind * (h->hent.n / 2);
+        int *qo = h->qoff.p + (size_t)kind * qn;
+        launch_hash_query_local(h->blo.p, h->bhi.p, a0, na, b0, kind == 0 ? Nt : Ne, ext, h->hmask, hs, he,
+                                kind == 0, h->tris.p, h->edges.p, nullptr, qo,
+                                h->cand.p + (kind == 0 ? 0 : res[0]), ovf, st);
+    }
+    *npt_out = res[0];
+    *nee_out = res[1];
+}
+
+static void broad_phase_sort(pd_ipc *h, const double4 *ds, double infl, int *npt_out, int *nee_out) {
     cudaStream_t st = h->st;
     const int Ns = h->Ns, Nt = h->Nt, Ne = h->Ne;
     const int nbox = Ns + Nt + Ne;
@@ -314,24 +375,19 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
                       h->ctype.p, h->cd2.p, st);
         launch_narrow(h->cand.p + cpt, cee, 0, Ne, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->dh2,
                       h->flag.p + cpt, h->ctype.p + cpt, h->cd2.p + cpt, st);
-        // scan flags of PT and EE separately so that actives are [PT | EE], each sorted
-        scan_exclusive(h->flag.p, h->pos.p, cpt, h->iscr.p, st);
-        CK(cudaMemcpyAsync(h->dint.p + 0, h->pos.p + cpt, sizeof(int), cudaMemcpyDeviceToDevice, st));
-        int npt_h;
-        sync_read_ints(h, &npt_h, h->dint.p, 1);
-        n_pt = npt_h;
+        // one scan over [PT flags | EE flags]: actives come out as [PT | EE], each sorted
         h->akeys.ensure(n_cand + 1);
         h->atype.ensure(n_cand + 1);
         h->ad2.ensure(n_cand + 1);
-        launch_compact_active(h->cand.p, cpt, h->flag.p, h->pos.p, h->ctype.p, h->cd2.p, 0, h->akeys.p,
+        scan_exclusive(h->flag.p, h->pos.p, n_cand, h->iscr.p, st);
+        launch_compact_active(h->cand.p, n_cand, h->flag.p, h->pos.p, h->ctype.p, h->cd2.p, 0, h->akeys.p,
                               h->atype.p, h->ad2.p, st);
-        scan_exclusive(h->flag.p + cpt, h->pos.p, cee, h->iscr.p, st);
-        CK(cudaMemcpyAsync(h->dint.p + 1, h->pos.p + cee, sizeof(int), cudaMemcpyDeviceToDevice, st));
-        launch_compact_active(h->cand.p + cpt, cee, h->flag.p + cpt, h->pos.p, h->ctype.p + cpt,
-                              h->cd2.p + cpt, n_pt, h->akeys.p, h->atype.p, h->ad2.p, st);
-        int nee_h;
-        sync_read_ints(h, &nee_h, h->dint.p + 1, 1);
-        n_ee = nee_h;
+        CK(cudaMemcpyAsync(h->dint.p + 0, h->pos.p + cpt, sizeof(int), cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(h->dint.p + 1, h->pos.p + n_cand, sizeof(int), cudaMemcpyDeviceToDevice, st));
+        int cnts[2];
+        sync_read_ints(h, cnts, h->dint.p, 2);
+        n_pt = cnts[0];
+        n_ee = cnts[1] - cnts[0];
         const int na = n_pt + n_ee;
         h->grad.ensure(12 * (size_t)na + 12);
         h->Hp.ensure(78 * (size_t)na + 78);
@@ -339,8 +395,11 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
         h->ids.ensure(4 * (size_t)na + 4);
         kt.stop(K_NARROW, st);
         kt.start(K_DERIV, st);
+        double *dmax = h->dscal.p + 11;
+        set_d(h, dmax, 0.0);
+        set_d(h, dmax + 1, 1e300);
         launch_pair_derivs(h->akeys.p, h->atype.p, h->ad2.p, n_pt, na, h->s.p, h->tris.p, h->edges.p, Nt,
-                           Ne, h->dh, h->kappa, h->grad.p, h->Hp.p, h->dist.p, h->ids.p, st);
+                           Ne, h->dh, h->kappa, h->grad.p, h->Hp.p, h->dist.p, h->ids.p, dmax, st);
         kt.stop(K_DERIV, st);
         kt.start(K_ASSEMBLY, st);
         // S
@@ -348,46 +407,23 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
         launch_mark_S(h->ids.p, na, h->Wp.p, h->Wc.p, h->v2q.p, h->mark.p, st);
         scan_exclusive(h->mark.p, h->spos.p, nf, h->iscr.p, st);
         launch_compact_S(h->mark.p, h->spos.p, nf, h->qS.p, st);
+        // gradient pull-back: deterministic fixed-point accumulation on the surface, then W^T
+        h->gsq.ensure(6 * (size_t)Ns + 6);
+        CK(cudaMemsetAsync(h->gsq.p, 0, sizeof(long long) * 6 * Ns, st));
+        launch_accum_grad_fx(h->ids.p, na, h->grad.p, dmax, h->gsq.p, st);
+        launch_grad_pullback_fx(h->g_el.p, h->WTp.p, h->WTr.p, h->WTv.p, h->gsq.p, dmax, na, nf, h->G.p, st);
         sync_read_ints(h, &nS, nS_dev, 1);
         if (nS > h->capS) throw CudaError("contact vertex set exceeds capacity", PD_IPC_E_CAPACITY);
-        if (na > 0) {
-            std::vector<double> dd(na);
-            CK(cudaMemcpy(dd.data(), h->dist.p, sizeof(double) * na, cudaMemcpyDeviceToHost));
-            min_dist = *std::min_element(dd.begin(), dd.end());
-            if (!(min_dist > 0)) throw CudaError("non-positive distance", PD_IPC_E_NONFINITE);
-        }
-        // gradient pull-back (deterministic: sort records by surface vertex)
-        CK(cudaMemsetAsync(h->gs.p, 0, sizeof(double4) * Ns, st));
-        if (na > 0) {
-            const int sh = bits_for(4ull * na);
-            h->rec.ensure(4 * (size_t)na + 1);
-            h->rec_tmp.ensure(4 * (size_t)na + 1);
-            h->iscr.ensure(radix_scratch_ints(4 * na) + 1024);
-            launch_grad_records(h->ids.p, na, sh, h->rec.p, st);
-            radix_sort_u64(reinterpret_cast<uint64_t *>(h->rec.p), reinterpret_cast<uint64_t *>(h->rec_tmp.p),
-                           4 * na, sh + bits_for(Ns), h->iscr.p, st);
-            launch_grad_reduce(h->rec.p, 4 * na, sh, h->grad.p, h->gs.p, st);
-        }
-        launch_grad_pullback(h->g_el.p, h->WTp.p, h->WTr.p, h->WTv.p, h->gs.p, nf, h->G.p, st);
-        // B-check records
+        // B-check: fixed-point accumulation into the dense 3nS x 3nS block, then to double
         if (nS > 0) {
-            h->bccnt.ensure(na + 1);
-            h->bcoff.ensure(na + 1);
-            launch_bc_count(h->ids.p, na, h->Wp.p, h->Wc.p, h->v2q.p, h->bccnt.p, st);
-            scan_exclusive(h->bccnt.p, h->bcoff.p, na, h->iscr.p, st);
-            int nrec;
-            sync_read_ints(h, &nrec, h->bcoff.p + na, 1);
-            const int sh = bits_for(256ull * na);
-            h->rec.ensure(nrec + 1);
-            h->rec_tmp.ensure(nrec + 1);
-            h->iscr.ensure(radix_scratch_ints(nrec) + 1024);
-            launch_bc_records(h->ids.p, na, h->Wp.p, h->Wc.p, h->v2q.p, h->spos.p, nS, sh, h->bcoff.p,
-                              h->rec.p, st);
-            radix_sort_u64(reinterpret_cast<uint64_t *>(h->rec.p), reinterpret_cast<uint64_t *>(h->rec_tmp.p),
-                           nrec, sh + bits_for((unsigned long long)nS * nS), h->iscr.p, st);
             const int ldb = 3 * h->capS;
+            // low words of the fixed-point sums live in the (not yet used) Sigma-hat buffer
+            long long *Bl = reinterpret_cast<long long *>(h->Sh.p);
             launch_zero_square(h->Bc.p, ldb, 3 * nS, st);
-            launch_bc_reduce(h->rec.p, nrec, sh, nS, h->ids.p, h->Wp.p, h->Wv.p, h->Hp.p, h->Bc.p, ldb, st);
+            launch_zero_square(h->Sh.p, ldb, 3 * nS, st);
+            launch_accum_bc_fx(h->ids.p, na, h->Wp.p, h->Wc.p, h->Wv.p, h->v2q.p, h->spos.p, h->Hp.p, dmax,
+                               reinterpret_cast<long long *>(h->Bc.p), Bl, ldb, st);
+            launch_fx_to_double(reinterpret_cast<long long *>(h->Bc.p), Bl, ldb, 3 * nS, dmax, na, st);
         }
         kt.stop(K_ASSEMBLY, st);
     } else {
@@ -503,7 +539,8 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
         sum_partials(h->part.p + nb1, nb2, scal + 1, st);
         CK(cudaMemcpyAsync(ls, amin, sizeof(double), cudaMemcpyDeviceToDevice, st));
         double zeros[2] = {0.0, 0.0};
-        CK(cudaMemcpyAsync(ls + 1, zeros, 2 * sizeof(double), cudaMemcpyHostToDevice, st));
+        (void)zeros;
+        CK(cudaMemsetAsync(ls + 1, 0, 2 * sizeof(double), st));
         const int nsw = spt + see;
         h->b0.ensure(nsw + 1);
         const int nbp = (spt + 255) / 256, nbe = (see + 255) / 256;
@@ -527,7 +564,7 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
     kt.stop(K_LS, st);
     CK(cudaEventRecord(ev[5], st));
     // ---------------- stats
-    double sc[11];
+    double sc[13];
     CK(cudaMemcpyAsync(sc, h->dscal.p, sizeof(sc), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     int info_h = 0, fault_h = 0;
@@ -553,6 +590,9 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
     S.ls_trials = (int)sc[6];
     S.dE = sc[7];
     S.flags = (int)sc[8];
+    min_dist = (n_pt + n_ee > 0) ? sc[12] : 0.0;
+    if (n_pt + n_ee > 0 && !(min_dist > 0))
+        throw CudaError("non-positive distance in the active set", PD_IPC_E_NONFINITE);
     S.min_dist = min_dist;
     if (!std::isfinite(sc[5]) || !std::isfinite(sc[9]) || !std::isfinite(sc[10]))
         throw CudaError("non-finite value in step", PD_IPC_E_NONFINITE);
@@ -899,6 +939,7 @@ void pd_ipc_destroy(pd_ipc *h) {
     for (auto &s : h->seqs) { rel(s->x); rel(s->A6); rel(s->p); }
     rel(h->fc); rel(h->G); rel(h->Z); rel(h->A9stage); rel(h->g_el); rel(h->s); rel(h->ds); rel(h->dx);
     rel(h->gs); rel(h->blo); rel(h->bhi); rel(h->hcnt); rel(h->hstart); rel(h->hent); rel(h->cand);
+    rel(h->qcnt); rel(h->qoff); rel(h->gsq);
     rel(h->cand_tmp); rel(h->akeys); rel(h->flag); rel(h->pos); rel(h->ctype); rel(h->atype); rel(h->ids);
     rel(h->iscr); rel(h->cd2); rel(h->ad2); rel(h->grad); rel(h->Hp); rel(h->dist); rel(h->mark);
     rel(h->spos); rel(h->qS); rel(h->rec); rel(h->rec_tmp); rel(h->bccnt); rel(h->bcoff); rel(h->ts_lo);

@@ -260,6 +260,67 @@ __global__ void k_hash_query(const double4 *__restrict__ lo, const double4 *__re
             }
 }
 
+// Sort-free variant: each query collects its partners, sorts and de-duplicates them locally,
+// so the concatenation over queries in index order IS the sorted unique key list.
+// pass 0 counts (cnt[a]), pass 1 writes at off[a].  ovf is set if a query exceeds kQCap.
+constexpr int kQCap = 128;
+__global__ void k_hash_query_local(const double4 *__restrict__ lo, const double4 *__restrict__ hi,
+                                   int a0, int na, int b0, int nB, const double *__restrict__ cell,
+                                   unsigned mask, const int *__restrict__ start,
+                                   const int *__restrict__ entries, int is_pt,
+                                   const int *__restrict__ tris, const int *__restrict__ edges,
+                                   int *__restrict__ cnt, const int *__restrict__ off,
+                                   unsigned long long *__restrict__ out, int *__restrict__ ovf) {
+    int a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= na) return;
+    int list[kQCap];
+    int n = 0;
+    const double inv = 1.0 / *cell;
+    const double4 la = lo[a0 + a], ha = hi[a0 + a];
+    int c0[3], c1[3];
+    cell_range(la, ha, inv, c0, c1);
+    int av[2] = {0, 0};
+    if (!is_pt) { av[0] = edges[2 * a]; av[1] = edges[2 * a + 1]; }
+    for (int x = c0[0]; x <= c1[0]; ++x)
+        for (int y = c0[1]; y <= c1[1]; ++y)
+            for (int z = c0[2]; z <= c1[2]; ++z) {
+                unsigned h = cell_hash(x, y, z, mask);
+                for (int k = start[h]; k < start[h + 1]; ++k) {
+                    int b = entries[k];
+                    if (!is_pt && b <= a) continue;
+                    const double4 lb = lo[b0 + b], hb = hi[b0 + b];
+                    if (!overlap(la, ha, lb, hb)) continue;
+                    int m0 = max(c0[0], (int)floor(lb.x * inv)), m1 = max(c0[1], (int)floor(lb.y * inv)),
+                        m2 = max(c0[2], (int)floor(lb.z * inv));
+                    if (m0 != x || m1 != y || m2 != z) continue;
+                    if (is_pt) {
+                        if (tris[3 * b] == a || tris[3 * b + 1] == a || tris[3 * b + 2] == a) continue;
+                    } else {
+                        int b0v = edges[2 * b], b1v = edges[2 * b + 1];
+                        if (b0v == av[0] || b0v == av[1] || b1v == av[0] || b1v == av[1]) continue;
+                    }
+                    if (n < kQCap) {
+                        int i = n++;                       // insertion sort, drop duplicates
+                        while (i > 0 && list[i - 1] > b) { list[i] = list[i - 1]; --i; }
+                        if (i > 0 && list[i - 1] == b) {
+                            for (int j = i; j < n - 1; ++j) list[j] = list[j + 1];
+                            --n;
+                        } else {
+                            list[i] = b;
+                        }
+                    } else {
+                        atomicExch(ovf, 1);
+                    }
+                }
+            }
+    if (!off) {
+        cnt[a] = n;
+        return;
+    }
+    unsigned long long *o = out + off[a];
+    for (int i = 0; i < n; ++i) o[i] = (unsigned long long)a * (unsigned long long)nB + list[i];
+}
+
 // ------------------------------------------------------------------ a5 narrow filter ------
 // flag[i] = d^2 < dh2 for candidate keys; stores type and d^2
 __global__ void k_narrow(const unsigned long long *__restrict__ keys, int n, int is_pt, int nB,
@@ -360,7 +421,7 @@ __global__ void __launch_bounds__(kPD_WARPS * 32) k_pair_derivs(
     const unsigned long long *__restrict__ akeys, const int *__restrict__ atype,
     const double *__restrict__ ad2, int n_pt, int n_all, PairCtx c, double dh, double kappa,
     double *__restrict__ grad, double *__restrict__ Hp, double *__restrict__ dist,
-    int *__restrict__ ids_out) {
+    int *__restrict__ ids_out, double *__restrict__ dmax) {
     __shared__ double Hs[kPD_WARPS][12][13];
     __shared__ double Vs[kPD_WARPS][12][13];
     __shared__ double gs[kPD_WARPS][12];
@@ -497,6 +558,7 @@ __global__ void __launch_bounds__(kPD_WARPS * 32) k_pair_derivs(
         }
     }
     // H^+ = sum_m max(lambda_m, 0) v_m v_m^T, packed upper
+    double mx = lane < 12 ? fabs(kappa * b1 * (gs[wl][lane] / (2.0 * d))) : 0.0;
     for (int e = lane; e < 78; e += 32) {
         int i = c_ui[e], j = c_uj[e];
         double acc = 0.0;
@@ -505,6 +567,12 @@ __global__ void __launch_bounds__(kPD_WARPS * 32) k_pair_derivs(
             if (l > 0.0) acc += l * V[i][m] * V[j][m];
         }
         Hp[78 * (size_t)k + e] = acc;
+        mx = fmax(mx, fabs(acc));
+    }
+    mx = warp_max(mx);                       // scale of the fixed-point assembly
+    if (lane == 0) {  // non-negative doubles order like their bit patterns
+        atomicMax(reinterpret_cast<unsigned long long *>(dmax), (unsigned long long)__double_as_longlong(mx));
+        atomic_min_nonneg(dmax + 1, d);       // min active distance (stats)
     }
 }
 
@@ -653,6 +721,128 @@ __global__ void k_bc_reduce(const unsigned long long *__restrict__ rec, int n, i
     int ia = (int)(tgt / nS), ib = (int)(tgt % nS);
     for (int a = 0; a < 3; ++a)
         for (int b = 0; b < 3; ++b) Bc[(size_t)(3 * ia + a) * ldb + 3 * ib + b] = acc[3 * a + b];
+}
+
+// ---- deterministic fixed-point accumulation (no sort, no value-order dependence) --------
+// Contributions are rounded to integers at a common power-of-two scale chosen from the largest
+// per-pair magnitude (dmax) and a bound on the number of contributions per entry; integer
+// addition is associative, so the sums are bit-identical for any atomic order.
+// Two-level fixed point: c = hi / s + lo / (s 2^40), hi = round(c s), lo = round((c s - hi) 2^40),
+// each level summed exactly in int64 (|hi sum| < 2^61, |lo sum| < 2^50): ~100 significant bits.
+__device__ __forceinline__ double fx_scale(const double *dmax, int n_pairs) {
+    const double m = fmax(*dmax, 1e-300);
+    const int e = ilogb(m) + 1 + ilogb((double)max(1, 64 * n_pairs)) + 1;   // |sum| < 2^e
+    return ldexp(1.0, 61 - e);
+}
+constexpr double kFxLo = 1099511627776.0;   // 2^40
+
+__device__ __forceinline__ void fx_add(long long *hi, long long *lo, double c, double sc) {
+    const double x = c * sc;                 // exact power-of-two scaling
+    const double h = rint(x);
+    atomicAdd(reinterpret_cast<unsigned long long *>(hi), (unsigned long long)(long long)h);
+    atomicAdd(reinterpret_cast<unsigned long long *>(lo), (unsigned long long)llrint((x - h) * kFxLo));
+}
+__device__ __forceinline__ double fx_get(long long hi, long long lo, double inv_sc) {
+    return ((double)hi + (double)lo / kFxLo) * inv_sc;
+}
+
+__global__ void k_accum_grad_fx(const int *__restrict__ ids, int n_all, const double *__restrict__ grad,
+                                const double *__restrict__ dmax, long long *__restrict__ gsq) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;     // (pair, slot)
+    if (i >= 4 * n_all) return;
+    const double sc = fx_scale(dmax, n_all);
+    const int j = ids[i];
+    for (int a = 0; a < 3; ++a)              // hi in gsq[j][0..2], lo in gsq[j][3..5]
+        fx_add(gsq + 6 * (size_t)j + a, gsq + 6 * (size_t)j + 3 + a, grad[3 * (size_t)i + a], sc);
+}
+
+// B-check: thread per (pair, slot_a, slot_b); target (S-index of v_a, S-index of v_b) blocks
+__global__ void k_accum_bc_fx(const int *__restrict__ ids, int n_all, const int *__restrict__ Wp,
+                              const int *__restrict__ Wc, const double *__restrict__ Wv,
+                              const int *__restrict__ v2q, const int *__restrict__ sidx,
+                              const double *__restrict__ Hp, const double *__restrict__ dmax,
+                              long long *__restrict__ Bq, long long *__restrict__ Bl, int ldb) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 16 * n_all) return;
+    const int k = i >> 4, sa = (i >> 2) & 3, sb = i & 3;
+    const double sc = fx_scale(dmax, n_all);
+    const int ja = ids[4 * k + sa], jb = ids[4 * k + sb];
+    const double *H = Hp + 78 * (size_t)k;
+    double blk[9];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) {
+            const int ii = 3 * sa + a, jj = 3 * sb + b;
+            blk[3 * a + b] = ii <= jj ? H[ii * 12 - (ii * (ii - 1)) / 2 + (jj - ii)]
+                                      : H[jj * 12 - (jj * (jj - 1)) / 2 + (ii - jj)];
+        }
+    for (int na = Wp[ja]; na < Wp[ja + 1]; ++na) {
+        const int qa = v2q[Wc[na]];
+        if (qa < 0) continue;
+        for (int nb = Wp[jb]; nb < Wp[jb + 1]; ++nb) {
+            const int qb = v2q[Wc[nb]];
+            if (qb < 0) continue;
+            const double w = Wv[na] * Wv[nb];
+            const size_t o = (size_t)(3 * sidx[qa]) * ldb + 3 * sidx[qb];
+            for (int a = 0; a < 3; ++a)
+                for (int b = 0; b < 3; ++b)
+                    fx_add(Bq + o + (size_t)a * ldb + b, Bl + o + (size_t)a * ldb + b, w * blk[3 * a + b], sc);
+        }
+    }
+}
+
+// in place: fixed point (hi in M, lo in Ml) -> double in M, n x n block, leading dimension ld
+__global__ void k_fx_to_double(long long *M, const long long *Ml, int ld, int n, const double *dmax,
+                               int n_pairs) {
+    const double inv = 1.0 / fx_scale(dmax, n_pairs);
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < (size_t)n * n;
+         e += (size_t)gridDim.x * blockDim.x) {
+        const size_t off = (e / n) * ld + e % n;
+        reinterpret_cast<double *>(M)[off] = fx_get(M[off], Ml[off], inv);
+    }
+}
+
+// G[q] = g_el[q] + sum_{(j,w) in W^T row q} w gs[j]   (gs in fixed point)
+__global__ void k_grad_pullback_fx(const double4 *__restrict__ g_el, const int *__restrict__ WTp,
+                                   const int *__restrict__ WTr, const double *__restrict__ WTv,
+                                   const long long *__restrict__ gsq, const double *__restrict__ dmax,
+                                   int n_pairs, int nf, double *__restrict__ G) {
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nf) return;
+    const double inv = 1.0 / fx_scale(dmax, n_pairs);
+    double4 g = g_el[q];
+    double bx = 0, by = 0, bz = 0;
+    for (int k = WTp[q]; k < WTp[q + 1]; ++k) {
+        const double w = WTv[k];
+        const long long *v = gsq + 6 * (size_t)WTr[k];
+        bx += w * fx_get(v[0], v[3], inv);
+        by += w * fx_get(v[1], v[4], inv);
+        bz += w * fx_get(v[2], v[5], inv);
+    }
+    G[4 * (size_t)q + 0] = g.x + bx;
+    G[4 * (size_t)q + 1] = g.y + by;
+    G[4 * (size_t)q + 2] = g.z + bz;
+    G[4 * (size_t)q + 3] = 0.0;
+}
+
+void launch_accum_grad_fx(const int *ids, int n_all, const double *grad, const double *dmax,
+                          long long *gsq, cudaStream_t st) {
+    if (n_all > 0) PDI_LAUNCH(k_accum_grad_fx, (4 * n_all + 255) / 256, 256, 0, st)(ids, n_all, grad, dmax, gsq);
+}
+void launch_accum_bc_fx(const int *ids, int n_all, const int *Wp, const int *Wc, const double *Wv,
+                        const int *v2q, const int *sidx, const double *Hp, const double *dmax,
+                        long long *Bq, long long *Bl, int ldb, cudaStream_t st) {
+    if (n_all > 0)
+        PDI_LAUNCH(k_accum_bc_fx, (16 * n_all + 127) / 128, 128, 0, st)(ids, n_all, Wp, Wc, Wv, v2q, sidx, Hp,
+                                                                        dmax, Bq, Bl, ldb);
+}
+void launch_fx_to_double(long long *M, const long long *Ml, int ld, int n, const double *dmax,
+                         int n_pairs, cudaStream_t st) {
+    if (n > 0) PDI_LAUNCH(k_fx_to_double, 256, 256, 0, st)(M, Ml, ld, n, dmax, n_pairs);
+}
+void launch_grad_pullback_fx(const double4 *g_el, const int *WTp, const int *WTr, const double *WTv,
+                             const long long *gsq, const double *dmax, int n_pairs, int nf, double *G,
+                             cudaStream_t st) {
+    PDI_LAUNCH(k_grad_pullback_fx, (nf + 255) / 256, 256, 0, st)(g_el, WTp, WTr, WTv, gsq, dmax, n_pairs, nf, G);
 }
 
 __global__ void k_zero_square(double *M, int ld, int n) {
@@ -815,6 +1005,15 @@ void launch_hash_query(const double4 *lo, const double4 *hi, int a0, int na, int
         PDI_LAUNCH(k_hash_query, (na + 127) / 128, 128, 0, st)(lo, hi, a0, na, b0, nB, cell, mask, start,
                                                        entries, is_pt, tris, edges, out, count, cap);
 }
+void launch_hash_query_local(const double4 *lo, const double4 *hi, int a0, int na, int b0, int nB,
+                             const double *cell, unsigned mask, const int *start, const int *entries,
+                             int is_pt, const int *tris, const int *edges, int *cnt, const int *off,
+                             unsigned long long *out, int *ovf, cudaStream_t st) {
+    if (na > 0)
+        PDI_LAUNCH(k_hash_query_local, (na + 127) / 128, 128, 0, st)(lo, hi, a0, na, b0, nB, cell, mask,
+                                                                    start, entries, is_pt, tris, edges,
+                                                                    cnt, off, out, ovf);
+}
 void launch_narrow(const unsigned long long *keys, int n, int is_pt, int nB, const double4 *s,
                    const int *tris, const int *edges, int Nt, int Ne, double dh2, int *flag,
                    int *type, double *d2, cudaStream_t st) {
@@ -831,11 +1030,11 @@ void launch_compact_active(const unsigned long long *keys, int n, const int *fla
 void launch_pair_derivs(const unsigned long long *akeys, const int *atype, const double *ad2,
                         int n_pt, int n_all, const double4 *s, const int *tris, const int *edges,
                         int Nt, int Ne, double dh, double kappa, double *grad, double *Hp,
-                        double *dist, int *ids, cudaStream_t st) {
+                        double *dist, int *ids, double *dmax, cudaStream_t st) {
     if (n_all <= 0) return;
     PairCtx c{s, tris, edges, Nt, Ne};
     PDI_LAUNCH(k_pair_derivs, (n_all + kPD_WARPS - 1) / kPD_WARPS, kPD_WARPS * 32, 0, st)(
-        akeys, atype, ad2, n_pt, n_all, c, dh, kappa, grad, Hp, dist, ids);
+        akeys, atype, ad2, n_pt, n_all, c, dh, kappa, grad, Hp, dist, ids, dmax);
 }
 void launch_mark_S(const int *ids, int n_all, const int *Wp, const int *Wc, const int *v2q,
                    int *mark, cudaStream_t st) {

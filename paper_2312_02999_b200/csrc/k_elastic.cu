@@ -297,7 +297,11 @@ __global__ void k_scatter_dx(const double *__restrict__ z, const int *__restrict
     dx[q2v[q]] = make_double4(-r[0], -r[1], -r[2], 0.0);
 }
 
+__global__ void k_set_double(double *p, double v) { *p = v; }
+
 // ------------------------------------------------------------------ host wrappers ---------
+void launch_set_double(double *p, double v, cudaStream_t st) { PDI_LAUNCH(k_set_double, 1, 1, 0, st)(p, v); }
+
 void launch_ingest_actuation(const double *A9, double *A6, int T, cudaStream_t st) {
     PDI_LAUNCH(k_ingest_actuation, (T + 255) / 256, 256, 0, st)(A9, A6, T);
 }

@@ -135,14 +135,15 @@ constexpr int kXS = 40;
 // M[i][k] at M + i*ldm_row + k*ldm_col; 32-column slabs of M are staged in Sg with cp.async.
 // In rows >= kdim must be zero (callers zero them).  Warp w owns the 8x8 tiles t = w + 8j of
 // the (ceil(m/8) x NCT) tile grid.
-template <bool LOWER>
+// TRI: 0 full, 1 lower (k <= i), 2 upper (k >= i)
+template <int TRI>
 __device__ __forceinline__ void stage_slab(const double *M, long long ldm_row, long long ldm_col,
                                            int m, int mr, int kc, int kn, double (*Sg)[kSS]) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if (ldm_row == 1) {                     // column-major source: coalesce over i
         for (int kk = wid; kk < 32; kk += kTS_NT / 32)
             for (int i = lane; i < mr; i += 32) {
-                if (i < m && kk < kn && (!LOWER || kc + kk <= i))
+                if (i < m && kk < kn && (TRI == 0 || (TRI == 1 ? kc + kk <= i : kc + kk >= i)))
                     cp_async8(&Sg[i][kk], M + (long long)i + (long long)(kc + kk) * ldm_col);
                 else
                     Sg[i][kk] = 0.0;
@@ -150,7 +151,7 @@ __device__ __forceinline__ void stage_slab(const double *M, long long ldm_row, l
     } else {                                // row-major source: coalesce over k
         for (int i = wid; i < mr; i += kTS_NT / 32) {
             const int kk = lane;
-            if (i < m && kk < kn && (!LOWER || kc + kk <= i))
+            if (i < m && kk < kn && (TRI == 0 || (TRI == 1 ? kc + kk <= i : kc + kk >= i)))
                 cp_async8(&Sg[i][kk], M + (long long)i * ldm_row + (long long)(kc + kk) * ldm_col);
             else
                 Sg[i][kk] = 0.0;
@@ -160,7 +161,7 @@ __device__ __forceinline__ void stage_slab(const double *M, long long ldm_row, l
 }
 
 // Sg points at TWO slab buffers (double buffering: chunk c+1 is in flight while chunk c runs).
-template <bool LOWER, int NCT>
+template <int TRI, int NCT, bool ACC = false>
 __device__ __forceinline__ void slab_dmma(const double *M, long long ldm_row, long long ldm_col,
                                           int m, int kdim, const double (*In)[kXS],
                                           double (*Sg)[kSS], double (*Out)[kXS]) {
@@ -172,12 +173,12 @@ __device__ __forceinline__ void slab_dmma(const double *M, long long ldm_row, lo
     for (int j = 0; j < kMaxT; ++j) acc[j][0] = acc[j][1] = 0.0;
     const int gr = lane >> 2, gc = lane & 3;
     const int nch = (kdim + 31) / 32;
-    stage_slab<LOWER>(M, ldm_row, ldm_col, m, mr, 0, min(32, kdim), Sg);
+    stage_slab<TRI>(M, ldm_row, ldm_col, m, mr, 0, min(32, kdim), Sg);
     for (int ch = 0; ch < nch; ++ch) {
         const int kc = ch * 32;
         double (*B)[kSS] = Sg + (ch & 1) * kTS_W;
         if (ch + 1 < nch) {
-            stage_slab<LOWER>(M, ldm_row, ldm_col, m, mr, kc + 32, min(32, kdim - kc - 32),
+            stage_slab<TRI>(M, ldm_row, ldm_col, m, mr, kc + 32, min(32, kdim - kc - 32),
                               Sg + ((ch + 1) & 1) * kTS_W);
             cp_async_wait_group<1>();
         } else {
@@ -206,8 +207,13 @@ __device__ __forceinline__ void slab_dmma(const double *M, long long ldm_row, lo
             const int tr = t / NCT, tc = t % NCT;
             const int r = tr * 8 + gr, c = tc * 8 + 2 * gc;
             if (r < m) {
-                Out[r][c] = acc[j][0];
-                Out[r][c + 1] = acc[j][1];
+                if (ACC) {
+                    Out[r][c] += acc[j][0];
+                    Out[r][c + 1] += acc[j][1];
+                } else {
+                    Out[r][c] = acc[j][0];
+                    Out[r][c + 1] = acc[j][1];
+                }
             }
         }
     }
@@ -297,25 +303,8 @@ __global__ void __launch_bounds__(kTS_NT) k_forward_solve(FwdArgs A) {
         // ---- 3. Y = Dinv X  (D row-major w x w, lower).  Panel: DMMA on staged slabs.
         //         Gradient (3 columns, no reuse to exploit): thread per row straight from L2,
         //         all loads independent.
-        if (grad) {
-            if (tid < w) {
-                const double *Di = D + (size_t)tid * w;
-                double a0 = 0, a1 = 0, a2 = 0;
-#pragma unroll 8
-                for (int k = 0; k <= tid; ++k) {
-                    const double d = __ldg(Di + k);
-                    a0 += d * X[k][0];
-                    a1 += d * X[k][1];
-                    a2 += d * X[k][2];
-                }
-                Y[tid][0] = a0;
-                Y[tid][1] = a1;
-                Y[tid][2] = a2;
-            }
-            __syncthreads();
-        } else {
-            slab_dmma<true, 4>(D, w, 1, w, w, X, Sg, Y);
-        }
+        if (grad) slab_dmma<1, 1>(D, w, 1, w, w, X, Sg, Y);
+        else slab_dmma<1, 4>(D, w, 1, w, w, X, Sg, Y);
         for (int e = tid; e < kTS_W * 32; e += kTS_NT) {
             const int i = e >> 5, c = e & 31;
             if (i >= w) { Y[i][c] = 0.0; continue; }        // k-padding of step 4
@@ -329,24 +318,19 @@ __global__ void __launch_bounds__(kTS_NT) k_forward_solve(FwdArgs A) {
         __syncthreads();
         // ---- 4. U_s = L_off Y  (L column-major, ld nr) on DMMA, 128-row blocks through X
         if (grad) {
-            double4 *Ug4 = reinterpret_cast<double4 *>(A.Ug);
-            for (int r = tid; r < noff; r += kTS_NT) {
-                const double *lr = Ls + w + r;
-                double a0 = 0, a1 = 0, a2 = 0;
-#pragma unroll 8
-                for (int k = 0; k < w; ++k) {
-                    const double l = __ldg(lr + (size_t)k * nr);
-                    a0 += l * Y[k][0];
-                    a1 += l * Y[k][1];
-                    a2 += l * Y[k][2];
+            for (int rb = 0; rb < noff; rb += kTS_W) {
+                const int m = min(kTS_W, noff - rb);
+                slab_dmma<0, 1>(Ls + w + rb, 1, nr, m, w, Y, Sg, X);
+                for (int e = tid; e < m * 4; e += kTS_NT) {
+                    const int r = e >> 2, c = e & 3;
+                    A.Ug[(size_t)(u0 + rb + r) * 4 + c] = c < 3 ? X[r][c] : 0.0;
                 }
-                Ug4[u0 + r] = make_double4(a0, a1, a2, 0.0);
+                __syncthreads();
             }
-            __syncthreads();
         } else {
             for (int rb = 0; rb < noff; rb += kTS_W) {
                 const int m = min(kTS_W, noff - rb);
-                slab_dmma<false, 4>(Ls + w + rb, 1, nr, m, w, Y, Sg, X);
+                slab_dmma<0, 4>(Ls + w + rb, 1, nr, m, w, Y, Sg, X);
                 for (int e = tid; e < m * 32; e += kTS_NT) {
                     const int r = e >> 5, c = e & 31;
                     A.Up[(size_t)(u0 + rb + r) * A.ldu + tbase + c] = X[r][c];
@@ -417,7 +401,7 @@ struct BwdArgs {
 
 constexpr int kBwdStage = 256;
 
-__global__ void __launch_bounds__(kTS_NT) k_backward_solve(BwdArgs A) {
+__global__ void __launch_bounds__(kTS_NT) k_backward_solve_v1(BwdArgs A) {
     __shared__ double X[kTS_W][4];
     __shared__ double4 xo[kBwdStage];
     __shared__ double Sg[32][kTS_W + 1];
@@ -499,6 +483,71 @@ __global__ void __launch_bounds__(kTS_NT) k_backward_solve(BwdArgs A) {
             zr[0] = a[0];
             zr[1] = a[1];
             zr[2] = a[2];
+        }
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) atomicExch(A.done + s, 1);
+    }
+}
+
+// Backward solve item s (reverse postorder, waits for its parent):
+//   X = z_s - L_off^T x_off    (DMMA over 128-row chunks of the solved ancestor rows x_off)
+//   x_s = Dinv^T X             (DMMA, upper-triangular slab staging)
+__global__ void __launch_bounds__(kTS_NT) k_backward_solve(BwdArgs A) {
+    extern __shared__ double bsm[];
+    double (*X)[kXS] = reinterpret_cast<double (*)[kXS]>(bsm);
+    double (*Y)[kXS] = reinterpret_cast<double (*)[kXS]>(bsm + kTS_W * kXS);
+    double (*Sg)[kSS] = reinterpret_cast<double (*)[kSS]>(bsm + 2 * kTS_W * kXS);
+    __shared__ int sh_item;
+    const int tid = threadIdx.x;
+    while (true) {
+        if (tid == 0) sh_item = atomicAdd(A.ticket, 1);
+        __syncthreads();
+        const int item = sh_item;
+        __syncthreads();
+        if (item >= A.nsn) return;
+        const int s = A.nsn - 1 - item;
+        if (tid == 0) {
+            int p = A.sn_parent[s];
+            if (p >= 0) {
+                volatile int *dp = A.done + p;
+                long long t0 = clock64();
+                while (*dp == 0) {
+                    __nanosleep(32);
+                    if (clock64() - t0 > kSpinLimit) { atomicExch(A.ticket + 1, 1); break; }
+                }
+            }
+            __threadfence();
+        }
+        __syncthreads();
+        const int c0 = A.sn_c0[s], w = A.sn_c0[s + 1] - c0;
+        const int r0 = A.sn_rowptr[s], nr = A.sn_rowptr[s + 1] - r0, noff = nr - w;
+        const double *Ls = A.L + A.sn_valptr[s];
+        const double *D = A.dinv + A.dinv_ptr[s];
+        // ---- acc = L_off^T x_off, chunks of 128 off rows staged in Y (cols >= 3 and padding 0)
+        for (int rb = 0; rb < noff; rb += kTS_W) {
+            const int m = min(kTS_W, noff - rb);
+            for (int e = tid; e < kTS_W * 8; e += kTS_NT) {
+                const int r = e >> 3, c = e & 7;
+                Y[r][c] = (r < m && c < 3) ? __ldcg(A.Z + (size_t)A.sn_rows[r0 + w + rb + r] * 4 + c) : 0.0;
+            }
+            __syncthreads();
+            if (rb == 0) slab_dmma<0, 1, false>(Ls + w + rb, nr, 1, w, m, Y, Sg, X);
+            else slab_dmma<0, 1, true>(Ls + w + rb, nr, 1, w, m, Y, Sg, X);
+        }
+        // ---- X = z_s - acc (rows >= w and columns >= 3 zeroed: k-padding of the next product)
+        for (int e = tid; e < kTS_W * 8; e += kTS_NT) {
+            const int k = e >> 3, c = e & 7;
+            double v = 0.0;
+            if (k < w && c < 3) v = __ldcg(A.Z + (size_t)(c0 + k) * 4 + c) - (noff > 0 ? X[k][c] : 0.0);
+            Y[k][c] = v;
+        }
+        __syncthreads();
+        // ---- x_s = Dinv^T X : element (i, k) = D[k][i] (column-major source, upper triangle)
+        slab_dmma<2, 1, false>(D, 1, w, w, w, Y, Sg, X);
+        for (int e = tid; e < w * 3; e += kTS_NT) {
+            const int i = e / 3, c = e % 3;
+            A.Z[(size_t)(c0 + i) * 4 + c] = X[i][c];
         }
         __threadfence();
         __syncthreads();
@@ -606,6 +655,7 @@ constexpr int kFwdSmem = (2 * kTS_W * kXS + 2 * kTS_W * kSS) * (int)sizeof(doubl
 
 void trisolve_init() {
     cudaFuncSetAttribute(k_forward_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem);
+    cudaFuncSetAttribute(k_backward_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem);
 }
 
 void launch_ts_items(const int *sn_c0, const int *sn_fd, const int *sn_parent, int nsn,
@@ -640,7 +690,7 @@ void launch_backward_solve(const DevFactor &F, int *done, int *ticket, double *Z
     A.nsn = F.nsn; A.done = done; A.ticket = ticket; A.Z = Z;
     cudaMemsetAsync(ticket, 0, sizeof(int), st);
     cudaMemsetAsync(done, 0, sizeof(int) * F.nsn, st);
-    PDI_LAUNCH(k_backward_solve, nsm * 2, kTS_NT, 0, st)(A);
+    PDI_LAUNCH(k_backward_solve, nsm, kTS_NT, kFwdSmem, st)(A);
 }
 
 void launch_panel_yS(const int *qS, const int *nS_ptr, int nS_host, const DevFactor &F,

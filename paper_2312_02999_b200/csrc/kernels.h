@@ -22,6 +22,7 @@ struct DevFactor {
 long long launch_count();   // prims.cu: kernels launched so far (PDI_LAUNCH)
 
 // ---- k_elastic.cu
+void launch_set_double(double *p, double v, cudaStream_t st);
 void launch_ingest_actuation(const double *A9, double *A6, int T, cudaStream_t st);
 void launch_local_step(const int4 *tets, const double4 *x, const double *B, const double *A6,
                        const double *w, int T, double *fc, double *p, cudaStream_t st);
@@ -86,6 +87,10 @@ void launch_hash_query(const double4 *lo, const double4 *hi, int a0, int na, int
                        const double *cell, unsigned mask, const int *start, const int *entries,
                        int is_pt, const int *tris, const int *edges, unsigned long long *out,
                        int *count, int cap, cudaStream_t st);
+void launch_hash_query_local(const double4 *lo, const double4 *hi, int a0, int na, int b0, int nB,
+                             const double *cell, unsigned mask, const int *start, const int *entries,
+                             int is_pt, const int *tris, const int *edges, int *cnt, const int *off,
+                             unsigned long long *out, int *ovf, cudaStream_t st);
 void launch_narrow(const unsigned long long *keys, int n, int is_pt, int nB, const double4 *s,
                    const int *tris, const int *edges, int Nt, int Ne, double dh2, int *flag,
                    int *type, double *d2, cudaStream_t st);
@@ -95,7 +100,17 @@ void launch_compact_active(const unsigned long long *keys, int n, const int *fla
 void launch_pair_derivs(const unsigned long long *akeys, const int *atype, const double *ad2,
                         int n_pt, int n_all, const double4 *s, const int *tris, const int *edges,
                         int Nt, int Ne, double dh, double kappa, double *grad, double *Hp,
-                        double *dist, int *ids, cudaStream_t st);
+                        double *dist, int *ids, double *dmax, cudaStream_t st);
+void launch_accum_grad_fx(const int *ids, int n_all, const double *grad, const double *dmax,
+                          long long *gsq, cudaStream_t st);
+void launch_accum_bc_fx(const int *ids, int n_all, const int *Wp, const int *Wc, const double *Wv,
+                        const int *v2q, const int *sidx, const double *Hp, const double *dmax,
+                        long long *Bq, long long *Bl, int ldb, cudaStream_t st);
+void launch_fx_to_double(long long *M, const long long *Ml, int ld, int n, const double *dmax,
+                         int n_pairs, cudaStream_t st);
+void launch_grad_pullback_fx(const double4 *g_el, const int *WTp, const int *WTr, const double *WTv,
+                             const long long *gsq, const double *dmax, int n_pairs, int nf, double *G,
+                             cudaStream_t st);
 void launch_mark_S(const int *ids, int n_all, const int *Wp, const int *Wc, const int *v2q,
                    int *mark, cudaStream_t st);
 void launch_compact_S(const int *mark, const int *pos, int nf, int *qS, cudaStream_t st);
