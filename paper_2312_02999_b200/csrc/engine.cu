@@ -164,7 +164,7 @@ struct pd_ipc {
     DBuf<double> fc, G, Z, A9stage;
     DBuf<double4> g_el, s, ds, dx, gs;
     DBuf<double4> blo, bhi;
-    DBuf<int> hcnt, hstart, hent, qcnt, qoff;
+    DBuf<int> hcnt, hstart, hent, qcnt, qoff, qlist;
     unsigned hmask = 0;
     DBuf<unsigned long long> cand, cand_tmp, akeys;
     DBuf<int> flag, pos, ctype, atype, ids, iscr;
@@ -207,59 +207,53 @@ static void broad_phase_sort(pd_ipc *h, const double4 *ds, double infl, int *npt
 // Broad phase: static (ds == nullptr, boxes inflated by infl) or swept.  Produces sorted unique
 // PT keys in cand[0..npt) and EE keys in cand[npt..npt+nee).  Sort-free: every query sorts its
 // own (short) partner list, so the lists come out globally sorted; one host read of the sizes.
+// Hash cell = min(max box extent, kCellCap * cell0): one long swept box must not coarsen the grid
+// for every query; boxes wider than the cap span several cells (bounded, see k_hash_insert).
+constexpr double kCellCap = 2.0;
+
 static void broad_phase(pd_ipc *h, const double4 *ds, double infl, int *npt_out, int *nee_out) {
     cudaStream_t st = h->st;
     const int Ns = h->Ns, Nt = h->Nt, Ne = h->Ne;
     const int nbox = Ns + Nt + Ne;
     h->blo.ensure(nbox);
     h->bhi.ensure(nbox);
-    double *ext = h->dscal.p + 0;
+    double *ext = h->dscal.p + 14;   // cell = [max box extent, cap]
     set_d(h, ext, h->cell0);
+    set_d(h, ext + 1, kCellCap * h->cell0);
     launch_boxes(h->s.p, ds, h->tris.p, h->edges.p, Ns, Nt, Ne, infl, h->blo.p, h->bhi.p, ext, st);
     const unsigned M = h->hmask + 1;
-    const int qn = std::max(Ns, Ne) + 1;
-    h->qcnt.ensure(2 * (size_t)qn);
-    h->qoff.ensure(2 * (size_t)qn);
+    const int nq = Ns + Ne, cap_ent = (int)h->hent.n;
+    h->qcnt.ensure((size_t)nq + 1);
+    h->qoff.ensure((size_t)nq + 1);
+    h->qlist.ensure((size_t)nq * hash_query_cap());
     int *ovf = h->dint.p + 6;
     CK(cudaMemsetAsync(ovf, 0, sizeof(int), st));
-    for (int kind = 0; kind < 2; ++kind) {   // 0 = PT (B = tris), 1 = EE (B = edges)
-        const int b0 = kind == 0 ? Ns : Ns + Nt, nb = kind == 0 ? Nt : Ne;
-        const int a0 = kind == 0 ? 0 : Ns + Nt, na = kind == 0 ? Ns : Ne;
-        int *hc = h->hcnt.p + (size_t)kind * (M + 1);
-        int *hs = h->hstart.p + (size_t)kind * (M + 1);
-        int *he = h->hent.p + (size_t)kind * (h->hent.n / 2);
-        CK(cudaMemsetAsync(hc, 0, sizeof(int) * (M + 1), st));
-        launch_hash_insert(h->blo.p, h->bhi.p, b0, nb, ext, h->hmask, hc, nullptr, nullptr, st);
-        scan_exclusive(hc, hs, (int)M, h->iscr.p, st);
-        CK(cudaMemsetAsync(hc, 0, sizeof(int) * (M + 1), st));
-        launch_hash_insert(h->blo.p, h->bhi.p, b0, nb, ext, h->hmask, hc, hs, he, st);
-        int *qc = h->qcnt.p + (size_t)kind * qn, *qo = h->qoff.p + (size_t)kind * qn;
-        launch_hash_query_local(h->blo.p, h->bhi.p, a0, na, b0, kind == 0 ? Nt : Ne, ext, h->hmask, hs, he,
-                                kind == 0, h->tris.p, h->edges.p, qc, nullptr, nullptr, ovf, st);
-        scan_exclusive(qc, qo, na, h->iscr.p, st);
-        CK(cudaMemcpyAsync(h->dint.p + 2 + kind, qo + na, sizeof(int), cudaMemcpyDeviceToDevice, st));
-    }
+    // both tables (tris, edges) in one pass each: count, scan, fill
+    CK(cudaMemsetAsync(h->hcnt.p, 0, sizeof(int) * 2 * (M + 1), st));
+    launch_hash_insert(h->blo.p, h->bhi.p, Ns, Nt, Ne, ext, h->hmask, h->hcnt.p, nullptr, nullptr, 0, ovf, st);
+    scan_exclusive(h->hcnt.p, h->hstart.p, (int)(2 * (M + 1)), h->iscr.p, st);
+    CK(cudaMemsetAsync(h->hcnt.p, 0, sizeof(int) * 2 * (M + 1), st));
+    launch_hash_insert(h->blo.p, h->bhi.p, Ns, Nt, Ne, ext, h->hmask, h->hcnt.p, h->hstart.p, h->hent.p,
+                       cap_ent, ovf, st);
+    // one warp per query (PT points, then EE edges): sorted unique partner lists
+    launch_hash_query_warp(h->blo.p, h->bhi.p, Ns, Nt, Ne, ext, h->hmask, h->hstart.p, h->hent.p, h->tris.p,
+                           h->edges.p, h->qcnt.p, h->qlist.p, ovf, st);
+    scan_exclusive(h->qcnt.p, h->qoff.p, nq, h->iscr.p, st);
+    CK(cudaMemcpyAsync(h->dint.p + 2, h->qoff.p + Ns, sizeof(int), cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(h->dint.p + 3, h->qoff.p + nq, sizeof(int), cudaMemcpyDeviceToDevice, st));
     int res[5];
-    sync_read_ints(h, res, h->dint.p + 2, 5);   // [2] npt, [3] nee, [6] overflow
-    if (res[4]) {                               // a query exceeded its local list: sort path
+    sync_read_ints(h, res, h->dint.p + 2, 5);   // [2] npt, [3] npt + nee, [6] overflow
+    if (res[4]) {                               // outlier box or table overflow: sort path
         broad_phase_sort(h, ds, infl, npt_out, nee_out);
         return;
     }
+    res[1] -= res[0];
     const size_t need = (size_t)res[0] + res[1] + 1;
     if (h->cand.n < need) {
         h->cand.exact(2 * need);
         h->cand_tmp.exact(2 * need);
     }
-    for (int kind = 0; kind < 2; ++kind) {
-        const int b0 = kind == 0 ? Ns : Ns + Nt;
-        const int a0 = kind == 0 ? 0 : Ns + Nt, na = kind == 0 ? Ns : Ne;
-        int *hs = h->hstart.p + (size_t)kind * (M + 1);
-        int *he = h->hent.p + (size_t)kind * (h->hent.n / 2);
-        int *qo = h->qoff.p + (size_t)kind * qn;
-        launch_hash_query_local(h->blo.p, h->bhi.p, a0, na, b0, kind == 0 ? Nt : Ne, ext, h->hmask, hs, he,
-                                kind == 0, h->tris.p, h->edges.p, nullptr, qo,
-                                h->cand.p + (kind == 0 ? 0 : res[0]), ovf, st);
-    }
+    launch_hash_emit(Ns, Nt, Ne, h->qcnt.p, h->qoff.p, h->qlist.p, h->cand.p, st);
     *npt_out = res[0];
     *nee_out = res[1];
 }
@@ -270,24 +264,26 @@ static void broad_phase_sort(pd_ipc *h, const double4 *ds, double infl, int *npt
     const int nbox = Ns + Nt + Ne;
     h->blo.ensure(nbox);
     h->bhi.ensure(nbox);
-    double *ext = h->dscal.p + 0;
+    double *ext = h->dscal.p + 14;   // uncapped cell: every box covers at most 8 cells
     set_d(h, ext, h->cell0);
+    set_d(h, ext + 1, 1e300);
     launch_boxes(h->s.p, ds, h->tris.p, h->edges.p, Ns, Nt, Ne, infl, h->blo.p, h->bhi.p, ext, st);
     const unsigned M = h->hmask + 1;
     int *cnt_pt = h->dint.p + 0, *cnt_ee = h->dint.p + 1;
+    int *ovf = h->dint.p + 7;   // cannot trip here: uncapped cells bound entries by 8 per box
+    CK(cudaMemsetAsync(ovf, 0, sizeof(int), st));
+    CK(cudaMemsetAsync(h->hcnt.p, 0, sizeof(int) * 2 * (M + 1), st));
+    launch_hash_insert(h->blo.p, h->bhi.p, Ns, Nt, Ne, ext, h->hmask, h->hcnt.p, nullptr, nullptr, 0, ovf, st);
+    scan_exclusive(h->hcnt.p, h->hstart.p, (int)(2 * (M + 1)), h->iscr.p, st);
+    CK(cudaMemsetAsync(h->hcnt.p, 0, sizeof(int) * 2 * (M + 1), st));
+    launch_hash_insert(h->blo.p, h->bhi.p, Ns, Nt, Ne, ext, h->hmask, h->hcnt.p, h->hstart.p, h->hent.p,
+                       (int)h->hent.n, ovf, st);
     for (int pass = 0; pass < 2; ++pass) {
         int counts[2];
         for (int kind = 0; kind < 2; ++kind) {   // 0 = PT (B = tris), 1 = EE (B = edges)
-            const int b0 = kind == 0 ? Ns : Ns + Nt, nb = kind == 0 ? Nt : Ne;
+            const int b0 = kind == 0 ? Ns : Ns + Nt;
             const int a0 = kind == 0 ? 0 : Ns + Nt, na = kind == 0 ? Ns : Ne;
-            int *hc = h->hcnt.p + (size_t)kind * (M + 1);
-            int *hs = h->hstart.p + (size_t)kind * (M + 1);
-            int *he = h->hent.p + (size_t)kind * (h->hent.n / 2);
-            CK(cudaMemsetAsync(hc, 0, sizeof(int) * (M + 1), st));
-            launch_hash_insert(h->blo.p, h->bhi.p, b0, nb, ext, h->hmask, hc, nullptr, nullptr, st);
-            scan_exclusive(hc, hs, (int)M, h->iscr.p, st);
-            CK(cudaMemsetAsync(hc, 0, sizeof(int) * (M + 1), st));
-            launch_hash_insert(h->blo.p, h->bhi.p, b0, nb, ext, h->hmask, hc, hs, he, st);
+            const int *hs = h->hstart.p + (size_t)kind * (M + 1), *he = h->hent.p;
             int *cnt = kind == 0 ? cnt_pt : cnt_ee;
             CK(cudaMemsetAsync(cnt, 0, sizeof(int), st));
             const int cap = (int)(h->cand.n / 2);
@@ -837,9 +833,9 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             while (M < 16u * (unsigned)std::max(m.Nt, m.Ne)) M <<= 1;
             h->hmask = M - 1;
             h->hcnt.exact(2 * (size_t)(M + 1));
-            h->hstart.exact(2 * (size_t)(M + 1));
-            h->hent.exact(2 * 8 * (size_t)std::max(1, std::max(m.Nt, m.Ne)));
-            h->iscr.ensure(scan_scratch_ints(M) + 1024);
+            h->hstart.exact(2 * (size_t)(M + 1) + 1);
+            h->hent.exact(64 * (size_t)std::max(1, m.Nt + m.Ne));
+            h->iscr.ensure(scan_scratch_ints(2 * (M + 1)) + scan_scratch_ints(m.Ns + m.Ne + 1) + 1024);
         }
         h->cell0 = std::max(m.mean_edge, 2.0 * d_hat);
         if (m.Nt > 0) {
@@ -939,7 +935,7 @@ void pd_ipc_destroy(pd_ipc *h) {
     for (auto &s : h->seqs) { rel(s->x); rel(s->A6); rel(s->p); }
     rel(h->fc); rel(h->G); rel(h->Z); rel(h->A9stage); rel(h->g_el); rel(h->s); rel(h->ds); rel(h->dx);
     rel(h->gs); rel(h->blo); rel(h->bhi); rel(h->hcnt); rel(h->hstart); rel(h->hent); rel(h->cand);
-    rel(h->qcnt); rel(h->qoff); rel(h->gsq);
+    rel(h->qcnt); rel(h->qoff); rel(h->qlist); rel(h->gsq);
     rel(h->cand_tmp); rel(h->akeys); rel(h->flag); rel(h->pos); rel(h->ctype); rel(h->atype); rel(h->ids);
     rel(h->iscr); rel(h->cd2); rel(h->ad2); rel(h->grad); rel(h->Hp); rel(h->dist); rel(h->mark);
     rel(h->spos); rel(h->qS); rel(h->rec); rel(h->rec_tmp); rel(h->bccnt); rel(h->bcoff); rel(h->ts_lo);

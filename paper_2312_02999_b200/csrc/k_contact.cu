@@ -14,6 +14,8 @@
 // THIS TRANSLATION UNIT IS COMPILED WITH -fmad=false: every product and sum is rounded
 // separately, exactly like the oracle's numpy ufuncs, so that the active set C and S are
 // bit-exact on identical positions.
+#include <climits>
+
 #include "kernels.h"
 
 #include "dev_common.cuh"
@@ -194,22 +196,40 @@ __device__ __forceinline__ void cell_range(double4 lo, double4 hi, double inv, i
     c0[2] = (int)floor(lo.z * inv); c1[2] = (int)floor(hi.z * inv);
 }
 
-// count / fill the hash table with the B-side boxes [b0, b0+nb)
+// a box may cover at most kMaxCells hash cells; larger ones flag overflow instead of looping
+constexpr long long kMaxCells = 4096;
+__device__ __forceinline__ bool range_ok(const int c0[3], const int c1[3]) {
+    return (long long)(c1[0] - c0[0] + 1) * (c1[1] - c0[1] + 1) * (c1[2] - c0[2] + 1) <= kMaxCells;
+}
+
+// Count / fill both hash tables in one launch: B-side boxes are the tris (kind 0, table 0) and the
+// edges (kind 1, table 1); box index Ns + i for i in [0, Nt + Ne).  Table k occupies buckets
+// [k (M+1), (k+1)(M+1)) of cnt/start; entries hold the kind-local B index.
 __global__ void k_hash_insert(const double4 *__restrict__ lo, const double4 *__restrict__ hi,
-                              int b0, int nb, const double *__restrict__ cell, unsigned mask,
+                              int Ns, int Nt, int Ne, const double *__restrict__ cell, unsigned mask,
                               int *__restrict__ cnt, const int *__restrict__ start,
-                              int *__restrict__ entries) {
+                              int *__restrict__ entries, int cap_entries, int *__restrict__ ovf) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nb) return;
-    const double inv = 1.0 / *cell;
+    if (i >= Nt + Ne) return;
+    const int kind = i < Nt ? 0 : 1, b = kind == 0 ? i : i - Nt;
+    const size_t tb = (size_t)kind * (mask + 2);
+    const double inv = 1.0 / fmin(cell[0], cell[1]);     // cell = [max extent, cap]
     int c0[3], c1[3];
-    cell_range(lo[b0 + i], hi[b0 + i], inv, c0, c1);
+    cell_range(lo[Ns + i], hi[Ns + i], inv, c0, c1);
+    if (!range_ok(c0, c1)) {   // outlier box under the capped cell size: unclamped sort path
+        if (entries) atomicExch(ovf, 1);
+        return;
+    }
     for (int x = c0[0]; x <= c1[0]; ++x)
         for (int y = c0[1]; y <= c1[1]; ++y)
             for (int z = c0[2]; z <= c1[2]; ++z) {
-                unsigned h = cell_hash(x, y, z, mask);
+                const size_t h = tb + cell_hash(x, y, z, mask);
                 int slot = atomicAdd(cnt + h, 1);
-                if (entries) entries[start[h] + slot] = i;
+                if (entries) {
+                    const int p = start[h] + slot;
+                    if (p < cap_entries) entries[p] = b;
+                    else atomicExch(ovf, 1);
+                }
             }
 }
 
@@ -229,7 +249,7 @@ __global__ void k_hash_query(const double4 *__restrict__ lo, const double4 *__re
                              int cap) {
     int a = blockIdx.x * blockDim.x + threadIdx.x;
     if (a >= na) return;
-    const double inv = 1.0 / *cell;
+    const double inv = 1.0 / fmin(cell[0], cell[1]);
     const double4 la = lo[a0 + a], ha = hi[a0 + a];
     int c0[3], c1[3];
     cell_range(la, ha, inv, c0, c1);
@@ -260,65 +280,135 @@ __global__ void k_hash_query(const double4 *__restrict__ lo, const double4 *__re
             }
 }
 
-// Sort-free variant: each query collects its partners, sorts and de-duplicates them locally,
-// so the concatenation over queries in index order IS the sorted unique key list.
-// pass 0 counts (cnt[a]), pass 1 writes at off[a].  ovf is set if a query exceeds kQCap.
-constexpr int kQCap = 128;
-__global__ void k_hash_query_local(const double4 *__restrict__ lo, const double4 *__restrict__ hi,
-                                   int a0, int na, int b0, int nB, const double *__restrict__ cell,
-                                   unsigned mask, const int *__restrict__ start,
-                                   const int *__restrict__ entries, int is_pt,
-                                   const int *__restrict__ tris, const int *__restrict__ edges,
-                                   int *__restrict__ cnt, const int *__restrict__ off,
-                                   unsigned long long *__restrict__ out, int *__restrict__ ovf) {
-    int a = blockIdx.x * blockDim.x + threadIdx.x;
-    if (a >= na) return;
-    int list[kQCap];
-    int n = 0;
-    const double inv = 1.0 / *cell;
-    const double4 la = lo[a0 + a], ha = hi[a0 + a];
+// Sort-free warp query: one warp per A box (PT points [0, Ns), then EE edges [Ns, Ns + Ne)).  The
+// warp flattens the (cell, bucket entry) pairs of the box's cell range 32 at a time, tests them in
+// parallel, collects hits in shared memory, then de-duplicates (hash collisions can repeat an
+// entry) and rank-sorts them, so list a is sorted and unique; concatenated in query order the
+// lists ARE the sorted unique key lists (keys a*nB + b).  Writes cnt[q] and qlist[q*kQCap ..].
+constexpr int kQCap = 256, kQWarps = 4;
+__global__ void __launch_bounds__(32 * kQWarps)
+k_hash_query_warp(const double4 *__restrict__ lo, const double4 *__restrict__ hi, int Ns, int Nt, int Ne,
+                  const double *__restrict__ cell, unsigned mask, const int *__restrict__ start,
+                  const int *__restrict__ entries, const int *__restrict__ tris,
+                  const int *__restrict__ edges, int *__restrict__ cnt, int *__restrict__ qlist,
+                  int *__restrict__ ovf) {
+    __shared__ int list[kQWarps][kQCap], key2[kQWarps][kQCap];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const int q = blockIdx.x * kQWarps + wl;
+    if (q >= Ns + Ne) return;
+    if (*ovf) {   // the table overflowed at insert: the sort path redoes this broad phase
+        if (lane == 0) cnt[q] = 0;
+        return;
+    }
+    const int is_pt = q < Ns, a = is_pt ? q : q - Ns;
+    const int abox = is_pt ? a : Ns + Nt + a, b0 = is_pt ? Ns : Ns + Nt;
+    const int *st = start + (is_pt ? 0 : (size_t)(mask + 2));
+    const double inv = 1.0 / fmin(cell[0], cell[1]);
+    const double4 la = lo[abox], ha = hi[abox];
     int c0[3], c1[3];
     cell_range(la, ha, inv, c0, c1);
-    int av[2] = {0, 0};
-    if (!is_pt) { av[0] = edges[2 * a]; av[1] = edges[2 * a + 1]; }
-    for (int x = c0[0]; x <= c1[0]; ++x)
-        for (int y = c0[1]; y <= c1[1]; ++y)
-            for (int z = c0[2]; z <= c1[2]; ++z) {
-                unsigned h = cell_hash(x, y, z, mask);
-                for (int k = start[h]; k < start[h + 1]; ++k) {
-                    int b = entries[k];
-                    if (!is_pt && b <= a) continue;
-                    const double4 lb = lo[b0 + b], hb = hi[b0 + b];
-                    if (!overlap(la, ha, lb, hb)) continue;
-                    int m0 = max(c0[0], (int)floor(lb.x * inv)), m1 = max(c0[1], (int)floor(lb.y * inv)),
-                        m2 = max(c0[2], (int)floor(lb.z * inv));
-                    if (m0 != x || m1 != y || m2 != z) continue;
+    if (!range_ok(c0, c1)) {
+        if (lane == 0) { atomicExch(ovf, 1); cnt[q] = 0; }
+        return;
+    }
+    const int ny = c1[1] - c0[1] + 1, nz = c1[2] - c0[2] + 1;
+    const int ncell = (c1[0] - c0[0] + 1) * ny * nz;
+    int av0 = 0, av1 = 0;
+    if (!is_pt) { av0 = edges[2 * a]; av1 = edges[2 * a + 1]; }
+    int n = 0;
+    bool over = false;
+    for (int cb = 0; cb < ncell; cb += 32) {
+        // lane j owns cell cb + j of the chunk: its bucket [s, s + len)
+        const int ci = cb + lane;
+        int bs = 0, len = 0;
+        if (ci < ncell) {
+            const int cx = c0[0] + ci / (ny * nz), cy = c0[1] + (ci / nz) % ny, cz = c0[2] + ci % nz;
+            const unsigned h = cell_hash(cx, cy, cz, mask);
+            bs = st[h];
+            len = st[h + 1] - bs;
+        }
+        int incl = len;
+        for (int o = 1; o < 32; o <<= 1) {
+            int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        for (int kb = 0; kb < total; kb += 32) {
+            const int k = kb + lane;
+            int j = 0;   // owner cell: smallest j with incl_j > k
+            for (int step = 16; step > 0; step >>= 1) {
+                int v = __shfl_sync(0xffffffffu, incl, j + step - 1);
+                if (v <= k) j += step;
+            }
+            const int sj = __shfl_sync(0xffffffffu, bs, j);
+            const int ej = __shfl_sync(0xffffffffu, incl, j) - __shfl_sync(0xffffffffu, len, j);
+            bool hit = false;
+            int b = 0;
+            if (k < total) {
+                b = entries[sj + (k - ej)];
+                const double4 lb = lo[b0 + b], hb = hi[b0 + b];
+                const int cj = cb + j;
+                const int x = c0[0] + cj / (ny * nz), y = c0[1] + (cj / nz) % ny, z = c0[2] + cj % nz;
+                hit = (is_pt || b > a) && overlap(la, ha, lb, hb) &&
+                      max(c0[0], (int)floor(lb.x * inv)) == x && max(c0[1], (int)floor(lb.y * inv)) == y &&
+                      max(c0[2], (int)floor(lb.z * inv)) == z;   // lowest shared cell only
+                if (hit) {
                     if (is_pt) {
-                        if (tris[3 * b] == a || tris[3 * b + 1] == a || tris[3 * b + 2] == a) continue;
+                        hit = tris[3 * b] != a && tris[3 * b + 1] != a && tris[3 * b + 2] != a;
                     } else {
-                        int b0v = edges[2 * b], b1v = edges[2 * b + 1];
-                        if (b0v == av[0] || b0v == av[1] || b1v == av[0] || b1v == av[1]) continue;
-                    }
-                    if (n < kQCap) {
-                        int i = n++;                       // insertion sort, drop duplicates
-                        while (i > 0 && list[i - 1] > b) { list[i] = list[i - 1]; --i; }
-                        if (i > 0 && list[i - 1] == b) {
-                            for (int j = i; j < n - 1; ++j) list[j] = list[j + 1];
-                            --n;
-                        } else {
-                            list[i] = b;
-                        }
-                    } else {
-                        atomicExch(ovf, 1);
+                        const int b0v = edges[2 * b], b1v = edges[2 * b + 1];
+                        hit = b0v != av0 && b0v != av1 && b1v != av0 && b1v != av1;
                     }
                 }
             }
-    if (!off) {
-        cnt[a] = n;
+            const unsigned m = __ballot_sync(0xffffffffu, hit);
+            const int pos = n + __popc(m & ((1u << lane) - 1u));
+            if (hit) {
+                if (pos < kQCap) list[wl][pos] = b;
+                else over = true;
+            }
+            n += __popc(m);
+        }
+    }
+    if (__any_sync(0xffffffffu, over)) {
+        if (lane == 0) { atomicExch(ovf, 1); cnt[q] = 0; }
         return;
     }
-    unsigned long long *o = out + off[a];
-    for (int i = 0; i < n; ++i) o[i] = (unsigned long long)a * (unsigned long long)nB + list[i];
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {   // drop repeats: keep the first occurrence
+        const int v = list[wl][i];
+        bool dup = false;
+        for (int t = 0; t < i && !dup; ++t) dup = list[wl][t] == v;
+        key2[wl][i] = dup ? INT_MAX : v;
+    }
+    __syncwarp();
+    int nu = 0;
+    int *out = qlist + (size_t)q * kQCap;
+    for (int i = lane; i < n; i += 32) {   // rank among the distinct values
+        const int v = key2[wl][i];
+        if (v == INT_MAX) continue;
+        int r = 0;
+        for (int t = 0; t < n; ++t) r += key2[wl][t] < v;
+        out[r] = v;
+        ++nu;
+    }
+    for (int o = 16; o > 0; o >>= 1) nu += __shfl_xor_sync(0xffffffffu, nu, o);
+    if (lane == 0) cnt[q] = nu;
+}
+
+// Emit the per-query lists at their scanned offsets as keys a*nB + b (PT block, then EE block).
+__global__ void __launch_bounds__(32 * kQWarps)
+k_hash_emit(int Ns, int Nt, int Ne, const int *__restrict__ cnt, const int *__restrict__ off,
+            const int *__restrict__ qlist, unsigned long long *__restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int q = blockIdx.x * kQWarps + (threadIdx.x >> 5);
+    if (q >= Ns + Ne) return;
+    const bool is_pt = q < Ns;
+    const unsigned long long a = is_pt ? q : q - Ns, nB = is_pt ? Nt : Ne;
+    const int c = cnt[q];
+    const int *l = qlist + (size_t)q * kQCap;
+    unsigned long long *o = out + off[q];
+    for (int i = lane; i < c; i += 32) o[i] = a * nB + (unsigned long long)l[i];
 }
 
 // ------------------------------------------------------------------ a5 narrow filter ------
@@ -993,9 +1083,12 @@ void launch_boxes(const double4 *s, const double4 *ds, const int *tris, const in
     int n = Ns + Nt + Ne;
     PDI_LAUNCH(k_boxes, (n + 255) / 256, 256, 0, st)(s, ds, tris, edges, Ns, Nt, Ne, infl, lo, hi, ext);
 }
-void launch_hash_insert(const double4 *lo, const double4 *hi, int b0, int nb, const double *cell,
-                        unsigned mask, int *cnt, const int *start, int *entries, cudaStream_t st) {
-    if (nb > 0) PDI_LAUNCH(k_hash_insert, (nb + 255) / 256, 256, 0, st)(lo, hi, b0, nb, cell, mask, cnt, start, entries);
+void launch_hash_insert(const double4 *lo, const double4 *hi, int Ns, int Nt, int Ne,
+                        const double *cell, unsigned mask, int *cnt, const int *start, int *entries,
+                        int cap_entries, int *ovf, cudaStream_t st) {
+    if (Nt + Ne > 0)
+        PDI_LAUNCH(k_hash_insert, (Nt + Ne + 255) / 256, 256, 0, st)(lo, hi, Ns, Nt, Ne, cell, mask, cnt,
+                                                                    start, entries, cap_entries, ovf);
 }
 void launch_hash_query(const double4 *lo, const double4 *hi, int a0, int na, int b0, int nB,
                        const double *cell, unsigned mask, const int *start, const int *entries,
@@ -1005,14 +1098,22 @@ void launch_hash_query(const double4 *lo, const double4 *hi, int a0, int na, int
         PDI_LAUNCH(k_hash_query, (na + 127) / 128, 128, 0, st)(lo, hi, a0, na, b0, nB, cell, mask, start,
                                                        entries, is_pt, tris, edges, out, count, cap);
 }
-void launch_hash_query_local(const double4 *lo, const double4 *hi, int a0, int na, int b0, int nB,
-                             const double *cell, unsigned mask, const int *start, const int *entries,
-                             int is_pt, const int *tris, const int *edges, int *cnt, const int *off,
-                             unsigned long long *out, int *ovf, cudaStream_t st) {
-    if (na > 0)
-        PDI_LAUNCH(k_hash_query_local, (na + 127) / 128, 128, 0, st)(lo, hi, a0, na, b0, nB, cell, mask,
-                                                                    start, entries, is_pt, tris, edges,
-                                                                    cnt, off, out, ovf);
+int hash_query_cap() { return kQCap; }
+void launch_hash_query_warp(const double4 *lo, const double4 *hi, int Ns, int Nt, int Ne,
+                            const double *cell, unsigned mask, const int *start, const int *entries,
+                            const int *tris, const int *edges, int *cnt, int *qlist, int *ovf,
+                            cudaStream_t st) {
+    const int nq = Ns + Ne;
+    if (nq > 0)
+        PDI_LAUNCH(k_hash_query_warp, (nq + kQWarps - 1) / kQWarps, 32 * kQWarps, 0, st)(
+            lo, hi, Ns, Nt, Ne, cell, mask, start, entries, tris, edges, cnt, qlist, ovf);
+}
+void launch_hash_emit(int Ns, int Nt, int Ne, const int *cnt, const int *off, const int *qlist,
+                      unsigned long long *out, cudaStream_t st) {
+    const int nq = Ns + Ne;
+    if (nq > 0)
+        PDI_LAUNCH(k_hash_emit, (nq + kQWarps - 1) / kQWarps, 32 * kQWarps, 0, st)(Ns, Nt, Ne, cnt, off,
+                                                                                 qlist, out);
 }
 void launch_narrow(const unsigned long long *keys, int n, int is_pt, int nB, const double4 *s,
                    const int *tris, const int *edges, int Nt, int Ne, double dh2, int *flag,

@@ -81,16 +81,20 @@ void contact_init();
 void launch_boxes(const double4 *s, const double4 *ds, const int *tris, const int *edges, int Ns,
                   int Nt, int Ne, double infl, double4 *lo, double4 *hi, double *ext,
                   cudaStream_t st);
-void launch_hash_insert(const double4 *lo, const double4 *hi, int b0, int nb, const double *cell,
-                        unsigned mask, int *cnt, const int *start, int *entries, cudaStream_t st);
+void launch_hash_insert(const double4 *lo, const double4 *hi, int Ns, int Nt, int Ne,
+                        const double *cell, unsigned mask, int *cnt, const int *start, int *entries,
+                        int cap_entries, int *ovf, cudaStream_t st);
 void launch_hash_query(const double4 *lo, const double4 *hi, int a0, int na, int b0, int nB,
                        const double *cell, unsigned mask, const int *start, const int *entries,
                        int is_pt, const int *tris, const int *edges, unsigned long long *out,
                        int *count, int cap, cudaStream_t st);
-void launch_hash_query_local(const double4 *lo, const double4 *hi, int a0, int na, int b0, int nB,
-                             const double *cell, unsigned mask, const int *start, const int *entries,
-                             int is_pt, const int *tris, const int *edges, int *cnt, const int *off,
-                             unsigned long long *out, int *ovf, cudaStream_t st);
+int hash_query_cap();
+void launch_hash_query_warp(const double4 *lo, const double4 *hi, int Ns, int Nt, int Ne,
+                            const double *cell, unsigned mask, const int *start, const int *entries,
+                            const int *tris, const int *edges, int *cnt, int *qlist, int *ovf,
+                            cudaStream_t st);
+void launch_hash_emit(int Ns, int Nt, int Ne, const int *cnt, const int *off, const int *qlist,
+                      unsigned long long *out, cudaStream_t st);
 void launch_narrow(const unsigned long long *keys, int n, int is_pt, int nB, const double4 *s,
                    const int *tris, const int *edges, int Nt, int Ne, double dh2, int *flag,
                    int *type, double *d2, cudaStream_t st);
