@@ -156,7 +156,9 @@ struct pd_ipc {
     DevFactor F;
     DBuf<int> f_c0, f_rowptr, f_rows, f_parent, f_seg_ptr, f_seg_d, f_seg_klo, f_seg_khi, f_fd, f_col2sn;
     DBuf<long long> f_valptr, f_dinv_ptr;
-    DBuf<double> f_L, f_dinv, Ug, Up;
+    DBuf<double> f_L, f_dinv, Ug, Up, Yw, bw_P;
+    DBuf<int2> f_bw_items, f_rc_src;
+    DBuf<int> f_bw_pbase, bw_cnt, f_ford;
     DBuf<int> f_uoff, f_urow_sn, f_rc_ptr, f_rc_idx, f_urel, f_ch_ptr, f_ch;
     // sequences
     std::vector<std::unique_ptr<Seq>> seqs;
@@ -460,14 +462,13 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
     const DevFactor &F = h->F;
     CK(cudaMemsetAsync(h->ticket.p, 0, 2 * sizeof(int), st));
     kt.start(K_FWD, st);
-    launch_ts_items(F.sn_c0, F.sn_fd, F.sn_parent, F.nsn, h->qS.p, nS_dev, h->ts_lo.p, h->ts_hi.p,
-                    h->ts_cnt.p, h->ts_rem.p, st);
+    launch_ts_items(F, h->qS.p, nS_dev, h->ts_lo.p, h->ts_hi.p, h->ts_cnt.p, h->ts_rem.p, st);
     scan_exclusive(h->ts_cnt.p, h->ts_ptr.p, F.nsn, h->iscr.p, st);
     const int ldu = std::max(32, ((nS + 31) / 32) * 32);
     if (nS > 0) h->Up.ensure((size_t)std::max(1, F.nU) * ldu);
-    if (h->trace_file) h->trace.ensure(4 * (size_t)F.nsn * (2 + (h->capS + 31) / 32));
+    if (h->trace_file) h->trace.ensure(4 * (size_t)F.bw_nblocks * (2 + (h->capS + 31) / 32));
     launch_forward_solve(F, h->ts_lo.p, h->ts_hi.p, h->ts_ptr.p, h->qS.p, h->ts_rem.p, h->ticket.p, h->G.p,
-                         h->V.p, h->ldv, h->Ug.p, nS > 0 ? h->Up.p : nullptr, ldu, h->nsm,
+                         h->Yw.p, h->V.p, h->ldv, h->Ug.p, nS > 0 ? h->Up.p : nullptr, ldu, h->nsm,
                          h->trace_file ? h->trace.p : nullptr, st);
     if (h->trace_file && nS > 0 && std::ftell(h->trace_file) < (30l << 20)) {
         int nitems;
@@ -489,7 +490,7 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
             h->sprof.ensure(1024);
             CK(cudaMemsetAsync(h->sprof.p, 0, 1024 * 8, st));
         }
-        CK((cudaError_t)launch_schur(F, h->V.p, h->ldv, h->G.p, h->qS.p, h->ts_lo.p, h->ts_hi.p, nS, h->K.p,
+        CK((cudaError_t)launch_schur(F, h->V.p, h->ldv, h->Yw.p, h->qS.p, h->ts_lo.p, h->ts_hi.p, nS, h->K.p,
                                      ldk, h->Bc.p, ldb, h->Sh.p, h->ldh, h->Lstore.p, h->Tt.p, h->U.p,
                                      h->yS.p, h->u.p, h->tv.p, h->Z.p, info,
                                      h->trace_file ? h->sprof.p : nullptr, st));
@@ -501,11 +502,11 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
             fflush(h->schur_file);
         }
     } else {
-        CK(cudaMemcpyAsync(h->Z.p, h->G.p, sizeof(double) * 4 * nf, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(h->Z.p, h->Yw.p, sizeof(double) * 4 * nf, cudaMemcpyDeviceToDevice, st));
     }
     kt.stop(K_DENSE, st);
     kt.start(K_BWD, st);
-    launch_backward_solve(F, h->ts_done.p, h->ticket.p, h->Z.p, h->nsm, st);
+    launch_backward_solve(F, h->ts_done.p, h->bw_cnt.p, h->ticket.p, h->bw_P.p, h->Z.p, h->nsm, st);
     kt.stop(K_BWD, st);
     CK(cudaMemsetAsync(h->dx.p, 0, sizeof(double4) * h->n, st));
     launch_scatter_dx(h->Z.p, h->q2v.p, nf, h->dx.p, st);
@@ -736,11 +737,51 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             std::vector<long long> vp(f.sn_valptr.begin(), f.sn_valptr.end());
             h->f_valptr.upload(vp.data(), vp.size());
         }
-        h->f_L.upload(f.vals.data(), f.vals.size());
+        h->f_L.upload(f.Q.data(), f.Q.size());
+        {   // Item dispatch orders (list scheduling on the elimination tree).  Forward: by
+            // decreasing cost-to-root (a child always precedes its parent), so the items on the
+            // longest chains start first.  Backward: by decreasing height (a parent precedes
+            // its children).  cost(s) = its row blocks.
+            const int nsn = f.nsn;
+            std::vector<int> nbk(nsn);
+            std::vector<double> ctr(nsn, 0.0), hgt(nsn, 0.0);
+            for (int s = 0; s < nsn; ++s)
+                nbk[s] = (f.sn_rowptr[s + 1] - f.sn_rowptr[s] + kSolveRB - 1) / kSolveRB;
+            for (int s = nsn - 1; s >= 0; --s)    // parents have larger postorder indices
+                ctr[s] = nbk[s] + (f.sn_parent[s] >= 0 ? ctr[f.sn_parent[s]] : 0.0);
+            for (int s = 0; s < nsn; ++s) {
+                hgt[s] += nbk[s];
+                if (f.sn_parent[s] >= 0) hgt[f.sn_parent[s]] = std::max(hgt[f.sn_parent[s]], hgt[s]);
+            }
+            std::vector<int> ford(nsn), bord(nsn);
+            for (int s = 0; s < nsn; ++s) ford[s] = bord[s] = s;
+            std::stable_sort(ford.begin(), ford.end(), [&](int a, int b) { return ctr[a] > ctr[b]; });
+            std::stable_sort(bord.begin(), bord.end(), [&](int a, int b) { return hgt[a] > hgt[b]; });
+            h->f_ford.upload(ford.data(), ford.size());
+            std::vector<int2> items;
+            std::vector<int> pbase(nsn);
+            int nblk = 0;
+            for (int s : bord) {
+                pbase[s] = nblk;
+                nblk += nbk[s];
+                for (int b = 0; b < nbk[s]; ++b) items.push_back(make_int2(s, b));
+            }
+            h->f_bw_items.upload(items.data(), items.size());
+            h->f_bw_pbase.upload(pbase.data(), pbase.size());
+            h->F.bw_nitems = (int)items.size();
+            h->F.bw_nblocks = nblk;
+            h->bw_P.exact((size_t)nblk * 128 * 4);
+            h->bw_cnt.exact(f.nsn);
+        }
         h->f_uoff.upload(f.uoff.data(), f.uoff.size());
         h->f_urow_sn.upload(f.urow_sn.data(), f.urow_sn.size());
         h->f_rc_ptr.upload(f.rc_ptr.data(), f.rc_ptr.size());
         h->f_rc_idx.upload(f.rc_idx.data(), f.rc_idx.size());
+        {   // (U row, owner child) per extend-add source
+            std::vector<int2> src(f.rc_idx.size());
+            for (size_t j = 0; j < src.size(); ++j) src[j] = make_int2(f.rc_idx[j], f.urow_sn[f.rc_idx[j]]);
+            h->f_rc_src.upload(src.data(), src.size());
+        }
         h->f_urel.upload(f.urel.data(), f.urel.size());
         h->f_ch_ptr.upload(f.ch_ptr.data(), f.ch_ptr.size());
         h->f_ch.upload(f.ch.data(), f.ch.size());
@@ -752,11 +793,13 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         h->Ug.exact(4 * (size_t)std::max(1, f.uoff[f.nsn]));
         DevFactor &F = h->F;
         F.uoff = h->f_uoff.p; F.urow_sn = h->f_urow_sn.p; F.rc_ptr = h->f_rc_ptr.p; F.rc_idx = h->f_rc_idx.p;
+        F.rc_src = h->f_rc_src.p;
         F.dinv_ptr = h->f_dinv_ptr.p; F.dinv = h->f_dinv.p; F.nU = f.uoff[f.nsn];
         F.urel = h->f_urel.p; F.ch_ptr = h->f_ch_ptr.p; F.ch = h->f_ch.p;
         F.nf = f.nf; F.nsn = f.nsn;
         F.sn_c0 = h->f_c0.p; F.sn_rowptr = h->f_rowptr.p; F.sn_rows = h->f_rows.p; F.sn_parent = h->f_parent.p;
-        F.sn_valptr = h->f_valptr.p; F.L = h->f_L.p;
+        F.sn_valptr = h->f_valptr.p; F.Q = h->f_L.p;
+        F.bw_items = h->f_bw_items.p; F.bw_pbase = h->f_bw_pbase.p; F.ford = h->f_ford.p;
         F.seg_ptr = h->f_seg_ptr.p; F.seg_d = h->f_seg_d.p; F.seg_klo = h->f_seg_klo.p; F.seg_khi = h->f_seg_khi.p;
         F.sn_fd = h->f_fd.p; F.col2sn = h->f_col2sn.p;
         // contact capacity: S is a subset of the free vertices in the W support (n2)
@@ -786,6 +829,7 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         h->fc.exact(12 * (size_t)m.T);
         h->g_el.exact(nf);
         h->G.exact(4 * (size_t)nf);
+        h->Yw.exact(4 * (size_t)nf);
         h->Z.exact(4 * (size_t)nf);
         h->dx.exact(m.n);
         h->s.exact(std::max(1, m.Ns));
@@ -930,7 +974,7 @@ void pd_ipc_destroy(pd_ipc *h) {
     rel(h->Wp); rel(h->Wc); rel(h->WTp); rel(h->WTr); rel(h->tris); rel(h->edges); rel(h->Wv); rel(h->WTv);
     rel(h->f_c0); rel(h->f_rowptr); rel(h->f_rows); rel(h->f_parent); rel(h->f_seg_ptr); rel(h->f_seg_d);
     rel(h->f_seg_klo); rel(h->f_seg_khi); rel(h->f_fd); rel(h->f_col2sn); rel(h->f_valptr); rel(h->f_L);
-    rel(h->f_dinv_ptr); rel(h->f_dinv); rel(h->Ug); rel(h->Up); rel(h->f_uoff); rel(h->f_urow_sn);
+    rel(h->f_dinv_ptr); rel(h->f_dinv); rel(h->Ug); rel(h->Up); rel(h->Yw); rel(h->bw_P); rel(h->f_bw_items); rel(h->f_ford); rel(h->f_rc_src); rel(h->f_bw_pbase); rel(h->bw_cnt); rel(h->f_uoff); rel(h->f_urow_sn);
     rel(h->f_rc_ptr); rel(h->f_rc_idx); rel(h->f_urel); rel(h->f_ch_ptr); rel(h->f_ch);
     for (auto &s : h->seqs) { rel(s->x); rel(s->A6); rel(s->p); }
     rel(h->fc); rel(h->G); rel(h->Z); rel(h->A9stage); rel(h->g_el); rel(h->s); rel(h->ds); rel(h->dx);

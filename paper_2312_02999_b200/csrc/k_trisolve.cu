@@ -34,13 +34,15 @@ constexpr int kLD = kPT + 1;           // smem row stride
 // waiting CTA records the fault in ticket[1] and proceeds instead of hanging the GPU.
 constexpr long long kSpinLimit = 4000000000LL;
 
-// per-iteration item setup: active column ranges and item counts
-__global__ void k_ts_items(const int *__restrict__ sn_c0, const int *__restrict__ sn_fd,
+// per-iteration item setup: active column ranges and item counts (row blocks x (1 + tiles))
+__global__ void k_ts_items(const int *__restrict__ ford, const int *__restrict__ sn_c0,
+                           const int *__restrict__ sn_rowptr, const int *__restrict__ sn_fd,
                            const int *__restrict__ sn_parent, int nsn, const int *__restrict__ qS,
-                           const int *__restrict__ nS_ptr, int *__restrict__ lo,
-                           int *__restrict__ hi, int *__restrict__ cnt, int *__restrict__ rem) {
-    int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= nsn) return;
+                           const int *__restrict__ nS_ptr, int *__restrict__ lo, int *__restrict__ hi,
+                           int *__restrict__ cnt, int *__restrict__ rem) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;   // dispatch position
+    if (k >= nsn) return;
+    const int s = ford[k];
     const int nS = *nS_ptr;
     const int a = sn_fd[s], b = sn_c0[s + 1];
     int l = 0, r = nS;
@@ -51,23 +53,23 @@ __global__ void k_ts_items(const int *__restrict__ sn_c0, const int *__restrict_
     int H0 = l;
     lo[s] = L0;
     hi[s] = H0;
-    int c = 1 + (H0 > L0 ? (H0 - 1) / kPT - L0 / kPT + 1 : 0);
-    cnt[s] = c;
+    const int nb = (sn_rowptr[s + 1] - sn_rowptr[s] + kSolveRB - 1) / kSolveRB;
+    int c = nb * (1 + (H0 > L0 ? (H0 - 1) / kPT - L0 / kPT + 1 : 0));
+    cnt[k] = c;
     int p = sn_parent[s];
     if (p >= 0) atomicAdd(rem + p, c);
 }
 
 struct FwdArgs {
-    const int *sn_c0, *sn_rowptr, *sn_parent;
+    const int *sn_c0, *sn_rowptr, *sn_parent, *uoff, *rc_ptr;
+    const int2 *rc_src;
     const long long *sn_valptr;
-    const double *L;
-    const int *uoff, *urel, *ch_ptr, *ch;
-    const long long *dinv_ptr;
-    const double *dinv;
-    const int *lo, *hi, *item_ptr, *qS;
+    const double *Q;
+    const int *lo, *hi, *item_ptr, *qS, *ford;
     int nsn;
     int *rem, *ticket;
-    double *G;                         // [nf][4] in: Pi g-hat, out: w
+    const double *G;                   // [nf][4] Pi g-hat
+    double *Y;                         // [nf][4] out: w = L^{-1} Pi g-hat
     double *V;                         // [nf][ldv] panel
     int ldv;
     double *Ug;                        // [nU][4] gradient update rows
@@ -131,60 +133,54 @@ __device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double
 constexpr int kSS = 36;
 constexpr int kXS = 40;
 
-// Out[i][n] = sum_k M[i][k] In[k][n] for i < m, n < 8*NCT, k < kdim (k <= i if LOWER), on DMMA.
-// M[i][k] at M + i*ldm_row + k*ldm_col; 32-column slabs of M are staged in Sg with cp.async.
-// In rows >= kdim must be zero (callers zero them).  Warp w owns the 8x8 tiles t = w + 8j of
-// the (ceil(m/8) x NCT) tile grid.
-// TRI: 0 full, 1 lower (k <= i), 2 upper (k >= i)
-template <int TRI>
-__device__ __forceinline__ void stage_slab(const double *M, long long ldm_row, long long ldm_col,
-                                           int m, int mr, int kc, int kn, double (*Sg)[kSS]) {
+constexpr int kSgRows = 256;
+constexpr int kMaxSrc = 4;             // cached extend-add sources per row (more: list walk)           // staged A-operand rows (all k-slabs of one block)
+
+// Issue (without waiting) the cp.async copies of A = M[0..m) x [0..kdim) into Sg as
+// ceil(kdim/32) slabs of round8(m) rows; out-of-range entries are zeroed.
+// M[i][k] at M + i*ldm_row + k*ldm_col.  Requires ceil(kdim/32) * round8(m) <= kSgRows.
+__device__ __forceinline__ void stage_block(const double *M, long long ldm_row, long long ldm_col,
+                                            int m, int kdim, double (*Sg)[kSS]) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (ldm_row == 1) {                     // column-major source: coalesce over i
-        for (int kk = wid; kk < 32; kk += kTS_NT / 32)
-            for (int i = lane; i < mr; i += 32) {
-                if (i < m && kk < kn && (TRI == 0 || (TRI == 1 ? kc + kk <= i : kc + kk >= i)))
-                    cp_async8(&Sg[i][kk], M + (long long)i + (long long)(kc + kk) * ldm_col);
+    const int mr = (m + 7) & ~7, nch = (kdim + 31) >> 5;
+    for (int ch = 0; ch < nch; ++ch) {
+        double (*S)[kSS] = Sg + ch * mr;
+        const int kc = ch * 32;
+        if (ldm_row == 1) {                 // column-major source: coalesce over i
+            for (int kk = wid; kk < 32; kk += kTS_NT / 32)
+                for (int i = lane; i < mr; i += 32) {
+                    if (i < m && kc + kk < kdim)
+                        cp_async8(&S[i][kk], M + (long long)i + (long long)(kc + kk) * ldm_col);
+                    else
+                        S[i][kk] = 0.0;
+                }
+        } else {                            // row-major source: coalesce over k
+            for (int i = wid; i < mr; i += kTS_NT / 32) {
+                if (i < m && kc + lane < kdim)
+                    cp_async8(&S[i][lane], M + (long long)i * ldm_row + (long long)(kc + lane) * ldm_col);
                 else
-                    Sg[i][kk] = 0.0;
+                    S[i][lane] = 0.0;
             }
-    } else {                                // row-major source: coalesce over k
-        for (int i = wid; i < mr; i += kTS_NT / 32) {
-            const int kk = lane;
-            if (i < m && kk < kn && (TRI == 0 || (TRI == 1 ? kc + kk <= i : kc + kk >= i)))
-                cp_async8(&Sg[i][kk], M + (long long)i * ldm_row + (long long)(kc + kk) * ldm_col);
-            else
-                Sg[i][kk] = 0.0;
         }
     }
     cp_async_commit();
 }
 
-// Sg points at TWO slab buffers (double buffering: chunk c+1 is in flight while chunk c runs).
-template <int TRI, int NCT, bool ACC = false>
-__device__ __forceinline__ void slab_dmma(const double *M, long long ldm_row, long long ldm_col,
-                                          int m, int kdim, const double (*In)[kXS],
-                                          double (*Sg)[kSS], double (*Out)[kXS]) {
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int rt = (m + 7) >> 3, ntiles = rt * NCT, mr = rt * 8;
-    constexpr int kMaxT = (kTS_W / 8) * NCT / 8;       // tiles per warp (16*NCT/8)
+// Out[i][n] = sum_k A[i][k] In[k][n] (i < m, n < 8*NCT) on DMMA from the staged block; In rows
+// in [kdim, 32*ceil(kdim/32)) must be zero.  Warp w owns 8x8 tiles t = w + 8j.  Caller has
+// waited for the staging and synchronised.
+template <int NCT, int MAXRT>
+__device__ __forceinline__ void block_dmma(int m, int kdim, const double (*Sg)[kSS],
+                                           const double (*In)[kXS], double (*Out)[kXS]) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int rt = (m + 7) >> 3, ntiles = rt * NCT, mr = rt * 8, nch = (kdim + 31) >> 5;
+    constexpr int kMaxT = (MAXRT * NCT + 7) / 8;
     double acc[kMaxT][2];
 #pragma unroll
     for (int j = 0; j < kMaxT; ++j) acc[j][0] = acc[j][1] = 0.0;
     const int gr = lane >> 2, gc = lane & 3;
-    const int nch = (kdim + 31) / 32;
-    stage_slab<TRI>(M, ldm_row, ldm_col, m, mr, 0, min(32, kdim), Sg);
     for (int ch = 0; ch < nch; ++ch) {
-        const int kc = ch * 32;
-        double (*B)[kSS] = Sg + (ch & 1) * kTS_W;
-        if (ch + 1 < nch) {
-            stage_slab<TRI>(M, ldm_row, ldm_col, m, mr, kc + 32, min(32, kdim - kc - 32),
-                              Sg + ((ch + 1) & 1) * kTS_W);
-            cp_async_wait_group<1>();
-        } else {
-            cp_async_wait_group<0>();
-        }
-        __syncthreads();
+        const double (*S)[kSS] = Sg + ch * mr;
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
 #pragma unroll
@@ -192,13 +188,11 @@ __device__ __forceinline__ void slab_dmma(const double *M, long long ldm_row, lo
                 const int t = wid + 8 * j;
                 if (t < ntiles) {
                     const int tr = t / NCT, tc = t % NCT;
-                    const double a = B[tr * 8 + gr][ks * 4 + gc];
-                    const double b = In[kc + ks * 4 + gc][tc * 8 + gr];
-                    dmma884(acc[j][0], acc[j][1], a, b);
+                    dmma884(acc[j][0], acc[j][1], S[tr * 8 + gr][ks * 4 + gc],
+                            In[ch * 32 + ks * 4 + gc][tc * 8 + gr]);
                 }
             }
         }
-        __syncthreads();
     }
 #pragma unroll
     for (int j = 0; j < kMaxT; ++j) {
@@ -207,27 +201,29 @@ __device__ __forceinline__ void slab_dmma(const double *M, long long ldm_row, lo
             const int tr = t / NCT, tc = t % NCT;
             const int r = tr * 8 + gr, c = tc * 8 + 2 * gc;
             if (r < m) {
-                if (ACC) {
-                    Out[r][c] += acc[j][0];
-                    Out[r][c + 1] += acc[j][1];
-                } else {
-                    Out[r][c] = acc[j][0];
-                    Out[r][c + 1] = acc[j][1];
-                }
+                Out[r][c] = acc[j][0];
+                Out[r][c + 1] = acc[j][1];
             }
         }
     }
-    __syncthreads();
 }
 
+// Forward solve.  Item (s, tile tk, row block b): tk = 0 is the 3-column gradient RHS, tk >= 1
+// the 32-column panel tiles active in s; rows [64b, 64b + 64) of s's row list R_s.
+//   X   = rhs_s - (children's update rows landing on s's columns)      (w x ncols, gathered)
+//   O   = Q_s[rows] X                                                   (DMMA)
+//   rows < w:  the solution rows of s (w = L^{-1} Pi g, or V);
+//   rows >= w: U_s rows = O + children's update rows landing there (consumed by the parent).
+// Every item of s depends only on s's children (Q_s folds L_ss^{-1} into the off-diagonal
+// block), so the row blocks of one supernode run on different SMs at the same time.
 __global__ void __launch_bounds__(kTS_NT) k_forward_solve(FwdArgs A) {
     extern __shared__ double fsm[];
     double (*X)[kXS] = reinterpret_cast<double (*)[kXS]>(fsm);
-    double (*Y)[kXS] = reinterpret_cast<double (*)[kXS]>(fsm + kTS_W * kXS);
-    double (*Sg)[kSS] = reinterpret_cast<double (*)[kSS]>(fsm + 2 * kTS_W * kXS);
+    double (*O)[kXS] = reinterpret_cast<double (*)[kXS]>(fsm + kTS_W * kXS);
+    double (*Sg)[kSS] = reinterpret_cast<double (*)[kSS]>(fsm + (kTS_W + kSolveRB) * kXS);
     __shared__ int sh_item;
-    __shared__ int prel[kTS_W];
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    __shared__ int src_n[kTS_W + kSolveRB], src_u[kTS_W + kSolveRB][kMaxSrc];
+    const int tid = threadIdx.x;
     const int total = A.item_ptr[A.nsn];
     while (true) {
         if (tid == 0) sh_item = atomicAdd(A.ticket, 1);
@@ -235,8 +231,22 @@ __global__ void __launch_bounds__(kTS_NT) k_forward_solve(FwdArgs A) {
         const int item = sh_item;
         __syncthreads();
         if (item >= total) return;
-        const int s = find_sn(A.item_ptr, A.nsn, item);
-        const int tk = item - A.item_ptr[s];
+        const int kpos = find_sn(A.item_ptr, A.nsn, item), s = A.ford[kpos];
+        const int c0 = A.sn_c0[s], w = A.sn_c0[s + 1] - c0;
+        const int slot0 = A.sn_rowptr[s], nr = A.sn_rowptr[s + 1] - slot0;
+        const int nb = (nr + kSolveRB - 1) / kSolveRB;
+        const int idx = item - A.item_ptr[kpos], tk = idx / nb, rb = (idx % nb) * kSolveRB;
+        const int m = min(kSolveRB, nr - rb);
+        const bool grad = tk == 0;
+        int lo_s = 0, hi_s = 0, tbase = 0;
+        if (!grad) {
+            lo_s = A.lo[s];
+            hi_s = A.hi[s];
+            tbase = (lo_s / kPT + tk - 1) * kPT;
+        }
+        const int ncc = grad ? 3 : 32;
+        // Q block rows in flight while we wait for the children and gather the RHS
+        stage_block(A.Q + A.sn_valptr[s] + rb, 1, nr, m, w, Sg);
         if (tid == 0) {
             if (A.trace) {
                 A.trace[4 * (size_t)item] = ((unsigned long long)s << 16) | (unsigned)tk;
@@ -246,136 +256,105 @@ __global__ void __launch_bounds__(kTS_NT) k_forward_solve(FwdArgs A) {
             if (A.trace) A.trace[4 * (size_t)item + 2] = gtimer();
         }
         __syncthreads();
-        const int c0 = A.sn_c0[s], w = A.sn_c0[s + 1] - c0;
-        const int nr = A.sn_rowptr[s + 1] - A.sn_rowptr[s], noff = nr - w;
-        const double *Ls = A.L + A.sn_valptr[s];
-        const double *D = A.dinv + A.dinv_ptr[s];
-        const int u0 = A.uoff[s];
-        const bool grad = tk == 0;
-        int lo_s = 0, hi_s = 0, tbase = 0;
-        if (!grad) {
-            lo_s = A.lo[s];
-            hi_s = A.hi[s];
-            tbase = (lo_s / kPT + tk - 1) * kPT;
-        }
-        const int col = tbase + lane;
-        const int ncc = grad ? 3 : 32;
-        // ---- 1. right-hand side block (rows >= w zeroed: they feed the DMMA k-padding)
-        for (int e = tid; e < kTS_W * 32; e += kTS_NT) {
-            const int j = e >> 5, c = e & 31;
-            double b = 0.0;
-            if (j < w) {
-                if (grad) b = c < 3 ? __ldcg(A.G + (size_t)(c0 + j) * 4 + c) : 0.0;
-                else {
-                    const int cc = tbase + c;
-                    b = (cc >= lo_s && cc < hi_s && A.qS[cc] == c0 + j) ? 1.0 : 0.0;
-                }
-            }
-            X[j][c] = b;
-        }
-        __syncthreads();
-        // ---- 2. children's update rows landing on s's columns (extend-add, child by child,
-        //         128-row chunks staged with cp.async into Y, which is free until step 3)
-        const int cb0 = A.ch_ptr[s], cb1 = A.ch_ptr[s + 1];
-        for (int ci = cb0; ci < cb1; ++ci) {
-            const int c = A.ch[ci];
-            if (!grad && !has_tile(A.lo[c], A.hi[c], tbase)) continue;   // zero contribution
-            const int uc = A.uoff[c], nc = A.uoff[c + 1] - uc;
-            for (int kb = 0; kb < nc; kb += kTS_W) {
-                const int m = min(kTS_W, nc - kb);
-                for (int k = wid; k < m; k += kTS_NT / 32) {
-                    if (lane < ncc) {
-                        const double *src = grad ? A.Ug + (size_t)(uc + kb + k) * 4 + lane
-                                                 : A.Up + (size_t)(uc + kb + k) * A.ldu + tbase + lane;
-                        cp_async8(&Y[k][lane], src);
-                    }
-                }
-                for (int k = tid; k < m; k += kTS_NT) prel[k] = __ldg(A.urel + uc + kb + k);
-                cp_async_wait_all();
-                __syncthreads();
-                for (int k = wid; k < m; k += kTS_NT / 32) {
-                    const int p = prel[k];
-                    if (p < w && lane < ncc) X[p][lane] -= Y[k][lane];
-                }
-                __syncthreads();
-            }
-        }
-        // ---- 3. Y = Dinv X  (D row-major w x w, lower).  Panel: DMMA on staged slabs.
-        //         Gradient (3 columns, no reuse to exploit): thread per row straight from L2,
-        //         all loads independent.
-        if (grad) slab_dmma<1, 1>(D, w, 1, w, w, X, Sg, Y);
-        else slab_dmma<1, 4>(D, w, 1, w, w, X, Sg, Y);
-        for (int e = tid; e < kTS_W * 32; e += kTS_NT) {
-            const int i = e >> 5, c = e & 31;
-            if (i >= w) { Y[i][c] = 0.0; continue; }        // k-padding of step 4
-            if (grad) {
-                if (c < 3) A.G[(size_t)(c0 + i) * 4 + c] = Y[i][c];
-            } else {
-                const int cc = tbase + c;
-                if (cc >= lo_s && cc < hi_s) A.V[(size_t)(c0 + i) * A.ldv + cc] = Y[i][c];
-            }
-        }
-        __syncthreads();
-        // ---- 4. U_s = L_off Y  (L column-major, ld nr) on DMMA, 128-row blocks through X
-        if (grad) {
-            for (int rb = 0; rb < noff; rb += kTS_W) {
-                const int m = min(kTS_W, noff - rb);
-                slab_dmma<0, 1>(Ls + w + rb, 1, nr, m, w, Y, Sg, X);
-                for (int e = tid; e < m * 4; e += kTS_NT) {
-                    const int r = e >> 2, c = e & 3;
-                    A.Ug[(size_t)(u0 + rb + r) * 4 + c] = c < 3 ? X[r][c] : 0.0;
-                }
-                __syncthreads();
-            }
-        } else {
-            for (int rb = 0; rb < noff; rb += kTS_W) {
-                const int m = min(kTS_W, noff - rb);
-                slab_dmma<0, 4>(Ls + w + rb, 1, nr, m, w, Y, Sg, X);
-                for (int e = tid; e < m * 32; e += kTS_NT) {
-                    const int r = e >> 5, c = e & 31;
-                    A.Up[(size_t)(u0 + rb + r) * A.ldu + tbase + c] = X[r][c];
-                }
-                __syncthreads();
-            }
-        }
-        // ---- 5. + children's update rows landing on s's off rows (block-private RMW; the
-        //         child rows are staged in X; 16 loads batched per thread)
-        for (int ci = cb0; ci < cb1; ++ci) {
-            const int c = A.ch[ci];
-            if (!grad && !has_tile(A.lo[c], A.hi[c], tbase)) continue;
-            const int uc = A.uoff[c], nc = A.uoff[c + 1] - uc;
-            for (int kb = 0; kb < nc; kb += kTS_W) {
-                const int m = min(kTS_W, nc - kb);
-                for (int k = wid; k < m; k += kTS_NT / 32) {
-                    if (lane < ncc) {
-                        const double *src = grad ? A.Ug + (size_t)(uc + kb + k) * 4 + lane
-                                                 : A.Up + (size_t)(uc + kb + k) * A.ldu + tbase + lane;
-                        cp_async8(&X[k][lane], src);
-                    }
-                }
-                for (int k = tid; k < m; k += kTS_NT) prel[k] = __ldg(A.urel + uc + kb + k);
-                cp_async_wait_all();
-                __syncthreads();
-                double cur[kTS_W / 8];
-                double *dst[kTS_W / 8];
+        // ---- extend-add sources of the rows this item touches: list slot q < w is column row
+        //      q (for X), slot w + i is row rb + i (epilogue, off rows only).  Resolved once,
+        //      thread per row, so the value gathers below are independent loads.
+        const double *Usrc = grad ? A.Ug : A.Up;
+        double *Udst = grad ? A.Ug : A.Up;
+        const int ldsrc = grad ? 4 : A.ldu, coff = grad ? 0 : tbase;
+        for (int q = tid; q < w + m; q += kTS_NT) {
+            const int row = q < w ? q : rb + q - w;
+            int cnt = 0;
+            if (q < w || row >= w) {
+                const int j0 = A.rc_ptr[slot0 + row], j1 = A.rc_ptr[slot0 + row + 1];
+                for (int jb = j0; jb < j1; jb += 4) {
+                    int2 sr[4];
 #pragma unroll
-                for (int q = 0; q < kTS_W / 8; ++q) {
-                    const int k = wid + 8 * q;
-                    dst[q] = nullptr;
-                    cur[q] = 0.0;
-                    if (k < m && lane < ncc) {
-                        const int p = prel[k];
-                        if (p >= w) {
-                            dst[q] = grad ? A.Ug + (size_t)(u0 + p - w) * 4 + lane
-                                          : A.Up + (size_t)(u0 + p - w) * A.ldu + tbase + lane;
-                            cur[q] = __ldcg(dst[q]);
+                    for (int k = 0; k < 4; ++k) sr[k] = jb + k < j1 ? A.rc_src[jb + k] : make_int2(-1, -1);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        if (sr[k].x < 0) continue;
+                        if (grad || has_tile(A.lo[sr[k].y], A.hi[sr[k].y], tbase)) {
+                            if (cnt < kMaxSrc) src_u[q][cnt] = sr[k].x;
+                            ++cnt;
                         }
                     }
                 }
+            }
+            src_n[q] = cnt;
+        }
+        __syncthreads();
+        // ---- X: rhs minus the children's rows landing on s's columns (fixed child order)
+        const int kpad = (w + 31) & ~31, ncw = grad ? 8 : 32, lg = grad ? 3 : 5;
+        for (int e0 = 0; e0 < kpad * ncw; e0 += 4 * kTS_NT) {
+            double v[4];
 #pragma unroll
-                for (int q = 0; q < kTS_W / 8; ++q)
-                    if (dst[q]) *dst[q] = cur[q] + X[wid + 8 * q][lane];
-                __syncthreads();
+            for (int k = 0; k < 4; ++k) {
+                const int e = e0 + k * kTS_NT + tid, p = e >> lg, c = e & (ncw - 1);
+                v[k] = 0.0;
+                if (p < w && c < ncc) {
+                    if (grad) v[k] = __ldcg(A.G + (size_t)(c0 + p) * 4 + c);
+                    else {
+                        const int cc = tbase + c;
+                        v[k] = (cc >= lo_s && cc < hi_s && A.qS[cc] == c0 + p) ? 1.0 : 0.0;
+                    }
+                    const int n = src_n[p];
+#pragma unroll
+                    for (int t = 0; t < kMaxSrc; ++t)
+                        if (t < n) v[k] -= __ldcg(Usrc + (size_t)src_u[p][t] * ldsrc + coff + c);
+                    if (n > kMaxSrc) {   // rare: more sources than cached, walk the list
+                        int t = 0;
+                        for (int j = A.rc_ptr[slot0 + p]; j < A.rc_ptr[slot0 + p + 1]; ++j) {
+                            const int2 sr = A.rc_src[j];
+                            if (grad || has_tile(A.lo[sr.y], A.hi[sr.y], tbase)) {
+                                if (t >= kMaxSrc) v[k] -= __ldcg(Usrc + (size_t)sr.x * ldsrc + coff + c);
+                                ++t;
+                            }
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int e = e0 + k * kTS_NT + tid, p = e >> lg, c = e & (ncw - 1);
+                if (p < kpad) X[p][c] = v[k];
+            }
+        }
+        cp_async_wait_group<0>();
+        __syncthreads();
+        if (grad) block_dmma<1, kSolveRB / 8>(m, w, Sg, X, O);
+        else block_dmma<4, kSolveRB / 8>(m, w, Sg, X, O);
+        __syncthreads();
+        // ---- epilogue: solution rows, or U rows = O + children's rows landing there
+        for (int e0 = 0; e0 < m * ncw; e0 += 4 * kTS_NT) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int e = e0 + k * kTS_NT + tid, i = e >> lg, c = e & (ncw - 1), r = rb + i;
+                if (i >= m || c >= (grad ? 4 : 32)) continue;
+                if (r < w) {
+                    if (grad) A.Y[(size_t)(c0 + r) * 4 + c] = c < 3 ? O[i][c] : 0.0;
+                    else {
+                        const int cc = tbase + c;
+                        if (cc >= lo_s && cc < hi_s) A.V[(size_t)(c0 + r) * A.ldv + cc] = O[i][c];
+                    }
+                    continue;
+                }
+                double u = c < ncc ? O[i][c] : 0.0;
+                const int q = w + i, n = src_n[q];
+#pragma unroll
+                for (int t = 0; t < kMaxSrc; ++t)
+                    if (t < n) u += __ldcg(Usrc + (size_t)src_u[q][t] * ldsrc + coff + c);
+                if (n > kMaxSrc) {
+                    int t = 0;
+                    for (int j = A.rc_ptr[slot0 + r]; j < A.rc_ptr[slot0 + r + 1]; ++j) {
+                        const int2 sr = A.rc_src[j];
+                        if (grad || has_tile(A.lo[sr.y], A.hi[sr.y], tbase)) {
+                            if (t >= kMaxSrc) u += __ldcg(Usrc + (size_t)sr.x * ldsrc + coff + c);
+                            ++t;
+                        }
+                    }
+                }
+                Udst[(size_t)(A.uoff[s] + r - w) * ldsrc + coff + c] = u;
             }
         }
         __threadfence();
@@ -391,122 +370,40 @@ __global__ void __launch_bounds__(kTS_NT) k_forward_solve(FwdArgs A) {
 struct BwdArgs {
     const int *sn_c0, *sn_rowptr, *sn_rows, *sn_parent;
     const long long *sn_valptr;
-    const double *L;
-    const long long *dinv_ptr;
-    const double *dinv;
-    int nsn;
-    int *done, *ticket;
+    const double *Q;
+    const int2 *items;                 // [nitems] (s, row block) in reverse postorder
+    const int *pbase;                  // [nsn] first partial block of s
+    int nitems;
+    int *done, *cnt, *ticket;
+    double *P;                         // [blocks][kTS_W][4] partial sums
     double *Z;                         // [nf][4] in: rhs, out: solution of L^T x = rhs
 };
 
-constexpr int kBwdStage = 256;
-
-__global__ void __launch_bounds__(kTS_NT) k_backward_solve_v1(BwdArgs A) {
-    __shared__ double X[kTS_W][4];
-    __shared__ double4 xo[kBwdStage];
-    __shared__ double Sg[32][kTS_W + 1];
-    __shared__ int sh_item;
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    while (true) {
-        if (tid == 0) sh_item = atomicAdd(A.ticket, 1);
-        __syncthreads();
-        const int item = sh_item;
-        __syncthreads();
-        if (item >= A.nsn) return;
-        const int s = A.nsn - 1 - item;
-        if (tid == 0) {
-            int p = A.sn_parent[s];
-            if (p >= 0) {
-                volatile int *dp = A.done + p;
-                long long t0 = clock64();
-                while (*dp == 0) {
-                    __nanosleep(32);
-                    if (clock64() - t0 > kSpinLimit) { atomicExch(A.ticket + 1, 1); break; }
-                }
-            }
-            __threadfence();
-        }
-        __syncthreads();
-        const int c0 = A.sn_c0[s], w = A.sn_c0[s + 1] - c0;
-        const int r0 = A.sn_rowptr[s], nr = A.sn_rowptr[s + 1] - r0, noff = nr - w;
-        const double *Ls = A.L + A.sn_valptr[s];
-        const double *D = A.dinv + A.dinv_ptr[s];
-        const double4 *Z4 = reinterpret_cast<const double4 *>(A.Z);
-        for (int k = tid; k < w; k += kTS_NT) {
-            const double4 z = ldcg4(Z4 + c0 + k);
-            X[k][0] = z.x;
-            X[k][1] = z.y;
-            X[k][2] = z.z;
-        }
-        // X[k] -= sum_r L[r][k] x[R(r)]: stage the solved ancestor rows, then warp per k
-        for (int rb = 0; rb < noff; rb += kBwdStage) {
-            const int m = min(kBwdStage, noff - rb);
-            for (int r = tid; r < m; r += kTS_NT) xo[r] = ldcg4(Z4 + A.sn_rows[r0 + w + rb + r]);
-            __syncthreads();
-            for (int k = wid; k < w; k += kTS_NT / 32) {
-                const double *lk = Ls + (size_t)k * nr + w + rb;
-                double a0 = 0, a1 = 0, a2 = 0;
-                for (int r = lane; r < m; r += 32) {
-                    const double l = lk[r];
-                    const double4 xv = xo[r];
-                    a0 += l * xv.x;
-                    a1 += l * xv.y;
-                    a2 += l * xv.z;
-                }
-                a0 = warp_sum(a0);
-                a1 = warp_sum(a1);
-                a2 = warp_sum(a2);
-                if (lane == 0) {
-                    X[k][0] -= a0;
-                    X[k][1] -= a1;
-                    X[k][2] -= a2;
-                }
-            }
-            __syncthreads();
-        }
-        __syncthreads();
-        // x_s[i] = sum_{k >= i} D[k][i] X[k]: thread per i, column i of D read straight from
-        // L2 (coalesced across threads), loads independent
-        double a[3] = {0, 0, 0};
-        if (tid < w) {
-            const int i = tid;
-#pragma unroll 8
-            for (int k = i; k < w; ++k) {
-                const double dv = __ldg(D + (size_t)k * w + i);
-                a[0] += dv * X[k][0];
-                a[1] += dv * X[k][1];
-                a[2] += dv * X[k][2];
-            }
-        }
-        if (tid < w) {
-            double *zr = A.Z + (size_t)(c0 + tid) * 4;
-            zr[0] = a[0];
-            zr[1] = a[1];
-            zr[2] = a[2];
-        }
-        __threadfence();
-        __syncthreads();
-        if (tid == 0) atomicExch(A.done + s, 1);
-    }
-}
-
-// Backward solve item s (reverse postorder, waits for its parent):
-//   X = z_s - L_off^T x_off    (DMMA over 128-row chunks of the solved ancestor rows x_off)
-//   x_s = Dinv^T X             (DMMA, upper-triangular slab staging)
+// Backward solve.  x_s = L_ss^{-T}(z_s - L_off^T x_R) = Q_s^T [z_s; -x_R].  Item (s, b) forms
+// the partial Q_s[rows]^T v[rows] of its 64-row block (DMMA); the last block of s to finish
+// sums the partials in block order (deterministic) and publishes x_s.  Items of s wait for
+// their parent (all of R_s's rows are solved by then).
 __global__ void __launch_bounds__(kTS_NT) k_backward_solve(BwdArgs A) {
     extern __shared__ double bsm[];
-    double (*X)[kXS] = reinterpret_cast<double (*)[kXS]>(bsm);
-    double (*Y)[kXS] = reinterpret_cast<double (*)[kXS]>(bsm + kTS_W * kXS);
-    double (*Sg)[kSS] = reinterpret_cast<double (*)[kSS]>(bsm + 2 * kTS_W * kXS);
-    __shared__ int sh_item;
+    double (*Vb)[kXS] = reinterpret_cast<double (*)[kXS]>(bsm);
+    double (*O)[kXS] = reinterpret_cast<double (*)[kXS]>(bsm + kSolveRB * kXS);
+    double (*Sg)[kSS] = reinterpret_cast<double (*)[kSS]>(bsm + (kTS_W + kSolveRB) * kXS);
+    __shared__ int sh_item, sh_last;
     const int tid = threadIdx.x;
     while (true) {
         if (tid == 0) sh_item = atomicAdd(A.ticket, 1);
         __syncthreads();
         const int item = sh_item;
         __syncthreads();
-        if (item >= A.nsn) return;
-        const int s = A.nsn - 1 - item;
+        if (item >= A.nitems) return;
+        const int2 it = A.items[item];
+        const int s = it.x, rb = it.y * kSolveRB;
+        const int c0 = A.sn_c0[s], w = A.sn_c0[s + 1] - c0;
+        const int slot0 = A.sn_rowptr[s], nr = A.sn_rowptr[s + 1] - slot0;
+        const int nb = (nr + kSolveRB - 1) / kSolveRB;
+        const int m = min(kSolveRB, nr - rb);
+        // A = Q_s[rb.., :]^T : element (k, i) = Q[rb + i][k]  (w x m)
+        stage_block(A.Q + A.sn_valptr[s] + rb, nr, 1, w, m, Sg);
         if (tid == 0) {
             int p = A.sn_parent[s];
             if (p >= 0) {
@@ -520,34 +417,44 @@ __global__ void __launch_bounds__(kTS_NT) k_backward_solve(BwdArgs A) {
             __threadfence();
         }
         __syncthreads();
-        const int c0 = A.sn_c0[s], w = A.sn_c0[s + 1] - c0;
-        const int r0 = A.sn_rowptr[s], nr = A.sn_rowptr[s + 1] - r0, noff = nr - w;
-        const double *Ls = A.L + A.sn_valptr[s];
-        const double *D = A.dinv + A.dinv_ptr[s];
-        // ---- acc = L_off^T x_off, chunks of 128 off rows staged in Y (cols >= 3 and padding 0)
-        for (int rb = 0; rb < noff; rb += kTS_W) {
-            const int m = min(kTS_W, noff - rb);
-            for (int e = tid; e < kTS_W * 8; e += kTS_NT) {
-                const int r = e >> 3, c = e & 7;
-                Y[r][c] = (r < m && c < 3) ? __ldcg(A.Z + (size_t)A.sn_rows[r0 + w + rb + r] * 4 + c) : 0.0;
-            }
-            __syncthreads();
-            if (rb == 0) slab_dmma<0, 1, false>(Ls + w + rb, nr, 1, w, m, Y, Sg, X);
-            else slab_dmma<0, 1, true>(Ls + w + rb, nr, 1, w, m, Y, Sg, X);
-        }
-        // ---- X = z_s - acc (rows >= w and columns >= 3 zeroed: k-padding of the next product)
-        for (int e = tid; e < kTS_W * 8; e += kTS_NT) {
-            const int k = e >> 3, c = e & 7;
+        const int kpad = (m + 31) & ~31;
+        for (int e = tid; e < kpad * 8; e += kTS_NT) {
+            const int i = e >> 3, c = e & 7, r = rb + i;
             double v = 0.0;
-            if (k < w && c < 3) v = __ldcg(A.Z + (size_t)(c0 + k) * 4 + c) - (noff > 0 ? X[k][c] : 0.0);
-            Y[k][c] = v;
+            if (i < m && c < 3) {
+                if (r < w) v = __ldcg(A.Z + (size_t)(c0 + r) * 4 + c);
+                else v = -__ldcg(A.Z + (size_t)A.sn_rows[slot0 + r] * 4 + c);
+            }
+            Vb[i][c] = v;
         }
+        cp_async_wait_group<0>();
         __syncthreads();
-        // ---- x_s = Dinv^T X : element (i, k) = D[k][i] (column-major source, upper triangle)
-        slab_dmma<2, 1, false>(D, 1, w, w, w, Y, Sg, X);
-        for (int e = tid; e < w * 3; e += kTS_NT) {
-            const int i = e / 3, c = e % 3;
-            A.Z[(size_t)(c0 + i) * 4 + c] = X[i][c];
+        block_dmma<1, kTS_W / 8>(w, m, Sg, Vb, O);
+        __syncthreads();
+        double *Pb = A.P + (size_t)(A.pbase[s] + it.y) * kTS_W * 4;
+        if (nb == 1) {   // single block: publish directly
+            for (int e = tid; e < w * 3; e += kTS_NT) {
+                const int i = e / 3, c = e % 3;
+                A.Z[(size_t)(c0 + i) * 4 + c] = O[i][c];
+            }
+        } else {
+            for (int e = tid; e < w * 3; e += kTS_NT) {
+                const int i = e / 3, c = e % 3;
+                Pb[i * 4 + c] = O[i][c];
+            }
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) sh_last = atomicAdd(A.cnt + s, 1) == nb - 1;
+            __syncthreads();
+            if (!sh_last) continue;
+            __threadfence();
+            const double *P0 = A.P + (size_t)A.pbase[s] * kTS_W * 4;
+            for (int e = tid; e < w * 3; e += kTS_NT) {
+                const int i = e / 3, c = e % 3;
+                double x = 0.0;
+                for (int b = 0; b < nb; ++b) x += __ldcg(P0 + (size_t)b * kTS_W * 4 + i * 4 + c);
+                A.Z[(size_t)(c0 + i) * 4 + c] = x;
+            }
         }
         __threadfence();
         __syncthreads();
@@ -651,45 +558,45 @@ __global__ void __launch_bounds__(256) k_panel_syrk(const int *__restrict__ sn_c
 }
 
 // ------------------------------------------------------------------ host wrappers ---------
-constexpr int kFwdSmem = (2 * kTS_W * kXS + 2 * kTS_W * kSS) * (int)sizeof(double);
+constexpr int kFwdSmem = ((kTS_W + kSolveRB) * kXS + kSgRows * kSS) * (int)sizeof(double);
 
 void trisolve_init() {
     cudaFuncSetAttribute(k_forward_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem);
     cudaFuncSetAttribute(k_backward_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem);
 }
 
-void launch_ts_items(const int *sn_c0, const int *sn_fd, const int *sn_parent, int nsn,
-                     const int *qS, const int *nS_ptr, int *lo, int *hi, int *cnt, int *rem,
-                     cudaStream_t st) {
-    cudaMemsetAsync(rem, 0, sizeof(int) * nsn, st);
-    PDI_LAUNCH(k_ts_items, (nsn + 255) / 256, 256, 0, st)(sn_c0, sn_fd, sn_parent, nsn, qS, nS_ptr,
-                                                           lo, hi, cnt, rem);
+void launch_ts_items(const DevFactor &F, const int *qS, const int *nS_ptr, int *lo, int *hi, int *cnt,
+                     int *rem, cudaStream_t st) {
+    cudaMemsetAsync(rem, 0, sizeof(int) * F.nsn, st);
+    PDI_LAUNCH(k_ts_items, (F.nsn + 255) / 256, 256, 0, st)(F.ford, F.sn_c0, F.sn_rowptr, F.sn_fd,
+                                                             F.sn_parent, F.nsn, qS, nS_ptr, lo, hi,
+                                                             cnt, rem);
 }
 
 void launch_forward_solve(const DevFactor &F, const int *lo, const int *hi, const int *item_ptr,
-                          const int *qS, int *rem, int *ticket, double *G, double *V, int ldv,
-                          double *Ug, double *Up, int ldu, int nsm, unsigned long long *trace,
+                          const int *qS, int *rem, int *ticket, const double *G, double *Y, double *V,
+                          int ldv, double *Ug, double *Up, int ldu, int nsm, unsigned long long *trace,
                           cudaStream_t st) {
     FwdArgs A;
     A.sn_c0 = F.sn_c0; A.sn_rowptr = F.sn_rowptr; A.sn_parent = F.sn_parent;
-    A.sn_valptr = F.sn_valptr; A.L = F.L;
-    A.uoff = F.uoff; A.urel = F.urel; A.ch_ptr = F.ch_ptr; A.ch = F.ch;
-    A.dinv_ptr = F.dinv_ptr; A.dinv = F.dinv;
-    A.lo = lo; A.hi = hi; A.item_ptr = item_ptr; A.qS = qS; A.nsn = F.nsn;
-    A.rem = rem; A.ticket = ticket; A.G = G; A.V = V; A.ldv = ldv; A.Ug = Ug; A.Up = Up; A.ldu = ldu;
-    A.trace = trace;
+    A.uoff = F.uoff; A.rc_ptr = F.rc_ptr; A.rc_src = F.rc_src;
+    A.sn_valptr = F.sn_valptr; A.Q = F.Q;
+    A.lo = lo; A.hi = hi; A.item_ptr = item_ptr; A.qS = qS; A.ford = F.ford; A.nsn = F.nsn;
+    A.rem = rem; A.ticket = ticket; A.G = G; A.Y = Y; A.V = V; A.ldv = ldv;
+    A.Ug = Ug; A.Up = Up; A.ldu = ldu; A.trace = trace;
     cudaMemsetAsync(ticket, 0, sizeof(int), st);
     PDI_LAUNCH(k_forward_solve, nsm, kTS_NT, kFwdSmem, st)(A);
 }
 
-void launch_backward_solve(const DevFactor &F, int *done, int *ticket, double *Z, int nsm,
-                           cudaStream_t st) {
+void launch_backward_solve(const DevFactor &F, int *done, int *cnt, int *ticket, double *P, double *Z,
+                           int nsm, cudaStream_t st) {
     BwdArgs A;
     A.sn_c0 = F.sn_c0; A.sn_rowptr = F.sn_rowptr; A.sn_rows = F.sn_rows; A.sn_parent = F.sn_parent;
-    A.sn_valptr = F.sn_valptr; A.L = F.L; A.dinv_ptr = F.dinv_ptr; A.dinv = F.dinv;
-    A.nsn = F.nsn; A.done = done; A.ticket = ticket; A.Z = Z;
+    A.sn_valptr = F.sn_valptr; A.Q = F.Q; A.items = F.bw_items; A.pbase = F.bw_pbase;
+    A.nitems = F.bw_nitems; A.done = done; A.cnt = cnt; A.ticket = ticket; A.P = P; A.Z = Z;
     cudaMemsetAsync(ticket, 0, sizeof(int), st);
     cudaMemsetAsync(done, 0, sizeof(int) * F.nsn, st);
+    cudaMemsetAsync(cnt, 0, sizeof(int) * F.nsn, st);
     PDI_LAUNCH(k_backward_solve, nsm, kTS_NT, kFwdSmem, st)(A);
 }
 

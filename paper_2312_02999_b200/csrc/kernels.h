@@ -9,10 +9,15 @@ struct DevFactor {
     int nf = 0, nsn = 0;
     int *sn_c0 = nullptr, *sn_rowptr = nullptr, *sn_rows = nullptr, *sn_parent = nullptr;
     long long *sn_valptr = nullptr;
-    double *L = nullptr;
+    double *Q = nullptr;               // per supernode [L_ss^-1; L_off L_ss^-1], layout of L
+    const int2 *bw_items = nullptr;    // backward items (s, row block), reverse postorder
+    int *bw_pbase = nullptr;           // first partial block of each supernode
+    int *ford = nullptr;               // forward dispatch order of the supernodes
+    int bw_nitems = 0, bw_nblocks = 0;
     int *seg_ptr = nullptr, *seg_d = nullptr, *seg_klo = nullptr, *seg_khi = nullptr;
     int *sn_fd = nullptr, *col2sn = nullptr;
     int *uoff = nullptr, *urow_sn = nullptr, *rc_ptr = nullptr, *rc_idx = nullptr;
+    const int2 *rc_src = nullptr;      // [rc entries] (U row, child supernode owning it)
     int *urel = nullptr, *ch_ptr = nullptr, *ch = nullptr;
     long long *dinv_ptr = nullptr;
     double *dinv = nullptr;
@@ -39,16 +44,16 @@ void launch_update(double4 *x, const double4 *dx, const int *q2v, int nf, const 
 void launch_scatter_dx(const double *z, const int *q2v, int nf, double4 *dx, cudaStream_t st);
 
 // ---- k_trisolve.cu
-void launch_ts_items(const int *sn_c0, const int *sn_fd, const int *sn_parent, int nsn,
-                     const int *qS, const int *nS_ptr, int *lo, int *hi, int *cnt, int *rem,
-                     cudaStream_t st);
+constexpr int kSolveRB = 64;   // rows of a supernode per solve work item
+void launch_ts_items(const DevFactor &F, const int *qS, const int *nS_ptr, int *lo, int *hi, int *cnt,
+                     int *rem, cudaStream_t st);
 void trisolve_init();
 void launch_forward_solve(const DevFactor &F, const int *lo, const int *hi, const int *item_ptr,
-                          const int *qS, int *rem, int *ticket, double *G, double *V, int ldv,
-                          double *Ug, double *Up, int ldu, int nsm, unsigned long long *trace,
+                          const int *qS, int *rem, int *ticket, const double *G, double *Y, double *V,
+                          int ldv, double *Ug, double *Up, int ldu, int nsm, unsigned long long *trace,
                           cudaStream_t st);
-void launch_backward_solve(const DevFactor &F, int *done, int *ticket, double *Z, int nsm,
-                           cudaStream_t st);
+void launch_backward_solve(const DevFactor &F, int *done, int *cnt, int *ticket, double *P, double *Z,
+                           int nsm, cudaStream_t st);
 void launch_panel_yS(const int *qS, const int *nS_ptr, int nS_host, const DevFactor &F,
                      const double *V, int ldv, const double *G, double *yS, cudaStream_t st);
 void launch_panel_correct(const DevFactor &F, const int *lo, const int *hi, const double *V,

@@ -556,6 +556,23 @@ int factorize(HostMesh &m, HostFactor &f, std::string &err) {
                     D[(size_t)i * w + c] = acc / Ls[i + (size_t)i * nr];
                 }
         }
+        // Q_s = [L_ss^{-1}; L_off L_ss^{-1}] (column-major, ld nr, the layout of L): the forward
+        // solve's item block b computes rows of Q_s x_s, the backward solve Q_s^T [z_s; -x_R].
+        f.Q.assign(f.vals.size(), 0.0);
+        for (int s = 0; s < nsn; ++s) {
+            const int w = sn_start[s + 1] - sn_start[s], nr = f.sn_rowptr[s + 1] - f.sn_rowptr[s];
+            const double *Ls = &f.vals[(size_t)f.sn_valptr[s]];
+            const double *D = &f.dinv[(size_t)f.dinv_ptr[s]];
+            double *Qs = &f.Q[(size_t)f.sn_valptr[s]];
+            for (int k = 0; k < w; ++k)
+                for (int i = k; i < w; ++i) Qs[i + (size_t)k * nr] = D[(size_t)i * w + k];
+            for (int k = 0; k < w; ++k)
+                for (int r = w; r < nr; ++r) {
+                    double acc = 0.0;
+                    for (int j = k; j < w; ++j) acc += Ls[r + (size_t)j * nr] * D[(size_t)j * w + k];
+                    Qs[r + (size_t)k * nr] = acc;
+                }
+        }
     }
     // ---- transpose incidence in factor order and W^T over factor positions
     {

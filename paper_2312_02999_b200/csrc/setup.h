@@ -57,6 +57,8 @@ struct HostFactor {
     // inverse of each diagonal block (lower triangular, row-major w x w)
     std::vector<int64_t> dinv_ptr;     // [nsn+1]
     std::vector<double> dinv;
+    // per supernode [L_ss^{-1}; L_off L_ss^{-1}], column-major ld nr, offsets sn_valptr (as vals)
+    std::vector<double> Q;
     int max_width = 0, max_rows = 0, depth = 0;
     int64_t nnzL = 0;
 };
