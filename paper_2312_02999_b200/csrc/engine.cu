@@ -496,6 +496,7 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
                                      h->trace_file ? h->sprof.p : nullptr, st));
         if (h->trace_file && h->schur_file) {
             std::vector<unsigned long long> pr(1024);
+            CK(cudaStreamSynchronize(st));
             CK(cudaMemcpy(pr.data(), h->sprof.p, 1024 * 8, cudaMemcpyDeviceToHost));
             fwrite(&nS, sizeof(int), 1, h->schur_file);
             fwrite(pr.data(), 8, 1024, h->schur_file);

@@ -24,6 +24,7 @@ namespace pdipc {
 constexpr int TB = 64;          // tile
 constexpr int TS = 68;          // smem tile stride (DMMA-friendly)
 constexpr int NT = 256;         // threads per CTA
+constexpr int kP4Single = 1536;  // P4 in one CTA (no grid barriers) up to this size (<= TB * TS)
 
 __device__ __forceinline__ void dmma_884(double &d0, double &d1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -49,7 +50,7 @@ struct SchurArgs {
     double *T;                  // 64x64 scratch (sweep pivot inverse)
     double *U;                  // sweep panel [capS+64][64]
     double *yS, *u, *t;         // [3capS]
-    double *Kpart;              // [grid][32*32] split-K partial tiles
+    double *Kpart;              // [grid][1152] split-K partial tiles (+ y_S partials)
     double *Z;                  // [nf][4]
     int *info;
     unsigned long long *prof;   // optional phase timestamps (PDIPC_TRACE), [1024]
@@ -112,225 +113,151 @@ __device__ __forceinline__ void tile_xyt(double *C, const double *X, const doubl
     __syncthreads();
 }
 
-// One warp: in-place Cholesky of the n x n (n <= 32) block at S (stride TS); pivots after
-// row `free_row` (the augmented right-hand-side row) are not checked.
-__device__ void chol32_warp(double *S, int n, int free_row, int *info) {
-    const int lane = threadIdx.x & 31;
-    for (int j = 0; j < n; ++j) {
-        double djj = S[j * TS + j];
-        if (!(djj > 0.0)) {
-            if (j < free_row && lane == 0) atomicExch(info, 1);
-            djj = 1.0;
-        }
-        const double d = sqrt(djj);
-        __syncwarp();
-        if (lane == j) S[j * TS + j] = d;
-        if (lane > j && lane < n) S[lane * TS + j] /= d;
-        __syncwarp();
-        if (lane > j && lane < n) {
-            const double lij = S[lane * TS + j];
-            for (int l = j + 1; l <= lane; ++l) S[lane * TS + l] -= lij * S[l * TS + j];
-        }
-        __syncwarp();
+// One thread: Cholesky of the 8x8 diagonal block at S (stride TS, lower part read) in
+// registers, its inverse into D (8 x 9), L written back to S.  Returns true on a bad pivot
+// below free_row (relative to the block).
+__device__ __forceinline__ bool chol8_thread(double *S, double (*D)[9], int free_row) {
+    double a[8][8], x[8][8], rinv[8];
+    bool bad = false;
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) a[r][c] = c <= r ? S[r * TS + c] : 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        double p = a[k][k];
+        bad |= !(p > 0.0) && k < free_row;
+        p = p > 0.0 ? p : 1.0;
+        const double rs = rsqrt(p);
+        rinv[k] = rs;
+        a[k][k] = p * rs;
+#pragma unroll
+        for (int r = k + 1; r < 8; ++r) a[r][k] *= rs;
+#pragma unroll
+        for (int r = k + 1; r < 8; ++r)
+#pragma unroll
+            for (int l = k + 1; l <= r; ++l) a[r][l] -= a[r][k] * a[l][k];
     }
+#pragma unroll
+    for (int c = 0; c < 8; ++c)                 // x = L^{-1}: column c by forward substitution
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            double acc = r == c ? 1.0 : 0.0;
+#pragma unroll
+            for (int q = 0; q < r; ++q) acc -= a[r][q] * x[q][c];
+            x[r][c] = r >= c ? acc * rinv[r] : 0.0;
+        }
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            if (c <= r) S[r * TS + c] = a[r][c];
+            D[r][c] = x[r][c];
+        }
+    return bad;
 }
 
-// One warp: Li = L^{-1} for the lower n x n block L (n <= 32), lane = column
-__device__ void trinv32_warp(const double *L, double *Li, int n) {
-    const int c = threadIdx.x & 31;
-    for (int i = 0; i < 32; ++i) {
-        double v = 0.0;
-        if (c < n && i < n && i >= c) {
-            double acc = (i == c) ? 1.0 : 0.0;
-            for (int q = c; q < i; ++q) acc -= L[i * TS + q] * Li[q * TS + c];
-            v = acc / L[i * TS + i];
-        }
-        Li[i * TS + c] = v;
-        __syncwarp();
-    }
+// One warp: C (8x8 at smem, stride TS) -= X Y^T with X, Y 8 x 8 (X[r][k] at X + r*TS + k,
+// Y[n][k] at Y + n*ys_row + k*ys_col) on DMMA (2 k-steps); lower_only keeps C's strict upper
+// triangle untouched (diagonal tiles).
+__device__ __forceinline__ void tile8_sub_xyt(double *C, const double *X, const double *Y, int ys_row,
+                                              int ys_col, bool lower_only) {
+    const int lane = threadIdx.x & 31, gr = lane >> 2, gc = lane & 3;
+    double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+    for (int k4 = 0; k4 < 2; ++k4)
+        dmma_884(d0, d1, X[gr * TS + 4 * k4 + gc], Y[gr * ys_row + (4 * k4 + gc) * ys_col]);
+    const int c = 2 * gc;
+    if (!lower_only || c <= gr) C[gr * TS + c] -= d0;
+    if (!lower_only || c + 1 <= gr) C[gr * TS + c + 1] -= d1;
 }
 
-// CTA: Cholesky of the nb x nb (nb <= 64) tile S in place (lower, upper zeroed) and its inverse
-// Li (64x64), blocked in 8x8 blocks: per block column one thread factors and inverts the 8x8
-// diagonal block in registers, the CTA does the 8-wide TRSM and the rank-8 trailing update
-// (3 barriers per block column); the inverse is assembled block row by block row.  Rows >= nb
-// are treated as identity.  Pivots at rows >= free_row are not checked.
-__device__ void tile_chol64_fast(double *S, double *Li, int nb, int free_row, int *info) {
-    const int tid = threadIdx.x;
-    __shared__ double DI[8][8][9];                       // inverses of the 8x8 diagonal blocks
-    for (int e = tid; e < TB * TB; e += NT) {            // identity padding, zero upper part
+// CTA: Cholesky of the nb x nb (nb <= 64) tile S in place (lower, upper and padding zeroed,
+// rows >= nb identity) and its inverse Li, in 8-wide block columns with one block of
+// look-ahead.  Per block column J (two barriers):
+//   (b) thread per row: L_IJ = A_IJ D_J^{-T}; thread per column: B_J <- D_J^{-1} B_J
+//       (B starts as I and ends as L^{-1});
+//   (c) warp 0 updates the next diagonal block and ONE thread factors and inverts it in
+//       registers, while warps 1..7 apply the rank-8 updates A_IL -= L_IJ L_LJ^T and
+//       B_I -= L_IJ B_J on DMMA.
+// Pivots at rows >= free_row are not checked.
+__device__ void tile_chol64(double *S, double *Li, int nb, int free_row, int *info) {
+    const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+    __shared__ double DI[2][8][9];
+    for (int e = tid; e < TB * TB; e += NT) {
         const int r = e >> 6, c = e & 63;
         if (r >= nb || c >= nb) S[r * TS + c] = (r == c) ? 1.0 : 0.0;
         else if (c > r) S[r * TS + c] = 0.0;
+        Li[r * TS + c] = (r == c) ? 1.0 : 0.0;
     }
+    __syncthreads();
+    bool bad = false;
+    if (tid == 0) bad |= chol8_thread(S, DI[0], free_row);
     __syncthreads();
     for (int J = 0; J < 8; ++J) {
         const int j0 = 8 * J;
-        if (tid < 32) {
-            // warp 0: lane r < 8 holds row r of the 8x8 diagonal block; shuffles carry columns
-            const int lane = tid, r = lane & 7;
-            double a[8], rinv[8];
+        const double (*D)[9] = DI[J & 1];
+        // (b)
+        if (tid < 64) {
+            const int i = tid;
+            if (i >= j0 + 8) {
+                double v[8], o[8];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) a[k] = (lane < 8 && k <= r) ? S[(j0 + r) * TS + j0 + k] : 0.0;
+                for (int q = 0; q < 8; ++q) v[q] = S[i * TS + j0 + q];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                double p = __shfl_sync(0xffffffffu, a[k], k);
-                if (!(p > 0.0)) {
-                    if (lane == 0 && j0 + k < free_row) atomicExch(info, 1);
-                    p = 1.0;
+                for (int c = 0; c < 8; ++c) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int q = 0; q <= c; ++q) acc += v[q] * D[c][q];
+                    o[c] = acc;
                 }
-                // one reciprocal square root per pivot (no division on the pivot chain)
-                const double inv = rsqrt(p);
-                rinv[k] = inv;
-                if (r == k) a[k] = p * inv;
-                else if (r > k) a[k] = a[k] * inv;
 #pragma unroll
-                for (int l = k + 1; l < 8; ++l) {
-                    const double llk = __shfl_sync(0xffffffffu, a[k], l);
-                    if (r >= l) a[l] -= a[k] * llk;
+                for (int c = 0; c < 8; ++c) S[i * TS + j0 + c] = o[c];
+            }
+        } else if (tid < 128) {
+            const int c = tid - 64;
+            if (c < j0 + 8) {
+                double v[8], o[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) v[q] = Li[(j0 + q) * TS + c];
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int q = 0; q <= r; ++q) acc += D[r][q] * v[q];
+                    o[r] = acc;
+                }
+#pragma unroll
+                for (int r = 0; r < 8; ++r) Li[(j0 + r) * TS + c] = o[r];
+            }
+        }
+        __syncthreads();
+        if (J == 7) break;
+        // (c)
+        const int T = 7 - J, j1 = j0 + 8;
+        if (wid == 0) {
+            tile8_sub_xyt(S + j1 * TS + j1, S + j1 * TS + j0, S + j1 * TS + j0, TS, 1, true);
+            __syncwarp();
+            if (lane == 0) bad |= chol8_thread(S + j1 * TS + j1, DI[(J + 1) & 1], free_row - j1);
+        } else {
+            const int nA = T * (T + 1) / 2 - 1, nB = T * (J + 1);
+            for (int t = wid - 1; t < nA + nB; t += NT / 32 - 1) {
+                if (t < nA) {              // A tile (I, L), J+1 <= L <= I, not (J+1, J+1)
+                    int u = t + 1, I = 0;
+                    while (u > I) { u -= I + 1; ++I; }
+                    const int L = u;       // I, L relative to J+1
+                    const int r0 = j1 + 8 * I, c0 = j1 + 8 * L;
+                    tile8_sub_xyt(S + r0 * TS + c0, S + r0 * TS + j0, S + c0 * TS + j0, TS, 1, I == L);
+                } else {                   // B tile (I, Lb), I >= J+1, Lb <= J
+                    const int u = t - nA, I = u / (J + 1), Lb = u % (J + 1);
+                    const int r0 = j1 + 8 * I, c0 = 8 * Lb;
+                    tile8_sub_xyt(Li + r0 * TS + c0, S + r0 * TS + j0, Li + j0 * TS + c0, 1, TS, false);
                 }
             }
-            // inverse: lane c < 8 solves L x = e_c; L[i][q] comes from lane i; 1/L_ii = rinv[i]
-            const int c = lane & 7;
-            double x[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                double acc = (i == c) ? 1.0 : 0.0;
-#pragma unroll
-                for (int q = 0; q < i; ++q) acc -= __shfl_sync(0xffffffffu, a[q], i) * x[q];
-                x[i] = (i >= c) ? acc * rinv[i] : 0.0;
-            }
-            if (lane < 8) {
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    S[(j0 + r) * TS + j0 + k] = k <= r ? a[k] : 0.0;
-                    DI[J][k][c] = x[k];
-                }
-            }
-        }
-        __syncthreads();
-        const int nrem = 64 - j0 - 8;
-        // TRSM: rows below, S[i][j0..j0+8) <- S[i][j0..] DI_J^T
-        for (int e = tid; e < nrem * 8; e += NT) {
-            const int i = j0 + 8 + (e >> 3), c = e & 7;
-            double acc = 0.0;
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                if (q <= c) acc += S[i * TS + j0 + q] * DI[J][c][q];
-            Li[i * TS + c] = acc;                         // Li rows used as scratch
-        }
-        __syncthreads();
-        for (int e = tid; e < nrem * 8; e += NT) {
-            const int i = j0 + 8 + (e >> 3), c = e & 7;
-            S[i * TS + j0 + c] = Li[i * TS + c];
-        }
-        __syncthreads();
-        // rank-8 trailing update of the lower part (16 x 16 thread grid, no integer division)
-        for (int i = j0 + 8 + (tid >> 4); i < 64; i += 16)
-            for (int l = j0 + 8 + (tid & 15); l <= i; l += 16) {
-                double acc = 0.0;
-#pragma unroll
-                for (int q = 0; q < 8; ++q) acc += S[i * TS + j0 + q] * S[l * TS + j0 + q];
-                S[i * TS + l] -= acc;
-            }
-        __syncthreads();
-    }
-    // inverse: Li_II = DI_I;  Li_IJ = -DI_I sum_{K=J}^{I-1} L_IK Li_KJ   (block row by block row)
-    for (int e = tid; e < TB * TB; e += NT) {
-        const int r = e >> 6, c = e & 63;
-        Li[r * TS + c] = ((r >> 3) == (c >> 3)) ? DI[r >> 3][r & 7][c & 7] : 0.0;
-    }
-    __syncthreads();
-    __shared__ double Tmp[8][64];
-    for (int I = 1; I < 8; ++I) {
-        const int i0 = 8 * I;
-        {                                                 // Tmp = sum_K L_IK Li_KJ, cols < i0
-            const int r = tid >> 5, c0 = tid & 31;        // 8 rows x 32 lanes, 2 columns each
-            for (int c = c0; c < i0; c += 32) {
-                double acc = 0.0;
-#pragma unroll 8
-                for (int q = (c & ~7); q < i0; ++q) acc += S[(i0 + r) * TS + q] * Li[q * TS + c];
-                Tmp[r][c] = acc;
-            }
-        }
-        __syncthreads();
-        {
-            const int r = tid >> 5, c0 = tid & 31;
-            for (int c = c0; c < i0; c += 32) {
-                double acc = 0.0;
-#pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    if (q <= r) acc += DI[I][r][q] * Tmp[q][c];
-                Li[(i0 + r) * TS + c] = -acc;
-            }
         }
         __syncthreads();
     }
-}
-
-// CTA: Cholesky of the nb x nb (nb <= 64) tile S in place (lower, upper zeroed) and its inverse
-// Li (64x64, zero padded).  W is a 64x64 scratch tile.  free_row: see chol32_warp.
-__device__ void tile_chol64(double *S, double *Li, double *W, int nb, int free_row, int *info) {
-    const int tid = threadIdx.x, w = tid >> 5;
-    const int n1 = min(32, nb), n2 = nb - n1;
-    for (int e = tid; e < TB * TB; e += NT) Li[(e >> 6) * TS + (e & 63)] = 0.0;
-    __syncthreads();
-    if (w == 0) chol32_warp(S, n1, free_row, info);
-    __syncthreads();
-    if (w == 0) trinv32_warp(S, Li, n1);                 // Li11
-    __syncthreads();
-    if (n2 > 0) {
-        // A21 <- A21 Li11^T   (rows 32..nb-1, cols 0..31)
-        for (int e = tid; e < 32 * 32; e += NT) {
-            const int r = e >> 5, c = e & 31;
-            double acc = 0.0;
-            if (r < n2)
-                for (int q = 0; q <= c; ++q) acc += S[(32 + r) * TS + q] * Li[c * TS + q];
-            W[r * TS + c] = acc;
-        }
-        __syncthreads();
-        for (int e = tid; e < 32 * 32; e += NT) {
-            const int r = e >> 5, c = e & 31;
-            if (r < n2) S[(32 + r) * TS + c] = W[r * TS + c];
-        }
-        __syncthreads();
-        // A22 -= L21 L21^T (lower part)
-        for (int e = tid; e < 32 * 32; e += NT) {
-            const int r = e >> 5, c = e & 31;
-            if (r < n2 && c <= r) {
-                double acc = 0.0;
-                for (int q = 0; q < 32; ++q) acc += S[(32 + r) * TS + q] * S[(32 + c) * TS + q];
-                S[(32 + r) * TS + 32 + c] -= acc;
-            }
-        }
-        __syncthreads();
-        if (w == 0) chol32_warp(S + 32 * TS + 32, n2, free_row - 32, info);
-        __syncthreads();
-        if (w == 0) trinv32_warp(S + 32 * TS + 32, Li + 32 * TS + 32, n2);   // Li22
-        __syncthreads();
-        // Li21 = -Li22 L21 Li11
-        for (int e = tid; e < 32 * 32; e += NT) {       // W = L21 Li11
-            const int r = e >> 5, c = e & 31;
-            double acc = 0.0;
-            if (r < n2)
-                for (int q = c; q < 32; ++q) acc += S[(32 + r) * TS + q] * Li[q * TS + c];
-            W[r * TS + c] = acc;
-        }
-        __syncthreads();
-        for (int e = tid; e < 32 * 32; e += NT) {
-            const int r = e >> 5, c = e & 31;
-            double acc = 0.0;
-            if (r < n2)
-                for (int q = 0; q <= r; ++q) acc += Li[(32 + r) * TS + 32 + q] * W[q * TS + c];
-            Li[(32 + r) * TS + c] = -acc;
-        }
-        __syncthreads();
-    }
-    for (int e = tid; e < TB * TB; e += NT) {            // clean the upper triangle / padding
-        const int r = e >> 6, c = e & 63;
-        if (c > r || r >= nb || c >= nb) S[r * TS + c] = 0.0;
-    }
-    __syncthreads();
+    if (bad) atomicExch(info, 1);
 }
 
 // ---------------------------------------------------------------- the kernel ---------------
@@ -349,91 +276,154 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
         grid.sync();                                                          \
         if (a.prof && bid == 0 && tid == 0 && np < 1023) a.prof[np++] = gtimer_s(); \
     } while (0)
-    // ------------------------------------------------ P0: y_S and K = V^T V
-    for (int c = bid; c < nS; c += G) {
-        double acc[3] = {0, 0, 0};
-        for (int s = a.col2sn[a.qS[c]]; s >= 0; s = a.sn_parent[s])
-            for (int r = a.sn_c0[s] + tid; r < a.sn_c0[s + 1]; r += NT) {
-                const double v = a.V[(size_t)r * a.ldv + c];
-                acc[0] += v * a.G[(size_t)r * 4 + 0];
-                acc[1] += v * a.G[(size_t)r * 4 + 1];
-                acc[2] += v * a.G[(size_t)r * 4 + 2];
-            }
-        for (int i = 0; i < 3; ++i) {
-            double tsum = block_sum<NT>(acc[i], red);
-            if (tid == 0) a.yS[3 * c + i] = -tsum;
-        }
-    }
-    const int ntk = (nS + 31) / 32;                  // 32x32 tiles of K (lower)
+    // ------------------------------------------------ P0: y_S = -V_s^T w and K = V_s^T V_s
+    // Tile-parallel over the 32x32 lower tiles of K, split over the supernodes (rows) when tiles
+    // are few; every CTA streams the 32-row chunks of its supernodes whose active column range
+    // [lo_s, hi_s) meets both tile ranges (cp.async double buffer, inactive entries zeroed) and
+    // accumulates on DMMA.  Diagonal tiles also accumulate y_S for their columns.  Split partials
+    // are reduced in a fixed order (deterministic).
+    const int ntk = (nS + 31) / 32;
     const int ntiles = ntk * (ntk + 1) / 2;
-    // split the supernode (row) loop of each tile over nsplit CTAs when tiles are few;
-    // partial tiles are reduced in a fixed order afterwards (deterministic)
-    const int nsplit = max(1, min(8, G / max(ntiles, 1)));
+    const int nsplit = max(1, min(16, G / max(ntiles, 1)));
     {
-        double *Va = T0, *Vb = T1;                   // 32 x 33 each
+        typedef double Chunk[32][36];
+        Chunk *Va = reinterpret_cast<Chunk *>(T0), *Vb = reinterpret_cast<Chunk *>(T1);   // [2] each
+        double (*Wc)[32][4] = reinterpret_cast<double (*)[32][4]>(T2);                   // [2]
+        const int gr = lane >> 2, gc = lane & 3;
         for (int bs = bid; bs < ntiles * nsplit; bs += G) {
             const int b = bs / nsplit, split = bs % nsplit;
             int ti = 0, rem = b;
             while (rem > ti) { rem -= ti + 1; ++ti; }
-            const int tj = rem;
-            const int ia = ti * 32, ja = tj * 32;
-            const int tx = tid & 31, ty = tid >> 5;
-            double acc[4] = {0, 0, 0, 0};
-            for (int s = split; s < a.nsn; s += nsplit) {
-                const int l = a.lo[s], h = a.hi[s];
-                if (h <= l || l >= min(ia + 32, nS) || h <= ia || l >= ja + 32 || h <= ja) continue;
-                const int c0 = a.sn_c0[s], c1 = a.sn_c0[s + 1];
-                for (int rb = c0; rb < c1; rb += 32) {
-                    const int nrb = min(32, c1 - rb);
-                    for (int e = tid; e < 32 * 32; e += NT) {
-                        const int rr = e >> 5, cc = e & 31;
-                        const int ca = ia + cc, cb = ja + cc;
-                        double va = 0, vb = 0;
-                        if (rr < nrb) {
-                            if (ca >= l && ca < h && ca < nS) va = a.V[(size_t)(rb + rr) * a.ldv + ca];
-                            if (cb >= l && cb < h && cb < nS) vb = a.V[(size_t)(rb + rr) * a.ldv + cb];
+            const int tj = rem, ia = ti * 32, ja = tj * 32;
+            const bool diag = ti == tj;
+            // chunk iterator over (supernode s, first row rb)
+            auto overlaps = [&](int sn) {
+                const int l = a.lo[sn], h = a.hi[sn];
+                return h > l && l < ia + 32 && h > ia && l < ja + 32 && h > ja;
+            };
+            auto next_chunk = [&](int &sn, int &rb) -> bool {
+                if (sn >= 0) {
+                    rb += 32;
+                    if (rb < a.sn_c0[sn + 1]) return true;
+                    sn += nsplit;
+                } else {
+                    sn = split;
+                }
+                for (; sn < a.nsn; sn += nsplit)
+                    if (overlaps(sn)) { rb = a.sn_c0[sn]; return true; }
+                return false;
+            };
+            auto stage = [&](int sn, int rb, int buf) {
+                const int l = a.lo[sn], h = a.hi[sn], nrb = min(32, a.sn_c0[sn + 1] - rb);
+                for (int e = tid; e < 32 * 32; e += NT) {
+                    const int rr = e >> 5, cc = e & 31;
+                    const int ca = ia + cc, cb = ja + cc;
+                    const double *row = a.V + (size_t)(rb + rr) * a.ldv;
+                    if (rr < nrb && ca >= l && ca < h) {
+                        const unsigned sa = (unsigned)__cvta_generic_to_shared(&Va[buf][rr][cc]);
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(row + ca));
+                    } else {
+                        Va[buf][rr][cc] = 0.0;
+                    }
+                    if (!diag) {
+                        if (rr < nrb && cb >= l && cb < h) {
+                            const unsigned sb = (unsigned)__cvta_generic_to_shared(&Vb[buf][rr][cc]);
+                            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sb), "l"(row + cb));
+                        } else {
+                            Vb[buf][rr][cc] = 0.0;
                         }
-                        Va[rr * 33 + cc] = va;
-                        Vb[rr * 33 + cc] = vb;
                     }
-                    __syncthreads();
-                    for (int rr = 0; rr < nrb; ++rr) {
-                        const double bv = Vb[rr * 33 + tx];
+                }
+                if (diag)
+                    for (int e = tid; e < 32 * 4; e += NT) {
+                        const int rr = e >> 2, i = e & 3;
+                        Wc[buf][rr][i] = (rr < nrb && i < 3) ? a.G[(size_t)(rb + rr) * 4 + i] : 0.0;
+                    }
+                asm volatile("cp.async.commit_group;\n" ::);
+            };
+            double acc[2][2] = {{0, 0}, {0, 0}};
+            double ya = 0.0;                         // y_S partial: thread (c = tid / 3, i = tid % 3)
+            int sn = -1, rb = 0;
+            bool have = next_chunk(sn, rb);
+            if (have) stage(sn, rb, 0);
+            int buf = 0;
+            while (have) {
+                int sn2 = sn, rb2 = rb;
+                const bool have2 = next_chunk(sn2, rb2);
+                if (have2) {
+                    stage(sn2, rb2, buf ^ 1);
+                    asm volatile("cp.async.wait_group 1;\n" ::);
+                } else {
+                    asm volatile("cp.async.wait_group 0;\n" ::);
+                }
+                __syncthreads();
+                const Chunk &A = Va[buf];
+                const Chunk &B = diag ? Va[buf] : Vb[buf];
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) acc[k] += Va[rr * 33 + ty * 4 + k] * bv;
+                for (int j = 0; j < 2; ++j) {        // warp w: 8x8 tiles t = w, w + 8 of 4 x 4
+                    const int t = wid + 8 * j, ta = t >> 2, tb = t & 3;
+#pragma unroll
+                    for (int k4 = 0; k4 < 8; ++k4)
+                        dmma_884(acc[j][0], acc[j][1], A[4 * k4 + gc][8 * ta + gr], B[4 * k4 + gc][8 * tb + gr]);
+                }
+                if (diag && tid < 96) {
+                    const int c = tid / 3, i = tid % 3;
+#pragma unroll 8
+                    for (int rr = 0; rr < 32; ++rr) ya += A[rr][c] * Wc[buf][rr][i];
+                }
+                __syncthreads();
+                sn = sn2;
+                rb = rb2;
+                have = have2;
+                buf ^= 1;
+            }
+            double *dst = a.Kpart + (size_t)bs * 1152;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int t = wid + 8 * j, ta = t >> 2, tb = t & 3;
+                const int r = 8 * ta + gr, c = 8 * tb + 2 * gc;
+                if (nsplit == 1) {
+                    for (int q = 0; q < 2; ++q) {
+                        const int R = ia + r, Cc = ja + c + q;
+                        if (R < nS && Cc < nS && Cc <= R) {
+                            a.K[(size_t)R * a.ldk + Cc] = acc[j][q];
+                            a.K[(size_t)Cc * a.ldk + R] = acc[j][q];
+                        }
                     }
-                    __syncthreads();
+                } else {
+                    dst[r * 32 + c] = acc[j][0];
+                    dst[r * 32 + c + 1] = acc[j][1];
                 }
             }
-            if (nsplit == 1) {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int r = ia + ty * 4 + k, c = ja + tx;
-                    if (r < nS && c < nS && c <= r) {
-                        a.K[(size_t)r * a.ldk + c] = acc[k];
-                        a.K[(size_t)c * a.ldk + r] = acc[k];
-                    }
+            if (diag && tid < 96) {
+                const int c = tid / 3, i = tid % 3;
+                if (nsplit == 1) {
+                    if (ia + c < nS) a.yS[3 * (ia + c) + i] = -ya;
+                } else {
+                    dst[1024 + tid] = ya;
                 }
-            } else {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) a.Kpart[(size_t)bs * 1024 + (ty * 4 + k) * 32 + tx] = acc[k];
             }
         }
     }
     if (nsplit > 1) {
         GSYNC();
-        for (int b = bid; b < ntiles; b += G) {
+        for (int e = bid * NT + tid; e < ntiles * 1120; e += G * NT) {
+            const int b = e / 1120, q = e % 1120;
             int ti = 0, rem = b;
             while (rem > ti) { rem -= ti + 1; ++ti; }
             const int tj = rem;
-            for (int e = tid; e < 1024; e += NT) {
-                double acc = 0.0;
-                for (int sp = 0; sp < nsplit; ++sp) acc += a.Kpart[((size_t)b * nsplit + sp) * 1024 + e];
-                const int r = ti * 32 + (e >> 5), c = tj * 32 + (e & 31);
+            if (q >= 1024 && ti != tj) continue;
+            double acc = 0.0;
+            for (int sp = 0; sp < nsplit; ++sp) acc += a.Kpart[((size_t)b * nsplit + sp) * 1152 + q];
+            if (q < 1024) {
+                const int r = ti * 32 + (q >> 5), c = tj * 32 + (q & 31);
                 if (r < nS && c < nS && c <= r) {
                     a.K[(size_t)r * a.ldk + c] = acc;
                     a.K[(size_t)c * a.ldk + r] = acc;
                 }
+            } else {
+                const int c = ti * 32 + (q - 1024) / 3, i = (q - 1024) % 3;
+                if (c < nS) a.yS[3 * c + i] = -acc;
             }
         }
     }
@@ -446,13 +436,14 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
             if (bid == 0) {          // P = A_kk^{-1} = Li^T Li
                 ld_tile(T0, a.K + (size_t)kc0 * a.ldk + kc0, a.ldk, kn, kn);
                 __syncthreads();
-                tile_chol64_fast(T0, T1, kn, kn, a.info);
-                for (int e = tid; e < TB * TB; e += NT) {
+                tile_chol64(T0, T1, kn, kn, a.info);
+                for (int e = tid; e < TB * TB; e += NT) {      // T2 = Li^T
                     const int r = e >> 6, c = e & 63;
-                    double acc = 0.0;
-                    for (int q = max(r, c); q < kn; ++q) acc += T1[q * TS + r] * T1[q * TS + c];
-                    a.T[e] = acc;
+                    T2[r * TS + c] = T1[c * TS + r];
                 }
+                __syncthreads();
+                tile_xyt(T3, T2, T2, 1.0, false);               // P = Li^T Li on DMMA
+                st_tile(T3, a.T, TB, TB, TB);
             }
             GSYNC();
             for (int b = bid; b < nt - 1; b += G) {      // U_i = A_ik P, i != k
@@ -511,7 +502,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
         if (bid == 0) {
             ld_tile(T0, a.Sh + (size_t)kc0 * a.ldh + kc0, a.ldh, kn, kn);
             __syncthreads();
-            tile_chol64_fast(T0, T1, kn, m - kc0, a.info);
+            tile_chol64(T0, T1, kn, m - kc0, a.info);
             st_tile(T0, a.Sh + (size_t)kc0 * a.ldh + kc0, a.ldh, kn, kn);
             for (int e = tid; e < TB * TB; e += NT) a.Lstore[(size_t)k * TB * TB + e] = T1[(e >> 6) * TS + (e & 63)];
         }
@@ -542,30 +533,62 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
     }
     // ------------------------------------------------ P4: u = C^{-T} y, y = row m of the factor
     // right-looking on C^T: u_k = Li_k^T y_k, then y_j -= (C_kj)^T u_k for j < k
-    for (int e = bid * NT + tid; e < m; e += G * NT) a.u[e] = a.Sh[(size_t)m * a.ldh + e];
-    GSYNC();
     const int ntm = (m + TB - 1) / TB;
-    for (int k = ntm - 1; k >= 0; --k) {
-        const int kc0 = k * TB, kn = min(TB, m - kc0);
+    if (m <= kP4Single) {
+        // small systems: one CTA, y resident in shared memory, no grid barriers
         if (bid == 0) {
-            double *yk = T3;                      // stage y_k
-            for (int i = tid; i < TB; i += NT) yk[i] = i < kn ? a.u[kc0 + i] : 0.0;
+            double *uy = T0, *part = T1;
+            for (int e = tid; e < m; e += NT) uy[e] = a.Sh[(size_t)m * a.ldh + e];
             __syncthreads();
-            const double *Li = a.Lstore + (size_t)k * TB * TB;
-            for (int i = tid; i < kn; i += NT) {  // u_k[i] = sum_r Li[r][i] y_k[r]
-                double acc = 0.0;
-                for (int r = i; r < kn; ++r) acc += Li[r * TB + i] * yk[r];
-                a.u[kc0 + i] = acc;
+            for (int k = ntm - 1; k >= 0; --k) {
+                const int kc0 = k * TB, kn = min(TB, m - kc0);
+                const double *Li = a.Lstore + (size_t)k * TB * TB;
+                {   // u_k[i] = sum_{r >= i} Li[r][i] y_k[r]: 4 partial sums per output
+                    const int i = tid & 63, pq = tid >> 6;
+                    double acc = 0.0;
+                    if (i < kn)
+                        for (int r = i + pq; r < kn; r += 4) acc += Li[r * TB + i] * uy[kc0 + r];
+                    part[pq * TB + i] = acc;
+                }
+                __syncthreads();
+                if (tid < kn) uy[kc0 + tid] = part[tid] + part[TB + tid] + part[2 * TB + tid] + part[3 * TB + tid];
+                __syncthreads();
+                for (int j = tid; j < kc0; j += NT) {   // y_j -= sum_r C[kc0 + r][j] u_k[r]
+                    double acc = 0.0;
+#pragma unroll 8
+                    for (int r = 0; r < kn; ++r) acc += a.Sh[(size_t)(kc0 + r) * a.ldh + j] * uy[kc0 + r];
+                    uy[j] -= acc;
+                }
+                __syncthreads();
             }
+            for (int e = tid; e < m; e += NT) a.u[e] = uy[e];
         }
         GSYNC();
-        // y_j -= C_kj^T u_k  for rows j < kc0 (block row k of the factor, columns j)
-        for (int j = bid * NT + tid; j < kc0; j += G * NT) {
-            double acc = 0.0;
-            for (int r = 0; r < kn; ++r) acc += a.Sh[(size_t)(kc0 + r) * a.ldh + j] * a.u[kc0 + r];
-            a.u[j] -= acc;
-        }
+    } else {
+        for (int e = bid * NT + tid; e < m; e += G * NT) a.u[e] = a.Sh[(size_t)m * a.ldh + e];
         GSYNC();
+        for (int k = ntm - 1; k >= 0; --k) {
+            const int kc0 = k * TB, kn = min(TB, m - kc0);
+            if (bid == 0) {
+                double *yk = T3;                      // stage y_k
+                for (int i = tid; i < TB; i += NT) yk[i] = i < kn ? a.u[kc0 + i] : 0.0;
+                __syncthreads();
+                const double *Li = a.Lstore + (size_t)k * TB * TB;
+                for (int i = tid; i < kn; i += NT) {  // u_k[i] = sum_r Li[r][i] y_k[r]
+                    double acc = 0.0;
+                    for (int r = i; r < kn; ++r) acc += Li[r * TB + i] * yk[r];
+                    a.u[kc0 + i] = acc;
+                }
+            }
+            GSYNC();
+            // y_j -= C_kj^T u_k  for rows j < kc0 (block row k of the factor, columns j)
+            for (int j = bid * NT + tid; j < kc0; j += G * NT) {
+                double acc = 0.0;
+                for (int r = 0; r < kn; ++r) acc += a.Sh[(size_t)(kc0 + r) * a.ldh + j] * a.u[kc0 + r];
+                a.u[j] -= acc;
+            }
+            GSYNC();
+        }
     }
     // ------------------------------------------------ P5: t = B u ; Z = w + V t
     for (int row = bid * (NT / 32) + wid; row < m; row += G * (NT / 32)) {
@@ -611,8 +634,8 @@ int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, 
     a.sn_parent = F.sn_parent; a.lo = lo; a.hi = hi; a.nsn = F.nsn; a.nf = F.nf; a.nS = nS;
     a.K = K; a.ldk = ldk; a.Bc = Bc; a.ldb = ldb; a.Sh = Sh; a.ldh = ldh; a.Lstore = Lstore;
     a.T = T; a.U = U; a.yS = yS; a.u = u; a.t = t; a.Z = Z; a.info = info; a.prof = prof;
-    static double *kpart = nullptr;                 // grid x 1024 doubles, allocated once
-    if (!kpart) cudaMalloc(&kpart, (size_t)g_schur_grid * 1024 * sizeof(double));
+    static double *kpart = nullptr;                 // grid x 1152 doubles, allocated once
+    if (!kpart) cudaMalloc(&kpart, (size_t)g_schur_grid * 1152 * sizeof(double));
     a.Kpart = kpart;
     void *args[] = {&a};
     note_launch();

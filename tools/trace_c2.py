@@ -61,3 +61,17 @@ for c in chain:
     its = np.nonzero(sid == c)[0]
     print(f"  {c:4d} w {w[c]:3d} nr {nr[c]:4d} items {len(its):3d}  wait {(start[c] - cf) / 1e3:6.2f}  "
           f"span {(fin[c] - start[c]) / 1e3:6.2f}  maxwork {work[its].max() / 1e3:6.2f}")
+
+# ---- fused Schur kernel: time between consecutive grid barriers (last traced call)
+sp = path + ".schur"
+if os.path.exists(sp):
+    raw = open(sp, "rb").read()
+    rec = 4 + 8 * 1024
+    nrec = len(raw) // rec
+    (nS,) = struct.unpack_from("i", raw, (nrec - 1) * rec)
+    ts = np.frombuffer(raw, np.uint64, 1024, (nrec - 1) * rec + 4).astype(np.int64)
+    print("records", nrec, "nonzero per record", [int((np.frombuffer(raw, np.uint64, 1024, r * rec + 4) > 0).sum()) for r in range(max(0, nrec - 5), nrec)])
+    ts = ts[ts > 0]
+    d = np.diff(ts) / 1e3
+    print(f"schur nS {nS}: {len(d)} barrier intervals, total {d.sum():.1f} us")
+    print("  intervals (us):", " ".join(f"{x:.1f}" for x in d))
