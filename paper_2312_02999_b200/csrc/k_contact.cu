@@ -597,7 +597,7 @@ __global__ void __launch_bounds__(kPD_WARPS * 32) k_pair_derivs(
             if (i != j) off += H[i][j] * H[i][j];
         }
         off = warp_sum(off);
-        if (off <= 1e-30 * fro) break;
+        if (off <= 1e-26 * fro) break;   // off-diagonal norm <= 1e-13 of the Frobenius norm
         for (int round = 0; round < 11; ++round) {
             // pairs of the round: players 0..11, player 11 fixed, others rotate
             if (lane < 6) {
