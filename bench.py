@@ -54,6 +54,14 @@ def _peaks():
         return 6650.0, 1590.0, "fallback"
 
 
+def _sm_max_mhz():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["sm_max_mhz"])
+    except Exception:
+        return 1965.0
+
+
 def _frame_index(f):
     return min(f, N_FRAMES - 1)
 
@@ -225,12 +233,14 @@ def run_ours(a):
     clocks.start()
     l0 = P.launch_count()
     t_wall = time.perf_counter()
+    torch.cuda.nvtx.range_push("timed")                          # ncu --nvtx-include timed/
     for i, f in enumerate(timed):
         flush.fill_(float(i))                                    # evict L2 between steps
         ev[i][0].record()
         st = s.step(A_device_ptr=frames_dev[_frame_index(f)].data_ptr(), n_iters=ITERS_PER_FRAME)
         ev[i][1].record()
         stats_log.append(st[0])
+    torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     t_wall = time.perf_counter() - t_wall
     launches = P.launch_count() - l0
@@ -282,12 +292,13 @@ def run_ours(a):
     iters_total = world * K * ITERS_PER_FRAME
     value = iters_total / (max_ms / 1000.0)
     hbm, bf16, peak_src = _peaks()
+    sm_max = _sm_max_mhz()
     # ---- roofline: dominant kernel group (live CUDA-event timings) and the local step
     name_dom = max(ktimes, key=lambda k: ktimes[k][0])
     n_iter_timed = K * ITERS_PER_FRAME
     nS_mean = statistics.mean(st["n_S"] for st in stats_log)
-    rl = _roofline(name_dom, ktimes, sc, hbm, bf16, peak_src, stats_log)
-    rl_local = _roofline("local_step", ktimes, sc, hbm, bf16, peak_src, stats_log)
+    rl = _roofline(name_dom, ktimes, sc, hbm, sm_max, peak_src, stats_log)
+    rl_local = _roofline("local_step", ktimes, sc, hbm, sm_max, peak_src, stats_log)
     cpu = None
     if world == 1 and not a.no_cpu_baseline:
         cpu = cpu_baseline(x_start, start, a.cpu_seconds)
@@ -321,8 +332,24 @@ def run_ours(a):
         dist.destroy_process_group()
 
 
-def _roofline(name, ktimes, sc, hbm, bf16, peak_src, stats_log):
-    """Achieved = algorithmic bytes (flops) per launch / average launch duration (DESIGN.md)."""
+# FP64 tensor (DMMA, mma.sync.m8n8k4.f64) throughput measured on this pool's B200 by
+# tools/micro/fp64_peaks.cu: 128 flop/clk/SM (profiles/fp64_peaks_r01.txt).  tcgen05 has no
+# f64 kind, so this is the FP64 contraction peak; x 148 SMs x the max SM clock.
+DMMA_FLOP_PER_CLK_SM = 128.0
+N_SM = 148
+
+
+def _traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full summary, or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(kernel)
+    except Exception:
+        return None
+
+
+def _roofline(name, ktimes, sc, hbm, sm_max_mhz, peak_src, stats_log):
+    """Achieved = algorithmic bytes (flops) per launch / average launch duration (DESIGN.md 5)."""
     ms, cnt = ktimes.get(name, (0.0, 0))
     if cnt == 0 or ms <= 0:
         return None
@@ -330,28 +357,31 @@ def _roofline(name, ktimes, sc, hbm, bf16, peak_src, stats_log):
     T, n = sc.n_tets, sc.n_verts
     nf = n - len(sc.fixed)
     if name == "local_step":
+        # per tet: tet ids 16 B, B_i 72, A_i (6 sym) 48, w_i 8, corner forces written 96;
+        # per vertex: x 32 (double4) read once
         byts = T * (16 + 72 + 48 + 8 + 96) + n * 32
-        return {"kernel": name, "bound": "hbm", "achieved": byts / avg_s / 1e9, "peak": hbm,
-                "unit": "GB/s", "frac": byts / avg_s / 1e9 / hbm, "traffic": None,
+        return {"kernel": "k_local_step", "bound": "hbm", "achieved": byts / avg_s / 1e9, "peak": hbm,
+                "unit": "GB/s", "frac": byts / avg_s / 1e9 / hbm, "traffic": _traffic("k_local_step"),
                 "bytes_per_launch": byts, "avg_launch_us": avg_s * 1e6, "peak_source": peak_src}
     if name == "gather":
         byts = nf * (8 + 32) + 4 * T * (4 + 24)
-        return {"kernel": name, "bound": "hbm", "achieved": byts / avg_s / 1e9, "peak": hbm,
-                "unit": "GB/s", "frac": byts / avg_s / 1e9 / hbm, "traffic": None,
+        return {"kernel": "k_gather_elastic", "bound": "hbm", "achieved": byts / avg_s / 1e9, "peak": hbm,
+                "unit": "GB/s", "frac": byts / avg_s / 1e9 / hbm, "traffic": _traffic("k_gather_elastic"),
                 "bytes_per_launch": byts, "avg_launch_us": avg_s * 1e6, "peak_source": peak_src}
     if name == "dense_schur":
-        m = statistics.mean(st["n_S"] for st in stats_log)
-        flops = 2 * m ** 3 + (3 * m) ** 3 / 3.0 + 2 * (3 * m) ** 2
-        fp64 = bf16 * (37.2 / 2250.0)
-        return {"kernel": name, "bound": "tensor", "achieved": flops / avg_s / 1e12, "peak": fp64,
-                "unit": "TFLOP/s", "frac": flops / avg_s / 1e12 / fp64, "traffic": None,
+        # algorithmic flops of a9 at n_c = |S|, m = 3 n_c: Sigma_s = K^-1 (n_c^3), Cholesky of
+        # the augmented Sigma-hat (m^3 / 3), back substitution 2 m^2, t = B u and Z 2 m^2
+        nc = statistics.mean(st["n_S"] for st in stats_log)
+        m = 3 * nc
+        flops = nc ** 3 + m ** 3 / 3.0 + 4 * m ** 2
+        fp64 = DMMA_FLOP_PER_CLK_SM * N_SM * sm_max_mhz * 1e6 / 1e12
+        return {"kernel": "k_schur_coop", "bound": "tensor", "achieved": flops / avg_s / 1e12, "peak": fp64,
+                "unit": "TFLOP/s", "frac": flops / avg_s / 1e12 / fp64, "traffic": _traffic("k_schur_coop"),
                 "flops_per_launch": flops, "avg_launch_us": avg_s * 1e6,
-                "peak_source": f"{peak_src} bf16 x FP64/bf16 nominal ratio 37.2/2250"}
-    # latency-bound groups: report against HBM with their algorithmic bytes estimate
-    byts = {"forward_solve": None, "backward_solve": None}.get(name)
-    return {"kernel": name, "bound": "hbm", "achieved": None, "peak": hbm, "unit": "GB/s",
-            "frac": None, "traffic": None, "avg_launch_us": avg_s * 1e6, "peak_source": peak_src,
-            "note": "latency-bound group; see DESIGN.md"}
+                "peak_source": "FP64 DMMA measured (tools/micro/fp64_peaks.cu) x 148 SMs x max clock"}
+    return {"kernel": name, "bound": "latency", "achieved": None, "peak": None, "unit": None,
+            "frac": None, "traffic": None, "avg_launch_us": avg_s * 1e6,
+            "note": "latency-bound stage; see DESIGN.md"}
 
 
 def main():

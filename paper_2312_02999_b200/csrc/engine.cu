@@ -461,6 +461,7 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
     // ---------------- G-Step
     const DevFactor &F = h->F;
     CK(cudaMemsetAsync(h->ticket.p, 0, 2 * sizeof(int), st));
+    CK(cudaMemsetAsync(h->dint.p + 4, 0, sizeof(int), st));   // Cholesky info of this iteration
     kt.start(K_FWD, st);
     launch_ts_items(F, h->qS.p, nS_dev, h->ts_lo.p, h->ts_hi.p, h->ts_cnt.p, h->ts_rem.p, st);
     scan_exclusive(h->ts_cnt.p, h->ts_ptr.p, F.nsn, h->iscr.p, st);
@@ -484,7 +485,6 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
     if (nS > 0) {
         const int ldk = h->capS, m3 = 3 * nS, ldb = 3 * h->capS;
         int *info = h->dint.p + 4;
-        CK(cudaMemsetAsync(info, 0, sizeof(int), st));
         (void)m3;
         if (h->trace_file) {
             h->sprof.ensure(1024);
@@ -536,8 +536,6 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
         int nb2 = quad_partials(h->tets.p, h->dx.p, h->B.p, h->w.p, T, h->part.p + nb1, st);
         sum_partials(h->part.p + nb1, nb2, scal + 1, st);
         CK(cudaMemcpyAsync(ls, amin, sizeof(double), cudaMemcpyDeviceToDevice, st));
-        double zeros[2] = {0.0, 0.0};
-        (void)zeros;
         CK(cudaMemsetAsync(ls + 1, 0, 2 * sizeof(double), st));
         const int nsw = spt + see;
         h->b0.ensure(nsw + 1);
@@ -848,6 +846,8 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         h->ticket.exact(4);
         h->dscal.exact(16);
         h->dint.exact(16);
+        CK(cudaMemset(h->dscal.p, 0, sizeof(double) * 16));   // flags / counters start cleared
+        CK(cudaMemset(h->dint.p, 0, sizeof(int) * 16));
         const size_t cap_cand = o.max_pairs > 0 ? (size_t)o.max_pairs
                                                 : std::max<size_t>(1 << 16, 16 * (size_t)(m.Ns + m.Ne));
         h->cand.exact(2 * cap_cand);

@@ -264,7 +264,6 @@ __device__ void tile_chol64(double *S, double *Li, int nb, int free_row, int *in
 __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
     extern __shared__ double sm[];
     double *T0 = sm, *T1 = sm + TB * TS, *T2 = sm + 2 * TB * TS, *T3 = sm + 3 * TB * TS;
-    __shared__ double red[32];
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int G = gridDim.x, bid = blockIdx.x;

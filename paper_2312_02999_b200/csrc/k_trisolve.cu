@@ -29,7 +29,6 @@ namespace pdipc {
 constexpr int kTS_NT = 256;            // threads per CTA
 constexpr int kTS_W = 128;             // max supernode width (host caps it)
 constexpr int kPT = 32;                // panel tile width
-constexpr int kLD = kPT + 1;           // smem row stride
 // Safety net: a dependency wait longer than ~2 s (at ~2 GHz) means a scheduling bug; the
 // waiting CTA records the fault in ticket[1] and proceeds instead of hanging the GPU.
 constexpr long long kSpinLimit = 4000000000LL;

@@ -141,3 +141,71 @@ def test_face_small_lockstep(P):
         x = ref["x"]
     assert seen_contact
     s.close()
+
+
+def test_c2_full_size_lockstep(P):
+    """BASELINE configs[1] at full size (47.5k tets), in the bench's launch configuration: run the
+    GPU into the contact regime, then one lockstep iteration against the oracle from the same x."""
+    from oracle import OracleSolver
+    sc = scenes.face_c2(n_frames=60)
+    s = P.Solver(sc)
+    for f in range(22):
+        s.step(A_next=sc.actuation(f)[None], n_iters=20)
+    x = s.positions()
+    A = sc.actuation(22)
+    o = OracleSolver(sc)
+    P.set_debug(s.h, 1)
+    for k in range(2):
+        ref = o.iterate(x, A)
+        P.set_positions(s.h, x)
+        st = s.step(A_next=A[None], n_iters=1)[0]
+        pt, ee, S = P.get_contacts(s.h)
+        assert ref["n_pt"] + ref["n_ee"] > 0, "not in the contact regime"
+        assert pt.shape[0] == ref["n_pt"] and ee.shape[0] == ref["n_ee"]
+        assert np.array_equal(pt[:, 0], ref["C"]["pt"][0]) and np.array_equal(pt[:, 1], ref["C"]["pt"][1])
+        assert np.array_equal(ee[:, 0], ref["C"]["ee"][0]) and np.array_equal(ee[:, 1], ref["C"]["ee"][1])
+        assert np.array_equal(S, ref["S"])
+        g = P.get_vector(s.h, sc.n_verts, 0)
+        gref = np.zeros((sc.n_verts, 3))
+        gref[o.mesh.free] = ref["ghat"].reshape(-1, 3)
+        assert _rel(g, gref) < 1e-10
+        dx = P.get_vector(s.h, sc.n_verts, 1)
+        assert _rel(dx, ref["dx"]) < 1e-8, _rel(dx, ref["dx"])
+        assert abs(st["alpha_max"] - ref["alpha_m"]) <= 1e-10 * ref["alpha_m"]
+        x = ref["x"]
+    s.close()
+
+
+def test_sequences_are_independent_and_deterministic(P):
+    """n_seq = 2 with different actuations: each sequence equals its single-sequence run bit for
+    bit, and a rerun reproduces it bit for bit (deterministic assembly, no atomics order)."""
+    sc = scenes.slabs_c1()
+    A1 = sc.actuation(0)
+    A2 = A1.copy()
+    A2[:, 8] = 1.2                        # a different (symmetric, det > 0) actuation
+    both = P.Solver(sc, A=np.stack([A1, A2]), n_seq=2)
+    both.step(n_iters=8)
+    xs = [both.positions(0), both.positions(1)]
+    both.close()
+    for A, xb in ((A1, xs[0]), (A2, xs[1])):
+        for _ in range(2):
+            one = P.Solver(sc, A=A[None])
+            one.step(n_iters=8)
+            assert np.array_equal(one.positions(), xb)
+            one.close()
+    assert not np.array_equal(xs[0], xs[1])
+
+
+def test_degenerate_meshes(P):
+    """Edge cases: a single tet and two tets without a collision surface (pure PD, no contact
+    work at all) step to the oracle's result."""
+    from oracle import OracleSolver
+    for sc in (scenes.single_tet(), scenes.two_tets()):
+        o = OracleSolver(sc)
+        A = np.tile(np.diag([1.2, 1.0, 0.9]).reshape(1, 9), (sc.n_tets, 1))
+        s = P.Solver(sc, A=A[None])
+        st = s.step(n_iters=1)[0]
+        ref = o.iterate(sc.rest.copy(), A)
+        assert st["n_S"] == 0 and st["n_active"] == 0
+        assert np.abs(s.positions() - ref["x"]).max() <= 1e-9 * max(sc.bbox_diag(), 1e-300)
+        s.close()
