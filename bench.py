@@ -192,6 +192,25 @@ def run_reference(a):
 
 
 # ------------------------------------------------------------------------------ ours -------
+def gather_rank_values(vals, world, device):
+    """All ranks' per-rank measurements as a (world, len(vals)) array (NCCL on the GPU path; any
+    backend works).  The job's time is the max over ranks of the device-timed region."""
+    import torch
+    import torch.distributed as dist
+    mine = torch.tensor(vals, dtype=torch.float64, device=device)
+    if world > 1:
+        allv = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(allv, mine)
+        return torch.stack(allv).cpu().numpy()
+    return mine.cpu().numpy()[None]
+
+
+def job_throughput(per_rank_ms, world, steps, iters_per_step=ITERS_PER_FRAME):
+    """Whole-job iterations/s: every rank ran `steps` frames of its own sequence (weak scaling);
+    the job took the slowest rank's time."""
+    return world * steps * iters_per_step / (max(per_rank_ms) / 1000.0)
+
+
 def run_ours(a):
     import numpy as np
     import torch
@@ -276,13 +295,7 @@ def run_ours(a):
         e2e = {"ms": e2e_ms, "h2d": T * 9 * 8, "d2h": n * 3 * 8}
 
     # ---------------- gather over ranks
-    mine = torch.tensor([my_ms, e2e["ms"] if e2e else 0.0], dtype=torch.float64, device=f"cuda:{local}")
-    if world > 1:
-        allv = [torch.zeros_like(mine) for _ in range(world)]
-        dist.all_gather(allv, mine)
-        allv = torch.stack(allv).cpu().numpy()
-    else:
-        allv = mine.cpu().numpy()[None]
+    allv = gather_rank_values([my_ms, e2e["ms"] if e2e else 0.0], world, f"cuda:{local}")
     max_ms, max_e2e = float(allv[:, 0].max()), float(allv[:, 1].max())
     if rank != 0:
         if world > 1:
@@ -290,7 +303,7 @@ def run_ours(a):
         return
 
     iters_total = world * K * ITERS_PER_FRAME
-    value = iters_total / (max_ms / 1000.0)
+    value = job_throughput(allv[:, 0], world, K)
     hbm, bf16, peak_src = _peaks()
     sm_max = _sm_max_mhz()
     # ---- roofline: dominant kernel group (live CUDA-event timings) and the local step
