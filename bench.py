@@ -338,6 +338,7 @@ def run_ours(a):
         "clocks": clk,
         "stage_ms_per_iter": {k: v[0] / max(v[1], 1) for k, v in ktimes.items()},
         "n_c_mean": nS_mean, "n_active_last": stats_log[-1]["n_active"],
+        "sigma_reuse_frac": sum(st["sigma_reused"] for st in stats_log) / float(K * ITERS_PER_FRAME),
         "alpha_last": stats_log[-1]["alpha"], "wall_s": t_wall,
     }
     print(json.dumps(line), flush=True)

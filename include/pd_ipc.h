@@ -73,6 +73,10 @@ typedef struct {
     int32_t A_on_device;      /* 0: A_next is host memory; 1: device pointer [n_seq][T][9]    */
     int32_t max_pairs;        /* capacity of candidate / active pair buffers (0 = auto)       */
     double accd_s;            /* ACCD gap fraction s_gap (default 0.1)                        */
+    int32_t no_sigma_reuse;   /* 0 (default): V_s, K_s and Sigma_s = K_s^{-1} -- functions of S
+                                 and the constant factor only -- are recomputed only when S
+                                 differs bit for bit from the S they were last computed for;
+                                 1: recompute them every iteration                             */
 } pd_ipc_options;
 
 /* Per sequence, describing the LAST iteration of the last pd_ipc_step call. */
@@ -89,6 +93,8 @@ typedef struct {
     double min_dist;          /* min active-pair distance before the step (0 if C empty)      */
     double ms[6];             /* device time per stage over the call: IPC, G-Step, CCD, LS,
                                  Misc, total (Table 1 categories)               */
+    int32_t sigma_reused;     /* iterations of the call that reused V_s, K_s, Sigma_s (S same) */
+    int32_t reserved;
 } pd_ipc_stats;
 
 /* Create a solver: validates the mesh, computes B_i = D_m^{-1} and w_i = det/6, assembles the

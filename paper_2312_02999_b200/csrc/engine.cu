@@ -158,7 +158,7 @@ struct pd_ipc {
     DBuf<long long> f_valptr, f_dinv_ptr;
     DBuf<double> f_L, f_dinv, Ug, Up, Yw, bw_P;
     DBuf<int2> f_bw_items, f_rc_src;
-    DBuf<int> f_bw_pbase, bw_cnt, f_ford;
+    DBuf<int> f_bw_pbase, bw_cnt, f_ford, qS_prev;
     DBuf<int> f_uoff, f_urow_sn, f_rc_ptr, f_rc_idx, f_urel, f_ch_ptr, f_ch;
     // sequences
     std::vector<std::unique_ptr<Seq>> seqs;
@@ -405,6 +405,10 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
         launch_mark_S(h->ids.p, na, h->Wp.p, h->Wc.p, h->v2q.p, h->mark.p, st);
         scan_exclusive(h->mark.p, h->spos.p, nf, h->iscr.p, st);
         launch_compact_S(h->mark.p, h->spos.p, nf, h->qS.p, st);
+        // V_s, K_s, Sigma_s depend on S (and the constant factor) only: reuse them while S is
+        // bit-identical to the S they were computed for (dint[8] = its size, dint[9] = flag)
+        launch_same_S(h->qS.p, nS_dev, h->qS_prev.p, h->dint.p + 8, h->dint.p + 9, h->capS,
+                      h->opt.no_sigma_reuse == 0, st);
         // gradient pull-back: deterministic fixed-point accumulation on the surface, then W^T
         h->gsq.ensure(6 * (size_t)Ns + 6);
         CK(cudaMemsetAsync(h->gsq.p, 0, sizeof(long long) * 6 * Ns, st));
@@ -426,6 +430,7 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
         kt.stop(K_ASSEMBLY, st);
     } else {
         CK(cudaMemsetAsync(nS_dev, 0, sizeof(int), st));
+        CK(cudaMemsetAsync(h->dint.p + 9, 0, sizeof(int), st));
         launch_grad_pullback(h->g_el.p, h->WTp.p, h->WTr.p, h->WTv.p, nullptr, nf, h->G.p, st);
     }
     if (h->debug) {
@@ -463,7 +468,7 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
     CK(cudaMemsetAsync(h->ticket.p, 0, 2 * sizeof(int), st));
     CK(cudaMemsetAsync(h->dint.p + 4, 0, sizeof(int), st));   // Cholesky info of this iteration
     kt.start(K_FWD, st);
-    launch_ts_items(F, h->qS.p, nS_dev, h->ts_lo.p, h->ts_hi.p, h->ts_cnt.p, h->ts_rem.p, st);
+    launch_ts_items(F, h->qS.p, nS_dev, h->dint.p + 9, h->ts_lo.p, h->ts_hi.p, h->ts_cnt.p, h->ts_rem.p, st);
     scan_exclusive(h->ts_cnt.p, h->ts_ptr.p, F.nsn, h->iscr.p, st);
     const int ldu = std::max(32, ((nS + 31) / 32) * 32);
     if (nS > 0) h->Up.ensure((size_t)std::max(1, F.nU) * ldu);
@@ -492,7 +497,7 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
         }
         CK((cudaError_t)launch_schur(F, h->V.p, h->ldv, h->Yw.p, h->qS.p, h->ts_lo.p, h->ts_hi.p, nS, h->K.p,
                                      ldk, h->Bc.p, ldb, h->Sh.p, h->ldh, h->Lstore.p, h->Tt.p, h->U.p,
-                                     h->yS.p, h->u.p, h->tv.p, h->Z.p, info,
+                                     h->yS.p, h->u.p, h->tv.p, h->Z.p, info, h->dint.p + 9,
                                      h->trace_file ? h->sprof.p : nullptr, st));
         if (h->trace_file && h->schur_file) {
             std::vector<unsigned long long> pr(1024);
@@ -563,8 +568,10 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
     double sc[13];
     CK(cudaMemcpyAsync(sc, h->dscal.p, sizeof(sc), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    int info_h = 0, fault_h = 0;
-    CK(cudaMemcpy(&info_h, h->dint.p + 4, sizeof(int), cudaMemcpyDeviceToHost));
+    int info_h = 0, fault_h = 0, flags_h[6];
+    CK(cudaMemcpy(flags_h, h->dint.p + 4, sizeof(flags_h), cudaMemcpyDeviceToHost));
+    info_h = flags_h[0];
+    q.stats.sigma_reused += nS > 0 ? flags_h[5] : 0;
     CK(cudaMemcpy(&fault_h, h->ticket.p + 1, sizeof(int), cudaMemcpyDeviceToHost));
     if (fault_h) throw CudaError("triangular solve dependency wait timed out", PD_IPC_E_CUDA);
     if (info_h) throw CudaError("dense Cholesky: matrix not SPD", PD_IPC_E_NOT_SPD);
@@ -837,6 +844,7 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         h->mark.exact(nf + 1);
         h->spos.exact(nf + 1);
         h->qS.exact(nf + 1);
+        h->qS_prev.exact(nf + 1);
         h->ts_lo.exact(f.nsn);
         h->ts_hi.exact(f.nsn);
         h->ts_cnt.exact(f.nsn + 1);
@@ -929,6 +937,7 @@ int pd_ipc_step(pd_ipc *h, const double *A_next, int32_t n_iters, pd_ipc_stats *
         }
         for (auto &sq : h->seqs) {
             double ms[6] = {0, 0, 0, 0, 0, 0};
+            sq->stats.sigma_reused = 0;
             for (int it = 0; it < n_iters; ++it) iterate(h, *sq, it == n_iters - 1, ms);
             sq->stats.iters = n_iters;
             for (int k = 0; k < 6; ++k) sq->stats.ms[k] = ms[k];
@@ -975,7 +984,7 @@ void pd_ipc_destroy(pd_ipc *h) {
     rel(h->Wp); rel(h->Wc); rel(h->WTp); rel(h->WTr); rel(h->tris); rel(h->edges); rel(h->Wv); rel(h->WTv);
     rel(h->f_c0); rel(h->f_rowptr); rel(h->f_rows); rel(h->f_parent); rel(h->f_seg_ptr); rel(h->f_seg_d);
     rel(h->f_seg_klo); rel(h->f_seg_khi); rel(h->f_fd); rel(h->f_col2sn); rel(h->f_valptr); rel(h->f_L);
-    rel(h->f_dinv_ptr); rel(h->f_dinv); rel(h->Ug); rel(h->Up); rel(h->Yw); rel(h->bw_P); rel(h->f_bw_items); rel(h->f_ford); rel(h->f_rc_src); rel(h->f_bw_pbase); rel(h->bw_cnt); rel(h->f_uoff); rel(h->f_urow_sn);
+    rel(h->f_dinv_ptr); rel(h->f_dinv); rel(h->Ug); rel(h->Up); rel(h->Yw); rel(h->bw_P); rel(h->f_bw_items); rel(h->f_ford); rel(h->qS_prev); rel(h->f_rc_src); rel(h->f_bw_pbase); rel(h->bw_cnt); rel(h->f_uoff); rel(h->f_urow_sn);
     rel(h->f_rc_ptr); rel(h->f_rc_idx); rel(h->f_urel); rel(h->f_ch_ptr); rel(h->f_ch);
     for (auto &s : h->seqs) { rel(s->x); rel(s->A6); rel(s->p); }
     rel(h->fc); rel(h->G); rel(h->Z); rel(h->A9stage); rel(h->g_el); rel(h->s); rel(h->ds); rel(h->dx);

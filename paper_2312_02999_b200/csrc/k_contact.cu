@@ -685,6 +685,21 @@ __global__ void k_compact_S(const int *__restrict__ mark, const int *__restrict_
     if (q < nf && mark[q]) qS[pos[q]] = q;
 }
 
+// same = (S == S_prev, bit for bit, |S| > 0); then S_prev <- S.  One CTA.
+__global__ void __launch_bounds__(1024) k_same_S(const int *__restrict__ qS, const int *__restrict__ nS_ptr,
+                                                 int *__restrict__ qS_prev, int *__restrict__ nS_prev,
+                                                 int *__restrict__ same, int enabled) {
+    const int nS = *nS_ptr, np = *nS_prev;
+    int eq = enabled && nS > 0 && nS == np;
+    for (int i = threadIdx.x; i < nS && eq; i += blockDim.x) eq = qS[i] == qS_prev[i];
+    eq = __syncthreads_and(eq);
+    for (int i = threadIdx.x; i < nS; i += blockDim.x) qS_prev[i] = qS[i];
+    if (threadIdx.x == 0) {
+        *nS_prev = nS;
+        *same = eq;
+    }
+}
+
 // gradient records: key = (surface vertex << sh) | (4k + slot)
 __global__ void k_grad_records(const int *__restrict__ ids, int n_all, int sh,
                                unsigned long long *__restrict__ rec) {
@@ -1140,6 +1155,11 @@ void launch_pair_derivs(const unsigned long long *akeys, const int *atype, const
 void launch_mark_S(const int *ids, int n_all, const int *Wp, const int *Wc, const int *v2q,
                    int *mark, cudaStream_t st) {
     if (n_all > 0) PDI_LAUNCH(k_mark_S, (4 * n_all + 255) / 256, 256, 0, st)(ids, n_all, Wp, Wc, v2q, mark);
+}
+void launch_same_S(const int *qS, const int *nS_ptr, int *qS_prev, int *nS_prev, int *same, int cap,
+                   bool enabled, cudaStream_t st) {
+    (void)cap;
+    PDI_LAUNCH(k_same_S, 1, 1024, 0, st)(qS, nS_ptr, qS_prev, nS_prev, same, enabled ? 1 : 0);
 }
 void launch_compact_S(const int *mark, const int *pos, int nf, int *qS, cudaStream_t st) {
     PDI_LAUNCH(k_compact_S, (nf + 255) / 256, 256, 0, st)(mark, pos, nf, qS);

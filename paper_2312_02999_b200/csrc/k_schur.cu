@@ -53,6 +53,7 @@ struct SchurArgs {
     double *Kpart;              // [grid][1152] split-K partial tiles (+ y_S partials)
     double *Z;                  // [nf][4]
     int *info;
+    const int *same;            // 1: S unchanged, K holds the previous -Sigma_s (reuse it)
     unsigned long long *prof;   // optional phase timestamps (PDIPC_TRACE), [1024]
 };
 
@@ -281,9 +282,19 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
     // [lo_s, hi_s) meets both tile ranges (cp.async double buffer, inactive entries zeroed) and
     // accumulates on DMMA.  Diagonal tiles also accumulate y_S for their columns.  Split partials
     // are reduced in a fixed order (deterministic).
+    const bool reuse = *a.same != 0;                 // uniform across the grid
     const int ntk = (nS + 31) / 32;
-    const int ntiles = ntk * (ntk + 1) / 2;
-    const int nsplit = max(1, min(16, G / max(ntiles, 1)));
+    // with reuse only the diagonal tiles run (they carry y_S); K keeps -Sigma_s
+    const int ntiles = reuse ? ntk : ntk * (ntk + 1) / 2;
+    // the split (hence the summation order of y_S) must not depend on reuse: bit-identical
+    const int nsplit = max(1, min(16, G / max(ntk * (ntk + 1) / 2, 1)));
+    auto tile_of = [&](int b, int &ti, int &tj) {
+        if (reuse) { ti = tj = b; return; }
+        int rem = b;
+        ti = 0;
+        while (rem > ti) { rem -= ti + 1; ++ti; }
+        tj = rem;
+    };
     {
         typedef double Chunk[32][36];
         Chunk *Va = reinterpret_cast<Chunk *>(T0), *Vb = reinterpret_cast<Chunk *>(T1);   // [2] each
@@ -291,9 +302,9 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
         const int gr = lane >> 2, gc = lane & 3;
         for (int bs = bid; bs < ntiles * nsplit; bs += G) {
             const int b = bs / nsplit, split = bs % nsplit;
-            int ti = 0, rem = b;
-            while (rem > ti) { rem -= ti + 1; ++ti; }
-            const int tj = rem, ia = ti * 32, ja = tj * 32;
+            int ti, tj;
+            tile_of(b, ti, tj);
+            const int ia = ti * 32, ja = tj * 32;
             const bool diag = ti == tj;
             // chunk iterator over (supernode s, first row rb)
             auto overlaps = [&](int sn) {
@@ -381,7 +392,8 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
             for (int j = 0; j < 2; ++j) {
                 const int t = wid + 8 * j, ta = t >> 2, tb = t & 3;
                 const int r = 8 * ta + gr, c = 8 * tb + 2 * gc;
-                if (nsplit == 1) {
+                if (reuse) {
+                } else if (nsplit == 1) {
                     for (int q = 0; q < 2; ++q) {
                         const int R = ia + r, Cc = ja + c + q;
                         if (R < nS && Cc < nS && Cc <= R) {
@@ -408,10 +420,10 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
         GSYNC();
         for (int e = bid * NT + tid; e < ntiles * 1120; e += G * NT) {
             const int b = e / 1120, q = e % 1120;
-            int ti = 0, rem = b;
-            while (rem > ti) { rem -= ti + 1; ++ti; }
-            const int tj = rem;
+            int ti, tj;
+            tile_of(b, ti, tj);
             if (q >= 1024 && ti != tj) continue;
+            if (q < 1024 && reuse) continue;
             double acc = 0.0;
             for (int sp = 0; sp < nsplit; ++sp) acc += a.Kpart[((size_t)b * nsplit + sp) * 1152 + q];
             if (q < 1024) {
@@ -428,7 +440,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
     }
     GSYNC();
     // ------------------------------------------------ P1: K <- -K^{-1} (block sweep)
-    {
+    if (!reuse) {
         const int nt = (nS + TB - 1) / TB;
         for (int k = 0; k < nt; ++k) {
             const int kc0 = k * TB, kn = min(TB, nS - kc0);
@@ -627,12 +639,13 @@ void schur_init(int device) {
 int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, const int *qS,
                  const int *lo, const int *hi, int nS, double *K, int ldk, const double *Bc, int ldb,
                  double *Sh, int ldh, double *Lstore, double *T, double *U, double *yS, double *u,
-                 double *t, double *Z, int *info, unsigned long long *prof, cudaStream_t st) {
+                 double *t, double *Z, int *info, const int *same_S, unsigned long long *prof,
+                 cudaStream_t st) {
     SchurArgs a;
     a.V = V; a.ldv = ldv; a.G = G; a.qS = qS; a.col2sn = F.col2sn; a.sn_c0 = F.sn_c0;
     a.sn_parent = F.sn_parent; a.lo = lo; a.hi = hi; a.nsn = F.nsn; a.nf = F.nf; a.nS = nS;
     a.K = K; a.ldk = ldk; a.Bc = Bc; a.ldb = ldb; a.Sh = Sh; a.ldh = ldh; a.Lstore = Lstore;
-    a.T = T; a.U = U; a.yS = yS; a.u = u; a.t = t; a.Z = Z; a.info = info; a.prof = prof;
+    a.T = T; a.U = U; a.yS = yS; a.u = u; a.t = t; a.Z = Z; a.info = info; a.same = same_S; a.prof = prof;
     static double *kpart = nullptr;                 // grid x 1152 doubles, allocated once
     if (!kpart) cudaMalloc(&kpart, (size_t)g_schur_grid * 1152 * sizeof(double));
     a.Kpart = kpart;

@@ -37,8 +37,9 @@ constexpr long long kSpinLimit = 4000000000LL;
 __global__ void k_ts_items(const int *__restrict__ ford, const int *__restrict__ sn_c0,
                            const int *__restrict__ sn_rowptr, const int *__restrict__ sn_fd,
                            const int *__restrict__ sn_parent, int nsn, const int *__restrict__ qS,
-                           const int *__restrict__ nS_ptr, int *__restrict__ lo, int *__restrict__ hi,
-                           int *__restrict__ cnt, int *__restrict__ rem) {
+                           const int *__restrict__ nS_ptr, const int *__restrict__ same_S,
+                           int *__restrict__ lo, int *__restrict__ hi, int *__restrict__ cnt,
+                           int *__restrict__ rem) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;   // dispatch position
     if (k >= nsn) return;
     const int s = ford[k];
@@ -53,7 +54,9 @@ __global__ void k_ts_items(const int *__restrict__ ford, const int *__restrict__
     lo[s] = L0;
     hi[s] = H0;
     const int nb = (sn_rowptr[s + 1] - sn_rowptr[s] + kSolveRB - 1) / kSolveRB;
-    int c = nb * (1 + (H0 > L0 ? (H0 - 1) / kPT - L0 / kPT + 1 : 0));
+    // panel tiles only when V_s must be recomputed (S changed)
+    const int tiles = (*same_S == 0 && H0 > L0) ? (H0 - 1) / kPT - L0 / kPT + 1 : 0;
+    int c = nb * (1 + tiles);
     cnt[k] = c;
     int p = sn_parent[s];
     if (p >= 0) atomicAdd(rem + p, c);
@@ -564,12 +567,12 @@ void trisolve_init() {
     cudaFuncSetAttribute(k_backward_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem);
 }
 
-void launch_ts_items(const DevFactor &F, const int *qS, const int *nS_ptr, int *lo, int *hi, int *cnt,
-                     int *rem, cudaStream_t st) {
+void launch_ts_items(const DevFactor &F, const int *qS, const int *nS_ptr, const int *same_S, int *lo,
+                     int *hi, int *cnt, int *rem, cudaStream_t st) {
     cudaMemsetAsync(rem, 0, sizeof(int) * F.nsn, st);
     PDI_LAUNCH(k_ts_items, (F.nsn + 255) / 256, 256, 0, st)(F.ford, F.sn_c0, F.sn_rowptr, F.sn_fd,
-                                                             F.sn_parent, F.nsn, qS, nS_ptr, lo, hi,
-                                                             cnt, rem);
+                                                             F.sn_parent, F.nsn, qS, nS_ptr, same_S, lo,
+                                                             hi, cnt, rem);
 }
 
 void launch_forward_solve(const DevFactor &F, const int *lo, const int *hi, const int *item_ptr,

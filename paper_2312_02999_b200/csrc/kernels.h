@@ -45,8 +45,8 @@ void launch_scatter_dx(const double *z, const int *q2v, int nf, double4 *dx, cud
 
 // ---- k_trisolve.cu
 constexpr int kSolveRB = 64;   // rows of a supernode per solve work item
-void launch_ts_items(const DevFactor &F, const int *qS, const int *nS_ptr, int *lo, int *hi, int *cnt,
-                     int *rem, cudaStream_t st);
+void launch_ts_items(const DevFactor &F, const int *qS, const int *nS_ptr, const int *same_S, int *lo,
+                     int *hi, int *cnt, int *rem, cudaStream_t st);
 void trisolve_init();
 void launch_forward_solve(const DevFactor &F, const int *lo, const int *hi, const int *item_ptr,
                           const int *qS, int *rem, int *ticket, const double *G, double *Y, double *V,
@@ -66,7 +66,8 @@ void schur_init(int device);
 int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, const int *qS,
                  const int *lo, const int *hi, int nS, double *K, int ldk, const double *Bc, int ldb,
                  double *Sh, int ldh, double *Lstore, double *T, double *U, double *yS, double *u,
-                 double *t, double *Z, int *info, unsigned long long *prof, cudaStream_t st);
+                 double *t, double *Z, int *info, const int *same_S, unsigned long long *prof,
+                 cudaStream_t st);
 void note_launch();
 
 // ---- k_dense.cu
@@ -123,6 +124,8 @@ void launch_grad_pullback_fx(const double4 *g_el, const int *WTp, const int *WTr
 void launch_mark_S(const int *ids, int n_all, const int *Wp, const int *Wc, const int *v2q,
                    int *mark, cudaStream_t st);
 void launch_compact_S(const int *mark, const int *pos, int nf, int *qS, cudaStream_t st);
+void launch_same_S(const int *qS, const int *nS_ptr, int *qS_prev, int *nS_prev, int *same, int cap,
+                   bool enabled, cudaStream_t st);
 void launch_grad_records(const int *ids, int n_all, int sh, unsigned long long *rec,
                          cudaStream_t st);
 void launch_grad_reduce(const unsigned long long *rec, int n, int sh, const double *grad,

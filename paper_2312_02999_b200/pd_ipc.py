@@ -30,17 +30,18 @@ class pd_ipc_mesh(C.Structure):
 class pd_ipc_options(C.Structure):
     _fields_ = [("n_seq", C.c_int32), ("device", C.c_int32), ("ls_max_halvings", C.c_int32),
                 ("accd_max_iters", C.c_int32), ("A_on_device", C.c_int32),
-                ("max_pairs", C.c_int32), ("accd_s", C.c_double)]
+                ("max_pairs", C.c_int32), ("accd_s", C.c_double), ("no_sigma_reuse", C.c_int32)]
 
 
 class pd_ipc_stats(C.Structure):
     _fields_ = [("iters", C.c_int32), ("n_cand", C.c_int32), ("n_active", C.c_int32),
                 ("n_S", C.c_int32), ("ls_trials", C.c_int32), ("flags", C.c_int32),
                 ("alpha_max", C.c_double), ("alpha", C.c_double), ("dE", C.c_double),
-                ("min_dist", C.c_double), ("ms", C.c_double * 6)]
+                ("min_dist", C.c_double), ("ms", C.c_double * 6), ("sigma_reused", C.c_int32),
+                ("reserved", C.c_int32)]
 
     def as_dict(self):
-        d = {k: getattr(self, k) for k, _ in self._fields_ if k != "ms"}
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("ms", "reserved")}
         d["ms"] = dict(zip(("ipc", "gstep", "ccd", "ls", "misc", "total"), list(self.ms)))
         return d
 
@@ -159,14 +160,15 @@ def _check(rc, h=None):
 
 
 def create(scene, A=None, n_seq=1, device=0, A_on_device=False, max_pairs=0,
-           ls_max_halvings=30, accd_max_iters=10_000, accd_s=0.1, d_hat=None, kappa=None):
+           ls_max_halvings=30, accd_max_iters=10_000, accd_s=0.1, d_hat=None, kappa=None,
+           sigma_reuse=True):
     """pd_ipc_create on a scenes.Scene.  A: (n_seq, T, 9) host actuation (default frame 0)."""
     m = _MeshArgs(scene)
     if A is None:
         A = np.stack([scene.actuation(0)] * n_seq)
     A = _f64(A).reshape(n_seq, -1, 9)
     opt = pd_ipc_options(n_seq, device, ls_max_halvings, accd_max_iters, int(A_on_device),
-                         max_pairs, accd_s)
+                         max_pairs, accd_s, 0 if sigma_reuse else 1)
     h = _P()
     rc = lib.pd_ipc_create(C.byref(m.mesh), _dp(m.rest), _dp(A),
                            float(scene.d_hat if d_hat is None else d_hat),

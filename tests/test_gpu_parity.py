@@ -209,3 +209,20 @@ def test_degenerate_meshes(P):
         assert st["n_S"] == 0 and st["n_active"] == 0
         assert np.abs(s.positions() - ref["x"]).max() <= 1e-9 * max(sc.bbox_diag(), 1e-300)
         s.close()
+
+
+def test_sigma_reuse_is_exact(P):
+    """V_s, K_s and Sigma_s are functions of S and the constant factor only: reusing them while S
+    is unchanged must give bit-identical iterates to recomputing them every iteration."""
+    sc = scenes.face_small(n_frames=2)
+    A = np.tile(np.eye(3).reshape(1, 9), (sc.n_tets, 1))
+    A[:, 4] += 0.5 * sc.meta["lip_mask"]
+    xs, reused = [], []
+    for reuse in (True, False):
+        s = P.Solver(sc, A=A[None], sigma_reuse=reuse)
+        st = s.step(n_iters=40)[0]
+        xs.append(s.positions())
+        reused.append(st["sigma_reused"])
+        s.close()
+    assert np.array_equal(xs[0], xs[1])
+    assert reused[0] > 0 and reused[1] == 0, reused
