@@ -695,7 +695,6 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             h->trace_file = std::fopen(tp, "wb");
             h->schur_file = std::fopen((std::string(tp) + ".schur").c_str(), "wb");
         }
-        dense_init();
         contact_init();
         trisolve_init();
         schur_init(o.device);

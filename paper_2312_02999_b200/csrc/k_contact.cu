@@ -700,34 +700,6 @@ __global__ void __launch_bounds__(1024) k_same_S(const int *__restrict__ qS, con
     }
 }
 
-// gradient records: key = (surface vertex << sh) | (4k + slot)
-__global__ void k_grad_records(const int *__restrict__ ids, int n_all, int sh,
-                               unsigned long long *__restrict__ rec) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= 4 * n_all) return;
-    rec[i] = ((unsigned long long)ids[i] << sh) | (unsigned long long)i;
-}
-
-// per run of equal surface vertex: gs[j] = sum of h_k[slot] in (k, slot) order
-__global__ void k_grad_reduce(const unsigned long long *__restrict__ rec, int n, int sh,
-                              const double *__restrict__ grad, double4 *__restrict__ gs) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    unsigned long long j = rec[i] >> sh;
-    if (i > 0 && (rec[i - 1] >> sh) == j) return;
-    double gx = 0, gy = 0, gz = 0;
-    const unsigned long long m = (1ull << sh) - 1;
-    for (int r = i; r < n && (rec[r] >> sh) == j; ++r) {
-        unsigned long long ks = rec[r] & m;
-        const double *g = grad + 12 * (ks >> 2) + 3 * (ks & 3);
-        gx += g[0];
-        gy += g[1];
-        gz += g[2];
-    }
-    gs[j] = make_double4(gx, gy, gz, 0.0);
-}
-
-// G[q] (solve RHS, factor order, [nf][4]) = g_el[q] + sum_{(j,w) in W^T row q} w gs[j]
 __global__ void k_grad_pullback(const double4 *__restrict__ g_el, const int *__restrict__ WTp,
                                 const int *__restrict__ WTr, const double *__restrict__ WTv,
                                 const double4 *__restrict__ gs, int nf, double *__restrict__ G) {
@@ -761,71 +733,6 @@ __device__ __forceinline__ int bc_count_pair(const int *id, const int *Wp, const
     int s = 0;
     for (int a = 0; a < 4; ++a) s += nfree[a];
     return s * s;
-}
-
-__global__ void k_bc_count(const int *__restrict__ ids, int n_all, const int *__restrict__ Wp,
-                           const int *__restrict__ Wc, const int *__restrict__ v2q,
-                           int *__restrict__ cnt) {
-    int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n_all) return;
-    cnt[k] = bc_count_pair(ids + 4 * k, Wp, Wc, v2q);
-}
-
-// key = ((ia * nS + ib) << sh) | (k * 256 + sa * 64 + sb * 16 + na * 4 + nb)
-__global__ void k_bc_records(const int *__restrict__ ids, int n_all, const int *__restrict__ Wp,
-                             const int *__restrict__ Wc, const int *__restrict__ v2q,
-                             const int *__restrict__ sidx, int nS, int sh,
-                             const int *__restrict__ off, unsigned long long *__restrict__ rec) {
-    int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n_all) return;
-    const int *id = ids + 4 * k;
-    int p = off[k];
-    for (int sa = 0; sa < 4; ++sa)
-        for (int na = 0; na < Wp[id[sa] + 1] - Wp[id[sa]]; ++na) {
-            int qa = v2q[Wc[Wp[id[sa]] + na]];
-            if (qa < 0) continue;
-            for (int sb = 0; sb < 4; ++sb)
-                for (int nb = 0; nb < Wp[id[sb] + 1] - Wp[id[sb]]; ++nb) {
-                    int qb = v2q[Wc[Wp[id[sb]] + nb]];
-                    if (qb < 0) continue;
-                    unsigned long long tgt = (unsigned long long)sidx[qa] * nS + sidx[qb];
-                    unsigned long long lo = (unsigned long long)k * 256 + sa * 64 + sb * 16 + na * 4 + nb;
-                    rec[p++] = (tgt << sh) | lo;
-                }
-        }
-}
-
-__device__ __forceinline__ int upk(int i, int j) {   // packed upper index, i <= j
-    return i * 12 - (i * (i - 1)) / 2 + (j - i);
-}
-
-__global__ void k_bc_reduce(const unsigned long long *__restrict__ rec, int n, int sh, int nS,
-                            const int *__restrict__ ids, const int *__restrict__ Wp,
-                            const double *__restrict__ Wv, const double *__restrict__ Hp,
-                            double *__restrict__ Bc, int ldb) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    unsigned long long tgt = rec[i] >> sh;
-    if (i > 0 && (rec[i - 1] >> sh) == tgt) return;
-    double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    const unsigned long long m = (1ull << sh) - 1;
-    for (int r = i; r < n && (rec[r] >> sh) == tgt; ++r) {
-        unsigned long long lo = rec[r] & m;
-        int k = (int)(lo >> 8), sa = (int)(lo >> 6) & 3, sb = (int)(lo >> 4) & 3, na = (int)(lo >> 2) & 3,
-            nb = (int)lo & 3;
-        const int *id = ids + 4 * k;
-        double w = Wv[Wp[id[sa]] + na] * Wv[Wp[id[sb]] + nb];
-        const double *H = Hp + 78 * (size_t)k;
-        for (int a = 0; a < 3; ++a)
-            for (int b = 0; b < 3; ++b) {
-                int ii = 3 * sa + a, jj = 3 * sb + b;
-                double h = ii <= jj ? H[upk(ii, jj)] : H[upk(jj, ii)];
-                acc[3 * a + b] += w * h;
-            }
-    }
-    int ia = (int)(tgt / nS), ib = (int)(tgt % nS);
-    for (int a = 0; a < 3; ++a)
-        for (int b = 0; b < 3; ++b) Bc[(size_t)(3 * ia + a) * ldb + 3 * ib + b] = acc[3 * a + b];
 }
 
 // ---- deterministic fixed-point accumulation (no sort, no value-order dependence) --------
@@ -1164,32 +1071,9 @@ void launch_same_S(const int *qS, const int *nS_ptr, int *qS_prev, int *nS_prev,
 void launch_compact_S(const int *mark, const int *pos, int nf, int *qS, cudaStream_t st) {
     PDI_LAUNCH(k_compact_S, (nf + 255) / 256, 256, 0, st)(mark, pos, nf, qS);
 }
-void launch_grad_records(const int *ids, int n_all, int sh, unsigned long long *rec,
-                         cudaStream_t st) {
-    if (n_all > 0) PDI_LAUNCH(k_grad_records, (4 * n_all + 255) / 256, 256, 0, st)(ids, n_all, sh, rec);
-}
-void launch_grad_reduce(const unsigned long long *rec, int n, int sh, const double *grad,
-                        double4 *gs, cudaStream_t st) {
-    if (n > 0) PDI_LAUNCH(k_grad_reduce, (n + 255) / 256, 256, 0, st)(rec, n, sh, grad, gs);
-}
 void launch_grad_pullback(const double4 *g_el, const int *WTp, const int *WTr, const double *WTv,
                           const double4 *gs, int nf, double *G, cudaStream_t st) {
     PDI_LAUNCH(k_grad_pullback, (nf + 255) / 256, 256, 0, st)(g_el, WTp, WTr, WTv, gs, nf, G);
-}
-void launch_bc_count(const int *ids, int n_all, const int *Wp, const int *Wc, const int *v2q,
-                     int *cnt, cudaStream_t st) {
-    if (n_all > 0) PDI_LAUNCH(k_bc_count, (n_all + 255) / 256, 256, 0, st)(ids, n_all, Wp, Wc, v2q, cnt);
-}
-void launch_bc_records(const int *ids, int n_all, const int *Wp, const int *Wc, const int *v2q,
-                       const int *sidx, int nS, int sh, const int *off, unsigned long long *rec,
-                       cudaStream_t st) {
-    if (n_all > 0)
-        PDI_LAUNCH(k_bc_records, (n_all + 127) / 128, 128, 0, st)(ids, n_all, Wp, Wc, v2q, sidx, nS, sh, off, rec);
-}
-void launch_bc_reduce(const unsigned long long *rec, int n, int sh, int nS, const int *ids,
-                      const int *Wp, const double *Wv, const double *Hp, double *Bc, int ldb,
-                      cudaStream_t st) {
-    if (n > 0) PDI_LAUNCH(k_bc_reduce, (n + 255) / 256, 256, 0, st)(rec, n, sh, nS, ids, Wp, Wv, Hp, Bc, ldb);
 }
 void launch_zero_square(double *M, int ld, int n, cudaStream_t st) {
     if (n > 0) PDI_LAUNCH(k_zero_square, 256, 256, 0, st)(M, ld, n);

@@ -464,101 +464,6 @@ __global__ void __launch_bounds__(kTS_NT) k_backward_solve(BwdArgs A) {
     }
 }
 
-// y_S[a][i] = -sum_{r in reach(a)} V[r][a] w[r][i]: walk the supernode path from q_a's supernode
-__global__ void k_panel_yS(const int *__restrict__ qS, const int *__restrict__ nS_ptr,
-                           const int *__restrict__ col2sn, const int *__restrict__ sn_c0,
-                           const int *__restrict__ sn_parent, const double *__restrict__ V, int ldv,
-                           const double *__restrict__ G, double *__restrict__ yS) {
-    const int a = blockIdx.x;
-    if (a >= *nS_ptr) return;
-    double acc[3] = {0, 0, 0};
-    for (int s = col2sn[qS[a]]; s >= 0; s = sn_parent[s]) {
-        for (int r = sn_c0[s] + threadIdx.x; r < sn_c0[s + 1]; r += blockDim.x) {
-            double v = V[(size_t)r * ldv + a];
-            acc[0] += v * G[(size_t)r * 4 + 0];
-            acc[1] += v * G[(size_t)r * 4 + 1];
-            acc[2] += v * G[(size_t)r * 4 + 2];
-        }
-    }
-    __shared__ double sh[8];
-    for (int i = 0; i < 3; ++i) {
-        double t = block_sum<256>(acc[i], sh);
-        if (threadIdx.x == 0) yS[3 * a + i] = -t;
-    }
-}
-
-// Z[r][i] = w[r][i] + sum_{a active in sn(r)} V[r][a] t[a][i]
-__global__ void k_panel_correct(const int *__restrict__ col2sn, const int *__restrict__ lo,
-                                const int *__restrict__ hi, int nf, const double *__restrict__ V,
-                                int ldv, const double *__restrict__ G, const double *__restrict__ t,
-                                double *__restrict__ Z) {
-    int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= nf) return;
-    int s = col2sn[r];
-    double z0 = G[(size_t)r * 4 + 0], z1 = G[(size_t)r * 4 + 1], z2 = G[(size_t)r * 4 + 2];
-    for (int a = lo[s]; a < hi[s]; ++a) {
-        double v = V[(size_t)r * ldv + a];
-        z0 += v * t[3 * a + 0];
-        z1 += v * t[3 * a + 1];
-        z2 += v * t[3 * a + 2];
-    }
-    Z[(size_t)r * 4 + 0] = z0;
-    Z[(size_t)r * 4 + 1] = z1;
-    Z[(size_t)r * 4 + 2] = z2;
-    Z[(size_t)r * 4 + 3] = 0.0;
-}
-
-// K[a][b] = sum over rows r active for both a and b of V[r][a] V[r][b]  (SYRK on the panel;
-// K = (L_FF^{-1})_SS).  One CTA per 32x32 lower tile; deterministic.
-__global__ void __launch_bounds__(256) k_panel_syrk(const int *__restrict__ sn_c0,
-                                                    const int *__restrict__ lo,
-                                                    const int *__restrict__ hi, int nsn,
-                                                    const double *__restrict__ V, int ldv,
-                                                    const int *__restrict__ nS_ptr,
-                                                    double *__restrict__ K, int ldk) {
-    const int nS = *nS_ptr;
-    const int ti = blockIdx.x, tj = blockIdx.y;     // tile row, tile col
-    if (tj > ti || ti * 32 >= nS) return;
-    const int ia = ti * 32, ja = tj * 32;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 8 row groups of 4 rows
-    double acc[4] = {0, 0, 0, 0};
-    __shared__ double Va[32][33], Vb[32][33];
-    for (int s = 0; s < nsn; ++s) {
-        const int l = lo[s], h = hi[s];
-        if (h <= l || l >= min(ia + 32, nS) || h <= ia || l >= ja + 32 || h <= ja) continue;
-        const int c0 = sn_c0[s], c1 = sn_c0[s + 1];
-        for (int rb = c0; rb < c1; rb += 32) {
-            const int nrb = min(32, c1 - rb);
-            for (int e = threadIdx.x; e < 32 * 32; e += 256) {
-                int rr = e >> 5, cc = e & 31;
-                int ca = ia + cc, cb = ja + cc;
-                double va = 0, vb = 0;
-                if (rr < nrb) {
-                    if (ca >= l && ca < h && ca < nS) va = V[(size_t)(rb + rr) * ldv + ca];
-                    if (cb >= l && cb < h && cb < nS) vb = V[(size_t)(rb + rr) * ldv + cb];
-                }
-                Va[rr][cc] = va;
-                Vb[rr][cc] = vb;
-            }
-            __syncthreads();
-            for (int rr = 0; rr < nrb; ++rr) {
-                double b = Vb[rr][tx];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) acc[k] += Va[rr][ty * 4 + k] * b;
-            }
-            __syncthreads();
-        }
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        int a = ia + ty * 4 + k, b = ja + tx;
-        if (a < nS && b < nS && b <= a) {
-            K[(size_t)a * ldk + b] = acc[k];
-            K[(size_t)b * ldk + a] = acc[k];
-        }
-    }
-}
-
 // ------------------------------------------------------------------ host wrappers ---------
 constexpr int kFwdSmem = ((kTS_W + kSolveRB) * kXS + kSgRows * kSS) * (int)sizeof(double);
 
@@ -602,24 +507,7 @@ void launch_backward_solve(const DevFactor &F, int *done, int *cnt, int *ticket,
     PDI_LAUNCH(k_backward_solve, nsm, kTS_NT, kFwdSmem, st)(A);
 }
 
-void launch_panel_yS(const int *qS, const int *nS_ptr, int nS_host, const DevFactor &F,
-                     const double *V, int ldv, const double *G, double *yS, cudaStream_t st) {
-    if (nS_host > 0)
-        PDI_LAUNCH(k_panel_yS, nS_host, 256, 0, st)(qS, nS_ptr, F.col2sn, F.sn_c0, F.sn_parent, V,
-                                                    ldv, G, yS);
-}
 
-void launch_panel_correct(const DevFactor &F, const int *lo, const int *hi, const double *V,
-                          int ldv, const double *G, const double *t, double *Z, cudaStream_t st) {
-    PDI_LAUNCH(k_panel_correct, (F.nf + 255) / 256, 256, 0, st)(F.col2sn, lo, hi, F.nf, V, ldv, G,
-                                                                 t, Z);
-}
 
-void launch_panel_syrk(const DevFactor &F, const int *lo, const int *hi, const double *V, int ldv,
-                       const int *nS_ptr, int nS_host, double *K, int ldk, cudaStream_t st) {
-    if (nS_host <= 0) return;
-    int nt = (nS_host + 31) / 32;
-    PDI_LAUNCH(k_panel_syrk, dim3(nt, nt), 256, 0, st)(F.sn_c0, lo, hi, F.nsn, V, ldv, nS_ptr, K, ldk);
-}
 
 }  // namespace pdipc

@@ -54,12 +54,6 @@ void launch_forward_solve(const DevFactor &F, const int *lo, const int *hi, cons
                           cudaStream_t st);
 void launch_backward_solve(const DevFactor &F, int *done, int *cnt, int *ticket, double *P, double *Z,
                            int nsm, cudaStream_t st);
-void launch_panel_yS(const int *qS, const int *nS_ptr, int nS_host, const DevFactor &F,
-                     const double *V, int ldv, const double *G, double *yS, cudaStream_t st);
-void launch_panel_correct(const DevFactor &F, const int *lo, const int *hi, const double *V,
-                          int ldv, const double *G, const double *t, double *Z, cudaStream_t st);
-void launch_panel_syrk(const DevFactor &F, const int *lo, const int *hi, const double *V, int ldv,
-                       const int *nS_ptr, int nS_host, double *K, int ldk, cudaStream_t st);
 
 // ---- k_schur.cu (fused cooperative dense Schur step, a9)
 void schur_init(int device);
@@ -69,18 +63,6 @@ int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, 
                  double *t, double *Z, int *info, const int *same_S, unsigned long long *prof,
                  cudaStream_t st);
 void note_launch();
-
-// ---- k_dense.cu
-void dense_init();
-void dense_potrf(double *A, int ld, int m, double *T, int *info, cudaStream_t st);
-void dense_spd_inverse(double *A, int ld, int m, double *U, double *T, int *info, cudaStream_t st);
-void dense_negate(double *A, int ld, int m, cudaStream_t st);
-void launch_assemble_sigma_hat(const double *Sig, int lds, const double *Bc, int ldb, double *Sh,
-                               int ldh, int nS, cudaStream_t st);
-void launch_kron_matvec(const double *Sig, int lds, int nS, const double *x, double *y,
-                        cudaStream_t st);
-void launch_matvec(const double *M, int ldm, int n, const double *x, double *y, cudaStream_t st);
-void launch_chol_solve(const double *L, int ld, int n, const double *b, double *u, cudaStream_t st);
 
 // ---- k_contact.cu
 void contact_init();
@@ -126,20 +108,8 @@ void launch_mark_S(const int *ids, int n_all, const int *Wp, const int *Wc, cons
 void launch_compact_S(const int *mark, const int *pos, int nf, int *qS, cudaStream_t st);
 void launch_same_S(const int *qS, const int *nS_ptr, int *qS_prev, int *nS_prev, int *same, int cap,
                    bool enabled, cudaStream_t st);
-void launch_grad_records(const int *ids, int n_all, int sh, unsigned long long *rec,
-                         cudaStream_t st);
-void launch_grad_reduce(const unsigned long long *rec, int n, int sh, const double *grad,
-                        double4 *gs, cudaStream_t st);
 void launch_grad_pullback(const double4 *g_el, const int *WTp, const int *WTr, const double *WTv,
                           const double4 *gs, int nf, double *G, cudaStream_t st);
-void launch_bc_count(const int *ids, int n_all, const int *Wp, const int *Wc, const int *v2q,
-                     int *cnt, cudaStream_t st);
-void launch_bc_records(const int *ids, int n_all, const int *Wp, const int *Wc, const int *v2q,
-                       const int *sidx, int nS, int sh, const int *off, unsigned long long *rec,
-                       cudaStream_t st);
-void launch_bc_reduce(const unsigned long long *rec, int n, int sh, int nS, const int *ids,
-                      const int *Wp, const double *Wv, const double *Hp, double *Bc, int ldb,
-                      cudaStream_t st);
 void launch_zero_square(double *M, int ld, int n, cudaStream_t st);
 void launch_accd(const unsigned long long *keys, int n, int is_pt, int nB, const double4 *s,
                  const int *tris, const int *edges, int Nt, int Ne, const double4 *ds, double s_gap,

@@ -41,8 +41,12 @@ __device__ int block_exclusive_scan(int v, int *sh, int *total) {
     return base + x - v;
 }
 
-__global__ void __launch_bounds__(kScanNT) k_scan_partials(const int *in, int n, int *part) {
+// n_dev != nullptr: the length is *n_dev (clamped to n, the capacity the grid was sized for)
+__device__ __forceinline__ int scan_len(int n, const int *n_dev) { return n_dev ? min(*n_dev, n) : n; }
+
+__global__ void __launch_bounds__(kScanNT) k_scan_partials(const int *in, int n, const int *n_dev, int *part) {
     __shared__ int sh[32];
+    n = scan_len(n, n_dev);
     int base = blockIdx.x * kScanTile + threadIdx.x * kScanIPT;
     int s = 0;
 #pragma unroll
@@ -52,10 +56,11 @@ __global__ void __launch_bounds__(kScanNT) k_scan_partials(const int *in, int n,
     if (threadIdx.x == 0) part[blockIdx.x] = tot;
 }
 
-__global__ void __launch_bounds__(kScanNT) k_scan_tiles(const int *in, int n, int *out,
+__global__ void __launch_bounds__(kScanNT) k_scan_tiles(const int *in, int n, const int *n_dev, int *out,
                                                         const int *part, int nparts) {
     __shared__ int sh[32];
     __shared__ int off;
+    n = scan_len(n, n_dev);
     if (threadIdx.x == 0) {
         int o = 0;
         for (int b = 0; b < (int)blockIdx.x; ++b) o += part[b];   // nparts is small
@@ -74,10 +79,9 @@ __global__ void __launch_bounds__(kScanNT) k_scan_tiles(const int *in, int n, in
     int ex = block_exclusive_scan<kScanNT>(s, sh, &tot) + off;
 #pragma unroll
     for (int i = 0; i < kScanIPT; ++i) {
-        if (base + i < n) out[base + i] = ex;
+        if (base + i <= n) out[base + i] = ex;      // out[n] = total
         ex += v[i];
     }
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == kScanNT - 1) out[n] = ex;
     (void)nparts;
 }
 
@@ -86,12 +90,18 @@ void scan_exclusive(const int *in, int *out, int n, int *scratch, cudaStream_t s
         cudaMemsetAsync(out, 0, sizeof(int), st);
         return;
     }
-    int nb = (n + kScanTile - 1) / kScanTile;
-    PDI_LAUNCH(k_scan_partials, nb, kScanNT, 0, st)(in, n, scratch);
-    PDI_LAUNCH(k_scan_tiles, nb, kScanNT, 0, st)(in, n, out, scratch, nb);
+    int nb = n / kScanTile + 1;                      // covers index n (the total)
+    PDI_LAUNCH(k_scan_partials, nb, kScanNT, 0, st)(in, n, nullptr, scratch);
+    PDI_LAUNCH(k_scan_tiles, nb, kScanNT, 0, st)(in, n, nullptr, out, scratch, nb);
 }
 
-int scan_scratch_ints(int n) { return (n + kScanTile - 1) / kScanTile + 1; }
+void scan_exclusive_dev(const int *in, int *out, const int *n_dev, int cap, int *scratch, cudaStream_t st) {
+    int nb = cap / kScanTile + 1;
+    PDI_LAUNCH(k_scan_partials, nb, kScanNT, 0, st)(in, cap, n_dev, scratch);
+    PDI_LAUNCH(k_scan_tiles, nb, kScanNT, 0, st)(in, cap, n_dev, out, scratch, nb);
+}
+
+int scan_scratch_ints(int n) { return n / kScanTile + 2; }
 
 // ----------------------------------------------------------------------- radix sort -------
 constexpr int kRsNT = 256, kRsIPT = 16, kRsTile = kRsNT * kRsIPT, kRsWarps = kRsNT / 32;

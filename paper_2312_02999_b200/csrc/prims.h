@@ -5,6 +5,8 @@
 namespace pdipc {
 // out[0..n] : exclusive scan of in[0..n), out[n] = total.  scratch: scan_scratch_ints(n).
 void scan_exclusive(const int *in, int *out, int n, int *scratch, cudaStream_t st);
+// same with the length read on the device (*n_dev, at most cap; grid sized for cap)
+void scan_exclusive_dev(const int *in, int *out, const int *n_dev, int cap, int *scratch, cudaStream_t st);
 int scan_scratch_ints(int n);
 // ascending LSD radix sort of the low `bits` bits; tmp: n keys; scratch: radix_scratch_ints(n)
 void radix_sort_u64(uint64_t *keys, uint64_t *tmp, int n, int bits, int *scratch,
