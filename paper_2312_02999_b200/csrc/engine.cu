@@ -172,8 +172,9 @@ struct pd_ipc {
     DBuf<int> flag, pos, ctype, atype, ids, iscr;
     DBuf<double> cd2, ad2, grad, Hp, dist;
     DBuf<int> mark, spos, qS;
-    DBuf<unsigned long long> rec, rec_tmp;
-    DBuf<int> bccnt, bcoff;
+    DBuf<double> lspart;    // line-search partial sums [8][ls_blocks()]
+    bool force_sort = false;  // next broad phases take the sort path (after a hash overflow)
+    int nS_host = 0;
     DBuf<int> ts_lo, ts_hi, ts_cnt, ts_ptr, ts_rem, ts_done, ticket;
     DBuf<double> V, K, Bc, Sh, U, Tt, yS, rhs, u, tv, part, b0, Lstore;
     DBuf<double> dscal;     // [0]=ext cell, [1]=amin, [2..4]=ls, [5..8]=ls_out, [9..10]=scal,
@@ -204,75 +205,153 @@ static void sync_read_ints(pd_ipc *h, int *dst, const int *src, int k) {
 // device scalar <- v, stream-ordered, no host staging (a pageable H2D copy would block)
 static void set_d(pd_ipc *h, double *dptr, double v) { launch_set_double(dptr, v, h->st); }
 
-static void broad_phase_sort(pd_ipc *h, const double4 *ds, double infl, int *npt_out, int *nee_out);
+static void ensure_pair_buffers(pd_ipc *h, size_t ncand) {
+    h->flag.ensure(ncand + 1);
+    h->pos.ensure(ncand + 1);
+    h->ctype.ensure(ncand + 1);
+    h->cd2.ensure(ncand + 1);
+    h->iscr.ensure(std::max(radix_scratch_ints((int)ncand + 1), scan_scratch_ints((int)ncand + 1)) + 1024);
+}
+
+// grow every candidate-capacity buffer to at least n keys (rare; synchronising)
+static void grow_candidates(pd_ipc *h, size_t n) {
+    if (n <= h->cand.n) return;
+    h->cand.exact(n);
+    h->cand_tmp.exact(n);
+    ensure_pair_buffers(h, n);
+    h->akeys.exact(n + 1);
+    h->atype.exact(n + 1);
+    h->ad2.exact(n + 1);
+    h->grad.exact(12 * n + 12);
+    h->Hp.exact(78 * n + 78);
+    h->dist.exact(n + 1);
+    h->ids.exact(4 * n + 4);
+    h->b0.exact(n + 1);
+}
+
+// parity / debugging copies of the last iteration (PD_IPC set_debug)
+static void debug_capture(pd_ipc *h, Seq &q, int n_pt, int n_ee, int nS) {
+    const int nf = h->nf;
+    std::vector<double> G4(4 * (size_t)nf), g4(4 * (size_t)nf);
+    CK(cudaMemcpy(G4.data(), h->G.p, sizeof(double) * 4 * nf, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(g4.data(), h->g_el.p, sizeof(double) * 4 * nf, cudaMemcpyDeviceToHost));
+    q.ghat.assign(3 * (size_t)h->n, 0.0);
+    q.gel.assign(3 * (size_t)h->n, 0.0);
+    for (int k = 0; k < nf; ++k)
+        for (int a = 0; a < 3; ++a) {
+            q.ghat[3 * (size_t)h->hm.q2v[k] + a] = G4[4 * (size_t)k + a];
+            q.gel[3 * (size_t)h->hm.q2v[k] + a] = g4[4 * (size_t)k + a];
+        }
+    const int na = n_pt + n_ee;
+    std::vector<unsigned long long> ak(na);
+    if (na) CK(cudaMemcpy(ak.data(), h->akeys.p, sizeof(unsigned long long) * na, cudaMemcpyDeviceToHost));
+    q.pt.clear();
+    q.ee.clear();
+    for (int k = 0; k < na; ++k) {
+        const unsigned long long nb = k < n_pt ? (unsigned long long)h->Nt : (unsigned long long)h->Ne;
+        auto &v = k < n_pt ? q.pt : q.ee;
+        v.push_back((int32_t)(ak[k] / nb));
+        v.push_back((int32_t)(ak[k] % nb));
+    }
+    std::vector<int> qs(nS);
+    if (nS) CK(cudaMemcpy(qs.data(), h->qS.p, sizeof(int) * nS, cudaMemcpyDeviceToHost));
+    q.S.clear();
+    for (int v : qs) q.S.push_back(h->hm.q2v[v]);
+    std::sort(q.S.begin(), q.S.end());
+    std::vector<double4> d4(h->n);
+    CK(cudaMemcpy(d4.data(), h->dx.p, sizeof(double4) * h->n, cudaMemcpyDeviceToHost));
+    q.dx.resize(3 * (size_t)h->n);
+    for (int v = 0; v < h->n; ++v) {
+        q.dx[3 * v] = d4[v].x;
+        q.dx[3 * v + 1] = d4[v].y;
+        q.dx[3 * v + 2] = d4[v].z;
+    }
+}
+
+// debugging aid (PDIPC_TRACE): per-item forward-solve timestamps and Schur phase timestamps
+static void dump_traces(pd_ipc *h, int nS) {
+    if (!h->trace_file || nS <= 0 || std::ftell(h->trace_file) >= (30l << 20)) return;
+    int nitems;
+    CK(cudaMemcpy(&nitems, h->ts_ptr.p + h->F.nsn, sizeof(int), cudaMemcpyDeviceToHost));
+    std::vector<unsigned long long> tr(4 * (size_t)nitems);
+    CK(cudaMemcpy(tr.data(), h->trace.p, tr.size() * 8, cudaMemcpyDeviceToHost));
+    fwrite(&nitems, sizeof(int), 1, h->trace_file);
+    fwrite(tr.data(), 8, tr.size(), h->trace_file);
+    fflush(h->trace_file);
+    if (h->schur_file) {
+        std::vector<unsigned long long> pr(1024);
+        CK(cudaMemcpy(pr.data(), h->sprof.p, 1024 * 8, cudaMemcpyDeviceToHost));
+        fwrite(&nS, sizeof(int), 1, h->schur_file);
+        fwrite(pr.data(), 8, 1024, h->schur_file);
+        fflush(h->schur_file);
+    }
+}
+
+// Device int slots (h->dint, 32 ints).  Every count the iteration needs stays on the device; the
+// host reads them once, at the end of the iteration.
+enum : int {
+    D_ACNT = 0,      // [0] n_pt, [1] n_all active pairs
+    D_CCNT = 2,      // [2] npt, [3] ntot candidates of the current broad phase
+    D_INFO = 4,      // Cholesky info
+    D_CAP = 5,       // capacity bits: 1 candidate buffer, 2 |S| > capS, 4 panel update rows
+    D_HOVF = 6,      // [6] static, [7] swept hash overflow (outlier box / table) -> sort path
+    D_SPREV = 8,     // [8] |S| of the S that V_s, K_s, Sigma_s belong to, [9] same-S flag
+    D_STAT = 10,     // [10] npt, [11] ntot of the static phase (stats)
+    D_SORT = 16,     // [16..17] scratch counters of the sort path
+};
+
+static void broad_phase_sort(pd_ipc *h, const double4 *ds, double infl, int *ccnt);
 
 // Broad phase: static (ds == nullptr, boxes inflated by infl) or swept.  Produces sorted unique
-// PT keys in cand[0..npt) and EE keys in cand[npt..npt+nee).  Sort-free: every query sorts its
-// own (short) partner list, so the lists come out globally sorted; one host read of the sizes.
+// PT keys in cand[0..npt) and EE keys in cand[npt..ntot) with ccnt = [npt, ntot] on the device,
+// no host round trip.  Sort-free: every query sorts its own (short) partner list, so the lists
+// come out globally sorted.  A table overflow raises *hovf; the iteration is then redone with
+// the sort path.
 // Hash cell = min(max box extent, kCellCap * cell0): one long swept box must not coarsen the grid
 // for every query; boxes wider than the cap span several cells (bounded, see k_hash_insert).
 constexpr double kCellCap = 2.0;
 
-static void broad_phase(pd_ipc *h, const double4 *ds, double infl, int *npt_out, int *nee_out) {
+static void broad_phase(pd_ipc *h, const double4 *ds, double infl, int *ccnt, int *hovf) {
+    if (h->force_sort) {
+        broad_phase_sort(h, ds, infl, ccnt);
+        return;
+    }
     cudaStream_t st = h->st;
     const int Ns = h->Ns, Nt = h->Nt, Ne = h->Ne;
-    const int nbox = Ns + Nt + Ne;
-    h->blo.ensure(nbox);
-    h->bhi.ensure(nbox);
     double *ext = h->dscal.p + 14;   // cell = [max box extent, cap]
     set_d(h, ext, h->cell0);
     set_d(h, ext + 1, kCellCap * h->cell0);
     launch_boxes(h->s.p, ds, h->tris.p, h->edges.p, Ns, Nt, Ne, infl, h->blo.p, h->bhi.p, ext, st);
     const unsigned M = h->hmask + 1;
     const int nq = Ns + Ne, cap_ent = (int)h->hent.n;
-    h->qcnt.ensure((size_t)nq + 1);
-    h->qoff.ensure((size_t)nq + 1);
-    h->qlist.ensure((size_t)nq * hash_query_cap());
-    int *ovf = h->dint.p + 6;
-    CK(cudaMemsetAsync(ovf, 0, sizeof(int), st));
+    CK(cudaMemsetAsync(hovf, 0, sizeof(int), st));
     // both tables (tris, edges) in one pass each: count, scan, fill
     CK(cudaMemsetAsync(h->hcnt.p, 0, sizeof(int) * 2 * (M + 1), st));
-    launch_hash_insert(h->blo.p, h->bhi.p, Ns, Nt, Ne, ext, h->hmask, h->hcnt.p, nullptr, nullptr, 0, ovf, st);
+    launch_hash_insert(h->blo.p, h->bhi.p, Ns, Nt, Ne, ext, h->hmask, h->hcnt.p, nullptr, nullptr, 0, hovf, st);
     scan_exclusive(h->hcnt.p, h->hstart.p, (int)(2 * (M + 1)), h->iscr.p, st);
     CK(cudaMemsetAsync(h->hcnt.p, 0, sizeof(int) * 2 * (M + 1), st));
     launch_hash_insert(h->blo.p, h->bhi.p, Ns, Nt, Ne, ext, h->hmask, h->hcnt.p, h->hstart.p, h->hent.p,
-                       cap_ent, ovf, st);
+                       cap_ent, hovf, st);
     // one warp per query (PT points, then EE edges): sorted unique partner lists
     launch_hash_query_warp(h->blo.p, h->bhi.p, Ns, Nt, Ne, ext, h->hmask, h->hstart.p, h->hent.p, h->tris.p,
-                           h->edges.p, h->qcnt.p, h->qlist.p, ovf, st);
+                           h->edges.p, h->qcnt.p, h->qlist.p, hovf, st);
     scan_exclusive(h->qcnt.p, h->qoff.p, nq, h->iscr.p, st);
-    CK(cudaMemcpyAsync(h->dint.p + 2, h->qoff.p + Ns, sizeof(int), cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemcpyAsync(h->dint.p + 3, h->qoff.p + nq, sizeof(int), cudaMemcpyDeviceToDevice, st));
-    int res[5];
-    sync_read_ints(h, res, h->dint.p + 2, 5);   // [2] npt, [3] npt + nee, [6] overflow
-    if (res[4]) {                               // outlier box or table overflow: sort path
-        broad_phase_sort(h, ds, infl, npt_out, nee_out);
-        return;
-    }
-    res[1] -= res[0];
-    const size_t need = (size_t)res[0] + res[1] + 1;
-    if (h->cand.n < need) {
-        h->cand.exact(2 * need);
-        h->cand_tmp.exact(2 * need);
-    }
-    launch_hash_emit(Ns, Nt, Ne, h->qcnt.p, h->qoff.p, h->qlist.p, h->cand.p, st);
-    *npt_out = res[0];
-    *nee_out = res[1];
+    launch_hash_emit(Ns, Nt, Ne, h->qcnt.p, h->qoff.p, h->qlist.p, h->cand.p, (int)h->cand.n, ccnt,
+                     h->dint.p + D_CAP, st);
 }
 
-static void broad_phase_sort(pd_ipc *h, const double4 *ds, double infl, int *npt_out, int *nee_out) {
+// Fallback after a hash overflow: uncapped cells (every box covers at most 8 of them), global
+// radix sort + unique.  Host-synchronous (rare path).
+static void broad_phase_sort(pd_ipc *h, const double4 *ds, double infl, int *ccnt) {
     cudaStream_t st = h->st;
     const int Ns = h->Ns, Nt = h->Nt, Ne = h->Ne;
-    const int nbox = Ns + Nt + Ne;
-    h->blo.ensure(nbox);
-    h->bhi.ensure(nbox);
-    double *ext = h->dscal.p + 14;   // uncapped cell: every box covers at most 8 cells
+    double *ext = h->dscal.p + 14;
     set_d(h, ext, h->cell0);
     set_d(h, ext + 1, 1e300);
     launch_boxes(h->s.p, ds, h->tris.p, h->edges.p, Ns, Nt, Ne, infl, h->blo.p, h->bhi.p, ext, st);
     const unsigned M = h->hmask + 1;
-    int *cnt_pt = h->dint.p + 0, *cnt_ee = h->dint.p + 1;
-    int *ovf = h->dint.p + 7;   // cannot trip here: uncapped cells bound entries by 8 per box
+    int *cnt_pt = h->dint.p + D_SORT, *cnt_ee = h->dint.p + D_SORT + 1;
+    int *ovf = h->dint.p + D_SORT + 2;   // cannot trip: uncapped cells bound entries by 8 per box
     CK(cudaMemsetAsync(ovf, 0, sizeof(int), st));
     CK(cudaMemsetAsync(h->hcnt.p, 0, sizeof(int) * 2 * (M + 1), st));
     launch_hash_insert(h->blo.p, h->bhi.p, Ns, Nt, Ne, ext, h->hmask, h->hcnt.p, nullptr, nullptr, 0, ovf, st);
@@ -282,19 +361,18 @@ static void broad_phase_sort(pd_ipc *h, const double4 *ds, double infl, int *npt
                        (int)h->hent.n, ovf, st);
     for (int pass = 0; pass < 2; ++pass) {
         int counts[2];
+        const int cap = (int)(h->cand.n / 2);
         for (int kind = 0; kind < 2; ++kind) {   // 0 = PT (B = tris), 1 = EE (B = edges)
             const int b0 = kind == 0 ? Ns : Ns + Nt;
             const int a0 = kind == 0 ? 0 : Ns + Nt, na = kind == 0 ? Ns : Ne;
             const int *hs = h->hstart.p + (size_t)kind * (M + 1), *he = h->hent.p;
             int *cnt = kind == 0 ? cnt_pt : cnt_ee;
             CK(cudaMemsetAsync(cnt, 0, sizeof(int), st));
-            const int cap = (int)(h->cand.n / 2);
             unsigned long long *out = h->cand.p + (size_t)kind * cap;
             launch_hash_query(h->blo.p, h->bhi.p, a0, na, b0, kind == 0 ? Nt : Ne, ext, h->hmask, hs,
                               he, kind == 0, h->tris.p, h->edges.p, out, cnt, cap, st);
         }
-        sync_read_ints(h, counts, h->dint.p, 2);
-        const int cap = (int)(h->cand.n / 2);
+        sync_read_ints(h, counts, cnt_pt, 2);
         if (counts[0] <= cap && counts[1] <= cap) {
             // sort + unique each list, then pack PT | EE contiguously in cand_tmp -> cand
             int res[2];
@@ -302,7 +380,6 @@ static void broad_phase_sort(pd_ipc *h, const double4 *ds, double infl, int *npt
                 unsigned long long *keys = h->cand.p + (size_t)kind * cap;
                 int nk = counts[kind];
                 unsigned long long range = kind == 0 ? (unsigned long long)Ns * Nt : (unsigned long long)Ne * Ne;
-                h->cand_tmp.ensure(2 * (size_t)cap);
                 // sort scratch = this kind's half of cand_tmp (the PT result lives in the other)
                 radix_sort_u64(reinterpret_cast<uint64_t *>(keys),
                                reinterpret_cast<uint64_t *>(h->cand_tmp.p + (size_t)kind * cap), nk,
@@ -310,41 +387,35 @@ static void broad_phase_sort(pd_ipc *h, const double4 *ds, double infl, int *npt
                 unique_sorted_u64(reinterpret_cast<uint64_t *>(keys), nk,
                                   reinterpret_cast<uint64_t *>(h->cand_tmp.p + (size_t)kind * cap), h->flag.p,
                                   h->pos.p, h->iscr.p, st);
-                CK(cudaMemcpyAsync(h->dint.p + 2 + kind, h->pos.p + nk, sizeof(int), cudaMemcpyDeviceToDevice, st));
+                CK(cudaMemcpyAsync(cnt_pt + kind, h->pos.p + nk, sizeof(int), cudaMemcpyDeviceToDevice, st));
             }
-            sync_read_ints(h, res, h->dint.p + 2, 2);
+            sync_read_ints(h, res, cnt_pt, 2);
             CK(cudaMemcpyAsync(h->cand.p, h->cand_tmp.p, sizeof(unsigned long long) * res[0],
                                cudaMemcpyDeviceToDevice, st));
             CK(cudaMemcpyAsync(h->cand.p + res[0], h->cand_tmp.p + cap, sizeof(unsigned long long) * res[1],
                                cudaMemcpyDeviceToDevice, st));
-            *npt_out = res[0];
-            *nee_out = res[1];
+            const int cc[2] = {res[0], res[0] + res[1]};
+            CK(cudaMemcpyAsync(ccnt, cc, sizeof(cc), cudaMemcpyHostToDevice, st));
+            CK(cudaStreamSynchronize(st));   // cc is a host stack array
             return;
         }
-        // grow and redo
-        size_t need = 2 * (size_t)std::max(counts[0], counts[1]) + 1024;
-        h->cand.exact(2 * need);
-        h->cand_tmp.exact(2 * need);
-        h->flag.exact(2 * need + 1);
-        h->pos.exact(2 * need + 1);
-        h->iscr.exact(std::max(radix_scratch_ints((int)(2 * need)), scan_scratch_ints((int)(2 * need))) + 1024);
+        grow_candidates(h, 2 * (size_t)std::max(counts[0], counts[1]) + 1024);
     }
     throw CudaError("broad phase capacity", PD_IPC_E_CAPACITY);
 }
 
-static void ensure_pair_buffers(pd_ipc *h, size_t ncand) {
-    h->flag.ensure(ncand + 1);
-    h->pos.ensure(ncand + 1);
-    h->ctype.ensure(ncand + 1);
-    h->cd2.ensure(ncand + 1);
-    h->iscr.ensure(std::max(radix_scratch_ints((int)ncand + 1), scan_scratch_ints((int)ncand + 1)) + 1024);
-}
-
-// One PD+IPC iteration of sequence q.  Returns 0 or an error code.
-static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
+// One PD+IPC iteration of sequence q.  No host round trip until the end: counts live on the
+// device and every launch is sized by a capacity.  Returns false if a capacity or hash overflow
+// was flagged: x was not updated, the caller redoes the iteration after the buffers were grown
+// (or with the sort broad phase).
+static bool iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
     cudaStream_t st = h->st;
     const int T = h->T, nf = h->nf, Ns = h->Ns, Nt = h->Nt, Ne = h->Ne;
+    const int cap = (int)h->cand.n;
     auto &ev = h->tm.ev;
+    int *acnt = h->dint.p + D_ACNT, *ccnt = h->dint.p + D_CCNT;
+    CK(cudaMemsetAsync(h->dint.p + D_INFO, 0, 4 * sizeof(int), st));   // info, capacity, hash flags
+    CK(cudaMemsetAsync(acnt, 0, 2 * sizeof(int), st));
     CK(cudaEventRecord(ev[0], st));
     // ---------------- Misc: a1 local step + a2 gather
     KTimer &kt = h->kt;
@@ -357,156 +428,82 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
     kt.stop(K_GATHER, st);
     CK(cudaEventRecord(ev[1], st));
     // ---------------- IPC
-    int n_pt = 0, n_ee = 0, nS = 0, n_cand = 0;
-    double min_dist = 0.0;
     int *nS_dev = h->spos.p + nf;     // exclusive scan total of the S marks
+    double *dmax = h->dscal.p + 11;
     if (Nt > 0) {
         kt.start(K_BROAD, st);
         launch_surface(h->Wp.p, h->Wc.p, h->Wv.p, q.x.p, Ns, h->s.p, st);
-        int cpt, cee;
-        broad_phase(h, nullptr, 0.5 * h->dh * 1.01, &cpt, &cee);
+        broad_phase(h, nullptr, 0.5 * h->dh * 1.01, ccnt, h->dint.p + D_HOVF);
+        CK(cudaMemcpyAsync(h->dint.p + D_STAT, ccnt, 2 * sizeof(int), cudaMemcpyDeviceToDevice, st));
         kt.stop(K_BROAD, st);
-        n_cand = cpt + cee;
-        ensure_pair_buffers(h, n_cand);
         kt.start(K_NARROW, st);
-        launch_narrow(h->cand.p, cpt, 1, Nt, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->dh2, h->flag.p,
+        // one pass over [PT | EE] candidates; one scan; actives come out as [PT | EE], each sorted
+        launch_narrow(h->cand.p, ccnt, cap, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->dh2, h->flag.p,
                       h->ctype.p, h->cd2.p, st);
-        launch_narrow(h->cand.p + cpt, cee, 0, Ne, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->dh2,
-                      h->flag.p + cpt, h->ctype.p + cpt, h->cd2.p + cpt, st);
-        // one scan over [PT flags | EE flags]: actives come out as [PT | EE], each sorted
-        h->akeys.ensure(n_cand + 1);
-        h->atype.ensure(n_cand + 1);
-        h->ad2.ensure(n_cand + 1);
-        scan_exclusive(h->flag.p, h->pos.p, n_cand, h->iscr.p, st);
-        launch_compact_active(h->cand.p, n_cand, h->flag.p, h->pos.p, h->ctype.p, h->cd2.p, 0, h->akeys.p,
-                              h->atype.p, h->ad2.p, st);
-        CK(cudaMemcpyAsync(h->dint.p + 0, h->pos.p + cpt, sizeof(int), cudaMemcpyDeviceToDevice, st));
-        CK(cudaMemcpyAsync(h->dint.p + 1, h->pos.p + n_cand, sizeof(int), cudaMemcpyDeviceToDevice, st));
-        int cnts[2];
-        sync_read_ints(h, cnts, h->dint.p, 2);
-        n_pt = cnts[0];
-        n_ee = cnts[1] - cnts[0];
-        const int na = n_pt + n_ee;
-        h->grad.ensure(12 * (size_t)na + 12);
-        h->Hp.ensure(78 * (size_t)na + 78);
-        h->dist.ensure(na + 1);
-        h->ids.ensure(4 * (size_t)na + 4);
+        scan_exclusive_dev(h->flag.p, h->pos.p, ccnt + 1, cap, h->iscr.p, st);
+        launch_compact_active(h->cand.p, ccnt, cap, h->flag.p, h->pos.p, h->ctype.p, h->cd2.p, h->akeys.p,
+                              h->atype.p, h->ad2.p, acnt, st);
         kt.stop(K_NARROW, st);
         kt.start(K_DERIV, st);
-        double *dmax = h->dscal.p + 11;
         set_d(h, dmax, 0.0);
         set_d(h, dmax + 1, 1e300);
-        launch_pair_derivs(h->akeys.p, h->atype.p, h->ad2.p, n_pt, na, h->s.p, h->tris.p, h->edges.p, Nt,
+        launch_pair_derivs(h->akeys.p, h->atype.p, h->ad2.p, acnt, cap, h->s.p, h->tris.p, h->edges.p, Nt,
                            Ne, h->dh, h->kappa, h->grad.p, h->Hp.p, h->dist.p, h->ids.p, dmax, st);
         kt.stop(K_DERIV, st);
         kt.start(K_ASSEMBLY, st);
         // S
         CK(cudaMemsetAsync(h->mark.p, 0, sizeof(int) * nf, st));
-        launch_mark_S(h->ids.p, na, h->Wp.p, h->Wc.p, h->v2q.p, h->mark.p, st);
+        launch_mark_S(h->ids.p, acnt, cap, h->Wp.p, h->Wc.p, h->v2q.p, h->mark.p, st);
         scan_exclusive(h->mark.p, h->spos.p, nf, h->iscr.p, st);
         launch_compact_S(h->mark.p, h->spos.p, nf, h->qS.p, st);
         // V_s, K_s, Sigma_s depend on S (and the constant factor) only: reuse them while S is
-        // bit-identical to the S they were computed for (dint[8] = its size, dint[9] = flag)
-        launch_same_S(h->qS.p, nS_dev, h->qS_prev.p, h->dint.p + 8, h->dint.p + 9, h->capS,
-                      h->opt.no_sigma_reuse == 0, st);
+        // bit-identical to the S they were computed for
+        launch_same_S(h->qS.p, nS_dev, h->qS_prev.p, h->dint.p + D_SPREV, h->dint.p + D_SPREV + 1, h->capS,
+                      h->opt.no_sigma_reuse == 0, h->dint.p + D_CAP, st);
         // gradient pull-back: deterministic fixed-point accumulation on the surface, then W^T
-        h->gsq.ensure(6 * (size_t)Ns + 6);
         CK(cudaMemsetAsync(h->gsq.p, 0, sizeof(long long) * 6 * Ns, st));
-        launch_accum_grad_fx(h->ids.p, na, h->grad.p, dmax, h->gsq.p, st);
-        launch_grad_pullback_fx(h->g_el.p, h->WTp.p, h->WTr.p, h->WTv.p, h->gsq.p, dmax, na, nf, h->G.p, st);
-        sync_read_ints(h, &nS, nS_dev, 1);
-        if (nS > h->capS) throw CudaError("contact vertex set exceeds capacity", PD_IPC_E_CAPACITY);
-        // B-check: fixed-point accumulation into the dense 3nS x 3nS block, then to double
-        if (nS > 0) {
-            const int ldb = 3 * h->capS;
-            // low words of the fixed-point sums live in the (not yet used) Sigma-hat buffer
-            long long *Bl = reinterpret_cast<long long *>(h->Sh.p);
-            launch_zero_square(h->Bc.p, ldb, 3 * nS, st);
-            launch_zero_square(h->Sh.p, ldb, 3 * nS, st);
-            launch_accum_bc_fx(h->ids.p, na, h->Wp.p, h->Wc.p, h->Wv.p, h->v2q.p, h->spos.p, h->Hp.p, dmax,
-                               reinterpret_cast<long long *>(h->Bc.p), Bl, ldb, st);
-            launch_fx_to_double(reinterpret_cast<long long *>(h->Bc.p), Bl, ldb, 3 * nS, dmax, na, st);
-        }
+        launch_accum_grad_fx(h->ids.p, acnt, cap, h->grad.p, dmax, h->gsq.p, st);
+        launch_grad_pullback_fx(h->g_el.p, h->WTp.p, h->WTr.p, h->WTv.p, h->gsq.p, dmax, acnt, nf, h->G.p, st);
+        // B-check: fixed-point accumulation into the dense 3|S| x 3|S| block, then to double; the
+        // low words of the fixed-point sums live in the (not yet used) Sigma-hat buffer
+        const int ldb = 3 * h->capS;
+        long long *Bl = reinterpret_cast<long long *>(h->Sh.p);
+        launch_zero_square(h->Bc.p, ldb, nS_dev, h->capS, st);
+        launch_zero_square(h->Sh.p, ldb, nS_dev, h->capS, st);
+        launch_accum_bc_fx(h->ids.p, acnt, cap, h->Wp.p, h->Wc.p, h->Wv.p, h->v2q.p, h->spos.p, h->Hp.p, dmax,
+                           reinterpret_cast<long long *>(h->Bc.p), Bl, ldb, st);
+        launch_fx_to_double(reinterpret_cast<long long *>(h->Bc.p), Bl, ldb, nS_dev, h->capS, dmax, acnt, st);
         kt.stop(K_ASSEMBLY, st);
     } else {
         CK(cudaMemsetAsync(nS_dev, 0, sizeof(int), st));
-        CK(cudaMemsetAsync(h->dint.p + 9, 0, sizeof(int), st));
+        CK(cudaMemsetAsync(h->dint.p + D_SPREV + 1, 0, sizeof(int), st));
+        CK(cudaMemsetAsync(h->dint.p + D_STAT, 0, 2 * sizeof(int), st));
         launch_grad_pullback(h->g_el.p, h->WTp.p, h->WTr.p, h->WTv.p, nullptr, nf, h->G.p, st);
-    }
-    if (h->debug) {
-        std::vector<double> G4(4 * (size_t)nf), g4(4 * (size_t)nf);
-        CK(cudaMemcpyAsync(G4.data(), h->G.p, sizeof(double) * 4 * nf, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(g4.data(), h->g_el.p, sizeof(double) * 4 * nf, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        q.ghat.assign(3 * (size_t)h->n, 0.0);
-        q.gel.assign(3 * (size_t)h->n, 0.0);
-        for (int k = 0; k < nf; ++k)
-            for (int a = 0; a < 3; ++a) {
-                q.ghat[3 * (size_t)h->hm.q2v[k] + a] = G4[4 * (size_t)k + a];
-                q.gel[3 * (size_t)h->hm.q2v[k] + a] = g4[4 * (size_t)k + a];
-            }
-        int na = n_pt + n_ee;
-        std::vector<unsigned long long> ak(na);
-        if (na) CK(cudaMemcpy(ak.data(), h->akeys.p, sizeof(unsigned long long) * na, cudaMemcpyDeviceToHost));
-        q.pt.clear();
-        q.ee.clear();
-        for (int k = 0; k < na; ++k) {
-            unsigned long long nb = k < n_pt ? (unsigned long long)Nt : (unsigned long long)Ne;
-            auto &v = k < n_pt ? q.pt : q.ee;
-            v.push_back((int32_t)(ak[k] / nb));
-            v.push_back((int32_t)(ak[k] % nb));
-        }
-        std::vector<int> qs(nS);
-        if (nS) CK(cudaMemcpy(qs.data(), h->qS.p, sizeof(int) * nS, cudaMemcpyDeviceToHost));
-        q.S.clear();
-        for (int v : qs) q.S.push_back(h->hm.q2v[v]);
-        std::sort(q.S.begin(), q.S.end());
     }
     CK(cudaEventRecord(ev[2], st));
     // ---------------- G-Step
     const DevFactor &F = h->F;
     CK(cudaMemsetAsync(h->ticket.p, 0, 2 * sizeof(int), st));
-    CK(cudaMemsetAsync(h->dint.p + 4, 0, sizeof(int), st));   // Cholesky info of this iteration
     kt.start(K_FWD, st);
-    launch_ts_items(F, h->qS.p, nS_dev, h->dint.p + 9, h->ts_lo.p, h->ts_hi.p, h->ts_cnt.p, h->ts_rem.p, st);
+    launch_ts_items(F, h->qS.p, nS_dev, h->capS, h->dint.p + D_SPREV + 1, (long long)h->Up.n,
+                    h->dint.p + D_CAP, h->ts_lo.p, h->ts_hi.p, h->ts_cnt.p, h->ts_rem.p, st);
     scan_exclusive(h->ts_cnt.p, h->ts_ptr.p, F.nsn, h->iscr.p, st);
-    const int ldu = std::max(32, ((nS + 31) / 32) * 32);
-    if (nS > 0) h->Up.ensure((size_t)std::max(1, F.nU) * ldu);
     if (h->trace_file) h->trace.ensure(4 * (size_t)F.bw_nblocks * (2 + (h->capS + 31) / 32));
     launch_forward_solve(F, h->ts_lo.p, h->ts_hi.p, h->ts_ptr.p, h->qS.p, h->ts_rem.p, h->ticket.p, h->G.p,
-                         h->Yw.p, h->V.p, h->ldv, h->Ug.p, nS > 0 ? h->Up.p : nullptr, ldu, h->nsm,
+                         h->Yw.p, h->V.p, h->ldv, h->Ug.p, h->Up.p, nS_dev, h->capS, h->nsm,
                          h->trace_file ? h->trace.p : nullptr, st);
-    if (h->trace_file && nS > 0 && std::ftell(h->trace_file) < (30l << 20)) {
-        int nitems;
-        sync_read_ints(h, &nitems, h->ts_ptr.p + F.nsn, 1);
-        std::vector<unsigned long long> tr(4 * (size_t)nitems);
-        CK(cudaMemcpy(tr.data(), h->trace.p, tr.size() * 8, cudaMemcpyDeviceToHost));
-        fwrite(&nitems, sizeof(int), 1, h->trace_file);
-        fwrite(tr.data(), 8, tr.size(), h->trace_file);
-        fflush(h->trace_file);
-    }
     kt.stop(K_FWD, st);
     kt.start(K_DENSE, st);
-    if (nS > 0) {
-        const int ldk = h->capS, m3 = 3 * nS, ldb = 3 * h->capS;
-        int *info = h->dint.p + 4;
-        (void)m3;
+    if (Nt > 0) {
         if (h->trace_file) {
             h->sprof.ensure(1024);
             CK(cudaMemsetAsync(h->sprof.p, 0, 1024 * 8, st));
         }
-        CK((cudaError_t)launch_schur(F, h->V.p, h->ldv, h->Yw.p, h->qS.p, h->ts_lo.p, h->ts_hi.p, nS, h->K.p,
-                                     ldk, h->Bc.p, ldb, h->Sh.p, h->ldh, h->Lstore.p, h->Tt.p, h->U.p,
-                                     h->yS.p, h->u.p, h->tv.p, h->Z.p, info, h->dint.p + 9,
+        CK((cudaError_t)launch_schur(F, h->V.p, h->ldv, h->Yw.p, h->qS.p, h->ts_lo.p, h->ts_hi.p, nS_dev,
+                                     h->capS, h->K.p, h->capS, h->Bc.p, 3 * h->capS, h->Sh.p, h->ldh,
+                                     h->Lstore.p, h->Tt.p, h->U.p, h->yS.p, h->u.p, h->tv.p, h->Z.p,
+                                     h->dint.p + D_INFO, h->dint.p + D_SPREV + 1,
                                      h->trace_file ? h->sprof.p : nullptr, st));
-        if (h->trace_file && h->schur_file) {
-            std::vector<unsigned long long> pr(1024);
-            CK(cudaStreamSynchronize(st));
-            CK(cudaMemcpy(pr.data(), h->sprof.p, 1024 * 8, cudaMemcpyDeviceToHost));
-            fwrite(&nS, sizeof(int), 1, h->schur_file);
-            fwrite(pr.data(), 8, 1024, h->schur_file);
-            fflush(h->schur_file);
-        }
     } else {
         CK(cudaMemcpyAsync(h->Z.p, h->Yw.p, sizeof(double) * 4 * nf, cudaMemcpyDeviceToDevice, st));
     }
@@ -521,15 +518,14 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
     double *amin = h->dscal.p + 1;
     double *ls = h->dscal.p + 2, *ls_out = h->dscal.p + 5, *scal = h->dscal.p + 9;
     set_d(h, amin, 1.0);
-    int spt = 0, see = 0;
     kt.start(K_CCD, st);
     if (Nt > 0) {
         launch_surface(h->Wp.p, h->Wc.p, h->Wv.p, h->dx.p, Ns, h->ds.p, st);
-        broad_phase(h, h->ds.p, h->dh, &spt, &see);
-        launch_accd(h->cand.p, spt, 1, Nt, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->ds.p, h->opt.accd_s,
+        broad_phase(h, h->ds.p, h->dh, ccnt, h->dint.p + D_HOVF + 1);
+        launch_accd(h->cand.p, ccnt, cap, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->ds.p, h->opt.accd_s,
                     h->opt.accd_max_iters, amin, st);
-        launch_accd(h->cand.p + spt, see, 0, Ne, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->ds.p,
-                    h->opt.accd_s, h->opt.accd_max_iters, amin, st);
+    } else {
+        CK(cudaMemsetAsync(ccnt, 0, 2 * sizeof(int), st));
     }
     kt.stop(K_CCD, st);
     CK(cudaEventRecord(ev[4], st));
@@ -542,39 +538,45 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
         sum_partials(h->part.p + nb1, nb2, scal + 1, st);
         CK(cudaMemcpyAsync(ls, amin, sizeof(double), cudaMemcpyDeviceToDevice, st));
         CK(cudaMemsetAsync(ls + 1, 0, 2 * sizeof(double), st));
-        const int nsw = spt + see;
-        h->b0.ensure(nsw + 1);
-        const int nbp = (spt + 255) / 256, nbe = (see + 255) / 256;
-        const int pld = nbp + nbe + 1;
-        h->part.ensure(std::max<size_t>(8 * (size_t)pld, 2 * (size_t)std::max(nb1, nb2) + 16));
-        if (nsw > 0) {
-            launch_ls_b0(h->cand.p, spt, 1, Nt, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->dh, h->b0.p, st);
-            launch_ls_b0(h->cand.p + spt, see, 0, Ne, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->dh,
-                         h->b0.p + spt, st);
-        }
         const int hmax = h->opt.ls_max_halvings;
         for (int h0 = 0; h0 <= hmax; h0 += 8) {
-            launch_ls_trials(h->cand.p, spt, 1, Nt, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->ds.p, h->dh,
-                             h->b0.p, ls, h0, h->part.p, pld, st);
-            launch_ls_trials(h->cand.p + spt, see, 0, Ne, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->ds.p,
-                             h->dh, h->b0.p + spt, ls, h0, h->part.p + nbp, pld, st);
-            launch_ls_decide(h->part.p, pld, nbp + nbe, scal, h->kappa, h0, hmax, ls, ls_out, st);
+            if (Nt > 0)
+                launch_ls_trials(h->cand.p, ccnt, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->ds.p, h->dh, h->b0.p,
+                                 ls, h0, h->lspart.p, st);
+            else if (h0 == 0)
+                CK(cudaMemsetAsync(h->lspart.p, 0, sizeof(double) * 8 * ls_blocks(), st));
+            launch_ls_decide(h->lspart.p, scal, h->kappa, h0, hmax, ls, ls_out, st);
         }
-        launch_update(q.x.p, h->dx.p, h->q2v.p, nf, ls_out, st);
+        launch_update(q.x.p, h->dx.p, h->q2v.p, nf, ls_out, h->dint.p + D_CAP, 3, st);
     }
     kt.stop(K_LS, st);
     CK(cudaEventRecord(ev[5], st));
-    // ---------------- stats
+    // ---------------- the one host round trip of the iteration: stats and flags
     double sc[13];
+    int di[12];
     CK(cudaMemcpyAsync(sc, h->dscal.p, sizeof(sc), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(di, h->dint.p, sizeof(di), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&h->nS_host, nS_dev, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    int info_h = 0, fault_h = 0, flags_h[6];
-    CK(cudaMemcpy(flags_h, h->dint.p + 4, sizeof(flags_h), cudaMemcpyDeviceToHost));
-    info_h = flags_h[0];
-    q.stats.sigma_reused += nS > 0 ? flags_h[5] : 0;
-    CK(cudaMemcpy(&fault_h, h->ticket.p + 1, sizeof(int), cudaMemcpyDeviceToHost));
-    if (fault_h) throw CudaError("triangular solve dependency wait timed out", PD_IPC_E_CUDA);
-    if (info_h) throw CudaError("dense Cholesky: matrix not SPD", PD_IPC_E_NOT_SPD);
+    const int fault_flag = [&] {
+        int f = 0;
+        CK(cudaMemcpy(&f, h->ticket.p + 1, sizeof(int), cudaMemcpyDeviceToHost));
+        return f;
+    }();
+    if (fault_flag) throw CudaError("triangular solve dependency wait timed out", PD_IPC_E_CUDA);
+    const int nS = h->nS_host;
+    if (di[D_CAP] & 2) throw CudaError("contact vertex set exceeds capacity", PD_IPC_E_CAPACITY);
+    if ((di[D_CAP] & 5) || di[D_HOVF] || di[D_HOVF + 1]) {        // redo with grown buffers
+        if (di[D_CAP] & 1) grow_candidates(h, 2 * (size_t)cap);
+        if (di[D_CAP] & 4) h->Up.exact((size_t)std::max(1, F.nU) * (((nS + 31) / 32) * 32 + 64));
+        if (di[D_HOVF] || di[D_HOVF + 1]) h->force_sort = true;
+        kt.collect();
+        return false;
+    }
+    h->force_sort = false;
+    if (di[D_INFO]) throw CudaError("dense Cholesky: matrix not SPD", PD_IPC_E_NOT_SPD);
+    q.stats.sigma_reused += nS > 0 ? di[D_SPREV + 1] : 0;
+    const int n_pt = di[D_ACNT], n_all = di[D_ACNT + 1];
     for (int k = 0; k < 5; ++k) {
         float f;
         CK(cudaEventElapsedTime(&f, ev[k], ev[k + 1]));
@@ -585,31 +587,24 @@ static void iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
     ms[5] += tot;
     kt.collect();
     pd_ipc_stats &S = q.stats;
-    S.n_cand = n_cand;
-    S.n_active = n_pt + n_ee;
+    S.n_cand = di[D_STAT + 1];
+    S.n_active = n_all;
     S.n_S = nS;
     S.alpha_max = sc[2];
     S.alpha = sc[5];
     S.ls_trials = (int)sc[6];
     S.dE = sc[7];
     S.flags = (int)sc[8];
-    min_dist = (n_pt + n_ee > 0) ? sc[12] : 0.0;
-    if (n_pt + n_ee > 0 && !(min_dist > 0))
+    const double min_dist = n_all > 0 ? sc[12] : 0.0;
+    if (n_all > 0 && !(min_dist > 0))
         throw CudaError("non-positive distance in the active set", PD_IPC_E_NONFINITE);
     S.min_dist = min_dist;
     if (!std::isfinite(sc[5]) || !std::isfinite(sc[9]) || !std::isfinite(sc[10]))
         throw CudaError("non-finite value in step", PD_IPC_E_NONFINITE);
-    if (h->debug) {
-        std::vector<double4> d4(h->n);
-        CK(cudaMemcpy(d4.data(), h->dx.p, sizeof(double4) * h->n, cudaMemcpyDeviceToHost));
-        q.dx.resize(3 * (size_t)h->n);
-        for (int v = 0; v < h->n; ++v) {
-            q.dx[3 * v] = d4[v].x;
-            q.dx[3 * v + 1] = d4[v].y;
-            q.dx[3 * v + 2] = d4[v].z;
-        }
-    }
+    if (h->debug) debug_capture(h, q, n_pt, n_all - n_pt, nS);
+    dump_traces(h, nS);
     (void)last;
+    return true;
 }
 
 // ------------------------------------------------------------------ ABI -------------------
@@ -852,9 +847,9 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         h->ts_done.exact(f.nsn);
         h->ticket.exact(4);
         h->dscal.exact(16);
-        h->dint.exact(16);
+        h->dint.exact(32);
         CK(cudaMemset(h->dscal.p, 0, sizeof(double) * 16));   // flags / counters start cleared
-        CK(cudaMemset(h->dint.p, 0, sizeof(int) * 16));
+        CK(cudaMemset(h->dint.p, 0, sizeof(int) * 32));
         const size_t cap_cand = o.max_pairs > 0 ? (size_t)o.max_pairs
                                                 : std::max<size_t>(1 << 16, 16 * (size_t)(m.Ns + m.Ne));
         h->cand.exact(2 * cap_cand);
@@ -862,8 +857,8 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         ensure_pair_buffers(h.get(), 2 * cap_cand);
         // pre-size the per-pair buffers so that no allocation happens inside the iteration
         // (an allocation synchronises the device); they still grow on demand
-        if (m.Nt > 0) {
-            const size_t cap_act = cap_cand;
+        if (m.Nt > 0) {   // active pairs <= candidates: same capacity, no overflow check needed
+            const size_t cap_act = h->cand.n;
             h->akeys.ensure(cap_act + 1);
             h->atype.ensure(cap_act + 1);
             h->ad2.ensure(cap_act + 1);
@@ -871,13 +866,15 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             h->Hp.ensure(78 * cap_act + 78);
             h->dist.ensure(cap_act + 1);
             h->ids.ensure(4 * cap_act + 4);
-            h->rec.ensure(16 * cap_act + 1);
-            h->rec_tmp.ensure(16 * cap_act + 1);
-            h->bccnt.ensure(cap_act + 1);
-            h->bcoff.ensure(cap_act + 1);
-            h->b0.ensure(2 * cap_cand + 1);
-            h->iscr.ensure(radix_scratch_ints((int)(16 * cap_act)) + 1024);
+            h->b0.ensure(cap_act + 1);
+            h->blo.exact((size_t)m.Ns + m.Nt + m.Ne);
+            h->bhi.exact((size_t)m.Ns + m.Nt + m.Ne);
+            h->qcnt.exact((size_t)m.Ns + m.Ne + 1);
+            h->qoff.exact((size_t)m.Ns + m.Ne + 1);
+            h->qlist.exact((size_t)(m.Ns + m.Ne) * hash_query_cap());
+            h->gsq.exact(6 * (size_t)m.Ns + 6);
         }
+        h->lspart.exact(8 * (size_t)ls_blocks());
         h->iscr.ensure(std::max({radix_scratch_ints((int)(2 * cap_cand)), scan_scratch_ints(nf + 1),
                                  scan_scratch_ints(f.nsn + 1)}) + 1024);
         {
@@ -937,7 +934,11 @@ int pd_ipc_step(pd_ipc *h, const double *A_next, int32_t n_iters, pd_ipc_stats *
         for (auto &sq : h->seqs) {
             double ms[6] = {0, 0, 0, 0, 0, 0};
             sq->stats.sigma_reused = 0;
-            for (int it = 0; it < n_iters; ++it) iterate(h, *sq, it == n_iters - 1, ms);
+            for (int it = 0; it < n_iters; ++it) {
+                int tries = 0;
+                while (!iterate(h, *sq, it == n_iters - 1, ms))   // capacity grown: redo
+                    if (++tries > 8) throw CudaError("capacity growth did not converge", PD_IPC_E_CAPACITY);
+            }
             sq->stats.iters = n_iters;
             for (int k = 0; k < 6; ++k) sq->stats.ms[k] = ms[k];
         }
@@ -991,7 +992,7 @@ void pd_ipc_destroy(pd_ipc *h) {
     rel(h->qcnt); rel(h->qoff); rel(h->qlist); rel(h->gsq);
     rel(h->cand_tmp); rel(h->akeys); rel(h->flag); rel(h->pos); rel(h->ctype); rel(h->atype); rel(h->ids);
     rel(h->iscr); rel(h->cd2); rel(h->ad2); rel(h->grad); rel(h->Hp); rel(h->dist); rel(h->mark);
-    rel(h->spos); rel(h->qS); rel(h->rec); rel(h->rec_tmp); rel(h->bccnt); rel(h->bcoff); rel(h->ts_lo);
+    rel(h->spos); rel(h->qS); rel(h->lspart); rel(h->ts_lo);
     rel(h->ts_hi); rel(h->ts_cnt); rel(h->ts_ptr); rel(h->ts_rem); rel(h->ts_done); rel(h->ticket);
     rel(h->V); rel(h->K); rel(h->Bc); rel(h->Sh); rel(h->U); rel(h->Tt); rel(h->yS); rel(h->rhs);
     rel(h->u); rel(h->tv); rel(h->part); rel(h->b0); rel(h->dscal); rel(h->dint); rel(h->Lstore);
@@ -1017,17 +1018,18 @@ int pd_ipc_set_positions(pd_ipc *h, int32_t seq, const double *x) {
         if (h->Nt > 0) {
             // intersection check: every pair within d_hat must have a positive distance
             launch_surface(h->Wp.p, h->Wc.p, h->Wv.p, h->seqs[seq]->x.p, h->Ns, h->s.p, h->st);
-            int cpt, cee;
-            broad_phase(h, nullptr, 0.5 * h->dh * 1.01, &cpt, &cee);
-            ensure_pair_buffers(h, cpt + cee);
-            launch_narrow(h->cand.p, cpt, 1, h->Nt, h->s.p, h->tris.p, h->edges.p, h->Nt, h->Ne, h->dh2,
+            const bool fs = h->force_sort;
+            h->force_sort = true;            // exact and host-checked: this is a validation hook
+            int *ccnt = h->dint.p + D_CCNT;
+            broad_phase(h, nullptr, 0.5 * h->dh * 1.01, ccnt, h->dint.p + D_HOVF);
+            h->force_sort = fs;
+            launch_narrow(h->cand.p, ccnt, (int)h->cand.n, h->s.p, h->tris.p, h->edges.p, h->Nt, h->Ne, h->dh2,
                           h->flag.p, h->ctype.p, h->cd2.p, h->st);
-            launch_narrow(h->cand.p + cpt, cee, 0, h->Ne, h->s.p, h->tris.p, h->edges.p, h->Nt, h->Ne, h->dh2,
-                          h->flag.p + cpt, h->ctype.p + cpt, h->cd2.p + cpt, h->st);
-            std::vector<double> d2(cpt + cee);
-            CK(cudaStreamSynchronize(h->st));
-            if (cpt + cee)
-                CK(cudaMemcpy(d2.data(), h->cd2.p, sizeof(double) * (cpt + cee), cudaMemcpyDeviceToHost));
+            int cc[2];
+            sync_read_ints(h, cc, ccnt, 2);
+            std::vector<double> d2(cc[1]);
+            if (cc[1])
+                CK(cudaMemcpy(d2.data(), h->cd2.p, sizeof(double) * cc[1], cudaMemcpyDeviceToHost));
             for (double v : d2)
                 if (!(v > 0)) return fail(h, PD_IPC_E_INTERSECTING, "intersecting state");
         }

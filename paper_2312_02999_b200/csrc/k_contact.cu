@@ -14,6 +14,7 @@
 // THIS TRANSLATION UNIT IS COMPILED WITH -fmad=false: every product and sum is rounded
 // separately, exactly like the oracle's numpy ufuncs, so that the active set C and S are
 // bit-exact on identical positions.
+#include <algorithm>
 #include <climits>
 
 #include "kernels.h"
@@ -21,6 +22,9 @@
 #include "dev_common.cuh"
 
 namespace pdipc {
+
+// grid for a grid-stride launch over at most `cap` items (counts are read on the device)
+static int grid_for(int cap, int nt, int maxb) { return std::max(1, std::min((cap + nt - 1) / nt, maxb)); }
 
 // ------------------------------------------------------------------ vector helpers --------
 struct V3 { double x, y, z; };
@@ -399,47 +403,65 @@ k_hash_query_warp(const double4 *__restrict__ lo, const double4 *__restrict__ hi
 // Emit the per-query lists at their scanned offsets as keys a*nB + b (PT block, then EE block).
 __global__ void __launch_bounds__(32 * kQWarps)
 k_hash_emit(int Ns, int Nt, int Ne, const int *__restrict__ cnt, const int *__restrict__ off,
-            const int *__restrict__ qlist, unsigned long long *__restrict__ out) {
+            const int *__restrict__ qlist, unsigned long long *__restrict__ out, int cap) {
     const int lane = threadIdx.x & 31;
     const int q = blockIdx.x * kQWarps + (threadIdx.x >> 5);
     if (q >= Ns + Ne) return;
     const bool is_pt = q < Ns;
     const unsigned long long a = is_pt ? q : q - Ns, nB = is_pt ? Nt : Ne;
-    const int c = cnt[q];
+    const int c = cnt[q], o0 = off[q];
     const int *l = qlist + (size_t)q * kQCap;
-    unsigned long long *o = out + off[q];
-    for (int i = lane; i < c; i += 32) o[i] = a * nB + (unsigned long long)l[i];
+    for (int i = lane; i < c && o0 + i < cap; i += 32) out[o0 + i] = a * nB + (unsigned long long)l[i];
+}
+
+// candidate counts [npt, ntot] from the scanned query offsets, clamped to the buffer capacity
+// (a clamp raises bit 1 of *flags: the iteration is redone with a larger buffer)
+__global__ void k_cand_counts(const int *__restrict__ off, int Ns, int nq, int cap, int *__restrict__ ccnt,
+                              int *__restrict__ flags) {
+    const int npt = off[Ns], ntot = off[nq];
+    if (ntot > cap) atomicOr(flags, 1);
+    ccnt[0] = min(npt, cap);
+    ccnt[1] = min(ntot, cap);
 }
 
 // ------------------------------------------------------------------ a5 narrow filter ------
 // flag[i] = d^2 < dh2 for candidate keys; stores type and d^2
-__global__ void k_narrow(const unsigned long long *__restrict__ keys, int n, int is_pt, int nB,
+// ccnt = [npt, ntot] candidate counts (device).  PT keys first, then EE keys.
+__global__ void k_narrow(const unsigned long long *__restrict__ keys, const int *__restrict__ ccnt,
                          PairCtx c, double dh2, int *__restrict__ flag, int *__restrict__ type,
                          double *__restrict__ d2out) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    unsigned long long k = keys[i];
-    int i0 = (int)(k / nB), i1 = (int)(k % nB);
-    int id[4];
-    pair_ids(c, is_pt, i0, i1, id);
-    int ty;
-    double d2 = pair_d2(is_pt, mk(c.s[id[0]]), mk(c.s[id[1]]), mk(c.s[id[2]]), mk(c.s[id[3]]), &ty);
-    flag[i] = d2 < dh2 ? 1 : 0;
-    type[i] = ty;
-    d2out[i] = d2;
+    const int npt = ccnt[0], n = ccnt[1];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const bool is_pt = i < npt;
+        const int nB = is_pt ? c.Nt : c.Ne;
+        const unsigned long long k = keys[i];
+        int id[4];
+        pair_ids(c, is_pt, (int)(k / nB), (int)(k % nB), id);
+        int ty;
+        const double d2 = pair_d2(is_pt, mk(c.s[id[0]]), mk(c.s[id[1]]), mk(c.s[id[2]]), mk(c.s[id[3]]), &ty);
+        flag[i] = d2 < dh2 ? 1 : 0;
+        type[i] = ty;
+        d2out[i] = d2;
+    }
 }
-
-__global__ void k_compact_active(const unsigned long long *__restrict__ keys, int n,
+// active pairs [PT | EE] (each sorted) at pos[i]; acnt = [n_pt, n_all]
+__global__ void k_compact_active(const unsigned long long *__restrict__ keys, const int *__restrict__ ccnt,
                                  const int *__restrict__ flag, const int *__restrict__ pos,
                                  const int *__restrict__ type, const double *__restrict__ d2,
-                                 int base, unsigned long long *__restrict__ akeys,
-                                 int *__restrict__ atype, double *__restrict__ ad2) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n || !flag[i]) return;
-    int p = base + pos[i];
-    akeys[p] = keys[i];
-    atype[p] = type[i];
-    ad2[p] = d2[i];
+                                 unsigned long long *__restrict__ akeys, int *__restrict__ atype,
+                                 double *__restrict__ ad2, int *__restrict__ acnt) {
+    const int npt = ccnt[0], n = ccnt[1];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        acnt[0] = pos[npt];
+        acnt[1] = pos[n];
+    }
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        if (!flag[i]) continue;
+        const int p = pos[i];
+        akeys[p] = keys[i];
+        atype[p] = type[i];
+        ad2[p] = d2[i];
+    }
 }
 
 // ------------------------------------------------------------------ a5 derivatives --------
@@ -509,7 +531,7 @@ constexpr int kPD_WARPS = 4;
 // H_k^+ (packed upper, 78) and h_k = kappa b' grad d (12).
 __global__ void __launch_bounds__(kPD_WARPS * 32) k_pair_derivs(
     const unsigned long long *__restrict__ akeys, const int *__restrict__ atype,
-    const double *__restrict__ ad2, int n_pt, int n_all, PairCtx c, double dh, double kappa,
+    const double *__restrict__ ad2, const int *__restrict__ acnt, PairCtx c, double dh, double kappa,
     double *__restrict__ grad, double *__restrict__ Hp, double *__restrict__ dist,
     int *__restrict__ ids_out, double *__restrict__ dmax) {
     __shared__ double Hs[kPD_WARPS][12][13];
@@ -517,8 +539,8 @@ __global__ void __launch_bounds__(kPD_WARPS * 32) k_pair_derivs(
     __shared__ double gs[kPD_WARPS][12];
     __shared__ double rot[kPD_WARPS][6][2];
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-    const int k = blockIdx.x * kPD_WARPS + wl;
-    if (k >= n_all) return;
+    const int n_pt = acnt[0], n_all = acnt[1];          // device-resident counts
+    for (int k = blockIdx.x * kPD_WARPS + wl; k < n_all; k += gridDim.x * kPD_WARPS) {
     const bool is_pt = k < n_pt;
     const int nB = is_pt ? c.Nt : c.Ne;
     const unsigned long long key = akeys[k];
@@ -664,18 +686,21 @@ __global__ void __launch_bounds__(kPD_WARPS * 32) k_pair_derivs(
         atomicMax(reinterpret_cast<unsigned long long *>(dmax), (unsigned long long)__double_as_longlong(mx));
         atomic_min_nonneg(dmax + 1, d);       // min active distance (stats)
     }
+    __syncwarp();
+    }
 }
 
 // ------------------------------------------------------------------ a6 contact set S ------
-__global__ void k_mark_S(const int *__restrict__ ids, int n_all, const int *__restrict__ Wp,
+__global__ void k_mark_S(const int *__restrict__ ids, const int *__restrict__ acnt, const int *__restrict__ Wp,
                          const int *__restrict__ Wc, const int *__restrict__ v2q,
                          int *__restrict__ mark) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= 4 * n_all) return;
-    int j = ids[i];
-    for (int k = Wp[j]; k < Wp[j + 1]; ++k) {
-        int q = v2q[Wc[k]];
-        if (q >= 0) mark[q] = 1;
+    const int n4 = 4 * acnt[1];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
+        const int j = ids[i];
+        for (int k = Wp[j]; k < Wp[j + 1]; ++k) {
+            const int q = v2q[Wc[k]];
+            if (q >= 0) mark[q] = 1;
+        }
     }
 }
 
@@ -688,8 +713,10 @@ __global__ void k_compact_S(const int *__restrict__ mark, const int *__restrict_
 // same = (S == S_prev, bit for bit, |S| > 0); then S_prev <- S.  One CTA.
 __global__ void __launch_bounds__(1024) k_same_S(const int *__restrict__ qS, const int *__restrict__ nS_ptr,
                                                  int *__restrict__ qS_prev, int *__restrict__ nS_prev,
-                                                 int *__restrict__ same, int enabled) {
-    const int nS = *nS_ptr, np = *nS_prev;
+                                                 int *__restrict__ same, int enabled, int cap,
+                                                 int *__restrict__ flags) {
+    const int nS = min(*nS_ptr, cap), np = *nS_prev;
+    if (threadIdx.x == 0 && *nS_ptr > cap) atomicOr(flags, 2);   // |S| beyond the dense buffers
     int eq = enabled && nS > 0 && nS == np;
     for (int i = threadIdx.x; i < nS && eq; i += blockDim.x) eq = qS[i] == qS_prev[i];
     eq = __syncthreads_and(eq);
@@ -758,69 +785,68 @@ __device__ __forceinline__ double fx_get(long long hi, long long lo, double inv_
     return ((double)hi + (double)lo / kFxLo) * inv_sc;
 }
 
-__global__ void k_accum_grad_fx(const int *__restrict__ ids, int n_all, const double *__restrict__ grad,
-                                const double *__restrict__ dmax, long long *__restrict__ gsq) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;     // (pair, slot)
-    if (i >= 4 * n_all) return;
+__global__ void k_accum_grad_fx(const int *__restrict__ ids, const int *__restrict__ acnt,
+                                const double *__restrict__ grad, const double *__restrict__ dmax,
+                                long long *__restrict__ gsq) {
+    const int n_all = acnt[1];
     const double sc = fx_scale(dmax, n_all);
-    const int j = ids[i];
-    for (int a = 0; a < 3; ++a)              // hi in gsq[j][0..2], lo in gsq[j][3..5]
-        fx_add(gsq + 6 * (size_t)j + a, gsq + 6 * (size_t)j + 3 + a, grad[3 * (size_t)i + a], sc);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 4 * n_all; i += gridDim.x * blockDim.x) {
+        const int j = ids[i];                    // (pair, slot); hi in gsq[j][0..2], lo in [3..5]
+        for (int a = 0; a < 3; ++a)
+            fx_add(gsq + 6 * (size_t)j + a, gsq + 6 * (size_t)j + 3 + a, grad[3 * (size_t)i + a], sc);
+    }
 }
-
-// B-check: thread per (pair, slot_a, slot_b); target (S-index of v_a, S-index of v_b) blocks
-__global__ void k_accum_bc_fx(const int *__restrict__ ids, int n_all, const int *__restrict__ Wp,
+__global__ void k_accum_bc_fx(const int *__restrict__ ids, const int *__restrict__ acnt, const int *__restrict__ Wp,
                               const int *__restrict__ Wc, const double *__restrict__ Wv,
                               const int *__restrict__ v2q, const int *__restrict__ sidx,
                               const double *__restrict__ Hp, const double *__restrict__ dmax,
                               long long *__restrict__ Bq, long long *__restrict__ Bl, int ldb) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= 16 * n_all) return;
-    const int k = i >> 4, sa = (i >> 2) & 3, sb = i & 3;
+    const int n_all = acnt[1];
     const double sc = fx_scale(dmax, n_all);
-    const int ja = ids[4 * k + sa], jb = ids[4 * k + sb];
-    const double *H = Hp + 78 * (size_t)k;
-    double blk[9];
-    for (int a = 0; a < 3; ++a)
-        for (int b = 0; b < 3; ++b) {
-            const int ii = 3 * sa + a, jj = 3 * sb + b;
-            blk[3 * a + b] = ii <= jj ? H[ii * 12 - (ii * (ii - 1)) / 2 + (jj - ii)]
-                                      : H[jj * 12 - (jj * (jj - 1)) / 2 + (ii - jj)];
-        }
-    for (int na = Wp[ja]; na < Wp[ja + 1]; ++na) {
-        const int qa = v2q[Wc[na]];
-        if (qa < 0) continue;
-        for (int nb = Wp[jb]; nb < Wp[jb + 1]; ++nb) {
-            const int qb = v2q[Wc[nb]];
-            if (qb < 0) continue;
-            const double w = Wv[na] * Wv[nb];
-            const size_t o = (size_t)(3 * sidx[qa]) * ldb + 3 * sidx[qb];
-            for (int a = 0; a < 3; ++a)
-                for (int b = 0; b < 3; ++b)
-                    fx_add(Bq + o + (size_t)a * ldb + b, Bl + o + (size_t)a * ldb + b, w * blk[3 * a + b], sc);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 16 * n_all; i += gridDim.x * blockDim.x) {
+        const int k = i >> 4, sa = (i >> 2) & 3, sb = i & 3;
+        const int ja = ids[4 * k + sa], jb = ids[4 * k + sb];
+        const double *H = Hp + 78 * (size_t)k;
+        double blk[9];
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) {
+                const int ii = 3 * sa + a, jj = 3 * sb + b;
+                blk[3 * a + b] = ii <= jj ? H[ii * 12 - (ii * (ii - 1)) / 2 + (jj - ii)]
+                                          : H[jj * 12 - (jj * (jj - 1)) / 2 + (ii - jj)];
+            }
+        for (int na = Wp[ja]; na < Wp[ja + 1]; ++na) {
+            const int qa = v2q[Wc[na]];
+            if (qa < 0 || 3 * sidx[qa] >= ldb) continue;          // |S| > capS is flagged, not written
+            for (int nb = Wp[jb]; nb < Wp[jb + 1]; ++nb) {
+                const int qb = v2q[Wc[nb]];
+                if (qb < 0 || 3 * sidx[qb] >= ldb) continue;
+                const double w = Wv[na] * Wv[nb];
+                const size_t o = (size_t)(3 * sidx[qa]) * ldb + 3 * sidx[qb];
+                for (int a = 0; a < 3; ++a)
+                    for (int b = 0; b < 3; ++b)
+                        fx_add(Bq + o + (size_t)a * ldb + b, Bl + o + (size_t)a * ldb + b, w * blk[3 * a + b], sc);
+            }
         }
     }
 }
-
-// in place: fixed point (hi in M, lo in Ml) -> double in M, n x n block, leading dimension ld
-__global__ void k_fx_to_double(long long *M, const long long *Ml, int ld, int n, const double *dmax,
-                               int n_pairs) {
-    const double inv = 1.0 / fx_scale(dmax, n_pairs);
+// n = 3 |S| from the device (clamped to 3 capS)
+__global__ void k_fx_to_double(long long *M, const long long *Ml, int ld, const int *nS_ptr, int capS,
+                               const double *dmax, const int *acnt) {
+    const int n = 3 * min(*nS_ptr, capS);
+    const double inv = 1.0 / fx_scale(dmax, acnt[1]);
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < (size_t)n * n;
          e += (size_t)gridDim.x * blockDim.x) {
         const size_t off = (e / n) * ld + e % n;
         reinterpret_cast<double *>(M)[off] = fx_get(M[off], Ml[off], inv);
     }
 }
-
-// G[q] = g_el[q] + sum_{(j,w) in W^T row q} w gs[j]   (gs in fixed point)
 __global__ void k_grad_pullback_fx(const double4 *__restrict__ g_el, const int *__restrict__ WTp,
                                    const int *__restrict__ WTr, const double *__restrict__ WTv,
                                    const long long *__restrict__ gsq, const double *__restrict__ dmax,
-                                   int n_pairs, int nf, double *__restrict__ G) {
+                                   const int *__restrict__ acnt, int nf, double *__restrict__ G) {
     int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nf) return;
-    const double inv = 1.0 / fx_scale(dmax, n_pairs);
+    const double inv = 1.0 / fx_scale(dmax, acnt[1]);
     double4 g = g_el[q];
     double bx = 0, by = 0, bz = 0;
     for (int k = WTp[q]; k < WTp[q + 1]; ++k) {
@@ -836,28 +862,28 @@ __global__ void k_grad_pullback_fx(const double4 *__restrict__ g_el, const int *
     G[4 * (size_t)q + 3] = 0.0;
 }
 
-void launch_accum_grad_fx(const int *ids, int n_all, const double *grad, const double *dmax,
+void launch_accum_grad_fx(const int *ids, const int *acnt, int cap, const double *grad, const double *dmax,
                           long long *gsq, cudaStream_t st) {
-    if (n_all > 0) PDI_LAUNCH(k_accum_grad_fx, (4 * n_all + 255) / 256, 256, 0, st)(ids, n_all, grad, dmax, gsq);
+    PDI_LAUNCH(k_accum_grad_fx, grid_for(4 * cap, 256, 148 * 8), 256, 0, st)(ids, acnt, grad, dmax, gsq);
 }
-void launch_accum_bc_fx(const int *ids, int n_all, const int *Wp, const int *Wc, const double *Wv,
+void launch_accum_bc_fx(const int *ids, const int *acnt, int cap, const int *Wp, const int *Wc, const double *Wv,
                         const int *v2q, const int *sidx, const double *Hp, const double *dmax,
                         long long *Bq, long long *Bl, int ldb, cudaStream_t st) {
-    if (n_all > 0)
-        PDI_LAUNCH(k_accum_bc_fx, (16 * n_all + 127) / 128, 128, 0, st)(ids, n_all, Wp, Wc, Wv, v2q, sidx, Hp,
-                                                                        dmax, Bq, Bl, ldb);
+    PDI_LAUNCH(k_accum_bc_fx, grid_for(16 * cap, 128, 148 * 16), 128, 0, st)(ids, acnt, Wp, Wc, Wv, v2q, sidx,
+                                                                           Hp, dmax, Bq, Bl, ldb);
 }
-void launch_fx_to_double(long long *M, const long long *Ml, int ld, int n, const double *dmax,
-                         int n_pairs, cudaStream_t st) {
-    if (n > 0) PDI_LAUNCH(k_fx_to_double, 256, 256, 0, st)(M, Ml, ld, n, dmax, n_pairs);
+void launch_fx_to_double(long long *M, const long long *Ml, int ld, const int *nS, int capS, const double *dmax,
+                         const int *acnt, cudaStream_t st) {
+    PDI_LAUNCH(k_fx_to_double, 296, 256, 0, st)(M, Ml, ld, nS, capS, dmax, acnt);
 }
 void launch_grad_pullback_fx(const double4 *g_el, const int *WTp, const int *WTr, const double *WTv,
-                             const long long *gsq, const double *dmax, int n_pairs, int nf, double *G,
+                             const long long *gsq, const double *dmax, const int *acnt, int nf, double *G,
                              cudaStream_t st) {
-    PDI_LAUNCH(k_grad_pullback_fx, (nf + 255) / 256, 256, 0, st)(g_el, WTp, WTr, WTv, gsq, dmax, n_pairs, nf, G);
+    PDI_LAUNCH(k_grad_pullback_fx, (nf + 255) / 256, 256, 0, st)(g_el, WTp, WTr, WTv, gsq, dmax, acnt, nf, G);
 }
 
-__global__ void k_zero_square(double *M, int ld, int n) {
+__global__ void k_zero_square(double *M, int ld, const int *nS_ptr, int capS) {
+    const int n = 3 * min(*nS_ptr, capS);
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < (size_t)n * n;
          e += (size_t)gridDim.x * blockDim.x)
         M[(e / n) * ld + e % n] = 0.0;
@@ -865,13 +891,15 @@ __global__ void k_zero_square(double *M, int ld, int n) {
 
 // ------------------------------------------------------------------ a10 ACCD --------------
 // SURVEY 8(c) O7 as written.  Swept candidate keys -> TOI; atomic min into *amin.
-__global__ void k_accd(const unsigned long long *__restrict__ keys, int n, int is_pt, int nB,
+__global__ void k_accd(const unsigned long long *__restrict__ keys, const int *__restrict__ ccnt,
                        PairCtx c, const double4 *__restrict__ ds, double s_gap, int max_iters,
                        double *__restrict__ amin) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    double toi = 1.0;
-    if (i < n) {
-        unsigned long long k = keys[i];
+    const int npt = ccnt[0], n = ccnt[1];
+    double toi_min = 1.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const bool is_pt = i < npt;
+        const int nB = is_pt ? c.Nt : c.Ne;
+        const unsigned long long k = keys[i];
         int id[4];
         pair_ids(c, is_pt, (int)(k / nB), (int)(k % nB), id);
         V3 P[4], D[4];
@@ -880,75 +908,74 @@ __global__ void k_accd(const unsigned long long *__restrict__ keys, int n, int i
                    (((D[0].z + D[1].z) + D[2].z) + D[3].z) / 4.0};
         double nr[4];
         for (int q = 0; q < 4; ++q) { V3 p = sub(D[q], mean); nr[q] = sqrt(dot(p, p)); }
-        double lp = is_pt ? nr[0] + fmax(fmax(nr[1], nr[2]), nr[3]) : fmax(nr[0], nr[1]) + fmax(nr[2], nr[3]);
+        const double lp = is_pt ? nr[0] + fmax(fmax(nr[1], nr[2]), nr[3]) : fmax(nr[0], nr[1]) + fmax(nr[2], nr[3]);
+        double toi = 1.0;
         if (lp > 0.0) {
             int ty;
-            double d_init = sqrt(pair_d2(is_pt, P[0], P[1], P[2], P[3], &ty));
-            double g = s_gap * d_init;
+            const double d_init = sqrt(pair_d2(is_pt, P[0], P[1], P[2], P[3], &ty));
+            const double g = s_gap * d_init;
             double t = 0.0, tl = (1.0 - s_gap) * d_init / lp;
             int it = 0;
             bool done = false;
             while (it < max_iters) {
-                double tt = t + tl;
-                double d = sqrt(pair_d2(is_pt, axpy(P[0], tt, D[0]), axpy(P[1], tt, D[1]),
-                                        axpy(P[2], tt, D[2]), axpy(P[3], tt, D[3]), &ty));
+                const double tt = t + tl;
+                const double d = sqrt(pair_d2(is_pt, axpy(P[0], tt, D[0]), axpy(P[1], tt, D[1]),
+                                              axpy(P[2], tt, D[2]), axpy(P[3], tt, D[3]), &ty));
                 ++it;
-                bool gap_exit = t > 0 && d < g;
-                if (gap_exit) { toi = t; done = true; break; }
+                if (t > 0 && d < g) { toi = t; done = true; break; }
                 if (tt > 1.0) { toi = 1.0; done = true; break; }
                 t = tt;
                 tl = 0.9 * d / lp;
             }
             if (!done) toi = t;
         }
+        toi_min = fmin(toi_min, toi);
     }
-    toi = warp_min(toi);
-    if ((threadIdx.x & 31) == 0) atomic_min_nonneg(amin, toi);
+    toi_min = warp_min(toi_min);
+    if ((threadIdx.x & 31) == 0) atomic_min_nonneg(amin, toi_min);
 }
 
 // ------------------------------------------------------------------ a11 line search -------
-// b0[i] = b(d(s)) per swept candidate
-__global__ void k_ls_b0(const unsigned long long *__restrict__ keys, int n, int is_pt, int nB,
-                        PairCtx c, double dh, double *__restrict__ b0) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    unsigned long long k = keys[i];
-    int id[4], ty;
-    pair_ids(c, is_pt, (int)(k / nB), (int)(k % nB), id);
-    double d2 = pair_d2(is_pt, mk(c.s[id[0]]), mk(c.s[id[1]]), mk(c.s[id[2]]), mk(c.s[id[3]]), &ty);
-    b0[i] = bar(sqrt(d2), dh);
-}
-
-// per block partial sums of b(d(alpha_h)) - b0 for trials h = h0 .. h0+7
+// per block partial sums over the swept candidates of b(d(alpha_h)) - b(d(0)) for the trials
+// h = h0 .. h0+7 (alpha_h = alpha_m 2^-h); b(d(0)) computed in the first round and kept in b0
 __global__ void __launch_bounds__(256) k_ls_trials(const unsigned long long *__restrict__ keys,
-                                                   int n, int is_pt, int nB, PairCtx c,
+                                                   const int *__restrict__ ccnt, PairCtx c,
                                                    const double4 *__restrict__ ds, double dh,
-                                                   const double *__restrict__ b0,
-                                                   const double *__restrict__ ls,  // [alpha_m, accepted flag, h0]
+                                                   double *__restrict__ b0,
+                                                   const double *__restrict__ ls,  // [alpha_m, accepted flag]
                                                    int h0, double *__restrict__ part, int part_ld) {
     if (ls[1] != 0.0) return;   // already accepted
     __shared__ double sh[8];
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int npt = ccnt[0], n = ccnt[1];
     const double am = ls[0];
-    int id[4];
-    V3 P[4], D[4];
-    double bb0 = 0.0;
-    if (i < n) {
-        unsigned long long k = keys[i];
+    double acc[8];
+#pragma unroll
+    for (int h = 0; h < 8; ++h) acc[h] = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const bool is_pt = i < npt;
+        const int nB = is_pt ? c.Nt : c.Ne;
+        const unsigned long long k = keys[i];
+        int id[4], ty;
         pair_ids(c, is_pt, (int)(k / nB), (int)(k % nB), id);
+        V3 P[4], D[4];
         for (int q = 0; q < 4; ++q) { P[q] = mk(c.s[id[q]]); D[q] = mk(ds[id[q]]); }
-        bb0 = b0[i];
+        double bb0;
+        if (h0 == 0) {
+            bb0 = bar(sqrt(pair_d2(is_pt, P[0], P[1], P[2], P[3], &ty)), dh);
+            b0[i] = bb0;
+        } else {
+            bb0 = b0[i];
+        }
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+            const double al = ldexp(am, -(h0 + h));
+            const double d2 = pair_d2(is_pt, axpy(P[0], al, D[0]), axpy(P[1], al, D[1]), axpy(P[2], al, D[2]),
+                                      axpy(P[3], al, D[3]), &ty);
+            acc[h] += bar(sqrt(d2), dh) - bb0;
+        }
     }
     for (int h = 0; h < 8; ++h) {
-        double v = 0.0;
-        if (i < n) {
-            double al = ldexp(am, -(h0 + h));
-            int ty;
-            double d2 = pair_d2(is_pt, axpy(P[0], al, D[0]), axpy(P[1], al, D[1]), axpy(P[2], al, D[2]),
-                                axpy(P[3], al, D[3]), &ty);
-            v = bar(sqrt(d2), dh) - bb0;
-        }
-        v = block_sum<256>(v, sh);
+        const double v = block_sum<256>(acc[h], sh);
         if (threadIdx.x == 0) part[(size_t)h * part_ld + blockIdx.x] = v;
     }
 }
@@ -1031,42 +1058,40 @@ void launch_hash_query_warp(const double4 *lo, const double4 *hi, int Ns, int Nt
             lo, hi, Ns, Nt, Ne, cell, mask, start, entries, tris, edges, cnt, qlist, ovf);
 }
 void launch_hash_emit(int Ns, int Nt, int Ne, const int *cnt, const int *off, const int *qlist,
-                      unsigned long long *out, cudaStream_t st) {
+                      unsigned long long *out, int cap, int *ccnt, int *flags, cudaStream_t st) {
     const int nq = Ns + Ne;
+    PDI_LAUNCH(k_cand_counts, 1, 1, 0, st)(off, Ns, nq, cap, ccnt, flags);
     if (nq > 0)
         PDI_LAUNCH(k_hash_emit, (nq + kQWarps - 1) / kQWarps, 32 * kQWarps, 0, st)(Ns, Nt, Ne, cnt, off,
-                                                                                 qlist, out);
+                                                                                 qlist, out, cap);
 }
-void launch_narrow(const unsigned long long *keys, int n, int is_pt, int nB, const double4 *s,
+void launch_narrow(const unsigned long long *keys, const int *ccnt, int cap, const double4 *s,
                    const int *tris, const int *edges, int Nt, int Ne, double dh2, int *flag,
                    int *type, double *d2, cudaStream_t st) {
-    if (n <= 0) return;
     PairCtx c{s, tris, edges, Nt, Ne};
-    PDI_LAUNCH(k_narrow, (n + 255) / 256, 256, 0, st)(keys, n, is_pt, nB, c, dh2, flag, type, d2);
+    PDI_LAUNCH(k_narrow, grid_for(cap, 256, 148 * 8), 256, 0, st)(keys, ccnt, c, dh2, flag, type, d2);
 }
-void launch_compact_active(const unsigned long long *keys, int n, const int *flag, const int *pos,
-                           const int *type, const double *d2, int base, unsigned long long *akeys,
-                           int *atype, double *ad2, cudaStream_t st) {
-    if (n > 0)
-        PDI_LAUNCH(k_compact_active, (n + 255) / 256, 256, 0, st)(keys, n, flag, pos, type, d2, base, akeys, atype, ad2);
+void launch_compact_active(const unsigned long long *keys, const int *ccnt, int cap, const int *flag,
+                           const int *pos, const int *type, const double *d2, unsigned long long *akeys,
+                           int *atype, double *ad2, int *acnt, cudaStream_t st) {
+    PDI_LAUNCH(k_compact_active, grid_for(cap, 256, 148 * 8), 256, 0, st)(keys, ccnt, flag, pos, type, d2,
+                                                                          akeys, atype, ad2, acnt);
 }
 void launch_pair_derivs(const unsigned long long *akeys, const int *atype, const double *ad2,
-                        int n_pt, int n_all, const double4 *s, const int *tris, const int *edges,
+                        const int *acnt, int cap, const double4 *s, const int *tris, const int *edges,
                         int Nt, int Ne, double dh, double kappa, double *grad, double *Hp,
                         double *dist, int *ids, double *dmax, cudaStream_t st) {
-    if (n_all <= 0) return;
     PairCtx c{s, tris, edges, Nt, Ne};
-    PDI_LAUNCH(k_pair_derivs, (n_all + kPD_WARPS - 1) / kPD_WARPS, kPD_WARPS * 32, 0, st)(
-        akeys, atype, ad2, n_pt, n_all, c, dh, kappa, grad, Hp, dist, ids, dmax);
+    PDI_LAUNCH(k_pair_derivs, grid_for(cap, kPD_WARPS, 148 * 2), kPD_WARPS * 32, 0, st)(
+        akeys, atype, ad2, acnt, c, dh, kappa, grad, Hp, dist, ids, dmax);
 }
-void launch_mark_S(const int *ids, int n_all, const int *Wp, const int *Wc, const int *v2q,
+void launch_mark_S(const int *ids, const int *acnt, int cap, const int *Wp, const int *Wc, const int *v2q,
                    int *mark, cudaStream_t st) {
-    if (n_all > 0) PDI_LAUNCH(k_mark_S, (4 * n_all + 255) / 256, 256, 0, st)(ids, n_all, Wp, Wc, v2q, mark);
+    PDI_LAUNCH(k_mark_S, grid_for(4 * cap, 256, 148 * 8), 256, 0, st)(ids, acnt, Wp, Wc, v2q, mark);
 }
 void launch_same_S(const int *qS, const int *nS_ptr, int *qS_prev, int *nS_prev, int *same, int cap,
-                   bool enabled, cudaStream_t st) {
-    (void)cap;
-    PDI_LAUNCH(k_same_S, 1, 1024, 0, st)(qS, nS_ptr, qS_prev, nS_prev, same, enabled ? 1 : 0);
+                   bool enabled, int *flags, cudaStream_t st) {
+    PDI_LAUNCH(k_same_S, 1, 1024, 0, st)(qS, nS_ptr, qS_prev, nS_prev, same, enabled ? 1 : 0, cap, flags);
 }
 void launch_compact_S(const int *mark, const int *pos, int nf, int *qS, cudaStream_t st) {
     PDI_LAUNCH(k_compact_S, (nf + 255) / 256, 256, 0, st)(mark, pos, nf, qS);
@@ -1075,36 +1100,25 @@ void launch_grad_pullback(const double4 *g_el, const int *WTp, const int *WTr, c
                           const double4 *gs, int nf, double *G, cudaStream_t st) {
     PDI_LAUNCH(k_grad_pullback, (nf + 255) / 256, 256, 0, st)(g_el, WTp, WTr, WTv, gs, nf, G);
 }
-void launch_zero_square(double *M, int ld, int n, cudaStream_t st) {
-    if (n > 0) PDI_LAUNCH(k_zero_square, 256, 256, 0, st)(M, ld, n);
+void launch_zero_square(double *M, int ld, const int *nS, int capS, cudaStream_t st) {
+    PDI_LAUNCH(k_zero_square, 296, 256, 0, st)(M, ld, nS, capS);
 }
-void launch_accd(const unsigned long long *keys, int n, int is_pt, int nB, const double4 *s,
+void launch_accd(const unsigned long long *keys, const int *ccnt, int cap, const double4 *s,
                  const int *tris, const int *edges, int Nt, int Ne, const double4 *ds, double s_gap,
                  int max_iters, double *amin, cudaStream_t st) {
-    if (n <= 0) return;
     PairCtx c{s, tris, edges, Nt, Ne};
-    PDI_LAUNCH(k_accd, (n + 127) / 128, 128, 0, st)(keys, n, is_pt, nB, c, ds, s_gap, max_iters, amin);
+    PDI_LAUNCH(k_accd, grid_for(cap, 128, 148 * 8), 128, 0, st)(keys, ccnt, c, ds, s_gap, max_iters, amin);
 }
-void launch_ls_b0(const unsigned long long *keys, int n, int is_pt, int nB, const double4 *s,
-                  const int *tris, const int *edges, int Nt, int Ne, double dh, double *b0,
-                  cudaStream_t st) {
-    if (n <= 0) return;
+int ls_blocks() { return 2 * 148; }
+void launch_ls_trials(const unsigned long long *keys, const int *ccnt, const double4 *s, const int *tris,
+                      const int *edges, int Nt, int Ne, const double4 *ds, double dh, double *b0,
+                      const double *ls, int h0, double *part, cudaStream_t st) {
     PairCtx c{s, tris, edges, Nt, Ne};
-    PDI_LAUNCH(k_ls_b0, (n + 255) / 256, 256, 0, st)(keys, n, is_pt, nB, c, dh, b0);
+    PDI_LAUNCH(k_ls_trials, ls_blocks(), 256, 0, st)(keys, ccnt, c, ds, dh, b0, ls, h0, part, ls_blocks());
 }
-int launch_ls_trials(const unsigned long long *keys, int n, int is_pt, int nB, const double4 *s,
-                     const int *tris, const int *edges, int Nt, int Ne, const double4 *ds,
-                     double dh, const double *b0, const double *ls, int h0, double *part,
-                     int part_ld, cudaStream_t st) {
-    if (n <= 0) return 0;
-    PairCtx c{s, tris, edges, Nt, Ne};
-    int nb = (n + 255) / 256;
-    PDI_LAUNCH(k_ls_trials, nb, 256, 0, st)(keys, n, is_pt, nB, c, ds, dh, b0, ls, h0, part, part_ld);
-    return nb;
-}
-void launch_ls_decide(const double *part, int part_ld, int npart, const double *scal, double kappa,
-                      int h0, int hmax, double *ls, double *out, cudaStream_t st) {
-    PDI_LAUNCH(k_ls_decide, 1, 1024, 0, st)(part, part_ld, npart, scal, kappa, h0, hmax, ls, out);
+void launch_ls_decide(const double *part, const double *scal, double kappa, int h0, int hmax, double *ls,
+                      double *out, cudaStream_t st) {
+    PDI_LAUNCH(k_ls_decide, 1, 1024, 0, st)(part, ls_blocks(), ls_blocks(), scal, kappa, h0, hmax, ls, out);
 }
 
 }  // namespace pdipc

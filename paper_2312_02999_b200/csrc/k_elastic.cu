@@ -275,10 +275,15 @@ __global__ void __launch_bounds__(256) k_gdx_partials(const double4 *__restrict_
 }
 
 // x[v] += alpha dx[v] for free v
+// x_F += alpha dx, unless a capacity / overflow flag of this iteration is raised (the host then
+// grows the buffer and redoes the iteration from the unchanged x)
 __global__ void k_update(double4 *__restrict__ x, const double4 *__restrict__ dx,
-                         const int *__restrict__ q2v, int nf, const double *__restrict__ alpha) {
+                         const int *__restrict__ q2v, int nf, const double *__restrict__ alpha,
+                         const int *__restrict__ abort_flags, int n_flags) {
     int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nf) return;
+    for (int f = 0; f < n_flags; ++f)
+        if (abort_flags[f]) return;
     int v = q2v[q];
     double a = *alpha;
     double4 xv = x[v], d = dx[v];
@@ -330,8 +335,8 @@ int gdx_partials(const double4 *g, const double4 *dx, const int *q2v, int nf, do
     return nb;
 }
 void launch_update(double4 *x, const double4 *dx, const int *q2v, int nf, const double *alpha,
-                   cudaStream_t st) {
-    PDI_LAUNCH(k_update, (nf + 255) / 256, 256, 0, st)(x, dx, q2v, nf, alpha);
+                   const int *abort_flags, int n_flags, cudaStream_t st) {
+    PDI_LAUNCH(k_update, (nf + 255) / 256, 256, 0, st)(x, dx, q2v, nf, alpha, abort_flags, n_flags);
 }
 void launch_scatter_dx(const double *z, const int *q2v, int nf, double4 *dx, cudaStream_t st) {
     PDI_LAUNCH(k_scatter_dx, (nf + 255) / 256, 256, 0, st)(z, q2v, nf, dx);

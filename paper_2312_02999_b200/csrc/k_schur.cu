@@ -38,7 +38,8 @@ struct SchurArgs {
     int ldv;
     const double *G;            // w [nf][4]
     const int *qS, *col2sn, *sn_c0, *sn_parent, *lo, *hi;
-    int nsn, nf, nS;
+    int nsn, nf, capS;
+    const int *nS_ptr;          // |S| (device); clamped to capS
     // dense buffers
     double *K;                  // [capS][ldk] -> Sigma_s
     int ldk;
@@ -268,7 +269,11 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int G = gridDim.x, bid = blockIdx.x;
-    const int nS = a.nS, m = 3 * nS, ma = m + 1;          // augmented size
+    const int nS = min(*a.nS_ptr, a.capS), m = 3 * nS, ma = m + 1;   // augmented size
+    if (nS == 0) {                                        // no contact: z = w
+        for (int r = bid * NT + tid; r < 4 * a.nf; r += G * NT) a.Z[r] = a.G[r];
+        return;
+    }
     int np = 0;                                           // phase-timestamp counter (debug)
     if (a.prof && bid == 0 && tid == 0) a.prof[np++] = gtimer_s();
 #define GSYNC()                                                               \
@@ -637,13 +642,13 @@ void schur_init(int device) {
 }
 
 int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, const int *qS,
-                 const int *lo, const int *hi, int nS, double *K, int ldk, const double *Bc, int ldb,
+                 const int *lo, const int *hi, const int *nS, int capS, double *K, int ldk, const double *Bc, int ldb,
                  double *Sh, int ldh, double *Lstore, double *T, double *U, double *yS, double *u,
                  double *t, double *Z, int *info, const int *same_S, unsigned long long *prof,
                  cudaStream_t st) {
     SchurArgs a;
     a.V = V; a.ldv = ldv; a.G = G; a.qS = qS; a.col2sn = F.col2sn; a.sn_c0 = F.sn_c0;
-    a.sn_parent = F.sn_parent; a.lo = lo; a.hi = hi; a.nsn = F.nsn; a.nf = F.nf; a.nS = nS;
+    a.sn_parent = F.sn_parent; a.lo = lo; a.hi = hi; a.nsn = F.nsn; a.nf = F.nf; a.nS_ptr = nS; a.capS = capS;
     a.K = K; a.ldk = ldk; a.Bc = Bc; a.ldb = ldb; a.Sh = Sh; a.ldh = ldh; a.Lstore = Lstore;
     a.T = T; a.U = U; a.yS = yS; a.u = u; a.t = t; a.Z = Z; a.info = info; a.same = same_S; a.prof = prof;
     static double *kpart = nullptr;                 // grid x 1152 doubles, allocated once

@@ -37,13 +37,17 @@ constexpr long long kSpinLimit = 4000000000LL;
 __global__ void k_ts_items(const int *__restrict__ ford, const int *__restrict__ sn_c0,
                            const int *__restrict__ sn_rowptr, const int *__restrict__ sn_fd,
                            const int *__restrict__ sn_parent, int nsn, const int *__restrict__ qS,
-                           const int *__restrict__ nS_ptr, const int *__restrict__ same_S,
+                           const int *__restrict__ nS_ptr, int capS, const int *__restrict__ same_S,
+                           int nU, long long up_cap, int *__restrict__ flags,
                            int *__restrict__ lo, int *__restrict__ hi, int *__restrict__ cnt,
                            int *__restrict__ rem) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;   // dispatch position
     if (k >= nsn) return;
     const int s = ford[k];
-    const int nS = *nS_ptr;
+    const int nS = min(*nS_ptr, capS);
+    // panel update rows need nU x round32(|S|) doubles; otherwise flag bit 4 (grow and redo)
+    const bool up_ok = (long long)nU * (((nS + 31) / 32) * 32) <= up_cap;
+    if (!up_ok && k == 0) atomicOr(flags, 4);
     const int a = sn_fd[s], b = sn_c0[s + 1];
     int l = 0, r = nS;
     while (l < r) { int m = (l + r) >> 1; if (qS[m] < a) l = m + 1; else r = m; }
@@ -55,7 +59,7 @@ __global__ void k_ts_items(const int *__restrict__ ford, const int *__restrict__
     hi[s] = H0;
     const int nb = (sn_rowptr[s + 1] - sn_rowptr[s] + kSolveRB - 1) / kSolveRB;
     // panel tiles only when V_s must be recomputed (S changed)
-    const int tiles = (*same_S == 0 && H0 > L0) ? (H0 - 1) / kPT - L0 / kPT + 1 : 0;
+    const int tiles = (up_ok && *same_S == 0 && H0 > L0) ? (H0 - 1) / kPT - L0 / kPT + 1 : 0;
     int c = nb * (1 + tiles);
     cnt[k] = c;
     int p = sn_parent[s];
@@ -75,8 +79,9 @@ struct FwdArgs {
     double *V;                         // [nf][ldv] panel
     int ldv;
     double *Ug;                        // [nU][4] gradient update rows
-    double *Up;                        // [nU][ldu] panel update rows
-    int ldu;
+    double *Up;                        // [nU][ldu] panel update rows, ldu = round32(|S|)
+    const int *nS_ptr;
+    int capS;
     unsigned long long *trace;         // optional [items][4]: s|tk, dispense, ready, done (ns)
 };
 
@@ -227,6 +232,7 @@ __global__ void __launch_bounds__(kTS_NT) k_forward_solve(FwdArgs A) {
     __shared__ int src_n[kTS_W + kSolveRB], src_u[kTS_W + kSolveRB][kMaxSrc];
     const int tid = threadIdx.x;
     const int total = A.item_ptr[A.nsn];
+    const int ldu = ((min(*A.nS_ptr, A.capS) + 31) / 32) * 32;
     while (true) {
         if (tid == 0) sh_item = atomicAdd(A.ticket, 1);
         __syncthreads();
@@ -263,7 +269,7 @@ __global__ void __launch_bounds__(kTS_NT) k_forward_solve(FwdArgs A) {
         //      thread per row, so the value gathers below are independent loads.
         const double *Usrc = grad ? A.Ug : A.Up;
         double *Udst = grad ? A.Ug : A.Up;
-        const int ldsrc = grad ? 4 : A.ldu, coff = grad ? 0 : tbase;
+        const int ldsrc = grad ? 4 : ldu, coff = grad ? 0 : tbase;
         for (int q = tid; q < w + m; q += kTS_NT) {
             const int row = q < w ? q : rb + q - w;
             int cnt = 0;
@@ -472,25 +478,25 @@ void trisolve_init() {
     cudaFuncSetAttribute(k_backward_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem);
 }
 
-void launch_ts_items(const DevFactor &F, const int *qS, const int *nS_ptr, const int *same_S, int *lo,
-                     int *hi, int *cnt, int *rem, cudaStream_t st) {
+void launch_ts_items(const DevFactor &F, const int *qS, const int *nS_ptr, int capS, const int *same_S,
+                     long long up_cap, int *flags, int *lo, int *hi, int *cnt, int *rem, cudaStream_t st) {
     cudaMemsetAsync(rem, 0, sizeof(int) * F.nsn, st);
     PDI_LAUNCH(k_ts_items, (F.nsn + 255) / 256, 256, 0, st)(F.ford, F.sn_c0, F.sn_rowptr, F.sn_fd,
-                                                             F.sn_parent, F.nsn, qS, nS_ptr, same_S, lo,
-                                                             hi, cnt, rem);
+                                                             F.sn_parent, F.nsn, qS, nS_ptr, capS, same_S,
+                                                             F.nU, up_cap, flags, lo, hi, cnt, rem);
 }
 
 void launch_forward_solve(const DevFactor &F, const int *lo, const int *hi, const int *item_ptr,
                           const int *qS, int *rem, int *ticket, const double *G, double *Y, double *V,
-                          int ldv, double *Ug, double *Up, int ldu, int nsm, unsigned long long *trace,
-                          cudaStream_t st) {
+                          int ldv, double *Ug, double *Up, const int *nS_ptr, int capS, int nsm,
+                          unsigned long long *trace, cudaStream_t st) {
     FwdArgs A;
     A.sn_c0 = F.sn_c0; A.sn_rowptr = F.sn_rowptr; A.sn_parent = F.sn_parent;
     A.uoff = F.uoff; A.rc_ptr = F.rc_ptr; A.rc_src = F.rc_src;
     A.sn_valptr = F.sn_valptr; A.Q = F.Q;
     A.lo = lo; A.hi = hi; A.item_ptr = item_ptr; A.qS = qS; A.ford = F.ford; A.nsn = F.nsn;
     A.rem = rem; A.ticket = ticket; A.G = G; A.Y = Y; A.V = V; A.ldv = ldv;
-    A.Ug = Ug; A.Up = Up; A.ldu = ldu; A.trace = trace;
+    A.Ug = Ug; A.Up = Up; A.nS_ptr = nS_ptr; A.capS = capS; A.trace = trace;
     cudaMemsetAsync(ticket, 0, sizeof(int), st);
     PDI_LAUNCH(k_forward_solve, nsm, kTS_NT, kFwdSmem, st)(A);
 }

@@ -40,25 +40,25 @@ int quad_partials(const int4 *tets, const double4 *dx, const double *B, const do
 int gdx_partials(const double4 *g, const double4 *dx, const int *q2v, int nf, double *part,
                  cudaStream_t st);
 void launch_update(double4 *x, const double4 *dx, const int *q2v, int nf, const double *alpha,
-                   cudaStream_t st);
+                   const int *abort_flags, int n_flags, cudaStream_t st);
 void launch_scatter_dx(const double *z, const int *q2v, int nf, double4 *dx, cudaStream_t st);
 
 // ---- k_trisolve.cu
 constexpr int kSolveRB = 64;   // rows of a supernode per solve work item
-void launch_ts_items(const DevFactor &F, const int *qS, const int *nS_ptr, const int *same_S, int *lo,
-                     int *hi, int *cnt, int *rem, cudaStream_t st);
+void launch_ts_items(const DevFactor &F, const int *qS, const int *nS_ptr, int capS, const int *same_S,
+                     long long up_cap, int *flags, int *lo, int *hi, int *cnt, int *rem, cudaStream_t st);
 void trisolve_init();
 void launch_forward_solve(const DevFactor &F, const int *lo, const int *hi, const int *item_ptr,
                           const int *qS, int *rem, int *ticket, const double *G, double *Y, double *V,
-                          int ldv, double *Ug, double *Up, int ldu, int nsm, unsigned long long *trace,
-                          cudaStream_t st);
+                          int ldv, double *Ug, double *Up, const int *nS_ptr, int capS, int nsm,
+                          unsigned long long *trace, cudaStream_t st);
 void launch_backward_solve(const DevFactor &F, int *done, int *cnt, int *ticket, double *P, double *Z,
                            int nsm, cudaStream_t st);
 
 // ---- k_schur.cu (fused cooperative dense Schur step, a9)
 void schur_init(int device);
 int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, const int *qS,
-                 const int *lo, const int *hi, int nS, double *K, int ldk, const double *Bc, int ldb,
+                 const int *lo, const int *hi, const int *nS, int capS, double *K, int ldk, const double *Bc, int ldb,
                  double *Sh, int ldh, double *Lstore, double *T, double *U, double *yS, double *u,
                  double *t, double *Z, int *info, const int *same_S, unsigned long long *prof,
                  cudaStream_t st);
@@ -82,46 +82,45 @@ void launch_hash_query_warp(const double4 *lo, const double4 *hi, int Ns, int Nt
                             const int *tris, const int *edges, int *cnt, int *qlist, int *ovf,
                             cudaStream_t st);
 void launch_hash_emit(int Ns, int Nt, int Ne, const int *cnt, const int *off, const int *qlist,
-                      unsigned long long *out, cudaStream_t st);
-void launch_narrow(const unsigned long long *keys, int n, int is_pt, int nB, const double4 *s,
+                      unsigned long long *out, int cap, int *ccnt, int *flags, cudaStream_t st);
+// Device-resident counts: ccnt = [npt, ntot] candidate keys (PT block then EE block), acnt =
+// [n_pt, n_all] active pairs, nS = |S|; `cap` sizes the (grid-stride) launch only.
+void launch_narrow(const unsigned long long *keys, const int *ccnt, int cap, const double4 *s,
                    const int *tris, const int *edges, int Nt, int Ne, double dh2, int *flag,
                    int *type, double *d2, cudaStream_t st);
-void launch_compact_active(const unsigned long long *keys, int n, const int *flag, const int *pos,
-                           const int *type, const double *d2, int base, unsigned long long *akeys,
-                           int *atype, double *ad2, cudaStream_t st);
+void launch_compact_active(const unsigned long long *keys, const int *ccnt, int cap, const int *flag,
+                           const int *pos, const int *type, const double *d2, unsigned long long *akeys,
+                           int *atype, double *ad2, int *acnt, cudaStream_t st);
 void launch_pair_derivs(const unsigned long long *akeys, const int *atype, const double *ad2,
-                        int n_pt, int n_all, const double4 *s, const int *tris, const int *edges,
+                        const int *acnt, int cap, const double4 *s, const int *tris, const int *edges,
                         int Nt, int Ne, double dh, double kappa, double *grad, double *Hp,
                         double *dist, int *ids, double *dmax, cudaStream_t st);
-void launch_accum_grad_fx(const int *ids, int n_all, const double *grad, const double *dmax,
-                          long long *gsq, cudaStream_t st);
-void launch_accum_bc_fx(const int *ids, int n_all, const int *Wp, const int *Wc, const double *Wv,
-                        const int *v2q, const int *sidx, const double *Hp, const double *dmax,
-                        long long *Bq, long long *Bl, int ldb, cudaStream_t st);
-void launch_fx_to_double(long long *M, const long long *Ml, int ld, int n, const double *dmax,
-                         int n_pairs, cudaStream_t st);
-void launch_grad_pullback_fx(const double4 *g_el, const int *WTp, const int *WTr, const double *WTv,
-                             const long long *gsq, const double *dmax, int n_pairs, int nf, double *G,
-                             cudaStream_t st);
-void launch_mark_S(const int *ids, int n_all, const int *Wp, const int *Wc, const int *v2q,
+void launch_mark_S(const int *ids, const int *acnt, int cap, const int *Wp, const int *Wc, const int *v2q,
                    int *mark, cudaStream_t st);
 void launch_compact_S(const int *mark, const int *pos, int nf, int *qS, cudaStream_t st);
 void launch_same_S(const int *qS, const int *nS_ptr, int *qS_prev, int *nS_prev, int *same, int cap,
-                   bool enabled, cudaStream_t st);
+                   bool enabled, int *flags, cudaStream_t st);
+void launch_accum_grad_fx(const int *ids, const int *acnt, int cap, const double *grad, const double *dmax,
+                          long long *gsq, cudaStream_t st);
+void launch_accum_bc_fx(const int *ids, const int *acnt, int cap, const int *Wp, const int *Wc, const double *Wv,
+                        const int *v2q, const int *sidx, const double *Hp, const double *dmax,
+                        long long *Bq, long long *Bl, int ldb, cudaStream_t st);
+void launch_fx_to_double(long long *M, const long long *Ml, int ld, const int *nS, int capS, const double *dmax,
+                         const int *acnt, cudaStream_t st);
+void launch_grad_pullback_fx(const double4 *g_el, const int *WTp, const int *WTr, const double *WTv,
+                             const long long *gsq, const double *dmax, const int *acnt, int nf, double *G,
+                             cudaStream_t st);
 void launch_grad_pullback(const double4 *g_el, const int *WTp, const int *WTr, const double *WTv,
                           const double4 *gs, int nf, double *G, cudaStream_t st);
-void launch_zero_square(double *M, int ld, int n, cudaStream_t st);
-void launch_accd(const unsigned long long *keys, int n, int is_pt, int nB, const double4 *s,
+void launch_zero_square(double *M, int ld, const int *nS, int capS, cudaStream_t st);
+void launch_accd(const unsigned long long *keys, const int *ccnt, int cap, const double4 *s,
                  const int *tris, const int *edges, int Nt, int Ne, const double4 *ds, double s_gap,
                  int max_iters, double *amin, cudaStream_t st);
-void launch_ls_b0(const unsigned long long *keys, int n, int is_pt, int nB, const double4 *s,
-                  const int *tris, const int *edges, int Nt, int Ne, double dh, double *b0,
-                  cudaStream_t st);
-int launch_ls_trials(const unsigned long long *keys, int n, int is_pt, int nB, const double4 *s,
-                     const int *tris, const int *edges, int Nt, int Ne, const double4 *ds,
-                     double dh, const double *b0, const double *ls, int h0, double *part,
-                     int part_ld, cudaStream_t st);
-void launch_ls_decide(const double *part, int part_ld, int npart, const double *scal, double kappa,
-                      int h0, int hmax, double *ls, double *out, cudaStream_t st);
+int ls_blocks();
+void launch_ls_trials(const unsigned long long *keys, const int *ccnt, const double4 *s, const int *tris,
+                      const int *edges, int Nt, int Ne, const double4 *ds, double dh, double *b0,
+                      const double *ls, int h0, double *part, cudaStream_t st);
+void launch_ls_decide(const double *part, const double *scal, double kappa, int h0, int hmax, double *ls,
+                      double *out, cudaStream_t st);
 
 }  // namespace pdipc
