@@ -72,7 +72,7 @@ __device__ void polar_rotation(const double M[3][3], double R[3][3]) {
     const double tr2 = S[0][0] * S[0][0] + S[1][1] * S[1][1] + S[2][2] * S[2][2];
     for (int sweep = 0; sweep < 12; ++sweep) {
         double off = S[0][1] * S[0][1] + S[0][2] * S[0][2] + S[1][2] * S[1][2];
-        if (off <= 1e-34 * tr2) break;
+        if (off <= 1e-30 * tr2) break;   // off-diagonal <= 1e-15 of the diagonal (squared)
         jacobi_rot(S, V, 0, 1);
         jacobi_rot(S, V, 0, 2);
         jacobi_rot(S, V, 1, 2);
@@ -121,6 +121,67 @@ __device__ void polar_rotation(const double M[3][3], double R[3][3]) {
         for (int b = 0; b < 3; ++b) R[a][b] = u1[a] * v1[b] + u2[a] * v2[b] + u3[a] * v3[b];
 }
 
+// Rotation factor of M by the scaled Newton iteration X <- (g X + X^{-T} / g) / 2 (Higham), with
+// X^{-T} from the cofactor matrix and the Frobenius scaling g = (|X^{-1}|_F / |X|_F)^{1/2}.  For
+// det M > 0 it converges quadratically to the unique R in SO(3) with M = R U (the same R as the
+// SVD route); 4-6 iterations at the strains of the workloads, no eigen-decomposition.  Returns
+// false when det M <= 0 (the caller takes the SVD route with the reflection fix).
+__device__ __forceinline__ bool polar_newton(const double M[3][3], double R[3][3]) {
+    double X[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) X[i][j] = M[i][j];
+    bool last = false;
+    for (int it = 0; it < 16; ++it) {
+        double C[3][3];
+        C[0][0] = X[1][1] * X[2][2] - X[1][2] * X[2][1];
+        C[0][1] = X[1][2] * X[2][0] - X[1][0] * X[2][2];
+        C[0][2] = X[1][0] * X[2][1] - X[1][1] * X[2][0];
+        C[1][0] = X[0][2] * X[2][1] - X[0][1] * X[2][2];
+        C[1][1] = X[0][0] * X[2][2] - X[0][2] * X[2][0];
+        C[1][2] = X[0][1] * X[2][0] - X[0][0] * X[2][1];
+        C[2][0] = X[0][1] * X[1][2] - X[0][2] * X[1][1];
+        C[2][1] = X[0][2] * X[1][0] - X[0][0] * X[1][2];
+        C[2][2] = X[0][0] * X[1][1] - X[0][1] * X[1][0];
+        const double det = X[0][0] * C[0][0] + X[0][1] * C[0][1] + X[0][2] * C[0][2];
+        if (!(det > 0.0)) return false;          // Newton keeps the sign of det: only at it == 0
+        const double idet = 1.0 / det;
+        double a = 0.5, b = 0.5 * idet;
+        if (it < 2) {                            // Frobenius scaling for the first steps only
+            double nx = 0.0, nc = 0.0;
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+#pragma unroll
+                for (int j = 0; j < 3; ++j) {
+                    nx += X[i][j] * X[i][j];
+                    nc += C[i][j] * C[i][j];
+                }
+            const double z = sqrt(nc / nx) * idet;       // g^2, |X^-1|_F = |C|_F / det
+            a = 0.5 * sqrt(z);
+            b = 0.5 * idet * rsqrt(z);
+        }
+        double delta = 0.0;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const double v = a * X[i][j] + b * C[i][j];
+                delta += (v - X[i][j]) * (v - X[i][j]);
+                X[i][j] = v;
+            }
+        if (last) break;
+        // quadratic convergence: once the step is below ~1e-9 (relative; |X| ~ sqrt 3) the next
+        // one lands at rounding level, so take exactly one more
+        last = delta <= 3e-18;
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) R[i][j] = X[i][j];
+    return true;
+}
+
 // ------------------------------------------------------------------ a1 local step ---------
 // One thread per tet.  Reads tet (int4), x (double4 per vertex, L2-resident gather),
 // B (SoA [9][T]), A (SoA [6][T]), w; writes the per-corner elastic forces
@@ -155,7 +216,7 @@ __global__ void __launch_bounds__(128) k_local_step(
     for (int a = 0; a < 3; ++a)
 #pragma unroll
         for (int b = 0; b < 3; ++b) M[a][b] = F[a][0] * A[0][b] + F[a][1] * A[1][b] + F[a][2] * A[2][b];
-    polar_rotation(M, R);
+    if (!polar_newton(M, R)) polar_rotation(M, R);   // det <= 0: SVD route, reflection fix
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
