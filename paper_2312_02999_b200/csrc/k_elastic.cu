@@ -187,7 +187,7 @@ __device__ __forceinline__ bool polar_newton(const double M[3][3], double R[3][3
 // B (SoA [9][T]), A (SoA [6][T]), w; writes the per-corner elastic forces
 // f_{i,c} = w_i (F_i - P_i) g_{i,c} as fc[T][4][3] (coalesced 96 B per tet) and, when
 // p != nullptr, p_i = vec(R_i A_i) (SoA [9][T]) for the parity hook.
-__global__ void __launch_bounds__(128) k_local_step(
+__global__ void __launch_bounds__(128, 5) k_local_step(
     const int4 *__restrict__ tets, const double4 *__restrict__ x, const double *__restrict__ B,
     const double *__restrict__ A6, const double *__restrict__ w, int T, double *__restrict__ fc,
     double *__restrict__ p) {
@@ -251,19 +251,33 @@ __global__ void __launch_bounds__(128) k_local_step(
 // ------------------------------------------------------------------ a2 gather -------------
 // g_el[q] = sum over incidences (t, c) of vertex q2v[q] of f_{t,c}: transpose-CSR gather in
 // factor order, deterministic, no atomics.  Output double4 [nf] (w = 0).
-__global__ void k_gather_elastic(const int *__restrict__ inc_ptr, const int *__restrict__ inc,
-                                 const double *__restrict__ fc, int nf, double4 *__restrict__ g) {
-    int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= nf) return;
+// 8 lanes per free vertex: lane l sums the incident corner forces l, l+8, ... of the vertex's
+// transpose-incidence list (independent loads in flight), then a fixed xor tree over the 8
+// lanes (deterministic order).
+constexpr int kGatherLanes = 8;
+__global__ void __launch_bounds__(256) k_gather_elastic(const int *__restrict__ inc_ptr, const int *__restrict__ inc,
+                                                        const double *__restrict__ fc, int nf,
+                                                        double4 *__restrict__ g) {
+    const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int q = gid / kGatherLanes, l = gid % kGatherLanes;
     double gx = 0, gy = 0, gz = 0;
-    for (int k = __ldg(inc_ptr + q); k < __ldg(inc_ptr + q + 1); ++k) {
-        int tc = __ldg(inc + k);
-        const double *f = fc + 12 * (size_t)(tc >> 2) + 3 * (tc & 3);
-        gx += f[0];
-        gy += f[1];
-        gz += f[2];
+    if (q < nf) {
+        const int k0 = __ldg(inc_ptr + q), k1 = __ldg(inc_ptr + q + 1);
+        for (int k = k0 + l; k < k1; k += kGatherLanes) {
+            const int tc = __ldg(inc + k);
+            const double *f = fc + 12 * (size_t)(tc >> 2) + 3 * (tc & 3);
+            gx += f[0];
+            gy += f[1];
+            gz += f[2];
+        }
     }
-    g[q] = make_double4(gx, gy, gz, 0.0);
+#pragma unroll
+    for (int o = kGatherLanes / 2; o > 0; o >>= 1) {
+        gx += __shfl_xor_sync(0xffffffffu, gx, o);
+        gy += __shfl_xor_sync(0xffffffffu, gy, o);
+        gz += __shfl_xor_sync(0xffffffffu, gz, o);
+    }
+    if (q < nf && l == 0) g[q] = make_double4(gx, gy, gz, 0.0);
 }
 
 // ------------------------------------------------------------------ a3 s = W x ------------
@@ -377,7 +391,8 @@ void launch_local_step(const int4 *tets, const double4 *x, const double *B, cons
 }
 void launch_gather_elastic(const int *inc_ptr, const int *inc, const double *fc, int nf,
                            double4 *g, cudaStream_t st) {
-    PDI_LAUNCH(k_gather_elastic, (nf + 127) / 128, 128, 0, st)(inc_ptr, inc, fc, nf, g);
+    PDI_LAUNCH(k_gather_elastic, (int)(((long long)nf * kGatherLanes + 255) / 256), 256, 0, st)(inc_ptr, inc, fc,
+                                                                                             nf, g);
 }
 void launch_surface(const int *Wp, const int *Wc, const double *Wv, const double4 *x, int Ns,
                     double4 *s, cudaStream_t st) {
