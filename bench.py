@@ -42,6 +42,7 @@ def _args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--c5", default="1M", help="pure-PD box size for the local-step HBM sweep ('' to skip)")
     return ap.parse_args()
 
 
@@ -52,6 +53,21 @@ def _peaks():
         return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
     except Exception:
         return 6650.0, 1590.0, "fallback"
+
+
+def _c5_local_step(size, hbm):
+    """Local-step and gather HBM GB/s on the pure-PD box of BASELINE.json configs[4] (the metric's
+    'local-step HBM GB/s' at a size where the step is bandwidth-relevant; C2 is latency-bound)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("c5_sweep", os.path.join(ROOT, "tools", "c5_sweep.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    r = mod.run(size)
+    return {"workload": f"C5 pure-PD box {size} ({r['tets']} tets, {r['verts']} verts), 20-iteration steps",
+            "local_step_GBps": r["local_step_GBps"], "local_step_frac": r["local_step_GBps"] / hbm,
+            "gather_GBps": r["gather_GBps"], "gather_frac": r["gather_GBps"] / hbm,
+            "pure_pd_iters_per_s": r["iters_per_s"], "peak_GBps": hbm,
+            "bytes_per_tet": "local 240 (+32 per vertex), gather 28 per incidence + 40 per free vertex"}
 
 
 def _sm_max_mhz():
@@ -315,6 +331,9 @@ def run_ours(a):
     cpu = None
     if world == 1 and not a.no_cpu_baseline:
         cpu = cpu_baseline(x_start, start, a.cpu_seconds)
+    c5 = None
+    if world == 1 and a.c5:
+        c5 = _c5_local_step(a.c5, hbm)
     line = {
         "metric": "PD+IPC iterations/s", "value": value, "unit": "iters/s", "n_gpus": world,
         "steps": K, "warmup": W, "ms_per_step": max_ms / K, "higher_is_better": True,
@@ -331,6 +350,7 @@ def run_ours(a):
                                                  "per-step CUDA events)",
                    "parallelism": f"dp{world} over independent sequences"},
         "roofline": rl, "roofline_local_step": rl_local,
+        "local_step_c5": c5,
         "cpu_baseline": cpu,
         "e2e": ({"value": iters_total / (max_e2e / 1000.0), "unit": "iters/s",
                  "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"]} if e2e else None),

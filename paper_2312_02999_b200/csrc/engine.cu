@@ -79,6 +79,11 @@ static int bits_for(unsigned long long v) {   // bits to represent values < v (v
 }
 
 struct Seq {
+    // captured CUDA graph of one iteration (asynchronous part), rebuilt when buffers move
+    cudaGraphExec_t exec = nullptr;
+    unsigned graph_key = ~0u;
+    long long graph_launches = 0;
+    bool kt_used[16] = {};
     DBuf<double4> x;
     DBuf<double> A6;
     DBuf<double> p;
@@ -102,6 +107,13 @@ static const char *kKernelNames[K_NUM] = {"local_step", "gather", "broad_phase",
                                           "dense_schur", "backward_solve", "ccd", "line_search",
                                           "dense.syrk", "dense.inverse", "dense.potrf",
                                           "dense.solve"};
+// During stream capture an event must be recorded as an external event node (a plain record
+// would only mark a capture dependency); outside capture a plain record.
+static bool g_capturing = false;
+static void record_event(cudaEvent_t e, cudaStream_t st) {
+    CK(g_capturing ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal) : cudaEventRecord(e, st));
+}
+
 struct KTimer {
     bool on = false;
     cudaEvent_t ev[K_NUM][2];
@@ -114,9 +126,9 @@ struct KTimer {
     void destroy() {
         for (int k = 0; k < K_NUM; ++k) { cudaEventDestroy(ev[k][0]); cudaEventDestroy(ev[k][1]); }
     }
-    void start(int k, cudaStream_t st) { if (on) CK(cudaEventRecord(ev[k][0], st)); }
+    void start(int k, cudaStream_t st) { if (on) record_event(ev[k][0], st); }
     void stop(int k, cudaStream_t st) {
-        if (on) { CK(cudaEventRecord(ev[k][1], st)); used[k] = true; }
+        if (on) { record_event(ev[k][1], st); used[k] = true; }
     }
     void collect() {     // after a stream synchronize
         for (int k = 0; k < K_NUM; ++k)
@@ -174,6 +186,8 @@ struct pd_ipc {
     DBuf<int> mark, spos, qS;
     DBuf<double> lspart;    // line-search partial sums [8][ls_blocks()]
     bool force_sort = false;  // next broad phases take the sort path (after a hash overflow)
+    bool graphs = true;       // replay each iteration as a CUDA graph (PDIPC_NO_GRAPH=1: off)
+    unsigned buf_epoch = 0;   // bumped whenever a buffer the iteration uses is reallocated
     int nS_host = 0;
     DBuf<int> ts_lo, ts_hi, ts_cnt, ts_ptr, ts_rem, ts_done, ticket;
     DBuf<double> V, K, Bc, Sh, U, Tt, yS, rhs, u, tv, part, b0, Lstore;
@@ -216,6 +230,7 @@ static void ensure_pair_buffers(pd_ipc *h, size_t ncand) {
 // grow every candidate-capacity buffer to at least n keys (rare; synchronising)
 static void grow_candidates(pd_ipc *h, size_t n) {
     if (n <= h->cand.n) return;
+    ++h->buf_epoch;
     h->cand.exact(n);
     h->cand_tmp.exact(n);
     ensure_pair_buffers(h, n);
@@ -408,7 +423,7 @@ static void broad_phase_sort(pd_ipc *h, const double4 *ds, double infl, int *ccn
 // device and every launch is sized by a capacity.  Returns false if a capacity or hash overflow
 // was flagged: x was not updated, the caller redoes the iteration after the buffers were grown
 // (or with the sort broad phase).
-static bool iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
+static void enqueue_iteration(pd_ipc *h, Seq &q) {
     cudaStream_t st = h->st;
     const int T = h->T, nf = h->nf, Ns = h->Ns, Nt = h->Nt, Ne = h->Ne;
     const int cap = (int)h->cand.n;
@@ -416,7 +431,7 @@ static bool iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
     int *acnt = h->dint.p + D_ACNT, *ccnt = h->dint.p + D_CCNT;
     CK(cudaMemsetAsync(h->dint.p + D_INFO, 0, 4 * sizeof(int), st));   // info, capacity, hash flags
     CK(cudaMemsetAsync(acnt, 0, 2 * sizeof(int), st));
-    CK(cudaEventRecord(ev[0], st));
+    record_event(ev[0], st);
     // ---------------- Misc: a1 local step + a2 gather
     KTimer &kt = h->kt;
     kt.start(K_LOCAL, st);
@@ -426,7 +441,7 @@ static bool iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
     kt.start(K_GATHER, st);
     launch_gather_elastic(h->inc_ptr.p, h->inc.p, h->fc.p, nf, h->g_el.p, st);
     kt.stop(K_GATHER, st);
-    CK(cudaEventRecord(ev[1], st));
+    record_event(ev[1], st);
     // ---------------- IPC
     int *nS_dev = h->spos.p + nf;     // exclusive scan total of the S marks
     double *dmax = h->dscal.p + 11;
@@ -480,7 +495,7 @@ static bool iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
         CK(cudaMemsetAsync(h->dint.p + D_STAT, 0, 2 * sizeof(int), st));
         launch_grad_pullback(h->g_el.p, h->WTp.p, h->WTr.p, h->WTv.p, nullptr, nf, h->G.p, st);
     }
-    CK(cudaEventRecord(ev[2], st));
+    record_event(ev[2], st);
     // ---------------- G-Step
     const DevFactor &F = h->F;
     CK(cudaMemsetAsync(h->ticket.p, 0, 2 * sizeof(int), st));
@@ -513,7 +528,7 @@ static bool iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
     kt.stop(K_BWD, st);
     CK(cudaMemsetAsync(h->dx.p, 0, sizeof(double4) * h->n, st));
     launch_scatter_dx(h->Z.p, h->q2v.p, nf, h->dx.p, st);
-    CK(cudaEventRecord(ev[3], st));
+    record_event(ev[3], st);
     // ---------------- CCD
     double *amin = h->dscal.p + 1;
     double *ls = h->dscal.p + 2, *ls_out = h->dscal.p + 5, *scal = h->dscal.p + 9;
@@ -528,7 +543,7 @@ static bool iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
         CK(cudaMemsetAsync(ccnt, 0, 2 * sizeof(int), st));
     }
     kt.stop(K_CCD, st);
-    CK(cudaEventRecord(ev[4], st));
+    record_event(ev[4], st);
     // ---------------- LS
     kt.start(K_LS, st);
     {
@@ -550,7 +565,61 @@ static bool iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
         launch_update(q.x.p, h->dx.p, h->q2v.p, nf, ls_out, h->dint.p + D_CAP, 3, st);
     }
     kt.stop(K_LS, st);
-    CK(cudaEventRecord(ev[5], st));
+    record_event(ev[5], st);
+}
+
+// Run one iteration: replay the captured CUDA graph of the asynchronous part when possible (the
+// whole iteration is launch-configuration static: every size lives on the device), else enqueue
+// it stream-ordered; then the one host round trip (stats, flags).
+static bool iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
+    cudaStream_t st = h->st;
+    const int nf = h->nf;
+    const DevFactor &F = h->F;
+    const int cap = (int)h->cand.n;
+    auto &ev = h->tm.ev;
+    KTimer &kt = h->kt;
+    int *nS_dev = h->spos.p + nf;
+    const bool graph = h->graphs && !h->debug && !h->trace_file && !h->force_sort;
+    const unsigned key = (h->buf_epoch << 1) | (kt.on ? 1u : 0u);
+    if (graph && (!q.exec || q.graph_key != key)) {
+        if (q.exec) {
+            cudaGraphExecDestroy(q.exec);
+            q.exec = nullptr;
+        }
+        cudaGraph_t g = nullptr;
+        const long long l0 = launch_count();
+        bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+        if (ok) {
+            g_capturing = true;
+            try {
+                enqueue_iteration(h, q);
+            } catch (const CudaError &) {
+                ok = false;
+            }
+            g_capturing = false;
+            ok = (cudaStreamEndCapture(st, &g) == cudaSuccess) && ok;
+        }
+        if (ok) ok = cudaGraphInstantiate(&q.exec, g, 0) == cudaSuccess;
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        const long long n_captured = launch_count() - l0;
+        add_launches(-n_captured);                     // counted on every replay instead
+        if (ok) {
+            q.graph_launches = n_captured;
+            q.graph_key = key;
+            for (int k = 0; k < K_NUM; ++k) q.kt_used[k] = kt.used[k];
+        } else {
+            q.exec = nullptr;
+            h->graphs = false;                         // capture unsupported: stream path from now on
+        }
+    }
+    if (graph && q.exec) {
+        CK(cudaGraphLaunch(q.exec, st));
+        add_launches(q.graph_launches);
+        for (int k = 0; k < K_NUM; ++k) kt.used[k] = q.kt_used[k];
+    } else {
+        enqueue_iteration(h, q);
+    }
     // ---------------- the one host round trip of the iteration: stats and flags
     double sc[13];
     int di[12];
@@ -568,7 +637,10 @@ static bool iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
     if (di[D_CAP] & 2) throw CudaError("contact vertex set exceeds capacity", PD_IPC_E_CAPACITY);
     if ((di[D_CAP] & 5) || di[D_HOVF] || di[D_HOVF + 1]) {        // redo with grown buffers
         if (di[D_CAP] & 1) grow_candidates(h, 2 * (size_t)cap);
-        if (di[D_CAP] & 4) h->Up.exact((size_t)std::max(1, F.nU) * (((nS + 31) / 32) * 32 + 64));
+        if (di[D_CAP] & 4) {
+            h->Up.exact((size_t)std::max(1, F.nU) * (((nS + 31) / 32) * 32 + 64));
+            ++h->buf_epoch;
+        }
         if (di[D_HOVF] || di[D_HOVF + 1]) h->force_sort = true;
         kt.collect();
         return false;
@@ -686,6 +758,7 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
         h->tm.init();
         h->kt.init();
+        if (const char *ng = std::getenv("PDIPC_NO_GRAPH")) h->graphs = !(ng[0] == '1');
         if (const char *tp = std::getenv("PDIPC_TRACE")) {
             h->trace_file = std::fopen(tp, "wb");
             h->schur_file = std::fopen((std::string(tp) + ".schur").c_str(), "wb");
@@ -972,6 +1045,8 @@ void pd_ipc_destroy(pd_ipc *h) {
     cudaSetDevice(h->device);
     cudaDeviceSynchronize();
     // DBuf members free in their own scope via release; explicit for clarity
+    for (auto &sq : h->seqs)
+        if (sq->exec) cudaGraphExecDestroy(sq->exec);
     h->tm.destroy();
     h->kt.destroy();
     if (h->trace_file) std::fclose(h->trace_file);

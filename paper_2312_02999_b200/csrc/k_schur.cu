@@ -632,6 +632,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
 
 constexpr int kSchurSmem = 4 * TB * TS * (int)sizeof(double);
 static int g_schur_grid = 0;
+static double *g_kpart = nullptr;   // split-K partial tiles, grid x 1152 doubles (allocated at init)
 
 void schur_init(int device) {
     cudaFuncSetAttribute(k_schur_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, kSchurSmem);
@@ -639,6 +640,7 @@ void schur_init(int device) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_schur_coop, NT, kSchurSmem);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
     g_schur_grid = std::max(1, per_sm) * nsm;
+    if (!g_kpart) cudaMalloc(&g_kpart, (size_t)g_schur_grid * 1152 * sizeof(double));
 }
 
 int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, const int *qS,
@@ -651,9 +653,7 @@ int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, 
     a.sn_parent = F.sn_parent; a.lo = lo; a.hi = hi; a.nsn = F.nsn; a.nf = F.nf; a.nS_ptr = nS; a.capS = capS;
     a.K = K; a.ldk = ldk; a.Bc = Bc; a.ldb = ldb; a.Sh = Sh; a.ldh = ldh; a.Lstore = Lstore;
     a.T = T; a.U = U; a.yS = yS; a.u = u; a.t = t; a.Z = Z; a.info = info; a.same = same_S; a.prof = prof;
-    static double *kpart = nullptr;                 // grid x 1152 doubles, allocated once
-    if (!kpart) cudaMalloc(&kpart, (size_t)g_schur_grid * 1152 * sizeof(double));
-    a.Kpart = kpart;
+    a.Kpart = g_kpart;
     void *args[] = {&a};
     note_launch();
     return (int)cudaLaunchCooperativeKernel((const void *)k_schur_coop, dim3(g_schur_grid), dim3(NT),

@@ -25,6 +25,7 @@ struct DevFactor {
 };
 
 long long launch_count();   // prims.cu: kernels launched so far (PDI_LAUNCH)
+void add_launches(long long n);   // graph replays account their captured launches
 
 // ---- k_elastic.cu
 void launch_set_double(double *p, double v, cudaStream_t st);

@@ -9,6 +9,7 @@ namespace pdipc {
 static long long g_launches = 0;     // handles are single-threaded (pd_ipc.h)
 void note_launch() { ++g_launches; }
 long long launch_count() { return g_launches; }
+void add_launches(long long n) { g_launches += n; }
 
 // ----------------------------------------------------------------------- exclusive scan ----
 constexpr int kScanNT = 1024, kScanIPT = 4, kScanTile = kScanNT * kScanIPT;
