@@ -154,7 +154,8 @@ int pd_ipc_debug_factor_solve(const pd_ipc_mesh *mesh, const double *rest_pos, c
                               double *x, int64_t *stats);
 
 /* Device timing of kernel groups (CUDA events on the library stream around each group, every
- * iteration; on = 1 enables).  pd_ipc_kernel_times copies the accumulated milliseconds and
+ * iteration; on = 1 enables all groups, on < 0 only the groups in the bit mask -on (bit k =
+ * group k), on = 0 disables).  pd_ipc_kernel_times copies the accumulated milliseconds and
  * launch counts of the K groups (returns K) into ms[K], counts[K] (either may be NULL) and
  * resets them if reset != 0; pd_ipc_kernel_name(i) names group i (0 = "local_step"). */
 int pd_ipc_set_timing(pd_ipc *h, int32_t on);

@@ -78,12 +78,16 @@ static int bits_for(unsigned long long v) {   // bits to represent values < v (v
     return std::max(b, 1);
 }
 
+constexpr int kMaxBatch = 32;   // iterations enqueued (or captured) before one host round trip
+
 struct Seq {
     // captured CUDA graph of one iteration (asynchronous part), rebuilt when buffers move
     cudaGraphExec_t exec = nullptr;
     unsigned graph_key = ~0u;
     long long graph_launches = 0;
-    bool kt_used[16] = {};
+    bool kt_used[kMaxBatch][16] = {};
+    int graph_batch = 0;
+    unsigned graph_mask = 0;
     DBuf<double4> x;
     DBuf<double> A6;
     DBuf<double> p;
@@ -93,10 +97,10 @@ struct Seq {
     std::vector<double> ghat, gel, dx, proj;
 };
 
-struct StageTimer {
-    cudaEvent_t ev[6];
-    void init() { for (auto &e : ev) CK(cudaEventCreate(&e)); }
-    void destroy() { for (auto &e : ev) cudaEventDestroy(e); }
+struct StageTimer {             // Table-1 stage boundaries, one event set per iteration slot
+    cudaEvent_t ev[kMaxBatch][6];
+    void init() { for (auto &a : ev) for (auto &e : a) CK(cudaEventCreate(&e)); }
+    void destroy() { for (auto &a : ev) for (auto &e : a) cudaEventDestroy(e); }
 };
 
 // Per-kernel-group device timing (CUDA events on the library stream), for the roofline report.
@@ -116,29 +120,34 @@ static void record_event(cudaEvent_t e, cudaStream_t st) {
 
 struct KTimer {
     bool on = false;
-    cudaEvent_t ev[K_NUM][2];
-    bool used[K_NUM] = {};
+    unsigned mask = ~0u;                // timed groups (bit k = group k)
+    int slot = 0;                       // iteration slot of the batch being enqueued
+    cudaEvent_t ev[kMaxBatch][K_NUM][2];
+    bool used[kMaxBatch][K_NUM] = {};
     double ms[K_NUM] = {};
     long long cnt[K_NUM] = {};
     void init() {
-        for (int k = 0; k < K_NUM; ++k) { CK(cudaEventCreate(&ev[k][0])); CK(cudaEventCreate(&ev[k][1])); }
+        for (auto &a : ev) for (auto &b : a) { CK(cudaEventCreate(&b[0])); CK(cudaEventCreate(&b[1])); }
     }
     void destroy() {
-        for (int k = 0; k < K_NUM; ++k) { cudaEventDestroy(ev[k][0]); cudaEventDestroy(ev[k][1]); }
+        for (auto &a : ev) for (auto &b : a) { cudaEventDestroy(b[0]); cudaEventDestroy(b[1]); }
     }
-    void start(int k, cudaStream_t st) { if (on) record_event(ev[k][0], st); }
+    void start(int k, cudaStream_t st) { if (on && (mask >> k & 1)) record_event(ev[slot][k][0], st); }
     void stop(int k, cudaStream_t st) {
-        if (on) { record_event(ev[k][1], st); used[k] = true; }
+        if (on && (mask >> k & 1)) { record_event(ev[slot][k][1], st); used[slot][k] = true; }
     }
-    void collect() {     // after a stream synchronize
-        for (int k = 0; k < K_NUM; ++k)
-            if (used[k]) {
-                float f;
-                CK(cudaEventElapsedTime(&f, ev[k][0], ev[k][1]));
-                ms[k] += f;
-                cnt[k] += 1;
-                used[k] = false;
-            }
+    void collect(int n_slots) {     // after a stream synchronize: the first n_slots iterations
+        for (int i = 0; i < kMaxBatch; ++i)
+            for (int k = 0; k < K_NUM; ++k)
+                if (used[i][k]) {
+                    if (i < n_slots) {
+                        float f;
+                        CK(cudaEventElapsedTime(&f, ev[i][k][0], ev[i][k][1]));
+                        ms[k] += f;
+                        cnt[k] += 1;
+                    }
+                    used[i][k] = false;
+                }
     }
 };
 
@@ -312,7 +321,9 @@ enum : int {
     D_HOVF = 6,      // [6] static, [7] swept hash overflow (outlier box / table) -> sort path
     D_SPREV = 8,     // [8] |S| of the S that V_s, K_s, Sigma_s belong to, [9] same-S flag
     D_STAT = 10,     // [10] npt, [11] ntot of the static phase (stats)
-    D_SORT = 16,     // [16..17] scratch counters of the sort path
+    D_ABORT = 12,    // [12] sticky: an iteration of the batch failed, [13] its index, [14] why
+    D_REUSED = 15,   // iterations of the batch that reused V_s, K_s, Sigma_s
+    D_SORT = 16,     // [16..18] scratch counters of the sort path
 };
 
 static void broad_phase_sort(pd_ipc *h, const double4 *ds, double infl, int *ccnt);
@@ -423,11 +434,12 @@ static void broad_phase_sort(pd_ipc *h, const double4 *ds, double infl, int *ccn
 // device and every launch is sized by a capacity.  Returns false if a capacity or hash overflow
 // was flagged: x was not updated, the caller redoes the iteration after the buffers were grown
 // (or with the sort broad phase).
-static void enqueue_iteration(pd_ipc *h, Seq &q) {
+static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
     cudaStream_t st = h->st;
+    h->kt.slot = slot;
     const int T = h->T, nf = h->nf, Ns = h->Ns, Nt = h->Nt, Ne = h->Ne;
     const int cap = (int)h->cand.n;
-    auto &ev = h->tm.ev;
+    auto &ev = h->tm.ev[slot];
     int *acnt = h->dint.p + D_ACNT, *ccnt = h->dint.p + D_CCNT;
     CK(cudaMemsetAsync(h->dint.p + D_INFO, 0, 4 * sizeof(int), st));   // info, capacity, hash flags
     CK(cudaMemsetAsync(acnt, 0, 2 * sizeof(int), st));
@@ -474,7 +486,7 @@ static void enqueue_iteration(pd_ipc *h, Seq &q) {
         // V_s, K_s, Sigma_s depend on S (and the constant factor) only: reuse them while S is
         // bit-identical to the S they were computed for
         launch_same_S(h->qS.p, nS_dev, h->qS_prev.p, h->dint.p + D_SPREV, h->dint.p + D_SPREV + 1, h->capS,
-                      h->opt.no_sigma_reuse == 0, h->dint.p + D_CAP, st);
+                      h->opt.no_sigma_reuse == 0, h->dint.p + D_CAP, h->dint.p + D_REUSED, st);
         // gradient pull-back: deterministic fixed-point accumulation on the surface, then W^T
         CK(cudaMemsetAsync(h->gsq.p, 0, sizeof(long long) * 6 * Ns, st));
         launch_accum_grad_fx(h->ids.p, acnt, cap, h->grad.p, dmax, h->gsq.p, st);
@@ -562,26 +574,33 @@ static void enqueue_iteration(pd_ipc *h, Seq &q) {
                 CK(cudaMemsetAsync(h->lspart.p, 0, sizeof(double) * 8 * ls_blocks(), st));
             launch_ls_decide(h->lspart.p, scal, h->kappa, h0, hmax, ls, ls_out, st);
         }
-        launch_update(q.x.p, h->dx.p, h->q2v.p, nf, ls_out, h->dint.p + D_CAP, 3, st);
+        launch_update(q.x.p, h->dx.p, h->q2v.p, nf, ls_out, h->dint.p + D_INFO, h->dint.p + D_ABORT, slot, st);
     }
     kt.stop(K_LS, st);
     record_event(ev[5], st);
 }
 
-// Run one iteration: replay the captured CUDA graph of the asynchronous part when possible (the
-// whole iteration is launch-configuration static: every size lives on the device), else enqueue
-// it stream-ordered; then the one host round trip (stats, flags).
-static bool iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
+// Run a batch of k <= kMaxBatch iterations with ONE host round trip: replay the captured CUDA
+// graph of the k iterations when possible (every launch configuration is static: all sizes live
+// on the device), else enqueue them stream-ordered.  A failing iteration (capacity / hash
+// overflow, Cholesky breakdown) raises a sticky device flag: it and every later iteration of the
+// batch leave x untouched, so x is the last accepted iterate.  Returns the number of iterations
+// applied; the caller grows buffers (done here) and runs the rest.
+static int run_batch(pd_ipc *h, Seq &q, int k, double ms[6]) {
     cudaStream_t st = h->st;
     const int nf = h->nf;
     const DevFactor &F = h->F;
     const int cap = (int)h->cand.n;
-    auto &ev = h->tm.ev;
     KTimer &kt = h->kt;
     int *nS_dev = h->spos.p + nf;
     const bool graph = h->graphs && !h->debug && !h->trace_file && !h->force_sort;
     const unsigned key = (h->buf_epoch << 1) | (kt.on ? 1u : 0u);
-    if (graph && (!q.exec || q.graph_key != key)) {
+    const unsigned key_mask = kt.on ? kt.mask : 0u;
+    auto enqueue_batch = [&]() {
+        CK(cudaMemsetAsync(h->dint.p + D_ABORT, 0, 4 * sizeof(int), st));   // abort, index, why, reused
+        for (int i = 0; i < k; ++i) enqueue_iteration(h, q, i);
+    };
+    if (graph && (!q.exec || q.graph_key != key || q.graph_batch != k || q.graph_mask != key_mask)) {
         if (q.exec) {
             cudaGraphExecDestroy(q.exec);
             q.exec = nullptr;
@@ -592,7 +611,7 @@ static bool iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
         if (ok) {
             g_capturing = true;
             try {
-                enqueue_iteration(h, q);
+                enqueue_batch();
             } catch (const CudaError &) {
                 ok = false;
             }
@@ -607,7 +626,10 @@ static bool iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
         if (ok) {
             q.graph_launches = n_captured;
             q.graph_key = key;
-            for (int k = 0; k < K_NUM; ++k) q.kt_used[k] = kt.used[k];
+            q.graph_batch = k;
+            q.graph_mask = key_mask;
+            for (int i = 0; i < kMaxBatch; ++i)
+                for (int j = 0; j < K_NUM; ++j) q.kt_used[i][j] = kt.used[i][j];
         } else {
             q.exec = nullptr;
             h->graphs = false;                         // capture unsupported: stream path from now on
@@ -616,48 +638,51 @@ static bool iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
     if (graph && q.exec) {
         CK(cudaGraphLaunch(q.exec, st));
         add_launches(q.graph_launches);
-        for (int k = 0; k < K_NUM; ++k) kt.used[k] = q.kt_used[k];
+        for (int i = 0; i < kMaxBatch; ++i)
+            for (int j = 0; j < K_NUM; ++j) kt.used[i][j] = q.kt_used[i][j];
     } else {
-        enqueue_iteration(h, q);
+        enqueue_batch();
     }
-    // ---------------- the one host round trip of the iteration: stats and flags
+    // ---------------- the one host round trip of the batch: stats and flags
     double sc[13];
-    int di[12];
+    int di[16];
     CK(cudaMemcpyAsync(sc, h->dscal.p, sizeof(sc), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(di, h->dint.p, sizeof(di), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&h->nS_host, nS_dev, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    const int fault_flag = [&] {
-        int f = 0;
-        CK(cudaMemcpy(&f, h->ticket.p + 1, sizeof(int), cudaMemcpyDeviceToHost));
-        return f;
-    }();
-    if (fault_flag) throw CudaError("triangular solve dependency wait timed out", PD_IPC_E_CUDA);
+    int fault = 0;
+    CK(cudaMemcpy(&fault, h->ticket.p + 1, sizeof(int), cudaMemcpyDeviceToHost));
+    if (fault) throw CudaError("triangular solve dependency wait timed out", PD_IPC_E_CUDA);
     const int nS = h->nS_host;
-    if (di[D_CAP] & 2) throw CudaError("contact vertex set exceeds capacity", PD_IPC_E_CAPACITY);
-    if ((di[D_CAP] & 5) || di[D_HOVF] || di[D_HOVF + 1]) {        // redo with grown buffers
-        if (di[D_CAP] & 1) grow_candidates(h, 2 * (size_t)cap);
-        if (di[D_CAP] & 4) {
-            h->Up.exact((size_t)std::max(1, F.nU) * (((nS + 31) / 32) * 32 + 64));
+    const int applied = di[D_ABORT] ? di[D_ABORT + 1] : k;
+    q.stats.sigma_reused += di[D_REUSED];
+    for (int i = 0; i < applied; ++i) {
+        auto &ev = h->tm.ev[i];
+        for (int s2 = 0; s2 < 5; ++s2) {
+            float f;
+            CK(cudaEventElapsedTime(&f, ev[s2], ev[s2 + 1]));
+            ms[s2 == 0 ? 4 : s2 - 1] += f;     // Misc, IPC, G, CCD, LS
+        }
+        float tot;
+        CK(cudaEventElapsedTime(&tot, ev[0], ev[5]));
+        ms[5] += tot;
+    }
+    kt.collect(applied);
+    if (di[D_ABORT]) {                           // why: 1 cand, 2 |S|, 4 Up, 8/16 hash, 32 info
+        const int why = di[D_ABORT + 2];
+        if (why & 2) throw CudaError("contact vertex set exceeds capacity", PD_IPC_E_CAPACITY);
+        if (why & 32) throw CudaError("dense Cholesky: matrix not SPD", PD_IPC_E_NOT_SPD);
+        if (why & 1) grow_candidates(h, 2 * (size_t)cap);
+        if (why & 4) {
+            h->Up.exact((size_t)std::max(1, F.nU) * (((std::min(nS, h->capS) + 31) / 32) * 32 + 64));
             ++h->buf_epoch;
         }
-        if (di[D_HOVF] || di[D_HOVF + 1]) h->force_sort = true;
-        kt.collect();
-        return false;
+        if (why & 24) h->force_sort = true;      // the next iteration takes the sort broad phase
+        return applied;
     }
     h->force_sort = false;
-    if (di[D_INFO]) throw CudaError("dense Cholesky: matrix not SPD", PD_IPC_E_NOT_SPD);
-    q.stats.sigma_reused += nS > 0 ? di[D_SPREV + 1] : 0;
+    // stats of the last iteration
     const int n_pt = di[D_ACNT], n_all = di[D_ACNT + 1];
-    for (int k = 0; k < 5; ++k) {
-        float f;
-        CK(cudaEventElapsedTime(&f, ev[k], ev[k + 1]));
-        ms[k == 0 ? 4 : k - 1] += f;       // Misc, IPC, G, CCD, LS
-    }
-    float tot;
-    CK(cudaEventElapsedTime(&tot, ev[0], ev[5]));
-    ms[5] += tot;
-    kt.collect();
     pd_ipc_stats &S = q.stats;
     S.n_cand = di[D_STAT + 1];
     S.n_active = n_all;
@@ -675,8 +700,7 @@ static bool iterate(pd_ipc *h, Seq &q, bool last, double ms[6]) {
         throw CudaError("non-finite value in step", PD_IPC_E_NONFINITE);
     if (h->debug) debug_capture(h, q, n_pt, n_all - n_pt, nS);
     dump_traces(h, nS);
-    (void)last;
-    return true;
+    return applied;
 }
 
 // ------------------------------------------------------------------ ABI -------------------
@@ -1007,10 +1031,13 @@ int pd_ipc_step(pd_ipc *h, const double *A_next, int32_t n_iters, pd_ipc_stats *
         for (auto &sq : h->seqs) {
             double ms[6] = {0, 0, 0, 0, 0, 0};
             sq->stats.sigma_reused = 0;
-            for (int it = 0; it < n_iters; ++it) {
-                int tries = 0;
-                while (!iterate(h, *sq, it == n_iters - 1, ms))   // capacity grown: redo
-                    if (++tries > 8) throw CudaError("capacity growth did not converge", PD_IPC_E_CAPACITY);
+            int done = 0, tries = 0;
+            while (done < n_iters) {
+                const int k = std::min(n_iters - done, kMaxBatch);
+                const int applied = run_batch(h, *sq, k, ms);
+                done += applied;
+                if (applied < k && ++tries > 8)            // buffers grown / sort path: redo the rest
+                    throw CudaError("capacity growth did not converge", PD_IPC_E_CAPACITY);
             }
             sq->stats.iters = n_iters;
             for (int k = 0; k < 6; ++k) sq->stats.ms[k] = ms[k];
@@ -1166,6 +1193,7 @@ const char *pd_ipc_build_info(void) {
 int pd_ipc_set_timing(pd_ipc *h, int32_t on) {
     if (!h) return fail(nullptr, PD_IPC_E_ARG, "NULL handle");
     h->kt.on = on != 0;
+    h->kt.mask = on < 0 ? (unsigned)(-(long long)on) : ~0u;
     return PD_IPC_OK;
 }
 

@@ -714,7 +714,7 @@ __global__ void k_compact_S(const int *__restrict__ mark, const int *__restrict_
 __global__ void __launch_bounds__(1024) k_same_S(const int *__restrict__ qS, const int *__restrict__ nS_ptr,
                                                  int *__restrict__ qS_prev, int *__restrict__ nS_prev,
                                                  int *__restrict__ same, int enabled, int cap,
-                                                 int *__restrict__ flags) {
+                                                 int *__restrict__ flags, int *__restrict__ reused) {
     const int nS = min(*nS_ptr, cap), np = *nS_prev;
     if (threadIdx.x == 0 && *nS_ptr > cap) atomicOr(flags, 2);   // |S| beyond the dense buffers
     int eq = enabled && nS > 0 && nS == np;
@@ -724,6 +724,7 @@ __global__ void __launch_bounds__(1024) k_same_S(const int *__restrict__ qS, con
     if (threadIdx.x == 0) {
         *nS_prev = nS;
         *same = eq;
+        if (eq) *reused += 1;
     }
 }
 
@@ -1090,8 +1091,9 @@ void launch_mark_S(const int *ids, const int *acnt, int cap, const int *Wp, cons
     PDI_LAUNCH(k_mark_S, grid_for(4 * cap, 256, 148 * 8), 256, 0, st)(ids, acnt, Wp, Wc, v2q, mark);
 }
 void launch_same_S(const int *qS, const int *nS_ptr, int *qS_prev, int *nS_prev, int *same, int cap,
-                   bool enabled, int *flags, cudaStream_t st) {
-    PDI_LAUNCH(k_same_S, 1, 1024, 0, st)(qS, nS_ptr, qS_prev, nS_prev, same, enabled ? 1 : 0, cap, flags);
+                   bool enabled, int *flags, int *reused, cudaStream_t st) {
+    PDI_LAUNCH(k_same_S, 1, 1024, 0, st)(qS, nS_ptr, qS_prev, nS_prev, same, enabled ? 1 : 0, cap, flags,
+                                         reused);
 }
 void launch_compact_S(const int *mark, const int *pos, int nf, int *qS, cudaStream_t st) {
     PDI_LAUNCH(k_compact_S, (nf + 255) / 256, 256, 0, st)(mark, pos, nf, qS);

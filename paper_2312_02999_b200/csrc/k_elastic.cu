@@ -349,18 +349,26 @@ __global__ void __launch_bounds__(256) k_gdx_partials(const double4 *__restrict_
     if (threadIdx.x == 0) part[blockIdx.x] = v;
 }
 
-// x[v] += alpha dx[v] for free v
-// x_F += alpha dx, unless a capacity / overflow flag of this iteration is raised (the host then
-// grows the buffer and redoes the iteration from the unchanged x)
+// x_F += alpha dx, unless this iteration raised a flag (flags = [Cholesky info, capacity bits,
+// static hash overflow, swept hash overflow]) or an earlier iteration of the batch did (abort =
+// [sticky, iteration index, why]); the first failing iteration records itself.
 __global__ void k_update(double4 *__restrict__ x, const double4 *__restrict__ dx,
                          const int *__restrict__ q2v, int nf, const double *__restrict__ alpha,
-                         const int *__restrict__ abort_flags, int n_flags) {
+                         const int *__restrict__ flags, int *__restrict__ abort, int it) {
     int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nf) return;
-    for (int f = 0; f < n_flags; ++f)
-        if (abort_flags[f]) return;
-    int v = q2v[q];
-    double a = *alpha;
+    const int bad = flags[0] | flags[1] | flags[2] | flags[3];
+    if (bad) {
+        if (q == 0 && abort[0] == 0) {
+            abort[0] = 1;
+            abort[1] = it;
+            abort[2] = flags[1] | (flags[2] ? 8 : 0) | (flags[3] ? 16 : 0) | (flags[0] ? 32 : 0);
+        }
+        return;
+    }
+    if (abort[0]) return;
+    const int v = q2v[q];
+    const double a = *alpha;
     double4 xv = x[v], d = dx[v];
     xv.x += a * d.x;
     xv.y += a * d.y;
@@ -411,8 +419,8 @@ int gdx_partials(const double4 *g, const double4 *dx, const int *q2v, int nf, do
     return nb;
 }
 void launch_update(double4 *x, const double4 *dx, const int *q2v, int nf, const double *alpha,
-                   const int *abort_flags, int n_flags, cudaStream_t st) {
-    PDI_LAUNCH(k_update, (nf + 255) / 256, 256, 0, st)(x, dx, q2v, nf, alpha, abort_flags, n_flags);
+                   const int *flags, int *abort, int it, cudaStream_t st) {
+    PDI_LAUNCH(k_update, (nf + 255) / 256, 256, 0, st)(x, dx, q2v, nf, alpha, flags, abort, it);
 }
 void launch_scatter_dx(const double *z, const int *q2v, int nf, double4 *dx, cudaStream_t st) {
     PDI_LAUNCH(k_scatter_dx, (nf + 255) / 256, 256, 0, st)(z, q2v, nf, dx);

@@ -41,7 +41,7 @@ int quad_partials(const int4 *tets, const double4 *dx, const double *B, const do
 int gdx_partials(const double4 *g, const double4 *dx, const int *q2v, int nf, double *part,
                  cudaStream_t st);
 void launch_update(double4 *x, const double4 *dx, const int *q2v, int nf, const double *alpha,
-                   const int *abort_flags, int n_flags, cudaStream_t st);
+                   const int *flags, int *abort, int it, cudaStream_t st);
 void launch_scatter_dx(const double *z, const int *q2v, int nf, double4 *dx, cudaStream_t st);
 
 // ---- k_trisolve.cu
@@ -100,7 +100,7 @@ void launch_mark_S(const int *ids, const int *acnt, int cap, const int *Wp, cons
                    int *mark, cudaStream_t st);
 void launch_compact_S(const int *mark, const int *pos, int nf, int *qS, cudaStream_t st);
 void launch_same_S(const int *qS, const int *nS_ptr, int *qS_prev, int *nS_prev, int *same, int cap,
-                   bool enabled, int *flags, cudaStream_t st);
+                   bool enabled, int *flags, int *reused, cudaStream_t st);
 void launch_accum_grad_fx(const int *ids, const int *acnt, int cap, const double *grad, const double *dmax,
                           long long *gsq, cudaStream_t st);
 void launch_accum_bc_fx(const int *ids, const int *acnt, int cap, const int *Wp, const int *Wc, const double *Wv,

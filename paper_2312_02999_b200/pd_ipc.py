@@ -96,7 +96,14 @@ EXPORTED = ["pd_ipc_create", "pd_ipc_step", "pd_ipc_positions", "pd_ipc_destroy"
             "pd_ipc_kernel_times", "pd_ipc_kernel_name", "pd_ipc_launch_count"]
 
 
-def set_timing(h, on=True):
+def set_timing(h, on=True, groups=None):
+    """Enable the CUDA-event timers of all kernel groups, or only of `groups` (names)."""
+    if groups is not None and on:
+        mask = 0
+        for g in groups:
+            mask |= 1 << [lib.pd_ipc_kernel_name(i).decode() for i in range(32)].index(g)
+        _check(lib.pd_ipc_set_timing(h, -mask), h)
+        return
     _check(lib.pd_ipc_set_timing(h, int(on)), h)
 
 
