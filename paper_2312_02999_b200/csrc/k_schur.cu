@@ -24,6 +24,8 @@ namespace pdipc {
 constexpr int TB = 64;          // tile
 constexpr int TS = 68;          // smem tile stride (DMMA-friendly)
 constexpr int NT = 256;         // threads per CTA
+constexpr int kPW = 4;          // P3 panel width in tiles (trailing update once per panel)
+constexpr int kPWMinTiles = 24; // ... for systems of at least this many tiles
 constexpr int kP4Single = 1536;  // P4 in one CTA (no grid barriers) up to this size (<= TB * TS)
 
 __device__ __forceinline__ void dmma_884(double &d0, double &d1, double a, double b) {
@@ -113,6 +115,32 @@ __device__ __forceinline__ void tile_xyt(double *C, const double *X, const doubl
         C[r * TS + c + 1] = acc[nb][1];
     }
     __syncthreads();
+}
+
+// ld_tile without the wait: the caller commits / waits (cp.async groups)
+__device__ __forceinline__ void ld_tile_async(double *S, const double *src, int ld, int rows, int cols) {
+    for (int e = threadIdx.x; e < TB * TB; e += NT) {
+        int r = e >> 6, c = e & 63;
+        if (r < rows && c < cols) {
+            const unsigned s = (unsigned)__cvta_generic_to_shared(S + r * TS + c);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src + (size_t)r * ld + c));
+        } else {
+            S[r * TS + c] = 0.0;
+        }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+}
+
+// acc (warp w: rows 8w..8w+7, all 64 columns, fragment layout of tile_xyt) -= X Y^T on DMMA
+__device__ __forceinline__ void tile_sub_xyt_regs(double (&acc)[8][2], const double *X, const double *Y) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int gr = lane >> 2, gc = lane & 3;
+#pragma unroll 4
+    for (int k4 = 0; k4 < TB / 4; ++k4) {
+        const double av = -X[(8 * w + gr) * TS + 4 * k4 + gc];
+#pragma unroll
+        for (int nb = 0; nb < 8; ++nb) dmma_884(acc[nb][0], acc[nb][1], av, Y[(8 * nb + gr) * TS + 4 * k4 + gc]);
+    }
 }
 
 // One thread: Cholesky of the 8x8 diagonal block at S (stride TS, lower part read) in
@@ -512,40 +540,93 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
     if (bid == 0 && tid == 0) a.Sh[(size_t)m * a.ldh + m] = 1.0;
     GSYNC();
     // ------------------------------------------------ P3: Cholesky of the augmented matrix
+    // Right-looking in panels of kPW tile columns: inside a panel, per tile column k: diagonal
+    // tile factor + inverse (CTA 0), L_ik = A_ik Li_k^T, update of the panel's later columns;
+    // then ONE trailing update of everything right of the panel with the panel's kPW tile
+    // columns (k streamed through shared memory, accumulator in registers): the trailing
+    // matrix is read and written once per panel instead of once per tile column.
     const int nt = (ma + TB - 1) / TB;
-    for (int k = 0; k < nt; ++k) {
-        const int kc0 = k * TB, kn = min(TB, ma - kc0);
-        if (bid == 0) {
-            ld_tile(T0, a.Sh + (size_t)kc0 * a.ldh + kc0, a.ldh, kn, kn);
-            __syncthreads();
-            tile_chol64(T0, T1, kn, m - kc0, a.info);
-            st_tile(T0, a.Sh + (size_t)kc0 * a.ldh + kc0, a.ldh, kn, kn);
-            for (int e = tid; e < TB * TB; e += NT) a.Lstore[(size_t)k * TB * TB + e] = T1[(e >> 6) * TS + (e & 63)];
+    const int pw = nt >= kPWMinTiles ? kPW : 1;      // small systems: one tile column per step
+    for (int p0 = 0; p0 < nt; p0 += pw) {
+        const int p1 = min(nt, p0 + pw);
+        for (int k = p0; k < p1; ++k) {
+            const int kc0 = k * TB, kn = min(TB, ma - kc0);
+            if (bid == 0) {
+                ld_tile(T0, a.Sh + (size_t)kc0 * a.ldh + kc0, a.ldh, kn, kn);
+                __syncthreads();
+                tile_chol64(T0, T1, kn, m - kc0, a.info);
+                st_tile(T0, a.Sh + (size_t)kc0 * a.ldh + kc0, a.ldh, kn, kn);
+                for (int e = tid; e < TB * TB; e += NT) a.Lstore[(size_t)k * TB * TB + e] = T1[(e >> 6) * TS + (e & 63)];
+            }
+            GSYNC();
+            for (int b = bid; b < nt - k - 1; b += G) {      // L_ik = A_ik Li^T
+                const int ti = k + 1 + b, r0 = ti * TB, rows = min(TB, ma - r0);
+                ld_tile(T0, a.Sh + (size_t)r0 * a.ldh + kc0, a.ldh, rows, kn);
+                ld_tile(T1, a.Lstore + (size_t)k * TB * TB, TB, TB, TB);
+                __syncthreads();
+                tile_xyt(T2, T0, T1, 1.0, false);
+                st_tile(T2, a.Sh + (size_t)r0 * a.ldh + kc0, a.ldh, rows, kn);
+            }
+            GSYNC();
+            const int nj = p1 - k - 1;                       // panel columns right of k
+            if (nj > 0) {
+                const int nrow = nt - k - 1;
+                for (int b = bid; b < nrow * nj; b += G) {   // A_ij -= L_ik L_jk^T, k < j < p1, i >= j
+                    const int tj = k + 1 + b % nj, ti = k + 1 + b / nj;
+                    if (ti < tj) continue;
+                    const int r0 = ti * TB, c0 = tj * TB, rows = min(TB, ma - r0), cols = min(TB, ma - c0);
+                    ld_tile(T0, a.Sh + (size_t)r0 * a.ldh + kc0, a.ldh, rows, kn);
+                    ld_tile(T1, a.Sh + (size_t)c0 * a.ldh + kc0, a.ldh, cols, kn);
+                    ld_tile(T2, a.Sh + (size_t)r0 * a.ldh + c0, a.ldh, rows, cols);
+                    __syncthreads();
+                    tile_xyt(T2, T0, T1, -1.0, true);
+                    st_tile(T2, a.Sh + (size_t)r0 * a.ldh + c0, a.ldh, rows, cols);
+                }
+                GSYNC();
+            }
         }
-        GSYNC();
-        for (int b = bid; b < nt - k - 1; b += G) {      // L_ik = A_ik Li^T
-            const int ti = k + 1 + b, r0 = ti * TB, rows = min(TB, ma - r0);
-            ld_tile(T0, a.Sh + (size_t)r0 * a.ldh + kc0, a.ldh, rows, kn);
-            ld_tile(T1, a.Lstore + (size_t)k * TB * TB, TB, TB, TB);
-            __syncthreads();
-            tile_xyt(T2, T0, T1, 1.0, false);
-            st_tile(T2, a.Sh + (size_t)r0 * a.ldh + kc0, a.ldh, rows, kn);
+        // trailing update with the whole panel: A_ij -= sum_{k in panel} L_ik L_jk^T, p1 <= j <= i
+        const int rr = nt - p1;
+        if (rr > 0) {
+            const int gr = lane >> 2, gc = lane & 3;
+            for (int b = bid; b < rr * (rr + 1) / 2; b += G) {
+                int i = 0, bb = b;
+                while (bb >= rr - i) { bb -= rr - i; ++i; }
+                const int tj = p1 + i, ti = tj + bb;
+                const int r0 = ti * TB, c0 = tj * TB, rows = min(TB, ma - r0), cols = min(TB, ma - c0);
+                double acc[8][2];
+#pragma unroll
+                for (int nb = 0; nb < 8; ++nb) {
+                    const int r = 8 * wid + gr, c = 8 * nb + 2 * gc;
+                    acc[nb][0] = (r < rows && c < cols) ? a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c] : 0.0;
+                    acc[nb][1] = (r < rows && c + 1 < cols) ? a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c + 1] : 0.0;
+                }
+                // k-chunks double-buffered: (T0, T1) and (T2, T3)
+                ld_tile_async(T0, a.Sh + (size_t)r0 * a.ldh + p0 * TB, a.ldh, rows, TB);
+                ld_tile_async(T1, a.Sh + (size_t)c0 * a.ldh + p0 * TB, a.ldh, cols, TB);
+                for (int k = p0; k < p1; ++k) {
+                    double *X = ((k - p0) & 1) ? T2 : T0, *Y = ((k - p0) & 1) ? T3 : T1;
+                    if (k + 1 < p1) {
+                        double *Xn = ((k - p0) & 1) ? T0 : T2, *Yn = ((k - p0) & 1) ? T1 : T3;
+                        ld_tile_async(Xn, a.Sh + (size_t)r0 * a.ldh + (k + 1) * TB, a.ldh, rows, TB);
+                        ld_tile_async(Yn, a.Sh + (size_t)c0 * a.ldh + (k + 1) * TB, a.ldh, cols, TB);
+                        asm volatile("cp.async.wait_group 2;\n" ::);
+                    } else {
+                        asm volatile("cp.async.wait_group 0;\n" ::);
+                    }
+                    __syncthreads();
+                    tile_sub_xyt_regs(acc, X, Y);
+                    __syncthreads();
+                }
+#pragma unroll
+                for (int nb = 0; nb < 8; ++nb) {
+                    const int r = 8 * wid + gr, c = 8 * nb + 2 * gc;
+                    if (r < rows && c < cols) a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c] = acc[nb][0];
+                    if (r < rows && c + 1 < cols) a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c + 1] = acc[nb][1];
+                }
+            }
+            GSYNC();
         }
-        GSYNC();
-        const int rr = nt - k - 1;
-        for (int b = bid; b < rr * (rr + 1) / 2; b += G) {   // A_ij -= L_ik L_jk^T, k < j <= i
-            int i = 0, bb = b;
-            while (bb >= rr - i) { bb -= rr - i; ++i; }
-            const int tj = k + 1 + i, ti = tj + bb;
-            const int r0 = ti * TB, c0 = tj * TB, rows = min(TB, ma - r0), cols = min(TB, ma - c0);
-            ld_tile(T0, a.Sh + (size_t)r0 * a.ldh + kc0, a.ldh, rows, kn);
-            ld_tile(T1, a.Sh + (size_t)c0 * a.ldh + kc0, a.ldh, cols, kn);
-            ld_tile(T2, a.Sh + (size_t)r0 * a.ldh + c0, a.ldh, rows, cols);
-            __syncthreads();
-            tile_xyt(T2, T0, T1, -1.0, true);
-            st_tile(T2, a.Sh + (size_t)r0 * a.ldh + c0, a.ldh, rows, cols);
-        }
-        GSYNC();
     }
     // ------------------------------------------------ P4: u = C^{-T} y, y = row m of the factor
     // right-looking on C^T: u_k = Li_k^T y_k, then y_j -= (C_kj)^T u_k for j < k
