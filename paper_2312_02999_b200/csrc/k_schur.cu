@@ -26,6 +26,7 @@ constexpr int TS = 68;          // smem tile stride (DMMA-friendly)
 constexpr int NT = 256;         // threads per CTA
 constexpr int kPW = 4;          // P3 panel width in tiles (trailing update once per panel)
 constexpr int kPWMinTiles = 24; // ... for systems of at least this many tiles
+constexpr int kLPTiles = kPWMinTiles;   // small-system P3: panel tiles per step
 constexpr int kP4Single = 1536;  // P4 in one CTA (no grid barriers) up to this size (<= TB * TS)
 
 __device__ __forceinline__ void dmma_884(double &d0, double &d1, double a, double b) {
@@ -50,6 +51,7 @@ struct SchurArgs {
     double *Sh;                 // [3capS+1][ldh] augmented Sigma-hat
     int ldh;
     double *Lstore;             // [nt][64][64] inverses of the diagonal factor tiles
+    double *LP;                 // [2][kLPTiles][64][64] panel scratch of the small-system P3
     double *T;                  // 64x64 scratch (sweep pivot inverse)
     double *U;                  // sweep panel [capS+64][64]
     double *yS, *u, *t;         // [3capS]
@@ -546,8 +548,73 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
     // columns (k streamed through shared memory, accumulator in registers): the trailing
     // matrix is read and written once per panel instead of once per tile column.
     const int nt = (ma + TB - 1) / TB;
-    const int pw = nt >= kPWMinTiles ? kPW : 1;      // small systems: one tile column per step
-    for (int p0 = 0; p0 < nt; p0 += pw) {
+    const int pw = nt >= kPWMinTiles ? kPW : nt + 1;  // small systems: look-ahead path below
+    if (nt < kPWMinTiles) {
+        // Small systems (latency-bound): ONE grid barrier per tile column.  Step k: every CTA
+        // updates one tile (i, j), k < j <= i, recomputing the panel tiles it needs
+        // (L_ik = A_ik Li_k^T) itself; CTA 0 takes (k+1, k+1) and then factors it (look-ahead).
+        // L_ik go to a ping-pong scratch (A_ik is still read by other CTAs in the step) and are
+        // written into the factor one step later.
+        if (bid == 0) {
+            ld_tile(T0, a.Sh, a.ldh, min(TB, ma), min(TB, ma));
+            __syncthreads();
+            tile_chol64(T0, T1, min(TB, ma), m, a.info);
+            st_tile(T0, a.Sh, a.ldh, min(TB, ma), min(TB, ma));
+            for (int e = tid; e < TB * TB; e += NT) a.Lstore[e] = T1[(e >> 6) * TS + (e & 63)];
+        }
+        GSYNC();
+        for (int k = 0; k < nt; ++k) {
+            const int kc0 = k * TB, kn = min(TB, ma - kc0);
+            double *LPk = a.LP + (size_t)(k & 1) * kLPTiles * TB * TB;      // L_ik of this step
+            const double *LPp = a.LP + (size_t)((k + 1) & 1) * kLPTiles * TB * TB;   // previous
+            const int rr = nt - k - 1;
+            const int ntile = rr * (rr + 1) / 2;
+            // write back the previous step's L_{i,k-1} (no CTA reads column k-1 any more)
+            if (k > 0)
+                for (size_t e = (size_t)bid * NT + tid; e < (size_t)(nt - k) * TB * TB; e += (size_t)G * NT) {
+                    const int t = (int)(e / (TB * TB)), q = (int)(e % (TB * TB)), r = q >> 6, c = q & 63;
+                    const int i = k + t, r0 = i * TB;
+                    if (r0 + r < ma && (k - 1) * TB + c < ma)
+                        a.Sh[(size_t)(r0 + r) * a.ldh + (k - 1) * TB + c] = LPp[(size_t)t * TB * TB + q];
+                }
+            for (int b = bid; b < ntile; b += G) {
+                // b == 0 -> the look-ahead tile (k+1, k+1) on CTA 0
+                int i = 0, bb = b;
+                while (bb >= rr - i) { bb -= rr - i; ++i; }
+                const int tj = k + 1 + i, ti = tj + bb;
+                const int r0 = ti * TB, c0 = tj * TB, rows = min(TB, ma - r0), cols = min(TB, ma - c0);
+                // L_ik (T2), L_jk (T3)
+                ld_tile(T0, a.Sh + (size_t)r0 * a.ldh + kc0, a.ldh, rows, kn);
+                ld_tile(T1, a.Lstore + (size_t)k * TB * TB, TB, TB, TB);
+                __syncthreads();
+                tile_xyt(T2, T0, T1, 1.0, false);
+                double *Ljk = T2;
+                if (tj != ti) {
+                    ld_tile(T0, a.Sh + (size_t)c0 * a.ldh + kc0, a.ldh, cols, kn);
+                    __syncthreads();
+                    tile_xyt(T3, T0, T1, 1.0, false);
+                    Ljk = T3;
+                } else {                                     // the diagonal-tile CTA keeps L_ik
+                    for (int e = tid; e < TB * TB; e += NT)
+                        LPk[(size_t)(ti - k - 1) * TB * TB + e] = T2[(e >> 6) * TS + (e & 63)];
+                }
+                ld_tile(T0, a.Sh + (size_t)r0 * a.ldh + c0, a.ldh, rows, cols);
+                __syncthreads();
+                tile_xyt(T0, T2, Ljk, -1.0, true);
+                if (b == 0) {                                // look-ahead: factor tile k+1 now
+                    tile_chol64(T0, T1, rows, m - r0, a.info);
+                    st_tile(T0, a.Sh + (size_t)r0 * a.ldh + c0, a.ldh, rows, cols);
+                    for (int e = tid; e < TB * TB; e += NT)
+                        a.Lstore[(size_t)(k + 1) * TB * TB + e] = T1[(e >> 6) * TS + (e & 63)];
+                } else {
+                    st_tile(T0, a.Sh + (size_t)r0 * a.ldh + c0, a.ldh, rows, cols);
+                }
+                __syncthreads();
+            }
+            GSYNC();
+        }
+    }
+    for (int p0 = 0; nt >= kPWMinTiles && p0 < nt; p0 += pw) {
         const int p1 = min(nt, p0 + pw);
         for (int k = p0; k < p1; ++k) {
             const int kc0 = k * TB, kn = min(TB, ma - kc0);
@@ -714,6 +781,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
 constexpr int kSchurSmem = 4 * TB * TS * (int)sizeof(double);
 static int g_schur_grid = 0;
 static double *g_kpart = nullptr;   // split-K partial tiles, grid x 1152 doubles (allocated at init)
+static double *g_lp = nullptr;      // small-system P3 panel scratch
 
 void schur_init(int device) {
     cudaFuncSetAttribute(k_schur_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, kSchurSmem);
@@ -722,6 +790,7 @@ void schur_init(int device) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
     g_schur_grid = std::max(1, per_sm) * nsm;
     if (!g_kpart) cudaMalloc(&g_kpart, (size_t)g_schur_grid * 1152 * sizeof(double));
+    if (!g_lp) cudaMalloc(&g_lp, (size_t)2 * kLPTiles * TB * TB * sizeof(double));
 }
 
 int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, const int *qS,
@@ -735,6 +804,7 @@ int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, 
     a.K = K; a.ldk = ldk; a.Bc = Bc; a.ldb = ldb; a.Sh = Sh; a.ldh = ldh; a.Lstore = Lstore;
     a.T = T; a.U = U; a.yS = yS; a.u = u; a.t = t; a.Z = Z; a.info = info; a.same = same_S; a.prof = prof;
     a.Kpart = g_kpart;
+    a.LP = g_lp;
     void *args[] = {&a};
     note_launch();
     return (int)cudaLaunchCooperativeKernel((const void *)k_schur_coop, dim3(g_schur_grid), dim3(NT),
