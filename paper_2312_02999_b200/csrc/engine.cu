@@ -179,7 +179,7 @@ struct pd_ipc {
     DBuf<long long> f_valptr, f_dinv_ptr;
     DBuf<double> f_L, f_dinv, Ug, Up, Yw, bw_P;
     DBuf<int2> f_bw_items, f_rc_src;
-    DBuf<int> f_bw_pbase, bw_cnt, f_ford, qS_prev;
+    DBuf<int> f_bw_pbase, bw_cnt, f_ford, qS_prev, f_path_ptr, f_path_sn;
     DBuf<int> f_uoff, f_urow_sn, f_rc_ptr, f_rc_idx, f_urel, f_ch_ptr, f_ch;
     // sequences
     std::vector<std::unique_ptr<Seq>> seqs;
@@ -528,7 +528,7 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
         }
         CK((cudaError_t)launch_schur(F, h->V.p, h->ldv, h->Yw.p, h->qS.p, h->ts_lo.p, h->ts_hi.p, nS_dev,
                                      h->capS, h->K.p, h->capS, h->Bc.p, 3 * h->capS, h->Sh.p, h->ldh,
-                                     h->Lstore.p, h->Tt.p, h->U.p, h->yS.p, h->u.p, h->tv.p, h->Z.p,
+                                     h->Lstore.p, h->Tt.p, h->U.p, h->yS.p, h->rhs.p, h->u.p, h->tv.p, h->Z.p,
                                      h->dint.p + D_INFO, h->dint.p + D_SPREV + 1,
                                      h->trace_file ? h->sprof.p : nullptr, st));
     } else {
@@ -835,6 +835,15 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             h->f_valptr.upload(vp.data(), vp.size());
         }
         h->f_L.upload(f.Q.data(), f.Q.size());
+        {   // etree path of every supernode (itself first, then its ancestors): y_S column walks
+            std::vector<int> pp(f.nsn + 1, 0), ps;
+            for (int s = 0; s < f.nsn; ++s) {
+                for (int t = s; t >= 0; t = f.sn_parent[t]) ps.push_back(t);
+                pp[s + 1] = (int)ps.size();
+            }
+            h->f_path_ptr.upload(pp.data(), pp.size());
+            h->f_path_sn.upload(ps.data(), ps.size());
+        }
         {   // Item dispatch orders (list scheduling on the elimination tree).  Forward: by
             // decreasing cost-to-root (a child always precedes its parent), so the items on the
             // longest chains start first.  Backward: by decreasing height (a parent precedes
@@ -897,6 +906,7 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         F.sn_c0 = h->f_c0.p; F.sn_rowptr = h->f_rowptr.p; F.sn_rows = h->f_rows.p; F.sn_parent = h->f_parent.p;
         F.sn_valptr = h->f_valptr.p; F.Q = h->f_L.p;
         F.bw_items = h->f_bw_items.p; F.bw_pbase = h->f_bw_pbase.p; F.ford = h->f_ford.p;
+        F.path_ptr = h->f_path_ptr.p; F.path_sn = h->f_path_sn.p;
         F.seg_ptr = h->f_seg_ptr.p; F.seg_d = h->f_seg_d.p; F.seg_klo = h->f_seg_klo.p; F.seg_khi = h->f_seg_khi.p;
         F.sn_fd = h->f_fd.p; F.col2sn = h->f_col2sn.p;
         // contact capacity: S is a subset of the free vertices in the W support (n2)
@@ -1086,7 +1096,7 @@ void pd_ipc_destroy(pd_ipc *h) {
     rel(h->Wp); rel(h->Wc); rel(h->WTp); rel(h->WTr); rel(h->tris); rel(h->edges); rel(h->Wv); rel(h->WTv);
     rel(h->f_c0); rel(h->f_rowptr); rel(h->f_rows); rel(h->f_parent); rel(h->f_seg_ptr); rel(h->f_seg_d);
     rel(h->f_seg_klo); rel(h->f_seg_khi); rel(h->f_fd); rel(h->f_col2sn); rel(h->f_valptr); rel(h->f_L);
-    rel(h->f_dinv_ptr); rel(h->f_dinv); rel(h->Ug); rel(h->Up); rel(h->Yw); rel(h->bw_P); rel(h->f_bw_items); rel(h->f_ford); rel(h->qS_prev); rel(h->f_rc_src); rel(h->f_bw_pbase); rel(h->bw_cnt); rel(h->f_uoff); rel(h->f_urow_sn);
+    rel(h->f_dinv_ptr); rel(h->f_dinv); rel(h->Ug); rel(h->Up); rel(h->Yw); rel(h->bw_P); rel(h->f_bw_items); rel(h->f_ford); rel(h->f_path_ptr); rel(h->f_path_sn); rel(h->qS_prev); rel(h->f_rc_src); rel(h->f_bw_pbase); rel(h->bw_cnt); rel(h->f_uoff); rel(h->f_urow_sn);
     rel(h->f_rc_ptr); rel(h->f_rc_idx); rel(h->f_urel); rel(h->f_ch_ptr); rel(h->f_ch);
     for (auto &s : h->seqs) { rel(s->x); rel(s->A6); rel(s->p); }
     rel(h->fc); rel(h->G); rel(h->Z); rel(h->A9stage); rel(h->g_el); rel(h->s); rel(h->ds); rel(h->dx);

@@ -27,7 +27,6 @@ constexpr int NT = 256;         // threads per CTA
 constexpr int kPW = 4;          // P3 panel width in tiles (trailing update once per panel)
 constexpr int kPWMinTiles = 24; // ... for systems of at least this many tiles
 constexpr int kLPTiles = kPWMinTiles;   // small-system P3: panel tiles per step
-constexpr int kP4Single = 1536;  // P4 in one CTA (no grid barriers) up to this size (<= TB * TS)
 
 __device__ __forceinline__ void dmma_884(double &d0, double &d1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -40,7 +39,7 @@ struct SchurArgs {
     const double *V;
     int ldv;
     const double *G;            // w [nf][4]
-    const int *qS, *col2sn, *sn_c0, *sn_parent, *lo, *hi;
+    const int *qS, *col2sn, *sn_c0, *sn_parent, *lo, *hi, *path_ptr, *path_sn;
     int nsn, nf, capS;
     const int *nS_ptr;          // |S| (device); clamped to capS
     // dense buffers
@@ -54,7 +53,7 @@ struct SchurArgs {
     double *LP;                 // [2][kLPTiles][64][64] panel scratch of the small-system P3
     double *T;                  // 64x64 scratch (sweep pivot inverse)
     double *U;                  // sweep panel [capS+64][64]
-    double *yS, *u, *t;         // [3capS]
+    double *yS, *y, *u, *t;     // [3capS]
     double *Kpart;              // [grid][1152] split-K partial tiles (+ y_S partials)
     double *Z;                  // [nf][4]
     int *info;
@@ -318,13 +317,30 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
     // accumulates on DMMA.  Diagonal tiles also accumulate y_S for their columns.  Split partials
     // are reduced in a fixed order (deterministic).
     const bool reuse = *a.same != 0;                 // uniform across the grid
+    // y_S[c] = -sum over the etree path of q_c's supernode of V[r][c] w[r]: one CTA per column,
+    // the path rows come from a static per-supernode list (independent loads), fixed-order
+    // block reduction: the same bits whether or not K is recomputed
+    for (int c = bid; c < nS; c += G) {
+        const int s0 = a.col2sn[a.qS[c]];
+        double acc[3] = {0, 0, 0};
+        for (int pi = a.path_ptr[s0]; pi < a.path_ptr[s0 + 1]; ++pi) {
+            const int sn = a.path_sn[pi];
+            for (int r = a.sn_c0[sn] + tid; r < a.sn_c0[sn + 1]; r += NT) {
+                const double v = a.V[(size_t)r * a.ldv + c];
+                acc[0] += v * a.G[(size_t)r * 4 + 0];
+                acc[1] += v * a.G[(size_t)r * 4 + 1];
+                acc[2] += v * a.G[(size_t)r * 4 + 2];
+            }
+        }
+        for (int i = 0; i < 3; ++i) {
+            const double tsum = block_sum<NT>(acc[i], T3);
+            if (tid == 0) a.yS[3 * c + i] = -tsum;
+        }
+    }
     const int ntk = (nS + 31) / 32;
-    // with reuse only the diagonal tiles run (they carry y_S); K keeps -Sigma_s
-    const int ntiles = reuse ? ntk : ntk * (ntk + 1) / 2;
-    // the split (hence the summation order of y_S) must not depend on reuse: bit-identical
+    const int ntiles = reuse ? 0 : ntk * (ntk + 1) / 2;   // K keeps -Sigma_s when S is unchanged
     const int nsplit = max(1, min(16, G / max(ntk * (ntk + 1) / 2, 1)));
     auto tile_of = [&](int b, int &ti, int &tj) {
-        if (reuse) { ti = tj = b; return; }
         int rem = b;
         ti = 0;
         while (rem > ti) { rem -= ti + 1; ++ti; }
@@ -333,7 +349,6 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
     {
         typedef double Chunk[32][36];
         Chunk *Va = reinterpret_cast<Chunk *>(T0), *Vb = reinterpret_cast<Chunk *>(T1);   // [2] each
-        double (*Wc)[32][4] = reinterpret_cast<double (*)[32][4]>(T2);                   // [2]
         const int gr = lane >> 2, gc = lane & 3;
         for (int bs = bid; bs < ntiles * nsplit; bs += G) {
             const int b = bs / nsplit, split = bs % nsplit;
@@ -379,15 +394,9 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
                         }
                     }
                 }
-                if (diag)
-                    for (int e = tid; e < 32 * 4; e += NT) {
-                        const int rr = e >> 2, i = e & 3;
-                        Wc[buf][rr][i] = (rr < nrb && i < 3) ? a.G[(size_t)(rb + rr) * 4 + i] : 0.0;
-                    }
                 asm volatile("cp.async.commit_group;\n" ::);
             };
             double acc[2][2] = {{0, 0}, {0, 0}};
-            double ya = 0.0;                         // y_S partial: thread (c = tid / 3, i = tid % 3)
             int sn = -1, rb = 0;
             bool have = next_chunk(sn, rb);
             if (have) stage(sn, rb, 0);
@@ -411,11 +420,6 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
                     for (int k4 = 0; k4 < 8; ++k4)
                         dmma_884(acc[j][0], acc[j][1], A[4 * k4 + gc][8 * ta + gr], B[4 * k4 + gc][8 * tb + gr]);
                 }
-                if (diag && tid < 96) {
-                    const int c = tid / 3, i = tid % 3;
-#pragma unroll 8
-                    for (int rr = 0; rr < 32; ++rr) ya += A[rr][c] * Wc[buf][rr][i];
-                }
                 __syncthreads();
                 sn = sn2;
                 rb = rb2;
@@ -427,8 +431,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
             for (int j = 0; j < 2; ++j) {
                 const int t = wid + 8 * j, ta = t >> 2, tb = t & 3;
                 const int r = 8 * ta + gr, c = 8 * tb + 2 * gc;
-                if (reuse) {
-                } else if (nsplit == 1) {
+                if (nsplit == 1) {
                     for (int q = 0; q < 2; ++q) {
                         const int R = ia + r, Cc = ja + c + q;
                         if (R < nS && Cc < nS && Cc <= R) {
@@ -441,35 +444,20 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
                     dst[r * 32 + c + 1] = acc[j][1];
                 }
             }
-            if (diag && tid < 96) {
-                const int c = tid / 3, i = tid % 3;
-                if (nsplit == 1) {
-                    if (ia + c < nS) a.yS[3 * (ia + c) + i] = -ya;
-                } else {
-                    dst[1024 + tid] = ya;
-                }
-            }
         }
     }
-    if (nsplit > 1) {
+    if (ntiles > 0 && nsplit > 1) {
         GSYNC();
-        for (int e = bid * NT + tid; e < ntiles * 1120; e += G * NT) {
-            const int b = e / 1120, q = e % 1120;
+        for (int e = bid * NT + tid; e < ntiles * 1024; e += G * NT) {
+            const int b = e / 1024, q = e % 1024;
             int ti, tj;
             tile_of(b, ti, tj);
-            if (q >= 1024 && ti != tj) continue;
-            if (q < 1024 && reuse) continue;
             double acc = 0.0;
             for (int sp = 0; sp < nsplit; ++sp) acc += a.Kpart[((size_t)b * nsplit + sp) * 1152 + q];
-            if (q < 1024) {
-                const int r = ti * 32 + (q >> 5), c = tj * 32 + (q & 31);
-                if (r < nS && c < nS && c <= r) {
-                    a.K[(size_t)r * a.ldk + c] = acc;
-                    a.K[(size_t)c * a.ldk + r] = acc;
-                }
-            } else {
-                const int c = ti * 32 + (q - 1024) / 3, i = (q - 1024) % 3;
-                if (c < nS) a.yS[3 * c + i] = -acc;
+            const int r = ti * 32 + (q >> 5), c = tj * 32 + (q & 31);
+            if (r < nS && c < nS && c <= r) {
+                a.K[(size_t)r * a.ldk + c] = acc;
+                a.K[(size_t)c * a.ldk + r] = acc;
             }
         }
     }
@@ -698,58 +686,35 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
     // ------------------------------------------------ P4: u = C^{-T} y, y = row m of the factor
     // right-looking on C^T: u_k = Li_k^T y_k, then y_j -= (C_kj)^T u_k for j < k
     const int ntm = (m + TB - 1) / TB;
-    if (m <= kP4Single) {
-        // small systems: one CTA, y resident in shared memory, no grid barriers
-        if (bid == 0) {
-            double *uy = T0, *part = T1;
-            for (int e = tid; e < m; e += NT) uy[e] = a.Sh[(size_t)m * a.ldh + e];
-            __syncthreads();
-            for (int k = ntm - 1; k >= 0; --k) {
-                const int kc0 = k * TB, kn = min(TB, m - kc0);
-                const double *Li = a.Lstore + (size_t)k * TB * TB;
-                {   // u_k[i] = sum_{r >= i} Li[r][i] y_k[r]: 4 partial sums per output
-                    const int i = tid & 63, pq = tid >> 6;
-                    double acc = 0.0;
-                    if (i < kn)
-                        for (int r = i + pq; r < kn; r += 4) acc += Li[r * TB + i] * uy[kc0 + r];
-                    part[pq * TB + i] = acc;
-                }
-                __syncthreads();
-                if (tid < kn) uy[kc0 + tid] = part[tid] + part[TB + tid] + part[2 * TB + tid] + part[3 * TB + tid];
-                __syncthreads();
-                for (int j = tid; j < kc0; j += NT) {   // y_j -= sum_r C[kc0 + r][j] u_k[r]
-                    double acc = 0.0;
-#pragma unroll 8
-                    for (int r = 0; r < kn; ++r) acc += a.Sh[(size_t)(kc0 + r) * a.ldh + j] * uy[kc0 + r];
-                    uy[j] -= acc;
-                }
-                __syncthreads();
-            }
-            for (int e = tid; e < m; e += NT) a.u[e] = uy[e];
-        }
+    {
+        // one grid barrier per tile step: every CTA forms u_k = Li_k^T y_k itself (64 x 64, from
+        // L2), CTA 0 publishes it, all CTAs update their slice of y_j -= C_kj^T u_k (j < k).
+        // y lives in a.y (updated in place), u in a.u.
+        for (int e = bid * NT + tid; e < m; e += G * NT) a.y[e] = a.Sh[(size_t)m * a.ldh + e];
         GSYNC();
-    } else {
-        for (int e = bid * NT + tid; e < m; e += G * NT) a.u[e] = a.Sh[(size_t)m * a.ldh + e];
-        GSYNC();
+        double *uk = T0, *part = T1;
         for (int k = ntm - 1; k >= 0; --k) {
             const int kc0 = k * TB, kn = min(TB, m - kc0);
-            if (bid == 0) {
-                double *yk = T3;                      // stage y_k
-                for (int i = tid; i < TB; i += NT) yk[i] = i < kn ? a.u[kc0 + i] : 0.0;
-                __syncthreads();
-                const double *Li = a.Lstore + (size_t)k * TB * TB;
-                for (int i = tid; i < kn; i += NT) {  // u_k[i] = sum_r Li[r][i] y_k[r]
-                    double acc = 0.0;
-                    for (int r = i; r < kn; ++r) acc += Li[r * TB + i] * yk[r];
-                    a.u[kc0 + i] = acc;
-                }
-            }
-            GSYNC();
-            // y_j -= C_kj^T u_k  for rows j < kc0 (block row k of the factor, columns j)
-            for (int j = bid * NT + tid; j < kc0; j += G * NT) {
+            const double *Li = a.Lstore + (size_t)k * TB * TB;
+            {   // u_k[i] = sum_{r >= i} Li[r][i] y_k[r]: 4 partial sums per output
+                const int i = tid & 63, pq = tid >> 6;
                 double acc = 0.0;
-                for (int r = 0; r < kn; ++r) acc += a.Sh[(size_t)(kc0 + r) * a.ldh + j] * a.u[kc0 + r];
-                a.u[j] -= acc;
+                if (i < kn)
+                    for (int r = i + pq; r < kn; r += 4) acc += Li[r * TB + i] * a.y[kc0 + r];
+                part[pq * TB + i] = acc;
+            }
+            __syncthreads();
+            if (tid < TB) {
+                const double v = tid < kn ? part[tid] + part[TB + tid] + part[2 * TB + tid] + part[3 * TB + tid] : 0.0;
+                uk[tid] = v;
+                if (bid == 0 && tid < kn) a.u[kc0 + tid] = v;
+            }
+            __syncthreads();
+            for (int j = bid * NT + tid; j < kc0; j += G * NT) {   // y_j -= sum_r C[kc0 + r][j] u_k[r]
+                double acc = 0.0;
+#pragma unroll 8
+                for (int r = 0; r < kn; ++r) acc += a.Sh[(size_t)(kc0 + r) * a.ldh + j] * uk[r];
+                a.y[j] -= acc;
             }
             GSYNC();
         }
@@ -795,14 +760,14 @@ void schur_init(int device) {
 
 int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, const int *qS,
                  const int *lo, const int *hi, const int *nS, int capS, double *K, int ldk, const double *Bc, int ldb,
-                 double *Sh, int ldh, double *Lstore, double *T, double *U, double *yS, double *u,
+                 double *Sh, int ldh, double *Lstore, double *T, double *U, double *yS, double *y, double *u,
                  double *t, double *Z, int *info, const int *same_S, unsigned long long *prof,
                  cudaStream_t st) {
     SchurArgs a;
     a.V = V; a.ldv = ldv; a.G = G; a.qS = qS; a.col2sn = F.col2sn; a.sn_c0 = F.sn_c0;
-    a.sn_parent = F.sn_parent; a.lo = lo; a.hi = hi; a.nsn = F.nsn; a.nf = F.nf; a.nS_ptr = nS; a.capS = capS;
+    a.sn_parent = F.sn_parent; a.path_ptr = F.path_ptr; a.path_sn = F.path_sn; a.lo = lo; a.hi = hi; a.nsn = F.nsn; a.nf = F.nf; a.nS_ptr = nS; a.capS = capS;
     a.K = K; a.ldk = ldk; a.Bc = Bc; a.ldb = ldb; a.Sh = Sh; a.ldh = ldh; a.Lstore = Lstore;
-    a.T = T; a.U = U; a.yS = yS; a.u = u; a.t = t; a.Z = Z; a.info = info; a.same = same_S; a.prof = prof;
+    a.T = T; a.U = U; a.yS = yS; a.y = y; a.u = u; a.t = t; a.Z = Z; a.info = info; a.same = same_S; a.prof = prof;
     a.Kpart = g_kpart;
     a.LP = g_lp;
     void *args[] = {&a};

@@ -13,6 +13,7 @@ struct DevFactor {
     const int2 *bw_items = nullptr;    // backward items (s, row block), reverse postorder
     int *bw_pbase = nullptr;           // first partial block of each supernode
     int *ford = nullptr;               // forward dispatch order of the supernodes
+    int *path_ptr = nullptr, *path_sn = nullptr;   // etree path (self, ancestors) per supernode
     int bw_nitems = 0, bw_nblocks = 0;
     int *seg_ptr = nullptr, *seg_d = nullptr, *seg_klo = nullptr, *seg_khi = nullptr;
     int *sn_fd = nullptr, *col2sn = nullptr;
@@ -60,7 +61,7 @@ void launch_backward_solve(const DevFactor &F, int *done, int *cnt, int *ticket,
 void schur_init(int device);
 int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, const int *qS,
                  const int *lo, const int *hi, const int *nS, int capS, double *K, int ldk, const double *Bc, int ldb,
-                 double *Sh, int ldh, double *Lstore, double *T, double *U, double *yS, double *u,
+                 double *Sh, int ldh, double *Lstore, double *T, double *U, double *yS, double *y, double *u,
                  double *t, double *Z, int *info, const int *same_S, unsigned long long *prof,
                  cudaStream_t st);
 void note_launch();
