@@ -107,9 +107,9 @@ struct StageTimer {             // Table-1 stage boundaries, one event set per i
 enum KId { K_LOCAL = 0, K_GATHER, K_BROAD, K_NARROW, K_DERIV, K_ASSEMBLY, K_FWD, K_DENSE, K_BWD,
            K_CCD, K_LS, K_D_SYRK, K_D_INV, K_D_POTRF, K_D_SOLVE, K_NUM };
 static const char *kKernelNames[K_NUM] = {"local_step", "gather", "broad_phase", "narrow_phase",
-                                          "pair_derivatives", "contact_assembly", "forward_solve",
+                                          "pair_derivatives", "contact_assembly", "panel_forward",
                                           "dense_schur", "backward_solve", "ccd", "line_search",
-                                          "dense.syrk", "dense.inverse", "dense.potrf",
+                                          "w_el_forward", "unused.1", "dense.potrf",
                                           "dense.solve"};
 // During stream capture an event must be recorded as an external event node (a plain record
 // would only mark a capture dependency); outside capture a plain record.
@@ -195,6 +195,13 @@ struct pd_ipc {
     DBuf<int> mark, spos, qS;
     DBuf<double> lspart;    // line-search partial sums [8][ls_blocks()]
     bool force_sort = false;  // next broad phases take the sort path (after a hash overflow)
+    // second stream: w_el = L^-1 Pi g_el runs concurrently with the contact stages (it depends
+    // on the elastic gradient only)
+    cudaStream_t st2 = nullptr;
+    int side_ctas = 74;       // persistent CTAs of the stream-2 solves (PDIPC_SIDE_CTAS)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    DBuf<double> gcS, Ug2;
+    DBuf<int> ts_lo2, ts_hi2, ts_cnt2, ts_ptr2, ts_rem2, ticket2, f_bord, iscr2;
     bool graphs = true;       // replay each iteration as a CUDA graph (PDIPC_NO_GRAPH=1: off)
     unsigned buf_epoch = 0;   // bumped whenever a buffer the iteration uses is reallocated
     int nS_host = 0;
@@ -453,6 +460,24 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
     kt.start(K_GATHER, st);
     launch_gather_elastic(h->inc_ptr.p, h->inc.p, h->fc.p, nf, h->g_el.p, st);
     kt.stop(K_GATHER, st);
+    // fork: w_el = L^-1 Pi g_el depends on the elastic gradient only -> stream 2, concurrent with
+    // the contact stages (the contact part of w is V_s gc, folded into the Schur step)
+    {
+        cudaStream_t s2 = h->st2;
+        const DevFactor &F2 = h->F;
+        CK(cudaEventRecord(h->ev_fork, st));
+        CK(cudaStreamWaitEvent(s2, h->ev_fork, 0));
+        CK(cudaMemsetAsync(h->ticket2.p, 0, 4 * sizeof(int), s2));   // [0] ticket, [1] fault, [2] |S| = 0
+        kt.start(K_D_SYRK, s2);
+        launch_ts_items(F2, nullptr, h->ticket2.p + 2, 0, h->ticket2.p + 2, 0, h->ticket2.p + 3, 1, h->ts_lo2.p,
+                        h->ts_hi2.p, h->ts_cnt2.p, h->ts_rem2.p, s2);
+        scan_exclusive(h->ts_cnt2.p, h->ts_ptr2.p, F2.nsn, h->iscr2.p, s2);
+        launch_forward_solve(F2, h->ts_lo2.p, h->ts_hi2.p, h->ts_ptr2.p, nullptr, h->ts_rem2.p, h->ticket2.p,
+                             reinterpret_cast<const double *>(h->g_el.p), h->Yw.p, nullptr, h->ldv, h->Ug2.p,
+                             nullptr, h->ticket2.p + 2, 0, 1, h->side_ctas, nullptr, s2);
+        kt.stop(K_D_SYRK, s2);
+        CK(cudaEventRecord(h->ev_join, s2));
+    }
     record_event(ev[1], st);
     // ---------------- IPC
     int *nS_dev = h->spos.p + nf;     // exclusive scan total of the S marks
@@ -491,6 +516,7 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
         CK(cudaMemsetAsync(h->gsq.p, 0, sizeof(long long) * 6 * Ns, st));
         launch_accum_grad_fx(h->ids.p, acnt, cap, h->grad.p, dmax, h->gsq.p, st);
         launch_grad_pullback_fx(h->g_el.p, h->WTp.p, h->WTr.p, h->WTv.p, h->gsq.p, dmax, acnt, nf, h->G.p, st);
+        launch_gather_gc(h->qS.p, nS_dev, h->capS, h->WTp.p, h->WTr.p, h->WTv.p, h->gsq.p, dmax, acnt, h->gcS.p, st);
         // B-check: fixed-point accumulation into the dense 3|S| x 3|S| block, then to double; the
         // low words of the fixed-point sums live in the (not yet used) Sigma-hat buffer
         const int ldb = 3 * h->capS;
@@ -509,28 +535,32 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
     }
     record_event(ev[2], st);
     // ---------------- G-Step
+    // pure-PD part on stream 2 (forked after the gather, see above); here the contact part
     const DevFactor &F = h->F;
     CK(cudaMemsetAsync(h->ticket.p, 0, 2 * sizeof(int), st));
     kt.start(K_FWD, st);
+    // panel V_s = L^-1 Pi E_S (panel tiles only; no items when S is unchanged)
     launch_ts_items(F, h->qS.p, nS_dev, h->capS, h->dint.p + D_SPREV + 1, (long long)h->Up.n,
-                    h->dint.p + D_CAP, h->ts_lo.p, h->ts_hi.p, h->ts_cnt.p, h->ts_rem.p, st);
+                    h->dint.p + D_CAP, 2, h->ts_lo.p, h->ts_hi.p, h->ts_cnt.p, h->ts_rem.p, st);
     scan_exclusive(h->ts_cnt.p, h->ts_ptr.p, F.nsn, h->iscr.p, st);
     if (h->trace_file) h->trace.ensure(4 * (size_t)F.bw_nblocks * (2 + (h->capS + 31) / 32));
     launch_forward_solve(F, h->ts_lo.p, h->ts_hi.p, h->ts_ptr.p, h->qS.p, h->ts_rem.p, h->ticket.p, h->G.p,
-                         h->Yw.p, h->V.p, h->ldv, h->Ug.p, h->Up.p, nS_dev, h->capS, h->nsm,
+                         h->Yw.p, h->V.p, h->ldv, h->Ug.p, h->Up.p, nS_dev, h->capS, 0, h->nsm,
                          h->trace_file ? h->trace.p : nullptr, st);
     kt.stop(K_FWD, st);
+    // join stream 2 (w_el): the Schur step forms Z = w_el + V_s (gc + t)
+    CK(cudaStreamWaitEvent(st, h->ev_join, 0));
     kt.start(K_DENSE, st);
     if (Nt > 0) {
         if (h->trace_file) {
             h->sprof.ensure(1024);
             CK(cudaMemsetAsync(h->sprof.p, 0, 1024 * 8, st));
         }
-        CK((cudaError_t)launch_schur(F, h->V.p, h->ldv, h->Yw.p, h->qS.p, h->ts_lo.p, h->ts_hi.p, nS_dev,
-                                     h->capS, h->K.p, h->capS, h->Bc.p, 3 * h->capS, h->Sh.p, h->ldh,
-                                     h->Lstore.p, h->Tt.p, h->U.p, h->yS.p, h->rhs.p, h->u.p, h->tv.p, h->Z.p,
-                                     h->dint.p + D_INFO, h->dint.p + D_SPREV + 1,
-                                     h->trace_file ? h->sprof.p : nullptr, st));
+        CK((cudaError_t)launch_schur(F, h->V.p, h->ldv, h->Yw.p, h->gcS.p, h->qS.p,
+                                     h->ts_lo.p, h->ts_hi.p, nS_dev, h->capS, h->K.p, h->capS, h->Bc.p,
+                                     3 * h->capS, h->Sh.p, h->ldh, h->Lstore.p, h->Tt.p, h->U.p, h->yS.p,
+                                     h->rhs.p, h->u.p, h->tv.p, h->Z.p, h->dint.p + D_INFO,
+                                     h->dint.p + D_SPREV + 1, h->trace_file ? h->sprof.p : nullptr, st));
     } else {
         CK(cudaMemcpyAsync(h->Z.p, h->Yw.p, sizeof(double) * 4 * nf, cudaMemcpyDeviceToDevice, st));
     }
@@ -650,8 +680,10 @@ static int run_batch(pd_ipc *h, Seq &q, int k, double ms[6]) {
     CK(cudaMemcpyAsync(di, h->dint.p, sizeof(di), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&h->nS_host, nS_dev, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    int fault = 0;
+    int fault = 0, f2 = 0;
     CK(cudaMemcpy(&fault, h->ticket.p + 1, sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&f2, h->ticket2.p + 1, sizeof(int), cudaMemcpyDeviceToHost));
+    fault |= f2;
     if (fault) throw CudaError("triangular solve dependency wait timed out", PD_IPC_E_CUDA);
     const int nS = h->nS_host;
     const int applied = di[D_ABORT] ? di[D_ABORT + 1] : k;
@@ -780,9 +812,13 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         h->device = o.device;
         CK(cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, o.device));
         CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
         h->tm.init();
         h->kt.init();
         if (const char *ng = std::getenv("PDIPC_NO_GRAPH")) h->graphs = !(ng[0] == '1');
+        if (const char *sc = std::getenv("PDIPC_SIDE_CTAS")) h->side_ctas = std::max(1, std::atoi(sc));
         if (const char *tp = std::getenv("PDIPC_TRACE")) {
             h->trace_file = std::fopen(tp, "wb");
             h->schur_file = std::fopen((std::string(tp) + ".schur").c_str(), "wb");
@@ -864,6 +900,7 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             std::stable_sort(ford.begin(), ford.end(), [&](int a, int b) { return ctr[a] > ctr[b]; });
             std::stable_sort(bord.begin(), bord.end(), [&](int a, int b) { return hgt[a] > hgt[b]; });
             h->f_ford.upload(ford.data(), ford.size());
+            h->f_bord.upload(bord.data(), bord.size());
             std::vector<int2> items;
             std::vector<int> pbase(nsn);
             int nblk = 0;
@@ -897,6 +934,8 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         }
         h->f_dinv.upload(f.dinv.data(), f.dinv.size());
         h->Ug.exact(4 * (size_t)std::max(1, f.uoff[f.nsn]));
+        h->Ug2.exact(4 * (size_t)std::max(1, f.uoff[f.nsn]));
+        h->iscr2.exact(scan_scratch_ints(f.nsn + 1) + 64);
         DevFactor &F = h->F;
         F.uoff = h->f_uoff.p; F.urow_sn = h->f_urow_sn.p; F.rc_ptr = h->f_rc_ptr.p; F.rc_idx = h->f_rc_idx.p;
         F.rc_src = h->f_rc_src.p;
@@ -906,7 +945,7 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         F.sn_c0 = h->f_c0.p; F.sn_rowptr = h->f_rowptr.p; F.sn_rows = h->f_rows.p; F.sn_parent = h->f_parent.p;
         F.sn_valptr = h->f_valptr.p; F.Q = h->f_L.p;
         F.bw_items = h->f_bw_items.p; F.bw_pbase = h->f_bw_pbase.p; F.ford = h->f_ford.p;
-        F.path_ptr = h->f_path_ptr.p; F.path_sn = h->f_path_sn.p;
+        F.path_ptr = h->f_path_ptr.p; F.path_sn = h->f_path_sn.p; F.bord = h->f_bord.p;
         F.seg_ptr = h->f_seg_ptr.p; F.seg_d = h->f_seg_d.p; F.seg_klo = h->f_seg_klo.p; F.seg_khi = h->f_seg_khi.p;
         F.sn_fd = h->f_fd.p; F.col2sn = h->f_col2sn.p;
         // contact capacity: S is a subset of the free vertices in the W support (n2)
@@ -937,6 +976,13 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         h->g_el.exact(nf);
         h->G.exact(4 * (size_t)nf);
         h->Yw.exact(4 * (size_t)nf);
+        h->ts_lo2.exact(f.nsn);
+        h->ts_hi2.exact(f.nsn);
+        h->ts_cnt2.exact(f.nsn + 1);
+        h->ts_ptr2.exact(f.nsn + 1);
+        h->ts_rem2.exact(f.nsn);
+        h->ticket2.exact(4);
+        CK(cudaMemset(h->ticket2.p, 0, 4 * sizeof(int)));
         h->Z.exact(4 * (size_t)nf);
         h->dx.exact(m.n);
         h->s.exact(std::max(1, m.Ns));
@@ -953,6 +999,7 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         h->ts_rem.exact(f.nsn);
         h->ts_done.exact(f.nsn);
         h->ticket.exact(4);
+        CK(cudaMemset(h->ticket.p, 0, 4 * sizeof(int)));
         h->dscal.exact(16);
         h->dint.exact(32);
         CK(cudaMemset(h->dscal.p, 0, sizeof(double) * 16));   // flags / counters start cleared
@@ -997,6 +1044,7 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         if (m.Nt > 0) {
             const int cS = h->capS;
             h->V.exact((size_t)nf * h->ldv);
+            h->gcS.exact(3 * (size_t)h->capS + 3);
             h->K.exact((size_t)cS * cS);
             h->Bc.exact((size_t)9 * cS * cS);
             h->ldh = 3 * cS + 8;
@@ -1090,13 +1138,16 @@ void pd_ipc_destroy(pd_ipc *h) {
     if (h->schur_file) std::fclose(h->schur_file);
     h->trace.release();
     h->sprof.release();
+    if (h->st2) cudaStreamDestroy(h->st2);
+    if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+    if (h->ev_join) cudaEventDestroy(h->ev_join);
     if (h->st) cudaStreamDestroy(h->st);
     auto rel = [](auto &b) { b.release(); };
     rel(h->tets); rel(h->B); rel(h->w); rel(h->inc_ptr); rel(h->inc); rel(h->q2v); rel(h->v2q);
     rel(h->Wp); rel(h->Wc); rel(h->WTp); rel(h->WTr); rel(h->tris); rel(h->edges); rel(h->Wv); rel(h->WTv);
     rel(h->f_c0); rel(h->f_rowptr); rel(h->f_rows); rel(h->f_parent); rel(h->f_seg_ptr); rel(h->f_seg_d);
     rel(h->f_seg_klo); rel(h->f_seg_khi); rel(h->f_fd); rel(h->f_col2sn); rel(h->f_valptr); rel(h->f_L);
-    rel(h->f_dinv_ptr); rel(h->f_dinv); rel(h->Ug); rel(h->Up); rel(h->Yw); rel(h->bw_P); rel(h->f_bw_items); rel(h->f_ford); rel(h->f_path_ptr); rel(h->f_path_sn); rel(h->qS_prev); rel(h->f_rc_src); rel(h->f_bw_pbase); rel(h->bw_cnt); rel(h->f_uoff); rel(h->f_urow_sn);
+    rel(h->f_dinv_ptr); rel(h->f_dinv); rel(h->Ug); rel(h->Up); rel(h->Yw); rel(h->bw_P); rel(h->f_bw_items); rel(h->f_ford); rel(h->f_bord); rel(h->gcS); rel(h->Ug2); rel(h->f_path_ptr); rel(h->f_path_sn); rel(h->qS_prev); rel(h->f_rc_src); rel(h->f_bw_pbase); rel(h->bw_cnt); rel(h->f_uoff); rel(h->f_urow_sn);
     rel(h->f_rc_ptr); rel(h->f_rc_idx); rel(h->f_urel); rel(h->f_ch_ptr); rel(h->f_ch);
     for (auto &s : h->seqs) { rel(s->x); rel(s->A6); rel(s->p); }
     rel(h->fc); rel(h->G); rel(h->Z); rel(h->A9stage); rel(h->g_el); rel(h->s); rel(h->ds); rel(h->dx);

@@ -883,6 +883,30 @@ void launch_grad_pullback_fx(const double4 *g_el, const int *WTp, const int *WTr
     PDI_LAUNCH(k_grad_pullback_fx, (nf + 255) / 256, 256, 0, st)(g_el, WTp, WTr, WTv, gsq, dmax, acnt, nf, G);
 }
 
+// gc[3a + i] = (W^T grad B)_{q_a, i}: the contact part of the gradient on S (same sums as the
+// pull-back of k_grad_pullback_fx)
+__global__ void k_gather_gc(const int *__restrict__ qS, const int *__restrict__ nS_ptr, int capS,
+                            const int *__restrict__ WTp, const int *__restrict__ WTr,
+                            const double *__restrict__ WTv, const long long *__restrict__ gsq,
+                            const double *__restrict__ dmax, const int *__restrict__ acnt,
+                            double *__restrict__ gc) {
+    const int nS = min(*nS_ptr, capS);
+    const double inv = 1.0 / fx_scale(dmax, acnt[1]);
+    for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < nS; a += gridDim.x * blockDim.x) {
+        const int q = qS[a];
+        double bx = 0, by = 0, bz = 0;
+        for (int k = WTp[q]; k < WTp[q + 1]; ++k) {
+            const double w = WTv[k];
+            const long long *v = gsq + 6 * (size_t)WTr[k];
+            bx += w * fx_get(v[0], v[3], inv);
+            by += w * fx_get(v[1], v[4], inv);
+            bz += w * fx_get(v[2], v[5], inv);
+        }
+        gc[3 * a + 0] = bx;
+        gc[3 * a + 1] = by;
+        gc[3 * a + 2] = bz;
+    }
+}
 __global__ void k_zero_square(double *M, int ld, const int *nS_ptr, int capS) {
     const int n = 3 * min(*nS_ptr, capS);
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < (size_t)n * n;
@@ -1101,6 +1125,10 @@ void launch_compact_S(const int *mark, const int *pos, int nf, int *qS, cudaStre
 void launch_grad_pullback(const double4 *g_el, const int *WTp, const int *WTr, const double *WTv,
                           const double4 *gs, int nf, double *G, cudaStream_t st) {
     PDI_LAUNCH(k_grad_pullback, (nf + 255) / 256, 256, 0, st)(g_el, WTp, WTr, WTv, gs, nf, G);
+}
+void launch_gather_gc(const int *qS, const int *nS, int capS, const int *WTp, const int *WTr, const double *WTv,
+                      const long long *gsq, const double *dmax, const int *acnt, double *gc, cudaStream_t st) {
+    PDI_LAUNCH(k_gather_gc, grid_for(capS, 128, 148), 128, 0, st)(qS, nS, capS, WTp, WTr, WTv, gsq, dmax, acnt, gc);
 }
 void launch_zero_square(double *M, int ld, const int *nS, int capS, cudaStream_t st) {
     PDI_LAUNCH(k_zero_square, 296, 256, 0, st)(M, ld, nS, capS);

@@ -38,7 +38,8 @@ struct SchurArgs {
     // panel
     const double *V;
     int ldv;
-    const double *G;            // w [nf][4]
+    const double *G;            // w_el = L^{-1} Pi g_el [nf][4] (elastic part only)
+    const double *gc;           // [3|S|] contact part of the gradient on S (Pi g = Pi g_el + E_S gc)
     const int *qS, *col2sn, *sn_c0, *sn_parent, *lo, *hi, *path_ptr, *path_sn;
     int nsn, nf, capS;
     const int *nS_ptr;          // |S| (device); clamped to capS
@@ -299,7 +300,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int G = gridDim.x, bid = blockIdx.x;
     const int nS = min(*a.nS_ptr, a.capS), m = 3 * nS, ma = m + 1;   // augmented size
-    if (nS == 0) {                                        // no contact: z = w
+    if (nS == 0) {                                        // no contact: z = w = w_el
         for (int r = bid * NT + tid; r < 4 * a.nf; r += G * NT) a.Z[r] = a.G[r];
         return;
     }
@@ -317,7 +318,8 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
     // accumulates on DMMA.  Diagonal tiles also accumulate y_S for their columns.  Split partials
     // are reduced in a fixed order (deterministic).
     const bool reuse = *a.same != 0;                 // uniform across the grid
-    // y_S[c] = -sum over the etree path of q_c's supernode of V[r][c] w[r]: one CTA per column,
+    // y_S^el[c] = -sum over the etree path of q_c's supernode of V[r][c] w_el[r] (the elastic
+    // part; the contact part -K gc is folded into b below since Sigma_s K = I): one CTA per column,
     // the path rows come from a static per-supernode list (independent loads), fixed-order
     // block reduction: the same bits whether or not K is recomputed
     for (int c = bid; c < nS; c += G) {
@@ -520,12 +522,13 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
         if (r % 3 == c % 3) v -= a.K[(size_t)(r / 3) * a.ldk + c / 3];
         a.Sh[(size_t)r * a.ldh + c] = v;
     }
-    for (int row = bid * (NT / 32) + wid; row < m; row += G * (NT / 32)) {   // b = Sigma_s yS
+    // b = (Sigma_s (x) I3) y_S with y_S = y_S^el - (K (x) I3) gc, i.e. b = Sigma_s y_S^el - gc
+    for (int row = bid * (NT / 32) + wid; row < m; row += G * (NT / 32)) {
         const int ai = row / 3, i = row % 3;
         double acc = 0.0;
         for (int bb = lane; bb < nS; bb += 32) acc -= a.K[(size_t)ai * a.ldk + bb] * a.yS[3 * bb + i];
         acc = warp_sum(acc);
-        if (lane == 0) a.Sh[(size_t)m * a.ldh + row] = acc;
+        if (lane == 0) a.Sh[(size_t)m * a.ldh + row] = acc - a.gc[row];
     }
     if (bid == 0 && tid == 0) a.Sh[(size_t)m * a.ldh + m] = 1.0;
     GSYNC();
@@ -719,15 +722,16 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
             GSYNC();
         }
     }
-    // ------------------------------------------------ P5: t = B u ; Z = w + V t
+    // ------------------------------------------------ P5: t = B u ; Z = w + V t = w_el + V (gc + t)
+    // (w = L^{-1} Pi g = w_el + V gc since the contact gradient is supported on S)
     for (int row = bid * (NT / 32) + wid; row < m; row += G * (NT / 32)) {
         double acc = 0.0;
         for (int c = lane; c < m; c += 32) acc += a.Bc[(size_t)row * a.ldb + c] * a.u[c];
         acc = warp_sum(acc);
-        if (lane == 0) a.t[row] = acc;
+        if (lane == 0) a.t[row] = acc + a.gc[row];
     }
     GSYNC();
-    for (int r = bid * NT + tid; r < a.nf; r += G * NT) {
+    for (int r = bid * NT + tid; r < a.nf; r += G * NT) {   // Z = w_el + V (gc + t)
         const int s = a.col2sn[r];
         double z0 = a.G[(size_t)r * 4 + 0], z1 = a.G[(size_t)r * 4 + 1], z2 = a.G[(size_t)r * 4 + 2];
         for (int c = a.lo[s]; c < a.hi[s]; ++c) {
@@ -758,13 +762,14 @@ void schur_init(int device) {
     if (!g_lp) cudaMalloc(&g_lp, (size_t)2 * kLPTiles * TB * TB * sizeof(double));
 }
 
-int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, const int *qS,
+int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, const double *gc,
+                 const int *qS,
                  const int *lo, const int *hi, const int *nS, int capS, double *K, int ldk, const double *Bc, int ldb,
                  double *Sh, int ldh, double *Lstore, double *T, double *U, double *yS, double *y, double *u,
                  double *t, double *Z, int *info, const int *same_S, unsigned long long *prof,
                  cudaStream_t st) {
     SchurArgs a;
-    a.V = V; a.ldv = ldv; a.G = G; a.qS = qS; a.col2sn = F.col2sn; a.sn_c0 = F.sn_c0;
+    a.V = V; a.ldv = ldv; a.G = G; a.gc = gc; a.qS = qS; a.col2sn = F.col2sn; a.sn_c0 = F.sn_c0;
     a.sn_parent = F.sn_parent; a.path_ptr = F.path_ptr; a.path_sn = F.path_sn; a.lo = lo; a.hi = hi; a.nsn = F.nsn; a.nf = F.nf; a.nS_ptr = nS; a.capS = capS;
     a.K = K; a.ldk = ldk; a.Bc = Bc; a.ldb = ldb; a.Sh = Sh; a.ldh = ldh; a.Lstore = Lstore;
     a.T = T; a.U = U; a.yS = yS; a.y = y; a.u = u; a.t = t; a.Z = Z; a.info = info; a.same = same_S; a.prof = prof;

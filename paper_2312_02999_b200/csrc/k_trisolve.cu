@@ -38,16 +38,24 @@ __global__ void k_ts_items(const int *__restrict__ ford, const int *__restrict__
                            const int *__restrict__ sn_rowptr, const int *__restrict__ sn_fd,
                            const int *__restrict__ sn_parent, int nsn, const int *__restrict__ qS,
                            const int *__restrict__ nS_ptr, int capS, const int *__restrict__ same_S,
-                           int nU, long long up_cap, int *__restrict__ flags,
+                           int nU, long long up_cap, int *__restrict__ flags, int mode,
                            int *__restrict__ lo, int *__restrict__ hi, int *__restrict__ cnt,
                            int *__restrict__ rem) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;   // dispatch position
     if (k >= nsn) return;
     const int s = ford[k];
+    const int nb = (sn_rowptr[s + 1] - sn_rowptr[s] + kSolveRB - 1) / kSolveRB;
+    if (!(mode & 2)) {                     // gradient items only: no contact data read at all
+        lo[s] = hi[s] = 0;
+        cnt[k] = nb;
+        const int p = sn_parent[s];
+        if (p >= 0) atomicAdd(rem + p, nb);
+        return;
+    }
     const int nS = min(*nS_ptr, capS);
     // panel update rows need nU x round32(|S|) doubles; otherwise flag bit 4 (grow and redo)
     const bool up_ok = (long long)nU * (((nS + 31) / 32) * 32) <= up_cap;
-    if (!up_ok && k == 0) atomicOr(flags, 4);
+    if ((mode & 2) && !up_ok && k == 0) atomicOr(flags, 4);
     const int a = sn_fd[s], b = sn_c0[s + 1];
     int l = 0, r = nS;
     while (l < r) { int m = (l + r) >> 1; if (qS[m] < a) l = m + 1; else r = m; }
@@ -57,10 +65,9 @@ __global__ void k_ts_items(const int *__restrict__ ford, const int *__restrict__
     int H0 = l;
     lo[s] = L0;
     hi[s] = H0;
-    const int nb = (sn_rowptr[s + 1] - sn_rowptr[s] + kSolveRB - 1) / kSolveRB;
     // panel tiles only when V_s must be recomputed (S changed)
-    const int tiles = (up_ok && *same_S == 0 && H0 > L0) ? (H0 - 1) / kPT - L0 / kPT + 1 : 0;
-    int c = nb * (1 + tiles);
+    const int tiles = ((mode & 2) && up_ok && *same_S == 0 && H0 > L0) ? (H0 - 1) / kPT - L0 / kPT + 1 : 0;
+    int c = nb * ((mode & 1) + tiles);
     cnt[k] = c;
     int p = sn_parent[s];
     if (p >= 0) atomicAdd(rem + p, c);
@@ -82,6 +89,7 @@ struct FwdArgs {
     double *Up;                        // [nU][ldu] panel update rows, ldu = round32(|S|)
     const int *nS_ptr;
     int capS;
+    int with_grad;                     // 0: panel tiles only (item tile index starts at 1)
     unsigned long long *trace;         // optional [items][4]: s|tk, dispense, ready, done (ns)
 };
 
@@ -243,7 +251,8 @@ __global__ void __launch_bounds__(kTS_NT) k_forward_solve(FwdArgs A) {
         const int c0 = A.sn_c0[s], w = A.sn_c0[s + 1] - c0;
         const int slot0 = A.sn_rowptr[s], nr = A.sn_rowptr[s + 1] - slot0;
         const int nb = (nr + kSolveRB - 1) / kSolveRB;
-        const int idx = item - A.item_ptr[kpos], tk = idx / nb, rb = (idx % nb) * kSolveRB;
+        const int idx = item - A.item_ptr[kpos], tk = idx / nb + (A.with_grad ? 0 : 1);
+        const int rb = (idx % nb) * kSolveRB;
         const int m = min(kSolveRB, nr - rb);
         const bool grad = tk == 0;
         int lo_s = 0, hi_s = 0, tbase = 0;
@@ -470,6 +479,7 @@ __global__ void __launch_bounds__(kTS_NT) k_backward_solve(BwdArgs A) {
     }
 }
 
+
 // ------------------------------------------------------------------ host wrappers ---------
 constexpr int kFwdSmem = ((kTS_W + kSolveRB) * kXS + kSgRows * kSS) * (int)sizeof(double);
 
@@ -479,24 +489,25 @@ void trisolve_init() {
 }
 
 void launch_ts_items(const DevFactor &F, const int *qS, const int *nS_ptr, int capS, const int *same_S,
-                     long long up_cap, int *flags, int *lo, int *hi, int *cnt, int *rem, cudaStream_t st) {
+                     long long up_cap, int *flags, int mode, int *lo, int *hi, int *cnt, int *rem,
+                     cudaStream_t st) {
     cudaMemsetAsync(rem, 0, sizeof(int) * F.nsn, st);
     PDI_LAUNCH(k_ts_items, (F.nsn + 255) / 256, 256, 0, st)(F.ford, F.sn_c0, F.sn_rowptr, F.sn_fd,
                                                              F.sn_parent, F.nsn, qS, nS_ptr, capS, same_S,
-                                                             F.nU, up_cap, flags, lo, hi, cnt, rem);
+                                                             F.nU, up_cap, flags, mode, lo, hi, cnt, rem);
 }
 
 void launch_forward_solve(const DevFactor &F, const int *lo, const int *hi, const int *item_ptr,
                           const int *qS, int *rem, int *ticket, const double *G, double *Y, double *V,
-                          int ldv, double *Ug, double *Up, const int *nS_ptr, int capS, int nsm,
-                          unsigned long long *trace, cudaStream_t st) {
+                          int ldv, double *Ug, double *Up, const int *nS_ptr, int capS, int with_grad,
+                          int nsm, unsigned long long *trace, cudaStream_t st) {
     FwdArgs A;
     A.sn_c0 = F.sn_c0; A.sn_rowptr = F.sn_rowptr; A.sn_parent = F.sn_parent;
     A.uoff = F.uoff; A.rc_ptr = F.rc_ptr; A.rc_src = F.rc_src;
     A.sn_valptr = F.sn_valptr; A.Q = F.Q;
     A.lo = lo; A.hi = hi; A.item_ptr = item_ptr; A.qS = qS; A.ford = F.ford; A.nsn = F.nsn;
     A.rem = rem; A.ticket = ticket; A.G = G; A.Y = Y; A.V = V; A.ldv = ldv;
-    A.Ug = Ug; A.Up = Up; A.nS_ptr = nS_ptr; A.capS = capS; A.trace = trace;
+    A.Ug = Ug; A.Up = Up; A.nS_ptr = nS_ptr; A.capS = capS; A.with_grad = with_grad; A.trace = trace;
     cudaMemsetAsync(ticket, 0, sizeof(int), st);
     PDI_LAUNCH(k_forward_solve, nsm, kTS_NT, kFwdSmem, st)(A);
 }
@@ -512,6 +523,7 @@ void launch_backward_solve(const DevFactor &F, int *done, int *cnt, int *ticket,
     cudaMemsetAsync(cnt, 0, sizeof(int) * F.nsn, st);
     PDI_LAUNCH(k_backward_solve, nsm, kTS_NT, kFwdSmem, st)(A);
 }
+
 
 
 

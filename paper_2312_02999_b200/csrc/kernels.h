@@ -13,6 +13,7 @@ struct DevFactor {
     const int2 *bw_items = nullptr;    // backward items (s, row block), reverse postorder
     int *bw_pbase = nullptr;           // first partial block of each supernode
     int *ford = nullptr;               // forward dispatch order of the supernodes
+    int *bord = nullptr;               // backward dispatch order (parents first)
     int *path_ptr = nullptr, *path_sn = nullptr;   // etree path (self, ancestors) per supernode
     int bw_nitems = 0, bw_nblocks = 0;
     int *seg_ptr = nullptr, *seg_d = nullptr, *seg_klo = nullptr, *seg_khi = nullptr;
@@ -47,19 +48,22 @@ void launch_scatter_dx(const double *z, const int *q2v, int nf, double4 *dx, cud
 
 // ---- k_trisolve.cu
 constexpr int kSolveRB = 64;   // rows of a supernode per solve work item
+// mode: bit 0 gradient items, bit 1 panel tiles
 void launch_ts_items(const DevFactor &F, const int *qS, const int *nS_ptr, int capS, const int *same_S,
-                     long long up_cap, int *flags, int *lo, int *hi, int *cnt, int *rem, cudaStream_t st);
+                     long long up_cap, int *flags, int mode, int *lo, int *hi, int *cnt, int *rem,
+                     cudaStream_t st);
 void trisolve_init();
 void launch_forward_solve(const DevFactor &F, const int *lo, const int *hi, const int *item_ptr,
                           const int *qS, int *rem, int *ticket, const double *G, double *Y, double *V,
-                          int ldv, double *Ug, double *Up, const int *nS_ptr, int capS, int nsm,
-                          unsigned long long *trace, cudaStream_t st);
+                          int ldv, double *Ug, double *Up, const int *nS_ptr, int capS, int with_grad,
+                          int nsm, unsigned long long *trace, cudaStream_t st);
 void launch_backward_solve(const DevFactor &F, int *done, int *cnt, int *ticket, double *P, double *Z,
                            int nsm, cudaStream_t st);
 
 // ---- k_schur.cu (fused cooperative dense Schur step, a9)
 void schur_init(int device);
-int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, const int *qS,
+int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, const double *gc,
+                 const int *qS,
                  const int *lo, const int *hi, const int *nS, int capS, double *K, int ldk, const double *Bc, int ldb,
                  double *Sh, int ldh, double *Lstore, double *T, double *U, double *yS, double *y, double *u,
                  double *t, double *Z, int *info, const int *same_S, unsigned long long *prof,
@@ -115,6 +119,8 @@ void launch_grad_pullback_fx(const double4 *g_el, const int *WTp, const int *WTr
 void launch_grad_pullback(const double4 *g_el, const int *WTp, const int *WTr, const double *WTv,
                           const double4 *gs, int nf, double *G, cudaStream_t st);
 void launch_zero_square(double *M, int ld, const int *nS, int capS, cudaStream_t st);
+void launch_gather_gc(const int *qS, const int *nS, int capS, const int *WTp, const int *WTr, const double *WTv,
+                      const long long *gsq, const double *dmax, const int *acnt, double *gc, cudaStream_t st);
 void launch_accd(const unsigned long long *keys, const int *ccnt, int cap, const double4 *s,
                  const int *tris, const int *edges, int Nt, int Ne, const double4 *ds, double s_gap,
                  int max_iters, double *amin, cudaStream_t st);
