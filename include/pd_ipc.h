@@ -138,6 +138,12 @@ int pd_ipc_get_projections(const pd_ipc *h, int32_t seq, double *p);
 int pd_ipc_get_contacts(const pd_ipc *h, int32_t seq, int32_t *pt, int32_t *n_pt,
                         int32_t *ee, int32_t *n_ee, int32_t *S, int32_t *n_S);
 
+/* Per active pair of the last iteration (order of pd_ipc_get_contacts: PT pairs, then EE
+ * pairs): grad [n][12] = kappa b'(d) grad d over the pair's 4 surface
+ * points (p, a, b, c) / (a, b, c, d), Hp [n][78] = packed upper triangle (row-major i <= j) of
+ * the PSD-projected 12x12 Hessian H+.  Pass NULL arrays to query n only.  Needs debug >= 1. */
+int pd_ipc_get_pair_terms(const pd_ipc *h, int32_t seq, double *grad, double *Hp, int32_t *n);
+
 /* Vectors of the last iteration of sequence seq, each [n_verts][3] with zeros on fixed
  * vertices: which = 0 g-hat (elastic + barrier gradient), 1 dx, 2 elastic gradient only. */
 int pd_ipc_get_vector(const pd_ipc *h, int32_t seq, int32_t which, double *out);

@@ -94,7 +94,7 @@ struct Seq {
     pd_ipc_stats stats;
     // debug copies of the last iteration
     std::vector<int32_t> pt, ee, S;
-    std::vector<double> ghat, gel, dx, proj;
+    std::vector<double> ghat, gel, dx, proj, pgrad, phess;
 };
 
 struct StageTimer {             // Table-1 stage boundaries, one event set per iteration slot
@@ -283,6 +283,12 @@ static void debug_capture(pd_ipc *h, Seq &q, int n_pt, int n_ee, int nS) {
         auto &v = k < n_pt ? q.pt : q.ee;
         v.push_back((int32_t)(ak[k] / nb));
         v.push_back((int32_t)(ak[k] % nb));
+    }
+    q.pgrad.resize(12 * (size_t)na);
+    q.phess.resize(78 * (size_t)na);
+    if (na) {
+        CK(cudaMemcpy(q.pgrad.data(), h->grad.p, sizeof(double) * q.pgrad.size(), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(q.phess.data(), h->Hp.p, sizeof(double) * q.phess.size(), cudaMemcpyDeviceToHost));
     }
     std::vector<int> qs(nS);
     if (nS) CK(cudaMemcpy(qs.data(), h->qS.p, sizeof(int) * nS, cudaMemcpyDeviceToHost));
@@ -474,7 +480,7 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
         scan_exclusive(h->ts_cnt2.p, h->ts_ptr2.p, F2.nsn, h->iscr2.p, s2);
         launch_forward_solve(F2, h->ts_lo2.p, h->ts_hi2.p, h->ts_ptr2.p, nullptr, h->ts_rem2.p, h->ticket2.p,
                              reinterpret_cast<const double *>(h->g_el.p), h->Yw.p, nullptr, h->ldv, h->Ug2.p,
-                             nullptr, h->ticket2.p + 2, 0, 1, h->side_ctas, nullptr, s2);
+                             nullptr, h->ticket2.p + 2, 0, 1, h->Nt > 0 ? h->side_ctas : h->nsm, nullptr, s2);
         kt.stop(K_D_SYRK, s2);
         CK(cudaEventRecord(h->ev_join, s2));
     }
@@ -1220,6 +1226,16 @@ int pd_ipc_get_projections(const pd_ipc *h, int32_t seq, double *p) {
     } catch (const CudaError &e) {
         return fail(const_cast<pd_ipc *>(h), e.code, e.what());
     }
+    return PD_IPC_OK;
+}
+
+int pd_ipc_get_pair_terms(const pd_ipc *h, int32_t seq, double *grad, double *Hp, int32_t *n) {
+    if (!h || !n) return fail(nullptr, PD_IPC_E_ARG, "NULL argument");
+    if (seq < 0 || seq >= (int)h->seqs.size()) return fail(const_cast<pd_ipc *>(h), PD_IPC_E_ARG, "bad sequence");
+    const Seq &q = *h->seqs[seq];
+    *n = (int32_t)(q.pgrad.size() / 12);
+    if (grad) std::copy(q.pgrad.begin(), q.pgrad.end(), grad);
+    if (Hp) std::copy(q.phess.begin(), q.phess.end(), Hp);
     return PD_IPC_OK;
 }
 

@@ -70,6 +70,8 @@ lib.pd_ipc_get_projections.argtypes = [_P, C.c_int32, C.POINTER(C.c_double)]
 lib.pd_ipc_get_projections.restype = C.c_int
 _IP = C.POINTER(C.c_int32)
 lib.pd_ipc_get_contacts.argtypes = [_P, C.c_int32, _IP, _IP, _IP, _IP, _IP, _IP]
+lib.pd_ipc_get_pair_terms.argtypes = [_P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double), _IP]
+lib.pd_ipc_get_pair_terms.restype = C.c_int
 lib.pd_ipc_get_contacts.restype = C.c_int
 lib.pd_ipc_get_vector.argtypes = [_P, C.c_int32, C.c_int32, C.POINTER(C.c_double)]
 lib.pd_ipc_get_vector.restype = C.c_int
@@ -91,7 +93,7 @@ lib.pd_ipc_launch_count.restype = C.c_int64
 
 EXPORTED = ["pd_ipc_create", "pd_ipc_step", "pd_ipc_positions", "pd_ipc_destroy",
             "pd_ipc_last_error", "pd_ipc_set_positions", "pd_ipc_set_debug",
-            "pd_ipc_get_projections", "pd_ipc_get_contacts", "pd_ipc_get_vector",
+            "pd_ipc_get_projections", "pd_ipc_get_contacts", "pd_ipc_get_vector", "pd_ipc_get_pair_terms",
             "pd_ipc_build_info", "pd_ipc_debug_factor_solve", "pd_ipc_set_timing",
             "pd_ipc_kernel_times", "pd_ipc_kernel_name", "pd_ipc_launch_count"]
 
@@ -234,6 +236,20 @@ def get_contacts(h, seq=0):
     _check(lib.pd_ipc_get_contacts(h, seq, _ip(pt), C.byref(n[0]), _ip(ee), C.byref(n[1]),
                                    _ip(S), C.byref(n[2])), h)
     return pt, ee, S
+
+
+def get_pair_terms(h, seq=0):
+    """(grad [n][12], H+ [n][12][12]) of the active pairs of the last iteration (debug >= 1)."""
+    n = C.c_int32(0)
+    _check(lib.pd_ipc_get_pair_terms(h, seq, None, None, C.byref(n)), h)
+    g = np.empty((n.value, 12))
+    hp = np.empty((n.value, 78))
+    _check(lib.pd_ipc_get_pair_terms(h, seq, _dp(g), _dp(hp), C.byref(n)), h)
+    iu = np.triu_indices(12)
+    H = np.zeros((n.value, 12, 12))
+    H[:, iu[0], iu[1]] = hp
+    H[:, iu[1], iu[0]] = hp
+    return g, H
 
 
 def get_vector(h, n_verts, which, seq=0):

@@ -88,6 +88,15 @@ def test_c1_lockstep(P, c1_oracle):
         assert np.array_equal(pt, rpt), f"iteration {k}: PT set differs"
         assert np.array_equal(ee, ree), f"iteration {k}: EE set differs"
         assert np.array_equal(S, ref["S"]), f"iteration {k}: S differs"
+        # per-pair barrier gradient and PSD-projected Hessian (<= 1e-9 relative)
+        pg, pH = P.get_pair_terms(s.h)
+        rg = [ref["pairs"][kd]["h"] for kd in ("pt", "ee") if ref["pairs"].get(kd) is not None]
+        rH = [ref["pairs"][kd]["Hp"] for kd in ("pt", "ee") if ref["pairs"].get(kd) is not None]
+        if rg:
+            rg, rH = np.concatenate(rg), np.concatenate(rH)
+            assert pg.shape == rg.shape
+            assert _rel(pg, rg) < 1e-9, (k, _rel(pg, rg))
+            assert _rel(pH, rH) < 1e-9, (k, _rel(pH, rH))
         g = P.get_vector(s.h, sc.n_verts, 0)
         gref = np.zeros((sc.n_verts, 3))
         gref[o.mesh.free] = ref["ghat"].reshape(-1, 3)
