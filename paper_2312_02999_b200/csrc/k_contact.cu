@@ -527,7 +527,7 @@ __constant__ unsigned char c_ui[78], c_uj[78];
 constexpr int kPD_WARPS = 4;
 
 // Warp per active pair: grad/hess of d^2 (hyper-dual, one Hessian entry per lane-evaluation),
-// chain rule to d, barrier derivatives, 12x12 H_k, parallel-ordered cyclic Jacobi, clamp,
+// chain rule to d, barrier derivatives, 12x12 H_k, PSD projection by the Newton-Schulz sign iteration,
 // H_k^+ (packed upper, 78) and h_k = kappa b' grad d (12).
 __global__ void __launch_bounds__(kPD_WARPS * 32) k_pair_derivs(
     const unsigned long long *__restrict__ akeys, const int *__restrict__ atype,
@@ -536,6 +536,7 @@ __global__ void __launch_bounds__(kPD_WARPS * 32) k_pair_derivs(
     int *__restrict__ ids_out, double *__restrict__ dmax) {
     __shared__ double Hs[kPD_WARPS][12][13];
     __shared__ double Vs[kPD_WARPS][12][13];
+    __shared__ double Ws[kPD_WARPS][12][13];
     __shared__ double gs[kPD_WARPS][12];
     __shared__ double rot[kPD_WARPS][6][2];
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
@@ -608,76 +609,84 @@ __global__ void __launch_bounds__(kPD_WARPS * 32) k_pair_derivs(
         }
     }
     __syncwarp();
-    // parallel-ordered cyclic Jacobi (round-robin tournament, 11 rounds x 6 disjoint pairs)
+    // PSD projection H+ = (H + H sign(H)) / 2, sign(H) by the Newton-Schulz iteration
+    // X <- X (3 I - X^2) / 2 from X = H / |H|_F: eigenvalues in [-1, 1], zeros stay 0, every
+    // other one converges to +-1 (small ones grow by 1.5 per step).  Stops one step after a step
+    // changes X by less than 1e-10 (Frobenius): the eigenvalues then still short of +-1 are
+    // below ~1e-10 |H| / 1.5^it, and each contributes less than its own size to H+.
     double fro = 0.0;
     for (int e = lane; e < 144; e += 32) fro += H[e / 12][e % 12] * H[e / 12][e % 12];
     fro = warp_sum(fro);
-    for (int sweep = 0; sweep < 20; ++sweep) {
-        double off = 0.0;
-        for (int e = lane; e < 144; e += 32) {
-            int i = e / 12, j = e % 12;
-            if (i != j) off += H[i][j] * H[i][j];
+    const double hinv = fro > 0.0 ? rsqrt(fro) : 0.0;
+    for (int e = lane; e < 144; e += 32) V[e / 12][e % 12] = H[e / 12][e % 12] * hinv;   // X
+    __syncwarp();
+    double (*X2)[13] = Ws[wl];
+    bool settled = false;
+    for (int it = 0; it < 120; ++it) {
+        double x2[5];
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {                     // X2 = X X
+            const int e = lane + 32 * q;
+            x2[q] = 0.0;
+            if (e < 144) {
+                const int i2 = e / 12, j2 = e % 12;
+                double acc = 0.0;
+#pragma unroll
+                for (int kk = 0; kk < 12; ++kk) acc += V[i2][kk] * V[kk][j2];
+                x2[q] = acc;
+            }
         }
-        off = warp_sum(off);
-        if (off <= 1e-26 * fro) break;   // off-diagonal norm <= 1e-13 of the Frobenius norm
-        for (int round = 0; round < 11; ++round) {
-            // pairs of the round: players 0..11, player 11 fixed, others rotate
-            if (lane < 6) {
-                int pa, pb;
-                if (lane == 0) { pa = 11; pb = round; }
-                else { pa = (round + lane) % 11; pb = (round + 11 - lane) % 11; }
-                int p = min(pa, pb), q = max(pa, pb);
-                double apq = H[p][q], cth = 1.0, sth = 0.0;
-                if (fabs(apq) > 1e-300) {
-                    double tau = (H[q][q] - H[p][p]) / (2.0 * apq);
-                    double tt = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                    cth = 1.0 / sqrt(1.0 + tt * tt);
-                    sth = tt * cth;
-                }
-                rot[wl][lane][0] = cth;
-                rot[wl][lane][1] = sth;
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            const int e = lane + 32 * q;
+            if (e < 144) X2[e / 12][e % 12] = x2[q];
+        }
+        __syncwarp();
+        double xn[5], dl = 0.0;
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {                     // X <- 1.5 X - 0.5 X X2
+            const int e = lane + 32 * q;
+            xn[q] = 0.0;
+            if (e < 144) {
+                const int i2 = e / 12, j2 = e % 12;
+                double acc = 0.0;
+#pragma unroll
+                for (int kk = 0; kk < 12; ++kk) acc += V[i2][kk] * X2[kk][j2];
+                xn[q] = 1.5 * V[i2][j2] - 0.5 * acc;
+                dl += (xn[q] - V[i2][j2]) * (xn[q] - V[i2][j2]);
             }
-            __syncwarp();
-            // rows: H <- J^T H
-            for (int e = lane; e < 72; e += 32) {
-                int pr = e / 12, m = e % 12;
-                int pa, pb;
-                if (pr == 0) { pa = 11; pb = round; }
-                else { pa = (round + pr) % 11; pb = (round + 11 - pr) % 11; }
-                int p = min(pa, pb), q = max(pa, pb);
-                double cth = rot[wl][pr][0], sth = rot[wl][pr][1];
-                double hp = H[p][m], hq = H[q][m];
-                H[p][m] = cth * hp - sth * hq;
-                H[q][m] = sth * hp + cth * hq;
-            }
-            __syncwarp();
-            // columns: H <- H J, V <- V J
-            for (int e = lane; e < 72; e += 32) {
-                int pr = e / 12, m = e % 12;
-                int pa, pb;
-                if (pr == 0) { pa = 11; pb = round; }
-                else { pa = (round + pr) % 11; pb = (round + 11 - pr) % 11; }
-                int p = min(pa, pb), q = max(pa, pb);
-                double cth = rot[wl][pr][0], sth = rot[wl][pr][1];
-                double hp = H[m][p], hq = H[m][q];
-                H[m][p] = cth * hp - sth * hq;
-                H[m][q] = sth * hp + cth * hq;
-                double vp = V[m][p], vq = V[m][q];
-                V[m][p] = cth * vp - sth * vq;
-                V[m][q] = sth * vp + cth * vq;
-            }
-            __syncwarp();
+        }
+        __syncwarp();
+        // keep X exactly symmetric: rounding asymmetry would otherwise seed non-normal
+        // components that the iteration amplifies by 1.5 per step
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            const int e = lane + 32 * q;
+            if (e < 144) X2[e / 12][e % 12] = xn[q];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            const int e = lane + 32 * q;
+            if (e < 144) V[e / 12][e % 12] = 0.5 * (X2[e / 12][e % 12] + X2[e % 12][e / 12]);
+        }
+        dl = warp_sum(dl);
+        __syncwarp();
+        if (dl <= 1e-20) {                 // quadratic phase reached: one more step, then stop
+            if (settled) break;
+            settled = true;
         }
     }
-    // H^+ = sum_m max(lambda_m, 0) v_m v_m^T, packed upper
+    // H+ = (H + H X) / 2 symmetrized, packed upper
     double mx = lane < 12 ? fabs(kappa * b1 * (gs[wl][lane] / (2.0 * d))) : 0.0;
     for (int e = lane; e < 78; e += 32) {
-        int i = c_ui[e], j = c_uj[e];
-        double acc = 0.0;
-        for (int m = 0; m < 12; ++m) {
-            double l = H[m][m];
-            if (l > 0.0) acc += l * V[i][m] * V[j][m];
+        const int i = c_ui[e], j = c_uj[e];
+        double a1 = 0.0, a2 = 0.0;
+        for (int kk = 0; kk < 12; ++kk) {
+            a1 += H[i][kk] * V[kk][j];
+            a2 += V[i][kk] * H[kk][j];
         }
+        const double acc = 0.5 * H[i][j] + 0.25 * (a1 + a2);
         Hp[78 * (size_t)k + e] = acc;
         mx = fmax(mx, fabs(acc));
     }
