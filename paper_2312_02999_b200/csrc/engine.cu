@@ -136,7 +136,21 @@ struct KTimer {
     void stop(int k, cudaStream_t st) {
         if (on && (mask >> k & 1)) { record_event(ev[slot][k][1], st); used[slot][k] = true; }
     }
+    bool timeline = false;          // PDIPC_TIMELINE=1: print start/stop offsets of every group
     void collect(int n_slots) {     // after a stream synchronize: the first n_slots iterations
+        if (timeline)
+            for (int i = 0; i < n_slots; ++i) {
+                if (!used[i][K_LOCAL]) continue;
+                std::fprintf(stderr, "timeline it %d:", i);
+                for (int k = 0; k < K_NUM; ++k)
+                    if (used[i][k]) {
+                        float a, b;
+                        CK(cudaEventElapsedTime(&a, ev[i][K_LOCAL][0], ev[i][k][0]));
+                        CK(cudaEventElapsedTime(&b, ev[i][K_LOCAL][0], ev[i][k][1]));
+                        std::fprintf(stderr, " %s=[%.1f,%.1f]", kKernelNames[k], 1e3 * a, 1e3 * b);
+                    }
+                std::fprintf(stderr, "\n");
+            }
         for (int i = 0; i < kMaxBatch; ++i)
             for (int k = 0; k < K_NUM; ++k)
                 if (used[i][k]) {
@@ -824,6 +838,7 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         h->tm.init();
         h->kt.init();
         if (const char *ng = std::getenv("PDIPC_NO_GRAPH")) h->graphs = !(ng[0] == '1');
+        if (const char *tl = std::getenv("PDIPC_TIMELINE")) h->kt.timeline = tl[0] == '1';
         if (const char *sc = std::getenv("PDIPC_SIDE_CTAS")) h->side_ctas = std::max(1, std::atoi(sc));
         if (const char *tp = std::getenv("PDIPC_TRACE")) {
             h->trace_file = std::fopen(tp, "wb");
@@ -831,6 +846,7 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         }
         contact_init();
         trisolve_init();
+        elastic_init(o.device);
         schur_init(o.device);
         HostMesh &m = h->hm;
         HostFactor &f = h->hf;
@@ -1055,7 +1071,8 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             h->Bc.exact((size_t)9 * cS * cS);
             h->ldh = 3 * cS + 8;
             h->Sh.exact((size_t)(3 * cS + 1) * h->ldh);
-            h->Lstore.exact((size_t)((3 * cS + 1 + 63) / 64 + 1) * 64 * 64);
+            // large systems: Li tiles [nt+1][64][64]; small: D blocks [nt+1][512] + X tiles [nt][64][64]
+            h->Lstore.exact((size_t)((3 * cS + 1 + 63) / 64 + 1) * (64 * 64 + 512));
             h->U.exact((size_t)(cS + 64) * 64);
             h->yS.exact(3 * (size_t)cS);
             h->rhs.exact(3 * (size_t)cS);

@@ -6,6 +6,9 @@
 // R_i using the polar decomposition of F_i A_i" in parallel over elements.
 // PAPER.md:97,113 (Eq. 4): elastic gradient sum_i w_i G_i^T (G_i x - p_i).
 // s = W x.
+#include <algorithm>
+#include <cstdlib>
+
 #include "kernels.h"
 
 #include "dev_common.cuh"
@@ -125,14 +128,9 @@ __device__ void polar_rotation(const double M[3][3], double R[3][3]) {
 // X^{-T} from the cofactor matrix and the Frobenius scaling g = (|X^{-1}|_F / |X|_F)^{1/2}.  For
 // det M > 0 it converges quadratically to the unique R in SO(3) with M = R U (the same R as the
 // SVD route); 4-6 iterations at the strains of the workloads, no eigen-decomposition.  Returns
-// false when det M <= 0 (the caller takes the SVD route with the reflection fix).
-__device__ __forceinline__ bool polar_newton(const double M[3][3], double R[3][3]) {
-    double X[3][3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) X[i][j] = M[i][j];
-    bool last = false;
+// false when det M <= 0, with X still equal to M (the caller takes the SVD route with the
+// reflection fix).  In place: X = M on entry, R on exit.
+__device__ __forceinline__ bool polar_newton(double X[3][3]) {
     for (int it = 0; it < 16; ++it) {
         double C[3][3];
         C[0][0] = X[1][1] * X[2][2] - X[1][2] * X[2][1];
@@ -170,15 +168,11 @@ __device__ __forceinline__ bool polar_newton(const double M[3][3], double R[3][3
                 delta += (v - X[i][j]) * (v - X[i][j]);
                 X[i][j] = v;
             }
-        if (last) break;
-        // quadratic convergence: once the step is below ~1e-9 (relative; |X| ~ sqrt 3) the next
-        // one lands at rounding level, so take exactly one more
-        last = delta <= 3e-18;
+        // quadratic convergence (Higham): |X_{k+1} - R| <= |X_k^{-1}| |X_k - R|^2 / 2 with
+        // |X_k - R| ~ |X_{k+1} - X_k|, so a step below 1e-9 (|X| ~ sqrt 3) leaves X_{k+1} at
+        // rounding level: stop
+        if (delta <= 1e-18) break;
     }
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) R[i][j] = X[i][j];
     return true;
 }
 
@@ -187,7 +181,8 @@ __device__ __forceinline__ bool polar_newton(const double M[3][3], double R[3][3
 // B (SoA [9][T]), A (SoA [6][T]), w; writes the per-corner elastic forces
 // f_{i,c} = w_i (F_i - P_i) g_{i,c} as fc[T][4][3] (coalesced 96 B per tet) and, when
 // p != nullptr, p_i = vec(R_i A_i) (SoA [9][T]) for the parity hook.
-__global__ void __launch_bounds__(128, 5) k_local_step(
+template <int MINB>
+__global__ void __launch_bounds__(128, MINB) k_local_step(
     const int4 *__restrict__ tets, const double4 *__restrict__ x, const double *__restrict__ B,
     const double *__restrict__ A6, const double *__restrict__ w, int T, double *__restrict__ fc,
     double *__restrict__ p) {
@@ -207,7 +202,7 @@ __global__ void __launch_bounds__(128, 5) k_local_step(
     const double Ds[3][3] = {{x1.x - x0.x, x2.x - x0.x, x3.x - x0.x},
                              {x1.y - x0.y, x2.y - x0.y, x3.y - x0.y},
                              {x1.z - x0.z, x2.z - x0.z, x3.z - x0.z}};
-    double F[3][3], M[3][3], R[3][3], P[3][3];
+    double F[3][3], R[3][3], P[3][3];
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
@@ -215,8 +210,12 @@ __global__ void __launch_bounds__(128, 5) k_local_step(
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
-        for (int b = 0; b < 3; ++b) M[a][b] = F[a][0] * A[0][b] + F[a][1] * A[1][b] + F[a][2] * A[2][b];
-    if (!polar_newton(M, R)) polar_rotation(M, R);   // det <= 0: SVD route, reflection fix
+        for (int b = 0; b < 3; ++b) R[a][b] = F[a][0] * A[0][b] + F[a][1] * A[1][b] + F[a][2] * A[2][b];
+    if (!polar_newton(R)) {                          // det <= 0: SVD route, reflection fix
+        const double M[3][3] = {{R[0][0], R[0][1], R[0][2]}, {R[1][0], R[1][1], R[1][2]},
+                                {R[2][0], R[2][1], R[2][2]}};
+        polar_rotation(M, R);
+    }
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
@@ -252,9 +251,11 @@ __global__ void __launch_bounds__(128, 5) k_local_step(
 // g_el[q] = sum over incidences (t, c) of vertex q2v[q] of f_{t,c}: transpose-CSR gather in
 // factor order, deterministic, no atomics.  Output double4 [nf] (w = 0).
 // 8 lanes per free vertex: lane l sums the incident corner forces l, l+8, ... of the vertex's
-// transpose-incidence list (independent loads in flight), then a fixed xor tree over the 8
-// lanes (deterministic order).
+// transpose-incidence list, then a fixed xor tree over the 8 lanes (deterministic order).  The
+// index loads of a lane are issued together (up to kGatherBatch), then all their force loads,
+// so the index -> force dependency costs one memory latency per batch, not per incidence.
 constexpr int kGatherLanes = 8;
+constexpr int kGatherBatch = 4;
 __global__ void __launch_bounds__(256) k_gather_elastic(const int *__restrict__ inc_ptr, const int *__restrict__ inc,
                                                         const double *__restrict__ fc, int nf,
                                                         double4 *__restrict__ g) {
@@ -263,12 +264,31 @@ __global__ void __launch_bounds__(256) k_gather_elastic(const int *__restrict__ 
     double gx = 0, gy = 0, gz = 0;
     if (q < nf) {
         const int k0 = __ldg(inc_ptr + q), k1 = __ldg(inc_ptr + q + 1);
-        for (int k = k0 + l; k < k1; k += kGatherLanes) {
-            const int tc = __ldg(inc + k);
-            const double *f = fc + 12 * (size_t)(tc >> 2) + 3 * (tc & 3);
-            gx += f[0];
-            gy += f[1];
-            gz += f[2];
+        for (int kb = k0 + l; kb < k1; kb += kGatherLanes * kGatherBatch) {
+            int tc[kGatherBatch];
+#pragma unroll
+            for (int u = 0; u < kGatherBatch; ++u) {
+                const int k = kb + u * kGatherLanes;
+                tc[u] = k < k1 ? __ldg(inc + k) : -1;
+            }
+            double f[kGatherBatch][3];
+#pragma unroll
+            for (int u = 0; u < kGatherBatch; ++u) {
+                if (tc[u] >= 0) {
+                    const double *p = fc + 12 * (size_t)(tc[u] >> 2) + 3 * (tc[u] & 3);
+                    f[u][0] = __ldcs(p);
+                    f[u][1] = __ldcs(p + 1);
+                    f[u][2] = __ldcs(p + 2);
+                } else {
+                    f[u][0] = f[u][1] = f[u][2] = 0.0;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kGatherBatch; ++u) {   // same order as one incidence at a time
+                gx += f[u][0];
+                gy += f[u][1];
+                gz += f[u][2];
+            }
         }
     }
 #pragma unroll
@@ -393,12 +413,21 @@ void launch_set_double(double *p, double v, cudaStream_t st) { PDI_LAUNCH(k_set_
 void launch_ingest_actuation(const double *A9, double *A6, int T, cudaStream_t st) {
     PDI_LAUNCH(k_ingest_actuation, (T + 255) / 256, 256, 0, st)(A9, A6, T);
 }
+static int g_ls_minb = 4;   // resident CTAs per SM the local step is compiled for (PDIPC_LS_MINB)
+void elastic_init(int) {
+    if (const char *e = std::getenv("PDIPC_LS_MINB")) g_ls_minb = std::atoi(e);
+}
 void launch_local_step(const int4 *tets, const double4 *x, const double *B, const double *A6,
                        const double *w, int T, double *fc, double *p, cudaStream_t st) {
-    PDI_LAUNCH(k_local_step, (T + 127) / 128, 128, 0, st)(tets, x, B, A6, w, T, fc, p);
+    if (T <= 0) return;
+    if (g_ls_minb == 5)
+        PDI_LAUNCH(k_local_step<5>, (T + 127) / 128, 128, 0, st)(tets, x, B, A6, w, T, fc, p);
+    else
+        PDI_LAUNCH(k_local_step<4>, (T + 127) / 128, 128, 0, st)(tets, x, B, A6, w, T, fc, p);
 }
 void launch_gather_elastic(const int *inc_ptr, const int *inc, const double *fc, int nf,
                            double4 *g, cudaStream_t st) {
+    if (nf <= 0) return;
     PDI_LAUNCH(k_gather_elastic, (int)(((long long)nf * kGatherLanes + 255) / 256), 256, 0, st)(inc_ptr, inc, fc,
                                                                                              nf, g);
 }

@@ -25,8 +25,12 @@ constexpr int TB = 64;          // tile
 constexpr int TS = 68;          // smem tile stride (DMMA-friendly)
 constexpr int NT = 256;         // threads per CTA
 constexpr int kPW = 4;          // P3 panel width in tiles (trailing update once per panel)
-constexpr int kPWMinTiles = 24; // ... for systems of at least this many tiles
+constexpr int kPWMinTiles = 21; // ... for systems of at least this many tiles (m >= 1280)
 constexpr int kLPTiles = kPWMinTiles;   // small-system P3: panel tiles per step
+// 4 tiles (P0-P3); the small-system P4 needs y, u (m each), 2 X tiles and 8 partial rows
+constexpr int kSmallMaxM = TB * (kPWMinTiles - 1);
+constexpr int kSchurSmem = (10 * kSmallMaxM + 8 + 2 * 64 * 65) * (int)sizeof(double);   // y, u, X[2], 8 partials
+static_assert(kSchurSmem >= 4 * TB * TS * (int)sizeof(double), "smem");
 
 __device__ __forceinline__ void dmma_884(double &d0, double &d1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -292,6 +296,207 @@ __device__ void tile_chol64(double *S, double *Li, int nb, int free_row, int *in
     if (bad) atomicExch(info, 1);
 }
 
+
+// ---------------------------------------------------------------- small-system tile kernels --
+// One thread: Cholesky of the 8x8 diagonal block at S (stride TS, lower part read) in
+// registers, L written back to S, the reciprocal pivots to rinv[0..7].  Returns true on a bad
+// pivot below free_row (relative to the block).
+__device__ __forceinline__ bool chol8_fac(double *S, double *rinv, int free_row) {
+    double a[8][8];
+    bool bad = false;
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) a[r][c] = c <= r ? S[r * TS + c] : 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        double p = a[k][k];
+        bad |= !(p > 0.0) && k < free_row;
+        p = p > 0.0 ? p : 1.0;
+        const double rs = rsqrt(p);
+        rinv[k] = rs;
+        a[k][k] = p * rs;
+#pragma unroll
+        for (int r = k + 1; r < 8; ++r) a[r][k] *= rs;
+#pragma unroll
+        for (int r = k + 1; r < 8; ++r)
+#pragma unroll
+            for (int l = k + 1; l <= r; ++l) a[r][l] -= a[r][k] * a[l][k];
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c <= r; ++c) S[r * TS + c] = a[r][c];
+    return bad;
+}
+
+// One thread: row i of a panel block, L_iJ = A_iJ L_JJ^{-T} by forward substitution with the
+// factored 8x8 block Ljj (stride TS) and its reciprocal pivots.
+__device__ __forceinline__ void panel_row8(double *row, const double *Ljj, const double *rinv) {
+    double o[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        double acc = row[c];
+#pragma unroll
+        for (int q = 0; q < c; ++q) acc -= o[q] * Ljj[c * TS + q];
+        o[c] = acc * rinv[c];
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) row[c] = o[c];
+}
+
+// Diagonal-tile factor without the explicit inverse: L (in place, lower; upper and padding
+// zeroed, rows >= nb identity) and the inverses D_J of its eight 8x8 diagonal blocks (Dsh[J]),
+// which is all the blocked triangular solves need.  Right-looking over 8-wide block columns
+// with the critical chain on warp 0: per block column J, warp 0 forms the panel rows of block
+// J+1 (lanes 0..7, forward substitution), updates the diagonal block (J+1, J+1) on DMMA and one
+// lane factors it; meanwhile the worker warps 1-3, 5-7 form the other panel rows, D_J, and apply
+// the rank-8 updates A_IL -= L_IJ L_LJ^T of block rows I >= J+2 (warp 4 shares warp 0's SM
+// sub-partition and FP64 pipe and stays idle).  Named barrier 1 (224 threads) hands warp 0's
+// panel rows to the workers.  Pivots at rows >= free_row are not checked.
+#ifdef CHOL_PROBE
+__device__ long long g_cp[8][64];
+#define CP_STAMP(w, i) do { if ((threadIdx.x & 31) == 0) g_cp[w][i] = clock64(); } while (0)
+#else
+#define CP_STAMP(w, i) do {} while (0)
+#endif
+__device__ void tile_chol64_d(double *S, double (*Dsh)[8][9], int nb, int free_row, int *info) {
+    const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+    __shared__ double rinv[64];
+    for (int e = tid; e < TB * TB; e += NT) {
+        const int r = e >> 6, c = e & 63;
+        if (r >= nb || c >= nb) S[r * TS + c] = (r == c) ? 1.0 : 0.0;
+        else if (c > r) S[r * TS + c] = 0.0;
+    }
+    __syncthreads();
+    bool bad = false;
+    if (tid == 0) bad |= chol8_fac(S, rinv, free_row);
+    __syncthreads();
+    const int wk = wid < 4 ? wid - 1 : wid - 2;           // worker index 0..5 (wid 1-3, 5-7)
+    for (int J = 0; J < 8; ++J) {
+        const int j0 = 8 * J, j1 = j0 + 8;
+        if (wid == 0) {
+            if (J < 7) {
+                CP_STAMP(0, 4 * J);
+                if (lane < 8) panel_row8(S + (j1 + lane) * TS + j0, S + j0 * TS + j0, rinv + j0);
+                __syncwarp();
+                CP_STAMP(0, 4 * J + 1);
+                asm volatile("bar.arrive 1, 224;\n" ::: "memory");
+                tile8_sub_xyt(S + j1 * TS + j1, S + j1 * TS + j0, S + j1 * TS + j0, TS, 1, true);
+                __syncwarp();
+                CP_STAMP(0, 4 * J + 2);
+                if (lane == 0) bad |= chol8_fac(S + j1 * TS + j1, rinv + j1, free_row - j1);
+                CP_STAMP(0, 4 * J + 3);
+            }
+        } else if (wid != 4) {
+            const int wt = wk * 32 + lane;
+            if (wid == 1) CP_STAMP(1, 4 * J);
+            if (j1 + 8 + wt < 64) panel_row8(S + (j1 + 8 + wt) * TS + j0, S + j0 * TS + j0, rinv + j0);
+            if (wt >= 160 && wt < 168) {                    // D_J column c = L_JJ^{-1} e_c
+                const int c = wt - 160;
+                double x[8];
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    double acc = r == c ? 1.0 : 0.0;
+#pragma unroll
+                    for (int q = 0; q < r; ++q) acc -= S[(j0 + r) * TS + j0 + q] * x[q];
+                    x[r] = r >= c ? acc * rinv[j0 + r] : 0.0;
+                    Dsh[J][r][c] = x[r];
+                }
+            }
+            if (wid == 1) CP_STAMP(1, 4 * J + 1);
+            if (J < 7) {
+                asm volatile("bar.sync 1, 224;\n" ::: "memory");
+                if (wid == 1) CP_STAMP(1, 4 * J + 2);
+                const int I = J + 2 + wk;                  // block row of this worker
+                if (I < 8)
+                    for (int L = J + 1; L <= I; ++L)
+                        tile8_sub_xyt(S + 8 * I * TS + 8 * L, S + 8 * I * TS + j0, S + 8 * L * TS + j0, TS, 1,
+                                      I == L);
+                if (wid == 1) CP_STAMP(1, 4 * J + 3);
+            }
+        }
+        __syncthreads();
+        if (wid == 2) CP_STAMP(2, J);
+    }
+    if (bad) atomicExch(info, 1);
+}
+
+// X <- X L^{-T} for a 64x64 tile X (rows independent) with L the factored diagonal tile and
+// Dsh its 8x8 diagonal-block inverses: per 8-wide block column J,
+// X_J = (X_J - sum_{K<J} X_K L_JK^T) D_J^T.  Warp w owns rows 8w..8w+7 (no CTA barrier inside;
+// the caller's __syncthreads publishes X).
+__device__ __forceinline__ void tile_trsm_d(double *X, const double *L, const double (*Dsh)[8][9]) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int gr = lane >> 2, gc = lane & 3;
+    double *xr = X + (8 * w + gr) * TS;
+    for (int J = 0; J < 8; ++J) {
+        double c0 = xr[8 * J + 2 * gc], c1 = xr[8 * J + 2 * gc + 1], e0 = 0.0, e1 = 0.0;
+        for (int K = 0; K < J; K += 2) {                   // two independent DMMA chains
+#pragma unroll
+            for (int k4 = 0; k4 < 2; ++k4)
+                dmma_884(c0, c1, -xr[8 * K + 4 * k4 + gc], L[(8 * J + gr) * TS + 8 * K + 4 * k4 + gc]);
+            if (K + 1 < J) {
+#pragma unroll
+                for (int k4 = 0; k4 < 2; ++k4)
+                    dmma_884(e0, e1, -xr[8 * K + 8 + 4 * k4 + gc], L[(8 * J + gr) * TS + 8 * K + 8 + 4 * k4 + gc]);
+            }
+        }
+        xr[8 * J + 2 * gc] = c0 + e0;
+        xr[8 * J + 2 * gc + 1] = c1 + e1;
+        __syncwarp();
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int k4 = 0; k4 < 2; ++k4) dmma_884(d0, d1, xr[8 * J + 4 * k4 + gc], Dsh[J][gr][4 * k4 + gc]);
+        __syncwarp();
+        xr[8 * J + 2 * gc] = d0;
+        xr[8 * J + 2 * gc + 1] = d1;
+        __syncwarp();
+    }
+}
+
+// C -= X X^T on the 36 lower 8x8 blocks of a 64x64 tile (the upper blocks are not touched);
+// warp w accumulates blocks w, w+8, ... in registers (independent DMMA chains)
+__device__ __forceinline__ void tile_syrk_lower_sub(double *C, const double *X) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int gr = lane >> 2, gc = lane & 3;
+    double acc[5][2];
+    int bi[5], bl[5];
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+        const int b = w + 8 * j;
+        int I = 0, u = b < 36 ? b : 0;
+        while (u > I) { u -= I + 1; ++I; }
+        bi[j] = I;
+        bl[j] = u;
+        acc[j][0] = b < 36 ? C[(8 * I + gr) * TS + 8 * u + 2 * gc] : 0.0;
+        acc[j][1] = b < 36 ? C[(8 * I + gr) * TS + 8 * u + 2 * gc + 1] : 0.0;
+    }
+#pragma unroll 4
+    for (int k4 = 0; k4 < TB / 4; ++k4) {
+#pragma unroll
+        for (int j = 0; j < 5; ++j)
+            if (w + 8 * j < 36)
+                dmma_884(acc[j][0], acc[j][1], -X[(8 * bi[j] + gr) * TS + 4 * k4 + gc],
+                         X[(8 * bl[j] + gr) * TS + 4 * k4 + gc]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 5; ++j)
+        if (w + 8 * j < 36) {
+            C[(8 * bi[j] + gr) * TS + 8 * bl[j] + 2 * gc] = acc[j][0];
+            C[(8 * bi[j] + gr) * TS + 8 * bl[j] + 2 * gc + 1] = acc[j][1];
+        }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void st_dblocks(const double (*Dsh)[8][9], double *dst) {
+    for (int e = threadIdx.x; e < 512; e += NT) dst[e] = Dsh[e >> 6][(e >> 3) & 7][e & 7];
+}
+__device__ __forceinline__ void ld_dblocks(double (*Dsh)[8][9], const double *src) {
+    for (int e = threadIdx.x; e < 512; e += NT) Dsh[e >> 6][(e >> 3) & 7][e & 7] = src[e];
+}
+
 // ---------------------------------------------------------------- the kernel ---------------
 __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
     extern __shared__ double sm[];
@@ -543,15 +748,19 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
     if (nt < kPWMinTiles) {
         // Small systems (latency-bound): ONE grid barrier per tile column.  Step k: every CTA
         // updates one tile (i, j), k < j <= i, recomputing the panel tiles it needs
-        // (L_ik = A_ik Li_k^T) itself; CTA 0 takes (k+1, k+1) and then factors it (look-ahead).
-        // L_ik go to a ping-pong scratch (A_ik is still read by other CTAs in the step) and are
-        // written into the factor one step later.
+        // (L_ik = A_ik L_kk^{-T}, blocked triangular solve with the 8x8 diagonal-block inverses
+        // D_k of the factored tile) itself; CTA 0 takes (k+1, k+1) and then factors it
+        // (look-ahead).  L_ik go to a ping-pong scratch (A_ik is still read by other CTAs in the
+        // step) and are written into the factor one step later.  D_k is kept in Lstore[k * 512].
+        __shared__ double Dsh[2][8][8][9];   // [0] D_k of the step, [1] the look-ahead tile's
+        double *Dst = a.Lstore;
         if (bid == 0) {
             ld_tile(T0, a.Sh, a.ldh, min(TB, ma), min(TB, ma));
             __syncthreads();
-            tile_chol64(T0, T1, min(TB, ma), m, a.info);
+            tile_chol64_d(T0, Dsh[0], min(TB, ma), m, a.info);
+            __syncthreads();
             st_tile(T0, a.Sh, a.ldh, min(TB, ma), min(TB, ma));
-            for (int e = tid; e < TB * TB; e += NT) a.Lstore[e] = T1[(e >> 6) * TS + (e & 63)];
+            st_dblocks(Dsh[0], Dst);
         }
         GSYNC();
         for (int k = 0; k < nt; ++k) {
@@ -568,37 +777,62 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
                     if (r0 + r < ma && (k - 1) * TB + c < ma)
                         a.Sh[(size_t)(r0 + r) * a.ldh + (k - 1) * TB + c] = LPp[(size_t)t * TB * TB + q];
                 }
+            // X_k = L_kk^{-T} (for the back substitution P4) on the first CTA without a tile this
+            // step (the last CTA when every CTA has one): X = I L_kk^{-T}, blocked solve
+            if (bid == (ntile < G ? ntile : G - 1)) {
+                ld_tile(T1, a.Sh + (size_t)kc0 * a.ldh + kc0, a.ldh, kn, kn);
+                ld_dblocks(Dsh[0], Dst + (size_t)k * 512);
+                __syncthreads();
+                for (int e = tid; e < TB * TB; e += NT) {
+                    const int r = e >> 6, c = e & 63;
+                    if (r >= kn || c >= kn) T1[r * TS + c] = (r == c) ? 1.0 : 0.0;
+                    T0[r * TS + c] = (r == c) ? 1.0 : 0.0;
+                }
+                __syncthreads();
+                tile_trsm_d(T0, T1, Dsh[0]);
+                __syncthreads();
+                st_tile(T0, Dst + (size_t)512 * (nt + 1) + (size_t)k * TB * TB, TB, TB, TB);
+                __syncthreads();
+            }
+            if (bid < ntile) {
+                // factored diagonal tile k (T1) and its block inverses
+                ld_tile(T1, a.Sh + (size_t)kc0 * a.ldh + kc0, a.ldh, kn, kn);
+                ld_dblocks(Dsh[0], Dst + (size_t)k * 512);
+                __syncthreads();
+                if (kn < TB)                                 // padding rows: identity (as factored)
+                    for (int e = tid; e < TB * TB; e += NT) {
+                        const int r = e >> 6, c = e & 63;
+                        if (r >= kn || c >= kn) T1[r * TS + c] = (r == c) ? 1.0 : 0.0;
+                    }
+                __syncthreads();
+            }
             for (int b = bid; b < ntile; b += G) {
                 // b == 0 -> the look-ahead tile (k+1, k+1) on CTA 0
                 int i = 0, bb = b;
                 while (bb >= rr - i) { bb -= rr - i; ++i; }
                 const int tj = k + 1 + i, ti = tj + bb;
                 const int r0 = ti * TB, c0 = tj * TB, rows = min(TB, ma - r0), cols = min(TB, ma - c0);
-                // L_ik (T2), L_jk (T3)
+                // L_ik (T0), L_jk (T3)
                 ld_tile(T0, a.Sh + (size_t)r0 * a.ldh + kc0, a.ldh, rows, kn);
-                ld_tile(T1, a.Lstore + (size_t)k * TB * TB, TB, TB, TB);
+                if (tj != ti) ld_tile(T3, a.Sh + (size_t)c0 * a.ldh + kc0, a.ldh, cols, kn);
                 __syncthreads();
-                tile_xyt(T2, T0, T1, 1.0, false);
-                double *Ljk = T2;
-                if (tj != ti) {
-                    ld_tile(T0, a.Sh + (size_t)c0 * a.ldh + kc0, a.ldh, cols, kn);
-                    __syncthreads();
-                    tile_xyt(T3, T0, T1, 1.0, false);
-                    Ljk = T3;
-                } else {                                     // the diagonal-tile CTA keeps L_ik
+                tile_trsm_d(T0, T1, Dsh[0]);
+                if (tj != ti) tile_trsm_d(T3, T1, Dsh[0]);
+                __syncthreads();
+                if (tj == ti)                                // the diagonal-tile CTA keeps L_ik
                     for (int e = tid; e < TB * TB; e += NT)
-                        LPk[(size_t)(ti - k - 1) * TB * TB + e] = T2[(e >> 6) * TS + (e & 63)];
-                }
-                ld_tile(T0, a.Sh + (size_t)r0 * a.ldh + c0, a.ldh, rows, cols);
+                        LPk[(size_t)(ti - k - 1) * TB * TB + e] = T0[(e >> 6) * TS + (e & 63)];
+                ld_tile(T2, a.Sh + (size_t)r0 * a.ldh + c0, a.ldh, rows, cols);
                 __syncthreads();
-                tile_xyt(T0, T2, Ljk, -1.0, true);
+                if (tj == ti) tile_syrk_lower_sub(T2, T0);
+                else tile_xyt(T2, T0, T3, -1.0, true);
                 if (b == 0) {                                // look-ahead: factor tile k+1 now
-                    tile_chol64(T0, T1, rows, m - r0, a.info);
-                    st_tile(T0, a.Sh + (size_t)r0 * a.ldh + c0, a.ldh, rows, cols);
-                    for (int e = tid; e < TB * TB; e += NT)
-                        a.Lstore[(size_t)(k + 1) * TB * TB + e] = T1[(e >> 6) * TS + (e & 63)];
+                    tile_chol64_d(T2, Dsh[1], rows, m - r0, a.info);
+                    __syncthreads();
+                    st_tile(T2, a.Sh + (size_t)r0 * a.ldh + c0, a.ldh, rows, cols);
+                    st_dblocks(Dsh[1], Dst + (size_t)(k + 1) * 512);
                 } else {
-                    st_tile(T0, a.Sh + (size_t)r0 * a.ldh + c0, a.ldh, rows, cols);
+                    st_tile(T2, a.Sh + (size_t)r0 * a.ldh + c0, a.ldh, rows, cols);
                 }
                 __syncthreads();
             }
@@ -687,39 +921,117 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
         }
     }
     // ------------------------------------------------ P4: u = C^{-T} y, y = row m of the factor
-    // right-looking on C^T: u_k = Li_k^T y_k, then y_j -= (C_kj)^T u_k for j < k
     const int ntm = (m + TB - 1) / TB;
-    {
-        // one grid barrier per tile step: every CTA forms u_k = Li_k^T y_k itself (64 x 64, from
-        // L2), CTA 0 publishes it, all CTAs update their slice of y_j -= C_kj^T u_k (j < k).
-        // y lives in a.y (updated in place), u in a.u.
-        for (int e = bid * NT + tid; e < m; e += G * NT) a.y[e] = a.Sh[(size_t)m * a.ldh + e];
+    if (nt < kPWMinTiles) {
+        // Small systems: CTA 0 alone, no grid barrier.  Per 64-row tile k of C from the last:
+        // u_k = X_k y_k with X_k = L_kk^{-T} (formed by P3), then y_j -= sum_r C[kc0+r][j] u_r for
+        // j < kc0 (rows of C read from L2, every load of a thread in flight at once).  X_k is
+        // prefetched into shared memory one tile ahead (cp.async).
+        if (bid == 0) {
+            const int mr = (m + 7) & ~7;
+            double *yv = sm, *uv = sm + mr;                     // y, u  [mr] each
+            double *Xt = sm + 2 * mr;                           // [2][64][65]
+            const double *Xg = a.Lstore + (size_t)512 * (nt + 1);
+            for (int e = tid; e < mr; e += NT) yv[e] = e < m ? a.Sh[(size_t)m * a.ldh + e] : 0.0;
+            auto issue = [&](int k) {
+                if (k >= 0)
+                    for (int e = tid; e < TB * TB; e += NT) {
+                        const unsigned sa = (unsigned)__cvta_generic_to_shared(Xt + (size_t)(k & 1) * 64 * 65 +
+                                                                               (e >> 6) * 65 + (e & 63));
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa),
+                                     "l"(Xg + (size_t)k * TB * TB + e));
+                    }
+                asm volatile("cp.async.commit_group;\n" ::);
+            };
+            const int ntm = (m + TB - 1) / TB;
+            issue(ntm - 1);
+            __syncthreads();
+            for (int k = ntm - 1; k >= 0; --k) {
+                issue(k - 1);
+                asm volatile("cp.async.wait_group 1;\n" ::);
+                __syncthreads();
+                const int kc0 = k * TB, kn = min(TB, m - kc0);
+                const double *X = Xt + (size_t)(k & 1) * 64 * 65;
+                {   // u_i = sum_{r >= i} X[i][r] y_r: 4 partial sums per output
+                    const int i = tid & 63, pq = tid >> 6;
+                    double acc = 0.0;
+                    if (i < kn)
+                        for (int r = i + pq; r < kn; r += 4) acc += X[i * 65 + r] * yv[kc0 + r];
+                    T3[pq * 64 + i] = acc;
+                }
+                __syncthreads();
+                if (tid < kn) uv[kc0 + tid] = T3[tid] + T3[64 + tid] + T3[128 + tid] + T3[192 + tid];
+                __syncthreads();
+                if (a.prof && tid == 0 && np < 1023) a.prof[np++] = gtimer_s();
+                // y_j -= sum_r C[kc0 + r][j] u_r: warp w takes rows w, w + 8, ..., lane the columns
+                // j = lane + 32 q (coalesced rows; 8 rows x 8 columns of loads in flight per chunk);
+                // the 8 warp partials are summed in a fixed order (deterministic)
+                double *part = Xt + 2 * 64 * 65;                // [8][mr]
+                for (int q0 = 0; q0 < kc0; q0 += 256) {
+                    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                    double v[8][8], ur[8];                      // unconditional loads (clamped
+#pragma unroll                                                  // indices): all 64 in flight
+                    for (int rr = 0; rr < 8; ++rr) {
+                        const int r = wid + 8 * rr, rc = min(r, kn - 1);
+                        ur[rr] = r < kn ? uv[kc0 + r] : 0.0;
+                        const double *row = a.Sh + (size_t)(kc0 + rc) * a.ldh;
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) v[rr][q] = __ldcg(row + min(q0 + lane + 32 * q, kc0 - 1));
+                    }
+#pragma unroll
+                    for (int rr = 0; rr < 8; ++rr)
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) acc[q] += v[rr][q] * ur[rr];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int j = q0 + lane + 32 * q;
+                        if (j < kc0) part[wid * mr + j] = acc[q];
+                    }
+                }
+                __syncthreads();
+                for (int j = tid; j < kc0; j += NT)
+                    yv[j] -= ((part[j] + part[mr + j]) + (part[2 * mr + j] + part[3 * mr + j])) +
+                             ((part[4 * mr + j] + part[5 * mr + j]) + (part[6 * mr + j] + part[7 * mr + j]));
+                __syncthreads();                                // this stage is refilled next
+                if (a.prof && tid == 0 && np < 1023) a.prof[np++] = gtimer_s();
+            }
+            asm volatile("cp.async.wait_group 0;\n" ::);
+            for (int e = tid; e < m; e += NT) a.u[e] = uv[e];
+        }
         GSYNC();
-        double *uk = T0, *part = T1;
-        for (int k = ntm - 1; k >= 0; --k) {
-            const int kc0 = k * TB, kn = min(TB, m - kc0);
-            const double *Li = a.Lstore + (size_t)k * TB * TB;
-            {   // u_k[i] = sum_{r >= i} Li[r][i] y_k[r]: 4 partial sums per output
-                const int i = tid & 63, pq = tid >> 6;
-                double acc = 0.0;
-                if (i < kn)
-                    for (int r = i + pq; r < kn; r += 4) acc += Li[r * TB + i] * a.y[kc0 + r];
-                part[pq * TB + i] = acc;
-            }
-            __syncthreads();
-            if (tid < TB) {
-                const double v = tid < kn ? part[tid] + part[TB + tid] + part[2 * TB + tid] + part[3 * TB + tid] : 0.0;
-                uk[tid] = v;
-                if (bid == 0 && tid < kn) a.u[kc0 + tid] = v;
-            }
-            __syncthreads();
-            for (int j = bid * NT + tid; j < kc0; j += G * NT) {   // y_j -= sum_r C[kc0 + r][j] u_k[r]
-                double acc = 0.0;
-#pragma unroll 8
-                for (int r = 0; r < kn; ++r) acc += a.Sh[(size_t)(kc0 + r) * a.ldh + j] * uk[r];
-                a.y[j] -= acc;
-            }
+    } else {
+        {
+            // one grid barrier per tile step: every CTA forms u_k = Li_k^T y_k itself (64 x 64, from
+            // L2), CTA 0 publishes it, all CTAs update their slice of y_j -= C_kj^T u_k (j < k).
+            // y lives in a.y (updated in place), u in a.u.
+            for (int e = bid * NT + tid; e < m; e += G * NT) a.y[e] = a.Sh[(size_t)m * a.ldh + e];
             GSYNC();
+            double *uk = T0, *part = T1;
+            for (int k = ntm - 1; k >= 0; --k) {
+                const int kc0 = k * TB, kn = min(TB, m - kc0);
+                const double *Li = a.Lstore + (size_t)k * TB * TB;
+                {   // u_k[i] = sum_{r >= i} Li[r][i] y_k[r]: 4 partial sums per output
+                    const int i = tid & 63, pq = tid >> 6;
+                    double acc = 0.0;
+                    if (i < kn)
+                        for (int r = i + pq; r < kn; r += 4) acc += Li[r * TB + i] * a.y[kc0 + r];
+                    part[pq * TB + i] = acc;
+                }
+                __syncthreads();
+                if (tid < TB) {
+                    const double v = tid < kn ? part[tid] + part[TB + tid] + part[2 * TB + tid] + part[3 * TB + tid] : 0.0;
+                    uk[tid] = v;
+                    if (bid == 0 && tid < kn) a.u[kc0 + tid] = v;
+                }
+                __syncthreads();
+                for (int j = bid * NT + tid; j < kc0; j += G * NT) {   // y_j -= sum_r C[kc0 + r][j] u_k[r]
+                    double acc = 0.0;
+#pragma unroll 8
+                    for (int r = 0; r < kn; ++r) acc += a.Sh[(size_t)(kc0 + r) * a.ldh + j] * uk[r];
+                    a.y[j] -= acc;
+                }
+                GSYNC();
+            }
         }
     }
     // ------------------------------------------------ P5: t = B u ; Z = w + V t = w_el + V (gc + t)
@@ -747,7 +1059,6 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
     }
 }
 
-constexpr int kSchurSmem = 4 * TB * TS * (int)sizeof(double);
 static int g_schur_grid = 0;
 static double *g_kpart = nullptr;   // split-K partial tiles, grid x 1152 doubles (allocated at init)
 static double *g_lp = nullptr;      // small-system P3 panel scratch

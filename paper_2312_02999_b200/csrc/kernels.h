@@ -32,6 +32,7 @@ void add_launches(long long n);   // graph replays account their captured launch
 // ---- k_elastic.cu
 void launch_set_double(double *p, double v, cudaStream_t st);
 void launch_ingest_actuation(const double *A9, double *A6, int T, cudaStream_t st);
+void elastic_init(int device);
 void launch_local_step(const int4 *tets, const double4 *x, const double *B, const double *A6,
                        const double *w, int T, double *fc, double *p, cudaStream_t st);
 void launch_gather_elastic(const int *inc_ptr, const int *inc, const double *fc, int nf,

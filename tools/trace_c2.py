@@ -32,35 +32,38 @@ while off < len(raw):
 print("traced iterations", len(recs))
 sn = np.loadtxt(path + ".sn", dtype=np.int64)
 w, nr, par = sn[:, 2], sn[:, 3], sn[:, 4]
-tr = recs[-1]
-t0 = tr[:, 1].min()
-sid, tk = tr[:, 0] >> 16, tr[:, 0] & 0xFFFF
-disp, ready, done = tr[:, 1] - t0, tr[:, 2] - t0, tr[:, 3] - t0
-work = done - ready
-print(f"items {len(tr)}  span {done.max() / 1e3:.1f} us  work mean {work.mean() / 1e3:.2f} us  "
-      f"p50 {np.median(work) / 1e3:.2f}  p90 {np.percentile(work, 90) / 1e3:.2f}  max {work.max() / 1e3:.2f}")
-print(f"sum of work {work.sum() / 1e3:.0f} us over {len(tr)} items")
-# per supernode: finish time = max done over its items
-fin = np.zeros(len(w), np.int64)
-start = np.full(len(w), 1 << 62, np.int64)
-for i in range(len(tr)):
-    fin[sid[i]] = max(fin[sid[i]], done[i])
-    start[sid[i]] = min(start[sid[i]], ready[i])
-# walk from the last-finishing root down the latest-finishing child
-r = int(np.argmax(fin))
-chain = [r]
-while True:
-    ch = np.nonzero(par == chain[-1])[0]
-    if len(ch) == 0:
-        break
-    chain.append(int(ch[np.argmax(fin[ch])]))
-print("critical chain (root first): s, w, nr, items, ready-after-children us, work span us")
-for c in chain:
-    ch = np.nonzero(par == c)[0]
-    cf = fin[ch].max() if len(ch) else 0
-    its = np.nonzero(sid == c)[0]
-    print(f"  {c:4d} w {w[c]:3d} nr {nr[c]:4d} items {len(its):3d}  wait {(start[c] - cf) / 1e3:6.2f}  "
-          f"span {(fin[c] - start[c]) / 1e3:6.2f}  maxwork {work[its].max() / 1e3:6.2f}")
+nonempty = [r for r in recs if len(r)]
+if nonempty:
+    tr = nonempty[-1]
+    t0 = tr[:, 1].min()
+    sid, tk = tr[:, 0] >> 16, tr[:, 0] & 0xFFFF
+    disp, ready, done = tr[:, 1] - t0, tr[:, 2] - t0, tr[:, 3] - t0
+    work = done - ready
+    print(f"items {len(tr)}  span {done.max() / 1e3:.1f} us  work mean {work.mean() / 1e3:.2f} us  "
+          f"p50 {np.median(work) / 1e3:.2f}  p90 {np.percentile(work, 90) / 1e3:.2f}  max {work.max() / 1e3:.2f}")
+    print(f"sum of work {work.sum() / 1e3:.0f} us over {len(tr)} items")
+    # per supernode: finish time = max done over its items
+    fin = np.zeros(len(w), np.int64)
+    start = np.full(len(w), 1 << 62, np.int64)
+    for i in range(len(tr)):
+        fin[sid[i]] = max(fin[sid[i]], done[i])
+        start[sid[i]] = min(start[sid[i]], ready[i])
+    # walk from the last-finishing root down the latest-finishing child
+    r = int(np.argmax(fin))
+    chain = [r]
+    while True:
+        ch = np.nonzero(par == chain[-1])[0]
+        if len(ch) == 0:
+            break
+        chain.append(int(ch[np.argmax(fin[ch])]))
+    print("critical chain (root first): s, w, nr, items, ready-after-children us, work span us")
+    for c in chain:
+        ch = np.nonzero(par == c)[0]
+        cf = fin[ch].max() if len(ch) else 0
+        its = np.nonzero(sid == c)[0]
+        print(f"  {c:4d} w {w[c]:3d} nr {nr[c]:4d} items {len(its):3d}  wait {(start[c] - cf) / 1e3:6.2f}  "
+              f"span {(fin[c] - start[c]) / 1e3:6.2f}  maxwork {work[its].max() / 1e3:6.2f}")
+
 
 # ---- fused Schur kernel: time between consecutive grid barriers (last traced call)
 sp = path + ".schur"
@@ -69,9 +72,10 @@ if os.path.exists(sp):
     rec = 4 + 8 * 1024
     nrec = len(raw) // rec
     (nS,) = struct.unpack_from("i", raw, (nrec - 1) * rec)
-    ts = np.frombuffer(raw, np.uint64, 1024, (nrec - 1) * rec + 4).astype(np.int64)
-    print("records", nrec, "nonzero per record", [int((np.frombuffer(raw, np.uint64, 1024, r * rec + 4) > 0).sum()) for r in range(max(0, nrec - 5), nrec)])
-    ts = ts[ts > 0]
-    d = np.diff(ts) / 1e3
-    print(f"schur nS {nS}: {len(d)} barrier intervals, total {d.sum():.1f} us")
-    print("  intervals (us):", " ".join(f"{x:.1f}" for x in d))
+    for r in range(max(0, nrec - 6), nrec):
+        (nS,) = struct.unpack_from("i", raw, r * rec)
+        ts = np.frombuffer(raw, np.uint64, 1024, r * rec + 4).astype(np.int64)
+        ts = ts[ts > 0]
+        d = np.diff(ts) / 1e3
+        print(f"schur nS {nS}: {len(d)} barrier intervals, total {d.sum():.1f} us")
+        print("  intervals (us):", " ".join(f"{x:.1f}" for x in d))
