@@ -377,12 +377,12 @@ static void broad_phase(pd_ipc *h, const double4 *ds, double infl, int *ccnt, in
     launch_boxes(h->s.p, ds, h->tris.p, h->edges.p, Ns, Nt, Ne, infl, h->blo.p, h->bhi.p, ext, st);
     const unsigned M = h->hmask + 1;
     const int nq = Ns + Ne, cap_ent = (int)h->hent.n;
-    CK(cudaMemsetAsync(hovf, 0, sizeof(int), st));
+    CK(dev_zero(hovf, sizeof(int), st));
     // both tables (tris, edges) in one pass each: count, scan, fill
-    CK(cudaMemsetAsync(h->hcnt.p, 0, sizeof(int) * 2 * (M + 1), st));
+    CK(dev_zero(h->hcnt.p, sizeof(int) * 2 * (M + 1), st));
     launch_hash_insert(h->blo.p, h->bhi.p, Ns, Nt, Ne, ext, h->hmask, h->hcnt.p, nullptr, nullptr, 0, hovf, st);
     scan_exclusive(h->hcnt.p, h->hstart.p, (int)(2 * (M + 1)), h->iscr.p, st);
-    CK(cudaMemsetAsync(h->hcnt.p, 0, sizeof(int) * 2 * (M + 1), st));
+    CK(dev_zero(h->hcnt.p, sizeof(int) * 2 * (M + 1), st));
     launch_hash_insert(h->blo.p, h->bhi.p, Ns, Nt, Ne, ext, h->hmask, h->hcnt.p, h->hstart.p, h->hent.p,
                        cap_ent, hovf, st);
     // one warp per query (PT points, then EE edges): sorted unique partner lists
@@ -405,11 +405,11 @@ static void broad_phase_sort(pd_ipc *h, const double4 *ds, double infl, int *ccn
     const unsigned M = h->hmask + 1;
     int *cnt_pt = h->dint.p + D_SORT, *cnt_ee = h->dint.p + D_SORT + 1;
     int *ovf = h->dint.p + D_SORT + 2;   // cannot trip: uncapped cells bound entries by 8 per box
-    CK(cudaMemsetAsync(ovf, 0, sizeof(int), st));
-    CK(cudaMemsetAsync(h->hcnt.p, 0, sizeof(int) * 2 * (M + 1), st));
+    CK(dev_zero(ovf, sizeof(int), st));
+    CK(dev_zero(h->hcnt.p, sizeof(int) * 2 * (M + 1), st));
     launch_hash_insert(h->blo.p, h->bhi.p, Ns, Nt, Ne, ext, h->hmask, h->hcnt.p, nullptr, nullptr, 0, ovf, st);
     scan_exclusive(h->hcnt.p, h->hstart.p, (int)(2 * (M + 1)), h->iscr.p, st);
-    CK(cudaMemsetAsync(h->hcnt.p, 0, sizeof(int) * 2 * (M + 1), st));
+    CK(dev_zero(h->hcnt.p, sizeof(int) * 2 * (M + 1), st));
     launch_hash_insert(h->blo.p, h->bhi.p, Ns, Nt, Ne, ext, h->hmask, h->hcnt.p, h->hstart.p, h->hent.p,
                        (int)h->hent.n, ovf, st);
     for (int pass = 0; pass < 2; ++pass) {
@@ -420,7 +420,7 @@ static void broad_phase_sort(pd_ipc *h, const double4 *ds, double infl, int *ccn
             const int a0 = kind == 0 ? 0 : Ns + Nt, na = kind == 0 ? Ns : Ne;
             const int *hs = h->hstart.p + (size_t)kind * (M + 1), *he = h->hent.p;
             int *cnt = kind == 0 ? cnt_pt : cnt_ee;
-            CK(cudaMemsetAsync(cnt, 0, sizeof(int), st));
+            CK(dev_zero(cnt, sizeof(int), st));
             unsigned long long *out = h->cand.p + (size_t)kind * cap;
             launch_hash_query(h->blo.p, h->bhi.p, a0, na, b0, kind == 0 ? Nt : Ne, ext, h->hmask, hs,
                               he, kind == 0, h->tris.p, h->edges.p, out, cnt, cap, st);
@@ -440,7 +440,7 @@ static void broad_phase_sort(pd_ipc *h, const double4 *ds, double infl, int *ccn
                 unique_sorted_u64(reinterpret_cast<uint64_t *>(keys), nk,
                                   reinterpret_cast<uint64_t *>(h->cand_tmp.p + (size_t)kind * cap), h->flag.p,
                                   h->pos.p, h->iscr.p, st);
-                CK(cudaMemcpyAsync(cnt_pt + kind, h->pos.p + nk, sizeof(int), cudaMemcpyDeviceToDevice, st));
+                CK(dev_copy(cnt_pt + kind, h->pos.p + nk, sizeof(int), st));
             }
             sync_read_ints(h, res, cnt_pt, 2);
             CK(cudaMemcpyAsync(h->cand.p, h->cand_tmp.p, sizeof(unsigned long long) * res[0],
@@ -468,8 +468,8 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
     const int cap = (int)h->cand.n;
     auto &ev = h->tm.ev[slot];
     int *acnt = h->dint.p + D_ACNT, *ccnt = h->dint.p + D_CCNT;
-    CK(cudaMemsetAsync(h->dint.p + D_INFO, 0, 4 * sizeof(int), st));   // info, capacity, hash flags
-    CK(cudaMemsetAsync(acnt, 0, 2 * sizeof(int), st));
+    CK(dev_zero(h->dint.p + D_INFO, 4 * sizeof(int), st));   // info, capacity, hash flags
+    CK(dev_zero(acnt, 2 * sizeof(int), st));
     record_event(ev[0], st);
     // ---------------- Misc: a1 local step + a2 gather
     KTimer &kt = h->kt;
@@ -487,7 +487,7 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
         const DevFactor &F2 = h->F;
         CK(cudaEventRecord(h->ev_fork, st));
         CK(cudaStreamWaitEvent(s2, h->ev_fork, 0));
-        CK(cudaMemsetAsync(h->ticket2.p, 0, 4 * sizeof(int), s2));   // [0] ticket, [1] fault, [2] |S| = 0
+        CK(dev_zero(h->ticket2.p, 4 * sizeof(int), s2));   // [0] ticket, [1] fault, [2] |S| = 0
         kt.start(K_D_SYRK, s2);
         launch_ts_items(F2, nullptr, h->ticket2.p + 2, 0, h->ticket2.p + 2, 0, h->ticket2.p + 3, 1, h->ts_lo2.p,
                         h->ts_hi2.p, h->ts_cnt2.p, h->ts_rem2.p, s2);
@@ -506,7 +506,7 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
         kt.start(K_BROAD, st);
         launch_surface(h->Wp.p, h->Wc.p, h->Wv.p, q.x.p, Ns, h->s.p, st);
         broad_phase(h, nullptr, 0.5 * h->dh * 1.01, ccnt, h->dint.p + D_HOVF);
-        CK(cudaMemcpyAsync(h->dint.p + D_STAT, ccnt, 2 * sizeof(int), cudaMemcpyDeviceToDevice, st));
+        CK(dev_copy(h->dint.p + D_STAT, ccnt, 2 * sizeof(int), st));
         kt.stop(K_BROAD, st);
         kt.start(K_NARROW, st);
         // one pass over [PT | EE] candidates; one scan; actives come out as [PT | EE], each sorted
@@ -524,7 +524,7 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
         kt.stop(K_DERIV, st);
         kt.start(K_ASSEMBLY, st);
         // S
-        CK(cudaMemsetAsync(h->mark.p, 0, sizeof(int) * nf, st));
+        CK(dev_zero(h->mark.p, sizeof(int) * nf, st));
         launch_mark_S(h->ids.p, acnt, cap, h->Wp.p, h->Wc.p, h->v2q.p, h->mark.p, st);
         scan_exclusive(h->mark.p, h->spos.p, nf, h->iscr.p, st);
         launch_compact_S(h->mark.p, h->spos.p, nf, h->qS.p, st);
@@ -533,7 +533,7 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
         launch_same_S(h->qS.p, nS_dev, h->qS_prev.p, h->dint.p + D_SPREV, h->dint.p + D_SPREV + 1, h->capS,
                       h->opt.no_sigma_reuse == 0, h->dint.p + D_CAP, h->dint.p + D_REUSED, st);
         // gradient pull-back: deterministic fixed-point accumulation on the surface, then W^T
-        CK(cudaMemsetAsync(h->gsq.p, 0, sizeof(long long) * 6 * Ns, st));
+        CK(dev_zero(h->gsq.p, sizeof(long long) * 6 * Ns, st));
         launch_accum_grad_fx(h->ids.p, acnt, cap, h->grad.p, dmax, h->gsq.p, st);
         launch_grad_pullback_fx(h->g_el.p, h->WTp.p, h->WTr.p, h->WTv.p, h->gsq.p, dmax, acnt, nf, h->G.p, st);
         launch_gather_gc(h->qS.p, nS_dev, h->capS, h->WTp.p, h->WTr.p, h->WTv.p, h->gsq.p, dmax, acnt, h->gcS.p, st);
@@ -548,16 +548,16 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
         launch_fx_to_double(reinterpret_cast<long long *>(h->Bc.p), Bl, ldb, nS_dev, h->capS, dmax, acnt, st);
         kt.stop(K_ASSEMBLY, st);
     } else {
-        CK(cudaMemsetAsync(nS_dev, 0, sizeof(int), st));
-        CK(cudaMemsetAsync(h->dint.p + D_SPREV + 1, 0, sizeof(int), st));
-        CK(cudaMemsetAsync(h->dint.p + D_STAT, 0, 2 * sizeof(int), st));
+        CK(dev_zero(nS_dev, sizeof(int), st));
+        CK(dev_zero(h->dint.p + D_SPREV + 1, sizeof(int), st));
+        CK(dev_zero(h->dint.p + D_STAT, 2 * sizeof(int), st));
         launch_grad_pullback(h->g_el.p, h->WTp.p, h->WTr.p, h->WTv.p, nullptr, nf, h->G.p, st);
     }
     record_event(ev[2], st);
     // ---------------- G-Step
     // pure-PD part on stream 2 (forked after the gather, see above); here the contact part
     const DevFactor &F = h->F;
-    CK(cudaMemsetAsync(h->ticket.p, 0, 2 * sizeof(int), st));
+    CK(dev_zero(h->ticket.p, 2 * sizeof(int), st));
     kt.start(K_FWD, st);
     // panel V_s = L^-1 Pi E_S (panel tiles only; no items when S is unchanged)
     launch_ts_items(F, h->qS.p, nS_dev, h->capS, h->dint.p + D_SPREV + 1, (long long)h->Up.n,
@@ -574,7 +574,7 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
     if (Nt > 0) {
         if (h->trace_file) {
             h->sprof.ensure(1024);
-            CK(cudaMemsetAsync(h->sprof.p, 0, 1024 * 8, st));
+            CK(dev_zero(h->sprof.p, 1024 * 8, st));
         }
         CK((cudaError_t)launch_schur(F, h->V.p, h->ldv, h->Yw.p, h->gcS.p, h->qS.p,
                                      h->ts_lo.p, h->ts_hi.p, nS_dev, h->capS, h->K.p, h->capS, h->Bc.p,
@@ -582,13 +582,13 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
                                      h->rhs.p, h->u.p, h->tv.p, h->Z.p, h->dint.p + D_INFO,
                                      h->dint.p + D_SPREV + 1, h->trace_file ? h->sprof.p : nullptr, st));
     } else {
-        CK(cudaMemcpyAsync(h->Z.p, h->Yw.p, sizeof(double) * 4 * nf, cudaMemcpyDeviceToDevice, st));
+        CK(dev_copy(h->Z.p, h->Yw.p, sizeof(double) * 4 * nf, st));
     }
     kt.stop(K_DENSE, st);
     kt.start(K_BWD, st);
     launch_backward_solve(F, h->ts_done.p, h->bw_cnt.p, h->ticket.p, h->bw_P.p, h->Z.p, h->nsm, st);
     kt.stop(K_BWD, st);
-    CK(cudaMemsetAsync(h->dx.p, 0, sizeof(double4) * h->n, st));
+    CK(dev_zero(h->dx.p, sizeof(double4) * h->n, st));
     launch_scatter_dx(h->Z.p, h->q2v.p, nf, h->dx.p, st);
     record_event(ev[3], st);
     // ---------------- CCD
@@ -602,7 +602,7 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
         launch_accd(h->cand.p, ccnt, cap, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->ds.p, h->opt.accd_s,
                     h->opt.accd_max_iters, amin, st);
     } else {
-        CK(cudaMemsetAsync(ccnt, 0, 2 * sizeof(int), st));
+        CK(dev_zero(ccnt, 2 * sizeof(int), st));
     }
     kt.stop(K_CCD, st);
     record_event(ev[4], st);
@@ -613,15 +613,15 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
         sum_partials(h->part.p, nb1, scal + 0, st);
         int nb2 = quad_partials(h->tets.p, h->dx.p, h->B.p, h->w.p, T, h->part.p + nb1, st);
         sum_partials(h->part.p + nb1, nb2, scal + 1, st);
-        CK(cudaMemcpyAsync(ls, amin, sizeof(double), cudaMemcpyDeviceToDevice, st));
-        CK(cudaMemsetAsync(ls + 1, 0, 2 * sizeof(double), st));
+        CK(dev_copy(ls, amin, sizeof(double), st));
+        CK(dev_zero(ls + 1, 2 * sizeof(double), st));
         const int hmax = h->opt.ls_max_halvings;
         for (int h0 = 0; h0 <= hmax; h0 += 8) {
             if (Nt > 0)
                 launch_ls_trials(h->cand.p, ccnt, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->ds.p, h->dh, h->b0.p,
                                  ls, h0, h->lspart.p, st);
             else if (h0 == 0)
-                CK(cudaMemsetAsync(h->lspart.p, 0, sizeof(double) * 8 * ls_blocks(), st));
+                CK(dev_zero(h->lspart.p, sizeof(double) * 8 * ls_blocks(), st));
             launch_ls_decide(h->lspart.p, scal, h->kappa, h0, hmax, ls, ls_out, st);
         }
         launch_update(q.x.p, h->dx.p, h->q2v.p, nf, ls_out, h->dint.p + D_INFO, h->dint.p + D_ABORT, slot, st);
@@ -647,7 +647,7 @@ static int run_batch(pd_ipc *h, Seq &q, int k, double ms[6]) {
     const unsigned key = (h->buf_epoch << 1) | (kt.on ? 1u : 0u);
     const unsigned key_mask = kt.on ? kt.mask : 0u;
     auto enqueue_batch = [&]() {
-        CK(cudaMemsetAsync(h->dint.p + D_ABORT, 0, 4 * sizeof(int), st));   // abort, index, why, reused
+        CK(dev_zero(h->dint.p + D_ABORT, 4 * sizeof(int), st));   // abort, index, why, reused
         for (int i = 0; i < k; ++i) enqueue_iteration(h, q, i);
     };
     if (graph && (!q.exec || q.graph_key != key || q.graph_batch != k || q.graph_mask != key_mask)) {

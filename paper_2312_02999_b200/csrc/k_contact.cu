@@ -469,9 +469,11 @@ __global__ void k_compact_active(const unsigned long long *__restrict__ keys, co
 struct HD { double v, a, b, ab; };
 __device__ __forceinline__ HD hsub(HD x, HD y) { return {x.v - y.v, x.a - y.a, x.b - y.b, x.ab - y.ab}; }
 __device__ __forceinline__ HD hadd(HD x, HD y) { return {x.v + y.v, x.a + y.a, x.b + y.b, x.ab + y.ab}; }
+// (explicit FMAs: the derivative terms need no bit-exactness, and this unit is built with
+// -fmad=false for the canonical distances)
 __device__ __forceinline__ HD hmul(HD x, HD y) {
-    return {x.v * y.v, x.a * y.v + x.v * y.a, x.b * y.v + x.v * y.b,
-            x.ab * y.v + x.a * y.b + x.b * y.a + x.v * y.ab};
+    return {x.v * y.v, fma(x.a, y.v, x.v * y.a), fma(x.b, y.v, x.v * y.b),
+            fma(x.ab, y.v, fma(x.a, y.b, fma(x.b, y.a, x.v * y.ab)))};
 }
 __device__ __forceinline__ HD hdiv(HD x, HD y) {
     double g = 1.0 / y.v, g1 = -g * g, g2 = 2.0 * g * g * g;
@@ -523,6 +525,9 @@ __device__ HD h_type_d2(int ty, const HV P[4]) {
 }
 
 __constant__ unsigned char c_ui[78], c_uj[78];
+constexpr double kNsFloor = 1e-10;   // smallest |eigenvalue| / |H|_F the sign iteration resolves
+__constant__ double c_ns_a[64];
+__constant__ int c_ns_k;
 
 constexpr int kPD_WARPS = 4;
 
@@ -609,11 +614,13 @@ __global__ void __launch_bounds__(kPD_WARPS * 32) k_pair_derivs(
         }
     }
     __syncwarp();
-    // PSD projection H+ = (H + H sign(H)) / 2, sign(H) by the Newton-Schulz iteration
-    // X <- X (3 I - X^2) / 2 from X = H / |H|_F: eigenvalues in [-1, 1], zeros stay 0, every
-    // other one converges to +-1 (small ones grow by 1.5 per step).  Stops one step after a step
-    // changes X by less than 1e-10 (Frobenius): the eigenvalues then still short of +-1 are
-    // below ~1e-10 |H| / 1.5^it, and each contributes less than its own size to H+.
+    // PSD projection H+ = (H + H sign(H)) / 2, sign(H) by the scaled Newton-Schulz iteration
+    // from X = H / |H|_F (eigenvalues in [-1, 1]): the odd cubic p_k(x) = (3 a_k x - a_k^3 x^3)/2
+    // with a_k = sqrt(3 / (1 + l_k + l_k^2)) maps [l_k, 1] onto [l_{k+1}, 1], l_{k+1} = p_k(l_k),
+    // never beyond 1; from l_0 = kNsFloor = 1e-10 the schedule reaches 1 - 1e-16 in 29 steps (the
+    // plain iteration grows small eigenvalues only 1.5x per step and runs until the rounding-level
+    // ones of the null space have grown to 1).  Eigenvalues below 1e-10 |H|_F contribute less
+    // than their own size to H+.
     double fro = 0.0;
     for (int e = lane; e < 144; e += 32) fro += H[e / 12][e % 12] * H[e / 12][e % 12];
     fro = warp_sum(fro);
@@ -621,61 +628,58 @@ __global__ void __launch_bounds__(kPD_WARPS * 32) k_pair_derivs(
     for (int e = lane; e < 144; e += 32) V[e / 12][e % 12] = H[e / 12][e % 12] * hinv;   // X
     __syncwarp();
     double (*X2)[13] = Ws[wl];
-    bool settled = false;
-    for (int it = 0; it < 120; ++it) {
-        double x2[5];
+    // register-blocked 12x12 products: lanes 0..23 own a 3x2 output block (rows 3 rb.., columns
+    // 2 cb..), 5 loads per 6 FMAs
+    const int rb = lane / 6, cb = lane % 6;
+    const bool own = lane < 24;
+    auto mm12 = [&](const double (*A)[13], const double (*Bm)[13], double (&o)[3][2]) {
 #pragma unroll
-        for (int q = 0; q < 5; ++q) {                     // X2 = X X
-            const int e = lane + 32 * q;
-            x2[q] = 0.0;
-            if (e < 144) {
-                const int i2 = e / 12, j2 = e % 12;
-                double acc = 0.0;
+        for (int r = 0; r < 3; ++r) o[r][0] = o[r][1] = 0.0;
+        if (own) {
 #pragma unroll
-                for (int kk = 0; kk < 12; ++kk) acc += V[i2][kk] * V[kk][j2];
-                x2[q] = acc;
+            for (int kk = 0; kk < 12; ++kk) {
+                const double b0 = Bm[kk][2 * cb], b1 = Bm[kk][2 * cb + 1];
+#pragma unroll
+                for (int r = 0; r < 3; ++r) {
+                    const double av = A[3 * rb + r][kk];
+                    o[r][0] = fma(av, b0, o[r][0]);         // explicit FMA: this unit is
+                    o[r][1] = fma(av, b1, o[r][1]);         // built with -fmad=false
+                }
             }
         }
+    };
+    // scaled Newton-Schulz steps X <- (3 a X - a^3 X^3) / 2 with the fixed schedule c_ns_a
+    // (contact_init): every eigenvalue of |X0| in [kNsFloor, 1] ends within 1e-16 of 1
+    for (int it = 0; it < c_ns_k; ++it) {
+        const double c1 = 1.5 * c_ns_a[it], c3 = 0.5 * c_ns_a[it] * c_ns_a[it] * c_ns_a[it];
+        double x2[3][2];
+        mm12(V, V, x2);                                   // X2 = X X
+        if (own)
 #pragma unroll
-        for (int q = 0; q < 5; ++q) {
-            const int e = lane + 32 * q;
-            if (e < 144) X2[e / 12][e % 12] = x2[q];
-        }
+            for (int r = 0; r < 3; ++r) {
+                X2[3 * rb + r][2 * cb] = x2[r][0];
+                X2[3 * rb + r][2 * cb + 1] = x2[r][1];
+            }
         __syncwarp();
-        double xn[5], dl = 0.0;
+        double xx[3][2], xn[3][2];
+        mm12(V, X2, xx);                                  // X <- c1 X - c3 X X2
+        if (own)
 #pragma unroll
-        for (int q = 0; q < 5; ++q) {                     // X <- 1.5 X - 0.5 X X2
-            const int e = lane + 32 * q;
-            xn[q] = 0.0;
-            if (e < 144) {
-                const int i2 = e / 12, j2 = e % 12;
-                double acc = 0.0;
+            for (int r = 0; r < 3; ++r)
 #pragma unroll
-                for (int kk = 0; kk < 12; ++kk) acc += V[i2][kk] * X2[kk][j2];
-                xn[q] = 1.5 * V[i2][j2] - 0.5 * acc;
-                dl += (xn[q] - V[i2][j2]) * (xn[q] - V[i2][j2]);
-            }
-        }
+                for (int q = 0; q < 2; ++q) xn[r][q] = c1 * V[3 * rb + r][2 * cb + q] - c3 * xx[r][q];
         __syncwarp();
         // keep X exactly symmetric: rounding asymmetry would otherwise seed non-normal
-        // components that the iteration amplifies by 1.5 per step
+        // components that the iteration amplifies
+        if (own)
 #pragma unroll
-        for (int q = 0; q < 5; ++q) {
-            const int e = lane + 32 * q;
-            if (e < 144) X2[e / 12][e % 12] = xn[q];
-        }
+            for (int r = 0; r < 3; ++r) {
+                X2[3 * rb + r][2 * cb] = xn[r][0];
+                X2[3 * rb + r][2 * cb + 1] = xn[r][1];
+            }
         __syncwarp();
-#pragma unroll
-        for (int q = 0; q < 5; ++q) {
-            const int e = lane + 32 * q;
-            if (e < 144) V[e / 12][e % 12] = 0.5 * (X2[e / 12][e % 12] + X2[e % 12][e / 12]);
-        }
-        dl = warp_sum(dl);
+        for (int e = lane; e < 144; e += 32) V[e / 12][e % 12] = 0.5 * (X2[e / 12][e % 12] + X2[e % 12][e / 12]);
         __syncwarp();
-        if (dl <= 1e-20) {                 // quadratic phase reached: one more step, then stop
-            if (settled) break;
-            settled = true;
-        }
     }
     // H+ = (H + H X) / 2 symmetrized, packed upper
     double mx = lane < 12 ? fabs(kappa * b1 * (gs[wl][lane] / (2.0 * d))) : 0.0;
@@ -683,8 +687,8 @@ __global__ void __launch_bounds__(kPD_WARPS * 32) k_pair_derivs(
         const int i = c_ui[e], j = c_uj[e];
         double a1 = 0.0, a2 = 0.0;
         for (int kk = 0; kk < 12; ++kk) {
-            a1 += H[i][kk] * V[kk][j];
-            a2 += V[i][kk] * H[kk][j];
+            a1 = fma(H[i][kk], V[kk][j], a1);
+            a2 = fma(V[i][kk], H[kk][j], a2);
         }
         const double acc = 0.5 * H[i][j] + 0.25 * (a1 + a2);
         Hp[78 * (size_t)k + e] = acc;
@@ -1058,6 +1062,17 @@ void contact_init() {
         for (int j = i; j < 12; ++j) { ui[e] = (unsigned char)i; uj[e] = (unsigned char)j; ++e; }
     cudaMemcpyToSymbol(c_ui, ui, 78);
     cudaMemcpyToSymbol(c_uj, uj, 78);
+    // scaled Newton-Schulz schedule: a_k = sqrt(3 / (1 + l + l^2)), l <- (3 a l - a^3 l^3) / 2
+    double tab[64], l = kNsFloor;
+    int k = 0;
+    while (k < 64) {
+        const double a = std::sqrt(3.0 / (1.0 + l + l * l));
+        tab[k++] = a;
+        l = 0.5 * a * l * (3.0 - a * a * l * l);
+        if (1.0 - l < 1e-16) break;
+    }
+    cudaMemcpyToSymbol(c_ns_a, tab, sizeof(double) * k);
+    cudaMemcpyToSymbol(c_ns_k, &k, sizeof(int));
 }
 
 void launch_boxes(const double4 *s, const double4 *ds, const int *tris, const int *edges, int Ns,

@@ -21,6 +21,7 @@
 // Backward solve: reverse postorder, 3 columns: stage the already-solved ancestor rows, column
 // dot products with L_off, then the transposed inverse of the diagonal block.
 #include "kernels.h"
+#include "prims.h"
 
 #include "dev_common.cuh"
 
@@ -421,6 +422,16 @@ __global__ void __launch_bounds__(kTS_NT) k_backward_solve(BwdArgs A) {
         const int m = min(kSolveRB, nr - rb);
         // A = Q_s[rb.., :]^T : element (k, i) = Q[rb + i][k]  (w x m)
         stage_block(A.Q + A.sn_valptr[s] + rb, nr, 1, w, m, Sg);
+        // source rows of this thread's right-hand-side entries (independent of the parent: loaded
+        // before the dependency wait)
+        const int kpad = (m + 31) & ~31;
+        int src[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int e = tid + u * kTS_NT, i = e >> 3, r = rb + i;
+            src[u] = -1;
+            if (e < kpad * 8 && i < m && (e & 7) < 3) src[u] = r < w ? c0 + r : A.sn_rows[slot0 + r];
+        }
         if (tid == 0) {
             int p = A.sn_parent[s];
             if (p >= 0) {
@@ -434,15 +445,18 @@ __global__ void __launch_bounds__(kTS_NT) k_backward_solve(BwdArgs A) {
             __threadfence();
         }
         __syncthreads();
-        const int kpad = (m + 31) & ~31;
-        for (int e = tid; e < kpad * 8; e += kTS_NT) {
-            const int i = e >> 3, c = e & 7, r = rb + i;
-            double v = 0.0;
-            if (i < m && c < 3) {
-                if (r < w) v = __ldcg(A.Z + (size_t)(c0 + r) * 4 + c);
-                else v = -__ldcg(A.Z + (size_t)A.sn_rows[slot0 + r] * 4 + c);
+        static_assert(kSolveRB * 8 <= 2 * kTS_NT, "two RHS entries per thread");
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int e = tid + u * kTS_NT, i = e >> 3, c = e & 7, r = rb + i;
+            if (e < kpad * 8) {
+                double v = 0.0;
+                if (src[u] >= 0) {
+                    v = __ldcg(A.Z + (size_t)src[u] * 4 + c);
+                    if (r >= w) v = -v;
+                }
+                Vb[i][c] = v;
             }
-            Vb[i][c] = v;
         }
         cp_async_wait_group<0>();
         __syncthreads();
@@ -491,7 +505,7 @@ void trisolve_init() {
 void launch_ts_items(const DevFactor &F, const int *qS, const int *nS_ptr, int capS, const int *same_S,
                      long long up_cap, int *flags, int mode, int *lo, int *hi, int *cnt, int *rem,
                      cudaStream_t st) {
-    cudaMemsetAsync(rem, 0, sizeof(int) * F.nsn, st);
+    dev_zero(rem, sizeof(int) * F.nsn, st);
     PDI_LAUNCH(k_ts_items, (F.nsn + 255) / 256, 256, 0, st)(F.ford, F.sn_c0, F.sn_rowptr, F.sn_fd,
                                                              F.sn_parent, F.nsn, qS, nS_ptr, capS, same_S,
                                                              F.nU, up_cap, flags, mode, lo, hi, cnt, rem);
@@ -508,7 +522,7 @@ void launch_forward_solve(const DevFactor &F, const int *lo, const int *hi, cons
     A.lo = lo; A.hi = hi; A.item_ptr = item_ptr; A.qS = qS; A.ford = F.ford; A.nsn = F.nsn;
     A.rem = rem; A.ticket = ticket; A.G = G; A.Y = Y; A.V = V; A.ldv = ldv;
     A.Ug = Ug; A.Up = Up; A.nS_ptr = nS_ptr; A.capS = capS; A.with_grad = with_grad; A.trace = trace;
-    cudaMemsetAsync(ticket, 0, sizeof(int), st);
+    dev_zero(ticket, sizeof(int), st);
     PDI_LAUNCH(k_forward_solve, nsm, kTS_NT, kFwdSmem, st)(A);
 }
 
@@ -518,9 +532,9 @@ void launch_backward_solve(const DevFactor &F, int *done, int *cnt, int *ticket,
     A.sn_c0 = F.sn_c0; A.sn_rowptr = F.sn_rowptr; A.sn_rows = F.sn_rows; A.sn_parent = F.sn_parent;
     A.sn_valptr = F.sn_valptr; A.Q = F.Q; A.items = F.bw_items; A.pbase = F.bw_pbase;
     A.nitems = F.bw_nitems; A.done = done; A.cnt = cnt; A.ticket = ticket; A.P = P; A.Z = Z;
-    cudaMemsetAsync(ticket, 0, sizeof(int), st);
-    cudaMemsetAsync(done, 0, sizeof(int) * F.nsn, st);
-    cudaMemsetAsync(cnt, 0, sizeof(int) * F.nsn, st);
+    dev_zero(ticket, sizeof(int), st);
+    dev_zero(done, sizeof(int) * F.nsn, st);
+    dev_zero(cnt, sizeof(int) * F.nsn, st);
     PDI_LAUNCH(k_backward_solve, nsm, kTS_NT, kFwdSmem, st)(A);
 }
 

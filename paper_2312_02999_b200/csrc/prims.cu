@@ -2,6 +2,10 @@
 // 64-bit keys, unique.  Hand-written (no CUB); deterministic for a given input.
 #include "prims.h"
 
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
 #include "dev_common.cuh"
 
 namespace pdipc {
@@ -10,6 +14,27 @@ static long long g_launches = 0;     // handles are single-threaded (pd_ipc.h)
 void note_launch() { ++g_launches; }
 long long launch_count() { return g_launches; }
 void add_launches(long long n) { g_launches += n; }
+// ----------------------------------------------------------------------- fill / copy ------
+// Stream-ordered zero fill and device copy as library kernels (not memset / memcpy nodes).
+__global__ void k_zero32(unsigned *__restrict__ p, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = 0u;
+}
+__global__ void k_copy32(unsigned *__restrict__ d, const unsigned *__restrict__ s, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) d[i] = s[i];
+}
+static int fill_grid(size_t n) { return (int)std::min<size_t>((n + 255) / 256, 148 * 4); }
+cudaError_t dev_zero(void *p, size_t bytes, cudaStream_t st) {
+    const size_t n = bytes / 4;                  // callers pass multiples of 4 bytes
+    if (n == 0) return cudaSuccess;
+    PDI_LAUNCH(k_zero32, fill_grid(n), 256, 0, st)(static_cast<unsigned *>(p), n);
+    return cudaGetLastError();
+}
+cudaError_t dev_copy(void *d, const void *s, size_t bytes, cudaStream_t st) {
+    const size_t n = bytes / 4;
+    if (n == 0) return cudaSuccess;
+    PDI_LAUNCH(k_copy32, fill_grid(n), 256, 0, st)(static_cast<unsigned *>(d), static_cast<const unsigned *>(s), n);
+    return cudaGetLastError();
+}
 
 // ----------------------------------------------------------------------- exclusive scan ----
 constexpr int kScanNT = 1024, kScanIPT = 4, kScanTile = kScanNT * kScanIPT;
@@ -86,9 +111,49 @@ __global__ void __launch_bounds__(kScanNT) k_scan_tiles(const int *in, int n, co
     (void)nparts;
 }
 
+// Small scans (capacity <= kScanSingleMax): ONE CTA walks tiles of kScanNT x 16 with a running
+// carry -- one launch instead of two, no partials round trip.
+constexpr int kScanSingleIPT = 16, kScanSingleTile = kScanNT * kScanSingleIPT, kScanSingleMax = 4 * kScanSingleTile;
+__global__ void __launch_bounds__(kScanNT) k_scan_single(const int *__restrict__ in, int n, const int *n_dev,
+                                                         int *__restrict__ out) {
+    __shared__ int sh[32];
+    n = scan_len(n, n_dev);
+    int carry = 0;
+    for (int t0 = 0; t0 <= n; t0 += kScanSingleTile) {   // covers index n (the total)
+        const int base = t0 + threadIdx.x * kScanSingleIPT;
+        int v[kScanSingleIPT];
+        if (base + kScanSingleIPT <= n) {
+            const int4 *p = reinterpret_cast<const int4 *>(in + base);
+#pragma unroll
+            for (int q = 0; q < kScanSingleIPT / 4; ++q) {
+                const int4 x = p[q];
+                v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < kScanSingleIPT; ++i) v[i] = base + i < n ? in[base + i] : 0;
+        }
+        int sum = 0;
+#pragma unroll
+        for (int i = 0; i < kScanSingleIPT; ++i) sum += v[i];
+        int tot;
+        int ex = block_exclusive_scan<kScanNT>(sum, sh, &tot) + carry;
+#pragma unroll
+        for (int i = 0; i < kScanSingleIPT; ++i) {
+            if (base + i <= n) out[base + i] = ex;      // out[n] = total
+            ex += v[i];
+        }
+        carry += tot;
+    }
+}
+
 void scan_exclusive(const int *in, int *out, int n, int *scratch, cudaStream_t st) {
     if (n <= 0) {
-        cudaMemsetAsync(out, 0, sizeof(int), st);
+        dev_zero(out, sizeof(int), st);
+        return;
+    }
+    if (n <= kScanSingleMax) {
+        PDI_LAUNCH(k_scan_single, 1, kScanNT, 0, st)(in, n, nullptr, out);
         return;
     }
     int nb = n / kScanTile + 1;                      // covers index n (the total)
@@ -97,6 +162,10 @@ void scan_exclusive(const int *in, int *out, int n, int *scratch, cudaStream_t s
 }
 
 void scan_exclusive_dev(const int *in, int *out, const int *n_dev, int cap, int *scratch, cudaStream_t st) {
+    if (cap <= kScanSingleMax) {
+        PDI_LAUNCH(k_scan_single, 1, kScanNT, 0, st)(in, cap, n_dev, out);
+        return;
+    }
     int nb = cap / kScanTile + 1;
     PDI_LAUNCH(k_scan_partials, nb, kScanNT, 0, st)(in, cap, n_dev, scratch);
     PDI_LAUNCH(k_scan_tiles, nb, kScanNT, 0, st)(in, cap, n_dev, out, scratch, nb);
@@ -184,7 +253,7 @@ void radix_sort_u64(uint64_t *keys, uint64_t *tmp, int n, int bits, int *scratch
         src = dst;
         dst = t;
     }
-    if (src != keys) cudaMemcpyAsync(keys, src, sizeof(uint64_t) * n, cudaMemcpyDeviceToDevice, st);
+    if (src != keys) dev_copy(keys, src, sizeof(uint64_t) * n, st);
 }
 
 // ----------------------------------------------------------------------- unique -----------
@@ -201,7 +270,7 @@ __global__ void k_unique_write(const uint64_t *k, int n, const int *pos, uint64_
 void unique_sorted_u64(const uint64_t *keys, int n, uint64_t *out, int *flags, int *pos,
                        int *scratch, cudaStream_t st) {
     if (n <= 0) {
-        cudaMemsetAsync(pos, 0, sizeof(int), st);
+        dev_zero(pos, sizeof(int), st);
         return;
     }
     int nb = (n + 255) / 256;
