@@ -77,6 +77,13 @@ typedef struct {
                                  and the constant factor only -- are recomputed only when S
                                  differs bit for bit from the S they were last computed for;
                                  1: recompute them every iteration                             */
+    int32_t no_cand_reuse;    /* 0 (default): iterations after the first of a pd_ipc_step batch
+                                 take the previous iteration's SWEPT candidate list (boxes over
+                                 [s, s + W dx] inflated by d_hat) as the candidate set of the
+                                 narrow phase: x_new = x + alpha dx with alpha in [0, 1], so every
+                                 pair closer than d_hat at x_new is in it (the
+                                 active set C is then identical, the narrow phase being exact);
+                                 1: static broad phase every iteration                         */
 } pd_ipc_options;
 
 /* Per sequence, describing the LAST iteration of the last pd_ipc_step call. */

@@ -505,7 +505,10 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
     if (Nt > 0) {
         kt.start(K_BROAD, st);
         launch_surface(h->Wp.p, h->Wc.p, h->Wv.p, q.x.p, Ns, h->s.p, st);
-        broad_phase(h, nullptr, 0.5 * h->dh * 1.01, ccnt, h->dint.p + D_HOVF);
+        // after the first iteration of a batch the previous iteration's swept candidate list
+        // (cand, ccnt; boxes over [s, s + ds] inflated by d_hat) contains every pair closer
+        // than d_hat at x + alpha dx: the narrow phase filters it exactly (same C)
+        if (slot == 0 || h->opt.no_cand_reuse) broad_phase(h, nullptr, 0.5 * h->dh * 1.01, ccnt, h->dint.p + D_HOVF);
         CK(dev_copy(h->dint.p + D_STAT, ccnt, 2 * sizeof(int), st));
         kt.stop(K_BROAD, st);
         kt.start(K_NARROW, st);

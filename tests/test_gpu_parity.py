@@ -235,3 +235,21 @@ def test_sigma_reuse_is_exact(P):
         s.close()
     assert np.array_equal(xs[0], xs[1])
     assert reused[0] > 0 and reused[1] == 0, reused
+
+
+def test_candidate_reuse_is_exact(P):
+    """Iterations after the first of a batch take the previous iteration's swept candidate list
+    (a superset of the pairs within d_hat at the new positions): the active sets, hence the
+    iterates, must be bit-identical to running the static broad phase every iteration."""
+    sc = scenes.face_small(n_frames=2)
+    A = np.tile(np.eye(3).reshape(1, 9), (sc.n_tets, 1))
+    A[:, 4] += 0.5 * sc.meta["lip_mask"]
+    xs, nact = [], []
+    for reuse in (True, False):
+        s = P.Solver(sc, A=A[None], cand_reuse=reuse)
+        st = s.step(n_iters=40)[0]
+        xs.append(s.positions())
+        nact.append(st["n_active"])
+        s.close()
+    assert nact[0] > 0 and nact[0] == nact[1]
+    assert np.array_equal(xs[0], xs[1])
