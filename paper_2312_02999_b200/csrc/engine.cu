@@ -212,7 +212,8 @@ struct pd_ipc {
     // second stream: w_el = L^-1 Pi g_el runs concurrently with the contact stages (it depends
     // on the elastic gradient only)
     cudaStream_t st2 = nullptr;
-    int side_ctas = 74;       // persistent CTAs of the stream-2 solves (PDIPC_SIDE_CTAS)
+    int side_ctas = 56;       // persistent CTAs of the stream-2 solves (PDIPC_SIDE_CTAS); the rest
+                              // of the SMs run the contact stages concurrently
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     DBuf<double> gcS, Ug2;
     DBuf<int> ts_lo2, ts_hi2, ts_cnt2, ts_ptr2, ts_rem2, ticket2, f_bord, iscr2;

@@ -534,7 +534,7 @@ constexpr int kPD_WARPS = 4;
 // Warp per active pair: grad/hess of d^2 (hyper-dual, one Hessian entry per lane-evaluation),
 // chain rule to d, barrier derivatives, 12x12 H_k, PSD projection by the Newton-Schulz sign iteration,
 // H_k^+ (packed upper, 78) and h_k = kappa b' grad d (12).
-__global__ void __launch_bounds__(kPD_WARPS * 32) k_pair_derivs(
+__global__ void __launch_bounds__(kPD_WARPS * 32, 4) k_pair_derivs(
     const unsigned long long *__restrict__ akeys, const int *__restrict__ atype,
     const double *__restrict__ ad2, const int *__restrict__ acnt, PairCtx c, double dh, double kappa,
     double *__restrict__ grad, double *__restrict__ Hp, double *__restrict__ dist,

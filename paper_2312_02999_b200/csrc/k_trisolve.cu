@@ -150,6 +150,7 @@ constexpr int kSS = 36;
 constexpr int kXS = 40;
 
 constexpr int kSgRows = 256;
+constexpr int kItemPtrSh = 4096;      // item_ptr entries cached in shared memory
 constexpr int kMaxSrc = 4;             // cached extend-add sources per row (more: list walk)           // staged A-operand rows (all k-slabs of one block)
 
 // Issue (without waiting) the cp.async copies of A = M[0..m) x [0..kdim) into Sg as
@@ -239,7 +240,12 @@ __global__ void __launch_bounds__(kTS_NT) k_forward_solve(FwdArgs A) {
     double (*Sg)[kSS] = reinterpret_cast<double (*)[kSS]>(fsm + (kTS_W + kSolveRB) * kXS);
     __shared__ int sh_item;
     __shared__ int src_n[kTS_W + kSolveRB], src_u[kTS_W + kSolveRB][kMaxSrc];
+    __shared__ int ip_sh[kItemPtrSh];                   // item_ptr cached (small factors)
     const int tid = threadIdx.x;
+    const bool ip_cached = A.nsn + 1 <= kItemPtrSh;
+    if (ip_cached)
+        for (int i = tid; i <= A.nsn; i += kTS_NT) ip_sh[i] = A.item_ptr[i];
+    const int *item_ptr = ip_cached ? ip_sh : A.item_ptr;
     const int total = A.item_ptr[A.nsn];
     const int ldu = ((min(*A.nS_ptr, A.capS) + 31) / 32) * 32;
     while (true) {
@@ -248,11 +254,11 @@ __global__ void __launch_bounds__(kTS_NT) k_forward_solve(FwdArgs A) {
         const int item = sh_item;
         __syncthreads();
         if (item >= total) return;
-        const int kpos = find_sn(A.item_ptr, A.nsn, item), s = A.ford[kpos];
+        const int kpos = find_sn(item_ptr, A.nsn, item), s = A.ford[kpos];
         const int c0 = A.sn_c0[s], w = A.sn_c0[s + 1] - c0;
         const int slot0 = A.sn_rowptr[s], nr = A.sn_rowptr[s + 1] - slot0;
         const int nb = (nr + kSolveRB - 1) / kSolveRB;
-        const int idx = item - A.item_ptr[kpos], tk = idx / nb + (A.with_grad ? 0 : 1);
+        const int idx = item - item_ptr[kpos], tk = idx / nb + (A.with_grad ? 0 : 1);
         const int rb = (idx % nb) * kSolveRB;
         const int m = min(kSolveRB, nr - rb);
         const bool grad = tk == 0;
@@ -265,16 +271,8 @@ __global__ void __launch_bounds__(kTS_NT) k_forward_solve(FwdArgs A) {
         const int ncc = grad ? 3 : 32;
         // Q block rows in flight while we wait for the children and gather the RHS
         stage_block(A.Q + A.sn_valptr[s] + rb, 1, nr, m, w, Sg);
-        if (tid == 0) {
-            if (A.trace) {
-                A.trace[4 * (size_t)item] = ((unsigned long long)s << 16) | (unsigned)tk;
-                A.trace[4 * (size_t)item + 1] = gtimer();
-            }
-            wait_zero(A.rem + s, A.ticket + 1);
-            if (A.trace) A.trace[4 * (size_t)item + 2] = gtimer();
-        }
-        __syncthreads();
-        // ---- extend-add sources of the rows this item touches: list slot q < w is column row
+        // ---- extend-add sources of the rows this item touches (static structure: resolved
+        //      while the children may still be running): list slot q < w is column row
         //      q (for X), slot w + i is row rb + i (epilogue, off rows only).  Resolved once,
         //      thread per row, so the value gathers below are independent loads.
         const double *Usrc = grad ? A.Ug : A.Up;
@@ -300,6 +298,14 @@ __global__ void __launch_bounds__(kTS_NT) k_forward_solve(FwdArgs A) {
                 }
             }
             src_n[q] = cnt;
+        }
+        if (tid == 0) {
+            if (A.trace) {
+                A.trace[4 * (size_t)item] = ((unsigned long long)s << 16) | (unsigned)tk;
+                A.trace[4 * (size_t)item + 1] = gtimer();
+            }
+            wait_zero(A.rem + s, A.ticket + 1);
+            if (A.trace) A.trace[4 * (size_t)item + 2] = gtimer();
         }
         __syncthreads();
         // ---- X: rhs minus the children's rows landing on s's columns (fixed child order)
