@@ -207,7 +207,7 @@ struct pd_ipc {
     DBuf<int> flag, pos, ctype, atype, ids, iscr;
     DBuf<double> cd2, ad2, grad, Hp, dist;
     DBuf<int> mark, spos, qS;
-    DBuf<double> lspart;    // line-search partial sums [8][ls_blocks()]
+    DBuf<double> lspart;    // line-search partial sums [ls_round_width()][ls_blocks()]
     bool force_sort = false;  // next broad phases take the sort path (after a hash overflow)
     // second stream: w_el = L^-1 Pi g_el runs concurrently with the contact stages (it depends
     // on the elastic gradient only)
@@ -352,6 +352,7 @@ enum : int {
     D_ABORT = 12,    // [12] sticky: an iteration of the batch failed, [13] its index, [14] why
     D_REUSED = 15,   // iterations of the batch that reused V_s, K_s, Sigma_s
     D_SORT = 16,     // [16..18] scratch counters of the sort path
+    D_LSCTR = 19,    // line-search round: blocks finished (the last one decides; reset by it)
 };
 
 static void broad_phase_sort(pd_ipc *h, const double4 *ds, double infl, int *ccnt);
@@ -620,14 +621,9 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
         CK(dev_copy(ls, amin, sizeof(double), st));
         CK(dev_zero(ls + 1, 2 * sizeof(double), st));
         const int hmax = h->opt.ls_max_halvings;
-        for (int h0 = 0; h0 <= hmax; h0 += 8) {
-            if (Nt > 0)
-                launch_ls_trials(h->cand.p, ccnt, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->ds.p, h->dh, h->b0.p,
-                                 ls, h0, h->lspart.p, st);
-            else if (h0 == 0)
-                CK(dev_zero(h->lspart.p, sizeof(double) * 8 * ls_blocks(), st));
-            launch_ls_decide(h->lspart.p, scal, h->kappa, h0, hmax, ls, ls_out, st);
-        }
+        for (int h0 = 0; h0 <= hmax; h0 = ls_round_next(h0))
+            launch_ls_round(h->cand.p, ccnt, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->ds.p, h->dh, h->b0.p, ls, h0,
+                            h->lspart.p, scal, h->kappa, hmax, ls_out, h->dint.p + D_LSCTR, st);
         launch_update(q.x.p, h->dx.p, h->q2v.p, nf, ls_out, h->dint.p + D_INFO, h->dint.p + D_ABORT, slot, st);
     }
     kt.stop(K_LS, st);
@@ -1054,7 +1050,7 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             h->qlist.exact((size_t)(m.Ns + m.Ne) * hash_query_cap());
             h->gsq.exact(6 * (size_t)m.Ns + 6);
         }
-        h->lspart.exact(8 * (size_t)ls_blocks());
+        h->lspart.exact((size_t)ls_round_width() * ls_blocks());
         h->iscr.ensure(std::max({radix_scratch_ints((int)(2 * cap_cand)), scan_scratch_ints(nf + 1),
                                  scan_scratch_ints(f.nsn + 1)}) + 1024);
         {

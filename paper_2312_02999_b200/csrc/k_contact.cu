@@ -530,6 +530,7 @@ __constant__ double c_ns_a[64];
 __constant__ int c_ns_k;
 
 constexpr int kPD_WARPS = 4;
+constexpr int kLsRound = 22;          // trial alphas of the last line-search round (h = 9..30)
 
 // Warp per active pair: grad/hess of d^2 (hyper-dual, one Hessian entry per lane-evaluation),
 // chain rule to d, barrier derivatives, 12x12 H_k, PSD projection by the Newton-Schulz sign iteration,
@@ -1054,6 +1055,90 @@ __global__ void k_ls_decide(const double *__restrict__ part, int part_ld, int np
     }
 }
 
+// One line-search round: trial alphas alpha_m 2^-(h0+h), h < KH, evaluated per candidate
+// (barrier differences), block partials, and the decision taken by the LAST block to finish
+// (atomic ticket; partials summed in fixed block order: deterministic).  Replaces the
+// trials + decide launch pair; a round after acceptance returns at once.
+template <int KH>
+__global__ void __launch_bounds__(256) k_ls_round(const unsigned long long *__restrict__ keys,
+                                                  const int *__restrict__ ccnt, PairCtx c,
+                                                  const double4 *__restrict__ ds, double dh,
+                                                  double *__restrict__ b0, double *__restrict__ ls,
+                                                  int h0, double *__restrict__ part, int part_ld,
+                                                  const double *__restrict__ scal, double kappa, int hmax,
+                                                  double *__restrict__ out, int *__restrict__ done_ctr) {
+    if (ls[1] != 0.0) return;   // already accepted
+    __shared__ double sh[8];
+    __shared__ int last;
+    const int npt = ccnt[0], n = ccnt[1];
+    const double am = ls[0];
+    double acc[KH];
+#pragma unroll
+    for (int h = 0; h < KH; ++h) acc[h] = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const bool is_pt = i < npt;
+        const int nB = is_pt ? c.Nt : c.Ne;
+        const unsigned long long k = keys[i];
+        int id[4], ty;
+        pair_ids(c, is_pt, (int)(k / nB), (int)(k % nB), id);
+        V3 P[4], D[4];
+        for (int q = 0; q < 4; ++q) { P[q] = mk(c.s[id[q]]); D[q] = mk(ds[id[q]]); }
+        double bb0;
+        if (h0 == 0) {
+            bb0 = bar(sqrt(pair_d2(is_pt, P[0], P[1], P[2], P[3], &ty)), dh);
+            b0[i] = bb0;
+        } else {
+            bb0 = b0[i];
+        }
+#pragma unroll
+        for (int h = 0; h < KH; ++h) {
+            const double al = ldexp(am, -(h0 + h));
+            const double d2 = pair_d2(is_pt, axpy(P[0], al, D[0]), axpy(P[1], al, D[1]), axpy(P[2], al, D[2]),
+                                      axpy(P[3], al, D[3]), &ty);
+            acc[h] += bar(sqrt(d2), dh) - bb0;
+        }
+    }
+    for (int h = 0; h < KH; ++h) {
+        const double v = block_sum<256>(acc[h], sh);
+        if (threadIdx.x == 0) part[(size_t)h * part_ld + blockIdx.x] = v;
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(done_ctr, 1) == (int)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    // decide: dE(alpha_h) = alpha gTdx + 0.5 alpha^2 quad + kappa dB
+    for (int h = 0; h < KH; ++h) {
+        double sum = 0.0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) sum += __ldcg(part + (size_t)h * part_ld + b);
+        sum = block_sum<256>(sum, sh);
+        if (threadIdx.x == 0) {
+            const int hh = h0 + h;
+            if (hh <= hmax && ls[1] == 0.0) {
+                const double al = ldexp(am, -hh);
+                const double dE = al * scal[0] + 0.5 * al * al * scal[1] + kappa * sum;
+                if (dE < 0.0) {
+                    ls[1] = 1.0;
+                    out[0] = al;
+                    out[1] = hh + 1;
+                    out[2] = dE;
+                    out[3] = 0;
+                } else if (hh == hmax) {
+                    ls[1] = 2.0;
+                    out[0] = 0.0;
+                    out[1] = hh + 1;
+                    out[2] = 0.0;
+                    out[3] = 1;   // stall
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *done_ctr = 0;    // ready for the next round
+}
+
 // ------------------------------------------------------------------ host wrappers ---------
 void contact_init() {
     unsigned char ui[78], uj[78];
@@ -1164,6 +1249,7 @@ void launch_accd(const unsigned long long *keys, const int *ccnt, int cap, const
     PDI_LAUNCH(k_accd, grid_for(cap, 128, 148 * 8), 128, 0, st)(keys, ccnt, c, ds, s_gap, max_iters, amin);
 }
 int ls_blocks() { return 2 * 148; }
+int ls_round_width() { return kLsRound; }
 void launch_ls_trials(const unsigned long long *keys, const int *ccnt, const double4 *s, const int *tris,
                       const int *edges, int Nt, int Ne, const double4 *ds, double dh, double *b0,
                       const double *ls, int h0, double *part, cudaStream_t st) {
@@ -1174,5 +1260,23 @@ void launch_ls_decide(const double *part, const double *scal, double kappa, int 
                       double *out, cudaStream_t st) {
     PDI_LAUNCH(k_ls_decide, 1, 1024, 0, st)(part, ls_blocks(), ls_blocks(), scal, kappa, h0, hmax, ls, out);
 }
+void launch_ls_round(const unsigned long long *keys, const int *ccnt, const double4 *s, const int *tris,
+                     const int *edges, int Nt, int Ne, const double4 *ds, double dh, double *b0, double *ls,
+                     int h0, double *part, const double *scal, double kappa, int hmax, double *out,
+                     int *done_ctr, cudaStream_t st) {
+    PairCtx c{s, tris, edges, Nt, Ne};
+    // rounds of 1, 8, then 22 trial alphas: the full step is accepted in most iterations, and a
+    // round after acceptance returns at once
+    if (h0 == 0)
+        PDI_LAUNCH(k_ls_round<1>, ls_blocks(), 256, 0, st)(keys, ccnt, c, ds, dh, b0, ls, h0, part, ls_blocks(), scal,
+                                                           kappa, hmax, out, done_ctr);
+    else if (h0 == 1)
+        PDI_LAUNCH(k_ls_round<8>, ls_blocks(), 256, 0, st)(keys, ccnt, c, ds, dh, b0, ls, h0, part, ls_blocks(), scal,
+                                                           kappa, hmax, out, done_ctr);
+    else
+        PDI_LAUNCH(k_ls_round<kLsRound>, ls_blocks(), 256, 0, st)(keys, ccnt, c, ds, dh, b0, ls, h0, part,
+                                                                  ls_blocks(), scal, kappa, hmax, out, done_ctr);
+}
+int ls_round_next(int h0) { return h0 == 0 ? 1 : h0 == 1 ? 9 : h0 + kLsRound; }
 
 }  // namespace pdipc
