@@ -977,84 +977,6 @@ __global__ void k_accd(const unsigned long long *__restrict__ keys, const int *_
 // ------------------------------------------------------------------ a11 line search -------
 // per block partial sums over the swept candidates of b(d(alpha_h)) - b(d(0)) for the trials
 // h = h0 .. h0+7 (alpha_h = alpha_m 2^-h); b(d(0)) computed in the first round and kept in b0
-__global__ void __launch_bounds__(256) k_ls_trials(const unsigned long long *__restrict__ keys,
-                                                   const int *__restrict__ ccnt, PairCtx c,
-                                                   const double4 *__restrict__ ds, double dh,
-                                                   double *__restrict__ b0,
-                                                   const double *__restrict__ ls,  // [alpha_m, accepted flag]
-                                                   int h0, double *__restrict__ part, int part_ld) {
-    if (ls[1] != 0.0) return;   // already accepted
-    __shared__ double sh[8];
-    const int npt = ccnt[0], n = ccnt[1];
-    const double am = ls[0];
-    double acc[8];
-#pragma unroll
-    for (int h = 0; h < 8; ++h) acc[h] = 0.0;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const bool is_pt = i < npt;
-        const int nB = is_pt ? c.Nt : c.Ne;
-        const unsigned long long k = keys[i];
-        int id[4], ty;
-        pair_ids(c, is_pt, (int)(k / nB), (int)(k % nB), id);
-        V3 P[4], D[4];
-        for (int q = 0; q < 4; ++q) { P[q] = mk(c.s[id[q]]); D[q] = mk(ds[id[q]]); }
-        double bb0;
-        if (h0 == 0) {
-            bb0 = bar(sqrt(pair_d2(is_pt, P[0], P[1], P[2], P[3], &ty)), dh);
-            b0[i] = bb0;
-        } else {
-            bb0 = b0[i];
-        }
-#pragma unroll
-        for (int h = 0; h < 8; ++h) {
-            const double al = ldexp(am, -(h0 + h));
-            const double d2 = pair_d2(is_pt, axpy(P[0], al, D[0]), axpy(P[1], al, D[1]), axpy(P[2], al, D[2]),
-                                      axpy(P[3], al, D[3]), &ty);
-            acc[h] += bar(sqrt(d2), dh) - bb0;
-        }
-    }
-    for (int h = 0; h < 8; ++h) {
-        const double v = block_sum<256>(acc[h], sh);
-        if (threadIdx.x == 0) part[(size_t)h * part_ld + blockIdx.x] = v;
-    }
-}
-
-// decide: dE(alpha_h) = alpha gTdx + 0.5 alpha alpha quad + kappa dB
-__global__ void k_ls_decide(const double *__restrict__ part, int part_ld, int npart,
-                            const double *__restrict__ scal,   // [gTdx, quad]
-                            double kappa, int h0, int hmax, double *__restrict__ ls,
-                            double *__restrict__ out /* alpha, trials, dE, flags */) {
-    if (ls[1] != 0.0) return;
-    __shared__ double sh[32];
-    const double am = ls[0];
-    for (int h = 0; h < 8; ++h) {
-        double s = 0.0;
-        for (int b = threadIdx.x; b < npart; b += blockDim.x) s += part[(size_t)h * part_ld + b];
-        s = block_sum<1024>(s, sh);
-        if (threadIdx.x == 0) {
-            int hh = h0 + h;
-            if (hh <= hmax && ls[1] == 0.0) {
-                double al = ldexp(am, -hh);
-                double dE = al * scal[0] + 0.5 * al * al * scal[1] + kappa * s;
-                if (dE < 0.0) {
-                    ls[1] = 1.0;
-                    out[0] = al;
-                    out[1] = hh + 1;
-                    out[2] = dE;
-                    out[3] = 0;
-                } else if (hh == hmax) {
-                    ls[1] = 2.0;
-                    out[0] = 0.0;
-                    out[1] = hh + 1;
-                    out[2] = 0.0;
-                    out[3] = 1;   // stall
-                }
-            }
-        }
-        __syncthreads();
-    }
-}
-
 // One line-search round: trial alphas alpha_m 2^-(h0+h), h < KH, evaluated per candidate
 // (barrier differences), block partials, and the decision taken by the LAST block to finish
 // (atomic ticket; partials summed in fixed block order: deterministic).  Replaces the
@@ -1250,16 +1172,6 @@ void launch_accd(const unsigned long long *keys, const int *ccnt, int cap, const
 }
 int ls_blocks() { return 2 * 148; }
 int ls_round_width() { return kLsRound; }
-void launch_ls_trials(const unsigned long long *keys, const int *ccnt, const double4 *s, const int *tris,
-                      const int *edges, int Nt, int Ne, const double4 *ds, double dh, double *b0,
-                      const double *ls, int h0, double *part, cudaStream_t st) {
-    PairCtx c{s, tris, edges, Nt, Ne};
-    PDI_LAUNCH(k_ls_trials, ls_blocks(), 256, 0, st)(keys, ccnt, c, ds, dh, b0, ls, h0, part, ls_blocks());
-}
-void launch_ls_decide(const double *part, const double *scal, double kappa, int h0, int hmax, double *ls,
-                      double *out, cudaStream_t st) {
-    PDI_LAUNCH(k_ls_decide, 1, 1024, 0, st)(part, ls_blocks(), ls_blocks(), scal, kappa, h0, hmax, ls, out);
-}
 void launch_ls_round(const unsigned long long *keys, const int *ccnt, const double4 *s, const int *tris,
                      const int *edges, int Nt, int Ne, const double4 *ds, double dh, double *b0, double *ls,
                      int h0, double *part, const double *scal, double kappa, int hmax, double *out,

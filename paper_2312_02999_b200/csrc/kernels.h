@@ -126,16 +126,11 @@ void launch_accd(const unsigned long long *keys, const int *ccnt, int cap, const
                  const int *tris, const int *edges, int Nt, int Ne, const double4 *ds, double s_gap,
                  int max_iters, double *amin, cudaStream_t st);
 int ls_blocks();
-void launch_ls_trials(const unsigned long long *keys, const int *ccnt, const double4 *s, const int *tris,
-                      const int *edges, int Nt, int Ne, const double4 *ds, double dh, double *b0,
-                      const double *ls, int h0, double *part, cudaStream_t st);
 void launch_ls_round(const unsigned long long *keys, const int *ccnt, const double4 *s, const int *tris,
                      const int *edges, int Nt, int Ne, const double4 *ds, double dh, double *b0, double *ls,
                      int h0, double *part, const double *scal, double kappa, int hmax, double *out,
                      int *done_ctr, cudaStream_t st);
 int ls_round_width();
 int ls_round_next(int h0);   // first halving of the round after the one starting at h0
-void launch_ls_decide(const double *part, const double *scal, double kappa, int h0, int hmax, double *ls,
-                      double *out, cudaStream_t st);
 
 }  // namespace pdipc

@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kScanNT) k_scan_tiles(const int *in, int n, co
 
 // Small scans (capacity <= kScanSingleMax): ONE CTA walks tiles of kScanNT x 16 with a running
 // carry -- one launch instead of two, no partials round trip.
-constexpr int kScanSingleIPT = 16, kScanSingleTile = kScanNT * kScanSingleIPT, kScanSingleMax = 4 * kScanSingleTile;
+constexpr int kScanSingleIPT = 16, kScanSingleTile = kScanNT * kScanSingleIPT, kScanSingleMax = 2 * kScanSingleTile;
 __global__ void __launch_bounds__(kScanNT) k_scan_single(const int *__restrict__ in, int n, const int *n_dev,
                                                          int *__restrict__ out) {
     __shared__ int sh[32];
