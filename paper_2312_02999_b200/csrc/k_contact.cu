@@ -530,6 +530,13 @@ __constant__ double c_ns_a[64];
 __constant__ int c_ns_k;
 
 constexpr int kPD_WARPS = 4;
+constexpr int kNsS = 20;               // smem row stride of the padded 16x16 sign iterate
+// D(8x8) += A(8x4) B(4x8) on the FP64 tensor pipe (mma.sync.m8n8k4.f64 -> DMMA)
+__device__ __forceinline__ void dmma_pd(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
 constexpr int kLsRound = 22;          // trial alphas of the last line-search round (h = 9..30)
 
 // Warp per active pair: grad/hess of d^2 (hyper-dual, one Hessian entry per lane-evaluation),
@@ -542,7 +549,8 @@ __global__ void __launch_bounds__(kPD_WARPS * 32, 4) k_pair_derivs(
     int *__restrict__ ids_out, double *__restrict__ dmax) {
     __shared__ double Hs[kPD_WARPS][12][13];
     __shared__ double Vs[kPD_WARPS][12][13];
-    __shared__ double Ws[kPD_WARPS][12][13];
+    __shared__ double Xs[kPD_WARPS][16][kNsS];
+    __shared__ double Ys[kPD_WARPS][16][kNsS];
     __shared__ double gs[kPD_WARPS][12];
     __shared__ double rot[kPD_WARPS][6][2];
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
@@ -626,62 +634,69 @@ __global__ void __launch_bounds__(kPD_WARPS * 32, 4) k_pair_derivs(
     for (int e = lane; e < 144; e += 32) fro += H[e / 12][e % 12] * H[e / 12][e % 12];
     fro = warp_sum(fro);
     const double hinv = fro > 0.0 ? rsqrt(fro) : 0.0;
-    for (int e = lane; e < 144; e += 32) V[e / 12][e % 12] = H[e / 12][e % 12] * hinv;   // X
+    // X (16 x 16, zero padded) on the FP64 tensor pipe: 8x8 output tiles (ti, tj), lane holds
+    // rows 8 ti + gr, columns 8 tj + 2 gc (+1); products of symmetric matrices take their B
+    // fragment by rows (P[i][j] = sum_k A[i][k] B[j][k])
+    double (*Xm)[kNsS] = Xs[wl], (*Ym)[kNsS] = Ys[wl];
+    for (int e = lane; e < 256; e += 32) {
+        const int i = e >> 4, j = e & 15;
+        Xm[i][j] = (i < 12 && j < 12) ? H[i][j] * hinv : 0.0;
+    }
     __syncwarp();
-    double (*X2)[13] = Ws[wl];
-    // register-blocked 12x12 products: lanes 0..23 own a 3x2 output block (rows 3 rb.., columns
-    // 2 cb..), 5 loads per 6 FMAs
-    const int rb = lane / 6, cb = lane % 6;
-    const bool own = lane < 24;
-    auto mm12 = [&](const double (*A)[13], const double (*Bm)[13], double (&o)[3][2]) {
-#pragma unroll
-        for (int r = 0; r < 3; ++r) o[r][0] = o[r][1] = 0.0;
-        if (own) {
-#pragma unroll
-            for (int kk = 0; kk < 12; ++kk) {
-                const double b0 = Bm[kk][2 * cb], b1 = Bm[kk][2 * cb + 1];
-#pragma unroll
-                for (int r = 0; r < 3; ++r) {
-                    const double av = A[3 * rb + r][kk];
-                    o[r][0] = fma(av, b0, o[r][0]);         // explicit FMA: this unit is
-                    o[r][1] = fma(av, b1, o[r][1]);         // built with -fmad=false
-                }
-            }
-        }
-    };
-    // scaled Newton-Schulz steps X <- (3 a X - a^3 X^3) / 2 with the fixed schedule c_ns_a
-    // (contact_init): every eigenvalue of |X0| in [kNsFloor, 1] ends within 1e-16 of 1
+    const int gr = lane >> 2, gc = lane & 3;
     for (int it = 0; it < c_ns_k; ++it) {
         const double c1 = 1.5 * c_ns_a[it], c3 = 0.5 * c_ns_a[it] * c_ns_a[it] * c_ns_a[it];
-        double x2[3][2];
-        mm12(V, V, x2);                                   // X2 = X X
-        if (own)
+        double y[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
 #pragma unroll
-            for (int r = 0; r < 3; ++r) {
-                X2[3 * rb + r][2 * cb] = x2[r][0];
-                X2[3 * rb + r][2 * cb + 1] = x2[r][1];
-            }
+        for (int k4 = 0; k4 < 3; ++k4) {                  // Y = X X  (k < 12)
+            const double a0 = Xm[gr][4 * k4 + gc], a1 = Xm[8 + gr][4 * k4 + gc];
+            dmma_pd(y[0], a0, a0);
+            dmma_pd(y[1], a0, a1);
+            dmma_pd(y[2], a1, a0);
+            dmma_pd(y[3], a1, a1);
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            Ym[8 * (t >> 1) + gr][8 * (t & 1) + 2 * gc] = y[t][0];
+            Ym[8 * (t >> 1) + gr][8 * (t & 1) + 2 * gc + 1] = y[t][1];
+        }
         __syncwarp();
-        double xx[3][2], xn[3][2];
-        mm12(V, X2, xx);                                  // X <- c1 X - c3 X X2
-        if (own)
+        double z[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
 #pragma unroll
-            for (int r = 0; r < 3; ++r)
+        for (int k4 = 0; k4 < 3; ++k4) {                  // Z = X Y
+            const double a0 = Xm[gr][4 * k4 + gc], a1 = Xm[8 + gr][4 * k4 + gc];
+            const double b0 = Ym[gr][4 * k4 + gc], b1 = Ym[8 + gr][4 * k4 + gc];
+            dmma_pd(z[0], a0, b0);
+            dmma_pd(z[1], a0, b1);
+            dmma_pd(z[2], a1, b0);
+            dmma_pd(z[3], a1, b1);
+        }
+        double xn[4][2];
 #pragma unroll
-                for (int q = 0; q < 2; ++q) xn[r][q] = c1 * V[3 * rb + r][2 * cb + q] - c3 * xx[r][q];
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+                xn[t][q] = c1 * Xm[8 * (t >> 1) + gr][8 * (t & 1) + 2 * gc + q] - c3 * z[t][q];
         __syncwarp();
         // keep X exactly symmetric: rounding asymmetry would otherwise seed non-normal
         // components that the iteration amplifies
-        if (own)
 #pragma unroll
-            for (int r = 0; r < 3; ++r) {
-                X2[3 * rb + r][2 * cb] = xn[r][0];
-                X2[3 * rb + r][2 * cb + 1] = xn[r][1];
+        for (int t = 0; t < 4; ++t) {
+            Ym[8 * (t >> 1) + gr][8 * (t & 1) + 2 * gc] = xn[t][0];
+            Ym[8 * (t >> 1) + gr][8 * (t & 1) + 2 * gc + 1] = xn[t][1];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int i = 8 * (t >> 1) + gr, j = 8 * (t & 1) + 2 * gc + q;
+                Xm[i][j] = 0.5 * (xn[t][q] + Ym[j][i]);
             }
         __syncwarp();
-        for (int e = lane; e < 144; e += 32) V[e / 12][e % 12] = 0.5 * (X2[e / 12][e % 12] + X2[e % 12][e / 12]);
-        __syncwarp();
     }
+    for (int e = lane; e < 144; e += 32) V[e / 12][e % 12] = Xm[e / 12][e % 12];
+    __syncwarp();
     // H+ = (H + H X) / 2 symmetrized, packed upper
     double mx = lane < 12 ? fabs(kappa * b1 * (gs[wl][lane] / (2.0 * d))) : 0.0;
     for (int e = lane; e < 78; e += 32) {
@@ -1138,7 +1153,7 @@ void launch_pair_derivs(const unsigned long long *akeys, const int *atype, const
                         int Nt, int Ne, double dh, double kappa, double *grad, double *Hp,
                         double *dist, int *ids, double *dmax, cudaStream_t st) {
     PairCtx c{s, tris, edges, Nt, Ne};
-    PDI_LAUNCH(k_pair_derivs, grid_for(cap, kPD_WARPS, 148 * 2), kPD_WARPS * 32, 0, st)(
+    PDI_LAUNCH(k_pair_derivs, grid_for(cap, kPD_WARPS, 148 * 4), kPD_WARPS * 32, 0, st)(
         akeys, atype, ad2, acnt, c, dh, kappa, grad, Hp, dist, ids, dmax);
 }
 void launch_mark_S(const int *ids, const int *acnt, int cap, const int *Wp, const int *Wc, const int *v2q,
