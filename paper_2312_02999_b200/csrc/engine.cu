@@ -489,11 +489,11 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
         const DevFactor &F2 = h->F;
         CK(cudaEventRecord(h->ev_fork, st));
         CK(cudaStreamWaitEvent(s2, h->ev_fork, 0));
-        CK(dev_zero(h->ticket2.p, 4 * sizeof(int), s2));   // [0] ticket, [1] fault, [2] |S| = 0
         kt.start(K_D_SYRK, s2);
-        launch_ts_items(F2, nullptr, h->ticket2.p + 2, 0, h->ticket2.p + 2, 0, h->ticket2.p + 3, 1, h->ts_lo2.p,
-                        h->ts_hi2.p, h->ts_cnt2.p, h->ts_rem2.p, s2);
-        scan_exclusive(h->ts_cnt2.p, h->ts_ptr2.p, F2.nsn, h->iscr2.p, s2);
+        // ticket2: [0] item dispenser (cleared by the plan), [1] fault (cleared per batch),
+        // [2] |S| = 0 (never written), [3] flags (unused in gradient-only mode)
+        launch_ts_plan(F2, nullptr, h->ticket2.p + 2, 0, h->ticket2.p + 2, 0, h->ticket2.p + 3, 1, h->ts_lo2.p,
+                       h->ts_hi2.p, h->ts_cnt2.p, h->ts_rem2.p, h->ts_ptr2.p, h->ticket2.p, s2);
         launch_forward_solve(F2, h->ts_lo2.p, h->ts_hi2.p, h->ts_ptr2.p, nullptr, h->ts_rem2.p, h->ticket2.p,
                              reinterpret_cast<const double *>(h->g_el.p), h->Yw.p, nullptr, h->ldv, h->Ug2.p,
                              nullptr, h->ticket2.p + 2, 0, 1, h->Nt > 0 ? h->side_ctas : h->nsm, nullptr, s2);
@@ -562,12 +562,10 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
     // ---------------- G-Step
     // pure-PD part on stream 2 (forked after the gather, see above); here the contact part
     const DevFactor &F = h->F;
-    CK(dev_zero(h->ticket.p, 2 * sizeof(int), st));
     kt.start(K_FWD, st);
     // panel V_s = L^-1 Pi E_S (panel tiles only; no items when S is unchanged)
-    launch_ts_items(F, h->qS.p, nS_dev, h->capS, h->dint.p + D_SPREV + 1, (long long)h->Up.n,
-                    h->dint.p + D_CAP, 2, h->ts_lo.p, h->ts_hi.p, h->ts_cnt.p, h->ts_rem.p, st);
-    scan_exclusive(h->ts_cnt.p, h->ts_ptr.p, F.nsn, h->iscr.p, st);
+    launch_ts_plan(F, h->qS.p, nS_dev, h->capS, h->dint.p + D_SPREV + 1, (long long)h->Up.n, h->dint.p + D_CAP, 2,
+                   h->ts_lo.p, h->ts_hi.p, h->ts_cnt.p, h->ts_rem.p, h->ts_ptr.p, h->ticket.p, st);
     if (h->trace_file) h->trace.ensure(4 * (size_t)F.bw_nblocks * (2 + (h->capS + 31) / 32));
     launch_forward_solve(F, h->ts_lo.p, h->ts_hi.p, h->ts_ptr.p, h->qS.p, h->ts_rem.p, h->ticket.p, h->G.p,
                          h->Yw.p, h->V.p, h->ldv, h->Ug.p, h->Up.p, nS_dev, h->capS, 0, h->nsm,
@@ -648,6 +646,8 @@ static int run_batch(pd_ipc *h, Seq &q, int k, double ms[6]) {
     const unsigned key_mask = kt.on ? kt.mask : 0u;
     auto enqueue_batch = [&]() {
         CK(dev_zero(h->dint.p + D_ABORT, 4 * sizeof(int), st));   // abort, index, why, reused
+        CK(dev_zero(h->ticket.p + 1, sizeof(int), st));             // solve fault flags of the batch
+        CK(dev_zero(h->ticket2.p + 1, sizeof(int), st));
         for (int i = 0; i < k; ++i) enqueue_iteration(h, q, i);
     };
     if (graph && (!q.exec || q.graph_key != key || q.graph_batch != k || q.graph_mask != key_mask)) {

@@ -34,29 +34,27 @@ constexpr int kPT = 32;                // panel tile width
 // waiting CTA records the fault in ticket[1] and proceeds instead of hanging the GPU.
 constexpr long long kSpinLimit = 4000000000LL;
 
-// per-iteration item setup: active column ranges and item counts (row blocks x (1 + tiles))
-__global__ void k_ts_items(const int *__restrict__ ford, const int *__restrict__ sn_c0,
-                           const int *__restrict__ sn_rowptr, const int *__restrict__ sn_fd,
-                           const int *__restrict__ sn_parent, int nsn, const int *__restrict__ qS,
-                           const int *__restrict__ nS_ptr, int capS, const int *__restrict__ same_S,
-                           int nU, long long up_cap, int *__restrict__ flags, int mode,
-                           int *__restrict__ lo, int *__restrict__ hi, int *__restrict__ cnt,
-                           int *__restrict__ rem) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;   // dispatch position
-    if (k >= nsn) return;
+// per-iteration item setup: active column ranges and item counts (row blocks x (1 + tiles)) of
+// the supernode at dispatch position k; adds the count to the parent's dependency counter
+__device__ __forceinline__ int ts_item_count(int k, const int *__restrict__ ford, const int *__restrict__ sn_c0,
+                                             const int *__restrict__ sn_rowptr, const int *__restrict__ sn_fd,
+                                             const int *__restrict__ sn_parent, const int *__restrict__ qS,
+                                             const int *__restrict__ nS_ptr, int capS,
+                                             const int *__restrict__ same_S, int nU, long long up_cap,
+                                             int *__restrict__ flags, int mode, int *__restrict__ lo,
+                                             int *__restrict__ hi, int *__restrict__ rem) {
     const int s = ford[k];
     const int nb = (sn_rowptr[s + 1] - sn_rowptr[s] + kSolveRB - 1) / kSolveRB;
     if (!(mode & 2)) {                     // gradient items only: no contact data read at all
         lo[s] = hi[s] = 0;
-        cnt[k] = nb;
         const int p = sn_parent[s];
         if (p >= 0) atomicAdd(rem + p, nb);
-        return;
+        return nb;
     }
     const int nS = min(*nS_ptr, capS);
     // panel update rows need nU x round32(|S|) doubles; otherwise flag bit 4 (grow and redo)
     const bool up_ok = (long long)nU * (((nS + 31) / 32) * 32) <= up_cap;
-    if ((mode & 2) && !up_ok && k == 0) atomicOr(flags, 4);
+    if (!up_ok && k == 0) atomicOr(flags, 4);
     const int a = sn_fd[s], b = sn_c0[s + 1];
     int l = 0, r = nS;
     while (l < r) { int m = (l + r) >> 1; if (qS[m] < a) l = m + 1; else r = m; }
@@ -67,11 +65,66 @@ __global__ void k_ts_items(const int *__restrict__ ford, const int *__restrict__
     lo[s] = L0;
     hi[s] = H0;
     // panel tiles only when V_s must be recomputed (S changed)
-    const int tiles = ((mode & 2) && up_ok && *same_S == 0 && H0 > L0) ? (H0 - 1) / kPT - L0 / kPT + 1 : 0;
-    int c = nb * ((mode & 1) + tiles);
-    cnt[k] = c;
-    int p = sn_parent[s];
+    const int tiles = (up_ok && *same_S == 0 && H0 > L0) ? (H0 - 1) / kPT - L0 / kPT + 1 : 0;
+    const int c = nb * ((mode & 1) + tiles);
+    const int p = sn_parent[s];
     if (p >= 0) atomicAdd(rem + p, c);
+    return c;
+}
+
+// The whole per-iteration plan of a solve in ONE block: dependency counters and the item
+// dispenser cleared, item counts and column ranges of every supernode, and their exclusive scan
+// item_ptr[0..nsn] (replaces a clear, the count kernel and a two-pass scan).
+constexpr int kPlanNT = 1024;
+__global__ void __launch_bounds__(kPlanNT) k_ts_plan(const int *__restrict__ ford, const int *__restrict__ sn_c0,
+                                                     const int *__restrict__ sn_rowptr, const int *__restrict__ sn_fd,
+                                                     const int *__restrict__ sn_parent, int nsn,
+                                                     const int *__restrict__ qS, const int *__restrict__ nS_ptr,
+                                                     int capS, const int *__restrict__ same_S, int nU,
+                                                     long long up_cap, int *__restrict__ flags, int mode,
+                                                     int *__restrict__ lo, int *__restrict__ hi,
+                                                     int *__restrict__ cnt, int *__restrict__ rem,
+                                                     int *__restrict__ item_ptr, int *__restrict__ ticket) {
+    __shared__ int wsum[kPlanNT / 32];
+    __shared__ int carry;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (int i = tid; i < nsn; i += kPlanNT) rem[i] = 0;
+    if (tid == 0) {
+        ticket[0] = 0;
+        carry = 0;
+    }
+    __syncthreads();
+    for (int k = tid; k < nsn; k += kPlanNT)
+        cnt[k] = ts_item_count(k, ford, sn_c0, sn_rowptr, sn_fd, sn_parent, qS, nS_ptr, capS, same_S, nU, up_cap,
+                               flags, mode, lo, hi, rem);
+    __syncthreads();
+    for (int k0 = 0; k0 <= nsn; k0 += kPlanNT) {          // exclusive scan, item_ptr[nsn] = total
+        const int k = k0 + tid;
+        const int v = k < nsn ? cnt[k] : 0;
+        int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            int t = wsum[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += y;
+            }
+            wsum[lane] = t;
+        }
+        __syncthreads();
+        const int ex = carry + (wid > 0 ? wsum[wid - 1] : 0) + x - v;
+        if (k <= nsn) item_ptr[k] = ex;
+        __syncthreads();
+        if (tid == 0) carry += wsum[kPlanNT / 32 - 1];
+        __syncthreads();
+    }
 }
 
 struct FwdArgs {
@@ -508,13 +561,12 @@ void trisolve_init() {
     cudaFuncSetAttribute(k_backward_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem);
 }
 
-void launch_ts_items(const DevFactor &F, const int *qS, const int *nS_ptr, int capS, const int *same_S,
-                     long long up_cap, int *flags, int mode, int *lo, int *hi, int *cnt, int *rem,
-                     cudaStream_t st) {
-    dev_zero(rem, sizeof(int) * F.nsn, st);
-    PDI_LAUNCH(k_ts_items, (F.nsn + 255) / 256, 256, 0, st)(F.ford, F.sn_c0, F.sn_rowptr, F.sn_fd,
-                                                             F.sn_parent, F.nsn, qS, nS_ptr, capS, same_S,
-                                                             F.nU, up_cap, flags, mode, lo, hi, cnt, rem);
+void launch_ts_plan(const DevFactor &F, const int *qS, const int *nS_ptr, int capS, const int *same_S,
+                    long long up_cap, int *flags, int mode, int *lo, int *hi, int *cnt, int *rem, int *item_ptr,
+                    int *ticket, cudaStream_t st) {
+    PDI_LAUNCH(k_ts_plan, 1, kPlanNT, 0, st)(F.ford, F.sn_c0, F.sn_rowptr, F.sn_fd, F.sn_parent, F.nsn, qS, nS_ptr,
+                                              capS, same_S, F.nU, up_cap, flags, mode, lo, hi, cnt, rem, item_ptr,
+                                              ticket);
 }
 
 void launch_forward_solve(const DevFactor &F, const int *lo, const int *hi, const int *item_ptr,
@@ -528,7 +580,6 @@ void launch_forward_solve(const DevFactor &F, const int *lo, const int *hi, cons
     A.lo = lo; A.hi = hi; A.item_ptr = item_ptr; A.qS = qS; A.ford = F.ford; A.nsn = F.nsn;
     A.rem = rem; A.ticket = ticket; A.G = G; A.Y = Y; A.V = V; A.ldv = ldv;
     A.Ug = Ug; A.Up = Up; A.nS_ptr = nS_ptr; A.capS = capS; A.with_grad = with_grad; A.trace = trace;
-    dev_zero(ticket, sizeof(int), st);
     PDI_LAUNCH(k_forward_solve, nsm, kTS_NT, kFwdSmem, st)(A);
 }
 
@@ -538,9 +589,7 @@ void launch_backward_solve(const DevFactor &F, int *done, int *cnt, int *ticket,
     A.sn_c0 = F.sn_c0; A.sn_rowptr = F.sn_rowptr; A.sn_rows = F.sn_rows; A.sn_parent = F.sn_parent;
     A.sn_valptr = F.sn_valptr; A.Q = F.Q; A.items = F.bw_items; A.pbase = F.bw_pbase;
     A.nitems = F.bw_nitems; A.done = done; A.cnt = cnt; A.ticket = ticket; A.P = P; A.Z = Z;
-    dev_zero(ticket, sizeof(int), st);
-    dev_zero(done, sizeof(int) * F.nsn, st);
-    dev_zero(cnt, sizeof(int) * F.nsn, st);
+    dev_zero3(ticket, sizeof(int), done, sizeof(int) * F.nsn, cnt, sizeof(int) * F.nsn, st);
     PDI_LAUNCH(k_backward_solve, nsm, kTS_NT, kFwdSmem, st)(A);
 }
 

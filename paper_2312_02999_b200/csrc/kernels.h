@@ -50,9 +50,11 @@ void launch_scatter_dx(const double *z, const int *q2v, int nf, double4 *dx, cud
 // ---- k_trisolve.cu
 constexpr int kSolveRB = 64;   // rows of a supernode per solve work item
 // mode: bit 0 gradient items, bit 1 panel tiles
-void launch_ts_items(const DevFactor &F, const int *qS, const int *nS_ptr, int capS, const int *same_S,
-                     long long up_cap, int *flags, int mode, int *lo, int *hi, int *cnt, int *rem,
-                     cudaStream_t st);
+// per-iteration plan of a solve (one block): clears rem and ticket[0], item counts, lo/hi,
+// item_ptr = exclusive scan of the counts
+void launch_ts_plan(const DevFactor &F, const int *qS, const int *nS_ptr, int capS, const int *same_S,
+                    long long up_cap, int *flags, int mode, int *lo, int *hi, int *cnt, int *rem, int *item_ptr,
+                    int *ticket, cudaStream_t st);
 void trisolve_init();
 void launch_forward_solve(const DevFactor &F, const int *lo, const int *hi, const int *item_ptr,
                           const int *qS, int *rem, int *ticket, const double *G, double *Y, double *V,

@@ -29,6 +29,20 @@ cudaError_t dev_zero(void *p, size_t bytes, cudaStream_t st) {
     PDI_LAUNCH(k_zero32, fill_grid(n), 256, 0, st)(static_cast<unsigned *>(p), n);
     return cudaGetLastError();
 }
+__global__ void k_zero32x3(unsigned *__restrict__ a, size_t na, unsigned *__restrict__ b, size_t nb,
+                           unsigned *__restrict__ c, size_t nc) {
+    const size_t i0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x, st = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = i0; i < na; i += st) a[i] = 0u;
+    for (size_t i = i0; i < nb; i += st) b[i] = 0u;
+    for (size_t i = i0; i < nc; i += st) c[i] = 0u;
+}
+cudaError_t dev_zero3(void *a, size_t ba, void *b, size_t bb, void *c, size_t bc, cudaStream_t st) {
+    const size_t n = std::max({ba, bb, bc}) / 4;
+    if (n == 0) return cudaSuccess;
+    PDI_LAUNCH(k_zero32x3, fill_grid(n), 256, 0, st)(static_cast<unsigned *>(a), ba / 4, static_cast<unsigned *>(b),
+                                                     bb / 4, static_cast<unsigned *>(c), bc / 4);
+    return cudaGetLastError();
+}
 cudaError_t dev_copy(void *d, const void *s, size_t bytes, cudaStream_t st) {
     const size_t n = bytes / 4;
     if (n == 0) return cudaSuccess;

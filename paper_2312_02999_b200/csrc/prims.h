@@ -6,6 +6,8 @@ namespace pdipc {
 // stream-ordered zero fill / device copy as library kernels (bytes: multiples of 4)
 cudaError_t dev_zero(void *p, size_t bytes, cudaStream_t st);
 cudaError_t dev_copy(void *d, const void *s, size_t bytes, cudaStream_t st);
+// three zero fills in one launch
+cudaError_t dev_zero3(void *a, size_t ba, void *b, size_t bb, void *c, size_t bc, cudaStream_t st);
 // out[0..n] : exclusive scan of in[0..n), out[n] = total.  scratch: scan_scratch_ints(n).
 void scan_exclusive(const int *in, int *out, int n, int *scratch, cudaStream_t st);
 // same with the length read on the device (*n_dev, at most cap; grid sized for cap)
