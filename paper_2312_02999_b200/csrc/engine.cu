@@ -374,17 +374,15 @@ static void broad_phase(pd_ipc *h, const double4 *ds, double infl, int *ccnt, in
     cudaStream_t st = h->st;
     const int Ns = h->Ns, Nt = h->Nt, Ne = h->Ne;
     double *ext = h->dscal.p + 14;   // cell = [max box extent, cap]
-    set_d(h, ext, h->cell0);
-    set_d(h, ext + 1, kCellCap * h->cell0);
-    launch_boxes(h->s.p, ds, h->tris.p, h->edges.p, Ns, Nt, Ne, infl, h->blo.p, h->bhi.p, ext, st);
     const unsigned M = h->hmask + 1;
     const int nq = Ns + Ne, cap_ent = (int)h->hent.n;
-    CK(dev_zero(hovf, sizeof(int), st));
-    // both tables (tris, edges) in one pass each: count, scan, fill
-    CK(dev_zero(h->hcnt.p, sizeof(int) * 2 * (M + 1), st));
+    // ext = [cell0, cap], overflow flag and both tables' bucket counts cleared in one launch
+    launch_broad_prep(ext, h->cell0, kCellCap * h->cell0, hovf, h->hcnt.p, (int)(2 * (M + 1)), st);
+    launch_boxes(h->s.p, ds, h->tris.p, h->edges.p, Ns, Nt, Ne, infl, h->blo.p, h->bhi.p, ext, st);
+    // both tables (tris, edges) in one pass each: count, scan (which clears the counts for the
+    // fill pass's cursors), fill
     launch_hash_insert(h->blo.p, h->bhi.p, Ns, Nt, Ne, ext, h->hmask, h->hcnt.p, nullptr, nullptr, 0, hovf, st);
-    scan_exclusive(h->hcnt.p, h->hstart.p, (int)(2 * (M + 1)), h->iscr.p, st);
-    CK(dev_zero(h->hcnt.p, sizeof(int) * 2 * (M + 1), st));
+    scan_exclusive_clear(h->hcnt.p, h->hstart.p, (int)(2 * (M + 1)), h->iscr.p, st);
     launch_hash_insert(h->blo.p, h->bhi.p, Ns, Nt, Ne, ext, h->hmask, h->hcnt.p, h->hstart.p, h->hent.p,
                        cap_ent, hovf, st);
     // one warp per query (PT points, then EE edges): sorted unique partner lists
@@ -522,14 +520,12 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
                               h->atype.p, h->ad2.p, acnt, st);
         kt.stop(K_NARROW, st);
         kt.start(K_DERIV, st);
-        set_d(h, dmax, 0.0);
-        set_d(h, dmax + 1, 1e300);
+        launch_contact_prep(h->mark.p, nf, h->gsq.p, 6 * Ns, dmax, st);   // clears of a5-a6
         launch_pair_derivs(h->akeys.p, h->atype.p, h->ad2.p, acnt, cap, h->s.p, h->tris.p, h->edges.p, Nt,
                            Ne, h->dh, h->kappa, h->grad.p, h->Hp.p, h->dist.p, h->ids.p, dmax, st);
         kt.stop(K_DERIV, st);
         kt.start(K_ASSEMBLY, st);
         // S
-        CK(dev_zero(h->mark.p, sizeof(int) * nf, st));
         launch_mark_S(h->ids.p, acnt, cap, h->Wp.p, h->Wc.p, h->v2q.p, h->mark.p, st);
         scan_exclusive(h->mark.p, h->spos.p, nf, h->iscr.p, st);
         launch_compact_S(h->mark.p, h->spos.p, nf, h->qS.p, st);
@@ -538,7 +534,6 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
         launch_same_S(h->qS.p, nS_dev, h->qS_prev.p, h->dint.p + D_SPREV, h->dint.p + D_SPREV + 1, h->capS,
                       h->opt.no_sigma_reuse == 0, h->dint.p + D_CAP, h->dint.p + D_REUSED, st);
         // gradient pull-back: deterministic fixed-point accumulation on the surface, then W^T
-        CK(dev_zero(h->gsq.p, sizeof(long long) * 6 * Ns, st));
         launch_accum_grad_fx(h->ids.p, acnt, cap, h->grad.p, dmax, h->gsq.p, st);
         launch_grad_pullback_fx(h->g_el.p, h->WTp.p, h->WTr.p, h->WTv.p, h->gsq.p, dmax, acnt, nf, h->G.p, st);
         launch_gather_gc(h->qS.p, nS_dev, h->capS, h->WTp.p, h->WTr.p, h->WTv.p, h->gsq.p, dmax, acnt, h->gcS.p, st);
@@ -546,8 +541,7 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
         // low words of the fixed-point sums live in the (not yet used) Sigma-hat buffer
         const int ldb = 3 * h->capS;
         long long *Bl = reinterpret_cast<long long *>(h->Sh.p);
-        launch_zero_square(h->Bc.p, ldb, nS_dev, h->capS, st);
-        launch_zero_square(h->Sh.p, ldb, nS_dev, h->capS, st);
+        launch_zero_square(h->Bc.p, h->Sh.p, ldb, nS_dev, h->capS, st);
         launch_accum_bc_fx(h->ids.p, acnt, cap, h->Wp.p, h->Wc.p, h->Wv.p, h->v2q.p, h->spos.p, h->Hp.p, dmax,
                            reinterpret_cast<long long *>(h->Bc.p), Bl, ldb, st);
         launch_fx_to_double(reinterpret_cast<long long *>(h->Bc.p), Bl, ldb, nS_dev, h->capS, dmax, acnt, st);

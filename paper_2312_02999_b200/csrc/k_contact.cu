@@ -403,9 +403,16 @@ k_hash_query_warp(const double4 *__restrict__ lo, const double4 *__restrict__ hi
 // Emit the per-query lists at their scanned offsets as keys a*nB + b (PT block, then EE block).
 __global__ void __launch_bounds__(32 * kQWarps)
 k_hash_emit(int Ns, int Nt, int Ne, const int *__restrict__ cnt, const int *__restrict__ off,
-            const int *__restrict__ qlist, unsigned long long *__restrict__ out, int cap) {
+            const int *__restrict__ qlist, unsigned long long *__restrict__ out, int cap, int *__restrict__ ccnt,
+            int *__restrict__ flags) {
     const int lane = threadIdx.x & 31;
     const int q = blockIdx.x * kQWarps + (threadIdx.x >> 5);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {   // candidate counts [npt, ntot], clamped (bit 1: grow)
+        const int npt = off[Ns], ntot = off[Ns + Ne];
+        if (ntot > cap) atomicOr(flags, 1);
+        ccnt[0] = min(npt, cap);
+        ccnt[1] = min(ntot, cap);
+    }
     if (q >= Ns + Ne) return;
     const bool is_pt = q < Ns;
     const unsigned long long a = is_pt ? q : q - Ns, nB = is_pt ? Nt : Ne;
@@ -414,15 +421,6 @@ k_hash_emit(int Ns, int Nt, int Ne, const int *__restrict__ cnt, const int *__re
     for (int i = lane; i < c && o0 + i < cap; i += 32) out[o0 + i] = a * nB + (unsigned long long)l[i];
 }
 
-// candidate counts [npt, ntot] from the scanned query offsets, clamped to the buffer capacity
-// (a clamp raises bit 1 of *flags: the iteration is redone with a larger buffer)
-__global__ void k_cand_counts(const int *__restrict__ off, int Ns, int nq, int cap, int *__restrict__ ccnt,
-                              int *__restrict__ flags) {
-    const int npt = off[Ns], ntot = off[nq];
-    if (ntot > cap) atomicOr(flags, 1);
-    ccnt[0] = min(npt, cap);
-    ccnt[1] = min(ntot, cap);
-}
 
 // ------------------------------------------------------------------ a5 narrow filter ------
 // flag[i] = d^2 < dh2 for candidate keys; stores type and d^2
@@ -936,11 +934,41 @@ __global__ void k_gather_gc(const int *__restrict__ qS, const int *__restrict__ 
         gc[3 * a + 2] = bz;
     }
 }
-__global__ void k_zero_square(double *M, int ld, const int *nS_ptr, int capS) {
+// broad-phase setup in one launch: cell size seed ext[0] and cap ext[1], overflow flag, cleared
+// bucket counts of both hash tables
+__global__ void k_broad_prep(double *__restrict__ ext, double cell0, double cap, int *__restrict__ ovf,
+                             int *__restrict__ hcnt, int n) {
+    const int i0 = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int i = i0; i < n; i += gridDim.x * blockDim.x) hcnt[i] = 0;
+    if (i0 == 0) {
+        ext[0] = cell0;
+        ext[1] = cap;
+        *ovf = 0;
+    }
+}
+
+// per-iteration clears of the contact stages in one launch: S marks, the fixed-point surface
+// gradient, the fixed-point scale (dmax[0] = 0) and the min-distance stat (dmax[1] = +inf)
+__global__ void k_contact_prep(int *__restrict__ mark, int nf, long long *__restrict__ gsq, int ngsq,
+                               double *__restrict__ dmax) {
+    const int i0 = blockIdx.x * blockDim.x + threadIdx.x, st = gridDim.x * blockDim.x;
+    for (int i = i0; i < nf; i += st) mark[i] = 0;
+    for (int i = i0; i < ngsq; i += st) gsq[i] = 0;
+    if (i0 == 0) {
+        dmax[0] = 0.0;
+        dmax[1] = 1e300;
+    }
+}
+
+// zero the leading 3|S| x 3|S| block of M and of M2 (when not null) in one launch
+__global__ void k_zero_square(double *M, double *M2, int ld, const int *nS_ptr, int capS) {
     const int n = 3 * min(*nS_ptr, capS);
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < (size_t)n * n;
-         e += (size_t)gridDim.x * blockDim.x)
-        M[(e / n) * ld + e % n] = 0.0;
+         e += (size_t)gridDim.x * blockDim.x) {
+        const size_t o = (e / n) * ld + e % n;
+        M[o] = 0.0;
+        if (M2) M2[o] = 0.0;
+    }
 }
 
 // ------------------------------------------------------------------ a10 ACCD --------------
@@ -1131,10 +1159,9 @@ void launch_hash_query_warp(const double4 *lo, const double4 *hi, int Ns, int Nt
 void launch_hash_emit(int Ns, int Nt, int Ne, const int *cnt, const int *off, const int *qlist,
                       unsigned long long *out, int cap, int *ccnt, int *flags, cudaStream_t st) {
     const int nq = Ns + Ne;
-    PDI_LAUNCH(k_cand_counts, 1, 1, 0, st)(off, Ns, nq, cap, ccnt, flags);
-    if (nq > 0)
-        PDI_LAUNCH(k_hash_emit, (nq + kQWarps - 1) / kQWarps, 32 * kQWarps, 0, st)(Ns, Nt, Ne, cnt, off,
-                                                                                 qlist, out, cap);
+    PDI_LAUNCH(k_hash_emit, std::max(1, (nq + kQWarps - 1) / kQWarps), 32 * kQWarps, 0, st)(Ns, Nt, Ne, cnt, off,
+                                                                                          qlist, out, cap, ccnt,
+                                                                                          flags);
 }
 void launch_narrow(const unsigned long long *keys, const int *ccnt, int cap, const double4 *s,
                    const int *tris, const int *edges, int Nt, int Ne, double dh2, int *flag,
@@ -1176,8 +1203,15 @@ void launch_gather_gc(const int *qS, const int *nS, int capS, const int *WTp, co
                       const long long *gsq, const double *dmax, const int *acnt, double *gc, cudaStream_t st) {
     PDI_LAUNCH(k_gather_gc, grid_for(capS, 128, 148), 128, 0, st)(qS, nS, capS, WTp, WTr, WTv, gsq, dmax, acnt, gc);
 }
-void launch_zero_square(double *M, int ld, const int *nS, int capS, cudaStream_t st) {
-    PDI_LAUNCH(k_zero_square, 296, 256, 0, st)(M, ld, nS, capS);
+void launch_broad_prep(double *ext, double cell0, double cap, int *ovf, int *hcnt, int n, cudaStream_t st) {
+    PDI_LAUNCH(k_broad_prep, std::max(1, std::min(148 * 2, (n + 255) / 256)), 256, 0, st)(ext, cell0, cap, ovf, hcnt, n);
+}
+void launch_contact_prep(int *mark, int nf, long long *gsq, int ngsq, double *dmax, cudaStream_t st) {
+    PDI_LAUNCH(k_contact_prep, std::max(1, std::min(148 * 2, (std::max(nf, ngsq) + 255) / 256)), 256, 0, st)(
+        mark, nf, gsq, ngsq, dmax);
+}
+void launch_zero_square(double *M, double *M2, int ld, const int *nS, int capS, cudaStream_t st) {
+    PDI_LAUNCH(k_zero_square, 296, 256, 0, st)(M, M2, ld, nS, capS);
 }
 void launch_accd(const unsigned long long *keys, const int *ccnt, int cap, const double4 *s,
                  const int *tris, const int *edges, int Nt, int Ne, const double4 *ds, double s_gap,

@@ -795,16 +795,14 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
                 __syncthreads();
             }
             if (bid < ntile) {
-                // factored diagonal tile k (T1) and its block inverses
-                ld_tile(T1, a.Sh + (size_t)kc0 * a.ldh + kc0, a.ldh, kn, kn);
-                ld_dblocks(Dsh[0], Dst + (size_t)k * 512);
-                __syncthreads();
-                if (kn < TB)                                 // padding rows: identity (as factored)
-                    for (int e = tid; e < TB * TB; e += NT) {
-                        const int r = e >> 6, c = e & 63;
-                        if (r >= kn || c >= kn) T1[r * TS + c] = (r == c) ? 1.0 : 0.0;
-                    }
-                __syncthreads();
+                // factored diagonal tile k (T1) and its block inverses: copies in flight together
+                // with the tile loads below (one wait per step)
+                ld_tile_async(T1, a.Sh + (size_t)kc0 * a.ldh + kc0, a.ldh, kn, kn);
+                for (int e = tid; e < 512; e += NT) {
+                    const unsigned sa = (unsigned)__cvta_generic_to_shared(&Dsh[0][e >> 6][(e >> 3) & 7][e & 7]);
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(Dst + (size_t)k * 512 + e));
+                }
+                asm volatile("cp.async.commit_group;\n" ::);
             }
             for (int b = bid; b < ntile; b += G) {
                 // b == 0 -> the look-ahead tile (k+1, k+1) on CTA 0
@@ -812,18 +810,24 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
                 while (bb >= rr - i) { bb -= rr - i; ++i; }
                 const int tj = k + 1 + i, ti = tj + bb;
                 const int r0 = ti * TB, c0 = tj * TB, rows = min(TB, ma - r0), cols = min(TB, ma - c0);
-                // L_ik (T0), L_jk (T3)
-                ld_tile(T0, a.Sh + (size_t)r0 * a.ldh + kc0, a.ldh, rows, kn);
-                if (tj != ti) ld_tile(T3, a.Sh + (size_t)c0 * a.ldh + kc0, a.ldh, cols, kn);
+                // A_ik (T0), A_jk (T3), A_ij (T2): all copies issued, one wait
+                ld_tile_async(T0, a.Sh + (size_t)r0 * a.ldh + kc0, a.ldh, rows, kn);
+                if (tj != ti) ld_tile_async(T3, a.Sh + (size_t)c0 * a.ldh + kc0, a.ldh, cols, kn);
+                ld_tile_async(T2, a.Sh + (size_t)r0 * a.ldh + c0, a.ldh, rows, cols);
+                asm volatile("cp.async.wait_all;\n" ::);
                 __syncthreads();
-                tile_trsm_d(T0, T1, Dsh[0]);
+                if (kn < TB)                                 // padding rows: identity (as factored)
+                    for (int e = tid; e < TB * TB; e += NT) {
+                        const int r = e >> 6, c = e & 63;
+                        if (r >= kn || c >= kn) T1[r * TS + c] = (r == c) ? 1.0 : 0.0;
+                    }
+                __syncthreads();
+                tile_trsm_d(T0, T1, Dsh[0]);                 // L_ik, L_jk
                 if (tj != ti) tile_trsm_d(T3, T1, Dsh[0]);
                 __syncthreads();
                 if (tj == ti)                                // the diagonal-tile CTA keeps L_ik
                     for (int e = tid; e < TB * TB; e += NT)
                         LPk[(size_t)(ti - k - 1) * TB * TB + e] = T0[(e >> 6) * TS + (e & 63)];
-                ld_tile(T2, a.Sh + (size_t)r0 * a.ldh + c0, a.ldh, rows, cols);
-                __syncthreads();
                 if (tj == ti) tile_syrk_lower_sub(T2, T0);
                 else tile_xyt(T2, T0, T3, -1.0, true);
                 if (b == 0) {                                // look-ahead: factor tile k+1 now

@@ -121,7 +121,9 @@ void launch_grad_pullback_fx(const double4 *g_el, const int *WTp, const int *WTr
                              cudaStream_t st);
 void launch_grad_pullback(const double4 *g_el, const int *WTp, const int *WTr, const double *WTv,
                           const double4 *gs, int nf, double *G, cudaStream_t st);
-void launch_zero_square(double *M, int ld, const int *nS, int capS, cudaStream_t st);
+void launch_broad_prep(double *ext, double cell0, double cap, int *ovf, int *hcnt, int n, cudaStream_t st);
+void launch_contact_prep(int *mark, int nf, long long *gsq, int ngsq, double *dmax, cudaStream_t st);
+void launch_zero_square(double *M, double *M2, int ld, const int *nS, int capS, cudaStream_t st);
 void launch_gather_gc(const int *qS, const int *nS, int capS, const int *WTp, const int *WTr, const double *WTv,
                       const long long *gsq, const double *dmax, const int *acnt, double *gc, cudaStream_t st);
 void launch_accd(const unsigned long long *keys, const int *ccnt, int cap, const double4 *s,

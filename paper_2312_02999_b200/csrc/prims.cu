@@ -96,8 +96,8 @@ __global__ void __launch_bounds__(kScanNT) k_scan_partials(const int *in, int n,
     if (threadIdx.x == 0) part[blockIdx.x] = tot;
 }
 
-__global__ void __launch_bounds__(kScanNT) k_scan_tiles(const int *in, int n, const int *n_dev, int *out,
-                                                        const int *part, int nparts) {
+__global__ void __launch_bounds__(kScanNT) k_scan_tiles(int *in, int n, const int *n_dev, int *out,
+                                                        const int *part, int nparts, int zero_in) {
     __shared__ int sh[32];
     __shared__ int off;
     n = scan_len(n, n_dev);
@@ -121,6 +121,7 @@ __global__ void __launch_bounds__(kScanNT) k_scan_tiles(const int *in, int n, co
     for (int i = 0; i < kScanIPT; ++i) {
         if (base + i <= n) out[base + i] = ex;      // out[n] = total
         ex += v[i];
+        if (zero_in && base + i < n) in[base + i] = 0;   // input consumed: cleared for reuse
     }
     (void)nparts;
 }
@@ -172,7 +173,7 @@ void scan_exclusive(const int *in, int *out, int n, int *scratch, cudaStream_t s
     }
     int nb = n / kScanTile + 1;                      // covers index n (the total)
     PDI_LAUNCH(k_scan_partials, nb, kScanNT, 0, st)(in, n, nullptr, scratch);
-    PDI_LAUNCH(k_scan_tiles, nb, kScanNT, 0, st)(in, n, nullptr, out, scratch, nb);
+    PDI_LAUNCH(k_scan_tiles, nb, kScanNT, 0, st)(const_cast<int *>(in), n, nullptr, out, scratch, nb, 0);
 }
 
 void scan_exclusive_dev(const int *in, int *out, const int *n_dev, int cap, int *scratch, cudaStream_t st) {
@@ -182,7 +183,14 @@ void scan_exclusive_dev(const int *in, int *out, const int *n_dev, int cap, int 
     }
     int nb = cap / kScanTile + 1;
     PDI_LAUNCH(k_scan_partials, nb, kScanNT, 0, st)(in, cap, n_dev, scratch);
-    PDI_LAUNCH(k_scan_tiles, nb, kScanNT, 0, st)(in, cap, n_dev, out, scratch, nb);
+    PDI_LAUNCH(k_scan_tiles, nb, kScanNT, 0, st)(const_cast<int *>(in), cap, n_dev, out, scratch, nb, 0);
+}
+
+// exclusive scan that also clears its input (large arrays: the two-pass scan; n > 0)
+void scan_exclusive_clear(int *in, int *out, int n, int *scratch, cudaStream_t st) {
+    int nb = n / kScanTile + 1;
+    PDI_LAUNCH(k_scan_partials, nb, kScanNT, 0, st)(in, n, nullptr, scratch);
+    PDI_LAUNCH(k_scan_tiles, nb, kScanNT, 0, st)(in, n, nullptr, out, scratch, nb, 1);
 }
 
 int scan_scratch_ints(int n) { return n / kScanTile + 2; }

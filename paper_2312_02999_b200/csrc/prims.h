@@ -13,6 +13,8 @@ void scan_exclusive(const int *in, int *out, int n, int *scratch, cudaStream_t s
 // same with the length read on the device (*n_dev, at most cap; grid sized for cap)
 void scan_exclusive_dev(const int *in, int *out, const int *n_dev, int cap, int *scratch, cudaStream_t st);
 int scan_scratch_ints(int n);
+// scan_exclusive that also zeroes in[0..n) after reading it (n > 0)
+void scan_exclusive_clear(int *in, int *out, int n, int *scratch, cudaStream_t st);
 // ascending LSD radix sort of the low `bits` bits; tmp: n keys; scratch: radix_scratch_ints(n)
 void radix_sort_u64(uint64_t *keys, uint64_t *tmp, int n, int bits, int *scratch,
                     cudaStream_t st);
