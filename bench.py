@@ -387,9 +387,13 @@ def _traffic(kernel):
     """DRAM bytes per launch of `kernel` from the committed ncu --set full summary, or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            return json.load(f).get(kernel)
+            t = json.load(f)
     except Exception:
         return None
+    for name, v in t.items():          # template instances are listed as e.g. k_local_step<4>
+        if name == kernel or name.startswith(kernel + "<"):
+            return v
+    return None
 
 
 def _roofline(name, ktimes, sc, hbm, sm_max_mhz, peak_src, stats_log):
