@@ -212,7 +212,7 @@ struct pd_ipc {
     // second stream: w_el = L^-1 Pi g_el runs concurrently with the contact stages (it depends
     // on the elastic gradient only)
     cudaStream_t st2 = nullptr;
-    int side_ctas = 56;       // persistent CTAs of the stream-2 solves (PDIPC_SIDE_CTAS); the rest
+    int side_ctas = 64;       // persistent CTAs of the stream-2 solves (PDIPC_SIDE_CTAS); the rest
                               // of the SMs run the contact stages concurrently
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     DBuf<double> gcS, Ug2;
