@@ -159,19 +159,15 @@ __device__ __forceinline__ bool polar_newton(double X[3][3]) {
             a = 0.5 * sqrt(z);
             b = 0.5 * idet * rsqrt(z);
         }
-        double delta = 0.0;
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                const double v = a * X[i][j] + b * C[i][j];
-                delta += (v - X[i][j]) * (v - X[i][j]);
-                X[i][j] = v;
-            }
-        // quadratic convergence (Higham): |X_{k+1} - R| <= |X_k^{-1}| |X_k - R|^2 / 2 with
-        // |X_k - R| ~ |X_{k+1} - X_k|, so a step below 1e-9 (|X| ~ sqrt 3) leaves X_{k+1} at
-        // rounding level: stop
-        if (delta <= 1e-18) break;
+            for (int j = 0; j < 3; ++j) X[i][j] = a * X[i][j] + b * C[i][j];
+        // convergence from the determinant computed anyway: after a (scaled) Newton step every
+        // singular value is (g s + 1/(g s))/2 >= 1, so det X - 1 = prod(1 + d_i) - 1 >= sum d_i;
+        // det X < 1 + 1e-9 bounds every error d_i by 1e-9, and the step just taken (quadratic,
+        // Higham) leaves X at rounding level
+        if (it >= 1 && det < 1.0 + 1e-9) break;
     }
     return true;
 }
