@@ -156,8 +156,9 @@ __device__ __forceinline__ bool polar_newton(double X[3][3]) {
                     nc += C[i][j] * C[i][j];
                 }
             const double z = sqrt(nc / nx) * idet;       // g^2, |X^-1|_F = |C|_F / det
-            a = 0.5 * sqrt(z);
-            b = 0.5 * idet * rsqrt(z);
+            const double rz = rsqrt(z);                  // a = g/2 = z rz / 2, b = 1/(2 g det)
+            a = 0.5 * z * rz;
+            b = 0.5 * idet * rz;
         }
 #pragma unroll
         for (int i = 0; i < 3; ++i)
