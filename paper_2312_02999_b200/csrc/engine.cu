@@ -468,14 +468,13 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
     const int cap = (int)h->cand.n;
     auto &ev = h->tm.ev[slot];
     int *acnt = h->dint.p + D_ACNT, *ccnt = h->dint.p + D_CCNT;
-    CK(dev_zero(h->dint.p + D_INFO, 4 * sizeof(int), st));   // info, capacity, hash flags
-    CK(dev_zero(acnt, 2 * sizeof(int), st));
+    static_assert(D_ACNT == 0 && D_CCNT == 2 && D_INFO == 4 && D_HOVF + 2 == 8, "cleared by the local step");
     record_event(ev[0], st);
     // ---------------- Misc: a1 local step + a2 gather
     KTimer &kt = h->kt;
     kt.start(K_LOCAL, st);
     launch_local_step(h->tets.p, q.x.p, h->B.p, q.A6.p, h->w.p, T, h->fc.p,
-                      h->debug ? q.p.p : nullptr, st);
+                      h->debug ? q.p.p : nullptr, h->dint.p, st);   // also clears acnt, info, flags
     kt.stop(K_LOCAL, st);
     kt.start(K_GATHER, st);
     launch_gather_elastic(h->inc_ptr.p, h->inc.p, h->fc.p, nf, h->g_el.p, st);
@@ -509,12 +508,11 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
         // (cand, ccnt; boxes over [s, s + ds] inflated by d_hat) contains every pair closer
         // than d_hat at x + alpha dx: the narrow phase filters it exactly (same C)
         if (slot == 0 || h->opt.no_cand_reuse) broad_phase(h, nullptr, 0.5 * h->dh * 1.01, ccnt, h->dint.p + D_HOVF);
-        CK(dev_copy(h->dint.p + D_STAT, ccnt, 2 * sizeof(int), st));
         kt.stop(K_BROAD, st);
         kt.start(K_NARROW, st);
         // one pass over [PT | EE] candidates; one scan; actives come out as [PT | EE], each sorted
         launch_narrow(h->cand.p, ccnt, cap, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->dh2, h->flag.p,
-                      h->ctype.p, h->cd2.p, st);
+                      h->ctype.p, h->cd2.p, h->dint.p + D_STAT, st);
         scan_exclusive_dev(h->flag.p, h->pos.p, ccnt + 1, cap, h->iscr.p, st);
         launch_compact_active(h->cand.p, ccnt, cap, h->flag.p, h->pos.p, h->ctype.p, h->cd2.p, h->akeys.p,
                               h->atype.p, h->ad2.p, acnt, st);
@@ -585,13 +583,11 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
     kt.start(K_BWD, st);
     launch_backward_solve(F, h->ts_done.p, h->bw_cnt.p, h->ticket.p, h->bw_P.p, h->Z.p, h->nsm, st);
     kt.stop(K_BWD, st);
-    CK(dev_zero(h->dx.p, sizeof(double4) * h->n, st));
-    launch_scatter_dx(h->Z.p, h->q2v.p, nf, h->dx.p, st);
-    record_event(ev[3], st);
-    // ---------------- CCD
     double *amin = h->dscal.p + 1;
     double *ls = h->dscal.p + 2, *ls_out = h->dscal.p + 5, *scal = h->dscal.p + 9;
-    set_d(h, amin, 1.0);
+    launch_scatter_dx(h->Z.p, h->q2v.p, nf, h->dx.p, amin, st);   // also seeds *amin = 1
+    record_event(ev[3], st);
+    // ---------------- CCD
     kt.start(K_CCD, st);
     if (Nt > 0) {
         launch_surface(h->Wp.p, h->Wc.p, h->Wv.p, h->dx.p, Ns, h->ds.p, st);
@@ -606,16 +602,14 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
     // ---------------- LS
     kt.start(K_LS, st);
     {
-        int nb1 = gdx_partials(h->g_el.p, h->dx.p, h->q2v.p, nf, h->part.p, st);
-        sum_partials(h->part.p, nb1, scal + 0, st);
-        int nb2 = quad_partials(h->tets.p, h->dx.p, h->B.p, h->w.p, T, h->part.p + nb1, st);
-        sum_partials(h->part.p + nb1, nb2, scal + 1, st);
-        CK(dev_copy(ls, amin, sizeof(double), st));
-        CK(dev_zero(ls + 1, 2 * sizeof(double), st));
+        // elastic terms: block partials here, summed (fixed order) by the first line-search round
+        const int nb1 = gdx_partials(h->g_el.p, h->dx.p, h->q2v.p, nf, h->part.p, st);
+        const int nb2 = quad_partials(h->tets.p, h->dx.p, h->B.p, h->w.p, T, h->part.p + nb1, st);
         const int hmax = h->opt.ls_max_halvings;
         for (int h0 = 0; h0 <= hmax; h0 = ls_round_next(h0))
             launch_ls_round(h->cand.p, ccnt, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->ds.p, h->dh, h->b0.p, ls, h0,
-                            h->lspart.p, scal, h->kappa, hmax, ls_out, h->dint.p + D_LSCTR, st);
+                            h->lspart.p, scal, h->kappa, hmax, ls_out, h->dint.p + D_LSCTR, h->part.p, nb1,
+                            h->part.p + nb1, nb2, amin, st);
         launch_update(q.x.p, h->dx.p, h->q2v.p, nf, ls_out, h->dint.p + D_INFO, h->dint.p + D_ABORT, slot, st);
     }
     kt.stop(K_LS, st);
@@ -1001,6 +995,7 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         CK(cudaMemset(h->ticket2.p, 0, 4 * sizeof(int)));
         h->Z.exact(4 * (size_t)nf);
         h->dx.exact(m.n);
+        CK(cudaMemset(h->dx.p, 0, sizeof(double4) * m.n));   // fixed vertices keep dx = 0
         h->s.exact(std::max(1, m.Ns));
         h->ds.exact(std::max(1, m.Ns));
         h->gs.exact(std::max(1, m.Ns));
@@ -1204,7 +1199,7 @@ int pd_ipc_set_positions(pd_ipc *h, int32_t seq, const double *x) {
             broad_phase(h, nullptr, 0.5 * h->dh * 1.01, ccnt, h->dint.p + D_HOVF);
             h->force_sort = fs;
             launch_narrow(h->cand.p, ccnt, (int)h->cand.n, h->s.p, h->tris.p, h->edges.p, h->Nt, h->Ne, h->dh2,
-                          h->flag.p, h->ctype.p, h->cd2.p, h->st);
+                          h->flag.p, h->ctype.p, h->cd2.p, nullptr, h->st);
             int cc[2];
             sync_read_ints(h, cc, ccnt, 2);
             std::vector<double> d2(cc[1]);

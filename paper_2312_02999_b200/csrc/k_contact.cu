@@ -427,8 +427,12 @@ k_hash_emit(int Ns, int Nt, int Ne, const int *__restrict__ cnt, const int *__re
 // ccnt = [npt, ntot] candidate counts (device).  PT keys first, then EE keys.
 __global__ void k_narrow(const unsigned long long *__restrict__ keys, const int *__restrict__ ccnt,
                          PairCtx c, double dh2, int *__restrict__ flag, int *__restrict__ type,
-                         double *__restrict__ d2out) {
+                         double *__restrict__ d2out, int *__restrict__ stat) {
     const int npt = ccnt[0], n = ccnt[1];
+    if (stat && blockIdx.x == 0 && threadIdx.x == 0) {   // candidate counts of this iteration (stats)
+        stat[0] = npt;
+        stat[1] = n;
+    }
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const bool is_pt = i < npt;
         const int nB = is_pt ? c.Nt : c.Ne;
@@ -535,6 +539,10 @@ __device__ __forceinline__ void dmma_pd(double (&d)[2], double a, double b) {
                  : "+d"(d[0]), "+d"(d[1])
                  : "d"(a), "d"(b));
 }
+struct LsFirst {                       // round 1 only: elastic partials and alpha_max
+    const double *pg, *pq, *amin;
+    int ng, nq;
+};
 constexpr int kLsRound = 22;          // trial alphas of the last line-search round (h = 9..30)
 
 // Warp per active pair: grad/hess of d^2 (hyper-dual, one Hessian entry per lane-evaluation),
@@ -1030,13 +1038,15 @@ __global__ void __launch_bounds__(256) k_ls_round(const unsigned long long *__re
                                                   const double4 *__restrict__ ds, double dh,
                                                   double *__restrict__ b0, double *__restrict__ ls,
                                                   int h0, double *__restrict__ part, int part_ld,
-                                                  const double *__restrict__ scal, double kappa, int hmax,
-                                                  double *__restrict__ out, int *__restrict__ done_ctr) {
-    if (ls[1] != 0.0) return;   // already accepted
+                                                  double *__restrict__ scal, double kappa, int hmax,
+                                                  double *__restrict__ out, int *__restrict__ done_ctr,
+                                                  LsFirst f) {
+    const bool first = h0 == 0;
+    if (!first && ls[1] != 0.0) return;   // already accepted
     __shared__ double sh[8];
     __shared__ int last;
     const int npt = ccnt[0], n = ccnt[1];
-    const double am = ls[0];
+    const double am = first ? *f.amin : ls[0];
     double acc[KH];
 #pragma unroll
     for (int h = 0; h < KH; ++h) acc[h] = 0.0;
@@ -1074,6 +1084,20 @@ __global__ void __launch_bounds__(256) k_ls_round(const unsigned long long *__re
     __syncthreads();
     if (!last) return;
     __threadfence();
+    if (first) {   // elastic terms gTdx, dx^T H dx from their block partials (fixed order); state
+        double g = 0.0, q = 0.0;
+        for (int b = threadIdx.x; b < f.ng; b += blockDim.x) g += __ldcg(f.pg + b);
+        for (int b = threadIdx.x; b < f.nq; b += blockDim.x) q += __ldcg(f.pq + b);
+        g = block_sum<256>(g, sh);
+        q = block_sum<256>(q, sh);
+        if (threadIdx.x == 0) {
+            scal[0] = g;
+            scal[1] = q;
+            ls[0] = am;
+            ls[1] = 0.0;
+        }
+        __syncthreads();
+    }
     // decide: dE(alpha_h) = alpha gTdx + 0.5 alpha^2 quad + kappa dB
     for (int h = 0; h < KH; ++h) {
         double sum = 0.0;
@@ -1165,9 +1189,9 @@ void launch_hash_emit(int Ns, int Nt, int Ne, const int *cnt, const int *off, co
 }
 void launch_narrow(const unsigned long long *keys, const int *ccnt, int cap, const double4 *s,
                    const int *tris, const int *edges, int Nt, int Ne, double dh2, int *flag,
-                   int *type, double *d2, cudaStream_t st) {
+                   int *type, double *d2, int *stat, cudaStream_t st) {
     PairCtx c{s, tris, edges, Nt, Ne};
-    PDI_LAUNCH(k_narrow, grid_for(cap, 256, 148 * 8), 256, 0, st)(keys, ccnt, c, dh2, flag, type, d2);
+    PDI_LAUNCH(k_narrow, grid_for(cap, 256, 148 * 8), 256, 0, st)(keys, ccnt, c, dh2, flag, type, d2, stat);
 }
 void launch_compact_active(const unsigned long long *keys, const int *ccnt, int cap, const int *flag,
                            const int *pos, const int *type, const double *d2, unsigned long long *akeys,
@@ -1223,20 +1247,22 @@ int ls_blocks() { return 2 * 148; }
 int ls_round_width() { return kLsRound; }
 void launch_ls_round(const unsigned long long *keys, const int *ccnt, const double4 *s, const int *tris,
                      const int *edges, int Nt, int Ne, const double4 *ds, double dh, double *b0, double *ls,
-                     int h0, double *part, const double *scal, double kappa, int hmax, double *out,
-                     int *done_ctr, cudaStream_t st) {
+                     int h0, double *part, double *scal, double kappa, int hmax, double *out,
+                     int *done_ctr, const double *pg, int ng, const double *pq, int nq, const double *amin,
+                     cudaStream_t st) {
     PairCtx c{s, tris, edges, Nt, Ne};
+    const LsFirst f{pg, pq, amin, ng, nq};
     // rounds of 1, 8, then 22 trial alphas: the full step is accepted in most iterations, and a
     // round after acceptance returns at once
     if (h0 == 0)
         PDI_LAUNCH(k_ls_round<1>, ls_blocks(), 256, 0, st)(keys, ccnt, c, ds, dh, b0, ls, h0, part, ls_blocks(), scal,
-                                                           kappa, hmax, out, done_ctr);
+                                                           kappa, hmax, out, done_ctr, f);
     else if (h0 == 1)
         PDI_LAUNCH(k_ls_round<8>, ls_blocks(), 256, 0, st)(keys, ccnt, c, ds, dh, b0, ls, h0, part, ls_blocks(), scal,
-                                                           kappa, hmax, out, done_ctr);
+                                                           kappa, hmax, out, done_ctr, f);
     else
         PDI_LAUNCH(k_ls_round<kLsRound>, ls_blocks(), 256, 0, st)(keys, ccnt, c, ds, dh, b0, ls, h0, part,
-                                                                  ls_blocks(), scal, kappa, hmax, out, done_ctr);
+                                                                  ls_blocks(), scal, kappa, hmax, out, done_ctr, f);
 }
 int ls_round_next(int h0) { return h0 == 0 ? 1 : h0 == 1 ? 9 : h0 + kLsRound; }
 

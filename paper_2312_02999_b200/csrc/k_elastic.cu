@@ -182,8 +182,11 @@ template <int MINB>
 __global__ void __launch_bounds__(128, MINB) k_local_step(
     const int4 *__restrict__ tets, const double4 *__restrict__ x, const double *__restrict__ B,
     const double *__restrict__ A6, const double *__restrict__ w, int T, double *__restrict__ fc,
-    double *__restrict__ p) {
+    double *__restrict__ p, int *__restrict__ clr) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
+    // the iteration's device counters, cleared by its first kernel: active-pair counts [0, 1] and
+    // info / capacity / hash flags [4, 8) (the candidate counts [2, 3] carry over, see R8)
+    if (clr && t < 8 && (t < 2 || t >= 4)) clr[t] = 0;
     if (t >= T) return;
     const int4 tv = tets[t];
     const double4 x0 = x[tv.x], x1 = x[tv.y], x2 = x[tv.z], x3 = x[tv.w];
@@ -394,9 +397,11 @@ __global__ void k_update(double4 *__restrict__ x, const double4 *__restrict__ dx
 }
 
 // scatter dx from factor order (solution of the backward solve, [nf][4], negated) to vertices
+// (fixed vertices keep dx = 0 from the clear at create); also seeds the CCD minimum *amin = 1
 __global__ void k_scatter_dx(const double *__restrict__ z, const int *__restrict__ q2v, int nf,
-                             double4 *__restrict__ dx) {
+                             double4 *__restrict__ dx, double *__restrict__ amin) {
     int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q == 0 && amin) *amin = 1.0;
     if (q >= nf) return;
     const double *r = z + 4 * (size_t)q;
     dx[q2v[q]] = make_double4(-r[0], -r[1], -r[2], 0.0);
@@ -415,12 +420,12 @@ void elastic_init(int) {
     if (const char *e = std::getenv("PDIPC_LS_MINB")) g_ls_minb = std::atoi(e);
 }
 void launch_local_step(const int4 *tets, const double4 *x, const double *B, const double *A6,
-                       const double *w, int T, double *fc, double *p, cudaStream_t st) {
+                       const double *w, int T, double *fc, double *p, int *clr, cudaStream_t st) {
     if (T <= 0) return;
     if (g_ls_minb == 5)
-        PDI_LAUNCH(k_local_step<5>, (T + 127) / 128, 128, 0, st)(tets, x, B, A6, w, T, fc, p);
+        PDI_LAUNCH(k_local_step<5>, (T + 127) / 128, 128, 0, st)(tets, x, B, A6, w, T, fc, p, clr);
     else
-        PDI_LAUNCH(k_local_step<4>, (T + 127) / 128, 128, 0, st)(tets, x, B, A6, w, T, fc, p);
+        PDI_LAUNCH(k_local_step<4>, (T + 127) / 128, 128, 0, st)(tets, x, B, A6, w, T, fc, p, clr);
 }
 void launch_gather_elastic(const int *inc_ptr, const int *inc, const double *fc, int nf,
                            double4 *g, cudaStream_t st) {
@@ -448,8 +453,8 @@ void launch_update(double4 *x, const double4 *dx, const int *q2v, int nf, const 
                    const int *flags, int *abort, int it, cudaStream_t st) {
     PDI_LAUNCH(k_update, (nf + 255) / 256, 256, 0, st)(x, dx, q2v, nf, alpha, flags, abort, it);
 }
-void launch_scatter_dx(const double *z, const int *q2v, int nf, double4 *dx, cudaStream_t st) {
-    PDI_LAUNCH(k_scatter_dx, (nf + 255) / 256, 256, 0, st)(z, q2v, nf, dx);
+void launch_scatter_dx(const double *z, const int *q2v, int nf, double4 *dx, double *amin, cudaStream_t st) {
+    PDI_LAUNCH(k_scatter_dx, (nf + 255) / 256, 256, 0, st)(z, q2v, nf, dx, amin);
 }
 
 }  // namespace pdipc

@@ -33,8 +33,10 @@ void add_launches(long long n);   // graph replays account their captured launch
 void launch_set_double(double *p, double v, cudaStream_t st);
 void launch_ingest_actuation(const double *A9, double *A6, int T, cudaStream_t st);
 void elastic_init(int device);
+// clr (nullable): device ints clr[0..1] and clr[4..7] zeroed by the kernel (the iteration's
+// active-pair counts and flags, engine.cu D_ACNT / D_INFO..)
 void launch_local_step(const int4 *tets, const double4 *x, const double *B, const double *A6,
-                       const double *w, int T, double *fc, double *p, cudaStream_t st);
+                       const double *w, int T, double *fc, double *p, int *clr, cudaStream_t st);
 void launch_gather_elastic(const int *inc_ptr, const int *inc, const double *fc, int nf,
                            double4 *g, cudaStream_t st);
 void launch_surface(const int *Wp, const int *Wc, const double *Wv, const double4 *x, int Ns,
@@ -45,7 +47,7 @@ int gdx_partials(const double4 *g, const double4 *dx, const int *q2v, int nf, do
                  cudaStream_t st);
 void launch_update(double4 *x, const double4 *dx, const int *q2v, int nf, const double *alpha,
                    const int *flags, int *abort, int it, cudaStream_t st);
-void launch_scatter_dx(const double *z, const int *q2v, int nf, double4 *dx, cudaStream_t st);
+void launch_scatter_dx(const double *z, const int *q2v, int nf, double4 *dx, double *amin, cudaStream_t st);
 
 // ---- k_trisolve.cu
 constexpr int kSolveRB = 64;   // rows of a supernode per solve work item
@@ -96,7 +98,7 @@ void launch_hash_emit(int Ns, int Nt, int Ne, const int *cnt, const int *off, co
 // [n_pt, n_all] active pairs, nS = |S|; `cap` sizes the (grid-stride) launch only.
 void launch_narrow(const unsigned long long *keys, const int *ccnt, int cap, const double4 *s,
                    const int *tris, const int *edges, int Nt, int Ne, double dh2, int *flag,
-                   int *type, double *d2, cudaStream_t st);
+                   int *type, double *d2, int *stat, cudaStream_t st);
 void launch_compact_active(const unsigned long long *keys, const int *ccnt, int cap, const int *flag,
                            const int *pos, const int *type, const double *d2, unsigned long long *akeys,
                            int *atype, double *ad2, int *acnt, cudaStream_t st);
@@ -130,10 +132,13 @@ void launch_accd(const unsigned long long *keys, const int *ccnt, int cap, const
                  const int *tris, const int *edges, int Nt, int Ne, const double4 *ds, double s_gap,
                  int max_iters, double *amin, cudaStream_t st);
 int ls_blocks();
+// round h0 == 0 also sums the elastic partials pg[0..ng), pq[0..nq) into scal and takes
+// alpha_max from *amin
 void launch_ls_round(const unsigned long long *keys, const int *ccnt, const double4 *s, const int *tris,
                      const int *edges, int Nt, int Ne, const double4 *ds, double dh, double *b0, double *ls,
-                     int h0, double *part, const double *scal, double kappa, int hmax, double *out,
-                     int *done_ctr, cudaStream_t st);
+                     int h0, double *part, double *scal, double kappa, int hmax, double *out,
+                     int *done_ctr, const double *pg, int ng, const double *pq, int nq, const double *amin,
+                     cudaStream_t st);
 int ls_round_width();
 int ls_round_next(int h0);   // first halving of the round after the one starting at h0
 
