@@ -525,8 +525,7 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
         kt.start(K_ASSEMBLY, st);
         // S
         launch_mark_S(h->ids.p, acnt, cap, h->Wp.p, h->Wc.p, h->v2q.p, h->mark.p, st);
-        scan_exclusive(h->mark.p, h->spos.p, nf, h->iscr.p, st);
-        launch_compact_S(h->mark.p, h->spos.p, nf, h->qS.p, st);
+        scan_compact(h->mark.p, h->spos.p, h->qS.p, nf, h->iscr.p, st);   // positions and S (sorted)
         // V_s, K_s, Sigma_s depend on S (and the constant factor) only: reuse them while S is
         // bit-identical to the S they were computed for
         launch_same_S(h->qS.p, nS_dev, h->qS_prev.p, h->dint.p + D_SPREV, h->dint.p + D_SPREV + 1, h->capS,
@@ -603,8 +602,8 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
     kt.start(K_LS, st);
     {
         // elastic terms: block partials here, summed (fixed order) by the first line-search round
-        const int nb1 = gdx_partials(h->g_el.p, h->dx.p, h->q2v.p, nf, h->part.p, st);
-        const int nb2 = quad_partials(h->tets.p, h->dx.p, h->B.p, h->w.p, T, h->part.p + nb1, st);
+        int nb1 = 0, nb2 = 0;
+        elastic_partials(h->g_el.p, h->dx.p, h->q2v.p, nf, h->tets.p, h->B.p, h->w.p, T, h->part.p, &nb1, &nb2, st);
         const int hmax = h->opt.ls_max_halvings;
         for (int h0 = 0; h0 <= hmax; h0 = ls_round_next(h0))
             launch_ls_round(h->cand.p, ccnt, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->ds.p, h->dh, h->b0.p, ls, h0,

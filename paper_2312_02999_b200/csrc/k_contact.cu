@@ -739,12 +739,6 @@ __global__ void k_mark_S(const int *__restrict__ ids, const int *__restrict__ ac
     }
 }
 
-__global__ void k_compact_S(const int *__restrict__ mark, const int *__restrict__ pos, int nf,
-                            int *__restrict__ qS) {
-    int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q < nf && mark[q]) qS[pos[q]] = q;
-}
-
 // same = (S == S_prev, bit for bit, |S| > 0); then S_prev <- S.  One CTA.
 __global__ void __launch_bounds__(1024) k_same_S(const int *__restrict__ qS, const int *__restrict__ nS_ptr,
                                                  int *__restrict__ qS_prev, int *__restrict__ nS_prev,
@@ -1215,9 +1209,6 @@ void launch_same_S(const int *qS, const int *nS_ptr, int *qS_prev, int *nS_prev,
                    bool enabled, int *flags, int *reused, cudaStream_t st) {
     PDI_LAUNCH(k_same_S, 1, 1024, 0, st)(qS, nS_ptr, qS_prev, nS_prev, same, enabled ? 1 : 0, cap, flags,
                                          reused);
-}
-void launch_compact_S(const int *mark, const int *pos, int nf, int *qS, cudaStream_t st) {
-    PDI_LAUNCH(k_compact_S, (nf + 255) / 256, 256, 0, st)(mark, pos, nf, qS);
 }
 void launch_grad_pullback(const double4 *g_el, const int *WTp, const int *WTr, const double *WTv,
                           const double4 *gs, int nf, double *G, cudaStream_t st) {

@@ -449,6 +449,55 @@ int gdx_partials(const double4 *g, const double4 *dx, const int *q2v, int nf, do
     PDI_LAUNCH(k_gdx_partials, nb, 256, 0, st)(g, dx, q2v, nf, part);
     return nb;
 }
+// both elastic line-search reductions in one launch: blocks [0, nb1) the gradient term,
+// [nb1, nb1 + nb2) the quadratic term; part[block] as the two separate kernels write them
+__global__ void __launch_bounds__(256) k_elastic_partials(const double4 *__restrict__ g,
+                                                          const double4 *__restrict__ dx,
+                                                          const int *__restrict__ q2v, int nf,
+                                                          const int4 *__restrict__ tets,
+                                                          const double *__restrict__ B,
+                                                          const double *__restrict__ w, int T, int nb1,
+                                                          double *__restrict__ part) {
+    __shared__ double sh[8];
+    double v = 0.0;
+    if ((int)blockIdx.x < nb1) {
+        const int q = blockIdx.x * blockDim.x + threadIdx.x;
+        if (q < nf) {
+            const double4 a = g[q], b = dx[q2v[q]];
+            v = a.x * b.x + a.y * b.y + a.z * b.z;
+        }
+    } else {
+        const int t = (blockIdx.x - nb1) * blockDim.x + threadIdx.x;
+        if (t < T) {
+            const int4 tv = tets[t];
+            const double4 x0 = dx[tv.x], x1 = dx[tv.y], x2 = dx[tv.z], x3 = dx[tv.w];
+            const double Ds[3][3] = {{x1.x - x0.x, x2.x - x0.x, x3.x - x0.x},
+                                     {x1.y - x0.y, x2.y - x0.y, x3.y - x0.y},
+                                     {x1.z - x0.z, x2.z - x0.z, x3.z - x0.z}};
+            double Bm[3][3];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) Bm[k / 3][k % 3] = B[(size_t)k * T + t];
+            double acc = 0;
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int b = 0; b < 3; ++b) {
+                    double F = Ds[a][0] * Bm[0][b] + Ds[a][1] * Bm[1][b] + Ds[a][2] * Bm[2][b];
+                    acc += F * F;
+                }
+            v = w[t] * acc;
+        }
+    }
+    v = block_sum<256>(v, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = v;
+}
+void elastic_partials(const double4 *g, const double4 *dx, const int *q2v, int nf, const int4 *tets,
+                      const double *B, const double *w, int T, double *part, int *nb1, int *nb2,
+                      cudaStream_t st) {
+    *nb1 = (nf + 255) / 256;
+    *nb2 = (T + 255) / 256;
+    PDI_LAUNCH(k_elastic_partials, *nb1 + *nb2, 256, 0, st)(g, dx, q2v, nf, tets, B, w, T, *nb1, part);
+}
 void launch_update(double4 *x, const double4 *dx, const int *q2v, int nf, const double *alpha,
                    const int *flags, int *abort, int it, cudaStream_t st) {
     PDI_LAUNCH(k_update, (nf + 255) / 256, 256, 0, st)(x, dx, q2v, nf, alpha, flags, abort, it);

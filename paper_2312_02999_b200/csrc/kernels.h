@@ -45,6 +45,10 @@ int quad_partials(const int4 *tets, const double4 *dx, const double *B, const do
                   double *part, cudaStream_t st);
 int gdx_partials(const double4 *g, const double4 *dx, const int *q2v, int nf, double *part,
                  cudaStream_t st);
+// gTdx and dx^T H dx block partials in one launch: part[0..nb1) and part[nb1..nb1+nb2)
+void elastic_partials(const double4 *g, const double4 *dx, const int *q2v, int nf, const int4 *tets,
+                      const double *B, const double *w, int T, double *part, int *nb1, int *nb2,
+                      cudaStream_t st);
 void launch_update(double4 *x, const double4 *dx, const int *q2v, int nf, const double *alpha,
                    const int *flags, int *abort, int it, cudaStream_t st);
 void launch_scatter_dx(const double *z, const int *q2v, int nf, double4 *dx, double *amin, cudaStream_t st);
@@ -108,7 +112,6 @@ void launch_pair_derivs(const unsigned long long *akeys, const int *atype, const
                         double *dist, int *ids, double *dmax, cudaStream_t st);
 void launch_mark_S(const int *ids, const int *acnt, int cap, const int *Wp, const int *Wc, const int *v2q,
                    int *mark, cudaStream_t st);
-void launch_compact_S(const int *mark, const int *pos, int nf, int *qS, cudaStream_t st);
 void launch_same_S(const int *qS, const int *nS_ptr, int *qS_prev, int *nS_prev, int *same, int cap,
                    bool enabled, int *flags, int *reused, cudaStream_t st);
 void launch_accum_grad_fx(const int *ids, const int *acnt, int cap, const double *grad, const double *dmax,

@@ -126,6 +126,13 @@ __global__ void __launch_bounds__(kScanNT) k_scan_tiles(int *in, int n, const in
     (void)nparts;
 }
 
+__global__ void k_compact_marks(const int *__restrict__ mark, const int *__restrict__ pos, int n,
+                                int *__restrict__ idx) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && mark[i]) idx[pos[i]] = i;
+}
+void scan_exclusive(const int *in, int *out, int n, int *scratch, cudaStream_t st);
+
 // Small scans (capacity <= kScanSingleMax): ONE CTA walks tiles of kScanNT x 16 with a running
 // carry -- one launch instead of two, no partials round trip.
 constexpr int kScanSingleIPT = 16, kScanSingleTile = kScanNT * kScanSingleIPT, kScanSingleMax = 2 * kScanSingleTile;
@@ -160,6 +167,40 @@ __global__ void __launch_bounds__(kScanNT) k_scan_single(const int *__restrict__
         }
         carry += tot;
     }
+}
+
+// exclusive scan of 0/1 marks that also compacts the marked indices: idx[out[i]] = i where
+// in[i] != 0 (single block; n <= kScanSingleMax keeps it one or two tiles)
+__global__ void __launch_bounds__(kScanNT) k_scan_compact(const int *__restrict__ in, int n, int *__restrict__ out,
+                                                          int *__restrict__ idx) {
+    __shared__ int sh[32];
+    int carry = 0;
+    for (int t0 = 0; t0 <= n; t0 += kScanSingleTile) {
+        const int base = t0 + threadIdx.x * kScanSingleIPT;
+        int v[kScanSingleIPT];
+#pragma unroll
+        for (int i = 0; i < kScanSingleIPT; ++i) v[i] = base + i < n ? in[base + i] : 0;
+        int sum = 0;
+#pragma unroll
+        for (int i = 0; i < kScanSingleIPT; ++i) sum += v[i];
+        int tot;
+        int ex = block_exclusive_scan<kScanNT>(sum, sh, &tot) + carry;
+#pragma unroll
+        for (int i = 0; i < kScanSingleIPT; ++i) {
+            if (base + i <= n) out[base + i] = ex;
+            if (v[i]) idx[ex] = base + i;
+            ex += v[i];
+        }
+        carry += tot;
+    }
+}
+void scan_compact(const int *in, int *out, int *idx, int n, int *scratch, cudaStream_t st) {
+    if (n <= kScanSingleMax) {
+        PDI_LAUNCH(k_scan_compact, 1, kScanNT, 0, st)(in, n, out, idx);
+        return;
+    }
+    scan_exclusive(in, out, n, scratch, st);
+    PDI_LAUNCH(k_compact_marks, (n + 255) / 256, 256, 0, st)(in, out, n, idx);
 }
 
 void scan_exclusive(const int *in, int *out, int n, int *scratch, cudaStream_t st) {

@@ -13,6 +13,8 @@ void scan_exclusive(const int *in, int *out, int n, int *scratch, cudaStream_t s
 // same with the length read on the device (*n_dev, at most cap; grid sized for cap)
 void scan_exclusive_dev(const int *in, int *out, const int *n_dev, int cap, int *scratch, cudaStream_t st);
 int scan_scratch_ints(int n);
+// scan_exclusive of 0/1 marks that also writes the marked indices: idx[out[i]] = i, in[i] != 0
+void scan_compact(const int *in, int *out, int *idx, int n, int *scratch, cudaStream_t st);
 // scan_exclusive that also zeroes in[0..n) after reading it (n > 0)
 void scan_exclusive_clear(int *in, int *out, int n, int *scratch, cudaStream_t st);
 // ascending LSD radix sort of the low `bits` bits; tmp: n keys; scratch: radix_scratch_ints(n)
