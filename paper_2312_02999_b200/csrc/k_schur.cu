@@ -523,11 +523,35 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
     // accumulates on DMMA.  Diagonal tiles also accumulate y_S for their columns.  Split partials
     // are reduced in a fixed order (deterministic).
     const bool reuse = *a.same != 0;                 // uniform across the grid
+    // Small systems with Sigma_s reused: CTA 0 assembles and factors the first diagonal tile of
+    // Sigma-hat right away (it needs only B-check and the stored Sigma_s), while the other CTAs
+    // run P0 and P2 -- the first tile factorisation leaves the critical path
+    const int nt0 = (ma + TB - 1) / TB;
+    const bool early0 = reuse && nt0 >= 2 && nt0 < kPWMinTiles && G > 1;
+    const int pb = early0 ? bid - 1 : bid, pG = early0 ? G - 1 : G;   // P0 / P2 workers
+    __shared__ double Dsh[2][8][8][9];   // small-system P3: [0] D_k of the step, [1] look-ahead
+    if (early0 && bid == 0) {
+        for (int e = tid; e < TB * TB; e += NT) {
+            const int r = e >> 6, c = e & 63;
+            double v = 0.0;
+            if (c <= r) {
+                v = a.Bc[(size_t)r * a.ldb + c];
+                if (r % 3 == c % 3) v -= a.K[(size_t)(r / 3) * a.ldk + c / 3];
+            }
+            T0[r * TS + c] = v;
+        }
+        __syncthreads();
+        tile_chol64_d(T0, Dsh[0], TB, m, a.info);
+        __syncthreads();
+        st_tile(T0, a.Sh, a.ldh, TB, TB);
+        st_dblocks(Dsh[0], a.Lstore);
+        __syncthreads();
+    }
     // y_S^el[c] = -sum over the etree path of q_c's supernode of V[r][c] w_el[r] (the elastic
     // part; the contact part -K gc is folded into b below since Sigma_s K = I): one CTA per column,
     // the path rows come from a static per-supernode list (independent loads), fixed-order
     // block reduction: the same bits whether or not K is recomputed
-    for (int c = bid; c < nS; c += G) {
+    for (int c = pb; pb >= 0 && c < nS; c += pG) {
         const int s0 = a.col2sn[a.qS[c]];
         double acc[3] = {0, 0, 0};
         for (int pi = a.path_ptr[s0]; pi < a.path_ptr[s0 + 1]; ++pi) {
@@ -720,15 +744,15 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
         }
     }
     // ------------------------------------------------ P2: augmented Sigma-hat (Sigma_s = -K)
-    for (size_t e = (size_t)bid * NT + tid; e < (size_t)m * m; e += (size_t)G * NT) {
+    for (size_t e = (size_t)pb * NT + tid; pb >= 0 && e < (size_t)m * m; e += (size_t)pG * NT) {
         const int r = (int)(e / m), c = (int)(e % m);
-        if (c > r) continue;
+        if (c > r || (early0 && r < TB)) continue;       // tile 0 rows: factored by CTA 0
         double v = a.Bc[(size_t)r * a.ldb + c];
         if (r % 3 == c % 3) v -= a.K[(size_t)(r / 3) * a.ldk + c / 3];
         a.Sh[(size_t)r * a.ldh + c] = v;
     }
     // b = (Sigma_s (x) I3) y_S with y_S = y_S^el - (K (x) I3) gc, i.e. b = Sigma_s y_S^el - gc
-    for (int row = bid * (NT / 32) + wid; row < m; row += G * (NT / 32)) {
+    for (int row = pb * (NT / 32) + wid; pb >= 0 && row < m; row += pG * (NT / 32)) {
         const int ai = row / 3, i = row % 3;
         double acc = 0.0;
         for (int bb = lane; bb < nS; bb += 32) acc -= a.K[(size_t)ai * a.ldk + bb] * a.yS[3 * bb + i];
@@ -752,17 +776,18 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
         // D_k of the factored tile) itself; CTA 0 takes (k+1, k+1) and then factors it
         // (look-ahead).  L_ik go to a ping-pong scratch (A_ik is still read by other CTAs in the
         // step) and are written into the factor one step later.  D_k is kept in Lstore[k * 512].
-        __shared__ double Dsh[2][8][8][9];   // [0] D_k of the step, [1] the look-ahead tile's
         double *Dst = a.Lstore;
-        if (bid == 0) {
-            ld_tile(T0, a.Sh, a.ldh, min(TB, ma), min(TB, ma));
-            __syncthreads();
-            tile_chol64_d(T0, Dsh[0], min(TB, ma), m, a.info);
-            __syncthreads();
-            st_tile(T0, a.Sh, a.ldh, min(TB, ma), min(TB, ma));
-            st_dblocks(Dsh[0], Dst);
+        if (!early0) {                                   // (else factored during P0 / P2)
+            if (bid == 0) {
+                ld_tile(T0, a.Sh, a.ldh, min(TB, ma), min(TB, ma));
+                __syncthreads();
+                tile_chol64_d(T0, Dsh[0], min(TB, ma), m, a.info);
+                __syncthreads();
+                st_tile(T0, a.Sh, a.ldh, min(TB, ma), min(TB, ma));
+                st_dblocks(Dsh[0], Dst);
+            }
+            GSYNC();
         }
-        GSYNC();
         for (int k = 0; k < nt; ++k) {
             const int kc0 = k * TB, kn = min(TB, ma - kc0);
             double *LPk = a.LP + (size_t)(k & 1) * kLPTiles * TB * TB;      // L_ik of this step
