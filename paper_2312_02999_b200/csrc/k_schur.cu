@@ -1072,19 +1072,27 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
         if (lane == 0) a.t[row] = acc + a.gc[row];
     }
     GSYNC();
-    for (int r = bid * NT + tid; r < a.nf; r += G * NT) {   // Z = w_el + V (gc + t)
-        const int s = a.col2sn[r];
-        double z0 = a.G[(size_t)r * 4 + 0], z1 = a.G[(size_t)r * 4 + 1], z2 = a.G[(size_t)r * 4 + 2];
-        for (int c = a.lo[s]; c < a.hi[s]; ++c) {
+    // Z = w_el + V (gc + t): warp per row, lanes over the row's active columns [lo_s, hi_s)
+    // (contiguous in V), fixed xor-tree reduction
+    for (int r = bid * (NT / 32) + wid; r < a.nf; r += G * (NT / 32)) {
+        const int sn = a.col2sn[r];
+        const int c0 = a.lo[sn], c1 = a.hi[sn];
+        double z0 = 0.0, z1 = 0.0, z2 = 0.0;
+        for (int c = c0 + lane; c < c1; c += 32) {
             const double v = a.V[(size_t)r * a.ldv + c];
             z0 += v * a.t[3 * c + 0];
             z1 += v * a.t[3 * c + 1];
             z2 += v * a.t[3 * c + 2];
         }
-        a.Z[(size_t)r * 4 + 0] = z0;
-        a.Z[(size_t)r * 4 + 1] = z1;
-        a.Z[(size_t)r * 4 + 2] = z2;
-        a.Z[(size_t)r * 4 + 3] = 0.0;
+        z0 = warp_sum(z0);
+        z1 = warp_sum(z1);
+        z2 = warp_sum(z2);
+        if (lane == 0) {
+            a.Z[(size_t)r * 4 + 0] = a.G[(size_t)r * 4 + 0] + z0;
+            a.Z[(size_t)r * 4 + 1] = a.G[(size_t)r * 4 + 1] + z1;
+            a.Z[(size_t)r * 4 + 2] = a.G[(size_t)r * 4 + 2] + z2;
+            a.Z[(size_t)r * 4 + 3] = 0.0;
+        }
     }
 }
 
