@@ -178,6 +178,19 @@ __device__ __forceinline__ bool polar_newton(double X[3][3]) {
 // B (SoA [9][T]), A (SoA [6][T]), w; writes the per-corner elastic forces
 // f_{i,c} = w_i (F_i - P_i) g_{i,c} as fc[T][4][3] (coalesced 96 B per tet) and, when
 // p != nullptr, p_i = vec(R_i A_i) (SoA [9][T]) for the parity hook.
+// L2 policy: the once-per-iteration mesh streams (tets, B, A, w) are read evict-first and the
+// forces are written with an evict-last policy, so the forces the gather reads next are the
+// lines the L2 keeps (C5 1M: local step 63.3 -> 61.8 us, gather 38.5 -> 36.3 us,
+// tools/gather_ab.sh; a persisting-L2 set-aside for the forces measured slower).
+__device__ __forceinline__ unsigned long long l2_policy_evict_last() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void st_f64x2_evict_last(double2 *a, double x, double y, unsigned long long pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(a), "d"(x), "d"(y), "l"(pol)
+                 : "memory");
+}
 template <int MINB>
 __global__ void __launch_bounds__(128, MINB) k_local_step(
     const int4 *__restrict__ tets, const double4 *__restrict__ x, const double *__restrict__ B,
@@ -188,16 +201,16 @@ __global__ void __launch_bounds__(128, MINB) k_local_step(
     // info / capacity / hash flags [4, 8) (the candidate counts [2, 3] carry over, see R8)
     if (clr && t < 8 && (t < 2 || t >= 4)) clr[t] = 0;
     if (t >= T) return;
-    const int4 tv = tets[t];
+    const int4 tv = __ldcs(tets + t);
     const double4 x0 = x[tv.x], x1 = x[tv.y], x2 = x[tv.z], x3 = x[tv.w];
     double Bm[3][3];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) Bm[k / 3][k % 3] = __ldg(B + (size_t)k * T + t);
-    const double a00 = __ldg(A6 + t), a01 = __ldg(A6 + (size_t)T + t), a02 = __ldg(A6 + 2 * (size_t)T + t),
-                 a11 = __ldg(A6 + 3 * (size_t)T + t), a12 = __ldg(A6 + 4 * (size_t)T + t),
-                 a22 = __ldg(A6 + 5 * (size_t)T + t);
+    for (int k = 0; k < 9; ++k) Bm[k / 3][k % 3] = __ldcs(B + (size_t)k * T + t);
+    const double a00 = __ldcs(A6 + t), a01 = __ldcs(A6 + (size_t)T + t), a02 = __ldcs(A6 + 2 * (size_t)T + t),
+                 a11 = __ldcs(A6 + 3 * (size_t)T + t), a12 = __ldcs(A6 + 4 * (size_t)T + t),
+                 a22 = __ldcs(A6 + 5 * (size_t)T + t);
     const double A[3][3] = {{a00, a01, a02}, {a01, a11, a12}, {a02, a12, a22}};
-    const double wt = __ldg(w + t);
+    const double wt = __ldcs(w + t);
     // D_s = [x1-x0, x2-x0, x3-x0] (columns); F = D_s B
     const double Ds[3][3] = {{x1.x - x0.x, x2.x - x0.x, x3.x - x0.x},
                              {x1.y - x0.y, x2.y - x0.y, x3.y - x0.y},
@@ -239,12 +252,13 @@ __global__ void __launch_bounds__(128, MINB) k_local_step(
 #pragma unroll
     for (int a = 0; a < 3; ++a) f[0][a] = -(f[1][a] + f[2][a] + f[3][a]);
     double2 *o = reinterpret_cast<double2 *>(fc + 12 * (size_t)t);
-    o[0] = make_double2(f[0][0], f[0][1]);
-    o[1] = make_double2(f[0][2], f[1][0]);
-    o[2] = make_double2(f[1][1], f[1][2]);
-    o[3] = make_double2(f[2][0], f[2][1]);
-    o[4] = make_double2(f[2][2], f[3][0]);
-    o[5] = make_double2(f[3][1], f[3][2]);
+    const unsigned long long pol = l2_policy_evict_last();
+    st_f64x2_evict_last(o + 0, f[0][0], f[0][1], pol);
+    st_f64x2_evict_last(o + 1, f[0][2], f[1][0], pol);
+    st_f64x2_evict_last(o + 2, f[1][1], f[1][2], pol);
+    st_f64x2_evict_last(o + 3, f[2][0], f[2][1], pol);
+    st_f64x2_evict_last(o + 4, f[2][2], f[3][0], pol);
+    st_f64x2_evict_last(o + 5, f[3][1], f[3][2], pol);
 }
 
 // ------------------------------------------------------------------ a2 gather -------------
