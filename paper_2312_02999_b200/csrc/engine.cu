@@ -212,9 +212,14 @@ struct pd_ipc {
     // second stream: w_el = L^-1 Pi g_el runs concurrently with the contact stages (it depends
     // on the elastic gradient only)
     cudaStream_t st2 = nullptr;
-    int side_ctas = 64;       // persistent CTAs of the stream-2 solves (PDIPC_SIDE_CTAS); the rest
-                              // of the SMs run the contact stages concurrently
+    int side_ctas = 74;       // persistent CTAs of the stream-2 solves (PDIPC_SIDE_CTAS); the rest
+                              // of the SMs run the contact stages concurrently (74: the w_el solve
+                              // and the contact path end together at C2, tools/side_sweep.sh)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // third stream: the contact-gradient pull-back (needs the pair gradients only) runs beside
+    // the S / B-check chain of the assembly
+    cudaStream_t st3 = nullptr;
+    cudaEvent_t ev_fork3 = nullptr, ev_join3 = nullptr, ev_S = nullptr;
     DBuf<double> gcS, Ug2;
     DBuf<int> ts_lo2, ts_hi2, ts_cnt2, ts_ptr2, ts_rem2, ticket2, f_bord, iscr2;
     bool graphs = true;       // replay each iteration as a CUDA graph (PDIPC_NO_GRAPH=1: off)
@@ -461,6 +466,21 @@ static void broad_phase_sort(pd_ipc *h, const double4 *ds, double infl, int *ccn
 // device and every launch is sized by a capacity.  Returns false if a capacity or hash overflow
 // was flagged: x was not updated, the caller redoes the iteration after the buffers were grown
 // (or with the sort broad phase).
+// panel V_s = L^-1 Pi E_S (panel tiles only; no items when S is unchanged).  Reads S, |S| and
+// the same-S flag; writes V, Up and the panel plan.  Stream 3 in the contact path.
+static void enqueue_panel_forward(pd_ipc *h, const int *nS_dev, cudaStream_t sp) {
+    const DevFactor &F = h->F;
+    KTimer &kt = h->kt;
+    kt.start(K_FWD, sp);
+    launch_ts_plan(F, h->qS.p, nS_dev, h->capS, h->dint.p + D_SPREV + 1, (long long)h->Up.n, h->dint.p + D_CAP, 2,
+                   h->ts_lo.p, h->ts_hi.p, h->ts_cnt.p, h->ts_rem.p, h->ts_ptr.p, h->ticket.p, sp);
+    if (h->trace_file) h->trace.ensure(4 * (size_t)F.bw_nblocks * (2 + (h->capS + 31) / 32));
+    launch_forward_solve(F, h->ts_lo.p, h->ts_hi.p, h->ts_ptr.p, h->qS.p, h->ts_rem.p, h->ticket.p, h->G.p,
+                         h->Yw.p, h->V.p, h->ldv, h->Ug.p, h->Up.p, nS_dev, h->capS, 0, h->nsm,
+                         h->trace_file ? h->trace.p : nullptr, sp);
+    kt.stop(K_FWD, sp);
+}
+
 static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
     cudaStream_t st = h->st;
     h->kt.slot = slot;
@@ -522,6 +542,14 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
         launch_pair_derivs(h->akeys.p, h->atype.p, h->ad2.p, acnt, cap, h->s.p, h->tris.p, h->edges.p, Nt,
                            Ne, h->dh, h->kappa, h->grad.p, h->Hp.p, h->dist.p, h->ids.p, dmax, st);
         kt.stop(K_DERIV, st);
+        // fork: stream 3 takes the gradient pull-back (reads ids, grad, dmax, g_el; writes gsq,
+        // G: deterministic fixed-point accumulation on the surface, then W^T), then -- once S is
+        // known -- the contact gradient on S and the panel forward solve, while this stream
+        // assembles B-check
+        CK(cudaEventRecord(h->ev_fork3, st));
+        CK(cudaStreamWaitEvent(h->st3, h->ev_fork3, 0));
+        launch_accum_grad_fx(h->ids.p, acnt, cap, h->grad.p, dmax, h->gsq.p, h->st3);
+        launch_grad_pullback_fx(h->g_el.p, h->WTp.p, h->WTr.p, h->WTv.p, h->gsq.p, dmax, acnt, nf, h->G.p, h->st3);
         kt.start(K_ASSEMBLY, st);
         // S
         launch_mark_S(h->ids.p, acnt, cap, h->Wp.p, h->Wc.p, h->v2q.p, h->mark.p, st);
@@ -530,10 +558,12 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
         // bit-identical to the S they were computed for
         launch_same_S(h->qS.p, nS_dev, h->qS_prev.p, h->dint.p + D_SPREV, h->dint.p + D_SPREV + 1, h->capS,
                       h->opt.no_sigma_reuse == 0, h->dint.p + D_CAP, h->dint.p + D_REUSED, st);
-        // gradient pull-back: deterministic fixed-point accumulation on the surface, then W^T
-        launch_accum_grad_fx(h->ids.p, acnt, cap, h->grad.p, dmax, h->gsq.p, st);
-        launch_grad_pullback_fx(h->g_el.p, h->WTp.p, h->WTr.p, h->WTv.p, h->gsq.p, dmax, acnt, nf, h->G.p, st);
-        launch_gather_gc(h->qS.p, nS_dev, h->capS, h->WTp.p, h->WTr.p, h->WTv.p, h->gsq.p, dmax, acnt, h->gcS.p, st);
+        CK(cudaEventRecord(h->ev_S, st));
+        CK(cudaStreamWaitEvent(h->st3, h->ev_S, 0));
+        launch_gather_gc(h->qS.p, nS_dev, h->capS, h->WTp.p, h->WTr.p, h->WTv.p, h->gsq.p, dmax, acnt, h->gcS.p,
+                         h->st3);
+        enqueue_panel_forward(h, nS_dev, h->st3);
+        CK(cudaEventRecord(h->ev_join3, h->st3));
         // B-check: fixed-point accumulation into the dense 3|S| x 3|S| block, then to double; the
         // low words of the fixed-point sums live in the (not yet used) Sigma-hat buffer
         const int ldb = 3 * h->capS;
@@ -543,25 +573,18 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
                            reinterpret_cast<long long *>(h->Bc.p), Bl, ldb, st);
         launch_fx_to_double(reinterpret_cast<long long *>(h->Bc.p), Bl, ldb, nS_dev, h->capS, dmax, acnt, st);
         kt.stop(K_ASSEMBLY, st);
+        CK(cudaStreamWaitEvent(st, h->ev_join3, 0));     // join stream 3
     } else {
         CK(dev_zero(nS_dev, sizeof(int), st));
         CK(dev_zero(h->dint.p + D_SPREV + 1, sizeof(int), st));
         CK(dev_zero(h->dint.p + D_STAT, 2 * sizeof(int), st));
         launch_grad_pullback(h->g_el.p, h->WTp.p, h->WTr.p, h->WTv.p, nullptr, nf, h->G.p, st);
+        enqueue_panel_forward(h, nS_dev, st);
     }
     record_event(ev[2], st);
     // ---------------- G-Step
-    // pure-PD part on stream 2 (forked after the gather, see above); here the contact part
+    // pure-PD part on stream 2 (forked after the gather, see above); the contact panel above
     const DevFactor &F = h->F;
-    kt.start(K_FWD, st);
-    // panel V_s = L^-1 Pi E_S (panel tiles only; no items when S is unchanged)
-    launch_ts_plan(F, h->qS.p, nS_dev, h->capS, h->dint.p + D_SPREV + 1, (long long)h->Up.n, h->dint.p + D_CAP, 2,
-                   h->ts_lo.p, h->ts_hi.p, h->ts_cnt.p, h->ts_rem.p, h->ts_ptr.p, h->ticket.p, st);
-    if (h->trace_file) h->trace.ensure(4 * (size_t)F.bw_nblocks * (2 + (h->capS + 31) / 32));
-    launch_forward_solve(F, h->ts_lo.p, h->ts_hi.p, h->ts_ptr.p, h->qS.p, h->ts_rem.p, h->ticket.p, h->G.p,
-                         h->Yw.p, h->V.p, h->ldv, h->Ug.p, h->Up.p, nS_dev, h->capS, 0, h->nsm,
-                         h->trace_file ? h->trace.p : nullptr, st);
-    kt.stop(K_FWD, st);
     // join stream 2 (w_el): the Schur step forms Z = w_el + V_s (gc + t)
     CK(cudaStreamWaitEvent(st, h->ev_join, 0));
     kt.start(K_DENSE, st);
@@ -822,6 +845,10 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         CK(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+        CK(cudaStreamCreateWithFlags(&h->st3, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&h->ev_fork3, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&h->ev_join3, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&h->ev_S, cudaEventDisableTiming));
         h->tm.init();
         h->kt.init();
         if (const char *ng = std::getenv("PDIPC_NO_GRAPH")) h->graphs = !(ng[0] == '1');
@@ -1152,6 +1179,10 @@ void pd_ipc_destroy(pd_ipc *h) {
     if (h->st2) cudaStreamDestroy(h->st2);
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     if (h->ev_join) cudaEventDestroy(h->ev_join);
+    if (h->st3) cudaStreamDestroy(h->st3);
+    if (h->ev_fork3) cudaEventDestroy(h->ev_fork3);
+    if (h->ev_join3) cudaEventDestroy(h->ev_join3);
+    if (h->ev_S) cudaEventDestroy(h->ev_S);
     if (h->st) cudaStreamDestroy(h->st);
     auto rel = [](auto &b) { b.release(); };
     rel(h->tets); rel(h->B); rel(h->w); rel(h->inc_ptr); rel(h->inc); rel(h->q2v); rel(h->v2q);
