@@ -436,10 +436,13 @@ void elastic_init(int) {
 void launch_local_step(const int4 *tets, const double4 *x, const double *B, const double *A6,
                        const double *w, int T, double *fc, double *p, int *clr, cudaStream_t st) {
     if (T <= 0) return;
+    // latency-bound small meshes (fewer than ~4 CTAs of 128 per SM): half-size CTAs spread the
+    // tets over twice as many CTAs, balancing the SMs
+    const int nt = T < 4 * 148 * 128 ? 64 : 128;
     if (g_ls_minb == 5)
-        PDI_LAUNCH(k_local_step<5>, (T + 127) / 128, 128, 0, st)(tets, x, B, A6, w, T, fc, p, clr);
+        PDI_LAUNCH(k_local_step<5>, (T + nt - 1) / nt, nt, 0, st)(tets, x, B, A6, w, T, fc, p, clr);
     else
-        PDI_LAUNCH(k_local_step<4>, (T + 127) / 128, 128, 0, st)(tets, x, B, A6, w, T, fc, p, clr);
+        PDI_LAUNCH(k_local_step<4>, (T + nt - 1) / nt, nt, 0, st)(tets, x, B, A6, w, T, fc, p, clr);
 }
 void launch_gather_elastic(const int *inc_ptr, const int *inc, const double *fc, int nf,
                            double4 *g, cudaStream_t st) {
