@@ -36,7 +36,8 @@ extern "C" {
                                      not summing to 1 within 1e-12, degenerate surface tri */
 #define PD_IPC_E_ACTUATION    -3  /* |A - A^T|max > 1e-9 |A|max, det A <= 0, or non-finite  */
 #define PD_IPC_E_NOT_SPD      -4  /* no fixed vertices, or the Cholesky factorisation failed */
-#define PD_IPC_E_INTERSECTING -5  /* a surface distance <= 0 at create / set_positions       */
+#define PD_IPC_E_INTERSECTING -5  /* at create / set_positions: a surface pair at distance <= 0
+                                     or a surface edge crossing a surface triangle            */
 #define PD_IPC_E_NONFINITE    -6  /* a NaN/Inf appeared during step (state = last iterate)   */
 #define PD_IPC_E_CUDA         -7  /* CUDA runtime error or no device                         */
 #define PD_IPC_E_OOM          -8  /* device or host allocation failed                        */
@@ -120,10 +121,14 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
  * the device when opt.A_on_device = 1.  stats: NULL or [n_seq].  Blocks until done. */
 int pd_ipc_step(pd_ipc *h, const double *A_next, int32_t n_iters, pd_ipc_stats *stats);
 
-/* Copy positions of sequence seq (all vertices, fixed ones at rest) into out [n_verts][3]. */
+/* Copy positions x of sequence seq (all vertices, fixed ones at rest) into out [n_verts][3]
+ * ("Output x_{t+1}": the state after the last pd_ipc_step).  out is caller
+ * owned.  PD_IPC_E_ARG on a NULL argument or a bad sequence index, PD_IPC_E_CUDA on a copy
+ * failure. */
 int pd_ipc_positions(const pd_ipc *h, int32_t seq, double *out);
 
-/* Free everything.  NULL is a no-op. */
+/* Free the handle and every device buffer it owns (factor, mesh, states, work buffers).
+ * NULL is a no-op.  (Setup/teardown of the one-time prefactorisation.) */
 void pd_ipc_destroy(pd_ipc *h);
 
 /* Last error text: owned by h, or by a thread-local buffer when h == NULL. */
@@ -131,8 +136,10 @@ const char *pd_ipc_last_error(const pd_ipc *h);
 
 /* ---- parity / test hooks (not on the timed path) ------------------------------------- */
 
-/* Overwrite the state of sequence seq with x [n_verts][3] (fixed vertices must be at rest).
- * Checks that the surface is intersection-free (all active distances > 0). */
+/* Overwrite the state of sequence seq with x [n_verts][3] (fixed vertices must be at rest;
+ * PAPER.md:103-104 "Input x_t").  The state is staged and checked first: every non-incident
+ * surface pair closer than d_hat must have a positive distance and no surface edge may cross a
+ * surface triangle; on PD_IPC_E_INTERSECTING the sequence keeps its state. */
 int pd_ipc_set_positions(pd_ipc *h, int32_t seq, const double *x);
 
 /* p_i = vec_rowmajor(R_i A_i) of the last local step of sequence seq: [n_tets][9]. */
@@ -165,6 +172,13 @@ int pd_ipc_set_debug(pd_ipc *h, int32_t level);
  * supernode width, supernodal etree depth]. */
 int pd_ipc_debug_factor_solve(const pd_ipc_mesh *mesh, const double *rest_pos, const double *b,
                               double *x, int64_t *stats);
+
+/* Host-only check (no GPU used): number of (surface edge, surface triangle) pairs sharing no
+ * vertex whose segment strictly crosses the triangle, with the surface at s = W x
+ * (PAPER.md:143), x [n_verts][3].  This is the crossing half of the intersection-free check
+ * that create and set_positions run (SURVEY.md 8(b) PD_IPC_E_INTERSECTING; 8(c) O0).
+ * Returns the count (>= 0) or a negative PD_IPC_E_* code for an invalid mesh. */
+int64_t pd_ipc_debug_crossings(const pd_ipc_mesh *mesh, const double *rest_pos, const double *x);
 
 /* Device timing of kernel groups (CUDA events on the library stream around each group, every
  * iteration; on = 1 enables all groups, on < 0 only the groups in the bit mask -on (bit k =

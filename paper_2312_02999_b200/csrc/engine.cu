@@ -199,6 +199,7 @@ struct pd_ipc {
     std::vector<std::unique_ptr<Seq>> seqs;
     // work buffers
     DBuf<double> fc, G, Z, A9stage;
+    DBuf<double4> xstage;   // set_positions: candidate state, checked before it is accepted
     DBuf<double4> g_el, s, ds, dx, gs;
     DBuf<double4> blo, bhi;
     DBuf<int> hcnt, hstart, hent, qcnt, qoff, qlist;
@@ -730,8 +731,13 @@ static int run_batch(pd_ipc *h, Seq &q, int k, double ms[6]) {
         ms[5] += tot;
     }
     kt.collect(applied);
-    if (di[D_ABORT]) {                           // why: 1 cand, 2 |S|, 4 Up, 8/16 hash, 32 info
+    if (di[D_ABORT]) {                           // why: 1 cand, 2 |S|, 4 Up, 8/16 hash, 32 info, 64 NaN
         const int why = di[D_ABORT + 2];
+        // V_s, K_s, Sigma_s of the aborted iteration (and of the batch's later, skipped ones) may
+        // not have been computed for the S recorded by k_same_S: invalidate the reuse key
+        CK(dev_zero(h->dint.p + D_SPREV, sizeof(int), st));
+        CK(cudaStreamSynchronize(st));
+        if (why & 64) throw CudaError("non-finite value in step (dx, gradient or energy)", PD_IPC_E_NONFINITE);
         if (why & 2) throw CudaError("contact vertex set exceeds capacity", PD_IPC_E_CAPACITY);
         if (why & 32) throw CudaError("dense Cholesky: matrix not SPD", PD_IPC_E_NOT_SPD);
         if (why & 1) grow_candidates(h, 2 * (size_t)cap);
@@ -795,6 +801,38 @@ static void upload_actuation(pd_ipc *h, const double *A, bool on_device) {
         }
         launch_ingest_actuation(dsrc, h->seqs[sq]->A6.p, T, h->st);
     }
+}
+
+// Intersection-free check of a state (SURVEY.md 8(b) E_INTERSECTING; 8(c) O0 rest-state check):
+// (1) no surface edge strictly crosses a surface triangle (host, uniform grid), (2) every
+// non-incident PT / EE pair closer than d_hat has a positive distance (device: exact sort broad
+// phase + the canonical narrow phase, host-checked).  xd: the state on the device; x: the same
+// state on the host [n][3].  Uses the handle's contact work buffers (not on the timed path).
+static int check_intersection_free(pd_ipc *h, const double4 *xd, const double *x, std::string &why) {
+    if (h->Nt == 0) return 0;
+    const long long nx = surface_edge_triangle_crossings(h->hm, x);
+    if (nx > 0) {
+        why = "intersecting state: " + std::to_string(nx) + " surface edge-triangle crossings";
+        return PD_IPC_E_INTERSECTING;
+    }
+    launch_surface(h->Wp.p, h->Wc.p, h->Wv.p, xd, h->Ns, h->s.p, h->st);
+    const bool fs = h->force_sort;
+    h->force_sort = true;            // exact and host-checked: this is a validation path
+    int *ccnt = h->dint.p + D_CCNT;
+    broad_phase(h, nullptr, 0.5 * h->dh * 1.01, ccnt, h->dint.p + D_HOVF);
+    h->force_sort = fs;
+    launch_narrow(h->cand.p, ccnt, (int)h->cand.n, h->s.p, h->tris.p, h->edges.p, h->Nt, h->Ne, h->dh2,
+                  h->flag.p, h->ctype.p, h->cd2.p, nullptr, h->st);
+    int cc[2];
+    sync_read_ints(h, cc, ccnt, 2);
+    std::vector<double> d2(cc[1]);
+    if (cc[1]) CK(cudaMemcpy(d2.data(), h->cd2.p, sizeof(double) * cc[1], cudaMemcpyDeviceToHost));
+    for (double v : d2)
+        if (!(v > 0)) {
+            why = "intersecting state: a surface pair at distance <= 0";
+            return PD_IPC_E_INTERSECTING;
+        }
+    return 0;
 }
 
 extern "C" {
@@ -1101,6 +1139,14 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         h->part.exact(std::max<size_t>(4096, (size_t)(m.T + 255) / 256 + (nf + 255) / 256 + 64));
         upload_actuation(h.get(), A, false);
         CK(cudaStreamSynchronize(h->st));
+        {   // the rest state must be intersection-free (SURVEY.md 8(b) E_INTERSECTING at create)
+            std::string why;
+            const int rc = check_intersection_free(h.get(), h->seqs[0]->x.p, rest_pos, why);
+            if (rc) {
+                pd_ipc_destroy(h.release());
+                return fail(nullptr, rc, why);
+            }
+        }
     } catch (const CudaError &e) {
         int code = e.code;
         std::string msg = e.what();
@@ -1192,7 +1238,7 @@ void pd_ipc_destroy(pd_ipc *h) {
     rel(h->f_dinv_ptr); rel(h->f_dinv); rel(h->Ug); rel(h->Up); rel(h->Yw); rel(h->bw_P); rel(h->f_bw_items); rel(h->f_ford); rel(h->f_bord); rel(h->gcS); rel(h->Ug2); rel(h->f_path_ptr); rel(h->f_path_sn); rel(h->qS_prev); rel(h->f_rc_src); rel(h->f_bw_pbase); rel(h->bw_cnt); rel(h->f_uoff); rel(h->f_urow_sn);
     rel(h->f_rc_ptr); rel(h->f_rc_idx); rel(h->f_urel); rel(h->f_ch_ptr); rel(h->f_ch);
     for (auto &s : h->seqs) { rel(s->x); rel(s->A6); rel(s->p); }
-    rel(h->fc); rel(h->G); rel(h->Z); rel(h->A9stage); rel(h->g_el); rel(h->s); rel(h->ds); rel(h->dx);
+    rel(h->fc); rel(h->xstage); rel(h->G); rel(h->Z); rel(h->A9stage); rel(h->g_el); rel(h->s); rel(h->ds); rel(h->dx);
     rel(h->gs); rel(h->blo); rel(h->bhi); rel(h->hcnt); rel(h->hstart); rel(h->hent); rel(h->cand);
     rel(h->qcnt); rel(h->qoff); rel(h->qlist); rel(h->gsq);
     rel(h->cand_tmp); rel(h->akeys); rel(h->flag); rel(h->pos); rel(h->ctype); rel(h->atype); rel(h->ids);
@@ -1217,27 +1263,16 @@ int pd_ipc_set_positions(pd_ipc *h, int32_t seq, const double *x) {
                 if (x[3 * v + a] != h->hm.rest[3 * v + a])
                     return fail(h, PD_IPC_E_ARG, "fixed vertex moved");
     try {
+        // the candidate state is staged and checked first; the sequence keeps its state when
+        // the check fails
         std::vector<double4> x4(h->n);
         for (int v = 0; v < h->n; ++v) x4[v] = make_double4(x[3 * v], x[3 * v + 1], x[3 * v + 2], 0.0);
-        CK(cudaMemcpy(h->seqs[seq]->x.p, x4.data(), sizeof(double4) * h->n, cudaMemcpyHostToDevice));
-        if (h->Nt > 0) {
-            // intersection check: every pair within d_hat must have a positive distance
-            launch_surface(h->Wp.p, h->Wc.p, h->Wv.p, h->seqs[seq]->x.p, h->Ns, h->s.p, h->st);
-            const bool fs = h->force_sort;
-            h->force_sort = true;            // exact and host-checked: this is a validation hook
-            int *ccnt = h->dint.p + D_CCNT;
-            broad_phase(h, nullptr, 0.5 * h->dh * 1.01, ccnt, h->dint.p + D_HOVF);
-            h->force_sort = fs;
-            launch_narrow(h->cand.p, ccnt, (int)h->cand.n, h->s.p, h->tris.p, h->edges.p, h->Nt, h->Ne, h->dh2,
-                          h->flag.p, h->ctype.p, h->cd2.p, nullptr, h->st);
-            int cc[2];
-            sync_read_ints(h, cc, ccnt, 2);
-            std::vector<double> d2(cc[1]);
-            if (cc[1])
-                CK(cudaMemcpy(d2.data(), h->cd2.p, sizeof(double) * cc[1], cudaMemcpyDeviceToHost));
-            for (double v : d2)
-                if (!(v > 0)) return fail(h, PD_IPC_E_INTERSECTING, "intersecting state");
-        }
+        h->xstage.ensure(h->n);
+        CK(cudaMemcpy(h->xstage.p, x4.data(), sizeof(double4) * h->n, cudaMemcpyHostToDevice));
+        std::string why;
+        const int rc = check_intersection_free(h, h->xstage.p, x, why);
+        if (rc) return fail(h, rc, why);
+        CK(cudaMemcpy(h->seqs[seq]->x.p, h->xstage.p, sizeof(double4) * h->n, cudaMemcpyDeviceToDevice));
     } catch (const CudaError &e) {
         return fail(h, e.code, e.what());
     }
@@ -1325,6 +1360,17 @@ const char *pd_ipc_kernel_name(int32_t id) {
 }
 
 int64_t pd_ipc_launch_count(void) { return pdipc::launch_count(); }
+
+int64_t pd_ipc_debug_crossings(const pd_ipc_mesh *mesh, const double *rest_pos, const double *x) {
+    if (!mesh || !rest_pos || !x) return fail(nullptr, PD_IPC_E_ARG, "NULL argument");
+    HostMesh m;
+    std::string err;
+    int rc = build_host_mesh(mesh->n_verts, mesh->n_tets, mesh->tets, mesh->n_fixed, mesh->fixed, rest_pos,
+                             mesh->n_surf_verts, mesh->n_surf_tris, mesh->surf_tris, mesh->embed_tet,
+                             mesh->embed_w, m, err);
+    if (rc) return fail(nullptr, rc, err);
+    return surface_edge_triangle_crossings(m, x);
+}
 
 // Host-only debug entry (no GPU needed): runs setup + factorisation and solves L_FF x = b on
 // the host with the supernodal factor; reports factor statistics.  Used by CPU tests of the

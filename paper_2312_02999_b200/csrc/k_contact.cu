@@ -1089,6 +1089,13 @@ __global__ void __launch_bounds__(256) k_ls_round(const unsigned long long *__re
             scal[1] = q;
             ls[0] = am;
             ls[1] = 0.0;
+            if (!isfinite(g) || !isfinite(q) || !isfinite(am)) {   // NaN/Inf in dx or the gradient:
+                ls[1] = 2.0;                                       // no trial, alpha = 0, and the
+                out[0] = 0.0;                                      // update aborts the batch (bit 64)
+                out[1] = 0;
+                out[2] = 0.0;
+                out[3] = 2;
+            }
         }
         __syncthreads();
     }
@@ -1102,7 +1109,13 @@ __global__ void __launch_bounds__(256) k_ls_round(const unsigned long long *__re
             if (hh <= hmax && ls[1] == 0.0) {
                 const double al = ldexp(am, -hh);
                 const double dE = al * scal[0] + 0.5 * al * al * scal[1] + kappa * sum;
-                if (dE < 0.0) {
+                if (!isfinite(dE)) {                 // non-finite barrier sum: abort (see above)
+                    ls[1] = 2.0;
+                    out[0] = 0.0;
+                    out[1] = hh + 1;
+                    out[2] = 0.0;
+                    out[3] = 2;
+                } else if (dE < 0.0) {
                     ls[1] = 1.0;
                     out[0] = al;
                     out[1] = hh + 1;

@@ -391,12 +391,14 @@ __global__ void k_update(double4 *__restrict__ x, const double4 *__restrict__ dx
                          const int *__restrict__ flags, int *__restrict__ abort, int it) {
     int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nf) return;
-    const int bad = flags[0] | flags[1] | flags[2] | flags[3];
+    // alpha[3] == 2: the line search saw a non-finite gradient, dx or energy (k_ls_round)
+    const int nonfinite = alpha[3] == 2.0 ? 64 : 0;
+    const int bad = flags[0] | flags[1] | flags[2] | flags[3] | nonfinite;
     if (bad) {
         if (q == 0 && abort[0] == 0) {
             abort[0] = 1;
             abort[1] = it;
-            abort[2] = flags[1] | (flags[2] ? 8 : 0) | (flags[3] ? 16 : 0) | (flags[0] ? 32 : 0);
+            abort[2] = flags[1] | (flags[2] ? 8 : 0) | (flags[3] ? 16 : 0) | (flags[0] ? 32 : 0) | nonfinite;
         }
         return;
     }

@@ -603,4 +603,88 @@ int factorize(HostMesh &m, HostFactor &f, std::string &err) {
     return PD_IPC_OK;
 }
 
+
+// ------------------------------------------------------------------ intersection check ------
+// Segment pq strictly crosses triangle abc iff p and q lie strictly on opposite sides of the
+// triangle's plane and the line pq passes strictly inside the three edges (signed volumes of
+// the same sign).  Zero volumes (touching, coplanar) are not counted: a touching pair has a
+// zero distance, which the distance check reports.
+static inline double orient3(const double *a, const double *b, const double *c, const double *d) {
+    const double ux = b[0] - a[0], uy = b[1] - a[1], uz = b[2] - a[2];
+    const double vx = c[0] - a[0], vy = c[1] - a[1], vz = c[2] - a[2];
+    const double wx = d[0] - a[0], wy = d[1] - a[1], wz = d[2] - a[2];
+    return ux * (vy * wz - vz * wy) - uy * (vx * wz - vz * wx) + uz * (vx * wy - vy * wx);
+}
+
+long long surface_edge_triangle_crossings(const HostMesh &m, const double *x) {
+    if (m.Nt == 0 || m.Ne == 0) return 0;
+    std::vector<double> s(3 * (size_t)m.Ns, 0.0);
+    for (int j = 0; j < m.Ns; ++j)
+        for (int k = m.W_ptr[j]; k < m.W_ptr[j + 1]; ++k)
+            for (int a = 0; a < 3; ++a) s[3 * (size_t)j + a] += m.W_val[k] * x[3 * (size_t)m.W_col[k] + a];
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (int j = 0; j < m.Ns; ++j)
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = std::min(lo[a], s[3 * (size_t)j + a]);
+            hi[a] = std::max(hi[a], s[3 * (size_t)j + a]);
+        }
+    // cell = max(mean edge, box extent / 256) so the grid stays bounded
+    double cell = std::max(m.mean_edge, 1e-300);
+    for (int a = 0; a < 3; ++a) cell = std::max(cell, (hi[a] - lo[a]) / 256.0);
+    int dim[3];
+    for (int a = 0; a < 3; ++a) dim[a] = std::max(1, (int)std::floor((hi[a] - lo[a]) / cell) + 1);
+    auto cidx = [&](double v, int a) { return std::min(dim[a] - 1, std::max(0, (int)std::floor((v - lo[a]) / cell))); };
+    // bin triangles by their boxes
+    std::vector<std::pair<long long, int>> ent;
+    for (int t = 0; t < m.Nt; ++t) {
+        int c0[3], c1[3];
+        for (int a = 0; a < 3; ++a) {
+            double l = 1e300, h = -1e300;
+            for (int k = 0; k < 3; ++k) {
+                const double v = s[3 * (size_t)m.tris[3 * t + k] + a];
+                l = std::min(l, v);
+                h = std::max(h, v);
+            }
+            c0[a] = cidx(l, a);
+            c1[a] = cidx(h, a);
+        }
+        for (int i = c0[0]; i <= c1[0]; ++i)
+            for (int j = c0[1]; j <= c1[1]; ++j)
+                for (int k = c0[2]; k <= c1[2]; ++k)
+                    ent.push_back({((long long)i * dim[1] + j) * dim[2] + k, t});
+    }
+    std::sort(ent.begin(), ent.end());
+    long long count = 0;
+    std::vector<int> seen;
+    for (int e = 0; e < m.Ne; ++e) {
+        const int p = m.edges[2 * e], q = m.edges[2 * e + 1];
+        const double *P = &s[3 * (size_t)p], *Q = &s[3 * (size_t)q];
+        int c0[3], c1[3];
+        for (int a = 0; a < 3; ++a) {
+            c0[a] = cidx(std::min(P[a], Q[a]), a);
+            c1[a] = cidx(std::max(P[a], Q[a]), a);
+        }
+        seen.clear();
+        for (int i = c0[0]; i <= c1[0]; ++i)
+            for (int j = c0[1]; j <= c1[1]; ++j)
+                for (int k = c0[2]; k <= c1[2]; ++k) {
+                    const long long key = ((long long)i * dim[1] + j) * dim[2] + k;
+                    auto it = std::lower_bound(ent.begin(), ent.end(), std::make_pair(key, -1));
+                    for (; it != ent.end() && it->first == key; ++it) seen.push_back(it->second);
+                }
+        std::sort(seen.begin(), seen.end());
+        seen.erase(std::unique(seen.begin(), seen.end()), seen.end());
+        for (int t : seen) {
+            const int a = m.tris[3 * t], b = m.tris[3 * t + 1], c = m.tris[3 * t + 2];
+            if (a == p || a == q || b == p || b == q || c == p || c == q) continue;
+            const double *A = &s[3 * (size_t)a], *B = &s[3 * (size_t)b], *Cc = &s[3 * (size_t)c];
+            const double op = orient3(A, B, Cc, P), oq = orient3(A, B, Cc, Q);
+            if (!((op > 0 && oq < 0) || (op < 0 && oq > 0))) continue;
+            const double u = orient3(P, Q, A, B), v = orient3(P, Q, B, Cc), w = orient3(P, Q, Cc, A);
+            if ((u > 0 && v > 0 && w > 0) || (u < 0 && v < 0 && w < 0)) ++count;
+        }
+    }
+    return count;
+}
+
 }  // namespace pdipc

@@ -70,4 +70,10 @@ int build_host_mesh(int n, int T, const int32_t *tets, int nfix, const int32_t *
                     std::string &err);
 int factorize(HostMesh &m, HostFactor &f, std::string &err);
 
+// Number of (surface edge, surface triangle) pairs sharing no vertex whose closed segment
+// strictly crosses the triangle at positions x [n][3] (surface s = W x).
+// E_INTERSECTING / 8(c) O0 "no surface edge crosses a surface triangle"; a touching (zero
+// distance) configuration is left to the distance check.  Uniform grid over the triangles.
+long long surface_edge_triangle_crossings(const HostMesh &m, const double *x);
+
 }  // namespace pdipc

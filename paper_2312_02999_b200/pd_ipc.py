@@ -82,6 +82,8 @@ lib.pd_ipc_debug_factor_solve.argtypes = [C.POINTER(pd_ipc_mesh), C.POINTER(C.c_
                                           C.POINTER(C.c_double), C.POINTER(C.c_double),
                                           C.POINTER(C.c_int64)]
 lib.pd_ipc_debug_factor_solve.restype = C.c_int
+lib.pd_ipc_debug_crossings.argtypes = [C.POINTER(pd_ipc_mesh), C.POINTER(C.c_double), C.POINTER(C.c_double)]
+lib.pd_ipc_debug_crossings.restype = C.c_int64
 
 lib.pd_ipc_set_timing.argtypes = [_P, C.c_int32]
 lib.pd_ipc_set_timing.restype = C.c_int
@@ -95,7 +97,7 @@ lib.pd_ipc_launch_count.restype = C.c_int64
 EXPORTED = ["pd_ipc_create", "pd_ipc_step", "pd_ipc_positions", "pd_ipc_destroy",
             "pd_ipc_last_error", "pd_ipc_set_positions", "pd_ipc_set_debug",
             "pd_ipc_get_projections", "pd_ipc_get_contacts", "pd_ipc_get_vector", "pd_ipc_get_pair_terms",
-            "pd_ipc_build_info", "pd_ipc_debug_factor_solve", "pd_ipc_set_timing",
+            "pd_ipc_build_info", "pd_ipc_debug_factor_solve", "pd_ipc_debug_crossings", "pd_ipc_set_timing",
             "pd_ipc_kernel_times", "pd_ipc_kernel_name", "pd_ipc_launch_count"]
 
 
@@ -280,6 +282,17 @@ def debug_factor_solve(scene, b=None):
                                        stats.ctypes.data_as(C.POINTER(C.c_int64)))
     _check(rc)
     return x, stats
+
+
+def debug_crossings(scene, x):
+    """Host-only: surface edge-triangle crossings at positions x (n, 3) (the crossing half of
+    the intersection-free check of create / set_positions)."""
+    m = _MeshArgs(scene)
+    x = _f64(x).reshape(-1, 3)
+    r = int(lib.pd_ipc_debug_crossings(C.byref(m.mesh), _dp(m.rest), _dp(x)))
+    if r < 0:
+        raise PdIpcError(r, last_error())
+    return r
 
 
 class Solver:

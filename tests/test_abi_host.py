@@ -80,3 +80,23 @@ def test_setup_rejects_bad_input(P):
     with pytest.raises(P.PdIpcError) as e:
         P.debug_factor_solve(bad)
     assert e.value.code == P.E_MESH
+
+
+def test_host_crossing_check_matches_brute_force(P):
+    """The crossing half of the create / set_positions intersection check (SURVEY 8(b)
+    E_INTERSECTING) counts exactly the edge-triangle piercings of an independent brute-force
+    Moller-Trumbore test, on the rest state (none) and on interpenetrating C1 states."""
+    from test_oracle_solve import edge_triangle_crossings
+    from oracle import build_mesh
+    sc = scenes.slabs_c1()
+    m = build_mesh(sc)
+    assert P.debug_crossings(sc, sc.rest) == 0
+    rng = np.random.default_rng(3)
+    upper = sc.rest[:, 2] > 2.25 * sc.h
+    for shift in (0.8, 1.0, 1.7):
+        x = sc.rest.copy()
+        x[upper, 2] -= shift * sc.h
+        x[upper] += rng.uniform(-0.05, 0.05, (int(upper.sum()), 3)) * sc.h
+        ref = edge_triangle_crossings(m.W @ x, m.tris, m.edges)
+        assert ref > 0
+        assert P.debug_crossings(sc, x) == ref
