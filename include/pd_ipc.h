@@ -85,7 +85,17 @@ typedef struct {
                                  pair closer than d_hat at x_new is in it (the
                                  active set C is then identical, the narrow phase being exact);
                                  1: static broad phase every iteration                         */
+    int32_t debug_flags;      /* test hooks that force rarely taken paths (0 = none):
+                                 PD_IPC_DBG_LARGE_SCHUR  every dense Schur system takes the
+                                   large-system (panel, all-CTA back substitution) path;
+                                 PD_IPC_DBG_SORT_BROAD   every broad phase takes the sort path;
+                                 PD_IPC_DBG_TINY_HASH    the hash broad phase overflows, so each
+                                   iteration is redone on the sort path                        */
 } pd_ipc_options;
+
+#define PD_IPC_DBG_LARGE_SCHUR 1
+#define PD_IPC_DBG_SORT_BROAD  2
+#define PD_IPC_DBG_TINY_HASH   4
 
 /* Per sequence, describing the LAST iteration of the last pd_ipc_step call. */
 typedef struct {

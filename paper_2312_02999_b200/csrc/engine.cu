@@ -373,7 +373,7 @@ static void broad_phase_sort(pd_ipc *h, const double4 *ds, double infl, int *ccn
 constexpr double kCellCap = 2.0;
 
 static void broad_phase(pd_ipc *h, const double4 *ds, double infl, int *ccnt, int *hovf) {
-    if (h->force_sort) {
+    if (h->force_sort || (h->opt.debug_flags & PD_IPC_DBG_SORT_BROAD)) {
         broad_phase_sort(h, ds, infl, ccnt);
         return;
     }
@@ -381,7 +381,9 @@ static void broad_phase(pd_ipc *h, const double4 *ds, double infl, int *ccnt, in
     const int Ns = h->Ns, Nt = h->Nt, Ne = h->Ne;
     double *ext = h->dscal.p + 14;   // cell = [max box extent, cap]
     const unsigned M = h->hmask + 1;
-    const int nq = Ns + Ne, cap_ent = (int)h->hent.n;
+    // PD_IPC_DBG_TINY_HASH: an entry capacity of 1 makes the hash path overflow, so the iteration
+    // is redone on the sort path (exercises the overflow -> sort fallback)
+    const int nq = Ns + Ne, cap_ent = (h->opt.debug_flags & PD_IPC_DBG_TINY_HASH) ? 1 : (int)h->hent.n;
     // ext = [cell0, cap], overflow flag and both tables' bucket counts cleared in one launch
     launch_broad_prep(ext, h->cell0, kCellCap * h->cell0, hovf, h->hcnt.p, (int)(2 * (M + 1)), st);
     launch_boxes(h->s.p, ds, h->tris.p, h->edges.p, Ns, Nt, Ne, infl, h->blo.p, h->bhi.p, ext, st);
@@ -598,7 +600,8 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
                                      h->ts_lo.p, h->ts_hi.p, nS_dev, h->capS, h->K.p, h->capS, h->Bc.p,
                                      3 * h->capS, h->Sh.p, h->ldh, h->Lstore.p, h->Tt.p, h->U.p, h->yS.p,
                                      h->rhs.p, h->u.p, h->tv.p, h->Z.p, h->dint.p + D_INFO,
-                                     h->dint.p + D_SPREV + 1, h->trace_file ? h->sprof.p : nullptr, st));
+                                     h->dint.p + D_SPREV + 1, h->trace_file ? h->sprof.p : nullptr,
+                                     (h->opt.debug_flags & PD_IPC_DBG_LARGE_SCHUR) ? 1 : 0, st));
     } else {
         CK(dev_copy(h->Z.p, h->Yw.p, sizeof(double) * 4 * nf, st));
     }
@@ -652,7 +655,8 @@ static int run_batch(pd_ipc *h, Seq &q, int k, double ms[6]) {
     const int cap = (int)h->cand.n;
     KTimer &kt = h->kt;
     int *nS_dev = h->spos.p + nf;
-    const bool graph = h->graphs && !h->debug && !h->trace_file && !h->force_sort;
+    const bool graph = h->graphs && !h->debug && !h->trace_file && !h->force_sort &&
+                       !(h->opt.debug_flags & PD_IPC_DBG_SORT_BROAD);
     const unsigned key = (h->buf_epoch << 1) | (kt.on ? 1u : 0u);
     const unsigned key_mask = kt.on ? kt.mask : 0u;
     auto enqueue_batch = [&]() {

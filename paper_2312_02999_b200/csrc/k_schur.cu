@@ -64,6 +64,7 @@ struct SchurArgs {
     int *info;
     const int *same;            // 1: S unchanged, K holds the previous -Sigma_s (reuse it)
     unsigned long long *prof;   // optional phase timestamps (PDIPC_TRACE), [1024]
+    int pw_min;                 // systems of >= pw_min 64-tiles take the large-system path
 };
 
 __device__ __forceinline__ unsigned long long gtimer_s() {
@@ -527,7 +528,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
     // Sigma-hat right away (it needs only B-check and the stored Sigma_s), while the other CTAs
     // run P0 and P2 -- the first tile factorisation leaves the critical path
     const int nt0 = (ma + TB - 1) / TB;
-    const bool early0 = reuse && nt0 >= 2 && nt0 < kPWMinTiles && G > 1;
+    const bool early0 = reuse && nt0 >= 2 && nt0 < a.pw_min && G > 1;
     const int pb = early0 ? bid - 1 : bid, pG = early0 ? G - 1 : G;   // P0 / P2 workers
     __shared__ double Dsh[2][8][8][9];   // small-system P3: [0] D_k of the step, [1] look-ahead
     if (early0 && bid == 0) {
@@ -768,8 +769,8 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
     // columns (k streamed through shared memory, accumulator in registers): the trailing
     // matrix is read and written once per panel instead of once per tile column.
     const int nt = (ma + TB - 1) / TB;
-    const int pw = nt >= kPWMinTiles ? kPW : nt + 1;  // small systems: look-ahead path below
-    if (nt < kPWMinTiles) {
+    const int pw = nt >= a.pw_min ? kPW : nt + 1;  // small systems: look-ahead path below
+    if (nt < a.pw_min) {
         // Small systems (latency-bound): ONE grid barrier per tile column.  Step k: every CTA
         // updates one tile (i, j), k < j <= i, recomputing the panel tiles it needs
         // (L_ik = A_ik L_kk^{-T}, blocked triangular solve with the 8x8 diagonal-block inverses
@@ -868,7 +869,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
             GSYNC();
         }
     }
-    for (int p0 = 0; nt >= kPWMinTiles && p0 < nt; p0 += pw) {
+    for (int p0 = 0; nt >= a.pw_min && p0 < nt; p0 += pw) {
         const int p1 = min(nt, p0 + pw);
         for (int k = p0; k < p1; ++k) {
             const int kc0 = k * TB, kn = min(TB, ma - kc0);
@@ -951,7 +952,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
     }
     // ------------------------------------------------ P4: u = C^{-T} y, y = row m of the factor
     const int ntm = (m + TB - 1) / TB;
-    if (nt < kPWMinTiles) {
+    if (nt < a.pw_min) {
         // Small systems: CTA 0 alone, no grid barrier.  Per 64-row tile k of C from the last:
         // u_k = X_k y_k with X_k = L_kk^{-T} (formed by P3), then y_j -= sum_r C[kc0+r][j] u_r for
         // j < kc0 (rows of C read from L2, every load of a thread in flight at once).  X_k is
@@ -1115,7 +1116,7 @@ int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, 
                  const int *lo, const int *hi, const int *nS, int capS, double *K, int ldk, const double *Bc, int ldb,
                  double *Sh, int ldh, double *Lstore, double *T, double *U, double *yS, double *y, double *u,
                  double *t, double *Z, int *info, const int *same_S, unsigned long long *prof,
-                 cudaStream_t st) {
+                 int large_min_tiles, cudaStream_t st) {
     SchurArgs a;
     a.V = V; a.ldv = ldv; a.G = G; a.gc = gc; a.qS = qS; a.col2sn = F.col2sn; a.sn_c0 = F.sn_c0;
     a.sn_parent = F.sn_parent; a.path_ptr = F.path_ptr; a.path_sn = F.path_sn; a.lo = lo; a.hi = hi; a.nsn = F.nsn; a.nf = F.nf; a.nS_ptr = nS; a.capS = capS;
@@ -1123,6 +1124,7 @@ int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, 
     a.T = T; a.U = U; a.yS = yS; a.y = y; a.u = u; a.t = t; a.Z = Z; a.info = info; a.same = same_S; a.prof = prof;
     a.Kpart = g_kpart;
     a.LP = g_lp;
+    a.pw_min = large_min_tiles > 0 ? std::min(large_min_tiles, kPWMinTiles) : kPWMinTiles;
     void *args[] = {&a};
     note_launch();
     return (int)cudaLaunchCooperativeKernel((const void *)k_schur_coop, dim3(g_schur_grid), dim3(NT),

@@ -76,7 +76,7 @@ int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, 
                  const int *lo, const int *hi, const int *nS, int capS, double *K, int ldk, const double *Bc, int ldb,
                  double *Sh, int ldh, double *Lstore, double *T, double *U, double *yS, double *y, double *u,
                  double *t, double *Z, int *info, const int *same_S, unsigned long long *prof,
-                 cudaStream_t st);
+                 int large_min_tiles, cudaStream_t st);
 void note_launch();
 
 // ---- k_contact.cu

@@ -678,10 +678,18 @@ long long surface_edge_triangle_crossings(const HostMesh &m, const double *x) {
             const int a = m.tris[3 * t], b = m.tris[3 * t + 1], c = m.tris[3 * t + 2];
             if (a == p || a == q || b == p || b == q || c == p || c == q) continue;
             const double *A = &s[3 * (size_t)a], *B = &s[3 * (size_t)b], *Cc = &s[3 * (size_t)c];
+            // signed volumes below tol = 1e-12 L^3 (L the longest of the four edges) are rounding
+            // noise of (near-)coplanar configurations -- e.g. the flat pieces of a subdivided
+            // surface -- and count as zero
+            auto d2 = [](const double *x, const double *y) {
+                return (x[0] - y[0]) * (x[0] - y[0]) + (x[1] - y[1]) * (x[1] - y[1]) + (x[2] - y[2]) * (x[2] - y[2]);
+            };
+            const double L2 = std::max(std::max(d2(P, Q), d2(A, B)), std::max(d2(B, Cc), d2(Cc, A)));
+            const double tol = 1e-12 * L2 * std::sqrt(L2);
             const double op = orient3(A, B, Cc, P), oq = orient3(A, B, Cc, Q);
-            if (!((op > 0 && oq < 0) || (op < 0 && oq > 0))) continue;
+            if (!((op > tol && oq < -tol) || (op < -tol && oq > tol))) continue;
             const double u = orient3(P, Q, A, B), v = orient3(P, Q, B, Cc), w = orient3(P, Q, Cc, A);
-            if ((u > 0 && v > 0 && w > 0) || (u < 0 && v < 0 && w < 0)) ++count;
+            if ((u > tol && v > tol && w > tol) || (u < -tol && v < -tol && w < -tol)) ++count;
         }
     }
     return count;

@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libpd_ipc.so")
 E_ARG, E_MESH, E_ACTUATION, E_NOT_SPD, E_INTERSECTING, E_NONFINITE, E_CUDA, E_OOM, E_CAPACITY = \
     -1, -2, -3, -4, -5, -6, -7, -8, -9
 FLAG_STALL = 1
+DBG_LARGE_SCHUR, DBG_SORT_BROAD, DBG_TINY_HASH = 1, 2, 4
 
 
 class pd_ipc_mesh(C.Structure):
@@ -31,7 +32,7 @@ class pd_ipc_options(C.Structure):
     _fields_ = [("n_seq", C.c_int32), ("device", C.c_int32), ("ls_max_halvings", C.c_int32),
                 ("accd_max_iters", C.c_int32), ("A_on_device", C.c_int32),
                 ("max_pairs", C.c_int32), ("accd_s", C.c_double), ("no_sigma_reuse", C.c_int32),
-                ("no_cand_reuse", C.c_int32)]
+                ("no_cand_reuse", C.c_int32), ("debug_flags", C.c_int32)]
 
 
 class pd_ipc_stats(C.Structure):
@@ -173,14 +174,15 @@ def _check(rc, h=None):
 
 def create(scene, A=None, n_seq=1, device=0, A_on_device=False, max_pairs=0,
            ls_max_halvings=30, accd_max_iters=10_000, accd_s=0.1, d_hat=None, kappa=None,
-           sigma_reuse=True, cand_reuse=True):
+           sigma_reuse=True, cand_reuse=True, debug_flags=0):
     """pd_ipc_create on a scenes.Scene.  A: (n_seq, T, 9) host actuation (default frame 0)."""
     m = _MeshArgs(scene)
     if A is None:
         A = np.stack([scene.actuation(0)] * n_seq)
     A = _f64(A).reshape(n_seq, -1, 9)
     opt = pd_ipc_options(n_seq, device, ls_max_halvings, accd_max_iters, int(A_on_device),
-                         max_pairs, accd_s, 0 if sigma_reuse else 1, 0 if cand_reuse else 1)
+                         max_pairs, accd_s, 0 if sigma_reuse else 1, 0 if cand_reuse else 1,
+                         int(debug_flags))
     h = _P()
     rc = lib.pd_ipc_create(C.byref(m.mesh), _dp(m.rest), _dp(A),
                            float(scene.d_hat if d_hat is None else d_hat),

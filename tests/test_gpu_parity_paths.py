@@ -1,0 +1,266 @@
+"""GPU parity on the paths the round-1 review found untested (VERDICT r1 "Next round" 2).
+
+Element by element against the CPU oracle on the same inputs, through the C ABI:
+  * the large-system dense Schur path (panel Cholesky, all-CTA back substitution): forced on C1
+    and face_small (PD_IPC_DBG_LARGE_SCHUR), and natively on C3 (n_c ~ 1.8k, m ~ 5.4k);
+  * the line search: forced halvings (rounds of 1, 8 and 22 trial alphas) and the STALL flag,
+    on C1 with a stiff barrier and a tight CCD gap;
+  * the local step's SVD route for inverted elements (det F_i A_i <= 0);
+  * the device-pointer actuation path (the bench's A_on_device = 1);
+  * the sort broad phase, forced directly and through a hash-table overflow;
+  * the intersection check of set_positions / create (E_INTERSECTING keeps the old state).
+Tolerances as tests/test_gpu_parity.py.
+"""
+import dataclasses
+
+import numpy as np
+import pytest
+
+import scenes
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2312_02999_b200 import pd_ipc
+    return pd_ipc
+
+
+def _rel(a, b):
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+def _contacts_ref(ref):
+    rpt = np.stack([ref["C"]["pt"][0], ref["C"]["pt"][1]], 1) if ref["n_pt"] else np.zeros((0, 2))
+    ree = np.stack([ref["C"]["ee"][0], ref["C"]["ee"][1]], 1) if ref["n_ee"] else np.zeros((0, 2))
+    return rpt, ree
+
+
+def _lockstep(P, s, sc, o, x, A, n, check_alpha=True, dx_tol=1e-8, on_ref=None):
+    """n lockstep iterations from x: the GPU iterates from the oracle's x every time.  Returns
+    the oracle log and the GPU stats."""
+    log, stats = [], []
+    for k in range(n):
+        ref = o.iterate(x, A)
+        P.set_positions(s.h, x)
+        st = s.step(n_iters=1)[0]
+        pt, ee, S = P.get_contacts(s.h)
+        rpt, ree = _contacts_ref(ref)
+        assert np.array_equal(pt, rpt), f"iteration {k}: PT set differs"
+        assert np.array_equal(ee, ree), f"iteration {k}: EE set differs"
+        assert np.array_equal(S, ref["S"]), f"iteration {k}: S differs"
+        g = P.get_vector(s.h, sc.n_verts, 0)
+        gref = np.zeros((sc.n_verts, 3))
+        gref[o.mesh.free] = ref["ghat"].reshape(-1, 3)
+        assert _rel(g, gref) < 1e-10, (k, _rel(g, gref))
+        dx = P.get_vector(s.h, sc.n_verts, 1)
+        assert _rel(dx, ref["dx"]) < dx_tol, (k, _rel(dx, ref["dx"]))
+        if check_alpha:
+            assert abs(st["alpha_max"] - ref["alpha_m"]) <= 1e-10 * ref["alpha_m"], (k, st["alpha_max"], ref["alpha_m"])
+            assert st["ls_trials"] == ref["ls_trials"], (k, st["ls_trials"], ref["ls_trials"])
+            assert st["flags"] == ref["flags"], (k, st["flags"], ref["flags"])
+            assert abs(st["alpha"] - ref["alpha"]) <= 1e-10 * ref["alpha_m"], (k, st["alpha"], ref["alpha"])
+            assert np.abs(s.positions() - ref["x"]).max() < 1e-9 * sc.bbox_diag()
+        if on_ref is not None:
+            on_ref(k, ref, st)
+        log.append(ref)
+        stats.append(st)
+        x = ref["x"]
+    return log, stats
+
+
+# ------------------------------------------------------------------ large Schur path -------
+@pytest.mark.parametrize("scene", ["c1", "face_small"])
+def test_large_schur_path_forced(P, scene):
+    from oracle import OracleSolver
+    if scene == "c1":
+        sc = scenes.slabs_c1()
+        A, n = sc.actuation(0), 12
+    else:
+        sc = scenes.face_small(n_frames=2)
+        A = np.tile(np.eye(3).reshape(1, 9), (sc.n_tets, 1))
+        A[:, 4] += 0.5 * sc.meta["lip_mask"]
+        n = 8
+    o = OracleSolver(sc)
+    s = P.Solver(sc, A=A[None], debug_flags=P.DBG_LARGE_SCHUR)
+    P.set_debug(s.h, 1)
+    log, _ = _lockstep(P, s, sc, o, sc.rest.copy(), A, n, check_alpha=False)
+    assert max(len(r["S"]) for r in log) > 50          # m = 3 n_c spans several 64-tiles
+    s.close()
+
+
+def test_large_schur_path_native_c3(P):
+    """C3 (BASELINE configs[2], 292k tets): the GPU runs 17 frames into contact; one lockstep
+    iteration from that state with n_c ~ 1.8k (m = 3 n_c ~ 5.4k > 1280: the large path)."""
+    from oracle import OracleSolver
+    sc = scenes.face_c3()
+    s = P.Solver(sc)
+    for f in range(17):
+        s.step(A_next=sc.actuation(f)[None], n_iters=20)
+    x = s.positions()
+    A = sc.actuation(17)
+    o = OracleSolver(sc)
+    P.set_debug(s.h, 1)
+    s.step(A_next=A[None], n_iters=0)
+    log, _ = _lockstep(P, s, sc, o, x, A, 1)
+    assert 3 * len(log[0]["S"]) >= 1280, len(log[0]["S"])
+    s.close()
+
+
+# ------------------------------------------------------------------ line search ----------
+def _stiff_c1(kappa_factor):
+    sc = scenes.slabs_c1()
+    return dataclasses.replace(sc, kappa=sc.kappa * kappa_factor)
+
+
+@pytest.fixture(scope="module")
+def stiff_runs():
+    """Oracle logs of C1 with a stiff barrier and a tight CCD gap: the line search halves
+    (rounds of 8 and 22 trials are reached) and, with a cap of 5 halvings, stalls."""
+    from oracle import OracleSolver
+    out = {}
+    for hmax in (30, 5):
+        sc = _stiff_c1(1e8)
+        o = OracleSolver(sc, s_gap=1e-5, ls_max_halvings=hmax)
+        out[hmax] = (sc, o)
+    return out
+
+
+@pytest.mark.parametrize("hmax", [30, 5])
+def test_line_search_halvings_and_stall(P, stiff_runs, hmax):
+    sc, o = stiff_runs[hmax]
+    A = sc.actuation(0)
+    s = P.Solver(sc, A=A[None], accd_s=1e-5, ls_max_halvings=hmax)
+    P.set_debug(s.h, 1)
+    log, stats = _lockstep(P, s, sc, o, sc.rest.copy(), A, 8, dx_tol=1e-7)
+    trials = [r["ls_trials"] for r in log]
+    if hmax == 30:
+        assert max(trials) >= 10, trials           # the round of 22 trial alphas was needed
+        assert any(2 <= t <= 9 for t in trials), trials
+    else:
+        assert any(r["flags"] == 1 for r in log), trials
+        assert all(st["alpha"] == 0.0 for st, r in zip(stats, log) if r["flags"] == 1)
+    s.close()
+
+
+# ------------------------------------------------------------------ inverted elements ------
+def test_local_step_inverted_elements(P):
+    """det(F_i A_i) <= 0 takes the SVD route with the reflection fix."""
+    from oracle import build_mesh
+    from oracle.local import local_step
+    sc = scenes.box_c5("10k")
+    m = build_mesh(sc)
+    s = P.Solver(sc)
+    P.set_debug(s.h, 1)
+    rng = np.random.default_rng(12)
+    x = sc.rest.copy()
+    free = np.setdiff1d(np.arange(sc.n_verts), sc.fixed)
+    x[free] += 0.05 * sc.h * rng.standard_normal((free.size, 3))
+    inner = free[(np.abs(sc.rest[free] - sc.rest.mean(0)) < 0.3 * np.ptp(sc.rest, 0)).all(1)]
+    for v in rng.choice(inner, 40, replace=False):          # fold vertices through their stars
+        x[v] += 1.5 * sc.h * rng.standard_normal(3)
+    A = sc.actuation(0)
+    F = m.deformation_gradients(x)
+    inverted = np.linalg.det(F @ A.reshape(-1, 3, 3)) <= 0
+    assert inverted.sum() > 20
+    P.set_positions(s.h, x)
+    s.step(n_iters=1)
+    p_gpu = P.get_projections(s.h, sc.n_tets)
+    p_ref = local_step(m, x, A)
+    rel = np.abs(p_gpu - p_ref).max(axis=1) / np.abs(p_ref).max(axis=1)
+    assert rel[inverted].max() < 1e-10, rel[inverted].max()
+    assert rel.max() < 1e-10
+    R = p_gpu[inverted].reshape(-1, 3, 3) @ np.linalg.inv(A.reshape(-1, 3, 3)[inverted])
+    assert np.abs(np.linalg.det(R) - 1).max() < 1e-10
+    s.close()
+
+
+# ------------------------------------------------------------------ device-pointer A -------
+def test_device_pointer_actuation(P):
+    """A_on_device = 1 (the bench's mode): bit-identical to the host-copy path, and the
+    free-running trajectory matches the oracle within 1e-5 x bbox."""
+    import torch
+    from oracle import OracleSolver
+    sc = scenes.slabs_c1()
+    A0 = sc.actuation(0)
+    A1 = A0.copy()
+    A1[:, 8] = 1.3
+    host = P.Solver(sc, A=A0[None])
+    dev = P.Solver(sc, A=A0[None], A_on_device=True)
+    Ad = torch.from_numpy(np.stack([A1])).cuda()
+    host.step(A_next=A1[None], n_iters=10)
+    dev.step(A_device_ptr=Ad.data_ptr(), n_iters=10)
+    torch.cuda.synchronize()
+    assert np.array_equal(host.positions(), dev.positions())
+    o = OracleSolver(sc)
+    xr = o.run_frame(sc.rest.copy(), A1, 10)
+    assert np.abs(dev.positions() - xr).max() <= 1e-5 * sc.bbox_diag()
+    host.close()
+    dev.close()
+
+
+# ------------------------------------------------------------------ sort broad phase -------
+@pytest.mark.parametrize("flags", ["sort", "tiny_hash"])
+def test_sort_broad_phase(P, flags):
+    """The sort broad phase (forced, or reached through a hash overflow) gives the same active
+    sets as the oracle's all-pairs enumeration and bit-identical iterates to the hash path."""
+    from oracle import OracleSolver
+    sc = scenes.face_small(n_frames=2)
+    A = np.tile(np.eye(3).reshape(1, 9), (sc.n_tets, 1))
+    A[:, 4] += 0.5 * sc.meta["lip_mask"]
+    f = P.DBG_SORT_BROAD if flags == "sort" else P.DBG_TINY_HASH
+    xs = []
+    for dbg in (0, f):
+        s = P.Solver(sc, A=A[None], debug_flags=dbg)
+        st = s.step(n_iters=30)[0]
+        assert st["n_active"] > 0
+        xs.append(s.positions())
+        s.close()
+    assert np.array_equal(xs[0], xs[1])
+    o = OracleSolver(sc)
+    s = P.Solver(sc, A=A[None], debug_flags=f)
+    P.set_debug(s.h, 1)
+    _lockstep(P, s, sc, o, xs[0], A, 2, check_alpha=False)
+    s.close()
+
+
+# ------------------------------------------------------------------ face_small, full lists -
+def test_face_small_full_contact_lists(P):
+    from oracle import OracleSolver
+    sc = scenes.face_small(n_frames=2)
+    A = np.tile(np.eye(3).reshape(1, 9), (sc.n_tets, 1))
+    A[:, 4] += 0.5 * sc.meta["lip_mask"]
+    o = OracleSolver(sc)
+    s = P.Solver(sc, A=A[None])
+    P.set_debug(s.h, 1)
+    log, _ = _lockstep(P, s, sc, o, sc.rest.copy(), A, 8, check_alpha=False)
+    assert any(r["n_pt"] > 0 for r in log) and any(r["n_ee"] > 0 for r in log)
+    s.close()
+
+
+# ------------------------------------------------------------------ intersection check -----
+def test_intersecting_states_are_rejected(P):
+    sc = scenes.slabs_c1()
+    s = P.Solver(sc)
+    s.step(n_iters=3)
+    x_before = s.positions()
+    x = sc.rest.copy()
+    upper = sc.rest[:, 2] > 2.25 * sc.h
+    x[upper, 2] -= 1.0 * sc.h                       # upper slab pushed into the lower one
+    fixed = np.zeros(sc.n_verts, bool)
+    fixed[sc.fixed] = True
+    x[fixed] = sc.rest[fixed]
+    with pytest.raises(P.PdIpcError) as e:
+        P.set_positions(s.h, x)
+    assert e.value.code == P.E_INTERSECTING
+    assert np.array_equal(s.positions(), x_before)   # the state was kept
+    s.step(n_iters=1)                                # and the handle still steps
+    s.close()
+    bad = dataclasses.replace(sc, rest=x)
+    with pytest.raises(P.PdIpcError) as e:
+        P.Solver(bad)
+    assert e.value.code in (P.E_INTERSECTING, P.E_MESH)
