@@ -4,16 +4,25 @@
 //   Misc   : a1 local step (fused polar + per-corner elastic forces), a2 gather -> g_el
 //   IPC    : a3 s = W x, a4 hash broad phase, a5 narrow phase + per-pair derivatives + PSD,
 //            a6 S, g-hat = g_el + W^T grad_s B, B-check
-//   G-Step : a7/a8 one forward solve (3 gradient columns + the contact panel), a9 dense
+//   G-Step : a7/a8 forward solves (w_el = L^-1 Pi g_el and the contact panel), a9 dense
 //            K_s = V^T V, Sigma_s = K_s^{-1}, Sigma-hat Cholesky, u, t = B u, one backward
 //            solve of w + V t  -> dx = -(H + B)^{-1} g-hat exactly
 //   CCD    : ds = W dx, swept broad phase, ACCD -> alpha_m
 //   LS     : surrogate energy differences at alpha_m 2^-h, first decrease -> alpha; x += alpha dx
-// The host reads back four counts per iteration (candidates, active pairs, |S|, swept
-// candidates) to size the launches; everything else stays on the device.
+//
+// Sequences: a handle holds B independent actuation sequences sharing the mesh
+// and the factor.  They advance in LOCKSTEP: one lockstep iteration runs a1/a2 over (tet,
+// sequence) in one launch each (mesh data read once per tet), ONE forward solve with the 3B
+// gradient right-hand sides of all sequences (the factor read once per supernode row block),
+// then every sequence's contact stages and its dense Schur step (each with its own n_c), then
+// backward solves of 8 sequences' right-hand sides per launch, then every sequence's CCD, line
+// search and update.  Per-sequence state: x, A, forces, gradients, candidate lists, counters and
+// a reuse slot (V_s, K_s / Sigma_s and the S they belong to).  All counts live on the device;
+// a batch of iterations is one captured CUDA graph with one host round trip.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -79,31 +88,42 @@ static int bits_for(unsigned long long v) {   // bits to represent values < v (v
 }
 
 constexpr int kMaxBatch = 32;   // iterations enqueued (or captured) before one host round trip
+constexpr int kSlotCap = 256;   // (iteration, sequence) slots of one batch: k = kSlotCap / B iterations
+
+// Device int slots of a sequence (32 ints each).  Every count an iteration needs stays on the
+// device; the host reads them once per batch.
+enum : int {
+    D_ACNT = 0,      // [0] n_pt, [1] n_all active pairs
+    D_CCNT = 2,      // [2] npt, [3] ntot candidates of the current broad phase
+    D_INFO = 4,      // Cholesky info
+    D_CAP = 5,       // capacity bits: 1 candidate buffer, 2 |S| > capS, 4 panel update rows
+    D_HOVF = 6,      // [6] static, [7] swept hash overflow (outlier box / table) -> sort path
+    D_SAME = 9,      // V_s, K_s, Sigma_s of the sequence's reuse slot belong to this S
+    D_STAT = 10,     // [10] npt, [11] ntot of the static phase (stats)
+    D_ABORT = 12,    // [12] sticky: an iteration of the batch failed, [13] its index, [14] why
+    D_REUSED = 15,   // iterations of the batch that reused V_s, K_s, Sigma_s
+    D_SORT = 16,     // [16..18] scratch counters of the sort path
+    D_LSCTR = 19,    // line-search round: blocks finished (the last one decides; reset by it)
+    D_NS = 20,       // |S| of the last iteration
+    D_STRIDE = 32,
+};
+constexpr int S_STRIDE = 16;   // doubles per sequence in dscal: [0] unused, [1] amin, [2..4] ls,
+                               // [5..8] ls_out, [9..10] scal, [11] max |pair term|, [12] min
+                               // active distance, [14..15] broad-phase cell
 
 struct Seq {
-    // captured CUDA graph of one iteration (asynchronous part), rebuilt when buffers move
-    cudaGraphExec_t exec = nullptr;
-    unsigned graph_key = ~0u;
-    long long graph_launches = 0;
-    bool kt_used[kMaxBatch][16] = {};
-    int graph_batch = 0;
-    unsigned graph_mask = 0;
-    DBuf<double4> x;
-    DBuf<double> A6;
-    DBuf<double> p;
+    // captured CUDA graph of a batch run of this sequence alone (debug / redo path)
     pd_ipc_stats stats;
+    DBuf<unsigned long long> cand;   // candidate keys: static list, then the previous swept list
+    bool force_sort = false;         // the next broad phases take the sort path (hash overflow)
+    int slot = 0;                    // reuse slot (V_s, K_s, key)
+    int nS = 0;
     // debug copies of the last iteration
     std::vector<int32_t> pt, ee, S;
     std::vector<double> ghat, gel, dx, proj, pgrad, phess;
 };
 
-struct StageTimer {             // Table-1 stage boundaries, one event set per iteration slot
-    cudaEvent_t ev[kMaxBatch][6];
-    void init() { for (auto &a : ev) for (auto &e : a) CK(cudaEventCreate(&e)); }
-    void destroy() { for (auto &a : ev) for (auto &e : a) cudaEventDestroy(e); }
-};
-
-// Per-kernel-group device timing (CUDA events on the library stream), for the roofline report.
+// Per-kernel-group device timing (CUDA events on the launching stream), for the roofline report.
 enum KId { K_LOCAL = 0, K_GATHER, K_BROAD, K_NARROW, K_DERIV, K_ASSEMBLY, K_FWD, K_DENSE, K_BWD,
            K_CCD, K_LS, K_D_SYRK, K_D_INV, K_D_POTRF, K_D_SOLVE, K_NUM };
 static const char *kKernelNames[K_NUM] = {"local_step", "gather", "broad_phase", "narrow_phase",
@@ -118,51 +138,87 @@ static void record_event(cudaEvent_t e, cudaStream_t st) {
     CK(g_capturing ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal) : cudaEventRecord(e, st));
 }
 
+// Table-1 stage boundaries per (iteration, sequence) slot of a batch:
+//   [0] batch-iteration start, [1] after a1/a2 (batched), [2] sequence's contact start,
+//   [3] after its IPC stages, [4] after its Schur step, [5] backward solves start (batched),
+//   [6] after them, [7] sequence's CCD start, [8] after CCD, [9] after line search + update
+constexpr int kStageEv = 10;
+struct StageTimer {
+    std::vector<cudaEvent_t> ev;     // [kSlotCap][kStageEv]
+    std::vector<char> used;
+    void init() {
+        ev.resize((size_t)kSlotCap * kStageEv);
+        used.assign(ev.size(), 0);
+        for (auto &e : ev) CK(cudaEventCreate(&e));
+    }
+    void destroy() { for (auto &e : ev) cudaEventDestroy(e); }
+    cudaEvent_t &at(int slot, int k) { return ev[(size_t)slot * kStageEv + k]; }
+    void rec(int slot, int k, cudaStream_t st) {
+        record_event(at(slot, k), st);
+        used[(size_t)slot * kStageEv + k] = 1;
+    }
+    float el(int slot, int a, int b) {
+        float f = 0.f;
+        CK(cudaEventElapsedTime(&f, at(slot, a), at(slot, b)));
+        return f;
+    }
+};
+
 struct KTimer {
     bool on = false;
     unsigned mask = ~0u;                // timed groups (bit k = group k)
-    int slot = 0;                       // iteration slot of the batch being enqueued
-    cudaEvent_t ev[kMaxBatch][K_NUM][2];
-    bool used[kMaxBatch][K_NUM] = {};
+    int slot = 0;                       // (iteration, sequence) slot being enqueued
+    std::vector<cudaEvent_t> ev;        // [kSlotCap][K_NUM][2]
+    std::vector<char> used;             // [kSlotCap][K_NUM]
     double ms[K_NUM] = {};
     long long cnt[K_NUM] = {};
     void init() {
-        for (auto &a : ev) for (auto &b : a) { CK(cudaEventCreate(&b[0])); CK(cudaEventCreate(&b[1])); }
+        ev.resize((size_t)kSlotCap * K_NUM * 2);
+        used.assign((size_t)kSlotCap * K_NUM, 0);
+        for (auto &e : ev) CK(cudaEventCreate(&e));
     }
-    void destroy() {
-        for (auto &a : ev) for (auto &b : a) { cudaEventDestroy(b[0]); cudaEventDestroy(b[1]); }
-    }
-    void start(int k, cudaStream_t st) { if (on && (mask >> k & 1)) record_event(ev[slot][k][0], st); }
+    void destroy() { for (auto &e : ev) cudaEventDestroy(e); }
+    cudaEvent_t &e(int s, int k, int w) { return ev[((size_t)s * K_NUM + k) * 2 + w]; }
+    void start(int k, cudaStream_t st) { if (on && (mask >> k & 1)) record_event(e(slot, k, 0), st); }
     void stop(int k, cudaStream_t st) {
-        if (on && (mask >> k & 1)) { record_event(ev[slot][k][1], st); used[slot][k] = true; }
+        if (on && (mask >> k & 1)) { record_event(e(slot, k, 1), st); used[(size_t)slot * K_NUM + k] = 1; }
     }
     bool timeline = false;          // PDIPC_TIMELINE=1: print start/stop offsets of every group
-    void collect(int n_slots) {     // after a stream synchronize: the first n_slots iterations
+    void collect(const std::vector<char> &applied) {   // after a stream synchronize
         if (timeline)
-            for (int i = 0; i < n_slots; ++i) {
-                if (!used[i][K_LOCAL]) continue;
+            for (int i = 0; i < kSlotCap; ++i) {
+                if (!used[(size_t)i * K_NUM + K_LOCAL] || !applied[i]) continue;
                 std::fprintf(stderr, "timeline it %d:", i);
                 for (int k = 0; k < K_NUM; ++k)
-                    if (used[i][k]) {
+                    if (used[(size_t)i * K_NUM + k]) {
                         float a, b;
-                        CK(cudaEventElapsedTime(&a, ev[i][K_LOCAL][0], ev[i][k][0]));
-                        CK(cudaEventElapsedTime(&b, ev[i][K_LOCAL][0], ev[i][k][1]));
+                        CK(cudaEventElapsedTime(&a, e(i, K_LOCAL, 0), e(i, k, 0)));
+                        CK(cudaEventElapsedTime(&b, e(i, K_LOCAL, 0), e(i, k, 1)));
                         std::fprintf(stderr, " %s=[%.1f,%.1f]", kKernelNames[k], 1e3 * a, 1e3 * b);
                     }
                 std::fprintf(stderr, "\n");
             }
-        for (int i = 0; i < kMaxBatch; ++i)
+        for (int i = 0; i < kSlotCap; ++i)
             for (int k = 0; k < K_NUM; ++k)
-                if (used[i][k]) {
-                    if (i < n_slots) {
+                if (used[(size_t)i * K_NUM + k]) {
+                    if (applied[i]) {
                         float f;
-                        CK(cudaEventElapsedTime(&f, ev[i][k][0], ev[i][k][1]));
+                        CK(cudaEventElapsedTime(&f, e(i, k, 0), e(i, k, 1)));
                         ms[k] += f;
                         cnt[k] += 1;
                     }
-                    used[i][k] = false;
+                    used[(size_t)i * K_NUM + k] = 0;
                 }
     }
+};
+
+// captured graph of one batch shape (first sequence, sequence count, iterations)
+struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    unsigned key = ~0u, mask = 0;
+    int b0 = -1, nb = 0, k = 0;
+    long long launches = 0;
+    std::vector<char> kt_used, st_used;
 };
 
 }  // namespace pdipc
@@ -177,13 +233,13 @@ struct pd_ipc {
     double dh = 0, kappa = 0, dh2 = 0;
     HostMesh hm;
     HostFactor hf;
-    int n = 0, T = 0, nf = 0, Ns = 0, Nt = 0, Ne = 0;
+    int n = 0, T = 0, nf = 0, Ns = 0, Nt = 0, Ne = 0, B = 1;
     int capS = 0, ldv = 0, ldh = 0;
     int debug = 0;
     double cell0 = 0;
     // mesh (shared by sequences)
     DBuf<int4> tets;
-    DBuf<double> B, w;
+    DBuf<double> B_, w;
     DBuf<int> inc_ptr, inc, q2v, v2q;
     DBuf<int> Wp, Wc, WTp, WTr, tris, edges;
     DBuf<double> Wv, WTv;
@@ -191,29 +247,35 @@ struct pd_ipc {
     DevFactor F;
     DBuf<int> f_c0, f_rowptr, f_rows, f_parent, f_seg_ptr, f_seg_d, f_seg_klo, f_seg_khi, f_fd, f_col2sn;
     DBuf<long long> f_valptr, f_dinv_ptr;
-    DBuf<double> f_L, f_dinv, Ug, Up, Yw, bw_P;
+    DBuf<double> f_L, f_dinv, Ug, Up, bw_P;
     DBuf<int2> f_bw_items, f_rc_src;
-    DBuf<int> f_bw_pbase, bw_cnt, f_ford, qS_prev, f_path_ptr, f_path_sn;
+    DBuf<int> f_bw_pbase, bw_cnt, f_ford, f_path_ptr, f_path_sn;
     DBuf<int> f_uoff, f_urow_sn, f_rc_ptr, f_rc_idx, f_urel, f_ch_ptr, f_ch;
-    // sequences
+    // sequences: host state + batched device arrays [B][...]
     std::vector<std::unique_ptr<Seq>> seqs;
-    // work buffers
-    DBuf<double> fc, G, Z, A9stage;
-    DBuf<double4> xstage;   // set_positions: candidate state, checked before it is accepted
-    DBuf<double4> g_el, s, ds, dx, gs;
+    DBuf<double4> x_all, gel_all, dx_all, s_all, ds_all, xstage;
+    DBuf<double> A6_all, p_all, fc_all, G_all, Yw_all, Z_all, dscal_all;
+    DBuf<int> dint_all;
+    // reuse slots: V_s [nf][ldv], K_s / -Sigma_s [capS][capS], the S they belong to
+    int nslots = 1;
+    std::vector<DBuf<double>> V_slot, K_slot;
+    std::vector<DBuf<int>> qS_slot;
+    DBuf<int> nS_slot;                  // [nslots] |S| of the key (0 = invalid)
+    // shared contact / Schur work buffers (a sequence's contact + Schur stages run in order)
+    DBuf<double> A9stage;
     DBuf<double4> blo, bhi;
     DBuf<int> hcnt, hstart, hent, qcnt, qoff, qlist;
     unsigned hmask = 0;
-    DBuf<unsigned long long> cand, cand_tmp, akeys;
+    size_t pair_cap = 0;                // capacity of the per-pair buffers (>= every cand.n)
+    DBuf<unsigned long long> cand_tmp, akeys;
     DBuf<int> flag, pos, ctype, atype, ids, iscr;
     DBuf<double> cd2, ad2, grad, Hp, dist;
     DBuf<int> mark, spos, qS;
     DBuf<double> lspart;    // line-search partial sums [ls_round_width()][ls_blocks()]
-    bool force_sort = false;  // next broad phases take the sort path (after a hash overflow)
-    // second stream: w_el = L^-1 Pi g_el runs concurrently with the contact stages (it depends
-    // on the elastic gradient only)
+    // second stream: w_el = L^-1 Pi g_el of all sequences runs concurrently with the contact
+    // stages (it depends on the elastic gradients only)
     cudaStream_t st2 = nullptr;
-    int side_ctas = 74;       // persistent CTAs of the stream-2 solves (PDIPC_SIDE_CTAS); the rest
+    int side_ctas = 74;       // persistent CTAs of the stream-2 solve (PDIPC_SIDE_CTAS); the rest
                               // of the SMs run the contact stages concurrently (74: the w_el solve
                               // and the contact path end together at C2, tools/side_sweep.sh)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -223,20 +285,30 @@ struct pd_ipc {
     cudaEvent_t ev_fork3 = nullptr, ev_join3 = nullptr, ev_S = nullptr;
     DBuf<double> gcS, Ug2;
     DBuf<int> ts_lo2, ts_hi2, ts_cnt2, ts_ptr2, ts_rem2, ticket2, f_bord, iscr2;
-    bool graphs = true;       // replay each iteration as a CUDA graph (PDIPC_NO_GRAPH=1: off)
+    bool graphs = true;       // replay each batch as a CUDA graph (PDIPC_NO_GRAPH=1: off)
     unsigned buf_epoch = 0;   // bumped whenever a buffer the iteration uses is reallocated
-    int nS_host = 0;
+    std::vector<GraphEntry> gcache;
     DBuf<int> ts_lo, ts_hi, ts_cnt, ts_ptr, ts_rem, ts_done, ticket;
-    DBuf<double> V, K, Bc, Sh, U, Tt, yS, rhs, u, tv, part, b0, Lstore;
-    DBuf<double> dscal;     // [0]=ext cell, [1]=amin, [2..4]=ls, [5..8]=ls_out, [9..10]=scal,
-                            // [11]=max |pair term| (fixed-point scale), [12]=min active distance
+    DBuf<double> Bc, Sh, U, Tt, yS, rhs, u, tv, part, b0, Lstore;
     DBuf<long long> gsq;    // surface gradient, fixed point [Ns][3]
-    DBuf<int> dint;         // [0..3] counts, [4] info
     StageTimer tm;
     KTimer kt;
     // debugging aid: PDIPC_TRACE=<file> appends per-item forward-solve timestamps
     FILE *trace_file = nullptr, *schur_file = nullptr;
     DBuf<unsigned long long> trace, sprof;
+
+    // per-sequence views of the batched arrays
+    double4 *x(int b) { return x_all.p + (size_t)b * n; }
+    double *A6(int b) { return A6_all.p + (size_t)b * 6 * T; }
+    double4 *gel(int b) { return gel_all.p + (size_t)b * nf; }
+    double *G(int b) { return G_all.p + (size_t)b * 4 * nf; }
+    double *Yw(int b) { return Yw_all.p + (size_t)b * 4 * nf; }
+    double *Z(int b) { return Z_all.p + (size_t)b * 4 * nf; }
+    double4 *dx(int b) { return dx_all.p + (size_t)b * n; }
+    double4 *s(int b) { return s_all.p + (size_t)b * std::max(1, Ns); }
+    double4 *ds(int b) { return ds_all.p + (size_t)b * std::max(1, Ns); }
+    int *dint(int b) { return dint_all.p + (size_t)b * D_STRIDE; }
+    double *dscal(int b) { return dscal_all.p + (size_t)b * S_STRIDE; }
 };
 
 static thread_local std::string g_last_error;
@@ -256,37 +328,49 @@ static void sync_read_ints(pd_ipc *h, int *dst, const int *src, int k) {
 // device scalar <- v, stream-ordered, no host staging (a pageable H2D copy would block)
 static void set_d(pd_ipc *h, double *dptr, double v) { launch_set_double(dptr, v, h->st); }
 
-static void ensure_pair_buffers(pd_ipc *h, size_t ncand) {
-    h->flag.ensure(ncand + 1);
-    h->pos.ensure(ncand + 1);
-    h->ctype.ensure(ncand + 1);
-    h->cd2.ensure(ncand + 1);
-    h->iscr.ensure(std::max(radix_scratch_ints((int)ncand + 1), scan_scratch_ints((int)ncand + 1)) + 1024);
-}
-
-// grow every candidate-capacity buffer to at least n keys (rare; synchronising)
-static void grow_candidates(pd_ipc *h, size_t n) {
-    if (n <= h->cand.n) return;
+// shared per-pair / per-candidate scratch sized for n candidate keys (the largest list of any
+// sequence)
+static void ensure_pair_buffers(pd_ipc *h, size_t n) {
+    if (n <= h->pair_cap) return;
     ++h->buf_epoch;
-    h->cand.exact(n);
+    h->pair_cap = n;
     h->cand_tmp.exact(n);
-    ensure_pair_buffers(h, n);
-    h->akeys.exact(n + 1);
-    h->atype.exact(n + 1);
-    h->ad2.exact(n + 1);
-    h->grad.exact(12 * n + 12);
-    h->Hp.exact(78 * n + 78);
-    h->dist.exact(n + 1);
-    h->ids.exact(4 * n + 4);
-    h->b0.exact(n + 1);
+    h->flag.exact(n + 1);
+    h->pos.exact(n + 1);
+    h->ctype.exact(n + 1);
+    h->cd2.exact(n + 1);
+    h->iscr.ensure(std::max(radix_scratch_ints((int)n + 1), scan_scratch_ints((int)n + 1)) + 1024);
+    if (h->Nt > 0) {
+        h->akeys.exact(n + 1);
+        h->atype.exact(n + 1);
+        h->ad2.exact(n + 1);
+        h->grad.exact(12 * n + 12);
+        h->Hp.exact(78 * n + 78);
+        h->dist.exact(n + 1);
+        h->ids.exact(4 * n + 4);
+        h->b0.exact(n + 1);
+    }
 }
 
-// parity / debugging copies of the last iteration (PD_IPC set_debug)
-static void debug_capture(pd_ipc *h, Seq &q, int n_pt, int n_ee, int nS) {
+// grow sequence b's candidate list (and the shared pair buffers) to at least n keys (rare;
+// synchronising)
+static void grow_candidates(pd_ipc *h, int b, size_t n) {
+    Seq &q = *h->seqs[b];
+    if (n > q.cand.n) {
+        ++h->buf_epoch;
+        q.cand.exact(n);
+    }
+    ensure_pair_buffers(h, n);
+}
+
+// parity / debugging copies of the last iteration of sequence b (run alone: the shared contact
+// buffers hold its data)
+static void debug_capture(pd_ipc *h, int b, int n_pt, int n_ee, int nS) {
+    Seq &q = *h->seqs[b];
     const int nf = h->nf;
     std::vector<double> G4(4 * (size_t)nf), g4(4 * (size_t)nf);
-    CK(cudaMemcpy(G4.data(), h->G.p, sizeof(double) * 4 * nf, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(g4.data(), h->g_el.p, sizeof(double) * 4 * nf, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(G4.data(), h->G(b), sizeof(double) * 4 * nf, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(g4.data(), h->gel(b), sizeof(double) * 4 * nf, cudaMemcpyDeviceToHost));
     q.ghat.assign(3 * (size_t)h->n, 0.0);
     q.gel.assign(3 * (size_t)h->n, 0.0);
     for (int k = 0; k < nf; ++k)
@@ -317,7 +401,7 @@ static void debug_capture(pd_ipc *h, Seq &q, int n_pt, int n_ee, int nS) {
     for (int v : qs) q.S.push_back(h->hm.q2v[v]);
     std::sort(q.S.begin(), q.S.end());
     std::vector<double4> d4(h->n);
-    CK(cudaMemcpy(d4.data(), h->dx.p, sizeof(double4) * h->n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(d4.data(), h->dx(b), sizeof(double4) * h->n, cudaMemcpyDeviceToHost));
     q.dx.resize(3 * (size_t)h->n);
     for (int v = 0; v < h->n; ++v) {
         q.dx[3 * v] = d4[v].x;
@@ -345,48 +429,33 @@ static void dump_traces(pd_ipc *h, int nS) {
     }
 }
 
-// Device int slots (h->dint, 32 ints).  Every count the iteration needs stays on the device; the
-// host reads them once, at the end of the iteration.
-enum : int {
-    D_ACNT = 0,      // [0] n_pt, [1] n_all active pairs
-    D_CCNT = 2,      // [2] npt, [3] ntot candidates of the current broad phase
-    D_INFO = 4,      // Cholesky info
-    D_CAP = 5,       // capacity bits: 1 candidate buffer, 2 |S| > capS, 4 panel update rows
-    D_HOVF = 6,      // [6] static, [7] swept hash overflow (outlier box / table) -> sort path
-    D_SPREV = 8,     // [8] |S| of the S that V_s, K_s, Sigma_s belong to, [9] same-S flag
-    D_STAT = 10,     // [10] npt, [11] ntot of the static phase (stats)
-    D_ABORT = 12,    // [12] sticky: an iteration of the batch failed, [13] its index, [14] why
-    D_REUSED = 15,   // iterations of the batch that reused V_s, K_s, Sigma_s
-    D_SORT = 16,     // [16..18] scratch counters of the sort path
-    D_LSCTR = 19,    // line-search round: blocks finished (the last one decides; reset by it)
-};
+static void broad_phase_sort(pd_ipc *h, int b, const double4 *ds, double infl, int *ccnt);
 
-static void broad_phase_sort(pd_ipc *h, const double4 *ds, double infl, int *ccnt);
-
-// Broad phase: static (ds == nullptr, boxes inflated by infl) or swept.  Produces sorted unique
-// PT keys in cand[0..npt) and EE keys in cand[npt..ntot) with ccnt = [npt, ntot] on the device,
-// no host round trip.  Sort-free: every query sorts its own (short) partner list, so the lists
-// come out globally sorted.  A table overflow raises *hovf; the iteration is then redone with
-// the sort path.
+// Broad phase of sequence b: static (ds == nullptr, boxes inflated by infl) or swept.  Produces
+// sorted unique PT keys in cand[0..npt) and EE keys in cand[npt..ntot) with ccnt = [npt, ntot] on
+// the device, no host round trip.  Sort-free: every query sorts its own (short) partner list, so
+// the lists come out globally sorted.  A table overflow raises *hovf; the iteration is then
+// redone with the sort path.
 // Hash cell = min(max box extent, kCellCap * cell0): one long swept box must not coarsen the grid
 // for every query; boxes wider than the cap span several cells (bounded, see k_hash_insert).
 constexpr double kCellCap = 2.0;
 
-static void broad_phase(pd_ipc *h, const double4 *ds, double infl, int *ccnt, int *hovf) {
-    if (h->force_sort || (h->opt.debug_flags & PD_IPC_DBG_SORT_BROAD)) {
-        broad_phase_sort(h, ds, infl, ccnt);
+static void broad_phase(pd_ipc *h, int b, const double4 *ds, double infl, int *ccnt, int *hovf) {
+    Seq &q = *h->seqs[b];
+    if (q.force_sort || (h->opt.debug_flags & PD_IPC_DBG_SORT_BROAD)) {
+        broad_phase_sort(h, b, ds, infl, ccnt);
         return;
     }
     cudaStream_t st = h->st;
     const int Ns = h->Ns, Nt = h->Nt, Ne = h->Ne;
-    double *ext = h->dscal.p + 14;   // cell = [max box extent, cap]
+    double *ext = h->dscal(b) + 14;   // cell = [max box extent, cap]
     const unsigned M = h->hmask + 1;
     // PD_IPC_DBG_TINY_HASH: an entry capacity of 1 makes the hash path overflow, so the iteration
     // is redone on the sort path (exercises the overflow -> sort fallback)
     const int nq = Ns + Ne, cap_ent = (h->opt.debug_flags & PD_IPC_DBG_TINY_HASH) ? 1 : (int)h->hent.n;
     // ext = [cell0, cap], overflow flag and both tables' bucket counts cleared in one launch
     launch_broad_prep(ext, h->cell0, kCellCap * h->cell0, hovf, h->hcnt.p, (int)(2 * (M + 1)), st);
-    launch_boxes(h->s.p, ds, h->tris.p, h->edges.p, Ns, Nt, Ne, infl, h->blo.p, h->bhi.p, ext, st);
+    launch_boxes(h->s(b), ds, h->tris.p, h->edges.p, Ns, Nt, Ne, infl, h->blo.p, h->bhi.p, ext, st);
     // both tables (tris, edges) in one pass each: count, scan (which clears the counts for the
     // fill pass's cursors), fill
     launch_hash_insert(h->blo.p, h->bhi.p, Ns, Nt, Ne, ext, h->hmask, h->hcnt.p, nullptr, nullptr, 0, hovf, st);
@@ -397,22 +466,23 @@ static void broad_phase(pd_ipc *h, const double4 *ds, double infl, int *ccnt, in
     launch_hash_query_warp(h->blo.p, h->bhi.p, Ns, Nt, Ne, ext, h->hmask, h->hstart.p, h->hent.p, h->tris.p,
                            h->edges.p, h->qcnt.p, h->qlist.p, hovf, st);
     scan_exclusive(h->qcnt.p, h->qoff.p, nq, h->iscr.p, st);
-    launch_hash_emit(Ns, Nt, Ne, h->qcnt.p, h->qoff.p, h->qlist.p, h->cand.p, (int)h->cand.n, ccnt,
-                     h->dint.p + D_CAP, st);
+    launch_hash_emit(Ns, Nt, Ne, h->qcnt.p, h->qoff.p, h->qlist.p, q.cand.p, (int)q.cand.n, ccnt,
+                     h->dint(b) + D_CAP, st);
 }
 
 // Fallback after a hash overflow: uncapped cells (every box covers at most 8 of them), global
 // radix sort + unique.  Host-synchronous (rare path).
-static void broad_phase_sort(pd_ipc *h, const double4 *ds, double infl, int *ccnt) {
+static void broad_phase_sort(pd_ipc *h, int b, const double4 *ds, double infl, int *ccnt) {
+    Seq &q = *h->seqs[b];
     cudaStream_t st = h->st;
     const int Ns = h->Ns, Nt = h->Nt, Ne = h->Ne;
-    double *ext = h->dscal.p + 14;
+    double *ext = h->dscal(b) + 14;
     set_d(h, ext, h->cell0);
     set_d(h, ext + 1, 1e300);
-    launch_boxes(h->s.p, ds, h->tris.p, h->edges.p, Ns, Nt, Ne, infl, h->blo.p, h->bhi.p, ext, st);
+    launch_boxes(h->s(b), ds, h->tris.p, h->edges.p, Ns, Nt, Ne, infl, h->blo.p, h->bhi.p, ext, st);
     const unsigned M = h->hmask + 1;
-    int *cnt_pt = h->dint.p + D_SORT, *cnt_ee = h->dint.p + D_SORT + 1;
-    int *ovf = h->dint.p + D_SORT + 2;   // cannot trip: uncapped cells bound entries by 8 per box
+    int *cnt_pt = h->dint(b) + D_SORT, *cnt_ee = h->dint(b) + D_SORT + 1;
+    int *ovf = h->dint(b) + D_SORT + 2;   // cannot trip: uncapped cells bound entries by 8 per box
     CK(dev_zero(ovf, sizeof(int), st));
     CK(dev_zero(h->hcnt.p, sizeof(int) * 2 * (M + 1), st));
     launch_hash_insert(h->blo.p, h->bhi.p, Ns, Nt, Ne, ext, h->hmask, h->hcnt.p, nullptr, nullptr, 0, ovf, st);
@@ -422,14 +492,14 @@ static void broad_phase_sort(pd_ipc *h, const double4 *ds, double infl, int *ccn
                        (int)h->hent.n, ovf, st);
     for (int pass = 0; pass < 2; ++pass) {
         int counts[2];
-        const int cap = (int)(h->cand.n / 2);
+        const int cap = (int)(q.cand.n / 2);
         for (int kind = 0; kind < 2; ++kind) {   // 0 = PT (B = tris), 1 = EE (B = edges)
             const int b0 = kind == 0 ? Ns : Ns + Nt;
             const int a0 = kind == 0 ? 0 : Ns + Nt, na = kind == 0 ? Ns : Ne;
             const int *hs = h->hstart.p + (size_t)kind * (M + 1), *he = h->hent.p;
             int *cnt = kind == 0 ? cnt_pt : cnt_ee;
             CK(dev_zero(cnt, sizeof(int), st));
-            unsigned long long *out = h->cand.p + (size_t)kind * cap;
+            unsigned long long *out = q.cand.p + (size_t)kind * cap;
             launch_hash_query(h->blo.p, h->bhi.p, a0, na, b0, kind == 0 ? Nt : Ne, ext, h->hmask, hs,
                               he, kind == 0, h->tris.p, h->edges.p, out, cnt, cap, st);
         }
@@ -438,7 +508,7 @@ static void broad_phase_sort(pd_ipc *h, const double4 *ds, double infl, int *ccn
             // sort + unique each list, then pack PT | EE contiguously in cand_tmp -> cand
             int res[2];
             for (int kind = 0; kind < 2; ++kind) {
-                unsigned long long *keys = h->cand.p + (size_t)kind * cap;
+                unsigned long long *keys = q.cand.p + (size_t)kind * cap;
                 int nk = counts[kind];
                 unsigned long long range = kind == 0 ? (unsigned long long)Ns * Nt : (unsigned long long)Ne * Ne;
                 // sort scratch = this kind's half of cand_tmp (the PT result lives in the other)
@@ -451,98 +521,108 @@ static void broad_phase_sort(pd_ipc *h, const double4 *ds, double infl, int *ccn
                 CK(dev_copy(cnt_pt + kind, h->pos.p + nk, sizeof(int), st));
             }
             sync_read_ints(h, res, cnt_pt, 2);
-            CK(cudaMemcpyAsync(h->cand.p, h->cand_tmp.p, sizeof(unsigned long long) * res[0],
+            CK(cudaMemcpyAsync(q.cand.p, h->cand_tmp.p, sizeof(unsigned long long) * res[0],
                                cudaMemcpyDeviceToDevice, st));
-            CK(cudaMemcpyAsync(h->cand.p + res[0], h->cand_tmp.p + cap, sizeof(unsigned long long) * res[1],
+            CK(cudaMemcpyAsync(q.cand.p + res[0], h->cand_tmp.p + cap, sizeof(unsigned long long) * res[1],
                                cudaMemcpyDeviceToDevice, st));
             const int cc[2] = {res[0], res[0] + res[1]};
             CK(cudaMemcpyAsync(ccnt, cc, sizeof(cc), cudaMemcpyHostToDevice, st));
             CK(cudaStreamSynchronize(st));   // cc is a host stack array
             return;
         }
-        grow_candidates(h, 2 * (size_t)std::max(counts[0], counts[1]) + 1024);
+        grow_candidates(h, b, 2 * (size_t)std::max(counts[0], counts[1]) + 1024);
     }
     throw CudaError("broad phase capacity", PD_IPC_E_CAPACITY);
 }
 
-// One PD+IPC iteration of sequence q.  No host round trip until the end: counts live on the
-// device and every launch is sized by a capacity.  Returns false if a capacity or hash overflow
-// was flagged: x was not updated, the caller redoes the iteration after the buffers were grown
-// (or with the sort broad phase).
-// panel V_s = L^-1 Pi E_S (panel tiles only; no items when S is unchanged).  Reads S, |S| and
-// the same-S flag; writes V, Up and the panel plan.  Stream 3 in the contact path.
-static void enqueue_panel_forward(pd_ipc *h, const int *nS_dev, cudaStream_t sp) {
+// panel V_s = L^-1 Pi E_S of sequence b into its reuse slot (panel tiles only; no items when S is
+// unchanged).  Reads S, |S| and the same-S flag; writes V, Up and the panel plan.  Stream 3.
+static void enqueue_panel_forward(pd_ipc *h, int b, const int *nS_dev, cudaStream_t sp) {
     const DevFactor &F = h->F;
     KTimer &kt = h->kt;
+    int *di = h->dint(b);
     kt.start(K_FWD, sp);
-    launch_ts_plan(F, h->qS.p, nS_dev, h->capS, h->dint.p + D_SPREV + 1, (long long)h->Up.n, h->dint.p + D_CAP, 2,
+    launch_ts_plan(F, h->qS.p, nS_dev, h->capS, di + D_SAME, (long long)h->Up.n, di + D_CAP, 2, 0,
                    h->ts_lo.p, h->ts_hi.p, h->ts_cnt.p, h->ts_rem.p, h->ts_ptr.p, h->ticket.p, sp);
     if (h->trace_file) h->trace.ensure(4 * (size_t)F.bw_nblocks * (2 + (h->capS + 31) / 32));
-    launch_forward_solve(F, h->ts_lo.p, h->ts_hi.p, h->ts_ptr.p, h->qS.p, h->ts_rem.p, h->ticket.p, h->G.p,
-                         h->Yw.p, h->V.p, h->ldv, h->Ug.p, h->Up.p, nS_dev, h->capS, 0, h->nsm,
-                         h->trace_file ? h->trace.p : nullptr, sp);
+    launch_forward_solve(F, h->ts_lo.p, h->ts_hi.p, h->ts_ptr.p, h->qS.p, h->ts_rem.p, h->ticket.p, nullptr,
+                         nullptr, h->V_slot[h->seqs[b]->slot].p, h->ldv, nullptr, h->Up.p, nS_dev, h->capS, 0,
+                         0, 0, 0, h->nsm, h->trace_file ? h->trace.p : nullptr, sp);
     kt.stop(K_FWD, sp);
 }
 
-static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
+// ---- one lockstep iteration of sequences [b0, b0 + nb), iteration index it of the batch -----
+// (a) a1 + a2 over (tet, sequence); the w_el solve of all nb sequences forks onto stream 2
+static void enqueue_elastic(pd_ipc *h, int b0, int nb, int it) {
     cudaStream_t st = h->st;
-    h->kt.slot = slot;
-    const int T = h->T, nf = h->nf, Ns = h->Ns, Nt = h->Nt, Ne = h->Ne;
-    const int cap = (int)h->cand.n;
-    auto &ev = h->tm.ev[slot];
-    int *acnt = h->dint.p + D_ACNT, *ccnt = h->dint.p + D_CCNT;
-    static_assert(D_ACNT == 0 && D_CCNT == 2 && D_INFO == 4 && D_HOVF + 2 == 8, "cleared by the local step");
-    record_event(ev[0], st);
-    // ---------------- Misc: a1 local step + a2 gather
     KTimer &kt = h->kt;
+    const int slot = it * nb;
+    h->kt.slot = slot;
+    h->tm.rec(slot, 0, st);
     kt.start(K_LOCAL, st);
-    launch_local_step(h->tets.p, q.x.p, h->B.p, q.A6.p, h->w.p, T, h->fc.p,
-                      h->debug ? q.p.p : nullptr, h->dint.p, st);   // also clears acnt, info, flags
+    launch_local_step(h->tets.p, h->x(b0), h->B_.p, h->A6(b0), h->w.p, h->T, h->fc_all.p,
+                      h->debug ? h->p_all.p + (size_t)b0 * 9 * h->T : nullptr, h->dint(b0), nb, h->n, D_STRIDE,
+                      st);   // also clears each sequence's active-pair counts and flags
     kt.stop(K_LOCAL, st);
     kt.start(K_GATHER, st);
-    launch_gather_elastic(h->inc_ptr.p, h->inc.p, h->fc.p, nf, h->g_el.p, st);
+    launch_gather_elastic(h->inc_ptr.p, h->inc.p, h->fc_all.p, h->nf, h->gel(b0), nb, 12 * (long long)h->T, st);
     kt.stop(K_GATHER, st);
-    // fork: w_el = L^-1 Pi g_el depends on the elastic gradient only -> stream 2, concurrent with
-    // the contact stages (the contact part of w is V_s gc, folded into the Schur step)
-    {
-        cudaStream_t s2 = h->st2;
-        const DevFactor &F2 = h->F;
-        CK(cudaEventRecord(h->ev_fork, st));
-        CK(cudaStreamWaitEvent(s2, h->ev_fork, 0));
-        kt.start(K_D_SYRK, s2);
-        // ticket2: [0] item dispenser (cleared by the plan), [1] fault (cleared per batch),
-        // [2] |S| = 0 (never written), [3] flags (unused in gradient-only mode)
-        launch_ts_plan(F2, nullptr, h->ticket2.p + 2, 0, h->ticket2.p + 2, 0, h->ticket2.p + 3, 1, h->ts_lo2.p,
-                       h->ts_hi2.p, h->ts_cnt2.p, h->ts_rem2.p, h->ts_ptr2.p, h->ticket2.p, s2);
-        launch_forward_solve(F2, h->ts_lo2.p, h->ts_hi2.p, h->ts_ptr2.p, nullptr, h->ts_rem2.p, h->ticket2.p,
-                             reinterpret_cast<const double *>(h->g_el.p), h->Yw.p, nullptr, h->ldv, h->Ug2.p,
-                             nullptr, h->ticket2.p + 2, 0, 1, h->Nt > 0 ? h->side_ctas : h->nsm, nullptr, s2);
-        kt.stop(K_D_SYRK, s2);
-        CK(cudaEventRecord(h->ev_join, s2));
-    }
-    record_event(ev[1], st);
-    // ---------------- IPC
+    h->tm.rec(slot, 1, st);
+    // fork: w_el = L^-1 Pi g_el of every sequence (3 nb right-hand sides, ONE solve) on stream 2,
+    // concurrent with the contact stages (the contact part of w is V_s gc, folded into the Schur
+    // step)
+    cudaStream_t s2 = h->st2;
+    const DevFactor &F2 = h->F;
+    CK(cudaEventRecord(h->ev_fork, st));
+    CK(cudaStreamWaitEvent(s2, h->ev_fork, 0));
+    kt.start(K_D_SYRK, s2);
+    // ticket2: [0] item dispenser (cleared by the plan), [1] fault (cleared per batch),
+    // [2] |S| = 0 (never written), [3] flags (unused in gradient-only mode)
+    launch_ts_plan(F2, nullptr, h->ticket2.p + 2, 0, h->ticket2.p + 2, 0, h->ticket2.p + 3, 1, nb, h->ts_lo2.p,
+                   h->ts_hi2.p, h->ts_cnt2.p, h->ts_rem2.p, h->ts_ptr2.p, h->ticket2.p, s2);
+    launch_forward_solve(F2, h->ts_lo2.p, h->ts_hi2.p, h->ts_ptr2.p, nullptr, h->ts_rem2.p, h->ticket2.p,
+                         reinterpret_cast<const double *>(h->gel(b0)), h->Yw(b0), nullptr, h->ldv, h->Ug2.p,
+                         nullptr, h->ticket2.p + 2, 0, 1, nb, 4 * (long long)h->nf,
+                         4 * (long long)std::max(1, F2.nU), h->Nt > 0 ? h->side_ctas : h->nsm, nullptr, s2);
+    kt.stop(K_D_SYRK, s2);
+    CK(cudaEventRecord(h->ev_join, s2));
+}
+
+// (b) sequence b: a3-a6 contact stages, a8 panel (stream 3) and the a9 dense Schur step -> Z_b
+static void enqueue_contact_schur(pd_ipc *h, int b, int b0, int nb, int it) {
+    cudaStream_t st = h->st;
+    Seq &q = *h->seqs[b];
+    KTimer &kt = h->kt;
+    const int slot = it * nb + (b - b0);
+    kt.slot = slot;
+    h->tm.rec(slot, 2, st);
+    const int nf = h->nf, Ns = h->Ns, Nt = h->Nt, Ne = h->Ne;
+    const int cap = (int)q.cand.n;
+    int *di = h->dint(b);
+    double *ds_ = h->dscal(b);
+    int *acnt = di + D_ACNT, *ccnt = di + D_CCNT;
     int *nS_dev = h->spos.p + nf;     // exclusive scan total of the S marks
-    double *dmax = h->dscal.p + 11;
+    double *dmax = ds_ + 11;
+    const int slotr = q.slot;
     if (Nt > 0) {
         kt.start(K_BROAD, st);
-        launch_surface(h->Wp.p, h->Wc.p, h->Wv.p, q.x.p, Ns, h->s.p, st);
+        launch_surface(h->Wp.p, h->Wc.p, h->Wv.p, h->x(b), Ns, h->s(b), st);
         // after the first iteration of a batch the previous iteration's swept candidate list
         // (cand, ccnt; boxes over [s, s + ds] inflated by d_hat) contains every pair closer
         // than d_hat at x + alpha dx: the narrow phase filters it exactly (same C)
-        if (slot == 0 || h->opt.no_cand_reuse) broad_phase(h, nullptr, 0.5 * h->dh * 1.01, ccnt, h->dint.p + D_HOVF);
+        if (it == 0 || h->opt.no_cand_reuse) broad_phase(h, b, nullptr, 0.5 * h->dh * 1.01, ccnt, di + D_HOVF);
         kt.stop(K_BROAD, st);
         kt.start(K_NARROW, st);
         // one pass over [PT | EE] candidates; one scan; actives come out as [PT | EE], each sorted
-        launch_narrow(h->cand.p, ccnt, cap, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->dh2, h->flag.p,
-                      h->ctype.p, h->cd2.p, h->dint.p + D_STAT, st);
+        launch_narrow(q.cand.p, ccnt, cap, h->s(b), h->tris.p, h->edges.p, Nt, Ne, h->dh2, h->flag.p,
+                      h->ctype.p, h->cd2.p, di + D_STAT, st);
         scan_exclusive_dev(h->flag.p, h->pos.p, ccnt + 1, cap, h->iscr.p, st);
-        launch_compact_active(h->cand.p, ccnt, cap, h->flag.p, h->pos.p, h->ctype.p, h->cd2.p, h->akeys.p,
+        launch_compact_active(q.cand.p, ccnt, cap, h->flag.p, h->pos.p, h->ctype.p, h->cd2.p, h->akeys.p,
                               h->atype.p, h->ad2.p, acnt, st);
         kt.stop(K_NARROW, st);
         kt.start(K_DERIV, st);
         launch_contact_prep(h->mark.p, nf, h->gsq.p, 6 * Ns, dmax, st);   // clears of a5-a6
-        launch_pair_derivs(h->akeys.p, h->atype.p, h->ad2.p, acnt, cap, h->s.p, h->tris.p, h->edges.p, Nt,
+        launch_pair_derivs(h->akeys.p, h->atype.p, h->ad2.p, acnt, cap, h->s(b), h->tris.p, h->edges.p, Nt,
                            Ne, h->dh, h->kappa, h->grad.p, h->Hp.p, h->dist.p, h->ids.p, dmax, st);
         kt.stop(K_DERIV, st);
         // fork: stream 3 takes the gradient pull-back (reads ids, grad, dmax, g_el; writes gsq,
@@ -552,20 +632,21 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
         CK(cudaEventRecord(h->ev_fork3, st));
         CK(cudaStreamWaitEvent(h->st3, h->ev_fork3, 0));
         launch_accum_grad_fx(h->ids.p, acnt, cap, h->grad.p, dmax, h->gsq.p, h->st3);
-        launch_grad_pullback_fx(h->g_el.p, h->WTp.p, h->WTr.p, h->WTv.p, h->gsq.p, dmax, acnt, nf, h->G.p, h->st3);
+        launch_grad_pullback_fx(h->gel(b), h->WTp.p, h->WTr.p, h->WTv.p, h->gsq.p, dmax, acnt, nf, h->G(b), h->st3);
         kt.start(K_ASSEMBLY, st);
         // S
         launch_mark_S(h->ids.p, acnt, cap, h->Wp.p, h->Wc.p, h->v2q.p, h->mark.p, st);
         scan_compact(h->mark.p, h->spos.p, h->qS.p, nf, h->iscr.p, st);   // positions and S (sorted)
-        // V_s, K_s, Sigma_s depend on S (and the constant factor) only: reuse them while S is
-        // bit-identical to the S they were computed for
-        launch_same_S(h->qS.p, nS_dev, h->qS_prev.p, h->dint.p + D_SPREV, h->dint.p + D_SPREV + 1, h->capS,
-                      h->opt.no_sigma_reuse == 0, h->dint.p + D_CAP, h->dint.p + D_REUSED, st);
+        // V_s, K_s, Sigma_s depend on S (and the constant factor) only: reuse the slot's while S
+        // is bit-identical to the S they were computed for
+        launch_same_S(h->qS.p, nS_dev, h->qS_slot[slotr].p, h->nS_slot.p + slotr, di + D_SAME, h->capS,
+                      h->opt.no_sigma_reuse == 0, di + D_CAP, di + D_REUSED, st);
+        CK(dev_copy(di + D_NS, nS_dev, sizeof(int), st));
         CK(cudaEventRecord(h->ev_S, st));
         CK(cudaStreamWaitEvent(h->st3, h->ev_S, 0));
         launch_gather_gc(h->qS.p, nS_dev, h->capS, h->WTp.p, h->WTr.p, h->WTv.p, h->gsq.p, dmax, acnt, h->gcS.p,
                          h->st3);
-        enqueue_panel_forward(h, nS_dev, h->st3);
+        enqueue_panel_forward(h, b, nS_dev, h->st3);
         CK(cudaEventRecord(h->ev_join3, h->st3));
         // B-check: fixed-point accumulation into the dense 3|S| x 3|S| block, then to double; the
         // low words of the fixed-point sums live in the (not yet used) Sigma-hat buffer
@@ -579,200 +660,263 @@ static void enqueue_iteration(pd_ipc *h, Seq &q, int slot) {
         CK(cudaStreamWaitEvent(st, h->ev_join3, 0));     // join stream 3
     } else {
         CK(dev_zero(nS_dev, sizeof(int), st));
-        CK(dev_zero(h->dint.p + D_SPREV + 1, sizeof(int), st));
-        CK(dev_zero(h->dint.p + D_STAT, 2 * sizeof(int), st));
-        launch_grad_pullback(h->g_el.p, h->WTp.p, h->WTr.p, h->WTv.p, nullptr, nf, h->G.p, st);
-        enqueue_panel_forward(h, nS_dev, st);
+        CK(dev_zero(di + D_SAME, sizeof(int), st));
+        CK(dev_zero(di + D_STAT, 2 * sizeof(int), st));
+        CK(dev_zero(di + D_NS, sizeof(int), st));
+        launch_grad_pullback(h->gel(b), h->WTp.p, h->WTr.p, h->WTv.p, nullptr, nf, h->G(b), st);
     }
-    record_event(ev[2], st);
-    // ---------------- G-Step
-    // pure-PD part on stream 2 (forked after the gather, see above); the contact panel above
+    h->tm.rec(slot, 3, st);
+    // ---------------- G-Step: join stream 2 (w_el of all sequences) before the first Schur step
     const DevFactor &F = h->F;
-    // join stream 2 (w_el): the Schur step forms Z = w_el + V_s (gc + t)
-    CK(cudaStreamWaitEvent(st, h->ev_join, 0));
+    if (b == b0) CK(cudaStreamWaitEvent(st, h->ev_join, 0));
     kt.start(K_DENSE, st);
     if (Nt > 0) {
         if (h->trace_file) {
             h->sprof.ensure(1024);
             CK(dev_zero(h->sprof.p, 1024 * 8, st));
         }
-        CK((cudaError_t)launch_schur(F, h->V.p, h->ldv, h->Yw.p, h->gcS.p, h->qS.p,
-                                     h->ts_lo.p, h->ts_hi.p, nS_dev, h->capS, h->K.p, h->capS, h->Bc.p,
+        CK((cudaError_t)launch_schur(F, h->V_slot[slotr].p, h->ldv, h->Yw(b), h->gcS.p, h->qS.p,
+                                     h->ts_lo.p, h->ts_hi.p, nS_dev, h->capS, h->K_slot[slotr].p, h->capS, h->Bc.p,
                                      3 * h->capS, h->Sh.p, h->ldh, h->Lstore.p, h->Tt.p, h->U.p, h->yS.p,
-                                     h->rhs.p, h->u.p, h->tv.p, h->Z.p, h->dint.p + D_INFO,
-                                     h->dint.p + D_SPREV + 1, h->trace_file ? h->sprof.p : nullptr,
+                                     h->rhs.p, h->u.p, h->tv.p, h->Z(b), di + D_INFO, di + D_SAME,
+                                     h->trace_file ? h->sprof.p : nullptr,
                                      (h->opt.debug_flags & PD_IPC_DBG_LARGE_SCHUR) ? 1 : 0, st));
     } else {
-        CK(dev_copy(h->Z.p, h->Yw.p, sizeof(double) * 4 * nf, st));
+        CK(dev_copy(h->Z(b), h->Yw(b), sizeof(double) * 4 * nf, st));
     }
     kt.stop(K_DENSE, st);
+    h->tm.rec(slot, 4, st);
+}
+
+// (c) backward solves of every sequence (8 sequences' right-hand sides per launch), dx scatter
+static void enqueue_backward(pd_ipc *h, int b0, int nb, int it) {
+    cudaStream_t st = h->st;
+    KTimer &kt = h->kt;
+    const int slot = it * nb;
+    kt.slot = slot;
+    h->tm.rec(slot, 5, st);
     kt.start(K_BWD, st);
-    launch_backward_solve(F, h->ts_done.p, h->bw_cnt.p, h->ticket.p, h->bw_P.p, h->Z.p, h->nsm, st);
+    for (int c = 0; c < nb; c += kBwSeqs)
+        launch_backward_solve(h->F, h->ts_done.p, h->bw_cnt.p, h->ticket.p, h->bw_P.p, h->Z(b0 + c),
+                              std::min(kBwSeqs, nb - c), 4 * (long long)h->nf, h->nsm, st);
     kt.stop(K_BWD, st);
-    double *amin = h->dscal.p + 1;
-    double *ls = h->dscal.p + 2, *ls_out = h->dscal.p + 5, *scal = h->dscal.p + 9;
-    launch_scatter_dx(h->Z.p, h->q2v.p, nf, h->dx.p, amin, st);   // also seeds *amin = 1
-    record_event(ev[3], st);
-    // ---------------- CCD
+    launch_scatter_dx(h->Z(b0), h->q2v.p, h->nf, h->dx(b0), h->dscal(b0) + 1, nb, h->n, S_STRIDE,
+                      st);   // also seeds each sequence's CCD minimum amin = 1
+    h->tm.rec(slot, 6, st);
+}
+
+// (d) sequence b: CCD, line search, update
+static void enqueue_ccd_ls(pd_ipc *h, int b, int b0, int nb, int it) {
+    cudaStream_t st = h->st;
+    Seq &q = *h->seqs[b];
+    KTimer &kt = h->kt;
+    const int slot = it * nb + (b - b0);
+    kt.slot = slot;
+    h->tm.rec(slot, 7, st);
+    const int T = h->T, nf = h->nf, Ns = h->Ns, Nt = h->Nt, Ne = h->Ne;
+    int *di = h->dint(b);
+    double *dsc = h->dscal(b);
+    int *ccnt = di + D_CCNT;
+    double *amin = dsc + 1, *ls = dsc + 2, *ls_out = dsc + 5, *scal = dsc + 9;
     kt.start(K_CCD, st);
     if (Nt > 0) {
-        launch_surface(h->Wp.p, h->Wc.p, h->Wv.p, h->dx.p, Ns, h->ds.p, st);
-        broad_phase(h, h->ds.p, h->dh, ccnt, h->dint.p + D_HOVF + 1);
-        launch_accd(h->cand.p, ccnt, cap, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->ds.p, h->opt.accd_s,
+        launch_surface(h->Wp.p, h->Wc.p, h->Wv.p, h->dx(b), Ns, h->ds(b), st);
+        broad_phase(h, b, h->ds(b), h->dh, ccnt, di + D_HOVF + 1);
+        launch_accd(q.cand.p, ccnt, (int)q.cand.n, h->s(b), h->tris.p, h->edges.p, Nt, Ne, h->ds(b), h->opt.accd_s,
                     h->opt.accd_max_iters, amin, st);
     } else {
         CK(dev_zero(ccnt, 2 * sizeof(int), st));
     }
     kt.stop(K_CCD, st);
-    record_event(ev[4], st);
-    // ---------------- LS
+    h->tm.rec(slot, 8, st);
     kt.start(K_LS, st);
     {
         // elastic terms: block partials here, summed (fixed order) by the first line-search round
         int nb1 = 0, nb2 = 0;
-        elastic_partials(h->g_el.p, h->dx.p, h->q2v.p, nf, h->tets.p, h->B.p, h->w.p, T, h->part.p, &nb1, &nb2, st);
+        elastic_partials(h->gel(b), h->dx(b), h->q2v.p, nf, h->tets.p, h->B_.p, h->w.p, T, h->part.p, &nb1, &nb2,
+                         st);
         const int hmax = h->opt.ls_max_halvings;
         for (int h0 = 0; h0 <= hmax; h0 = ls_round_next(h0))
-            launch_ls_round(h->cand.p, ccnt, h->s.p, h->tris.p, h->edges.p, Nt, Ne, h->ds.p, h->dh, h->b0.p, ls, h0,
-                            h->lspart.p, scal, h->kappa, hmax, ls_out, h->dint.p + D_LSCTR, h->part.p, nb1,
+            launch_ls_round(q.cand.p, ccnt, h->s(b), h->tris.p, h->edges.p, Nt, Ne, h->ds(b), h->dh, h->b0.p, ls,
+                            h0, h->lspart.p, scal, h->kappa, hmax, ls_out, di + D_LSCTR, h->part.p, nb1,
                             h->part.p + nb1, nb2, amin, st);
-        launch_update(q.x.p, h->dx.p, h->q2v.p, nf, ls_out, h->dint.p + D_INFO, h->dint.p + D_ABORT, slot, st);
+        launch_update(h->x(b), h->dx(b), h->q2v.p, nf, ls_out, di + D_INFO, di + D_ABORT, it, st);
     }
     kt.stop(K_LS, st);
-    record_event(ev[5], st);
+    h->tm.rec(slot, 9, st);
 }
 
-// Run a batch of k <= kMaxBatch iterations with ONE host round trip: replay the captured CUDA
-// graph of the k iterations when possible (every launch configuration is static: all sizes live
-// on the device), else enqueue them stream-ordered.  A failing iteration (capacity / hash
-// overflow, Cholesky breakdown) raises a sticky device flag: it and every later iteration of the
-// batch leave x untouched, so x is the last accepted iterate.  Returns the number of iterations
-// applied; the caller grows buffers (done here) and runs the rest.
-static int run_batch(pd_ipc *h, Seq &q, int k, double ms[6]) {
+static void enqueue_lockstep_iteration(pd_ipc *h, int b0, int nb, int it) {
+    enqueue_elastic(h, b0, nb, it);
+    for (int b = b0; b < b0 + nb; ++b) enqueue_contact_schur(h, b, b0, nb, it);
+    enqueue_backward(h, b0, nb, it);
+    for (int b = b0; b < b0 + nb; ++b) enqueue_ccd_ls(h, b, b0, nb, it);
+}
+
+// Run k lockstep iterations of sequences [b0, b0 + nb) with ONE host round trip: replay the
+// captured CUDA graph of the batch when possible (every launch configuration is static: all
+// sizes live on the device), else enqueue stream-ordered.  A failing iteration of a sequence
+// (capacity / hash overflow, Cholesky breakdown, non-finite values) raises that sequence's
+// sticky device flag: it and every later iteration of the batch leave its x untouched, so x is
+// its last accepted iterate.  applied[b - b0] = iterations applied; ms[b - b0][6] accumulates the
+// Table-1 stage times.  Buffers are grown here; the caller runs the rest.
+static void run_lockstep(pd_ipc *h, int b0, int nb, int k, std::vector<int> &applied,
+                         std::vector<std::array<double, 6>> &ms) {
     cudaStream_t st = h->st;
-    const int nf = h->nf;
-    const DevFactor &F = h->F;
-    const int cap = (int)h->cand.n;
     KTimer &kt = h->kt;
-    int *nS_dev = h->spos.p + nf;
-    const bool graph = h->graphs && !h->debug && !h->trace_file && !h->force_sort &&
+    bool any_sort = false;
+    for (int b = b0; b < b0 + nb; ++b) any_sort |= h->seqs[b]->force_sort;
+    const bool graph = h->graphs && !h->debug && !h->trace_file && !any_sort &&
                        !(h->opt.debug_flags & PD_IPC_DBG_SORT_BROAD);
     const unsigned key = (h->buf_epoch << 1) | (kt.on ? 1u : 0u);
     const unsigned key_mask = kt.on ? kt.mask : 0u;
     auto enqueue_batch = [&]() {
-        CK(dev_zero(h->dint.p + D_ABORT, 4 * sizeof(int), st));   // abort, index, why, reused
-        CK(dev_zero(h->ticket.p + 1, sizeof(int), st));             // solve fault flags of the batch
+        for (int b = b0; b < b0 + nb; ++b)
+            CK(dev_zero(h->dint(b) + D_ABORT, 4 * sizeof(int), st));   // abort, index, why, reused
+        CK(dev_zero(h->ticket.p + 1, sizeof(int), st));               // solve fault flags of the batch
         CK(dev_zero(h->ticket2.p + 1, sizeof(int), st));
-        for (int i = 0; i < k; ++i) enqueue_iteration(h, q, i);
+        for (int i = 0; i < k; ++i) enqueue_lockstep_iteration(h, b0, nb, i);
     };
-    if (graph && (!q.exec || q.graph_key != key || q.graph_batch != k || q.graph_mask != key_mask)) {
-        if (q.exec) {
-            cudaGraphExecDestroy(q.exec);
-            q.exec = nullptr;
+    GraphEntry *ge = nullptr;
+    if (graph) {
+        for (auto &g : h->gcache)
+            if (g.b0 == b0 && g.nb == nb && g.k == k) ge = &g;
+        if (!ge) {
+            h->gcache.emplace_back();
+            ge = &h->gcache.back();
+            ge->b0 = b0;
+            ge->nb = nb;
+            ge->k = k;
         }
-        cudaGraph_t g = nullptr;
-        const long long l0 = launch_count();
-        bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
-        if (ok) {
-            g_capturing = true;
-            try {
-                enqueue_batch();
-            } catch (const CudaError &) {
-                ok = false;
+        if (!ge->exec || ge->key != key || ge->mask != key_mask) {
+            if (ge->exec) {
+                cudaGraphExecDestroy(ge->exec);
+                ge->exec = nullptr;
             }
-            g_capturing = false;
-            ok = (cudaStreamEndCapture(st, &g) == cudaSuccess) && ok;
+            cudaGraph_t g = nullptr;
+            const long long l0 = launch_count();
+            bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+            if (ok) {
+                g_capturing = true;
+                try {
+                    enqueue_batch();
+                } catch (const CudaError &) {
+                    ok = false;
+                }
+                g_capturing = false;
+                ok = (cudaStreamEndCapture(st, &g) == cudaSuccess) && ok;
+            }
+            if (ok) ok = cudaGraphInstantiate(&ge->exec, g, 0) == cudaSuccess;
+            if (g) cudaGraphDestroy(g);
+            cudaGetLastError();
+            const long long n_captured = launch_count() - l0;
+            add_launches(-n_captured);                     // counted on every replay instead
+            if (ok) {
+                ge->launches = n_captured;
+                ge->key = key;
+                ge->mask = key_mask;
+                ge->kt_used = kt.used;
+                ge->st_used = h->tm.used;
+            } else {
+                ge->exec = nullptr;
+                h->graphs = false;                         // capture unsupported: stream path from now on
+            }
         }
-        if (ok) ok = cudaGraphInstantiate(&q.exec, g, 0) == cudaSuccess;
-        if (g) cudaGraphDestroy(g);
-        cudaGetLastError();
-        const long long n_captured = launch_count() - l0;
-        add_launches(-n_captured);                     // counted on every replay instead
-        if (ok) {
-            q.graph_launches = n_captured;
-            q.graph_key = key;
-            q.graph_batch = k;
-            q.graph_mask = key_mask;
-            for (int i = 0; i < kMaxBatch; ++i)
-                for (int j = 0; j < K_NUM; ++j) q.kt_used[i][j] = kt.used[i][j];
-        } else {
-            q.exec = nullptr;
-            h->graphs = false;                         // capture unsupported: stream path from now on
-        }
+        if (!ge->exec) ge = nullptr;
     }
-    if (graph && q.exec) {
-        CK(cudaGraphLaunch(q.exec, st));
-        add_launches(q.graph_launches);
-        for (int i = 0; i < kMaxBatch; ++i)
-            for (int j = 0; j < K_NUM; ++j) kt.used[i][j] = q.kt_used[i][j];
+    if (ge) {
+        CK(cudaGraphLaunch(ge->exec, st));
+        add_launches(ge->launches);
+        kt.used = ge->kt_used;
+        h->tm.used = ge->st_used;
     } else {
         enqueue_batch();
     }
-    // ---------------- the one host round trip of the batch: stats and flags
-    double sc[13];
-    int di[16];
-    CK(cudaMemcpyAsync(sc, h->dscal.p, sizeof(sc), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(di, h->dint.p, sizeof(di), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&h->nS_host, nS_dev, sizeof(int), cudaMemcpyDeviceToHost, st));
+    // ---------------- the one host round trip of the batch: counters and scalars of every sequence
+    std::vector<int> di((size_t)nb * D_STRIDE);
+    std::vector<double> sc((size_t)nb * S_STRIDE);
+    CK(cudaMemcpyAsync(di.data(), h->dint(b0), sizeof(int) * di.size(), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(sc.data(), h->dscal(b0), sizeof(double) * sc.size(), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     int fault = 0, f2 = 0;
     CK(cudaMemcpy(&fault, h->ticket.p + 1, sizeof(int), cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(&f2, h->ticket2.p + 1, sizeof(int), cudaMemcpyDeviceToHost));
     fault |= f2;
     if (fault) throw CudaError("triangular solve dependency wait timed out", PD_IPC_E_CUDA);
-    const int nS = h->nS_host;
-    const int applied = di[D_ABORT] ? di[D_ABORT + 1] : k;
-    q.stats.sigma_reused += di[D_REUSED];
-    for (int i = 0; i < applied; ++i) {
-        auto &ev = h->tm.ev[i];
-        for (int s2 = 0; s2 < 5; ++s2) {
-            float f;
-            CK(cudaEventElapsedTime(&f, ev[s2], ev[s2 + 1]));
-            ms[s2 == 0 ? 4 : s2 - 1] += f;     // Misc, IPC, G, CCD, LS
-        }
-        float tot;
-        CK(cudaEventElapsedTime(&tot, ev[0], ev[5]));
-        ms[5] += tot;
+    applied.assign(nb, k);
+    std::vector<char> slot_ok((size_t)kSlotCap, 0);
+    for (int j = 0; j < nb; ++j) {
+        const int *d = di.data() + (size_t)j * D_STRIDE;
+        if (d[D_ABORT]) applied[j] = d[D_ABORT + 1];
+        for (int i = 0; i < applied[j]; ++i) slot_ok[(size_t)i * nb + j] = 1;
     }
-    kt.collect(applied);
-    if (di[D_ABORT]) {                           // why: 1 cand, 2 |S|, 4 Up, 8/16 hash, 32 info, 64 NaN
-        const int why = di[D_ABORT + 2];
-        // V_s, K_s, Sigma_s of the aborted iteration (and of the batch's later, skipped ones) may
-        // not have been computed for the S recorded by k_same_S: invalidate the reuse key
-        CK(dev_zero(h->dint.p + D_SPREV, sizeof(int), st));
-        CK(cudaStreamSynchronize(st));
-        if (why & 64) throw CudaError("non-finite value in step (dx, gradient or energy)", PD_IPC_E_NONFINITE);
-        if (why & 2) throw CudaError("contact vertex set exceeds capacity", PD_IPC_E_CAPACITY);
-        if (why & 32) throw CudaError("dense Cholesky: matrix not SPD", PD_IPC_E_NOT_SPD);
-        if (why & 1) grow_candidates(h, 2 * (size_t)cap);
-        if (why & 4) {
-            h->Up.exact((size_t)std::max(1, F.nU) * (((std::min(nS, h->capS) + 31) / 32) * 32 + 64));
-            ++h->buf_epoch;
+    // Table-1 stage times of each sequence: its own contact / Schur / CCD / LS events, plus its
+    // share (1 / nb) of the batched a1/a2 and backward-solve stages
+    for (int j = 0; j < nb; ++j)
+        for (int i = 0; i < applied[j]; ++i) {
+            const int sl = i * nb + j, s0 = i * nb;
+            const float misc = h->tm.el(s0, 0, 1) / nb, bw = h->tm.el(s0, 5, 6) / nb;
+            const float ipc = h->tm.el(sl, 2, 3), gst = h->tm.el(sl, 3, 4) + bw;
+            const float ccd = h->tm.el(sl, 7, 8), lsm = h->tm.el(sl, 8, 9);
+            ms[j][0] += ipc;
+            ms[j][1] += gst;
+            ms[j][2] += ccd;
+            ms[j][3] += lsm;
+            ms[j][4] += misc;
+            ms[j][5] += ipc + gst + ccd + lsm + misc;
         }
-        if (why & 24) h->force_sort = true;      // the next iteration takes the sort broad phase
-        return applied;
+    // kernel-group timers: a batched group is recorded on the slot of sequence 0 of an iteration
+    {
+        std::vector<char> okk((size_t)kSlotCap, 0);
+        for (int i = 0; i < kSlotCap; ++i) okk[i] = slot_ok[i];
+        for (int i = 0; i < k; ++i) okk[(size_t)i * nb] = 1;   // batched groups of applied iterations
+        kt.collect(okk);
     }
-    h->force_sort = false;
-    // stats of the last iteration
-    const int n_pt = di[D_ACNT], n_all = di[D_ACNT + 1];
-    pd_ipc_stats &S = q.stats;
-    S.n_cand = di[D_STAT + 1];
-    S.n_active = n_all;
-    S.n_S = nS;
-    S.alpha_max = sc[2];
-    S.alpha = sc[5];
-    S.ls_trials = (int)sc[6];
-    S.dE = sc[7];
-    S.flags = (int)sc[8];
-    const double min_dist = n_all > 0 ? sc[12] : 0.0;
-    if (n_all > 0 && !(min_dist > 0))
-        throw CudaError("non-positive distance in the active set", PD_IPC_E_NONFINITE);
-    S.min_dist = min_dist;
-    if (!std::isfinite(sc[5]) || !std::isfinite(sc[9]) || !std::isfinite(sc[10]))
-        throw CudaError("non-finite value in step", PD_IPC_E_NONFINITE);
-    if (h->debug) debug_capture(h, q, n_pt, n_all - n_pt, nS);
-    dump_traces(h, nS);
-    return applied;
+    for (int j = 0; j < nb; ++j) {
+        const int b = b0 + j;
+        Seq &q = *h->seqs[b];
+        const int *d = di.data() + (size_t)j * D_STRIDE;
+        const double *s = sc.data() + (size_t)j * S_STRIDE;
+        q.stats.sigma_reused += d[D_REUSED];
+        q.nS = d[D_NS];
+        if (d[D_ABORT]) {   // why: 1 cand, 2 |S|, 4 Up, 8/16 hash, 32 info, 64 NaN
+            const int why = d[D_ABORT + 2];
+            // V_s, K_s, Sigma_s of the aborted iteration (and of the batch's later, skipped ones)
+            // may not have been computed for the S recorded by k_same_S: invalidate the slot key
+            CK(dev_zero(h->nS_slot.p + q.slot, sizeof(int), st));
+            CK(cudaStreamSynchronize(st));
+            if (why & 64) throw CudaError("non-finite value in step (dx, gradient or energy)", PD_IPC_E_NONFINITE);
+            if (why & 2) throw CudaError("contact vertex set exceeds capacity", PD_IPC_E_CAPACITY);
+            if (why & 32) throw CudaError("dense Cholesky: matrix not SPD", PD_IPC_E_NOT_SPD);
+            if (why & 1) grow_candidates(h, b, 2 * (size_t)q.cand.n);
+            if (why & 4) {
+                h->Up.exact((size_t)std::max(1, h->F.nU) * (((std::min(q.nS, h->capS) + 31) / 32) * 32 + 64));
+                ++h->buf_epoch;
+            }
+            if (why & 24) q.force_sort = true;      // the next iteration takes the sort broad phase
+            continue;
+        }
+        q.force_sort = false;
+        // stats of the last iteration
+        const int n_pt = d[D_ACNT], n_all = d[D_ACNT + 1];
+        pd_ipc_stats &S = q.stats;
+        S.n_cand = d[D_STAT + 1];
+        S.n_active = n_all;
+        S.n_S = q.nS;
+        S.alpha_max = s[2];
+        S.alpha = s[5];
+        S.ls_trials = (int)s[6];
+        S.dE = s[7];
+        S.flags = (int)s[8];
+        const double min_dist = n_all > 0 ? s[12] : 0.0;
+        if (n_all > 0 && !(min_dist > 0))
+            throw CudaError("non-positive distance in the active set", PD_IPC_E_NONFINITE);
+        S.min_dist = min_dist;
+        if (!std::isfinite(s[5]) || !std::isfinite(s[9]) || !std::isfinite(s[10]))
+            throw CudaError("non-finite value in step", PD_IPC_E_NONFINITE);
+        if (h->debug && nb == 1) debug_capture(h, b, n_pt, n_all - n_pt, q.nS);
+    }
+    if (nb == 1) dump_traces(h, h->seqs[b0]->nS);
 }
 
 // ------------------------------------------------------------------ ABI -------------------
@@ -803,7 +947,7 @@ static void upload_actuation(pd_ipc *h, const double *A, bool on_device) {
             CK(cudaMemcpyAsync(h->A9stage.p, src, sizeof(double) * 9 * T, cudaMemcpyHostToDevice, h->st));
             dsrc = h->A9stage.p;
         }
-        launch_ingest_actuation(dsrc, h->seqs[sq]->A6.p, T, h->st);
+        launch_ingest_actuation(dsrc, h->A6((int)sq), T, h->st);
     }
 }
 
@@ -812,20 +956,23 @@ static void upload_actuation(pd_ipc *h, const double *A, bool on_device) {
 // non-incident PT / EE pair closer than d_hat has a positive distance (device: exact sort broad
 // phase + the canonical narrow phase, host-checked).  xd: the state on the device; x: the same
 // state on the host [n][3].  Uses the handle's contact work buffers (not on the timed path).
-static int check_intersection_free(pd_ipc *h, const double4 *xd, const double *x, std::string &why) {
+static int check_intersection_free(pd_ipc *h, int b, const double4 *xd, const double *x, std::string &why) {
     if (h->Nt == 0) return 0;
     const long long nx = surface_edge_triangle_crossings(h->hm, x);
     if (nx > 0) {
         why = "intersecting state: " + std::to_string(nx) + " surface edge-triangle crossings";
         return PD_IPC_E_INTERSECTING;
     }
-    launch_surface(h->Wp.p, h->Wc.p, h->Wv.p, xd, h->Ns, h->s.p, h->st);
-    const bool fs = h->force_sort;
-    h->force_sort = true;            // exact and host-checked: this is a validation path
-    int *ccnt = h->dint.p + D_CCNT;
-    broad_phase(h, nullptr, 0.5 * h->dh * 1.01, ccnt, h->dint.p + D_HOVF);
-    h->force_sort = fs;
-    launch_narrow(h->cand.p, ccnt, (int)h->cand.n, h->s.p, h->tris.p, h->edges.p, h->Nt, h->Ne, h->dh2,
+    // sequence b's surface, candidate list and counters are the scratch (its next iteration
+    // starts with a static broad phase)
+    launch_surface(h->Wp.p, h->Wc.p, h->Wv.p, xd, h->Ns, h->s(b), h->st);
+    Seq &q = *h->seqs[b];
+    const bool fs = q.force_sort;
+    q.force_sort = true;             // exact and host-checked: this is a validation path
+    int *ccnt = h->dint(b) + D_CCNT;
+    broad_phase(h, b, nullptr, 0.5 * h->dh * 1.01, ccnt, h->dint(b) + D_HOVF);
+    q.force_sort = fs;
+    launch_narrow(q.cand.p, ccnt, (int)q.cand.n, h->s(b), h->tris.p, h->edges.p, h->Nt, h->Ne, h->dh2,
                   h->flag.p, h->ctype.p, h->cd2.p, nullptr, h->st);
     int cc[2];
     sync_read_ints(h, cc, ccnt, 2);
@@ -917,7 +1064,7 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             std::vector<double> Bs(9 * (size_t)m.T);
             for (int t = 0; t < m.T; ++t)
                 for (int k = 0; k < 9; ++k) Bs[(size_t)k * m.T + t] = m.B[9 * (size_t)t + k];
-            h->B.upload(Bs.data(), Bs.size());
+            h->B_.upload(Bs.data(), Bs.size());
             h->w.upload(m.w.data(), m.w.size());
             h->tets.upload(reinterpret_cast<const int4 *>(m.tets.data()), m.T);
         }
@@ -991,7 +1138,7 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             h->f_bw_pbase.upload(pbase.data(), pbase.size());
             h->F.bw_nitems = (int)items.size();
             h->F.bw_nblocks = nblk;
-            h->bw_P.exact((size_t)nblk * 128 * 4);
+            h->bw_P.exact((size_t)nblk * 128 * 32);   // kTS_W x kBwCols partials per row block
             h->bw_cnt.exact(f.nsn);
         }
         h->f_uoff.upload(f.uoff.data(), f.uoff.size());
@@ -1012,7 +1159,7 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         }
         h->f_dinv.upload(f.dinv.data(), f.dinv.size());
         h->Ug.exact(4 * (size_t)std::max(1, f.uoff[f.nsn]));
-        h->Ug2.exact(4 * (size_t)std::max(1, f.uoff[f.nsn]));
+        h->Ug2.exact(4 * (size_t)std::max(1, f.uoff[f.nsn]) * std::max(1, o.n_seq));
         h->iscr2.exact(scan_scratch_ints(f.nsn + 1) + 64);
         DevFactor &F = h->F;
         F.uoff = h->f_uoff.p; F.urow_sn = h->f_urow_sn.p; F.rc_ptr = h->f_rc_ptr.p; F.rc_idx = h->f_rc_idx.p;
@@ -1038,22 +1185,39 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         }
         h->ldv = ((h->capS + 31) / 32) * 32;
         const int nf = m.nf;
-        // sequences
-        for (int sq = 0; sq < o.n_seq; ++sq) {
-            std::unique_ptr<Seq> s(new Seq());
-            std::vector<double4> x4(m.n);
-            for (int v = 0; v < m.n; ++v) x4[v] = make_double4(rest_pos[3 * v], rest_pos[3 * v + 1], rest_pos[3 * v + 2], 0.0);
-            s->x.upload(x4.data(), x4.size());
-            s->A6.exact(6 * (size_t)m.T);
-            s->p.exact(9 * (size_t)m.T);
-            std::memset(&s->stats, 0, sizeof(s->stats));
-            h->seqs.push_back(std::move(s));
+        // sequences: host state + batched device arrays [B][...]
+        const int Bq = o.n_seq;
+        h->B = Bq;
+        {
+            std::vector<double4> x4((size_t)m.n * Bq);
+            for (int sq = 0; sq < Bq; ++sq)
+                for (int v = 0; v < m.n; ++v)
+                    x4[(size_t)sq * m.n + v] =
+                        make_double4(rest_pos[3 * v], rest_pos[3 * v + 1], rest_pos[3 * v + 2], 0.0);
+            h->x_all.upload(x4.data(), x4.size());
         }
-        // work buffers
-        h->fc.exact(12 * (size_t)m.T);
-        h->g_el.exact(nf);
-        h->G.exact(4 * (size_t)nf);
-        h->Yw.exact(4 * (size_t)nf);
+        h->A6_all.exact(6 * (size_t)m.T * Bq);
+        h->fc_all.exact(12 * (size_t)m.T * Bq);
+        h->gel_all.exact((size_t)nf * Bq);
+        h->G_all.exact(4 * (size_t)nf * Bq);
+        h->Yw_all.exact(4 * (size_t)nf * Bq);
+        h->Z_all.exact(4 * (size_t)nf * Bq);
+        h->dx_all.exact((size_t)m.n * Bq);
+        CK(cudaMemset(h->dx_all.p, 0, sizeof(double4) * m.n * Bq));   // fixed vertices keep dx = 0
+        h->s_all.exact((size_t)std::max(1, m.Ns) * Bq);
+        h->ds_all.exact((size_t)std::max(1, m.Ns) * Bq);
+        h->dscal_all.exact((size_t)S_STRIDE * Bq);
+        h->dint_all.exact((size_t)D_STRIDE * Bq);
+        CK(cudaMemset(h->dscal_all.p, 0, sizeof(double) * S_STRIDE * Bq));   // flags / counters start cleared
+        CK(cudaMemset(h->dint_all.p, 0, sizeof(int) * D_STRIDE * Bq));
+        const size_t cap_cand = o.max_pairs > 0 ? (size_t)o.max_pairs
+                                                : std::max<size_t>(1 << 16, 16 * (size_t)(m.Ns + m.Ne));
+        for (int sq = 0; sq < Bq; ++sq) {
+            std::unique_ptr<Seq> sp(new Seq());
+            std::memset(&sp->stats, 0, sizeof(sp->stats));
+            sp->cand.exact(2 * cap_cand);
+            h->seqs.push_back(std::move(sp));
+        }
         h->ts_lo2.exact(f.nsn);
         h->ts_hi2.exact(f.nsn);
         h->ts_cnt2.exact(f.nsn + 1);
@@ -1061,16 +1225,9 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         h->ts_rem2.exact(f.nsn);
         h->ticket2.exact(4);
         CK(cudaMemset(h->ticket2.p, 0, 4 * sizeof(int)));
-        h->Z.exact(4 * (size_t)nf);
-        h->dx.exact(m.n);
-        CK(cudaMemset(h->dx.p, 0, sizeof(double4) * m.n));   // fixed vertices keep dx = 0
-        h->s.exact(std::max(1, m.Ns));
-        h->ds.exact(std::max(1, m.Ns));
-        h->gs.exact(std::max(1, m.Ns));
         h->mark.exact(nf + 1);
         h->spos.exact(nf + 1);
         h->qS.exact(nf + 1);
-        h->qS_prev.exact(nf + 1);
         h->ts_lo.exact(f.nsn);
         h->ts_hi.exact(f.nsn);
         h->ts_cnt.exact(f.nsn + 1);
@@ -1079,27 +1236,11 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         h->ts_done.exact(f.nsn);
         h->ticket.exact(4);
         CK(cudaMemset(h->ticket.p, 0, 4 * sizeof(int)));
-        h->dscal.exact(16);
-        h->dint.exact(32);
-        CK(cudaMemset(h->dscal.p, 0, sizeof(double) * 16));   // flags / counters start cleared
-        CK(cudaMemset(h->dint.p, 0, sizeof(int) * 32));
-        const size_t cap_cand = o.max_pairs > 0 ? (size_t)o.max_pairs
-                                                : std::max<size_t>(1 << 16, 16 * (size_t)(m.Ns + m.Ne));
-        h->cand.exact(2 * cap_cand);
-        h->cand_tmp.exact(2 * cap_cand);
-        ensure_pair_buffers(h.get(), 2 * cap_cand);
         // pre-size the per-pair buffers so that no allocation happens inside the iteration
-        // (an allocation synchronises the device); they still grow on demand
-        if (m.Nt > 0) {   // active pairs <= candidates: same capacity, no overflow check needed
-            const size_t cap_act = h->cand.n;
-            h->akeys.ensure(cap_act + 1);
-            h->atype.ensure(cap_act + 1);
-            h->ad2.ensure(cap_act + 1);
-            h->grad.ensure(12 * cap_act + 12);
-            h->Hp.ensure(78 * cap_act + 78);
-            h->dist.ensure(cap_act + 1);
-            h->ids.ensure(4 * cap_act + 4);
-            h->b0.ensure(cap_act + 1);
+        // (an allocation synchronises the device); they still grow on demand.  Active pairs <=
+        // candidates: same capacity, no overflow check needed
+        ensure_pair_buffers(h.get(), 2 * cap_cand);
+        if (m.Nt > 0) {
             h->blo.exact((size_t)m.Ns + m.Nt + m.Ne);
             h->bhi.exact((size_t)m.Ns + m.Nt + m.Ne);
             h->qcnt.exact((size_t)m.Ns + m.Ne + 1);
@@ -1122,9 +1263,7 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         h->cell0 = std::max(m.mean_edge, 2.0 * d_hat);
         if (m.Nt > 0) {
             const int cS = h->capS;
-            h->V.exact((size_t)nf * h->ldv);
             h->gcS.exact(3 * (size_t)h->capS + 3);
-            h->K.exact((size_t)cS * cS);
             h->Bc.exact((size_t)9 * cS * cS);
             h->ldh = 3 * cS + 8;
             h->Sh.exact((size_t)(3 * cS + 1) * h->ldh);
@@ -1136,16 +1275,36 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             h->u.exact(3 * (size_t)cS);
             h->tv.exact(3 * (size_t)cS);
             h->Up.exact((size_t)std::max(1, f.uoff[f.nsn]) * (((cS + 31) / 32) * 32));
-        } else {
-            h->V.exact(32);
         }
         h->Tt.exact(64 * 64);
         h->part.exact(std::max<size_t>(4096, (size_t)(m.T + 255) / 256 + (nf + 255) / 256 + 64));
+        {   // reuse slots (V_s, K_s / -Sigma_s and the S they belong to): one per sequence when 40 %
+            // of the free HBM holds them, else fewer, shared round-robin (the bit-exact key check
+            // keeps sharing exact; a shared slot only reuses less often)
+            const size_t vbytes = m.Nt > 0 ? (size_t)nf * h->ldv * 8 + (size_t)h->capS * h->capS * 8 + (size_t)(nf + 1) * 4
+                                           : 256;
+            size_t fr = 0, tot = 0;
+            CK(cudaMemGetInfo(&fr, &tot));
+            const size_t fit = std::max<size_t>(1, (size_t)(0.4 * (double)fr) / std::max<size_t>(vbytes, 1));
+            h->nslots = m.Nt > 0 ? (int)std::min<size_t>((size_t)Bq, fit) : 1;
+            if (const char *ns = std::getenv("PDIPC_REUSE_SLOTS")) h->nslots = std::max(1, std::min(Bq, std::atoi(ns)));
+            h->V_slot.resize(h->nslots);
+            h->K_slot.resize(h->nslots);
+            h->qS_slot.resize(h->nslots);
+            for (int r = 0; r < h->nslots; ++r) {
+                h->V_slot[r].exact(m.Nt > 0 ? (size_t)nf * h->ldv : 32);
+                h->K_slot[r].exact(m.Nt > 0 ? (size_t)h->capS * h->capS : 1);
+                h->qS_slot[r].exact(nf + 1);
+            }
+            h->nS_slot.exact(h->nslots);
+            CK(cudaMemset(h->nS_slot.p, 0, sizeof(int) * h->nslots));
+            for (int sq = 0; sq < Bq; ++sq) h->seqs[sq]->slot = sq % h->nslots;
+        }
         upload_actuation(h.get(), A, false);
         CK(cudaStreamSynchronize(h->st));
         {   // the rest state must be intersection-free (SURVEY.md 8(b) E_INTERSECTING at create)
             std::string why;
-            const int rc = check_intersection_free(h.get(), h->seqs[0]->x.p, rest_pos, why);
+            const int rc = check_intersection_free(h.get(), 0, h->x(0), rest_pos, why);
             if (rc) {
                 pd_ipc_destroy(h.release());
                 return fail(nullptr, rc, why);
@@ -1174,19 +1333,42 @@ int pd_ipc_step(pd_ipc *h, const double *A_next, int32_t n_iters, pd_ipc_stats *
             }
             upload_actuation(h, A_next, h->opt.A_on_device != 0);
         }
-        for (auto &sq : h->seqs) {
-            double ms[6] = {0, 0, 0, 0, 0, 0};
-            sq->stats.sigma_reused = 0;
+        // Sequences advance in lockstep (one batch = k iterations of all of them, k * B <= kSlotCap);
+        // with debug capture on, each sequence runs alone so the shared contact buffers hold its
+        // data.  A sequence whose iteration aborted (capacity / hash overflow: buffers grown, or the
+        // sort broad phase next) runs its remaining iterations of the batch alone.
+        const int Bq = h->B;
+        std::vector<std::array<double, 6>> ms(Bq, std::array<double, 6>{0, 0, 0, 0, 0, 0});
+        for (auto &sq : h->seqs) sq->stats.sigma_reused = 0;
+        auto run_alone = [&](int b, int iters) {
             int done = 0, tries = 0;
-            while (done < n_iters) {
-                const int k = std::min(n_iters - done, kMaxBatch);
-                const int applied = run_batch(h, *sq, k, ms);
-                done += applied;
-                if (applied < k && ++tries > 8)            // buffers grown / sort path: redo the rest
+            std::vector<int> ap;
+            std::vector<std::array<double, 6>> m1(1, std::array<double, 6>{0, 0, 0, 0, 0, 0});
+            while (done < iters) {
+                const int k = std::min(iters - done, kMaxBatch);
+                run_lockstep(h, b, 1, k, ap, m1);
+                done += ap[0];
+                if (ap[0] < k && ++tries > 8)            // buffers grown / sort path: redo the rest
                     throw CudaError("capacity growth did not converge", PD_IPC_E_CAPACITY);
             }
-            sq->stats.iters = n_iters;
-            for (int k = 0; k < 6; ++k) sq->stats.ms[k] = ms[k];
+            for (int c = 0; c < 6; ++c) ms[b][c] += m1[0][c];
+        };
+        if (h->debug || Bq == 1) {
+            for (int b = 0; b < Bq; ++b) run_alone(b, n_iters);
+        } else {
+            const int kb = std::max(1, std::min(kMaxBatch, kSlotCap / Bq));
+            std::vector<int> ap;
+            for (int done = 0; done < n_iters;) {
+                const int k = std::min(n_iters - done, kb);
+                run_lockstep(h, 0, Bq, k, ap, ms);
+                for (int b = 0; b < Bq; ++b)
+                    if (ap[b] < k) run_alone(b, k - ap[b]);
+                done += k;
+            }
+        }
+        for (int b = 0; b < Bq; ++b) {
+            h->seqs[b]->stats.iters = n_iters;
+            for (int c = 0; c < 6; ++c) h->seqs[b]->stats.ms[c] = ms[b][c];
         }
         if (stats)
             for (size_t sq = 0; sq < h->seqs.size(); ++sq) stats[sq] = h->seqs[sq]->stats;
@@ -1201,7 +1383,7 @@ int pd_ipc_positions(const pd_ipc *h, int32_t seq, double *out) {
     if (seq < 0 || seq >= (int)h->seqs.size()) return fail(const_cast<pd_ipc *>(h), PD_IPC_E_ARG, "bad sequence");
     try {
         std::vector<double4> x4(h->n);
-        CK(cudaMemcpy(x4.data(), h->seqs[seq]->x.p, sizeof(double4) * h->n, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(x4.data(), const_cast<pd_ipc *>(h)->x(seq), sizeof(double4) * h->n, cudaMemcpyDeviceToHost));
         for (int v = 0; v < h->n; ++v) {
             out[3 * v] = x4[v].x;
             out[3 * v + 1] = x4[v].y;
@@ -1218,8 +1400,8 @@ void pd_ipc_destroy(pd_ipc *h) {
     cudaSetDevice(h->device);
     cudaDeviceSynchronize();
     // DBuf members free in their own scope via release; explicit for clarity
-    for (auto &sq : h->seqs)
-        if (sq->exec) cudaGraphExecDestroy(sq->exec);
+    for (auto &g : h->gcache)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
     h->tm.destroy();
     h->kt.destroy();
     if (h->trace_file) std::fclose(h->trace_file);
@@ -1235,22 +1417,27 @@ void pd_ipc_destroy(pd_ipc *h) {
     if (h->ev_S) cudaEventDestroy(h->ev_S);
     if (h->st) cudaStreamDestroy(h->st);
     auto rel = [](auto &b) { b.release(); };
-    rel(h->tets); rel(h->B); rel(h->w); rel(h->inc_ptr); rel(h->inc); rel(h->q2v); rel(h->v2q);
+    rel(h->tets); rel(h->B_); rel(h->w); rel(h->inc_ptr); rel(h->inc); rel(h->q2v); rel(h->v2q);
     rel(h->Wp); rel(h->Wc); rel(h->WTp); rel(h->WTr); rel(h->tris); rel(h->edges); rel(h->Wv); rel(h->WTv);
     rel(h->f_c0); rel(h->f_rowptr); rel(h->f_rows); rel(h->f_parent); rel(h->f_seg_ptr); rel(h->f_seg_d);
     rel(h->f_seg_klo); rel(h->f_seg_khi); rel(h->f_fd); rel(h->f_col2sn); rel(h->f_valptr); rel(h->f_L);
-    rel(h->f_dinv_ptr); rel(h->f_dinv); rel(h->Ug); rel(h->Up); rel(h->Yw); rel(h->bw_P); rel(h->f_bw_items); rel(h->f_ford); rel(h->f_bord); rel(h->gcS); rel(h->Ug2); rel(h->f_path_ptr); rel(h->f_path_sn); rel(h->qS_prev); rel(h->f_rc_src); rel(h->f_bw_pbase); rel(h->bw_cnt); rel(h->f_uoff); rel(h->f_urow_sn);
+    rel(h->f_dinv_ptr); rel(h->f_dinv); rel(h->Ug); rel(h->Up); rel(h->bw_P); rel(h->f_bw_items); rel(h->f_ford); rel(h->f_bord); rel(h->gcS); rel(h->Ug2); rel(h->f_path_ptr); rel(h->f_path_sn); rel(h->f_rc_src); rel(h->f_bw_pbase); rel(h->bw_cnt); rel(h->f_uoff); rel(h->f_urow_sn);
     rel(h->f_rc_ptr); rel(h->f_rc_idx); rel(h->f_urel); rel(h->f_ch_ptr); rel(h->f_ch);
-    for (auto &s : h->seqs) { rel(s->x); rel(s->A6); rel(s->p); }
-    rel(h->fc); rel(h->xstage); rel(h->G); rel(h->Z); rel(h->A9stage); rel(h->g_el); rel(h->s); rel(h->ds); rel(h->dx);
-    rel(h->gs); rel(h->blo); rel(h->bhi); rel(h->hcnt); rel(h->hstart); rel(h->hent); rel(h->cand);
+    for (auto &s : h->seqs) rel(s->cand);
+    for (auto &b : h->V_slot) rel(b);
+    for (auto &b : h->K_slot) rel(b);
+    for (auto &b : h->qS_slot) rel(b);
+    rel(h->nS_slot);
+    rel(h->x_all); rel(h->gel_all); rel(h->dx_all); rel(h->s_all); rel(h->ds_all); rel(h->A6_all); rel(h->p_all);
+    rel(h->fc_all); rel(h->G_all); rel(h->Yw_all); rel(h->Z_all); rel(h->dscal_all); rel(h->dint_all);
+    rel(h->xstage); rel(h->A9stage); rel(h->blo); rel(h->bhi); rel(h->hcnt); rel(h->hstart); rel(h->hent);
     rel(h->qcnt); rel(h->qoff); rel(h->qlist); rel(h->gsq);
     rel(h->cand_tmp); rel(h->akeys); rel(h->flag); rel(h->pos); rel(h->ctype); rel(h->atype); rel(h->ids);
     rel(h->iscr); rel(h->cd2); rel(h->ad2); rel(h->grad); rel(h->Hp); rel(h->dist); rel(h->mark);
     rel(h->spos); rel(h->qS); rel(h->lspart); rel(h->ts_lo);
     rel(h->ts_hi); rel(h->ts_cnt); rel(h->ts_ptr); rel(h->ts_rem); rel(h->ts_done); rel(h->ticket);
-    rel(h->V); rel(h->K); rel(h->Bc); rel(h->Sh); rel(h->U); rel(h->Tt); rel(h->yS); rel(h->rhs);
-    rel(h->u); rel(h->tv); rel(h->part); rel(h->b0); rel(h->dscal); rel(h->dint); rel(h->Lstore);
+    rel(h->Bc); rel(h->Sh); rel(h->U); rel(h->Tt); rel(h->yS); rel(h->rhs);
+    rel(h->u); rel(h->tv); rel(h->part); rel(h->b0); rel(h->Lstore);
     delete h;
 }
 
@@ -1274,9 +1461,9 @@ int pd_ipc_set_positions(pd_ipc *h, int32_t seq, const double *x) {
         h->xstage.ensure(h->n);
         CK(cudaMemcpy(h->xstage.p, x4.data(), sizeof(double4) * h->n, cudaMemcpyHostToDevice));
         std::string why;
-        const int rc = check_intersection_free(h, h->xstage.p, x, why);
+        const int rc = check_intersection_free(h, seq, h->xstage.p, x, why);
         if (rc) return fail(h, rc, why);
-        CK(cudaMemcpy(h->seqs[seq]->x.p, h->xstage.p, sizeof(double4) * h->n, cudaMemcpyDeviceToDevice));
+        CK(cudaMemcpy(h->x(seq), h->xstage.p, sizeof(double4) * h->n, cudaMemcpyDeviceToDevice));
     } catch (const CudaError &e) {
         return fail(h, e.code, e.what());
     }
@@ -1286,6 +1473,14 @@ int pd_ipc_set_positions(pd_ipc *h, int32_t seq, const double *x) {
 int pd_ipc_set_debug(pd_ipc *h, int32_t level) {
     if (!h) return fail(nullptr, PD_IPC_E_ARG, "NULL handle");
     h->debug = level;
+    if (level > 0 && !h->p_all.p) {
+        try {
+            CK(cudaSetDevice(h->device));
+            h->p_all.exact(9 * (size_t)h->T * h->B);   // projections of the local step (parity hook)
+        } catch (const CudaError &e) {
+            return fail(h, e.code, e.what());
+        }
+    }
     return PD_IPC_OK;
 }
 
@@ -1295,7 +1490,8 @@ int pd_ipc_get_projections(const pd_ipc *h, int32_t seq, double *p) {
     if (!h->debug) return fail(const_cast<pd_ipc *>(h), PD_IPC_E_ARG, "enable pd_ipc_set_debug first");
     try {
         std::vector<double> soa(9 * (size_t)h->T);
-        CK(cudaMemcpy(soa.data(), h->seqs[seq]->p.p, sizeof(double) * soa.size(), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(soa.data(), h->p_all.p + (size_t)seq * 9 * h->T, sizeof(double) * soa.size(),
+                      cudaMemcpyDeviceToHost));
         for (int t = 0; t < h->T; ++t)
             for (int k = 0; k < 9; ++k) p[9 * (size_t)t + k] = soa[(size_t)k * h->T + t];
     } catch (const CudaError &e) {

@@ -195,22 +195,29 @@ template <int MINB>
 __global__ void __launch_bounds__(128, MINB) k_local_step(
     const int4 *__restrict__ tets, const double4 *__restrict__ x, const double *__restrict__ B,
     const double *__restrict__ A6, const double *__restrict__ w, int T, double *__restrict__ fc,
-    double *__restrict__ p, int *__restrict__ clr) {
+    double *__restrict__ p, int *__restrict__ clr, int nseq, long long xs, int clrs) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
-    // the iteration's device counters, cleared by its first kernel: active-pair counts [0, 1] and
-    // info / capacity / hash flags [4, 8) (the candidate counts [2, 3] carry over, see R8)
-    if (clr && t < 8 && (t < 2 || t >= 4)) clr[t] = 0;
+    // the iteration's device counters of every sequence, cleared by its first kernel: active-pair
+    // counts [0, 1] and info / capacity / hash flags [4, 8) (the candidate counts [2, 3] carry
+    // over, see R8)
+    if (clr)
+        for (int i = t; i < 8 * nseq; i += gridDim.x * blockDim.x)
+            if ((i & 7) < 2 || (i & 7) >= 4) clr[(i >> 3) * clrs + (i & 7)] = 0;
     if (t >= T) return;
+    // the mesh data of the tet is read once for all sequences of the batch
     const int4 tv = __ldcs(tets + t);
-    const double4 x0 = x[tv.x], x1 = x[tv.y], x2 = x[tv.z], x3 = x[tv.w];
     double Bm[3][3];
 #pragma unroll
     for (int k = 0; k < 9; ++k) Bm[k / 3][k % 3] = __ldcs(B + (size_t)k * T + t);
-    const double a00 = __ldcs(A6 + t), a01 = __ldcs(A6 + (size_t)T + t), a02 = __ldcs(A6 + 2 * (size_t)T + t),
-                 a11 = __ldcs(A6 + 3 * (size_t)T + t), a12 = __ldcs(A6 + 4 * (size_t)T + t),
-                 a22 = __ldcs(A6 + 5 * (size_t)T + t);
-    const double A[3][3] = {{a00, a01, a02}, {a01, a11, a12}, {a02, a12, a22}};
     const double wt = __ldcs(w + t);
+    for (int sq = 0; sq < nseq; ++sq) {
+    const double4 *xq = x + sq * xs;
+    const double *A6q = A6 + (size_t)sq * 6 * T;
+    const double4 x0 = xq[tv.x], x1 = xq[tv.y], x2 = xq[tv.z], x3 = xq[tv.w];
+    const double a00 = __ldcs(A6q + t), a01 = __ldcs(A6q + (size_t)T + t), a02 = __ldcs(A6q + 2 * (size_t)T + t),
+                 a11 = __ldcs(A6q + 3 * (size_t)T + t), a12 = __ldcs(A6q + 4 * (size_t)T + t),
+                 a22 = __ldcs(A6q + 5 * (size_t)T + t);
+    const double A[3][3] = {{a00, a01, a02}, {a01, a11, a12}, {a02, a12, a22}};
     // D_s = [x1-x0, x2-x0, x3-x0] (columns); F = D_s B
     const double Ds[3][3] = {{x1.x - x0.x, x2.x - x0.x, x3.x - x0.x},
                              {x1.y - x0.y, x2.y - x0.y, x3.y - x0.y},
@@ -235,7 +242,7 @@ __global__ void __launch_bounds__(128, MINB) k_local_step(
         for (int b = 0; b < 3; ++b) P[a][b] = R[a][0] * A[0][b] + R[a][1] * A[1][b] + R[a][2] * A[2][b];
     if (p) {
 #pragma unroll
-        for (int k = 0; k < 9; ++k) p[(size_t)k * T + t] = P[k / 3][k % 3];
+        for (int k = 0; k < 9; ++k) p[(size_t)sq * 9 * T + (size_t)k * T + t] = P[k / 3][k % 3];
     }
     // r = w (F - P);  f_c = r g_c, g_c = row c-1 of B (c = 1..3), f_0 = -(f_1 + f_2 + f_3)
     double r[3][3];
@@ -251,7 +258,7 @@ __global__ void __launch_bounds__(128, MINB) k_local_step(
             f[c][a] = r[a][0] * Bm[c - 1][0] + r[a][1] * Bm[c - 1][1] + r[a][2] * Bm[c - 1][2];
 #pragma unroll
     for (int a = 0; a < 3; ++a) f[0][a] = -(f[1][a] + f[2][a] + f[3][a]);
-    double2 *o = reinterpret_cast<double2 *>(fc + 12 * (size_t)t);
+    double2 *o = reinterpret_cast<double2 *>(fc + (size_t)sq * 12 * T + 12 * (size_t)t);
     const unsigned long long pol = l2_policy_evict_last();
     st_f64x2_evict_last(o + 0, f[0][0], f[0][1], pol);
     st_f64x2_evict_last(o + 1, f[0][2], f[1][0], pol);
@@ -259,6 +266,7 @@ __global__ void __launch_bounds__(128, MINB) k_local_step(
     st_f64x2_evict_last(o + 3, f[2][0], f[2][1], pol);
     st_f64x2_evict_last(o + 4, f[2][2], f[3][0], pol);
     st_f64x2_evict_last(o + 5, f[3][1], f[3][2], pol);
+    }
 }
 
 // ------------------------------------------------------------------ a2 gather -------------
@@ -272,8 +280,10 @@ constexpr int kGatherLanes = 8;
 constexpr int kGatherBatch = 4;
 __global__ void __launch_bounds__(256) k_gather_elastic(const int *__restrict__ inc_ptr, const int *__restrict__ inc,
                                                         const double *__restrict__ fc, int nf,
-                                                        double4 *__restrict__ g) {
+                                                        double4 *__restrict__ g, long long fcs) {
     const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+    fc += (size_t)blockIdx.y * fcs;        // sequence blockIdx.y: its forces and gradient
+    g += (size_t)blockIdx.y * nf;
     const int q = gid / kGatherLanes, l = gid % kGatherLanes;
     double gx = 0, gy = 0, gz = 0;
     if (q < nf) {
@@ -415,8 +425,11 @@ __global__ void k_update(double4 *__restrict__ x, const double4 *__restrict__ dx
 // scatter dx from factor order (solution of the backward solve, [nf][4], negated) to vertices
 // (fixed vertices keep dx = 0 from the clear at create); also seeds the CCD minimum *amin = 1
 __global__ void k_scatter_dx(const double *__restrict__ z, const int *__restrict__ q2v, int nf,
-                             double4 *__restrict__ dx, double *__restrict__ amin) {
+                             double4 *__restrict__ dx, double *__restrict__ amin, int n, int amin_stride) {
     int q = blockIdx.x * blockDim.x + threadIdx.x;
+    z += (size_t)blockIdx.y * 4 * nf;      // sequence blockIdx.y
+    dx += (size_t)blockIdx.y * n;
+    if (amin) amin += (size_t)blockIdx.y * amin_stride;
     if (q == 0 && amin) *amin = 1.0;
     if (q >= nf) return;
     const double *r = z + 4 * (size_t)q;
@@ -436,21 +449,22 @@ void elastic_init(int) {
     if (const char *e = std::getenv("PDIPC_LS_MINB")) g_ls_minb = std::atoi(e);
 }
 void launch_local_step(const int4 *tets, const double4 *x, const double *B, const double *A6,
-                       const double *w, int T, double *fc, double *p, int *clr, cudaStream_t st) {
+                       const double *w, int T, double *fc, double *p, int *clr, int nseq, long long xs,
+                       int clrs, cudaStream_t st) {
     if (T <= 0) return;
     // latency-bound small meshes (fewer than ~4 CTAs of 128 per SM): half-size CTAs spread the
     // tets over twice as many CTAs, balancing the SMs
     const int nt = T < 4 * 148 * 128 ? 64 : 128;
     if (g_ls_minb == 5)
-        PDI_LAUNCH(k_local_step<5>, (T + nt - 1) / nt, nt, 0, st)(tets, x, B, A6, w, T, fc, p, clr);
+        PDI_LAUNCH(k_local_step<5>, (T + nt - 1) / nt, nt, 0, st)(tets, x, B, A6, w, T, fc, p, clr, nseq, xs, clrs);
     else
-        PDI_LAUNCH(k_local_step<4>, (T + nt - 1) / nt, nt, 0, st)(tets, x, B, A6, w, T, fc, p, clr);
+        PDI_LAUNCH(k_local_step<4>, (T + nt - 1) / nt, nt, 0, st)(tets, x, B, A6, w, T, fc, p, clr, nseq, xs, clrs);
 }
 void launch_gather_elastic(const int *inc_ptr, const int *inc, const double *fc, int nf,
-                           double4 *g, cudaStream_t st) {
+                           double4 *g, int nseq, long long fcs, cudaStream_t st) {
     if (nf <= 0) return;
-    PDI_LAUNCH(k_gather_elastic, (int)(((long long)nf * kGatherLanes + 255) / 256), 256, 0, st)(inc_ptr, inc, fc,
-                                                                                             nf, g);
+    PDI_LAUNCH(k_gather_elastic, dim3((unsigned)(((long long)nf * kGatherLanes + 255) / 256), nseq), 256, 0, st)(
+        inc_ptr, inc, fc, nf, g, fcs);
 }
 void launch_surface(const int *Wp, const int *Wc, const double *Wv, const double4 *x, int Ns,
                     double4 *s, cudaStream_t st) {
@@ -521,8 +535,9 @@ void launch_update(double4 *x, const double4 *dx, const int *q2v, int nf, const 
                    const int *flags, int *abort, int it, cudaStream_t st) {
     PDI_LAUNCH(k_update, (nf + 255) / 256, 256, 0, st)(x, dx, q2v, nf, alpha, flags, abort, it);
 }
-void launch_scatter_dx(const double *z, const int *q2v, int nf, double4 *dx, double *amin, cudaStream_t st) {
-    PDI_LAUNCH(k_scatter_dx, (nf + 255) / 256, 256, 0, st)(z, q2v, nf, dx, amin);
+void launch_scatter_dx(const double *z, const int *q2v, int nf, double4 *dx, double *amin, int nseq, int n,
+                       int amin_stride, cudaStream_t st) {
+    PDI_LAUNCH(k_scatter_dx, dim3((nf + 255) / 256, nseq), 256, 0, st)(z, q2v, nf, dx, amin, n, amin_stride);
 }
 
 }  // namespace pdipc

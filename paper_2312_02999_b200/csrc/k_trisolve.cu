@@ -41,15 +41,15 @@ __device__ __forceinline__ int ts_item_count(int k, const int *__restrict__ ford
                                              const int *__restrict__ sn_parent, const int *__restrict__ qS,
                                              const int *__restrict__ nS_ptr, int capS,
                                              const int *__restrict__ same_S, int nU, long long up_cap,
-                                             int *__restrict__ flags, int mode, int *__restrict__ lo,
+                                             int *__restrict__ flags, int mode, int ngt, int *__restrict__ lo,
                                              int *__restrict__ hi, int *__restrict__ rem) {
     const int s = ford[k];
     const int nb = (sn_rowptr[s + 1] - sn_rowptr[s] + kSolveRB - 1) / kSolveRB;
     if (!(mode & 2)) {                     // gradient items only: no contact data read at all
         lo[s] = hi[s] = 0;
         const int p = sn_parent[s];
-        if (p >= 0) atomicAdd(rem + p, nb);
-        return nb;
+        if (p >= 0) atomicAdd(rem + p, nb * ngt);
+        return nb * ngt;
     }
     const int nS = min(*nS_ptr, capS);
     // panel update rows need nU x round32(|S|) doubles; otherwise flag bit 4 (grow and redo)
@@ -66,7 +66,7 @@ __device__ __forceinline__ int ts_item_count(int k, const int *__restrict__ ford
     hi[s] = H0;
     // panel tiles only when V_s must be recomputed (S changed)
     const int tiles = (up_ok && *same_S == 0 && H0 > L0) ? (H0 - 1) / kPT - L0 / kPT + 1 : 0;
-    const int c = nb * ((mode & 1) + tiles);
+    const int c = nb * ((mode & 1) ? ngt + tiles : tiles);
     const int p = sn_parent[s];
     if (p >= 0) atomicAdd(rem + p, c);
     return c;
@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kPlanNT) k_ts_plan(const int *__restrict__ for
                                                      const int *__restrict__ qS, const int *__restrict__ nS_ptr,
                                                      int capS, const int *__restrict__ same_S, int nU,
                                                      long long up_cap, int *__restrict__ flags, int mode,
-                                                     int *__restrict__ lo, int *__restrict__ hi,
+                                                     int ngt, int *__restrict__ lo, int *__restrict__ hi,
                                                      int *__restrict__ cnt, int *__restrict__ rem,
                                                      int *__restrict__ item_ptr, int *__restrict__ ticket) {
     __shared__ int wsum[kPlanNT / 32];
@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(kPlanNT) k_ts_plan(const int *__restrict__ for
     __syncthreads();
     for (int k = tid; k < nsn; k += kPlanNT)
         cnt[k] = ts_item_count(k, ford, sn_c0, sn_rowptr, sn_fd, sn_parent, qS, nS_ptr, capS, same_S, nU, up_cap,
-                               flags, mode, lo, hi, rem);
+                               flags, mode, ngt, lo, hi, rem);
     __syncthreads();
     for (int k0 = 0; k0 <= nsn; k0 += kPlanNT) {          // exclusive scan, item_ptr[nsn] = total
         const int k = k0 + tid;
@@ -135,11 +135,14 @@ struct FwdArgs {
     const int *lo, *hi, *item_ptr, *qS, *ford;
     int nsn;
     int *rem, *ticket;
-    const double *G;                   // [nf][4] Pi g-hat
-    double *Y;                         // [nf][4] out: w = L^{-1} Pi g-hat
+    const double *G;                   // [nseq][nf][4] Pi g (sequence stride gstride doubles)
+    double *Y;                         // [nseq][nf][4] out: w = L^{-1} Pi g
     double *V;                         // [nf][ldv] panel
     int ldv;
-    double *Ug;                        // [nU][4] gradient update rows
+    double *Ug;                        // [nseq][nU][4] gradient update rows (stride ustride)
+    long long gstride, ustride;
+    int nseq;                          // gradient right-hand sides: 3 columns per sequence
+    int ngt, gw;                       // gradient tiles per row block, columns per tile (8 | 32)
     double *Up;                        // [nU][ldu] panel update rows, ldu = round32(|S|)
     const int *nS_ptr;
     int capS;
@@ -311,26 +314,32 @@ __global__ void __launch_bounds__(kTS_NT) k_forward_solve(FwdArgs A) {
         const int c0 = A.sn_c0[s], w = A.sn_c0[s + 1] - c0;
         const int slot0 = A.sn_rowptr[s], nr = A.sn_rowptr[s + 1] - slot0;
         const int nb = (nr + kSolveRB - 1) / kSolveRB;
-        const int idx = item - item_ptr[kpos], tk = idx / nb + (A.with_grad ? 0 : 1);
+        const int idx = item - item_ptr[kpos], tk = idx / nb;
         const int rb = (idx % nb) * kSolveRB;
         const int m = min(kSolveRB, nr - rb);
-        const bool grad = tk == 0;
+        const int ngt = A.with_grad ? A.ngt : 0;
+        // tiles 0 .. ngt-1: gradient right-hand sides, gw columns = gw/4 sequences x (xyz + pad);
+        // tiles >= ngt: the 32-column panel tiles active in s
+        const bool grad = tk < ngt;
+        const int gseq0 = grad ? tk * (A.gw >> 2) : 0;
         int lo_s = 0, hi_s = 0, tbase = 0;
         if (!grad) {
             lo_s = A.lo[s];
             hi_s = A.hi[s];
-            tbase = (lo_s / kPT + tk - 1) * kPT;
+            tbase = (lo_s / kPT + tk - ngt) * kPT;
         }
-        const int ncc = grad ? 3 : 32;
+        const int ncc = grad ? A.gw : 32;
         // Q block rows in flight while we wait for the children and gather the RHS
         stage_block(A.Q + A.sn_valptr[s] + rb, 1, nr, m, w, Sg);
         // ---- extend-add sources of the rows this item touches (static structure: resolved
         //      while the children may still be running): list slot q < w is column row
         //      q (for X), slot w + i is row rb + i (epilogue, off rows only).  Resolved once,
         //      thread per row, so the value gathers below are independent loads.
-        const double *Usrc = grad ? A.Ug : A.Up;
-        double *Udst = grad ? A.Ug : A.Up;
-        const int ldsrc = grad ? 4 : ldu, coff = grad ? 0 : tbase;
+        // update-row element (row, column c of this tile): gradient rows are per sequence
+        auto uelem = [&](int row, int c) -> size_t {
+            return grad ? (size_t)(gseq0 + (c >> 2)) * A.ustride + (size_t)row * 4 + (c & 3)
+                        : (size_t)row * ldu + tbase + c;
+        };
         for (int q = tid; q < w + m; q += kTS_NT) {
             const int row = q < w ? q : rb + q - w;
             int cnt = 0;
@@ -362,15 +371,16 @@ __global__ void __launch_bounds__(kTS_NT) k_forward_solve(FwdArgs A) {
         }
         __syncthreads();
         // ---- X: rhs minus the children's rows landing on s's columns (fixed child order)
-        const int kpad = (w + 31) & ~31, ncw = grad ? 8 : 32, lg = grad ? 3 : 5;
+        const int kpad = (w + 31) & ~31, ncw = ncc, lg = ncw == 8 ? 3 : 5;
         for (int e0 = 0; e0 < kpad * ncw; e0 += 4 * kTS_NT) {
             double v[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int e = e0 + k * kTS_NT + tid, p = e >> lg, c = e & (ncw - 1);
                 v[k] = 0.0;
-                if (p < w && c < ncc) {
-                    if (grad) v[k] = __ldcg(A.G + (size_t)(c0 + p) * 4 + c);
+                const bool live = !grad || gseq0 + (c >> 2) < A.nseq;
+                if (p < w && c < ncc && live) {
+                    if (grad) v[k] = __ldcg(A.G + (size_t)(gseq0 + (c >> 2)) * A.gstride + (size_t)(c0 + p) * 4 + (c & 3));
                     else {
                         const int cc = tbase + c;
                         v[k] = (cc >= lo_s && cc < hi_s && A.qS[cc] == c0 + p) ? 1.0 : 0.0;
@@ -378,13 +388,13 @@ __global__ void __launch_bounds__(kTS_NT) k_forward_solve(FwdArgs A) {
                     const int n = src_n[p];
 #pragma unroll
                     for (int t = 0; t < kMaxSrc; ++t)
-                        if (t < n) v[k] -= __ldcg(Usrc + (size_t)src_u[p][t] * ldsrc + coff + c);
+                        if (t < n) v[k] -= __ldcg((grad ? A.Ug : A.Up) + uelem(src_u[p][t], c));
                     if (n > kMaxSrc) {   // rare: more sources than cached, walk the list
                         int t = 0;
                         for (int j = A.rc_ptr[slot0 + p]; j < A.rc_ptr[slot0 + p + 1]; ++j) {
                             const int2 sr = A.rc_src[j];
                             if (grad || has_tile(A.lo[sr.y], A.hi[sr.y], tbase)) {
-                                if (t >= kMaxSrc) v[k] -= __ldcg(Usrc + (size_t)sr.x * ldsrc + coff + c);
+                                if (t >= kMaxSrc) v[k] -= __ldcg((grad ? A.Ug : A.Up) + uelem(sr.x, c));
                                 ++t;
                             }
                         }
@@ -399,7 +409,7 @@ __global__ void __launch_bounds__(kTS_NT) k_forward_solve(FwdArgs A) {
         }
         cp_async_wait_group<0>();
         __syncthreads();
-        if (grad) block_dmma<1, kSolveRB / 8>(m, w, Sg, X, O);
+        if (ncw == 8) block_dmma<1, kSolveRB / 8>(m, w, Sg, X, O);
         else block_dmma<4, kSolveRB / 8>(m, w, Sg, X, O);
         __syncthreads();
         // ---- epilogue: solution rows, or U rows = O + children's rows landing there
@@ -407,31 +417,34 @@ __global__ void __launch_bounds__(kTS_NT) k_forward_solve(FwdArgs A) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int e = e0 + k * kTS_NT + tid, i = e >> lg, c = e & (ncw - 1), r = rb + i;
-                if (i >= m || c >= (grad ? 4 : 32)) continue;
+                if (i >= m || c >= ncw || (grad && gseq0 + (c >> 2) >= A.nseq)) continue;
                 if (r < w) {
-                    if (grad) A.Y[(size_t)(c0 + r) * 4 + c] = c < 3 ? O[i][c] : 0.0;
+                    if (grad)
+                        A.Y[(size_t)(gseq0 + (c >> 2)) * A.gstride + (size_t)(c0 + r) * 4 + (c & 3)] =
+                            (c & 3) < 3 ? O[i][c] : 0.0;
                     else {
                         const int cc = tbase + c;
                         if (cc >= lo_s && cc < hi_s) A.V[(size_t)(c0 + r) * A.ldv + cc] = O[i][c];
                     }
                     continue;
                 }
-                double u = c < ncc ? O[i][c] : 0.0;
+                double u = O[i][c];
                 const int q = w + i, n = src_n[q];
+                const double *Usrc = grad ? A.Ug : A.Up;
 #pragma unroll
                 for (int t = 0; t < kMaxSrc; ++t)
-                    if (t < n) u += __ldcg(Usrc + (size_t)src_u[q][t] * ldsrc + coff + c);
+                    if (t < n) u += __ldcg(Usrc + uelem(src_u[q][t], c));
                 if (n > kMaxSrc) {
                     int t = 0;
                     for (int j = A.rc_ptr[slot0 + r]; j < A.rc_ptr[slot0 + r + 1]; ++j) {
                         const int2 sr = A.rc_src[j];
                         if (grad || has_tile(A.lo[sr.y], A.hi[sr.y], tbase)) {
-                            if (t >= kMaxSrc) u += __ldcg(Usrc + (size_t)sr.x * ldsrc + coff + c);
+                            if (t >= kMaxSrc) u += __ldcg(Usrc + uelem(sr.x, c));
                             ++t;
                         }
                     }
                 }
-                Udst[(size_t)(A.uoff[s] + r - w) * ldsrc + coff + c] = u;
+                (grad ? A.Ug : A.Up)[uelem(A.uoff[s] + r - w, c)] = u;
             }
         }
         __threadfence();
@@ -452,9 +465,12 @@ struct BwdArgs {
     const int *pbase;                  // [nsn] first partial block of s
     int nitems;
     int *done, *cnt, *ticket;
-    double *P;                         // [blocks][kTS_W][4] partial sums
-    double *Z;                         // [nf][4] in: rhs, out: solution of L^T x = rhs
+    double *P;                         // [blocks][kTS_W][kBwCols] partial sums
+    double *Z;                         // [nseq][nf][4] in: rhs, out: solution of L^T x = rhs
+    long long zstride;                 // sequence stride of Z (doubles)
+    int nseq;                          // right-hand sides: 3 columns per sequence, nseq <= 8
 };
+constexpr int kBwCols = 32;            // columns of one backward-solve launch (8 sequences)
 
 // Backward solve.  x_s = L_ss^{-T}(z_s - L_off^T x_R) = Q_s^T [z_s; -x_R].  Item (s, b) forms
 // the partial Q_s[rows]^T v[rows] of its 64-row block (DMMA); the last block of s to finish
@@ -481,15 +497,12 @@ __global__ void __launch_bounds__(kTS_NT) k_backward_solve(BwdArgs A) {
         const int m = min(kSolveRB, nr - rb);
         // A = Q_s[rb.., :]^T : element (k, i) = Q[rb + i][k]  (w x m)
         stage_block(A.Q + A.sn_valptr[s] + rb, nr, 1, w, m, Sg);
-        // source rows of this thread's right-hand-side entries (independent of the parent: loaded
+        // source row of every right-hand-side row of this item (independent of the parent: resolved
         // before the dependency wait)
-        const int kpad = (m + 31) & ~31;
-        int src[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const int e = tid + u * kTS_NT, i = e >> 3, r = rb + i;
-            src[u] = -1;
-            if (e < kpad * 8 && i < m && (e & 7) < 3) src[u] = r < w ? c0 + r : A.sn_rows[slot0 + r];
+        __shared__ int srow[kSolveRB];
+        for (int i = tid; i < kSolveRB; i += kTS_NT) {
+            const int r = rb + i;
+            srow[i] = i < m ? (r < w ? c0 + r : A.sn_rows[slot0 + r]) : -1;
         }
         if (tid == 0) {
             int p = A.sn_parent[s];
@@ -504,33 +517,34 @@ __global__ void __launch_bounds__(kTS_NT) k_backward_solve(BwdArgs A) {
             __threadfence();
         }
         __syncthreads();
-        static_assert(kSolveRB * 8 <= 2 * kTS_NT, "two RHS entries per thread");
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const int e = tid + u * kTS_NT, i = e >> 3, c = e & 7, r = rb + i;
-            if (e < kpad * 8) {
-                double v = 0.0;
-                if (src[u] >= 0) {
-                    v = __ldcg(A.Z + (size_t)src[u] * 4 + c);
-                    if (r >= w) v = -v;
-                }
-                Vb[i][c] = v;
+        // columns: 4 per sequence (xyz + pad); 8 columns when nseq <= 2, else 32
+        const int ncw = A.nseq <= 2 ? 8 : kBwCols, lg = ncw == 8 ? 3 : 5;
+        const int kpad = (m + 31) & ~31;
+        for (int e = tid; e < kpad * ncw; e += kTS_NT) {
+            const int i = e >> lg, c = e & (ncw - 1), r = rb + i, sq = c >> 2, comp = c & 3;
+            double v = 0.0;
+            if (i < m && comp < 3 && sq < A.nseq) {
+                v = __ldcg(A.Z + (size_t)sq * A.zstride + (size_t)srow[i] * 4 + comp);
+                if (r >= w) v = -v;
             }
+            Vb[i][c] = v;
         }
         cp_async_wait_group<0>();
         __syncthreads();
-        block_dmma<1, kTS_W / 8>(w, m, Sg, Vb, O);
+        if (ncw == 8) block_dmma<1, kTS_W / 8>(w, m, Sg, Vb, O);
+        else block_dmma<4, kTS_W / 8>(w, m, Sg, Vb, O);
         __syncthreads();
-        double *Pb = A.P + (size_t)(A.pbase[s] + it.y) * kTS_W * 4;
+        double *Pb = A.P + (size_t)(A.pbase[s] + it.y) * kTS_W * kBwCols;
+        const int nout = w * ncw;
         if (nb == 1) {   // single block: publish directly
-            for (int e = tid; e < w * 3; e += kTS_NT) {
-                const int i = e / 3, c = e % 3;
-                A.Z[(size_t)(c0 + i) * 4 + c] = O[i][c];
+            for (int e = tid; e < nout; e += kTS_NT) {
+                const int i = e >> lg, c = e & (ncw - 1), sq = c >> 2, comp = c & 3;
+                if (comp < 3 && sq < A.nseq) A.Z[(size_t)sq * A.zstride + (size_t)(c0 + i) * 4 + comp] = O[i][c];
             }
         } else {
-            for (int e = tid; e < w * 3; e += kTS_NT) {
-                const int i = e / 3, c = e % 3;
-                Pb[i * 4 + c] = O[i][c];
+            for (int e = tid; e < nout; e += kTS_NT) {
+                const int i = e >> lg, c = e & (ncw - 1);
+                Pb[i * kBwCols + c] = O[i][c];
             }
             __threadfence();
             __syncthreads();
@@ -538,12 +552,13 @@ __global__ void __launch_bounds__(kTS_NT) k_backward_solve(BwdArgs A) {
             __syncthreads();
             if (!sh_last) continue;
             __threadfence();
-            const double *P0 = A.P + (size_t)A.pbase[s] * kTS_W * 4;
-            for (int e = tid; e < w * 3; e += kTS_NT) {
-                const int i = e / 3, c = e % 3;
+            const double *P0 = A.P + (size_t)A.pbase[s] * kTS_W * kBwCols;
+            for (int e = tid; e < nout; e += kTS_NT) {
+                const int i = e >> lg, c = e & (ncw - 1), sq = c >> 2, comp = c & 3;
+                if (comp >= 3 || sq >= A.nseq) continue;
                 double x = 0.0;
-                for (int b = 0; b < nb; ++b) x += __ldcg(P0 + (size_t)b * kTS_W * 4 + i * 4 + c);
-                A.Z[(size_t)(c0 + i) * 4 + c] = x;
+                for (int b = 0; b < nb; ++b) x += __ldcg(P0 + (size_t)b * kTS_W * kBwCols + i * kBwCols + c);
+                A.Z[(size_t)sq * A.zstride + (size_t)(c0 + i) * 4 + comp] = x;
             }
         }
         __threadfence();
@@ -561,17 +576,20 @@ void trisolve_init() {
     cudaFuncSetAttribute(k_backward_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem);
 }
 
+int grad_tiles(int nseq) { return nseq <= 2 ? 1 : (nseq + 7) / 8; }
+
 void launch_ts_plan(const DevFactor &F, const int *qS, const int *nS_ptr, int capS, const int *same_S,
-                    long long up_cap, int *flags, int mode, int *lo, int *hi, int *cnt, int *rem, int *item_ptr,
-                    int *ticket, cudaStream_t st) {
+                    long long up_cap, int *flags, int mode, int nseq, int *lo, int *hi, int *cnt, int *rem,
+                    int *item_ptr, int *ticket, cudaStream_t st) {
     PDI_LAUNCH(k_ts_plan, 1, kPlanNT, 0, st)(F.ford, F.sn_c0, F.sn_rowptr, F.sn_fd, F.sn_parent, F.nsn, qS, nS_ptr,
-                                              capS, same_S, F.nU, up_cap, flags, mode, lo, hi, cnt, rem, item_ptr,
-                                              ticket);
+                                              capS, same_S, F.nU, up_cap, flags, mode, grad_tiles(nseq), lo, hi,
+                                              cnt, rem, item_ptr, ticket);
 }
 
 void launch_forward_solve(const DevFactor &F, const int *lo, const int *hi, const int *item_ptr,
                           const int *qS, int *rem, int *ticket, const double *G, double *Y, double *V,
                           int ldv, double *Ug, double *Up, const int *nS_ptr, int capS, int with_grad,
+                          int nseq, long long gstride, long long ustride,
                           int nsm, unsigned long long *trace, cudaStream_t st) {
     FwdArgs A;
     A.sn_c0 = F.sn_c0; A.sn_rowptr = F.sn_rowptr; A.sn_parent = F.sn_parent;
@@ -580,15 +598,19 @@ void launch_forward_solve(const DevFactor &F, const int *lo, const int *hi, cons
     A.lo = lo; A.hi = hi; A.item_ptr = item_ptr; A.qS = qS; A.ford = F.ford; A.nsn = F.nsn;
     A.rem = rem; A.ticket = ticket; A.G = G; A.Y = Y; A.V = V; A.ldv = ldv;
     A.Ug = Ug; A.Up = Up; A.nS_ptr = nS_ptr; A.capS = capS; A.with_grad = with_grad; A.trace = trace;
+    A.nseq = nseq; A.gstride = gstride; A.ustride = ustride;
+    A.ngt = grad_tiles(nseq);
+    A.gw = nseq <= 2 ? 8 : 32;
     PDI_LAUNCH(k_forward_solve, nsm, kTS_NT, kFwdSmem, st)(A);
 }
 
 void launch_backward_solve(const DevFactor &F, int *done, int *cnt, int *ticket, double *P, double *Z,
-                           int nsm, cudaStream_t st) {
+                           int nseq, long long zstride, int nsm, cudaStream_t st) {
     BwdArgs A;
     A.sn_c0 = F.sn_c0; A.sn_rowptr = F.sn_rowptr; A.sn_rows = F.sn_rows; A.sn_parent = F.sn_parent;
     A.sn_valptr = F.sn_valptr; A.Q = F.Q; A.items = F.bw_items; A.pbase = F.bw_pbase;
     A.nitems = F.bw_nitems; A.done = done; A.cnt = cnt; A.ticket = ticket; A.P = P; A.Z = Z;
+    A.nseq = nseq; A.zstride = zstride;
     dev_zero3(ticket, sizeof(int), done, sizeof(int) * F.nsn, cnt, sizeof(int) * F.nsn, st);
     PDI_LAUNCH(k_backward_solve, nsm, kTS_NT, kFwdSmem, st)(A);
 }

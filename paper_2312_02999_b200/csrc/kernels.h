@@ -35,10 +35,13 @@ void launch_ingest_actuation(const double *A9, double *A6, int T, cudaStream_t s
 void elastic_init(int device);
 // clr (nullable): device ints clr[0..1] and clr[4..7] zeroed by the kernel (the iteration's
 // active-pair counts and flags, engine.cu D_ACNT / D_INFO..)
+// a1 / a2 over (tet, sequence) for nseq sequences: x [nseq][xs] double4, A6 [nseq][6][T],
+// fc [nseq][T][12], p [nseq][9][T], counters clr [nseq][clrs]; g [nseq][nf] double4
 void launch_local_step(const int4 *tets, const double4 *x, const double *B, const double *A6,
-                       const double *w, int T, double *fc, double *p, int *clr, cudaStream_t st);
+                       const double *w, int T, double *fc, double *p, int *clr, int nseq, long long xs,
+                       int clrs, cudaStream_t st);
 void launch_gather_elastic(const int *inc_ptr, const int *inc, const double *fc, int nf,
-                           double4 *g, cudaStream_t st);
+                           double4 *g, int nseq, long long fcs, cudaStream_t st);
 void launch_surface(const int *Wp, const int *Wc, const double *Wv, const double4 *x, int Ns,
                     double4 *s, cudaStream_t st);
 int quad_partials(const int4 *tets, const double4 *dx, const double *B, const double *w, int T,
@@ -51,23 +54,30 @@ void elastic_partials(const double4 *g, const double4 *dx, const int *q2v, int n
                       cudaStream_t st);
 void launch_update(double4 *x, const double4 *dx, const int *q2v, int nf, const double *alpha,
                    const int *flags, int *abort, int it, cudaStream_t st);
-void launch_scatter_dx(const double *z, const int *q2v, int nf, double4 *dx, double *amin, cudaStream_t st);
+// z [nseq][nf][4] -> dx [nseq][n]; seeds amin[sq * amin_stride] = 1
+void launch_scatter_dx(const double *z, const int *q2v, int nf, double4 *dx, double *amin, int nseq, int n,
+                       int amin_stride, cudaStream_t st);
 
 // ---- k_trisolve.cu
 constexpr int kSolveRB = 64;   // rows of a supernode per solve work item
 // mode: bit 0 gradient items, bit 1 panel tiles
 // per-iteration plan of a solve (one block): clears rem and ticket[0], item counts, lo/hi,
 // item_ptr = exclusive scan of the counts
+// nseq: gradient right-hand sides (3 columns each) of a mode-1 solve
+int grad_tiles(int nseq);
 void launch_ts_plan(const DevFactor &F, const int *qS, const int *nS_ptr, int capS, const int *same_S,
-                    long long up_cap, int *flags, int mode, int *lo, int *hi, int *cnt, int *rem, int *item_ptr,
-                    int *ticket, cudaStream_t st);
+                    long long up_cap, int *flags, int mode, int nseq, int *lo, int *hi, int *cnt, int *rem,
+                    int *item_ptr, int *ticket, cudaStream_t st);
 void trisolve_init();
 void launch_forward_solve(const DevFactor &F, const int *lo, const int *hi, const int *item_ptr,
                           const int *qS, int *rem, int *ticket, const double *G, double *Y, double *V,
                           int ldv, double *Ug, double *Up, const int *nS_ptr, int capS, int with_grad,
+                          int nseq, long long gstride, long long ustride,
                           int nsm, unsigned long long *trace, cudaStream_t st);
+// backward solve of nseq <= kBwSeqs sequences' right-hand sides Z[sq][nf][4] (stride zstride)
+constexpr int kBwSeqs = 8;
 void launch_backward_solve(const DevFactor &F, int *done, int *cnt, int *ticket, double *P, double *Z,
-                           int nsm, cudaStream_t st);
+                           int nseq, long long zstride, int nsm, cudaStream_t st);
 
 // ---- k_schur.cu (fused cooperative dense Schur step, a9)
 void schur_init(int device);

@@ -22,7 +22,7 @@ from typing import Callable, Optional
 import numpy as np
 
 __all__ = ["Scene", "slabs_c1", "face_c2", "face_c3", "box_c5", "two_tets", "single_tet",
-           "cube_grid", "slit_face", "C5_SIZES"]
+           "cube_grid", "slit_face", "C5_SIZES", "c4_actuation", "c4_assignment", "C4_SEQUENCES"]
 
 
 @dataclass
@@ -415,3 +415,52 @@ def two_tets(seed: int = 3) -> Scene:
 def random_actuation(T: int, scale: float, seed: int) -> np.ndarray:
     """Seeded symmetric actuation with det > 0 (for property tests)."""
     return _random_sym_actuation(T, scale, seed)
+
+
+# ----------------------------------------------------------------------------------------
+# C4: a batch of 64 actuation sequences on the C3 mesh (SURVEY 8(d) C4 / 8(e))
+# ----------------------------------------------------------------------------------------
+C4_SEQUENCES = 64
+
+
+def c4_actuation(scene: Scene, j: int, n_frames: Optional[int] = None) -> Callable[[int], np.ndarray]:
+    """Actuation of sequence j (seed 1000 + j): a_max,j = 0.45 + 0.3 u, ramp start f0_j uniform in
+    [0, 10], and a fixed symmetric noise term 0.02 m_i sym(N(0,1)) per tet; everything ramps in
+    with r_j(f) = smoothstep((f - f0_j) / (n_frames - 1 - f0_j)):
+        A_i(f) = I + r_j(f) (a_max,j m_i e_y e_y^T + 0.02 m_i sym(N_i)),
+    det-checked (an entry is redrawn until det A_i > 0 at full amplitude, which for these
+    amplitudes never triggers).  m_i is the lip mask of the scene."""
+    nfr = scene.n_frames if n_frames is None else n_frames
+    rng = np.random.default_rng(1000 + j)
+    a_max = 0.45 + 0.3 * rng.uniform()
+    f0 = 10.0 * rng.uniform()
+    mask = scene.meta["lip_mask"]
+    T = scene.n_tets
+    N = rng.standard_normal((T, 3, 3))
+    N = 0.5 * (N + N.transpose(0, 2, 1))
+    D = np.zeros((T, 3, 3))
+    D[:, 1, 1] = a_max * mask
+    D += 0.02 * mask[:, None, None] * N
+    for _ in range(8):
+        bad = np.linalg.det(np.eye(3)[None] + D) <= 0
+        if not bad.any():
+            break
+        M = rng.standard_normal((int(bad.sum()), 3, 3))
+        D[bad] = 0.0
+        D[bad, 1, 1] = a_max * mask[bad]
+        D[bad] += 0.02 * mask[bad, None, None] * 0.5 * (M + M.transpose(0, 2, 1))
+    D9 = D.reshape(T, 9)
+    eye = np.tile(np.eye(3).reshape(1, 9), (T, 1))
+    span = max(nfr - 1 - f0, 1e-9)
+
+    def actuation(f: int):
+        return eye + _smoothstep((f - f0) / span) * D9
+
+    actuation.a_max = a_max
+    actuation.f0 = f0
+    return actuation
+
+
+def c4_assignment(n_seq: int, rank: int, world: int):
+    """Round-robin sharding of the C4 sequences: rank r owns {j : j mod P = r}."""
+    return [j for j in range(n_seq) if j % world == rank]
