@@ -1,22 +1,29 @@
 #!/usr/bin/env python
 """Benchmark of the PD+IPC iteration (arXiv 2312.02999) on B200: prints ONE JSON line.
 
-Workload (BASELINE.json configs[1]): synthetic face-like block of 47.5k tets
-with a mouth slit, lips closing under actuation, 60 frames x 20 PD+IPC iterations.  A bench
-"step" is one frame = 20 iterations of the whole hot path (local step, gather, broad/narrow
-phase, contact assembly, contact-reduced global solve, CCD, line search, update).  The timed
-frames are taken from the contact regime of the sequence (frames before it run untimed as
-setup / warm-up, because frames are sequential: each starts from the previous equilibrium).
+Headline workload (BASELINE.json configs[3]): the batch of 64 seeded
+actuation sequences on the ~300k-tet two-slit face mesh (C3), sharded round-robin over the P
+GPUs (rank r owns sequences j = r mod P).  Each rank runs its sequences in LOCKSTEP in one
+handle.  A bench "step" is one pass of the whole hot path (local step, gather, broad/narrow
+phase, contact assembly, contact-reduced global solve, CCD, line search, update) over the rank's
+batch, i.e. one PD+IPC iteration of every sequence it owns; 20 steps = one frame.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Multi-GPU (torchrun): one process per GPU, each rank simulates its own actuation sequence
-(independent problems, no data-path collective: weak scaling); NCCL only carries the
-per-rank timing / statistics; value = total iterations of all ranks / max-over-ranks time.
+Per sequence j: untimed preparation = PREP_ITERS iterations from rest under the frame-(F-1)
+actuation (the frame-(F-1) equilibrium), then W warm-up steps continuing that frame, then the
+K timed steps under the frame-F actuation (F = TIMED_FRAME), warm-started.  The frame subset and
+the per-sequence inputs are identical for every P.  value = all ranks' sequence-iterations /
+max-over-ranks device time (weak scaling over sequences, no data-path collective); NCCL
+all-gathers the per-rank times, statistics and per-sequence position checksums.
+
+Extra fields: C3 single sequence (configs[2]), C2 (configs[1]) and the C5 1M-tet pure-PD
+local-step / gather HBM roofline (configs[4]).
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
@@ -29,21 +36,26 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 ITERS_PER_FRAME = 20
-TIMED_GROUPS = ["local_step", "dense_schur"]      # the two roofline kernels (timers cost time)
-N_FRAMES = 60
-CONTACT_START = 20          # first frame of the timed window (lips in contact from ~frame 20)
+N_SEQ = 64                 # C4 batch
+TIMED_FRAME = 30           # F: every sequence is ramped and in contact by frame 30
+PREP_ITERS = 20            # untimed iterations from rest under the frame-(F-1) actuation
+C2_FRAMES = 60
+C2_CONTACT_START = 20
 
 
 def _args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--seqs", type=int, default=N_SEQ, help="C4 batch size (64 = BASELINE configs[3])")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--c5", default="1M", help="pure-PD box size for the local-step HBM sweep ('' to skip)")
+    ap.add_argument("--no-extras", action="store_true", help="skip the C3-single / C2 / C5 fields")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--ref-seconds", type=float, default=150.0)
+    ap.add_argument("--c5", default="1M", help="pure-PD box size for the local-step HBM field ('' to skip)")
     return ap.parse_args()
 
 
@@ -56,31 +68,12 @@ def _peaks():
         return 6650.0, 1590.0, "fallback"
 
 
-def _c5_local_step(size, hbm):
-    """Local-step and gather HBM GB/s on the pure-PD box of BASELINE.json configs[4] (the metric's
-    'local-step HBM GB/s' at a size where the step is bandwidth-relevant; C2 is latency-bound)."""
-    import importlib.util
-    spec = importlib.util.spec_from_file_location("c5_sweep", os.path.join(ROOT, "tools", "c5_sweep.py"))
-    mod = importlib.util.module_from_spec(spec)
-    spec.loader.exec_module(mod)
-    r = mod.run(size)
-    return {"workload": f"C5 pure-PD box {size} ({r['tets']} tets, {r['verts']} verts), 20-iteration steps",
-            "local_step_GBps": r["local_step_GBps"], "local_step_frac": r["local_step_GBps"] / hbm,
-            "gather_GBps": r["gather_GBps"], "gather_frac": r["gather_GBps"] / hbm,
-            "pure_pd_iters_per_s": r["iters_per_s"], "peak_GBps": hbm,
-            "bytes_per_tet": "local 240 (+32 per vertex), gather 28 per incidence + 40 per free vertex"}
-
-
 def _sm_max_mhz():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             return float(json.load(f)["sm_max_mhz"])
     except Exception:
         return 1965.0
-
-
-def _frame_index(f):
-    return min(f, N_FRAMES - 1)
 
 
 # ------------------------------------------------------------------------------ clocks -----
@@ -126,89 +119,19 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-# ------------------------------------------------------------------------------ oracle -----
-_CPU_SCRIPT = r"""
-import json, sys, time
-import numpy as np
-sys.path.insert(0, sys.argv[1])
-import scenes
-from oracle import OracleSolver
-sc = scenes.face_c2()
-x = np.load(sys.argv[2])
-frame = int(sys.argv[3]); budget = float(sys.argv[4])
-o = OracleSolver(sc)
-A = sc.actuation(frame)
-t0 = time.perf_counter(); n = 0
-while True:
-    it = o.iterate(x, A); x = it["x"]; n += 1
-    if time.perf_counter() - t0 >= budget: break
-dt = time.perf_counter() - t0
-print(json.dumps({"iters": n, "seconds": dt, "n_active": it["n_pt"] + it["n_ee"], "n_S": int(it["S"].size)}))
-"""
+def _host_info():
+    model = ""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "lscpu_model": model}
 
 
-def cpu_baseline(x_state, frame, budget):
-    """The oracle as it stands, single thread, on a bounded sample of the same workload."""
-    env = dict(os.environ, OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1",
-               NUMEXPR_NUM_THREADS="1", CUDA_VISIBLE_DEVICES="")
-    with tempfile.TemporaryDirectory() as td:
-        xp = os.path.join(td, "x.npy")
-        import numpy as np
-        np.save(xp, x_state)
-        sp = os.path.join(td, "cpu.py")
-        with open(sp, "w") as f:
-            f.write(_CPU_SCRIPT)
-        r = subprocess.run([sys.executable, sp, ROOT, xp, str(frame), str(budget)], env=env,
-                           capture_output=True, text=True, timeout=600)
-    if r.returncode != 0:
-        return {"value": None, "unit": "iters/s", "cores": 1, "kind": "oracle",
-                "sample": "failed: " + r.stderr.strip().splitlines()[-1][:200]}
-    d = json.loads(r.stdout.strip().splitlines()[-1])
-    return {"value": d["iters"] / d["seconds"], "unit": "iters/s", "cores": 1, "kind": "oracle",
-            "sample": f"{d['iters']} oracle iterations of C2 frame {frame} from the GPU state at the "
-                      f"start of the timed window ({d['seconds']:.1f} s, |C| {d['n_active']}, "
-                      f"n_c {d['n_S']}); full sparse LU of H-hat per iteration, 1 thread"}
-
-
-# ------------------------------------------------------------------------------ reference --
-def run_reference(a):
-    """--impl reference: the CPU oracle, timed as it stands, on this arm's config and metric."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
-    import numpy as np
-    import scenes
-    from oracle import OracleSolver
-    sc = scenes.face_c2()
-    o = OracleSolver(sc)
-    frame = CONTACT_START + 10
-    A = sc.actuation(frame)
-    x = sc.rest.copy()
-    for _ in range(a.warmup):
-        x = o.iterate(x, A)["x"]
-    t0 = time.perf_counter()
-    for _ in range(a.steps):
-        it = o.iterate(x, A)
-        x = it["x"]
-    dt = time.perf_counter() - t0
-    v = a.steps / dt
-    line = {"impl": "reference", "metric": "PD+IPC iterations/s", "value": v, "unit": "iters/s",
-            "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1000 * dt / a.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "frames_per_sec": v / ITERS_PER_FRAME,
-            "config": {"workload": "C2: face-like 47.5k-tet block, mouth-slit lip contact "
-                                   "(BASELINE.json configs[1])",
-                       "step": "one oracle PD+IPC iteration (bounded sample)",
-                       "sample": f"frame-{frame} actuation applied from rest; {a.warmup} untimed + "
-                                 f"{a.steps} timed iterations"},
-            "cpu_baseline": {"value": v, "unit": "iters/s", "cores": 1, "kind": "oracle",
-                             "sample": f"{a.steps} oracle iterations (|C| {it['n_pt'] + it['n_ee']}, "
-                                       f"n_c {int(it['S'].size)})"},
-            "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
-
-
-# ------------------------------------------------------------------------------ ours -------
+# ------------------------------------------------------------------------------ host logic -
 def gather_rank_values(vals, world, device):
     """All ranks' per-rank measurements as a (world, len(vals)) array (NCCL on the GPU path; any
     backend works).  The job's time is the max over ranks of the device-timed region."""
@@ -222,160 +145,146 @@ def gather_rank_values(vals, world, device):
     return mine.cpu().numpy()[None]
 
 
-def job_throughput(per_rank_ms, world, steps, iters_per_step=ITERS_PER_FRAME):
-    """Whole-job iterations/s: every rank ran `steps` frames of its own sequence (weak scaling);
-    the job took the slowest rank's time."""
-    return world * steps * iters_per_step / (max(per_rank_ms) / 1000.0)
+def job_throughput(per_rank_ms, units_per_rank):
+    """Whole-job throughput: every rank processed units_per_rank[r] sequence-iterations (weak
+    scaling over sequences); the job took the slowest rank's time."""
+    return float(sum(units_per_rank)) / (max(per_rank_ms) / 1000.0)
 
 
-def run_ours(a):
+def seq_checksum(x):
+    """64-bit checksum of a sequence's positions (float64 bytes), for the cross-P determinism check."""
     import numpy as np
+    return int.from_bytes(hashlib.sha256(np.ascontiguousarray(x, dtype=np.float64).tobytes()).digest()[:7], "little")
+
+
+def gather_checksums(pairs, world, device, n_seq):
+    """{sequence j: checksum} over all ranks (all_gather of a dense [n_seq] vector, 0 = not mine)."""
     import torch
     import torch.distributed as dist
+    v = torch.zeros(n_seq, dtype=torch.int64, device=device)
+    for j, c in pairs:
+        v[j] = c
+    if world > 1:
+        allv = [torch.zeros_like(v) for _ in range(world)]
+        dist.all_gather(allv, v)
+        v = torch.stack(allv).sum(0)
+    return {j: int(c) for j, c in enumerate(v.cpu().tolist())}
 
-    import scenes
-    from paper_2312_02999_b200 import pd_ipc as P
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+def combined_checksum(by_seq):
+    """One hex digest over all sequences in j order: equal across P iff every trajectory is."""
+    h = hashlib.sha256()
+    for j in sorted(by_seq):
+        h.update(int(by_seq[j]).to_bytes(8, "little"))
+    return h.hexdigest()[:16]
+
+
+# ------------------------------------------------------------------------------ oracle -----
+_CPU_SCRIPT = r"""
+import json, sys, time
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import scenes
+from oracle import OracleSolver
+sc = scenes.face_c3()
+x = np.load(sys.argv[2])
+j = int(sys.argv[3]); frame = int(sys.argv[4]); budget = float(sys.argv[5])
+o = OracleSolver(sc)
+A = scenes.c4_actuation(sc, j)(frame)
+t0 = time.perf_counter(); n = 0
+while True:
+    it = o.iterate(x, A); x = it["x"]; n += 1
+    if time.perf_counter() - t0 >= budget: break
+dt = time.perf_counter() - t0
+print(json.dumps({"iters": n, "seconds": dt, "n_active": it["n_pt"] + it["n_ee"], "n_S": int(it["S"].size),
+                  "timers": o.timers}))
+"""
+
+
+def cpu_baseline(x_state, j, frame, budget):
+    """The oracle as it stands, single thread, on a bounded sample of the same workload: whole
+    iterations of C4 sequence j from the GPU state at the start of the timed region, until the
+    budget is used (at least one)."""
+    env = dict(os.environ, OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1",
+               NUMEXPR_NUM_THREADS="1", CUDA_VISIBLE_DEVICES="")
+    with tempfile.TemporaryDirectory() as td:
+        import numpy as np
+        xp = os.path.join(td, "x.npy")
+        np.save(xp, x_state)
+        sp = os.path.join(td, "cpu.py")
+        with open(sp, "w") as f:
+            f.write(_CPU_SCRIPT)
+        r = subprocess.run([sys.executable, sp, ROOT, xp, str(j), str(frame), str(budget)], env=env,
+                           capture_output=True, text=True, timeout=1800)
+    hi = _host_info()
+    if r.returncode != 0:
+        return {"value": None, "unit": "iters/s", "cores": 1, "kind": "oracle", **hi,
+                "sample": "failed: " + (r.stderr.strip().splitlines() or ["?"])[-1][:200]}
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    return {"value": d["iters"] / d["seconds"], "unit": "iters/s", "cores": 1, "kind": "oracle", **hi,
+            "threads_used": 1,
+            "sample": f"{d['iters']} oracle iteration(s) of C4 sequence {j}, frame {frame}, from the GPU state "
+                      f"at the start of the timed region ({d['seconds']:.1f} s, |C| {d['n_active']}, "
+                      f"n_c {d['n_S']}); full sparse LU of H-hat per iteration, 1 thread",
+            "stage_s": {k: round(v, 2) for k, v in d["timers"].items()}}
+
+
+# ------------------------------------------------------------------------------ reference --
+def run_reference(a):
+    """--impl reference: the CPU oracle as it stands, on this arm's config (C4) and metric.
+
+    A step of the oracle is one iteration of one C4 sequence (the batch's sequences are
+    independent, so the rate per sequence-iteration is the batch rate).  One oracle iteration at
+    this size refactorises the full 180k-DOF H-hat (tens of seconds), so the run is bounded in
+    time: at most min(W, 1) warm-up and K timed iterations, stopping after --ref-seconds; the
+    line states the counts actually run."""
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    sc = scenes.face_c2()
-    T, n = sc.n_tets, sc.n_verts
-    frames_host = np.stack([sc.actuation(f) for f in range(N_FRAMES)])      # (60, T, 9)
-    frames_dev = torch.from_numpy(frames_host).to(f"cuda:{local}")
-    K, W = a.steps, a.warmup
-    start = max(CONTACT_START, W)
-    timed = [start + i for i in range(K)]
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")   # 256 MB
-
-    # ---------------- device-resident run (value)
-    s = P.Solver(sc, A=frames_host[0][None], device=local, A_on_device=True)
-    for f in range(start - W):                                   # untimed setup frames
-        s.step(A_device_ptr=frames_dev[_frame_index(f)].data_ptr(), n_iters=ITERS_PER_FRAME)
-    for f in range(start - W, start):                            # warm-up frames
-        s.step(A_device_ptr=frames_dev[_frame_index(f)].data_ptr(), n_iters=ITERS_PER_FRAME)
-    x_start = s.positions()
-    # live CUDA-event timers in the timed region only around the kernel groups the roofline needs
-    # (an event pair per group per iteration is a graph node: timing every group costs ~15%)
-    P.set_timing(s.h, True, groups=TIMED_GROUPS)
-    P.kernel_times(s.h, reset=True)
-    clocks = ClockSampler(local)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in timed]
-    stats_log = []
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clocks.start()
-    l0 = P.launch_count()
-    t_wall = time.perf_counter()
-    torch.cuda.nvtx.range_push("timed")                          # ncu --nvtx-include timed/
-    for i, f in enumerate(timed):
-        flush.fill_(float(i))                                    # evict L2 between steps
-        ev[i][0].record()
-        st = s.step(A_device_ptr=frames_dev[_frame_index(f)].data_ptr(), n_iters=ITERS_PER_FRAME)
-        ev[i][1].record()
-        stats_log.append(st[0])
-    torch.cuda.nvtx.range_pop()
-    torch.cuda.synchronize()
-    t_wall = time.perf_counter() - t_wall
-    launches = P.launch_count() - l0
-    if world > 1:
-        dist.barrier()
-    clk = clocks.stop()
-    step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
-    my_ms = float(sum(step_ms))
-    ktimes = P.kernel_times(s.h, reset=True)
-    # stage breakdown: every group timed, in a separate 2-frame pass after the timed region
-    P.set_timing(s.h, True)
-    for f in range(timed[-1] + 1, timed[-1] + 3):
-        s.step(A_device_ptr=frames_dev[_frame_index(f)].data_ptr(), n_iters=ITERS_PER_FRAME)
-    stages = P.kernel_times(s.h, reset=True)
-    s.close()
-
-    # ---------------- end-to-end through the C ABI with host buffers
-    e2e = None
-    if not a.no_e2e:
-        pin = torch.empty((N_FRAMES, T, 9), dtype=torch.float64, pin_memory=True)
-        pin.copy_(torch.from_numpy(frames_host))
-        pin_np = pin.numpy()
-        xout = torch.empty((n, 3), dtype=torch.float64, pin_memory=True).numpy()
-        s2 = P.Solver(sc, A=frames_host[0][None], device=local)
-        for f in range(start):
-            s2.step(A_next=pin_np[_frame_index(f)][None], n_iters=ITERS_PER_FRAME)
-        ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in timed]
-        torch.cuda.synchronize()
-        for i, f in enumerate(timed):
-            flush.fill_(float(i))
-            ev2[i][0].record()
-            s2.step(A_next=pin_np[_frame_index(f)][None], n_iters=ITERS_PER_FRAME)
-            P.lib.pd_ipc_positions(s2.h, 0, xout.ctypes.data_as(P.C.POINTER(P.C.c_double)))
-            ev2[i][1].record()
-        torch.cuda.synchronize()
-        e2e_ms = float(sum(e0.elapsed_time(e1) for e0, e1 in ev2))
-        s2.close()
-        e2e = {"ms": e2e_ms, "h2d": T * 9 * 8, "d2h": n * 3 * 8}
-
-    # ---------------- gather over ranks
-    allv = gather_rank_values([my_ms, e2e["ms"] if e2e else 0.0], world, f"cuda:{local}")
-    max_ms, max_e2e = float(allv[:, 0].max()), float(allv[:, 1].max())
     if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
         return
-
-    iters_total = world * K * ITERS_PER_FRAME
-    value = job_throughput(allv[:, 0], world, K)
-    hbm, bf16, peak_src = _peaks()
-    sm_max = _sm_max_mhz()
-    # ---- roofline: dominant kernel group (live CUDA-event timings) and the local step
-    name_dom = max(TIMED_GROUPS, key=lambda k: ktimes.get(k, (0.0, 0))[0])
-    n_iter_timed = K * ITERS_PER_FRAME
-    nS_mean = statistics.mean(st["n_S"] for st in stats_log)
-    rl = _roofline(name_dom, ktimes, sc, hbm, sm_max, peak_src, stats_log)
-    rl_local = _roofline("local_step", ktimes, sc, hbm, sm_max, peak_src, stats_log)
-    cpu = None
-    if world == 1 and not a.no_cpu_baseline:
-        cpu = cpu_baseline(x_start, start, a.cpu_seconds)
-    c5 = None
-    if world == 1 and a.c5:
-        c5 = _c5_local_step(a.c5, hbm)
-    line = {
-        "metric": "PD+IPC iterations/s", "value": value, "unit": "iters/s", "n_gpus": world,
-        "steps": K, "warmup": W, "ms_per_step": max_ms / K, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded generator, SURVEY.md 8(d) C2)",
-        "frames_per_sec": world * K / (max_ms / 1000.0),
-        "config": {"workload": "C2: face-like 47.5k-tet block, mouth-slit lip contact, 60 frames x "
-                               "20 iterations (BASELINE.json configs[1])",
-                   "tets": T, "verts": n, "surface_tris": int(sc.surf_tris.shape[0]),
-                   "step": "one frame = 20 PD+IPC iterations",
-                   "timed_frames": f"{timed[0]}..{timed[-1]} (contact regime; frames 0..{start - W - 1} "
-                                   f"untimed setup, {start - W}..{start - 1} warm-up)",
-                   "sequences_per_gpu": 1, "l2": "flushed between steps (256 MB write, outside the "
-                                                 "per-step CUDA events)",
-                   "parallelism": f"dp{world} over independent sequences"},
-        "roofline": rl, "roofline_local_step": rl_local,
-        "local_step_c5": c5,
-        "cpu_baseline": cpu,
-        "e2e": ({"value": iters_total / (max_e2e / 1000.0), "unit": "iters/s",
-                 "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"]} if e2e else None),
-        "gpu_launches": launches,
-        "clocks": clk,
-        "stage_ms_per_iter": {k: v[0] / max(v[1], 1) for k, v in stages.items() if v[1]},
-        "stage_note": "stage_ms_per_iter from a separate 2-frame pass with every group timed; the timed "
-                      "region times only " + ", ".join(TIMED_GROUPS),
-        "n_c_mean": nS_mean, "n_active_last": stats_log[-1]["n_active"],
-        "sigma_reuse_frac": sum(st["sigma_reused"] for st in stats_log) / float(K * ITERS_PER_FRAME),
-        "alpha_last": stats_log[-1]["alpha"], "wall_s": t_wall,
-    }
+    import scenes
+    from oracle import OracleSolver
+    sc = scenes.face_c3()
+    j = 0
+    act = scenes.c4_actuation(sc, j)
+    o = OracleSolver(sc)
+    x = sc.rest.copy()
+    t_all = time.perf_counter()
+    w_done = 0
+    for _ in range(min(a.warmup, 1)):
+        x = o.iterate(x, act(TIMED_FRAME - 1))["x"]
+        w_done += 1
+    A = act(TIMED_FRAME)
+    t0 = time.perf_counter()
+    n = 0
+    it = None
+    while n < a.steps:
+        it = o.iterate(x, A)
+        x = it["x"]
+        n += 1
+        if time.perf_counter() - t_all >= a.ref_seconds:
+            break
+    dt = time.perf_counter() - t0
+    v = n / dt
+    hi = _host_info()
+    line = {"impl": "reference", "metric": "PD+IPC iterations/s", "value": v, "unit": "iters/s",
+            "n_gpus": a.gpus, "steps": n, "warmup": w_done, "steps_requested": a.steps,
+            "warmup_requested": a.warmup, "ms_per_step": 1000 * dt / n,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator, SURVEY.md 8(d) C4)", "frames_per_sec": v / ITERS_PER_FRAME,
+            "config": {"workload": "C4: 64 actuation sequences on the ~300k-tet two-slit face (C3 mesh) "
+                                   "(BASELINE.json configs[3])",
+                       "step": "one oracle PD+IPC iteration of one sequence (bounded sample)",
+                       "sample": f"sequence {j}: {w_done} warm-up iteration(s) from rest under the frame-"
+                                 f"{TIMED_FRAME - 1} actuation, then {n} timed iteration(s) under frame "
+                                 f"{TIMED_FRAME} (time-bounded at {a.ref_seconds:.0f} s)"},
+            "cpu_baseline": {"value": v, "unit": "iters/s", "cores": 1, "kind": "oracle", **hi,
+                             "sample": f"{n} oracle iteration(s) (|C| {it['n_pt'] + it['n_ee']}, "
+                                       f"n_c {int(it['S'].size)})"},
+            "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
 
 
+# ------------------------------------------------------------------------------ rooflines --
 # FP64 tensor (DMMA, mma.sync.m8n8k4.f64) throughput measured on this pool's B200 by
 # tools/micro/fp64_peaks.cu: 128 flop/clk/SM (profiles/fp64_peaks_r01.txt).  tcgen05 has no
 # f64 kind, so this is the FP64 contraction peak; x 148 SMs x the max SM clock.
@@ -396,40 +305,309 @@ def _traffic(kernel):
     return None
 
 
-def _roofline(name, ktimes, sc, hbm, sm_max_mhz, peak_src, stats_log):
-    """Achieved = algorithmic bytes (flops) per launch / average launch duration."""
-    ms, cnt = ktimes.get(name, (0.0, 0))
-    if cnt == 0 or ms <= 0:
-        return None
-    avg_s = ms / cnt / 1000.0
+def _fp64_peak(sm_max_mhz):
+    return DMMA_FLOP_PER_CLK_SM * N_SM * sm_max_mhz * 1e6 / 1e12
+
+
+def rooflines(kt, info, nb, nS_list, reuse_frac, hbm, sm_max_mhz, peak_src):
+    """Per kernel group: achieved = ALGORITHMIC bytes (flops) per launch / average launch time
+    (live CUDA events), DESIGN.md section 5.  kt: {group: (ms, launches)}; nb sequences per
+    lockstep iteration; nS_list: n_c of every sequence."""
+    out = {}
+    T, n, nf, nnzL = info["n_tets"], info["n_verts"], info["n_free"], info["nnz_L"]
+
+    def avg(k):
+        ms, c = kt.get(k, (0.0, 0))
+        return (ms / c / 1000.0, c) if c else (None, 0)
+
+    t, _ = avg("local_step")
+    if t:   # per tet: ids 16 + B 72 + w 8 once; per (tet, seq): A 48 + forces 96; x 32 per vertex and seq
+        b = T * (16 + 72 + 8) + nb * (T * (48 + 96) + n * 32)
+        out["local_step"] = {"bound": "hbm", "achieved": b / t / 1e9, "peak": hbm, "unit": "GB/s",
+                             "frac": b / t / 1e9 / hbm, "bytes_per_launch": b, "avg_launch_us": t * 1e6}
+    t, _ = avg("gather")
+    if t:
+        b = nb * (nf * (8 + 32) + 4 * T * (4 + 24))
+        out["gather"] = {"bound": "hbm", "achieved": b / t / 1e9, "peak": hbm, "unit": "GB/s",
+                         "frac": b / t / 1e9 / hbm, "bytes_per_launch": b, "avg_launch_us": t * 1e6}
+    t, _ = avg("w_el_forward")
+    if t:   # the factor (Q blocks, nnz(L) doubles) read once + 3 nb right-hand sides in / out
+        b = nnzL * 8 + nb * nf * 32 * 2
+        out["w_el_forward"] = {"bound": "hbm", "achieved": b / t / 1e9, "peak": hbm, "unit": "GB/s",
+                               "frac": b / t / 1e9 / hbm, "bytes_per_launch": b, "avg_launch_us": t * 1e6,
+                               "note": "one launch solves all nb sequences' gradients; dependency-depth bound"}
+    t, _ = avg("backward_solve")
+    if t:   # one timer spans the ceil(nb/8) backward launches of an iteration
+        nl = (nb + 7) // 8
+        b = nl * nnzL * 8 + nb * nf * 32 * 2
+        out["backward_solve"] = {"bound": "hbm", "achieved": b / t / 1e9, "peak": hbm, "unit": "GB/s",
+                                 "frac": b / t / 1e9 / hbm, "bytes_per_iteration": b, "avg_iteration_us": t * 1e6,
+                                 "launches_per_iteration": nl}
+    t, _ = avg("dense_schur")
+    if t and nS_list:
+        # per sequence at n_c, m = 3 n_c: Cholesky of the augmented Sigma-hat (m^3 / 3), Sigma_s =
+        # K_s^-1 when S changed (n_c^3, reuse fraction excluded), back substitution and t = B u,
+        # Z (4 m^2)
+        fl = [(1.0 - reuse_frac) * nc ** 3 + (3 * nc) ** 3 / 3.0 + 4 * (3 * nc) ** 2 for nc in nS_list]
+        f = statistics.mean(fl)
+        pk = _fp64_peak(sm_max_mhz)
+        out["dense_schur"] = {"kernel": "k_schur_coop", "bound": "tensor", "achieved": f / t / 1e12, "peak": pk,
+                              "unit": "TFLOP/s", "frac": f / t / 1e12 / pk, "flops_per_launch": f,
+                              "avg_launch_us": t * 1e6, "n_c_mean": statistics.mean(nS_list),
+                              "peak_source": "FP64 DMMA measured (tools/micro/fp64_peaks.cu) x 148 SMs x max clock"}
+    for k in ("pair_derivatives", "panel_forward", "contact_assembly", "narrow_phase", "broad_phase", "ccd",
+              "line_search"):
+        t, c = avg(k)
+        if t:
+            out[k] = {"bound": "latency", "avg_launch_us": t * 1e6, "launches": c}
+    return out
+
+
+# ------------------------------------------------------------------------------ ours -------
+def _stage_pass(P, s, steps):
+    P.set_timing(s.h, True)
+    P.kernel_times(s.h, reset=True)
+    for _ in range(steps):
+        s.step(n_iters=1)
+    kt = P.kernel_times(s.h, reset=True)
+    P.set_timing(s.h, False)
+    return kt
+
+
+def c3_single(P, local, steps):
+    """Extra field: C3 single sequence (configs[2]) with its canonical actuation, frame F warm-
+    started from the frame-(F-1) equilibrium computed like the batch's."""
+    import torch
+    import scenes
+    sc = scenes.face_c3()
+    s = P.Solver(sc, A=sc.actuation(TIMED_FRAME - 1)[None], device=local)
+    s.step(n_iters=PREP_ITERS)
+    s.step(A_next=sc.actuation(TIMED_FRAME)[None], n_iters=0)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    st = None
+    for _ in range(steps):
+        st = s.step(n_iters=1)[0]
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    s.close()
+    return {"workload": "C3: ~300k-tet two-slit face, canonical actuation 0.6 smoothstep, frame "
+                        f"{TIMED_FRAME} warm-started (BASELINE.json configs[2])",
+            "iters_per_s": steps / (ms / 1000.0), "ms_per_iter": ms / steps, "n_S_last": st["n_S"],
+            "n_active_last": st["n_active"]}
+
+
+def c2_extra(P, local, K):
+    """Extra field: C2 (configs[1]) one sequence, frames 20.. warm-started, A on the device."""
+    import numpy as np
+    import torch
+    import scenes
+    sc = scenes.face_c2()
+    frames = torch.from_numpy(np.stack([sc.actuation(f) for f in range(C2_FRAMES)])).to(f"cuda:{local}")
+    s = P.Solver(sc, A=sc.actuation(0)[None], device=local, A_on_device=True)
+    for f in range(C2_CONTACT_START):
+        s.step(A_device_ptr=frames[f].data_ptr(), n_iters=ITERS_PER_FRAME)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(K):
+        s.step(A_device_ptr=frames[min(C2_CONTACT_START + i, C2_FRAMES - 1)].data_ptr(), n_iters=ITERS_PER_FRAME)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    kt = _stage_pass(P, s, 20)
+    s.close()
+    return {"workload": "C2: face-like 47.5k-tet block, mouth slit (BASELINE.json configs[1])",
+            "iters_per_s": K * ITERS_PER_FRAME / (ms / 1000.0),
+            "frames_per_sec": K / (ms / 1000.0), "timed_frames": f"{C2_CONTACT_START}..{C2_CONTACT_START + K - 1}",
+            "stage_us_per_launch": {k: round(v[0] / v[1] * 1000, 1) for k, v in kt.items() if v[1]}}
+
+
+def _c5_local_step(size, hbm):
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("c5_sweep", os.path.join(ROOT, "tools", "c5_sweep.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    r = mod.run(size)
+    return {"workload": f"C5 pure-PD box {size} ({r['tets']} tets, {r['verts']} verts), 20-iteration steps "
+                        "(BASELINE.json configs[4])",
+            "local_step_GBps": r["local_step_GBps"], "local_step_frac": r["local_step_GBps"] / hbm,
+            "gather_GBps": r["gather_GBps"], "gather_frac": r["gather_GBps"] / hbm,
+            "pure_pd_iters_per_s": r["iters_per_s"], "peak_GBps": hbm,
+            "bytes_per_tet": "local 240 (+32 per vertex), gather 28 per incidence + 40 per free vertex"}
+
+
+def run_ours(a):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import scenes
+    from paper_2312_02999_b200 import pd_ipc as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = f"cuda:{local}"
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    t_setup = time.perf_counter()
+    sc = scenes.face_c3()
+    mine = scenes.c4_assignment(a.seqs, rank, world)
+    nb = len(mine)
+    acts = [scenes.c4_actuation(sc, j) for j in mine]
     T, n = sc.n_tets, sc.n_verts
-    nf = n - len(sc.fixed)
-    if name == "local_step":
-        # per tet: tet ids 16 B, B_i 72, A_i (6 sym) 48, w_i 8, corner forces written 96;
-        # per vertex: x 32 (double4) read once
-        byts = T * (16 + 72 + 48 + 8 + 96) + n * 32
-        return {"kernel": "k_local_step", "bound": "hbm", "achieved": byts / avg_s / 1e9, "peak": hbm,
-                "unit": "GB/s", "frac": byts / avg_s / 1e9 / hbm, "traffic": _traffic("k_local_step"),
-                "bytes_per_launch": byts, "avg_launch_us": avg_s * 1e6, "peak_source": peak_src}
-    if name == "gather":
-        byts = nf * (8 + 32) + 4 * T * (4 + 24)
-        return {"kernel": "k_gather_elastic", "bound": "hbm", "achieved": byts / avg_s / 1e9, "peak": hbm,
-                "unit": "GB/s", "frac": byts / avg_s / 1e9 / hbm, "traffic": _traffic("k_gather_elastic"),
-                "bytes_per_launch": byts, "avg_launch_us": avg_s * 1e6, "peak_source": peak_src}
-    if name == "dense_schur":
-        # algorithmic flops of a9 at n_c = |S|, m = 3 n_c: Sigma_s = K^-1 (n_c^3), Cholesky of
-        # the augmented Sigma-hat (m^3 / 3), back substitution 2 m^2, t = B u and Z 2 m^2
-        nc = statistics.mean(st["n_S"] for st in stats_log)
-        m = 3 * nc
-        flops = nc ** 3 + m ** 3 / 3.0 + 4 * m ** 2
-        fp64 = DMMA_FLOP_PER_CLK_SM * N_SM * sm_max_mhz * 1e6 / 1e12
-        return {"kernel": "k_schur_coop", "bound": "tensor", "achieved": flops / avg_s / 1e12, "peak": fp64,
-                "unit": "TFLOP/s", "frac": flops / avg_s / 1e12 / fp64, "traffic": _traffic("k_schur_coop"),
-                "flops_per_launch": flops, "avg_launch_us": avg_s * 1e6,
-                "peak_source": "FP64 DMMA measured (tools/micro/fp64_peaks.cu) x 148 SMs x max clock"}
-    return {"kernel": name, "bound": "latency", "achieved": None, "peak": None, "unit": None,
-            "frac": None, "traffic": None, "avg_launch_us": avg_s * 1e6,
-            "note": "latency-bound stage; see DESIGN.md"}
+    A_prep = np.stack([f(TIMED_FRAME - 1) for f in acts])
+    A_host = np.stack([f(TIMED_FRAME) for f in acts])
+    K, W = a.steps, a.warmup
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MB > L2
+
+    # ---------------- device-resident run (value): the frame-F actuation is uploaded into the
+    # handle BEFORE the timed region (pd_ipc_step with n_iters = 0), so the timed steps move no
+    # host data
+    s = P.Solver(sc, A=A_prep, n_seq=nb, device=local)
+    info = P.get_info(s.h)
+    s.step(n_iters=PREP_ITERS)                                          # untimed preparation
+    for _ in range(W):                                                   # warm-up steps
+        s.step(n_iters=1)
+    s.step(A_next=A_host, n_iters=0)                                     # inputs resident in HBM
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t_setup
+    x_start0 = s.positions(0)
+    clocks = ClockSampler(local)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    stats = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    l0 = P.launch_count()
+    t_wall = time.perf_counter()
+    torch.cuda.nvtx.range_push("timed")                          # ncu --nvtx-include timed/
+    for i in range(K):
+        flush.fill_(float(i))                                    # evict L2 between steps
+        ev[i][0].record()
+        st = s.step(n_iters=1)
+        ev[i][1].record()
+        stats.append(st)
+    torch.cuda.nvtx.range_pop()
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter() - t_wall
+    launches = P.launch_count() - l0
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    my_ms = float(sum(e0.elapsed_time(e1) for e0, e1 in ev))
+    checks = [(j, seq_checksum(s.positions(b))) for b, j in enumerate(mine)]
+    nS_all = [st[b]["n_S"] for st in stats for b in range(nb)]
+    reuse = sum(st[b]["sigma_reused"] for st in stats for b in range(nb)) / float(max(1, K * nb))
+    # exposed time of the reduced solve per sequence-iteration: B-check ready (end of the
+    # sequence's assembly) -> dx ready (its Schur step + its share of the batched backward solves)
+    exposed = statistics.mean(st[b]["ms"]["gstep"] for st in stats for b in range(nb))
+    seq_ms = {k: statistics.mean(st[b]["ms"][k] for st in stats for b in range(nb))
+              for k in ("ipc", "gstep", "ccd", "ls", "misc", "total")}
+
+    # ---------------- end-to-end through the C ABI with host buffers (pinned): the same handle
+    # continues frame F; every step copies the actuation of all the rank's sequences host ->
+    # device (pd_ipc_step) and every sequence's positions device -> host (pd_ipc_positions)
+    e2e = None
+    if not a.no_e2e:
+        pin = torch.empty(A_host.shape, dtype=torch.float64, pin_memory=True)
+        pin.copy_(torch.from_numpy(A_host))
+        pin_np = pin.numpy()
+        xout = torch.empty((n, 3), dtype=torch.float64, pin_memory=True).numpy()
+        ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        torch.cuda.synchronize()
+        for i in range(K):
+            flush.fill_(float(i))
+            ev2[i][0].record()
+            s.step(A_next=pin_np, n_iters=1)
+            for b in range(nb):
+                P.lib.pd_ipc_positions(s.h, b, xout.ctypes.data_as(P.C.POINTER(P.C.c_double)))
+            ev2[i][1].record()
+        torch.cuda.synchronize()
+        e2e_ms = float(sum(e0.elapsed_time(e1) for e0, e1 in ev2))
+        e2e = {"ms": e2e_ms, "h2d": nb * T * 9 * 8, "d2h": nb * n * 3 * 8}
+    # per-kernel-group rooflines and the exposed reduced-solve time: a separate pass with every
+    # group timed (timers in the timed region would cost time)
+    kt = _stage_pass(P, s, 2)
+    s.close()
+
+    # ---------------- gather over ranks (NCCL): times, units, checksums
+    allv = gather_rank_values([my_ms, e2e["ms"] if e2e else 0.0, float(nb * K)], world, dev)
+    by_seq = gather_checksums(checks, world, dev, a.seqs)
+    max_ms, max_e2e = float(allv[:, 0].max()), float(allv[:, 1].max())
+    extras = {}
+    if rank == 0 and world == 1 and not a.no_extras:
+        extras["c3_single"] = c3_single(P, local, ITERS_PER_FRAME)
+        extras["c2"] = c2_extra(P, local, 5)
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    value = job_throughput(allv[:, 0], allv[:, 2])
+    hbm, bf16, peak_src = _peaks()
+    sm_max = _sm_max_mhz()
+    rl_all = rooflines(kt, info, nb, nS_all, reuse, hbm, sm_max, peak_src)
+    dom = rl_all.get("dense_schur")
+    rl = None
+    if dom:
+        rl = {"bound": "tensor", "achieved": dom["achieved"], "peak": dom["peak"], "unit": "TFLOP/s",
+              "frac": dom["frac"], "traffic": _traffic("k_schur_coop"), "kernel": "k_schur_coop",
+              "flops_per_launch": dom["flops_per_launch"], "avg_launch_us": dom["avg_launch_us"],
+              "peak_source": dom["peak_source"]}
+    cpu = None
+    if world == 1 and not a.no_cpu_baseline:
+        cpu = cpu_baseline(x_start0, mine[0], TIMED_FRAME, a.cpu_seconds)
+    c5 = None
+    if world == 1 and a.c5 and not a.no_extras:
+        c5 = _c5_local_step(a.c5, hbm)
+    units_total = float(allv[:, 2].sum())
+    line = {
+        "metric": "PD+IPC iterations/s", "value": value, "unit": "iters/s", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": max_ms / K, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generators, SURVEY.md 8(d) C3 mesh + C4 actuations)",
+        "frames_per_sec": value / ITERS_PER_FRAME,
+        "config": {"workload": f"C4: {a.seqs} actuation sequences on the ~300k-tet two-slit face (C3 mesh), "
+                               f"sharded j mod {world} (BASELINE.json configs[3])",
+                   "tets": T, "verts": n, "surface_tris": int(sc.surf_tris.shape[0]),
+                   "sequences_per_gpu": nb, "sequences_total": a.seqs,
+                   "step": "one lockstep PD+IPC iteration of every sequence of the rank (20 steps = 1 frame)",
+                   "timed": f"frame {TIMED_FRAME}, iterations 1..{K}, warm-started from the frame-"
+                            f"{TIMED_FRAME - 1} state ({PREP_ITERS} untimed iterations from rest + {W} warm-up steps)",
+                   "l2": "flushed between steps (256 MB write, outside the per-step CUDA events); the "
+                         "batch's working set is also larger than L2",
+                   "parallelism": f"dp{world} over independent sequences (no data-path collective)"},
+        "roofline": rl,
+        "rooflines": rl_all,
+        "exposed_reduced_solve_ms_per_seq_iter": exposed,
+        "stage_ms_per_seq_iter": seq_ms,
+        "n_c_mean": statistics.mean(nS_all), "n_c_max": max(nS_all),
+        "sigma_reuse_frac": reuse,
+        "cpu_baseline": cpu,
+        "e2e": ({"value": units_total / (max_e2e / 1000.0), "unit": "iters/s",
+                 "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
+                 "note": "every step: the actuation of all the rank's sequences copied from pinned host memory "
+                         "(pd_ipc_step) and every sequence's positions copied back (pd_ipc_positions)"}
+                if e2e else None),
+        "gpu_launches": launches,
+        "clocks": clk,
+        "checksum": combined_checksum(by_seq),
+        "checksum_note": "sha256 over the per-sequence position checksums in j order after the timed "
+                         "steps: equal for every P iff every sequence's trajectory is bit-identical",
+        "per_rank_ms": [float(v) for v in allv[:, 0]],
+        "local_step_c5": c5,
+        **extras,
+        "info": info, "setup_s": t_setup, "wall_s": t_wall,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def main():

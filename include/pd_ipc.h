@@ -91,6 +91,16 @@ typedef struct {
                                  PD_IPC_DBG_SORT_BROAD   every broad phase takes the sort path;
                                  PD_IPC_DBG_TINY_HASH    the hash broad phase overflows, so each
                                    iteration is redone on the sort path                        */
+    int32_t reduced_backend;  /* how K_s = (L^-1)_SS and the contact part of dx are formed (the
+                                 same dx either way):
+                                 1 panel: V_s = L^-1 Pi E_S per S (reach-limited forward solve),
+                                   K_s = V_s^T V_s, dx from w_el + V_s (gc + t);
+                                 2 gather: G2 = (L^-1)_RR over the region R of W-supported free
+                                   vertices precomputed at create (the paper's precomputed inverse
+                                   of the collision region), K_s gathered from
+                                   G2, y_S from the base solve, dx from one more forward solve of
+                                   the S-sparse right-hand side;
+                                 0 auto: gather when |R| >= 1024, else panel                    */
 } pd_ipc_options;
 
 #define PD_IPC_DBG_LARGE_SCHUR 1
@@ -198,6 +208,13 @@ int64_t pd_ipc_debug_crossings(const pd_ipc_mesh *mesh, const double *rest_pos, 
 int pd_ipc_set_timing(pd_ipc *h, int32_t on);
 int pd_ipc_kernel_times(pd_ipc *h, double *ms, int64_t *counts, int32_t reset);
 const char *pd_ipc_kernel_name(int32_t id);
+
+/* Sizes of the handle (for measurement reports): info[0..n) of
+ *   [n_verts, n_tets, n_free, n_surf_verts, n_surf_tris, n_surf_edges, supernodes, nnz(L),
+ *    supernodal etree depth, capS (max |S|), reuse slots, n_seq, backward row blocks, nU,
+ *    reduced backend (1 panel, 2 gather), |R|]
+ * (nnz(L): the prefactorised PD matrix).  Returns the number of fields written. */
+int pd_ipc_get_info(const pd_ipc *h, int64_t *info, int32_t n);
 
 /* Number of CUDA kernels this library has launched in the process so far. */
 int64_t pd_ipc_launch_count(void);

@@ -261,6 +261,12 @@ struct pd_ipc {
     std::vector<DBuf<double>> V_slot, K_slot;
     std::vector<DBuf<int>> qS_slot;
     DBuf<int> nS_slot;                  // [nslots] |S| of the key (0 = invalid)
+    // reduced-solve backend: panel (V_s on the fly) or gather (precomputed
+    // G2 = (L^-1)_RR over the region R of W-supported free vertices, n2 = |R|)
+    bool gather = false;
+    int n2 = 0;
+    DBuf<double> G2, Yel_all, Zf_all, bw_P2;
+    DBuf<int> rpos, ts_done2, bw_cnt2;
     // shared contact / Schur work buffers (a sequence's contact + Schur stages run in order)
     DBuf<double> A9stage;
     DBuf<double4> blo, bhi;
@@ -304,6 +310,8 @@ struct pd_ipc {
     double *G(int b) { return G_all.p + (size_t)b * 4 * nf; }
     double *Yw(int b) { return Yw_all.p + (size_t)b * 4 * nf; }
     double *Z(int b) { return Z_all.p + (size_t)b * 4 * nf; }
+    double *Yel(int b) { return Yel_all.p + (size_t)b * 4 * nf; }
+    double *Zf(int b) { return Zf_all.p + (size_t)b * 4 * nf; }
     double4 *dx(int b) { return dx_all.p + (size_t)b * n; }
     double4 *s(int b) { return s_all.p + (size_t)b * std::max(1, Ns); }
     double4 *ds(int b) { return ds_all.p + (size_t)b * std::max(1, Ns); }
@@ -413,6 +421,16 @@ static void debug_capture(pd_ipc *h, int b, int n_pt, int n_ee, int nS) {
 // debugging aid (PDIPC_TRACE): per-item forward-solve timestamps and Schur phase timestamps
 static void dump_traces(pd_ipc *h, int nS) {
     if (!h->trace_file || nS <= 0 || std::ftell(h->trace_file) >= (30l << 20)) return;
+    if (h->gather || !h->trace.p) {   // no panel forward solve to trace: Schur phases only
+        if (h->schur_file) {
+            std::vector<unsigned long long> pr(1024);
+            CK(cudaMemcpy(pr.data(), h->sprof.p, 1024 * 8, cudaMemcpyDeviceToHost));
+            fwrite(&nS, sizeof(int), 1, h->schur_file);
+            fwrite(pr.data(), 8, 1024, h->schur_file);
+            fflush(h->schur_file);
+        }
+        return;
+    }
     int nitems;
     CK(cudaMemcpy(&nitems, h->ts_ptr.p + h->F.nsn, sizeof(int), cudaMemcpyDeviceToHost));
     std::vector<unsigned long long> tr(4 * (size_t)nitems);
@@ -584,6 +602,13 @@ static void enqueue_elastic(pd_ipc *h, int b0, int nb, int it) {
                          reinterpret_cast<const double *>(h->gel(b0)), h->Yw(b0), nullptr, h->ldv, h->Ug2.p,
                          nullptr, h->ticket2.p + 2, 0, 1, nb, 4 * (long long)h->nf,
                          4 * (long long)std::max(1, F2.nU), h->Nt > 0 ? h->side_ctas : h->nsm, nullptr, s2);
+    if (h->gather && h->Nt > 0) {
+        // gather backend: y_el = L^-T w_el (the base solve), whose rows S give y_S
+        CK(dev_copy(h->Yel(b0), h->Yw(b0), sizeof(double) * 4 * h->nf * nb, s2));
+        for (int c = 0; c < nb; c += kBwSeqs)
+            launch_backward_solve(h->F, h->ts_done2.p, h->bw_cnt2.p, h->ticket2.p, h->bw_P2.p, h->Yel(b0 + c),
+                                  std::min(kBwSeqs, nb - c), 4 * (long long)h->nf, h->side_ctas, s2);
+    }
     kt.stop(K_D_SYRK, s2);
     CK(cudaEventRecord(h->ev_join, s2));
 }
@@ -646,7 +671,7 @@ static void enqueue_contact_schur(pd_ipc *h, int b, int b0, int nb, int it) {
         CK(cudaStreamWaitEvent(h->st3, h->ev_S, 0));
         launch_gather_gc(h->qS.p, nS_dev, h->capS, h->WTp.p, h->WTr.p, h->WTv.p, h->gsq.p, dmax, acnt, h->gcS.p,
                          h->st3);
-        enqueue_panel_forward(h, b, nS_dev, h->st3);
+        if (!h->gather) enqueue_panel_forward(h, b, nS_dev, h->st3);
         CK(cudaEventRecord(h->ev_join3, h->st3));
         // B-check: fixed-point accumulation into the dense 3|S| x 3|S| block, then to double; the
         // low words of the fixed-point sums live in the (not yet used) Sigma-hat buffer
@@ -680,7 +705,9 @@ static void enqueue_contact_schur(pd_ipc *h, int b, int b0, int nb, int it) {
                                      3 * h->capS, h->Sh.p, h->ldh, h->Lstore.p, h->Tt.p, h->U.p, h->yS.p,
                                      h->rhs.p, h->u.p, h->tv.p, h->Z(b), di + D_INFO, di + D_SAME,
                                      h->trace_file ? h->sprof.p : nullptr,
-                                     (h->opt.debug_flags & PD_IPC_DBG_LARGE_SCHUR) ? 1 : 0, st));
+                                     (h->opt.debug_flags & PD_IPC_DBG_LARGE_SCHUR) ? 1 : 0,
+                                     h->gather ? kSchurGather : kSchurPanel, h->G2.p, h->n2, h->rpos.p,
+                                     h->gather ? h->Yel(b) : nullptr, st));
     } else {
         CK(dev_copy(h->Z(b), h->Yw(b), sizeof(double) * 4 * nf, st));
     }
@@ -695,12 +722,26 @@ static void enqueue_backward(pd_ipc *h, int b0, int nb, int it) {
     const int slot = it * nb;
     kt.slot = slot;
     h->tm.rec(slot, 5, st);
+    double *Zb = h->Z(b0);
+    if (h->gather && h->Nt > 0) {
+        // gather backend: Zf = w_el + L^-1 Pi E_S (gc + t) -- one forward solve of every sequence's
+        // sparse right-hand side (the Schur step left it in Z), added to w_el
+        kt.start(K_FWD, st);
+        launch_ts_plan(h->F, nullptr, h->ticket2.p + 2, 0, h->ticket2.p + 2, 0, h->ticket2.p + 3, 1, nb, h->ts_lo2.p,
+                       h->ts_hi2.p, h->ts_cnt2.p, h->ts_rem2.p, h->ts_ptr2.p, h->ticket2.p, st);
+        launch_forward_solve(h->F, h->ts_lo2.p, h->ts_hi2.p, h->ts_ptr2.p, nullptr, h->ts_rem2.p, h->ticket2.p,
+                             h->Z(b0), h->Zf(b0), nullptr, h->ldv, h->Ug2.p, nullptr, h->ticket2.p + 2, 0, 1, nb,
+                             4 * (long long)h->nf, 4 * (long long)std::max(1, h->F.nU), h->nsm, nullptr, st,
+                             h->Yw(b0));
+        kt.stop(K_FWD, st);
+        Zb = h->Zf(b0);
+    }
     kt.start(K_BWD, st);
     for (int c = 0; c < nb; c += kBwSeqs)
-        launch_backward_solve(h->F, h->ts_done.p, h->bw_cnt.p, h->ticket.p, h->bw_P.p, h->Z(b0 + c),
+        launch_backward_solve(h->F, h->ts_done.p, h->bw_cnt.p, h->ticket.p, h->bw_P.p, Zb + (size_t)c * 4 * h->nf,
                               std::min(kBwSeqs, nb - c), 4 * (long long)h->nf, h->nsm, st);
     kt.stop(K_BWD, st);
-    launch_scatter_dx(h->Z(b0), h->q2v.p, h->nf, h->dx(b0), h->dscal(b0) + 1, nb, h->n, S_STRIDE,
+    launch_scatter_dx(Zb, h->q2v.p, h->nf, h->dx(b0), h->dscal(b0) + 1, nb, h->n, S_STRIDE,
                       st);   // also seeds each sequence's CCD minimum amin = 1
     h->tm.rec(slot, 6, st);
 }
@@ -1278,10 +1319,27 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         }
         h->Tt.exact(64 * 64);
         h->part.exact(std::max<size_t>(4096, (size_t)(m.T + 255) / 256 + (nf + 255) / 256 + 64));
+        std::vector<int> Rq;   // region R: factor positions of the W-supported free vertices, sorted
+        {
+            std::vector<char> sup(m.nf, 0);
+            for (size_t k = 0; k < m.W_col.size(); ++k) {
+                const int qv = m.v2q[m.W_col[k]];
+                if (qv >= 0) sup[qv] = 1;
+            }
+            for (int qv = 0; qv < m.nf; ++qv)
+                if (sup[qv]) Rq.push_back(qv);
+            h->n2 = (int)Rq.size();
+            // reduced-solve backend: 1 panel, 2 gather, 0 auto (gather for regions of >= 1024
+            // vertices: there the panel and K_s = V_s^T V_s dominate an iteration whenever S changes)
+            const int be = o.reduced_backend;
+            const bool want = be == 2 || (be == 0 && h->n2 >= 1024);
+            h->gather = m.Nt > 0 && want && h->n2 <= h->capS;
+        }
         {   // reuse slots (V_s, K_s / -Sigma_s and the S they belong to): one per sequence when 40 %
             // of the free HBM holds them, else fewer, shared round-robin (the bit-exact key check
             // keeps sharing exact; a shared slot only reuses less often)
-            const size_t vbytes = m.Nt > 0 ? (size_t)nf * h->ldv * 8 + (size_t)h->capS * h->capS * 8 + (size_t)(nf + 1) * 4
+            const size_t vbytes = m.Nt > 0 ? (h->gather ? 0 : (size_t)nf * h->ldv * 8) + (size_t)h->capS * h->capS * 8 +
+                                                 (size_t)(nf + 1) * 4
                                            : 256;
             size_t fr = 0, tot = 0;
             CK(cudaMemGetInfo(&fr, &tot));
@@ -1292,13 +1350,50 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             h->K_slot.resize(h->nslots);
             h->qS_slot.resize(h->nslots);
             for (int r = 0; r < h->nslots; ++r) {
-                h->V_slot[r].exact(m.Nt > 0 ? (size_t)nf * h->ldv : 32);
+                h->V_slot[r].exact(m.Nt > 0 && !h->gather ? (size_t)nf * h->ldv : 32);
                 h->K_slot[r].exact(m.Nt > 0 ? (size_t)h->capS * h->capS : 1);
                 h->qS_slot[r].exact(nf + 1);
             }
             h->nS_slot.exact(h->nslots);
             CK(cudaMemset(h->nS_slot.p, 0, sizeof(int) * h->nslots));
             for (int sq = 0; sq < Bq; ++sq) h->seqs[sq]->slot = sq % h->nslots;
+        }
+        if (h->gather) {
+            // one-time (untimed) precompute of G2 = (L^-1)_RR = V_R^T V_R with V_R = L^-1 Pi E_R: the
+            // panel forward solve and the K-only Schur phase with S = R (the
+            // paper's precomputed Sigma^-1 of the collision region)
+            const int n2 = h->n2;
+            std::vector<int> rp(nf, -1);
+            for (int i = 0; i < n2; ++i) rp[Rq[i]] = i;
+            h->rpos.upload(rp.data(), rp.size());
+            CK(cudaMemcpy(h->qS.p, Rq.data(), sizeof(int) * n2, cudaMemcpyHostToDevice));
+            int *nS_dev = h->spos.p + nf;
+            CK(cudaMemcpy(nS_dev, &n2, sizeof(int), cudaMemcpyHostToDevice));
+            DBuf<double> Vtmp;
+            Vtmp.exact((size_t)nf * h->ldv);
+            h->G2.exact((size_t)n2 * n2);
+            int *zero = h->ticket2.p + 2, *flags = h->dint(0) + D_CAP;
+            launch_ts_plan(F, h->qS.p, nS_dev, h->capS, zero, (long long)h->Up.n, flags, 2, 0, h->ts_lo.p, h->ts_hi.p,
+                           h->ts_cnt.p, h->ts_rem.p, h->ts_ptr.p, h->ticket.p, h->st);
+            launch_forward_solve(F, h->ts_lo.p, h->ts_hi.p, h->ts_ptr.p, h->qS.p, h->ts_rem.p, h->ticket.p, nullptr,
+                                 nullptr, Vtmp.p, h->ldv, nullptr, h->Up.p, nS_dev, h->capS, 0, 0, 0, 0, h->nsm,
+                                 nullptr, h->st);
+            CK((cudaError_t)launch_schur(F, Vtmp.p, h->ldv, h->Yw(0), h->gcS.p, h->qS.p, h->ts_lo.p, h->ts_hi.p,
+                                         nS_dev, h->capS, h->G2.p, n2, h->Bc.p, 3 * h->capS, h->Sh.p, h->ldh,
+                                         h->Lstore.p, h->Tt.p, h->U.p, h->yS.p, h->rhs.p, h->u.p, h->tv.p, h->Z(0),
+                                         h->dint(0) + D_INFO, zero, nullptr, 0, kSchurKOnly, nullptr, 0, nullptr,
+                                         nullptr, h->st));
+            CK(cudaStreamSynchronize(h->st));
+            int cap_flags = 0;
+            CK(cudaMemcpy(&cap_flags, flags, sizeof(int), cudaMemcpyDeviceToHost));
+            if (cap_flags) throw CudaError("region precompute: panel capacity", PD_IPC_E_CAPACITY);
+            CK(cudaMemset(flags, 0, sizeof(int)));
+            Vtmp.release();
+            h->Yel_all.exact(4 * (size_t)nf * Bq);
+            h->Zf_all.exact(4 * (size_t)nf * Bq);
+            h->bw_P2.exact(h->bw_P.n);
+            h->ts_done2.exact(f.nsn);
+            h->bw_cnt2.exact(f.nsn);
         }
         upload_actuation(h.get(), A, false);
         CK(cudaStreamSynchronize(h->st));
@@ -1430,7 +1525,8 @@ void pd_ipc_destroy(pd_ipc *h) {
     rel(h->nS_slot);
     rel(h->x_all); rel(h->gel_all); rel(h->dx_all); rel(h->s_all); rel(h->ds_all); rel(h->A6_all); rel(h->p_all);
     rel(h->fc_all); rel(h->G_all); rel(h->Yw_all); rel(h->Z_all); rel(h->dscal_all); rel(h->dint_all);
-    rel(h->xstage); rel(h->A9stage); rel(h->blo); rel(h->bhi); rel(h->hcnt); rel(h->hstart); rel(h->hent);
+    rel(h->xstage); rel(h->A9stage); rel(h->blo);
+    rel(h->G2); rel(h->Yel_all); rel(h->Zf_all); rel(h->bw_P2); rel(h->rpos); rel(h->ts_done2); rel(h->bw_cnt2); rel(h->bhi); rel(h->hcnt); rel(h->hstart); rel(h->hent);
     rel(h->qcnt); rel(h->qoff); rel(h->qlist); rel(h->gsq);
     rel(h->cand_tmp); rel(h->akeys); rel(h->flag); rel(h->pos); rel(h->ctype); rel(h->atype); rel(h->ids);
     rel(h->iscr); rel(h->cd2); rel(h->ad2); rel(h->grad); rel(h->Hp); rel(h->dist); rel(h->mark);
@@ -1560,6 +1656,15 @@ const char *pd_ipc_kernel_name(int32_t id) {
 }
 
 int64_t pd_ipc_launch_count(void) { return pdipc::launch_count(); }
+
+int pd_ipc_get_info(const pd_ipc *h, int64_t *info, int32_t n) {
+    if (!h || !info) return fail(nullptr, PD_IPC_E_ARG, "NULL argument");
+    const int64_t v[16] = {h->n, h->T, h->nf, h->Ns, h->Nt, h->Ne, h->hf.nsn, h->hf.nnzL, h->hf.depth,
+                           h->capS, h->nslots, h->B, h->F.bw_nblocks, h->F.nU, h->gather ? 2 : 1, h->n2};
+    const int k = std::max(0, std::min<int>(n, 16));
+    for (int i = 0; i < k; ++i) info[i] = v[i];
+    return k;
+}
 
 int64_t pd_ipc_debug_crossings(const pd_ipc_mesh *mesh, const double *rest_pos, const double *x) {
     if (!mesh || !rest_pos || !x) return fail(nullptr, PD_IPC_E_ARG, "NULL argument");

@@ -65,7 +65,34 @@ struct SchurArgs {
     const int *same;            // 1: S unchanged, K holds the previous -Sigma_s (reuse it)
     unsigned long long *prof;   // optional phase timestamps (PDIPC_TRACE), [1024]
     int pw_min;                 // systems of >= pw_min 64-tiles take the large-system path
+    // reduced-solve backend (the paper's precomputed-inverse variant):
+    //   kSchurPanel  : K_s = V_s^T V_s and y_S = -V_s^T w_el from the panel; Z = w_el + V_s (gc + t)
+    //   kSchurKOnly  : setup: K = V_s^T V_s only (S = the region R), then return
+    //   kSchurGather : K_s = G2[r(S), r(S)] gathered from the precomputed (L^-1)_RR, y_S = rows S of
+    //                  the base solve y_el = L^-T L^-1 Pi g_el (y_S = -y_el[S]); output Z = the
+    //                  sparse right-hand side E_S (gc + t) (zero off S), solved by the caller
+    int mode;
+    const double *G2;           // [n2][n2] (L^-1)_RR (gather mode)
+    int n2;
+    const int *rpos;            // [nf] index of a factor position in R, -1 outside (gather mode)
+    const double *Yel;          // [nf][4] y_el (gather mode)
+    unsigned *bar;              // [kMaxPanels] group-barrier counters of the large-system P3
 };
+constexpr int kMaxPanels = 512;
+
+// Barrier among the `target / k`-member group that shares counter *ctr (k-th use: target =
+// k x members).  Members are co-resident (cooperative launch).
+__device__ __forceinline__ void group_bar(unsigned *ctr, unsigned target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(ctr, 1u);
+        volatile unsigned *v = ctr;
+        while (*v < target) __nanosleep(32);
+        __threadfence();
+    }
+    __syncthreads();
+}
 
 __device__ __forceinline__ unsigned long long gtimer_s() {
     unsigned long long t;
@@ -506,8 +533,8 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int G = gridDim.x, bid = blockIdx.x;
     const int nS = min(*a.nS_ptr, a.capS), m = 3 * nS, ma = m + 1;   // augmented size
-    if (nS == 0) {                                        // no contact: z = w = w_el
-        for (int r = bid * NT + tid; r < 4 * a.nf; r += G * NT) a.Z[r] = a.G[r];
+    if (nS == 0) {   // no contact: z = w = w_el (gather backend: the sparse right-hand side is 0)
+        for (int r = bid * NT + tid; r < 4 * a.nf; r += G * NT) a.Z[r] = a.mode == kSchurGather ? 0.0 : a.G[r];
         return;
     }
     int np = 0;                                           // phase-timestamp counter (debug)
@@ -515,7 +542,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
 #define GSYNC()                                                               \
     do {                                                                      \
         grid.sync();                                                          \
-        if (a.prof && bid == 0 && tid == 0 && np < 1023) a.prof[np++] = gtimer_s(); \
+        if (a.prof && bid == 0 && tid == 0 && np < 1000) a.prof[np++] = gtimer_s(); \
     } while (0)
     // ------------------------------------------------ P0: y_S = -V_s^T w and K = V_s^T V_s
     // Tile-parallel over the 32x32 lower tiles of K, split over the supernodes (rows) when tiles
@@ -552,7 +579,11 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
     // part; the contact part -K gc is folded into b below since Sigma_s K = I): one CTA per column,
     // the path rows come from a static per-supernode list (independent loads), fixed-order
     // block reduction: the same bits whether or not K is recomputed
-    for (int c = pb; pb >= 0 && c < nS; c += pG) {
+    if (a.mode == kSchurGather) {   // y_S = -(L^-T L^-1 Pi g_el)_S: rows S of the base solve
+        for (int e = pb * NT + tid; pb >= 0 && e < 3 * nS; e += pG * NT)
+            a.yS[e] = -a.Yel[(size_t)a.qS[e / 3] * 4 + e % 3];
+    }
+    for (int c = pb; pb >= 0 && a.mode == kSchurPanel && c < nS; c += pG) {
         const int s0 = a.col2sn[a.qS[c]];
         double acc[3] = {0, 0, 0};
         for (int pi = a.path_ptr[s0]; pi < a.path_ptr[s0 + 1]; ++pi) {
@@ -570,7 +601,13 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
         }
     }
     const int ntk = (nS + 31) / 32;
-    const int ntiles = reuse ? 0 : ntk * (ntk + 1) / 2;   // K keeps -Sigma_s when S is unchanged
+    // K keeps -Sigma_s when S is unchanged; the gather backend reads K from G2 instead
+    const int ntiles = (reuse || a.mode == kSchurGather) ? 0 : ntk * (ntk + 1) / 2;
+    if (a.mode == kSchurGather && !reuse)     // K_s = (L^-1)_SS = G2[r(S), r(S)] (a gather)
+        for (size_t e = (size_t)bid * NT + tid; e < (size_t)nS * nS; e += (size_t)G * NT) {
+            const int i = (int)(e / nS), j = (int)(e % nS);
+            a.K[(size_t)i * a.ldk + j] = a.G2[(size_t)a.rpos[a.qS[i]] * a.n2 + a.rpos[a.qS[j]]];
+        }
     const int nsplit = max(1, min(16, G / max(ntk * (ntk + 1) / 2, 1)));
     auto tile_of = [&](int b, int &ti, int &tj) {
         int rem = b;
@@ -694,6 +731,8 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
         }
     }
     GSYNC();
+    if (a.mode == kSchurKOnly) return;        // setup: K = V^T V of the region only
+    if (a.prof && bid == 0 && tid == 0) { a.prof[1000 + 1] = np; a.prof[np < 1000 ? np++ : np] = gtimer_s(); }   // phase marker (PDIPC_TRACE)
     // ------------------------------------------------ P1: K <- -K^{-1} (block sweep)
     if (!reuse) {
         const int nt = (nS + TB - 1) / TB;
@@ -744,6 +783,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
             GSYNC();
         }
     }
+    if (a.prof && bid == 0 && tid == 0) { a.prof[1000 + 2] = np; a.prof[np < 1000 ? np++ : np] = gtimer_s(); }   // phase marker (PDIPC_TRACE)
     // ------------------------------------------------ P2: augmented Sigma-hat (Sigma_s = -K)
     for (size_t e = (size_t)pb * NT + tid; pb >= 0 && e < (size_t)m * m; e += (size_t)pG * NT) {
         const int r = (int)(e / m), c = (int)(e % m);
@@ -761,7 +801,10 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
         if (lane == 0) a.Sh[(size_t)m * a.ldh + row] = acc - a.gc[row];
     }
     if (bid == 0 && tid == 0) a.Sh[(size_t)m * a.ldh + m] = 1.0;
+    if (bid == 0)
+        for (int e = tid; e < kMaxPanels; e += NT) a.bar[e] = 0u;   // P3 group-barrier counters
     GSYNC();
+    if (a.prof && bid == 0 && tid == 0) { a.prof[1000 + 3] = np; a.prof[np < 1000 ? np++ : np] = gtimer_s(); }   // phase marker (PDIPC_TRACE)
     // ------------------------------------------------ P3: Cholesky of the augmented matrix
     // Right-looking in panels of kPW tile columns: inside a panel, per tile column k: diagonal
     // tile factor + inverse (CTA 0), L_ik = A_ik Li_k^T, update of the panel's later columns;
@@ -869,87 +912,128 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
             GSYNC();
         }
     }
-    for (int p0 = 0; nt >= a.pw_min && p0 < nt; p0 += pw) {
-        const int p1 = min(nt, p0 + pw);
-        for (int k = p0; k < p1; ++k) {
-            const int kc0 = k * TB, kn = min(TB, ma - kc0);
-            if (bid == 0) {
-                ld_tile(T0, a.Sh + (size_t)kc0 * a.ldh + kc0, a.ldh, kn, kn);
-                __syncthreads();
-                tile_chol64(T0, T1, kn, m - kc0, a.info);
-                st_tile(T0, a.Sh + (size_t)kc0 * a.ldh + kc0, a.ldh, kn, kn);
-                for (int e = tid; e < TB * TB; e += NT) a.Lstore[(size_t)k * TB * TB + e] = T1[(e >> 6) * TS + (e & 63)];
+    // Large systems: right-looking in panels of kPW tile columns with LOOK-AHEAD.  Iteration q:
+    //   panel group (CTAs [0, npg)): applies panel q-1 to panel q's tile columns, then factors
+    //     panel q -- per tile column k: diagonal tile factor + inverse on the group's first CTA,
+    //     L_ik = A_ik Li_k^T, update of the panel's later columns -- with group barriers;
+    //   update group (CTAs [npg, G)): applies panel q-1 to every tile column right of panel q
+    //     (accumulators in registers, k streamed through shared memory, double-buffered).
+    // ONE grid barrier per panel: the serial panel chain runs beside the trailing update.  npg
+    // balances the two groups' estimated work (identical on every CTA).
+    // A_ij -= sum_{k in [k0, k1)} L_ik L_jk^T for one 64 x 64 tile (ti, tj)
+    auto update_tile = [&](int ti, int tj, int k0, int k1) {
+        const int gr = lane >> 2, gc = lane & 3;
+        const int r0 = ti * TB, c0 = tj * TB, rows = min(TB, ma - r0), cols = min(TB, ma - c0);
+        double acc[8][2];
+#pragma unroll
+        for (int nb = 0; nb < 8; ++nb) {
+            const int r = 8 * wid + gr, c = 8 * nb + 2 * gc;
+            acc[nb][0] = (r < rows && c < cols) ? a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c] : 0.0;
+            acc[nb][1] = (r < rows && c + 1 < cols) ? a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c + 1] : 0.0;
+        }
+        ld_tile_async(T0, a.Sh + (size_t)r0 * a.ldh + k0 * TB, a.ldh, rows, TB);
+        ld_tile_async(T1, a.Sh + (size_t)c0 * a.ldh + k0 * TB, a.ldh, cols, TB);
+        for (int k = k0; k < k1; ++k) {
+            double *X = ((k - k0) & 1) ? T2 : T0, *Y = ((k - k0) & 1) ? T3 : T1;
+            if (k + 1 < k1) {
+                double *Xn = ((k - k0) & 1) ? T0 : T2, *Yn = ((k - k0) & 1) ? T1 : T3;
+                ld_tile_async(Xn, a.Sh + (size_t)r0 * a.ldh + (k + 1) * TB, a.ldh, rows, TB);
+                ld_tile_async(Yn, a.Sh + (size_t)c0 * a.ldh + (k + 1) * TB, a.ldh, cols, TB);
+                asm volatile("cp.async.wait_group 2;\n" ::);
+            } else {
+                asm volatile("cp.async.wait_group 0;\n" ::);
             }
-            GSYNC();
-            for (int b = bid; b < nt - k - 1; b += G) {      // L_ik = A_ik Li^T
-                const int ti = k + 1 + b, r0 = ti * TB, rows = min(TB, ma - r0);
-                ld_tile(T0, a.Sh + (size_t)r0 * a.ldh + kc0, a.ldh, rows, kn);
-                ld_tile(T1, a.Lstore + (size_t)k * TB * TB, TB, TB, TB);
-                __syncthreads();
-                tile_xyt(T2, T0, T1, 1.0, false);
-                st_tile(T2, a.Sh + (size_t)r0 * a.ldh + kc0, a.ldh, rows, kn);
+            __syncthreads();
+            tile_sub_xyt_regs(acc, X, Y);
+            __syncthreads();
+        }
+#pragma unroll
+        for (int nb = 0; nb < 8; ++nb) {
+            const int r = 8 * wid + gr, c = 8 * nb + 2 * gc;
+            if (r < rows && c < cols) a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c] = acc[nb][0];
+            if (r < rows && c + 1 < cols) a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c + 1] = acc[nb][1];
+        }
+    };
+    const int npan = nt >= a.pw_min ? (nt + kPW - 1) / kPW : 0;
+    for (int q = 0; q < npan; ++q) {
+        const int c0t = q * kPW, c1t = min(nt, c0t + kPW);       // panel q: tile columns [c0t, c1t)
+        const int rr = nt - c1t;                                   // tile columns right of panel q
+        int npg = G;
+        if (q > 0 && rr > 0 && G > 1) {
+            // work estimates in units of a 64^3 tile product: a k = 4-tile update ~ 4, a TRSM or
+            // single-k update ~ 1.3, the diagonal factor ~ 4 (serial), a barrier ~ 0.3 (serial)
+            double wp = 0.0, ws = 0.0;
+            for (int j = c0t; j < c1t; ++j) wp += 4.0 * (nt - j);
+            for (int k = c0t; k < c1t; ++k) {
+                wp += 1.3 * (nt - k - 1);
+                for (int j = k + 1; j < c1t; ++j) wp += 1.3 * (nt - j);
+                ws += 4.0 + 3 * 0.3;
             }
-            GSYNC();
-            const int nj = p1 - k - 1;                       // panel columns right of k
-            if (nj > 0) {
-                const int nrow = nt - k - 1;
-                for (int b = bid; b < nrow * nj; b += G) {   // A_ij -= L_ik L_jk^T, k < j < p1, i >= j
-                    const int tj = k + 1 + b % nj, ti = k + 1 + b / nj;
-                    if (ti < tj) continue;
-                    const int r0 = ti * TB, c0 = tj * TB, rows = min(TB, ma - r0), cols = min(TB, ma - c0);
-                    ld_tile(T0, a.Sh + (size_t)r0 * a.ldh + kc0, a.ldh, rows, kn);
-                    ld_tile(T1, a.Sh + (size_t)c0 * a.ldh + kc0, a.ldh, cols, kn);
-                    ld_tile(T2, a.Sh + (size_t)r0 * a.ldh + c0, a.ldh, rows, cols);
-                    __syncthreads();
-                    tile_xyt(T2, T0, T1, -1.0, true);
-                    st_tile(T2, a.Sh + (size_t)r0 * a.ldh + c0, a.ldh, rows, cols);
-                }
-                GSYNC();
+            const double wu = 4.0 * rr * (rr + 1) / 2.0;
+            double best = 1e300;
+            for (int x = 1; x < G; ++x) {
+                const double t = fmax(ws + wp / x, wu / (G - x));
+                if (t < best) { best = t; npg = x; }
             }
         }
-        // trailing update with the whole panel: A_ij -= sum_{k in panel} L_ik L_jk^T, p1 <= j <= i
-        const int rr = nt - p1;
-        if (rr > 0) {
-            const int gr = lane >> 2, gc = lane & 3;
-            for (int b = bid; b < rr * (rr + 1) / 2; b += G) {
+        if (bid < npg) {
+            unsigned *ctr = a.bar + q;
+            unsigned nbar = 0;
+            if (q > 0) {        // panel q-1 applied to panel q's tiles (i, j), c0t <= j < c1t, i >= j
+                int tot = 0;
+                for (int j = c0t; j < c1t; ++j) tot += nt - j;
+                for (int b = bid; b < tot; b += npg) {
+                    int j = c0t, bb = b;
+                    while (bb >= nt - j) { bb -= nt - j; ++j; }
+                    update_tile(j + bb, j, c0t - kPW, c0t);
+                }
+                group_bar(ctr, ++nbar * npg);
+            }
+            if (a.prof && bid == 0 && tid == 0 && q < 100) a.prof[500 + q] = gtimer_s();   // panel update done
+            for (int k = c0t; k < c1t; ++k) {
+                const int kc0 = k * TB, kn = min(TB, ma - kc0);
+                if (bid == 0) {
+                    ld_tile(T0, a.Sh + (size_t)kc0 * a.ldh + kc0, a.ldh, kn, kn);
+                    __syncthreads();
+                    tile_chol64(T0, T1, kn, m - kc0, a.info);
+                    st_tile(T0, a.Sh + (size_t)kc0 * a.ldh + kc0, a.ldh, kn, kn);
+                    for (int e = tid; e < TB * TB; e += NT) a.Lstore[(size_t)k * TB * TB + e] = T1[(e >> 6) * TS + (e & 63)];
+                }
+                group_bar(ctr, ++nbar * npg);
+                for (int b = bid; b < nt - k - 1; b += npg) {      // L_ik = A_ik Li^T
+                    const int ti = k + 1 + b, r0 = ti * TB, rows = min(TB, ma - r0);
+                    ld_tile(T0, a.Sh + (size_t)r0 * a.ldh + kc0, a.ldh, rows, kn);
+                    ld_tile(T1, a.Lstore + (size_t)k * TB * TB, TB, TB, TB);
+                    __syncthreads();
+                    tile_xyt(T2, T0, T1, 1.0, false);
+                    st_tile(T2, a.Sh + (size_t)r0 * a.ldh + kc0, a.ldh, rows, kn);
+                }
+                group_bar(ctr, ++nbar * npg);
+                if (k + 1 < c1t) {          // A_ij -= L_ik L_jk^T, k < j < c1t, i >= j
+                    int tot = 0;
+                    for (int j = k + 1; j < c1t; ++j) tot += nt - j;
+                    for (int b = bid; b < tot; b += npg) {
+                        int j = k + 1, bb = b;
+                        while (bb >= nt - j) { bb -= nt - j; ++j; }
+                        update_tile(j + bb, j, k, k + 1);
+                    }
+                    group_bar(ctr, ++nbar * npg);
+                }
+            }
+            if (a.prof && bid == 0 && tid == 0 && q < 100) { a.prof[600 + q] = gtimer_s(); a.prof[800 + q] = npg; }
+        } else if (q > 0) {     // panel q-1 applied to the tile columns right of panel q
+            const int ub = bid - npg, nu = G - npg;
+            for (int b = ub; b < rr * (rr + 1) / 2; b += nu) {
                 int i = 0, bb = b;
                 while (bb >= rr - i) { bb -= rr - i; ++i; }
-                const int tj = p1 + i, ti = tj + bb;
-                const int r0 = ti * TB, c0 = tj * TB, rows = min(TB, ma - r0), cols = min(TB, ma - c0);
-                double acc[8][2];
-#pragma unroll
-                for (int nb = 0; nb < 8; ++nb) {
-                    const int r = 8 * wid + gr, c = 8 * nb + 2 * gc;
-                    acc[nb][0] = (r < rows && c < cols) ? a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c] : 0.0;
-                    acc[nb][1] = (r < rows && c + 1 < cols) ? a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c + 1] : 0.0;
-                }
-                // k-chunks double-buffered: (T0, T1) and (T2, T3)
-                ld_tile_async(T0, a.Sh + (size_t)r0 * a.ldh + p0 * TB, a.ldh, rows, TB);
-                ld_tile_async(T1, a.Sh + (size_t)c0 * a.ldh + p0 * TB, a.ldh, cols, TB);
-                for (int k = p0; k < p1; ++k) {
-                    double *X = ((k - p0) & 1) ? T2 : T0, *Y = ((k - p0) & 1) ? T3 : T1;
-                    if (k + 1 < p1) {
-                        double *Xn = ((k - p0) & 1) ? T0 : T2, *Yn = ((k - p0) & 1) ? T1 : T3;
-                        ld_tile_async(Xn, a.Sh + (size_t)r0 * a.ldh + (k + 1) * TB, a.ldh, rows, TB);
-                        ld_tile_async(Yn, a.Sh + (size_t)c0 * a.ldh + (k + 1) * TB, a.ldh, cols, TB);
-                        asm volatile("cp.async.wait_group 2;\n" ::);
-                    } else {
-                        asm volatile("cp.async.wait_group 0;\n" ::);
-                    }
-                    __syncthreads();
-                    tile_sub_xyt_regs(acc, X, Y);
-                    __syncthreads();
-                }
-#pragma unroll
-                for (int nb = 0; nb < 8; ++nb) {
-                    const int r = 8 * wid + gr, c = 8 * nb + 2 * gc;
-                    if (r < rows && c < cols) a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c] = acc[nb][0];
-                    if (r < rows && c + 1 < cols) a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c + 1] = acc[nb][1];
-                }
+                const int tj = c1t + i, ti = tj + bb;
+                update_tile(ti, tj, c0t - kPW, c0t);
             }
-            GSYNC();
+            if (a.prof && tid == 0 && q < 100) atomicMax(a.prof + 700 + q, gtimer_s());   // update group done
         }
+        GSYNC();
     }
+    if (a.prof && bid == 0 && tid == 0) { a.prof[1000 + 4] = np; a.prof[np < 1000 ? np++ : np] = gtimer_s(); }   // phase marker (PDIPC_TRACE)
     // ------------------------------------------------ P4: u = C^{-T} y, y = row m of the factor
     const int ntm = (m + TB - 1) / TB;
     if (nt < a.pw_min) {
@@ -992,7 +1076,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
                 __syncthreads();
                 if (tid < kn) uv[kc0 + tid] = T3[tid] + T3[64 + tid] + T3[128 + tid] + T3[192 + tid];
                 __syncthreads();
-                if (a.prof && tid == 0 && np < 1023) a.prof[np++] = gtimer_s();
+                if (a.prof && tid == 0 && np < 1000) a.prof[np++] = gtimer_s();
                 // y_j -= sum_r C[kc0 + r][j] u_r: warp w takes rows w, w + 8, ..., lane the columns
                 // j = lane + 32 q (coalesced rows; 8 rows x 8 columns of loads in flight per chunk);
                 // the 8 warp partials are summed in a fixed order (deterministic)
@@ -1023,7 +1107,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
                     yv[j] -= ((part[j] + part[mr + j]) + (part[2 * mr + j] + part[3 * mr + j])) +
                              ((part[4 * mr + j] + part[5 * mr + j]) + (part[6 * mr + j] + part[7 * mr + j]));
                 __syncthreads();                                // this stage is refilled next
-                if (a.prof && tid == 0 && np < 1023) a.prof[np++] = gtimer_s();
+                if (a.prof && tid == 0 && np < 1000) a.prof[np++] = gtimer_s();
             }
             asm volatile("cp.async.wait_group 0;\n" ::);
             for (int e = tid; e < m; e += NT) a.u[e] = uv[e];
@@ -1064,6 +1148,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
             }
         }
     }
+    if (a.prof && bid == 0 && tid == 0) { a.prof[1000 + 5] = np; a.prof[np < 1000 ? np++ : np] = gtimer_s(); }   // phase marker (PDIPC_TRACE)
     // ------------------------------------------------ P5: t = B u ; Z = w + V t = w_el + V (gc + t)
     // (w = L^{-1} Pi g = w_el + V gc since the contact gradient is supported on S)
     for (int row = bid * (NT / 32) + wid; row < m; row += G * (NT / 32)) {
@@ -1071,6 +1156,13 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
         for (int c = lane; c < m; c += 32) acc += a.Bc[(size_t)row * a.ldb + c] * a.u[c];
         acc = warp_sum(acc);
         if (lane == 0) a.t[row] = acc + a.gc[row];
+    }
+    if (a.mode == kSchurGather) {
+        // sparse right-hand side E_S (gc + t) of the caller's solve: zero, then the rows of S
+        for (size_t e = (size_t)bid * NT + tid; e < (size_t)4 * a.nf; e += (size_t)G * NT) a.Z[e] = 0.0;
+        GSYNC();
+        for (int e = bid * NT + tid; e < m; e += G * NT) a.Z[(size_t)a.qS[e / 3] * 4 + e % 3] = a.t[e];
+        return;
     }
     GSYNC();
     // Z = w_el + V (gc + t): warp per row, lanes over the row's active columns [lo_s, hi_s)
@@ -1100,6 +1192,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
 static int g_schur_grid = 0;
 static double *g_kpart = nullptr;   // split-K partial tiles, grid x 1152 doubles (allocated at init)
 static double *g_lp = nullptr;      // small-system P3 panel scratch
+static unsigned *g_bar = nullptr;   // large-system P3 group-barrier counters
 
 void schur_init(int device) {
     cudaFuncSetAttribute(k_schur_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, kSchurSmem);
@@ -1109,6 +1202,7 @@ void schur_init(int device) {
     g_schur_grid = std::max(1, per_sm) * nsm;
     if (!g_kpart) cudaMalloc(&g_kpart, (size_t)g_schur_grid * 1152 * sizeof(double));
     if (!g_lp) cudaMalloc(&g_lp, (size_t)2 * kLPTiles * TB * TB * sizeof(double));
+    if (!g_bar) cudaMalloc(&g_bar, (size_t)kMaxPanels * sizeof(unsigned));
 }
 
 int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, const double *gc,
@@ -1116,7 +1210,8 @@ int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, 
                  const int *lo, const int *hi, const int *nS, int capS, double *K, int ldk, const double *Bc, int ldb,
                  double *Sh, int ldh, double *Lstore, double *T, double *U, double *yS, double *y, double *u,
                  double *t, double *Z, int *info, const int *same_S, unsigned long long *prof,
-                 int large_min_tiles, cudaStream_t st) {
+                 int large_min_tiles, int mode, const double *G2, int n2, const int *rpos, const double *Yel,
+                 cudaStream_t st) {
     SchurArgs a;
     a.V = V; a.ldv = ldv; a.G = G; a.gc = gc; a.qS = qS; a.col2sn = F.col2sn; a.sn_c0 = F.sn_c0;
     a.sn_parent = F.sn_parent; a.path_ptr = F.path_ptr; a.path_sn = F.path_sn; a.lo = lo; a.hi = hi; a.nsn = F.nsn; a.nf = F.nf; a.nS_ptr = nS; a.capS = capS;
@@ -1124,7 +1219,9 @@ int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, 
     a.T = T; a.U = U; a.yS = yS; a.y = y; a.u = u; a.t = t; a.Z = Z; a.info = info; a.same = same_S; a.prof = prof;
     a.Kpart = g_kpart;
     a.LP = g_lp;
+    a.bar = g_bar;
     a.pw_min = large_min_tiles > 0 ? std::min(large_min_tiles, kPWMinTiles) : kPWMinTiles;
+    a.mode = mode; a.G2 = G2; a.n2 = n2; a.rpos = rpos; a.Yel = Yel;
     void *args[] = {&a};
     note_launch();
     return (int)cudaLaunchCooperativeKernel((const void *)k_schur_coop, dim3(g_schur_grid), dim3(NT),

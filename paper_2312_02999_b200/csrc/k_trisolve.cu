@@ -136,7 +136,8 @@ struct FwdArgs {
     int nsn;
     int *rem, *ticket;
     const double *G;                   // [nseq][nf][4] Pi g (sequence stride gstride doubles)
-    double *Y;                         // [nseq][nf][4] out: w = L^{-1} Pi g
+    double *Y;                         // [nseq][nf][4] out: w = L^{-1} Pi g (+ Yadd)
+    const double *Yadd;                // nullable [nseq][nf][4] added to the solution rows
     double *V;                         // [nf][ldv] panel
     int ldv;
     double *Ug;                        // [nseq][nU][4] gradient update rows (stride ustride)
@@ -419,9 +420,10 @@ __global__ void __launch_bounds__(kTS_NT) k_forward_solve(FwdArgs A) {
                 const int e = e0 + k * kTS_NT + tid, i = e >> lg, c = e & (ncw - 1), r = rb + i;
                 if (i >= m || c >= ncw || (grad && gseq0 + (c >> 2) >= A.nseq)) continue;
                 if (r < w) {
-                    if (grad)
-                        A.Y[(size_t)(gseq0 + (c >> 2)) * A.gstride + (size_t)(c0 + r) * 4 + (c & 3)] =
-                            (c & 3) < 3 ? O[i][c] : 0.0;
+                    if (grad) {
+                        const size_t yi = (size_t)(gseq0 + (c >> 2)) * A.gstride + (size_t)(c0 + r) * 4 + (c & 3);
+                        A.Y[yi] = (c & 3) < 3 ? O[i][c] + (A.Yadd ? __ldcg(A.Yadd + yi) : 0.0) : 0.0;
+                    }
                     else {
                         const int cc = tbase + c;
                         if (cc >= lo_s && cc < hi_s) A.V[(size_t)(c0 + r) * A.ldv + cc] = O[i][c];
@@ -590,7 +592,7 @@ void launch_forward_solve(const DevFactor &F, const int *lo, const int *hi, cons
                           const int *qS, int *rem, int *ticket, const double *G, double *Y, double *V,
                           int ldv, double *Ug, double *Up, const int *nS_ptr, int capS, int with_grad,
                           int nseq, long long gstride, long long ustride,
-                          int nsm, unsigned long long *trace, cudaStream_t st) {
+                          int nsm, unsigned long long *trace, cudaStream_t st, const double *Yadd) {
     FwdArgs A;
     A.sn_c0 = F.sn_c0; A.sn_rowptr = F.sn_rowptr; A.sn_parent = F.sn_parent;
     A.uoff = F.uoff; A.rc_ptr = F.rc_ptr; A.rc_src = F.rc_src;
@@ -598,7 +600,7 @@ void launch_forward_solve(const DevFactor &F, const int *lo, const int *hi, cons
     A.lo = lo; A.hi = hi; A.item_ptr = item_ptr; A.qS = qS; A.ford = F.ford; A.nsn = F.nsn;
     A.rem = rem; A.ticket = ticket; A.G = G; A.Y = Y; A.V = V; A.ldv = ldv;
     A.Ug = Ug; A.Up = Up; A.nS_ptr = nS_ptr; A.capS = capS; A.with_grad = with_grad; A.trace = trace;
-    A.nseq = nseq; A.gstride = gstride; A.ustride = ustride;
+    A.nseq = nseq; A.gstride = gstride; A.ustride = ustride; A.Yadd = Yadd;
     A.ngt = grad_tiles(nseq);
     A.gw = nseq <= 2 ? 8 : 32;
     PDI_LAUNCH(k_forward_solve, nsm, kTS_NT, kFwdSmem, st)(A);

@@ -73,7 +73,7 @@ void launch_forward_solve(const DevFactor &F, const int *lo, const int *hi, cons
                           const int *qS, int *rem, int *ticket, const double *G, double *Y, double *V,
                           int ldv, double *Ug, double *Up, const int *nS_ptr, int capS, int with_grad,
                           int nseq, long long gstride, long long ustride,
-                          int nsm, unsigned long long *trace, cudaStream_t st);
+                          int nsm, unsigned long long *trace, cudaStream_t st, const double *Yadd = nullptr);
 // backward solve of nseq <= kBwSeqs sequences' right-hand sides Z[sq][nf][4] (stride zstride)
 constexpr int kBwSeqs = 8;
 void launch_backward_solve(const DevFactor &F, int *done, int *cnt, int *ticket, double *P, double *Z,
@@ -86,8 +86,10 @@ int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, 
                  const int *lo, const int *hi, const int *nS, int capS, double *K, int ldk, const double *Bc, int ldb,
                  double *Sh, int ldh, double *Lstore, double *T, double *U, double *yS, double *y, double *u,
                  double *t, double *Z, int *info, const int *same_S, unsigned long long *prof,
-                 int large_min_tiles, cudaStream_t st);
+                 int large_min_tiles, int mode, const double *G2, int n2, const int *rpos, const double *Yel,
+                 cudaStream_t st);
 void note_launch();
+constexpr int kSchurPanel = 0, kSchurKOnly = 1, kSchurGather = 2;   // launch_schur modes
 
 // ---- k_contact.cu
 void contact_init();

@@ -32,7 +32,7 @@ class pd_ipc_options(C.Structure):
     _fields_ = [("n_seq", C.c_int32), ("device", C.c_int32), ("ls_max_halvings", C.c_int32),
                 ("accd_max_iters", C.c_int32), ("A_on_device", C.c_int32),
                 ("max_pairs", C.c_int32), ("accd_s", C.c_double), ("no_sigma_reuse", C.c_int32),
-                ("no_cand_reuse", C.c_int32), ("debug_flags", C.c_int32)]
+                ("no_cand_reuse", C.c_int32), ("debug_flags", C.c_int32), ("reduced_backend", C.c_int32)]
 
 
 class pd_ipc_stats(C.Structure):
@@ -92,6 +92,8 @@ lib.pd_ipc_kernel_times.argtypes = [_P, C.POINTER(C.c_double), C.POINTER(C.c_int
 lib.pd_ipc_kernel_times.restype = C.c_int
 lib.pd_ipc_kernel_name.argtypes = [C.c_int32]
 lib.pd_ipc_kernel_name.restype = C.c_char_p
+lib.pd_ipc_get_info.argtypes = [_P, C.POINTER(C.c_int64), C.c_int32]
+lib.pd_ipc_get_info.restype = C.c_int
 lib.pd_ipc_launch_count.argtypes = []
 lib.pd_ipc_launch_count.restype = C.c_int64
 
@@ -99,7 +101,7 @@ EXPORTED = ["pd_ipc_create", "pd_ipc_step", "pd_ipc_positions", "pd_ipc_destroy"
             "pd_ipc_last_error", "pd_ipc_set_positions", "pd_ipc_set_debug",
             "pd_ipc_get_projections", "pd_ipc_get_contacts", "pd_ipc_get_vector", "pd_ipc_get_pair_terms",
             "pd_ipc_build_info", "pd_ipc_debug_factor_solve", "pd_ipc_debug_crossings", "pd_ipc_set_timing",
-            "pd_ipc_kernel_times", "pd_ipc_kernel_name", "pd_ipc_launch_count"]
+            "pd_ipc_kernel_times", "pd_ipc_kernel_name", "pd_ipc_launch_count", "pd_ipc_get_info"]
 
 
 def set_timing(h, on=True, groups=None):
@@ -119,6 +121,19 @@ def kernel_times(h, reset=False):
     cnt = (C.c_int64 * 32)()
     k = lib.pd_ipc_kernel_times(h, ms, cnt, int(reset))
     return {lib.pd_ipc_kernel_name(i).decode(): (ms[i], cnt[i]) for i in range(k)}
+
+
+INFO_FIELDS = ("n_verts", "n_tets", "n_free", "n_surf_verts", "n_surf_tris", "n_surf_edges", "supernodes",
+               "nnz_L", "etree_depth", "capS", "reuse_slots", "n_seq", "bw_row_blocks", "nU", "reduced_backend",
+               "region_size")
+
+
+def get_info(h) -> dict:
+    buf = (C.c_int64 * len(INFO_FIELDS))()
+    k = lib.pd_ipc_get_info(h, buf, len(INFO_FIELDS))
+    if k < 0:
+        raise PdIpcError(k, last_error(h))
+    return {INFO_FIELDS[i]: int(buf[i]) for i in range(k)}
 
 
 def launch_count() -> int:
@@ -174,7 +189,7 @@ def _check(rc, h=None):
 
 def create(scene, A=None, n_seq=1, device=0, A_on_device=False, max_pairs=0,
            ls_max_halvings=30, accd_max_iters=10_000, accd_s=0.1, d_hat=None, kappa=None,
-           sigma_reuse=True, cand_reuse=True, debug_flags=0):
+           sigma_reuse=True, cand_reuse=True, debug_flags=0, reduced_backend=0):
     """pd_ipc_create on a scenes.Scene.  A: (n_seq, T, 9) host actuation (default frame 0)."""
     m = _MeshArgs(scene)
     if A is None:
@@ -182,7 +197,7 @@ def create(scene, A=None, n_seq=1, device=0, A_on_device=False, max_pairs=0,
     A = _f64(A).reshape(n_seq, -1, 9)
     opt = pd_ipc_options(n_seq, device, ls_max_halvings, accd_max_iters, int(A_on_device),
                          max_pairs, accd_s, 0 if sigma_reuse else 1, 0 if cand_reuse else 1,
-                         int(debug_flags))
+                         int(debug_flags), int(reduced_backend))
     h = _P()
     rc = lib.pd_ipc_create(C.byref(m.mesh), _dp(m.rest), _dp(A),
                            float(scene.d_hat if d_hat is None else d_hat),

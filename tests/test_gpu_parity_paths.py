@@ -93,12 +93,15 @@ def test_large_schur_path_forced(P, scene):
     s.close()
 
 
-def test_large_schur_path_native_c3(P):
+@pytest.mark.parametrize("backend", [1, 2])
+def test_large_schur_path_native_c3(P, backend):
     """C3 (BASELINE configs[2], 292k tets): the GPU runs 17 frames into contact; one lockstep
-    iteration from that state with n_c ~ 1.8k (m = 3 n_c ~ 5.4k > 1280: the large path)."""
+    iteration from that state with n_c ~ 1.8k (m = 3 n_c ~ 5.4k > 1280: the large path), with
+    the panel backend (1) and the precomputed-region gather backend (2, the default here)."""
     from oracle import OracleSolver
     sc = scenes.face_c3()
-    s = P.Solver(sc)
+    s = P.Solver(sc, reduced_backend=backend)
+    assert P.get_info(s.h)["reduced_backend"] == backend
     for f in range(17):
         s.step(A_next=sc.actuation(f)[None], n_iters=20)
     x = s.positions()
@@ -264,3 +267,45 @@ def test_intersecting_states_are_rejected(P):
     with pytest.raises(P.PdIpcError) as e:
         P.Solver(bad)
     assert e.value.code in (P.E_INTERSECTING, P.E_MESH)
+
+
+# ------------------------------------------------------------------ reduced-solve backends --
+@pytest.mark.parametrize("scene", ["c1", "face_small"])
+def test_gather_backend_lockstep(P, scene):
+    """The gather backend (K_s from the precomputed G2 = (L^-1)_RR, y_S from the base solve, dx
+    through a second forward solve of the S-sparse right-hand side) forced on
+    small scenes: C, S bit-exact, g-hat 1e-10, dx 1e-8, alpha exact against the oracle."""
+    from oracle import OracleSolver
+    if scene == "c1":
+        sc = scenes.slabs_c1()
+        A, n = sc.actuation(0), 12
+    else:
+        sc = scenes.face_small(n_frames=2)
+        A = np.tile(np.eye(3).reshape(1, 9), (sc.n_tets, 1))
+        A[:, 4] += 0.5 * sc.meta["lip_mask"]
+        n = 8
+    o = OracleSolver(sc)
+    s = P.Solver(sc, A=A[None], reduced_backend=2)
+    assert P.get_info(s.h)["reduced_backend"] == 2
+    P.set_debug(s.h, 1)
+    log, _ = _lockstep(P, s, sc, o, sc.rest.copy(), A, n, check_alpha=False)
+    assert max(len(r["S"]) for r in log) > 50
+    s.close()
+
+
+def test_gather_backend_lockstep_batch(P):
+    """Gather backend in a lockstep batch: each sequence equals its single run bit for bit."""
+    sc = scenes.face_small(n_frames=4)
+    acts = [scenes.c4_actuation(sc, j, n_frames=4) for j in range(5)]
+    s = P.Solver(sc, A=np.stack([a(0) for a in acts]), n_seq=5, reduced_backend=2)
+    for f in range(4):
+        st = s.step(A_next=np.stack([a(f) for a in acts]), n_iters=10)
+    xs = [s.positions(b) for b in range(5)]
+    assert max(t["n_S"] for t in st) > 0
+    s.close()
+    for j in (0, 3):
+        s1 = P.Solver(sc, A=acts[j](0)[None], reduced_backend=2)
+        for f in range(4):
+            s1.step(A_next=acts[j](f)[None], n_iters=10)
+        assert np.array_equal(s1.positions(), xs[j]), j
+        s1.close()

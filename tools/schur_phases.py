@@ -1,0 +1,50 @@
+"""Phase breakdown of the dense Schur kernel (PDIPC_TRACE): runs C3 into contact with the
+trace on and prints, per traced iteration, n_c and the microseconds of P0 (y_S, K = V^T V),
+P1 (Sigma_s = K^-1), P2 (assembly), P3 (Cholesky), P4 (back substitution), P5 (t, Z).
+Usage: python tools/schur_phases.py [frames]"""
+import os
+import struct
+import sys
+import tempfile
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+path = os.path.join(tempfile.mkdtemp(), "tr.bin")
+os.environ["PDIPC_TRACE"] = path
+import numpy as np  # noqa: E402
+
+import scenes  # noqa: E402
+from paper_2312_02999_b200 import pd_ipc as P  # noqa: E402
+
+frames = int(sys.argv[1]) if len(sys.argv) > 1 else 24
+sc = scenes.face_c3()
+s = P.Solver(sc)
+for f in range(frames):
+    s.step(A_next=sc.actuation(f)[None], n_iters=20 if f < frames - 1 else 4)
+s.close()
+data = open(path + ".schur", "rb").read()
+rec = 4 + 8 * 1024
+rows = []
+for i in range(len(data) // rec):
+    nS = struct.unpack_from("i", data, i * rec)[0]
+    pr = np.frombuffer(data, dtype=np.uint64, count=1024, offset=i * rec + 4).astype(np.int64)
+    mk = [0] + [int(pr[1000 + k]) for k in range(1, 6)]
+    n_end = max(j for j in range(1000) if pr[j] != 0)
+    ts = [pr[mk[k]] for k in range(6)] + [pr[n_end]]
+    rows.append((nS, [(ts[k + 1] - ts[k]) / 1e3 for k in range(6)]))
+for nS, ph in rows[-12:]:
+    print(f"n_c {nS:5d}  " + "  ".join(f"P{k} {v:8.1f}" for k, v in enumerate(ph)) + f"  total {sum(ph):8.1f} us")
+# large-system P3 look-ahead detail of the last traced iteration: per panel iteration q, the
+# panel group's time (its update of panel q + the panel factorisation) and the update group's
+nS, _ = rows[-1]
+i = len(data) // rec - 1
+pr = np.frombuffer(data, dtype=np.uint64, count=1024, offset=i * rec + 4).astype(np.int64)
+m3 = int(pr[1003])
+print("P3 detail (us from the iteration start): q  npg  panel_upd_done  panel_done  update_done  end")
+for q in range(100):
+    if pr[800 + q] == 0:
+        break
+    t0 = pr[m3 + q]
+    t1 = pr[m3 + q + 1]
+    print(q, int(pr[800 + q]), round((pr[500 + q] - t0) / 1e3, 1) if pr[500 + q] else "-",
+          round((pr[600 + q] - t0) / 1e3, 1), round((pr[700 + q] - t0) / 1e3, 1) if pr[700 + q] else "-",
+          round((t1 - t0) / 1e3, 1))
