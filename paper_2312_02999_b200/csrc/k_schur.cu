@@ -165,6 +165,21 @@ __device__ __forceinline__ void ld_tile_async(double *S, const double *src, int 
     asm volatile("cp.async.commit_group;\n" ::);
 }
 
+// acc (warp w: rows 8w..8w+7, all 64 columns, fragment layout of tile_xyt) += X Y^T on DMMA (the
+// caller keeps the accumulator negated to subtract: no per-step negation on the operand path)
+__device__ __forceinline__ void tile_add_xyt_regs(double (&acc)[8][2], const double *X, const double *Y) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int gr = lane >> 2, gc = lane & 3;
+    const double *xr = X + (8 * w + gr) * TS + gc;
+    const double *yr = Y + gr * TS + gc;
+#pragma unroll 4
+    for (int k4 = 0; k4 < TB / 4; ++k4) {
+        const double av = xr[4 * k4];
+#pragma unroll
+        for (int nb = 0; nb < 8; ++nb) dmma_884(acc[nb][0], acc[nb][1], av, yr[8 * nb * TS + 4 * k4]);
+    }
+}
+
 // acc (warp w: rows 8w..8w+7, all 64 columns, fragment layout of tile_xyt) -= X Y^T on DMMA
 __device__ __forceinline__ void tile_sub_xyt_regs(double (&acc)[8][2], const double *X, const double *Y) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -785,12 +800,15 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
     }
     if (a.prof && bid == 0 && tid == 0) { a.prof[1000 + 2] = np; a.prof[np < 1000 ? np++ : np] = gtimer_s(); }   // phase marker (PDIPC_TRACE)
     // ------------------------------------------------ P2: augmented Sigma-hat (Sigma_s = -K)
-    for (size_t e = (size_t)pb * NT + tid; pb >= 0 && e < (size_t)m * m; e += (size_t)pG * NT) {
-        const int r = (int)(e / m), c = (int)(e % m);
-        if (c > r || (early0 && r < TB)) continue;       // tile 0 rows: factored by CTA 0
-        double v = a.Bc[(size_t)r * a.ldb + c];
-        if (r % 3 == c % 3) v -= a.K[(size_t)(r / 3) * a.ldk + c / 3];
-        a.Sh[(size_t)r * a.ldh + c] = v;
+    // lower triangle, a warp per row (tile-0 rows: factored by CTA 0 when early0); the Sigma_s
+    // entries of row r sit at columns c = r mod 3 + 3 j
+    for (int r = (early0 ? TB : 0) + pb * (NT / 32) + wid; pb >= 0 && r < m; r += pG * (NT / 32)) {
+        const double *brow = a.Bc + (size_t)r * a.ldb;
+        double *srow = a.Sh + (size_t)r * a.ldh;
+        for (int c = lane; c <= r; c += 32) srow[c] = brow[c];
+        __syncwarp();
+        const double *krow = a.K + (size_t)(r / 3) * a.ldk;
+        for (int j = lane; 3 * j + r % 3 <= r; j += 32) srow[3 * j + r % 3] = brow[3 * j + r % 3] - krow[j];
     }
     // b = (Sigma_s (x) I3) y_S with y_S = y_S^el - (K (x) I3) gc, i.e. b = Sigma_s y_S^el - gc
     for (int row = pb * (NT / 32) + wid; pb >= 0 && row < m; row += pG * (NT / 32)) {
@@ -924,15 +942,16 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
     auto update_tile = [&](int ti, int tj, int k0, int k1) {
         const int gr = lane >> 2, gc = lane & 3;
         const int r0 = ti * TB, c0 = tj * TB, rows = min(TB, ma - r0), cols = min(TB, ma - c0);
+        // first k-chunk in flight before the accumulator (kept negated: acc = -A_ij) is read
+        ld_tile_async(T0, a.Sh + (size_t)r0 * a.ldh + k0 * TB, a.ldh, rows, TB);
+        ld_tile_async(T1, a.Sh + (size_t)c0 * a.ldh + k0 * TB, a.ldh, cols, TB);
         double acc[8][2];
 #pragma unroll
         for (int nb = 0; nb < 8; ++nb) {
             const int r = 8 * wid + gr, c = 8 * nb + 2 * gc;
-            acc[nb][0] = (r < rows && c < cols) ? a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c] : 0.0;
-            acc[nb][1] = (r < rows && c + 1 < cols) ? a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c + 1] : 0.0;
+            acc[nb][0] = (r < rows && c < cols) ? -a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c] : 0.0;
+            acc[nb][1] = (r < rows && c + 1 < cols) ? -a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c + 1] : 0.0;
         }
-        ld_tile_async(T0, a.Sh + (size_t)r0 * a.ldh + k0 * TB, a.ldh, rows, TB);
-        ld_tile_async(T1, a.Sh + (size_t)c0 * a.ldh + k0 * TB, a.ldh, cols, TB);
         for (int k = k0; k < k1; ++k) {
             double *X = ((k - k0) & 1) ? T2 : T0, *Y = ((k - k0) & 1) ? T3 : T1;
             if (k + 1 < k1) {
@@ -944,14 +963,14 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
                 asm volatile("cp.async.wait_group 0;\n" ::);
             }
             __syncthreads();
-            tile_sub_xyt_regs(acc, X, Y);
+            tile_add_xyt_regs(acc, X, Y);
             __syncthreads();
         }
 #pragma unroll
         for (int nb = 0; nb < 8; ++nb) {
             const int r = 8 * wid + gr, c = 8 * nb + 2 * gc;
-            if (r < rows && c < cols) a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c] = acc[nb][0];
-            if (r < rows && c + 1 < cols) a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c + 1] = acc[nb][1];
+            if (r < rows && c < cols) a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c] = -acc[nb][0];
+            if (r < rows && c + 1 < cols) a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c + 1] = -acc[nb][1];
         }
     };
     const int npan = nt >= a.pw_min ? (nt + kPW - 1) / kPW : 0;
