@@ -116,6 +116,13 @@ __device__ __forceinline__ void ld_tile(double *S, const double *src, int ld, in
     }
     asm volatile("cp.async.wait_all;\n" ::);
 }
+// S[r][c] = src[c * ld + r] (the transposed rows x cols block), zero padded
+__device__ __forceinline__ void ld_tile_T(double *S, const double *src, int ld, int rows, int cols) {
+    for (int e = threadIdx.x; e < TB * TB; e += NT) {
+        const int c = e >> 6, r = e & 63;
+        S[r * TS + c] = (r < rows && c < cols) ? src[(size_t)c * ld + r] : 0.0;
+    }
+}
 __device__ __forceinline__ void st_tile(const double *S, double *dst, int ld, int rows, int cols) {
     for (int e = threadIdx.x; e < TB * TB; e += NT) {
         int r = e >> 6, c = e & 63;
@@ -766,23 +773,30 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
                 st_tile(T3, a.T, TB, TB, TB);
             }
             GSYNC();
+            // K is kept in its LOWER triangle: column k's tile i is (i, k) for i > k and the
+            // transpose of (k, i) for i < k
+            auto ld_colk = [&](double *S, int ti, int rows) {
+                if (ti > k) ld_tile(S, a.K + (size_t)(ti * TB) * a.ldk + kc0, a.ldk, rows, kn);
+                else ld_tile_T(S, a.K + (size_t)kc0 * a.ldk + ti * TB, a.ldk, rows, kn);
+            };
             for (int b = bid; b < nt - 1; b += G) {      // U_i = A_ik P, i != k
                 const int ti = b < k ? b : b + 1;
                 const int r0 = ti * TB, rows = min(TB, nS - r0);
-                ld_tile(T0, a.K + (size_t)r0 * a.ldk + kc0, a.ldk, rows, kn);
+                ld_colk(T0, ti, rows);
                 ld_tile(T1, a.T, TB, TB, TB);
                 __syncthreads();
                 tile_xyt(T2, T0, T1, 1.0, false);
                 st_tile(T2, a.U + (size_t)r0 * TB, TB, rows, TB);
             }
             GSYNC();
-            for (int b = bid; b < (nt - 1) * (nt - 1); b += G) {   // A_ij -= U_i A_jk^T
-                const int bi = b / (nt - 1), bj = b % (nt - 1);
+            for (int b = bid; b < (nt - 1) * nt / 2; b += G) {   // A_ij -= U_i A_jk^T, lower tiles
+                int bi = 0, bj = b;
+                while (bj > bi) { bj -= bi + 1; ++bi; }
                 const int ti = bi < k ? bi : bi + 1, tj = bj < k ? bj : bj + 1;
                 const int r0 = ti * TB, c0 = tj * TB;
                 const int rows = min(TB, nS - r0), cols = min(TB, nS - c0);
                 ld_tile(T0, a.U + (size_t)r0 * TB, TB, rows, TB);
-                ld_tile(T1, a.K + (size_t)c0 * a.ldk + kc0, a.ldk, cols, kn);
+                ld_colk(T1, tj, cols);
                 ld_tile(T2, a.K + (size_t)r0 * a.ldk + c0, a.ldk, rows, cols);
                 __syncthreads();
                 tile_xyt(T2, T0, T1, -1.0, true);
@@ -792,8 +806,8 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
             for (size_t e = (size_t)bid * NT + tid; e < (size_t)nS * kn; e += (size_t)G * NT) {
                 const int r = (int)(e / kn), c = (int)(e % kn);
                 const double v = (r >= kc0 && r < kc0 + kn) ? -a.T[(r - kc0) * TB + c] : a.U[(size_t)r * TB + c];
-                a.K[(size_t)r * a.ldk + kc0 + c] = v;
-                a.K[(size_t)(kc0 + c) * a.ldk + r] = v;
+                if (r >= kc0) a.K[(size_t)r * a.ldk + kc0 + c] = v;        // lower: (r, k) block
+                else a.K[(size_t)(kc0 + c) * a.ldk + r] = v;                // lower: (k, r) block
             }
             GSYNC();
         }
@@ -814,7 +828,8 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
     for (int row = pb * (NT / 32) + wid; pb >= 0 && row < m; row += pG * (NT / 32)) {
         const int ai = row / 3, i = row % 3;
         double acc = 0.0;
-        for (int bb = lane; bb < nS; bb += 32) acc -= a.K[(size_t)ai * a.ldk + bb] * a.yS[3 * bb + i];
+        for (int bb = lane; bb < nS; bb += 32)           // -Sigma_s in K's lower triangle
+            acc -= a.K[(size_t)max(ai, bb) * a.ldk + min(ai, bb)] * a.yS[3 * bb + i];
         acc = warp_sum(acc);
         if (lane == 0) a.Sh[(size_t)m * a.ldh + row] = acc - a.gc[row];
     }
