@@ -1306,7 +1306,7 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             const int cS = h->capS;
             h->gcS.exact(3 * (size_t)h->capS + 3);
             h->Bc.exact((size_t)9 * cS * cS);
-            h->ldh = 3 * cS + 8;
+            h->ldh = (3 * cS + 8 + 1) & ~1;   // even: 16-byte aligned rows (cp.async 16 B)
             h->Sh.exact((size_t)(3 * cS + 1) * h->ldh);
             // large systems: Li tiles [nt+1][64][64]; small: D blocks [nt+1][512] + X tiles [nt][64][64]
             h->Lstore.exact((size_t)((3 * cS + 1 + 63) / 64 + 1) * (64 * 64 + 512));

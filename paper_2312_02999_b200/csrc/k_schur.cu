@@ -988,6 +988,90 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
             if (r < rows && c + 1 < cols) a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c + 1] = -acc[nb][1];
         }
     };
+    // A_ij -= sum_k L_ik L_jk^T for the 128 x 64 block of row tiles (ti, ti + 1) x column tile tj
+    // (ti + 1 may lie beyond the matrix: zero rows, not stored).  k is streamed in 32-wide chunks
+    // through a 3-stage pipeline of 16-byte cp.async copies; warp w owns rows 16w .. 16w + 15 (two
+    // 8-row groups) x 64 columns, so per 4-wide k step 2 + 8 fragment loads feed 16 independent
+    // DMMAs.  The accumulator is kept negated (adds only).
+    constexpr int KC = 32, XS = 36;
+    static_assert(3 * (128 + 64) * XS * (int)sizeof(double) <= kSchurSmem, "pair pipeline smem");
+    auto update_pair = [&](int ti, int tj, int k0, int k1) {
+        const int gr = lane >> 2, gc = lane & 3;
+        const int r0 = ti * TB, c0 = tj * TB;
+        const int rows = min(2 * TB, ma - r0), cols = min(TB, ma - c0);
+        double *Xs = sm, *Ys = sm + 3 * 128 * XS;
+        const int kbeg = k0 * TB, nch = (k1 - k0) * TB / KC;
+        auto issue = [&](int ch) {
+            if (ch < nch) {
+                const int sg = ch % 3, kc = kbeg + ch * KC;
+                double *X = Xs + sg * 128 * XS, *Y = Ys + sg * 64 * XS;
+                for (int e = tid; e < 3 * 1024; e += NT) {      // 2048 X pieces, then 1024 Y pieces
+                    const bool isx = e < 2048;
+                    const int ee = isx ? e : e - 2048, r = ee >> 4, c2 = (ee & 15) * 2;
+                    double *dst = (isx ? X : Y) + r * XS + c2;
+                    if (r < (isx ? rows : cols)) {
+                        const double *src = a.Sh + (size_t)((isx ? r0 : c0) + r) * a.ldh + kc + c2;
+                        const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src));
+                    } else {
+                        dst[0] = 0.0;
+                        dst[1] = 0.0;
+                    }
+                }
+            }
+            asm volatile("cp.async.commit_group;\n" ::);
+        };
+        issue(0);
+        issue(1);
+        double acc[2][8][2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int nb = 0; nb < 8; ++nb) {
+                const int r = 16 * wid + 8 * h + gr, c = 8 * nb + 2 * gc;
+                acc[h][nb][0] = (r < rows && c < cols) ? -a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c] : 0.0;
+                acc[h][nb][1] = (r < rows && c + 1 < cols) ? -a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c + 1] : 0.0;
+            }
+        for (int ch = 0; ch < nch; ++ch) {
+            issue(ch + 2);
+            asm volatile("cp.async.wait_group 2;\n" ::);
+            __syncthreads();
+            const double *X = Xs + (ch % 3) * 128 * XS + (16 * wid + gr) * XS + gc;
+            const double *Y = Ys + (ch % 3) * 64 * XS + gr * XS + gc;
+#pragma unroll
+            for (int k4 = 0; k4 < KC / 4; ++k4) {
+                const double a0 = X[4 * k4], a1 = X[8 * XS + 4 * k4];
+#pragma unroll
+                for (int nb = 0; nb < 8; ++nb) {
+                    const double bv = Y[8 * nb * XS + 4 * k4];
+                    dmma_884(acc[0][nb][0], acc[0][nb][1], a0, bv);
+                    dmma_884(acc[1][nb][0], acc[1][nb][1], a1, bv);
+                }
+            }
+            __syncthreads();                       // stage ch % 3 is refilled by issue(ch + 3)
+        }
+        asm volatile("cp.async.wait_group 0;\n" ::);
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int nb = 0; nb < 8; ++nb) {
+                const int r = 16 * wid + 8 * h + gr, c = 8 * nb + 2 * gc;
+                if (r < rows && c < cols) a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c] = -acc[h][nb][0];
+                if (r < rows && c + 1 < cols) a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c + 1] = -acc[h][nb][1];
+            }
+    };
+    // pairs of row tiles (ti, ti + 1), ti = tj + 2p, over the tile columns [ja, jb): linear index b
+    auto pair_of = [&](int b, int ja, int &ti, int &tj) {
+        int j = ja;
+        while (b >= (nt - j + 1) / 2) { b -= (nt - j + 1) / 2; ++j; }
+        tj = j;
+        ti = j + 2 * b;
+    };
+    auto pairs_in = [&](int ja, int jb) {
+        int t = 0;
+        for (int j = ja; j < jb; ++j) t += (nt - j + 1) / 2;
+        return t;
+    };
     const int npan = nt >= a.pw_min ? (nt + kPW - 1) / kPW : 0;
     for (int q = 0; q < npan; ++q) {
         const int c0t = q * kPW, c1t = min(nt, c0t + kPW);       // panel q: tile columns [c0t, c1t)
@@ -1014,12 +1098,11 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
             unsigned *ctr = a.bar + q;
             unsigned nbar = 0;
             if (q > 0) {        // panel q-1 applied to panel q's tiles (i, j), c0t <= j < c1t, i >= j
-                int tot = 0;
-                for (int j = c0t; j < c1t; ++j) tot += nt - j;
+                const int tot = pairs_in(c0t, c1t);
                 for (int b = bid; b < tot; b += npg) {
-                    int j = c0t, bb = b;
-                    while (bb >= nt - j) { bb -= nt - j; ++j; }
-                    update_tile(j + bb, j, c0t - kPW, c0t);
+                    int ti, tj;
+                    pair_of(b, c0t, ti, tj);
+                    update_pair(ti, tj, c0t - kPW, c0t);
                 }
                 group_bar(ctr, ++nbar * npg);
             }
@@ -1044,24 +1127,22 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
                 }
                 group_bar(ctr, ++nbar * npg);
                 if (k + 1 < c1t) {          // A_ij -= L_ik L_jk^T, k < j < c1t, i >= j
-                    int tot = 0;
-                    for (int j = k + 1; j < c1t; ++j) tot += nt - j;
+                    const int tot = pairs_in(k + 1, c1t);
                     for (int b = bid; b < tot; b += npg) {
-                        int j = k + 1, bb = b;
-                        while (bb >= nt - j) { bb -= nt - j; ++j; }
-                        update_tile(j + bb, j, k, k + 1);
+                        int ti, tj;
+                        pair_of(b, k + 1, ti, tj);
+                        update_pair(ti, tj, k, k + 1);
                     }
                     group_bar(ctr, ++nbar * npg);
                 }
             }
             if (a.prof && bid == 0 && tid == 0 && q < 100) { a.prof[600 + q] = gtimer_s(); a.prof[800 + q] = npg; }
         } else if (q > 0) {     // panel q-1 applied to the tile columns right of panel q
-            const int ub = bid - npg, nu = G - npg;
-            for (int b = ub; b < rr * (rr + 1) / 2; b += nu) {
-                int i = 0, bb = b;
-                while (bb >= rr - i) { bb -= rr - i; ++i; }
-                const int tj = c1t + i, ti = tj + bb;
-                update_tile(ti, tj, c0t - kPW, c0t);
+            const int ub = bid - npg, nu = G - npg, tot = pairs_in(c1t, nt);
+            for (int b = ub; b < tot; b += nu) {
+                int ti, tj;
+                pair_of(b, c1t, ti, tj);
+                update_pair(ti, tj, c0t - kPW, c0t);
             }
             if (a.prof && tid == 0 && q < 100) atomicMax(a.prof + 700 + q, gtimer_s());   // update group done
         }
