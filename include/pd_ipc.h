@@ -193,6 +193,24 @@ int pd_ipc_set_debug(pd_ipc *h, int32_t level);
 int pd_ipc_debug_factor_solve(const pd_ipc_mesh *mesh, const double *rest_pos, const double *b,
                               double *x, int64_t *stats);
 
+/* Embedding construction (host only, no GPU used): the rows of W for points
+ * embedded in the rest tet mesh -- the paper's embedded collision surface s = W x (PAPER.md:143,
+ * :161; SPEC.md:53-61 build_embedding).  For point q, embed_tet[q] = the LOWEST-index tet whose
+ * barycentric coordinates of the point are all >= -tol (SPEC.md:81 tie rule: a point on a shared
+ * face goes to the lower-index tet), embed_w[q][4] = those coordinates with the negatives clamped
+ * to 0 and renormalised to sum 1 (so W rest_pos reproduces the point within ~tol x edge length).
+ * tets [n_tets][4], rest_pos [n_verts][3], points [n_points][3]; outputs caller-owned
+ * embed_tet [n_points], embed_w [n_points][4] (the pd_ipc_mesh fields).  tol <= 0 means 1e-9.
+ * PD_IPC_E_ARG on NULL / negative sizes, PD_IPC_E_MESH on a bad tet index or a point outside
+ * every tet. */
+int pd_ipc_build_embedding(const int32_t *tets, int32_t n_tets, const double *rest_pos, int32_t n_verts,
+                           const double *points, int32_t n_points, double tol, int32_t *embed_tet,
+                           double *embed_w);
+
+/* Export of the embedded surface of sequence seq at its current positions: out [n_surf_verts][3]
+ * = s = W x, computed on the device.  Caller-owned out. */
+int pd_ipc_surface_positions(const pd_ipc *h, int32_t seq, double *out);
+
 /* Host-only check (no GPU used): number of (surface edge, surface triangle) pairs sharing no
  * vertex whose segment strictly crosses the triangle, with the surface at s = W x
  * (PAPER.md:143), x [n_verts][3].  This is the crossing half of the intersection-free check

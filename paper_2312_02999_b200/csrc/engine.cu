@@ -253,7 +253,7 @@ struct pd_ipc {
     DBuf<int> f_uoff, f_urow_sn, f_rc_ptr, f_rc_idx, f_urel, f_ch_ptr, f_ch;
     // sequences: host state + batched device arrays [B][...]
     std::vector<std::unique_ptr<Seq>> seqs;
-    DBuf<double4> x_all, gel_all, dx_all, s_all, ds_all, xstage;
+    DBuf<double4> x_all, gel_all, dx_all, s_all, ds_all, xstage, surf_out;
     DBuf<double> A6_all, p_all, fc_all, G_all, Yw_all, Z_all, dscal_all;
     DBuf<int> dint_all;
     // reuse slots: V_s [nf][ldv], K_s / -Sigma_s [capS][capS], the S they belong to
@@ -1525,7 +1525,7 @@ void pd_ipc_destroy(pd_ipc *h) {
     rel(h->nS_slot);
     rel(h->x_all); rel(h->gel_all); rel(h->dx_all); rel(h->s_all); rel(h->ds_all); rel(h->A6_all); rel(h->p_all);
     rel(h->fc_all); rel(h->G_all); rel(h->Yw_all); rel(h->Z_all); rel(h->dscal_all); rel(h->dint_all);
-    rel(h->xstage); rel(h->A9stage); rel(h->blo);
+    rel(h->xstage); rel(h->surf_out); rel(h->A9stage); rel(h->blo);
     rel(h->G2); rel(h->Yel_all); rel(h->Zf_all); rel(h->bw_P2); rel(h->rpos); rel(h->ts_done2); rel(h->bw_cnt2); rel(h->bhi); rel(h->hcnt); rel(h->hstart); rel(h->hent);
     rel(h->qcnt); rel(h->qoff); rel(h->qlist); rel(h->gsq);
     rel(h->cand_tmp); rel(h->akeys); rel(h->flag); rel(h->pos); rel(h->ctype); rel(h->atype); rel(h->ids);
@@ -1664,6 +1664,38 @@ int pd_ipc_get_info(const pd_ipc *h, int64_t *info, int32_t n) {
     const int k = std::max(0, std::min<int>(n, 16));
     for (int i = 0; i < k; ++i) info[i] = v[i];
     return k;
+}
+
+int pd_ipc_build_embedding(const int32_t *tets, int32_t n_tets, const double *rest_pos, int32_t n_verts,
+                           const double *points, int32_t n_points, double tol, int32_t *embed_tet,
+                           double *embed_w) {
+    std::string err;
+    const int rc = build_embedding(n_verts, n_tets, tets, rest_pos, n_points, points, tol > 0 ? tol : 1e-9,
+                                   embed_tet, embed_w, err);
+    return rc ? fail(nullptr, rc, err) : PD_IPC_OK;
+}
+
+int pd_ipc_surface_positions(const pd_ipc *h_, int32_t seq, double *out) {
+    pd_ipc *h = const_cast<pd_ipc *>(h_);
+    if (!h || !out) return fail(nullptr, PD_IPC_E_ARG, "NULL argument");
+    if (seq < 0 || seq >= (int)h->seqs.size()) return fail(h, PD_IPC_E_ARG, "bad sequence");
+    if (h->Ns == 0) return PD_IPC_OK;
+    try {
+        CK(cudaSetDevice(h->device));
+        h->surf_out.ensure(h->Ns);
+        launch_surface(h->Wp.p, h->Wc.p, h->Wv.p, h->x(seq), h->Ns, h->surf_out.p, h->st);
+        std::vector<double4> s4(h->Ns);
+        CK(cudaMemcpyAsync(s4.data(), h->surf_out.p, sizeof(double4) * h->Ns, cudaMemcpyDeviceToHost, h->st));
+        CK(cudaStreamSynchronize(h->st));
+        for (int j = 0; j < h->Ns; ++j) {
+            out[3 * (size_t)j] = s4[j].x;
+            out[3 * (size_t)j + 1] = s4[j].y;
+            out[3 * (size_t)j + 2] = s4[j].z;
+        }
+    } catch (const CudaError &e) {
+        return fail(h, e.code, e.what());
+    }
+    return PD_IPC_OK;
 }
 
 int64_t pd_ipc_debug_crossings(const pd_ipc_mesh *mesh, const double *rest_pos, const double *x) {

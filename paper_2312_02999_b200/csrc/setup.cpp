@@ -696,3 +696,113 @@ long long surface_edge_triangle_crossings(const HostMesh &m, const double *x) {
 }
 
 }  // namespace pdipc
+
+namespace pdipc {
+
+// ------------------------------------------------------------------ embedding --
+// W rows for points embedded in the rest tet mesh ("embedded surface"; SPEC.md:53-61
+// build_embedding, :81 tie rule): the lowest-index tet whose barycentric coordinates of the point
+// are all >= -tol; weights = those coordinates with negatives (|.| <= tol) clamped to 0 and the
+// row renormalised to sum 1.  Uniform grid over the tets' rest boxes.
+int build_embedding(int n, int T, const int32_t *tets, const double *X, int np, const double *pts, double tol,
+                    int32_t *etet, double *ew, std::string &err) {
+    if (n <= 0 || T <= 0 || np < 0 || !tets || !X || (np > 0 && (!pts || !etet || !ew))) {
+        err = "build_embedding: bad arguments";
+        return PD_IPC_E_ARG;
+    }
+    for (int t = 0; t < 4 * T; ++t)
+        if (tets[t] < 0 || tets[t] >= n) {
+            err = "build_embedding: tet vertex index out of range";
+            return PD_IPC_E_MESH;
+        }
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300}, el = 0.0;
+    for (int v = 0; v < n; ++v)
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = std::min(lo[a], X[3 * (size_t)v + a]);
+            hi[a] = std::max(hi[a], X[3 * (size_t)v + a]);
+        }
+    for (int t = 0; t < T; ++t) {
+        const double *p0 = X + 3 * (size_t)tets[4 * t], *p1 = X + 3 * (size_t)tets[4 * t + 1];
+        el += std::sqrt((p1[0] - p0[0]) * (p1[0] - p0[0]) + (p1[1] - p0[1]) * (p1[1] - p0[1]) +
+                        (p1[2] - p0[2]) * (p1[2] - p0[2]));
+    }
+    const double cell = std::max(el / T, 1e-300);
+    int dim[3];
+    for (int a = 0; a < 3; ++a) dim[a] = std::max(1, std::min(1024, (int)std::floor((hi[a] - lo[a]) / cell) + 1));
+    auto cid = [&](double v, int a) {
+        const double c = (hi[a] > lo[a]) ? (v - lo[a]) / (hi[a] - lo[a]) * dim[a] : 0.0;
+        return std::min(dim[a] - 1, std::max(0, (int)std::floor(c)));
+    };
+    std::vector<std::pair<long long, int>> ent;
+    for (int t = 0; t < T; ++t) {
+        int c0[3], c1[3];
+        for (int a = 0; a < 3; ++a) {
+            double l = 1e300, h = -1e300;
+            for (int k = 0; k < 4; ++k) {
+                const double v = X[3 * (size_t)tets[4 * t + k] + a];
+                l = std::min(l, v);
+                h = std::max(h, v);
+            }
+            const double pad = 1e-9 * cell;   // points within tolerance just outside the box
+            c0[a] = cid(l - pad, a);
+            c1[a] = cid(h + pad, a);
+        }
+        for (int i = c0[0]; i <= c1[0]; ++i)
+            for (int j = c0[1]; j <= c1[1]; ++j)
+                for (int k = c0[2]; k <= c1[2]; ++k) ent.push_back({((long long)i * dim[1] + j) * dim[2] + k, t});
+    }
+    std::sort(ent.begin(), ent.end());   // within a cell: increasing tet index
+    for (int q = 0; q < np; ++q) {
+        const double *p = pts + 3 * (size_t)q;
+        const long long key = ((long long)cid(p[0], 0) * dim[1] + cid(p[1], 1)) * dim[2] + cid(p[2], 2);
+        auto it = std::lower_bound(ent.begin(), ent.end(), std::make_pair(key, -1));
+        int found = -1;
+        double lam[4] = {0, 0, 0, 0};
+        for (; it != ent.end() && it->first == key; ++it) {
+            const int t = it->second;
+            const double *x0 = X + 3 * (size_t)tets[4 * t];
+            double D[3][3], r[3];
+            for (int a = 0; a < 3; ++a) {
+                for (int c = 0; c < 3; ++c) D[a][c] = X[3 * (size_t)tets[4 * t + c + 1] + a] - x0[a];
+                r[a] = p[a] - x0[a];
+            }
+            const double det = D[0][0] * (D[1][1] * D[2][2] - D[1][2] * D[2][1]) -
+                               D[0][1] * (D[1][0] * D[2][2] - D[1][2] * D[2][0]) +
+                               D[0][2] * (D[1][0] * D[2][1] - D[1][1] * D[2][0]);
+            if (!(std::fabs(det) > 0)) continue;
+            double l[3];   // Cramer's rule: D l = r
+            for (int c = 0; c < 3; ++c) {
+                double M[3][3];
+                for (int a = 0; a < 3; ++a)
+                    for (int b = 0; b < 3; ++b) M[a][b] = b == c ? r[a] : D[a][b];
+                l[c] = (M[0][0] * (M[1][1] * M[2][2] - M[1][2] * M[2][1]) -
+                        M[0][1] * (M[1][0] * M[2][2] - M[1][2] * M[2][0]) +
+                        M[0][2] * (M[1][0] * M[2][1] - M[1][1] * M[2][0])) / det;
+            }
+            const double l0 = 1.0 - l[0] - l[1] - l[2];
+            if (l0 >= -tol && l[0] >= -tol && l[1] >= -tol && l[2] >= -tol) {
+                if (found < 0 || t < found) {
+                    found = t;
+                    lam[0] = l0;
+                    lam[1] = l[0];
+                    lam[2] = l[1];
+                    lam[3] = l[2];
+                }
+            }
+        }
+        if (found < 0) {
+            err = "build_embedding: point " + std::to_string(q) + " lies outside every tet";
+            return PD_IPC_E_MESH;
+        }
+        double sum = 0.0;
+        for (int k = 0; k < 4; ++k) {
+            lam[k] = std::max(0.0, lam[k]);
+            sum += lam[k];
+        }
+        etet[q] = found;
+        for (int k = 0; k < 4; ++k) ew[4 * (size_t)q + k] = lam[k] / sum;
+    }
+    return 0;
+}
+
+}  // namespace pdipc

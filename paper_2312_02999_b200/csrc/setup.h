@@ -76,4 +76,9 @@ int factorize(HostMesh &m, HostFactor &f, std::string &err);
 // distance) configuration is left to the distance check.  Uniform grid over the triangles.
 long long surface_edge_triangle_crossings(const HostMesh &m, const double *x);
 
+// W rows of points embedded in the rest mesh (lowest-index containing tet, barycentric weights
+// clamped at -tol..0 and renormalised); 0 or PD_IPC_E_* with err filled.
+int build_embedding(int n, int T, const int32_t *tets, const double *X, int np, const double *pts, double tol,
+                    int32_t *etet, double *ew, std::string &err);
+
 }  // namespace pdipc

@@ -83,6 +83,12 @@ lib.pd_ipc_debug_factor_solve.argtypes = [C.POINTER(pd_ipc_mesh), C.POINTER(C.c_
                                           C.POINTER(C.c_double), C.POINTER(C.c_double),
                                           C.POINTER(C.c_int64)]
 lib.pd_ipc_debug_factor_solve.restype = C.c_int
+lib.pd_ipc_build_embedding.argtypes = [C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_double), C.c_int32,
+                                       C.POINTER(C.c_double), C.c_int32, C.c_double, C.POINTER(C.c_int32),
+                                       C.POINTER(C.c_double)]
+lib.pd_ipc_build_embedding.restype = C.c_int
+lib.pd_ipc_surface_positions.argtypes = [_P, C.c_int32, C.POINTER(C.c_double)]
+lib.pd_ipc_surface_positions.restype = C.c_int
 lib.pd_ipc_debug_crossings.argtypes = [C.POINTER(pd_ipc_mesh), C.POINTER(C.c_double), C.POINTER(C.c_double)]
 lib.pd_ipc_debug_crossings.restype = C.c_int64
 
@@ -100,7 +106,8 @@ lib.pd_ipc_launch_count.restype = C.c_int64
 EXPORTED = ["pd_ipc_create", "pd_ipc_step", "pd_ipc_positions", "pd_ipc_destroy",
             "pd_ipc_last_error", "pd_ipc_set_positions", "pd_ipc_set_debug",
             "pd_ipc_get_projections", "pd_ipc_get_contacts", "pd_ipc_get_vector", "pd_ipc_get_pair_terms",
-            "pd_ipc_build_info", "pd_ipc_debug_factor_solve", "pd_ipc_debug_crossings", "pd_ipc_set_timing",
+            "pd_ipc_build_info", "pd_ipc_debug_factor_solve", "pd_ipc_debug_crossings",
+            "pd_ipc_build_embedding", "pd_ipc_surface_positions", "pd_ipc_set_timing",
             "pd_ipc_kernel_times", "pd_ipc_kernel_name", "pd_ipc_launch_count", "pd_ipc_get_info"]
 
 
@@ -299,6 +306,26 @@ def debug_factor_solve(scene, b=None):
                                        stats.ctypes.data_as(C.POINTER(C.c_int64)))
     _check(rc)
     return x, stats
+
+
+def build_embedding(tets, rest, points, tol=1e-9):
+    """Host-only: (embed_tet [n_points], embed_w [n_points][4]) of points in the rest tet mesh."""
+    tets = _i32(tets).reshape(-1, 4)
+    rest = _f64(rest).reshape(-1, 3)
+    points = _f64(points).reshape(-1, 3)
+    et = np.empty(points.shape[0], np.int32)
+    ew = np.empty((points.shape[0], 4))
+    rc = lib.pd_ipc_build_embedding(_ip(tets), tets.shape[0], _dp(rest), rest.shape[0], _dp(points),
+                                    points.shape[0], float(tol), _ip(et), _dp(ew))
+    _check(rc)
+    return et, ew
+
+
+def surface_positions(h, n_surf_verts, seq=0):
+    """s = W x of sequence seq, [n_surf_verts][3] (the embedded surface export)."""
+    out = np.empty((n_surf_verts, 3))
+    _check(lib.pd_ipc_surface_positions(h, seq, _dp(out)), h)
+    return out
 
 
 def debug_crossings(scene, x):
