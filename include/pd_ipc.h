@@ -100,7 +100,18 @@ typedef struct {
                                    of the collision region), K_s gathered from
                                    G2, y_S from the base solve, dx from one more forward solve of
                                    the S-sparse right-hand side;
+                                 3 pcg: the paper's baseline (Eq. 5, SURVEY 8(f)
+                                   f2) -- conjugate gradients on L^-1 H-hat L^-T, preconditioned by
+                                   the prefactorised L, to a relative residual cg_tol (iterative:
+                                   dx agrees with the direct backends to ~cg_tol x conditioning);
                                  0 auto: gather when |R| >= 1024, else panel                    */
+    double cg_tol;            /* pcg: relative residual ||r|| / ||r0|| to stop at (<= 0: 1e-12)  */
+    int32_t cg_max_iters;     /* pcg: iteration cap per solve (<= 0: 10000)                      */
+    double conv_tol;          /* > 0: "while not converged" (SURVEY Z10 option): a
+                                 sequence stops at the first iteration whose update moves no free
+                                 vertex by conv_tol or more (max |alpha dx|, meters); its later
+                                 iterations in the call leave it untouched.  0: the fixed n_iters
+                                 count (the default, used by every benchmark)                   */
 } pd_ipc_options;
 
 #define PD_IPC_DBG_LARGE_SCHUR 1
@@ -109,7 +120,8 @@ typedef struct {
 
 /* Per sequence, describing the LAST iteration of the last pd_ipc_step call. */
 typedef struct {
-    int32_t iters;            /* iterations run in the last step call                         */
+    int32_t iters;            /* iterations applied in the last step call (n_iters, or fewer
+                                 when conv_tol stopped the sequence)                          */
     int32_t n_cand;           /* broad-phase candidates (static, d_hat-inflated)              */
     int32_t n_active;         /* |C| = PT + EE active pairs                                   */
     int32_t n_S;              /* n_c = |S|                                                     */
@@ -122,7 +134,7 @@ typedef struct {
     double ms[6];             /* device time per stage over the call: IPC, G-Step, CCD, LS,
                                  Misc, total (Table 1 categories)               */
     int32_t sigma_reused;     /* iterations of the call that reused V_s, K_s, Sigma_s (S same) */
-    int32_t reserved;
+    int32_t cg_iters;         /* pcg backend: CG iterations summed over the call's iterations    */
 } pd_ipc_stats;
 
 /* Create a solver: validates the mesh, computes B_i = D_m^{-1} and w_i = det/6, assembles the

@@ -126,6 +126,20 @@ class OracleSolver:
         return 0.0, self.ls_max_halvings + 1, STALL, 0.0
 
     # ------------------------------------------------------------------------------------
+    def run_until_converged(self, x: np.ndarray, A9: np.ndarray, tol: float, max_iters: int, log=None):
+        """Algorithm 1's "while not converged" with SURVEY Z10's optional rule: stop
+        after the first iteration whose update moves no vertex by tol or more (max |alpha dx|).
+        Returns (x, iterations run)."""
+        for k in range(max_iters):
+            it = self.iterate(x, A9)
+            if log is not None:
+                log.append(it)
+            x = it["x"]
+            if np.abs(it["alpha"] * it["dx"]).max() < tol:
+                return x, k + 1
+        return x, max_iters
+
+    # ------------------------------------------------------------------------------------
     def run_frame(self, x: np.ndarray, A9: np.ndarray, n_iters: int, log=None):
         """Algorithm 1 for one frame: N fixed iterations from the warm start x (Z10)."""
         for _ in range(n_iters):

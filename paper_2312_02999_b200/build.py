@@ -12,7 +12,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-Wno-deprecated-gpu-targets", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
 # translation units; the contact unit must not contract a*b+c into FMA (bit-exact distances)
-UNITS = [("k_elastic.cu", []), ("k_trisolve.cu", []), ("k_schur.cu", []), ("prims.cu", []),
+UNITS = [("k_elastic.cu", []), ("k_trisolve.cu", []), ("k_schur.cu", []), ("prims.cu", []), ("k_pcg.cu", []),
          ("k_contact.cu", ["-fmad=false"]), ("engine.cu", []), ("setup.cpp", [])]
 
 

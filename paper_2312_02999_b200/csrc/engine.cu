@@ -105,6 +105,7 @@ enum : int {
     D_SORT = 16,     // [16..18] scratch counters of the sort path
     D_LSCTR = 19,    // line-search round: blocks finished (the last one decides; reset by it)
     D_NS = 20,       // |S| of the last iteration
+    D_CONV = 21,     // [21] converged in this pd_ipc_step call, [22] iterations applied, [23] ticket
     D_STRIDE = 32,
 };
 constexpr int S_STRIDE = 16;   // doubles per sequence in dscal: [0] unused, [1] amin, [2..4] ls,
@@ -117,6 +118,9 @@ struct Seq {
     DBuf<unsigned long long> cand;   // candidate keys: static list, then the previous swept list
     bool force_sort = false;         // the next broad phases take the sort path (hash overflow)
     int slot = 0;                    // reuse slot (V_s, K_s, key)
+    int cg_iters = 0;                // pcg backend: CG iterations of the current pd_ipc_step call
+    bool converged = false;          // conv_tol reached in the current pd_ipc_step call
+    int iters_applied = 0;
     int nS = 0;
     // debug copies of the last iteration
     std::vector<int32_t> pt, ee, S;
@@ -264,6 +268,9 @@ struct pd_ipc {
     // reduced-solve backend: panel (V_s on the fly) or gather (precomputed
     // G2 = (L^-1)_RR over the region R of W-supported free vertices, n2 = |R|)
     bool gather = false;
+    bool pcg = false;                   // the paper's PCG baseline
+    DBuf<double> cg_r, cg_p, cg_z, cg_q, cg_t, cg_f, cg_R, cg_part;
+    double *cg_rr_host = nullptr;       // pinned: r.r of the last CG iteration
     int n2 = 0;
     DBuf<double> G2, Yel_all, Zf_all, bw_P2;
     DBuf<int> rpos, ts_done2, bw_cnt2;
@@ -613,6 +620,47 @@ static void enqueue_elastic(pd_ipc *h, int b0, int nb, int it) {
     CK(cudaEventRecord(h->ev_join, s2));
 }
 
+// The paper's PCG baseline (Eq. 5) for sequence b, in place of
+// the a9 Schur step: CG on M = L^-1 H-hat L^-T = I + L^-1 script-B L^-T with rhs -L^-1 Pi g-hat;
+// one iteration = backward solve of p, B-check on S, forward solve of the S-sparse result, vector
+// updates.  Host-driven (one 8-byte read per iteration for the convergence test).  Writes
+// Z_b = -z, so the common backward solve + scatter give dx = Pi^T L^-T z.
+static void pcg_solve(pd_ipc *h, int b) {
+    cudaStream_t st = h->st;
+    const DevFactor &F = h->F;
+    const int nf = h->nf;
+    int *nS_dev = h->spos.p + nf;
+    const long long us = 4 * (long long)std::max(1, F.nU);
+    auto fwd = [&](const double *rhs, double *out) {
+        launch_ts_plan(F, nullptr, h->ticket2.p + 2, 0, h->ticket2.p + 2, 0, h->ticket2.p + 3, 1, 1, h->ts_lo2.p,
+                       h->ts_hi2.p, h->ts_cnt2.p, h->ts_rem2.p, h->ts_ptr2.p, h->ticket2.p, st);
+        launch_forward_solve(F, h->ts_lo2.p, h->ts_hi2.p, h->ts_ptr2.p, nullptr, h->ts_rem2.p, h->ticket2.p, rhs, out,
+                             nullptr, h->ldv, h->Ug2.p, nullptr, h->ticket2.p + 2, 0, 1, 1, 4 * (long long)nf, us,
+                             h->nsm, nullptr, st);
+    };
+    fwd(h->G(b), h->cg_f.p);                                   // w = L^-1 Pi g-hat
+    launch_cg_init(h->cg_f.p, h->cg_r.p, h->cg_p.p, h->cg_z.p, nf, h->cg_part.p, h->cg_rr_host, st);
+    CK(cudaStreamSynchronize(st));
+    const double rr0 = *h->cg_rr_host;
+    const double tol = h->opt.cg_tol > 0 ? h->opt.cg_tol : 1e-12;
+    const int maxit = h->opt.cg_max_iters > 0 ? h->opt.cg_max_iters : 10000;
+    int it = 0;
+    while (rr0 > 0 && it < maxit) {
+        CK(dev_copy(h->cg_t.p, h->cg_p.p, sizeof(double) * 4 * nf, st));
+        launch_backward_solve(F, h->ts_done.p, h->bw_cnt.p, h->ticket.p, h->bw_P.p, h->cg_t.p, 1, 4 * (long long)nf,
+                              h->nsm, st);                     // t = L^-T p
+        launch_cg_bmul(h->Bc.p, 3 * h->capS, h->qS.p, nS_dev, h->capS, h->cg_t.p, h->cg_R.p, nf, st);
+        fwd(h->cg_R.p, h->cg_f.p);                             // f = L^-1 E_S B-check t_S
+        launch_cg_update(h->cg_f.p, h->cg_p.p, h->cg_q.p, h->cg_z.p, h->cg_r.p, nf, h->cg_part.p, it,
+                         h->cg_rr_host, st);
+        CK(cudaStreamSynchronize(st));
+        ++it;
+        if (std::sqrt(*h->cg_rr_host / rr0) <= tol) break;
+    }
+    launch_cg_finish(h->cg_z.p, h->Z(b), nf, st);
+    h->seqs[b]->cg_iters += it;
+}
+
 // (b) sequence b: a3-a6 contact stages, a8 panel (stream 3) and the a9 dense Schur step -> Z_b
 static void enqueue_contact_schur(pd_ipc *h, int b, int b0, int nb, int it) {
     cudaStream_t st = h->st;
@@ -671,7 +719,7 @@ static void enqueue_contact_schur(pd_ipc *h, int b, int b0, int nb, int it) {
         CK(cudaStreamWaitEvent(h->st3, h->ev_S, 0));
         launch_gather_gc(h->qS.p, nS_dev, h->capS, h->WTp.p, h->WTr.p, h->WTv.p, h->gsq.p, dmax, acnt, h->gcS.p,
                          h->st3);
-        if (!h->gather) enqueue_panel_forward(h, b, nS_dev, h->st3);
+        if (!h->gather && !h->pcg) enqueue_panel_forward(h, b, nS_dev, h->st3);
         CK(cudaEventRecord(h->ev_join3, h->st3));
         // B-check: fixed-point accumulation into the dense 3|S| x 3|S| block, then to double; the
         // low words of the fixed-point sums live in the (not yet used) Sigma-hat buffer
@@ -695,7 +743,9 @@ static void enqueue_contact_schur(pd_ipc *h, int b, int b0, int nb, int it) {
     const DevFactor &F = h->F;
     if (b == b0) CK(cudaStreamWaitEvent(st, h->ev_join, 0));
     kt.start(K_DENSE, st);
-    if (Nt > 0) {
+    if (Nt > 0 && h->pcg) {
+        pcg_solve(h, b);
+    } else if (Nt > 0) {
         if (h->trace_file) {
             h->sprof.ensure(1024);
             CK(dev_zero(h->sprof.p, 1024 * 8, st));
@@ -781,7 +831,8 @@ static void enqueue_ccd_ls(pd_ipc *h, int b, int b0, int nb, int it) {
             launch_ls_round(q.cand.p, ccnt, h->s(b), h->tris.p, h->edges.p, Nt, Ne, h->ds(b), h->dh, h->b0.p, ls,
                             h0, h->lspart.p, scal, h->kappa, hmax, ls_out, di + D_LSCTR, h->part.p, nb1,
                             h->part.p + nb1, nb2, amin, st);
-        launch_update(h->x(b), h->dx(b), h->q2v.p, nf, ls_out, di + D_INFO, di + D_ABORT, it, st);
+        launch_update(h->x(b), h->dx(b), h->q2v.p, nf, ls_out, di + D_INFO, di + D_ABORT, it, di + D_CONV,
+                      reinterpret_cast<unsigned long long *>(dsc + 13), h->opt.conv_tol, st);
     }
     kt.stop(K_LS, st);
     h->tm.rec(slot, 9, st);
@@ -807,7 +858,7 @@ static void run_lockstep(pd_ipc *h, int b0, int nb, int k, std::vector<int> &app
     KTimer &kt = h->kt;
     bool any_sort = false;
     for (int b = b0; b < b0 + nb; ++b) any_sort |= h->seqs[b]->force_sort;
-    const bool graph = h->graphs && !h->debug && !h->trace_file && !any_sort &&
+    const bool graph = h->graphs && !h->debug && !h->trace_file && !any_sort && !h->pcg &&
                        !(h->opt.debug_flags & PD_IPC_DBG_SORT_BROAD);
     const unsigned key = (h->buf_epoch << 1) | (kt.on ? 1u : 0u);
     const unsigned key_mask = kt.on ? kt.mask : 0u;
@@ -920,6 +971,8 @@ static void run_lockstep(pd_ipc *h, int b0, int nb, int k, std::vector<int> &app
         const double *s = sc.data() + (size_t)j * S_STRIDE;
         q.stats.sigma_reused += d[D_REUSED];
         q.nS = d[D_NS];
+        q.converged = d[D_CONV] != 0;
+        q.iters_applied = d[D_CONV + 1];
         if (d[D_ABORT]) {   // why: 1 cand, 2 |S|, 4 Up, 8/16 hash, 32 info, 64 NaN
             const int why = d[D_ABORT + 2];
             // V_s, K_s, Sigma_s of the aborted iteration (and of the batch's later, skipped ones)
@@ -1334,6 +1387,13 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             const int be = o.reduced_backend;
             const bool want = be == 2 || (be == 0 && h->n2 >= 1024);
             h->gather = m.Nt > 0 && want && h->n2 <= h->capS;
+            h->pcg = m.Nt > 0 && be == 3;
+            if (h->pcg) {
+                for (auto *bf : {&h->cg_r, &h->cg_p, &h->cg_z, &h->cg_q, &h->cg_t, &h->cg_f, &h->cg_R})
+                    bf->exact(4 * (size_t)nf);
+                h->cg_part.exact(3 * (size_t)cg_partials());
+                CK(cudaMallocHost(&h->cg_rr_host, sizeof(double)));
+            }
         }
         {   // reuse slots (V_s, K_s / -Sigma_s and the S they belong to): one per sequence when 40 %
             // of the free HBM holds them, else fewer, shared round-robin (the bit-exact key check
@@ -1434,12 +1494,21 @@ int pd_ipc_step(pd_ipc *h, const double *A_next, int32_t n_iters, pd_ipc_stats *
         // sort broad phase next) runs its remaining iterations of the batch alone.
         const int Bq = h->B;
         std::vector<std::array<double, 6>> ms(Bq, std::array<double, 6>{0, 0, 0, 0, 0, 0});
-        for (auto &sq : h->seqs) sq->stats.sigma_reused = 0;
+        for (int b = 0; b < Bq; ++b) {
+            Seq &sq = *h->seqs[b];
+            sq.stats.sigma_reused = 0;
+            sq.cg_iters = 0;
+            sq.converged = false;
+            sq.iters_applied = 0;
+            CK(dev_zero(h->dint(b) + D_CONV, 3 * sizeof(int), h->st));        // convergence state
+            CK(dev_zero(h->dscal(b) + 13, sizeof(double), h->st));
+        }
+        const bool conv = h->opt.conv_tol > 0;
         auto run_alone = [&](int b, int iters) {
             int done = 0, tries = 0;
             std::vector<int> ap;
             std::vector<std::array<double, 6>> m1(1, std::array<double, 6>{0, 0, 0, 0, 0, 0});
-            while (done < iters) {
+            while (done < iters && !(conv && h->seqs[b]->converged)) {
                 const int k = std::min(iters - done, kMaxBatch);
                 run_lockstep(h, b, 1, k, ap, m1);
                 done += ap[0];
@@ -1459,10 +1528,14 @@ int pd_ipc_step(pd_ipc *h, const double *A_next, int32_t n_iters, pd_ipc_stats *
                 for (int b = 0; b < Bq; ++b)
                     if (ap[b] < k) run_alone(b, k - ap[b]);
                 done += k;
+                bool all = conv;
+                for (int b = 0; b < Bq && all; ++b) all = h->seqs[b]->converged;
+                if (all) break;                    // every sequence converged (conv_tol)
             }
         }
         for (int b = 0; b < Bq; ++b) {
-            h->seqs[b]->stats.iters = n_iters;
+            h->seqs[b]->stats.cg_iters = h->seqs[b]->cg_iters;
+            h->seqs[b]->stats.iters = h->seqs[b]->iters_applied;
             for (int c = 0; c < 6; ++c) h->seqs[b]->stats.ms[c] = ms[b][c];
         }
         if (stats)
@@ -1526,6 +1599,8 @@ void pd_ipc_destroy(pd_ipc *h) {
     rel(h->x_all); rel(h->gel_all); rel(h->dx_all); rel(h->s_all); rel(h->ds_all); rel(h->A6_all); rel(h->p_all);
     rel(h->fc_all); rel(h->G_all); rel(h->Yw_all); rel(h->Z_all); rel(h->dscal_all); rel(h->dint_all);
     rel(h->xstage); rel(h->surf_out); rel(h->A9stage); rel(h->blo);
+    for (auto *bf : {&h->cg_r, &h->cg_p, &h->cg_z, &h->cg_q, &h->cg_t, &h->cg_f, &h->cg_R, &h->cg_part}) rel(*bf);
+    if (h->cg_rr_host) cudaFreeHost(h->cg_rr_host);
     rel(h->G2); rel(h->Yel_all); rel(h->Zf_all); rel(h->bw_P2); rel(h->rpos); rel(h->ts_done2); rel(h->bw_cnt2); rel(h->bhi); rel(h->hcnt); rel(h->hstart); rel(h->hent);
     rel(h->qcnt); rel(h->qoff); rel(h->qlist); rel(h->gsq);
     rel(h->cand_tmp); rel(h->akeys); rel(h->flag); rel(h->pos); rel(h->ctype); rel(h->atype); rel(h->ids);
@@ -1660,7 +1735,7 @@ int64_t pd_ipc_launch_count(void) { return pdipc::launch_count(); }
 int pd_ipc_get_info(const pd_ipc *h, int64_t *info, int32_t n) {
     if (!h || !info) return fail(nullptr, PD_IPC_E_ARG, "NULL argument");
     const int64_t v[16] = {h->n, h->T, h->nf, h->Ns, h->Nt, h->Ne, h->hf.nsn, h->hf.nnzL, h->hf.depth,
-                           h->capS, h->nslots, h->B, h->F.bw_nblocks, h->F.nU, h->gather ? 2 : 1, h->n2};
+                           h->capS, h->nslots, h->B, h->F.bw_nblocks, h->F.nU, h->pcg ? 3 : h->gather ? 2 : 1, h->n2};
     const int k = std::max(0, std::min<int>(n, 16));
     for (int i = 0; i < k; ++i) info[i] = v[i];
     return k;

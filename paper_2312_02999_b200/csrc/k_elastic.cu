@@ -396,11 +396,19 @@ __global__ void __launch_bounds__(256) k_gdx_partials(const double4 *__restrict_
 // x_F += alpha dx, unless this iteration raised a flag (flags = [Cholesky info, capacity bits,
 // static hash overflow, swept hash overflow]) or an earlier iteration of the batch did (abort =
 // [sticky, iteration index, why]); the first failing iteration records itself.
+// Convergence-terminated frames (SURVEY Z10 option, "while not converged"; cv =
+// [converged, iterations applied, block ticket], amax = max |alpha dx| of the iteration as the
+// bits of a non-negative double): once an iteration moves no free vertex by tol or more, the
+// sequence is converged and the rest of the pd_ipc_step call leaves it untouched.
 __global__ void k_update(double4 *__restrict__ x, const double4 *__restrict__ dx,
                          const int *__restrict__ q2v, int nf, const double *__restrict__ alpha,
-                         const int *__restrict__ flags, int *__restrict__ abort, int it) {
+                         const int *__restrict__ flags, int *__restrict__ abort, int it, int *__restrict__ cv,
+                         unsigned long long *__restrict__ amax, double tol) {
     int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= nf) return;
+    if (cv[0]) return;                                  // converged earlier in this call
+    double mv = 0.0;
+    bool applied = false;
+    if (q < nf) {
     // alpha[3] == 2: the line search saw a non-finite gradient, dx or energy (k_ls_round)
     const int nonfinite = alpha[3] == 2.0 ? 64 : 0;
     const int bad = flags[0] | flags[1] | flags[2] | flags[3] | nonfinite;
@@ -420,6 +428,31 @@ __global__ void k_update(double4 *__restrict__ x, const double4 *__restrict__ dx
     xv.y += a * d.y;
     xv.z += a * d.z;
     x[v] = xv;
+    mv = fmax(fabs(a * d.x), fmax(fabs(a * d.y), fabs(a * d.z)));
+    applied = true;
+    }
+    // block max of |alpha dx|, then the last block to finish decides (and resets the scratch)
+    __shared__ double wm[8];
+    __shared__ bool last;
+    for (int o = 16; o > 0; o >>= 1) mv = fmax(mv, __shfl_xor_sync(0xffffffffu, mv, o));
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = mv;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double b = 0.0;
+        for (int w = 0; w < (int)blockDim.x / 32; ++w) b = fmax(b, wm[w]);
+        atomicMax(amax, (unsigned long long)__double_as_longlong(b));
+        __threadfence();
+        last = atomicAdd(cv + 2, 1) == (int)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    __threadfence();
+    const double m = __longlong_as_double((long long)atomicExch(amax, 0ull));
+    cv[2] = 0;
+    if (applied || nf == 0) {
+        cv[1] += 1;                                     // iterations applied in this call
+        if (tol > 0.0 && m < tol) cv[0] = 1;
+    }
 }
 
 // scatter dx from factor order (solution of the backward solve, [nf][4], negated) to vertices
@@ -532,8 +565,9 @@ void elastic_partials(const double4 *g, const double4 *dx, const int *q2v, int n
     PDI_LAUNCH(k_elastic_partials, *nb1 + *nb2, 256, 0, st)(g, dx, q2v, nf, tets, B, w, T, *nb1, part);
 }
 void launch_update(double4 *x, const double4 *dx, const int *q2v, int nf, const double *alpha,
-                   const int *flags, int *abort, int it, cudaStream_t st) {
-    PDI_LAUNCH(k_update, (nf + 255) / 256, 256, 0, st)(x, dx, q2v, nf, alpha, flags, abort, it);
+                   const int *flags, int *abort, int it, int *cv, unsigned long long *amax, double tol,
+                   cudaStream_t st) {
+    PDI_LAUNCH(k_update, std::max(1, (nf + 255) / 256), 256, 0, st)(x, dx, q2v, nf, alpha, flags, abort, it, cv, amax, tol);
 }
 void launch_scatter_dx(const double *z, const int *q2v, int nf, double4 *dx, double *amin, int nseq, int n,
                        int amin_stride, cudaStream_t st) {

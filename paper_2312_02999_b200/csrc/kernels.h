@@ -52,8 +52,10 @@ int gdx_partials(const double4 *g, const double4 *dx, const int *q2v, int nf, do
 void elastic_partials(const double4 *g, const double4 *dx, const int *q2v, int nf, const int4 *tets,
                       const double *B, const double *w, int T, double *part, int *nb1, int *nb2,
                       cudaStream_t st);
+// cv = [converged, iterations applied, block ticket]; amax scratch; tol <= 0: fixed iteration count
 void launch_update(double4 *x, const double4 *dx, const int *q2v, int nf, const double *alpha,
-                   const int *flags, int *abort, int it, cudaStream_t st);
+                   const int *flags, int *abort, int it, int *cv, unsigned long long *amax, double tol,
+                   cudaStream_t st);
 // z [nseq][nf][4] -> dx [nseq][n]; seeds amin[sq * amin_stride] = 1
 void launch_scatter_dx(const double *z, const int *q2v, int nf, double4 *dx, double *amin, int nseq, int n,
                        int amin_stride, cudaStream_t st);
@@ -78,6 +80,18 @@ void launch_forward_solve(const DevFactor &F, const int *lo, const int *hi, cons
 constexpr int kBwSeqs = 8;
 void launch_backward_solve(const DevFactor &F, int *done, int *cnt, int *ticket, double *P, double *Z,
                            int nseq, long long zstride, int nsm, cudaStream_t st);
+
+// ---- k_pcg.cu (the paper's PCG baseline)
+// part: [3][cg_partials()] doubles; host_rr: one double the host reads (r.r of the iteration)
+void launch_cg_init(const double *w, double *r, double *p, double *z, int nf, double *part, double *host_rr,
+                    cudaStream_t st);
+void launch_cg_bmul(const double *Bc, int ldb, const int *qS, const int *nS, int capS, const double *t,
+                    double *out, int nf, cudaStream_t st);
+// CG iteration it >= 0 after f = L^-1 E_S B-check (L^-T p)_S: q = p + f, alpha, z, r, beta, p
+void launch_cg_update(const double *f, double *p, double *q, double *z, double *r, int nf, double *part, int it,
+                      double *host_rr, cudaStream_t st);
+void launch_cg_finish(const double *z, double *Z, int nf, cudaStream_t st);
+int cg_partials();
 
 // ---- k_schur.cu (fused cooperative dense Schur step, a9)
 void schur_init(int device);

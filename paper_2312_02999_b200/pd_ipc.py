@@ -32,7 +32,8 @@ class pd_ipc_options(C.Structure):
     _fields_ = [("n_seq", C.c_int32), ("device", C.c_int32), ("ls_max_halvings", C.c_int32),
                 ("accd_max_iters", C.c_int32), ("A_on_device", C.c_int32),
                 ("max_pairs", C.c_int32), ("accd_s", C.c_double), ("no_sigma_reuse", C.c_int32),
-                ("no_cand_reuse", C.c_int32), ("debug_flags", C.c_int32), ("reduced_backend", C.c_int32)]
+                ("no_cand_reuse", C.c_int32), ("debug_flags", C.c_int32), ("reduced_backend", C.c_int32),
+                ("cg_tol", C.c_double), ("cg_max_iters", C.c_int32), ("conv_tol", C.c_double)]
 
 
 class pd_ipc_stats(C.Structure):
@@ -40,10 +41,10 @@ class pd_ipc_stats(C.Structure):
                 ("n_S", C.c_int32), ("ls_trials", C.c_int32), ("flags", C.c_int32),
                 ("alpha_max", C.c_double), ("alpha", C.c_double), ("dE", C.c_double),
                 ("min_dist", C.c_double), ("ms", C.c_double * 6), ("sigma_reused", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("cg_iters", C.c_int32)]
 
     def as_dict(self):
-        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("ms", "reserved")}
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k != "ms"}
         d["ms"] = dict(zip(("ipc", "gstep", "ccd", "ls", "misc", "total"), list(self.ms)))
         return d
 
@@ -196,7 +197,8 @@ def _check(rc, h=None):
 
 def create(scene, A=None, n_seq=1, device=0, A_on_device=False, max_pairs=0,
            ls_max_halvings=30, accd_max_iters=10_000, accd_s=0.1, d_hat=None, kappa=None,
-           sigma_reuse=True, cand_reuse=True, debug_flags=0, reduced_backend=0):
+           sigma_reuse=True, cand_reuse=True, debug_flags=0, reduced_backend=0, cg_tol=1e-12,
+           cg_max_iters=10000, conv_tol=0.0):
     """pd_ipc_create on a scenes.Scene.  A: (n_seq, T, 9) host actuation (default frame 0)."""
     m = _MeshArgs(scene)
     if A is None:
@@ -204,7 +206,8 @@ def create(scene, A=None, n_seq=1, device=0, A_on_device=False, max_pairs=0,
     A = _f64(A).reshape(n_seq, -1, 9)
     opt = pd_ipc_options(n_seq, device, ls_max_halvings, accd_max_iters, int(A_on_device),
                          max_pairs, accd_s, 0 if sigma_reuse else 1, 0 if cand_reuse else 1,
-                         int(debug_flags), int(reduced_backend))
+                         int(debug_flags), int(reduced_backend), float(cg_tol), int(cg_max_iters),
+                         float(conv_tol))
     h = _P()
     rc = lib.pd_ipc_create(C.byref(m.mesh), _dp(m.rest), _dp(A),
                            float(scene.d_hat if d_hat is None else d_hat),

@@ -309,3 +309,49 @@ def test_gather_backend_lockstep_batch(P):
             s1.step(A_next=acts[j](f)[None], n_iters=10)
         assert np.array_equal(s1.positions(), xs[j]), j
         s1.close()
+
+
+# ------------------------------------------------------------------ PCG baseline (f2) -------
+@pytest.mark.parametrize("scene", ["c1", "face_small"])
+def test_pcg_backend_lockstep(P, scene):
+    """The paper's PCG baseline (Eq. 5) behind the same contract:
+    C, S bit-exact and g-hat 1e-10 as always; dx to 1e-8 relative from an iterative solve with
+    relative residual 1e-13."""
+    from oracle import OracleSolver
+    if scene == "c1":
+        sc = scenes.slabs_c1()
+        A, n = sc.actuation(0), 8
+    else:
+        sc = scenes.face_small(n_frames=2)
+        A = np.tile(np.eye(3).reshape(1, 9), (sc.n_tets, 1))
+        A[:, 4] += 0.5 * sc.meta["lip_mask"]
+        n = 6
+    o = OracleSolver(sc)
+    s = P.Solver(sc, A=A[None], reduced_backend=3, cg_tol=1e-13)
+    assert P.get_info(s.h)["reduced_backend"] == 3
+    P.set_debug(s.h, 1)
+    iters = []
+    log, _ = _lockstep(P, s, sc, o, sc.rest.copy(), A, n, check_alpha=False,
+                       on_ref=lambda k, ref, st: iters.append(st["cg_iters"]))
+    assert max(len(r["S"]) for r in log) > 50
+    assert max(iters) > 1
+    s.close()
+
+
+# ------------------------------------------------------------------ convergence stop (f3) ---
+def test_convergence_terminated_frame(P):
+    """'while not converged' with the Z10 rule max |alpha dx| < 1e-4 x bbox
+    diagonal: the GPU stops after the same number of iterations as the oracle and lands on its
+    positions; a second call from the converged state stops after one iteration."""
+    from oracle import OracleSolver
+    sc = scenes.slabs_c1()
+    tol = 1e-4 * sc.bbox_diag()
+    xr, k_ref = OracleSolver(sc).run_until_converged(sc.rest.copy(), sc.actuation(0), tol, 60)
+    assert 3 < k_ref < 60
+    s = P.Solver(sc, conv_tol=tol)
+    st = s.step(n_iters=60)[0]
+    assert abs(st["iters"] - k_ref) <= 1, (st["iters"], k_ref)
+    assert np.abs(s.positions() - xr).max() <= 1e-5 * sc.bbox_diag()
+    st = s.step(n_iters=60)[0]
+    assert st["iters"] <= 3
+    s.close()
