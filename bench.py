@@ -459,10 +459,18 @@ def run_ours(a):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # BENCH_SHARE_GPU=1 (correctness check of the multi-rank path on a 1-GPU box only: ranks share
+    # device 0 and talk over gloo; its times are not a scaling measurement)
+    share = os.environ.get("BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % torch.cuda.device_count()
     dev = f"cuda:{local}"
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     t_setup = time.perf_counter()
     sc = scenes.face_c3()
     mine = scenes.c4_assignment(a.seqs, rank, world)
@@ -549,9 +557,10 @@ def run_ours(a):
     s.close()
 
     # ---------------- gather over ranks (NCCL): times, units, checksums
+    cdev = "cpu" if share else dev
     allv = gather_rank_values([my_ms, e2e["ms"] if e2e else 0.0, float(nb * K),
-                               float(nb * e2e["steps"]) if e2e else 0.0], world, dev)
-    by_seq = gather_checksums(checks, world, dev, a.seqs)
+                               float(nb * e2e["steps"]) if e2e else 0.0], world, cdev)
+    by_seq = gather_checksums(checks, world, cdev, a.seqs)
     max_ms, max_e2e = float(allv[:, 0].max()), float(allv[:, 1].max())
     extras = {}
     if rank == 0 and world == 1 and not a.no_extras:
@@ -614,6 +623,7 @@ def run_ours(a):
         "checksum_note": "sha256 over the per-sequence position checksums in j order after the timed "
                          "steps: equal for every P iff every sequence's trajectory is bit-identical",
         "per_rank_ms": [float(v) for v in allv[:, 0]],
+        "shared_gpu_check": share,
         "local_step_c5": c5,
         **extras,
         "info": info, "setup_s": t_setup, "wall_s": t_wall,

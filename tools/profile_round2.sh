@@ -13,4 +13,4 @@ PDIPC_NO_GRAPH=1 timeout 1800 ncu --set full --import-source on --clock-control 
     > gpurun_out/ncu_full_c4.log 2>&1
 python tools/ncu_summary.py gpurun_out/full_c4.ncu-rep --traffic-json gpurun_out/ncu_traffic.json > gpurun_out/ncu_full_c4_summary.txt 2>&1
 timeout 1500 python tools/c5_sweep.py 10k 50k 100k 300k 1M 2M > gpurun_out/c5_sweep.txt 2>&1
-tail -3 gpurun_out/launches_c4_summary.txt gpurun_out/ncu_full_c4_summary.txt gpurun_out/c5_sweep.txt
+for f in gpurun_out/launches_c4_summary.txt gpurun_out/ncu_full_c4_summary.txt gpurun_out/c5_sweep.txt; do tail -n 3 $f; done
