@@ -864,11 +864,13 @@ __global__ void k_fx_to_double(long long *M, const long long *Ml, int ld, const 
                                const double *dmax, const int *acnt) {
     const int n = 3 * min(*nS_ptr, capS);
     const double inv = 1.0 / fx_scale(dmax, acnt[1]);
-    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < (size_t)n * n;
-         e += (size_t)gridDim.x * blockDim.x) {
-        const size_t off = (e / n) * ld + e % n;
-        reinterpret_cast<double *>(M)[off] = fx_get(M[off], Ml[off], inv);
-    }
+    // a warp per row, lanes over the columns (no per-element division)
+    const int lane = threadIdx.x & 31, nw = (gridDim.x * blockDim.x) >> 5;
+    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw)
+        for (int c = lane; c < n; c += 32) {
+            const size_t off = (size_t)r * ld + c;
+            reinterpret_cast<double *>(M)[off] = fx_get(M[off], Ml[off], inv);
+        }
 }
 __global__ void k_grad_pullback_fx(const double4 *__restrict__ g_el, const int *__restrict__ WTp,
                                    const int *__restrict__ WTr, const double *__restrict__ WTv,
@@ -965,12 +967,17 @@ __global__ void k_contact_prep(int *__restrict__ mark, int nf, long long *__rest
 // zero the leading 3|S| x 3|S| block of M and of M2 (when not null) in one launch
 __global__ void k_zero_square(double *M, double *M2, int ld, const int *nS_ptr, int capS) {
     const int n = 3 * min(*nS_ptr, capS);
-    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < (size_t)n * n;
-         e += (size_t)gridDim.x * blockDim.x) {
-        const size_t o = (e / n) * ld + e % n;
-        M[o] = 0.0;
-        if (M2) M2[o] = 0.0;
-    }
+    const int lane = threadIdx.x & 31, nw = (gridDim.x * blockDim.x) >> 5;
+    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw)
+        for (int c = 2 * lane; c < n; c += 64) {          // 16-byte stores where aligned
+            const size_t o = (size_t)r * ld + c;
+            M[o] = 0.0;
+            if (c + 1 < n) M[o + 1] = 0.0;
+            if (M2) {
+                M2[o] = 0.0;
+                if (c + 1 < n) M2[o + 1] = 0.0;
+            }
+        }
 }
 
 // ------------------------------------------------------------------ a10 ACCD --------------

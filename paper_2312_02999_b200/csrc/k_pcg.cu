@@ -33,11 +33,17 @@ __global__ void __launch_bounds__(kCgNT) k_cg_init(const double *__restrict__ w,
     if (threadIdx.x == 0) part[blockIdx.x] = acc;
 }
 
-// fixed-order sum of the block partials (every thread of the block gets it)
+// fixed-order sum of the block partials, broadcast to every thread of the block
 __device__ __forceinline__ double sum_parts(const double *part, int n, double *sh) {
+    __shared__ double bc;
     double v = 0.0;
     for (int b = threadIdx.x; b < n; b += blockDim.x) v += __ldcg(part + b);
-    return block_sum<kCgNT>(v, sh);
+    v = block_sum<kCgNT>(v, sh);            // valid in thread 0
+    if (threadIdx.x == 0) bc = v;
+    __syncthreads();
+    v = bc;
+    __syncthreads();
+    return v;
 }
 
 // out = sparse E_S (B-check t_S): rows of S get B-check (3|S| x 3|S|, ld ldb) times t gathered on S
