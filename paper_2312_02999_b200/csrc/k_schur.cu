@@ -77,6 +77,9 @@ struct SchurArgs {
     const int *rpos;            // [nf] index of a factor position in R, -1 outside (gather mode)
     const double *Yel;          // [nf][4] y_el (gather mode)
     unsigned *bar;              // [kMaxPanels] group-barrier counters of the large-system P3
+    int phase;                  // 0: P0-P5; large systems split over three launches: 1 = P0-P2,
+                                // then k_chol_large (P3), then 2 = P4-P5 (small systems: the
+                                // phase-1 launch does everything, the others return at once)
 };
 constexpr int kMaxPanels = 512;
 
@@ -104,8 +107,9 @@ __device__ __forceinline__ unsigned long long gtimer_s() {
 // load a rows x cols block (row-major, ld) into smem S (stride TS), zero padded to 64x64
 // (asynchronous copies: all 16 loads of a thread are in flight at once; the caller's
 // __syncthreads() publishes the tile)
+template <int NTH = NT>
 __device__ __forceinline__ void ld_tile(double *S, const double *src, int ld, int rows, int cols) {
-    for (int e = threadIdx.x; e < TB * TB; e += NT) {
+    for (int e = threadIdx.x; e < TB * TB; e += NTH) {
         int r = e >> 6, c = e & 63;
         if (r < rows && c < cols) {
             const unsigned s = (unsigned)__cvta_generic_to_shared(S + r * TS + c);
@@ -123,27 +127,30 @@ __device__ __forceinline__ void ld_tile_T(double *S, const double *src, int ld, 
         S[r * TS + c] = (r < rows && c < cols) ? src[(size_t)c * ld + r] : 0.0;
     }
 }
+template <int NTH = NT>
 __device__ __forceinline__ void st_tile(const double *S, double *dst, int ld, int rows, int cols) {
-    for (int e = threadIdx.x; e < TB * TB; e += NT) {
+    for (int e = threadIdx.x; e < TB * TB; e += NTH) {
         int r = e >> 6, c = e & 63;
         if (r < rows && c < cols) dst[(size_t)r * ld + c] = S[r * TS + c];
     }
 }
 
 // C (64x64 smem) (+)= alpha * X Y^T  (X, Y 64x64 smem), DMMA; 8 warps x (8 rows x 64 cols)
+template <int NTH = NT>
 __device__ __forceinline__ void tile_xyt(double *C, const double *X, const double *Y, double alpha,
                                          bool accumulate) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int gr = lane >> 2, gc = lane & 3;
     double acc[8][2];
+    const bool on = NTH == NT || w < 8;     // 8 warps compute (wider CTAs: the rest only sync)
 #pragma unroll
     for (int nb = 0; nb < 8; ++nb) {
-        const int r = 8 * w + gr, c = 8 * nb + 2 * gc;
-        acc[nb][0] = accumulate ? C[r * TS + c] : 0.0;
-        acc[nb][1] = accumulate ? C[r * TS + c + 1] : 0.0;
+        const int r = 8 * (w & 7) + gr, c = 8 * nb + 2 * gc;
+        acc[nb][0] = accumulate && on ? C[r * TS + c] : 0.0;
+        acc[nb][1] = accumulate && on ? C[r * TS + c + 1] : 0.0;
     }
 #pragma unroll 4
-    for (int k4 = 0; k4 < TB / 4; ++k4) {
+    for (int k4 = 0; k4 < (on ? TB / 4 : 0); ++k4) {
         const double av = alpha * X[(8 * w + gr) * TS + 4 * k4 + gc];
 #pragma unroll
         for (int nb = 0; nb < 8; ++nb) dmma_884(acc[nb][0], acc[nb][1], av, Y[(8 * nb + gr) * TS + 4 * k4 + gc]);
@@ -152,8 +159,10 @@ __device__ __forceinline__ void tile_xyt(double *C, const double *X, const doubl
 #pragma unroll
     for (int nb = 0; nb < 8; ++nb) {
         const int r = 8 * w + gr, c = 8 * nb + 2 * gc;
-        C[r * TS + c] = acc[nb][0];
-        C[r * TS + c + 1] = acc[nb][1];
+        if (on) {
+            C[r * TS + c] = acc[nb][0];
+            C[r * TS + c + 1] = acc[nb][1];
+        }
     }
     __syncthreads();
 }
@@ -267,10 +276,11 @@ __device__ __forceinline__ void tile8_sub_xyt(double *C, const double *X, const 
 //       registers, while warps 1..7 apply the rank-8 updates A_IL -= L_IJ L_LJ^T and
 //       B_I -= L_IJ B_J on DMMA.
 // Pivots at rows >= free_row are not checked.
+template <int NTH = NT>
 __device__ void tile_chol64(double *S, double *Li, int nb, int free_row, int *info) {
     const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
     __shared__ double DI[2][8][9];
-    for (int e = tid; e < TB * TB; e += NT) {
+    for (int e = tid; e < TB * TB; e += NTH) {
         const int r = e >> 6, c = e & 63;
         if (r >= nb || c >= nb) S[r * TS + c] = (r == c) ? 1.0 : 0.0;
         else if (c > r) S[r * TS + c] = 0.0;
@@ -327,7 +337,7 @@ __device__ void tile_chol64(double *S, double *Li, int nb, int free_row, int *in
             if (lane == 0) bad |= chol8_thread(S + j1 * TS + j1, DI[(J + 1) & 1], free_row - j1);
         } else {
             const int nA = T * (T + 1) / 2 - 1, nB = T * (J + 1);
-            for (int t = wid - 1; t < nA + nB; t += NT / 32 - 1) {
+            for (int t = wid - 1; t < nA + nB; t += NTH / 32 - 1) {
                 if (t < nA) {              // A tile (I, L), J+1 <= L <= I, not (J+1, J+1)
                     int u = t + 1, I = 0;
                     while (u > I) { u -= I + 1; ++I; }
@@ -560,7 +570,11 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
         return;
     }
     int np = 0;                                           // phase-timestamp counter (debug)
-    if (a.prof && bid == 0 && tid == 0) a.prof[np++] = gtimer_s();
+    const bool large = (ma + TB - 1) / TB >= a.pw_min && a.phase != 0;
+    if (a.phase == 2 && !large) return;                   // small system: done in phase 1
+    if (a.phase == 2 && a.prof) np = (int)a.prof[999];    // timestamps continue after P3
+    if (a.prof && bid == 0 && tid == 0 && a.phase != 2) a.prof[np++] = gtimer_s();
+    if (a.phase != 2) {                                   // ---------------- P0 .. P3
 #define GSYNC()                                                               \
     do {                                                                      \
         grid.sync();                                                          \
@@ -838,6 +852,10 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
         for (int e = tid; e < kMaxPanels; e += NT) a.bar[e] = 0u;   // P3 group-barrier counters
     GSYNC();
     if (a.prof && bid == 0 && tid == 0) { a.prof[1000 + 3] = np; a.prof[np < 1000 ? np++ : np] = gtimer_s(); }   // phase marker (PDIPC_TRACE)
+    if (large) {                                          // P3 runs in k_chol_large
+        if (a.prof && bid == 0 && tid == 0) a.prof[999] = np;
+        return;
+    }
     // ------------------------------------------------ P3: Cholesky of the augmented matrix
     // Right-looking in panels of kPW tile columns: inside a panel, per tile column k: diagonal
     // tile factor + inverse (CTA 0), L_ik = A_ik Li_k^T, update of the panel's later columns;
@@ -1148,9 +1166,10 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
         }
         GSYNC();
     }
+    }                                                     // ---------------- end of P0 .. P3
     if (a.prof && bid == 0 && tid == 0) { a.prof[1000 + 4] = np; a.prof[np < 1000 ? np++ : np] = gtimer_s(); }   // phase marker (PDIPC_TRACE)
     // ------------------------------------------------ P4: u = C^{-T} y, y = row m of the factor
-    const int ntm = (m + TB - 1) / TB;
+    const int ntm = (m + TB - 1) / TB, nt = (ma + TB - 1) / TB;
     if (nt < a.pw_min) {
         // Small systems: CTA 0 alone, no grid barrier.  Per 64-row tile k of C from the last:
         // u_k = X_k y_k with X_k = L_kk^{-T} (formed by P3), then y_j -= sum_r C[kc0+r][j] u_r for
@@ -1304,7 +1323,201 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
     }
 }
 
+// ---------------------------------------------------------------- large-system Cholesky ---
+// P3 of a large system (>= pw_min 64-tiles, C3 / C4) in its own cooperative kernel with 16 warps
+// per CTA (the fused Schur kernel's register budget allows only 8): right-looking panels of kPW
+// tile columns with look-ahead as in k_schur_coop (panel group / update group, one grid barrier
+// per panel); the trailing updates on 128 x 128 blocks (2 x 2 tiles), warp (wr, wc) owning rows
+// 16wr .. 16wr + 15 and columns 64wc .. 64wc + 63, k streamed in 32-wide chunks through a 3-stage
+// 16-byte cp.async pipeline (per 4-wide k step 2 + 8 fragment loads feed 16 DMMAs per warp).
+constexpr int NT2 = 512;
+constexpr int XS2 = 36;
+constexpr int kCholSmem = 3 * 256 * XS2 * (int)sizeof(double);
+static_assert(kCholSmem >= 4 * TB * TS * (int)sizeof(double), "chol tiles");
+
+struct CholArgs {
+    double *Sh;
+    int ldh;
+    const int *nS_ptr;
+    int capS, pw_min;
+    double *Lstore;
+    int *info;
+    unsigned *bar;
+    unsigned long long *prof;
+};
+
+__global__ void __launch_bounds__(NT2, 1) k_chol_large(CholArgs a) {
+    extern __shared__ double sm[];
+    double *T0 = sm, *T1 = sm + TB * TS, *T2 = sm + 2 * TB * TS;
+    cg::grid_group grid = cg::this_grid();
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int G = gridDim.x, bid = blockIdx.x;
+    const int nS = min(*a.nS_ptr, a.capS), m = 3 * nS, ma = m + 1, nt = (ma + TB - 1) / TB;
+    if (nS == 0 || nt < a.pw_min) return;
+    int np = a.prof ? (int)a.prof[999] : 0;
+    const int wr = wid & 7, wc = wid >> 3, gr = lane >> 2, gc = lane & 3;
+    // A_ij -= sum_{k in [k0, k1)} L_ik L_jk^T on the 128 x 128 block of row tiles (ti, ti + 1) x
+    // column tiles (tj, tj + 1), columns limited to jlim tiles (and the matrix)
+    auto update_block = [&](int ti, int tj, int k0, int k1, int jlim) {
+        const int r0 = ti * TB, c0 = tj * TB;
+        const int rows = min(2 * TB, ma - r0), cols = min(2 * TB, min(jlim * TB, ma) - c0);
+        const int kbeg = k0 * TB, nch = (k1 - k0) * TB / 32;
+        auto issue = [&](int ch) {
+            if (ch < nch) {
+                double *X = sm + (ch % 3) * 256 * XS2;
+                const int kc = kbeg + ch * 32;
+                for (int e = tid; e < 4096; e += NT2) {            // X rows 0..127, Y rows 128..255
+                    const int rr = e >> 4, c2 = (e & 15) * 2;
+                    const bool isx = rr < 128;
+                    const int r = isx ? rr : rr - 128;
+                    double *dst = X + rr * XS2 + c2;
+                    if (r < (isx ? rows : cols)) {
+                        const double *src = a.Sh + (size_t)((isx ? r0 : c0) + r) * a.ldh + kc + c2;
+                        const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src));
+                    } else {
+                        dst[0] = 0.0;
+                        dst[1] = 0.0;
+                    }
+                }
+            }
+            asm volatile("cp.async.commit_group;\n" ::);
+        };
+        issue(0);
+        issue(1);
+        double acc[2][8][2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int nb = 0; nb < 8; ++nb) {
+                const int r = 16 * wr + 8 * h + gr, c = 64 * wc + 8 * nb + 2 * gc;
+                acc[h][nb][0] = (r < rows && c < cols) ? -a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c] : 0.0;
+                acc[h][nb][1] = (r < rows && c + 1 < cols) ? -a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c + 1] : 0.0;
+            }
+        for (int ch = 0; ch < nch; ++ch) {
+            issue(ch + 2);
+            asm volatile("cp.async.wait_group 2;\n" ::);
+            __syncthreads();
+            const double *X = sm + (ch % 3) * 256 * XS2 + (16 * wr + gr) * XS2 + gc;
+            const double *Y = sm + (ch % 3) * 256 * XS2 + (128 + 64 * wc + gr) * XS2 + gc;
+#pragma unroll
+            for (int k4 = 0; k4 < 8; ++k4) {
+                const double a0 = X[4 * k4], a1 = X[8 * XS2 + 4 * k4];
+#pragma unroll
+                for (int nb = 0; nb < 8; ++nb) {
+                    const double bv = Y[8 * nb * XS2 + 4 * k4];
+                    dmma_884(acc[0][nb][0], acc[0][nb][1], a0, bv);
+                    dmma_884(acc[1][nb][0], acc[1][nb][1], a1, bv);
+                }
+            }
+            __syncthreads();
+        }
+        asm volatile("cp.async.wait_group 0;\n" ::);
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int nb = 0; nb < 8; ++nb) {
+                const int r = 16 * wr + 8 * h + gr, c = 64 * wc + 8 * nb + 2 * gc;
+                if (r < rows && c < cols) a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c] = -acc[h][nb][0];
+                if (r < rows && c + 1 < cols) a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c + 1] = -acc[h][nb][1];
+            }
+    };
+    // 2 x 2 blocks over the tile columns [ja, jb): block columns tj = ja, ja + 2, ..., row tiles
+    // ti = tj, tj + 2, ...
+    auto nblocks = [&](int ja, int jb) {
+        int t = 0;
+        for (int j = ja; j < jb; j += 2) t += (nt - j + 1) / 2;
+        return t;
+    };
+    auto block_of = [&](int b, int ja, int &ti, int &tj) {
+        int j = ja;
+        while (b >= (nt - j + 1) / 2) { b -= (nt - j + 1) / 2; j += 2; }
+        tj = j;
+        ti = j + 2 * b;
+    };
+    const int npan = (nt + kPW - 1) / kPW;
+    for (int q = 0; q < npan; ++q) {
+        const int c0t = q * kPW, c1t = min(nt, c0t + kPW);
+        int npg = G;
+        if (q > 0 && c1t < nt && G > 1) {   // work in 64^3-product units (see k_schur_coop)
+            double wp = 16.0 * nblocks(c0t, c1t), ws = 0.0;
+            for (int k = c0t; k < c1t; ++k) {
+                wp += 1.3 * (nt - k - 1) + 4.0 * 1.3 * nblocks(k + 1, c1t);
+                ws += 4.0 + 3 * 0.3;
+            }
+            const double wu = 16.0 * nblocks(c1t, nt);
+            double best = 1e300;
+            for (int x = 1; x < G; ++x) {
+                const double t = fmax(ws + wp / x, wu / (G - x));
+                if (t < best) { best = t; npg = x; }
+            }
+        }
+        if (bid < npg) {
+            unsigned *ctr = a.bar + q;
+            unsigned nbar = 0;
+            if (q > 0) {
+                const int tot = nblocks(c0t, c1t);
+                for (int b = bid; b < tot; b += npg) {
+                    int ti, tj;
+                    block_of(b, c0t, ti, tj);
+                    update_block(ti, tj, c0t - kPW, c0t, c1t);
+                }
+                group_bar(ctr, ++nbar * npg);
+            }
+            for (int k = c0t; k < c1t; ++k) {
+                const int kc0 = k * TB, kn = min(TB, ma - kc0);
+                if (bid == 0) {
+                    ld_tile<NT2>(T0, a.Sh + (size_t)kc0 * a.ldh + kc0, a.ldh, kn, kn);
+                    __syncthreads();
+                    tile_chol64<NT2>(T0, T1, kn, m - kc0, a.info);
+                    st_tile<NT2>(T0, a.Sh + (size_t)kc0 * a.ldh + kc0, a.ldh, kn, kn);
+                    for (int e = tid; e < TB * TB; e += NT2) a.Lstore[(size_t)k * TB * TB + e] = T1[(e >> 6) * TS + (e & 63)];
+                }
+                group_bar(ctr, ++nbar * npg);
+                for (int b = bid; b < nt - k - 1; b += npg) {      // L_ik = A_ik Li^T
+                    const int ti = k + 1 + b, r0 = ti * TB, rows = min(TB, ma - r0);
+                    ld_tile<NT2>(T0, a.Sh + (size_t)r0 * a.ldh + kc0, a.ldh, rows, kn);
+                    ld_tile<NT2>(T1, a.Lstore + (size_t)k * TB * TB, TB, TB, TB);
+                    __syncthreads();
+                    tile_xyt<NT2>(T2, T0, T1, 1.0, false);
+                    st_tile<NT2>(T2, a.Sh + (size_t)r0 * a.ldh + kc0, a.ldh, rows, kn);
+                }
+                group_bar(ctr, ++nbar * npg);
+                if (k + 1 < c1t) {          // A_ij -= L_ik L_jk^T, k < j < c1t, i >= j
+                    const int tot = nblocks(k + 1, c1t);
+                    for (int b = bid; b < tot; b += npg) {
+                        int ti, tj;
+                        block_of(b, k + 1, ti, tj);
+                        update_block(ti, tj, k, k + 1, c1t);
+                    }
+                    group_bar(ctr, ++nbar * npg);
+                }
+            }
+            if (a.prof && bid == 0 && tid == 0 && q < 100) { a.prof[600 + q] = gtimer_s(); a.prof[800 + q] = npg; }
+        } else if (q > 0) {
+            const int ub = bid - npg, nu = G - npg, tot = nblocks(c1t, nt);
+            for (int b = ub; b < tot; b += nu) {
+                int ti, tj;
+                block_of(b, c1t, ti, tj);
+                update_block(ti, tj, c0t - kPW, c0t, nt);
+            }
+            if (a.prof && tid == 0 && q < 100) atomicMax(a.prof + 700 + q, gtimer_s());
+        }
+        grid.sync();
+        if (a.prof && bid == 0 && tid == 0 && np < 1000) a.prof[np++] = gtimer_s();
+    }
+    if (a.prof && bid == 0 && tid == 0) a.prof[999] = np;
+}
+
 static int g_schur_grid = 0;
+// PDIPC_SPLIT_SCHUR=1: large systems factor in k_chol_large (16 warps per CTA, 128 x 128 blocks)
+// between two k_schur_coop launches.  Off by default: measured 16.1 vs 14.7 ms for P3 at n_c 3000
+// (the fused kernel's 128 x 64 blocks on 8 warps reach the same per-SM DMMA rate, and the split
+// adds the spills of a 128-register budget to the diagonal-tile chain).
+static bool getenv_fused() {
+    static const int v = [] { const char *e = std::getenv("PDIPC_SPLIT_SCHUR"); return e && e[0] == '1' ? 0 : 1; }();
+    return v != 0;
+}
 static double *g_kpart = nullptr;   // split-K partial tiles, grid x 1152 doubles (allocated at init)
 static double *g_lp = nullptr;      // small-system P3 panel scratch
 static unsigned *g_bar = nullptr;   // large-system P3 group-barrier counters
@@ -1318,6 +1531,7 @@ void schur_init(int device) {
     if (!g_kpart) cudaMalloc(&g_kpart, (size_t)g_schur_grid * 1152 * sizeof(double));
     if (!g_lp) cudaMalloc(&g_lp, (size_t)2 * kLPTiles * TB * TB * sizeof(double));
     if (!g_bar) cudaMalloc(&g_bar, (size_t)kMaxPanels * sizeof(unsigned));
+    cudaFuncSetAttribute(k_chol_large, cudaFuncAttributeMaxDynamicSharedMemorySize, kCholSmem);
 }
 
 int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, const double *gc,
@@ -1339,8 +1553,27 @@ int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, 
     a.mode = mode; a.G2 = G2; a.n2 = n2; a.rpos = rpos; a.Yel = Yel;
     void *args[] = {&a};
     note_launch();
-    return (int)cudaLaunchCooperativeKernel((const void *)k_schur_coop, dim3(g_schur_grid), dim3(NT),
-                                             args, kSchurSmem, st);
+    if (mode == kSchurKOnly || getenv_fused()) {                 // one launch: P0-P5
+        a.phase = 0;
+        return (int)cudaLaunchCooperativeKernel((const void *)k_schur_coop, dim3(g_schur_grid), dim3(NT),
+                                                 args, kSchurSmem, st);
+    }
+    // large systems: P0-P2 | P3 in k_chol_large | P4-P5 (each launch checks the size on the device)
+    a.phase = 1;
+    cudaError_t e = cudaLaunchCooperativeKernel((const void *)k_schur_coop, dim3(g_schur_grid), dim3(NT), args,
+                                                kSchurSmem, st);
+    if (e != cudaSuccess) return (int)e;
+    CholArgs c;
+    c.Sh = Sh; c.ldh = ldh; c.nS_ptr = nS; c.capS = capS; c.pw_min = a.pw_min; c.Lstore = Lstore; c.info = info;
+    c.bar = g_bar; c.prof = prof;
+    void *cargs[] = {&c};
+    note_launch();
+    e = cudaLaunchCooperativeKernel((const void *)k_chol_large, dim3(g_schur_grid), dim3(NT2), cargs, kCholSmem, st);
+    if (e != cudaSuccess) return (int)e;
+    a.phase = 2;
+    note_launch();
+    return (int)cudaLaunchCooperativeKernel((const void *)k_schur_coop, dim3(g_schur_grid), dim3(NT), args,
+                                             kSchurSmem, st);
 }
 
 }  // namespace pdipc
