@@ -358,11 +358,12 @@ def rooflines(kt, info, nb, nS_list, reuse_frac, hbm, sm_max_mhz, peak_src):
         # K_s^-1 when S changed (n_c^3, reuse fraction excluded), back substitution and t = B u,
         # Z (4 m^2)
         fl = [(1.0 - reuse_frac) * nc ** 3 + (3 * nc) ** 3 / 3.0 + 4 * (3 * nc) ** 2 for nc in nS_list]
-        f = statistics.mean(fl)
+        f = statistics.mean(fl) * info.get("schur_systems_per_launch", 1)   # systems per launch
         pk = _fp64_peak(sm_max_mhz)
         out["dense_schur"] = {"kernel": "k_schur_coop", "bound": "tensor", "achieved": f / t / 1e12, "peak": pk,
                               "unit": "TFLOP/s", "frac": f / t / 1e12 / pk, "flops_per_launch": f,
                               "avg_launch_us": t * 1e6, "n_c_mean": statistics.mean(nS_list),
+                              "systems_per_launch": info.get("schur_systems_per_launch", 1),
                               "peak_source": "FP64 DMMA measured (tools/micro/fp64_peaks.cu) x 148 SMs x max clock"}
     for k in ("pair_derivatives", "panel_forward", "contact_assembly", "narrow_phase", "broad_phase", "ccd",
               "line_search"):

@@ -242,7 +242,7 @@ const char *pd_ipc_kernel_name(int32_t id);
 /* Sizes of the handle (for measurement reports): info[0..n) of
  *   [n_verts, n_tets, n_free, n_surf_verts, n_surf_tris, n_surf_edges, supernodes, nnz(L),
  *    supernodal etree depth, capS (max |S|), reuse slots, n_seq, backward row blocks, nU,
- *    reduced backend (1 panel, 2 gather), |R|]
+ *    reduced backend (1 panel, 2 gather, 3 pcg), |R|, Schur systems per launch]
  * (nnz(L): the prefactorised PD matrix).  Returns the number of fields written. */
 int pd_ipc_get_info(const pd_ipc *h, int64_t *info, int32_t n);
 

@@ -283,7 +283,7 @@ struct pd_ipc {
     DBuf<unsigned long long> cand_tmp, akeys;
     DBuf<int> flag, pos, ctype, atype, ids, iscr;
     DBuf<double> cd2, ad2, grad, Hp, dist;
-    DBuf<int> mark, spos, qS;
+    DBuf<int> mark;
     DBuf<double> lspart;    // line-search partial sums [ls_round_width()][ls_blocks()]
     // second stream: w_el = L^-1 Pi g_el of all sequences runs concurrently with the contact
     // stages (it depends on the elastic gradients only)
@@ -296,13 +296,22 @@ struct pd_ipc {
     // the S / B-check chain of the assembly
     cudaStream_t st3 = nullptr;
     cudaEvent_t ev_fork3 = nullptr, ev_join3 = nullptr, ev_S = nullptr;
-    DBuf<double> gcS, Ug2;
+    DBuf<double> Ug2;
     DBuf<int> ts_lo2, ts_hi2, ts_cnt2, ts_ptr2, ts_rem2, ticket2, f_bord, iscr2;
     bool graphs = true;       // replay each batch as a CUDA graph (PDIPC_NO_GRAPH=1: off)
     unsigned buf_epoch = 0;   // bumped whenever a buffer the iteration uses is reallocated
     std::vector<GraphEntry> gcache;
     DBuf<int> ts_lo, ts_hi, ts_cnt, ts_ptr, ts_rem, ts_done, ticket;
-    DBuf<double> Bc, Sh, U, Tt, yS, rhs, u, tv, part, b0, Lstore;
+    DBuf<double> part, b0;
+    // per-system buffers of the Schur step: a sequence's contact stages fill the set of its group
+    // (b mod nsysb) and the batched Schur launch runs nsysb systems at once (gather backend, B > 1)
+    struct SysBufs {
+        DBuf<int> qS, spos;                                  // S (factor positions), S positions / |S|
+        DBuf<double> Bc, Sh, gcS, Lstore, U, Tt, yS, rhs, u, tv;
+    };
+    std::vector<SysBufs> sys;
+    int nsysb = 1;
+    SysBufs &sb(int b) { return sys[b % nsysb]; }
     DBuf<long long> gsq;    // surface gradient, fixed point [Ns][3]
     StageTimer tm;
     KTimer kt;
@@ -382,6 +391,7 @@ static void grow_candidates(pd_ipc *h, int b, size_t n) {
 // buffers hold its data)
 static void debug_capture(pd_ipc *h, int b, int n_pt, int n_ee, int nS) {
     Seq &q = *h->seqs[b];
+    pd_ipc::SysBufs &SB = h->sb(b);
     const int nf = h->nf;
     std::vector<double> G4(4 * (size_t)nf), g4(4 * (size_t)nf);
     CK(cudaMemcpy(G4.data(), h->G(b), sizeof(double) * 4 * nf, cudaMemcpyDeviceToHost));
@@ -411,7 +421,7 @@ static void debug_capture(pd_ipc *h, int b, int n_pt, int n_ee, int nS) {
         CK(cudaMemcpy(q.phess.data(), h->Hp.p, sizeof(double) * q.phess.size(), cudaMemcpyDeviceToHost));
     }
     std::vector<int> qs(nS);
-    if (nS) CK(cudaMemcpy(qs.data(), h->qS.p, sizeof(int) * nS, cudaMemcpyDeviceToHost));
+    if (nS) CK(cudaMemcpy(qs.data(), SB.qS.p, sizeof(int) * nS, cudaMemcpyDeviceToHost));
     q.S.clear();
     for (int v : qs) q.S.push_back(h->hm.q2v[v]);
     std::sort(q.S.begin(), q.S.end());
@@ -564,13 +574,14 @@ static void broad_phase_sort(pd_ipc *h, int b, const double4 *ds, double infl, i
 // unchanged).  Reads S, |S| and the same-S flag; writes V, Up and the panel plan.  Stream 3.
 static void enqueue_panel_forward(pd_ipc *h, int b, const int *nS_dev, cudaStream_t sp) {
     const DevFactor &F = h->F;
+    pd_ipc::SysBufs &SB = h->sb(b);
     KTimer &kt = h->kt;
     int *di = h->dint(b);
     kt.start(K_FWD, sp);
-    launch_ts_plan(F, h->qS.p, nS_dev, h->capS, di + D_SAME, (long long)h->Up.n, di + D_CAP, 2, 0,
+    launch_ts_plan(F, SB.qS.p, nS_dev, h->capS, di + D_SAME, (long long)h->Up.n, di + D_CAP, 2, 0,
                    h->ts_lo.p, h->ts_hi.p, h->ts_cnt.p, h->ts_rem.p, h->ts_ptr.p, h->ticket.p, sp);
     if (h->trace_file) h->trace.ensure(4 * (size_t)F.bw_nblocks * (2 + (h->capS + 31) / 32));
-    launch_forward_solve(F, h->ts_lo.p, h->ts_hi.p, h->ts_ptr.p, h->qS.p, h->ts_rem.p, h->ticket.p, nullptr,
+    launch_forward_solve(F, h->ts_lo.p, h->ts_hi.p, h->ts_ptr.p, SB.qS.p, h->ts_rem.p, h->ticket.p, nullptr,
                          nullptr, h->V_slot[h->seqs[b]->slot].p, h->ldv, nullptr, h->Up.p, nS_dev, h->capS, 0,
                          0, 0, 0, h->nsm, h->trace_file ? h->trace.p : nullptr, sp);
     kt.stop(K_FWD, sp);
@@ -627,9 +638,10 @@ static void enqueue_elastic(pd_ipc *h, int b0, int nb, int it) {
 // Z_b = -z, so the common backward solve + scatter give dx = Pi^T L^-T z.
 static void pcg_solve(pd_ipc *h, int b) {
     cudaStream_t st = h->st;
+    pd_ipc::SysBufs &SB = h->sb(b);
     const DevFactor &F = h->F;
     const int nf = h->nf;
-    int *nS_dev = h->spos.p + nf;
+    int *nS_dev = SB.spos.p + nf;
     const long long us = 4 * (long long)std::max(1, F.nU);
     auto fwd = [&](const double *rhs, double *out) {
         launch_ts_plan(F, nullptr, h->ticket2.p + 2, 0, h->ticket2.p + 2, 0, h->ticket2.p + 3, 1, 1, h->ts_lo2.p,
@@ -649,7 +661,7 @@ static void pcg_solve(pd_ipc *h, int b) {
         CK(dev_copy(h->cg_t.p, h->cg_p.p, sizeof(double) * 4 * nf, st));
         launch_backward_solve(F, h->ts_done.p, h->bw_cnt.p, h->ticket.p, h->bw_P.p, h->cg_t.p, 1, 4 * (long long)nf,
                               h->nsm, st);                     // t = L^-T p
-        launch_cg_bmul(h->Bc.p, 3 * h->capS, h->qS.p, nS_dev, h->capS, h->cg_t.p, h->cg_R.p, nf, st);
+        launch_cg_bmul(SB.Bc.p, 3 * h->capS, SB.qS.p, nS_dev, h->capS, h->cg_t.p, h->cg_R.p, nf, st);
         fwd(h->cg_R.p, h->cg_f.p);                             // f = L^-1 E_S B-check t_S
         launch_cg_update(h->cg_f.p, h->cg_p.p, h->cg_q.p, h->cg_z.p, h->cg_r.p, nf, h->cg_part.p, it,
                          h->cg_rr_host, st);
@@ -662,9 +674,10 @@ static void pcg_solve(pd_ipc *h, int b) {
 }
 
 // (b) sequence b: a3-a6 contact stages, a8 panel (stream 3) and the a9 dense Schur step -> Z_b
-static void enqueue_contact_schur(pd_ipc *h, int b, int b0, int nb, int it) {
+static void enqueue_contact(pd_ipc *h, int b, int b0, int nb, int it) {
     cudaStream_t st = h->st;
     Seq &q = *h->seqs[b];
+    pd_ipc::SysBufs &SB = h->sb(b);
     KTimer &kt = h->kt;
     const int slot = it * nb + (b - b0);
     kt.slot = slot;
@@ -674,7 +687,7 @@ static void enqueue_contact_schur(pd_ipc *h, int b, int b0, int nb, int it) {
     int *di = h->dint(b);
     double *ds_ = h->dscal(b);
     int *acnt = di + D_ACNT, *ccnt = di + D_CCNT;
-    int *nS_dev = h->spos.p + nf;     // exclusive scan total of the S marks
+    int *nS_dev = SB.spos.p + nf;     // exclusive scan total of the S marks
     double *dmax = ds_ + 11;
     const int slotr = q.slot;
     if (Nt > 0) {
@@ -709,26 +722,26 @@ static void enqueue_contact_schur(pd_ipc *h, int b, int b0, int nb, int it) {
         kt.start(K_ASSEMBLY, st);
         // S
         launch_mark_S(h->ids.p, acnt, cap, h->Wp.p, h->Wc.p, h->v2q.p, h->mark.p, st);
-        scan_compact(h->mark.p, h->spos.p, h->qS.p, nf, h->iscr.p, st);   // positions and S (sorted)
+        scan_compact(h->mark.p, SB.spos.p, SB.qS.p, nf, h->iscr.p, st);   // positions and S (sorted)
         // V_s, K_s, Sigma_s depend on S (and the constant factor) only: reuse the slot's while S
         // is bit-identical to the S they were computed for
-        launch_same_S(h->qS.p, nS_dev, h->qS_slot[slotr].p, h->nS_slot.p + slotr, di + D_SAME, h->capS,
+        launch_same_S(SB.qS.p, nS_dev, h->qS_slot[slotr].p, h->nS_slot.p + slotr, di + D_SAME, h->capS,
                       h->opt.no_sigma_reuse == 0, di + D_CAP, di + D_REUSED, st);
         CK(dev_copy(di + D_NS, nS_dev, sizeof(int), st));
         CK(cudaEventRecord(h->ev_S, st));
         CK(cudaStreamWaitEvent(h->st3, h->ev_S, 0));
-        launch_gather_gc(h->qS.p, nS_dev, h->capS, h->WTp.p, h->WTr.p, h->WTv.p, h->gsq.p, dmax, acnt, h->gcS.p,
+        launch_gather_gc(SB.qS.p, nS_dev, h->capS, h->WTp.p, h->WTr.p, h->WTv.p, h->gsq.p, dmax, acnt, SB.gcS.p,
                          h->st3);
         if (!h->gather && !h->pcg) enqueue_panel_forward(h, b, nS_dev, h->st3);
         CK(cudaEventRecord(h->ev_join3, h->st3));
         // B-check: fixed-point accumulation into the dense 3|S| x 3|S| block, then to double; the
         // low words of the fixed-point sums live in the (not yet used) Sigma-hat buffer
         const int ldb = 3 * h->capS;
-        long long *Bl = reinterpret_cast<long long *>(h->Sh.p);
-        launch_zero_square(h->Bc.p, h->Sh.p, ldb, nS_dev, h->capS, st);
-        launch_accum_bc_fx(h->ids.p, acnt, cap, h->Wp.p, h->Wc.p, h->Wv.p, h->v2q.p, h->spos.p, h->Hp.p, dmax,
-                           reinterpret_cast<long long *>(h->Bc.p), Bl, ldb, st);
-        launch_fx_to_double(reinterpret_cast<long long *>(h->Bc.p), Bl, ldb, nS_dev, h->capS, dmax, acnt, st);
+        long long *Bl = reinterpret_cast<long long *>(SB.Sh.p);
+        launch_zero_square(SB.Bc.p, SB.Sh.p, ldb, nS_dev, h->capS, st);
+        launch_accum_bc_fx(h->ids.p, acnt, cap, h->Wp.p, h->Wc.p, h->Wv.p, h->v2q.p, SB.spos.p, h->Hp.p, dmax,
+                           reinterpret_cast<long long *>(SB.Bc.p), Bl, ldb, st);
+        launch_fx_to_double(reinterpret_cast<long long *>(SB.Bc.p), Bl, ldb, nS_dev, h->capS, dmax, acnt, st);
         kt.stop(K_ASSEMBLY, st);
         CK(cudaStreamWaitEvent(st, h->ev_join3, 0));     // join stream 3
     } else {
@@ -739,30 +752,46 @@ static void enqueue_contact_schur(pd_ipc *h, int b, int b0, int nb, int it) {
         launch_grad_pullback(h->gel(b), h->WTp.p, h->WTr.p, h->WTv.p, nullptr, nf, h->G(b), st);
     }
     h->tm.rec(slot, 3, st);
-    // ---------------- G-Step: join stream 2 (w_el of all sequences) before the first Schur step
+}
+
+// (b') the a9 G-step of sequences [c0, c1) (one group each): ONE batched Schur launch (gather
+// backend), or per sequence the single-system Schur / PCG solve
+static void enqueue_schur(pd_ipc *h, int c0, int c1, int b0, int nb, int it) {
+    cudaStream_t st = h->st;
+    KTimer &kt = h->kt;
+    const int nf = h->nf, Nt = h->Nt;
     const DevFactor &F = h->F;
-    if (b == b0) CK(cudaStreamWaitEvent(st, h->ev_join, 0));
+    // join stream 2 (w_el of all sequences) before the first Schur step of the iteration
+    if (c0 == b0) CK(cudaStreamWaitEvent(st, h->ev_join, 0));
+    kt.slot = it * nb + (c0 - b0);
     kt.start(K_DENSE, st);
     if (Nt > 0 && h->pcg) {
-        pcg_solve(h, b);
+        for (int b = c0; b < c1; ++b) pcg_solve(h, b);
     } else if (Nt > 0) {
         if (h->trace_file) {
             h->sprof.ensure(1024);
             CK(dev_zero(h->sprof.p, 1024 * 8, st));
         }
-        CK((cudaError_t)launch_schur(F, h->V_slot[slotr].p, h->ldv, h->Yw(b), h->gcS.p, h->qS.p,
-                                     h->ts_lo.p, h->ts_hi.p, nS_dev, h->capS, h->K_slot[slotr].p, h->capS, h->Bc.p,
-                                     3 * h->capS, h->Sh.p, h->ldh, h->Lstore.p, h->Tt.p, h->U.p, h->yS.p,
-                                     h->rhs.p, h->u.p, h->tv.p, h->Z(b), di + D_INFO, di + D_SAME,
-                                     h->trace_file ? h->sprof.p : nullptr,
-                                     (h->opt.debug_flags & PD_IPC_DBG_LARGE_SCHUR) ? 1 : 0,
-                                     h->gather ? kSchurGather : kSchurPanel, h->G2.p, h->n2, h->rpos.p,
-                                     h->gather ? h->Yel(b) : nullptr, st));
+        SchurArgs args[kMaxSchurSys];
+        for (int b = c0; b < c1; ++b) {
+            pd_ipc::SysBufs &SB = h->sb(b);
+            const int slotr = h->seqs[b]->slot;
+            int *di = h->dint(b);
+            args[b - c0] = schur_args(F, h->V_slot[slotr].p, h->ldv, h->Yw(b), SB.gcS.p, SB.qS.p, h->ts_lo.p,
+                                      h->ts_hi.p, SB.spos.p + nf, h->capS, h->K_slot[slotr].p, h->capS, SB.Bc.p,
+                                      3 * h->capS, SB.Sh.p, h->ldh, SB.Lstore.p, SB.Tt.p, SB.U.p, SB.yS.p,
+                                      SB.rhs.p, SB.u.p, SB.tv.p, h->Z(b), di + D_INFO, di + D_SAME,
+                                      h->trace_file ? h->sprof.p : nullptr,
+                                      (h->opt.debug_flags & PD_IPC_DBG_LARGE_SCHUR) ? 1 : 0,
+                                      h->gather ? kSchurGather : kSchurPanel, h->G2.p, h->n2, h->rpos.p,
+                                      h->gather ? h->Yel(b) : nullptr);
+        }
+        CK((cudaError_t)launch_schur_batch(args, c1 - c0, st));
     } else {
-        CK(dev_copy(h->Z(b), h->Yw(b), sizeof(double) * 4 * nf, st));
+        for (int b = c0; b < c1; ++b) CK(dev_copy(h->Z(b), h->Yw(b), sizeof(double) * 4 * nf, st));
     }
     kt.stop(K_DENSE, st);
-    h->tm.rec(slot, 4, st);
+    for (int b = c0; b < c1; ++b) h->tm.rec(it * nb + (b - b0), 4, st);
 }
 
 // (c) backward solves of every sequence (8 sequences' right-hand sides per launch), dx scatter
@@ -840,7 +869,12 @@ static void enqueue_ccd_ls(pd_ipc *h, int b, int b0, int nb, int it) {
 
 static void enqueue_lockstep_iteration(pd_ipc *h, int b0, int nb, int it) {
     enqueue_elastic(h, b0, nb, it);
-    for (int b = b0; b < b0 + nb; ++b) enqueue_contact_schur(h, b, b0, nb, it);
+    for (int c0 = b0; c0 < b0 + nb; c0 += h->nsysb) {      // groups of nsysb sequences (c0 = 0 mod nsysb)
+        const int c1 = std::min(b0 + nb, c0 - c0 % h->nsysb + h->nsysb);
+        for (int b = c0; b < c1; ++b) enqueue_contact(h, b, b0, nb, it);
+        enqueue_schur(h, c0, c1, b0, nb, it);
+        c0 = c1 - h->nsysb;
+    }
     enqueue_backward(h, b0, nb, it);
     for (int b = b0; b < b0 + nb; ++b) enqueue_ccd_ls(h, b, b0, nb, it);
 }
@@ -1320,8 +1354,27 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         h->ticket2.exact(4);
         CK(cudaMemset(h->ticket2.p, 0, 4 * sizeof(int)));
         h->mark.exact(nf + 1);
-        h->spos.exact(nf + 1);
-        h->qS.exact(nf + 1);
+        // per-system Schur buffers: group 0 now, more groups once the backend is known
+        auto alloc_sys = [&](pd_ipc::SysBufs &g) {
+            g.spos.exact(nf + 1);
+            g.qS.exact(nf + 1);
+            g.Tt.exact(64 * 64);
+            if (m.Nt > 0) {
+                const int cS = h->capS;
+                g.gcS.exact(3 * (size_t)cS + 3);
+                g.Bc.exact((size_t)9 * cS * cS);
+                g.Sh.exact((size_t)(3 * cS + 1) * ((3 * cS + 8 + 1) & ~1));
+                // large systems: Li tiles [nt+1][64][64]; small: D blocks [nt+1][512] + X tiles [nt][64][64]
+                g.Lstore.exact((size_t)((3 * cS + 1 + 63) / 64 + 1) * (64 * 64 + 512));
+                g.U.exact((size_t)(cS + 64) * 64);
+                g.yS.exact(3 * (size_t)cS);
+                g.rhs.exact(3 * (size_t)cS);
+                g.u.exact(3 * (size_t)cS);
+                g.tv.exact(3 * (size_t)cS);
+            }
+        };
+        h->sys.resize(1);
+        alloc_sys(h->sys[0]);
         h->ts_lo.exact(f.nsn);
         h->ts_hi.exact(f.nsn);
         h->ts_cnt.exact(f.nsn + 1);
@@ -1357,20 +1410,9 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         h->cell0 = std::max(m.mean_edge, 2.0 * d_hat);
         if (m.Nt > 0) {
             const int cS = h->capS;
-            h->gcS.exact(3 * (size_t)h->capS + 3);
-            h->Bc.exact((size_t)9 * cS * cS);
             h->ldh = (3 * cS + 8 + 1) & ~1;   // even: 16-byte aligned rows (cp.async 16 B)
-            h->Sh.exact((size_t)(3 * cS + 1) * h->ldh);
-            // large systems: Li tiles [nt+1][64][64]; small: D blocks [nt+1][512] + X tiles [nt][64][64]
-            h->Lstore.exact((size_t)((3 * cS + 1 + 63) / 64 + 1) * (64 * 64 + 512));
-            h->U.exact((size_t)(cS + 64) * 64);
-            h->yS.exact(3 * (size_t)cS);
-            h->rhs.exact(3 * (size_t)cS);
-            h->u.exact(3 * (size_t)cS);
-            h->tv.exact(3 * (size_t)cS);
             h->Up.exact((size_t)std::max(1, f.uoff[f.nsn]) * (((cS + 31) / 32) * 32));
         }
-        h->Tt.exact(64 * 64);
         h->part.exact(std::max<size_t>(4096, (size_t)(m.T + 255) / 256 + (nf + 255) / 256 + 64));
         std::vector<int> Rq;   // region R: factor positions of the W-supported free vertices, sorted
         {
@@ -1388,6 +1430,14 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             const bool want = be == 2 || (be == 0 && h->n2 >= 1024);
             h->gather = m.Nt > 0 && want && h->n2 <= h->capS;
             h->pcg = m.Nt > 0 && be == 3;
+            // batched Schur: with the gather backend and several sequences, 2 systems per launch
+            // (each on half the SMs: one system's serial panel chain overlaps the other's updates)
+            h->nsysb = (h->gather && Bq > 1) ? 2 : 1;
+            if (const char *sbv = std::getenv("PDIPC_SCHUR_BATCH"))
+                h->nsysb = std::max(1, std::min(std::min(Bq, (int)kMaxSchurSys), std::atoi(sbv)));
+            if (!h->gather) h->nsysb = 1;                  // (panel mode: split-K sums depend on the grid)
+            h->sys.resize(h->nsysb);
+            for (int g = 1; g < h->nsysb; ++g) alloc_sys(h->sys[g]);
             if (h->pcg) {
                 for (auto *bf : {&h->cg_r, &h->cg_p, &h->cg_z, &h->cg_q, &h->cg_t, &h->cg_f, &h->cg_R})
                     bf->exact(4 * (size_t)nf);
@@ -1426,21 +1476,21 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             std::vector<int> rp(nf, -1);
             for (int i = 0; i < n2; ++i) rp[Rq[i]] = i;
             h->rpos.upload(rp.data(), rp.size());
-            CK(cudaMemcpy(h->qS.p, Rq.data(), sizeof(int) * n2, cudaMemcpyHostToDevice));
-            int *nS_dev = h->spos.p + nf;
+            CK(cudaMemcpy(h->sys[0].qS.p, Rq.data(), sizeof(int) * n2, cudaMemcpyHostToDevice));
+            int *nS_dev = h->sys[0].spos.p + nf;
             CK(cudaMemcpy(nS_dev, &n2, sizeof(int), cudaMemcpyHostToDevice));
             DBuf<double> Vtmp;
             Vtmp.exact((size_t)nf * h->ldv);
             h->G2.exact((size_t)n2 * n2);
             int *zero = h->ticket2.p + 2, *flags = h->dint(0) + D_CAP;
-            launch_ts_plan(F, h->qS.p, nS_dev, h->capS, zero, (long long)h->Up.n, flags, 2, 0, h->ts_lo.p, h->ts_hi.p,
+            launch_ts_plan(F, h->sys[0].qS.p, nS_dev, h->capS, zero, (long long)h->Up.n, flags, 2, 0, h->ts_lo.p, h->ts_hi.p,
                            h->ts_cnt.p, h->ts_rem.p, h->ts_ptr.p, h->ticket.p, h->st);
-            launch_forward_solve(F, h->ts_lo.p, h->ts_hi.p, h->ts_ptr.p, h->qS.p, h->ts_rem.p, h->ticket.p, nullptr,
+            launch_forward_solve(F, h->ts_lo.p, h->ts_hi.p, h->ts_ptr.p, h->sys[0].qS.p, h->ts_rem.p, h->ticket.p, nullptr,
                                  nullptr, Vtmp.p, h->ldv, nullptr, h->Up.p, nS_dev, h->capS, 0, 0, 0, 0, h->nsm,
                                  nullptr, h->st);
-            CK((cudaError_t)launch_schur(F, Vtmp.p, h->ldv, h->Yw(0), h->gcS.p, h->qS.p, h->ts_lo.p, h->ts_hi.p,
-                                         nS_dev, h->capS, h->G2.p, n2, h->Bc.p, 3 * h->capS, h->Sh.p, h->ldh,
-                                         h->Lstore.p, h->Tt.p, h->U.p, h->yS.p, h->rhs.p, h->u.p, h->tv.p, h->Z(0),
+            CK((cudaError_t)launch_schur(F, Vtmp.p, h->ldv, h->Yw(0), h->sys[0].gcS.p, h->sys[0].qS.p, h->ts_lo.p, h->ts_hi.p,
+                                         nS_dev, h->capS, h->G2.p, n2, h->sys[0].Bc.p, 3 * h->capS, h->sys[0].Sh.p, h->ldh,
+                                         h->sys[0].Lstore.p, h->sys[0].Tt.p, h->sys[0].U.p, h->sys[0].yS.p, h->sys[0].rhs.p, h->sys[0].u.p, h->sys[0].tv.p, h->Z(0),
                                          h->dint(0) + D_INFO, zero, nullptr, 0, kSchurKOnly, nullptr, 0, nullptr,
                                          nullptr, h->st));
             CK(cudaStreamSynchronize(h->st));
@@ -1589,7 +1639,7 @@ void pd_ipc_destroy(pd_ipc *h) {
     rel(h->Wp); rel(h->Wc); rel(h->WTp); rel(h->WTr); rel(h->tris); rel(h->edges); rel(h->Wv); rel(h->WTv);
     rel(h->f_c0); rel(h->f_rowptr); rel(h->f_rows); rel(h->f_parent); rel(h->f_seg_ptr); rel(h->f_seg_d);
     rel(h->f_seg_klo); rel(h->f_seg_khi); rel(h->f_fd); rel(h->f_col2sn); rel(h->f_valptr); rel(h->f_L);
-    rel(h->f_dinv_ptr); rel(h->f_dinv); rel(h->Ug); rel(h->Up); rel(h->bw_P); rel(h->f_bw_items); rel(h->f_ford); rel(h->f_bord); rel(h->gcS); rel(h->Ug2); rel(h->f_path_ptr); rel(h->f_path_sn); rel(h->f_rc_src); rel(h->f_bw_pbase); rel(h->bw_cnt); rel(h->f_uoff); rel(h->f_urow_sn);
+    rel(h->f_dinv_ptr); rel(h->f_dinv); rel(h->Ug); rel(h->Up); rel(h->bw_P); rel(h->f_bw_items); rel(h->f_ford); rel(h->f_bord); rel(h->Ug2); rel(h->f_path_ptr); rel(h->f_path_sn); rel(h->f_rc_src); rel(h->f_bw_pbase); rel(h->bw_cnt); rel(h->f_uoff); rel(h->f_urow_sn);
     rel(h->f_rc_ptr); rel(h->f_rc_idx); rel(h->f_urel); rel(h->f_ch_ptr); rel(h->f_ch);
     for (auto &s : h->seqs) rel(s->cand);
     for (auto &b : h->V_slot) rel(b);
@@ -1605,10 +1655,12 @@ void pd_ipc_destroy(pd_ipc *h) {
     rel(h->qcnt); rel(h->qoff); rel(h->qlist); rel(h->gsq);
     rel(h->cand_tmp); rel(h->akeys); rel(h->flag); rel(h->pos); rel(h->ctype); rel(h->atype); rel(h->ids);
     rel(h->iscr); rel(h->cd2); rel(h->ad2); rel(h->grad); rel(h->Hp); rel(h->dist); rel(h->mark);
-    rel(h->spos); rel(h->qS); rel(h->lspart); rel(h->ts_lo);
+    for (auto &g : h->sys)
+        for (auto *bf : {&g.Bc, &g.Sh, &g.gcS, &g.Lstore, &g.U, &g.Tt, &g.yS, &g.rhs, &g.u, &g.tv}) rel(*bf);
+    for (auto &g : h->sys) { rel(g.qS); rel(g.spos); }
+    rel(h->lspart); rel(h->ts_lo);
     rel(h->ts_hi); rel(h->ts_cnt); rel(h->ts_ptr); rel(h->ts_rem); rel(h->ts_done); rel(h->ticket);
-    rel(h->Bc); rel(h->Sh); rel(h->U); rel(h->Tt); rel(h->yS); rel(h->rhs);
-    rel(h->u); rel(h->tv); rel(h->part); rel(h->b0); rel(h->Lstore);
+    rel(h->part); rel(h->b0);
     delete h;
 }
 
@@ -1734,9 +1786,10 @@ int64_t pd_ipc_launch_count(void) { return pdipc::launch_count(); }
 
 int pd_ipc_get_info(const pd_ipc *h, int64_t *info, int32_t n) {
     if (!h || !info) return fail(nullptr, PD_IPC_E_ARG, "NULL argument");
-    const int64_t v[16] = {h->n, h->T, h->nf, h->Ns, h->Nt, h->Ne, h->hf.nsn, h->hf.nnzL, h->hf.depth,
-                           h->capS, h->nslots, h->B, h->F.bw_nblocks, h->F.nU, h->pcg ? 3 : h->gather ? 2 : 1, h->n2};
-    const int k = std::max(0, std::min<int>(n, 16));
+    const int64_t v[17] = {h->n, h->T, h->nf, h->Ns, h->Nt, h->Ne, h->hf.nsn, h->hf.nnzL, h->hf.depth,
+                           h->capS, h->nslots, h->B, h->F.bw_nblocks, h->F.nU, h->pcg ? 3 : h->gather ? 2 : 1, h->n2,
+                           h->nsysb};
+    const int k = std::max(0, std::min<int>(n, 17));
     for (int i = 0; i < k; ++i) info[i] = v[i];
     return k;
 }

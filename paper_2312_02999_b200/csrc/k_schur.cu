@@ -14,6 +14,8 @@
 #include <cooperative_groups.h>
 
 #include "kernels.h"
+#include "prims.h"
+#include <cstring>
 
 #include "dev_common.cuh"
 
@@ -38,50 +40,7 @@ __device__ __forceinline__ void dmma_884(double &d0, double &d1, double a, doubl
                  : "d"(a), "d"(b));
 }
 
-struct SchurArgs {
-    // panel
-    const double *V;
-    int ldv;
-    const double *G;            // w_el = L^{-1} Pi g_el [nf][4] (elastic part only)
-    const double *gc;           // [3|S|] contact part of the gradient on S (Pi g = Pi g_el + E_S gc)
-    const int *qS, *col2sn, *sn_c0, *sn_parent, *lo, *hi, *path_ptr, *path_sn;
-    int nsn, nf, capS;
-    const int *nS_ptr;          // |S| (device); clamped to capS
-    // dense buffers
-    double *K;                  // [capS][ldk] -> Sigma_s
-    int ldk;
-    const double *Bc;           // [3capS][ldb]
-    int ldb;
-    double *Sh;                 // [3capS+1][ldh] augmented Sigma-hat
-    int ldh;
-    double *Lstore;             // [nt][64][64] inverses of the diagonal factor tiles
-    double *LP;                 // [2][kLPTiles][64][64] panel scratch of the small-system P3
-    double *T;                  // 64x64 scratch (sweep pivot inverse)
-    double *U;                  // sweep panel [capS+64][64]
-    double *yS, *y, *u, *t;     // [3capS]
-    double *Kpart;              // [grid][1152] split-K partial tiles (+ y_S partials)
-    double *Z;                  // [nf][4]
-    int *info;
-    const int *same;            // 1: S unchanged, K holds the previous -Sigma_s (reuse it)
-    unsigned long long *prof;   // optional phase timestamps (PDIPC_TRACE), [1024]
-    int pw_min;                 // systems of >= pw_min 64-tiles take the large-system path
-    // reduced-solve backend (the paper's precomputed-inverse variant):
-    //   kSchurPanel  : K_s = V_s^T V_s and y_S = -V_s^T w_el from the panel; Z = w_el + V_s (gc + t)
-    //   kSchurKOnly  : setup: K = V_s^T V_s only (S = the region R), then return
-    //   kSchurGather : K_s = G2[r(S), r(S)] gathered from the precomputed (L^-1)_RR, y_S = rows S of
-    //                  the base solve y_el = L^-T L^-1 Pi g_el (y_S = -y_el[S]); output Z = the
-    //                  sparse right-hand side E_S (gc + t) (zero off S), solved by the caller
-    int mode;
-    const double *G2;           // [n2][n2] (L^-1)_RR (gather mode)
-    int n2;
-    const int *rpos;            // [nf] index of a factor position in R, -1 outside (gather mode)
-    const double *Yel;          // [nf][4] y_el (gather mode)
-    unsigned *bar;              // [kMaxPanels] group-barrier counters of the large-system P3
-    int phase;                  // 0: P0-P5; large systems split over three launches: 1 = P0-P2,
-                                // then k_chol_large (P3), then 2 = P4-P5 (small systems: the
-                                // phase-1 launch does everything, the others return at once)
-};
-constexpr int kMaxPanels = 512;
+
 
 // Barrier among the `target / k`-member group that shares counter *ctr (k-th use: target =
 // k x members).  Members are co-resident (cooperative launch).
@@ -558,12 +517,19 @@ __device__ __forceinline__ void ld_dblocks(double (*Dsh)[8][9], const double *sr
 }
 
 // ---------------------------------------------------------------- the kernel ---------------
-__global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
+__global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurBatch P) {
     extern __shared__ double sm[];
     double *T0 = sm, *T1 = sm + TB * TS, *T2 = sm + 2 * TB * TS, *T3 = sm + 3 * TB * TS;
-    cg::grid_group grid = cg::this_grid();
+    // CTA group grp runs system P.s[grp]: group-local CTA index and count, group barriers
+    const int gsz = gridDim.x / P.nsys, grp = blockIdx.x / gsz;
+    if (grp >= P.nsys) return;
+    __shared__ SchurArgs a_sh;
+    if (threadIdx.x == 0) a_sh = P.s[grp];
+    __syncthreads();
+    const SchurArgs &a = a_sh;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int G = gridDim.x, bid = blockIdx.x;
+    const int G = gsz, bid = blockIdx.x - grp * gsz;
+    unsigned nsync = 0;
     const int nS = min(*a.nS_ptr, a.capS), m = 3 * nS, ma = m + 1;   // augmented size
     if (nS == 0) {   // no contact: z = w = w_el (gather backend: the sparse right-hand side is 0)
         for (int r = bid * NT + tid; r < 4 * a.nf; r += G * NT) a.Z[r] = a.mode == kSchurGather ? 0.0 : a.G[r];
@@ -577,7 +543,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurArgs a) {
     if (a.phase != 2) {                                   // ---------------- P0 .. P3
 #define GSYNC()                                                               \
     do {                                                                      \
-        grid.sync();                                                          \
+        group_bar(a.gbar, ++nsync * (unsigned)G);                             \
         if (a.prof && bid == 0 && tid == 0 && np < 1000) a.prof[np++] = gtimer_s(); \
     } while (0)
     // ------------------------------------------------ P0: y_S = -V_s^T w and K = V_s^T V_s
@@ -1510,6 +1476,7 @@ __global__ void __launch_bounds__(NT2, 1) k_chol_large(CholArgs a) {
 }
 
 static int g_schur_grid = 0;
+static unsigned *g_gbar = nullptr;  // group barrier counters, kMaxSchurSys x 32 (one cache line each)
 // PDIPC_SPLIT_SCHUR=1: large systems factor in k_chol_large (16 warps per CTA, 128 x 128 blocks)
 // between two k_schur_coop launches.  Off by default: measured 16.1 vs 14.7 ms for P3 at n_c 3000
 // (the fused kernel's 128 x 64 blocks on 8 warps reach the same per-SM DMMA rate, and the split
@@ -1528,10 +1495,70 @@ void schur_init(int device) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_schur_coop, NT, kSchurSmem);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
     g_schur_grid = std::max(1, per_sm) * nsm;
-    if (!g_kpart) cudaMalloc(&g_kpart, (size_t)g_schur_grid * 1152 * sizeof(double));
-    if (!g_lp) cudaMalloc(&g_lp, (size_t)2 * kLPTiles * TB * TB * sizeof(double));
-    if (!g_bar) cudaMalloc(&g_bar, (size_t)kMaxPanels * sizeof(unsigned));
+    if (!g_kpart) cudaMalloc(&g_kpart, (size_t)g_schur_grid * 1152 * sizeof(double));   // split by group
+    if (!g_lp) cudaMalloc(&g_lp, (size_t)kMaxSchurSys * 2 * kLPTiles * TB * TB * sizeof(double));
+    if (!g_bar) cudaMalloc(&g_bar, (size_t)kMaxSchurSys * kMaxPanels * sizeof(unsigned));
+    if (!g_gbar) cudaMalloc(&g_gbar, (size_t)kMaxSchurSys * 32 * sizeof(unsigned));
     cudaFuncSetAttribute(k_chol_large, cudaFuncAttributeMaxDynamicSharedMemorySize, kCholSmem);
+}
+
+SchurArgs schur_args(const DevFactor &F, const double *V, int ldv, const double *G, const double *gc,
+                     const int *qS, const int *lo, const int *hi, const int *nS, int capS, double *K, int ldk,
+                     const double *Bc, int ldb, double *Sh, int ldh, double *Lstore, double *T, double *U,
+                     double *yS, double *y, double *u, double *t, double *Z, int *info, const int *same_S,
+                     unsigned long long *prof, int large_min_tiles, int mode, const double *G2, int n2,
+                     const int *rpos, const double *Yel) {
+    SchurArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.V = V; a.ldv = ldv; a.G = G; a.gc = gc; a.qS = qS; a.col2sn = F.col2sn; a.sn_c0 = F.sn_c0;
+    a.sn_parent = F.sn_parent; a.path_ptr = F.path_ptr; a.path_sn = F.path_sn; a.lo = lo; a.hi = hi; a.nsn = F.nsn; a.nf = F.nf; a.nS_ptr = nS; a.capS = capS;
+    a.K = K; a.ldk = ldk; a.Bc = Bc; a.ldb = ldb; a.Sh = Sh; a.ldh = ldh; a.Lstore = Lstore;
+    a.T = T; a.U = U; a.yS = yS; a.y = y; a.u = u; a.t = t; a.Z = Z; a.info = info; a.same = same_S; a.prof = prof;
+    a.pw_min = large_min_tiles > 0 ? std::min(large_min_tiles, kPWMinTiles) : kPWMinTiles;
+    a.mode = mode; a.G2 = G2; a.n2 = n2; a.rpos = rpos; a.Yel = Yel;
+    return a;
+}
+
+int launch_schur_batch(const SchurArgs *sys, int nsys, cudaStream_t st) {
+    if (nsys < 1 || nsys > kMaxSchurSys) return (int)cudaErrorInvalidValue;
+    SchurBatch b;
+    std::memset(&b, 0, sizeof(b));
+    const int gsz = g_schur_grid / nsys;
+    for (int g = 0; g < nsys; ++g) {          // per-group scratch (split-K partials, panels, barriers)
+        b.s[g] = sys[g];
+        b.s[g].Kpart = g_kpart + (size_t)g * gsz * 1152;
+        b.s[g].LP = g_lp + (size_t)g * 2 * kLPTiles * TB * TB;
+        b.s[g].bar = g_bar + (size_t)g * kMaxPanels;
+        b.s[g].gbar = g_gbar + (size_t)g * 32;
+        b.s[g].phase = 0;
+    }
+    b.nsys = nsys;
+    cudaError_t e = dev_zero(g_gbar, kMaxSchurSys * 32 * sizeof(unsigned), st);
+    if (e != cudaSuccess) return (int)e;
+    const bool split = nsys == 1 && !getenv_fused() && sys[0].mode != kSchurKOnly;
+    void *args[] = {&b};
+    note_launch();
+    if (!split)
+        return (int)cudaLaunchCooperativeKernel((const void *)k_schur_coop, dim3(g_schur_grid), dim3(NT), args,
+                                                 kSchurSmem, st);
+    // large systems (PDIPC_SPLIT_SCHUR=1): P0-P2 | P3 in k_chol_large | P4-P5 (each launch checks
+    // the size on the device)
+    b.s[0].phase = 1;
+    e = cudaLaunchCooperativeKernel((const void *)k_schur_coop, dim3(g_schur_grid), dim3(NT), args, kSchurSmem, st);
+    if (e != cudaSuccess) return (int)e;
+    CholArgs c;
+    c.Sh = b.s[0].Sh; c.ldh = b.s[0].ldh; c.nS_ptr = b.s[0].nS_ptr; c.capS = b.s[0].capS; c.pw_min = b.s[0].pw_min;
+    c.Lstore = b.s[0].Lstore; c.info = b.s[0].info; c.bar = b.s[0].bar; c.prof = b.s[0].prof;
+    void *cargs[] = {&c};
+    note_launch();
+    e = cudaLaunchCooperativeKernel((const void *)k_chol_large, dim3(g_schur_grid), dim3(NT2), cargs, kCholSmem, st);
+    if (e != cudaSuccess) return (int)e;
+    b.s[0].phase = 2;
+    e = dev_zero(g_gbar, kMaxSchurSys * 32 * sizeof(unsigned), st);
+    if (e != cudaSuccess) return (int)e;
+    note_launch();
+    return (int)cudaLaunchCooperativeKernel((const void *)k_schur_coop, dim3(g_schur_grid), dim3(NT), args,
+                                             kSchurSmem, st);
 }
 
 int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, const double *gc,
@@ -1541,39 +1568,9 @@ int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, 
                  double *t, double *Z, int *info, const int *same_S, unsigned long long *prof,
                  int large_min_tiles, int mode, const double *G2, int n2, const int *rpos, const double *Yel,
                  cudaStream_t st) {
-    SchurArgs a;
-    a.V = V; a.ldv = ldv; a.G = G; a.gc = gc; a.qS = qS; a.col2sn = F.col2sn; a.sn_c0 = F.sn_c0;
-    a.sn_parent = F.sn_parent; a.path_ptr = F.path_ptr; a.path_sn = F.path_sn; a.lo = lo; a.hi = hi; a.nsn = F.nsn; a.nf = F.nf; a.nS_ptr = nS; a.capS = capS;
-    a.K = K; a.ldk = ldk; a.Bc = Bc; a.ldb = ldb; a.Sh = Sh; a.ldh = ldh; a.Lstore = Lstore;
-    a.T = T; a.U = U; a.yS = yS; a.y = y; a.u = u; a.t = t; a.Z = Z; a.info = info; a.same = same_S; a.prof = prof;
-    a.Kpart = g_kpart;
-    a.LP = g_lp;
-    a.bar = g_bar;
-    a.pw_min = large_min_tiles > 0 ? std::min(large_min_tiles, kPWMinTiles) : kPWMinTiles;
-    a.mode = mode; a.G2 = G2; a.n2 = n2; a.rpos = rpos; a.Yel = Yel;
-    void *args[] = {&a};
-    note_launch();
-    if (mode == kSchurKOnly || getenv_fused()) {                 // one launch: P0-P5
-        a.phase = 0;
-        return (int)cudaLaunchCooperativeKernel((const void *)k_schur_coop, dim3(g_schur_grid), dim3(NT),
-                                                 args, kSchurSmem, st);
-    }
-    // large systems: P0-P2 | P3 in k_chol_large | P4-P5 (each launch checks the size on the device)
-    a.phase = 1;
-    cudaError_t e = cudaLaunchCooperativeKernel((const void *)k_schur_coop, dim3(g_schur_grid), dim3(NT), args,
-                                                kSchurSmem, st);
-    if (e != cudaSuccess) return (int)e;
-    CholArgs c;
-    c.Sh = Sh; c.ldh = ldh; c.nS_ptr = nS; c.capS = capS; c.pw_min = a.pw_min; c.Lstore = Lstore; c.info = info;
-    c.bar = g_bar; c.prof = prof;
-    void *cargs[] = {&c};
-    note_launch();
-    e = cudaLaunchCooperativeKernel((const void *)k_chol_large, dim3(g_schur_grid), dim3(NT2), cargs, kCholSmem, st);
-    if (e != cudaSuccess) return (int)e;
-    a.phase = 2;
-    note_launch();
-    return (int)cudaLaunchCooperativeKernel((const void *)k_schur_coop, dim3(g_schur_grid), dim3(NT), args,
-                                             kSchurSmem, st);
+    const SchurArgs a = schur_args(F, V, ldv, G, gc, qS, lo, hi, nS, capS, K, ldk, Bc, ldb, Sh, ldh, Lstore, T, U,
+                                   yS, y, u, t, Z, info, same_S, prof, large_min_tiles, mode, G2, n2, rpos, Yel);
+    return launch_schur_batch(&a, 1, st);
 }
 
 }  // namespace pdipc

@@ -94,6 +94,66 @@ void launch_cg_finish(const double *z, double *Z, int nf, cudaStream_t st);
 int cg_partials();
 
 // ---- k_schur.cu (fused cooperative dense Schur step, a9)
+constexpr int kMaxPanels = 512;
+struct SchurArgs {
+    // panel
+    const double *V;
+    int ldv;
+    const double *G;            // w_el = L^{-1} Pi g_el [nf][4] (elastic part only)
+    const double *gc;           // [3|S|] contact part of the gradient on S (Pi g = Pi g_el + E_S gc)
+    const int *qS, *col2sn, *sn_c0, *sn_parent, *lo, *hi, *path_ptr, *path_sn;
+    int nsn, nf, capS;
+    const int *nS_ptr;          // |S| (device); clamped to capS
+    // dense buffers
+    double *K;                  // [capS][ldk] -> Sigma_s
+    int ldk;
+    const double *Bc;           // [3capS][ldb]
+    int ldb;
+    double *Sh;                 // [3capS+1][ldh] augmented Sigma-hat
+    int ldh;
+    double *Lstore;             // [nt][64][64] inverses of the diagonal factor tiles
+    double *LP;                 // [2][kLPTiles][64][64] panel scratch of the small-system P3
+    double *T;                  // 64x64 scratch (sweep pivot inverse)
+    double *U;                  // sweep panel [capS+64][64]
+    double *yS, *y, *u, *t;     // [3capS]
+    double *Kpart;              // [grid][1152] split-K partial tiles (+ y_S partials)
+    double *Z;                  // [nf][4]
+    int *info;
+    const int *same;            // 1: S unchanged, K holds the previous -Sigma_s (reuse it)
+    unsigned long long *prof;   // optional phase timestamps (PDIPC_TRACE), [1024]
+    int pw_min;                 // systems of >= pw_min 64-tiles take the large-system path
+    // reduced-solve backend (the paper's precomputed-inverse variant):
+    //   kSchurPanel  : K_s = V_s^T V_s and y_S = -V_s^T w_el from the panel; Z = w_el + V_s (gc + t)
+    //   kSchurKOnly  : setup: K = V_s^T V_s only (S = the region R), then return
+    //   kSchurGather : K_s = G2[r(S), r(S)] gathered from the precomputed (L^-1)_RR, y_S = rows S of
+    //                  the base solve y_el = L^-T L^-1 Pi g_el (y_S = -y_el[S]); output Z = the
+    //                  sparse right-hand side E_S (gc + t) (zero off S), solved by the caller
+    int mode;
+    const double *G2;           // [n2][n2] (L^-1)_RR (gather mode)
+    int n2;
+    const int *rpos;            // [nf] index of a factor position in R, -1 outside (gather mode)
+    const double *Yel;          // [nf][4] y_el (gather mode)
+    unsigned *bar;              // [kMaxPanels] group-barrier counters of the large-system P3
+    int phase;                  // 0: P0-P5; large systems split over three launches: 1 = P0-P2,
+                                // then k_chol_large (P3), then 2 = P4-P5 (small systems: the
+                                // phase-1 launch does everything, the others return at once)
+    unsigned *gbar;             // barrier counter of the CTA group that runs this system
+};
+// Several systems (sequences) per launch: the grid splits into nsys equal CTA groups, group g
+// running system s[g] with group barriers (the batched variable-n_c Schur step of SURVEY 8(e)).
+constexpr int kMaxSchurSys = 4;
+struct SchurBatch {
+    SchurArgs s[kMaxSchurSys];
+    int nsys;
+};
+SchurArgs schur_args(const DevFactor &F, const double *V, int ldv, const double *G, const double *gc,
+                     const int *qS, const int *lo, const int *hi, const int *nS, int capS, double *K, int ldk,
+                     const double *Bc, int ldb, double *Sh, int ldh, double *Lstore, double *T, double *U,
+                     double *yS, double *y, double *u, double *t, double *Z, int *info, const int *same_S,
+                     unsigned long long *prof, int large_min_tiles, int mode, const double *G2, int n2,
+                     const int *rpos, const double *Yel);
+// nsys systems in one cooperative launch (nsys <= kMaxSchurSys; the grid splits into equal groups)
+int launch_schur_batch(const SchurArgs *sys, int nsys, cudaStream_t st);
 void schur_init(int device);
 int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, const double *gc,
                  const int *qS,

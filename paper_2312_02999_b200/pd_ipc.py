@@ -133,7 +133,7 @@ def kernel_times(h, reset=False):
 
 INFO_FIELDS = ("n_verts", "n_tets", "n_free", "n_surf_verts", "n_surf_tris", "n_surf_edges", "supernodes",
                "nnz_L", "etree_depth", "capS", "reuse_slots", "n_seq", "bw_row_blocks", "nU", "reduced_backend",
-               "region_size")
+               "region_size", "schur_systems_per_launch")
 
 
 def get_info(h) -> dict:
