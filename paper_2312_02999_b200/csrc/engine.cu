@@ -238,7 +238,7 @@ struct pd_ipc {
     HostMesh hm;
     HostFactor hf;
     int n = 0, T = 0, nf = 0, Ns = 0, Nt = 0, Ne = 0, B = 1;
-    int capS = 0, ldv = 0, ldh = 0;
+    int capS = 0, ldv = 0, ldh = 0, ldk = 0;   // ldk: even row stride of K / Sigma_s (16-byte rows)
     int debug = 0;
     double cell0 = 0;
     // mesh (shared by sequences)
@@ -778,7 +778,7 @@ static void enqueue_schur(pd_ipc *h, int c0, int c1, int b0, int nb, int it) {
             const int slotr = h->seqs[b]->slot;
             int *di = h->dint(b);
             args[b - c0] = schur_args(F, h->V_slot[slotr].p, h->ldv, h->Yw(b), SB.gcS.p, SB.qS.p, h->ts_lo.p,
-                                      h->ts_hi.p, SB.spos.p + nf, h->capS, h->K_slot[slotr].p, h->capS, SB.Bc.p,
+                                      h->ts_hi.p, SB.spos.p + nf, h->capS, h->K_slot[slotr].p, h->ldk, SB.Bc.p,
                                       3 * h->capS, SB.Sh.p, h->ldh, SB.Lstore.p, SB.Tt.p, SB.U.p, SB.yS.p,
                                       SB.rhs.p, SB.u.p, SB.tv.p, h->Z(b), di + D_INFO, di + D_SAME,
                                       h->trace_file ? h->sprof.p : nullptr,
@@ -1358,7 +1358,7 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         auto alloc_sys = [&](pd_ipc::SysBufs &g) {
             g.spos.exact(nf + 1);
             g.qS.exact(nf + 1);
-            g.Tt.exact(64 * 64);
+            g.Tt.exact(2 * 64 * 64);                 // P1 pivot inverses, double-buffered
             if (m.Nt > 0) {
                 const int cS = h->capS;
                 g.gcS.exact(3 * (size_t)cS + 3);
@@ -1366,7 +1366,7 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
                 g.Sh.exact((size_t)(3 * cS + 1) * ((3 * cS + 8 + 1) & ~1));
                 // large systems: Li tiles [nt+1][64][64]; small: D blocks [nt+1][512] + X tiles [nt][64][64]
                 g.Lstore.exact((size_t)((3 * cS + 1 + 63) / 64 + 1) * (64 * 64 + 512));
-                g.U.exact((size_t)(cS + 64) * 64);
+                g.U.exact((size_t)2 * (cS + 64) * 64);   // P1 sweep panels, double-buffered
                 g.yS.exact(3 * (size_t)cS);
                 g.rhs.exact(3 * (size_t)cS);
                 g.u.exact(3 * (size_t)cS);
@@ -1411,6 +1411,7 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         if (m.Nt > 0) {
             const int cS = h->capS;
             h->ldh = (3 * cS + 8 + 1) & ~1;   // even: 16-byte aligned rows (cp.async 16 B)
+            h->ldk = (cS + 1) & ~1;           // even: 16-byte aligned rows of K / Sigma_s
             h->Up.exact((size_t)std::max(1, f.uoff[f.nsn]) * (((cS + 31) / 32) * 32));
         }
         h->part.exact(std::max<size_t>(4096, (size_t)(m.T + 255) / 256 + (nf + 255) / 256 + 64));
@@ -1461,7 +1462,7 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             h->qS_slot.resize(h->nslots);
             for (int r = 0; r < h->nslots; ++r) {
                 h->V_slot[r].exact(m.Nt > 0 && !h->gather ? (size_t)nf * h->ldv : 32);
-                h->K_slot[r].exact(m.Nt > 0 ? (size_t)h->capS * h->capS : 1);
+                h->K_slot[r].exact(m.Nt > 0 ? (size_t)h->capS * h->ldk : 1);
                 h->qS_slot[r].exact(nf + 1);
             }
             h->nS_slot.exact(h->nslots);

@@ -16,6 +16,7 @@
 #include "kernels.h"
 #include "prims.h"
 #include <cstring>
+#include <cudaTypedefs.h>
 
 #include "dev_common.cuh"
 
@@ -31,7 +32,13 @@ constexpr int kPWMinTiles = 21; // ... for systems of at least this many tiles (
 constexpr int kLPTiles = kPWMinTiles;   // small-system P3: panel tiles per step
 // 4 tiles (P0-P3); the small-system P4 needs y, u (m each), 2 X tiles and 8 partial rows
 constexpr int kSmallMaxM = TB * (kPWMinTiles - 1);
-constexpr int kSchurSmem = (10 * kSmallMaxM + 8 + 2 * 64 * 65) * (int)sizeof(double);   // y, u, X[2], 8 partials
+constexpr int kSchurSmemBase = (10 * kSmallMaxM + 8 + 2 * 64 * 65) * (int)sizeof(double);   // y, u, X[2], 8 partials
+// large-system trailing updates: kTmaStages stages of one 32-wide k chunk of a 128 x 64 block
+// (X: 128 rows, Y: 64 rows, 256 B each, dense with the 128-byte TMA swizzle), 1024-B aligned
+constexpr int kTmaStages = 4, kTmaAhead = 3, kTmaStageB = 192 * 256;
+constexpr int cmax(int x, int y) { return x > y ? x : y; }
+// (P1's update pipeline: two sets of three 64 x 64 tiles)
+constexpr int kSchurSmem = cmax(cmax(kSchurSmemBase, kTmaStages * kTmaStageB + 1024), 6 * TB * TS * 8);
 static_assert(kSchurSmem >= 4 * TB * TS * (int)sizeof(double), "smem");
 
 __device__ __forceinline__ void dmma_884(double &d0, double &d1, double a, double b) {
@@ -517,15 +524,33 @@ __device__ __forceinline__ void ld_dblocks(double (*Dsh)[8][9], const double *sr
 }
 
 // ---------------------------------------------------------------- the kernel ---------------
-__global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurBatch P) {
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+    asm volatile("{\n.reg .pred P1;\nWAIT_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+                 "@!P1 bra WAIT_%=;\n}\n" ::"r"(bar), "r"(parity) : "memory");
+}
+
+__global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ SchurBatch P) {
     extern __shared__ double sm[];
+    // TMA ring of the large-system trailing updates: full[s] (TMA bytes landed), empty[s] (the 8
+    // warps are done with stage s); phases tracked by the chunk counter tma_g (uniform per CTA)
+    __shared__ __align__(8) unsigned long long tma_bar[2 * kTmaStages];
     double *T0 = sm, *T1 = sm + TB * TS, *T2 = sm + 2 * TB * TS, *T3 = sm + 3 * TB * TS;
     // CTA group grp runs system P.s[grp]: group-local CTA index and count, group barriers
     const int gsz = gridDim.x / P.nsys, grp = blockIdx.x / gsz;
     if (grp >= P.nsys) return;
     __shared__ SchurArgs a_sh;
-    if (threadIdx.x == 0) a_sh = P.s[grp];
+    if (threadIdx.x == 0) {
+        a_sh = P.s[grp];
+        for (int i = 0; i < kTmaStages; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&tma_bar[i])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&tma_bar[kTmaStages + i])),
+                         "r"(NT / 32));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
     __syncthreads();
+    unsigned tma_g = 0;                                   // k chunks streamed so far (TMA ring)
     const SchurArgs &a = a_sh;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int G = gsz, bid = blockIdx.x - grp * gsz;
@@ -736,61 +761,159 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurBatch P) {
     if (a.mode == kSchurKOnly) return;        // setup: K = V^T V of the region only
     if (a.prof && bid == 0 && tid == 0) { a.prof[1000 + 1] = np; a.prof[np < 1000 ? np++ : np] = gtimer_s(); }   // phase marker (PDIPC_TRACE)
     // ------------------------------------------------ P1: K <- -K^{-1} (block sweep)
+    // Gauss-Jordan sweep over 64-wide pivot blocks k on the SPD K (kept in its LOWER triangle:
+    // column k's tile i is (i, k) for i > k and the transpose of (k, i) for i < k):
+    //   P_k = A_kk^{-1};  U_i = A_ik P_k (i != k);  A_ij -= U_i A_jk^T (i, j != k);
+    //   column k <- U, A_kk <- -P_k;      after all steps K = -K^{-1}.
+    // Two grid barriers per step: phase A computes U (double-buffered) and writes the PREVIOUS
+    // step's column (its values are in the other U buffer: the one tile of it phase A needs,
+    // (k, k-1), is read from there); phase B runs the rank-64 update with a two-deep cp.async
+    // tile pipeline per CTA, while CTA 0 updates the next pivot tile and inverts it (look-ahead).
     if (!reuse) {
         const int nt = (nS + TB - 1) / TB;
-        for (int k = 0; k < nt; ++k) {
+        const size_t ustride = (size_t)(a.capS + 64) * TB;
+        auto Ubuf = [&](int k) { return a.U + (size_t)(k & 1) * ustride; };
+        auto Tbuf = [&](int k) { return a.T + (size_t)(k & 1) * TB * TB; };
+        // CTA 0: P_k = (A_kk - [U_k A_k,k-1^T])^{-1} = Li^T Li into Tbuf(k)
+        auto pivot_inverse = [&](int k, bool update_first) {
             const int kc0 = k * TB, kn = min(TB, nS - kc0);
-            if (bid == 0) {          // P = A_kk^{-1} = Li^T Li
-                ld_tile(T0, a.K + (size_t)kc0 * a.ldk + kc0, a.ldk, kn, kn);
-                __syncthreads();
-                tile_chol64(T0, T1, kn, kn, a.info);
-                for (int e = tid; e < TB * TB; e += NT) {      // T2 = Li^T
-                    const int r = e >> 6, c = e & 63;
-                    T2[r * TS + c] = T1[c * TS + r];
-                }
-                __syncthreads();
-                tile_xyt(T3, T2, T2, 1.0, false);               // P = Li^T Li on DMMA
-                st_tile(T3, a.T, TB, TB, TB);
+            ld_tile(T0, a.K + (size_t)kc0 * a.ldk + kc0, a.ldk, kn, kn);
+            if (update_first) {
+                ld_tile(T1, Ubuf(k - 1) + (size_t)kc0 * TB, TB, kn, TB);
+                ld_tile(T2, a.K + (size_t)kc0 * a.ldk + kc0 - TB, a.ldk, kn, TB);
             }
-            GSYNC();
-            // K is kept in its LOWER triangle: column k's tile i is (i, k) for i > k and the
-            // transpose of (k, i) for i < k
-            auto ld_colk = [&](double *S, int ti, int rows) {
-                if (ti > k) ld_tile(S, a.K + (size_t)(ti * TB) * a.ldk + kc0, a.ldk, rows, kn);
-                else ld_tile_T(S, a.K + (size_t)kc0 * a.ldk + ti * TB, a.ldk, rows, kn);
-            };
-            for (int b = bid; b < nt - 1; b += G) {      // U_i = A_ik P, i != k
-                const int ti = b < k ? b : b + 1;
-                const int r0 = ti * TB, rows = min(TB, nS - r0);
-                ld_colk(T0, ti, rows);
-                ld_tile(T1, a.T, TB, TB, TB);
+            __syncthreads();
+            if (update_first) {
+                tile_xyt(T0, T1, T2, -1.0, true);
                 __syncthreads();
-                tile_xyt(T2, T0, T1, 1.0, false);
-                st_tile(T2, a.U + (size_t)r0 * TB, TB, rows, TB);
             }
-            GSYNC();
-            for (int b = bid; b < (nt - 1) * nt / 2; b += G) {   // A_ij -= U_i A_jk^T, lower tiles
-                int bi = 0, bj = b;
-                while (bj > bi) { bj -= bi + 1; ++bi; }
-                const int ti = bi < k ? bi : bi + 1, tj = bj < k ? bj : bj + 1;
-                const int r0 = ti * TB, c0 = tj * TB;
-                const int rows = min(TB, nS - r0), cols = min(TB, nS - c0);
-                ld_tile(T0, a.U + (size_t)r0 * TB, TB, rows, TB);
-                ld_colk(T1, tj, cols);
-                ld_tile(T2, a.K + (size_t)r0 * a.ldk + c0, a.ldk, rows, cols);
-                __syncthreads();
-                tile_xyt(T2, T0, T1, -1.0, true);
-                st_tile(T2, a.K + (size_t)r0 * a.ldk + c0, a.ldk, rows, cols);
+            tile_chol64(T0, T1, kn, kn, a.info);
+            for (int e = tid; e < TB * TB; e += NT) {      // T2 = Li^T
+                const int r = e >> 6, c = e & 63;
+                T2[r * TS + c] = T1[c * TS + r];
             }
-            GSYNC();
+            __syncthreads();
+            tile_xyt(T3, T2, T2, 1.0, false);               // P = Li^T Li on DMMA
+            st_tile(T3, Tbuf(k), TB, TB, TB);
+        };
+        // column k of the swept matrix: (r, k) = U_r for r != k, (k, k) = -P_k (lower storage)
+        auto write_column = [&](int k) {
+            const int kc0 = k * TB, kn = min(TB, nS - kc0);
+            const double *Uk = Ubuf(k), *Tk = Tbuf(k);
             for (size_t e = (size_t)bid * NT + tid; e < (size_t)nS * kn; e += (size_t)G * NT) {
                 const int r = (int)(e / kn), c = (int)(e % kn);
-                const double v = (r >= kc0 && r < kc0 + kn) ? -a.T[(r - kc0) * TB + c] : a.U[(size_t)r * TB + c];
+                const double v = (r >= kc0 && r < kc0 + kn) ? -Tk[(r - kc0) * TB + c] : Uk[(size_t)r * TB + c];
                 if (r >= kc0) a.K[(size_t)r * a.ldk + kc0 + c] = v;        // lower: (r, k) block
                 else a.K[(size_t)(kc0 + c) * a.ldk + r] = v;                // lower: (k, r) block
             }
+        };
+        if (bid == 0) pivot_inverse(0, false);
+        GSYNC();
+        double *B0 = sm, *B1 = sm + 3 * TB * TS;             // two sets {X, Y, C} of the pipeline
+        for (int k = 0; k < nt; ++k) {
+            const int kc0 = k * TB, kn = min(TB, nS - kc0);
+            double *Uk = Ubuf(k);
+            // ---- phase A: U_i = A_ik P_k (i != k); column k-1 written
+            for (int b = bid; b < nt - 1; b += G) {
+                const int ti = b < k ? b : b + 1;
+                const int r0 = ti * TB, rows = min(TB, nS - r0);
+                if (ti > k) ld_tile(T0, a.K + (size_t)r0 * a.ldk + kc0, a.ldk, rows, kn);
+                else if (ti == k - 1) {              // (k-1, k) = (k, k-1)^T = U_k(k-1)^T
+                    const double *src = Ubuf(k - 1) + (size_t)kc0 * TB;
+                    for (int e = tid; e < TB * TB; e += NT) {
+                        const int c = e >> 6, r = e & 63;   // T0[r][c] = U_k(k-1)[c][r]
+                        T0[r * TS + c] = (r < rows && c < kn) ? src[(size_t)c * TB + r] : 0.0;
+                    }
+                } else ld_tile_T(T0, a.K + (size_t)kc0 * a.ldk + r0, a.ldk, rows, kn);
+                ld_tile(T1, Tbuf(k), TB, TB, TB);
+                __syncthreads();
+                tile_xyt(T2, T0, T1, 1.0, false);
+                st_tile(T2, Uk + (size_t)r0 * TB, TB, rows, TB);
+                __syncthreads();
+            }
+            if (k > 0) write_column(k - 1);
+            GSYNC();
+            // ---- phase B: A_ij -= U_i A_jk^T over the lower tiles (i, j != k); CTA 0 takes the
+            // next pivot (k+1, k+1) instead (look-ahead), the others the rest
+            const bool la = k + 1 < nt;
+            if (la && bid == 0) pivot_inverse(k + 1, true);
+            const int w0 = (la && G > 1) ? 1 : 0, nw = G - w0;
+            const int ntile = (nt - 1) * nt / 2;
+            auto tile_of = [&](int b, int &ti, int &tj) {
+                int bi = 0, bj = b;
+                while (bj > bi) { bj -= bi + 1; ++bi; }
+                ti = bi < k ? bi : bi + 1;
+                tj = bj < k ? bj : bj + 1;
+            };
+            auto next_b = [&](int b) {               // this CTA's next tile index (skips the pivot)
+                while (b < ntile && w0 == 1) {
+                    int ti, tj;
+                    tile_of(b, ti, tj);
+                    if (!(ti == k + 1 && tj == k + 1)) break;
+                    b += nw;
+                }
+                return b;
+            };
+            auto issue = [&](int b, double *Bs) {    // U_i, A_jk (as Y: rows j), A_ij into {X, Y, C}
+                int ti, tj;
+                tile_of(b, ti, tj);
+                const int r0 = ti * TB, c0 = tj * TB, rows = min(TB, nS - r0), cols = min(TB, nS - c0);
+                double *X = Bs, *Y = Bs + TB * TS, *C = Bs + 2 * TB * TS;
+                // 16-byte pieces (rows of U, K are 16-byte aligned: TB and ldk even); a piece
+                // that straddles the valid width is copied element by element
+                auto cp16 = [&](double *dst, const double *src, int c, int width) {
+                    if (c + 1 < width) {
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src));
+                    } else {
+                        if (c < width) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src));
+                        else dst[0] = 0.0;
+                        dst[1] = 0.0;
+                    }
+                };
+                for (int e = tid; e < TB * TB / 2; e += NT) {
+                    const int r = e >> 5, c = (e & 31) * 2;
+                    if (r < rows) cp16(X + r * TS + c, Uk + (size_t)(r0 + r) * TB + c, c, TB);
+                    else { X[r * TS + c] = 0.0; X[r * TS + c + 1] = 0.0; }
+                    if (r < rows) cp16(C + r * TS + c, a.K + (size_t)(r0 + r) * a.ldk + c0 + c, c, cols);
+                    else { C[r * TS + c] = 0.0; C[r * TS + c + 1] = 0.0; }
+                    if (tj > k) {                    // Y = tile (j, k)
+                        if (r < cols) cp16(Y + r * TS + c, a.K + (size_t)(c0 + r) * a.ldk + kc0 + c, c, kn);
+                        else { Y[r * TS + c] = 0.0; Y[r * TS + c + 1] = 0.0; }
+                    }
+                }
+                if (tj < k)                          // Y = (k, j)^T: coalesced reads of (k, j)
+                    for (int e = tid; e < TB * TB; e += NT) {
+                        const int r = e >> 6, c = e & 63;
+                        if (r < kn && c < cols)
+                            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(Y + c * TS + r)),
+                                         "l"(a.K + (size_t)(kc0 + r) * a.ldk + c0 + c));
+                        else Y[c * TS + r] = 0.0;
+                    }
+                asm volatile("cp.async.commit_group;\n" ::);
+            };
+            if (bid >= w0) {
+                int b = next_b(bid - w0), par = 0;
+                if (b < ntile) issue(b, B0);
+                while (b < ntile) {
+                    const int bn = next_b(b + nw);
+                    asm volatile("cp.async.wait_group 0;\n" ::);
+                    __syncthreads();                 // tile b landed; the other set is free
+                    if (bn < ntile) issue(bn, par ? B0 : B1);
+                    double *Bs = par ? B1 : B0;
+                    tile_xyt(Bs + 2 * TB * TS, Bs, Bs + TB * TS, -1.0, true);
+                    __syncthreads();
+                    int ti, tj;
+                    tile_of(b, ti, tj);
+                    st_tile(Bs + 2 * TB * TS, a.K + (size_t)(ti * TB) * a.ldk + tj * TB, a.ldk, min(TB, nS - ti * TB),
+                            min(TB, nS - tj * TB));
+                    b = bn;
+                    par ^= 1;
+                }
+            }
             GSYNC();
         }
+        write_column(nt - 1);
+        GSYNC();
     }
     if (a.prof && bid == 0 && tid == 0) { a.prof[1000 + 2] = np; a.prof[np < 1000 ? np++ : np] = gtimer_s(); }   // phase marker (PDIPC_TRACE)
     // ------------------------------------------------ P2: augmented Sigma-hat (Sigma_s = -K)
@@ -973,40 +1096,54 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurBatch P) {
         }
     };
     // A_ij -= sum_k L_ik L_jk^T for the 128 x 64 block of row tiles (ti, ti + 1) x column tile tj
-    // (ti + 1 may lie beyond the matrix: zero rows, not stored).  k is streamed in 32-wide chunks
-    // through a 3-stage pipeline of 16-byte cp.async copies; warp w owns rows 16w .. 16w + 15 (two
-    // 8-row groups) x 64 columns, so per 4-wide k step 2 + 8 fragment loads feed 16 independent
-    // DMMAs.  The accumulator is kept negated (adds only).
-    constexpr int KC = 32, XS = 36;
-    static_assert(3 * (128 + 64) * XS * (int)sizeof(double) <= kSchurSmem, "pair pipeline smem");
+    // (ti + 1 may lie beyond the matrix: those rows are not stored).  k is streamed in 32-wide
+    // chunks by thread 0 with 2-D TMA tensor copies (6 boxes of 16 doubles x 64 rows per chunk,
+    // 128-byte swizzle: dense stages, conflict-free fragment loads) into a kTmaStages ring, kTmaAhead
+    // chunks ahead, with mbarriers instead of CTA barriers: full[s] completes when the chunk's
+    // 48 KB landed, empty[s] when all 8 warps are done with it.  Rows of X or Y beyond the matrix
+    // hold whatever Sh holds there (zero beyond the allocation); they only reach accumulator rows /
+    // columns that are not stored.  Warp w owns rows 16w .. 16w + 15 x 64 columns: per 4-wide k step
+    // 2 + 8 fragment loads feed 16 independent DMMAs; the accumulator is kept negated (adds only).
+    constexpr int KC = 32;
     auto update_pair = [&](int ti, int tj, int k0, int k1) {
         const int gr = lane >> 2, gc = lane & 3;
         const int r0 = ti * TB, c0 = tj * TB;
         const int rows = min(2 * TB, ma - r0), cols = min(TB, ma - c0);
-        double *Xs = sm, *Ys = sm + 3 * 128 * XS;
         const int kbeg = k0 * TB, nch = (k1 - k0) * TB / KC;
-        auto issue = [&](int ch) {
-            if (ch < nch) {
-                const int sg = ch % 3, kc = kbeg + ch * KC;
-                double *X = Xs + sg * 128 * XS, *Y = Ys + sg * 64 * XS;
-                for (int e = tid; e < 3 * 1024; e += NT) {      // 2048 X pieces, then 1024 Y pieces
-                    const bool isx = e < 2048;
-                    const int ee = isx ? e : e - 2048, r = ee >> 4, c2 = (ee & 15) * 2;
-                    double *dst = (isx ? X : Y) + r * XS + c2;
-                    if (r < (isx ? rows : cols)) {
-                        const double *src = a.Sh + (size_t)((isx ? r0 : c0) + r) * a.ldh + kc + c2;
-                        const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
-                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src));
-                    } else {
-                        dst[0] = 0.0;
-                        dst[1] = 0.0;
-                    }
-                }
+        const unsigned g0 = tma_g;
+        const unsigned ring = (smem_u32(sm) + 1023u) & ~1023u;
+        const unsigned fullb = smem_u32(tma_bar), emptyb = fullb + 8 * kTmaStages;
+        // earlier generic-proxy writes of the ring (other phases) before the async-proxy writes
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncthreads();
+        auto produce = [&](int ch) {                      // thread 0
+            const unsigned g = g0 + ch, st = g % kTmaStages;
+            if (g >= (unsigned)kTmaStages) mbar_wait(emptyb + 8 * st, ((g / kTmaStages) - 1) & 1);
+            const unsigned fb = fullb + 8 * st, sb = ring + st * kTmaStageB;
+            const int kc = kbeg + ch * KC;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(fb), "r"(kTmaStageB)
+                         : "memory");
+            const unsigned long long tm = reinterpret_cast<unsigned long long>(&P.s[grp].tmap_sh);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+                    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+                                 "[%0], [%1, {%2, %3}], [%4];\n" ::"r"(sb + h * 16384 + j * 8192),
+                                 "l"(tm), "r"(kc + 16 * h), "r"(r0 + 64 * j), "r"(fb)
+                                 : "memory");
+                asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+                             "[%0], [%1, {%2, %3}], [%4];\n" ::"r"(sb + 32768 + h * 8192),
+                             "l"(tm), "r"(kc + 16 * h), "r"(c0), "r"(fb)
+                             : "memory");
             }
-            asm volatile("cp.async.commit_group;\n" ::);
         };
-        issue(0);
-        issue(1);
+        if (tid == 0) {
+            // Sh written through the generic proxy (this and other CTAs, ordered by the barriers)
+            // before the tensor copies read it
+            asm volatile("fence.proxy.async.global;\n" ::: "memory");
+            for (int ch = 0; ch < min(nch, kTmaAhead); ++ch) produce(ch);
+        }
         double acc[2][8][2];
 #pragma unroll
         for (int h = 0; h < 2; ++h)
@@ -1016,25 +1153,34 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurBatch P) {
                 acc[h][nb][0] = (r < rows && c < cols) ? -a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c] : 0.0;
                 acc[h][nb][1] = (r < rows && c + 1 < cols) ? -a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c + 1] : 0.0;
             }
+        // 128-byte swizzle: the 16-byte unit u of row r sits at u ^ (r & 7); rows of a fragment
+        // load have r & 7 = gr (all row bases are multiples of 8)
+        unsigned sw[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) sw[q] = ((((2 * q) + (gc >> 1)) ^ gr) << 4) + ((gc & 1) << 3);
+        const char *smc = reinterpret_cast<const char *>(sm) + (ring - smem_u32(sm));
         for (int ch = 0; ch < nch; ++ch) {
-            issue(ch + 2);
-            asm volatile("cp.async.wait_group 2;\n" ::);
-            __syncthreads();
-            const double *X = Xs + (ch % 3) * 128 * XS + (16 * wid + gr) * XS + gc;
-            const double *Y = Ys + (ch % 3) * 64 * XS + gr * XS + gc;
+            if (tid == 0 && ch + kTmaAhead < nch) produce(ch + kTmaAhead);
+            const unsigned g = g0 + ch, st = g % kTmaStages;
+            mbar_wait(fullb + 8 * st, (g / kTmaStages) & 1);
+            const char *xa = smc + st * kTmaStageB + (16 * wid + gr) * 128;
+            const char *yb = smc + st * kTmaStageB + 32768 + gr * 128;
 #pragma unroll
             for (int k4 = 0; k4 < KC / 4; ++k4) {
-                const double a0 = X[4 * k4], a1 = X[8 * XS + 4 * k4];
+                const int hx = (k4 >> 2) * 16384 + sw[k4 & 3], hy = (k4 >> 2) * 8192 + sw[k4 & 3];
+                const double a0 = *reinterpret_cast<const double *>(xa + hx);
+                const double a1 = *reinterpret_cast<const double *>(xa + 1024 + hx);
 #pragma unroll
                 for (int nb = 0; nb < 8; ++nb) {
-                    const double bv = Y[8 * nb * XS + 4 * k4];
+                    const double bv = *reinterpret_cast<const double *>(yb + nb * 1024 + hy);
                     dmma_884(acc[0][nb][0], acc[0][nb][1], a0, bv);
                     dmma_884(acc[1][nb][0], acc[1][nb][1], a1, bv);
                 }
             }
-            __syncthreads();                       // stage ch % 3 is refilled by issue(ch + 3)
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(emptyb + 8 * st) : "memory");
         }
-        asm volatile("cp.async.wait_group 0;\n" ::);
+        tma_g = g0 + nch;
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -1043,6 +1189,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurBatch P) {
                 if (r < rows && c < cols) a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c] = -acc[h][nb][0];
                 if (r < rows && c + 1 < cols) a.Sh[(size_t)(r0 + r) * a.ldh + c0 + c + 1] = -acc[h][nb][1];
             }
+        __syncthreads();                                  // the ring is free for the caller's next phase
     };
     // pairs of row tiles (ti, ti + 1), ti = tj + 2p, over the tile columns [ja, jb): linear index b
     auto pair_of = [&](int b, int ja, int &ti, int &tj) {
@@ -1057,6 +1204,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurBatch P) {
         return t;
     };
     const int npan = nt >= a.pw_min ? (nt + kPW - 1) / kPW : 0;
+    if (a.prof && bid == 0 && tid == 0) a.prof[997] = (unsigned long long)(a.wu_coef * 1000.0);
     for (int q = 0; q < npan; ++q) {
         const int c0t = q * kPW, c1t = min(nt, c0t + kPW);       // panel q: tile columns [c0t, c1t)
         const int rr = nt - c1t;                                   // tile columns right of panel q
@@ -1071,7 +1219,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurBatch P) {
                 for (int j = k + 1; j < c1t; ++j) wp += 1.3 * (nt - j);
                 ws += 4.0 + 3 * 0.3;
             }
-            const double wu = 4.0 * rr * (rr + 1) / 2.0;
+            const double wu = a.wu_coef * rr * (rr + 1) / 2.0;
             double best = 1e300;
             for (int x = 1; x < G; ++x) {
                 const double t = fmax(ws + wp / x, wu / (G - x));
@@ -1091,16 +1239,34 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurBatch P) {
                 group_bar(ctr, ++nbar * npg);
             }
             if (a.prof && bid == 0 && tid == 0 && q < 100) a.prof[500 + q] = gtimer_s();   // panel update done
+            // Per tile column k: TRSM of the tiles below the diagonal, then the intra-panel update,
+            // with the NEXT diagonal tile taken out of it (look-ahead): CTA 0 updates (k+1, k+1)
+            // in shared memory and factors it while the other CTAs update the rest of the panel,
+            // so the serial tile factor overlaps the update (one group barrier per step saved).
+            // The tile (k+2, k+1), the other half of the pair that holds (k+1, k+1), becomes a
+            // single-tile update.
+            auto factor_diag = [&](int k, bool update_first) {    // CTA 0
+                const int kc0 = k * TB, kn = min(TB, ma - kc0);
+                ld_tile(T0, a.Sh + (size_t)kc0 * a.ldh + kc0, a.ldh, kn, kn);
+                if (update_first) ld_tile(T1, a.Sh + (size_t)kc0 * a.ldh + kc0 - TB, a.ldh, kn, TB);
+                __syncthreads();
+                if (update_first) {               // A_kk -= L_k,k-1 L_k,k-1^T
+                    tile_xyt(T0, T1, T1, -1.0, true);
+                    __syncthreads();
+                }
+                tile_chol64(T0, T1, kn, m - kc0, a.info);
+                st_tile(T0, a.Sh + (size_t)kc0 * a.ldh + kc0, a.ldh, kn, kn);
+                for (int e = tid; e < TB * TB; e += NT) a.Lstore[(size_t)k * TB * TB + e] = T1[(e >> 6) * TS + (e & 63)];
+            };
+            if (bid == 0) factor_diag(c0t, false);
+            group_bar(ctr, ++nbar * npg);
             for (int k = c0t; k < c1t; ++k) {
                 const int kc0 = k * TB, kn = min(TB, ma - kc0);
-                if (bid == 0) {
-                    ld_tile(T0, a.Sh + (size_t)kc0 * a.ldh + kc0, a.ldh, kn, kn);
-                    __syncthreads();
-                    tile_chol64(T0, T1, kn, m - kc0, a.info);
-                    st_tile(T0, a.Sh + (size_t)kc0 * a.ldh + kc0, a.ldh, kn, kn);
-                    for (int e = tid; e < TB * TB; e += NT) a.Lstore[(size_t)k * TB * TB + e] = T1[(e >> 6) * TS + (e & 63)];
-                }
-                group_bar(ctr, ++nbar * npg);
+                // per-column detail of panels 2 and 30 (PDIPC_TRACE): diagonal factored, TRSM
+                // done, intra-panel update done
+                const int pslot = (q == 2 || q == 30) && a.prof && bid == 0 && tid == 0
+                                      ? 900 + (q == 30 ? 16 : 0) + 3 * (k - c0t) : -1;
+                if (pslot >= 0) a.prof[pslot] = gtimer_s();
                 for (int b = bid; b < nt - k - 1; b += npg) {      // L_ik = A_ik Li^T
                     const int ti = k + 1 + b, r0 = ti * TB, rows = min(TB, ma - r0);
                     ld_tile(T0, a.Sh + (size_t)r0 * a.ldh + kc0, a.ldh, rows, kn);
@@ -1110,15 +1276,24 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(SchurBatch P) {
                     st_tile(T2, a.Sh + (size_t)r0 * a.ldh + kc0, a.ldh, rows, kn);
                 }
                 group_bar(ctr, ++nbar * npg);
+                if (pslot >= 0) a.prof[pslot + 1] = gtimer_s();
                 if (k + 1 < c1t) {          // A_ij -= L_ik L_jk^T, k < j < c1t, i >= j
+                    // pair 0 is (k+1, k+2) x (k+1): its diagonal tile goes to CTA 0 (look-ahead),
+                    // its lower tile (k+2, k+1) to the last CTA; pairs 1.. to CTAs 1.. (all
+                    // CTAs when npg == 1)
                     const int tot = pairs_in(k + 1, c1t);
-                    for (int b = bid; b < tot; b += npg) {
-                        int ti, tj;
-                        pair_of(b, k + 1, ti, tj);
-                        update_pair(ti, tj, k, k + 1);
-                    }
+                    if (bid == 0) factor_diag(k + 1, true);
+                    if (bid == npg - 1 && k + 2 < nt) update_tile(k + 2, k + 1, k, k + 1);
+                    const int w0 = npg > 1 ? 1 : 0, nw = npg > 1 ? npg - 1 : 1;
+                    if (bid >= w0)
+                        for (int b = 1 + (bid - w0); b < tot; b += nw) {
+                            int ti, tj;
+                            pair_of(b, k + 1, ti, tj);
+                            update_pair(ti, tj, k, k + 1);
+                        }
                     group_bar(ctr, ++nbar * npg);
                 }
+                if (pslot >= 0) a.prof[pslot + 2] = gtimer_s();
             }
             if (a.prof && bid == 0 && tid == 0 && q < 100) { a.prof[600 + q] = gtimer_s(); a.prof[800 + q] = npg; }
         } else if (q > 0) {     // panel q-1 applied to the tile columns right of panel q
@@ -1489,7 +1664,15 @@ static double *g_kpart = nullptr;   // split-K partial tiles, grid x 1152 double
 static double *g_lp = nullptr;      // small-system P3 panel scratch
 static unsigned *g_bar = nullptr;   // large-system P3 group-barrier counters
 
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;   // driver entry point (no -lcuda)
+
 void schur_init(int device) {
+    if (!g_encode) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void **)&g_encode, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            g_encode = nullptr;
+    }
     cudaFuncSetAttribute(k_schur_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, kSchurSmem);
     int per_sm = 0, nsm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_schur_coop, NT, kSchurSmem);
@@ -1516,11 +1699,22 @@ SchurArgs schur_args(const DevFactor &F, const double *V, int ldv, const double 
     a.T = T; a.U = U; a.yS = yS; a.y = y; a.u = u; a.t = t; a.Z = Z; a.info = info; a.same = same_S; a.prof = prof;
     a.pw_min = large_min_tiles > 0 ? std::min(large_min_tiles, kPWMinTiles) : kPWMinTiles;
     a.mode = mode; a.G2 = G2; a.n2 = n2; a.rpos = rpos; a.Yel = Yel;
+    static const double wu = [] { const char *e = std::getenv("PDIPC_SCHUR_WU"); return e ? std::atof(e) : 4.0; }();
+    a.wu_coef = wu;
+    if (g_encode && Sh && ldh > 0 && capS > 0) {
+        const cuuint64_t dims[2] = {(cuuint64_t)ldh, (cuuint64_t)(3 * capS + 1)};
+        const cuuint64_t strides[1] = {(cuuint64_t)ldh * sizeof(double)};
+        const cuuint32_t box[2] = {16, 64}, es[2] = {1, 1};
+        g_encode(&a.tmap_sh, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, Sh, dims, strides, box, es,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
     return a;
 }
 
 int launch_schur_batch(const SchurArgs *sys, int nsys, cudaStream_t st) {
     if (nsys < 1 || nsys > kMaxSchurSys) return (int)cudaErrorInvalidValue;
+    if (!g_encode) return (int)cudaErrorNotSupported;    // the trailing updates need TMA descriptors
     SchurBatch b;
     std::memset(&b, 0, sizeof(b));
     const int gsz = g_schur_grid / nsys;

@@ -1,6 +1,7 @@
 // Host-callable launchers of the CUDA kernels (internal to the library).
 #pragma once
 #include <cuda_runtime.h>
+#include <cuda.h>
 #include <cstdint>
 
 namespace pdipc {
@@ -138,6 +139,12 @@ struct SchurArgs {
                                 // then k_chol_large (P3), then 2 = P4-P5 (small systems: the
                                 // phase-1 launch does everything, the others return at once)
     unsigned *gbar;             // barrier counter of the CTA group that runs this system
+    double wu_coef;             // large-system P3 split: work of a trailing 128x64 k=256 update (units of
+                                // a 64^3 tile product; PDIPC_SCHUR_WU, default 4)
+    // TMA descriptor of Sh ([3capS+1] rows x ldh doubles, boxes of 16 doubles x 64 rows, 128-byte
+    // swizzle): the large-system trailing updates stream their k chunks with tensor copies.
+    // Encoded on the host by schur_args(); read by the kernel from the (grid-constant) parameter.
+    alignas(64) CUtensorMap tmap_sh;
 };
 // Several systems (sequences) per launch: the grid splits into nsys equal CTA groups, group g
 // running system s[g] with group barriers (the batched variable-n_c Schur step of SURVEY 8(e)).

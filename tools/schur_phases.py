@@ -39,7 +39,7 @@ nS, _ = rows[-1]
 i = len(data) // rec - 1
 pr = np.frombuffer(data, dtype=np.uint64, count=1024, offset=i * rec + 4).astype(np.int64)
 m3 = int(pr[1003])
-print("P3 detail (us from the iteration start): q  npg  panel_upd_done  panel_done  update_done  end")
+print("P3 detail (us from the iteration start): q  npg  panel_upd_done  panel_done  update_done  end;  wu_coef", pr[997] / 1000)
 for q in range(100):
     if pr[800 + q] == 0:
         break
@@ -48,3 +48,24 @@ for q in range(100):
     print(q, int(pr[800 + q]), round((pr[500 + q] - t0) / 1e3, 1) if pr[500 + q] else "-",
           round((pr[600 + q] - t0) / 1e3, 1), round((pr[700 + q] - t0) / 1e3, 1) if pr[700 + q] else "-",
           round((t1 - t0) / 1e3, 1))
+# per-column detail of panels 2 and 30: after the diagonal factor, after the TRSM barrier, after
+# the intra-panel update barrier (us from the panel-update-done stamp)
+for qq, off in ((2, 900), (30, 916)):
+    if pr[off] == 0:
+        continue
+    base = pr[500 + qq]
+    cols = [[round((pr[off + 3 * c + j] - base) / 1e3, 1) for j in range(3)] for c in range(4)]
+    print(f"panel {qq} columns (diag, trsm, update) us after its panel update:", cols)
+# P1 sweep detail of the last traced iteration with S changed: per pivot step, phase A (U, the
+# previous column) and phase B (rank-64 update + next pivot) in us, from the grid-barrier stamps
+for i in range(len(data) // rec - 1, -1, -1):
+    pr = np.frombuffer(data, dtype=np.uint64, count=1024, offset=i * rec + 4).astype(np.int64)
+    m1, m2 = int(pr[1001]), int(pr[1002])
+    if m2 - m1 > 8:
+        st = [pr[j] for j in range(m1, m2 + 1)]
+        d = np.diff(np.array(st, dtype=np.float64)) / 1e3
+        A, B = d[1:-2:2], d[2:-2:2]
+        print(f"P1 detail (n_c {struct.unpack_from('i', data, i * rec)[0]}): first pivot {d[0]:.1f} us, "
+              f"phase A mean {A.mean():.1f} (first {A[:3].round(1).tolist()}), phase B mean {B.mean():.1f} "
+              f"(first {B[:3].round(1).tolist()}, last {B[-3:].round(1).tolist()}), steps {len(B)}")
+        break
