@@ -797,14 +797,22 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
             st_tile(T3, Tbuf(k), TB, TB, TB);
         };
         // column k of the swept matrix: (r, k) = U_r for r != k, (k, k) = -P_k (lower storage)
-        auto write_column = [&](int k) {
+        // mirror (last column): also the transposed entry in the upper triangle, from the lower
+        // entry (P2 reads rows of Sigma_s)
+        auto write_column = [&](int k, bool mirror) {
             const int kc0 = k * TB, kn = min(TB, nS - kc0);
             const double *Uk = Ubuf(k), *Tk = Tbuf(k);
             for (size_t e = (size_t)bid * NT + tid; e < (size_t)nS * kn; e += (size_t)G * NT) {
                 const int r = (int)(e / kn), c = (int)(e % kn);
-                const double v = (r >= kc0 && r < kc0 + kn) ? -Tk[(r - kc0) * TB + c] : Uk[(size_t)r * TB + c];
-                if (r >= kc0) a.K[(size_t)r * a.ldk + kc0 + c] = v;        // lower: (r, k) block
-                else a.K[(size_t)(kc0 + c) * a.ldk + r] = v;                // lower: (k, r) block
+                const bool diag = r >= kc0 && r < kc0 + kn;
+                const double v = diag ? -Tk[(r - kc0) * TB + c] : Uk[(size_t)r * TB + c];
+                if (!mirror) {
+                    if (r >= kc0) a.K[(size_t)r * a.ldk + kc0 + c] = v;        // lower: (r, k) block
+                    else a.K[(size_t)(kc0 + c) * a.ldk + r] = v;                // lower: (k, r) block
+                } else if (!diag || r - kc0 >= c) {
+                    a.K[(size_t)r * a.ldk + kc0 + c] = v;
+                    a.K[(size_t)(kc0 + c) * a.ldk + r] = v;
+                }
             }
         };
         if (bid == 0) pivot_inverse(0, false);
@@ -831,7 +839,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
                 st_tile(T2, Uk + (size_t)r0 * TB, TB, rows, TB);
                 __syncthreads();
             }
-            if (k > 0) write_column(k - 1);
+            if (k > 0) write_column(k - 1, false);
             GSYNC();
             // ---- phase B: A_ij -= U_i A_jk^T over the lower tiles (i, j != k); CTA 0 takes the
             // next pivot (k+1, k+1) instead (look-ahead), the others the rest
@@ -904,15 +912,27 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
                     __syncthreads();
                     int ti, tj;
                     tile_of(b, ti, tj);
-                    st_tile(Bs + 2 * TB * TS, a.K + (size_t)(ti * TB) * a.ldk + tj * TB, a.ldk, min(TB, nS - ti * TB),
-                            min(TB, nS - tj * TB));
+                    const int rows = min(TB, nS - ti * TB), cols = min(TB, nS - tj * TB);
+                    if (k + 1 < nt) {
+                        st_tile(Bs + 2 * TB * TS, a.K + (size_t)(ti * TB) * a.ldk + tj * TB, a.ldk, rows, cols);
+                    } else {                         // final values: lower entries and their mirror
+                        const double *Cs = Bs + 2 * TB * TS;
+                        for (int e = tid; e < TB * TB; e += NT) {
+                            const int r = e >> 6, cc = e & 63;
+                            if (r < rows && cc < cols && (ti > tj || r >= cc)) {
+                                const double v = Cs[r * TS + cc];
+                                a.K[(size_t)(ti * TB + r) * a.ldk + tj * TB + cc] = v;
+                                a.K[(size_t)(tj * TB + cc) * a.ldk + ti * TB + r] = v;
+                            }
+                        }
+                    }
                     b = bn;
                     par ^= 1;
                 }
             }
             GSYNC();
         }
-        write_column(nt - 1);
+        write_column(nt - 1, true);
         GSYNC();
     }
     if (a.prof && bid == 0 && tid == 0) { a.prof[1000 + 2] = np; a.prof[np < 1000 ? np++ : np] = gtimer_s(); }   // phase marker (PDIPC_TRACE)
@@ -928,13 +948,25 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
         for (int j = lane; 3 * j + r % 3 <= r; j += 32) srow[3 * j + r % 3] = brow[3 * j + r % 3] - krow[j];
     }
     // b = (Sigma_s (x) I3) y_S with y_S = y_S^el - (K (x) I3) gc, i.e. b = Sigma_s y_S^el - gc
-    for (int row = pb * (NT / 32) + wid; pb >= 0 && row < m; row += pG * (NT / 32)) {
-        const int ai = row / 3, i = row % 3;
-        double acc = 0.0;
-        for (int bb = lane; bb < nS; bb += 32)           // -Sigma_s in K's lower triangle
-            acc -= a.K[(size_t)max(ai, bb) * a.ldk + min(ai, bb)] * a.yS[3 * bb + i];
-        acc = warp_sum(acc);
-        if (lane == 0) a.Sh[(size_t)m * a.ldh + row] = acc - a.gc[row];
+    // (K holds -Sigma_s in both triangles: the sweep mirrors its final values; a warp reads a row
+    // once for the three components)
+    for (int ai = pb * (NT / 32) + wid; pb >= 0 && ai < nS; ai += pG * (NT / 32)) {
+        const double *krow = a.K + (size_t)ai * a.ldk;
+        double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+        for (int bb = lane; bb < nS; bb += 32) {
+            const double kv = krow[bb];
+            acc0 -= kv * a.yS[3 * bb + 0];
+            acc1 -= kv * a.yS[3 * bb + 1];
+            acc2 -= kv * a.yS[3 * bb + 2];
+        }
+        acc0 = warp_sum(acc0);
+        acc1 = warp_sum(acc1);
+        acc2 = warp_sum(acc2);
+        if (lane == 0) {
+            a.Sh[(size_t)m * a.ldh + 3 * ai + 0] = acc0 - a.gc[3 * ai + 0];
+            a.Sh[(size_t)m * a.ldh + 3 * ai + 1] = acc1 - a.gc[3 * ai + 1];
+            a.Sh[(size_t)m * a.ldh + 3 * ai + 2] = acc2 - a.gc[3 * ai + 2];
+        }
     }
     if (bid == 0 && tid == 0) a.Sh[(size_t)m * a.ldh + m] = 1.0;
     if (bid == 0)
@@ -1386,6 +1418,65 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
             }
             asm volatile("cp.async.wait_group 0;\n" ::);
             for (int e = tid; e < m; e += NT) a.u[e] = uv[e];
+        }
+        GSYNC();
+    } else if (ntm <= kMaxPanels / 2) {
+        // Dataflow back substitution (no grid barrier per tile): CTA b owns the tiles j = b, b+G,
+        // ... (descending).  For tile j it accumulates y_j - sum_{k>j} C_kj^T u_k in registers, k
+        // descending, each u_k as soon as its flag is set (fixed order: deterministic), then forms
+        // u_j = Li_j^T y_j, stores it and sets flag j.  Every dependency points to a higher tile,
+        // so the wait chain is acyclic; the critical path is one tile product + one flag hand-off
+        // per tile.  Flags: a.bar[512 + j], zeroed in P2.
+        volatile unsigned *flag = a.bar + kMaxPanels / 2;
+        double *yj = T0, *part = T1;                       // [64], [4][64]
+        const int c = tid & 63, rq = tid >> 6;
+        const int jtop = bid < ntm ? bid + ((ntm - 1 - bid) / G) * G : -1;
+        double *Cl = T2, *Lj = T3;                         // last tile C_{j+1,j}, Li_j (smem)
+        for (int j = jtop; j >= 0; j -= G) {
+            const int jc0 = j * TB, jn = min(TB, m - jc0);
+            double acc = 0.0;                              // column c of y_j, rows r = rq, rq + 4, ...
+            for (int k = ntm - 1; k > j + 1; --k) {       // all but the last tile: from L2
+                if (tid == 0)
+                    while (flag[k] == 0u) __nanosleep(32);
+                __syncthreads();
+                const int kc0 = k * TB, kn = min(TB, m - kc0);
+                const double *Ck = a.Sh + (size_t)kc0 * a.ldh + jc0 + c;
+                const double *uk = a.u + kc0;
+                if (c < jn)
+#pragma unroll 4
+                    for (int r = rq; r < kn; r += 4) acc += __ldcg(Ck + (size_t)r * a.ldh) * __ldcg(uk + r);
+            }
+            // the critical step: C_{j+1,j} and Li_j staged in shared memory before the wait
+            const bool has_last = j + 1 < ntm;
+            const int lc0 = (j + 1) * TB, ln = has_last ? min(TB, m - lc0) : 0;
+            if (has_last) ld_tile_async(Cl, a.Sh + (size_t)lc0 * a.ldh + jc0, a.ldh, ln, jn);
+            ld_tile_async(Lj, a.Lstore + (size_t)j * TB * TB, TB, TB, TB);
+            asm volatile("cp.async.commit_group;\n" ::);
+            if (has_last && tid == 0)
+                while (flag[j + 1] == 0u) __nanosleep(20);
+            asm volatile("cp.async.wait_group 0;\n" ::);
+            __syncthreads();
+            if (has_last)
+                for (int r = rq; r < ln; r += 4) acc += Cl[r * TS + c] * __ldcg(a.u + lc0 + r);
+            part[rq * TB + c] = acc;
+            __syncthreads();
+            if (tid < TB)
+                yj[tid] = tid < jn ? a.Sh[(size_t)m * a.ldh + jc0 + tid] -
+                                         ((part[tid] + part[TB + tid]) + (part[2 * TB + tid] + part[3 * TB + tid]))
+                                   : 0.0;
+            __syncthreads();
+            {   // u_j[i] = sum_{r >= i} Li[r][i] y_j[r]: 4 partial sums per output
+                const int i = tid & 63, pq = tid >> 6;
+                double s = 0.0;
+                if (i < jn)
+                    for (int r = i + pq; r < jn; r += 4) s += Lj[r * TS + i] * yj[r];
+                part[pq * TB + i] = s;
+            }
+            __syncthreads();
+            if (tid < jn) a.u[jc0 + tid] = (part[tid] + part[TB + tid]) + (part[2 * TB + tid] + part[3 * TB + tid]);
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) atomicExch((unsigned *)&flag[j], 1u);
         }
         GSYNC();
     } else {

@@ -95,7 +95,7 @@ void launch_cg_finish(const double *z, double *Z, int nf, cudaStream_t st);
 int cg_partials();
 
 // ---- k_schur.cu (fused cooperative dense Schur step, a9)
-constexpr int kMaxPanels = 512;
+constexpr int kMaxPanels = 1024;   // [0, 512): P3 panel barriers, [512, 1024): P4 tile flags
 struct SchurArgs {
     // panel
     const double *V;
