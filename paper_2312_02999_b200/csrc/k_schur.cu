@@ -942,10 +942,21 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
     for (int r = (early0 ? TB : 0) + pb * (NT / 32) + wid; pb >= 0 && r < m; r += pG * (NT / 32)) {
         const double *brow = a.Bc + (size_t)r * a.ldb;
         double *srow = a.Sh + (size_t)r * a.ldh;
-        for (int c = lane; c <= r; c += 32) srow[c] = brow[c];
-        __syncwarp();
         const double *krow = a.K + (size_t)(r / 3) * a.ldk;
-        for (int j = lane; 3 * j + r % 3 <= r; j += 32) srow[3 * j + r % 3] = brow[3 * j + r % 3] - krow[j];
+        const int r3 = r % 3;
+        for (int c0 = 0; c0 <= r; c0 += 128) {           // 4 loads per lane in flight
+            double v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int c = c0 + lane + 32 * u;
+                v[u] = c <= r ? brow[c] - (c % 3 == r3 ? krow[c / 3] : 0.0) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int c = c0 + lane + 32 * u;
+                if (c <= r) srow[c] = v[u];
+            }
+        }
     }
     // b = (Sigma_s (x) I3) y_S with y_S = y_S^el - (K (x) I3) gc, i.e. b = Sigma_s y_S^el - gc
     // (K holds -Sigma_s in both triangles: the sweep mirrors its final values; a warp reads a row
@@ -1235,23 +1246,27 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
         for (int j = ja; j < jb; ++j) t += (nt - j + 1) / 2;
         return t;
     };
-    const int npan = nt >= a.pw_min ? (nt + kPW - 1) / kPW : 0;
+    // panel width in tiles: wider panels amortise the trailing updates (k = 64 kpw per pass) and
+    // the grid barriers; measured best at n_c ~ 3000 (141 tiles): 10 (tools/gpu_kpw_sweep.sh,
+    // profiles/schur_kpw_sweep_r02.txt); narrower for smaller systems
+    const int kpw = min(a.kpw, max(4, nt / 14));
+    const int npan = nt >= a.pw_min ? (nt + kpw - 1) / kpw : 0;
     if (a.prof && bid == 0 && tid == 0) a.prof[997] = (unsigned long long)(a.wu_coef * 1000.0);
     for (int q = 0; q < npan; ++q) {
-        const int c0t = q * kPW, c1t = min(nt, c0t + kPW);       // panel q: tile columns [c0t, c1t)
+        const int c0t = q * kpw, c1t = min(nt, c0t + kpw);       // panel q: tile columns [c0t, c1t)
         const int rr = nt - c1t;                                   // tile columns right of panel q
         int npg = G;
         if (q > 0 && rr > 0 && G > 1) {
             // work estimates in units of a 64^3 tile product: a k = 4-tile update ~ 4, a TRSM or
             // single-k update ~ 1.3, the diagonal factor ~ 4 (serial), a barrier ~ 0.3 (serial)
             double wp = 0.0, ws = 0.0;
-            for (int j = c0t; j < c1t; ++j) wp += 4.0 * (nt - j);
+            for (int j = c0t; j < c1t; ++j) wp += (double)kpw * (nt - j);
             for (int k = c0t; k < c1t; ++k) {
                 wp += 1.3 * (nt - k - 1);
                 for (int j = k + 1; j < c1t; ++j) wp += 1.3 * (nt - j);
                 ws += 4.0 + 3 * 0.3;
             }
-            const double wu = a.wu_coef * rr * (rr + 1) / 2.0;
+            const double wu = 0.25 * a.wu_coef * kpw * rr * (rr + 1) / 2.0;
             double best = 1e300;
             for (int x = 1; x < G; ++x) {
                 const double t = fmax(ws + wp / x, wu / (G - x));
@@ -1266,7 +1281,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
                 for (int b = bid; b < tot; b += npg) {
                     int ti, tj;
                     pair_of(b, c0t, ti, tj);
-                    update_pair(ti, tj, c0t - kPW, c0t);
+                    update_pair(ti, tj, c0t - kpw, c0t);
                 }
                 group_bar(ctr, ++nbar * npg);
             }
@@ -1333,7 +1348,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
             for (int b = ub; b < tot; b += nu) {
                 int ti, tj;
                 pair_of(b, c1t, ti, tj);
-                update_pair(ti, tj, c0t - kPW, c0t);
+                update_pair(ti, tj, c0t - kpw, c0t);
             }
             if (a.prof && tid == 0 && q < 100) atomicMax(a.prof + 700 + q, gtimer_s());   // update group done
         }
@@ -1790,8 +1805,10 @@ SchurArgs schur_args(const DevFactor &F, const double *V, int ldv, const double 
     a.T = T; a.U = U; a.yS = yS; a.y = y; a.u = u; a.t = t; a.Z = Z; a.info = info; a.same = same_S; a.prof = prof;
     a.pw_min = large_min_tiles > 0 ? std::min(large_min_tiles, kPWMinTiles) : kPWMinTiles;
     a.mode = mode; a.G2 = G2; a.n2 = n2; a.rpos = rpos; a.Yel = Yel;
-    static const double wu = [] { const char *e = std::getenv("PDIPC_SCHUR_WU"); return e ? std::atof(e) : 4.0; }();
+    static const double wu = [] { const char *e = std::getenv("PDIPC_SCHUR_WU"); return e ? std::atof(e) : 3.5; }();
     a.wu_coef = wu;
+    static const int kpw = [] { const char *e = std::getenv("PDIPC_SCHUR_KPW"); return e ? std::max(1, std::atoi(e)) : 10; }();
+    a.kpw = kpw;
     if (g_encode && Sh && ldh > 0 && capS > 0) {
         const cuuint64_t dims[2] = {(cuuint64_t)ldh, (cuuint64_t)(3 * capS + 1)};
         const cuuint64_t strides[1] = {(cuuint64_t)ldh * sizeof(double)};

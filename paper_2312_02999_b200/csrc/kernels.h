@@ -139,8 +139,9 @@ struct SchurArgs {
                                 // then k_chol_large (P3), then 2 = P4-P5 (small systems: the
                                 // phase-1 launch does everything, the others return at once)
     unsigned *gbar;             // barrier counter of the CTA group that runs this system
+    int kpw;                    // large-system P3 panel width in 64-tiles (PDIPC_SCHUR_KPW, default 10)
     double wu_coef;             // large-system P3 split: work of a trailing 128x64 k=256 update (units of
-                                // a 64^3 tile product; PDIPC_SCHUR_WU, default 4)
+                                // a 64^3 tile product; PDIPC_SCHUR_WU, default 3.5)
     // TMA descriptor of Sh ([3capS+1] rows x ldh doubles, boxes of 16 doubles x 64 rows, 128-byte
     // swizzle): the large-system trailing updates stream their k chunks with tensor copies.
     // Encoded on the host by schur_args(); read by the kernel from the (grid-constant) parameter.
