@@ -850,6 +850,9 @@ __global__ void k_accum_bc_fx(const int *__restrict__ ids, const int *__restrict
             for (int nb = Wp[jb]; nb < Wp[jb + 1]; ++nb) {
                 const int qb = v2q[Wc[nb]];
                 if (qb < 0 || 3 * sidx[qb] >= ldb) continue;
+                // lower block triangle only (B-check is symmetric: the (b, a) block is the
+                // transpose of the same sums); k_fx_to_double mirrors it
+                if (sidx[qa] < sidx[qb]) continue;
                 const double w = Wv[na] * Wv[nb];
                 const size_t o = (size_t)(3 * sidx[qa]) * ldb + 3 * sidx[qb];
                 for (int a = 0; a < 3; ++a)
@@ -860,17 +863,44 @@ __global__ void k_accum_bc_fx(const int *__restrict__ ids, const int *__restrict
     }
 }
 // n = 3 |S| from the device (clamped to 3 capS)
-__global__ void k_fx_to_double(long long *M, const long long *Ml, int ld, const int *nS_ptr, int capS,
-                               const double *dmax, const int *acnt) {
+// The lower block triangle (row r: columns c < 3 floor(r/3) + 3) of the fixed-point B-check to
+// doubles, in place, and its mirror into the strict upper part: one CTA per 64 x 64 lower tile,
+// the mirror written through shared memory (coalesced on both sides).
+__global__ void __launch_bounds__(256) k_fx_to_double(long long *M, const long long *Ml, int ld, const int *nS_ptr,
+                                                      int capS, const double *dmax, const int *acnt) {
+    __shared__ double S[64][65];
     const int n = 3 * min(*nS_ptr, capS);
     const double inv = 1.0 / fx_scale(dmax, acnt[1]);
-    // a warp per row, lanes over the columns (no per-element division)
-    const int lane = threadIdx.x & 31, nw = (gridDim.x * blockDim.x) >> 5;
-    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw)
-        for (int c = lane; c < n; c += 32) {
-            const size_t off = (size_t)r * ld + c;
-            reinterpret_cast<double *>(M)[off] = fx_get(M[off], Ml[off], inv);
+    const int nt = (n + 63) / 64, ntile = nt * (nt + 1) / 2;
+    double *D = reinterpret_cast<double *>(M);
+    for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+        int R = 0, C = t;
+        while (C > R) { C -= R + 1; ++R; }
+        const int r0 = 64 * R, c0 = 64 * C;
+        for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {
+            const int rr = e >> 6, cc = e & 63, r = r0 + rr, c = c0 + cc;
+            double v = 0.0;
+            if (r < n && c < n && c < 3 * (r / 3) + 3) {
+                const size_t off = (size_t)r * ld + c;
+                v = fx_get(M[off], Ml[off], inv);
+                D[off] = v;
+            }
+            S[rr][cc] = v;
         }
+        if (R == C && threadIdx.x < 64) {           // a 3 x 3 diagonal block straddling the tile edge:
+            const int r = r0 + threadIdx.x;          // its entries right of the tile (no mirror)
+            for (int c = c0 + 64; r < n && c < min(n, 3 * (r / 3) + 3); ++c) {
+                const size_t off = (size_t)r * ld + c;
+                D[off] = fx_get(M[off], Ml[off], inv);
+            }
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {   // (c, r) = (r, c), c < 3 floor(r/3)
+            const int cc = e >> 6, rr = e & 63, r = r0 + rr, c = c0 + cc;
+            if (r < n && c < 3 * (r / 3)) D[(size_t)c * ld + r] = S[rr][cc];
+        }
+        __syncthreads();
+    }
 }
 __global__ void k_grad_pullback_fx(const double4 *__restrict__ g_el, const int *__restrict__ WTp,
                                    const int *__restrict__ WTr, const double *__restrict__ WTv,
@@ -906,7 +936,7 @@ void launch_accum_bc_fx(const int *ids, const int *acnt, int cap, const int *Wp,
 }
 void launch_fx_to_double(long long *M, const long long *Ml, int ld, const int *nS, int capS, const double *dmax,
                          const int *acnt, cudaStream_t st) {
-    PDI_LAUNCH(k_fx_to_double, 296, 256, 0, st)(M, Ml, ld, nS, capS, dmax, acnt);
+    PDI_LAUNCH(k_fx_to_double, 148 * 4, 256, 0, st)(M, Ml, ld, nS, capS, dmax, acnt);
 }
 void launch_grad_pullback_fx(const double4 *g_el, const int *WTp, const int *WTr, const double *WTv,
                              const long long *gsq, const double *dmax, const int *acnt, int nf, double *G,
@@ -964,20 +994,29 @@ __global__ void k_contact_prep(int *__restrict__ mark, int nf, long long *__rest
     }
 }
 
-// zero the leading 3|S| x 3|S| block of M and of M2 (when not null) in one launch
+// zero the lower block triangle (row r: columns c < 3 floor(r/3) + 3) of the leading
+// 3|S| x 3|S| block of M and of M2 (when not null) in one launch; 16-byte stores on even ld
 __global__ void k_zero_square(double *M, double *M2, int ld, const int *nS_ptr, int capS) {
     const int n = 3 * min(*nS_ptr, capS);
     const int lane = threadIdx.x & 31, nw = (gridDim.x * blockDim.x) >> 5;
-    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw)
-        for (int c = 2 * lane; c < n; c += 64) {          // 16-byte stores where aligned
-            const size_t o = (size_t)r * ld + c;
-            M[o] = 0.0;
-            if (c + 1 < n) M[o + 1] = 0.0;
-            if (M2) {
-                M2[o] = 0.0;
-                if (c + 1 < n) M2[o + 1] = 0.0;
+    const bool vec = (ld & 1) == 0;
+    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
+        const int cm = min(n, 3 * (r / 3) + 3);
+        double *m = M + (size_t)r * ld, *m2 = M2 ? M2 + (size_t)r * ld : nullptr;
+        for (int c = 2 * lane; c < cm; c += 64) {
+            if (vec && c + 1 < cm) {
+                *reinterpret_cast<double2 *>(m + c) = make_double2(0.0, 0.0);
+                if (m2) *reinterpret_cast<double2 *>(m2 + c) = make_double2(0.0, 0.0);
+            } else {
+                m[c] = 0.0;
+                if (c + 1 < cm) m[c + 1] = 0.0;
+                if (m2) {
+                    m2[c] = 0.0;
+                    if (c + 1 < cm) m2[c + 1] = 0.0;
+                }
             }
         }
+    }
 }
 
 // ------------------------------------------------------------------ a10 ACCD --------------
@@ -1246,7 +1285,7 @@ void launch_contact_prep(int *mark, int nf, long long *gsq, int ngsq, double *dm
         mark, nf, gsq, ngsq, dmax);
 }
 void launch_zero_square(double *M, double *M2, int ld, const int *nS, int capS, cudaStream_t st) {
-    PDI_LAUNCH(k_zero_square, 296, 256, 0, st)(M, M2, ld, nS, capS);
+    PDI_LAUNCH(k_zero_square, 148 * 8, 256, 0, st)(M, M2, ld, nS, capS);
 }
 void launch_accd(const unsigned long long *keys, const int *ccnt, int cap, const double4 *s,
                  const int *tris, const int *edges, int Nt, int Ne, const double4 *ds, double s_gap,
