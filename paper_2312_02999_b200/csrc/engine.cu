@@ -308,6 +308,11 @@ struct pd_ipc {
     struct SysBufs {
         DBuf<int> qS, spos;                                  // S (factor positions), S positions / |S|
         DBuf<double> Bc, Sh, gcS, Lstore, U, Tt, yS, rhs, u, tv;
+        // B-check assembly: fixed-point accumulators (hi, lo words; zero between uses), the bits
+        // and list of the lower 3 x 3 blocks touched by the current use, and its count
+        DBuf<long long> Bh, Bl;
+        DBuf<unsigned> tbits;
+        DBuf<int> tlist, tcnt;
     };
     std::vector<SysBufs> sys;
     int nsysb = 1;
@@ -734,14 +739,15 @@ static void enqueue_contact(pd_ipc *h, int b, int b0, int nb, int it) {
                          h->st3);
         if (!h->gather && !h->pcg) enqueue_panel_forward(h, b, nS_dev, h->st3);
         CK(cudaEventRecord(h->ev_join3, h->st3));
-        // B-check: fixed-point accumulation into the dense 3|S| x 3|S| block, then to double; the
-        // low words of the fixed-point sums live in the (not yet used) Sigma-hat buffer
+        // B-check: the previous use's blocks cleared in the dense double B-check, fixed-point
+        // accumulation of the lower blocks (recorded in the block list), then the listed blocks
+        // converted (with their mirrors) and their accumulators re-zeroed
         const int ldb = 3 * h->capS;
-        long long *Bl = reinterpret_cast<long long *>(SB.Sh.p);
-        launch_zero_square(SB.Bc.p, SB.Sh.p, ldb, nS_dev, h->capS, st);
+        launch_bc_clear(SB.Bc.p, ldb, h->capS, SB.tlist.p, SB.tcnt.p, st);
+        CK(dev_zero(SB.tcnt.p, sizeof(int), st));
         launch_accum_bc_fx(h->ids.p, acnt, cap, h->Wp.p, h->Wc.p, h->Wv.p, h->v2q.p, SB.spos.p, h->Hp.p, dmax,
-                           reinterpret_cast<long long *>(SB.Bc.p), Bl, ldb, st);
-        launch_fx_to_double(reinterpret_cast<long long *>(SB.Bc.p), Bl, ldb, nS_dev, h->capS, dmax, acnt, st);
+                           SB.Bh.p, SB.Bl.p, ldb, h->capS, SB.tbits.p, SB.tlist.p, SB.tcnt.p, st);
+        launch_bc_convert(SB.Bh.p, SB.Bl.p, SB.Bc.p, ldb, h->capS, SB.tlist.p, SB.tcnt.p, SB.tbits.p, dmax, acnt, st);
         kt.stop(K_ASSEMBLY, st);
         CK(cudaStreamWaitEvent(st, h->ev_join3, 0));     // join stream 3
     } else {
@@ -1363,6 +1369,16 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
                 const int cS = h->capS;
                 g.gcS.exact(3 * (size_t)cS + 3);
                 g.Bc.exact((size_t)9 * cS * cS);
+                g.Bh.exact((size_t)9 * cS * cS);
+                g.Bl.exact((size_t)9 * cS * cS);
+                g.tbits.exact(((size_t)cS * cS + 31) / 32);
+                g.tlist.exact((size_t)cS * (cS + 1) / 2);
+                g.tcnt.exact(1);
+                CK(cudaMemset(g.Bc.p, 0, g.Bc.n * sizeof(double)));
+                CK(cudaMemset(g.Bh.p, 0, g.Bh.n * sizeof(long long)));
+                CK(cudaMemset(g.Bl.p, 0, g.Bl.n * sizeof(long long)));
+                CK(cudaMemset(g.tbits.p, 0, g.tbits.n * sizeof(unsigned)));
+                CK(cudaMemset(g.tcnt.p, 0, sizeof(int)));
                 g.Sh.exact((size_t)(3 * cS + 1) * ((3 * cS + 8 + 1) & ~1));
                 // large systems: Li tiles [nt+1][64][64]; small: D blocks [nt+1][512] + X tiles [nt][64][64]
                 g.Lstore.exact((size_t)((3 * cS + 1 + 63) / 64 + 1) * (64 * 64 + 512));
@@ -1656,8 +1672,14 @@ void pd_ipc_destroy(pd_ipc *h) {
     rel(h->qcnt); rel(h->qoff); rel(h->qlist); rel(h->gsq);
     rel(h->cand_tmp); rel(h->akeys); rel(h->flag); rel(h->pos); rel(h->ctype); rel(h->atype); rel(h->ids);
     rel(h->iscr); rel(h->cd2); rel(h->ad2); rel(h->grad); rel(h->Hp); rel(h->dist); rel(h->mark);
-    for (auto &g : h->sys)
+    for (auto &g : h->sys) {
         for (auto *bf : {&g.Bc, &g.Sh, &g.gcS, &g.Lstore, &g.U, &g.Tt, &g.yS, &g.rhs, &g.u, &g.tv}) rel(*bf);
+        rel(g.Bh);
+        rel(g.Bl);
+        rel(g.tbits);
+        rel(g.tlist);
+        rel(g.tcnt);
+    }
     for (auto &g : h->sys) { rel(g.qS); rel(g.spos); }
     rel(h->lspart); rel(h->ts_lo);
     rel(h->ts_hi); rel(h->ts_cnt); rel(h->ts_ptr); rel(h->ts_rem); rel(h->ts_done); rel(h->ticket);

@@ -830,7 +830,8 @@ __global__ void k_accum_bc_fx(const int *__restrict__ ids, const int *__restrict
                               const int *__restrict__ Wc, const double *__restrict__ Wv,
                               const int *__restrict__ v2q, const int *__restrict__ sidx,
                               const double *__restrict__ Hp, const double *__restrict__ dmax,
-                              long long *__restrict__ Bq, long long *__restrict__ Bl, int ldb) {
+                              long long *__restrict__ Bq, long long *__restrict__ Bl, int ldb, int capS,
+                              unsigned *__restrict__ tbits, int *__restrict__ tlist, int *__restrict__ tcnt) {
     const int n_all = acnt[1];
     const double sc = fx_scale(dmax, n_all);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 16 * n_all; i += gridDim.x * blockDim.x) {
@@ -853,6 +854,12 @@ __global__ void k_accum_bc_fx(const int *__restrict__ ids, const int *__restrict
                 // lower block triangle only (B-check is symmetric: the (b, a) block is the
                 // transpose of the same sums); k_fx_to_double mirrors it
                 if (sidx[qa] < sidx[qb]) continue;
+                {   // record the 3 x 3 block (first touch appends it to the list)
+                    const unsigned key = (unsigned)sidx[qa] * (unsigned)capS + (unsigned)sidx[qb];
+                    const unsigned bit = 1u << (key & 31);
+                    if (!(__ldcg(tbits + (key >> 5)) & bit) && !(atomicOr(tbits + (key >> 5), bit) & bit))
+                        tlist[atomicAdd(tcnt, 1)] = (int)key;
+                }
                 const double w = Wv[na] * Wv[nb];
                 const size_t o = (size_t)(3 * sidx[qa]) * ldb + 3 * sidx[qb];
                 for (int a = 0; a < 3; ++a)
@@ -862,44 +869,36 @@ __global__ void k_accum_bc_fx(const int *__restrict__ ids, const int *__restrict
         }
     }
 }
-// n = 3 |S| from the device (clamped to 3 capS)
-// The lower block triangle (row r: columns c < 3 floor(r/3) + 3) of the fixed-point B-check to
-// doubles, in place, and its mirror into the strict upper part: one CTA per 64 x 64 lower tile,
-// the mirror written through shared memory (coalesced on both sides).
-__global__ void __launch_bounds__(256) k_fx_to_double(long long *M, const long long *Ml, int ld, const int *nS_ptr,
-                                                      int capS, const double *dmax, const int *acnt) {
-    __shared__ double S[64][65];
-    const int n = 3 * min(*nS_ptr, capS);
+// B-check is block-sparse (3 x 3 blocks of S-vertex pairs a pair's embedding weights reach):
+// the accumulation records every lower block (a >= b) it touches in a list; only those blocks
+// are converted to doubles (with their mirror (b, a)), and the fixed-point words are re-zeroed
+// in the same pass, so the accumulators stay zero between uses.  The dense double B-check is zero
+// outside the listed blocks: each use first clears the blocks the previous use wrote.
+__global__ void k_bc_clear(double *__restrict__ Bc, int ld, int capS, const int *__restrict__ tlist,
+                           const int *__restrict__ tcnt) {
+    const int n = *tcnt;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 9 * n; i += gridDim.x * blockDim.x) {
+        const int key = tlist[i / 9], e = i % 9, a = key / capS, b = key % capS;
+        const int r = 3 * a + e / 3, c = 3 * b + e % 3;
+        Bc[(size_t)r * ld + c] = 0.0;
+        if (a != b) Bc[(size_t)c * ld + r] = 0.0;
+    }
+}
+__global__ void k_bc_convert(long long *__restrict__ Bh, long long *__restrict__ Bl, double *__restrict__ Bc, int ld,
+                             int capS, const int *__restrict__ tlist, const int *__restrict__ tcnt,
+                             unsigned *__restrict__ tbits, const double *__restrict__ dmax, const int *__restrict__ acnt) {
+    const int n = *tcnt;
     const double inv = 1.0 / fx_scale(dmax, acnt[1]);
-    const int nt = (n + 63) / 64, ntile = nt * (nt + 1) / 2;
-    double *D = reinterpret_cast<double *>(M);
-    for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
-        int R = 0, C = t;
-        while (C > R) { C -= R + 1; ++R; }
-        const int r0 = 64 * R, c0 = 64 * C;
-        for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {
-            const int rr = e >> 6, cc = e & 63, r = r0 + rr, c = c0 + cc;
-            double v = 0.0;
-            if (r < n && c < n && c < 3 * (r / 3) + 3) {
-                const size_t off = (size_t)r * ld + c;
-                v = fx_get(M[off], Ml[off], inv);
-                D[off] = v;
-            }
-            S[rr][cc] = v;
-        }
-        if (R == C && threadIdx.x < 64) {           // a 3 x 3 diagonal block straddling the tile edge:
-            const int r = r0 + threadIdx.x;          // its entries right of the tile (no mirror)
-            for (int c = c0 + 64; r < n && c < min(n, 3 * (r / 3) + 3); ++c) {
-                const size_t off = (size_t)r * ld + c;
-                D[off] = fx_get(M[off], Ml[off], inv);
-            }
-        }
-        __syncthreads();
-        for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {   // (c, r) = (r, c), c < 3 floor(r/3)
-            const int cc = e >> 6, rr = e & 63, r = r0 + rr, c = c0 + cc;
-            if (r < n && c < 3 * (r / 3)) D[(size_t)c * ld + r] = S[rr][cc];
-        }
-        __syncthreads();
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 9 * n; i += gridDim.x * blockDim.x) {
+        const int key = tlist[i / 9], e = i % 9, a = key / capS, b = key % capS;
+        const int r = 3 * a + e / 3, c = 3 * b + e % 3;
+        const size_t o = (size_t)r * ld + c;
+        const double v = fx_get(Bh[o], Bl[o], inv);
+        Bh[o] = 0;
+        Bl[o] = 0;
+        Bc[o] = v;
+        if (a != b) Bc[(size_t)c * ld + r] = v;
+        if (e == 0) atomicAnd(tbits + ((unsigned)key >> 5), ~(1u << ((unsigned)key & 31)));
     }
 }
 __global__ void k_grad_pullback_fx(const double4 *__restrict__ g_el, const int *__restrict__ WTp,
@@ -930,13 +929,18 @@ void launch_accum_grad_fx(const int *ids, const int *acnt, int cap, const double
 }
 void launch_accum_bc_fx(const int *ids, const int *acnt, int cap, const int *Wp, const int *Wc, const double *Wv,
                         const int *v2q, const int *sidx, const double *Hp, const double *dmax,
-                        long long *Bq, long long *Bl, int ldb, cudaStream_t st) {
+                        long long *Bq, long long *Bl, int ldb, int capS, unsigned *tbits, int *tlist, int *tcnt,
+                        cudaStream_t st) {
     PDI_LAUNCH(k_accum_bc_fx, grid_for(16 * cap, 128, 148 * 16), 128, 0, st)(ids, acnt, Wp, Wc, Wv, v2q, sidx,
-                                                                           Hp, dmax, Bq, Bl, ldb);
+                                                                           Hp, dmax, Bq, Bl, ldb, capS, tbits,
+                                                                           tlist, tcnt);
 }
-void launch_fx_to_double(long long *M, const long long *Ml, int ld, const int *nS, int capS, const double *dmax,
-                         const int *acnt, cudaStream_t st) {
-    PDI_LAUNCH(k_fx_to_double, 148 * 4, 256, 0, st)(M, Ml, ld, nS, capS, dmax, acnt);
+void launch_bc_clear(double *Bc, int ld, int capS, const int *tlist, const int *tcnt, cudaStream_t st) {
+    PDI_LAUNCH(k_bc_clear, 148 * 4, 256, 0, st)(Bc, ld, capS, tlist, tcnt);
+}
+void launch_bc_convert(long long *Bh, long long *Bl, double *Bc, int ld, int capS, const int *tlist, const int *tcnt,
+                       unsigned *tbits, const double *dmax, const int *acnt, cudaStream_t st) {
+    PDI_LAUNCH(k_bc_convert, 148 * 4, 256, 0, st)(Bh, Bl, Bc, ld, capS, tlist, tcnt, tbits, dmax, acnt);
 }
 void launch_grad_pullback_fx(const double4 *g_el, const int *WTp, const int *WTr, const double *WTv,
                              const long long *gsq, const double *dmax, const int *acnt, int nf, double *G,
@@ -991,31 +995,6 @@ __global__ void k_contact_prep(int *__restrict__ mark, int nf, long long *__rest
     if (i0 == 0) {
         dmax[0] = 0.0;
         dmax[1] = 1e300;
-    }
-}
-
-// zero the lower block triangle (row r: columns c < 3 floor(r/3) + 3) of the leading
-// 3|S| x 3|S| block of M and of M2 (when not null) in one launch; 16-byte stores on even ld
-__global__ void k_zero_square(double *M, double *M2, int ld, const int *nS_ptr, int capS) {
-    const int n = 3 * min(*nS_ptr, capS);
-    const int lane = threadIdx.x & 31, nw = (gridDim.x * blockDim.x) >> 5;
-    const bool vec = (ld & 1) == 0;
-    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
-        const int cm = min(n, 3 * (r / 3) + 3);
-        double *m = M + (size_t)r * ld, *m2 = M2 ? M2 + (size_t)r * ld : nullptr;
-        for (int c = 2 * lane; c < cm; c += 64) {
-            if (vec && c + 1 < cm) {
-                *reinterpret_cast<double2 *>(m + c) = make_double2(0.0, 0.0);
-                if (m2) *reinterpret_cast<double2 *>(m2 + c) = make_double2(0.0, 0.0);
-            } else {
-                m[c] = 0.0;
-                if (c + 1 < cm) m[c + 1] = 0.0;
-                if (m2) {
-                    m2[c] = 0.0;
-                    if (c + 1 < cm) m2[c + 1] = 0.0;
-                }
-            }
-        }
     }
 }
 
@@ -1283,9 +1262,6 @@ void launch_broad_prep(double *ext, double cell0, double cap, int *ovf, int *hcn
 void launch_contact_prep(int *mark, int nf, long long *gsq, int ngsq, double *dmax, cudaStream_t st) {
     PDI_LAUNCH(k_contact_prep, std::max(1, std::min(148 * 2, (std::max(nf, ngsq) + 255) / 256)), 256, 0, st)(
         mark, nf, gsq, ngsq, dmax);
-}
-void launch_zero_square(double *M, double *M2, int ld, const int *nS, int capS, cudaStream_t st) {
-    PDI_LAUNCH(k_zero_square, 148 * 8, 256, 0, st)(M, M2, ld, nS, capS);
 }
 void launch_accd(const unsigned long long *keys, const int *ccnt, int cap, const double4 *s,
                  const int *tris, const int *edges, int Nt, int Ne, const double4 *ds, double s_gap,

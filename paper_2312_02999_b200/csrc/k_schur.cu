@@ -1250,23 +1250,31 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
     // the grid barriers; measured best at n_c ~ 3000 (141 tiles): 10 (tools/gpu_kpw_sweep.sh,
     // profiles/schur_kpw_sweep_r02.txt); narrower for smaller systems
     const int kpw = min(a.kpw, max(4, nt / 14));
-    const int npan = nt >= a.pw_min ? (nt + kpw - 1) / kpw : 0;
+    // variable panel widths: the first panel (factored with nothing to overlap) a.kpw0 wide, the
+    // last ones narrower (the panel chain is the critical path there): w = min(kpw, max(4,
+    // remaining / a.ktail)); identical on every CTA
+    auto width = [&](int q, int c0) {
+        if (q == 0) return min(nt, max(1, min(kpw, a.kpw0)));
+        const int w = a.ktail > 0 ? min(kpw, max(4, (nt - c0) / a.ktail)) : kpw;
+        return min(nt - c0, w);
+    };
     if (a.prof && bid == 0 && tid == 0) a.prof[997] = (unsigned long long)(a.wu_coef * 1000.0);
-    for (int q = 0; q < npan; ++q) {
-        const int c0t = q * kpw, c1t = min(nt, c0t + kpw);       // panel q: tile columns [c0t, c1t)
+    int c0t = 0, pc0 = 0;                                 // panel q: [c0t, c1t); previous: [pc0, c0t)
+    for (int q = 0; nt >= a.pw_min && c0t < nt; ++q) {
+        const int c1t = c0t + width(q, c0t), ppw = c0t - pc0;
         const int rr = nt - c1t;                                   // tile columns right of panel q
         int npg = G;
         if (q > 0 && rr > 0 && G > 1) {
             // work estimates in units of a 64^3 tile product: a k = 4-tile update ~ 4, a TRSM or
             // single-k update ~ 1.3, the diagonal factor ~ 4 (serial), a barrier ~ 0.3 (serial)
             double wp = 0.0, ws = 0.0;
-            for (int j = c0t; j < c1t; ++j) wp += (double)kpw * (nt - j);
+            for (int j = c0t; j < c1t; ++j) wp += (double)ppw * (nt - j);
             for (int k = c0t; k < c1t; ++k) {
                 wp += 1.3 * (nt - k - 1);
                 for (int j = k + 1; j < c1t; ++j) wp += 1.3 * (nt - j);
                 ws += 4.0 + 3 * 0.3;
             }
-            const double wu = 0.25 * a.wu_coef * kpw * rr * (rr + 1) / 2.0;
+            const double wu = 0.25 * a.wu_coef * ppw * rr * (rr + 1) / 2.0;
             double best = 1e300;
             for (int x = 1; x < G; ++x) {
                 const double t = fmax(ws + wp / x, wu / (G - x));
@@ -1281,7 +1289,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
                 for (int b = bid; b < tot; b += npg) {
                     int ti, tj;
                     pair_of(b, c0t, ti, tj);
-                    update_pair(ti, tj, c0t - kpw, c0t);
+                    update_pair(ti, tj, pc0, c0t);
                 }
                 group_bar(ctr, ++nbar * npg);
             }
@@ -1348,11 +1356,13 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
             for (int b = ub; b < tot; b += nu) {
                 int ti, tj;
                 pair_of(b, c1t, ti, tj);
-                update_pair(ti, tj, c0t - kpw, c0t);
+                update_pair(ti, tj, pc0, c0t);
             }
             if (a.prof && tid == 0 && q < 100) atomicMax(a.prof + 700 + q, gtimer_s());   // update group done
         }
         GSYNC();
+        pc0 = c0t;
+        c0t = c1t;
     }
     }                                                     // ---------------- end of P0 .. P3
     if (a.prof && bid == 0 && tid == 0) { a.prof[1000 + 4] = np; a.prof[np < 1000 ? np++ : np] = gtimer_s(); }   // phase marker (PDIPC_TRACE)
@@ -1809,6 +1819,10 @@ SchurArgs schur_args(const DevFactor &F, const double *V, int ldv, const double 
     a.wu_coef = wu;
     static const int kpw = [] { const char *e = std::getenv("PDIPC_SCHUR_KPW"); return e ? std::max(1, std::atoi(e)) : 10; }();
     a.kpw = kpw;
+    static const int kpw0 = [] { const char *e = std::getenv("PDIPC_SCHUR_KPW0"); return e ? std::max(1, std::atoi(e)) : 10; }();
+    static const int ktail = [] { const char *e = std::getenv("PDIPC_SCHUR_KTAIL"); return e ? std::atoi(e) : 0; }();
+    a.kpw0 = kpw0;
+    a.ktail = ktail;
     if (g_encode && Sh && ldh > 0 && capS > 0) {
         const cuuint64_t dims[2] = {(cuuint64_t)ldh, (cuuint64_t)(3 * capS + 1)};
         const cuuint64_t strides[1] = {(cuuint64_t)ldh * sizeof(double)};

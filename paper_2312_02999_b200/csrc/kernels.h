@@ -139,6 +139,7 @@ struct SchurArgs {
                                 // then k_chol_large (P3), then 2 = P4-P5 (small systems: the
                                 // phase-1 launch does everything, the others return at once)
     unsigned *gbar;             // barrier counter of the CTA group that runs this system
+    int kpw0, ktail;            // first-panel width; tail narrowing divisor (0: off)
     int kpw;                    // large-system P3 panel width in 64-tiles (PDIPC_SCHUR_KPW, default 10)
     double wu_coef;             // large-system P3 split: work of a trailing 128x64 k=256 update (units of
                                 // a 64^3 tile product; PDIPC_SCHUR_WU, default 3.5)
@@ -212,9 +213,13 @@ void launch_accum_grad_fx(const int *ids, const int *acnt, int cap, const double
                           long long *gsq, cudaStream_t st);
 void launch_accum_bc_fx(const int *ids, const int *acnt, int cap, const int *Wp, const int *Wc, const double *Wv,
                         const int *v2q, const int *sidx, const double *Hp, const double *dmax,
-                        long long *Bq, long long *Bl, int ldb, cudaStream_t st);
-void launch_fx_to_double(long long *M, const long long *Ml, int ld, const int *nS, int capS, const double *dmax,
-                         const int *acnt, cudaStream_t st);
+                        long long *Bq, long long *Bl, int ldb, int capS, unsigned *tbits, int *tlist, int *tcnt,
+                        cudaStream_t st);
+// B-check blocks: clear the previous use's blocks in the dense double B-check; convert the listed
+// fixed-point blocks (and their mirrors), re-zeroing the accumulators and the block bits
+void launch_bc_clear(double *Bc, int ld, int capS, const int *tlist, const int *tcnt, cudaStream_t st);
+void launch_bc_convert(long long *Bh, long long *Bl, double *Bc, int ld, int capS, const int *tlist, const int *tcnt,
+                       unsigned *tbits, const double *dmax, const int *acnt, cudaStream_t st);
 void launch_grad_pullback_fx(const double4 *g_el, const int *WTp, const int *WTr, const double *WTv,
                              const long long *gsq, const double *dmax, const int *acnt, int nf, double *G,
                              cudaStream_t st);
@@ -222,7 +227,6 @@ void launch_grad_pullback(const double4 *g_el, const int *WTp, const int *WTr, c
                           const double4 *gs, int nf, double *G, cudaStream_t st);
 void launch_broad_prep(double *ext, double cell0, double cap, int *ovf, int *hcnt, int n, cudaStream_t st);
 void launch_contact_prep(int *mark, int nf, long long *gsq, int ngsq, double *dmax, cudaStream_t st);
-void launch_zero_square(double *M, double *M2, int ld, const int *nS, int capS, cudaStream_t st);
 void launch_gather_gc(const int *qS, const int *nS, int capS, const int *WTp, const int *WTr, const double *WTv,
                       const long long *gsq, const double *dmax, const int *acnt, double *gc, cudaStream_t st);
 void launch_accd(const unsigned long long *keys, const int *ccnt, int cap, const double4 *s,
