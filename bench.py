@@ -318,7 +318,7 @@ def _fp64_peak(sm_max_mhz):
     return DMMA_FLOP_PER_CLK_SM * N_SM * sm_max_mhz * 1e6 / 1e12
 
 
-def rooflines(kt, info, nb, nS_list, reuse_frac, hbm, sm_max_mhz, peak_src):
+def rooflines(kt, info, nb, nS_list, reuse_frac, hbm, sm_max_mhz, peak_src, upd_frac=0.0):
     """Per kernel group: achieved = ALGORITHMIC bytes (flops) per launch / average launch time
     (live CUDA events), DESIGN.md section 5.  kt: {group: (ms, launches)}; nb sequences per
     lockstep iteration; nS_list: n_c of every sequence."""
@@ -355,9 +355,11 @@ def rooflines(kt, info, nb, nS_list, reuse_frac, hbm, sm_max_mhz, peak_src):
     t, _ = avg("dense_schur")
     if t and nS_list:
         # per sequence at n_c, m = 3 n_c: Cholesky of the augmented Sigma-hat (m^3 / 3), Sigma_s =
-        # K_s^-1 when S changed (n_c^3, reuse fraction excluded), back substitution and t = B u,
-        # Z (4 m^2)
-        fl = [(1.0 - reuse_frac) * nc ** 3 + (3 * nc) ** 3 / 3.0 + 4 * (3 * nc) ** 2 for nc in nS_list]
+        # K_s^-1 by the full sweep (n_c^3) for the iterations that neither reused it (S unchanged)
+        # nor updated it by low-rank steps (counted as 0 flops: conservative), back substitution
+        # and t = B u, Z (4 m^2)
+        fl = [max(0.0, 1.0 - reuse_frac - upd_frac) * nc ** 3 + (3 * nc) ** 3 / 3.0 + 4 * (3 * nc) ** 2
+              for nc in nS_list]
         f = statistics.mean(fl) * info.get("schur_systems_per_launch", 1)   # systems per launch
         pk = _fp64_peak(sm_max_mhz)
         out["dense_schur"] = {"kernel": "k_schur_coop", "bound": "tensor", "achieved": f / t / 1e12, "peak": pk,
@@ -524,6 +526,7 @@ def run_ours(a):
     checks = [(j, seq_checksum(s.positions(b))) for b, j in enumerate(mine)]
     nS_all = [st[b]["n_S"] for st in stats for b in range(nb)]
     reuse = sum(st[b]["sigma_reused"] for st in stats for b in range(nb)) / float(max(1, K * nb))
+    upd = sum(st[b]["sigma_updated"] for st in stats for b in range(nb)) / float(max(1, K * nb))
     # exposed time of the reduced solve per sequence-iteration: B-check ready (end of the
     # sequence's assembly) -> dx ready (its Schur step + its share of the batched backward solves)
     exposed = statistics.mean(st[b]["ms"]["gstep"] for st in stats for b in range(nb))
@@ -575,7 +578,7 @@ def run_ours(a):
     value = job_throughput(allv[:, 0], allv[:, 2])
     hbm, bf16, peak_src = _peaks()
     sm_max = _sm_max_mhz()
-    rl_all = rooflines(kt, info, nb, nS_all, reuse, hbm, sm_max, peak_src)
+    rl_all = rooflines(kt, info, nb, nS_all, reuse, hbm, sm_max, peak_src, upd)
     dom = rl_all.get("dense_schur")
     rl = None
     if dom:
@@ -612,6 +615,7 @@ def run_ours(a):
         "stage_ms_per_seq_iter": seq_ms,
         "n_c_mean": statistics.mean(nS_all), "n_c_max": max(nS_all),
         "sigma_reuse_frac": reuse,
+        "sigma_update_frac": upd,
         "cpu_baseline": cpu,
         "e2e": ({"value": float(allv[:, 3].sum()) / (max_e2e / 1000.0), "unit": "iters/s", "steps": e2e["steps"],
                  "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],

@@ -90,7 +90,9 @@ typedef struct {
                                    large-system (panel, all-CTA back substitution) path;
                                  PD_IPC_DBG_SORT_BROAD   every broad phase takes the sort path;
                                  PD_IPC_DBG_TINY_HASH    the hash broad phase overflows, so each
-                                   iteration is redone on the sort path                        */
+                                   iteration is redone on the sort path;
+                                 PD_IPC_DBG_NO_SIGMA_UPDATE  Sigma_s is swept afresh whenever S
+                                   changed (the exact reuse for an unchanged S stays)           */
     int32_t reduced_backend;  /* how K_s = (L^-1)_SS and the contact part of dx are formed (the
                                  same dx either way):
                                  1 panel: V_s = L^-1 Pi E_S per S (reach-limited forward solve),
@@ -117,6 +119,7 @@ typedef struct {
 #define PD_IPC_DBG_LARGE_SCHUR 1
 #define PD_IPC_DBG_SORT_BROAD  2
 #define PD_IPC_DBG_TINY_HASH   4
+#define PD_IPC_DBG_NO_SIGMA_UPDATE 8   /* full Sigma_s sweep whenever S changed (no low-rank update) */
 
 /* Per sequence, describing the LAST iteration of the last pd_ipc_step call. */
 typedef struct {
@@ -135,6 +138,10 @@ typedef struct {
                                  Misc, total (Table 1 categories)               */
     int32_t sigma_reused;     /* iterations of the call that reused V_s, K_s, Sigma_s (S same) */
     int32_t cg_iters;         /* pcg backend: CG iterations summed over the call's iterations    */
+    int32_t sigma_updated;    /* iterations of the call that updated Sigma_s = K_s^-1 by low-rank
+                                 steps (S changed by <= 64 removed / added vertices, gather
+                                 backend) instead of the full sweep; exact in exact arithmetic, a
+                                 full sweep every 32 consecutive updates bounds the rounding drift */
 } pd_ipc_stats;
 
 /* Create a solver: validates the mesh, computes B_i = D_m^{-1} and w_i = det/6, assembles the
@@ -150,7 +157,10 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
 
 /* Run n_iters iterations of Algorithm 1 (a fixed count) on every sequence.
  * A_next: NULL keeps the current actuation; otherwise [n_seq][n_tets][9] on the host, or on
- * the device when opt.A_on_device = 1.  stats: NULL or [n_seq].  Blocks until done. */
+ * the device when opt.A_on_device = 1.  Every matrix of every sequence is checked
+ * on the device before any sequence takes the new actuation: a non-finite, asymmetric
+ * (|A - A^T|max > 1e-9 |A|max) or det <= 0 matrix fails the call with PD_IPC_E_ACTUATION and the
+ * state is unchanged.  stats: NULL or [n_seq].  Blocks until done. */
 int pd_ipc_step(pd_ipc *h, const double *A_next, int32_t n_iters, pd_ipc_stats *stats);
 
 /* Copy positions x of sequence seq (all vertices, fixed ones at rest) into out [n_verts][3]

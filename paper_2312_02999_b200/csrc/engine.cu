@@ -106,6 +106,7 @@ enum : int {
     D_LSCTR = 19,    // line-search round: blocks finished (the last one decides; reset by it)
     D_NS = 20,       // |S| of the last iteration
     D_CONV = 21,     // [21] converged in this pd_ipc_step call, [22] iterations applied, [23] ticket
+    D_UPDATED = 24,  // iterations of the batch that updated Sigma_s by low-rank steps
     D_STRIDE = 32,
 };
 constexpr int S_STRIDE = 16;   // doubles per sequence in dscal: [0] unused, [1] amin, [2..4] ls,
@@ -265,6 +266,7 @@ struct pd_ipc {
     std::vector<DBuf<double>> V_slot, K_slot;
     std::vector<DBuf<int>> qS_slot;
     DBuf<int> nS_slot;                  // [nslots] |S| of the key (0 = invalid)
+    DBuf<int> nupd_slot;                // [nslots] low-rank Sigma_s updates since the last full sweep
     // reduced-solve backend: panel (V_s on the fly) or gather (precomputed
     // G2 = (L^-1)_RR over the region R of W-supported free vertices, n2 = |R|)
     bool gather = false;
@@ -275,7 +277,8 @@ struct pd_ipc {
     DBuf<double> G2, Yel_all, Zf_all, bw_P2;
     DBuf<int> rpos, ts_done2, bw_cnt2;
     // shared contact / Schur work buffers (a sequence's contact + Schur stages run in order)
-    DBuf<double> A9stage;
+    DBuf<double> A9stage;               // actuation of all sequences (host input), [B][T][9]
+    DBuf<int> aflag;                    // actuation check bits
     DBuf<double4> blo, bhi;
     DBuf<int> hcnt, hstart, hent, qcnt, qoff, qlist;
     unsigned hmask = 0;
@@ -313,6 +316,7 @@ struct pd_ipc {
         DBuf<long long> Bh, Bl;
         DBuf<unsigned> tbits;
         DBuf<int> tlist, tcnt;
+        DBuf<int> dpos, rl, al, uinfo;                      // low-rank Sigma_s update plan
     };
     std::vector<SysBufs> sys;
     int nsysb = 1;
@@ -731,7 +735,9 @@ static void enqueue_contact(pd_ipc *h, int b, int b0, int nb, int it) {
         // V_s, K_s, Sigma_s depend on S (and the constant factor) only: reuse the slot's while S
         // is bit-identical to the S they were computed for
         launch_same_S(SB.qS.p, nS_dev, h->qS_slot[slotr].p, h->nS_slot.p + slotr, di + D_SAME, h->capS,
-                      h->opt.no_sigma_reuse == 0, di + D_CAP, di + D_REUSED, st);
+                      h->opt.no_sigma_reuse == 0, di + D_CAP, di + D_REUSED, SB.dpos.p, SB.rl.p, SB.al.p,
+                      SB.uinfo.p, h->nupd_slot.p + slotr,
+                      h->gather && !(h->opt.debug_flags & PD_IPC_DBG_NO_SIGMA_UPDATE), di + D_UPDATED, st);
         CK(dev_copy(di + D_NS, nS_dev, sizeof(int), st));
         CK(cudaEventRecord(h->ev_S, st));
         CK(cudaStreamWaitEvent(h->st3, h->ev_S, 0));
@@ -791,6 +797,12 @@ static void enqueue_schur(pd_ipc *h, int c0, int c1, int b0, int nb, int it) {
                                       (h->opt.debug_flags & PD_IPC_DBG_LARGE_SCHUR) ? 1 : 0,
                                       h->gather ? kSchurGather : kSchurPanel, h->G2.p, h->n2, h->rpos.p,
                                       h->gather ? h->Yel(b) : nullptr);
+            if (h->gather) {                // the low-rank Sigma_s update plan of k_same_S
+                args[b - c0].uinfo = SB.uinfo.p;
+                args[b - c0].dpos = SB.dpos.p;
+                args[b - c0].rl = SB.rl.p;
+                args[b - c0].al = SB.al.p;
+            }
         }
         CK((cudaError_t)launch_schur_batch(args, c1 - c0, st));
     } else {
@@ -903,8 +915,10 @@ static void run_lockstep(pd_ipc *h, int b0, int nb, int k, std::vector<int> &app
     const unsigned key = (h->buf_epoch << 1) | (kt.on ? 1u : 0u);
     const unsigned key_mask = kt.on ? kt.mask : 0u;
     auto enqueue_batch = [&]() {
-        for (int b = b0; b < b0 + nb; ++b)
+        for (int b = b0; b < b0 + nb; ++b) {
             CK(dev_zero(h->dint(b) + D_ABORT, 4 * sizeof(int), st));   // abort, index, why, reused
+            CK(dev_zero(h->dint(b) + D_UPDATED, sizeof(int), st));
+        }
         CK(dev_zero(h->ticket.p + 1, sizeof(int), st));               // solve fault flags of the batch
         CK(dev_zero(h->ticket2.p + 1, sizeof(int), st));
         for (int i = 0; i < k; ++i) enqueue_lockstep_iteration(h, b0, nb, i);
@@ -1010,6 +1024,7 @@ static void run_lockstep(pd_ipc *h, int b0, int nb, int k, std::vector<int> &app
         const int *d = di.data() + (size_t)j * D_STRIDE;
         const double *s = sc.data() + (size_t)j * S_STRIDE;
         q.stats.sigma_reused += d[D_REUSED];
+        q.stats.sigma_updated += d[D_UPDATED];
         q.nS = d[D_NS];
         q.converged = d[D_CONV] != 0;
         q.iters_applied = d[D_CONV + 1];
@@ -1054,6 +1069,7 @@ static void run_lockstep(pd_ipc *h, int b0, int nb, int k, std::vector<int> &app
 }
 
 // ------------------------------------------------------------------ ABI -------------------
+// host check of the create-time actuation (the same predicate as k_validate_actuation)
 static int validate_actuation(const double *A, size_t nmat, std::string &err) {
     for (size_t t = 0; t < nmat; ++t) {
         const double *a = A + 9 * t;
@@ -1071,18 +1087,30 @@ static int validate_actuation(const double *A, size_t nmat, std::string &err) {
     return 0;
 }
 
-static void upload_actuation(pd_ipc *h, const double *A, bool on_device) {
+// A_next of all sequences checked on the device (non-finite / asymmetric / det <= 0) BEFORE any
+// sequence ingests it: a rejected call leaves the state untouched.  Host input: one H2D copy into
+// a staging buffer; device input (A_on_device): checked in place.
+static int stage_actuation(pd_ipc *h, const double *A, bool on_device, std::string &err) {
     const int T = h->T;
-    for (size_t sq = 0; sq < h->seqs.size(); ++sq) {
-        const double *src = A + 9 * (size_t)T * sq;
-        const double *dsrc = src;
-        if (!on_device) {
-            h->A9stage.ensure(9 * (size_t)T);
-            CK(cudaMemcpyAsync(h->A9stage.p, src, sizeof(double) * 9 * T, cudaMemcpyHostToDevice, h->st));
-            dsrc = h->A9stage.p;
-        }
-        launch_ingest_actuation(dsrc, h->A6((int)sq), T, h->st);
+    const size_t nm = h->seqs.size() * (size_t)T;
+    const double *dA = A;
+    if (!on_device) {
+        h->A9stage.ensure(9 * nm);
+        CK(cudaMemcpyAsync(h->A9stage.p, A, sizeof(double) * 9 * nm, cudaMemcpyHostToDevice, h->st));
+        dA = h->A9stage.p;
     }
+    h->aflag.ensure(1);
+    CK(dev_zero(h->aflag.p, sizeof(int), h->st));
+    launch_validate_actuation(dA, nm, h->aflag.p, h->st);
+    int bits = 0;
+    CK(cudaMemcpyAsync(&bits, h->aflag.p, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    if (bits & 1) { err = "non-finite actuation"; return PD_IPC_E_ACTUATION; }
+    if (bits & 2) { err = "actuation not symmetric"; return PD_IPC_E_ACTUATION; }
+    if (bits & 4) { err = "actuation det <= 0"; return PD_IPC_E_ACTUATION; }
+    for (size_t sq = 0; sq < h->seqs.size(); ++sq)
+        launch_ingest_actuation(dA + 9 * (size_t)T * sq, h->A6((int)sq), T, h->st);
+    return 0;
 }
 
 // Intersection-free check of a state (SURVEY.md 8(b) E_INTERSECTING; 8(c) O0 rest-state check):
@@ -1374,6 +1402,11 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
                 g.tbits.exact(((size_t)cS * cS + 31) / 32);
                 g.tlist.exact((size_t)cS * (cS + 1) / 2);
                 g.tcnt.exact(1);
+                g.dpos.exact((size_t)cS + 1);
+                g.rl.exact(64);
+                g.al.exact(64);
+                g.uinfo.exact(4);
+                CK(cudaMemset(g.uinfo.p, 0, 4 * sizeof(int)));
                 CK(cudaMemset(g.Bc.p, 0, g.Bc.n * sizeof(double)));
                 CK(cudaMemset(g.Bh.p, 0, g.Bh.n * sizeof(long long)));
                 CK(cudaMemset(g.Bl.p, 0, g.Bl.n * sizeof(long long)));
@@ -1483,6 +1516,8 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             }
             h->nS_slot.exact(h->nslots);
             CK(cudaMemset(h->nS_slot.p, 0, sizeof(int) * h->nslots));
+            h->nupd_slot.exact(h->nslots);
+            CK(cudaMemset(h->nupd_slot.p, 0, sizeof(int) * h->nslots));
             for (int sq = 0; sq < Bq; ++sq) h->seqs[sq]->slot = sq % h->nslots;
         }
         if (h->gather) {
@@ -1522,7 +1557,10 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             h->ts_done2.exact(f.nsn);
             h->bw_cnt2.exact(f.nsn);
         }
-        upload_actuation(h.get(), A, false);
+        {
+            std::string e2;
+            if (stage_actuation(h.get(), A, false, e2)) throw CudaError(e2.c_str(), PD_IPC_E_ACTUATION);
+        }
         CK(cudaStreamSynchronize(h->st));
         {   // the rest state must be intersection-free (SURVEY.md 8(b) E_INTERSECTING at create)
             std::string why;
@@ -1548,12 +1586,9 @@ int pd_ipc_step(pd_ipc *h, const double *A_next, int32_t n_iters, pd_ipc_stats *
     try {
         CK(cudaSetDevice(h->device));
         if (A_next) {
-            if (!h->opt.A_on_device) {
-                std::string err;
-                int rc = validate_actuation(A_next, h->seqs.size() * (size_t)h->T, err);
-                if (rc) return fail(h, rc, err);
-            }
-            upload_actuation(h, A_next, h->opt.A_on_device != 0);
+            std::string err;
+            const int rc = stage_actuation(h, A_next, h->opt.A_on_device != 0, err);
+            if (rc) return fail(h, rc, err);
         }
         // Sequences advance in lockstep (one batch = k iterations of all of them, k * B <= kSlotCap);
         // with debug capture on, each sequence runs alone so the shared contact buffers hold its
@@ -1564,6 +1599,7 @@ int pd_ipc_step(pd_ipc *h, const double *A_next, int32_t n_iters, pd_ipc_stats *
         for (int b = 0; b < Bq; ++b) {
             Seq &sq = *h->seqs[b];
             sq.stats.sigma_reused = 0;
+            sq.stats.sigma_updated = 0;
             sq.cg_iters = 0;
             sq.converged = false;
             sq.iters_applied = 0;
@@ -1663,9 +1699,10 @@ void pd_ipc_destroy(pd_ipc *h) {
     for (auto &b : h->K_slot) rel(b);
     for (auto &b : h->qS_slot) rel(b);
     rel(h->nS_slot);
+    rel(h->nupd_slot);
     rel(h->x_all); rel(h->gel_all); rel(h->dx_all); rel(h->s_all); rel(h->ds_all); rel(h->A6_all); rel(h->p_all);
     rel(h->fc_all); rel(h->G_all); rel(h->Yw_all); rel(h->Z_all); rel(h->dscal_all); rel(h->dint_all);
-    rel(h->xstage); rel(h->surf_out); rel(h->A9stage); rel(h->blo);
+    rel(h->xstage); rel(h->surf_out); rel(h->A9stage); rel(h->aflag); rel(h->blo);
     for (auto *bf : {&h->cg_r, &h->cg_p, &h->cg_z, &h->cg_q, &h->cg_t, &h->cg_f, &h->cg_R, &h->cg_part}) rel(*bf);
     if (h->cg_rr_host) cudaFreeHost(h->cg_rr_host);
     rel(h->G2); rel(h->Yel_all); rel(h->Zf_all); rel(h->bw_P2); rel(h->rpos); rel(h->ts_done2); rel(h->bw_cnt2); rel(h->bhi); rel(h->hcnt); rel(h->hstart); rel(h->hent);
@@ -1679,6 +1716,10 @@ void pd_ipc_destroy(pd_ipc *h) {
         rel(g.tbits);
         rel(g.tlist);
         rel(g.tcnt);
+        rel(g.dpos);
+        rel(g.rl);
+        rel(g.al);
+        rel(g.uinfo);
     }
     for (auto &g : h->sys) { rel(g.qS); rel(g.spos); }
     rel(h->lspart); rel(h->ts_lo);

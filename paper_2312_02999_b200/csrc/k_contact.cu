@@ -740,20 +740,77 @@ __global__ void k_mark_S(const int *__restrict__ ids, const int *__restrict__ ac
 }
 
 // same = (S == S_prev, bit for bit, |S| > 0); then S_prev <- S.  One CTA.
+// Sigma_s low-rank update plan (gather backend): when S changed, the new positions' old
+// positions (dpos, -1 = added) and the ordered lists of removed old positions (rl) and added new
+// positions (al), at most kSigmaUpdMax each; uinfo = {update?, |removed|, |added|, n_old}.  The
+// update is taken when the slot holds Sigma_s of the previous S, both lists fit, and the slot has
+// taken fewer than kSigmaUpdRefresh updates in a row (then a full sweep refreshes it).
+constexpr int kSigmaUpdMax = 64, kSigmaUpdRefresh = 32;
+__device__ __forceinline__ int find_sorted(const int *v, int n, int key) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (v[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo < n && v[lo] == key ? lo : -1;
+}
+// block-ordered collection: positions [0, n) flagged by pred, in increasing order, first cap of them
+template <class Pred>
+__device__ int collect_ordered(int n, Pred pred, int *out, int cap, int *scan) {
+    const int nt = blockDim.x, per = (n + nt - 1) / nt, i0 = min(n, threadIdx.x * per), i1 = min(n, i0 + per);
+    int c = 0;
+    for (int i = i0; i < i1; ++i) c += pred(i) ? 1 : 0;
+    scan[threadIdx.x] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int run = 0;
+        for (int t = 0; t < nt; ++t) { const int v = scan[t]; scan[t] = run; run += v; }
+        scan[nt] = run;
+    }
+    __syncthreads();
+    int o = scan[threadIdx.x];
+    for (int i = i0; i < i1; ++i)
+        if (pred(i)) { if (o < cap) out[o] = i; ++o; }
+    const int tot = scan[nt];
+    __syncthreads();
+    return tot;
+}
 __global__ void __launch_bounds__(1024) k_same_S(const int *__restrict__ qS, const int *__restrict__ nS_ptr,
                                                  int *__restrict__ qS_prev, int *__restrict__ nS_prev,
                                                  int *__restrict__ same, int enabled, int cap,
-                                                 int *__restrict__ flags, int *__restrict__ reused) {
+                                                 int *__restrict__ flags, int *__restrict__ reused,
+                                                 int *__restrict__ dpos, int *__restrict__ rl, int *__restrict__ al,
+                                                 int *__restrict__ uinfo, int *__restrict__ nupd, int allow_upd,
+                                                 int *__restrict__ updated) {
+    __shared__ int scan[1025];
     const int nS = min(*nS_ptr, cap), np = *nS_prev;
     if (threadIdx.x == 0 && *nS_ptr > cap) atomicOr(flags, 2);   // |S| beyond the dense buffers
     int eq = enabled && nS > 0 && nS == np;
     for (int i = threadIdx.x; i < nS && eq; i += blockDim.x) eq = qS[i] == qS_prev[i];
     eq = __syncthreads_and(eq);
+    int upd = 0, nr = 0, na = 0;
+    if (!eq && allow_upd && enabled && np > 0 && nS > 0 && dpos) {
+        for (int i = threadIdx.x; i < nS; i += blockDim.x) dpos[i] = find_sorted(qS_prev, np, qS[i]);
+        __syncthreads();
+        na = collect_ordered(nS, [&](int i) { return dpos[i] < 0; }, al, kSigmaUpdMax, scan);
+        nr = collect_ordered(np, [&](int p) { return find_sorted(qS, nS, qS_prev[p]) < 0; }, rl, kSigmaUpdMax, scan);
+        upd = nr <= kSigmaUpdMax && na <= kSigmaUpdMax && *nupd < kSigmaUpdRefresh;
+    }
+    __syncthreads();                                  // every read of the old S is done
     for (int i = threadIdx.x; i < nS; i += blockDim.x) qS_prev[i] = qS[i];
     if (threadIdx.x == 0) {
         *nS_prev = nS;
         *same = eq;
         if (eq) *reused += 1;
+        if (uinfo) {
+            uinfo[0] = upd;
+            uinfo[1] = nr;
+            uinfo[2] = na;
+            uinfo[3] = np;
+        }
+        if (nupd && !eq) *nupd = upd ? *nupd + 1 : 0;
+        if (upd) *updated += 1;
     }
 }
 
@@ -1244,9 +1301,10 @@ void launch_mark_S(const int *ids, const int *acnt, int cap, const int *Wp, cons
     PDI_LAUNCH(k_mark_S, grid_for(4 * cap, 256, 148 * 8), 256, 0, st)(ids, acnt, Wp, Wc, v2q, mark);
 }
 void launch_same_S(const int *qS, const int *nS_ptr, int *qS_prev, int *nS_prev, int *same, int cap,
-                   bool enabled, int *flags, int *reused, cudaStream_t st) {
+                   bool enabled, int *flags, int *reused, int *dpos, int *rl, int *al, int *uinfo, int *nupd,
+                   bool allow_upd, int *updated, cudaStream_t st) {
     PDI_LAUNCH(k_same_S, 1, 1024, 0, st)(qS, nS_ptr, qS_prev, nS_prev, same, enabled ? 1 : 0, cap, flags,
-                                         reused);
+                                         reused, dpos, rl, al, uinfo, nupd, allow_upd ? 1 : 0, updated);
 }
 void launch_grad_pullback(const double4 *g_el, const int *WTp, const int *WTr, const double *WTv,
                           const double4 *gs, int nf, double *G, cudaStream_t st) {

@@ -29,6 +29,30 @@ __global__ void k_ingest_actuation(const double *__restrict__ A9, double *__rest
     A6[5 * (size_t)T + t] = a[8];
 }
 
+// Actuation check on the device (pd_ipc_step rejects a call whose A_next has any matrix that is
+// non-finite (bit 1), not symmetric to 1e-9 of its largest entry (bit 2) or of det <= 0 (bit 4))
+__global__ void k_validate_actuation(const double *__restrict__ A, size_t nmat, int *__restrict__ flag) {
+    int bits = 0;
+    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < nmat; t += (size_t)gridDim.x * blockDim.x) {
+        const double *a = A + 9 * t;
+        double v[9], mx = 0.0;
+        bool fin = true;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+            v[k] = a[k];
+            fin &= isfinite(v[k]);
+            mx = fmax(mx, fabs(v[k]));
+        }
+        if (!fin) { bits |= 1; continue; }
+        const double asym = fmax(fmax(fabs(v[1] - v[3]), fabs(v[2] - v[6])), fabs(v[5] - v[7]));
+        if (asym > 1e-9 * mx) bits |= 2;
+        const double det = v[0] * (v[4] * v[8] - v[5] * v[7]) - v[1] * (v[3] * v[8] - v[5] * v[6]) +
+                           v[2] * (v[3] * v[7] - v[4] * v[6]);
+        if (!(det > 0)) bits |= 4;
+    }
+    if (bits) atomicOr(flag, bits);
+}
+
 // ------------------------------------------------------------------ 3x3 polar -------------
 // Symmetric 3x3 eigen-decomposition by cyclic Jacobi (FP64).  S = V diag(l) V^T.
 __device__ __forceinline__ void jacobi_rot(double S[3][3], double V[3][3], int p, int q) {
@@ -476,6 +500,9 @@ void launch_set_double(double *p, double v, cudaStream_t st) { PDI_LAUNCH(k_set_
 
 void launch_ingest_actuation(const double *A9, double *A6, int T, cudaStream_t st) {
     PDI_LAUNCH(k_ingest_actuation, (T + 255) / 256, 256, 0, st)(A9, A6, T);
+}
+void launch_validate_actuation(const double *A, size_t nmat, int *flag, cudaStream_t st) {
+    PDI_LAUNCH(k_validate_actuation, 148 * 8, 256, 0, st)(A, nmat, flag);
 }
 static int g_ls_minb = 4;   // resident CTAs per SM the local step is compiled for (PDIPC_LS_MINB)
 void elastic_init(int) {

@@ -578,6 +578,8 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
     // accumulates on DMMA.  Diagonal tiles also accumulate y_S for their columns.  Split partials
     // are reduced in a fixed order (deterministic).
     const bool reuse = *a.same != 0;                 // uniform across the grid
+    // S changed by a few vertices: Sigma_s updated by low-rank steps from the slot's previous one
+    const bool supd = !reuse && a.uinfo != nullptr && a.uinfo[0] != 0;
     // Small systems with Sigma_s reused: CTA 0 assembles and factors the first diagonal tile of
     // Sigma-hat right away (it needs only B-check and the stored Sigma_s), while the other CTAs
     // run P0 and P2 -- the first tile factorisation leaves the critical path
@@ -630,7 +632,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
     const int ntk = (nS + 31) / 32;
     // K keeps -Sigma_s when S is unchanged; the gather backend reads K from G2 instead
     const int ntiles = (reuse || a.mode == kSchurGather) ? 0 : ntk * (ntk + 1) / 2;
-    if (a.mode == kSchurGather && !reuse)     // K_s = (L^-1)_SS = G2[r(S), r(S)] (a gather)
+    if (a.mode == kSchurGather && !reuse && !supd)   // K_s = (L^-1)_SS = G2[r(S), r(S)] (a gather)
         for (size_t e = (size_t)bid * NT + tid; e < (size_t)nS * nS; e += (size_t)G * NT) {
             const int i = (int)(e / nS), j = (int)(e % nS);
             a.K[(size_t)i * a.ldk + j] = a.G2[(size_t)a.rpos[a.qS[i]] * a.n2 + a.rpos[a.qS[j]]];
@@ -769,7 +771,168 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
     // step's column (its values are in the other U buffer: the one tile of it phase A needs,
     // (k, k-1), is read from there); phase B runs the rank-64 update with a two-deep cp.async
     // tile pipeline per CTA, while CTA 0 updates the next pivot tile and inverts it (look-ahead).
-    if (!reuse) {
+    if (!reuse && supd) {
+        // Low-rank update (S changed by at most 64 removed and 64 added vertices; K holds -Sigma_old
+        // of the previous S, both triangles).  With Sigma = K_s^{-1} (exact identities):
+        //   removal of R:  Sigma' = Sigma_kk - Sigma_kR Sigma_RR^{-1} Sigma_Rk   (kept rows / cols)
+        //   addition of A: b = K_s[keep, A], X = Sigma' b, Sc = K_s[A, A] - b^T X,
+        //     Sigma_new = [[Sigma' + X Sc^{-1} X^T, -X Sc^{-1}], [-Sc^{-1} X^T, Sc^{-1}]]
+        // in the new S order (dpos: old position of each new one).  Sigma' lives in Sh (free until
+        // P2); Y / Z / X / P in the two U buffers; Sigma_RR^{-1}, Sc^{-1} in T; the partials of b^T X
+        // in Lstore (free until P3).  O(n^2 (|R| + |A|)) instead of the sweep's O(n^3).
+        const int nr = a.uinfo[1], nad = a.uinfo[2], nold = a.uinfo[3], ldk = a.ldk;
+        const size_t ustride = (size_t)(a.capS + 64) * TB;
+        double *Yb = a.U, *Zb = a.U + ustride;             // [n][64] each
+        double *Tm = a.T, *Tm2 = a.T + TB * TB;
+        double *W = a.Sh;                                   // Sigma' (new order, ld = ldk)
+        const int nto = (nold + TB - 1) / TB, ntn = (nS + TB - 1) / TB;
+        auto inv_spd = [&](int nb, double *dst) {         // CTA: dst = T0[0:nb, 0:nb]^{-1} (identity pad)
+            tile_chol64(T0, T1, nb, nb, a.info);
+            for (int e = tid; e < TB * TB; e += NT) {
+                const int r = e >> 6, c = e & 63;
+                T2[r * TS + c] = T1[c * TS + r];
+            }
+            __syncthreads();
+            tile_xyt(T3, T2, T2, 1.0, false);               // Li^T Li
+            st_tile(T3, dst, TB, TB, TB);
+        };
+        auto g2 = [&](int i, int j) {                      // K_s entry of new positions i, j
+            return a.G2[(size_t)a.rpos[a.qS[i]] * a.n2 + a.rpos[a.qS[j]]];
+        };
+        auto find_al = [&](int i) {
+            int lo = 0, hi = nad;
+            while (lo < hi) { const int mid = (lo + hi) >> 1; if (a.al[mid] < i) lo = mid + 1; else hi = mid; }
+            return lo;
+        };
+        if (nr > 0) {
+            if (bid == 0) {                                 // Sigma_RR^{-1}
+                for (int e = tid; e < TB * TB; e += NT) {
+                    const int r = e >> 6, c = e & 63;
+                    T0[r * TS + c] = (r < nr && c < nr) ? -a.K[(size_t)a.rl[r] * ldk + a.rl[c]] : 0.0;
+                }
+                __syncthreads();
+                inv_spd(nr, Tm);
+            }
+            GSYNC();
+            for (int t = bid; t < nto; t += G) {           // Z = Sigma_old[:, R], Y = Z Sigma_RR^{-1}
+                const int p0 = t * TB, rows = min(TB, nold - p0);
+                for (int e = tid; e < TB * TB; e += NT) {
+                    const int r = e >> 6, c = e & 63;
+                    T0[r * TS + c] = (r < rows && c < nr) ? -a.K[(size_t)(p0 + r) * ldk + a.rl[c]] : 0.0;
+                }
+                ld_tile(T1, Tm, TB, TB, TB);
+                __syncthreads();
+                tile_xyt(T2, T0, T1, 1.0, false);
+                st_tile(T0, Zb + (size_t)p0 * TB, TB, rows, TB);
+                st_tile(T2, Yb + (size_t)p0 * TB, TB, rows, TB);
+                __syncthreads();
+            }
+            GSYNC();
+        }
+        for (int t = bid; t < ntn * ntn; t += G) {         // Sigma' = Sigma_old - Y Z^T, new order
+            const int I = t / ntn, J = t % ntn, i0 = I * TB, j0 = J * TB;
+            const int rows = min(TB, nS - i0), cols = min(TB, nS - j0);
+            for (int e = tid; e < TB * TB; e += NT) {
+                const int r = e >> 6, c = e & 63;
+                const int pi = r < rows ? a.dpos[i0 + r] : -1, pj = c < cols ? a.dpos[j0 + c] : -1;
+                T0[r * TS + c] = (pi >= 0 && pj >= 0) ? -a.K[(size_t)pi * ldk + pj] : 0.0;
+                if (nr > 0) {
+                    const int pr = r < cols ? a.dpos[j0 + r] : -1;
+                    T1[r * TS + c] = pi >= 0 ? Yb[(size_t)pi * TB + c] : 0.0;
+                    T2[r * TS + c] = pr >= 0 ? Zb[(size_t)pr * TB + c] : 0.0;
+                }
+            }
+            __syncthreads();
+            if (nr > 0) tile_xyt(T0, T1, T2, -1.0, true);
+            st_tile(T0, W + (size_t)i0 * ldk + j0, ldk, rows, cols);
+            __syncthreads();
+        }
+        GSYNC();
+        if (nad > 0) {
+            for (int e = bid * NT + tid; e < nS * TB; e += G * NT) {   // b = K_s[:, A] (0 on added rows)
+                const int j = e >> 6, k = e & 63;
+                Yb[e] = (k < nad && a.dpos[j] >= 0) ? g2(j, a.al[k]) : 0.0;
+            }
+            GSYNC();
+            for (int I = bid; I < ntn; I += G) {           // X_I = sum_J Sigma'_IJ b_J; Q_I = b_I^T X_I
+                const int i0 = I * TB, rows = min(TB, nS - i0);
+                for (int J = 0; J < ntn; ++J) {
+                    const int j0 = J * TB, cols = min(TB, nS - j0);
+                    ld_tile(T0, W + (size_t)i0 * ldk + j0, ldk, rows, cols);
+                    ld_tile(T3, Yb + (size_t)j0 * TB, TB, cols, TB);
+                    __syncthreads();
+                    for (int e = tid; e < TB * TB; e += NT) {
+                        const int k = e >> 6, jj = e & 63;
+                        T1[k * TS + jj] = T3[jj * TS + k];
+                    }
+                    __syncthreads();
+                    tile_xyt(T2, T0, T1, 1.0, J > 0);
+                }
+                st_tile(T2, Zb + (size_t)i0 * TB, TB, rows, TB);
+                ld_tile(T3, Yb + (size_t)i0 * TB, TB, rows, TB);
+                __syncthreads();
+                for (int e = tid; e < TB * TB; e += NT) {
+                    const int k = e >> 6, ii = e & 63;
+                    T1[k * TS + ii] = T3[ii * TS + k];      // b_I^T
+                    T0[k * TS + ii] = T2[ii * TS + k];      // X_I^T
+                }
+                __syncthreads();
+                tile_xyt(T3, T1, T0, 1.0, false);
+                st_tile(T3, a.Lstore + (size_t)I * TB * TB, TB, TB, TB);
+                __syncthreads();
+            }
+            GSYNC();
+            if (bid == 0) {                                 // Sc = K_s[A, A] - sum_I Q_I; its inverse
+                for (int e = tid; e < TB * TB; e += NT) {
+                    const int k = e >> 6, l = e & 63;
+                    double v = 0.0;
+                    if (k < nad && l < nad) {
+                        v = g2(a.al[k], a.al[l]);
+                        for (int I = 0; I < ntn; ++I) v -= a.Lstore[(size_t)I * TB * TB + k * TB + l];
+                    }
+                    T0[k * TS + l] = v;
+                }
+                __syncthreads();
+                inv_spd(nad, Tm2);
+            }
+            GSYNC();
+            for (int t = bid; t < ntn; t += G) {           // P = X Sc^{-1}
+                const int i0 = t * TB, rows = min(TB, nS - i0);
+                ld_tile(T0, Zb + (size_t)i0 * TB, TB, rows, TB);
+                ld_tile(T1, Tm2, TB, TB, TB);
+                __syncthreads();
+                tile_xyt(T2, T0, T1, 1.0, false);
+                st_tile(T2, Yb + (size_t)i0 * TB, TB, rows, TB);
+                __syncthreads();
+            }
+            GSYNC();
+        }
+        for (int t = bid; t < ntn * ntn; t += G) {         // K = -Sigma_new
+            const int I = t / ntn, J = t % ntn, i0 = I * TB, j0 = J * TB;
+            const int rows = min(TB, nS - i0), cols = min(TB, nS - j0);
+            ld_tile(T0, W + (size_t)i0 * ldk + j0, ldk, rows, cols);
+            if (nad > 0) {
+                ld_tile(T1, Yb + (size_t)i0 * TB, TB, rows, TB);
+                ld_tile(T2, Zb + (size_t)j0 * TB, TB, cols, TB);
+            }
+            __syncthreads();
+            if (nad > 0) tile_xyt(T0, T1, T2, 1.0, true);  // Sigma' + P X^T
+            for (int e = tid; e < TB * TB; e += NT) {
+                const int r = e >> 6, c = e & 63;
+                if (r < rows && c < cols) {
+                    const int i = i0 + r, j = j0 + c;
+                    const bool ai = nad > 0 && a.dpos[i] < 0, aj = nad > 0 && a.dpos[j] < 0;
+                    double v = T0[r * TS + c];
+                    if (ai && aj) v = Tm2[find_al(i) * TB + find_al(j)];
+                    else if (ai) v = -Yb[(size_t)j * TB + find_al(i)];
+                    else if (aj) v = -Yb[(size_t)i * TB + find_al(j)];
+                    a.K[(size_t)i * ldk + j] = -v;
+                }
+            }
+            __syncthreads();
+        }
+        GSYNC();
+    } else if (!reuse) {
         const int nt = (nS + TB - 1) / TB;
         const size_t ustride = (size_t)(a.capS + 64) * TB;
         auto Ubuf = [&](int k) { return a.U + (size_t)(k & 1) * ustride; };

@@ -32,6 +32,8 @@ void add_launches(long long n);   // graph replays account their captured launch
 
 // ---- k_elastic.cu
 void launch_set_double(double *p, double v, cudaStream_t st);
+// bits of *flag (or-ed): 1 non-finite, 2 asymmetric, 4 det <= 0 (the caller zeroes it)
+void launch_validate_actuation(const double *A, size_t nmat, int *flag, cudaStream_t st);
 void launch_ingest_actuation(const double *A9, double *A6, int T, cudaStream_t st);
 void elastic_init(int device);
 // clr (nullable): device ints clr[0..1] and clr[4..7] zeroed by the kernel (the iteration's
@@ -147,6 +149,10 @@ struct SchurArgs {
     // swizzle): the large-system trailing updates stream their k chunks with tensor copies.
     // Encoded on the host by schur_args(); read by the kernel from the (grid-constant) parameter.
     alignas(64) CUtensorMap tmap_sh;
+    // low-rank Sigma_s update instead of the full sweep (gather backend; null: never): uinfo =
+    // {update?, |removed|, |added|, n_old}, dpos = old position of each new position (-1 added),
+    // rl / al = removed old / added new positions (ordered, <= 64 each)
+    const int *uinfo, *dpos, *rl, *al;
 };
 // Several systems (sequences) per launch: the grid splits into nsys equal CTA groups, group g
 // running system s[g] with group barriers (the batched variable-n_c Schur step of SURVEY 8(e)).
@@ -207,8 +213,11 @@ void launch_pair_derivs(const unsigned long long *akeys, const int *atype, const
                         double *dist, int *ids, double *dmax, cudaStream_t st);
 void launch_mark_S(const int *ids, const int *acnt, int cap, const int *Wp, const int *Wc, const int *v2q,
                    int *mark, cudaStream_t st);
+// S against the slot's previous S: bit-identical (reuse), or the plan of a low-rank Sigma_s update
+// (dpos / rl / al / uinfo, gather backend, allow_upd) -- see k_contact.cu
 void launch_same_S(const int *qS, const int *nS_ptr, int *qS_prev, int *nS_prev, int *same, int cap,
-                   bool enabled, int *flags, int *reused, cudaStream_t st);
+                   bool enabled, int *flags, int *reused, int *dpos, int *rl, int *al, int *uinfo, int *nupd,
+                   bool allow_upd, int *updated, cudaStream_t st);
 void launch_accum_grad_fx(const int *ids, const int *acnt, int cap, const double *grad, const double *dmax,
                           long long *gsq, cudaStream_t st);
 void launch_accum_bc_fx(const int *ids, const int *acnt, int cap, const int *Wp, const int *Wc, const double *Wv,

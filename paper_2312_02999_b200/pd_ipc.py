@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libpd_ipc.so")
 E_ARG, E_MESH, E_ACTUATION, E_NOT_SPD, E_INTERSECTING, E_NONFINITE, E_CUDA, E_OOM, E_CAPACITY = \
     -1, -2, -3, -4, -5, -6, -7, -8, -9
 FLAG_STALL = 1
-DBG_LARGE_SCHUR, DBG_SORT_BROAD, DBG_TINY_HASH = 1, 2, 4
+DBG_LARGE_SCHUR, DBG_SORT_BROAD, DBG_TINY_HASH, DBG_NO_SIGMA_UPDATE = 1, 2, 4, 8
 
 
 class pd_ipc_mesh(C.Structure):
@@ -41,7 +41,7 @@ class pd_ipc_stats(C.Structure):
                 ("n_S", C.c_int32), ("ls_trials", C.c_int32), ("flags", C.c_int32),
                 ("alpha_max", C.c_double), ("alpha", C.c_double), ("dE", C.c_double),
                 ("min_dist", C.c_double), ("ms", C.c_double * 6), ("sigma_reused", C.c_int32),
-                ("cg_iters", C.c_int32)]
+                ("cg_iters", C.c_int32), ("sigma_updated", C.c_int32)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_ if k != "ms"}

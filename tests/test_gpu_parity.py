@@ -228,13 +228,35 @@ def test_sigma_reuse_is_exact(P):
     A[:, 4] += 0.5 * sc.meta["lip_mask"]
     xs, reused = [], []
     for reuse in (True, False):
-        s = P.Solver(sc, A=A[None], sigma_reuse=reuse)
+        # (the low-rank Sigma_s update, exact only in exact arithmetic, is off here)
+        s = P.Solver(sc, A=A[None], sigma_reuse=reuse, debug_flags=P.DBG_NO_SIGMA_UPDATE)
         st = s.step(n_iters=40)[0]
         xs.append(s.positions())
         reused.append(st["sigma_reused"])
         s.close()
     assert np.array_equal(xs[0], xs[1])
     assert reused[0] > 0 and reused[1] == 0, reused
+
+
+@pytest.mark.parametrize("backend", [2])
+def test_sigma_update_tracks_full_sweep(P, backend):
+    """When S changes by a few vertices, Sigma_s = K_s^{-1} is updated by low-rank steps (removal:
+    Sigma_kk - Sigma_kR Sigma_RR^-1 Sigma_Rk; addition: the bordered inverse with the Schur
+    complement of the added block) instead of the full sweep: the iterates must agree with
+    sweeping afresh to rounding (updates actually taken)."""
+    sc = scenes.face_small(n_frames=2)
+    A = np.tile(np.eye(3).reshape(1, 9), (sc.n_tets, 1))
+    A[:, 4] += 0.5 * sc.meta["lip_mask"]
+    xs, upd = [], []
+    for flags in (0, P.DBG_NO_SIGMA_UPDATE):
+        s = P.Solver(sc, A=A[None], reduced_backend=backend, debug_flags=flags)
+        st = s.step(n_iters=40)[0]
+        xs.append(s.positions())
+        upd.append(st["sigma_updated"])
+        s.close()
+    assert upd[0] > 0 and upd[1] == 0, upd
+    err = np.abs(xs[0] - xs[1]).max()
+    assert err < 1e-9 * sc.bbox_diag(), err
 
 
 def test_candidate_reuse_is_exact(P):

@@ -206,6 +206,37 @@ def test_device_pointer_actuation(P):
     dev.close()
 
 
+@pytest.mark.parametrize("on_device", [False, True])
+def test_invalid_actuation_is_rejected(P, on_device):
+    """pd_ipc_step checks A_next on the device before any sequence ingests it (host and device
+    input alike): a non-finite, asymmetric or det <= 0 matrix in any sequence fails the call with
+    E_ACTUATION and leaves the state untouched."""
+    import torch
+    sc = scenes.slabs_c1()
+    A0 = np.stack([sc.actuation(0)] * 2)
+    s = P.Solver(sc, A=A0, n_seq=2, A_on_device=on_device)
+    s.step(n_iters=2)
+    x0 = [s.positions(b).copy() for b in range(2)]
+    for bad in ("nan", "asym", "det"):
+        A = A0.copy()
+        if bad == "nan":
+            A[1, 7, 4] = np.nan
+        elif bad == "asym":
+            A[1, 7, 1] += 1e-3
+        else:
+            A[1, 7] = np.array([-1.0, 0, 0, 0, 1.0, 0, 0, 0, 1.0])
+        with pytest.raises(P.PdIpcError) as ei:
+            if on_device:
+                Ad = torch.from_numpy(A).cuda()
+                s.step(A_device_ptr=Ad.data_ptr(), n_iters=1)
+            else:
+                s.step(A_next=A, n_iters=1)
+        assert ei.value.code == P.E_ACTUATION, (bad, str(ei.value))
+        for b in range(2):
+            assert np.array_equal(s.positions(b), x0[b])
+    s.close()
+
+
 # ------------------------------------------------------------------ sort broad phase -------
 @pytest.mark.parametrize("flags", ["sort", "tiny_hash"])
 def test_sort_broad_phase(P, flags):
