@@ -749,7 +749,7 @@ static void enqueue_contact(pd_ipc *h, int b, int b0, int nb, int it) {
         // accumulation of the lower blocks (recorded in the block list), then the listed blocks
         // converted (with their mirrors) and their accumulators re-zeroed
         const int ldb = 3 * h->capS;
-        launch_bc_clear(SB.Bc.p, ldb, h->capS, SB.tlist.p, SB.tcnt.p, st);
+        launch_bc_clear(SB.Bc.p, ldb, h->capS, SB.tlist.p, SB.tcnt.p, SB.tbits.p, st);
         CK(dev_zero(SB.tcnt.p, sizeof(int), st));
         launch_accum_bc_fx(h->ids.p, acnt, cap, h->Wp.p, h->Wc.p, h->Wv.p, h->v2q.p, SB.spos.p, h->Hp.p, dmax,
                            SB.Bh.p, SB.Bl.p, ldb, h->capS, SB.tbits.p, SB.tlist.p, SB.tcnt.p, st);
@@ -797,6 +797,7 @@ static void enqueue_schur(pd_ipc *h, int c0, int c1, int b0, int nb, int it) {
                                       (h->opt.debug_flags & PD_IPC_DBG_LARGE_SCHUR) ? 1 : 0,
                                       h->gather ? kSchurGather : kSchurPanel, h->G2.p, h->n2, h->rpos.p,
                                       h->gather ? h->Yel(b) : nullptr);
+            args[b - c0].tbits = SB.tbits.p;   // B-check block bits: t = B u over the nonzero blocks
             if (h->gather) {                // the low-rank Sigma_s update plan of k_same_S
                 args[b - c0].uinfo = SB.uinfo.p;
                 args[b - c0].dpos = SB.dpos.p;

@@ -916,6 +916,11 @@ __global__ void k_accum_bc_fx(const int *__restrict__ ids, const int *__restrict
                     const unsigned bit = 1u << (key & 31);
                     if (!(__ldcg(tbits + (key >> 5)) & bit) && !(atomicOr(tbits + (key >> 5), bit) & bit))
                         tlist[atomicAdd(tcnt, 1)] = (int)key;
+                    if (sidx[qa] != sidx[qb]) {   // the mirror block's bit (row scans of t = B u)
+                        const unsigned mk = (unsigned)sidx[qb] * (unsigned)capS + (unsigned)sidx[qa];
+                        const unsigned mb = 1u << (mk & 31);
+                        if (!(__ldcg(tbits + (mk >> 5)) & mb)) atomicOr(tbits + (mk >> 5), mb);
+                    }
                 }
                 const double w = Wv[na] * Wv[nb];
                 const size_t o = (size_t)(3 * sidx[qa]) * ldb + 3 * sidx[qb];
@@ -932,13 +937,20 @@ __global__ void k_accum_bc_fx(const int *__restrict__ ids, const int *__restrict
 // in the same pass, so the accumulators stay zero between uses.  The dense double B-check is zero
 // outside the listed blocks: each use first clears the blocks the previous use wrote.
 __global__ void k_bc_clear(double *__restrict__ Bc, int ld, int capS, const int *__restrict__ tlist,
-                           const int *__restrict__ tcnt) {
+                           const int *__restrict__ tcnt, unsigned *__restrict__ tbits) {
     const int n = *tcnt;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 9 * n; i += gridDim.x * blockDim.x) {
         const int key = tlist[i / 9], e = i % 9, a = key / capS, b = key % capS;
         const int r = 3 * a + e / 3, c = 3 * b + e % 3;
         Bc[(size_t)r * ld + c] = 0.0;
         if (a != b) Bc[(size_t)c * ld + r] = 0.0;
+        if (e == 0) {       // the block's bits (kept through the Schur step for its row scans)
+            atomicAnd(tbits + ((unsigned)key >> 5), ~(1u << ((unsigned)key & 31)));
+            if (a != b) {
+                const unsigned mk = (unsigned)b * (unsigned)capS + (unsigned)a;
+                atomicAnd(tbits + (mk >> 5), ~(1u << (mk & 31)));
+            }
+        }
     }
 }
 __global__ void k_bc_convert(long long *__restrict__ Bh, long long *__restrict__ Bl, double *__restrict__ Bc, int ld,
@@ -955,7 +967,6 @@ __global__ void k_bc_convert(long long *__restrict__ Bh, long long *__restrict__
         Bl[o] = 0;
         Bc[o] = v;
         if (a != b) Bc[(size_t)c * ld + r] = v;
-        if (e == 0) atomicAnd(tbits + ((unsigned)key >> 5), ~(1u << ((unsigned)key & 31)));
     }
 }
 __global__ void k_grad_pullback_fx(const double4 *__restrict__ g_el, const int *__restrict__ WTp,
@@ -992,8 +1003,9 @@ void launch_accum_bc_fx(const int *ids, const int *acnt, int cap, const int *Wp,
                                                                            Hp, dmax, Bq, Bl, ldb, capS, tbits,
                                                                            tlist, tcnt);
 }
-void launch_bc_clear(double *Bc, int ld, int capS, const int *tlist, const int *tcnt, cudaStream_t st) {
-    PDI_LAUNCH(k_bc_clear, 148 * 4, 256, 0, st)(Bc, ld, capS, tlist, tcnt);
+void launch_bc_clear(double *Bc, int ld, int capS, const int *tlist, const int *tcnt, unsigned *tbits,
+                     cudaStream_t st) {
+    PDI_LAUNCH(k_bc_clear, 148 * 4, 256, 0, st)(Bc, ld, capS, tlist, tcnt, tbits);
 }
 void launch_bc_convert(long long *Bh, long long *Bl, double *Bc, int ld, int capS, const int *tlist, const int *tcnt,
                        unsigned *tbits, const double *dmax, const int *acnt, cudaStream_t st) {

@@ -1107,15 +1107,15 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
         double *srow = a.Sh + (size_t)r * a.ldh;
         const double *krow = a.K + (size_t)(r / 3) * a.ldk;
         const int r3 = r % 3;
-        for (int c0 = 0; c0 <= r; c0 += 128) {           // 4 loads per lane in flight
-            double v[4];
+        for (int c0 = 0; c0 <= r; c0 += 256) {           // 8 loads per lane in flight
+            double v[8];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < 8; ++u) {
                 const int c = c0 + lane + 32 * u;
                 v[u] = c <= r ? brow[c] - (c % 3 == r3 ? krow[c / 3] : 0.0) : 0.0;
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < 8; ++u) {
                 const int c = c0 + lane + 32 * u;
                 if (c <= r) srow[c] = v[u];
             }
@@ -1432,11 +1432,13 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
             // single-k update ~ 1.3, the diagonal factor ~ 4 (serial), a barrier ~ 0.3 (serial)
             double wp = 0.0, ws = 0.0;
             for (int j = c0t; j < c1t; ++j) wp += (double)ppw * (nt - j);
+            const int mid = c1t - c0t >= 6 && nt - c1t >= a.split_min ? c0t + (c1t - c0t + 1) / 2 : c1t;
             for (int k = c0t; k < c1t; ++k) {
                 wp += 1.3 * (nt - k - 1);
-                for (int j = k + 1; j < c1t; ++j) wp += 1.3 * (nt - j);
+                for (int j = k + 1; j < (k < mid ? mid : c1t); ++j) wp += 1.3 * (nt - j);
                 ws += 4.0 + 3 * 0.3;
             }
+            for (int j = mid; j < c1t; ++j) wp += (double)(mid - c0t) * (nt - j);
             const double wu = 0.25 * a.wu_coef * ppw * rr * (rr + 1) / 2.0;
             double best = 1e300;
             for (int x = 1; x < G; ++x) {
@@ -1478,6 +1480,10 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
             };
             if (bid == 0) factor_diag(c0t, false);
             group_bar(ctr, ++nbar * npg);
+            // two halves (panels of >= 6 columns): the first half's intra-panel updates stay in
+            // the first half; then ONE update of the second half with all first-half columns
+            // (k = 64 x half width: the long, efficient update) and the second half
+            const int mid = c1t - c0t >= 6 && nt - c1t >= a.split_min ? c0t + (c1t - c0t + 1) / 2 : c1t;
             for (int k = c0t; k < c1t; ++k) {
                 const int kc0 = k * TB, kn = min(TB, ma - kc0);
                 // per-column detail of panels 2 and 30 (PDIPC_TRACE): diagonal factored, TRSM
@@ -1495,11 +1501,22 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
                 }
                 group_bar(ctr, ++nbar * npg);
                 if (pslot >= 0) a.prof[pslot + 1] = gtimer_s();
-                if (k + 1 < c1t) {          // A_ij -= L_ik L_jk^T, k < j < c1t, i >= j
+                const int kend = k < mid ? mid : c1t;
+                if (k + 1 == mid && mid < c1t) {   // second half += first half (k in [c0t, mid))
+                    const int tot = pairs_in(mid, c1t);
+                    for (int b = bid; b < tot; b += npg) {
+                        int ti, tj;
+                        pair_of(b, mid, ti, tj);
+                        update_pair(ti, tj, c0t, mid);
+                    }
+                    group_bar(ctr, ++nbar * npg);
+                    if (bid == 0) factor_diag(mid, false);
+                    group_bar(ctr, ++nbar * npg);
+                } else if (k + 1 < kend) {  // A_ij -= L_ik L_jk^T, k < j < kend, i >= j
                     // pair 0 is (k+1, k+2) x (k+1): its diagonal tile goes to CTA 0 (look-ahead),
                     // its lower tile (k+2, k+1) to the last CTA; pairs 1.. to CTAs 1.. (all
                     // CTAs when npg == 1)
-                    const int tot = pairs_in(k + 1, c1t);
+                    const int tot = pairs_in(k + 1, kend);
                     if (bid == 0) factor_diag(k + 1, true);
                     if (bid == npg - 1 && k + 2 < nt) update_tile(k + 2, k + 1, k, k + 1);
                     const int w0 = npg > 1 ? 1 : 0, nw = npg > 1 ? npg - 1 : 1;
@@ -1705,17 +1722,54 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
     if (a.prof && bid == 0 && tid == 0) { a.prof[1000 + 5] = np; a.prof[np < 1000 ? np++ : np] = gtimer_s(); }   // phase marker (PDIPC_TRACE)
     // ------------------------------------------------ P5: t = B u ; Z = w + V t = w_el + V (gc + t)
     // (w = L^{-1} Pi g = w_el + V gc since the contact gradient is supported on S)
-    for (int row = bid * (NT / 32) + wid; row < m; row += G * (NT / 32)) {
-        double acc = 0.0;
-        for (int c = lane; c < m; c += 32) acc += a.Bc[(size_t)row * a.ldb + c] * a.u[c];
-        acc = warp_sum(acc);
-        if (lane == 0) a.t[row] = acc + a.gc[row];
+    if (a.tbits) {
+        // B-check is block-sparse: a warp per vertex row ab scans the row's block bits (lane per
+        // 32-bit word, bits in increasing order) and multiplies only the nonzero 3 x 3 blocks;
+        // the lane partials are summed by the fixed xor tree (deterministic)
+        for (int ab = bid * (NT / 32) + wid; ab < nS; ab += G * (NT / 32)) {
+            const unsigned long long k0 = (unsigned long long)ab * a.capS, k1 = k0 + nS;
+            const unsigned long long w0 = k0 >> 5, w1 = (k1 - 1) >> 5;
+            double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+            const double *r0 = a.Bc + (size_t)(3 * ab) * a.ldb;
+            for (unsigned long long w = w0 + lane; w <= w1; w += 32) {
+                unsigned bits = a.tbits[w];
+                if (w == w0) bits &= ~0u << (unsigned)(k0 & 31);
+                if (w == w1 && (k1 & 31)) bits &= (1u << (unsigned)(k1 & 31)) - 1u;
+                while (bits) {
+                    const int bp = __ffs(bits) - 1;
+                    bits &= bits - 1u;
+                    const int b3 = 3 * (int)(w * 32 + bp - k0);
+                    const double u0 = a.u[b3], u1 = a.u[b3 + 1], u2 = a.u[b3 + 2];
+                    acc0 += r0[b3] * u0 + r0[b3 + 1] * u1 + r0[b3 + 2] * u2;
+                    acc1 += r0[a.ldb + b3] * u0 + r0[a.ldb + b3 + 1] * u1 + r0[a.ldb + b3 + 2] * u2;
+                    acc2 += r0[2 * (size_t)a.ldb + b3] * u0 + r0[2 * (size_t)a.ldb + b3 + 1] * u1 +
+                            r0[2 * (size_t)a.ldb + b3 + 2] * u2;
+                }
+            }
+            acc0 = warp_sum(acc0);
+            acc1 = warp_sum(acc1);
+            acc2 = warp_sum(acc2);
+            if (lane == 0) {
+                a.t[3 * ab + 0] = acc0 + a.gc[3 * ab + 0];
+                a.t[3 * ab + 1] = acc1 + a.gc[3 * ab + 1];
+                a.t[3 * ab + 2] = acc2 + a.gc[3 * ab + 2];
+            }
+        }
+    } else {
+        for (int row = bid * (NT / 32) + wid; row < m; row += G * (NT / 32)) {
+            double acc = 0.0;
+            for (int c = lane; c < m; c += 32) acc += a.Bc[(size_t)row * a.ldb + c] * a.u[c];
+            acc = warp_sum(acc);
+            if (lane == 0) a.t[row] = acc + a.gc[row];
+        }
     }
+    if (a.prof && bid == 0 && tid == 0) { a.prof[1000 + 7] = np; a.prof[np < 1000 ? np++ : np] = gtimer_s(); }
     if (a.mode == kSchurGather) {
         // sparse right-hand side E_S (gc + t) of the caller's solve: zero, then the rows of S
         for (size_t e = (size_t)bid * NT + tid; e < (size_t)4 * a.nf; e += (size_t)G * NT) a.Z[e] = 0.0;
         GSYNC();
         for (int e = bid * NT + tid; e < m; e += G * NT) a.Z[(size_t)a.qS[e / 3] * 4 + e % 3] = a.t[e];
+        if (a.prof && bid == 0 && tid == 0) { a.prof[1000 + 6] = np; a.prof[np < 1000 ? np++ : np] = gtimer_s(); }
         return;
     }
     GSYNC();
@@ -1985,6 +2039,8 @@ SchurArgs schur_args(const DevFactor &F, const double *V, int ldv, const double 
     static const int kpw0 = [] { const char *e = std::getenv("PDIPC_SCHUR_KPW0"); return e ? std::max(1, std::atoi(e)) : 10; }();
     static const int ktail = [] { const char *e = std::getenv("PDIPC_SCHUR_KTAIL"); return e ? std::atoi(e) : 0; }();
     a.kpw0 = kpw0;
+    static const int split_min = [] { const char *e = std::getenv("PDIPC_SCHUR_SPLIT"); return e ? std::atoi(e) : 80; }();
+    a.split_min = split_min;
     a.ktail = ktail;
     if (g_encode && Sh && ldh > 0 && capS > 0) {
         const cuuint64_t dims[2] = {(cuuint64_t)ldh, (cuuint64_t)(3 * capS + 1)};

@@ -142,6 +142,7 @@ struct SchurArgs {
                                 // phase-1 launch does everything, the others return at once)
     unsigned *gbar;             // barrier counter of the CTA group that runs this system
     int kpw0, ktail;            // first-panel width; tail narrowing divisor (0: off)
+    int split_min;              // panels split in two halves while >= split_min tile columns remain right of them
     int kpw;                    // large-system P3 panel width in 64-tiles (PDIPC_SCHUR_KPW, default 10)
     double wu_coef;             // large-system P3 split: work of a trailing 128x64 k=256 update (units of
                                 // a 64^3 tile product; PDIPC_SCHUR_WU, default 3.5)
@@ -153,6 +154,9 @@ struct SchurArgs {
     // {update?, |removed|, |added|, n_old}, dpos = old position of each new position (-1 added),
     // rl / al = removed old / added new positions (ordered, <= 64 each)
     const int *uinfo, *dpos, *rl, *al;
+    // bits of the 3 x 3 blocks of B-check that are nonzero this iteration (both triangles; row a
+    // at bits [a capS, a capS + capS)): t = B u by row scans (null: dense rows)
+    const unsigned *tbits;
 };
 // Several systems (sequences) per launch: the grid splits into nsys equal CTA groups, group g
 // running system s[g] with group barriers (the batched variable-n_c Schur step of SURVEY 8(e)).
@@ -226,7 +230,8 @@ void launch_accum_bc_fx(const int *ids, const int *acnt, int cap, const int *Wp,
                         cudaStream_t st);
 // B-check blocks: clear the previous use's blocks in the dense double B-check; convert the listed
 // fixed-point blocks (and their mirrors), re-zeroing the accumulators and the block bits
-void launch_bc_clear(double *Bc, int ld, int capS, const int *tlist, const int *tcnt, cudaStream_t st);
+void launch_bc_clear(double *Bc, int ld, int capS, const int *tlist, const int *tcnt, unsigned *tbits,
+                     cudaStream_t st);
 void launch_bc_convert(long long *Bh, long long *Bl, double *Bc, int ld, int capS, const int *tlist, const int *tcnt,
                        unsigned *tbits, const double *dmax, const int *acnt, cudaStream_t st);
 void launch_grad_pullback_fx(const double4 *g_el, const int *WTp, const int *WTr, const double *WTv,

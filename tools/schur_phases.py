@@ -28,14 +28,17 @@ for i in range(len(data) // rec):
     nS = struct.unpack_from("i", data, i * rec)[0]
     pr = np.frombuffer(data, dtype=np.uint64, count=1024, offset=i * rec + 4).astype(np.int64)
     mk = [0] + [int(pr[1000 + k]) for k in range(1, 6)]
-    n_end = max(j for j in range(1000) if pr[j] != 0)
-    ts = [pr[mk[k]] for k in range(6)] + [pr[n_end]]
-    rows.append((nS, [(ts[k + 1] - ts[k]) / 1e3 for k in range(6)]))
-for nS, ph in rows[-12:]:
-    print(f"n_c {nS:5d}  " + "  ".join(f"P{k} {v:8.1f}" for k, v in enumerate(ph)) + f"  total {sum(ph):8.1f} us")
+    # end of P5: the stamp after the CTA-0 stamp of 'CTA 0 done with t = B u' (1007) when the
+    # gather backend's end stamp (1006) is absent
+    e6 = int(pr[1006]) if pr[1006] else int(pr[1007])
+    ts = [pr[mk[k]] for k in range(6)] + [pr[e6]]
+    rows.append((nS, [(ts[k + 1] - ts[k]) / 1e3 for k in range(6)], (pr[int(pr[1007])] - pr[mk[5]]) / 1e3))
+for nS, ph, tbu in rows[-12:]:
+    print(f"n_c {nS:5d}  " + "  ".join(f"P{k} {v:8.1f}" for k, v in enumerate(ph)) +
+          f"  total {sum(ph):8.1f} us  (t = B u: {tbu:.1f})")
 # large-system P3 look-ahead detail of the last traced iteration: per panel iteration q, the
 # panel group's time (its update of panel q + the panel factorisation) and the update group's
-nS, _ = rows[-1]
+nS, _, _ = rows[-1]
 i = len(data) // rec - 1
 pr = np.frombuffer(data, dtype=np.uint64, count=1024, offset=i * rec + 4).astype(np.int64)
 m3 = int(pr[1003])
