@@ -1102,7 +1102,44 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
     // ------------------------------------------------ P2: augmented Sigma-hat (Sigma_s = -K)
     // lower triangle, a warp per row (tile-0 rows: factored by CTA 0 when early0); the Sigma_s
     // entries of row r sit at columns c = r mod 3 + 3 j
-    for (int r = (early0 ? TB : 0) + pb * (NT / 32) + wid; pb >= 0 && r < m; r += pG * (NT / 32)) {
+    // With the block bits of B-check (a.tbits), the row is written from Sigma_s alone (writes
+    // only) and the nonzero 3 x 3 blocks of B-check (b <= a in vertex row a = r / 3) are added
+    // after: fl(-k + B) = fl(B - k), bit-identical to reading the dense row.
+    for (int r = (early0 ? TB : 0) + pb * (NT / 32) + wid; a.tbits && pb >= 0 && r < m; r += pG * (NT / 32)) {
+        const double *brow = a.Bc + (size_t)r * a.ldb;
+        double *srow = a.Sh + (size_t)r * a.ldh;
+        const int av = r / 3, r3 = r % 3;
+        const double *krow = a.K + (size_t)av * a.ldk;
+        for (int c0 = 0; c0 <= r; c0 += 512) {           // 16 loads per lane in flight
+            double v[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int c = c0 + lane + 32 * u;
+                v[u] = (c <= r && c % 3 == r3) ? -krow[c / 3] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int c = c0 + lane + 32 * u;
+                if (c <= r) srow[c] = v[u];
+            }
+        }
+        __syncwarp();
+        const unsigned long long k0 = (unsigned long long)av * a.capS, k1 = k0 + av + 1;
+        for (unsigned long long w = (k0 >> 5) + lane; w <= ((k1 - 1) >> 5); w += 32) {
+            unsigned bits = a.tbits[w];
+            if (w == (k0 >> 5)) bits &= ~0u << (unsigned)(k0 & 31);
+            if (w == ((k1 - 1) >> 5) && (k1 & 31)) bits &= (1u << (unsigned)(k1 & 31)) - 1u;
+            while (bits) {
+                const int bp = __ffs(bits) - 1;
+                bits &= bits - 1u;
+                const int c3 = 3 * (int)(w * 32 + bp - k0);
+#pragma unroll
+                for (int j = 0; j < 3; ++j)
+                    if (c3 + j <= r) srow[c3 + j] += brow[c3 + j];
+            }
+        }
+    }
+    for (int r = (early0 ? TB : 0) + pb * (NT / 32) + wid; !a.tbits && pb >= 0 && r < m; r += pG * (NT / 32)) {
         const double *brow = a.Bc + (size_t)r * a.ldb;
         double *srow = a.Sh + (size_t)r * a.ldh;
         const double *krow = a.K + (size_t)(r / 3) * a.ldk;
@@ -1121,6 +1158,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
             }
         }
     }
+    if (a.prof && bid == 0 && tid == 0) a.prof[996] = gtimer_s();   // CTA 0: assembly rows done
     // b = (Sigma_s (x) I3) y_S with y_S = y_S^el - (K (x) I3) gc, i.e. b = Sigma_s y_S^el - gc
     // (K holds -Sigma_s in both triangles: the sweep mirrors its final values; a warp reads a row
     // once for the three components)
@@ -1142,6 +1180,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
             a.Sh[(size_t)m * a.ldh + 3 * ai + 2] = acc2 - a.gc[3 * ai + 2];
         }
     }
+    if (a.prof && bid == 0 && tid == 0) a.prof[995] = gtimer_s();   // CTA 0: b rows done
     if (bid == 0 && tid == 0) a.Sh[(size_t)m * a.ldh + m] = 1.0;
     if (bid == 0)
         for (int e = tid; e < kMaxPanels; e += NT) a.bar[e] = 0u;   // P3 group-barrier counters

@@ -33,6 +33,8 @@ for i in range(len(data) // rec):
     e6 = int(pr[1006]) if pr[1006] else int(pr[1007])
     ts = [pr[mk[k]] for k in range(6)] + [pr[e6]]
     rows.append((nS, [(ts[k + 1] - ts[k]) / 1e3 for k in range(6)], (pr[int(pr[1007])] - pr[mk[5]]) / 1e3))
+    if pr[996] and pr[995]:
+        print(f"  (n_c {nS}: P2 CTA 0 assembly rows {(pr[996] - pr[mk[2]]) / 1e3:.1f} us, b rows {(pr[995] - pr[996]) / 1e3:.1f} us)")
 for nS, ph, tbu in rows[-12:]:
     print(f"n_c {nS:5d}  " + "  ".join(f"P{k} {v:8.1f}" for k, v in enumerate(ph)) +
           f"  total {sum(ph):8.1f} us  (t = B u: {tbu:.1f})")
