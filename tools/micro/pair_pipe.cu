@@ -607,6 +607,128 @@ __global__ void __launch_bounds__(NT, 1) k_tma(const __grid_constant__ CUtensorM
     CYC1
 }
 
+template <int NSTG, int PREF>
+__global__ void __launch_bounds__(NT, 1) k_tma_c(const __grid_constant__ CUtensorMap tmap, double *Sh, int ldh, int ma,
+                                               int P, int nrow_pairs) {
+    CYC0
+    extern __shared__ unsigned char smraw[];
+    const unsigned base = (su32(smraw) + 1023u) & ~1023u;
+    const unsigned bars = base + NSTG * TS_STAGE_B + 65536;  // full[S], empty[S], cfull, cempty
+    const unsigned cbase = base + NSTG * TS_STAGE_B;                  // C staging, 128 x 64 swizzled
+    const unsigned cfull = bars + 16 * NSTG, cempty = cfull + 8;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, gr = lane >> 2, gc = lane & 3;
+    constexpr int nch = 4 * TB / KC;
+    const int G = P * nch;
+    if (tid == 0) {
+        for (int i = 0; i < NSTG; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" :: "r"(bars + 8 * i));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;\n" :: "r"(bars + 8 * (NSTG + i)));
+        }
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" :: "r"(cfull));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;\n" :: "r"(cempty));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    auto block_rc = [&](int p, int &r0, int &c0) {
+        const int b = blockIdx.x * P + p;
+        r0 = (4 + 2 * (b % nrow_pairs)) * TB;
+        c0 = (4 + (b / nrow_pairs) % ((ma / TB) - 4)) * TB;
+    };
+    int gi = 0;                                   // next chunk to issue (thread 0)
+    auto produce = [&](int upto) {
+        for (; gi < upto && gi < G; ++gi) {
+            const int st = gi % NSTG;
+            if (gi >= NSTG) mb_wait(bars + 8 * (NSTG + st), ((gi / NSTG) - 1) & 1);
+            int r0, c0;
+            block_rc(gi / nch, r0, c0);
+            const int kc = (gi % nch) * KC;
+            const unsigned fb = bars + 8 * st, sb = base + st * TS_STAGE_B;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" :: "r"(fb), "r"(TS_STAGE_B) : "memory");
+            const unsigned long long tm = reinterpret_cast<unsigned long long>(&tmap);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+                    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+                                 :: "r"(sb + h * 16384 + j * 8192), "l"(tm), "r"(kc + 16 * h), "r"(r0 + 64 * j), "r"(fb) : "memory");
+                asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+                             :: "r"(sb + 32768 + h * 8192), "l"(tm), "r"(kc + 16 * h), "r"(c0), "r"(fb) : "memory");
+            }
+        }
+    };
+    auto produce_c = [&](int p) {                 // thread 0: C of block p into the staging buffer
+        int r0, c0;
+        block_rc(p, r0, c0);
+        const unsigned long long tm = reinterpret_cast<unsigned long long>(&tmap);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" :: "r"(cfull), "r"(65536) : "memory");
+        for (int g4 = 0; g4 < 4; ++g4)
+            for (int j = 0; j < 2; ++j)
+                asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+                             :: "r"(cbase + g4 * 16384 + j * 8192), "l"(tm), "r"(c0 + 16 * g4), "r"(r0 + 64 * j), "r"(cfull) : "memory");
+    };
+    if (tid == 0) { produce_c(0); produce(PREF); }
+    unsigned sw[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) sw[q] = ((((2 * q) + (gc >> 1)) ^ gr) << 4) + ((gc & 1) << 3);
+    int g = 0;
+    for (int p = 0; p < P; ++p) {
+        int r0, c0;
+        block_rc(p, r0, c0);
+        const int rows = min(2 * TB, ma - r0), cols = min(TB, ma - c0);
+        double acc[2][8][2];
+        mb_wait(cfull, p & 1);
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int nb = 0; nb < 8; ++nb) {
+                const int r = 16 * wid + 8 * h + gr;
+                const unsigned ad = cbase + (nb >> 1) * 16384 + r * 128 + ((((nb & 1) * 4 + gc) ^ gr) << 4);
+                double v0, v1;
+                asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v0), "=d"(v1) : "r"(ad));
+                acc[h][nb][0] = -v0;
+                acc[h][nb][1] = -v1;
+            }
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" :: "r"(cempty) : "memory");
+        if (tid == 0 && p + 1 < P) {
+            mb_wait(cempty, p & 1);
+            produce_c(p + 1);
+        }
+        for (int ch = 0; ch < nch; ++ch, ++g) {
+            if (tid == 0) produce(g + PREF);
+            const int st = g % NSTG;
+            mb_wait(bars + 8 * st, (g / NSTG) & 1);
+            const unsigned sb = base + st * TS_STAGE_B;
+            const unsigned xa = sb + (16 * wid + gr) * 128, yb = sb + 32768 + gr * 128;
+#pragma unroll
+            for (int k4 = 0; k4 < KC / 4; ++k4) {
+                const unsigned hx = (k4 >> 2) * 16384 + sw[k4 & 3], hy = (k4 >> 2) * 8192 + sw[k4 & 3];
+                double a0, a1;
+                asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(a0) : "r"(xa + hx));
+                asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(a1) : "r"(xa + 1024 + hx));
+#pragma unroll
+                for (int nb = 0; nb < 8; ++nb) {
+                    double bv;
+                    asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(bv) : "r"(yb + nb * 1024 + hy));
+                    dmma(acc[0][nb][0], acc[0][nb][1], a0, bv);
+                    dmma(acc[1][nb][0], acc[1][nb][1], a1, bv);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" :: "r"(bars + 8 * (NSTG + st)) : "memory");
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int nb = 0; nb < 8; ++nb) {
+                const int r = 16 * wid + 8 * h + gr, c = 8 * nb + 2 * gc;
+                if (r < rows && c < cols) Sh[(size_t)(r0 + r) * ldh + c0 + c] = -acc[h][nb][0];
+                if (r < rows && c + 1 < cols) Sh[(size_t)(r0 + r) * ldh + c0 + c + 1] = -acc[h][nb][1];
+            }
+    }
+    CYC1
+}
+
 template <int PREF>
 void run_tma(double *Sh, int ldh, int ma, int nsm, double clk_ghz) {
     static PFN_cuTensorMapEncodeTiled enc = nullptr;
@@ -643,6 +765,42 @@ void run_tma(double *Sh, int ldh, int ma, int nsm, double clk_ghz) {
            err == cudaSuccess ? "" : cudaGetErrorString(err));
 }
 
+template <int NSTG, int PREF>
+void run_tma_c(double *Sh, int ldh, int ma, int nsm, double clk_ghz) {
+    static PFN_cuTensorMapEncodeTiled enc = nullptr;
+    if (!enc) {
+        cudaDriverEntryPointQueryResult q;
+        cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void **)&enc, cudaEnableDefault, &q);
+    }
+    CUtensorMap tm;
+    cuuint64_t dims[2] = {(cuuint64_t)ldh, (cuuint64_t)ma};
+    cuuint64_t strides[1] = {(cuuint64_t)ldh * 8};
+    cuuint32_t box[2] = {16, 64}, es[2] = {1, 1};
+    CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, Sh, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) { printf("encode failed %d\n", (int)r); return; }
+    cudaFuncSetAttribute(k_tma_c<NSTG, PREF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (NSTG * TS_STAGE_B + 65536 + 1024 + 64));
+    const int P = 24, nrow_pairs = (ma / TB - 4) / 2;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int it = 0; it < 4; ++it) {
+        cudaEventRecord(e0);
+        k_tma_c<NSTG, PREF><<<nsm, NT, (NSTG * TS_STAGE_B + 65536 + 1024 + 64)>>>(tm, Sh, ldh, ma, P, nrow_pairs);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms < best) best = ms;
+    }
+    cudaError_t err = cudaGetLastError();
+    const double us = best * 1e3 / P;
+    const double ideal_us = 2.0 * 128 * 64 * 256 / (128.0 * clk_ghz * 1e3);
+    printf("TMA %d-stage + C staging, %d chunks ahead: %.2f us per block, %.1f %% of the DMMA rate %s\n", NSTG, PREF, us, 100.0 * ideal_us / us,
+           err == cudaSuccess ? "" : cudaGetErrorString(err));
+}
+
 int main() {
     int nsm, clk_khz;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
@@ -662,5 +820,6 @@ int main() {
     run<7>(Sh, ldh, ma, nsm, out, ghz);
     run_tma<2>(Sh, ldh, ma, nsm, ghz);
     run_tma<3>(Sh, ldh, ma, nsm, ghz);
+    run_tma_c<3, 2>(Sh, ldh, ma, nsm, ghz);
     return 0;
 }
