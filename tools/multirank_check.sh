@@ -10,7 +10,3 @@ b = json.loads(open("gpurun_out/p2.json").read().strip().splitlines()[-1])
 print("P=1 checksum", a["checksum"], "P=2 checksum", b["checksum"], "equal", a["checksum"] == b["checksum"])
 print("P=2 per-rank ms", b["per_rank_ms"], "sequences_per_gpu", b["config"]["sequences_per_gpu"])
 PY
-timeout 1200 python -m pytest tests/test_gpu_parity_paths.py -k "pcg or convergence" -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu_r02h.log 2>&1
-tail -3 gpurun_out/pytest_gpu_r02h.log
-timeout 1500 python tools/pcg_kappa.py C2 C3 > gpurun_out/pcg_kappa.txt 2>&1
-cat gpurun_out/pcg_kappa.txt
