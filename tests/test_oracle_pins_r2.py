@@ -290,3 +290,39 @@ def test_swept_pairs_equal_all_pairs_enumeration(c1_contact):
             b = np.stack(bf[kind], 1)
             b = b[np.lexsort((b[:, 1], b[:, 0]))]
             assert a.shape[0] > 0 and np.array_equal(a, b), kind
+
+
+# ------------------------------------------------------------------ low-rank Sigma_s update --
+@pytest.mark.parametrize("n_rm, n_add", [(0, 5), (7, 0), (4, 9), (64, 64)])
+def test_sigma_update_identities(n_rm, n_add):
+    """The two identities the CUDA path's low-rank update of Sigma_s = K_s^-1 rests on (DESIGN.md
+    5.3; exact in exact arithmetic), checked against direct inverses of a random SPD K on the
+    union of old and new vertex sets: removal Sigma' = Sigma_kk - Sigma_kR Sigma_RR^-1 Sigma_Rk;
+    addition with b = K[keep, A], X = Sigma' b, Sc = K[A, A] - b^T X:
+    Sigma_new = [[Sigma' + X Sc^-1 X^T, -X Sc^-1], [-Sc^-1 X^T, Sc^-1]]."""
+    rng = np.random.default_rng(7 + n_rm + 100 * n_add)
+    n_keep = 150
+    N = n_keep + n_rm + n_add
+    Q = rng.standard_normal((N, N))
+    K = Q @ Q.T / N + 0.5 * np.eye(N)
+    perm = rng.permutation(N)
+    keep, rem, add = perm[:n_keep], perm[n_keep:n_keep + n_rm], perm[n_keep + n_rm:]
+    old = np.concatenate([keep, rem])
+    Sig_old = np.linalg.inv(K[np.ix_(old, old)])
+    k, r = np.arange(n_keep), np.arange(n_keep, n_keep + n_rm)
+    Sig_p = Sig_old[np.ix_(k, k)]
+    if n_rm:
+        Sig_p = Sig_p - Sig_old[np.ix_(k, r)] @ np.linalg.solve(Sig_old[np.ix_(r, r)], Sig_old[np.ix_(r, k)])
+    assert np.allclose(Sig_p, np.linalg.inv(K[np.ix_(keep, keep)]), rtol=1e-10, atol=1e-12)
+    new = np.concatenate([keep, add])
+    if n_add:
+        b = K[np.ix_(keep, add)]
+        X = Sig_p @ b
+        Sc = K[np.ix_(add, add)] - b.T @ X
+        Sci = np.linalg.inv(Sc)
+        top = np.hstack([Sig_p + X @ Sci @ X.T, -X @ Sci])
+        bot = np.hstack([-Sci @ X.T, Sci])
+        Sig_new = np.vstack([top, bot])
+    else:
+        Sig_new = Sig_p
+    assert np.allclose(Sig_new, np.linalg.inv(K[np.ix_(new, new)]), rtol=1e-10, atol=1e-12)
