@@ -1527,8 +1527,8 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
                 const int kc0 = k * TB, kn = min(TB, ma - kc0);
                 // per-column detail of panels 2 and 30 (PDIPC_TRACE): diagonal factored, TRSM
                 // done, intra-panel update done
-                const int pslot = (q == 2 || q == 30) && a.prof && bid == 0 && tid == 0
-                                      ? 900 + (q == 30 ? 16 : 0) + 3 * (k - c0t) : -1;
+                const int pslot = (q == 0 || q == 12) && a.prof && bid == 0 && tid == 0 && k - c0t < 10
+                                      ? 900 + (q == 12 ? 40 : 0) + 3 * (k - c0t) : -1;
                 if (pslot >= 0) a.prof[pslot] = gtimer_s();
                 for (int b = bid; b < nt - k - 1; b += npg) {      // L_ik = A_ik Li^T
                     const int ti = k + 1 + b, r0 = ti * TB, rows = min(TB, ma - r0);

@@ -53,14 +53,14 @@ for q in range(100):
     print(q, int(pr[800 + q]), round((pr[500 + q] - t0) / 1e3, 1) if pr[500 + q] else "-",
           round((pr[600 + q] - t0) / 1e3, 1), round((pr[700 + q] - t0) / 1e3, 1) if pr[700 + q] else "-",
           round((t1 - t0) / 1e3, 1))
-# per-column detail of panels 2 and 30: after the diagonal factor, after the TRSM barrier, after
-# the intra-panel update barrier (us from the panel-update-done stamp)
-for qq, off in ((2, 900), (30, 916)):
+# per-column detail of panels 0 and 12: after the diagonal factor / TRSM / intra-panel update
+# barriers (us from the panel-update-done stamp)
+for qq, off in ((0, 900), (12, 940)):
     if pr[off] == 0:
         continue
     base = pr[500 + qq]
-    cols = [[round((pr[off + 3 * c + j] - base) / 1e3, 1) for j in range(3)] for c in range(4)]
-    print(f"panel {qq} columns (diag, trsm, update) us after its panel update:", cols)
+    cols = [[round(float(pr[off + 3 * c + j] - base) / 1e3, 1) for j in range(3)] for c in range(10) if pr[off + 3 * c]]
+    print(f"panel {qq} columns (start, after TRSM, after update) us after its panel update:", cols)
 # P1 sweep detail of the last traced iteration with S changed: per pivot step, phase A (U, the
 # previous column) and phase B (rank-64 update + next pivot) in us, from the grid-barrier stamps
 for i in range(len(data) // rec - 1, -1, -1):
