@@ -37,6 +37,22 @@ def elastic_energy(mesh, x: np.ndarray, p: np.ndarray) -> float:
     return 0.5 * float(np.sum(mesh.w * np.einsum("ti,ti->t", r, r)))
 
 
+def true_elastic_energies(mesh, x: np.ndarray, A9: np.ndarray) -> np.ndarray:
+    """Per-element true energies e_i(x) = min_{R in SO(3)} ||F_i(x) - R A_i||_F^2 (Eq. 1,
+    PAPER.md:75), the minimiser being the polar rotation of F_i A_i -> (T,).
+    Used by the true-energy line search (reading Z7's alternative)."""
+    F = mesh.deformation_gradients(x)
+    A = A9.reshape(-1, 3, 3)
+    R = polar_rotation(F @ A)
+    r = (F - R @ A).reshape(-1, 9)
+    return np.einsum("ti,ti->t", r, r)
+
+
+def true_elastic_energy(mesh, x: np.ndarray, A9: np.ndarray) -> float:
+    """E(x) = 1/2 sum_i w_i e_i(x) (Eq. 1 with the Z6 factor 1/2)."""
+    return 0.5 * float(np.sum(mesh.w * true_elastic_energies(mesh, x, A9)))
+
+
 def elastic_gradient(mesh, x: np.ndarray, p: np.ndarray) -> np.ndarray:
     """g_el[v] = sum_{i contains v} w_i (F_i - P_i) g_{i,c(v)} on ALL vertices -> (n, 3).
 
