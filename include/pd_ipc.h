@@ -106,7 +106,14 @@ typedef struct {
                                    f2) -- conjugate gradients on L^-1 H-hat L^-T, preconditioned by
                                    the prefactorised L, to a relative residual cg_tol (iterative:
                                    dx agrees with the direct backends to ~cg_tol x conditioning);
-                                 0 auto: gather when |R| >= 1024, else panel                    */
+                                 4 region: the paper's literal prescribed-region solve (PAPER.md
+                                   :161-198 Eq. 6-8, SURVEY 8(f) f1 "square"): the gather backend
+                                   with S = R, the whole W-supported region, every iteration --
+                                   Sigma_R = ((L^-1)_RR)^-1 computed once, the dense 3|R| x 3|R|
+                                   Sigma-hat refactorised each iteration (3.7x the K-Schur form's
+                                   largest system at C3); the same dx;
+                                 0 auto: gather when |R| >= 1024, else panel
+                                 (any other value: PD_IPC_E_ARG)                                 */
     double cg_tol;            /* pcg: relative residual ||r|| / ||r0|| to stop at (<= 0: 1e-12)  */
     int32_t cg_max_iters;     /* pcg: iteration cap per solve (<= 0: 10000)                      */
     double conv_tol;          /* > 0: "while not converged" (SURVEY Z10 option): a
@@ -114,6 +121,21 @@ typedef struct {
                                  vertex by conv_tol or more (max |alpha dx|, meters); its later
                                  iterations in the call leave it untouched.  0: the fixed n_iters
                                  count (the default, used by every benchmark)                   */
+    int32_t ls_energy;        /* line-search energy: 0 (default) the
+                                 surrogate E_p with p fixed at x (a closed-form quadratic elastic
+                                 part); 1 the true energy E = 1/2 sum w_i min_R ||F_i - R A_i||^2
+                                 (Eq. 1), R re-minimised (polar of F_i A_i) at every
+                                 trial alpha, summed as per-element differences e_i(x + alpha dx)
+                                 - e_i(x)                                                        */
+    double kappa_adapt_eps;   /* > 0: adaptive barrier stiffness ("kappa is
+                                 initialized according to the average stiffness ... and
+                                 adaptively adjusted", IPC's rule, reading R-kappa):
+                                 before the barrier terms of an iteration, kappa of the sequence
+                                 doubles (capped at kappa_max) when the minimum active-pair
+                                 distance is below kappa_adapt_eps (meters) and smaller than the
+                                 previous iteration's; kappa persists across step calls.
+                                 0 (default): kappa fixed                                        */
+    double kappa_max;         /* cap of the adaptive kappa (<= 0: 100 x the create-time kappa)   */
 } pd_ipc_options;
 
 #define PD_IPC_DBG_LARGE_SCHUR 1
@@ -132,7 +154,8 @@ typedef struct {
     int32_t flags;            /* PD_IPC_FLAG_*                                                 */
     double alpha_max;         /* alpha_m from CCD                                              */
     double alpha;             /* accepted step                                                 */
-    double dE;                /* surrogate energy change at the accepted step                  */
+    double dE;                /* line-search energy change at the accepted step (surrogate, or
+                                 true energy with ls_energy = 1)                                 */
     double min_dist;          /* min active-pair distance before the step (0 if C empty)      */
     double ms[6];             /* device time per stage over the call: IPC, G-Step, CCD, LS,
                                  Misc, total (Table 1 categories)               */
@@ -142,6 +165,8 @@ typedef struct {
                                  steps (S changed by <= 64 removed / added vertices, gather
                                  backend) instead of the full sweep; exact in exact arithmetic, a
                                  full sweep every 32 consecutive updates bounds the rounding drift */
+    double kappa;             /* barrier stiffness of the last iteration (= the create-time kappa
+                                 unless kappa_adapt_eps > 0)                                      */
 } pd_ipc_stats;
 
 /* Create a solver: validates the mesh, computes B_i = D_m^{-1} and w_i = det/6, assembles the
@@ -252,7 +277,7 @@ const char *pd_ipc_kernel_name(int32_t id);
 /* Sizes of the handle (for measurement reports): info[0..n) of
  *   [n_verts, n_tets, n_free, n_surf_verts, n_surf_tris, n_surf_edges, supernodes, nnz(L),
  *    supernodal etree depth, capS (max |S|), reuse slots, n_seq, backward row blocks, nU,
- *    reduced backend (1 panel, 2 gather, 3 pcg), |R|, Schur systems per launch]
+ *    reduced backend (1 panel, 2 gather, 3 pcg, 4 region), |R|, Schur systems per launch]
  * (nnz(L): the prefactorised PD matrix).  Returns the number of fields written. */
 int pd_ipc_get_info(const pd_ipc *h, int64_t *info, int32_t n);
 

@@ -109,9 +109,10 @@ enum : int {
     D_UPDATED = 24,  // iterations of the batch that updated Sigma_s by low-rank steps
     D_STRIDE = 32,
 };
-constexpr int S_STRIDE = 16;   // doubles per sequence in dscal: [0] unused, [1] amin, [2..4] ls,
+constexpr int S_STRIDE = 18;   // doubles per sequence in dscal: [0] unused, [1] amin, [2..4] ls,
                                // [5..8] ls_out, [9..10] scal, [11] max |pair term|, [12] min
-                               // active distance, [14..15] broad-phase cell
+                               // active distance, [14..15] broad-phase cell, [16] kappa of the
+                               // sequence, [17] previous min active d^2 (adaptive kappa)
 
 struct Seq {
     // captured CUDA graph of a batch run of this sequence alone (debug / redo path)
@@ -271,6 +272,8 @@ struct pd_ipc {
     // G2 = (L^-1)_RR over the region R of W-supported free vertices, n2 = |R|)
     bool gather = false;
     bool pcg = false;                   // the paper's PCG baseline
+    bool region = false;                // the paper's literal prescribed-region solve (backend 4: S = R)
+    DBuf<int> Rq_dev;                   // region R (factor positions), backend 4
     DBuf<double> cg_r, cg_p, cg_z, cg_q, cg_t, cg_f, cg_R, cg_part;
     double *cg_rr_host = nullptr;       // pinned: r.r of the last CG iteration
     int n2 = 0;
@@ -288,6 +291,7 @@ struct pd_ipc {
     DBuf<double> cd2, ad2, grad, Hp, dist;
     DBuf<int> mark;
     DBuf<double> lspart;    // line-search partial sums [ls_round_width()][ls_blocks()]
+    DBuf<double> tepart;    // true-energy line search: elastic partials [ls_round_width()][ls_te_blocks(T)]
     // second stream: w_el = L^-1 Pi g_el of all sequences runs concurrently with the contact
     // stages (it depends on the elastic gradients only)
     cudaStream_t st2 = nullptr;
@@ -717,8 +721,11 @@ static void enqueue_contact(pd_ipc *h, int b, int b0, int nb, int it) {
         kt.stop(K_NARROW, st);
         kt.start(K_DERIV, st);
         launch_contact_prep(h->mark.p, nf, h->gsq.p, 6 * Ns, dmax, st);   // clears of a5-a6
+        if (h->opt.kappa_adapt_eps > 0)       // f3: adaptive kappa from this iteration's min active d^2
+            launch_kappa_update(h->ad2.p, acnt, ds_ + 16, h->opt.kappa_adapt_eps * h->opt.kappa_adapt_eps,
+                                h->opt.kappa_max, st);
         launch_pair_derivs(h->akeys.p, h->atype.p, h->ad2.p, acnt, cap, h->s(b), h->tris.p, h->edges.p, Nt,
-                           Ne, h->dh, h->kappa, h->grad.p, h->Hp.p, h->dist.p, h->ids.p, dmax, st);
+                           Ne, h->dh, ds_ + 16, h->grad.p, h->Hp.p, h->dist.p, h->ids.p, dmax, st);
         kt.stop(K_DERIV, st);
         // fork: stream 3 takes the gradient pull-back (reads ids, grad, dmax, g_el; writes gsq,
         // G: deterministic fixed-point accumulation on the surface, then W^T), then -- once S is
@@ -731,6 +738,8 @@ static void enqueue_contact(pd_ipc *h, int b, int b0, int nb, int it) {
         kt.start(K_ASSEMBLY, st);
         // S
         launch_mark_S(h->ids.p, acnt, cap, h->Wp.p, h->Wc.p, h->v2q.p, h->mark.p, st);
+        if (h->region)   // backend 4 (the paper's prescribed region x_2, Eq. 6-8): S = R every iteration
+            launch_mark_list(h->Rq_dev.p, h->n2, h->mark.p, st);
         scan_compact(h->mark.p, SB.spos.p, SB.qS.p, nf, h->iscr.p, st);   // positions and S (sorted)
         // V_s, K_s, Sigma_s depend on S (and the constant factor) only: reuse the slot's while S
         // is bit-identical to the S they were computed for
@@ -875,10 +884,16 @@ static void enqueue_ccd_ls(pd_ipc *h, int b, int b0, int nb, int it) {
         elastic_partials(h->gel(b), h->dx(b), h->q2v.p, nf, h->tets.p, h->B_.p, h->w.p, T, h->part.p, &nb1, &nb2,
                          st);
         const int hmax = h->opt.ls_max_halvings;
-        for (int h0 = 0; h0 <= hmax; h0 = ls_round_next(h0))
+        const bool te = h->opt.ls_energy == 1;
+        for (int h0 = 0; h0 <= hmax; h0 = ls_round_next(h0)) {
+            int nte = 0;
+            if (te)   // f3: true elastic energy differences of the round's trials (block partials)
+                nte = launch_ls_true_elastic(h->tets.p, h->x(b), h->dx(b), h->B_.p, h->A6(b), h->w.p, T, amin, ls,
+                                             h0, ls_round_width_at(h0), h->tepart.p, st);
             launch_ls_round(q.cand.p, ccnt, h->s(b), h->tris.p, h->edges.p, Nt, Ne, h->ds(b), h->dh, h->b0.p, ls,
-                            h0, h->lspart.p, scal, h->kappa, hmax, ls_out, di + D_LSCTR, h->part.p, nb1,
-                            h->part.p + nb1, nb2, amin, st);
+                            h0, h->lspart.p, scal, dsc + 16, hmax, ls_out, di + D_LSCTR, h->part.p, nb1,
+                            h->part.p + nb1, nb2, amin, te ? h->tepart.p : nullptr, nte, st);
+        }
         launch_update(h->x(b), h->dx(b), h->q2v.p, nf, ls_out, di + D_INFO, di + D_ABORT, it, di + D_CONV,
                       reinterpret_cast<unsigned long long *>(dsc + 13), h->opt.conv_tol, st);
     }
@@ -1062,6 +1077,7 @@ static void run_lockstep(pd_ipc *h, int b0, int nb, int k, std::vector<int> &app
         if (n_all > 0 && !(min_dist > 0))
             throw CudaError("non-positive distance in the active set", PD_IPC_E_NONFINITE);
         S.min_dist = min_dist;
+        S.kappa = s[16];
         if (!std::isfinite(s[5]) || !std::isfinite(s[9]) || !std::isfinite(s[10]))
             throw CudaError("non-finite value in step", PD_IPC_E_NONFINITE);
         if (h->debug && nb == 1) debug_capture(h, b, n_pt, n_all - n_pt, q.nS);
@@ -1172,6 +1188,10 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         if (o.accd_max_iters <= 0) o.accd_max_iters = 10000;
         if (!(o.accd_s > 0 && o.accd_s < 1)) o.accd_s = 0.1;
     }
+    if (o.reduced_backend < 0 || o.reduced_backend > 4) return fail(nullptr, PD_IPC_E_ARG, "reduced_backend must be 0..4");
+    if (o.ls_energy != 0 && o.ls_energy != 1) return fail(nullptr, PD_IPC_E_ARG, "ls_energy must be 0 or 1");
+    if (!(o.kappa_adapt_eps >= 0)) return fail(nullptr, PD_IPC_E_ARG, "kappa_adapt_eps must be >= 0");
+    if (!(o.kappa_max > 0)) o.kappa_max = 100.0 * kappa;
     h->opt = o;
     h->dh = d_hat;
     h->kappa = kappa;
@@ -1372,6 +1392,15 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         h->dscal_all.exact((size_t)S_STRIDE * Bq);
         h->dint_all.exact((size_t)D_STRIDE * Bq);
         CK(cudaMemset(h->dscal_all.p, 0, sizeof(double) * S_STRIDE * Bq));   // flags / counters start cleared
+        {   // per-sequence kappa (constant unless adaptive) and the previous min active d^2 (+inf)
+            std::vector<double> kk(2 * (size_t)Bq);
+            for (int sq = 0; sq < Bq; ++sq) {
+                kk[2 * sq] = kappa;
+                kk[2 * sq + 1] = HUGE_VAL;
+            }
+            CK(cudaMemcpy2D(h->dscal_all.p + 16, S_STRIDE * sizeof(double), kk.data(), 2 * sizeof(double),
+                            2 * sizeof(double), Bq, cudaMemcpyHostToDevice));
+        }
         CK(cudaMemset(h->dint_all.p, 0, sizeof(int) * D_STRIDE * Bq));
         const size_t cap_cand = o.max_pairs > 0 ? (size_t)o.max_pairs
                                                 : std::max<size_t>(1 << 16, 16 * (size_t)(m.Ns + m.Ne));
@@ -1446,6 +1475,7 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             h->gsq.exact(6 * (size_t)m.Ns + 6);
         }
         h->lspart.exact((size_t)ls_round_width() * ls_blocks());
+        if (h->opt.ls_energy == 1) h->tepart.exact((size_t)ls_round_width() * ls_te_blocks(h->T));
         h->iscr.ensure(std::max({radix_scratch_ints((int)(2 * cap_cand)), scan_scratch_ints(nf + 1),
                                  scan_scratch_ints(f.nsn + 1)}) + 1024);
         {
@@ -1478,8 +1508,10 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             // reduced-solve backend: 1 panel, 2 gather, 0 auto (gather for regions of >= 1024
             // vertices: there the panel and K_s = V_s^T V_s dominate an iteration whenever S changes)
             const int be = o.reduced_backend;
-            const bool want = be == 2 || (be == 0 && h->n2 >= 1024);
+            const bool want = be == 2 || be == 4 || (be == 0 && h->n2 >= 1024);
             h->gather = m.Nt > 0 && want && h->n2 <= h->capS;
+            h->region = h->gather && be == 4;
+            if (h->region) h->Rq_dev.upload(Rq.data(), Rq.size());
             h->pcg = m.Nt > 0 && be == 3;
             // batched Schur: with the gather backend and several sequences, 2 systems per launch
             // (each on half the SMs: one system's serial panel chain overlaps the other's updates)
@@ -1706,7 +1738,7 @@ void pd_ipc_destroy(pd_ipc *h) {
     rel(h->xstage); rel(h->surf_out); rel(h->A9stage); rel(h->aflag); rel(h->blo);
     for (auto *bf : {&h->cg_r, &h->cg_p, &h->cg_z, &h->cg_q, &h->cg_t, &h->cg_f, &h->cg_R, &h->cg_part}) rel(*bf);
     if (h->cg_rr_host) cudaFreeHost(h->cg_rr_host);
-    rel(h->G2); rel(h->Yel_all); rel(h->Zf_all); rel(h->bw_P2); rel(h->rpos); rel(h->ts_done2); rel(h->bw_cnt2); rel(h->bhi); rel(h->hcnt); rel(h->hstart); rel(h->hent);
+    rel(h->G2); rel(h->Rq_dev); rel(h->Yel_all); rel(h->Zf_all); rel(h->bw_P2); rel(h->rpos); rel(h->ts_done2); rel(h->bw_cnt2); rel(h->bhi); rel(h->hcnt); rel(h->hstart); rel(h->hent);
     rel(h->qcnt); rel(h->qoff); rel(h->qlist); rel(h->gsq);
     rel(h->cand_tmp); rel(h->akeys); rel(h->flag); rel(h->pos); rel(h->ctype); rel(h->atype); rel(h->ids);
     rel(h->iscr); rel(h->cd2); rel(h->ad2); rel(h->grad); rel(h->Hp); rel(h->dist); rel(h->mark);
@@ -1723,7 +1755,7 @@ void pd_ipc_destroy(pd_ipc *h) {
         rel(g.uinfo);
     }
     for (auto &g : h->sys) { rel(g.qS); rel(g.spos); }
-    rel(h->lspart); rel(h->ts_lo);
+    rel(h->lspart); rel(h->tepart); rel(h->ts_lo);
     rel(h->ts_hi); rel(h->ts_cnt); rel(h->ts_ptr); rel(h->ts_rem); rel(h->ts_done); rel(h->ticket);
     rel(h->part); rel(h->b0);
     delete h;
@@ -1852,7 +1884,7 @@ int64_t pd_ipc_launch_count(void) { return pdipc::launch_count(); }
 int pd_ipc_get_info(const pd_ipc *h, int64_t *info, int32_t n) {
     if (!h || !info) return fail(nullptr, PD_IPC_E_ARG, "NULL argument");
     const int64_t v[17] = {h->n, h->T, h->nf, h->Ns, h->Nt, h->Ne, h->hf.nsn, h->hf.nnzL, h->hf.depth,
-                           h->capS, h->nslots, h->B, h->F.bw_nblocks, h->F.nU, h->pcg ? 3 : h->gather ? 2 : 1, h->n2,
+                           h->capS, h->nslots, h->B, h->F.bw_nblocks, h->F.nU, h->pcg ? 3 : h->region ? 4 : h->gather ? 2 : 1, h->n2,
                            h->nsysb};
     const int k = std::max(0, std::min<int>(n, 17));
     for (int i = 0; i < k; ++i) info[i] = v[i];

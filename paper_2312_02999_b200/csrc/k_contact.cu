@@ -542,6 +542,8 @@ __device__ __forceinline__ void dmma_pd(double (&d)[2], double a, double b) {
 struct LsFirst {                       // round 1 only: elastic partials and alpha_max
     const double *pg, *pq, *amin;
     int ng, nq;
+    const double *pte;                 // true-energy line search (f3): per-trial block partials of
+    int nte;                           // 1/2 sum w (e_i(alpha) - e_i(0)), [KH][nte]; null: surrogate
 };
 constexpr int kLsRound = 22;          // trial alphas of the last line-search round (h = 9..30)
 
@@ -550,9 +552,10 @@ constexpr int kLsRound = 22;          // trial alphas of the last line-search ro
 // H_k^+ (packed upper, 78) and h_k = kappa b' grad d (12).
 __global__ void __launch_bounds__(kPD_WARPS * 32, 4) k_pair_derivs(
     const unsigned long long *__restrict__ akeys, const int *__restrict__ atype,
-    const double *__restrict__ ad2, const int *__restrict__ acnt, PairCtx c, double dh, double kappa,
-    double *__restrict__ grad, double *__restrict__ Hp, double *__restrict__ dist,
+    const double *__restrict__ ad2, const int *__restrict__ acnt, PairCtx c, double dh,
+    const double *__restrict__ kap, double *__restrict__ grad, double *__restrict__ Hp, double *__restrict__ dist,
     int *__restrict__ ids_out, double *__restrict__ dmax) {
+    const double kappa = *kap;                           // the sequence's (possibly adaptive) kappa
     __shared__ double Hs[kPD_WARPS][12][13];
     __shared__ double Vs[kPD_WARPS][12][13];
     __shared__ double Xs[kPD_WARPS][16][kNsS];
@@ -737,6 +740,14 @@ __global__ void k_mark_S(const int *__restrict__ ids, const int *__restrict__ ac
             if (q >= 0) mark[q] = 1;
         }
     }
+}
+
+// backend 4 (prescribed region): every vertex of the list is in S
+__global__ void k_mark_list(const int *__restrict__ list, int n, int *__restrict__ mark) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) mark[list[i]] = 1;
+}
+void launch_mark_list(const int *list, int n, int *mark, cudaStream_t st) {
+    if (n > 0) PDI_LAUNCH(k_mark_list, std::min(148 * 4, (n + 255) / 256), 256, 0, st)(list, n, mark);
 }
 
 // same = (S == S_prev, bit for bit, |S| > 0); then S_prev <- S.  One CTA.
@@ -1126,11 +1137,12 @@ __global__ void __launch_bounds__(256) k_ls_round(const unsigned long long *__re
                                                   const double4 *__restrict__ ds, double dh,
                                                   double *__restrict__ b0, double *__restrict__ ls,
                                                   int h0, double *__restrict__ part, int part_ld,
-                                                  double *__restrict__ scal, double kappa, int hmax,
+                                                  double *__restrict__ scal, const double *__restrict__ kap, int hmax,
                                                   double *__restrict__ out, int *__restrict__ done_ctr,
                                                   LsFirst f) {
     const bool first = h0 == 0;
     if (!first && ls[1] != 0.0) return;   // already accepted
+    const double kappa = *kap;
     __shared__ double sh[8];
     __shared__ int last;
     const int npt = ccnt[0], n = ccnt[1];
@@ -1193,16 +1205,22 @@ __global__ void __launch_bounds__(256) k_ls_round(const unsigned long long *__re
         }
         __syncthreads();
     }
-    // decide: dE(alpha_h) = alpha gTdx + 0.5 alpha^2 quad + kappa dB
+    // decide: dE(alpha_h) = alpha gTdx + 0.5 alpha^2 quad + kappa dB, or with the
+    // true-energy line search (f3) dE = 1/2 sum w (e_i(alpha_h) - e_i(0)) + kappa dB
     for (int h = 0; h < KH; ++h) {
         double sum = 0.0;
         for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) sum += __ldcg(part + (size_t)h * part_ld + b);
         sum = block_sum<256>(sum, sh);
+        double el = 0.0;
+        if (f.pte) {
+            for (int b = threadIdx.x; b < f.nte; b += blockDim.x) el += __ldcg(f.pte + (size_t)h * f.nte + b);
+            el = block_sum<256>(el, sh);
+        }
         if (threadIdx.x == 0) {
             const int hh = h0 + h;
             if (hh <= hmax && ls[1] == 0.0) {
                 const double al = ldexp(am, -hh);
-                const double dE = al * scal[0] + 0.5 * al * al * scal[1] + kappa * sum;
+                const double dE = (f.pte ? el : al * scal[0] + 0.5 * al * al * scal[1]) + kappa * sum;
                 if (!isfinite(dE)) {                 // non-finite barrier sum: abort (see above)
                     ls[1] = 2.0;
                     out[0] = 0.0;
@@ -1229,7 +1247,31 @@ __global__ void __launch_bounds__(256) k_ls_round(const unsigned long long *__re
     if (threadIdx.x == 0) *done_ctr = 0;    // ready for the next round
 }
 
+// ------------------------------------------------------------------ f3 adaptive kappa -------
+// IPC's rule ("adaptively adjusted"; reading R-kappa), once per iteration
+// before the barrier terms: d2min = min active d^2 (exact, the narrow phase's canonical values;
+// +inf for an empty C); kappa doubles, capped at kmax, when d2min < eps^2 and d2min < the previous
+// iteration's.  kd = [kappa, previous d2min] of the sequence.  One block; min is order-free.
+__global__ void __launch_bounds__(256) k_kappa_update(const double *__restrict__ ad2, const int *__restrict__ acnt,
+                                                      double *__restrict__ kd, double eps2, double kmax) {
+    __shared__ double sh[8];
+    const int n = acnt[1];
+    double m = HUGE_VAL;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) m = fmin(m, ad2[i]);
+    for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) m = fmin(m, sh[w]);
+        if (m < eps2 && m < kd[1]) kd[0] = fmin(2.0 * kd[0], kmax);
+        kd[1] = m;
+    }
+}
+
 // ------------------------------------------------------------------ host wrappers ---------
+void launch_kappa_update(const double *ad2, const int *acnt, double *kd, double eps2, double kmax, cudaStream_t st) {
+    PDI_LAUNCH(k_kappa_update, 1, 256, 0, st)(ad2, acnt, kd, eps2, kmax);
+}
 void contact_init() {
     unsigned char ui[78], uj[78];
     int e = 0;
@@ -1302,7 +1344,7 @@ void launch_compact_active(const unsigned long long *keys, const int *ccnt, int 
 }
 void launch_pair_derivs(const unsigned long long *akeys, const int *atype, const double *ad2,
                         const int *acnt, int cap, const double4 *s, const int *tris, const int *edges,
-                        int Nt, int Ne, double dh, double kappa, double *grad, double *Hp,
+                        int Nt, int Ne, double dh, const double *kappa, double *grad, double *Hp,
                         double *dist, int *ids, double *dmax, cudaStream_t st) {
     PairCtx c{s, tris, edges, Nt, Ne};
     PDI_LAUNCH(k_pair_derivs, grid_for(cap, kPD_WARPS, 148 * 4), kPD_WARPS * 32, 0, st)(
@@ -1341,13 +1383,14 @@ void launch_accd(const unsigned long long *keys, const int *ccnt, int cap, const
 }
 int ls_blocks() { return 2 * 148; }
 int ls_round_width() { return kLsRound; }
+int ls_round_width_at(int h0) { return h0 == 0 ? 1 : h0 == 1 ? 8 : kLsRound; }
 void launch_ls_round(const unsigned long long *keys, const int *ccnt, const double4 *s, const int *tris,
                      const int *edges, int Nt, int Ne, const double4 *ds, double dh, double *b0, double *ls,
-                     int h0, double *part, double *scal, double kappa, int hmax, double *out,
+                     int h0, double *part, double *scal, const double *kappa, int hmax, double *out,
                      int *done_ctr, const double *pg, int ng, const double *pq, int nq, const double *amin,
-                     cudaStream_t st) {
+                     const double *pte, int nte, cudaStream_t st) {
     PairCtx c{s, tris, edges, Nt, Ne};
-    const LsFirst f{pg, pq, amin, ng, nq};
+    const LsFirst f{pg, pq, amin, ng, nq, pte, nte};
     // rounds of 1, 8, then 22 trial alphas: the full step is accepted in most iterations, and a
     // round after acceptance returns at once
     if (h0 == 0)

@@ -495,6 +495,110 @@ __global__ void k_scatter_dx(const double *__restrict__ z, const int *__restrict
 
 __global__ void k_set_double(double *p, double v) { *p = v; }
 
+// ------------------------------------------------------------------ f3 true-energy LS -----
+// Elastic part of the true-energy line search (SURVEY 8(f) f3, Z7's alternative): for the trials
+// alpha_h = am 2^-(h0+h), h < KH, block partials of 1/2 sum_i w_i (e_i(x + alpha_h dx) - e_i(x)),
+// e_i(y) = min_{R in SO(3)} ||F_i(y) - R A_i||_F^2 (Eq. 1), R = polar(F_i A_i)
+// by the local step's scaled Newton iteration, SVD route with the reflection fix for
+// det <= 0.  One thread per tet (grid-stride over a fixed grid: deterministic block sums);
+// written to pte[h * gridDim.x + block] and summed in fixed order by k_ls_round's decision.
+__device__ __forceinline__ double true_elastic_e(const double F[3][3], const double A[3][3]) {
+    double R[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) R[a][b] = F[a][0] * A[0][b] + F[a][1] * A[1][b] + F[a][2] * A[2][b];
+    if (!polar_newton(R)) {
+        const double M[3][3] = {{R[0][0], R[0][1], R[0][2]}, {R[1][0], R[1][1], R[1][2]},
+                                {R[2][0], R[2][1], R[2][2]}};
+        polar_rotation(M, R);
+    }
+    double e = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+            const double r = F[a][b] - (R[a][0] * A[0][b] + R[a][1] * A[1][b] + R[a][2] * A[2][b]);
+            e += r * r;
+        }
+    return e;
+}
+template <int KH>
+__global__ void __launch_bounds__(256) k_ls_true_elastic(const int4 *__restrict__ tets, const double4 *__restrict__ x,
+                                                         const double4 *__restrict__ dx, const double *__restrict__ B,
+                                                         const double *__restrict__ A6, const double *__restrict__ w,
+                                                         int T, const double *__restrict__ amin,
+                                                         const double *__restrict__ ls, int h0,
+                                                         double *__restrict__ pte) {
+    if (h0 > 0 && ls[1] != 0.0) return;    // accepted (or aborted) in an earlier round
+    __shared__ double sh[8];
+    const double am = h0 == 0 ? *amin : ls[0];
+    double acc[KH];
+#pragma unroll
+    for (int h = 0; h < KH; ++h) acc[h] = 0.0;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
+        const int4 tv = tets[t];
+        double Bm[3][3];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) Bm[k / 3][k % 3] = B[(size_t)k * T + t];
+        const double a00 = A6[t], a01 = A6[(size_t)T + t], a02 = A6[2 * (size_t)T + t], a11 = A6[3 * (size_t)T + t],
+                     a12 = A6[4 * (size_t)T + t], a22 = A6[5 * (size_t)T + t];
+        const double A[3][3] = {{a00, a01, a02}, {a01, a11, a12}, {a02, a12, a22}};
+        const double4 X[4] = {x[tv.x], x[tv.y], x[tv.z], x[tv.w]};
+        const double4 D[4] = {dx[tv.x], dx[tv.y], dx[tv.z], dx[tv.w]};
+        const double hw = 0.5 * w[t];
+        double e0;
+        {
+            double F[3][3];
+            const double Ds[3][3] = {{X[1].x - X[0].x, X[2].x - X[0].x, X[3].x - X[0].x},
+                                     {X[1].y - X[0].y, X[2].y - X[0].y, X[3].y - X[0].y},
+                                     {X[1].z - X[0].z, X[2].z - X[0].z, X[3].z - X[0].z}};
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int b = 0; b < 3; ++b) F[a][b] = Ds[a][0] * Bm[0][b] + Ds[a][1] * Bm[1][b] + Ds[a][2] * Bm[2][b];
+            e0 = true_elastic_e(F, A);
+        }
+#pragma unroll 1
+        for (int h = 0; h < KH; ++h) {
+            const double al = ldexp(am, -(h0 + h));
+            double Y[4][3];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                Y[c][0] = X[c].x + al * D[c].x;
+                Y[c][1] = X[c].y + al * D[c].y;
+                Y[c][2] = X[c].z + al * D[c].z;
+            }
+            double F[3][3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int b = 0; b < 3; ++b)
+                    F[a][b] = (Y[1][a] - Y[0][a]) * Bm[0][b] + (Y[2][a] - Y[0][a]) * Bm[1][b] +
+                              (Y[3][a] - Y[0][a]) * Bm[2][b];
+            acc[h] += hw * (true_elastic_e(F, A) - e0);
+        }
+    }
+#pragma unroll 1
+    for (int h = 0; h < KH; ++h) {
+        const double v = block_sum<256>(acc[h], sh);
+        if (threadIdx.x == 0) pte[(size_t)h * gridDim.x + blockIdx.x] = v;
+    }
+}
+int ls_te_blocks(int T) { return std::max(1, std::min((T + 255) / 256, 148 * 4)); }
+int launch_ls_true_elastic(const int4 *tets, const double4 *x, const double4 *dx, const double *B, const double *A6,
+                           const double *w, int T, const double *amin, const double *ls, int h0, int kh,
+                           double *pte, cudaStream_t st) {
+    const int nb = ls_te_blocks(T);
+    if (kh == 1)
+        PDI_LAUNCH(k_ls_true_elastic<1>, nb, 256, 0, st)(tets, x, dx, B, A6, w, T, amin, ls, h0, pte);
+    else if (kh == 8)
+        PDI_LAUNCH(k_ls_true_elastic<8>, nb, 256, 0, st)(tets, x, dx, B, A6, w, T, amin, ls, h0, pte);
+    else
+        PDI_LAUNCH(k_ls_true_elastic<22>, nb, 256, 0, st)(tets, x, dx, B, A6, w, T, amin, ls, h0, pte);
+    return nb;
+}
+
 // ------------------------------------------------------------------ host wrappers ---------
 void launch_set_double(double *p, double v, cudaStream_t st) { PDI_LAUNCH(k_set_double, 1, 1, 0, st)(p, v); }
 

@@ -59,6 +59,14 @@ void elastic_partials(const double4 *g, const double4 *dx, const int *q2v, int n
 void launch_update(double4 *x, const double4 *dx, const int *q2v, int nf, const double *alpha,
                    const int *flags, int *abort, int it, int *cv, unsigned long long *amax, double tol,
                    cudaStream_t st);
+// f3 true-energy line search: block partials pte[h][b] of 1/2 sum w (e_i(alpha_h) - e_i(0)),
+// e_i = min_R ||F_i - R A_i||^2, for the round's trials alpha_h = am 2^-(h0+h), h < kh; am = *amin
+// in the first round, ls[0] after; a round after acceptance (ls[1] != 0) returns at once.
+// Returns the number of blocks (ls_te_blocks(T)).
+int launch_ls_true_elastic(const int4 *tets, const double4 *x, const double4 *dx, const double *B, const double *A6,
+                           const double *w, int T, const double *amin, const double *ls, int h0, int kh,
+                           double *pte, cudaStream_t st);
+int ls_te_blocks(int T);
 // z [nseq][nf][4] -> dx [nseq][n]; seeds amin[sq * amin_stride] = 1
 void launch_scatter_dx(const double *z, const int *q2v, int nf, double4 *dx, double *amin, int nseq, int n,
                        int amin_stride, cudaStream_t st);
@@ -213,10 +221,13 @@ void launch_compact_active(const unsigned long long *keys, const int *ccnt, int 
                            int *atype, double *ad2, int *acnt, cudaStream_t st);
 void launch_pair_derivs(const unsigned long long *akeys, const int *atype, const double *ad2,
                         const int *acnt, int cap, const double4 *s, const int *tris, const int *edges,
-                        int Nt, int Ne, double dh, double kappa, double *grad, double *Hp,
+                        int Nt, int Ne, double dh, const double *kappa, double *grad, double *Hp,
                         double *dist, int *ids, double *dmax, cudaStream_t st);
+// f3 adaptive kappa: kd = [kappa, previous min active d^2] of the sequence (see k_contact.cu)
+void launch_kappa_update(const double *ad2, const int *acnt, double *kd, double eps2, double kmax, cudaStream_t st);
 void launch_mark_S(const int *ids, const int *acnt, int cap, const int *Wp, const int *Wc, const int *v2q,
                    int *mark, cudaStream_t st);
+void launch_mark_list(const int *list, int n, int *mark, cudaStream_t st);   // mark[list[i]] = 1
 // S against the slot's previous S: bit-identical (reuse), or the plan of a low-rank Sigma_s update
 // (dpos / rl / al / uinfo, gather backend, allow_upd) -- see k_contact.cu
 void launch_same_S(const int *qS, const int *nS_ptr, int *qS_prev, int *nS_prev, int *same, int cap,
@@ -251,10 +262,11 @@ int ls_blocks();
 // alpha_max from *amin
 void launch_ls_round(const unsigned long long *keys, const int *ccnt, const double4 *s, const int *tris,
                      const int *edges, int Nt, int Ne, const double4 *ds, double dh, double *b0, double *ls,
-                     int h0, double *part, double *scal, double kappa, int hmax, double *out,
+                     int h0, double *part, double *scal, const double *kappa, int hmax, double *out,
                      int *done_ctr, const double *pg, int ng, const double *pq, int nq, const double *amin,
-                     cudaStream_t st);
+                     const double *pte, int nte, cudaStream_t st);
 int ls_round_width();
+int ls_round_width_at(int h0);   // trial alphas of the round starting at h0 (1, 8, 22)
 int ls_round_next(int h0);   // first halving of the round after the one starting at h0
 
 }  // namespace pdipc

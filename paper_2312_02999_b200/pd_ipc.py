@@ -33,7 +33,8 @@ class pd_ipc_options(C.Structure):
                 ("accd_max_iters", C.c_int32), ("A_on_device", C.c_int32),
                 ("max_pairs", C.c_int32), ("accd_s", C.c_double), ("no_sigma_reuse", C.c_int32),
                 ("no_cand_reuse", C.c_int32), ("debug_flags", C.c_int32), ("reduced_backend", C.c_int32),
-                ("cg_tol", C.c_double), ("cg_max_iters", C.c_int32), ("conv_tol", C.c_double)]
+                ("cg_tol", C.c_double), ("cg_max_iters", C.c_int32), ("conv_tol", C.c_double),
+                ("ls_energy", C.c_int32), ("kappa_adapt_eps", C.c_double), ("kappa_max", C.c_double)]
 
 
 class pd_ipc_stats(C.Structure):
@@ -41,7 +42,7 @@ class pd_ipc_stats(C.Structure):
                 ("n_S", C.c_int32), ("ls_trials", C.c_int32), ("flags", C.c_int32),
                 ("alpha_max", C.c_double), ("alpha", C.c_double), ("dE", C.c_double),
                 ("min_dist", C.c_double), ("ms", C.c_double * 6), ("sigma_reused", C.c_int32),
-                ("cg_iters", C.c_int32), ("sigma_updated", C.c_int32)]
+                ("cg_iters", C.c_int32), ("sigma_updated", C.c_int32), ("kappa", C.c_double)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_ if k != "ms"}
@@ -198,7 +199,7 @@ def _check(rc, h=None):
 def create(scene, A=None, n_seq=1, device=0, A_on_device=False, max_pairs=0,
            ls_max_halvings=30, accd_max_iters=10_000, accd_s=0.1, d_hat=None, kappa=None,
            sigma_reuse=True, cand_reuse=True, debug_flags=0, reduced_backend=0, cg_tol=1e-12,
-           cg_max_iters=10000, conv_tol=0.0):
+           cg_max_iters=10000, conv_tol=0.0, ls_energy="surrogate", kappa_adapt_eps=0.0, kappa_max=0.0):
     """pd_ipc_create on a scenes.Scene.  A: (n_seq, T, 9) host actuation (default frame 0)."""
     m = _MeshArgs(scene)
     if A is None:
@@ -207,7 +208,8 @@ def create(scene, A=None, n_seq=1, device=0, A_on_device=False, max_pairs=0,
     opt = pd_ipc_options(n_seq, device, ls_max_halvings, accd_max_iters, int(A_on_device),
                          max_pairs, accd_s, 0 if sigma_reuse else 1, 0 if cand_reuse else 1,
                          int(debug_flags), int(reduced_backend), float(cg_tol), int(cg_max_iters),
-                         float(conv_tol))
+                         float(conv_tol), {"surrogate": 0, "true": 1}[ls_energy], float(kappa_adapt_eps),
+                         float(kappa_max))
     h = _P()
     rc = lib.pd_ipc_create(C.byref(m.mesh), _dp(m.rest), _dp(A),
                            float(scene.d_hat if d_hat is None else d_hat),

@@ -46,6 +46,24 @@ def test_create_without_gpu_fails_loudly(P):
     assert e.value.code == P.E_CUDA
 
 
+@pytest.mark.parametrize("kw", [dict(reduced_backend=5), dict(reduced_backend=-1), dict(kappa_adapt_eps=-1.0)])
+def test_create_rejects_bad_options(P, kw):
+    """Option validation happens before any device work (include/pd_ipc.h: E_ARG)."""
+    with pytest.raises(P.PdIpcError) as e:
+        P.create(scenes.slabs_c1(), **kw)
+    assert e.value.code == P.E_ARG
+
+
+def test_create_rejects_bad_ls_energy(P):
+    opt = P.pd_ipc_options()
+    opt.n_seq, opt.ls_energy = 1, 2
+    m = P._MeshArgs(scenes.slabs_c1())
+    A = P._f64(scenes.slabs_c1().actuation(0))
+    h = P._P()
+    rc = P.lib.pd_ipc_create(P.C.byref(m.mesh), P._dp(m.rest), P._dp(A), 1e-3, 1.0, P.C.byref(opt), P.C.byref(h))
+    assert rc == P.E_ARG
+
+
 @pytest.mark.parametrize("make", [scenes.slabs_c1, scenes.face_small, lambda: scenes.box_c5("10k")])
 def test_host_factor_solves_oracle_laplacian(P, make):
     from oracle import build_mesh
@@ -100,3 +118,29 @@ def test_host_crossing_check_matches_brute_force(P):
         ref = edge_triangle_crossings(m.W @ x, m.tris, m.edges)
         assert ref > 0
         assert P.debug_crossings(sc, x) == ref
+
+
+def test_struct_layouts_match_header(P, tmp_path):
+    """The ctypes mirrors of pd_ipc_options / pd_ipc_stats / pd_ipc_mesh have the header's
+    size and field offsets (gcc compiles include/pd_ipc.h and prints them)."""
+    import ctypes
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    structs = {"pd_ipc_options": P.pd_ipc_options, "pd_ipc_stats": P.pd_ipc_stats, "pd_ipc_mesh": P.pd_ipc_mesh}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "pd_ipc.h"', "int main(void) {"]
+    for name, cls in structs.items():
+        lines.append(f'printf("{name} size %zu\\n", sizeof({name}));')
+        for f, _ in cls._fields_:
+            lines.append(f'printf("{name} {f} %zu\\n", offsetof({name}, {f}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(root, "include"), str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split("\n")
+    got = {tuple(l.split()[:2]): int(l.split()[2]) for l in out if l.strip()}
+    for name, cls in structs.items():
+        assert got[(name, "size")] == ctypes.sizeof(cls), name
+        for f, _ in cls._fields_:
+            assert got[(name, f)] == getattr(cls, f).offset, (name, f)
