@@ -1,4 +1,5 @@
-"""f1 ablation: the two reduced-solve backends (panel vs precomputed-region gather) behind the same
+"""f1 ablation: the reduced-solve backends (panel, precomputed-region gather, the paper's prescribed-region
+solve with S = R) behind the same
 dx contract, on C2 and C3 (BASELINE configs[1], [2]): warm-started frame, ms per iteration and
 stage times.  Usage: python tools/backend_ablation.py"""
 import json
@@ -29,7 +30,7 @@ def run(name, sc, frame, backend, prep=20, iters=20):
     kt = P.kernel_times(s.h, reset=True)
     x = s.positions()
     s.close()
-    return {"scene": name, "backend": {1: "panel", 2: "gather"}[info["reduced_backend"]],
+    return {"scene": name, "backend": {1: "panel", 2: "gather", 4: "region"}[info["reduced_backend"]],
             "region_size": info["region_size"], "ms_per_iter": e0.elapsed_time(e1) / iters,
             "n_S_last": st["n_S"], "sigma_reused": st["sigma_reused"],
             "stage_ms_per_iter": {k: round(v[0] / iters, 3) for k, v in kt.items() if v[1]}}, x
@@ -38,9 +39,10 @@ def run(name, sc, frame, backend, prep=20, iters=20):
 for name, mk, frame in (("C2", scenes.face_c2, 30), ("C3", scenes.face_c3, 30)):
     sc = mk()
     xs = []
-    for be in (1, 2):
+    for be in (1, 2, 4):
         r, x = run(name, sc, frame, be)
         xs.append(x)
         print(json.dumps(r), flush=True)
-    print(json.dumps({"scene": name, "max_position_difference_between_backends": float(np.abs(xs[0] - xs[1]).max()),
+    print(json.dumps({"scene": name, "max_position_difference_between_backends":
+                      float(max(np.abs(xs[0] - y).max() for y in xs[1:])),
                       "bbox_diag": sc.bbox_diag()}), flush=True)
