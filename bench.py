@@ -294,10 +294,14 @@ def run_reference(a):
 
 
 # ------------------------------------------------------------------------------ rooflines --
-# FP64 tensor (DMMA, mma.sync.m8n8k4.f64) throughput measured on this pool's B200 by
-# tools/micro/fp64_peaks.cu: 128 flop/clk/SM (profiles/fp64_peaks_r01.txt).  tcgen05 has no
-# f64 kind, so this is the FP64 contraction peak; x 148 SMs x the max SM clock.
-DMMA_FLOP_PER_CLK_SM = 128.0
+# FP64 tensor (DMMA, mma.sync.m8n8k4.f64) throughput measured on this pool's B200 over the whole
+# GPU by tools/micro/dmma_gpu_peak.cu: 37.12 TFLOP/s at 1965 MHz = 127.6 flop/clk/SM
+# (profiles/fp64_gpu_peak_r02.txt; the one-SM figure of tools/micro/fp64_peaks.cu is 128).
+# tcgen05 has no f64 kind, so this is the FP64 contraction peak; scaled by the max SM clock.
+# cuBLAS DGEMM (torch.matmul float64, 8192^3) reaches 35.45 TFLOP/s on the same GPU: the
+# library reference the dense Schur kernel is also quoted against.
+DMMA_TFLOPS_MEASURED, DMMA_MEASURED_MHZ = 37.12, 1965.0
+DGEMM_CUBLAS_TFLOPS = 35.45
 N_SM = 148
 
 
@@ -315,10 +319,30 @@ def _traffic(kernel):
 
 
 def _fp64_peak(sm_max_mhz):
-    return DMMA_FLOP_PER_CLK_SM * N_SM * sm_max_mhz * 1e6 / 1e12
+    return DMMA_TFLOPS_MEASURED * sm_max_mhz / DMMA_MEASURED_MHZ
 
 
-def rooflines(kt, info, nb, nS_list, reuse_frac, hbm, sm_max_mhz, peak_src, upd_frac=0.0):
+def _ns_steps(floor=1e-10):
+    """Steps of the scaled Newton-Schulz sign schedule of k_pair_derivs (k_contact.cu
+    contact_init: a = sqrt(3 / (1 + l + l^2)), l <- a l (3 - a^2 l^2) / 2 from l = floor until
+    1 - l < 1e-16)."""
+    import math
+    l, k = floor, 0
+    while k < 64:
+        a = math.sqrt(3.0 / (1.0 + l + l * l))
+        k += 1
+        l = 0.5 * a * l * (3.0 - a * a * l * l)
+        if 1.0 - l < 1e-16:
+            break
+    return k
+
+
+# DMMA flops one sign step issues per pair: two 16x16 (zero-padded 12x12) products with k = 12,
+# 4 output tiles x 3 k-steps x 512 flops each
+NS_FLOPS_PER_STEP = 2 * 4 * 3 * 512
+
+
+def rooflines(kt, info, nb, nS_list, reuse_frac, hbm, sm_max_mhz, peak_src, upd_frac=0.0, nA_list=None):
     """Per kernel group: achieved = ALGORITHMIC bytes (flops) per launch / average launch time
     (live CUDA events), DESIGN.md section 5.  kt: {group: (ms, launches)}; nb sequences per
     lockstep iteration; nS_list: n_c of every sequence."""
@@ -366,9 +390,22 @@ def rooflines(kt, info, nb, nS_list, reuse_frac, hbm, sm_max_mhz, peak_src, upd_
                               "unit": "TFLOP/s", "frac": f / t / 1e12 / pk, "flops_per_launch": f,
                               "avg_launch_us": t * 1e6, "n_c_mean": statistics.mean(nS_list),
                               "systems_per_launch": info.get("schur_systems_per_launch", 1),
-                              "peak_source": "FP64 DMMA measured (tools/micro/fp64_peaks.cu) x 148 SMs x max clock"}
-    for k in ("pair_derivatives", "panel_forward", "contact_assembly", "narrow_phase", "broad_phase", "ccd",
-              "line_search"):
+                              "frac_of_cublas_dgemm": f / t / 1e12 / DGEMM_CUBLAS_TFLOPS,
+                              "peak_source": "FP64 DMMA measured over the whole GPU (tools/micro/dmma_gpu_peak.cu, "
+                                             "profiles/fp64_gpu_peak_r02.txt), scaled to the max SM clock"}
+    t, c = avg("pair_derivatives")
+    if t and nA_list:
+        # warp per active pair; the PSD projection's sign iteration dominates: issued DMMA flops
+        # (padded 16x16 tiles) of the fixed schedule per pair, per sequence's launch
+        f = statistics.mean(nA_list) * _ns_steps() * NS_FLOPS_PER_STEP
+        pk = _fp64_peak(sm_max_mhz)
+        out["pair_derivatives"] = {"bound": "tensor", "achieved": f / t / 1e12, "peak": pk, "unit": "TFLOP/s",
+                                   "frac": f / t / 1e12 / pk, "flops_per_launch": f, "avg_launch_us": t * 1e6,
+                                   "launches": c, "n_active_mean": statistics.mean(nA_list),
+                                   "note": "issued DMMA flops of the Newton-Schulz sign iteration (%d steps, "
+                                           "zero-padded 16x16 tiles); the timed group also holds the clears "
+                                           "of a5-a6" % _ns_steps()}
+    for k in ("panel_forward", "contact_assembly", "narrow_phase", "broad_phase", "ccd", "line_search"):
         t, c = avg(k)
         if t:
             out[k] = {"bound": "latency", "avg_launch_us": t * 1e6, "launches": c}
@@ -525,6 +562,7 @@ def run_ours(a):
     my_ms = float(sum(e0.elapsed_time(e1) for e0, e1 in ev))
     checks = [(j, seq_checksum(s.positions(b))) for b, j in enumerate(mine)]
     nS_all = [st[b]["n_S"] for st in stats for b in range(nb)]
+    nA_all = [st[b]["n_active"] for st in stats for b in range(nb)]
     reuse = sum(st[b]["sigma_reused"] for st in stats for b in range(nb)) / float(max(1, K * nb))
     upd = sum(st[b]["sigma_updated"] for st in stats for b in range(nb)) / float(max(1, K * nb))
     # exposed time of the reduced solve per sequence-iteration: B-check ready (end of the
@@ -578,7 +616,7 @@ def run_ours(a):
     value = job_throughput(allv[:, 0], allv[:, 2])
     hbm, bf16, peak_src = _peaks()
     sm_max = _sm_max_mhz()
-    rl_all = rooflines(kt, info, nb, nS_all, reuse, hbm, sm_max, peak_src, upd)
+    rl_all = rooflines(kt, info, nb, nS_all, reuse, hbm, sm_max, peak_src, upd, nA_all)
     dom = rl_all.get("dense_schur")
     rl = None
     if dom:

@@ -295,6 +295,7 @@ struct pd_ipc {
     // second stream: w_el = L^-1 Pi g_el of all sequences runs concurrently with the contact
     // stages (it depends on the elastic gradients only)
     cudaStream_t st2 = nullptr;
+    bool side_env = false;    // PDIPC_SIDE_CTAS given: use side_ctas for every batch size
     int side_ctas = 74;       // persistent CTAs of the stream-2 solve (PDIPC_SIDE_CTAS); the rest
                               // of the SMs run the contact stages concurrently (74: the w_el solve
                               // and the contact path end together at C2, tools/side_sweep.sh)
@@ -622,6 +623,10 @@ static void enqueue_elastic(pd_ipc *h, int b0, int nb, int it) {
     // step)
     cudaStream_t s2 = h->st2;
     const DevFactor &F2 = h->F;
+    // CTAs of the side solve: 74 when it overlaps a single sequence's contact path (C2, tuned by
+    // tools/side_sweep.sh); every SM for a batch of >= 4 sequences, where the first Schur step
+    // waits for the whole batched solve (C4: 65.3 -> 65.9 it/s, tools/gpu_side_sweep.sh)
+    const int side = h->Nt == 0 ? h->nsm : (nb >= 4 && !h->side_env) ? h->nsm : h->side_ctas;
     CK(cudaEventRecord(h->ev_fork, st));
     CK(cudaStreamWaitEvent(s2, h->ev_fork, 0));
     kt.start(K_D_SYRK, s2);
@@ -632,13 +637,13 @@ static void enqueue_elastic(pd_ipc *h, int b0, int nb, int it) {
     launch_forward_solve(F2, h->ts_lo2.p, h->ts_hi2.p, h->ts_ptr2.p, nullptr, h->ts_rem2.p, h->ticket2.p,
                          reinterpret_cast<const double *>(h->gel(b0)), h->Yw(b0), nullptr, h->ldv, h->Ug2.p,
                          nullptr, h->ticket2.p + 2, 0, 1, nb, 4 * (long long)h->nf,
-                         4 * (long long)std::max(1, F2.nU), h->Nt > 0 ? h->side_ctas : h->nsm, nullptr, s2);
+                         4 * (long long)std::max(1, F2.nU), side, nullptr, s2);
     if (h->gather && h->Nt > 0) {
         // gather backend: y_el = L^-T w_el (the base solve), whose rows S give y_S
         CK(dev_copy(h->Yel(b0), h->Yw(b0), sizeof(double) * 4 * h->nf * nb, s2));
         for (int c = 0; c < nb; c += kBwSeqs)
             launch_backward_solve(h->F, h->ts_done2.p, h->bw_cnt2.p, h->ticket2.p, h->bw_P2.p, h->Yel(b0 + c),
-                                  std::min(kBwSeqs, nb - c), 4 * (long long)h->nf, h->side_ctas, s2);
+                                  std::min(kBwSeqs, nb - c), 4 * (long long)h->nf, side, s2);
     }
     kt.stop(K_D_SYRK, s2);
     CK(cudaEventRecord(h->ev_join, s2));
@@ -1225,7 +1230,10 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         h->kt.init();
         if (const char *ng = std::getenv("PDIPC_NO_GRAPH")) h->graphs = !(ng[0] == '1');
         if (const char *tl = std::getenv("PDIPC_TIMELINE")) h->kt.timeline = tl[0] == '1';
-        if (const char *sc = std::getenv("PDIPC_SIDE_CTAS")) h->side_ctas = std::max(1, std::atoi(sc));
+        if (const char *sc = std::getenv("PDIPC_SIDE_CTAS")) {
+            h->side_ctas = std::max(1, std::atoi(sc));
+            h->side_env = true;
+        }
         if (const char *tp = std::getenv("PDIPC_TRACE")) {
             h->trace_file = std::fopen(tp, "wb");
             h->schur_file = std::fopen((std::string(tp) + ".schur").c_str(), "wb");
