@@ -12,13 +12,14 @@ Rules (task statement, tier framing):
 
 Modules
   setup      O0  element matrices, the PD Laplacian L (H = L (x) I3), surface edges, W
-  local      O1  polar local step (Eq. 1)
+  local      O1  polar local step (Eq. 1); the true element energies min_R ||F - R A||^2 (f3)
   elastic    O2  elastic gradient (Eq. 2 / Eq. 4)
   distance   O3  canonical primitive distances (type + squared distance)
   barrier    O4  barrier b(d), its derivatives, per-pair gradient/Hessian, PSD projection
   contact    O3-O5 active set C, contact vertex set S, pulled-back gradient and Hessian
   ccd        O7  additive conservative advancement
-  solver     O6, O8, O9, frames: full sparse solve, line search, update, Algorithm 1 driver
+  solver     O6, O8, O9, frames: full sparse solve, line search (surrogate or true energy),
+             update, adaptive kappa (IPC's rule), Algorithm 1 driver
 
 Parity pins: every function is pinned by tests/test_oracle_*.py against closed forms,
 finite differences, brute force or textbook special cases; the one unpinned quantity (the
