@@ -370,12 +370,13 @@ def rooflines(kt, info, nb, nS_list, reuse_frac, hbm, sm_max_mhz, peak_src, upd_
                                "frac": b / t / 1e9 / hbm, "bytes_per_launch": b, "avg_launch_us": t * 1e6,
                                "note": "one launch solves all nb sequences' gradients; dependency-depth bound"}
     t, _ = avg("backward_solve")
-    if t:   # one timer spans the ceil(nb/8) backward launches of an iteration
-        nl = (nb + 7) // 8
-        b = nl * nnzL * 8 + nb * nf * 32 * 2
+    if t:   # ONE launch per iteration for all nb sequences (column tiles of 8 sequences): the factor
+        # (nnz(L) doubles) counted once -- the tiles' re-reads of a Q block come from L2 -- plus the
+        # right-hand sides in and out
+        b = nnzL * 8 + nb * nf * 32 * 2
         out["backward_solve"] = {"bound": "hbm", "achieved": b / t / 1e9, "peak": hbm, "unit": "GB/s",
                                  "frac": b / t / 1e9 / hbm, "bytes_per_iteration": b, "avg_iteration_us": t * 1e6,
-                                 "launches_per_iteration": nl}
+                                 "launches_per_iteration": 1, "column_tiles": (nb + 7) // 8}
     t, _ = avg("dense_schur")
     if t and nS_list:
         # per sequence at n_c, m = 3 n_c: Cholesky of the augmented Sigma-hat (m^3 / 3), Sigma_s =

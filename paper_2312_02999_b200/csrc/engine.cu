@@ -641,9 +641,8 @@ static void enqueue_elastic(pd_ipc *h, int b0, int nb, int it) {
     if (h->gather && h->Nt > 0) {
         // gather backend: y_el = L^-T w_el (the base solve), whose rows S give y_S
         CK(dev_copy(h->Yel(b0), h->Yw(b0), sizeof(double) * 4 * h->nf * nb, s2));
-        for (int c = 0; c < nb; c += kBwSeqs)
-            launch_backward_solve(h->F, h->ts_done2.p, h->bw_cnt2.p, h->ticket2.p, h->bw_P2.p, h->Yel(b0 + c),
-                                  std::min(kBwSeqs, nb - c), 4 * (long long)h->nf, side, s2);
+        launch_backward_solve(h->F, h->ts_done2.p, h->bw_cnt2.p, h->ticket2.p, h->bw_P2.p, h->Yel(b0), nb,
+                              4 * (long long)h->nf, side, s2);
     }
     kt.stop(K_D_SYRK, s2);
     CK(cudaEventRecord(h->ev_join, s2));
@@ -849,9 +848,8 @@ static void enqueue_backward(pd_ipc *h, int b0, int nb, int it) {
         Zb = h->Zf(b0);
     }
     kt.start(K_BWD, st);
-    for (int c = 0; c < nb; c += kBwSeqs)
-        launch_backward_solve(h->F, h->ts_done.p, h->bw_cnt.p, h->ticket.p, h->bw_P.p, Zb + (size_t)c * 4 * h->nf,
-                              std::min(kBwSeqs, nb - c), 4 * (long long)h->nf, h->nsm, st);
+    launch_backward_solve(h->F, h->ts_done.p, h->bw_cnt.p, h->ticket.p, h->bw_P.p, Zb, nb, 4 * (long long)h->nf,
+                          h->nsm, st);
     kt.stop(K_BWD, st);
     launch_scatter_dx(Zb, h->q2v.p, h->nf, h->dx(b0), h->dscal(b0) + 1, nb, h->n, S_STRIDE,
                       st);   // also seeds each sequence's CCD minimum amin = 1
@@ -1217,6 +1215,7 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         if (o.device < 0 || o.device >= ndev) return fail(nullptr, PD_IPC_E_ARG, "bad device ordinal");
         CK(cudaSetDevice(o.device));
         h->device = o.device;
+        const int bw_tiles = (o.n_seq + kBwSeqs - 1) / kBwSeqs;   // backward solve: one launch, all sequences
         CK(cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, o.device));
         CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
@@ -1329,8 +1328,8 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             h->f_bw_pbase.upload(pbase.data(), pbase.size());
             h->F.bw_nitems = (int)items.size();
             h->F.bw_nblocks = nblk;
-            h->bw_P.exact((size_t)nblk * 128 * 32);   // kTS_W x kBwCols partials per row block
-            h->bw_cnt.exact(f.nsn);
+            h->bw_P.exact((size_t)nblk * 128 * 32 * bw_tiles);   // kTS_W x kBwCols partials per row block and tile
+            h->bw_cnt.exact((size_t)f.nsn * bw_tiles);
         }
         h->f_uoff.upload(f.uoff.data(), f.uoff.size());
         h->f_urow_sn.upload(f.urow_sn.data(), f.urow_sn.size());
@@ -1467,7 +1466,7 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
         h->ts_cnt.exact(f.nsn + 1);
         h->ts_ptr.exact(f.nsn + 1);
         h->ts_rem.exact(f.nsn);
-        h->ts_done.exact(f.nsn);
+        h->ts_done.exact((size_t)f.nsn * bw_tiles);
         h->ticket.exact(4);
         CK(cudaMemset(h->ticket.p, 0, 4 * sizeof(int)));
         // pre-size the per-pair buffers so that no allocation happens inside the iteration
@@ -1595,8 +1594,8 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             h->Yel_all.exact(4 * (size_t)nf * Bq);
             h->Zf_all.exact(4 * (size_t)nf * Bq);
             h->bw_P2.exact(h->bw_P.n);
-            h->ts_done2.exact(f.nsn);
-            h->bw_cnt2.exact(f.nsn);
+            h->ts_done2.exact((size_t)f.nsn * bw_tiles);
+            h->bw_cnt2.exact((size_t)f.nsn * bw_tiles);
         }
         {
             std::string e2;

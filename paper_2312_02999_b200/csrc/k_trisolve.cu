@@ -470,14 +470,20 @@ struct BwdArgs {
     double *P;                         // [blocks][kTS_W][kBwCols] partial sums
     double *Z;                         // [nseq][nf][4] in: rhs, out: solution of L^T x = rhs
     long long zstride;                 // sequence stride of Z (doubles)
-    int nseq;                          // right-hand sides: 3 columns per sequence, nseq <= 8
+    int nseq;                          // right-hand sides: 3 columns per sequence, nseq <= 8 ntile
+    int ntile;                         // column tiles of 8 sequences: items (s, row block, tile)
+    int nsn;                           // done / cnt stride per tile
+    long long pstride;                 // P stride per tile (doubles)
 };
 constexpr int kBwCols = 32;            // columns of one backward-solve launch (8 sequences)
 
-// Backward solve.  x_s = L_ss^{-T}(z_s - L_off^T x_R) = Q_s^T [z_s; -x_R].  Item (s, b) forms
-// the partial Q_s[rows]^T v[rows] of its 64-row block (DMMA); the last block of s to finish
-// sums the partials in block order (deterministic) and publishes x_s.  Items of s wait for
-// their parent (all of R_s's rows are solved by then).
+// Backward solve.  x_s = L_ss^{-T}(z_s - L_off^T x_R) = Q_s^T [z_s; -x_R].  Item (s, b, tile)
+// forms the partial Q_s[rows]^T v[rows] of its 64-row block for the tile's 8 sequences (DMMA);
+// the last block of (s, tile) to finish sums the partials in block order (deterministic) and
+// publishes x_s.  Items of (s, tile) wait for (parent, tile) (all of R_s's rows are solved by
+// then).  The tiles of one (s, b) are dispensed back to back (the Q block is re-read from L2), so
+// one launch covers every sequence of a batch and pays the etree's dependency depth once; each
+// tile's arithmetic is that of an 8-sequence launch (bit-identical results).
 __global__ void __launch_bounds__(kTS_NT) k_backward_solve(BwdArgs A) {
     extern __shared__ double bsm[];
     double (*Vb)[kXS] = reinterpret_cast<double (*)[kXS]>(bsm);
@@ -490,8 +496,14 @@ __global__ void __launch_bounds__(kTS_NT) k_backward_solve(BwdArgs A) {
         __syncthreads();
         const int item = sh_item;
         __syncthreads();
-        if (item >= A.nitems) return;
-        const int2 it = A.items[item];
+        if (item >= A.nitems * A.ntile) return;
+        const int tile = item % A.ntile;
+        const int2 it = A.items[item / A.ntile];
+        int *const done = A.done + (size_t)tile * A.nsn;
+        int *const cntp = A.cnt + (size_t)tile * A.nsn;
+        double *const Pt = A.P + (size_t)tile * A.pstride;
+        double *const Zt = A.Z + (size_t)tile * 8 * A.zstride;
+        const int nseq = min(8, A.nseq - 8 * tile);
         const int s = it.x, rb = it.y * kSolveRB;
         const int c0 = A.sn_c0[s], w = A.sn_c0[s + 1] - c0;
         const int slot0 = A.sn_rowptr[s], nr = A.sn_rowptr[s + 1] - slot0;
@@ -509,7 +521,7 @@ __global__ void __launch_bounds__(kTS_NT) k_backward_solve(BwdArgs A) {
         if (tid == 0) {
             int p = A.sn_parent[s];
             if (p >= 0) {
-                volatile int *dp = A.done + p;
+                volatile int *dp = done + p;
                 long long t0 = clock64();
                 while (*dp == 0) {
                     __nanosleep(32);
@@ -520,13 +532,13 @@ __global__ void __launch_bounds__(kTS_NT) k_backward_solve(BwdArgs A) {
         }
         __syncthreads();
         // columns: 4 per sequence (xyz + pad); 8 columns when nseq <= 2, else 32
-        const int ncw = A.nseq <= 2 ? 8 : kBwCols, lg = ncw == 8 ? 3 : 5;
+        const int ncw = nseq <= 2 ? 8 : kBwCols, lg = ncw == 8 ? 3 : 5;
         const int kpad = (m + 31) & ~31;
         for (int e = tid; e < kpad * ncw; e += kTS_NT) {
             const int i = e >> lg, c = e & (ncw - 1), r = rb + i, sq = c >> 2, comp = c & 3;
             double v = 0.0;
-            if (i < m && comp < 3 && sq < A.nseq) {
-                v = __ldcg(A.Z + (size_t)sq * A.zstride + (size_t)srow[i] * 4 + comp);
+            if (i < m && comp < 3 && sq < nseq) {
+                v = __ldcg(Zt + (size_t)sq * A.zstride + (size_t)srow[i] * 4 + comp);
                 if (r >= w) v = -v;
             }
             Vb[i][c] = v;
@@ -536,12 +548,12 @@ __global__ void __launch_bounds__(kTS_NT) k_backward_solve(BwdArgs A) {
         if (ncw == 8) block_dmma<1, kTS_W / 8>(w, m, Sg, Vb, O);
         else block_dmma<4, kTS_W / 8>(w, m, Sg, Vb, O);
         __syncthreads();
-        double *Pb = A.P + (size_t)(A.pbase[s] + it.y) * kTS_W * kBwCols;
+        double *Pb = Pt + (size_t)(A.pbase[s] + it.y) * kTS_W * kBwCols;
         const int nout = w * ncw;
         if (nb == 1) {   // single block: publish directly
             for (int e = tid; e < nout; e += kTS_NT) {
                 const int i = e >> lg, c = e & (ncw - 1), sq = c >> 2, comp = c & 3;
-                if (comp < 3 && sq < A.nseq) A.Z[(size_t)sq * A.zstride + (size_t)(c0 + i) * 4 + comp] = O[i][c];
+                if (comp < 3 && sq < nseq) Zt[(size_t)sq * A.zstride + (size_t)(c0 + i) * 4 + comp] = O[i][c];
             }
         } else {
             for (int e = tid; e < nout; e += kTS_NT) {
@@ -550,22 +562,22 @@ __global__ void __launch_bounds__(kTS_NT) k_backward_solve(BwdArgs A) {
             }
             __threadfence();
             __syncthreads();
-            if (tid == 0) sh_last = atomicAdd(A.cnt + s, 1) == nb - 1;
+            if (tid == 0) sh_last = atomicAdd(cntp + s, 1) == nb - 1;
             __syncthreads();
             if (!sh_last) continue;
             __threadfence();
-            const double *P0 = A.P + (size_t)A.pbase[s] * kTS_W * kBwCols;
+            const double *P0 = Pt + (size_t)A.pbase[s] * kTS_W * kBwCols;
             for (int e = tid; e < nout; e += kTS_NT) {
                 const int i = e >> lg, c = e & (ncw - 1), sq = c >> 2, comp = c & 3;
-                if (comp >= 3 || sq >= A.nseq) continue;
+                if (comp >= 3 || sq >= nseq) continue;
                 double x = 0.0;
                 for (int b = 0; b < nb; ++b) x += __ldcg(P0 + (size_t)b * kTS_W * kBwCols + i * kBwCols + c);
-                A.Z[(size_t)sq * A.zstride + (size_t)(c0 + i) * 4 + comp] = x;
+                Zt[(size_t)sq * A.zstride + (size_t)(c0 + i) * 4 + comp] = x;
             }
         }
         __threadfence();
         __syncthreads();
-        if (tid == 0) atomicExch(A.done + s, 1);
+        if (tid == 0) atomicExch(done + s, 1);
     }
 }
 
@@ -613,7 +625,10 @@ void launch_backward_solve(const DevFactor &F, int *done, int *cnt, int *ticket,
     A.sn_valptr = F.sn_valptr; A.Q = F.Q; A.items = F.bw_items; A.pbase = F.bw_pbase;
     A.nitems = F.bw_nitems; A.done = done; A.cnt = cnt; A.ticket = ticket; A.P = P; A.Z = Z;
     A.nseq = nseq; A.zstride = zstride;
-    dev_zero3(ticket, sizeof(int), done, sizeof(int) * F.nsn, cnt, sizeof(int) * F.nsn, st);
+    A.ntile = (nseq + kBwSeqs - 1) / kBwSeqs;
+    A.nsn = F.nsn;
+    A.pstride = (long long)F.bw_nblocks * kTS_W * kBwCols;
+    dev_zero3(ticket, sizeof(int), done, sizeof(int) * F.nsn * A.ntile, cnt, sizeof(int) * F.nsn * A.ntile, st);
     PDI_LAUNCH(k_backward_solve, nsm, kTS_NT, kFwdSmem, st)(A);
 }
 

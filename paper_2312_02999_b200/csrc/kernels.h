@@ -87,7 +87,9 @@ void launch_forward_solve(const DevFactor &F, const int *lo, const int *hi, cons
                           int ldv, double *Ug, double *Up, const int *nS_ptr, int capS, int with_grad,
                           int nseq, long long gstride, long long ustride,
                           int nsm, unsigned long long *trace, cudaStream_t st, const double *Yadd = nullptr);
-// backward solve of nseq <= kBwSeqs sequences' right-hand sides Z[sq][nf][4] (stride zstride)
+// backward solve of nseq sequences' right-hand sides Z[sq][nf][4] (stride zstride) in ONE launch:
+// column tiles of kBwSeqs sequences; done / cnt hold ceil(nseq / kBwSeqs) x nsn ints and P that many
+// x bw_nblocks x 128 x 32 doubles
 constexpr int kBwSeqs = 8;
 void launch_backward_solve(const DevFactor &F, int *done, int *cnt, int *ticket, double *P, double *Z,
                            int nseq, long long zstride, int nsm, cudaStream_t st);
