@@ -64,3 +64,21 @@ def test_region_backend_lockstep(P, scene):
         assert np.abs(s.positions() - ref["x"]).max() < 1e-9 * sc.bbox_diag()
         x = ref["x"]
     s.close()
+
+
+def test_region_backend_batch_equals_single(P):
+    """Two lockstep sequences with S = R (batched Schur: both systems in one launch) are bit-identical
+    to one sequence run alone, with the true-energy line search and adaptive kappa switched on too
+    (every f-row option composed with the batched path)."""
+    sc = scenes.slabs_c1()
+    A = sc.actuation(0)
+    kw = dict(reduced_backend=4, ls_energy="true", kappa_adapt_eps=sc.d_hat)
+    one = P.Solver(sc, A=A[None], **kw)
+    two = P.Solver(sc, A=np.stack([A, A]), n_seq=2, **kw)
+    st1 = one.step(n_iters=12)[0]
+    st2 = two.step(n_iters=12)
+    for q in range(2):
+        assert np.array_equal(two.positions(q), one.positions())
+        assert st2[q]["kappa"] == st1["kappa"] and st2[q]["alpha"] == st1["alpha"]
+    one.close()
+    two.close()
