@@ -231,6 +231,15 @@ struct GraphEntry {
 
 using namespace pdipc;
 
+// Scratch of the contact stage (a3-a6) of one sequence: a second set lets the two sequences of a
+// batched Schur group run their contact stages concurrently on two streams (the stage is a chain of
+// small latency-bound kernels).  X(member) for every per-stage buffer, stream and event.
+#define PD_CONTACT_SCRATCH(X)                                                                         \
+    X(cand_tmp) X(flag) X(pos) X(ctype) X(cd2) X(iscr) X(akeys) X(atype) X(ad2) X(grad) X(Hp) X(dist) \
+    X(ids) X(blo) X(bhi) X(qcnt) X(qoff) X(qlist) X(gsq) X(hcnt) X(hstart) X(hent) X(mark) X(st) X(st3) \
+    X(ev_fork3) X(ev_join3) X(ev_S)
+struct ContactAlt;
+
 struct pd_ipc {
     std::string err;
     int device = 0, nsm = 148;
@@ -273,6 +282,8 @@ struct pd_ipc {
     bool gather = false;
     bool pcg = false;                   // the paper's PCG baseline
     bool region = false;                // the paper's literal prescribed-region solve (backend 4: S = R)
+    ContactAlt *alt = nullptr;          // second contact-stage scratch set (batched Schur groups)
+    cudaEvent_t ev_cfork = nullptr, ev_cjoin = nullptr;
     DBuf<int> Rq_dev;                   // region R (factor positions), backend 4
     DBuf<double> cg_r, cg_p, cg_z, cg_q, cg_t, cg_f, cg_R, cg_part;
     double *cg_rr_host = nullptr;       // pinned: r.r of the last CG iteration
@@ -357,6 +368,19 @@ static int fail(pd_ipc *h, int code, const std::string &msg) {
     return code;
 }
 
+struct ContactAlt {
+#define PD_ALT_MEMBER(m) decltype(pd_ipc::m) m{};
+    PD_CONTACT_SCRATCH(PD_ALT_MEMBER)
+#undef PD_ALT_MEMBER
+};
+// swap the handle's contact-stage scratch with the second set (host-side pointers only: what the
+// kernels enqueued next see)
+static void swap_contact_scratch(pd_ipc *h) {
+#define PD_SWAP_MEMBER(m) std::swap(h->m, h->alt->m);
+    PD_CONTACT_SCRATCH(PD_SWAP_MEMBER)
+#undef PD_SWAP_MEMBER
+}
+
 // ------------------------------------------------------------------ helpers --------------
 static void sync_read_ints(pd_ipc *h, int *dst, const int *src, int k) {
     CK(cudaMemcpyAsync(dst, src, sizeof(int) * k, cudaMemcpyDeviceToHost, h->st));
@@ -368,10 +392,20 @@ static void set_d(pd_ipc *h, double *dptr, double v) { launch_set_double(dptr, v
 
 // shared per-pair / per-candidate scratch sized for n candidate keys (the largest list of any
 // sequence)
+static void grow_pair_set(pd_ipc *h, size_t n);
 static void ensure_pair_buffers(pd_ipc *h, size_t n) {
     if (n <= h->pair_cap) return;
     ++h->buf_epoch;
     h->pair_cap = n;
+    grow_pair_set(h, n);
+    if (h->Nt > 0) h->b0.exact(n + 1);              // line-search scratch (main set only)
+    if (h->alt) {
+        swap_contact_scratch(h);
+        grow_pair_set(h, n);
+        swap_contact_scratch(h);
+    }
+}
+static void grow_pair_set(pd_ipc *h, size_t n) {
     h->cand_tmp.exact(n);
     h->flag.exact(n + 1);
     h->pos.exact(n + 1);
@@ -386,7 +420,6 @@ static void ensure_pair_buffers(pd_ipc *h, size_t n) {
         h->Hp.exact(78 * n + 78);
         h->dist.exact(n + 1);
         h->ids.exact(4 * n + 4);
-        h->b0.exact(n + 1);
     }
 }
 
@@ -908,7 +941,21 @@ static void enqueue_lockstep_iteration(pd_ipc *h, int b0, int nb, int it) {
     enqueue_elastic(h, b0, nb, it);
     for (int c0 = b0; c0 < b0 + nb; c0 += h->nsysb) {      // groups of nsysb sequences (c0 = 0 mod nsysb)
         const int c1 = std::min(b0 + nb, c0 - c0 % h->nsysb + h->nsysb);
-        for (int b = c0; b < c1; ++b) enqueue_contact(h, b, b0, nb, it);
+        if (h->alt && c1 - c0 >= 2) {
+            // the group's contact stages on two streams: even members on the main stream's
+            // scratch, odd ones on the second set (its own main / side streams), joined before
+            // the Schur launch
+            CK(cudaEventRecord(h->ev_cfork, h->st));
+            CK(cudaStreamWaitEvent(h->alt->st, h->ev_cfork, 0));
+            for (int b = c0; b < c1; b += 2) enqueue_contact(h, b, b0, nb, it);
+            swap_contact_scratch(h);
+            for (int b = c0 + 1; b < c1; b += 2) enqueue_contact(h, b, b0, nb, it);
+            CK(cudaEventRecord(h->ev_cjoin, h->st));
+            swap_contact_scratch(h);
+            CK(cudaStreamWaitEvent(h->st, h->ev_cjoin, 0));
+        } else {
+            for (int b = c0; b < c1; ++b) enqueue_contact(h, b, b0, nb, it);
+        }
         enqueue_schur(h, c0, c1, b0, nb, it);
         c0 = c1 - h->nsysb;
     }
@@ -1597,6 +1644,29 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             h->ts_done2.exact((size_t)f.nsn * bw_tiles);
             h->bw_cnt2.exact((size_t)f.nsn * bw_tiles);
         }
+        // second contact-stage scratch set: the sequences of a batched Schur group run their contact
+        // stages concurrently (PDIPC_SERIAL_CONTACT=1 keeps them on one stream)
+        const char *sc_env = std::getenv("PDIPC_SERIAL_CONTACT");
+        // (the members of a group must own distinct reuse slots: their k_same_S run concurrently)
+        if (m.Nt > 0 && h->gather && !h->pcg && h->nsysb >= 2 && h->nslots >= h->nsysb &&
+            !(sc_env && sc_env[0] == '1')) {
+            h->alt = new ContactAlt();
+            ContactAlt &a = *h->alt;
+#define PD_ALT_ALLOC(b) a.b.exact(h->b.n);
+            PD_ALT_ALLOC(cand_tmp) PD_ALT_ALLOC(flag) PD_ALT_ALLOC(pos) PD_ALT_ALLOC(ctype) PD_ALT_ALLOC(cd2)
+            PD_ALT_ALLOC(iscr) PD_ALT_ALLOC(akeys) PD_ALT_ALLOC(atype) PD_ALT_ALLOC(ad2) PD_ALT_ALLOC(grad)
+            PD_ALT_ALLOC(Hp) PD_ALT_ALLOC(dist) PD_ALT_ALLOC(ids) PD_ALT_ALLOC(blo) PD_ALT_ALLOC(bhi)
+            PD_ALT_ALLOC(qcnt) PD_ALT_ALLOC(qoff) PD_ALT_ALLOC(qlist) PD_ALT_ALLOC(gsq) PD_ALT_ALLOC(hcnt)
+            PD_ALT_ALLOC(hstart) PD_ALT_ALLOC(hent) PD_ALT_ALLOC(mark)
+#undef PD_ALT_ALLOC
+            CK(cudaStreamCreateWithFlags(&a.st, cudaStreamNonBlocking));
+            CK(cudaStreamCreateWithFlags(&a.st3, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&a.ev_fork3, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&a.ev_join3, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&a.ev_S, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&h->ev_cfork, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&h->ev_cjoin, cudaEventDisableTiming));
+        }
         {
             std::string e2;
             if (stage_actuation(h.get(), A, false, e2)) throw CudaError(e2.c_str(), PD_IPC_E_ACTUATION);
@@ -1727,6 +1797,25 @@ void pd_ipc_destroy(pd_ipc *h) {
     if (h->ev_join3) cudaEventDestroy(h->ev_join3);
     if (h->ev_S) cudaEventDestroy(h->ev_S);
     if (h->st) cudaStreamDestroy(h->st);
+    if (h->alt) {
+        ContactAlt &a = *h->alt;
+        if (a.st) cudaStreamDestroy(a.st);
+        if (a.st3) cudaStreamDestroy(a.st3);
+        for (cudaEvent_t e : {a.ev_fork3, a.ev_join3, a.ev_S})
+            if (e) cudaEventDestroy(e);
+        for (auto *b : {&a.cand_tmp, &a.akeys}) b->release();
+        for (auto *b : {&a.flag, &a.pos, &a.ctype, &a.atype, &a.ids, &a.iscr, &a.mark, &a.hcnt, &a.hstart, &a.hent,
+                        &a.qcnt, &a.qoff, &a.qlist})
+            b->release();
+        for (auto *b : {&a.cd2, &a.ad2, &a.grad, &a.Hp, &a.dist}) b->release();
+        a.blo.release();
+        a.bhi.release();
+        a.gsq.release();
+        delete h->alt;
+        h->alt = nullptr;
+    }
+    if (h->ev_cfork) cudaEventDestroy(h->ev_cfork);
+    if (h->ev_cjoin) cudaEventDestroy(h->ev_cjoin);
     auto rel = [](auto &b) { b.release(); };
     rel(h->tets); rel(h->B_); rel(h->w); rel(h->inc_ptr); rel(h->inc); rel(h->q2v); rel(h->v2q);
     rel(h->Wp); rel(h->Wc); rel(h->WTp); rel(h->WTr); rel(h->tris); rel(h->edges); rel(h->Wv); rel(h->WTv);
