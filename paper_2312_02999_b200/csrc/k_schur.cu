@@ -536,12 +536,27 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
     // warps are done with stage s); phases tracked by the chunk counter tma_g (uniform per CTA)
     __shared__ __align__(8) unsigned long long tma_bar[2 * kTmaStages];
     double *T0 = sm, *T1 = sm + TB * TS, *T2 = sm + 2 * TB * TS, *T3 = sm + 3 * TB * TS;
-    // CTA group grp runs system P.s[grp]: group-local CTA index and count, group barriers
-    const int gsz = gridDim.x / P.nsys, grp = blockIdx.x / gsz;
+    // CTA group grp runs system P.s[grp]: group-local CTA index and count, group barriers.  Two
+    // systems split the grid in proportion to their work m^3 (m = 3 n_c + 1, the Cholesky's
+    // cube; read from the device-resident |S| of both, identical on every CTA), so the smaller one
+    // does not idle while the larger finishes; every other count splits evenly.  A system's
+    // arithmetic does not depend on its CTA count (batched == single runs, bit for bit).
+    int g0 = gridDim.x / P.nsys, gsz = g0, grp = blockIdx.x / gsz, gbase = grp * gsz;
+    if (P.nsys == 2) {
+        const double m0 = 3.0 * min(*P.s[0].nS_ptr, P.s[0].capS) + 1.0;
+        const double m1 = 3.0 * min(*P.s[1].nS_ptr, P.s[1].capS) + 1.0;
+        const double w0 = m0 * m0 * m0, w1 = m1 * m1 * m1;
+        const int lo = max(1, (int)gridDim.x / 8);
+        g0 = min((int)gridDim.x - lo, max(lo, (int)lrint((double)gridDim.x * w0 / (w0 + w1))));
+        grp = (int)blockIdx.x < g0 ? 0 : 1;
+        gsz = grp == 0 ? g0 : (int)gridDim.x - g0;
+        gbase = grp == 0 ? 0 : g0;
+    }
     if (grp >= P.nsys) return;
     __shared__ SchurArgs a_sh;
     if (threadIdx.x == 0) {
         a_sh = P.s[grp];
+        if (P.nsys == 2) a_sh.Kpart = P.s[0].Kpart + (size_t)gbase * 1152;   // per-CTA split-K partials
         for (int i = 0; i < kTmaStages; ++i) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&tma_bar[i])));
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&tma_bar[kTmaStages + i])),
@@ -553,7 +568,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
     unsigned tma_g = 0;                                   // k chunks streamed so far (TMA ring)
     const SchurArgs &a = a_sh;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int G = gsz, bid = blockIdx.x - grp * gsz;
+    const int G = gsz, bid = blockIdx.x - gbase;
     unsigned nsync = 0;
     const int nS = min(*a.nS_ptr, a.capS), m = 3 * nS, ma = m + 1;   // augmented size
     if (nS == 0) {   // no contact: z = w = w_el (gather backend: the sparse right-hand side is 0)
