@@ -1567,9 +1567,11 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             h->region = h->gather && be == 4;
             if (h->region) h->Rq_dev.upload(Rq.data(), Rq.size());
             h->pcg = m.Nt > 0 && be == 3;
-            // batched Schur: with the gather backend and several sequences, 2 systems per launch
-            // (each on half the SMs: one system's serial panel chain overlaps the other's updates)
-            h->nsysb = (h->gather && Bq > 1) ? 2 : 1;
+            // batched Schur: with the gather backend and several sequences, 4 systems per launch
+            // (the grid split in proportion to their work: the systems' serial panel chains overlap
+            // each other's updates; C4 2 / 3 / 4 / 6 / 8 systems: 70.7 / 71.9 / 72.3 / 71.7 / 70.3
+            // it/s, profiles/schur_split_r02.txt)
+            h->nsysb = (h->gather && Bq > 1) ? std::min(Bq, 4) : 1;
             if (const char *sbv = std::getenv("PDIPC_SCHUR_BATCH"))
                 h->nsysb = std::max(1, std::min(std::min(Bq, (int)kMaxSchurSys), std::atoi(sbv)));
             if (!h->gather) h->nsysb = 1;                  // (panel mode: split-K sums depend on the grid)

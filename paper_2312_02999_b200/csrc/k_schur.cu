@@ -536,27 +536,41 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
     // warps are done with stage s); phases tracked by the chunk counter tma_g (uniform per CTA)
     __shared__ __align__(8) unsigned long long tma_bar[2 * kTmaStages];
     double *T0 = sm, *T1 = sm + TB * TS, *T2 = sm + 2 * TB * TS, *T3 = sm + 3 * TB * TS;
-    // CTA group grp runs system P.s[grp]: group-local CTA index and count, group barriers.  Two
-    // systems split the grid in proportion to their work m^3 (m = 3 n_c + 1, the Cholesky's
-    // cube; read from the device-resident |S| of both, identical on every CTA), so the smaller one
-    // does not idle while the larger finishes; every other count splits evenly.  A system's
-    // arithmetic does not depend on its CTA count (batched == single runs, bit for bit).
-    int g0 = gridDim.x / P.nsys, gsz = g0, grp = blockIdx.x / gsz, gbase = grp * gsz;
-    if (P.nsys == 2) {
-        const double m0 = 3.0 * min(*P.s[0].nS_ptr, P.s[0].capS) + 1.0;
-        const double m1 = 3.0 * min(*P.s[1].nS_ptr, P.s[1].capS) + 1.0;
-        const double w0 = m0 * m0 * m0, w1 = m1 * m1 * m1;
-        const int lo = max(1, (int)gridDim.x / 8);
-        g0 = min((int)gridDim.x - lo, max(lo, (int)lrint((double)gridDim.x * w0 / (w0 + w1))));
-        grp = (int)blockIdx.x < g0 ? 0 : 1;
-        gsz = grp == 0 ? g0 : (int)gridDim.x - g0;
-        gbase = grp == 0 ? 0 : g0;
+    // CTA group grp runs system P.s[grp]: group-local CTA index and count, group barriers.  The
+    // systems of a launch split the grid in proportion to their work m^3 (m = 3 n_c + 1, the
+    // Cholesky's cube; read from the device-resident |S| of every system, identical on every CTA),
+    // so a smaller system does not idle while a larger one finishes.  Group g owns CTAs
+    // [start_g, start_{g+1}), start_{g+1} = round(grid x W_<=g / W), at least one CTA each (a system
+    // without contact returns at once).  A system's arithmetic does not depend on its CTA count
+    // (batched == single runs, bit for bit).
+    int grp = 0, gsz = gridDim.x, gbase = 0;
+    {
+        double w[kMaxSchurSys], W = 0.0;
+        for (int g = 0; g < P.nsys; ++g) {
+            const double m = 3.0 * min(*P.s[g].nS_ptr, P.s[g].capS) + 1.0;
+            w[g] = m * m * m;
+            W += w[g];
+        }
+        double cum = 0.0;
+        int start = 0;
+        for (int g = 0; g < P.nsys; ++g) {
+            cum += w[g];
+            const int next = g == P.nsys - 1 ? (int)gridDim.x
+                                             : min((int)gridDim.x - (P.nsys - 1 - g),
+                                                   max(start + 1, (int)lrint((double)gridDim.x * cum / W)));
+            if ((int)blockIdx.x >= start && (int)blockIdx.x < next) {
+                grp = g;
+                gbase = start;
+                gsz = next - start;
+            }
+            start = next;
+        }
     }
     if (grp >= P.nsys) return;
     __shared__ SchurArgs a_sh;
     if (threadIdx.x == 0) {
         a_sh = P.s[grp];
-        if (P.nsys == 2) a_sh.Kpart = P.s[0].Kpart + (size_t)gbase * 1152;   // per-CTA split-K partials
+        a_sh.Kpart = P.s[0].Kpart + (size_t)gbase * 1152;   // per-CTA split-K partials of the group
         for (int i = 0; i < kTmaStages; ++i) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&tma_bar[i])));
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&tma_bar[kTmaStages + i])),

@@ -170,7 +170,7 @@ struct SchurArgs {
 };
 // Several systems (sequences) per launch: the grid splits into nsys equal CTA groups, group g
 // running system s[g] with group barriers (the batched variable-n_c Schur step of SURVEY 8(e)).
-constexpr int kMaxSchurSys = 4;
+constexpr int kMaxSchurSys = 8;
 struct SchurBatch {
     SchurArgs s[kMaxSchurSys];
     int nsys;
@@ -181,7 +181,8 @@ SchurArgs schur_args(const DevFactor &F, const double *V, int ldv, const double 
                      double *yS, double *y, double *u, double *t, double *Z, int *info, const int *same_S,
                      unsigned long long *prof, int large_min_tiles, int mode, const double *G2, int n2,
                      const int *rpos, const double *Yel);
-// nsys systems in one cooperative launch (nsys <= kMaxSchurSys; the grid splits into equal groups)
+// nsys systems in one cooperative launch (nsys <= kMaxSchurSys; the grid splits into groups in
+// proportion to the systems' work m^3)
 int launch_schur_batch(const SchurArgs *sys, int nsys, cudaStream_t st);
 void schur_init(int device);
 int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, const double *gc,
