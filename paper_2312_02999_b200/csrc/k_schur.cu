@@ -537,8 +537,8 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
     __shared__ __align__(8) unsigned long long tma_bar[2 * kTmaStages];
     double *T0 = sm, *T1 = sm + TB * TS, *T2 = sm + 2 * TB * TS, *T3 = sm + 3 * TB * TS;
     // CTA group grp runs system P.s[grp]: group-local CTA index and count, group barriers.  The
-    // systems of a launch split the grid in proportion to their work m^3 (m = 3 n_c + 1, the
-    // Cholesky's cube; read from the device-resident |S| of every system, identical on every CTA),
+    // systems of a launch split the grid in proportion to their work m^wexp (m = 3 n_c + 1, wexp 2.5
+    // by default; read from the device-resident |S| of every system, identical on every CTA),
     // so a smaller system does not idle while a larger one finishes.  Group g owns CTAs
     // [start_g, start_{g+1}), start_{g+1} = round(grid x W_<=g / W), at least one CTA each (a system
     // without contact returns at once).  A system's arithmetic does not depend on its CTA count
@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(NT, 1) k_schur_coop(const __grid_constant__ Sc
         double w[kMaxSchurSys], W = 0.0;
         for (int g = 0; g < P.nsys; ++g) {
             const double m = 3.0 * min(*P.s[g].nS_ptr, P.s[g].capS) + 1.0;
-            w[g] = m * m * m;
+            w[g] = P.wexp == 3.0 ? m * m * m : pow(m, P.wexp);
             W += w[g];
         }
         double cum = 0.0;
@@ -2136,6 +2136,11 @@ int launch_schur_batch(const SchurArgs *sys, int nsys, cudaStream_t st) {
         b.s[g].phase = 0;
     }
     b.nsys = nsys;
+    // weights m^2.5 rather than the Cholesky's m^3: a larger system's serial panel chain does not
+    // shrink with more CTAs (C4 exponent 2 / 2.25 / 2.5 / 3 / 3.5: 71.9 / 72.3 / 72.7 / 72.4 / 71.1
+    // it/s, profiles/schur_split_r02.txt; PDIPC_SCHUR_WEXP)
+    static const double wexp = [] { const char *e = std::getenv("PDIPC_SCHUR_WEXP"); return e ? std::atof(e) : 2.5; }();
+    b.wexp = wexp;
     cudaError_t e = dev_zero(g_gbar, kMaxSchurSys * 32 * sizeof(unsigned), st);
     if (e != cudaSuccess) return (int)e;
     const bool split = nsys == 1 && !getenv_fused() && sys[0].mode != kSchurKOnly;

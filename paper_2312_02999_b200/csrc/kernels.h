@@ -174,6 +174,7 @@ constexpr int kMaxSchurSys = 8;
 struct SchurBatch {
     SchurArgs s[kMaxSchurSys];
     int nsys;
+    double wexp;                  // the CTA split weighs system g by m_g^wexp (default 2.5)
 };
 SchurArgs schur_args(const DevFactor &F, const double *V, int ldv, const double *G, const double *gc,
                      const int *qS, const int *lo, const int *hi, const int *nS, int capS, double *K, int ldk,
@@ -182,7 +183,7 @@ SchurArgs schur_args(const DevFactor &F, const double *V, int ldv, const double 
                      unsigned long long *prof, int large_min_tiles, int mode, const double *G2, int n2,
                      const int *rpos, const double *Yel);
 // nsys systems in one cooperative launch (nsys <= kMaxSchurSys; the grid splits into groups in
-// proportion to the systems' work m^3)
+// proportion to the systems' work m^wexp)
 int launch_schur_batch(const SchurArgs *sys, int nsys, cudaStream_t st);
 void schur_init(int device);
 int launch_schur(const DevFactor &F, const double *V, int ldv, const double *G, const double *gc,
