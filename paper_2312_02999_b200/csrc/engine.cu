@@ -231,13 +231,13 @@ struct GraphEntry {
 
 using namespace pdipc;
 
-// Scratch of the contact stage (a3-a6) of one sequence: a second set lets the two sequences of a
-// batched Schur group run their contact stages concurrently on two streams (the stage is a chain of
-// small latency-bound kernels).  X(member) for every per-stage buffer, stream and event.
+// Scratch of the contact stage (a3-a6) and of the CCD / line-search stage (a10-a11) of one
+// sequence: a second set lets pairs of sequences run these stages concurrently on two streams
+// (chains of small latency-bound kernels).  X(member) for every per-stage buffer, stream, event.
 #define PD_CONTACT_SCRATCH(X)                                                                         \
     X(cand_tmp) X(flag) X(pos) X(ctype) X(cd2) X(iscr) X(akeys) X(atype) X(ad2) X(grad) X(Hp) X(dist) \
     X(ids) X(blo) X(bhi) X(qcnt) X(qoff) X(qlist) X(gsq) X(hcnt) X(hstart) X(hent) X(mark) X(st) X(st3) \
-    X(ev_fork3) X(ev_join3) X(ev_S)
+    X(ev_fork3) X(ev_join3) X(ev_S) X(part) X(b0) X(lspart) X(tepart)
 struct ContactAlt;
 
 struct pd_ipc {
@@ -398,7 +398,6 @@ static void ensure_pair_buffers(pd_ipc *h, size_t n) {
     ++h->buf_epoch;
     h->pair_cap = n;
     grow_pair_set(h, n);
-    if (h->Nt > 0) h->b0.exact(n + 1);              // line-search scratch (main set only)
     if (h->alt) {
         swap_contact_scratch(h);
         grow_pair_set(h, n);
@@ -420,6 +419,7 @@ static void grow_pair_set(pd_ipc *h, size_t n) {
         h->Hp.exact(78 * n + 78);
         h->dist.exact(n + 1);
         h->ids.exact(4 * n + 4);
+        h->b0.exact(n + 1);
     }
 }
 
@@ -960,7 +960,18 @@ static void enqueue_lockstep_iteration(pd_ipc *h, int b0, int nb, int it) {
         c0 = c1 - h->nsysb;
     }
     enqueue_backward(h, b0, nb, it);
-    for (int b = b0; b < b0 + nb; ++b) enqueue_ccd_ls(h, b, b0, nb, it);
+    if (h->alt && nb >= 2) {   // CCD / line search of even sequences on the main set, odd ones on the second
+        CK(cudaEventRecord(h->ev_cfork, h->st));
+        CK(cudaStreamWaitEvent(h->alt->st, h->ev_cfork, 0));
+        for (int b = b0; b < b0 + nb; b += 2) enqueue_ccd_ls(h, b, b0, nb, it);
+        swap_contact_scratch(h);
+        for (int b = b0 + 1; b < b0 + nb; b += 2) enqueue_ccd_ls(h, b, b0, nb, it);
+        CK(cudaEventRecord(h->ev_cjoin, h->st));
+        swap_contact_scratch(h);
+        CK(cudaStreamWaitEvent(h->st, h->ev_cjoin, 0));
+    } else {
+        for (int b = b0; b < b0 + nb; ++b) enqueue_ccd_ls(h, b, b0, nb, it);
+    }
 }
 
 // Run k lockstep iterations of sequences [b0, b0 + nb) with ONE host round trip: replay the
@@ -1659,7 +1670,9 @@ int pd_ipc_create(const pd_ipc_mesh *mesh, const double *rest_pos, const double 
             PD_ALT_ALLOC(iscr) PD_ALT_ALLOC(akeys) PD_ALT_ALLOC(atype) PD_ALT_ALLOC(ad2) PD_ALT_ALLOC(grad)
             PD_ALT_ALLOC(Hp) PD_ALT_ALLOC(dist) PD_ALT_ALLOC(ids) PD_ALT_ALLOC(blo) PD_ALT_ALLOC(bhi)
             PD_ALT_ALLOC(qcnt) PD_ALT_ALLOC(qoff) PD_ALT_ALLOC(qlist) PD_ALT_ALLOC(gsq) PD_ALT_ALLOC(hcnt)
-            PD_ALT_ALLOC(hstart) PD_ALT_ALLOC(hent) PD_ALT_ALLOC(mark)
+            PD_ALT_ALLOC(hstart) PD_ALT_ALLOC(hent) PD_ALT_ALLOC(mark) PD_ALT_ALLOC(part) PD_ALT_ALLOC(b0)
+            PD_ALT_ALLOC(lspart)
+            if (h->tepart.n) PD_ALT_ALLOC(tepart)
 #undef PD_ALT_ALLOC
             CK(cudaStreamCreateWithFlags(&a.st, cudaStreamNonBlocking));
             CK(cudaStreamCreateWithFlags(&a.st3, cudaStreamNonBlocking));
@@ -1809,7 +1822,7 @@ void pd_ipc_destroy(pd_ipc *h) {
         for (auto *b : {&a.flag, &a.pos, &a.ctype, &a.atype, &a.ids, &a.iscr, &a.mark, &a.hcnt, &a.hstart, &a.hent,
                         &a.qcnt, &a.qoff, &a.qlist})
             b->release();
-        for (auto *b : {&a.cd2, &a.ad2, &a.grad, &a.Hp, &a.dist}) b->release();
+        for (auto *b : {&a.cd2, &a.ad2, &a.grad, &a.Hp, &a.dist, &a.part, &a.b0, &a.lspart, &a.tepart}) b->release();
         a.blo.release();
         a.bhi.release();
         a.gsq.release();
