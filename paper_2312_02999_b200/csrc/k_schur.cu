@@ -2107,7 +2107,8 @@ SchurArgs schur_args(const DevFactor &F, const double *V, int ldv, const double 
     static const int kpw0 = [] { const char *e = std::getenv("PDIPC_SCHUR_KPW0"); return e ? std::max(1, std::atoi(e)) : 10; }();
     static const int ktail = [] { const char *e = std::getenv("PDIPC_SCHUR_KTAIL"); return e ? std::atoi(e) : 0; }();
     a.kpw0 = kpw0;
-    static const int split_min = [] { const char *e = std::getenv("PDIPC_SCHUR_SPLIT"); return e ? std::atoi(e) : 80; }();
+    // -1: chosen per launch in launch_schur_batch (PDIPC_SCHUR_SPLIT overrides)
+    static const int split_min = [] { const char *e = std::getenv("PDIPC_SCHUR_SPLIT"); return e ? std::atoi(e) : -1; }();
     a.split_min = split_min;
     a.ktail = ktail;
     if (g_encode && Sh && ldh > 0 && capS > 0) {
@@ -2129,6 +2130,11 @@ int launch_schur_batch(const SchurArgs *sys, int nsys, cudaStream_t st) {
     const int gsz = g_schur_grid / nsys;
     for (int g = 0; g < nsys; ++g) {          // per-group scratch (split-K partials, panels, barriers)
         b.s[g] = sys[g];
+        // half-panel split threshold: 80 tile columns for a system on the whole grid (C3 single,
+        // profiles/schur_kpw_sweep_r02.txt), 20 in a batched launch where each system has ~1/nsys
+        // of the CTAs (C4 4 systems: never / 40 / 30 / 20 / always 70.1 / 73.5 / 73.6 / 73.6 / 73.4
+        // it/s, profiles/schur_split_r02.txt)
+        if (b.s[g].split_min < 0) b.s[g].split_min = nsys == 1 ? 80 : 20;
         b.s[g].Kpart = g_kpart + (size_t)g * gsz * 1152;
         b.s[g].LP = g_lp + (size_t)g * 2 * kLPTiles * TB * TB;
         b.s[g].bar = g_bar + (size_t)g * kMaxPanels;
